@@ -1,0 +1,398 @@
+/*
+ * cyclescope_b200.h — C ABI of the B200-native trace-analysis core.
+ *
+ * This is the drop-in boundary for the reference's analysis hot path
+ * (`/root/reference/proj/include/cyclescope/{cycles,detector,baseline,rca}.hpp`).
+ * The reference exposes that path as C++ functions over `Trace`; it has no
+ * FFI.  The entry points below are what a C++ shim (or cgo/ctypes/JNI
+ * binding) re-implementing those functions binds to.  Each entry cites the
+ * reference interface it replaces.
+ *
+ * Conventions
+ *  - Every function returns an int status: CS_OK (0) or a CS_E_* code whose
+ *    machine-readable type string (cs_status_type) equals the reference's
+ *    EngineError::type() (errors.hpp:12-85).  No exception crosses the ABI;
+ *    the message of the last error is available from cs_last_error(ctx).
+ *  - Inputs are borrowed, plain pointers + sizes.  Outputs go to
+ *    caller-owned buffers with an explicit capacity and a size_t* count.
+ *  - Events are in the reference's canonical order (start_ts, event_id)
+ *    (trace.hpp:110-113).  All event indices returned (first_event,
+ *    last_event, anchor position) are indices into that order, i.e. into the
+ *    caller's Trace::events (cycles.hpp:71-73).
+ *  - There is no CPU fallback: without a CUDA device every compute entry
+ *    point returns CS_E_NO_DEVICE.
+ */
+#ifndef CYCLESCOPE_B200_H_
+#define CYCLESCOPE_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CS_ABI_VERSION 1
+
+/* ------------------------------------------------------------------ status */
+enum cs_status {
+  CS_OK = 0,
+  CS_E_INVALID_ARGUMENT = 1,   /* "invalid_argument" (ABI misuse)            */
+  CS_E_NO_DEVICE = 2,          /* "no_device": no CUDA device / ext missing   */
+  CS_E_CUDA = 3,               /* "cuda_error"                               */
+  CS_E_NO_ANCHOR_FOUND = 4,    /* "no_anchor_found"        errors.hpp:41-43  */
+  CS_E_MISSING_WORKLOAD = 5,   /* "missing_workload_args"  errors.hpp:44-46  */
+  CS_E_FEATURE_MISMATCH = 6,   /* "feature_mismatch"       errors.hpp:50-52  */
+  CS_E_NON_POSITIVE_LATENCY = 7, /* "non_positive_latency" errors.hpp:56-58  */
+  CS_E_INSUFFICIENT_DATA = 8,  /* "insufficient_data"      errors.hpp:47-49  */
+  CS_E_INSUFFICIENT_CALIBRATION = 9, /* "insufficient_calibration" 59-61     */
+  CS_E_NO_LABELS = 10,         /* "no_labels"              errors.hpp:62-64  */
+  CS_E_MODEL_FORMAT = 11,      /* "model_format_error"     errors.hpp:80-82  */
+  CS_E_UNSUPPORTED = 12,       /* "unsupported": outside the device limits   */
+  CS_E_CONFIG = 13,            /* "config_error"           errors.hpp:77-79  */
+  CS_E_INTERNAL = 14           /* "internal"                                 */
+};
+
+/* ------------------------------------------------------- event record (A1)
+ * 32-byte record, 16-byte aligned: two 16-B vector loads per event.
+ * Replaces TraceEvent (trace.hpp:67-81) + the std::map args the hot path
+ * reads (arg_int/arg_string/arg_number, trace.cpp:76-101); the host interns
+ * strings at ingest, the device never sees them.
+ */
+typedef struct cs_event {
+  int64_t start_ts;   /* ns, canonical order key                          */
+  int64_t duration;   /* ns for Span; for Counter: bit pattern of the f64
+                         `value` arg (CS_EV_HAS_VALUE); 0 otherwise         */
+  uint32_t name_id;   /* index into the name table (names interned in
+                         lexicographic byte order, so name_id == lex rank)  */
+  uint8_t kind;       /* cs_kind                                          */
+  uint8_t category;   /* cs_category                                      */
+  uint16_t flags;     /* CS_EV_* bits                                     */
+  uint64_t payload;   /* low 32: workload-table index (CS_EV_HAS_BATCH)
+                         high 32: collective slot (CS_EV_HAS_COMM)          */
+} cs_event;
+
+enum cs_kind { CS_SPAN = 0, CS_INSTANT = 1, CS_COUNTER = 2, CS_FLOW = 3 };
+enum cs_category { /* trace.hpp:22-31 */
+  CS_CAT_PYTHON_CALL = 0, CS_CAT_RUNTIME_API = 1, CS_CAT_GPU_KERNEL = 2,
+  CS_CAT_MEM_COPY = 3, CS_CAT_OS_SCHED = 4, CS_CAT_NET_IO = 5,
+  CS_CAT_COUNTER_TELEMETRY = 6, CS_CAT_COLLECTIVE_COMM = 7
+};
+
+/* forward_mode class of arg_string(e, forward_mode_key) after tolower
+ * (cycles.cpp:205-220): none / contains prefill|extend / contains decode /
+ * any other string (stops the first-forward_mode search, decides nothing). */
+#define CS_EV_FM_MASK      0x0003u
+#define CS_EV_FM_NONE      0u
+#define CS_EV_FM_PREFILL   1u
+#define CS_EV_FM_DECODE    2u
+#define CS_EV_FM_OTHER     3u
+#define CS_EV_HAS_BATCH    0x0004u /* arg_int(batch_size_key) present        */
+#define CS_EV_WL_OK        0x0008u /* + input/output lens present, all >= 0  */
+#define CS_EV_HAS_COMM     0x0010u /* CollectiveComm span w/ commHash + rank */
+#define CS_EV_HAS_VALUE    0x0020u /* Counter with numeric `value`           */
+
+/* One entry per batch-size carrier event.  input_len/output_len are
+ * INT64_MIN when the arg is absent (MissingWorkloadArgs, cycles.cpp:264-267). */
+typedef struct cs_workload { /* WorkloadFeatures (cycles.hpp:92-100) */
+  int64_t batch;
+  int64_t input_len;
+  int64_t output_len;
+} cs_workload;
+
+/* Per interned name. Derived on the host from CycleConfig (cycles.hpp:18-43)
+ * and the set of span names. */
+typedef struct cs_name_info {
+  uint32_t flags;      /* CS_NAME_* */
+  int32_t phase;       /* index into CycleConfig::phase_functions, -1 none */
+  int32_t beta_slot;   /* dense class slot for stage attribution, -1 none  */
+  uint32_t reserved;
+} cs_name_info;
+#define CS_NAME_PREFILL_KW 0x1u /* name contains a prefill keyword (174-179) */
+#define CS_NAME_DECODE_KW  0x2u /* name contains a decode keyword            */
+
+/* ------------------------------------------------------------- configs */
+typedef struct cs_cycle_config { /* CycleConfig + PipelineOptions */
+  int64_t anchor_hint_name;       /* name id, -1 = discover (cycles.hpp:20)
+                                     -2 = hint given but not in name table */
+  uint64_t min_anchor_calls;      /* 10 */
+  double prefill_duration_factor; /* 3.0 */
+  double prefill_gap_factor;      /* 2.0 */
+  uint64_t stage_window;          /* 32 */
+  uint64_t stage_min_history;     /* 8  */
+  int64_t frequency_bin_ns;       /* 1'000'000 */
+  int32_t n_phases;               /* |phase_functions| after dedup         */
+  int32_t latency_phase;          /* PipelineOptions::latency_component as
+                                     phase index; -1 = full cycle span      */
+  int32_t include_prefill;        /* PipelineOptions::include_prefill       */
+  int32_t n_beta_slots;           /* number of dense class slots (<= 64)    */
+  int32_t n_comm_slots;           /* collective (name,comm,rank) slots      */
+  int32_t reserved;
+} cs_cycle_config;
+
+enum cs_strategy { CS_FIXED_POINT = 0, CS_FIXED_WINDOW = 1, CS_DYNAMIC_WINDOW = 2 };
+
+typedef struct cs_control_config { /* ControlConfig detector.hpp:25-34 */
+  int32_t strategy;
+  int32_t reserved;
+  uint64_t window;         /* 10   */
+  double fixed_threshold;  /* 0.15 */
+  double sigma_k;          /* 3.0  */
+  double theta_max;        /* 0.18 */
+  double min_ucl;          /* 0.02 */
+  uint64_t warmup;         /* 100  */
+  double epsilon;          /* 1e-9 */
+} cs_control_config;
+
+/* Feature ids a model may request (main.cpp:59-78 features_by_name). */
+enum cs_feature { CS_F_BATCH = 0, CS_F_W_KV = 1, CS_F_INPUT_LEN = 2,
+                  CS_F_OUTPUT_LEN = 3, CS_F_STAGE = 4 };
+
+/* Flattened GbdtModel (gbdt.hpp:33-84) + LatencyModel stats (baseline.hpp:50-67).
+ * Trees are concatenated node arrays; tree t owns nodes
+ * [tree_offsets[t], tree_offsets[t+1]); child indices are tree-local. */
+typedef struct cs_tree_node {
+  int32_t feature;   /* -1 = leaf */
+  int32_t left;
+  int32_t right;
+  int32_t reserved;
+  double threshold;  /* go left iff x[feature] <= threshold */
+  double value;      /* leaf output */
+} cs_tree_node;
+
+typedef struct cs_model {
+  uint32_t n_features;
+  uint32_t n_trees;
+  const int32_t* feature_ids;     /* n_features cs_feature ids */
+  const uint32_t* tree_offsets;   /* n_trees + 1 */
+  const cs_tree_node* nodes;
+  double base;
+  double learning_rate;
+  double prediction_floor;
+  double mu_train;
+  double sigma_train;
+  int32_t degenerate;
+  int32_t reserved;
+} cs_model;
+
+/* ------------------------------------------------------------- outputs */
+enum cs_stage { CS_STAGE_PREFILL = 0, CS_STAGE_DECODE = 1, CS_STAGE_UNKNOWN = 2 };
+
+typedef struct cs_cycle { /* Cycle (cycles.hpp:62-77) */
+  uint64_t index;
+  int64_t start_ts;
+  int64_t end_ts;
+  uint64_t anchor_pos;     /* canonical index of the anchor occurrence;
+                              UINT64_MAX for frequency-fallback cycles */
+  int64_t anchor_span_end;
+  uint64_t first_event;
+  uint64_t last_event;
+  int32_t stage;
+  int32_t workload_status; /* 0 ok, 1 no carrier, 2 carrier w/o lens/neg */
+} cs_cycle;
+
+typedef struct cs_record { /* CycleRecord (cycles.hpp:114-121) + ResidualSample
+                              + StepResult (detector.hpp:43-73) */
+  uint64_t cycle_index;
+  int64_t start_ts;
+  int64_t batch;
+  int64_t input_len;
+  int64_t output_len;
+  double latency_s;
+  double predicted_s;
+  double residual;         /* ppe */
+  double statistic;        /* E_t or window mean */
+  int32_t stage;
+  uint8_t armed;
+  uint8_t flagged;
+  uint8_t alert;
+  uint8_t reserved;
+  uint64_t episode_id;     /* valid when alert */
+} cs_record;
+
+typedef struct cs_alert { /* Alert (detector.hpp:52-63) */
+  uint64_t cycle;
+  int64_t ts;
+  double smoothed_error;
+  double limit;
+  int32_t strategy;
+  int32_t reserved;
+  int64_t batch;
+  int64_t input_len;
+  int64_t output_len;
+  uint64_t episode_id;
+  uint64_t record_index;
+} cs_alert;
+
+typedef struct cs_anchor_candidate { /* AnchorCandidate (cycles.hpp:45-52) */
+  uint32_t name_id;
+  uint32_t reserved;
+  uint64_t call_count;
+  double mean_duration_ns;
+  double duration_cv;
+  double score;
+} cs_anchor_candidate;
+
+typedef struct cs_instance_summary {
+  uint32_t anchor_name_id;   /* UINT32_MAX when frequency fallback used */
+  int32_t status;            /* per-instance cs_status of the analysis    */
+  uint64_t n_cycles;
+  uint64_t n_records;
+  uint64_t n_alerts;
+  uint64_t first_bad_record; /* record whose latency <= 0 (UINT64_MAX none) */
+  double ucl;                /* detector limit in force                   */
+  int32_t used_frequency_fallback;
+  int32_t anchor_ambiguous;  /* exact-stat ranking needed the ordered fold */
+} cs_instance_summary;
+
+/* ----------------------------------------------------------- context API */
+typedef struct cs_ctx cs_ctx;
+
+/* Stage mask for cs_run. */
+#define CS_RUN_SEGMENT   0x1u  /* anchor + segment + classify + records  */
+#define CS_RUN_BETA      0x2u  /* per-cycle class occupancy beta         */
+#define CS_RUN_SCORE     0x4u  /* GBDT predict + ppe                     */
+#define CS_RUN_DETECT    0x8u  /* control chart + alerts                 */
+#define CS_RUN_ALL       0xFu
+
+int cs_abi_version(void);
+const char* cs_status_type(int status);
+
+int cs_ctx_create(int device, cs_ctx** out);
+void cs_ctx_destroy(cs_ctx* ctx);
+const char* cs_last_error(const cs_ctx* ctx);
+
+/* CycleConfig/PipelineOptions (cycles.hpp:18-43,123-128) and ControlConfig
+ * (detector.hpp:25-34). */
+int cs_set_config(cs_ctx* ctx, const cs_cycle_config* cycle,
+                  const cs_control_config* control);
+
+/* Name table: one entry per interned name id. */
+int cs_set_name_table(cs_ctx* ctx, uint32_t n_names, const cs_name_info* names);
+
+/* Upload a batch of monitored instances (events of instance i are
+ * ev[inst_offsets[i] .. inst_offsets[i+1]) ).  H2D copy on the ctx stream;
+ * host buffers may be pinned (cs_host_alloc) for full link bandwidth. */
+int cs_upload(cs_ctx* ctx, uint32_t n_inst, const uint64_t* inst_offsets,
+              const cs_event* ev, uint64_t n_workloads, const cs_workload* wl);
+
+/* Latency model for instance `inst` (UINT32_MAX = all instances).
+ * Replaces LatencyModel::load/predict (baseline.cpp:288-317, gbdt.cpp:173-184). */
+int cs_load_model(cs_ctx* ctx, uint32_t inst, const cs_model* model);
+
+/* Runs the selected stages on the device for every uploaded instance.
+ * Replaces segment_and_classify + build_cycle_records (cycles.cpp:345-409),
+ * cycle_stats beta (rca.cpp:71-130), predict + ppe, Detector::step
+ * (detector.cpp:14-19, 91-130).  Asynchronous w.r.t. the host until a getter
+ * or cs_sync is called. */
+int cs_run(cs_ctx* ctx, uint32_t stage_mask);
+int cs_sync(cs_ctx* ctx);
+
+int cs_get_summary(cs_ctx* ctx, uint32_t inst, cs_instance_summary* out);
+int cs_get_candidates(cs_ctx* ctx, uint32_t inst, cs_anchor_candidate* buf,
+                      size_t cap, size_t* n);
+int cs_get_cycles(cs_ctx* ctx, uint32_t inst, cs_cycle* buf, size_t cap, size_t* n);
+/* component_durations: n_cycles x n_phases int64, row-major */
+int cs_get_components(cs_ctx* ctx, uint32_t inst, int64_t* buf, size_t cap, size_t* n);
+/* stage attribution: n_cycles x n_beta_slots; total clipped span ns (int64)
+ * and beta (f64); a class is absent from the reference's map iff total == 0 */
+int cs_get_beta(cs_ctx* ctx, uint32_t inst, int64_t* totals, double* beta,
+                size_t cap, size_t* n);
+/* collective per-(name,comm,rank) beta: n_cycles x n_comm_slots f64;
+ * presence mask: n_cycles x n_comm_slots uint8 */
+int cs_get_collective_beta(cs_ctx* ctx, uint32_t inst, double* beta,
+                           uint8_t* present, size_t cap, size_t* n);
+int cs_get_records(cs_ctx* ctx, uint32_t inst, cs_record* buf, size_t cap, size_t* n);
+int cs_get_alerts(cs_ctx* ctx, uint32_t inst, cs_alert* buf, size_t cap, size_t* n);
+
+/* Pinned host memory helpers (cudaHostAlloc) for the e2e path. */
+int cs_host_alloc(size_t bytes, void** out);
+int cs_host_free(void* p);
+
+/* Device timing of the last cs_run per kernel family (ms, CUDA events on the
+ * ctx stream).  names: comma-separated list written to `names` (cap bytes). */
+int cs_get_timings(cs_ctx* ctx, double* ms, size_t cap, size_t* n,
+                   char* names, size_t names_cap);
+/* Number of kernels launched by the last cs_run. */
+int cs_get_launch_count(cs_ctx* ctx, uint64_t* n);
+
+/* ----------------------------------------------------- host-side services */
+/* Deterministic GBDT fit (fit_latency_model, baseline.cpp:168-208 and
+ * fit_gbdt, gbdt.cpp:40-171), bit-identical to the reference.  Host C++,
+ * reported separately from events/s.  x: n x n_features
+ * row-major; y: latency seconds.  The result is kept in an opaque handle. */
+typedef struct cs_fitted_model cs_fitted_model;
+typedef struct cs_gbdt_params { /* GbdtParams gbdt.hpp:25-31 */
+  uint64_t n_trees;
+  uint64_t max_depth;
+  double learning_rate;
+  uint64_t min_samples_leaf;
+  double prediction_floor;
+} cs_gbdt_params;
+typedef struct cs_fit_options { /* FitOptions baseline.hpp:42-47 */
+  double calibration_fraction;
+  double ppe_epsilon;
+  int32_t stratify_col;     /* column index of the stratify feature, -1 = 0 */
+  int32_t reserved;
+  uint64_t min_samples;
+} cs_fit_options;
+int cs_fit_latency_model(uint64_t n, uint32_t n_features, const int32_t* feature_ids,
+                         const double* x, const double* y,
+                         const cs_gbdt_params* params, const cs_fit_options* opt,
+                         cs_fitted_model** out, char* err, size_t err_cap);
+/* Parse a LatencyModel JSON document (baseline.cpp:288-302). */
+int cs_model_from_json(const char* json, cs_fitted_model** out, char* err, size_t err_cap);
+/* Serialize to the reference's LatencyModel JSON (baseline.cpp:277-286). */
+int cs_model_to_json(const cs_fitted_model* m, char* buf, size_t cap, size_t* n);
+int cs_model_view(const cs_fitted_model* m, cs_model* view);
+void cs_model_free(cs_fitted_model* m);
+
+/* Single-record host helpers with the reference's exact arithmetic, used by
+ * the C++ drop-in shim for ppe / ucl_from_stats / compute_ucl
+ * (detector.cpp:14-19, 41-60). */
+double cs_ucl_from_stats(double mu, double sigma, const cs_control_config* cfg);
+int cs_compute_ucl(const double* residuals, size_t n, double k, double theta_max,
+                   double min_ucl, size_t min_n, double* out);
+
+/* RunConfig JSON (the reference's schema, config.cpp:78-188; unknown keys are
+ * rejected with CS_E_CONFIG) -> device configs + name table.  `names` are the
+ * interned names in id order; name_is_span marks names occurring as Spans
+ * (they receive dense beta slots in name order).  Replaces the CycleConfig /
+ * PipelineOptions / ControlConfig plumbing of monitor_loop (main.cpp:142-214). */
+int cs_config_from_json(const char* run_config_json, uint32_t n_names,
+                        const char* const* names, const uint8_t* name_is_span,
+                        uint32_t n_comm_slots, cs_name_info* out_names,
+                        cs_cycle_config* out_cycle, cs_control_config* out_control,
+                        char* err, size_t err_cap);
+
+/* ------------------------------------------------- synthetic trace producer
+ * Restatement of the reference's simkit generator (simkit.cpp:34-86,
+ * 195-246, 276-506) writing cs_event records directly; benchmark input only.
+ * n_chunks > 1 concatenates independent generator calls (substream seeds per
+ * chunk) in time so large instances can be produced on all host cores. */
+typedef struct cs_synth_params {
+  uint64_t n_cycles;
+  uint64_t workload_seed;
+  uint64_t synth_seed;
+  int32_t fault_family;    /* -1 none, else FaultFamily enum (simkit.hpp:70-79) */
+  int32_t target_rank;
+  uint64_t fault_onset;    /* global cycle index */
+  uint64_t fault_duration;
+  double severity;         /* <= 0: default_severity (simkit.cpp:134-146) */
+  uint64_t n_ranks;
+  double noise;            /* < 0: GroundTruthModel default 0.05 */
+} cs_synth_params;
+typedef struct cs_synth_trace cs_synth_trace;
+int cs_synth_generate(const cs_synth_params* p, uint32_t n_chunks, uint32_t n_threads,
+                      int compact_names, cs_synth_trace** out);
+int cs_synth_view(const cs_synth_trace* t, const cs_event** ev, uint64_t* n_ev,
+                  const uint64_t** event_ids, const cs_workload** wl, uint64_t* n_wl,
+                  const uint8_t** labels, uint64_t* n_cycles);
+int cs_synth_names(const cs_synth_trace* t, const char** packed, size_t* n_bytes,
+                   uint32_t* n_names, uint32_t* n_comm);
+void cs_synth_free(cs_synth_trace* t);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CYCLESCOPE_B200_H_ */

@@ -1,0 +1,725 @@
+// ref_bridge.cpp — TEST INFRASTRUCTURE ONLY (the parity checker, never the
+// product).  A C ABI over the reference implementation compiled unmodified
+// from /root/reference/proj/src into oracle/_ref/ (see oracle/Makefile).
+//
+// It lets tests, __graft_entry__.smoke() and bench.py's reference arm:
+//   * synthesize traces with the reference's simkit (simkit.cpp:34-86,276-506),
+//   * build a reference `Trace` from our binary records (inverse ingest),
+//   * export a `Trace` into our binary records (the oracle-side ingest, an
+//     implementation independent of the product's),
+//   * run the reference hot path exactly like `monitor_loop`
+//     (tools/main.cpp:142-214) plus `cycle_stats` beta (rca.cpp:71-130) and
+//     capture every intermediate for bit-exact comparison.
+// Only the reference's public headers are used; no reference code is copied.
+
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <set>
+#include <string>
+#include <thread>
+#include <tuple>
+#include <vector>
+
+#include <nlohmann/json.hpp>
+
+#include "cyclescope/baseline.hpp"
+#include "cyclescope/config.hpp"
+#include "cyclescope/cycles.hpp"
+#include "cyclescope/detector.hpp"
+#include "cyclescope/errors.hpp"
+#include "cyclescope/gbdt.hpp"
+#include "cyclescope/rca.hpp"
+#include "cyclescope/rng.hpp"
+#include "cyclescope/simkit.hpp"
+#include "cyclescope/trace.hpp"
+#include "cyclescope_b200.h"
+
+using namespace cyclescope;
+using nlohmann::json;
+
+namespace {
+
+struct Exported {
+  std::vector<cs_event> events;
+  std::vector<cs_workload> workloads;
+  std::vector<std::string> names;
+  std::string names_packed;  // NUL separated
+  std::vector<std::tuple<std::string, std::string, int>> comm;  // slot -> key
+  std::vector<int32_t> comm_name, comm_rank;
+  std::string comm_hash_packed;
+  std::vector<uint64_t> event_ids;
+};
+
+struct Results {
+  int status = 0;
+  std::string err_type, err_msg;
+  std::vector<cs_anchor_candidate> candidates;
+  std::string anchor;
+  bool fallback = false;
+  std::vector<cs_cycle> cycles;
+  std::vector<int64_t> components;  // n_cycles x n_phases
+  std::vector<int64_t> beta_totals; // n_cycles x n_slots
+  std::vector<double> beta;
+  std::vector<double> coll_beta;    // n_cycles x n_comm
+  std::vector<uint8_t> coll_present;
+  std::vector<cs_record> records;
+  std::vector<cs_alert> alerts;
+  std::string model_json;
+  double ucl = 0.0;
+  uint64_t first_bad_record = UINT64_MAX;
+  double seconds = 0.0;
+};
+
+struct Handle {
+  LabeledDataset ds;
+  Exported ex;
+  bool exported = false;
+  Results res;
+  std::string last_config;
+};
+
+int stage_code(Stage s) {
+  switch (s) {
+    case Stage::Prefill: return CS_STAGE_PREFILL;
+    case Stage::Decode: return CS_STAGE_DECODE;
+    default: return CS_STAGE_UNKNOWN;
+  }
+}
+
+// The oracle-side ingest: Trace -> 32-byte records.  Written independently of
+// the product's ingest; the shared contract is include/cyclescope_b200.h.
+void export_trace(Handle& h, const CycleConfig& cfg) {
+  Exported& ex = h.ex;
+  ex = Exported{};
+  const auto& ev = h.ds.trace.events;
+  std::set<std::string> name_set;
+  std::set<std::tuple<std::string, std::string, int>> comm_set;
+  for (const auto& e : ev) {
+    name_set.insert(e.name);
+    if (e.kind == EventKind::Span && e.category == EventCategory::CollectiveComm) {
+      auto comm = arg_string(e, "commHash");
+      auto rank = arg_int(e, "rank");
+      if (comm && rank) comm_set.insert({e.name, *comm, static_cast<int>(*rank)});
+    }
+  }
+  ex.names.assign(name_set.begin(), name_set.end());
+  std::map<std::string, uint32_t> name_id;
+  for (uint32_t i = 0; i < ex.names.size(); ++i) {
+    name_id[ex.names[i]] = i;
+    ex.names_packed += ex.names[i];
+    ex.names_packed.push_back('\0');
+  }
+  std::map<std::tuple<std::string, std::string, int>, uint32_t> comm_slot;
+  for (const auto& k : comm_set) {
+    comm_slot[k] = static_cast<uint32_t>(ex.comm.size());
+    ex.comm.push_back(k);
+    ex.comm_name.push_back(static_cast<int32_t>(name_id[std::get<0>(k)]));
+    ex.comm_rank.push_back(std::get<2>(k));
+    ex.comm_hash_packed += std::get<1>(k);
+    ex.comm_hash_packed.push_back('\0');
+  }
+  ex.events.resize(ev.size());
+  ex.event_ids.resize(ev.size());
+  for (size_t i = 0; i < ev.size(); ++i) {
+    const auto& e = ev[i];
+    cs_event& r = ex.events[i];
+    std::memset(&r, 0, sizeof r);
+    r.start_ts = e.start_ts;
+    r.duration = e.kind == EventKind::Span ? e.duration : 0;
+    r.name_id = name_id[e.name];
+    r.kind = static_cast<uint8_t>(e.kind);
+    r.category = static_cast<uint8_t>(e.category);
+    uint16_t flags = 0;
+    if (auto fm = arg_string(e, cfg.forward_mode_key)) {
+      std::string m = *fm;
+      for (auto& c : m) c = static_cast<char>(std::tolower(static_cast<unsigned char>(c)));
+      if (m.find("prefill") != std::string::npos || m.find("extend") != std::string::npos)
+        flags |= CS_EV_FM_PREFILL;
+      else if (m.find("decode") != std::string::npos)
+        flags |= CS_EV_FM_DECODE;
+      else
+        flags |= CS_EV_FM_OTHER;
+    }
+    if (auto b = arg_int(e, cfg.batch_size_key)) {
+      flags |= CS_EV_HAS_BATCH;
+      auto in = arg_int(e, cfg.input_len_key);
+      auto out = arg_int(e, cfg.output_len_key);
+      cs_workload w{*b, in ? *in : INT64_MIN, out ? *out : INT64_MIN};
+      if (in && out && *b >= 0 && *in >= 0 && *out >= 0) flags |= CS_EV_WL_OK;
+      r.payload |= static_cast<uint64_t>(ex.workloads.size());
+      ex.workloads.push_back(w);
+    }
+    if (e.kind == EventKind::Span && e.category == EventCategory::CollectiveComm) {
+      auto comm = arg_string(e, "commHash");
+      auto rank = arg_int(e, "rank");
+      if (comm && rank) {
+        flags |= CS_EV_HAS_COMM;
+        r.payload |= static_cast<uint64_t>(comm_slot[{e.name, *comm, static_cast<int>(*rank)}]) << 32;
+      }
+    }
+    if (e.kind == EventKind::Counter) {
+      if (auto v = arg_number(e, "value")) {
+        flags |= CS_EV_HAS_VALUE;
+        std::memcpy(&r.duration, &*v, sizeof(double));
+      }
+    }
+    r.flags = flags;
+    ex.event_ids[i] = e.event_id;
+  }
+  h.exported = true;
+}
+
+void set_error(Results& r, const EngineError& e) {
+  r.status = 1;
+  r.err_type = e.type();
+  r.err_msg = e.what();
+}
+
+// monitor_loop (main.cpp:142-214) trace branch, plus beta for every cycle.
+void run_reference(Handle& h, const RunConfig& config, const char* model_json,
+                   uint64_t train_cycles, int do_beta) {
+  Results& R = h.res;
+  R = Results{};
+  const Trace& trace = h.ds.trace;
+  std::map<uint64_t, uint64_t> pos_of_id;
+  for (size_t i = 0; i < trace.events.size(); ++i) pos_of_id[trace.events[i].event_id] = i;
+  if (!h.exported) export_trace(h, config.cycle);
+  std::map<std::string, uint32_t> name_id;
+  for (uint32_t i = 0; i < h.ex.names.size(); ++i) name_id[h.ex.names[i]] = i;
+
+  // dense beta slots over names that occur as spans, lexicographic order
+  std::map<std::string, int> beta_slot;
+  {
+    std::set<std::string> span_names;
+    for (const auto& e : trace.events)
+      if (e.kind == EventKind::Span) span_names.insert(e.name);
+    int s = 0;
+    for (const auto& n : span_names) beta_slot[n] = s++;
+  }
+  std::map<std::tuple<std::string, std::string, int>, int> comm_slot;
+  for (size_t i = 0; i < h.ex.comm.size(); ++i) comm_slot[h.ex.comm[i]] = static_cast<int>(i);
+
+  // phase order = first occurrence in phase_functions
+  std::vector<std::string> phases;
+  for (const auto& p : config.cycle.phase_functions)
+    if (std::find(phases.begin(), phases.end(), p) == phases.end()) phases.push_back(p);
+
+  const auto t0 = std::chrono::steady_clock::now();
+  std::vector<Cycle> cycles;
+  try {
+    try {
+      auto cands = rank_anchor_candidates(trace, config.cycle);
+      for (const auto& c : cands) {
+        cs_anchor_candidate a{};
+        a.name_id = name_id.count(c.name) ? name_id[c.name] : UINT32_MAX;
+        a.call_count = c.call_count;
+        a.mean_duration_ns = c.mean_duration_ns;
+        a.duration_cv = c.duration_cv;
+        a.score = c.score;
+        R.candidates.push_back(a);
+      }
+      const auto anchor = discover_anchor(trace, config.cycle);
+      R.anchor = anchor.name;
+      cycles = segment(trace, anchor.name, config.cycle);
+    } catch (const NoAnchorFound&) {
+      R.fallback = true;
+      cycles = segment_by_frequency(trace, config.cycle);
+      if (cycles.empty()) throw;
+    }
+    classify_stages(cycles, trace, config.cycle);
+  } catch (const EngineError& e) {
+    set_error(R, e);
+    return;
+  }
+  for (const auto& c : cycles) {
+    cs_cycle o{};
+    o.index = c.index;
+    o.start_ts = c.start_ts;
+    o.end_ts = c.end_ts;
+    o.anchor_pos = c.anchor_event_id ? pos_of_id[*c.anchor_event_id] : UINT64_MAX;
+    o.anchor_span_end = c.anchor_span_end;
+    o.first_event = c.first_event;
+    o.last_event = c.last_event;
+    o.stage = stage_code(c.stage);
+    try {
+      extract_workload(c, trace, config.cycle);
+      o.workload_status = 0;
+    } catch (const MissingWorkloadArgs&) {
+      bool carrier = false;
+      for (size_t j = c.first_event; j < c.last_event && !carrier; ++j)
+        carrier = arg_int(trace.events[j], config.cycle.batch_size_key).has_value();
+      o.workload_status = carrier ? 2 : 1;
+    }
+    R.cycles.push_back(o);
+    for (const auto& p : phases) {
+      auto it = c.component_durations.find(p);
+      R.components.push_back(it == c.component_durations.end() ? 0 : it->second);
+    }
+  }
+  if (do_beta) {
+    const size_t ns = beta_slot.size(), nc = comm_slot.size();
+    R.beta_totals.assign(cycles.size() * ns, 0);
+    R.beta.assign(cycles.size() * ns, 0.0);
+    R.coll_beta.assign(cycles.size() * nc, 0.0);
+    R.coll_present.assign(cycles.size() * nc, 0);
+    const CounterTable no_counters;
+    const MetricMap no_metrics;
+    for (size_t ci = 0; ci < cycles.size(); ++ci) {
+      const auto st = cycle_stats(cycles[ci], trace, no_counters, no_metrics);
+      for (const auto& [name, cs] : st.classes) {
+        R.beta_totals[ci * ns + beta_slot[name]] = cs.total_duration;
+        R.beta[ci * ns + beta_slot[name]] = cs.beta;
+      }
+      for (const auto& [key, b] : st.collective_rank_beta) {
+        const int s = comm_slot[key];
+        R.coll_beta[ci * nc + s] = b;
+        R.coll_present[ci * nc + s] = 1;
+      }
+    }
+  }
+  std::vector<CycleRecord> records;
+  try {
+    records = build_cycle_records(trace, cycles, config.cycle, config.pipeline);
+  } catch (const EngineError& e) {
+    set_error(R, e);
+    return;
+  }
+  LatencyModel model;
+  try {
+    if (model_json && *model_json) {
+      model = LatencyModel::from_json(json::parse(model_json));
+    } else {
+      std::vector<CycleRecord> train;
+      for (const auto& r : records)
+        if (r.cycle_index < train_cycles) train.push_back(r);
+      const auto samples = to_sample_set(train, config.feature_set);
+      model = fit_latency_model(samples, config.gbdt, config.fit);
+    }
+    R.model_json = model.to_json().dump();
+  } catch (const EngineError& e) {
+    set_error(R, e);
+    return;
+  }
+  // monitor_loop process lambda (main.cpp:151-177), every record in order
+  const double ucl = ucl_from_stats(model.mu_train, model.sigma_train, config.detector);
+  R.ucl = ucl;
+  Detector detector(config.detector, ucl);
+  try {
+    for (size_t i = 0; i < records.size(); ++i) {
+      const auto& rec = records[i];
+      cs_record o{};
+      o.cycle_index = rec.cycle_index;
+      o.start_ts = rec.start_ts;
+      o.batch = rec.workload.batch;
+      o.input_len = rec.workload.input_len;
+      o.output_len = rec.workload.output_len;
+      o.latency_s = rec.latency_s;
+      o.stage = stage_code(rec.stage);
+      std::vector<double> row;
+      for (const auto& name : model.feature_names) {
+        if (name == "batch") row.push_back(static_cast<double>(rec.workload.batch));
+        else if (name == "w_kv") row.push_back(static_cast<double>(rec.workload.kv_token_slots()));
+        else if (name == "input_len") row.push_back(static_cast<double>(rec.workload.input_len));
+        else if (name == "output_len") row.push_back(static_cast<double>(rec.workload.output_len));
+        else if (name == "stage") row.push_back(rec.stage == Stage::Prefill ? 1.0 : 0.0);
+        else throw FeatureMismatch("input lacks feature '" + name + "'");
+      }
+      o.predicted_s = model.predict(row);
+      R.records.push_back(o);
+      if (!(rec.latency_s > 0.0)) {
+        R.first_bad_record = i;
+        o.residual = ppe(rec.latency_s, o.predicted_s, config.detector.epsilon);  // throws
+      }
+      ResidualSample sample;
+      sample.cycle = rec.cycle_index;
+      sample.ts = rec.start_ts;
+      sample.workload = rec.workload;
+      sample.actual_s = rec.latency_s;
+      sample.predicted_s = o.predicted_s;
+      sample.error = ppe(rec.latency_s, o.predicted_s, config.detector.epsilon);
+      const auto step = detector.step(sample);
+      auto& out = R.records.back();
+      out.residual = sample.error;
+      out.statistic = step.statistic;
+      out.armed = step.armed;
+      out.flagged = step.flagged;
+      out.alert = step.alert.has_value();
+      if (step.alert) {
+        out.episode_id = step.alert->episode_id;
+        cs_alert a{};
+        a.cycle = step.alert->cycle;
+        a.ts = step.alert->ts;
+        a.smoothed_error = step.alert->smoothed_error;
+        a.limit = step.alert->limit;
+        a.strategy = static_cast<int32_t>(step.alert->strategy);
+        a.batch = step.alert->workload.batch;
+        a.input_len = step.alert->workload.input_len;
+        a.output_len = step.alert->workload.output_len;
+        a.episode_id = step.alert->episode_id;
+        a.record_index = i;
+        R.alerts.push_back(a);
+      }
+    }
+  } catch (const EngineError& e) {
+    set_error(R, e);
+  }
+  R.seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+template <typename T>
+int copy_out(const std::vector<T>& v, T* buf, size_t cap, size_t* n) {
+  if (n) *n = v.size();
+  if (!buf) return 0;
+  if (cap < v.size()) return 1;
+  if (!v.empty()) std::memcpy(buf, v.data(), v.size() * sizeof(T));
+  return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+struct ref_synth_params {
+  uint64_t n_cycles;
+  uint64_t workload_seed;
+  uint64_t synth_seed;
+  int32_t fault_family;   // -1 none
+  int32_t target_rank;
+  uint64_t fault_onset;
+  uint64_t fault_duration;
+  double severity;        // <= 0: default_severity
+  uint64_t n_ranks;
+  double noise;           // < 0: default
+};
+
+void* ref_synth(const ref_synth_params* p) {
+  auto h = std::make_unique<Handle>();
+  const auto workloads = generate_workload(WorkloadProfile{}, p->n_cycles, p->workload_seed);
+  GroundTruthModel model;
+  if (p->noise >= 0.0) model.noise = p->noise;
+  std::vector<FaultSpec> faults;
+  if (p->fault_family >= 0) {
+    FaultSpec f;
+    f.family = static_cast<FaultFamily>(p->fault_family);
+    f.onset = p->fault_onset;
+    f.duration = p->fault_duration;
+    f.severity = p->severity > 0.0 ? p->severity : default_severity(f.family);
+    f.target_rank = p->target_rank;
+    faults.push_back(f);
+  }
+  SynthOptions opt;
+  opt.n_ranks = p->n_ranks;
+  h->ds = synthesize_trace(workloads, model, faults, opt, p->synth_seed);
+  return h.release();
+}
+
+// Inverse ingest: binary records -> reference Trace.  forward_mode classes map
+// to "prefill"/"decode"/"other"; comm slots to commHash strings.
+void* ref_build(uint64_t n, const cs_event* ev, const uint64_t* event_ids,
+                uint32_t n_names, const char* names_packed, const cs_workload* wl,
+                uint32_t n_comm, const char* comm_hash_packed, const int32_t* comm_rank,
+                int sort) {
+  auto h = std::make_unique<Handle>();
+  std::vector<std::string> names;
+  const char* p = names_packed;
+  for (uint32_t i = 0; i < n_names; ++i) {
+    names.emplace_back(p);
+    p += names.back().size() + 1;
+  }
+  std::vector<std::string> comms;
+  p = comm_hash_packed;
+  for (uint32_t i = 0; i < n_comm; ++i) {
+    comms.emplace_back(p);
+    p += comms.back().size() + 1;
+  }
+  auto& events = h->ds.trace.events;
+  events.resize(n);
+  for (uint64_t i = 0; i < n; ++i) {
+    const cs_event& r = ev[i];
+    TraceEvent& e = events[i];
+    e.event_id = event_ids ? event_ids[i] : i + 1;
+    e.kind = static_cast<EventKind>(r.kind);
+    e.category = static_cast<EventCategory>(r.category);
+    e.name = names.at(r.name_id);
+    e.start_ts = r.start_ts;
+    e.duration = r.kind == CS_SPAN ? r.duration : 0;
+    const uint32_t fm = r.flags & CS_EV_FM_MASK;
+    if (fm == CS_EV_FM_PREFILL) e.args["forward_mode"] = std::string("prefill");
+    if (fm == CS_EV_FM_DECODE) e.args["forward_mode"] = std::string("decode");
+    if (fm == CS_EV_FM_OTHER) e.args["forward_mode"] = std::string("idle");
+    if (r.flags & CS_EV_HAS_BATCH) {
+      const cs_workload& w = wl[r.payload & 0xffffffffu];
+      e.args["batch_size"] = w.batch;
+      if (w.input_len != INT64_MIN) e.args["input_len"] = w.input_len;
+      if (w.output_len != INT64_MIN) e.args["output_len"] = w.output_len;
+    }
+    if (r.flags & CS_EV_HAS_COMM) {
+      const uint32_t s = static_cast<uint32_t>(r.payload >> 32);
+      e.args["commHash"] = comms.at(s);
+      e.args["rank"] = static_cast<int64_t>(comm_rank[s]);
+    }
+    if (r.kind == CS_COUNTER && (r.flags & CS_EV_HAS_VALUE)) {
+      double v;
+      std::memcpy(&v, &r.duration, sizeof v);
+      e.args["value"] = v;
+    }
+  }
+  if (sort) h->ds.trace.sort_events();
+  return h.release();
+}
+
+void ref_free(void* h) { delete static_cast<Handle*>(h); }
+
+uint64_t ref_n_events(void* hv) { return static_cast<Handle*>(hv)->ds.trace.events.size(); }
+
+int ref_labels(void* hv, uint8_t* buf, size_t cap, size_t* n) {
+  auto* h = static_cast<Handle*>(hv);
+  std::vector<uint8_t> v(h->ds.labels.anomalous.begin(), h->ds.labels.anomalous.end());
+  return copy_out(v, buf, cap, n);
+}
+
+// Export with the CycleConfig of a RunConfig JSON ("" = defaults).
+int ref_export(void* hv, const char* run_config_json) {
+  auto* h = static_cast<Handle*>(hv);
+  try {
+    RunConfig cfg = (run_config_json && *run_config_json)
+                        ? RunConfig::from_json(json::parse(run_config_json))
+                        : RunConfig{};
+    export_trace(*h, cfg.cycle);
+  } catch (const std::exception&) {
+    return 1;
+  }
+  return 0;
+}
+
+int ref_get_events(void* hv, cs_event* buf, size_t cap, size_t* n) {
+  return copy_out(static_cast<Handle*>(hv)->ex.events, buf, cap, n);
+}
+int ref_get_event_ids(void* hv, uint64_t* buf, size_t cap, size_t* n) {
+  return copy_out(static_cast<Handle*>(hv)->ex.event_ids, buf, cap, n);
+}
+int ref_get_workloads(void* hv, cs_workload* buf, size_t cap, size_t* n) {
+  return copy_out(static_cast<Handle*>(hv)->ex.workloads, buf, cap, n);
+}
+int ref_get_names(void* hv, char* buf, size_t cap, size_t* n_bytes, uint32_t* n_names) {
+  auto* h = static_cast<Handle*>(hv);
+  if (n_names) *n_names = static_cast<uint32_t>(h->ex.names.size());
+  std::vector<char> v(h->ex.names_packed.begin(), h->ex.names_packed.end());
+  return copy_out(v, buf, cap, n_bytes);
+}
+int ref_get_comm(void* hv, int32_t* name, int32_t* rank, char* hash_buf, size_t cap,
+                 size_t* n_bytes, uint32_t* n_comm) {
+  auto* h = static_cast<Handle*>(hv);
+  if (n_comm) *n_comm = static_cast<uint32_t>(h->ex.comm.size());
+  if (name) std::copy(h->ex.comm_name.begin(), h->ex.comm_name.end(), name);
+  if (rank) std::copy(h->ex.comm_rank.begin(), h->ex.comm_rank.end(), rank);
+  std::vector<char> v(h->ex.comm_hash_packed.begin(), h->ex.comm_hash_packed.end());
+  return copy_out(v, hash_buf, cap, n_bytes);
+}
+
+// Runs the reference hot path.  model_json: LatencyModel JSON, or NULL/"" to
+// fit on records with cycle_index < train_cycles (evaluate_trial split,
+// simkit.cpp:836-846).  Returns 0; the reference's outcome is in ref_status.
+int ref_run(void* hv, const char* run_config_json, const char* model_json,
+            uint64_t train_cycles, int do_beta) {
+  auto* h = static_cast<Handle*>(hv);
+  RunConfig cfg;
+  try {
+    if (run_config_json && *run_config_json) cfg = RunConfig::from_json(json::parse(run_config_json));
+  } catch (const std::exception& e) {
+    h->res = Results{};
+    h->res.status = 2;
+    h->res.err_type = "config_error";
+    h->res.err_msg = e.what();
+    return 0;
+  }
+  run_reference(*h, cfg, model_json, train_cycles, do_beta);
+  return 0;
+}
+
+int ref_status(void* hv, char* type_buf, size_t type_cap, char* msg_buf, size_t msg_cap) {
+  auto* h = static_cast<Handle*>(hv);
+  if (type_buf && type_cap) {
+    std::strncpy(type_buf, h->res.err_type.c_str(), type_cap - 1);
+    type_buf[type_cap - 1] = 0;
+  }
+  if (msg_buf && msg_cap) {
+    std::strncpy(msg_buf, h->res.err_msg.c_str(), msg_cap - 1);
+    msg_buf[msg_cap - 1] = 0;
+  }
+  return h->res.status;
+}
+
+int ref_anchor(void* hv, char* buf, size_t cap, int* fallback) {
+  auto* h = static_cast<Handle*>(hv);
+  if (fallback) *fallback = h->res.fallback;
+  if (buf && cap) {
+    std::strncpy(buf, h->res.anchor.c_str(), cap - 1);
+    buf[cap - 1] = 0;
+  }
+  return 0;
+}
+double ref_ucl(void* hv) { return static_cast<Handle*>(hv)->res.ucl; }
+double ref_seconds(void* hv) { return static_cast<Handle*>(hv)->res.seconds; }
+uint64_t ref_first_bad_record(void* hv) { return static_cast<Handle*>(hv)->res.first_bad_record; }
+
+int ref_get_candidates(void* hv, cs_anchor_candidate* buf, size_t cap, size_t* n) {
+  return copy_out(static_cast<Handle*>(hv)->res.candidates, buf, cap, n);
+}
+int ref_get_cycles(void* hv, cs_cycle* buf, size_t cap, size_t* n) {
+  return copy_out(static_cast<Handle*>(hv)->res.cycles, buf, cap, n);
+}
+int ref_get_components(void* hv, int64_t* buf, size_t cap, size_t* n) {
+  return copy_out(static_cast<Handle*>(hv)->res.components, buf, cap, n);
+}
+int ref_get_beta(void* hv, int64_t* totals, double* beta, size_t cap, size_t* n) {
+  auto* h = static_cast<Handle*>(hv);
+  if (copy_out(h->res.beta_totals, totals, cap, n)) return 1;
+  return copy_out(h->res.beta, beta, cap, n);
+}
+int ref_get_collective_beta(void* hv, double* beta, uint8_t* present, size_t cap, size_t* n) {
+  auto* h = static_cast<Handle*>(hv);
+  if (copy_out(h->res.coll_beta, beta, cap, n)) return 1;
+  return copy_out(h->res.coll_present, present, cap, n);
+}
+int ref_get_records(void* hv, cs_record* buf, size_t cap, size_t* n) {
+  return copy_out(static_cast<Handle*>(hv)->res.records, buf, cap, n);
+}
+int ref_get_alerts(void* hv, cs_alert* buf, size_t cap, size_t* n) {
+  return copy_out(static_cast<Handle*>(hv)->res.alerts, buf, cap, n);
+}
+int ref_get_model_json(void* hv, char* buf, size_t cap, size_t* n) {
+  auto* h = static_cast<Handle*>(hv);
+  std::vector<char> v(h->res.model_json.begin(), h->res.model_json.end());
+  v.push_back('\0');
+  return copy_out(v, buf, cap, n);
+}
+
+// Reference fit on explicit samples (fit_latency_model, baseline.cpp:168-208),
+// returns the model JSON (dump()).  Used to pin the product's host fit.
+int ref_fit(uint64_t n, uint32_t n_features, const char* feature_names_packed,
+            const double* x, const double* y, const cs_gbdt_params* gp,
+            const cs_fit_options* fo, char* buf, size_t cap, size_t* n_out,
+            char* err, size_t err_cap) {
+  try {
+    SampleSet s;
+    const char* p = feature_names_packed;
+    for (uint32_t i = 0; i < n_features; ++i) {
+      s.feature_names.emplace_back(p);
+      p += s.feature_names.back().size() + 1;
+    }
+    s.x.cols = n_features;
+    for (uint64_t i = 0; i < n; ++i) {
+      s.x.push_row(std::span<const double>(x + i * n_features, n_features));
+      s.y.push_back(y[i]);
+    }
+    GbdtParams params;
+    params.n_trees = gp->n_trees;
+    params.max_depth = gp->max_depth;
+    params.learning_rate = gp->learning_rate;
+    params.min_samples_leaf = gp->min_samples_leaf;
+    params.prediction_floor = gp->prediction_floor;
+    FitOptions opt;
+    opt.calibration_fraction = fo->calibration_fraction;
+    opt.ppe_epsilon = fo->ppe_epsilon;
+    opt.min_samples = fo->min_samples;
+    if (fo->stratify_col >= 0 && static_cast<uint32_t>(fo->stratify_col) < n_features)
+      opt.stratify_feature = s.feature_names[fo->stratify_col];
+    const auto m = fit_latency_model(s, params, opt);
+    std::string j = m.to_json().dump();
+    std::vector<char> v(j.begin(), j.end());
+    v.push_back('\0');
+    return copy_out(v, buf, cap, n_out);
+  } catch (const EngineError& e) {
+    if (err && err_cap) {
+      std::snprintf(err, err_cap, "%s: %s", e.type().c_str(), e.what());
+    }
+    return 2;
+  }
+}
+
+// The CPU baseline (bench.py --impl reference): `n_threads` std::threads, one
+// monitored instance each, on simkit traces generated in-process.
+// Times the A4-A16 chain (segment_and_classify + build_cycle_records + beta
+// cycle_stats + predict + ppe + Detector::step) with the model fit excluded.
+// Returns total events analysed; *seconds = wall time of the timed region.
+uint64_t ref_cpu_baseline(uint32_t n_instances, uint32_t n_threads, uint64_t cycles_per_instance,
+                          uint64_t n_ranks, uint64_t seed, double* seconds,
+                          uint64_t* n_alerts_out) {
+  std::vector<std::unique_ptr<Handle>> inst(n_instances);
+  std::vector<LatencyModel> models(n_instances);
+  auto prepare = [&](uint32_t i) {
+    ref_synth_params p{};
+    p.n_cycles = cycles_per_instance;
+    p.workload_seed = Rng::substream_seed(seed, 2 * i);
+    p.synth_seed = Rng::substream_seed(seed, 2 * i + 1);
+    p.fault_family = static_cast<int32_t>(FaultFamily::NvlinkSaturation);
+    p.target_rank = 3 % static_cast<int32_t>(std::max<uint64_t>(1, n_ranks));
+    p.fault_onset = cycles_per_instance * 4 / 5;
+    p.fault_duration = 150;
+    p.severity = -1;
+    p.n_ranks = n_ranks;
+    p.noise = -1;
+    inst[i].reset(static_cast<Handle*>(ref_synth(&p)));
+    CycleConfig cc;
+    PipelineOptions po;
+    auto recs = build_cycle_records(inst[i]->ds.trace, cc, po);
+    std::vector<CycleRecord> train;
+    for (auto& r : recs)
+      if (r.cycle_index < 2400) train.push_back(r);
+    models[i] = fit_latency_model(to_sample_set(train, FeatureSet::Physical), GbdtParams{});
+  };
+  {
+    std::vector<std::thread> th;
+    for (uint32_t t = 0; t < n_threads; ++t)
+      th.emplace_back([&, t] {
+        for (uint32_t i = t; i < n_instances; i += n_threads) prepare(i);
+      });
+    for (auto& x : th) x.join();
+  }
+  std::vector<uint64_t> alerts(n_instances, 0);
+  auto work = [&](uint32_t i) {
+    const Trace& tr = inst[i]->ds.trace;
+    CycleConfig cc;
+    PipelineOptions po;
+    ControlConfig dc;
+    const auto cycles = segment_and_classify(tr, cc);
+    const CounterTable no_counters;
+    const MetricMap no_metrics;
+    double sink = 0.0;
+    for (const auto& c : cycles) sink += cycle_stats(c, tr, no_counters, no_metrics).classes.size();
+    const auto recs = build_cycle_records(tr, cycles, cc, po);
+    Detector det(dc, ucl_from_stats(models[i].mu_train, models[i].sigma_train, dc));
+    for (const auto& r : recs) {
+      const double row[2] = {static_cast<double>(r.workload.batch),
+                             static_cast<double>(r.workload.kv_token_slots())};
+      ResidualSample s;
+      s.cycle = r.cycle_index;
+      s.error = ppe(r.latency_s, models[i].predict(row), dc.epsilon);
+      if (det.step(s).alert) ++alerts[i];
+    }
+    if (sink < 0) alerts[i] += 1;
+  };
+  const auto t0 = std::chrono::steady_clock::now();
+  {
+    std::vector<std::thread> th;
+    for (uint32_t t = 0; t < n_threads; ++t)
+      th.emplace_back([&, t] {
+        for (uint32_t i = t; i < n_instances; i += n_threads) work(i);
+      });
+    for (auto& x : th) x.join();
+  }
+  *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  uint64_t events = 0, na = 0;
+  for (uint32_t i = 0; i < n_instances; ++i) {
+    events += inst[i]->ds.trace.events.size();
+    na += alerts[i];
+  }
+  if (n_alerts_out) *n_alerts_out = na;
+  return events;
+}
+
+}  // extern "C"

@@ -1,0 +1,252 @@
+"""TEST INFRASTRUCTURE ONLY — Python handle on oracle/_ref/libcsref.so.
+
+The library is the reference implementation (/root/reference/proj/src)
+compiled unmodified plus our bridge (oracle/ref_bridge.cpp).  Only tests/,
+__graft_entry__.smoke() and bench.py's reference / cpu_baseline legs may use
+it, and only as the checker or the timed CPU baseline.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import json
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from paper_2601_09258_b200 import abi
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "_ref", "libcsref.so")
+
+_lib = None
+
+
+def available() -> bool:
+    return os.path.exists(LIB_PATH)
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not available():
+            raise RuntimeError(f"reference oracle not built: {LIB_PATH} (run make -C oracle)")
+        L = C.CDLL(LIB_PATH)
+        vp, sz = C.c_void_p, C.c_size_t
+        L.ref_synth.restype = vp
+        L.ref_synth.argtypes = [C.c_void_p]
+        L.ref_build.restype = vp
+        L.ref_build.argtypes = [C.c_uint64, vp, vp, C.c_uint32, C.c_char_p, vp, C.c_uint32,
+                                C.c_char_p, vp, C.c_int]
+        L.ref_free.argtypes = [vp]
+        L.ref_n_events.restype = C.c_uint64
+        L.ref_n_events.argtypes = [vp]
+        L.ref_export.argtypes = [vp, C.c_char_p]
+        L.ref_run.argtypes = [vp, C.c_char_p, C.c_char_p, C.c_uint64, C.c_int]
+        L.ref_status.argtypes = [vp, C.c_char_p, sz, C.c_char_p, sz]
+        L.ref_anchor.argtypes = [vp, C.c_char_p, sz, C.POINTER(C.c_int)]
+        L.ref_ucl.restype = C.c_double
+        L.ref_ucl.argtypes = [vp]
+        L.ref_seconds.restype = C.c_double
+        L.ref_seconds.argtypes = [vp]
+        L.ref_first_bad_record.restype = C.c_uint64
+        L.ref_first_bad_record.argtypes = [vp]
+        for fn in ("ref_get_events", "ref_get_event_ids", "ref_get_workloads", "ref_labels",
+                   "ref_get_candidates", "ref_get_cycles", "ref_get_components",
+                   "ref_get_records", "ref_get_alerts", "ref_get_model_json"):
+            getattr(L, fn).argtypes = [vp, vp, sz, C.POINTER(sz)]
+        L.ref_get_names.argtypes = [vp, vp, sz, C.POINTER(sz), C.POINTER(C.c_uint32)]
+        L.ref_get_comm.argtypes = [vp, vp, vp, vp, sz, C.POINTER(sz), C.POINTER(C.c_uint32)]
+        L.ref_get_beta.argtypes = [vp, vp, vp, sz, C.POINTER(sz)]
+        L.ref_get_collective_beta.argtypes = [vp, vp, vp, sz, C.POINTER(sz)]
+        L.ref_fit.argtypes = [C.c_uint64, C.c_uint32, C.c_char_p, vp, vp, vp, vp, vp, sz,
+                              C.POINTER(sz), C.c_char_p, sz]
+        L.ref_cpu_baseline.restype = C.c_uint64
+        L.ref_cpu_baseline.argtypes = [C.c_uint32, C.c_uint32, C.c_uint64, C.c_uint64,
+                                       C.c_uint64, C.POINTER(C.c_double),
+                                       C.POINTER(C.c_uint64)]
+        _lib = L
+    return _lib
+
+
+class SynthParams(C.Structure):
+    _fields_ = [("n_cycles", C.c_uint64), ("workload_seed", C.c_uint64),
+                ("synth_seed", C.c_uint64), ("fault_family", C.c_int32),
+                ("target_rank", C.c_int32), ("fault_onset", C.c_uint64),
+                ("fault_duration", C.c_uint64), ("severity", C.c_double),
+                ("n_ranks", C.c_uint64), ("noise", C.c_double)]
+
+
+FAULT_FAMILIES = ["cpu_contention", "cpu_freq_drop", "gpu_contention", "gpu_clock_lock",
+                  "memory_thrash", "nvlink_saturation", "pcie_bottleneck", "bus_contention"]
+
+
+def _get(fn, h, dtype, n_hint=None):
+    n = C.c_size_t(0)
+    fn(h, None, 0, C.byref(n))
+    out = np.zeros(n.value, dtype=dtype)
+    if n.value:
+        fn(h, out.ctypes.data, n.value, C.byref(n))
+    return out
+
+
+@dataclass
+class Exported:
+    events: np.ndarray
+    event_ids: np.ndarray
+    workloads: np.ndarray
+    names: list
+    comm_name: np.ndarray
+    comm_rank: np.ndarray
+    comm_hash: list
+
+
+@dataclass
+class RefResult:
+    status: int
+    err_type: str
+    err_msg: str
+    anchor: str
+    fallback: bool
+    candidates: np.ndarray
+    cycles: np.ndarray
+    components: np.ndarray
+    beta_totals: np.ndarray
+    beta: np.ndarray
+    coll_beta: np.ndarray
+    coll_present: np.ndarray
+    records: np.ndarray
+    alerts: np.ndarray
+    model_json: str
+    ucl: float
+    first_bad_record: int
+    seconds: float
+    extra: dict = field(default_factory=dict)
+
+
+class RefTrace:
+    """A reference `Trace` living in the oracle library."""
+
+    def __init__(self, handle):
+        self.h = handle
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.ref_free(self.h)
+            self.h = None
+
+    @classmethod
+    def synth(cls, n_cycles, workload_seed, synth_seed, fault=None, onset=0, duration=0,
+              severity=-1.0, target_rank=0, n_ranks=1, noise=-1.0):
+        fam = -1 if fault is None else (FAULT_FAMILIES.index(fault) if isinstance(fault, str) else int(fault))
+        p = SynthParams(n_cycles, workload_seed, synth_seed, fam, target_rank, onset, duration,
+                        severity, n_ranks, noise)
+        return cls(lib().ref_synth(C.byref(p)))
+
+    @classmethod
+    def build(cls, events, names, workloads=None, comm_hash=(), comm_rank=(), event_ids=None,
+              sort=True):
+        events = np.ascontiguousarray(events, dtype=abi.EVENT_DTYPE)
+        wl = np.ascontiguousarray(workloads if workloads is not None else
+                                  np.zeros(0, abi.WORKLOAD_DTYPE), dtype=abi.WORKLOAD_DTYPE)
+        packed = b"".join(n.encode() + b"\0" for n in names)
+        cpacked = b"".join(c.encode() + b"\0" for c in comm_hash) or b"\0"
+        crank = np.ascontiguousarray(np.asarray(comm_rank, dtype=np.int32))
+        ids = None if event_ids is None else np.ascontiguousarray(event_ids, dtype=np.uint64)
+        h = lib().ref_build(len(events), events.ctypes.data,
+                            None if ids is None else ids.ctypes.data, len(names), packed,
+                            wl.ctypes.data if len(wl) else None, len(comm_hash), cpacked,
+                            crank.ctypes.data if len(crank) else None, int(sort))
+        t = cls(h)
+        t._keep = (events, wl, crank, ids)
+        return t
+
+    def n_events(self):
+        return int(lib().ref_n_events(self.h))
+
+    def labels(self):
+        return _get(lib().ref_labels, self.h, np.uint8).astype(bool)
+
+    def export(self, run_config: dict | None = None) -> Exported:
+        L = lib()
+        assert L.ref_export(self.h, json.dumps(run_config or {}).encode()) == 0
+        ev = _get(L.ref_get_events, self.h, abi.EVENT_DTYPE)
+        ids = _get(L.ref_get_event_ids, self.h, np.uint64)
+        wl = _get(L.ref_get_workloads, self.h, abi.WORKLOAD_DTYPE)
+        nb, nn = C.c_size_t(0), C.c_uint32(0)
+        L.ref_get_names(self.h, None, 0, C.byref(nb), C.byref(nn))
+        buf = C.create_string_buffer(nb.value + 1)
+        L.ref_get_names(self.h, buf, nb.value, C.byref(nb), C.byref(nn))
+        names = buf.raw[:nb.value].split(b"\0")[:nn.value]
+        cb, nc = C.c_size_t(0), C.c_uint32(0)
+        L.ref_get_comm(self.h, None, None, None, 0, C.byref(cb), C.byref(nc))
+        cn = np.zeros(nc.value, np.int32)
+        cr = np.zeros(nc.value, np.int32)
+        cbuf = C.create_string_buffer(cb.value + 1)
+        L.ref_get_comm(self.h, cn.ctypes.data, cr.ctypes.data, cbuf, cb.value, C.byref(cb),
+                       C.byref(nc))
+        hashes = cbuf.raw[:cb.value].split(b"\0")[:nc.value]
+        return Exported(ev, ids, wl, [n.decode() for n in names], cn, cr,
+                        [h.decode() for h in hashes])
+
+    def run(self, run_config: dict | None = None, model_json: str | None = None,
+            train_cycles: int = 2400, beta: bool = True) -> RefResult:
+        L = lib()
+        L.ref_run(self.h, json.dumps(run_config or {}).encode(),
+                  (model_json or "").encode(), train_cycles, int(beta))
+        tb, mb = C.create_string_buffer(256), C.create_string_buffer(4096)
+        status = L.ref_status(self.h, tb, 256, mb, 4096)
+        ab, fb = C.create_string_buffer(4096), C.c_int(0)
+        L.ref_anchor(self.h, ab, 4096, C.byref(fb))
+        n = C.c_size_t(0)
+        L.ref_get_beta(self.h, None, None, 0, C.byref(n))
+        bt = np.zeros(n.value, np.int64)
+        bb = np.zeros(n.value, np.float64)
+        if n.value:
+            L.ref_get_beta(self.h, bt.ctypes.data, bb.ctypes.data, n.value, C.byref(n))
+        L.ref_get_collective_beta(self.h, None, None, 0, C.byref(n))
+        cbeta = np.zeros(n.value, np.float64)
+        cpres = np.zeros(n.value, np.uint8)
+        if n.value:
+            L.ref_get_collective_beta(self.h, cbeta.ctypes.data, cpres.ctypes.data, n.value,
+                                      C.byref(n))
+        mj = _get(L.ref_get_model_json, self.h, np.uint8)
+        return RefResult(
+            status=status, err_type=tb.value.decode(), err_msg=mb.value.decode(),
+            anchor=ab.value.decode(), fallback=bool(fb.value),
+            candidates=_get(L.ref_get_candidates, self.h, abi.CANDIDATE_DTYPE),
+            cycles=_get(L.ref_get_cycles, self.h, abi.CYCLE_DTYPE),
+            components=_get(L.ref_get_components, self.h, np.int64),
+            beta_totals=bt, beta=bb, coll_beta=cbeta, coll_present=cpres,
+            records=_get(L.ref_get_records, self.h, abi.RECORD_DTYPE),
+            alerts=_get(L.ref_get_alerts, self.h, abi.ALERT_DTYPE),
+            model_json=bytes(mj[:-1]).decode() if len(mj) else "",
+            ucl=L.ref_ucl(self.h), first_bad_record=int(L.ref_first_bad_record(self.h)),
+            seconds=L.ref_seconds(self.h))
+
+
+def ref_fit(x: np.ndarray, y: np.ndarray, feature_names, params=None, options=None) -> str:
+    """Reference fit_latency_model on explicit samples -> model JSON."""
+    L = lib()
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    params = params or abi.default_gbdt_params()
+    options = options or abi.default_fit_options(len(feature_names))
+    packed = b"".join(n.encode() + b"\0" for n in feature_names)
+    n = C.c_size_t(0)
+    err = C.create_string_buffer(1024)
+    cap = 1 << 24
+    buf = C.create_string_buffer(cap)
+    rc = L.ref_fit(len(y), len(feature_names), packed, x.ctypes.data, y.ctypes.data,
+                   C.byref(params), C.byref(options), buf, cap, C.byref(n), err, 1024)
+    if rc == 2:
+        raise RuntimeError(err.value.decode())
+    return buf.raw[:n.value - 1].decode()
+
+
+def cpu_baseline(n_instances, n_threads, cycles_per_instance, n_ranks, seed=42):
+    """Reference CPU analyzer on `n_threads` threads; returns (events, seconds, alerts)."""
+    secs, na = C.c_double(0), C.c_uint64(0)
+    ev = lib().ref_cpu_baseline(n_instances, n_threads, cycles_per_instance, n_ranks, seed,
+                                C.byref(secs), C.byref(na))
+    return int(ev), secs.value, int(na.value)

@@ -1,0 +1,1115 @@
+// cs_api.cpp — host runtime behind include/cyclescope_b200.h.
+//
+// Owns device memory (grow-only buffers sized for whole instances resident in
+// HBM), the ctx stream, and the orchestration of the kernels in
+// cs_kernels.cu.  Rare control-flow paths of the reference (ordered-fold
+// anchor tie break, wrong speculative anchor, NoAnchorFound -> frequency
+// fallback) are driven from here; every per-event / per-cycle / per-record
+// computation runs on the device.  There is no CPU fallback: without a device
+// every compute entry point fails with CS_E_NO_DEVICE.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <array>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "cs_internal.h"
+#include "cyclescope_b200.h"
+
+using namespace csb;
+
+namespace {
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  void* get(size_t bytes) {
+    if (bytes > cap) {
+      if (p) cudaFree(p);
+      p = nullptr;
+      cap = 0;
+      if (bytes == 0) return nullptr;
+      if (cudaMalloc(&p, bytes) != cudaSuccess) {
+        p = nullptr;
+        return nullptr;
+      }
+      cap = bytes;
+    }
+    return p;
+  }
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+};
+
+struct PackedModel {
+  uint32_t n_trees = 0, depth = 0, n_features = 0, degenerate = 0;
+  std::vector<int32_t> feature_ids;
+  std::vector<double> thr, leaf;
+  std::vector<uint8_t> feat;
+  double base = 0, lr = 0, floor_ = 0, mu = 0, sigma = 0;
+  DevBuf d_thr, d_leaf, d_feat;
+};
+
+}  // namespace
+
+struct cs_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::string err;
+  cs_cycle_config cyc{};
+  cs_control_config ctl{};
+  bool have_config = false;
+  std::vector<cs_name_info> names;
+  // inputs
+  uint32_t n_inst = 0;
+  uint64_t n_ev = 0, n_wl = 0;
+  std::vector<uint64_t> inst_off;
+  DevBuf d_ev, d_wl, d_names, d_inst_off;
+  // tiles
+  std::vector<uint32_t> tile_inst, inst_first_tile;
+  std::vector<uint64_t> tile_begin, tile_end;
+  DevBuf d_tile_inst, d_tile_begin, d_tile_end, d_inst_first_tile, d_tile_state, d_ticket;
+  // state
+  DevBuf d_stats, d_inst, d_a_pos, d_a_start, d_a_end;
+  std::vector<InstState> h_inst;
+  // cycles
+  std::vector<uint64_t> cyc_off;
+  uint64_t n_cycles = 0;
+  DevBuf d_cyc_off, c_start, c_end, c_apos, c_aend, c_first, c_last, c_inst, c_stage, c_local,
+      c_wl, c_comp, c_beta_tot, c_beta, c_coll, c_coll_n;
+  // records
+  DevBuf d_rec_off, rec_cycle, rec_pred, rec_resid, rec_stat, rec_flags, alert_rec, d_alert_off,
+      block_tmp;
+  std::vector<uint64_t> rec_off, alert_off;
+  uint64_t n_records = 0;
+  // models
+  std::vector<PackedModel*> model_store;
+  std::vector<int> model_of_inst;
+  DevBuf d_models;
+  std::vector<DevModel> h_models;
+  // fold results per instance: name -> (mean, cv, score)
+  std::vector<std::map<uint32_t, std::array<double, 3>>> folded;
+  std::vector<int> inst_status;
+  std::vector<int> used_fallback;
+  std::vector<uint64_t> fallback_cycles;
+  bool ran = false;
+  uint32_t last_mask = 0;
+  // timing
+  cudaEvent_t ev[16]{};
+  std::vector<std::pair<std::string, std::pair<int, int>>> timed;
+  uint64_t launches = 0;
+  DevBuf d_scratch;
+
+  ~cs_ctx() {
+    for (auto* m : model_store) delete m;
+    for (auto& e : ev)
+      if (e) cudaEventDestroy(e);
+    if (stream) cudaStreamDestroy(stream);
+  }
+};
+
+namespace {
+
+int fail(cs_ctx* ctx, int code, const std::string& msg) {
+  if (ctx) ctx->err = msg;
+  return code;
+}
+
+#define CS_CUDA(call)                                                                \
+  do {                                                                               \
+    cudaError_t e_ = (call);                                                         \
+    if (e_ != cudaSuccess)                                                           \
+      return fail(ctx, CS_E_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+double ucl_from_stats_host(double mu, double sigma, const cs_control_config& c) {
+  // detector.cpp:57-60
+  const double ucl = std::min(mu + c.sigma_k * sigma, c.theta_max);
+  return std::max(ucl, c.min_ucl);
+}
+
+template <typename T>
+T* dev(DevBuf& b, size_t n) {
+  return static_cast<T*>(b.get(std::max<size_t>(1, n) * sizeof(T)));
+}
+
+DevBuffers make_buffers(cs_ctx* ctx) {
+  DevBuffers b{};
+  b.ev = static_cast<const cs_event*>(ctx->d_ev.p);
+  b.wl = static_cast<const cs_workload*>(ctx->d_wl.p);
+  b.names = static_cast<const cs_name_info*>(ctx->d_names.p);
+  b.n_names = static_cast<uint32_t>(ctx->names.size());
+  b.n_inst = ctx->n_inst;
+  b.inst_off = static_cast<const uint64_t*>(ctx->d_inst_off.p);
+  b.tile_inst = static_cast<const uint32_t*>(ctx->d_tile_inst.p);
+  b.tile_begin = static_cast<const uint64_t*>(ctx->d_tile_begin.p);
+  b.tile_end = static_cast<const uint64_t*>(ctx->d_tile_end.p);
+  b.inst_first_tile = static_cast<const uint32_t*>(ctx->d_inst_first_tile.p);
+  b.n_tiles = static_cast<uint32_t>(ctx->tile_inst.size());
+  b.stats = static_cast<NameStat*>(ctx->d_stats.p);
+  b.inst = static_cast<InstState*>(ctx->d_inst.p);
+  b.tile_state = static_cast<unsigned long long*>(ctx->d_tile_state.p);
+  b.ticket = static_cast<unsigned int*>(ctx->d_ticket.p);
+  b.a_pos = static_cast<uint64_t*>(ctx->d_a_pos.p);
+  b.a_start = static_cast<int64_t*>(ctx->d_a_start.p);
+  b.a_end = static_cast<int64_t*>(ctx->d_a_end.p);
+  b.cyc_off = static_cast<const uint64_t*>(ctx->d_cyc_off.p);
+  b.n_cycles = ctx->n_cycles;
+  b.c_start = static_cast<int64_t*>(ctx->c_start.p);
+  b.c_end = static_cast<int64_t*>(ctx->c_end.p);
+  b.c_apos = static_cast<uint64_t*>(ctx->c_apos.p);
+  b.c_aend = static_cast<int64_t*>(ctx->c_aend.p);
+  b.c_first = static_cast<uint64_t*>(ctx->c_first.p);
+  b.c_last = static_cast<uint64_t*>(ctx->c_last.p);
+  b.c_inst = static_cast<uint32_t*>(ctx->c_inst.p);
+  b.c_stage = static_cast<uint8_t*>(ctx->c_stage.p);
+  b.c_local = static_cast<uint8_t*>(ctx->c_local.p);
+  b.c_wl = static_cast<int32_t*>(ctx->c_wl.p);
+  b.c_comp = static_cast<int64_t*>(ctx->c_comp.p);
+  b.c_beta_tot = static_cast<int64_t*>(ctx->c_beta_tot.p);
+  b.c_beta = static_cast<double*>(ctx->c_beta.p);
+  b.c_coll = static_cast<double*>(ctx->c_coll.p);
+  b.c_coll_n = static_cast<uint8_t*>(ctx->c_coll_n.p);
+  b.rec_off = static_cast<uint64_t*>(ctx->d_rec_off.p);
+  b.rec_cycle = static_cast<uint64_t*>(ctx->rec_cycle.p);
+  b.rec_pred = static_cast<double*>(ctx->rec_pred.p);
+  b.rec_resid = static_cast<double*>(ctx->rec_resid.p);
+  b.rec_stat = static_cast<double*>(ctx->rec_stat.p);
+  b.rec_flags = static_cast<uint8_t*>(ctx->rec_flags.p);
+  b.alert_rec = static_cast<uint64_t*>(ctx->alert_rec.p);
+  b.alert_off = static_cast<uint64_t*>(ctx->d_alert_off.p);
+  b.block_tmp = static_cast<uint64_t*>(ctx->block_tmp.p);
+  b.models = static_cast<const DevModel*>(ctx->d_models.p);
+  return b;
+}
+
+int tree_depth(const cs_tree_node* nodes, uint32_t n, int32_t i, int d, int* out_max,
+               int guard) {
+  if (i < 0 || static_cast<uint32_t>(i) >= n || guard > 64) return -1;
+  *out_max = std::max(*out_max, d);
+  if (nodes[i].feature < 0) return 0;
+  if (tree_depth(nodes, n, nodes[i].left, d + 1, out_max, guard + 1) < 0) return -1;
+  if (tree_depth(nodes, n, nodes[i].right, d + 1, out_max, guard + 1) < 0) return -1;
+  return 0;
+}
+
+void fill_complete(const cs_tree_node* nodes, int32_t i, uint32_t pos, int d, int D,
+                   double* thr, uint8_t* feat, double* leaf, int32_t const* fmap) {
+  const uint32_t ni = (1u << D) - 1;
+  if (d == D) {
+    leaf[pos - ni] = nodes[i].value;
+    return;
+  }
+  if (nodes[i].feature < 0) {
+    // leaf above the padded depth: always-left internal node, value copied
+    // to every descendant leaf (all but the leftmost are unreachable)
+    thr[pos] = std::numeric_limits<double>::infinity();
+    feat[pos] = 0;
+    fill_complete(nodes, i, 2 * pos + 1, d + 1, D, thr, feat, leaf, fmap);
+    fill_complete(nodes, i, 2 * pos + 2, d + 1, D, thr, feat, leaf, fmap);
+    return;
+  }
+  thr[pos] = nodes[i].threshold;
+  feat[pos] = static_cast<uint8_t>(nodes[i].feature);
+  fill_complete(nodes, nodes[i].left, 2 * pos + 1, d + 1, D, thr, feat, leaf, fmap);
+  fill_complete(nodes, nodes[i].right, 2 * pos + 2, d + 1, D, thr, feat, leaf, fmap);
+}
+
+}  // namespace
+
+extern "C" {
+
+int cs_abi_version(void) { return CS_ABI_VERSION; }
+
+const char* cs_status_type(int status) {
+  switch (status) {
+    case CS_OK: return "ok";
+    case CS_E_INVALID_ARGUMENT: return "invalid_argument";
+    case CS_E_NO_DEVICE: return "no_device";
+    case CS_E_CUDA: return "cuda_error";
+    case CS_E_NO_ANCHOR_FOUND: return "no_anchor_found";
+    case CS_E_MISSING_WORKLOAD: return "missing_workload_args";
+    case CS_E_FEATURE_MISMATCH: return "feature_mismatch";
+    case CS_E_NON_POSITIVE_LATENCY: return "non_positive_latency";
+    case CS_E_INSUFFICIENT_DATA: return "insufficient_data";
+    case CS_E_INSUFFICIENT_CALIBRATION: return "insufficient_calibration";
+    case CS_E_NO_LABELS: return "no_labels";
+    case CS_E_MODEL_FORMAT: return "model_format_error";
+    case CS_E_UNSUPPORTED: return "unsupported";
+    case CS_E_CONFIG: return "config_error";
+    default: return "internal";
+  }
+}
+
+int cs_ctx_create(int device, cs_ctx** out) {
+  if (!out) return CS_E_INVALID_ARGUMENT;
+  *out = nullptr;
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+    cudaGetLastError();
+    return CS_E_NO_DEVICE;
+  }
+  if (device < 0 || device >= n) return CS_E_INVALID_ARGUMENT;
+  if (cudaSetDevice(device) != cudaSuccess) return CS_E_NO_DEVICE;
+  auto* ctx = new cs_ctx();
+  ctx->device = device;
+  if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
+    delete ctx;
+    return CS_E_CUDA;
+  }
+  for (auto& e : ctx->ev) cudaEventCreate(&e);
+  // defaults: CycleConfig / ControlConfig
+  ctx->cyc.anchor_hint_name = -1;
+  ctx->cyc.min_anchor_calls = 10;
+  ctx->cyc.prefill_duration_factor = 3.0;
+  ctx->cyc.prefill_gap_factor = 2.0;
+  ctx->cyc.stage_window = 32;
+  ctx->cyc.stage_min_history = 8;
+  ctx->cyc.frequency_bin_ns = 1000000;
+  ctx->cyc.latency_phase = -1;
+  ctx->ctl.strategy = CS_DYNAMIC_WINDOW;
+  ctx->ctl.window = 10;
+  ctx->ctl.fixed_threshold = 0.15;
+  ctx->ctl.sigma_k = 3.0;
+  ctx->ctl.theta_max = 0.18;
+  ctx->ctl.min_ucl = 0.02;
+  ctx->ctl.warmup = 100;
+  ctx->ctl.epsilon = 1e-9;
+  *out = ctx;
+  return CS_OK;
+}
+
+void cs_ctx_destroy(cs_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  delete ctx;
+}
+
+const char* cs_last_error(const cs_ctx* ctx) { return ctx ? ctx->err.c_str() : ""; }
+
+int cs_set_config(cs_ctx* ctx, const cs_cycle_config* cycle, const cs_control_config* control) {
+  if (!ctx) return CS_E_INVALID_ARGUMENT;
+  if (cycle) {
+    if (cycle->n_phases < 0 || cycle->n_phases > kMaxPhases)
+      return fail(ctx, CS_E_UNSUPPORTED, "at most 8 phase functions are supported");
+    if (cycle->n_beta_slots < 0 || cycle->n_beta_slots > kMaxBetaSlots)
+      return fail(ctx, CS_E_UNSUPPORTED, "at most 64 span classes are supported");
+    if (cycle->n_comm_slots < 0 || cycle->n_comm_slots > kMaxCommSlots)
+      return fail(ctx, CS_E_UNSUPPORTED, "at most 64 collective slots are supported");
+    if (cycle->stage_window == 0 || cycle->stage_window > 32)
+      return fail(ctx, CS_E_UNSUPPORTED, "stage_window must be in [1, 32]");
+    if (cycle->latency_phase >= cycle->n_phases)
+      return fail(ctx, CS_E_INVALID_ARGUMENT, "latency_phase out of range");
+    if (cycle->frequency_bin_ns <= 0)
+      return fail(ctx, CS_E_INVALID_ARGUMENT, "frequency_bin_ns must be positive");
+    ctx->cyc = *cycle;
+  }
+  if (control) {
+    if (control->strategy < 0 || control->strategy > 2)
+      return fail(ctx, CS_E_CONFIG, "unknown detector strategy");
+    if (control->window == 0) return fail(ctx, CS_E_CONFIG, "window must be positive");
+    ctx->ctl = *control;
+  }
+  ctx->have_config = true;
+  return CS_OK;
+}
+
+int cs_set_name_table(cs_ctx* ctx, uint32_t n_names, const cs_name_info* names) {
+  if (!ctx || (n_names && !names)) return CS_E_INVALID_ARGUMENT;
+  cudaSetDevice(ctx->device);
+  ctx->names.assign(names, names + n_names);
+  for (const auto& n : ctx->names) {
+    if (n.phase >= kMaxPhases) return fail(ctx, CS_E_UNSUPPORTED, "phase index out of range");
+    if (n.beta_slot >= kMaxBetaSlots) return fail(ctx, CS_E_UNSUPPORTED, "beta slot out of range");
+  }
+  void* d = ctx->d_names.get(std::max<size_t>(1, n_names) * sizeof(cs_name_info));
+  if (!d) return fail(ctx, CS_E_CUDA, "cudaMalloc(names)");
+  if (n_names) CS_CUDA(cudaMemcpyAsync(d, names, n_names * sizeof(cs_name_info),
+                                       cudaMemcpyHostToDevice, ctx->stream));
+  return CS_OK;
+}
+
+int cs_upload(cs_ctx* ctx, uint32_t n_inst, const uint64_t* inst_offsets, const cs_event* ev,
+              uint64_t n_workloads, const cs_workload* wl) {
+  if (!ctx || !inst_offsets || n_inst == 0) return CS_E_INVALID_ARGUMENT;
+  cudaSetDevice(ctx->device);
+  if (inst_offsets[0] != 0) return fail(ctx, CS_E_INVALID_ARGUMENT, "inst_offsets[0] must be 0");
+  for (uint32_t i = 0; i < n_inst; ++i)
+    if (inst_offsets[i + 1] < inst_offsets[i])
+      return fail(ctx, CS_E_INVALID_ARGUMENT, "inst_offsets must be non-decreasing");
+  const uint64_t n_ev = inst_offsets[n_inst];
+  if (n_ev && !ev) return CS_E_INVALID_ARGUMENT;
+  if (n_workloads && !wl) return CS_E_INVALID_ARGUMENT;
+  ctx->n_inst = n_inst;
+  ctx->n_ev = n_ev;
+  ctx->n_wl = n_workloads;
+  ctx->inst_off.assign(inst_offsets, inst_offsets + n_inst + 1);
+  void* de = ctx->d_ev.get(std::max<uint64_t>(1, n_ev) * sizeof(cs_event));
+  void* dw = ctx->d_wl.get(std::max<uint64_t>(1, n_workloads) * sizeof(cs_workload));
+  void* doff = ctx->d_inst_off.get((n_inst + 1) * sizeof(uint64_t));
+  if (!de || !dw || !doff) return fail(ctx, CS_E_CUDA, "cudaMalloc(events)");
+  if (n_ev) CS_CUDA(cudaMemcpyAsync(de, ev, n_ev * sizeof(cs_event), cudaMemcpyHostToDevice,
+                                    ctx->stream));
+  if (n_workloads)
+    CS_CUDA(cudaMemcpyAsync(dw, wl, n_workloads * sizeof(cs_workload), cudaMemcpyHostToDevice,
+                            ctx->stream));
+  CS_CUDA(cudaMemcpyAsync(doff, ctx->inst_off.data(), (n_inst + 1) * sizeof(uint64_t),
+                          cudaMemcpyHostToDevice, ctx->stream));
+  // instance-aligned tiles
+  ctx->tile_inst.clear();
+  ctx->tile_begin.clear();
+  ctx->tile_end.clear();
+  ctx->inst_first_tile.assign(n_inst, 0);
+  for (uint32_t i = 0; i < n_inst; ++i) {
+    ctx->inst_first_tile[i] = static_cast<uint32_t>(ctx->tile_inst.size());
+    for (uint64_t t = inst_offsets[i]; t < inst_offsets[i + 1]; t += kTileEvents) {
+      ctx->tile_inst.push_back(i);
+      ctx->tile_begin.push_back(t);
+      ctx->tile_end.push_back(std::min<uint64_t>(t + kTileEvents, inst_offsets[i + 1]));
+    }
+  }
+  const size_t nt = ctx->tile_inst.size();
+  if (nt > 0xffffffffull) return fail(ctx, CS_E_UNSUPPORTED, "too many tiles");
+  auto* dti = dev<uint32_t>(ctx->d_tile_inst, nt);
+  auto* dtb = dev<uint64_t>(ctx->d_tile_begin, nt);
+  auto* dte = dev<uint64_t>(ctx->d_tile_end, nt);
+  auto* dft = dev<uint32_t>(ctx->d_inst_first_tile, n_inst);
+  if (!dti || !dtb || !dte || !dft || !dev<unsigned long long>(ctx->d_tile_state, nt) ||
+      !dev<unsigned int>(ctx->d_ticket, 1))
+    return fail(ctx, CS_E_CUDA, "cudaMalloc(tiles)");
+  if (nt) {
+    CS_CUDA(cudaMemcpyAsync(dti, ctx->tile_inst.data(), nt * 4, cudaMemcpyHostToDevice, ctx->stream));
+    CS_CUDA(cudaMemcpyAsync(dtb, ctx->tile_begin.data(), nt * 8, cudaMemcpyHostToDevice, ctx->stream));
+    CS_CUDA(cudaMemcpyAsync(dte, ctx->tile_end.data(), nt * 8, cudaMemcpyHostToDevice, ctx->stream));
+  }
+  CS_CUDA(cudaMemcpyAsync(dft, ctx->inst_first_tile.data(), n_inst * 4, cudaMemcpyHostToDevice,
+                          ctx->stream));
+  if (ctx->model_of_inst.size() != n_inst) ctx->model_of_inst.assign(n_inst, -1);
+  ctx->ran = false;
+  return CS_OK;
+}
+
+int cs_load_model(cs_ctx* ctx, uint32_t inst, const cs_model* m) {
+  if (!ctx || !m) return CS_E_INVALID_ARGUMENT;
+  cudaSetDevice(ctx->device);
+  if (m->n_features > static_cast<uint32_t>(kMaxFeatures))
+    return fail(ctx, CS_E_UNSUPPORTED, "at most 8 model features are supported on device");
+  auto* pm = new PackedModel();
+  pm->n_trees = m->n_trees;
+  pm->n_features = m->n_features;
+  pm->degenerate = m->degenerate ? 1u : 0u;
+  pm->base = m->base;
+  pm->lr = m->learning_rate;
+  pm->floor_ = m->prediction_floor;
+  pm->mu = m->mu_train;
+  pm->sigma = m->sigma_train;
+  for (uint32_t f = 0; f < m->n_features; ++f) {
+    const int32_t id = m->feature_ids[f];
+    if (id < CS_F_BATCH || id > CS_F_STAGE) {
+      delete pm;
+      return fail(ctx, CS_E_FEATURE_MISMATCH,
+                  "model feature is not one of batch/w_kv/input_len/output_len/stage");
+    }
+    pm->feature_ids.push_back(id);
+  }
+  int D = 0;
+  for (uint32_t t = 0; t < m->n_trees; ++t) {
+    const uint32_t n = m->tree_offsets[t + 1] - m->tree_offsets[t];
+    int dmax = 0;
+    if (n == 0 || tree_depth(m->nodes + m->tree_offsets[t], n, 0, 0, &dmax, 0) < 0) {
+      delete pm;
+      return fail(ctx, CS_E_MODEL_FORMAT, "malformed tree " + std::to_string(t));
+    }
+    for (uint32_t k = 0; k < n; ++k) {
+      const auto& nd = m->nodes[m->tree_offsets[t] + k];
+      if (nd.feature >= static_cast<int32_t>(m->n_features)) {
+        delete pm;
+        return fail(ctx, CS_E_MODEL_FORMAT, "tree node feature out of range");
+      }
+    }
+    D = std::max(D, dmax);
+  }
+  if (D > kMaxTreeDepth) {
+    delete pm;
+    return fail(ctx, CS_E_UNSUPPORTED, "tree depth > 8 is not supported on device");
+  }
+  pm->depth = static_cast<uint32_t>(D);
+  const uint32_t ni = (1u << D) - 1, nl = 1u << D;
+  pm->thr.assign(static_cast<size_t>(m->n_trees) * ni, 0.0);
+  pm->feat.assign(static_cast<size_t>(m->n_trees) * ni, 0);
+  pm->leaf.assign(static_cast<size_t>(m->n_trees) * nl, 0.0);
+  for (uint32_t t = 0; t < m->n_trees; ++t)
+    fill_complete(m->nodes + m->tree_offsets[t], 0, 0, 0, D, pm->thr.data() + t * ni,
+                  pm->feat.data() + t * ni, pm->leaf.data() + t * nl, nullptr);
+  void* a = pm->d_thr.get(std::max<size_t>(8, pm->thr.size() * 8));
+  void* b = pm->d_leaf.get(std::max<size_t>(8, pm->leaf.size() * 8));
+  void* c = pm->d_feat.get(std::max<size_t>(8, pm->feat.size()));
+  if (!a || !b || !c) {
+    delete pm;
+    return fail(ctx, CS_E_CUDA, "cudaMalloc(model)");
+  }
+  if (!pm->thr.empty()) cudaMemcpy(a, pm->thr.data(), pm->thr.size() * 8, cudaMemcpyHostToDevice);
+  if (!pm->leaf.empty()) cudaMemcpy(b, pm->leaf.data(), pm->leaf.size() * 8, cudaMemcpyHostToDevice);
+  if (!pm->feat.empty()) cudaMemcpy(c, pm->feat.data(), pm->feat.size(), cudaMemcpyHostToDevice);
+  ctx->model_store.push_back(pm);
+  const int id = static_cast<int>(ctx->model_store.size() - 1);
+  if (inst == UINT32_MAX) {
+    ctx->model_of_inst.assign(std::max<uint32_t>(ctx->n_inst, 1), id);
+  } else {
+    if (inst >= ctx->n_inst) return fail(ctx, CS_E_INVALID_ARGUMENT, "instance out of range");
+    if (ctx->model_of_inst.size() != ctx->n_inst) ctx->model_of_inst.assign(ctx->n_inst, -1);
+    ctx->model_of_inst[inst] = id;
+  }
+  return CS_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+int record_event(cs_ctx* ctx, int idx) {
+  cudaEventRecord(ctx->ev[idx], ctx->stream);
+  return idx;
+}
+
+// NoAnchorFound -> segment_by_frequency (cycles.cpp:283-343) for one instance.
+// Returns the number of cycles (0 = still NoAnchorFound); fills t0/period.
+int frequency_plan(cs_ctx* ctx, uint32_t i, int64_t* t0, int64_t* period, uint64_t* n) {
+  *n = 0;
+  const uint64_t b = ctx->inst_off[i], e = ctx->inst_off[i + 1];
+  auto* ext = dev<unsigned long long>(ctx->d_scratch, 3);
+  if (!ext) return fail(ctx, CS_E_CUDA, "cudaMalloc(scratch)");
+  unsigned long long init[3] = {0, ~0ull, 0};
+  CS_CUDA(cudaMemcpyAsync(ext, init, sizeof init, cudaMemcpyHostToDevice, ctx->stream));
+  launch_gpu_kernel_extent(static_cast<const cs_event*>(ctx->d_ev.p), b, e, ext, ctx->stream,
+                           &ctx->launches);
+  unsigned long long h[3];
+  CS_CUDA(cudaMemcpyAsync(h, ext, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
+  CS_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (h[0] < 4) return CS_OK;
+  const int64_t lo = static_cast<int64_t>(h[1] ^ (1ull << 63));
+  const int64_t hi = static_cast<int64_t>(h[2] ^ (1ull << 63));
+  const int64_t bin = ctx->cyc.frequency_bin_ns;
+  const uint64_t bins = static_cast<uint64_t>((hi - lo) / bin) + 1;
+  if (bins < 4) return CS_OK;
+  DevBuf hist, acc;
+  auto* dh = static_cast<double*>(hist.get(bins * 2 * sizeof(double)));
+  auto* da = static_cast<double*>(acc.get((bins / 2 + 1) * sizeof(double)));
+  if (!dh || !da) return fail(ctx, CS_E_CUDA, "cudaMalloc(hist)");
+  launch_freq_hist(static_cast<const cs_event*>(ctx->d_ev.p), b, e, lo, bin, bins, dh,
+                   ctx->stream, &ctx->launches);
+  launch_freq_autocorr(dh, bins, da, ctx->stream, &ctx->launches);
+  std::vector<double> a(bins / 2 + 1, 0.0);
+  CS_CUDA(cudaMemcpyAsync(a.data(), da, a.size() * sizeof(double), cudaMemcpyDeviceToHost,
+                          ctx->stream));
+  CS_CUDA(cudaStreamSynchronize(ctx->stream));
+  double best = 0.0;
+  uint64_t best_lag = 0;
+  for (uint64_t lag = 1; lag <= bins / 2; ++lag)
+    if (a[lag] > best) {
+      best = a[lag];
+      best_lag = lag;
+    }
+  if (best_lag == 0) return CS_OK;
+  *period = static_cast<int64_t>(best_lag) * bin;
+  *t0 = lo;
+  *n = static_cast<uint64_t>((hi - lo) / *period);
+  return CS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int cs_run(cs_ctx* ctx, uint32_t mask) {
+  if (!ctx) return CS_E_INVALID_ARGUMENT;
+  if (!(mask & CS_RUN_SEGMENT)) return fail(ctx, CS_E_INVALID_ARGUMENT, "CS_RUN_SEGMENT required");
+  if (ctx->n_inst == 0) return fail(ctx, CS_E_INVALID_ARGUMENT, "nothing uploaded");
+  CS_CUDA(cudaSetDevice(ctx->device));
+  cudaStream_t s = ctx->stream;
+  ctx->launches = 0;
+  ctx->timed.clear();
+  const uint32_t n_inst = ctx->n_inst;
+  const uint32_t n_names = static_cast<uint32_t>(ctx->names.size());
+  const int64_t hint = ctx->cyc.anchor_hint_name;
+  if (hint >= static_cast<int64_t>(n_names))
+    return fail(ctx, CS_E_INVALID_ARGUMENT, "anchor hint name id out of range");
+  if (n_names == 0 && ctx->n_ev) return fail(ctx, CS_E_INVALID_ARGUMENT, "name table not set");
+  // per-instance state
+  ctx->h_inst.assign(n_inst, InstState{});
+  for (auto& st : ctx->h_inst) {
+    st.guess = hint >= 0 ? static_cast<uint32_t>(hint) : UINT32_MAX;
+    st.anchor = UINT32_MAX;
+    st.first_bad_record = UINT64_MAX;
+  }
+  auto* d_inst = dev<InstState>(ctx->d_inst, n_inst);
+  auto* d_stats = dev<NameStat>(ctx->d_stats, static_cast<size_t>(n_inst) * std::max(1u, n_names));
+  const size_t cap_ev = std::max<uint64_t>(1, ctx->n_ev);
+  if (!d_inst || !d_stats || !dev<uint64_t>(ctx->d_a_pos, cap_ev) ||
+      !dev<int64_t>(ctx->d_a_start, cap_ev) || !dev<int64_t>(ctx->d_a_end, cap_ev))
+    return fail(ctx, CS_E_CUDA, "cudaMalloc(state)");
+  CS_CUDA(cudaMemcpyAsync(d_inst, ctx->h_inst.data(), n_inst * sizeof(InstState),
+                          cudaMemcpyHostToDevice, s));
+  const size_t stats_bytes = static_cast<size_t>(n_inst) * n_names * sizeof(NameStat);
+  const size_t nt = ctx->tile_inst.size();
+  DevConfig cfg{ctx->cyc, ctx->ctl, 0.0};
+  DevBuffers b = make_buffers(ctx);
+
+  const int e0 = record_event(ctx, 0);
+  if (hint == -1) {
+    // speculative anchor from a sample of every instance
+    if (stats_bytes) CS_CUDA(cudaMemsetAsync(d_stats, 0, stats_bytes, s));
+    launch_scan_events(b, cfg, 1, true, s, &ctx->launches);
+    launch_rank(b, cfg, 0, s, &ctx->launches);
+  }
+  if (stats_bytes) CS_CUDA(cudaMemsetAsync(d_stats, 0, stats_bytes, s));
+  CS_CUDA(cudaMemsetAsync(ctx->d_tile_state.p, 0, std::max<size_t>(1, nt) * 8, s));
+  CS_CUDA(cudaMemsetAsync(ctx->d_ticket.p, 0, 4, s));
+  const int e1 = record_event(ctx, 1);
+  launch_scan_events(b, cfg, 3, false, s, &ctx->launches);
+  const int e2 = record_event(ctx, 2);
+  ctx->timed.push_back({"scan_events", {e1, e2}});
+  launch_rank(b, cfg, 1, s, &ctx->launches);
+  CS_CUDA(cudaMemcpyAsync(ctx->h_inst.data(), d_inst, n_inst * sizeof(InstState),
+                          cudaMemcpyDeviceToHost, s));
+  CS_CUDA(cudaStreamSynchronize(s));
+
+  // ---- rare paths: ordered fold for uncertified rankings
+  ctx->folded.assign(n_inst, {});
+  std::vector<uint32_t> pi, pn;
+  std::vector<NameStat> hs;
+  bool any_amb = false;
+  for (uint32_t i = 0; i < n_inst; ++i) any_amb |= ctx->h_inst[i].ambiguous != 0;
+  if (any_amb) {
+    hs.resize(static_cast<size_t>(n_inst) * n_names);
+    CS_CUDA(cudaMemcpy(hs.data(), d_stats, stats_bytes, cudaMemcpyDeviceToHost));
+    for (uint32_t i = 0; i < n_inst; ++i) {
+      if (!ctx->h_inst[i].ambiguous) continue;
+      for (uint32_t n = 0; n < n_names; ++n) {
+        const NameStat& st = hs[static_cast<size_t>(i) * n_names + n];
+        if (st.count >= ctx->cyc.min_anchor_calls && st.count > 0) {
+          pi.push_back(i);
+          pn.push_back(n);
+        }
+      }
+    }
+    DevBuf dpi, dpn, dout;
+    auto* a = static_cast<uint32_t*>(dpi.get(pi.size() * 4));
+    auto* c = static_cast<uint32_t*>(dpn.get(pn.size() * 4));
+    auto* o = static_cast<double*>(dout.get(pi.size() * 24));
+    if (!a || !c || !o) return fail(ctx, CS_E_CUDA, "cudaMalloc(fold)");
+    CS_CUDA(cudaMemcpy(a, pi.data(), pi.size() * 4, cudaMemcpyHostToDevice));
+    CS_CUDA(cudaMemcpy(c, pn.data(), pn.size() * 4, cudaMemcpyHostToDevice));
+    launch_fold(b, cfg, a, c, static_cast<uint32_t>(pi.size()), o, s, &ctx->launches);
+    std::vector<double> res(pi.size() * 3);
+    CS_CUDA(cudaMemcpyAsync(res.data(), o, res.size() * 8, cudaMemcpyDeviceToHost, s));
+    CS_CUDA(cudaStreamSynchronize(s));
+    std::vector<double> best_score(n_inst, -1.0);
+    std::vector<uint32_t> best_name(n_inst, UINT32_MAX);
+    for (size_t k = 0; k < pi.size(); ++k) {
+      const uint32_t i = pi[k];
+      ctx->folded[i][pn[k]] = {res[3 * k], res[3 * k + 1], res[3 * k + 2]};
+      const double sc = res[3 * k + 2];
+      // std::sort by score desc then name asc (cycles.cpp:81-85)
+      if (sc > best_score[i] || (sc == best_score[i] && pn[k] < best_name[i])) {
+        best_score[i] = sc;
+        best_name[i] = pn[k];
+      }
+    }
+    for (uint32_t i = 0; i < n_inst; ++i) {
+      if (!ctx->h_inst[i].ambiguous) continue;
+      auto& st = ctx->h_inst[i];
+      st.anchor = best_name[i];
+      st.no_anchor = best_name[i] == UINT32_MAX;
+      st.redo = (!st.no_anchor && st.anchor != st.guess) ? 1u : 0u;
+    }
+  }
+  // ---- wrong speculation: compact again for the right anchor
+  bool any_redo = false;
+  for (uint32_t i = 0; i < n_inst; ++i) any_redo |= ctx->h_inst[i].redo != 0;
+  if (any_redo || any_amb) {
+    CS_CUDA(cudaMemcpyAsync(d_inst, ctx->h_inst.data(), n_inst * sizeof(InstState),
+                            cudaMemcpyHostToDevice, s));
+  }
+  if (any_redo) {
+    CS_CUDA(cudaMemsetAsync(ctx->d_tile_state.p, 0, std::max<size_t>(1, nt) * 8, s));
+    CS_CUDA(cudaMemsetAsync(ctx->d_ticket.p, 0, 4, s));
+    launch_scan_events(b, cfg, 2 | 4, false, s, &ctx->launches);
+    CS_CUDA(cudaMemcpyAsync(ctx->h_inst.data(), d_inst, n_inst * sizeof(InstState),
+                            cudaMemcpyDeviceToHost, s));
+    CS_CUDA(cudaStreamSynchronize(s));
+  }
+  // ---- cycles per instance (frequency fallback where no anchor)
+  ctx->inst_status.assign(n_inst, CS_OK);
+  ctx->used_fallback.assign(n_inst, 0);
+  ctx->fallback_cycles.assign(n_inst, 0);
+  std::vector<int64_t> f_t0(n_inst, 0), f_period(n_inst, 0);
+  ctx->cyc_off.assign(n_inst + 1, 0);
+  for (uint32_t i = 0; i < n_inst; ++i) {
+    uint64_t nc = 0;
+    const auto& st = ctx->h_inst[i];
+    if (st.no_anchor) {
+      int rc = frequency_plan(ctx, i, &f_t0[i], &f_period[i], &nc);
+      if (rc != CS_OK) return rc;
+      ctx->used_fallback[i] = 1;
+      ctx->fallback_cycles[i] = nc;
+      if (nc == 0) ctx->inst_status[i] = CS_E_NO_ANCHOR_FOUND;
+    } else {
+      nc = st.n_anchors >= 2 ? st.n_anchors - 1 : 0;
+    }
+    ctx->cyc_off[i + 1] = ctx->cyc_off[i] + nc;
+  }
+  const uint64_t n_cyc = ctx->cyc_off[n_inst];
+  ctx->n_cycles = n_cyc;
+  const int P = ctx->cyc.n_phases, C = ctx->cyc.n_beta_slots, R = ctx->cyc.n_comm_slots;
+  const size_t nc1 = std::max<uint64_t>(1, n_cyc);
+  if (!dev<uint64_t>(ctx->d_cyc_off, n_inst + 1) || !dev<int64_t>(ctx->c_start, nc1) ||
+      !dev<int64_t>(ctx->c_end, nc1) || !dev<uint64_t>(ctx->c_apos, nc1) ||
+      !dev<int64_t>(ctx->c_aend, nc1) || !dev<uint64_t>(ctx->c_first, nc1) ||
+      !dev<uint64_t>(ctx->c_last, nc1) || !dev<uint32_t>(ctx->c_inst, nc1) ||
+      !dev<uint8_t>(ctx->c_stage, nc1) || !dev<uint8_t>(ctx->c_local, nc1) ||
+      !dev<int32_t>(ctx->c_wl, nc1) || !dev<int64_t>(ctx->c_comp, nc1 * std::max(P, 1)) ||
+      !dev<int64_t>(ctx->c_beta_tot, nc1 * std::max(C, 1)) ||
+      !dev<double>(ctx->c_beta, nc1 * std::max(C, 1)) ||
+      !dev<double>(ctx->c_coll, nc1 * std::max(R, 1)) ||
+      !dev<uint8_t>(ctx->c_coll_n, nc1 * std::max(R, 1)) ||
+      !dev<uint64_t>(ctx->d_rec_off, n_inst + 1) || !dev<uint64_t>(ctx->rec_cycle, nc1) ||
+      !dev<double>(ctx->rec_pred, nc1) || !dev<double>(ctx->rec_resid, nc1) ||
+      !dev<double>(ctx->rec_stat, nc1) || !dev<uint8_t>(ctx->rec_flags, nc1) ||
+      !dev<uint64_t>(ctx->alert_rec, nc1) || !dev<uint64_t>(ctx->d_alert_off, n_inst + 1) ||
+      !dev<uint64_t>(ctx->block_tmp, nc1 / 1024 + 16))
+    return fail(ctx, CS_E_CUDA, "cudaMalloc(cycles)");
+  CS_CUDA(cudaMemcpyAsync(ctx->d_cyc_off.p, ctx->cyc_off.data(), (n_inst + 1) * 8,
+                          cudaMemcpyHostToDevice, s));
+  b = make_buffers(ctx);
+  const int e3 = record_event(ctx, 3);
+  launch_bounds(b, s, &ctx->launches);
+  for (uint32_t i = 0; i < n_inst; ++i)
+    if (ctx->used_fallback[i] && ctx->fallback_cycles[i])
+      launch_freq_cycles(static_cast<const cs_event*>(ctx->d_ev.p), ctx->inst_off[i],
+                         ctx->inst_off[i + 1], f_t0[i], f_period[i], ctx->fallback_cycles[i],
+                         ctx->cyc_off[i], b, i, s, &ctx->launches);
+  const int e4 = record_event(ctx, 4);
+  launch_cycle_reduce(b, cfg, (mask & CS_RUN_BETA) ? 1 : 0, s, &ctx->launches);
+  const int e5 = record_event(ctx, 5);
+  launch_stage_heuristic(b, cfg, s, &ctx->launches);
+  launch_records(b, cfg, 0, s, &ctx->launches);
+  const int e6 = record_event(ctx, 6);
+  ctx->timed.push_back({"bounds", {e3, e4}});
+  ctx->timed.push_back({"cycle_reduce", {e4, e5}});
+  ctx->timed.push_back({"stage_records", {e5, e6}});
+  ctx->rec_off.assign(n_inst + 1, 0);
+  CS_CUDA(cudaMemcpyAsync(ctx->rec_off.data(), ctx->d_rec_off.p, (n_inst + 1) * 8,
+                          cudaMemcpyDeviceToHost, s));
+  CS_CUDA(cudaStreamSynchronize(s));
+  ctx->n_records = ctx->rec_off[n_inst];
+  int last = e6;
+  // ---- score + detect
+  if (mask & (CS_RUN_SCORE | CS_RUN_DETECT)) {
+    ctx->h_models.assign(n_inst, DevModel{});
+    uint32_t nf0 = UINT32_MAX;
+    for (uint32_t i = 0; i < n_inst; ++i) {
+      const int id = i < ctx->model_of_inst.size() ? ctx->model_of_inst[i] : -1;
+      if (id < 0) return fail(ctx, CS_E_INVALID_ARGUMENT, "no model loaded for an instance");
+      const PackedModel* pm = ctx->model_store[id];
+      if (nf0 == UINT32_MAX) nf0 = pm->n_features;
+      if (pm->n_features != nf0)
+        return fail(ctx, CS_E_UNSUPPORTED, "all instances of a batch must share the feature count");
+      DevModel& dm = ctx->h_models[i];
+      dm.n_trees = pm->n_trees;
+      dm.depth = pm->depth;
+      dm.n_features = pm->n_features;
+      dm.degenerate = pm->degenerate;
+      for (uint32_t f = 0; f < pm->n_features; ++f) dm.feature_ids[f] = pm->feature_ids[f];
+      dm.base = pm->base;
+      dm.lr = pm->lr;
+      dm.floor_ = pm->floor_;
+      dm.mu = pm->mu;
+      dm.sigma = pm->sigma;
+      dm.ucl = ctx->ctl.strategy == CS_DYNAMIC_WINDOW ? ucl_from_stats_host(pm->mu, pm->sigma, ctx->ctl)
+                                                      : ctx->ctl.fixed_threshold;
+      dm.thr = static_cast<const double*>(pm->d_thr.p);
+      dm.leaf = static_cast<const double*>(pm->d_leaf.p);
+      dm.feat = static_cast<const uint8_t*>(pm->d_feat.p);
+      dm.smem_bytes = static_cast<uint64_t>(pm->thr.size()) * 8 + pm->leaf.size() * 8 +
+                      pm->feat.size();
+    }
+    auto* dm = dev<DevModel>(ctx->d_models, n_inst);
+    if (!dm) return fail(ctx, CS_E_CUDA, "cudaMalloc(models)");
+    CS_CUDA(cudaMemcpyAsync(dm, ctx->h_models.data(), n_inst * sizeof(DevModel),
+                            cudaMemcpyHostToDevice, s));
+    b = make_buffers(ctx);
+    if (!dev<uint64_t>(ctx->block_tmp, ctx->n_records / 1024 + 16))
+      return fail(ctx, CS_E_CUDA, "cudaMalloc(block_tmp)");
+    b = make_buffers(ctx);
+    launch_score(b, cfg, ctx->n_records, ctx->rec_off.data(), ctx->model_of_inst.data(),
+                 ctx->h_models.data(), s, &ctx->launches);
+    const int e7 = record_event(ctx, 7);
+    ctx->timed.push_back({"score", {e6, e7}});
+    last = e7;
+    if (mask & CS_RUN_DETECT) {
+      launch_detect(b, cfg, ctx->n_records, s, &ctx->launches);
+      const int e8 = record_event(ctx, 8);
+      ctx->timed.push_back({"detect", {e7, e8}});
+      last = e8;
+    }
+  }
+  ctx->timed.push_back({"total", {e0, last}});
+  CS_CUDA(cudaMemcpyAsync(ctx->h_inst.data(), d_inst, n_inst * sizeof(InstState),
+                          cudaMemcpyDeviceToHost, s));
+  ctx->alert_off.assign(n_inst + 1, 0);
+  if (mask & CS_RUN_DETECT)
+    CS_CUDA(cudaMemcpyAsync(ctx->alert_off.data(), ctx->d_alert_off.p, (n_inst + 1) * 8,
+                            cudaMemcpyDeviceToHost, s));
+  CS_CUDA(cudaStreamSynchronize(s));
+  CS_CUDA(cudaGetLastError());
+  for (uint32_t i = 0; i < n_inst; ++i)
+    if (ctx->inst_status[i] == CS_OK && ctx->h_inst[i].first_bad_record != UINT64_MAX &&
+        (mask & (CS_RUN_SCORE | CS_RUN_DETECT)))
+      ctx->inst_status[i] = CS_E_NON_POSITIVE_LATENCY;
+  ctx->ran = true;
+  ctx->last_mask = mask;
+  return CS_OK;
+}
+
+int cs_sync(cs_ctx* ctx) {
+  if (!ctx) return CS_E_INVALID_ARGUMENT;
+  CS_CUDA(cudaStreamSynchronize(ctx->stream));
+  return CS_OK;
+}
+
+int cs_get_summary(cs_ctx* ctx, uint32_t inst, cs_instance_summary* out) {
+  if (!ctx || !out || !ctx->ran || inst >= ctx->n_inst) return CS_E_INVALID_ARGUMENT;
+  const auto& st = ctx->h_inst[inst];
+  out->anchor_name_id = ctx->used_fallback[inst] ? UINT32_MAX : st.anchor;
+  out->status = ctx->inst_status[inst];
+  out->n_cycles = ctx->cyc_off[inst + 1] - ctx->cyc_off[inst];
+  out->n_records = ctx->rec_off[inst + 1] - ctx->rec_off[inst];
+  out->n_alerts = ctx->alert_off[inst + 1] - ctx->alert_off[inst];
+  out->first_bad_record = st.first_bad_record;
+  out->ucl = inst < ctx->h_models.size() ? ctx->h_models[inst].ucl : 0.0;
+  out->used_frequency_fallback = ctx->used_fallback[inst];
+  out->anchor_ambiguous = static_cast<int32_t>(st.ambiguous);
+  return CS_OK;
+}
+
+int cs_get_candidates(cs_ctx* ctx, uint32_t inst, cs_anchor_candidate* buf, size_t cap,
+                      size_t* n) {
+  if (!ctx || !ctx->ran || inst >= ctx->n_inst) return CS_E_INVALID_ARGUMENT;
+  const uint32_t nn = static_cast<uint32_t>(ctx->names.size());
+  std::vector<NameStat> hs(nn);
+  if (nn)
+    CS_CUDA(cudaMemcpy(hs.data(), static_cast<NameStat*>(ctx->d_stats.p) + static_cast<size_t>(inst) * nn,
+                       nn * sizeof(NameStat), cudaMemcpyDeviceToHost));
+  std::vector<cs_anchor_candidate> out;
+  for (uint32_t k = 0; k < nn; ++k) {
+    const NameStat& s = hs[k];
+    if (s.count < ctx->cyc.min_anchor_calls || s.count == 0) continue;
+    cs_anchor_candidate c{};
+    c.name_id = k;
+    c.call_count = s.count;
+    auto it = ctx->folded[inst].find(k);
+    if (it != ctx->folded[inst].end()) {
+      c.mean_duration_ns = it->second[0];
+      c.duration_cv = it->second[1];
+      c.score = it->second[2];
+    } else {
+      // exact moments; within a few ulps of the reference's ordered sums
+      const double nd = static_cast<double>(s.count);
+      const double sumsq = static_cast<double>(s.sumsq_hi) * 18446744073709551616.0 +
+                           static_cast<double>(s.sumsq_lo);
+      c.mean_duration_ns = static_cast<double>(static_cast<int64_t>(s.sum)) / nd;
+      double cv = 0.0;
+      if (c.mean_duration_ns > 0.0) {
+        const double var = std::max(0.0, sumsq / nd - c.mean_duration_ns * c.mean_duration_ns);
+        cv = std::sqrt(var) / c.mean_duration_ns;
+      }
+      c.duration_cv = cv;
+      c.score = nd / (1.0 + cv);
+    }
+    out.push_back(c);
+  }
+  std::sort(out.begin(), out.end(), [](const cs_anchor_candidate& a, const cs_anchor_candidate& b) {
+    if (a.score != b.score) return a.score > b.score;
+    return a.name_id < b.name_id;
+  });
+  if (n) *n = out.size();
+  if (!buf) return CS_OK;
+  if (cap < out.size()) return fail(ctx, CS_E_INVALID_ARGUMENT, "buffer too small");
+  std::copy(out.begin(), out.end(), buf);
+  return CS_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+template <typename T>
+int d2h(cs_ctx* ctx, std::vector<T>& v, const DevBuf& b, uint64_t off, uint64_t n) {
+  v.resize(n);
+  if (n) CS_CUDA(cudaMemcpy(v.data(), static_cast<const T*>(b.p) + off, n * sizeof(T),
+                            cudaMemcpyDeviceToHost));
+  return CS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int cs_get_cycles(cs_ctx* ctx, uint32_t inst, cs_cycle* buf, size_t cap, size_t* n) {
+  if (!ctx || !ctx->ran || inst >= ctx->n_inst) return CS_E_INVALID_ARGUMENT;
+  const uint64_t c0 = ctx->cyc_off[inst], nc = ctx->cyc_off[inst + 1] - c0;
+  if (n) *n = nc;
+  if (!buf) return CS_OK;
+  if (cap < nc) return fail(ctx, CS_E_INVALID_ARGUMENT, "buffer too small");
+  std::vector<int64_t> st, en, ae;
+  std::vector<uint64_t> ap, fi, la;
+  std::vector<uint8_t> sg;
+  std::vector<int32_t> wl;
+  int rc;
+  if ((rc = d2h(ctx, st, ctx->c_start, c0, nc)) || (rc = d2h(ctx, en, ctx->c_end, c0, nc)) ||
+      (rc = d2h(ctx, ae, ctx->c_aend, c0, nc)) || (rc = d2h(ctx, ap, ctx->c_apos, c0, nc)) ||
+      (rc = d2h(ctx, fi, ctx->c_first, c0, nc)) || (rc = d2h(ctx, la, ctx->c_last, c0, nc)) ||
+      (rc = d2h(ctx, sg, ctx->c_stage, c0, nc)) || (rc = d2h(ctx, wl, ctx->c_wl, c0, nc)))
+    return rc;
+  const uint64_t ib = ctx->inst_off[inst];
+  for (uint64_t k = 0; k < nc; ++k) {
+    cs_cycle& c = buf[k];
+    c.index = k;
+    c.start_ts = st[k];
+    c.end_ts = en[k];
+    c.anchor_pos = ap[k] == UINT64_MAX ? UINT64_MAX : ap[k] - ib;
+    c.anchor_span_end = ae[k];
+    c.first_event = fi[k] - ib;
+    c.last_event = la[k] - ib;
+    c.stage = sg[k];
+    c.workload_status = wl[k] >= 0 ? 0 : (wl[k] == -1 ? 1 : 2);
+  }
+  return CS_OK;
+}
+
+int cs_get_components(cs_ctx* ctx, uint32_t inst, int64_t* buf, size_t cap, size_t* n) {
+  if (!ctx || !ctx->ran || inst >= ctx->n_inst) return CS_E_INVALID_ARGUMENT;
+  const uint64_t P = static_cast<uint64_t>(ctx->cyc.n_phases);
+  const uint64_t c0 = ctx->cyc_off[inst], nc = ctx->cyc_off[inst + 1] - c0;
+  if (n) *n = nc * P;
+  if (!buf) return CS_OK;
+  if (cap < nc * P) return fail(ctx, CS_E_INVALID_ARGUMENT, "buffer too small");
+  if (nc * P != 0)
+    CS_CUDA(cudaMemcpy(buf, static_cast<int64_t*>(ctx->c_comp.p) + c0 * P, nc * P * 8,
+                       cudaMemcpyDeviceToHost));
+  return CS_OK;
+}
+
+int cs_get_beta(cs_ctx* ctx, uint32_t inst, int64_t* totals, double* beta, size_t cap, size_t* n) {
+  if (!ctx || !ctx->ran || inst >= ctx->n_inst) return CS_E_INVALID_ARGUMENT;
+  if (!(ctx->last_mask & CS_RUN_BETA)) return fail(ctx, CS_E_INVALID_ARGUMENT, "beta not computed");
+  const uint64_t Cs = static_cast<uint64_t>(ctx->cyc.n_beta_slots);
+  const uint64_t c0 = ctx->cyc_off[inst], nc = ctx->cyc_off[inst + 1] - c0;
+  if (n) *n = nc * Cs;
+  if (cap < nc * Cs && (totals || beta)) return fail(ctx, CS_E_INVALID_ARGUMENT, "buffer too small");
+  if (totals && nc * Cs)
+    CS_CUDA(cudaMemcpy(totals, static_cast<int64_t*>(ctx->c_beta_tot.p) + c0 * Cs, nc * Cs * 8,
+                       cudaMemcpyDeviceToHost));
+  if (beta && nc * Cs)
+    CS_CUDA(cudaMemcpy(beta, static_cast<double*>(ctx->c_beta.p) + c0 * Cs, nc * Cs * 8,
+                       cudaMemcpyDeviceToHost));
+  return CS_OK;
+}
+
+int cs_get_collective_beta(cs_ctx* ctx, uint32_t inst, double* beta, uint8_t* present,
+                           size_t cap, size_t* n) {
+  if (!ctx || !ctx->ran || inst >= ctx->n_inst) return CS_E_INVALID_ARGUMENT;
+  if (!(ctx->last_mask & CS_RUN_BETA)) return fail(ctx, CS_E_INVALID_ARGUMENT, "beta not computed");
+  const uint64_t R = static_cast<uint64_t>(ctx->cyc.n_comm_slots);
+  const uint64_t c0 = ctx->cyc_off[inst], nc = ctx->cyc_off[inst + 1] - c0;
+  if (n) *n = nc * R;
+  if (cap < nc * R && (beta || present)) return fail(ctx, CS_E_INVALID_ARGUMENT, "buffer too small");
+  if (beta && nc * R)
+    CS_CUDA(cudaMemcpy(beta, static_cast<double*>(ctx->c_coll.p) + c0 * R, nc * R * 8,
+                       cudaMemcpyDeviceToHost));
+  if (present && nc * R) {
+    CS_CUDA(cudaMemcpy(present, static_cast<uint8_t*>(ctx->c_coll_n.p) + c0 * R, nc * R,
+                       cudaMemcpyDeviceToHost));
+    for (uint64_t k = 0; k < nc * R; ++k) present[k] = present[k] ? 1 : 0;
+  }
+  return CS_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+int gather_records(cs_ctx* ctx, uint32_t inst, uint64_t r0, uint64_t nr, cs_record* out) {
+  std::vector<uint64_t> rc;
+  std::vector<double> pr, re, stt;
+  std::vector<uint8_t> fl;
+  int rcode;
+  if ((rcode = d2h(ctx, rc, ctx->rec_cycle, r0, nr))) return rcode;
+  const bool scored = ctx->last_mask & (CS_RUN_SCORE | CS_RUN_DETECT);
+  const bool det = ctx->last_mask & CS_RUN_DETECT;
+  if (scored && ((rcode = d2h(ctx, pr, ctx->rec_pred, r0, nr)) ||
+                 (rcode = d2h(ctx, re, ctx->rec_resid, r0, nr))))
+    return rcode;
+  if (det && ((rcode = d2h(ctx, stt, ctx->rec_stat, r0, nr)) ||
+              (rcode = d2h(ctx, fl, ctx->rec_flags, r0, nr))))
+    return rcode;
+  const uint64_t c0 = ctx->cyc_off[inst], nc = ctx->cyc_off[inst + 1] - c0;
+  std::vector<int64_t> st, en, comp;
+  std::vector<uint8_t> sg;
+  std::vector<int32_t> wl;
+  if ((rcode = d2h(ctx, st, ctx->c_start, c0, nc)) || (rcode = d2h(ctx, en, ctx->c_end, c0, nc)) ||
+      (rcode = d2h(ctx, sg, ctx->c_stage, c0, nc)) || (rcode = d2h(ctx, wl, ctx->c_wl, c0, nc)))
+    return rcode;
+  const int P = ctx->cyc.n_phases, lat = ctx->cyc.latency_phase;
+  if (lat >= 0 && (rcode = d2h(ctx, comp, ctx->c_comp, c0 * P, nc * P))) return rcode;
+  std::vector<cs_workload> wls;
+  if ((rcode = d2h(ctx, wls, ctx->d_wl, 0, ctx->n_wl))) return rcode;
+  for (uint64_t k = 0; k < nr; ++k) {
+    const uint64_t c = rc[k] - c0;
+    cs_record& r = out[k];
+    std::memset(&r, 0, sizeof r);
+    r.cycle_index = c;
+    r.start_ts = st[c];
+    r.stage = sg[c];
+    const cs_workload& w = wls[wl[c]];
+    r.batch = w.batch;
+    r.input_len = w.input_len;
+    r.output_len = w.output_len;
+    int64_t target = en[c] - st[c];
+    if (lat >= 0 && comp[c * P + lat] > 0) target = comp[c * P + lat];
+    r.latency_s = static_cast<double>(target) * 1e-9;  // cycles.cpp:390
+    if (scored) {
+      r.predicted_s = pr[k];
+      r.residual = re[k];
+    }
+    if (det) {
+      r.statistic = stt[k];
+      r.armed = fl[k] & 1;
+      r.flagged = (fl[k] >> 1) & 1;
+      r.alert = (fl[k] >> 2) & 1;
+    }
+  }
+  return CS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int cs_get_records(cs_ctx* ctx, uint32_t inst, cs_record* buf, size_t cap, size_t* n) {
+  if (!ctx || !ctx->ran || inst >= ctx->n_inst) return CS_E_INVALID_ARGUMENT;
+  const uint64_t r0 = ctx->rec_off[inst], nr = ctx->rec_off[inst + 1] - r0;
+  if (n) *n = nr;
+  if (!buf) return CS_OK;
+  if (cap < nr) return fail(ctx, CS_E_INVALID_ARGUMENT, "buffer too small");
+  int rc = gather_records(ctx, inst, r0, nr, buf);
+  if (rc) return rc;
+  if (ctx->last_mask & CS_RUN_DETECT) {
+    // episode ids: running alert count within the instance
+    uint64_t ep = 0;
+    for (uint64_t k = 0; k < nr; ++k)
+      if (buf[k].alert) buf[k].episode_id = ep++;
+  }
+  return CS_OK;
+}
+
+int cs_get_alerts(cs_ctx* ctx, uint32_t inst, cs_alert* buf, size_t cap, size_t* n) {
+  if (!ctx || !ctx->ran || inst >= ctx->n_inst) return CS_E_INVALID_ARGUMENT;
+  if (!(ctx->last_mask & CS_RUN_DETECT)) return fail(ctx, CS_E_INVALID_ARGUMENT, "detect not run");
+  const uint64_t a0 = ctx->alert_off[inst], na_all = ctx->alert_off[inst + 1] - a0;
+  std::vector<uint64_t> ar;
+  int rc;
+  if ((rc = d2h(ctx, ar, ctx->alert_rec, a0, na_all))) return rc;
+  const uint64_t r0 = ctx->rec_off[inst];
+  const uint64_t bad = ctx->h_inst[inst].first_bad_record;
+  // monitor_loop stops at the first NonPositiveLatency (main.cpp:162)
+  uint64_t na = 0;
+  while (na < na_all && ar[na] - r0 < bad) ++na;
+  if (n) *n = na;
+  if (!buf) return CS_OK;
+  if (cap < na) return fail(ctx, CS_E_INVALID_ARGUMENT, "buffer too small");
+  for (uint64_t k = 0; k < na; ++k) {
+    cs_record r;
+    if ((rc = gather_records(ctx, inst, ar[k], 1, &r))) return rc;
+    cs_alert& a = buf[k];
+    std::memset(&a, 0, sizeof a);
+    a.cycle = r.cycle_index;
+    a.ts = r.start_ts;
+    a.smoothed_error = r.statistic;
+    a.limit = ctx->h_models[inst].ucl;
+    a.strategy = ctx->ctl.strategy;
+    a.batch = r.batch;
+    a.input_len = r.input_len;
+    a.output_len = r.output_len;
+    a.episode_id = k;
+    a.record_index = ar[k] - r0;
+  }
+  return CS_OK;
+}
+
+int cs_host_alloc(size_t bytes, void** out) {
+  if (!out) return CS_E_INVALID_ARGUMENT;
+  if (cudaHostAlloc(out, bytes, cudaHostAllocPortable) != cudaSuccess) {
+    cudaGetLastError();
+    return CS_E_NO_DEVICE;
+  }
+  return CS_OK;
+}
+
+int cs_host_free(void* p) {
+  if (p) cudaFreeHost(p);
+  return CS_OK;
+}
+
+int cs_get_timings(cs_ctx* ctx, double* ms, size_t cap, size_t* n, char* names, size_t names_cap) {
+  if (!ctx) return CS_E_INVALID_ARGUMENT;
+  if (n) *n = ctx->timed.size();
+  std::string all;
+  for (size_t k = 0; k < ctx->timed.size(); ++k) {
+    float t = 0.f;
+    cudaEventElapsedTime(&t, ctx->ev[ctx->timed[k].second.first], ctx->ev[ctx->timed[k].second.second]);
+    if (ms && k < cap) ms[k] = t;
+    if (k) all += ",";
+    all += ctx->timed[k].first;
+  }
+  if (names && names_cap) {
+    std::strncpy(names, all.c_str(), names_cap - 1);
+    names[names_cap - 1] = 0;
+  }
+  return CS_OK;
+}
+
+int cs_get_launch_count(cs_ctx* ctx, uint64_t* n) {
+  if (!ctx || !n) return CS_E_INVALID_ARGUMENT;
+  *n = ctx->launches;
+  return CS_OK;
+}
+
+double cs_ucl_from_stats(double mu, double sigma, const cs_control_config* cfg) {
+  return ucl_from_stats_host(mu, sigma, *cfg);
+}
+
+int cs_compute_ucl(const double* r, size_t n, double k, double theta_max, double min_ucl,
+                   size_t min_n, double* out) {
+  // detector.cpp:41-55, two-pass sample variance
+  if (n < min_n) return CS_E_INSUFFICIENT_CALIBRATION;
+  double mean = 0.0;
+  for (size_t i = 0; i < n; ++i) mean += r[i];
+  mean /= static_cast<double>(n);
+  double var = 0.0;
+  for (size_t i = 0; i < n; ++i) var += (r[i] - mean) * (r[i] - mean);
+  var /= static_cast<double>(n - 1);
+  *out = std::max(std::min(mean + k * std::sqrt(var), theta_max), min_ucl);
+  return CS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,158 @@
+// cs_internal.h — shared declarations between the host runtime (cs_api.cpp)
+// and the sm_100a kernels (cs_kernels.cu).  Not part of the public ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "cyclescope_b200.h"
+
+namespace csb {
+
+// ------------------------------------------------------------ tiling
+constexpr int kScanThreads = 256;               // 8 warps
+constexpr int kScanEvPerWarpIter = 32;
+constexpr int kScanIters = 16;                  // events per lane per tile
+constexpr int kTileEvents = kScanThreads * kScanIters;  // 4096 events = 128 KiB
+constexpr int kSmemNames = 1024;                // name stats staged in smem
+constexpr int kMaxPhases = 8;
+constexpr int kMaxBetaSlots = 64;
+constexpr int kMaxCommSlots = 64;
+constexpr int kMaxFeatures = 8;
+constexpr int kMaxTreeDepth = 8;
+constexpr uint64_t kSampleEvents = 1u << 20;    // anchor-guess sample per instance
+
+// name-stat accumulator (per instance x name); exact integer moments
+struct NameStat {
+  unsigned long long count;
+  unsigned long long sum;      // sum of durations, two's complement int64
+  unsigned long long sumsq_lo; // unsigned 128-bit sum of squares
+  unsigned long long sumsq_hi;
+  unsigned long long span_count;  // Spans of this name in any category
+  unsigned long long pad[3];
+};
+
+// per-instance device state
+struct InstState {
+  uint32_t guess;          // speculated anchor name id (UINT32_MAX none)
+  uint32_t anchor;         // final anchor name id (UINT32_MAX: none)
+  uint32_t redo;           // anchors compacted for a different name
+  uint32_t ambiguous;      // ranking needs the ordered fold
+  uint32_t no_anchor;      // NoAnchorFound
+  uint32_t n_candidates;
+  unsigned long long n_anchors;      // anchor occurrences compacted (for `anchor`)
+  unsigned long long n_unknown;      // cycles whose local stage is Unknown
+  unsigned long long first_bad_record;
+  unsigned long long n_records;
+  unsigned long long n_alerts;
+  unsigned long long bad_workload;   // reserved
+};
+
+// flattened model in complete-binary-tree layout (see pack_model)
+struct DevModel {
+  uint32_t n_trees;
+  uint32_t depth;          // padded depth D: 2^D-1 internal, 2^D leaves per tree
+  uint32_t n_features;
+  uint32_t degenerate;
+  int32_t feature_ids[kMaxFeatures];
+  double base, lr, floor_, mu, sigma, ucl;
+  // device pointers (SoA over trees): thr[t*(2^D-1)+n], feat[t*(2^D-1)+n],
+  // leaf[t*2^D+l]
+  const double* thr;
+  const uint8_t* feat;
+  const double* leaf;
+  uint64_t smem_bytes;     // bytes of thr+feat+leaf when staged
+};
+
+struct DevConfig {
+  cs_cycle_config cyc;
+  cs_control_config ctl;
+  double limit_unused;
+};
+
+// all device pointers of one run
+struct DevBuffers {
+  const cs_event* ev;
+  const cs_workload* wl;
+  const cs_name_info* names;
+  uint32_t n_names;
+  uint32_t n_inst;
+  const uint64_t* inst_off;     // n_inst+1 event offsets
+  // tiles over events (instance-aligned)
+  const uint32_t* tile_inst;
+  const uint64_t* tile_begin;   // n_tiles+1 (tile t = [begin[t], end[t]) )
+  const uint64_t* tile_end;
+  const uint32_t* inst_first_tile;
+  uint32_t n_tiles;
+  NameStat* stats;              // n_inst * n_names
+  InstState* inst;
+  unsigned long long* tile_state;
+  unsigned int* ticket;
+  // anchors (capacity = events; instance i at inst_off[i])
+  uint64_t* a_pos;
+  int64_t* a_start;
+  int64_t* a_end;
+  // cycles (instance i at cyc_off[i])
+  const uint64_t* cyc_off;      // n_inst+1
+  uint64_t n_cycles;
+  int64_t* c_start;
+  int64_t* c_end;
+  uint64_t* c_apos;
+  int64_t* c_aend;
+  uint64_t* c_first;
+  uint64_t* c_last;
+  uint32_t* c_inst;
+  uint8_t* c_stage;             // final stage
+  uint8_t* c_local;             // local (args/keyword) stage
+  int32_t* c_wl;                // workload index, -1 no carrier, -2 invalid carrier
+  int64_t* c_comp;              // n_cycles x n_phases
+  int64_t* c_beta_tot;          // n_cycles x n_beta
+  double* c_beta;               // n_cycles x n_beta
+  double* c_coll;               // n_cycles x n_comm
+  uint8_t* c_coll_n;            // contributions per (cycle, comm slot)
+  // records (instance i at rec_off[i], device-computed)
+  uint64_t* rec_off;            // n_inst+1
+  uint64_t* rec_cycle;          // record -> global cycle index
+  double* rec_pred;
+  double* rec_resid;
+  double* rec_stat;
+  uint8_t* rec_flags;           // bit0 armed, bit1 flagged, bit2 alert
+  uint64_t* alert_rec;          // alert -> record index
+  uint64_t* alert_off;          // n_inst+1
+  uint64_t* block_tmp;          // scratch for scans
+  const DevModel* models;       // per instance (device array)
+};
+
+// launchers (cs_kernels.cu); all asynchronous on `s`
+void launch_scan_events(const DevBuffers& b, const DevConfig& cfg, int mode, bool sample,
+                        cudaStream_t s, uint64_t* launches);
+void launch_rank(const DevBuffers& b, const DevConfig& cfg, int final_pass, cudaStream_t s,
+                 uint64_t* launches);
+void launch_fold(const DevBuffers& b, const DevConfig& cfg, const uint32_t* pairs_inst,
+                 const uint32_t* pairs_name, uint32_t n_pairs, double* out_scores,
+                 cudaStream_t s, uint64_t* launches);
+void launch_bounds(const DevBuffers& b, cudaStream_t s, uint64_t* launches);
+void launch_cycle_reduce(const DevBuffers& b, const DevConfig& cfg, int do_beta,
+                         cudaStream_t s, uint64_t* launches);
+void launch_stage_heuristic(const DevBuffers& b, const DevConfig& cfg, cudaStream_t s,
+                            uint64_t* launches);
+void launch_records(const DevBuffers& b, const DevConfig& cfg, uint64_t n_blocks_cap,
+                    cudaStream_t s, uint64_t* launches);
+void launch_score(const DevBuffers& b, const DevConfig& cfg, uint64_t n_records_total,
+                  const uint64_t* h_rec_off, const int* h_model_of_inst, const DevModel* h_models,
+                  cudaStream_t s, uint64_t* launches);
+void launch_detect(const DevBuffers& b, const DevConfig& cfg, uint64_t n_records_total,
+                   cudaStream_t s, uint64_t* launches);
+void launch_freq_hist(const cs_event* ev, uint64_t begin, uint64_t end, int64_t t0,
+                      int64_t bin_ns, uint64_t bins, double* hist, cudaStream_t s,
+                      uint64_t* launches);
+void launch_freq_autocorr(const double* hist, uint64_t bins, double* acc, cudaStream_t s,
+                          uint64_t* launches);
+void launch_gpu_kernel_extent(const cs_event* ev, uint64_t begin, uint64_t end,
+                              unsigned long long* out3, cudaStream_t s, uint64_t* launches);
+void launch_freq_cycles(const cs_event* ev, uint64_t begin, uint64_t end, int64_t t0,
+                        int64_t period, uint64_t n, uint64_t cyc_base, const DevBuffers& b,
+                        uint32_t inst, cudaStream_t s, uint64_t* launches);
+
+}  // namespace csb

@@ -1,0 +1,1219 @@
+// cs_kernels.cu — hand-written sm_100a kernels of the trace-analysis hot path.
+//
+// Data flow (one cs_run over a batch of instances):
+//   K1s  k_scan_events<sample>   name moments over the first 1 Mi events of each
+//                                instance -> speculative anchor guess
+//   K1r  k_rank                  exact-moment anchor ranking (cycles.cpp:47-110)
+//   K12  k_scan_events           ONE pass over all events: exact per-name moments
+//                                (cycles.cpp:50-59) + anchor-occurrence
+//                                compaction for the guessed anchor
+//                                (cycles.cpp:127-131) via decoupled look-back
+//   K1r  k_rank(final)           winner; redo flag when the guess was wrong
+//   K2   k_bounds                cycle bounds, lower_bound group starts
+//                                (cycles.cpp:135-156)
+//   K3   k_cycle_reduce          warp per cycle: component durations
+//                                (cycles.cpp:157-166), forward_mode / keyword
+//                                stage signals (205-229), workload carrier
+//                                (256-281), class occupancy beta and per-rank
+//                                collective beta (rca.cpp:71-130)
+//   K4   k_stage_heuristic       trailing-median heuristic for Unknown cycles
+//                                only (cycles.cpp:230-250), warp selection
+//   K5   k_records_*             record compaction (cycles.cpp:366-409)
+//   K6   k_score                 GBDT in shared memory + PPE (gbdt.cpp:22-30,
+//                                173-184; detector.cpp:14-19)
+//   K7   k_detect_*              control chart, episode ids, alert compaction
+//                                (detector.cpp:91-130)
+// All f64 arithmetic that must match the reference bit for bit is written with
+// explicit __dadd_rn/__dmul_rn/__ddiv_rn (the reference objects contain no FMA)
+// and the whole file is compiled with --fmad=false.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "cs_internal.h"
+
+namespace csb {
+
+using u64 = unsigned long long;
+using i64 = long long;
+
+constexpr u64 kFlagAgg = 1ull << 62;
+constexpr u64 kFlagPrefix = 2ull << 62;
+constexpr u64 kValMask = (1ull << 62) - 1;
+constexpr u64 kNone = ~0ull;
+
+// ------------------------------------------------------------ primitives
+__device__ __forceinline__ u64 ld_acquire(const u64* p) {
+  u64 v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(u64* p, u64 v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ u64 warp_sum_u64(u64 v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+struct Ev {
+  i64 start, dur;
+  uint32_t name;
+  uint32_t kind, cat, flags;
+  u64 payload;
+};
+
+// 32-byte record as two 16-byte vector loads; streaming (evict-first) since
+// every event is read exactly once per pass.
+__device__ __forceinline__ Ev load_ev_stream(const cs_event* p) {
+  const int4* q = reinterpret_cast<const int4*>(p);
+  int4 a = __ldcs(q);
+  int4 b = __ldcs(q + 1);
+  Ev e;
+  e.start = (i64)(((u64)(uint32_t)a.y << 32) | (uint32_t)a.x);
+  e.dur = (i64)(((u64)(uint32_t)a.w << 32) | (uint32_t)a.z);
+  e.name = (uint32_t)b.x;
+  e.kind = (uint32_t)b.y & 0xffu;
+  e.cat = ((uint32_t)b.y >> 8) & 0xffu;
+  e.flags = (uint32_t)b.y >> 16;
+  e.payload = ((u64)(uint32_t)b.w << 32) | (uint32_t)b.z;
+  return e;
+}
+__device__ __forceinline__ Ev load_ev(const cs_event* p) {
+  const int4* q = reinterpret_cast<const int4*>(p);
+  int4 a = __ldg(q);
+  int4 b = __ldg(q + 1);
+  Ev e;
+  e.start = (i64)(((u64)(uint32_t)a.y << 32) | (uint32_t)a.x);
+  e.dur = (i64)(((u64)(uint32_t)a.w << 32) | (uint32_t)a.z);
+  e.name = (uint32_t)b.x;
+  e.kind = (uint32_t)b.y & 0xffu;
+  e.cat = ((uint32_t)b.y >> 8) & 0xffu;
+  e.flags = (uint32_t)b.y >> 16;
+  e.payload = ((u64)(uint32_t)b.w << 32) | (uint32_t)b.z;
+  return e;
+}
+
+// 128-bit accumulate of d*d (d as signed int64) into (lo, hi) with atomics.
+__device__ __forceinline__ void atomic_add_u128(u64* lo, u64* hi, u64 add_lo, u64 add_hi) {
+  u64 old = atomicAdd(lo, add_lo);
+  u64 carry = (old + add_lo < old) ? 1ull : 0ull;
+  if (add_hi + carry) atomicAdd(hi, add_hi + carry);
+}
+__device__ __forceinline__ void square_u128(i64 d, u64& lo, u64& hi) {
+  u64 a = (u64)(d < 0 ? -d : d);
+  lo = a * a;
+  hi = __umul64hi(a, a);
+}
+
+// warp-parallel decoupled look-back (Merrill & Garland) over one instance's
+// tiles; returns the exclusive prefix.  Must be called by a full warp.
+__device__ u64 lookback_warp(u64* state, uint32_t tile, uint32_t first_tile, u64 agg) {
+  const int lane = threadIdx.x & 31;
+  if (tile == first_tile) {
+    if (lane == 0) st_release(&state[tile], kFlagPrefix | agg);
+    return 0;
+  }
+  if (lane == 0) st_release(&state[tile], kFlagAgg | agg);
+  u64 excl = 0;
+  i64 j = (i64)tile - 1 - lane;
+  while (true) {
+    const bool in = j >= (i64)first_tile;
+    u64 s = 0;
+    if (in) {
+      do {
+        s = ld_acquire(&state[j]);
+      } while ((s >> 62) == 0);
+    }
+    const uint32_t pmask = __ballot_sync(0xffffffffu, !in || (s >> 62) == 2);
+    const int stop = pmask ? __ffs(pmask) - 1 : 32;
+    u64 v = (in && lane <= stop) ? (s & kValMask) : 0;
+    excl += warp_sum_u64(v);
+    if (pmask) break;
+    j -= 32;
+  }
+  if (lane == 0) st_release(&state[tile], kFlagPrefix | (excl + agg));
+  return excl;
+}
+
+// --------------------------------------------------- K1 / K12 event scan
+// mode bit 0: name moments; bit 1: anchor compaction for inst[].guess
+// (or inst[].anchor when bit 2 "redo" is set: only instances with redo).
+__global__ void __launch_bounds__(kScanThreads)
+    k_scan_events(DevBuffers b, int mode, int sample) {
+  __shared__ uint32_t s_cnt[kSmemNames];
+  __shared__ uint32_t s_spn[kSmemNames];
+  __shared__ u64 s_sum[kSmemNames];
+  __shared__ u64 s_sq_lo[kSmemNames];
+  __shared__ u64 s_sq_hi[kSmemNames];
+  __shared__ uint32_t s_tile;
+  __shared__ uint32_t s_warp_cnt[kScanThreads / 32];
+  __shared__ u64 s_excl;
+
+  const bool do_stats = mode & 1;
+  const bool do_anchor = (mode & 2) && !sample;
+  const bool redo = mode & 4;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+
+  if (threadIdx.x == 0) s_tile = do_anchor ? atomicAdd(b.ticket, 1u) : blockIdx.x;
+  const uint32_t nn = b.n_names < (uint32_t)kSmemNames ? b.n_names : (uint32_t)kSmemNames;
+  if (do_stats)
+    for (uint32_t i = threadIdx.x; i < nn; i += blockDim.x) {
+      s_cnt[i] = 0;
+      s_spn[i] = 0;
+      s_sum[i] = 0;
+      s_sq_lo[i] = 0;
+      s_sq_hi[i] = 0;
+    }
+  __syncthreads();
+  const uint32_t tile = s_tile;
+  if (tile >= b.n_tiles) return;
+  const uint32_t inst = b.tile_inst[tile];
+  const u64 tb = b.tile_begin[tile], te = b.tile_end[tile];
+  const u64 ib = b.inst_off[inst];
+  if (sample && tb >= ib + kSampleEvents) return;
+  const u64 se = sample ? min(te, ib + kSampleEvents) : te;
+
+  uint32_t anchor = 0xffffffffu;
+  bool inst_active = do_anchor;
+  if (do_anchor) {
+    const InstState& st = b.inst[inst];
+    anchor = redo ? st.anchor : st.guess;
+    if (redo && !st.redo) inst_active = false;
+  }
+  NameStat* gstats = b.stats + (u64)inst * b.n_names;
+
+  uint32_t masks[kScanIters];
+  uint32_t my_count = 0;
+#pragma unroll
+  for (int k = 0; k < kScanIters; ++k) {
+    const u64 j = tb + (u64)warp * (kScanIters * 32) + (u64)k * 32 + lane;
+    const bool valid = j < se;
+    bool is_anchor = false;
+    if (valid) {
+      const Ev e = load_ev_stream(b.ev + j);
+      const bool span = e.kind == CS_SPAN;
+      if (do_stats && span) {
+        const bool py = e.cat == CS_CAT_PYTHON_CALL;
+        u64 lo = 0, hi = 0;
+        if (py) square_u128(e.dur, lo, hi);
+        if (e.name < nn) {
+          atomicAdd(&s_spn[e.name], 1u);
+          if (py) {
+            atomicAdd(&s_cnt[e.name], 1u);
+            atomicAdd(&s_sum[e.name], (u64)e.dur);
+            atomic_add_u128(&s_sq_lo[e.name], &s_sq_hi[e.name], lo, hi);
+          }
+        } else {
+          NameStat* g = gstats + e.name;
+          atomicAdd(&g->span_count, 1ull);
+          if (py) {
+            atomicAdd(&g->count, 1ull);
+            atomicAdd(&g->sum, (u64)e.dur);
+            atomic_add_u128(&g->sumsq_lo, &g->sumsq_hi, lo, hi);
+          }
+        }
+      }
+      is_anchor = inst_active && span && e.name == anchor;
+    }
+    masks[k] = __ballot_sync(0xffffffffu, is_anchor);
+    my_count += __popc(masks[k]);
+  }
+
+  if (do_anchor) {
+    if (lane == 0) s_warp_cnt[warp] = my_count;
+    __syncthreads();
+    if (warp == 0) {
+      uint32_t c = lane < kScanThreads / 32 ? s_warp_cnt[lane] : 0;
+      // inclusive scan over 8 warp counts
+      for (int o = 1; o < 8; o <<= 1) {
+        uint32_t n = __shfl_up_sync(0xffffffffu, c, o);
+        if (lane >= o) c += n;
+      }
+      const uint32_t total = __shfl_sync(0xffffffffu, c, 7);
+      if (lane < kScanThreads / 32) s_warp_cnt[lane] = c - (lane < 8 ? s_warp_cnt[lane] : 0);
+      const u64 excl = lookback_warp(b.tile_state, tile, b.inst_first_tile[inst], total);
+      if (lane == 0) {
+        s_excl = excl;
+        // last tile of the instance publishes the occurrence count
+        if (inst_active && (tile + 1 == b.n_tiles || b.tile_inst[tile + 1] != inst))
+          b.inst[inst].n_anchors = excl + total;
+      }
+    }
+    __syncthreads();
+    u64 rank = s_excl + s_warp_cnt[warp];
+#pragma unroll
+    for (int k = 0; k < kScanIters; ++k) {
+      const uint32_t m = masks[k];
+      if (m) {
+        if (m & (1u << lane)) {
+          const u64 j = tb + (u64)warp * (kScanIters * 32) + (u64)k * 32 + lane;
+          const u64 r = ib + rank + __popc(m & lanemask_lt());
+          const cs_event* p = b.ev + j;
+          const i64 st = p->start_ts;
+          b.a_pos[r] = j;
+          b.a_start[r] = st;
+          b.a_end[r] = st + p->duration;
+        }
+        rank += __popc(m);
+      }
+    }
+  }
+
+  if (do_stats) {
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < nn; i += blockDim.x) {
+      if (s_spn[i]) {
+        NameStat* g = gstats + i;
+        atomicAdd(&g->span_count, (u64)s_spn[i]);
+        if (s_cnt[i]) {
+          atomicAdd(&g->count, (u64)s_cnt[i]);
+          atomicAdd(&g->sum, s_sum[i]);
+          atomic_add_u128(&g->sumsq_lo, &g->sumsq_hi, s_sq_lo[i], s_sq_hi[i]);
+        }
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------ K1r rank
+// One warp per instance.  score = count / (1 + cv) computed from exact
+// moments; an interval bound on the reference's sequentially rounded
+// sum_sq (|err| <= n*u*sum_sq) certifies the winner, otherwise the host runs
+// the ordered fold (k_fold).  Ties break by name (name id == lex rank).
+struct Cand {
+  double score, lo, hi;
+  uint32_t name;
+};
+
+__device__ __forceinline__ double u128_to_double(u64 lo, u64 hi) {
+  return __dadd_rn(__dmul_rn((double)hi, 18446744073709551616.0), (double)lo);
+}
+
+__device__ void score_from_moments(u64 count, i64 sum, double sumsq, double& mean, double& cv,
+                                   double& score) {
+  const double n = (double)count;
+  mean = __ddiv_rn((double)sum, n);
+  cv = 0.0;
+  if (mean > 0.0) {
+    double var = __dsub_rn(__ddiv_rn(sumsq, n), __dmul_rn(mean, mean));
+    var = 0.0 < var ? var : 0.0;
+    cv = __ddiv_rn(sqrt(var), mean);
+  }
+  score = __ddiv_rn(n, __dadd_rn(1.0, cv));
+}
+
+__global__ void k_rank(DevBuffers b, DevConfig cfg, int final_pass) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t inst = blockIdx.x;
+  if (inst >= b.n_inst) return;
+  InstState& st = b.inst[inst];
+  const NameStat* gs = b.stats + (u64)inst * b.n_names;
+  const u64 min_calls = cfg.cyc.min_anchor_calls;
+  const i64 hint = cfg.cyc.anchor_hint_name;
+
+  Cand best{-1.0, 0, 0, 0xffffffffu};
+  uint32_t ncand = 0;
+  bool inexact = false;
+  for (uint32_t n = lane; n < b.n_names; n += 32) {
+    const NameStat s = gs[n];
+    if (s.count < min_calls || s.count == 0) continue;
+    ++ncand;
+    const i64 sum = (i64)s.sum;
+    const bool sum_exact = (sum < (1ll << 53)) && (sum > -(1ll << 53));
+    const double S = u128_to_double(s.sumsq_lo, s.sumsq_hi);
+    const double u = 1.1102230246251565e-16;
+    const double gamma = (double)(s.count + 2) * u;
+    double m, cv, sc, sc_lo, sc_hi;
+    score_from_moments(s.count, sum, S, m, cv, sc);
+    {
+      double m2, cv2;
+      // larger sum_sq -> larger var -> smaller score
+      score_from_moments(s.count, sum, S * (1.0 + gamma), m2, cv2, sc_lo);
+      score_from_moments(s.count, sum, S * (1.0 - gamma), m2, cv2, sc_hi);
+      // cancellation guard on var = E[d^2] - mean^2: absolute slack
+      const double mean2 = m * m;
+      const double slack = 8.0 * u * (S / (double)s.count + mean2);
+      if (m > 0.0) {
+        const double n = (double)s.count;
+        const double vlo = fmax(0.0, S * (1.0 - gamma) / n - mean2 - slack);
+        const double vhi = fmax(0.0, S * (1.0 + gamma) / n - mean2 + slack);
+        sc_hi = fmax(sc_hi, n / (1.0 + sqrt(vlo) / m));
+        sc_lo = fmin(sc_lo, n / (1.0 + sqrt(vhi) / m));
+      }
+      sc_lo *= (1.0 - 16 * u);
+      sc_hi *= (1.0 + 16 * u);
+    }
+    if (!sum_exact) inexact = true;
+    if (sc > best.score || (sc == best.score && n < best.name)) best = Cand{sc, sc_lo, sc_hi, n};
+  }
+  // warp argmax (score desc, name asc)
+  for (int o = 16; o > 0; o >>= 1) {
+    Cand c;
+    c.score = __shfl_xor_sync(0xffffffffu, best.score, o);
+    c.lo = __shfl_xor_sync(0xffffffffu, best.lo, o);
+    c.hi = __shfl_xor_sync(0xffffffffu, best.hi, o);
+    c.name = __shfl_xor_sync(0xffffffffu, best.name, o);
+    if (c.score > best.score || (c.score == best.score && c.name < best.name)) best = c;
+  }
+  for (int o = 16; o > 0; o >>= 1) ncand += __shfl_xor_sync(0xffffffffu, ncand, o);
+  inexact = __any_sync(0xffffffffu, inexact);
+  // ambiguity: any other candidate whose interval reaches the winner's
+  bool amb = false;
+  if (best.name != 0xffffffffu) {
+    for (uint32_t n = lane; n < b.n_names; n += 32) {
+      if (n == best.name) continue;
+      const NameStat s = gs[n];
+      if (s.count < min_calls || s.count == 0) continue;
+      const i64 sum = (i64)s.sum;
+      const double S = u128_to_double(s.sumsq_lo, s.sumsq_hi);
+      const double u = 1.1102230246251565e-16;
+      const double gamma = (double)(s.count + 2) * u;
+      double m, cv, sc_hi;
+      score_from_moments(s.count, sum, S * (1.0 - gamma), m, cv, sc_hi);
+      if (m > 0.0) {
+        const double nd = (double)s.count;
+        const double slack = 8.0 * u * (S / nd + m * m);
+        const double vlo = fmax(0.0, S * (1.0 - gamma) / nd - m * m - slack);
+        sc_hi = fmax(sc_hi, nd / (1.0 + sqrt(vlo) / m));
+      }
+      sc_hi *= (1.0 + 16 * u);
+      if (sc_hi >= best.lo) amb = true;
+    }
+  }
+  amb = __any_sync(0xffffffffu, amb) || inexact;
+
+  if (lane == 0) {
+    uint32_t winner = best.name;
+    if (hint >= 0) {
+      // discover_anchor with a hint (cycles.cpp:90-104): the hint wins when it
+      // occurs as any Span at all
+      winner = gs[hint].span_count > 0 ? (uint32_t)hint : 0xffffffffu;
+      amb = false;
+    } else if (hint == -2) {
+      winner = 0xffffffffu;
+      amb = false;
+    }
+    if (!final_pass) {
+      st.guess = winner;
+    } else {
+      st.anchor = winner;
+      st.ambiguous = amb ? 1u : 0u;
+      st.no_anchor = winner == 0xffffffffu ? 1u : 0u;
+      st.redo = (winner != 0xffffffffu && winner != st.guess) ? 1u : 0u;
+      st.n_candidates = ncand;
+    }
+  }
+}
+
+// Ordered fold: the reference's own sequential arithmetic for one
+// (instance, name): count, sum += d, sum_sq += d*d in event order
+// (cycles.cpp:50-59), then mean/cv/score (66-77).  One thread per pair; only
+// launched when k_rank cannot certify the winner.
+__global__ void k_fold(DevBuffers b, const uint32_t* pairs_inst, const uint32_t* pairs_name,
+                       uint32_t n_pairs, double* out) {
+  const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n_pairs) return;
+  const uint32_t inst = pairs_inst[p], name = pairs_name[p];
+  u64 count = 0;
+  double sum = 0.0, sum_sq = 0.0;
+  for (u64 j = b.inst_off[inst]; j < b.inst_off[inst + 1]; ++j) {
+    const cs_event* e = b.ev + j;
+    if (e->kind != CS_SPAN || e->category != CS_CAT_PYTHON_CALL || e->name_id != name) continue;
+    ++count;
+    const double d = (double)e->duration;
+    sum = __dadd_rn(sum, d);
+    sum_sq = __dadd_rn(sum_sq, __dmul_rn(d, d));
+  }
+  const double n = (double)count;
+  const double mean = __ddiv_rn(sum, n);
+  double cv = 0.0;
+  if (mean > 0.0) {
+    double var = __dsub_rn(__ddiv_rn(sum_sq, n), __dmul_rn(mean, mean));
+    var = 0.0 < var ? var : 0.0;
+    cv = __ddiv_rn(sqrt(var), mean);
+  }
+  out[3 * p + 0] = mean;
+  out[3 * p + 1] = cv;
+  out[3 * p + 2] = __ddiv_rn(n, __dadd_rn(1.0, cv));
+}
+
+// ------------------------------------------------------------ K2 bounds
+__device__ __forceinline__ uint32_t upper_bound_u64(const uint64_t* a, uint32_t n, u64 v) {
+  uint32_t lo = 0, hi = n;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (a[mid] <= v) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+// lower_bound(events, ts) restricted to the instance, starting from a known
+// position with start_ts == ts (cycles.cpp:137-144): walk back over equal keys.
+__device__ __forceinline__ u64 group_start(const cs_event* ev, u64 pos, u64 begin, i64 ts) {
+  while (pos > begin && ev[pos - 1].start_ts == ts) --pos;
+  return pos;
+}
+
+__global__ void k_bounds(DevBuffers b) {
+  const u64 g = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= b.n_cycles) return;
+  const uint32_t inst = upper_bound_u64(b.cyc_off, b.n_inst + 1, g) - 1;
+  if (b.inst[inst].no_anchor) return;  // frequency-fallback cycles: k_freq_cycles
+  const u64 c = g - b.cyc_off[inst];
+  const u64 base = b.inst_off[inst];
+  const u64 ib = b.inst_off[inst];
+  const i64 s = b.a_start[base + c], e = b.a_start[base + c + 1];
+  const u64 p0 = b.a_pos[base + c], p1 = b.a_pos[base + c + 1];
+  b.c_start[g] = s;
+  b.c_end[g] = e;
+  b.c_apos[g] = p0;
+  b.c_aend[g] = b.a_end[base + c];
+  b.c_first[g] = group_start(b.ev, p0, ib, s);
+  b.c_last[g] = group_start(b.ev, p1, ib, e);
+  b.c_inst[g] = inst;
+}
+
+// ------------------------------------------------------ K3 cycle reduce
+constexpr int kReduceWarps = 8;
+struct WarpScratch {
+  i64 comp[kMaxPhases];
+  i64 beta[kMaxBetaSlots];
+  double coll[kMaxCommSlots];
+  uint32_t colln[kMaxCommSlots];
+};
+
+__global__ void __launch_bounds__(kReduceWarps * 32)
+    k_cycle_reduce(DevBuffers b, DevConfig cfg, int do_beta) {
+  __shared__ WarpScratch s_ws[kReduceWarps];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  WarpScratch& ws = s_ws[warp];
+  const int P = cfg.cyc.n_phases, C = cfg.cyc.n_beta_slots, R = cfg.cyc.n_comm_slots;
+  const int lat = cfg.cyc.latency_phase;
+  const u64 n_warps = (u64)gridDim.x * kReduceWarps;
+
+  for (u64 g = (u64)blockIdx.x * kReduceWarps + warp; g < b.n_cycles; g += n_warps) {
+    const i64 cs = b.c_start[g], ce = b.c_end[g];
+    const u64 first = b.c_first[g], last = b.c_last[g];
+    const i64 dur = ce - cs;
+    // frequency-fallback cycles carry no component map (cycles.cpp:332-340)
+    const bool no_comp = b.c_apos[g] == kNone;
+    for (int i = lane; i < kMaxPhases; i += 32) ws.comp[i] = 0;
+    if (do_beta) {
+      for (int i = lane; i < C; i += 32) ws.beta[i] = 0;
+      for (int i = lane; i < R; i += 32) {
+        ws.coll[i] = 0.0;
+        ws.colln[i] = 0;
+      }
+    }
+    __syncwarp();
+    uint32_t fm_cls = 0;
+    bool fm_found = false, pkw = false, dkw = false, batch_found = false;
+    int32_t wl = -1;
+    for (u64 base = first; base < last; base += 32) {
+      const u64 j = base + lane;
+      const bool valid = j < last;
+      Ev e{};
+      cs_name_info ni{0, -1, -1, 0};
+      if (valid) {
+        e = load_ev_stream(b.ev + j);
+        ni = b.names[e.name];
+      }
+      const bool span = valid && e.kind == CS_SPAN;
+      const i64 clipped = (e.start + e.dur < ce ? e.start + e.dur : ce) - e.start;
+      if (span && !no_comp && ni.phase >= 0 && clipped > 0)
+        atomicAdd(reinterpret_cast<u64*>(&ws.comp[ni.phase]), (u64)clipped);
+      if (do_beta) {
+        const bool occ = span && e.dur > 0 && clipped > 0;
+        if (occ && ni.beta_slot >= 0)
+          atomicAdd(reinterpret_cast<u64*>(&ws.beta[ni.beta_slot]), (u64)clipped);
+        // per-(name, commHash, rank) beta: doubles summed in event order
+        // (rca.cpp:108-115) -> sequential fold by lane 0 in lane order
+        uint32_t m = __ballot_sync(0xffffffffu, occ && e.cat == CS_CAT_COLLECTIVE_COMM &&
+                                                    (e.flags & CS_EV_HAS_COMM));
+        while (m) {
+          const int l = __ffs(m) - 1;
+          m &= m - 1;
+          const uint32_t slot = __shfl_sync(0xffffffffu, (uint32_t)(e.payload >> 32), l);
+          const i64 ov = __shfl_sync(0xffffffffu, clipped, l);
+          if (lane == 0 && slot < (uint32_t)R) {
+            ws.coll[slot] = __dadd_rn(ws.coll[slot], __ddiv_rn((double)ov, (double)dur));
+            ws.colln[slot] += 1;
+          }
+        }
+      }
+      if (!fm_found) {
+        const uint32_t m = __ballot_sync(0xffffffffu, valid && (e.flags & CS_EV_FM_MASK));
+        if (m) {
+          fm_found = true;
+          fm_cls = __shfl_sync(0xffffffffu, e.flags & CS_EV_FM_MASK, __ffs(m) - 1);
+        }
+      }
+      pkw |= __any_sync(0xffffffffu, span && (ni.flags & CS_NAME_PREFILL_KW));
+      dkw |= __any_sync(0xffffffffu, span && (ni.flags & CS_NAME_DECODE_KW));
+      if (!batch_found) {
+        const uint32_t m = __ballot_sync(0xffffffffu, valid && (e.flags & CS_EV_HAS_BATCH));
+        if (m) {
+          batch_found = true;
+          const int l = __ffs(m) - 1;
+          const uint32_t ok = __shfl_sync(0xffffffffu, e.flags & CS_EV_WL_OK, l);
+          const uint32_t idx = __shfl_sync(0xffffffffu, (uint32_t)(e.payload & 0xffffffffu), l);
+          wl = ok ? (int32_t)idx : -2;
+        }
+      }
+    }
+    __syncwarp();
+    // classify_stages local signals (cycles.cpp:205-229)
+    uint8_t stage = CS_STAGE_UNKNOWN;
+    if (fm_cls == CS_EV_FM_PREFILL) stage = CS_STAGE_PREFILL;
+    else if (fm_cls == CS_EV_FM_DECODE) stage = CS_STAGE_DECODE;
+    if (stage == CS_STAGE_UNKNOWN && pkw != dkw) stage = pkw ? CS_STAGE_PREFILL : CS_STAGE_DECODE;
+    if (lane == 0) {
+      b.c_local[g] = stage;
+      b.c_stage[g] = stage;
+      b.c_wl[g] = wl;
+      if (stage == CS_STAGE_UNKNOWN) atomicAdd(&b.inst[b.c_inst[g]].n_unknown, 1ull);
+    }
+    if (lane < P) b.c_comp[g * P + lane] = ws.comp[lane];
+    (void)lat;
+    if (do_beta) {
+      for (int i = lane; i < C; i += 32) {
+        const i64 t = dur > 0 ? ws.beta[i] : 0;
+        b.c_beta_tot[g * C + i] = t;
+        b.c_beta[g * C + i] = t > 0 ? __ddiv_rn((double)t, (double)dur) : 0.0;
+      }
+      for (int i = lane; i < R; i += 32) {
+        b.c_coll[g * R + i] = ws.coll[i];
+        b.c_coll_n[g * R + i] = (uint8_t)(ws.colln[i] > 255 ? 255 : ws.colln[i]);
+      }
+    }
+    __syncwarp();
+  }
+}
+
+// --------------------------------------------------- K4 stage heuristic
+// One warp per instance; only Unknown cycles are decided, in order
+// (cycles.cpp:230-250).  For each, the trailing windows (<= 32 most recent
+// non-Prefill durations; <= 32 most recent non-Prefill idle gaps >= 0) are
+// gathered by a backward ballot scan over already-final stages, and the
+// medians come from a 32-lane rank selection.
+__device__ double warp_median(double v, bool has, int n) {
+  // rank of each lane's value among valid lanes (stable on ties)
+  const int lane = threadIdx.x & 31;
+  int rank = 0;
+  for (int l = 0; l < 32; ++l) {
+    const double o = __shfl_sync(0xffffffffu, v, l);
+    const bool oh = __shfl_sync(0xffffffffu, has, l);
+    if (has && oh && (o < v || (o == v && l < lane))) ++rank;
+  }
+  const int want_hi = n / 2;
+  const uint32_t mhi = __ballot_sync(0xffffffffu, has && rank == want_hi);
+  const double hi = __shfl_sync(0xffffffffu, v, __ffs(mhi) - 1);
+  if (n % 2 == 1) return hi;
+  const uint32_t mlo = __ballot_sync(0xffffffffu, has && rank == want_hi - 1);
+  const double lo = __shfl_sync(0xffffffffu, v, __ffs(mlo) - 1);
+  return __dmul_rn(0.5, __dadd_rn(lo, hi));
+}
+
+__global__ void k_stage_heuristic(DevBuffers b, DevConfig cfg) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t inst = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  if (inst >= b.n_inst) return;
+  if (b.inst[inst].n_unknown == 0) return;
+  const u64 c0 = b.cyc_off[inst], c1 = b.cyc_off[inst + 1];
+  const int W = (int)cfg.cyc.stage_window;
+  const u64 min_hist = cfg.cyc.stage_min_history;
+  for (u64 base = c0; base < c1; base += 32) {
+    const u64 g = base + lane;
+    uint32_t um = __ballot_sync(0xffffffffu, g < c1 && b.c_local[g] == CS_STAGE_UNKNOWN);
+    while (um) {
+      const int l = __ffs(um) - 1;
+      um &= um - 1;
+      const u64 u = base + l;
+      const double gap =
+          u > c0 ? (double)(b.c_start[u] - b.c_aend[u - 1]) : -1.0;
+      uint8_t stage = CS_STAGE_UNKNOWN;
+      if (gap >= 0.0) {
+        // gather windows, most recent first
+        double dv = 0.0, gv = 0.0;
+        bool dh = false, gh = false;
+        int nd = 0, ng = 0;
+        for (i64 top = (i64)u - 1; top >= (i64)c0 && (nd < W || ng < W); top -= 32) {
+          const i64 j = top - lane;
+          const bool in = j >= (i64)c0;
+          bool nonp = false, gok = false;
+          double jd = 0.0, jg = -1.0;
+          if (in) {
+            nonp = b.c_stage[j] != CS_STAGE_PREFILL;
+            jd = (double)(b.c_end[j] - b.c_start[j]);
+            jg = j > (i64)c0 ? (double)(b.c_start[j] - b.c_aend[j - 1]) : -1.0;
+            gok = nonp && jg >= 0.0;
+          }
+          const uint32_t md = __ballot_sync(0xffffffffu, in && nonp);
+          const uint32_t mg = __ballot_sync(0xffffffffu, in && gok);
+          // k-th collected value goes to lane (nd + k)
+          const int kd = __popc(md & lanemask_lt());
+          const int kg = __popc(mg & lanemask_lt());
+          for (int src = 0; src < 32; ++src) {
+            const double sd = __shfl_sync(0xffffffffu, jd, src);
+            const double sg = __shfl_sync(0xffffffffu, jg, src);
+            const int skd = __shfl_sync(0xffffffffu, kd, src);
+            const int skg = __shfl_sync(0xffffffffu, kg, src);
+            if ((md >> src) & 1u) {
+              const int slot = nd + skd;
+              if (slot < W && slot == lane) { dv = sd; dh = true; }
+            }
+            if ((mg >> src) & 1u) {
+              const int slot = ng + skg;
+              if (slot < W && slot == lane) { gv = sg; gh = true; }
+            }
+          }
+          nd = min(W, nd + __popc(md));
+          ng = min(W, ng + __popc(mg));
+        }
+        if ((u64)nd >= min_hist) {
+          const double med_dur = warp_median(dv, dh, nd);
+          double med_gap = ng > 0 ? warp_median(gv, gh, ng) : 0.0;
+          med_gap = 1.0 < med_gap ? med_gap : 1.0;
+          const double cdur = (double)(b.c_end[u] - b.c_start[u]);
+          const bool long_cycle = cdur > __dmul_rn(cfg.cyc.prefill_duration_factor, med_dur);
+          const bool long_gap = gap > __dmul_rn(cfg.cyc.prefill_gap_factor, med_gap);
+          stage = (long_cycle && long_gap) ? CS_STAGE_PREFILL : CS_STAGE_DECODE;
+        }
+      }
+      if (lane == 0) b.c_stage[u] = stage;
+      __syncwarp();
+      __threadfence_block();
+    }
+  }
+}
+
+// ------------------------------------------------------------ K5 records
+// record := cycle with (include_prefill || stage != Prefill) && workload ok
+// (cycles.cpp:372-383).  Global compaction in cycle order; instance i's
+// records are contiguous and start at rec_off[i].
+constexpr int kRecBlock = 1024;
+
+__global__ void k_records_count(DevBuffers b, DevConfig cfg) {
+  __shared__ uint32_t s_w[32];
+  const u64 g = (u64)blockIdx.x * kRecBlock + threadIdx.x;
+  bool ok = false;
+  if (g < b.n_cycles)
+    ok = b.c_wl[g] >= 0 && (cfg.cyc.include_prefill || b.c_stage[g] != CS_STAGE_PREFILL);
+  const uint32_t m = __ballot_sync(0xffffffffu, ok);
+  if ((threadIdx.x & 31) == 0) s_w[threadIdx.x >> 5] = __popc(m);
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    u64 v = s_w[threadIdx.x];
+    v = warp_sum_u64(v);
+    if (threadIdx.x == 0) b.block_tmp[blockIdx.x] = v;
+  }
+}
+
+// single-CTA exclusive scan of n u64 values in place; total to *total
+__global__ void k_scan_exclusive(uint64_t* v, uint64_t n, uint64_t* total) {
+  __shared__ u64 s_part[32];
+  __shared__ u64 s_carry;
+  if (threadIdx.x == 0) s_carry = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (u64 base = 0; base < n; base += blockDim.x) {
+    const u64 i = base + threadIdx.x;
+    u64 x = i < n ? v[i] : 0;
+    u64 incl = x;
+    for (int o = 1; o < 32; o <<= 1) {
+      const u64 y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) s_part[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+      u64 p = lane < (int)(blockDim.x / 32) ? s_part[lane] : 0;
+      for (int o = 1; o < 32; o <<= 1) {
+        const u64 y = __shfl_up_sync(0xffffffffu, p, o);
+        if (lane >= o) p += y;
+      }
+      s_part[lane] = p;
+    }
+    __syncthreads();
+    const u64 warp_base = warp ? s_part[warp - 1] : 0;
+    if (i < n) v[i] = s_carry + warp_base + incl - x;
+    __syncthreads();
+    if (threadIdx.x == 0) s_carry += s_part[blockDim.x / 32 - 1];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0 && total) *total = s_carry;
+}
+
+__global__ void k_records_scatter(DevBuffers b, DevConfig cfg) {
+  __shared__ uint32_t s_w[32];
+  const u64 g = (u64)blockIdx.x * kRecBlock + threadIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  bool ok = false;
+  if (g < b.n_cycles)
+    ok = b.c_wl[g] >= 0 && (cfg.cyc.include_prefill || b.c_stage[g] != CS_STAGE_PREFILL);
+  const uint32_t m = __ballot_sync(0xffffffffu, ok);
+  if (lane == 0) s_w[warp] = __popc(m);
+  __syncthreads();
+  if (warp == 0) {
+    uint32_t c = lane < kRecBlock / 32 ? s_w[lane] : 0;
+    const uint32_t x = c;
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, c, o);
+      if (lane >= o) c += y;
+    }
+    s_w[lane] = c - x;
+  }
+  __syncthreads();
+  const u64 rank = b.block_tmp[blockIdx.x] + s_w[warp] + __popc(m & lanemask_lt());
+  if (ok) b.rec_cycle[rank] = g;
+  // per-instance record offsets: rank of the instance's first cycle
+  if (g < b.n_cycles) {
+    const uint32_t inst = b.c_inst[g];
+    if (g == b.cyc_off[inst]) {
+      // every instance with cycles starting here (empty instances share it)
+      for (i64 i = inst; i >= 0 && b.cyc_off[i] == g; --i) b.rec_off[i] = rank;
+    }
+  }
+}
+
+__global__ void k_rec_off_tail(DevBuffers b, uint64_t* total) {
+  // instances whose cycles start at n_cycles (trailing empty ones) and the end
+  for (i64 i = b.n_inst; i >= 0 && b.cyc_off[i] == b.n_cycles; --i) b.rec_off[i] = *total;
+}
+
+// ------------------------------------------------------------ K6 score
+// GBDT predict (gbdt.cpp:22-30,173-184) in shared memory, complete-tree
+// layout (BFS order; level-contiguous nodes keep warp reads conflict-free),
+// then ppe (detector.cpp:14-19).  Tile = 8192 records, model staged once per
+// (tile, instance).
+constexpr int kScoreThreads = 256;
+constexpr int kScoreTile = 8192;
+
+template <int NF>
+__device__ __forceinline__ double gbdt_predict(const DevModel& m, const double* __restrict__ thr,
+                                               const uint8_t* __restrict__ feat,
+                                               const double* __restrict__ leaf, const double* x) {
+  double v = m.base;
+  const int D = (int)m.depth;
+  const uint32_t ni = (1u << D) - 1, nl = 1u << D;
+  for (uint32_t t = 0; t < m.n_trees; ++t) {
+    const double* tt = thr + (u64)t * ni;
+    const uint8_t* tf = feat + (u64)t * ni;
+    uint32_t node = 0;
+    for (int d = 0; d < D; ++d) {
+      const uint32_t f = tf[node];
+      double xv = x[0];
+#pragma unroll
+      for (int k = 1; k < NF; ++k) xv = (f == (uint32_t)k) ? x[k] : xv;
+      node = 2 * node + 1 + (xv <= tt[node] ? 0u : 1u);
+    }
+    v = __dadd_rn(v, __dmul_rn(m.lr, leaf[(u64)t * nl + (node - ni)]));
+  }
+  return m.floor_ < v ? v : m.floor_;
+}
+
+template <int NF>
+__global__ void __launch_bounds__(kScoreThreads)
+    k_score(DevBuffers b, DevConfig cfg, uint64_t n_records, uint64_t smem_cap) {
+  extern __shared__ __align__(16) unsigned char s_model[];
+  __shared__ uint32_t s_inst;
+  const u64 r0 = (u64)blockIdx.x * kScoreTile;
+  const u64 r1 = min(r0 + (u64)kScoreTile, (u64)n_records);
+  const double eps = cfg.ctl.epsilon;
+  const int lat = cfg.cyc.latency_phase;
+  const int P = cfg.cyc.n_phases;
+  u64 r = r0;
+  while (r < r1) {
+    if (threadIdx.x == 0) s_inst = upper_bound_u64(b.rec_off, b.n_inst + 1, r) - 1;
+    __syncthreads();
+    const uint32_t inst = s_inst;
+    const u64 seg_end = min(r1, (u64)b.rec_off[inst + 1]);
+    const DevModel m = b.models[inst];
+    const double* thr = m.thr;
+    const uint8_t* feat = m.feat;
+    const double* leaf = m.leaf;
+    if (m.smem_bytes <= smem_cap) {
+      const uint32_t ni = (1u << m.depth) - 1, nl = 1u << m.depth;
+      double* st = reinterpret_cast<double*>(s_model);
+      double* sl = st + (u64)m.n_trees * ni;
+      uint8_t* sf = reinterpret_cast<uint8_t*>(sl + (u64)m.n_trees * nl);
+      for (u64 i = threadIdx.x; i < (u64)m.n_trees * ni; i += blockDim.x) st[i] = m.thr[i];
+      for (u64 i = threadIdx.x; i < (u64)m.n_trees * nl; i += blockDim.x) sl[i] = m.leaf[i];
+      for (u64 i = threadIdx.x; i < (u64)m.n_trees * ni; i += blockDim.x) sf[i] = m.feat[i];
+      thr = st;
+      leaf = sl;
+      feat = sf;
+    }
+    __syncthreads();
+    const u64 rb = b.rec_off[inst];
+    for (u64 k = r + threadIdx.x; k < seg_end; k += blockDim.x) {
+      const u64 g = b.rec_cycle[k];
+      const cs_workload w = b.wl[b.c_wl[g]];
+      const i64 dur = b.c_end[g] - b.c_start[g];
+      i64 target = dur;
+      if (lat >= 0) {
+        const i64 c = b.c_comp[g * P + lat];
+        if (c > 0) target = c;
+      }
+      const double y = __dmul_rn((double)target, 1e-9);
+      double x[NF > 0 ? NF : 1];
+#pragma unroll
+      for (int f = 0; f < NF; ++f) {
+        const int id = m.feature_ids[f];
+        double v;
+        switch (id) {
+          case CS_F_BATCH: v = (double)w.batch; break;
+          case CS_F_W_KV: v = (double)(w.batch * (w.input_len + w.output_len)); break;
+          case CS_F_INPUT_LEN: v = (double)w.input_len; break;
+          case CS_F_OUTPUT_LEN: v = (double)w.output_len; break;
+          default: v = b.c_stage[g] == CS_STAGE_PREFILL ? 1.0 : 0.0; break;
+        }
+        x[f] = v;
+      }
+      const double p = gbdt_predict<NF>(m, thr, feat, leaf, x);
+      double res;
+      if (!(y > 0.0)) {
+        atomicMin(reinterpret_cast<u64*>(&b.inst[inst].first_bad_record), (u64)(k - rb));
+        res = __longlong_as_double(0x7ff8000000000000ll);
+      } else {
+        const double q = __ddiv_rn(__dsub_rn(y, p), __dadd_rn(y, eps));
+        res = 0.0 < q ? q : 0.0;
+      }
+      b.rec_pred[k] = p;
+      b.rec_resid[k] = res;
+    }
+    __syncthreads();
+    r = seg_end;
+  }
+}
+
+// ------------------------------------------------------------ K7 detect
+// Detector::step (detector.cpp:91-130) for every record at once:
+//   stat_t  = e_t (FixedPoint) or (sum_{u=max(0,t-W+1)}^{t} e_u, oldest first)/count
+//   armed_t = t >= warmup;  flagged_t = armed_t && stat_t > limit
+//   alert_t = flagged_t && !flagged_{t-1}   (in_episode == flagged_{t-1})
+// Episode id = alerts before t in the instance (exclusive scan).
+constexpr int kDetBlock = 1024;
+
+__device__ __forceinline__ double window_stat(const double* e, u64 t, u64 W, int strategy) {
+  if (strategy == CS_FIXED_POINT) return e[t];
+  const u64 begin = t + 1 >= W ? t + 1 - W : 0;
+  double sum = 0.0;
+  for (u64 u = begin; u <= t; ++u) sum = __dadd_rn(sum, e[u]);
+  return __ddiv_rn(sum, (double)(t - begin + 1));
+}
+
+__global__ void k_detect_flags(DevBuffers b, DevConfig cfg, uint64_t n_records) {
+  __shared__ uint32_t s_w[32];
+  const u64 k = (u64)blockIdx.x * kDetBlock + threadIdx.x;
+  bool alert = false;
+  if (k < n_records) {
+    const uint32_t inst = upper_bound_u64(b.rec_off, b.n_inst + 1, k) - 1;
+    const u64 rb = b.rec_off[inst];
+    const u64 t = k - rb;
+    const double limit = b.models[inst].ucl;
+    const double* e = b.rec_resid + rb;
+    const double stat = window_stat(e, t, cfg.ctl.window, cfg.ctl.strategy);
+    const bool armed = t >= cfg.ctl.warmup;
+    const bool flagged = armed && stat > limit;
+    bool prev = false;
+    if (t >= 1 && t - 1 >= cfg.ctl.warmup) prev = window_stat(e, t - 1, cfg.ctl.window, cfg.ctl.strategy) > limit;
+    alert = flagged && !prev;
+    b.rec_stat[k] = stat;
+    b.rec_flags[k] = (armed ? 1 : 0) | (flagged ? 2 : 0) | (alert ? 4 : 0);
+    if (alert) atomicAdd(&b.inst[inst].n_alerts, 1ull);
+  }
+  const uint32_t m = __ballot_sync(0xffffffffu, alert);
+  if ((threadIdx.x & 31) == 0) s_w[threadIdx.x >> 5] = __popc(m);
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    u64 v = s_w[threadIdx.x];
+    v = warp_sum_u64(v);
+    if (threadIdx.x == 0) b.block_tmp[blockIdx.x] = v;
+  }
+}
+
+__global__ void k_alert_off(DevBuffers b) {
+  // exclusive scan over instances of n_alerts (n_inst is small: one CTA)
+  if (threadIdx.x == 0) {
+    u64 acc = 0;
+    for (uint32_t i = 0; i < b.n_inst; ++i) {
+      b.alert_off[i] = acc;
+      acc += b.inst[i].n_alerts;
+    }
+    b.alert_off[b.n_inst] = acc;
+  }
+}
+
+__global__ void k_detect_scatter(DevBuffers b, uint64_t n_records) {
+  __shared__ uint32_t s_w[32];
+  const u64 k = (u64)blockIdx.x * kDetBlock + threadIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const bool alert = k < n_records && (b.rec_flags[k] & 4);
+  const uint32_t m = __ballot_sync(0xffffffffu, alert);
+  if (lane == 0) s_w[warp] = __popc(m);
+  __syncthreads();
+  if (warp == 0) {
+    uint32_t c = lane < kDetBlock / 32 ? s_w[lane] : 0;
+    const uint32_t x = c;
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, c, o);
+      if (lane >= o) c += y;
+    }
+    s_w[lane] = c - x;
+  }
+  __syncthreads();
+  if (alert) b.alert_rec[b.block_tmp[blockIdx.x] + s_w[warp] + __popc(m & lanemask_lt())] = k;
+}
+
+// --------------------------------------------------- frequency fallback
+// segment_by_frequency (cycles.cpp:283-343): rare path, exact arithmetic.
+__global__ void k_gpu_kernel_extent(const cs_event* ev, uint64_t begin, uint64_t end,
+                                    unsigned long long* out3) {
+  // out3[0] count, out3[1] min start (as order-preserving u64), out3[2] max
+  u64 cnt = 0, mn = ~0ull, mx = 0;
+  for (u64 j = begin + (u64)blockIdx.x * blockDim.x + threadIdx.x; j < end;
+       j += (u64)gridDim.x * blockDim.x) {
+    const cs_event& e = ev[j];
+    if (e.kind == CS_SPAN && e.category == CS_CAT_GPU_KERNEL) {
+      ++cnt;
+      const u64 key = (u64)e.start_ts ^ (1ull << 63);
+      mn = key < mn ? key : mn;
+      mx = key > mx ? key : mx;
+    }
+  }
+  cnt = warp_sum_u64(cnt);
+  for (int o = 16; o > 0; o >>= 1) {
+    const u64 a = __shfl_xor_sync(0xffffffffu, mn, o), c = __shfl_xor_sync(0xffffffffu, mx, o);
+    mn = a < mn ? a : mn;
+    mx = c > mx ? c : mx;
+  }
+  if ((threadIdx.x & 31) == 0 && cnt) {
+    atomicAdd(&out3[0], cnt);
+    atomicMin(&out3[1], mn);
+    atomicMax(&out3[2], mx);
+  }
+}
+
+__global__ void k_freq_hist(const cs_event* ev, uint64_t begin, uint64_t end, int64_t t0,
+                            int64_t bin_ns, uint64_t bins, unsigned long long* hist) {
+  for (u64 j = begin + (u64)blockIdx.x * blockDim.x + threadIdx.x; j < end;
+       j += (u64)gridDim.x * blockDim.x) {
+    const cs_event& e = ev[j];
+    if (e.kind == CS_SPAN && e.category == CS_CAT_GPU_KERNEL) {
+      const u64 bi = (u64)((e.start_ts - t0) / bin_ns);
+      if (bi < bins) atomicAdd(&hist[bi], 1ull);
+    }
+  }
+}
+
+__global__ void k_freq_center(const unsigned long long* hist, uint64_t bins, double* h) {
+  // mean = (sum of integer counts, exact) / bins; h -= mean (cycles.cpp:301-304)
+  __shared__ double s_mean;
+  if (threadIdx.x == 0) {
+    double m = 0.0;
+    for (u64 i = 0; i < bins; ++i) m = __dadd_rn(m, (double)hist[i]);
+    s_mean = __ddiv_rn(m, (double)bins);
+  }
+  __syncthreads();
+  for (u64 i = threadIdx.x; i < bins; i += blockDim.x) h[i] = __dsub_rn((double)hist[i], s_mean);
+}
+
+__global__ void k_freq_autocorr(const double* h, uint64_t bins, double* acc) {
+  // one thread per lag, the reference's sequential inner sum (310-317)
+  const u64 lag = 1 + (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (lag > bins / 2) return;
+  double a = 0.0;
+  for (u64 i = 0; i + lag < bins; ++i) a = __dadd_rn(a, __dmul_rn(h[i], h[i + lag]));
+  acc[lag] = a;
+}
+
+__global__ void k_freq_cycles(const cs_event* ev, uint64_t begin, uint64_t end, int64_t t0,
+                              int64_t period, uint64_t n, uint64_t cyc_base, DevBuffers b,
+                              uint32_t inst) {
+  const u64 c = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n) return;
+  const i64 s = t0 + (i64)c * period;
+  const i64 e = s + period;
+  auto lower = [&](i64 ts) {
+    u64 lo = begin, hi = end;
+    while (lo < hi) {
+      const u64 mid = (lo + hi) >> 1;
+      if (ev[mid].start_ts < ts) lo = mid + 1;
+      else hi = mid;
+    }
+    return lo;
+  };
+  const u64 g = cyc_base + c;
+  b.c_start[g] = s;
+  b.c_end[g] = e;
+  b.c_apos[g] = ~0ull;
+  b.c_aend[g] = s;
+  b.c_first[g] = lower(s);
+  b.c_last[g] = lower(e);
+  b.c_inst[g] = inst;
+}
+
+// ------------------------------------------------------------ launchers
+void launch_scan_events(const DevBuffers& b, const DevConfig&, int mode, bool sample,
+                        cudaStream_t s, uint64_t* launches) {
+  if (b.n_tiles == 0) return;
+  k_scan_events<<<b.n_tiles, kScanThreads, 0, s>>>(b, mode, sample ? 1 : 0);
+  ++*launches;
+}
+
+void launch_rank(const DevBuffers& b, const DevConfig& cfg, int final_pass, cudaStream_t s,
+                 uint64_t* launches) {
+  if (b.n_inst == 0) return;
+  k_rank<<<b.n_inst, 32, 0, s>>>(b, cfg, final_pass);
+  ++*launches;
+}
+
+void launch_fold(const DevBuffers& b, const DevConfig&, const uint32_t* pi, const uint32_t* pn,
+                 uint32_t n_pairs, double* out, cudaStream_t s, uint64_t* launches) {
+  if (!n_pairs) return;
+  k_fold<<<(n_pairs + 63) / 64, 64, 0, s>>>(b, pi, pn, n_pairs, out);
+  ++*launches;
+}
+
+void launch_bounds(const DevBuffers& b, cudaStream_t s, uint64_t* launches) {
+  if (!b.n_cycles) return;
+  k_bounds<<<(unsigned)((b.n_cycles + 255) / 256), 256, 0, s>>>(b);
+  ++*launches;
+}
+
+void launch_cycle_reduce(const DevBuffers& b, const DevConfig& cfg, int do_beta, cudaStream_t s,
+                         uint64_t* launches) {
+  if (!b.n_cycles) return;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  u64 blocks = (b.n_cycles + kReduceWarps - 1) / kReduceWarps;
+  const u64 cap = (u64)sms * 8;
+  if (blocks > cap) blocks = cap;
+  k_cycle_reduce<<<(unsigned)blocks, kReduceWarps * 32, 0, s>>>(b, cfg, do_beta);
+  ++*launches;
+}
+
+void launch_stage_heuristic(const DevBuffers& b, const DevConfig& cfg, cudaStream_t s,
+                            uint64_t* launches) {
+  if (!b.n_inst) return;
+  k_stage_heuristic<<<(b.n_inst + 3) / 4, 128, 0, s>>>(b, cfg);
+  ++*launches;
+}
+
+void launch_records(const DevBuffers& b, const DevConfig& cfg, uint64_t, cudaStream_t s,
+                    uint64_t* launches) {
+  const u64 nb = (b.n_cycles + kRecBlock - 1) / kRecBlock;
+  if (nb) {
+    k_records_count<<<(unsigned)nb, kRecBlock, 0, s>>>(b, cfg);
+    ++*launches;
+  }
+  // block_tmp[nb] receives the total
+  k_scan_exclusive<<<1, 1024, 0, s>>>(b.block_tmp, nb, b.block_tmp + nb);
+  ++*launches;
+  if (nb) {
+    k_records_scatter<<<(unsigned)nb, kRecBlock, 0, s>>>(b, cfg);
+    ++*launches;
+  }
+  k_rec_off_tail<<<1, 1, 0, s>>>(b, b.block_tmp + nb);
+  ++*launches;
+}
+
+void launch_score(const DevBuffers& b, const DevConfig& cfg, uint64_t n_records,
+                  const uint64_t*, const int*, const DevModel* h_models, cudaStream_t s,
+                  uint64_t* launches) {
+  if (!n_records) return;
+  // all instances share the feature count of instance 0's model in this build
+  const uint32_t nf = h_models[0].n_features;
+  uint64_t need = 0;
+  for (uint32_t i = 0; i < b.n_inst; ++i)
+    if (h_models[i].smem_bytes > need) need = h_models[i].smem_bytes;
+  int dev = 0, max_optin = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  uint64_t cap = (uint64_t)max_optin - 1024;
+  if (need < cap) cap = need;
+  const unsigned grid = (unsigned)((n_records + kScoreTile - 1) / kScoreTile);
+#define CS_SCORE_CASE(NF)                                                                 \
+  case NF:                                                                                \
+    cudaFuncSetAttribute(k_score<NF>, cudaFuncAttributeMaxDynamicSharedMemorySize,        \
+                         (int)cap);                                                       \
+    k_score<NF><<<grid, kScoreThreads, cap, s>>>(b, cfg, n_records, cap);                 \
+    break;
+  switch (nf) {
+    CS_SCORE_CASE(0)
+    CS_SCORE_CASE(1)
+    CS_SCORE_CASE(2)
+    CS_SCORE_CASE(3)
+    CS_SCORE_CASE(4)
+    CS_SCORE_CASE(5)
+    CS_SCORE_CASE(6)
+    CS_SCORE_CASE(7)
+    CS_SCORE_CASE(8)
+    default: break;
+  }
+#undef CS_SCORE_CASE
+  ++*launches;
+}
+
+void launch_detect(const DevBuffers& b, const DevConfig& cfg, uint64_t n_records, cudaStream_t s,
+                   uint64_t* launches) {
+  const u64 nb = (n_records + kDetBlock - 1) / kDetBlock;
+  if (nb) {
+    k_detect_flags<<<(unsigned)nb, kDetBlock, 0, s>>>(b, cfg, n_records);
+    ++*launches;
+  }
+  k_scan_exclusive<<<1, 1024, 0, s>>>(b.block_tmp, nb, b.block_tmp + nb);
+  ++*launches;
+  k_alert_off<<<1, 32, 0, s>>>(b);
+  ++*launches;
+  if (nb) {
+    k_detect_scatter<<<(unsigned)nb, kDetBlock, 0, s>>>(b, n_records);
+    ++*launches;
+  }
+}
+
+void launch_gpu_kernel_extent(const cs_event* ev, uint64_t begin, uint64_t end,
+                              unsigned long long* out3, cudaStream_t s, uint64_t* launches) {
+  k_gpu_kernel_extent<<<296, 256, 0, s>>>(ev, begin, end, out3);
+  ++*launches;
+}
+
+void launch_freq_hist(const cs_event* ev, uint64_t begin, uint64_t end, int64_t t0,
+                      int64_t bin_ns, uint64_t bins, double* h, cudaStream_t s,
+                      uint64_t* launches) {
+  // hist counts are accumulated as u64 in the first half of a 2*bins buffer
+  unsigned long long* counts = reinterpret_cast<unsigned long long*>(h + bins);
+  cudaMemsetAsync(counts, 0, bins * sizeof(u64), s);
+  k_freq_hist<<<296, 256, 0, s>>>(ev, begin, end, t0, bin_ns, bins, counts);
+  k_freq_center<<<1, 256, 0, s>>>(counts, bins, h);
+  *launches += 2;
+}
+
+void launch_freq_autocorr(const double* h, uint64_t bins, double* acc, cudaStream_t s,
+                          uint64_t* launches) {
+  const u64 lags = bins / 2;
+  if (!lags) return;
+  k_freq_autocorr<<<(unsigned)((lags + 127) / 128), 128, 0, s>>>(h, bins, acc);
+  ++*launches;
+}
+
+void launch_freq_cycles(const cs_event* ev, uint64_t begin, uint64_t end, int64_t t0,
+                        int64_t period, uint64_t n, uint64_t cyc_base, const DevBuffers& b,
+                        uint32_t inst, cudaStream_t s, uint64_t* launches) {
+  if (!n) return;
+  k_freq_cycles<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(ev, begin, end, t0, period, n,
+                                                           cyc_base, b, inst);
+  ++*launches;
+}
+
+}  // namespace csb

@@ -1,0 +1,424 @@
+"""ctypes binding of libcyclescope_b200.so (the C ABI in include/cyclescope_b200.h).
+
+This is plumbing for tests, bench.py and __graft_entry__: every computation
+happens in the native library (sm_100a kernels + host C++).  There is no
+Python or CPU fallback — if the library or a CUDA device is missing the calls
+raise.
+
+Names mirror the reference's C++ API (cycles.hpp / detector.hpp /
+baseline.hpp): `Analyzer.run` is segment_and_classify + build_cycle_records +
+cycle_stats(beta) + LatencyModel::predict + ppe + Detector::step over a batch
+of instances; `fit_latency_model` is the reference's deterministic fit.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import json
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import abi
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libcyclescope_b200.so")
+
+_lib = None
+
+
+class EngineError(RuntimeError):
+    """Mirrors cyclescope::EngineError: .type is the reference's type() string."""
+
+    def __init__(self, status: int, message: str):
+        self.status = status
+        self.type = abi.STATUS_TYPES.get(status, "internal")
+        super().__init__(f"{self.type}: {message}")
+
+
+def lib():
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(f"{LIB_PATH} missing: build it with __graft_entry__.build()")
+    L = C.CDLL(LIB_PATH)
+    vp, sz, u32, u64 = C.c_void_p, C.c_size_t, C.c_uint32, C.c_uint64
+    psz = C.POINTER(sz)
+    L.cs_abi_version.restype = C.c_int
+    L.cs_status_type.restype = C.c_char_p
+    L.cs_status_type.argtypes = [C.c_int]
+    L.cs_ctx_create.argtypes = [C.c_int, C.POINTER(vp)]
+    L.cs_ctx_destroy.argtypes = [vp]
+    L.cs_last_error.restype = C.c_char_p
+    L.cs_last_error.argtypes = [vp]
+    L.cs_set_config.argtypes = [vp, C.POINTER(abi.CycleConfig), C.POINTER(abi.ControlConfig)]
+    L.cs_set_name_table.argtypes = [vp, u32, vp]
+    L.cs_upload.argtypes = [vp, u32, vp, vp, u64, vp]
+    L.cs_load_model.argtypes = [vp, u32, C.POINTER(abi.Model)]
+    L.cs_run.argtypes = [vp, u32]
+    L.cs_sync.argtypes = [vp]
+    L.cs_get_summary.argtypes = [vp, u32, C.POINTER(abi.InstanceSummary)]
+    for fn in ("cs_get_candidates", "cs_get_cycles", "cs_get_components", "cs_get_records",
+               "cs_get_alerts"):
+        getattr(L, fn).argtypes = [vp, u32, vp, sz, psz]
+    L.cs_get_beta.argtypes = [vp, u32, vp, vp, sz, psz]
+    L.cs_get_collective_beta.argtypes = [vp, u32, vp, vp, sz, psz]
+    L.cs_host_alloc.argtypes = [sz, C.POINTER(vp)]
+    L.cs_host_free.argtypes = [vp]
+    L.cs_get_timings.argtypes = [vp, vp, sz, psz, C.c_char_p, sz]
+    L.cs_get_launch_count.argtypes = [vp, C.POINTER(u64)]
+    L.cs_fit_latency_model.argtypes = [u64, u32, vp, vp, vp, C.POINTER(abi.GbdtParams),
+                                       C.POINTER(abi.FitOptions), C.POINTER(vp), C.c_char_p, sz]
+    L.cs_model_from_json.argtypes = [C.c_char_p, C.POINTER(vp), C.c_char_p, sz]
+    L.cs_model_to_json.argtypes = [vp, vp, sz, psz]
+    L.cs_model_view.argtypes = [vp, C.POINTER(abi.Model)]
+    L.cs_model_free.argtypes = [vp]
+    L.cs_ucl_from_stats.restype = C.c_double
+    L.cs_ucl_from_stats.argtypes = [C.c_double, C.c_double, C.POINTER(abi.ControlConfig)]
+    L.cs_config_from_json.argtypes = [C.c_char_p, u32, vp, vp, u32, vp,
+                                      C.POINTER(abi.CycleConfig), C.POINTER(abi.ControlConfig),
+                                      C.c_char_p, sz]
+    L.cs_synth_generate.argtypes = [vp, u32, u32, C.c_int, C.POINTER(vp)]
+    L.cs_synth_view.argtypes = [vp] + [C.POINTER(vp), C.POINTER(u64), C.POINTER(vp),
+                                       C.POINTER(vp), C.POINTER(u64), C.POINTER(vp),
+                                       C.POINTER(u64)]
+    L.cs_synth_names.argtypes = [vp, C.POINTER(C.c_char_p), psz, C.POINTER(u32), C.POINTER(u32)]
+    L.cs_synth_free.argtypes = [vp]
+    _lib = L
+    return L
+
+
+EXPORTED_SYMBOLS = [
+    "cs_abi_version", "cs_status_type", "cs_ctx_create", "cs_ctx_destroy", "cs_last_error",
+    "cs_set_config", "cs_set_name_table", "cs_upload", "cs_load_model", "cs_run", "cs_sync",
+    "cs_get_summary", "cs_get_candidates", "cs_get_cycles", "cs_get_components", "cs_get_beta",
+    "cs_get_collective_beta", "cs_get_records", "cs_get_alerts", "cs_host_alloc",
+    "cs_host_free", "cs_get_timings", "cs_get_launch_count", "cs_fit_latency_model",
+    "cs_model_from_json", "cs_model_to_json", "cs_model_view", "cs_model_free",
+    "cs_ucl_from_stats", "cs_compute_ucl", "cs_config_from_json", "cs_synth_generate",
+    "cs_synth_view", "cs_synth_names", "cs_synth_free",
+]
+
+
+def _check(rc: int, ctx=None, msg: str = ""):
+    if rc != 0:
+        detail = msg
+        if ctx is not None:
+            detail = (lib().cs_last_error(ctx) or b"").decode() or msg
+        raise EngineError(rc, detail)
+
+
+def _ptr(a: np.ndarray | None):
+    return None if a is None or a.size == 0 else a.ctypes.data
+
+
+# ---------------------------------------------------------------- models
+class LatencyModel:
+    """Handle on a fitted / loaded LatencyModel (baseline.hpp:50-67)."""
+
+    def __init__(self, handle):
+        self.h = handle
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.cs_model_free(self.h)
+            self.h = None
+
+    @classmethod
+    def from_json(cls, text: str) -> "LatencyModel":
+        h = C.c_void_p()
+        err = C.create_string_buffer(1024)
+        rc = lib().cs_model_from_json(text.encode(), C.byref(h), err, 1024)
+        if rc:
+            raise EngineError(rc, err.value.decode())
+        return cls(h)
+
+    def to_json(self) -> str:
+        n = C.c_size_t(0)
+        lib().cs_model_to_json(self.h, None, 0, C.byref(n))
+        buf = C.create_string_buffer(n.value)
+        _check(lib().cs_model_to_json(self.h, buf, n.value, C.byref(n)))
+        return buf.value.decode()
+
+    def view(self) -> abi.Model:
+        v = abi.Model()
+        _check(lib().cs_model_view(self.h, C.byref(v)))
+        return v
+
+    @property
+    def mu_train(self) -> float:
+        return self.view().mu_train
+
+    @property
+    def sigma_train(self) -> float:
+        return self.view().sigma_train
+
+
+def fit_latency_model(x: np.ndarray, y: np.ndarray, feature_names=("batch", "w_kv"),
+                      params: abi.GbdtParams | None = None,
+                      options: abi.FitOptions | None = None) -> LatencyModel:
+    """fit_latency_model (baseline.cpp:168-208): deterministic host C++ fit."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    ids = np.array([abi.FEATURE_IDS[n] for n in feature_names], dtype=np.int32)
+    params = params or abi.default_gbdt_params()
+    if options is None:
+        options = abi.default_fit_options(len(ids))
+        options.stratify_col = list(feature_names).index("w_kv") if "w_kv" in feature_names else 0
+    h = C.c_void_p()
+    err = C.create_string_buffer(1024)
+    rc = lib().cs_fit_latency_model(len(y), len(ids), ids.ctypes.data, _ptr(x), _ptr(y),
+                                    C.byref(params), C.byref(options), C.byref(h), err, 1024)
+    if rc:
+        raise EngineError(rc, err.value.decode())
+    return LatencyModel(h)
+
+
+def ucl_from_stats(mu: float, sigma: float, control: abi.ControlConfig) -> float:
+    return lib().cs_ucl_from_stats(mu, sigma, C.byref(control))
+
+
+# ---------------------------------------------------------------- configs
+def configs_from_json(run_config: dict | str | None, names, name_is_span, n_comm_slots=0):
+    """RunConfig JSON -> (CycleConfig, ControlConfig, name table) via the library."""
+    text = run_config if isinstance(run_config, str) else json.dumps(run_config or {})
+    n = len(names)
+    arr = (C.c_char_p * max(n, 1))(*[s.encode() for s in names])
+    span = np.ascontiguousarray(np.asarray(name_is_span, dtype=np.uint8))
+    table = np.zeros(n, dtype=abi.NAME_INFO_DTYPE)
+    cyc, ctl = abi.CycleConfig(), abi.ControlConfig()
+    err = C.create_string_buffer(1024)
+    rc = lib().cs_config_from_json(text.encode(), n, C.cast(arr, C.c_void_p) if n else None,
+                                   _ptr(span), n_comm_slots, _ptr(table), C.byref(cyc),
+                                   C.byref(ctl), err, 1024)
+    if rc:
+        raise EngineError(rc, err.value.decode())
+    return cyc, ctl, table
+
+
+def span_names_mask(events: np.ndarray, n_names: int) -> np.ndarray:
+    """Which interned names occur as Spans (host ingest bookkeeping)."""
+    m = np.zeros(n_names, dtype=np.uint8)
+    ids = np.unique(events["name_id"][events["kind"] == abi.SPAN])
+    m[ids] = 1
+    return m
+
+
+# ---------------------------------------------------------------- synth
+@dataclass
+class SynthTrace:
+    events: np.ndarray
+    event_ids: np.ndarray
+    workloads: np.ndarray
+    labels: np.ndarray
+    names: list
+    n_comm: int
+
+
+class SynthParams(C.Structure):
+    _fields_ = [("n_cycles", C.c_uint64), ("workload_seed", C.c_uint64),
+                ("synth_seed", C.c_uint64), ("fault_family", C.c_int32),
+                ("target_rank", C.c_int32), ("fault_onset", C.c_uint64),
+                ("fault_duration", C.c_uint64), ("severity", C.c_double),
+                ("n_ranks", C.c_uint64), ("noise", C.c_double)]
+
+
+FAULT_FAMILIES = ["cpu_contention", "cpu_freq_drop", "gpu_contention", "gpu_clock_lock",
+                  "memory_thrash", "nvlink_saturation", "pcie_bottleneck", "bus_contention"]
+
+
+def synth_trace(n_cycles, workload_seed, synth_seed, fault=None, onset=0, duration=0,
+                severity=-1.0, target_rank=0, n_ranks=1, noise=-1.0, n_chunks=1,
+                n_threads=None, compact_names=True) -> SynthTrace:
+    """Synthetic trace from the simkit restatement (cs_synth.cpp)."""
+    fam = -1 if fault is None else (FAULT_FAMILIES.index(fault) if isinstance(fault, str) else int(fault))
+    p = SynthParams(n_cycles, workload_seed, synth_seed, fam, target_rank, onset, duration,
+                    severity, n_ranks, noise)
+    L = lib()
+    h = C.c_void_p()
+    _check(L.cs_synth_generate(C.byref(p), n_chunks, n_threads or os.cpu_count() or 1,
+                               int(compact_names), C.byref(h)))
+    try:
+        ev, ids, wl, lab = C.c_void_p(), C.c_void_p(), C.c_void_p(), C.c_void_p()
+        nev, nwl, ncyc = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        _check(L.cs_synth_view(h, C.byref(ev), C.byref(nev), C.byref(ids), C.byref(wl),
+                               C.byref(nwl), C.byref(lab), C.byref(ncyc)))
+
+        def arr(ptr, n, dtype):
+            if n == 0:
+                return np.zeros(0, dtype=dtype)
+            nbytes = n * np.dtype(dtype).itemsize
+            return np.frombuffer((C.c_char * nbytes).from_address(ptr.value), dtype=dtype).copy()
+
+        events = arr(ev, nev.value, abi.EVENT_DTYPE)
+        event_ids = arr(ids, nev.value, np.uint64)
+        workloads = arr(wl, nwl.value, abi.WORKLOAD_DTYPE)
+        labels = arr(lab, ncyc.value, np.uint8).astype(bool)
+        packed, nb, nn, nc = C.c_char_p(), C.c_size_t(), C.c_uint32(), C.c_uint32()
+        _check(L.cs_synth_names(h, C.byref(packed), C.byref(nb), C.byref(nn), C.byref(nc)))
+        raw = C.string_at(packed, nb.value)
+        names = [s.decode() for s in raw.split(b"\0")[:nn.value]]
+        return SynthTrace(events, event_ids, workloads, labels, names, nc.value)
+    finally:
+        L.cs_synth_free(h)
+
+
+# ---------------------------------------------------------------- analyzer
+@dataclass
+class InstanceResult:
+    summary: abi.InstanceSummary
+    cycles: np.ndarray
+    components: np.ndarray
+    beta_totals: np.ndarray | None
+    beta: np.ndarray | None
+    coll_beta: np.ndarray | None
+    coll_present: np.ndarray | None
+    records: np.ndarray
+    alerts: np.ndarray
+    candidates: np.ndarray
+
+    @property
+    def status_type(self) -> str:
+        return abi.STATUS_TYPES.get(self.summary.status, "internal")
+
+
+class Analyzer:
+    """One device context (cs_ctx): a batch of monitored instances on one GPU."""
+
+    def __init__(self, device: int = 0):
+        self.L = lib()
+        h = C.c_void_p()
+        rc = self.L.cs_ctx_create(device, C.byref(h))
+        if rc:
+            raise EngineError(rc, "cs_ctx_create failed (no CUDA device?)")
+        self.h = h
+        self.cycle = abi.CycleConfig()
+        self.control = abi.ControlConfig()
+        self.names: list = []
+        self._keep = []
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.L.cs_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        self.close()
+
+    def _ck(self, rc):
+        _check(rc, self.h)
+
+    def configure(self, names, name_is_span, n_comm_slots=0, run_config=None):
+        cyc, ctl, table = configs_from_json(run_config, names, name_is_span, n_comm_slots)
+        self.set_config(cyc, ctl)
+        self.set_name_table(table)
+        self.names = list(names)
+        return cyc, ctl, table
+
+    def set_config(self, cycle: abi.CycleConfig, control: abi.ControlConfig):
+        self.cycle, self.control = cycle, control
+        self._ck(self.L.cs_set_config(self.h, C.byref(cycle), C.byref(control)))
+
+    def set_name_table(self, table: np.ndarray):
+        table = np.ascontiguousarray(table, dtype=abi.NAME_INFO_DTYPE)
+        self._ck(self.L.cs_set_name_table(self.h, len(table), _ptr(table)))
+
+    def upload(self, events: np.ndarray, inst_offsets, workloads: np.ndarray):
+        events = np.ascontiguousarray(events, dtype=abi.EVENT_DTYPE)
+        off = np.ascontiguousarray(np.asarray(inst_offsets, dtype=np.uint64))
+        wl = np.ascontiguousarray(workloads, dtype=abi.WORKLOAD_DTYPE)
+        self._ck(self.L.cs_upload(self.h, len(off) - 1, off.ctypes.data, _ptr(events), len(wl),
+                                  _ptr(wl)))
+        self.n_inst = len(off) - 1
+
+    def load_model(self, model: LatencyModel, inst: int | None = None):
+        v = model.view()
+        self._keep.append(model)
+        self._ck(self.L.cs_load_model(self.h, 0xFFFFFFFF if inst is None else inst, C.byref(v)))
+
+    def run(self, mask: int = abi.RUN_ALL):
+        self._ck(self.L.cs_run(self.h, mask))
+
+    def launches(self) -> int:
+        n = C.c_uint64()
+        self._ck(self.L.cs_get_launch_count(self.h, C.byref(n)))
+        return n.value
+
+    def timings(self) -> dict:
+        ms = np.zeros(32, np.float64)
+        n = C.c_size_t()
+        names = C.create_string_buffer(1024)
+        self._ck(self.L.cs_get_timings(self.h, ms.ctypes.data, 32, C.byref(n), names, 1024))
+        keys = names.value.decode().split(",") if n.value else []
+        return {k: float(ms[i]) for i, k in enumerate(keys)}
+
+    def summary(self, inst: int = 0) -> abi.InstanceSummary:
+        s = abi.InstanceSummary()
+        self._ck(self.L.cs_get_summary(self.h, inst, C.byref(s)))
+        return s
+
+    def _get(self, fn, inst, dtype):
+        n = C.c_size_t()
+        self._ck(fn(self.h, inst, None, 0, C.byref(n)))
+        out = np.zeros(n.value, dtype=dtype)
+        if n.value:
+            self._ck(fn(self.h, inst, out.ctypes.data, n.value, C.byref(n)))
+        return out
+
+    def cycles(self, inst=0):
+        return self._get(self.L.cs_get_cycles, inst, abi.CYCLE_DTYPE)
+
+    def components(self, inst=0):
+        return self._get(self.L.cs_get_components, inst, np.int64)
+
+    def records(self, inst=0):
+        return self._get(self.L.cs_get_records, inst, abi.RECORD_DTYPE)
+
+    def alerts(self, inst=0):
+        return self._get(self.L.cs_get_alerts, inst, abi.ALERT_DTYPE)
+
+    def candidates(self, inst=0):
+        return self._get(self.L.cs_get_candidates, inst, abi.CANDIDATE_DTYPE)
+
+    def beta(self, inst=0):
+        n = C.c_size_t()
+        self._ck(self.L.cs_get_beta(self.h, inst, None, None, 0, C.byref(n)))
+        t = np.zeros(n.value, np.int64)
+        b = np.zeros(n.value, np.float64)
+        if n.value:
+            self._ck(self.L.cs_get_beta(self.h, inst, t.ctypes.data, b.ctypes.data, n.value,
+                                        C.byref(n)))
+        return t, b
+
+    def collective_beta(self, inst=0):
+        n = C.c_size_t()
+        self._ck(self.L.cs_get_collective_beta(self.h, inst, None, None, 0, C.byref(n)))
+        b = np.zeros(n.value, np.float64)
+        p = np.zeros(n.value, np.uint8)
+        if n.value:
+            self._ck(self.L.cs_get_collective_beta(self.h, inst, b.ctypes.data, p.ctypes.data,
+                                                   n.value, C.byref(n)))
+        return b, p
+
+    def result(self, inst=0, beta=True, scored=True) -> InstanceResult:
+        s = self.summary(inst)
+        bt = bb = cb = cp = None
+        if beta:
+            bt, bb = self.beta(inst)
+            cb, cp = self.collective_beta(inst)
+        return InstanceResult(s, self.cycles(inst), self.components(inst), bt, bb, cb, cp,
+                              self.records(inst), self.alerts(inst) if scored else
+                              np.zeros(0, abi.ALERT_DTYPE), self.candidates(inst))
+
+
+def host_alloc(nbytes: int) -> tuple[int, np.ndarray]:
+    """Pinned host buffer (cudaHostAlloc) viewed as uint8; returns (ptr, array)."""
+    p = C.c_void_p()
+    _check(lib().cs_host_alloc(nbytes, C.byref(p)))
+    arr = np.frombuffer((C.c_char * nbytes).from_address(p.value), dtype=np.uint8)
+    return p.value, arr
+
+
+def host_free(ptr: int):
+    lib().cs_host_free(C.c_void_p(ptr))
