@@ -305,8 +305,8 @@ void run_reference(Handle& h, const RunConfig& config, const char* model_json,
   }
   // monitor_loop process lambda (main.cpp:151-177), every record in order
   const double ucl = ucl_from_stats(model.mu_train, model.sigma_train, config.detector);
-  R.ucl = ucl;
   Detector detector(config.detector, ucl);
+  R.ucl = detector.limit();  // limit in force (strategy dependent)
   try {
     for (size_t i = 0; i < records.size(); ++i) {
       const auto& rec = records[i];
