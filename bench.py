@@ -1,0 +1,402 @@
+#!/usr/bin/env python
+"""Benchmark: trace events/sec analysed on B200 (BASELINE.json metric).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--workload c2|c1|c3]
+
+Workload (default c2 = BASELINE configs[1]): one 8-rank tensor-parallel serving
+instance, ~100 M events (3.70 M cycles x 27 events), mixed prefill/decode,
+NvlinkSaturation x18 straggler on rank 3 — synthetic, produced by the simkit
+restatement (cs_synth.cpp, byte-identical to the reference generator per
+chunk; 64 chunks with substream seeds, generated on all host cores).  The
+latency model is fit once in setup (host C++, bit-identical to the
+reference's fit) on the first 2400 cycles.
+
+A step = one cs_run over the whole instance: anchor discovery, segmentation,
+stage classification, beta stage attribution, records, GBDT predict + ppe,
+control chart + alerts.  `value` = events / device time per step with inputs
+resident in HBM (CUDA events on the ctx stream, max over ranks).  `e2e` = the
+same through the public C ABI with host buffers: H2D of the step's events
+from pinned memory + cs_run + D2H of alerts and summary.
+N > 1: one process per GPU, each analysing its own instance (instances shard
+with no data-path collective: "weak" scaling); the per-shard alert lists and
+summaries are gathered to rank 0 over NCCL.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "trace events/sec analysed (1/2/4/8 B200, % HBM roofline); alert parity vs CPU"
+UNIT = "events/s"
+
+WORKLOADS = {
+    # name: (cycles, n_ranks, fault family, onset, duration, chunks, description)
+    "c2": (3_700_000, 8, "nvlink_saturation", 3_000_000, 150, 64,
+           "configs[1]: one 8-rank TP serving instance, ~100M events, mixed prefill/decode"),
+    "c1": (50_000, 1, "cpu_contention", 40_000, 150, 1,
+           "configs[0]: single decode instance, 1M events, injected stalls"),
+    "c3": (97_700, 1, None, 0, 0, 1, "configs[2] shard: 128 instances x ~1.95M events per GPU"),
+}
+
+
+def env_int(k, d):
+    try:
+        return int(os.environ.get(k, d))
+    except ValueError:
+        return d
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        fd, self.path = tempfile.mkstemp(prefix="clocks_", suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        rows = []
+        with open(self.path) as f:
+            for line in f:
+                p = [x.strip() for x in line.split(",")]
+                if len(p) >= 9:
+                    rows.append(p)
+        os.unlink(self.path)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = max(float(r[2]) for r in rows if r[2].replace(".", "").isdigit())
+        loaded = [s for s in sm if s > 0.5 * mx] or sm
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            for k, v in zip(names, r[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(k)
+        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(rows)}
+
+
+def cpu_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the reference CPU analyzer (oracle/_ref, compiled
+    unmodified from /root/reference) on this box's host cores, rank 0 only."""
+    if rank != 0:
+        return
+    from oracle import refbridge as rb
+    cores = cpu_cores()
+    line = {"impl": "reference", "metric": METRIC, "unit": UNIT, "n_gpus": args.gpus,
+            "higher_is_better": True}
+    if not rb.available():
+        line["unavailable"] = "oracle/_ref/libcsref.so not built"
+        print(json.dumps(line))
+        return
+    cyc, ranks = (100_000, 8) if args.workload == "c2" else (50_000, 1)
+    cb = rb.CpuBaseline(cores, cores, cyc, ranks, seed=42)
+    for _ in range(args.warmup):
+        cb.run()
+    times = []
+    alerts = 0
+    for _ in range(args.steps):
+        s, alerts = cb.run()
+        times.append(s)
+    ms = 1e3 * sum(times) / len(times)
+    value = cb.events / (ms / 1e3)
+    sample = (f"{cores} simkit instances x {cyc} cycles (R={ranks}, {cb.events} events), "
+              f"one instance per std::thread; segment_and_classify + build_cycle_records + "
+              f"beta cycle_stats + predict + ppe + Detector::step (fit excluded: "
+              f"{cb.fit_seconds:.2f} core-s)")
+    line.update({
+        "value": value, "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms, "scaling": "weak", "vs_baseline": None, "dtype": "int64+f64",
+        "data": "synthetic (reference simkit)",
+        "config": {"workload": WORKLOADS[args.workload][6], "sample": sample},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "alerts": alerts,
+    })
+    cb.close()
+    print(json.dumps(line))
+
+
+def make_instance(rt, workload, seed, threads):
+    cyc, ranks, fault, onset, dur, chunks, _ = WORKLOADS[workload]
+    return rt.synth_trace(cyc, seed, seed + 1, fault=fault, onset=onset, duration=dur,
+                          target_rank=3 % ranks, n_ranks=ranks, n_chunks=chunks,
+                          n_threads=threads, compact_names=False)
+
+
+def run_ours(args, rank, world, local_rank):
+    import ctypes as C
+
+    import torch
+
+    from paper_2601_09258_b200 import abi, runtime as rt
+
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    dev = local_rank
+    threads = max(1, cpu_cores() // max(1, env_int("LOCAL_WORLD_SIZE", world)))
+
+    t_setup = time.time()
+    if args.workload == "c3":
+        per_gpu = 128
+        traces = [rt.synth_trace(WORKLOADS["c3"][0], 1000 + rank * per_gpu + i,
+                                 5000 + rank * per_gpu + i, fault=rt.FAULT_FAMILIES[i % 8],
+                                 onset=80_000, duration=150, compact_names=False,
+                                 n_threads=1) for i in range(per_gpu)]
+    else:
+        traces = [make_instance(rt, args.workload, 7 + 1000 * rank, threads)]
+    names = traces[0].names
+    events = np.concatenate([t.events for t in traces]) if len(traces) > 1 else traces[0].events
+    wl_parts, offs, base = [], [0], 0
+    if len(traces) > 1:
+        evs = []
+        for t in traces:
+            ev = t.events.copy()
+            has = (ev["flags"] & abi.EV_HAS_BATCH) != 0
+            ev["payload"][has] = (ev["payload"][has] & np.uint64(0xFFFFFFFF00000000)) | \
+                ((ev["payload"][has] & np.uint64(0xFFFFFFFF)) + np.uint64(base))
+            base += len(t.workloads)
+            wl_parts.append(t.workloads)
+            evs.append(ev)
+            offs.append(offs[-1] + len(ev))
+        events = np.concatenate(evs)
+        workloads = np.concatenate(wl_parts)
+    else:
+        workloads = traces[0].workloads
+        offs = [0, len(events)]
+    n_comm = max(t.n_comm for t in traces)
+    n_events = len(events)
+    n_inst = len(offs) - 1
+    del traces
+
+    # pinned host copy (e2e leg) + resident device copy (value leg)
+    ev_bytes = events.nbytes
+    wl_bytes = workloads.nbytes
+    pin_ptr, pin = rt.host_alloc(ev_bytes + wl_bytes)
+    pin[:ev_bytes] = events.view(np.uint8)
+    pin[ev_bytes:] = workloads.view(np.uint8)
+    pin_ev = pin[:ev_bytes].view(abi.EVENT_DTYPE)
+    pin_wl = pin[ev_bytes:].view(abi.WORKLOAD_DTYPE)
+    del events
+
+    an = rt.Analyzer(dev)
+    span = rt.span_names_mask(pin_ev, len(names))
+    an.configure(names, span, n_comm_slots=n_comm)
+    an.upload(pin_ev, offs, pin_wl)
+    # setup: fit the model on the first 2400 cycles of each instance (A17, host)
+    an.run(abi.RUN_SEGMENT)
+    fit_s = 0.0
+    for i in range(n_inst):
+        recs = an.records(i)
+        tr = recs[recs["cycle_index"] < 2400]
+        x = np.stack([tr["batch"].astype(float),
+                      (tr["batch"] * (tr["input_len"] + tr["output_len"])).astype(float)], 1)
+        t0 = time.time()
+        model = rt.fit_latency_model(x, tr["latency_s"])
+        fit_s += time.time() - t0
+        an.load_model(model, inst=i)
+    setup_s = time.time() - t_setup
+
+    mask = abi.RUN_ALL
+    for _ in range(args.warmup):
+        an.run(mask)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    clocks = ClockSampler(dev)
+    clocks.start()
+    time.sleep(0.3)
+    step_ms, scan_ms, reduce_ms, launches = [], [], [], 0
+    for _ in range(args.steps):
+        an.run(mask)
+        tm = an.timings()
+        step_ms.append(tm["total"])
+        scan_ms.append(tm["scan_events"])
+        reduce_ms.append(tm["cycle_reduce"])
+        launches += an.launches()
+    torch.cuda.synchronize(dev)
+    if dist:
+        dist.barrier()
+    clk = clocks.stop()
+    dev_ms = sum(step_ms) / len(step_ms)
+
+    # e2e through the public API with host buffers
+    e2e_ms = []
+    d2h = 0
+    alerts_total = 0
+    for k in range(args.warmup + args.steps):
+        if dist:
+            dist.barrier()
+        t0 = time.perf_counter()
+        an.upload(pin_ev, offs, pin_wl)
+        an.run(mask)
+        al = [an.alerts(i) for i in range(n_inst)]
+        sums = [an.summary(i) for i in range(n_inst)]
+        payload = np.concatenate(al).view(np.uint8) if al else np.zeros(0, np.uint8)
+        if dist:
+            # final gather of per-shard alerts + summaries to rank 0 (NCCL)
+            t = torch.from_numpy(payload.copy()).cuda(dev)
+            n = torch.tensor([t.numel()], device=f"cuda:{dev}")
+            sizes = [torch.zeros_like(n) for _ in range(world)]
+            dist.all_gather(sizes, n)
+            mx = int(max(s.item() for s in sizes))
+            buf = torch.zeros(max(mx, 1), dtype=torch.uint8, device=f"cuda:{dev}")
+            buf[:t.numel()] = t
+            bufs = [torch.zeros_like(buf) for _ in range(world)]
+            dist.all_gather(bufs, buf)
+            torch.cuda.synchronize(dev)
+        el = (time.perf_counter() - t0) * 1e3
+        if k >= args.warmup:
+            e2e_ms.append(el)
+            d2h = payload.nbytes + n_inst * C.sizeof(abi.InstanceSummary)
+            alerts_total = sum(len(a) for a in al)
+    e2e = sum(e2e_ms) / len(e2e_ms)
+
+    if dist:
+        tt = torch.tensor([dev_ms, e2e], dtype=torch.float64, device=f"cuda:{dev}")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        dev_ms, e2e = float(tt[0]), float(tt[1])
+
+    # roofline: dominant kernel measured live (CUDA events on the ctx stream)
+    import json as _json
+    peaks = {}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            peaks = _json.load(f)
+    except OSError:
+        pass
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
+    summ = [an.summary(i) for i in range(n_inst)]
+    n_cycles = sum(s.n_cycles for s in summ)
+    n_records = sum(s.n_records for s in summ)
+    P, Cs, R = an.cycle.n_phases, an.cycle.n_beta_slots, an.cycle.n_comm_slots
+    # algorithmic bytes per launch
+    scan_bytes = 32 * n_events + 24 * (n_cycles + n_inst)
+    reduce_bytes = 32 * n_events + n_cycles * (48 + 2 + 4 + 8 * P + 16 * Cs + 9 * R)
+    scan_t = sum(scan_ms) / len(scan_ms)
+    red_t = sum(reduce_ms) / len(reduce_ms)
+    dom = ("cycle_reduce", reduce_bytes, red_t) if red_t >= scan_t else ("scan_events", scan_bytes, scan_t)
+    achieved = dom[1] / (dom[2] * 1e-3) / 1e9
+    path_bytes = 44.5 * n_events  # SURVEY §8d per-event figure
+    line = {
+        "metric": METRIC,
+        "value": world * n_events / (dev_ms * 1e-3),
+        "unit": UNIT,
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": dev_ms,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "int64+f64",
+        "data": "synthetic (simkit restatement, byte-identical to the reference generator per chunk)",
+        "config": {"workload": WORKLOADS[args.workload][6], "events_per_gpu": n_events,
+                   "instances_per_gpu": n_inst, "cycles_per_gpu": n_cycles,
+                   "records_per_gpu": n_records, "parallelism": f"instance-sharded x{world}",
+                   "l2": "inputs (3.2 GB/GPU) larger than L2; no flush needed",
+                   "model_fit_s": round(fit_s, 3), "setup_s": round(setup_s, 1)},
+        "roofline": {"bound": "hbm", "kernel": dom[0], "achieved": achieved, "peak": peak,
+                     "peak_source": peak_src, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": None,
+                     "kernel_ms": dom[2], "scan_events_ms": scan_t, "cycle_reduce_ms": red_t,
+                     "path_frac_44p5B_per_event": path_bytes / (dev_ms * 1e-3) / 1e9 / peak},
+        "e2e": {"value": world * n_events / (e2e * 1e-3), "unit": UNIT,
+                "h2d_bytes_per_step": ev_bytes + wl_bytes, "d2h_bytes_per_step": d2h,
+                "ms_per_step": e2e, "timer": "host wall clock around the synchronous API calls"},
+        "gpu_launches": launches,
+        "clocks": clk,
+        "alerts_per_step": alerts_total,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            from oracle import refbridge as rb
+            if rb.available():
+                cores = cpu_cores()
+                cyc, ranks = (100_000, 8) if args.workload == "c2" else (50_000, 1)
+                cb = rb.CpuBaseline(cores, cores, cyc, ranks, seed=42)
+                cb.run()
+                s, _ = cb.run()
+                line["cpu_baseline"] = {
+                    "value": cb.events / s, "unit": UNIT, "cores": cores, "kind": "reference",
+                    "sample": f"{cores} reference simkit instances x {cyc} cycles "
+                              f"(R={ranks}, {cb.events} events), one per std::thread"}
+                cb.close()
+        except Exception as e:  # the baseline must not break the bench line
+            line["cpu_baseline"] = {"value": None, "error": str(e)}
+    if rank == 0:
+        print(json.dumps(line))
+    an.close()
+    rt.host_free(pin_ptr)
+    if dist:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c2")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    rank = env_int("RANK", 0)
+    world = env_int("WORLD_SIZE", 1)
+    local_rank = env_int("LOCAL_RANK", 0)
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+    else:
+        run_ours(args, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    main()

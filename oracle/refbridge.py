@@ -61,10 +61,16 @@ def lib():
         L.ref_get_collective_beta.argtypes = [vp, vp, vp, sz, C.POINTER(sz)]
         L.ref_fit.argtypes = [C.c_uint64, C.c_uint32, C.c_char_p, vp, vp, vp, vp, vp, sz,
                               C.POINTER(sz), C.c_char_p, sz]
-        L.ref_cpu_baseline.restype = C.c_uint64
-        L.ref_cpu_baseline.argtypes = [C.c_uint32, C.c_uint32, C.c_uint64, C.c_uint64,
-                                       C.c_uint64, C.POINTER(C.c_double),
-                                       C.POINTER(C.c_uint64)]
+        L.ref_cpu_prepare.restype = vp
+        L.ref_cpu_prepare.argtypes = [C.c_uint32, C.c_uint32, C.c_uint64, C.c_uint64,
+                                      C.c_uint64]
+        L.ref_cpu_events.restype = C.c_uint64
+        L.ref_cpu_events.argtypes = [vp]
+        L.ref_cpu_fit_seconds.restype = C.c_double
+        L.ref_cpu_fit_seconds.argtypes = [vp]
+        L.ref_cpu_free.argtypes = [vp]
+        L.ref_cpu_run.restype = C.c_double
+        L.ref_cpu_run.argtypes = [vp, C.c_uint32, C.POINTER(C.c_uint64)]
         _lib = L
     return _lib
 
@@ -244,9 +250,22 @@ def ref_fit(x: np.ndarray, y: np.ndarray, feature_names, params=None, options=No
     return buf.raw[:n.value - 1].decode()
 
 
-def cpu_baseline(n_instances, n_threads, cycles_per_instance, n_ranks, seed=42):
-    """Reference CPU analyzer on `n_threads` threads; returns (events, seconds, alerts)."""
-    secs, na = C.c_double(0), C.c_uint64(0)
-    ev = lib().ref_cpu_baseline(n_instances, n_threads, cycles_per_instance, n_ranks, seed,
-                                C.byref(secs), C.byref(na))
-    return int(ev), secs.value, int(na.value)
+class CpuBaseline:
+    """Reference CPU analyzer on prepared simkit traces (one instance/thread)."""
+
+    def __init__(self, n_instances, n_threads, cycles_per_instance, n_ranks, seed=42):
+        self.n_threads = n_threads
+        self.h = lib().ref_cpu_prepare(n_instances, n_threads, cycles_per_instance, n_ranks, seed)
+        self.events = int(lib().ref_cpu_events(self.h))
+        self.fit_seconds = lib().ref_cpu_fit_seconds(self.h)
+
+    def run(self):
+        """One timed pass; returns (seconds, alerts)."""
+        na = C.c_uint64(0)
+        secs = lib().ref_cpu_run(self.h, self.n_threads, C.byref(na))
+        return secs, int(na.value)
+
+    def close(self):
+        if self.h:
+            lib().ref_cpu_free(self.h)
+            self.h = None

@@ -14,6 +14,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <cstdint>
 #include <limits>
 #include <map>
 #include <string>
@@ -51,10 +52,11 @@ struct DevBuf {
 struct PackedModel {
   uint32_t n_trees = 0, depth = 0, n_features = 0, degenerate = 0;
   std::vector<int32_t> feature_ids;
-  std::vector<double> thr, leaf;
+  std::vector<double> thr, leaf;   // leaf holds fl(lr * value)
+  std::vector<int64_t> thr_i;       // floor(thr) for exact integer compares
   std::vector<uint8_t> feat;
   double base = 0, lr = 0, floor_ = 0, mu = 0, sigma = 0;
-  DevBuf d_thr, d_leaf, d_feat;
+  DevBuf d_thr, d_thr_i, d_leaf, d_feat;
 };
 
 }  // namespace
@@ -75,7 +77,9 @@ struct cs_ctx {
   // tiles
   std::vector<uint32_t> tile_inst, inst_first_tile;
   std::vector<uint64_t> tile_begin, tile_end;
-  DevBuf d_tile_inst, d_tile_begin, d_tile_end, d_inst_first_tile, d_tile_state, d_ticket;
+  DevBuf d_tile_inst, d_tile_begin, d_tile_end, d_inst_first_tile, d_tile_cnt, d_tile_pref;
+  std::vector<uint32_t> sample_tiles;
+  DevBuf d_sample_tiles, d_redo_tiles;
   // state
   DevBuf d_stats, d_inst, d_a_pos, d_a_start, d_a_end;
   std::vector<InstState> h_inst;
@@ -155,8 +159,8 @@ DevBuffers make_buffers(cs_ctx* ctx) {
   b.n_tiles = static_cast<uint32_t>(ctx->tile_inst.size());
   b.stats = static_cast<NameStat*>(ctx->d_stats.p);
   b.inst = static_cast<InstState*>(ctx->d_inst.p);
-  b.tile_state = static_cast<unsigned long long*>(ctx->d_tile_state.p);
-  b.ticket = static_cast<unsigned int*>(ctx->d_ticket.p);
+  b.tile_cnt = static_cast<uint64_t*>(ctx->d_tile_cnt.p);
+  b.tile_pref = static_cast<uint64_t*>(ctx->d_tile_pref.p);
   b.a_pos = static_cast<uint64_t*>(ctx->d_a_pos.p);
   b.a_start = static_cast<int64_t*>(ctx->d_a_start.p);
   b.a_end = static_cast<int64_t*>(ctx->d_a_end.p);
@@ -382,9 +386,17 @@ int cs_upload(cs_ctx* ctx, uint32_t n_inst, const uint64_t* inst_offsets, const 
   auto* dtb = dev<uint64_t>(ctx->d_tile_begin, nt);
   auto* dte = dev<uint64_t>(ctx->d_tile_end, nt);
   auto* dft = dev<uint32_t>(ctx->d_inst_first_tile, n_inst);
-  if (!dti || !dtb || !dte || !dft || !dev<unsigned long long>(ctx->d_tile_state, nt) ||
-      !dev<unsigned int>(ctx->d_ticket, 1))
+  ctx->sample_tiles.clear();
+  for (size_t t = 0; t < nt; ++t)
+    if (ctx->tile_begin[t] < inst_offsets[ctx->tile_inst[t]] + kSampleEvents)
+      ctx->sample_tiles.push_back(static_cast<uint32_t>(t));
+  auto* dst = dev<uint32_t>(ctx->d_sample_tiles, ctx->sample_tiles.size());
+  if (!dti || !dtb || !dte || !dft || !dst || !dev<uint64_t>(ctx->d_tile_cnt, nt) ||
+      !dev<uint64_t>(ctx->d_tile_pref, nt + 1))
     return fail(ctx, CS_E_CUDA, "cudaMalloc(tiles)");
+  if (!ctx->sample_tiles.empty())
+    CS_CUDA(cudaMemcpyAsync(dst, ctx->sample_tiles.data(), ctx->sample_tiles.size() * 4,
+                            cudaMemcpyHostToDevice, ctx->stream));
   if (nt) {
     CS_CUDA(cudaMemcpyAsync(dti, ctx->tile_inst.data(), nt * 4, cudaMemcpyHostToDevice, ctx->stream));
     CS_CUDA(cudaMemcpyAsync(dtb, ctx->tile_begin.data(), nt * 8, cudaMemcpyHostToDevice, ctx->stream));
@@ -449,14 +461,28 @@ int cs_load_model(cs_ctx* ctx, uint32_t inst, const cs_model* m) {
   for (uint32_t t = 0; t < m->n_trees; ++t)
     fill_complete(m->nodes + m->tree_offsets[t], 0, 0, 0, D, pm->thr.data() + t * ni,
                   pm->feat.data() + t * ni, pm->leaf.data() + t * nl, nullptr);
+  // premultiplied leaves: the reference adds fl(learning_rate * value)
+  // (gbdt.cpp:178); integer thresholds: x <= t <=> x <= floor(t) for integer x
+  pm->thr_i.resize(pm->thr.size());
+  for (size_t k = 0; k < pm->thr.size(); ++k) {
+    const double t = pm->thr[k];
+    int64_t ti;
+    if (std::isnan(t) || t < -9.2e18) ti = -(int64_t{1} << 62);
+    else if (t >= 9.2e18) ti = INT64_MAX;
+    else ti = static_cast<int64_t>(std::floor(t));
+    pm->thr_i[k] = ti;
+  }
+  for (auto& v : pm->leaf) v = pm->lr * v;
   void* a = pm->d_thr.get(std::max<size_t>(8, pm->thr.size() * 8));
+  void* ai = pm->d_thr_i.get(std::max<size_t>(8, pm->thr_i.size() * 8));
   void* b = pm->d_leaf.get(std::max<size_t>(8, pm->leaf.size() * 8));
   void* c = pm->d_feat.get(std::max<size_t>(8, pm->feat.size()));
-  if (!a || !b || !c) {
+  if (!a || !ai || !b || !c) {
     delete pm;
     return fail(ctx, CS_E_CUDA, "cudaMalloc(model)");
   }
   if (!pm->thr.empty()) cudaMemcpy(a, pm->thr.data(), pm->thr.size() * 8, cudaMemcpyHostToDevice);
+  if (!pm->thr_i.empty()) cudaMemcpy(ai, pm->thr_i.data(), pm->thr_i.size() * 8, cudaMemcpyHostToDevice);
   if (!pm->leaf.empty()) cudaMemcpy(b, pm->leaf.data(), pm->leaf.size() * 8, cudaMemcpyHostToDevice);
   if (!pm->feat.empty()) cudaMemcpy(c, pm->feat.data(), pm->feat.size(), cudaMemcpyHostToDevice);
   ctx->model_store.push_back(pm);
@@ -567,15 +593,16 @@ int cs_run(cs_ctx* ctx, uint32_t mask) {
   if (hint == -1) {
     // speculative anchor from a sample of every instance
     if (stats_bytes) CS_CUDA(cudaMemsetAsync(d_stats, 0, stats_bytes, s));
-    launch_scan_events(b, cfg, 1, true, s, &ctx->launches);
+    launch_scan_events(b, cfg, 1, true, static_cast<const uint32_t*>(ctx->d_sample_tiles.p),
+                       static_cast<uint32_t>(ctx->sample_tiles.size()), s, &ctx->launches);
     launch_rank(b, cfg, 0, s, &ctx->launches);
   }
   if (stats_bytes) CS_CUDA(cudaMemsetAsync(d_stats, 0, stats_bytes, s));
-  CS_CUDA(cudaMemsetAsync(ctx->d_tile_state.p, 0, std::max<size_t>(1, nt) * 8, s));
-  CS_CUDA(cudaMemsetAsync(ctx->d_ticket.p, 0, 4, s));
+  CS_CUDA(cudaMemsetAsync(ctx->d_tile_cnt.p, 0, std::max<size_t>(1, nt) * 8, s));
   const int e1 = record_event(ctx, 1);
-  launch_scan_events(b, cfg, 3, false, s, &ctx->launches);
+  launch_scan_events(b, cfg, 3, false, nullptr, static_cast<uint32_t>(nt), s, &ctx->launches);
   const int e2 = record_event(ctx, 2);
+  launch_tile_prefix(b, s, &ctx->launches);
   ctx->timed.push_back({"scan_events", {e1, e2}});
   launch_rank(b, cfg, 1, s, &ctx->launches);
   CS_CUDA(cudaMemcpyAsync(ctx->h_inst.data(), d_inst, n_inst * sizeof(InstState),
@@ -640,9 +667,16 @@ int cs_run(cs_ctx* ctx, uint32_t mask) {
                             cudaMemcpyHostToDevice, s));
   }
   if (any_redo) {
-    CS_CUDA(cudaMemsetAsync(ctx->d_tile_state.p, 0, std::max<size_t>(1, nt) * 8, s));
-    CS_CUDA(cudaMemsetAsync(ctx->d_ticket.p, 0, 4, s));
-    launch_scan_events(b, cfg, 2 | 4, false, s, &ctx->launches);
+    std::vector<uint32_t> redo_tiles;
+    for (size_t t = 0; t < nt; ++t)
+      if (ctx->h_inst[ctx->tile_inst[t]].redo) redo_tiles.push_back(static_cast<uint32_t>(t));
+    auto* drt = dev<uint32_t>(ctx->d_redo_tiles, redo_tiles.size());
+    if (!drt) return fail(ctx, CS_E_CUDA, "cudaMalloc(redo)");
+    CS_CUDA(cudaMemcpyAsync(drt, redo_tiles.data(), redo_tiles.size() * 4,
+                            cudaMemcpyHostToDevice, s));
+    launch_scan_events(b, cfg, 2 | 4, false, drt, static_cast<uint32_t>(redo_tiles.size()), s,
+                       &ctx->launches);
+    launch_tile_prefix(b, s, &ctx->launches);
     CS_CUDA(cudaMemcpyAsync(ctx->h_inst.data(), d_inst, n_inst * sizeof(InstState),
                             cudaMemcpyDeviceToHost, s));
     CS_CUDA(cudaStreamSynchronize(s));
@@ -737,9 +771,10 @@ int cs_run(cs_ctx* ctx, uint32_t mask) {
       dm.ucl = ctx->ctl.strategy == CS_DYNAMIC_WINDOW ? ucl_from_stats_host(pm->mu, pm->sigma, ctx->ctl)
                                                       : ctx->ctl.fixed_threshold;
       dm.thr = static_cast<const double*>(pm->d_thr.p);
+      dm.thr_i = static_cast<const long long*>(pm->d_thr_i.p);
       dm.leaf = static_cast<const double*>(pm->d_leaf.p);
       dm.feat = static_cast<const uint8_t*>(pm->d_feat.p);
-      dm.smem_bytes = static_cast<uint64_t>(pm->thr.size()) * 8 + pm->leaf.size() * 8 +
+      dm.smem_bytes = static_cast<uint64_t>(pm->thr_i.size()) * 8 + pm->leaf.size() * 8 +
                       pm->feat.size();
     }
     auto* dm = dev<DevModel>(ctx->d_models, n_inst);
@@ -949,55 +984,15 @@ int cs_get_collective_beta(cs_ctx* ctx, uint32_t inst, double* beta, uint8_t* pr
 namespace {
 
 int gather_records(cs_ctx* ctx, uint32_t inst, uint64_t r0, uint64_t nr, cs_record* out) {
-  std::vector<uint64_t> rc;
-  std::vector<double> pr, re, stt;
-  std::vector<uint8_t> fl;
-  int rcode;
-  if ((rcode = d2h(ctx, rc, ctx->rec_cycle, r0, nr))) return rcode;
+  if (!nr) return CS_OK;
+  auto* d = dev<cs_record>(ctx->d_scratch, nr);
+  if (!d) return fail(ctx, CS_E_CUDA, "cudaMalloc(gather)");
+  DevConfig cfg{ctx->cyc, ctx->ctl, 0.0};
   const bool scored = ctx->last_mask & (CS_RUN_SCORE | CS_RUN_DETECT);
   const bool det = ctx->last_mask & CS_RUN_DETECT;
-  if (scored && ((rcode = d2h(ctx, pr, ctx->rec_pred, r0, nr)) ||
-                 (rcode = d2h(ctx, re, ctx->rec_resid, r0, nr))))
-    return rcode;
-  if (det && ((rcode = d2h(ctx, stt, ctx->rec_stat, r0, nr)) ||
-              (rcode = d2h(ctx, fl, ctx->rec_flags, r0, nr))))
-    return rcode;
-  const uint64_t c0 = ctx->cyc_off[inst], nc = ctx->cyc_off[inst + 1] - c0;
-  std::vector<int64_t> st, en, comp;
-  std::vector<uint8_t> sg;
-  std::vector<int32_t> wl;
-  if ((rcode = d2h(ctx, st, ctx->c_start, c0, nc)) || (rcode = d2h(ctx, en, ctx->c_end, c0, nc)) ||
-      (rcode = d2h(ctx, sg, ctx->c_stage, c0, nc)) || (rcode = d2h(ctx, wl, ctx->c_wl, c0, nc)))
-    return rcode;
-  const int P = ctx->cyc.n_phases, lat = ctx->cyc.latency_phase;
-  if (lat >= 0 && (rcode = d2h(ctx, comp, ctx->c_comp, c0 * P, nc * P))) return rcode;
-  std::vector<cs_workload> wls;
-  if ((rcode = d2h(ctx, wls, ctx->d_wl, 0, ctx->n_wl))) return rcode;
-  for (uint64_t k = 0; k < nr; ++k) {
-    const uint64_t c = rc[k] - c0;
-    cs_record& r = out[k];
-    std::memset(&r, 0, sizeof r);
-    r.cycle_index = c;
-    r.start_ts = st[c];
-    r.stage = sg[c];
-    const cs_workload& w = wls[wl[c]];
-    r.batch = w.batch;
-    r.input_len = w.input_len;
-    r.output_len = w.output_len;
-    int64_t target = en[c] - st[c];
-    if (lat >= 0 && comp[c * P + lat] > 0) target = comp[c * P + lat];
-    r.latency_s = static_cast<double>(target) * 1e-9;  // cycles.cpp:390
-    if (scored) {
-      r.predicted_s = pr[k];
-      r.residual = re[k];
-    }
-    if (det) {
-      r.statistic = stt[k];
-      r.armed = fl[k] & 1;
-      r.flagged = (fl[k] >> 1) & 1;
-      r.alert = (fl[k] >> 2) & 1;
-    }
-  }
+  launch_gather_records(make_buffers(ctx), cfg, inst, r0, nr, scored, det, d, ctx->stream);
+  CS_CUDA(cudaMemcpyAsync(out, d, nr * sizeof(cs_record), cudaMemcpyDeviceToHost, ctx->stream));
+  CS_CUDA(cudaStreamSynchronize(ctx->stream));
   return CS_OK;
 }
 
@@ -1026,33 +1021,24 @@ int cs_get_alerts(cs_ctx* ctx, uint32_t inst, cs_alert* buf, size_t cap, size_t*
   if (!ctx || !ctx->ran || inst >= ctx->n_inst) return CS_E_INVALID_ARGUMENT;
   if (!(ctx->last_mask & CS_RUN_DETECT)) return fail(ctx, CS_E_INVALID_ARGUMENT, "detect not run");
   const uint64_t a0 = ctx->alert_off[inst], na_all = ctx->alert_off[inst + 1] - a0;
-  std::vector<uint64_t> ar;
-  int rc;
-  if ((rc = d2h(ctx, ar, ctx->alert_rec, a0, na_all))) return rc;
-  const uint64_t r0 = ctx->rec_off[inst];
-  const uint64_t bad = ctx->h_inst[inst].first_bad_record;
+  std::vector<cs_alert> all(na_all);
+  if (na_all) {
+    auto* d = dev<cs_alert>(ctx->d_scratch, na_all);
+    if (!d) return fail(ctx, CS_E_CUDA, "cudaMalloc(alerts)");
+    DevConfig cfg{ctx->cyc, ctx->ctl, 0.0};
+    launch_gather_alerts(make_buffers(ctx), cfg, inst, a0, na_all, d, ctx->stream);
+    CS_CUDA(cudaMemcpyAsync(all.data(), d, na_all * sizeof(cs_alert), cudaMemcpyDeviceToHost,
+                            ctx->stream));
+    CS_CUDA(cudaStreamSynchronize(ctx->stream));
+  }
   // monitor_loop stops at the first NonPositiveLatency (main.cpp:162)
+  const uint64_t bad = ctx->h_inst[inst].first_bad_record;
   uint64_t na = 0;
-  while (na < na_all && ar[na] - r0 < bad) ++na;
+  while (na < na_all && all[na].record_index < bad) ++na;
   if (n) *n = na;
   if (!buf) return CS_OK;
   if (cap < na) return fail(ctx, CS_E_INVALID_ARGUMENT, "buffer too small");
-  for (uint64_t k = 0; k < na; ++k) {
-    cs_record r;
-    if ((rc = gather_records(ctx, inst, ar[k], 1, &r))) return rc;
-    cs_alert& a = buf[k];
-    std::memset(&a, 0, sizeof a);
-    a.cycle = r.cycle_index;
-    a.ts = r.start_ts;
-    a.smoothed_error = r.statistic;
-    a.limit = ctx->h_models[inst].ucl;
-    a.strategy = ctx->ctl.strategy;
-    a.batch = r.batch;
-    a.input_len = r.input_len;
-    a.output_len = r.output_len;
-    a.episode_id = k;
-    a.record_index = ar[k] - r0;
-  }
+  std::copy(all.begin(), all.begin() + na, buf);
   return CS_OK;
 }
 

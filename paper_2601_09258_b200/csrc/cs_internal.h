@@ -12,9 +12,7 @@ namespace csb {
 
 // ------------------------------------------------------------ tiling
 constexpr int kScanThreads = 256;               // 8 warps
-constexpr int kScanEvPerWarpIter = 32;
-constexpr int kScanIters = 16;                  // events per lane per tile
-constexpr int kTileEvents = kScanThreads * kScanIters;  // 4096 events = 128 KiB
+constexpr int kTileEvents = 2048;               // 64 KiB tile, one TMA bulk copy
 constexpr int kSmemNames = 1024;                // name stats staged in smem
 constexpr int kMaxPhases = 8;
 constexpr int kMaxBetaSlots = 64;
@@ -59,10 +57,11 @@ struct DevModel {
   double base, lr, floor_, mu, sigma, ucl;
   // device pointers (SoA over trees): thr[t*(2^D-1)+n], feat[t*(2^D-1)+n],
   // leaf[t*2^D+l]
-  const double* thr;
+  const double* thr;       // f64 thresholds (fallback compare path)
+  const long long* thr_i;  // floor(thr): exact compare for integer-valued x
   const uint8_t* feat;
-  const double* leaf;
-  uint64_t smem_bytes;     // bytes of thr+feat+leaf when staged
+  const double* leaf;      // fl(learning_rate * leaf value), as the reference adds
+  uint64_t smem_bytes;     // bytes of thr_i+leaf+feat when staged
 };
 
 struct DevConfig {
@@ -87,8 +86,8 @@ struct DevBuffers {
   uint32_t n_tiles;
   NameStat* stats;              // n_inst * n_names
   InstState* inst;
-  unsigned long long* tile_state;
-  unsigned int* ticket;
+  uint64_t* tile_cnt;           // anchors per tile (tile-local compaction)
+  uint64_t* tile_pref;          // exclusive prefix of tile_cnt, n_tiles+1
   // anchors (capacity = events; instance i at inst_off[i])
   uint64_t* a_pos;
   int64_t* a_start;
@@ -126,7 +125,9 @@ struct DevBuffers {
 
 // launchers (cs_kernels.cu); all asynchronous on `s`
 void launch_scan_events(const DevBuffers& b, const DevConfig& cfg, int mode, bool sample,
-                        cudaStream_t s, uint64_t* launches);
+                        const uint32_t* list, uint32_t n_list, cudaStream_t s,
+                        uint64_t* launches);
+void launch_tile_prefix(const DevBuffers& b, cudaStream_t s, uint64_t* launches);
 void launch_rank(const DevBuffers& b, const DevConfig& cfg, int final_pass, cudaStream_t s,
                  uint64_t* launches);
 void launch_fold(const DevBuffers& b, const DevConfig& cfg, const uint32_t* pairs_inst,
@@ -154,5 +155,10 @@ void launch_gpu_kernel_extent(const cs_event* ev, uint64_t begin, uint64_t end,
 void launch_freq_cycles(const cs_event* ev, uint64_t begin, uint64_t end, int64_t t0,
                         int64_t period, uint64_t n, uint64_t cyc_base, const DevBuffers& b,
                         uint32_t inst, cudaStream_t s, uint64_t* launches);
+
+void launch_gather_records(const DevBuffers& b, const DevConfig& cfg, uint32_t inst, uint64_t r0,
+                           uint64_t nr, int scored, int det, cs_record* out, cudaStream_t s);
+void launch_gather_alerts(const DevBuffers& b, const DevConfig& cfg, uint32_t inst, uint64_t a0,
+                          uint64_t na, cs_alert* out, cudaStream_t s);
 
 }  // namespace csb

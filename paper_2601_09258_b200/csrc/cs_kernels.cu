@@ -112,57 +112,119 @@ __device__ __forceinline__ void square_u128(i64 d, u64& lo, u64& hi) {
   hi = __umul64hi(a, a);
 }
 
-// warp-parallel decoupled look-back (Merrill & Garland) over one instance's
-// tiles; returns the exclusive prefix.  Must be called by a full warp.
-__device__ u64 lookback_warp(u64* state, uint32_t tile, uint32_t first_tile, u64 agg) {
-  const int lane = threadIdx.x & 31;
-  if (tile == first_tile) {
-    if (lane == 0) st_release(&state[tile], kFlagPrefix | agg);
-    return 0;
-  }
-  if (lane == 0) st_release(&state[tile], kFlagAgg | agg);
-  u64 excl = 0;
-  i64 j = (i64)tile - 1 - lane;
-  while (true) {
-    const bool in = j >= (i64)first_tile;
-    u64 s = 0;
-    if (in) {
-      do {
-        s = ld_acquire(&state[j]);
-      } while ((s >> 62) == 0);
-    }
-    const uint32_t pmask = __ballot_sync(0xffffffffu, !in || (s >> 62) == 2);
-    const int stop = pmask ? __ffs(pmask) - 1 : 32;
-    u64 v = (in && lane <= stop) ? (s & kValMask) : 0;
-    excl += warp_sum_u64(v);
-    if (pmask) break;
-    j -= 32;
-  }
-  if (lane == 0) st_release(&state[tile], kFlagPrefix | (excl + agg));
-  return excl;
+// ------------------------------------------------ TMA bulk-copy pipeline
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_fence_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// 1-D TMA: global -> shared, completion reported as tx bytes on `bar`
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ Ev ev_from_smem(const cs_event* p) {
+  const int4* q = reinterpret_cast<const int4*>(p);
+  const int4 a = q[0];
+  const int4 b = q[1];
+  Ev e;
+  e.start = (i64)(((u64)(uint32_t)a.y << 32) | (uint32_t)a.x);
+  e.dur = (i64)(((u64)(uint32_t)a.w << 32) | (uint32_t)a.z);
+  e.name = (uint32_t)b.x;
+  e.kind = (uint32_t)b.y & 0xffu;
+  e.cat = ((uint32_t)b.y >> 8) & 0xffu;
+  e.flags = (uint32_t)b.y >> 16;
+  e.payload = ((u64)(uint32_t)b.w << 32) | (uint32_t)b.z;
+  return e;
 }
 
 // --------------------------------------------------- K1 / K12 event scan
-// mode bit 0: name moments; bit 1: anchor compaction for inst[].guess
-// (or inst[].anchor when bit 2 "redo" is set: only instances with redo).
-__global__ void __launch_bounds__(kScanThreads)
-    k_scan_events(DevBuffers b, int mode, int sample) {
+// Persistent CTAs stream instance-aligned tiles of 2048 events (64 KiB)
+// through a kStages-deep ring of TMA bulk copies, so ~kStages x 64 KiB per SM
+// are in flight.  Per tile:
+//   mode bit 0: exact per-(instance, name) moments of PythonCall spans
+//               (count, sum d, sum d^2 as u128) in shared memory, flushed to
+//               global atomics when the CTA moves to another instance;
+//   mode bit 1: anchor occurrences (Spans named inst[].guess, or inst[].anchor
+//               with bit 2) compacted tile-locally: a_*[tile_begin + rank] and
+//               tile_cnt[t]; a prefix over tile_cnt (k_scan_exclusive) then
+//               gives every anchor its instance-global rank.
+constexpr int kStages = 3;
+constexpr uint32_t kTileBytes = kTileEvents * sizeof(cs_event);
+
+__device__ void flush_name_stats(NameStat* g, uint32_t nn, const uint32_t* s_cnt,
+                                 const uint32_t* s_spn, const u64* s_sum, const u64* s_lo,
+                                 const u64* s_hi) {
+  for (uint32_t i = threadIdx.x; i < nn; i += blockDim.x) {
+    if (!s_spn[i]) continue;
+    atomicAdd(&g[i].span_count, (u64)s_spn[i]);
+    if (s_cnt[i]) {
+      atomicAdd(&g[i].count, (u64)s_cnt[i]);
+      atomicAdd(&g[i].sum, s_sum[i]);
+      atomic_add_u128(&g[i].sumsq_lo, &g[i].sumsq_hi, s_lo[i], s_hi[i]);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kScanThreads, 1)
+    k_scan_events(DevBuffers b, int mode, const uint32_t* __restrict__ list, uint32_t n_list,
+                  int sample) {
+  extern __shared__ __align__(128) unsigned char s_tiles[];
+  __shared__ uint64_t s_bar[kStages];
   __shared__ uint32_t s_cnt[kSmemNames];
   __shared__ uint32_t s_spn[kSmemNames];
   __shared__ u64 s_sum[kSmemNames];
   __shared__ u64 s_sq_lo[kSmemNames];
   __shared__ u64 s_sq_hi[kSmemNames];
-  __shared__ uint32_t s_tile;
   __shared__ uint32_t s_warp_cnt[kScanThreads / 32];
-  __shared__ u64 s_excl;
 
   const bool do_stats = mode & 1;
   const bool do_anchor = (mode & 2) && !sample;
   const bool redo = mode & 4;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-
-  if (threadIdx.x == 0) s_tile = do_anchor ? atomicAdd(b.ticket, 1u) : blockIdx.x;
   const uint32_t nn = b.n_names < (uint32_t)kSmemNames ? b.n_names : (uint32_t)kSmemNames;
+  const uint32_t G = gridDim.x;
+
+  auto tile_of = [&](uint32_t k) { return list ? list[k] : k; };
+  auto tile_span = [&](uint32_t t, u64& tb, u64& te) {
+    tb = b.tile_begin[t];
+    te = b.tile_end[t];
+    if (sample) {
+      const u64 lim = b.inst_off[b.tile_inst[t]] + kSampleEvents;
+      te = te < lim ? te : lim;
+      if (te < tb) te = tb;
+    }
+  };
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) mbar_init(&s_bar[s], 1);
+    mbar_fence_init();
+  }
   if (do_stats)
     for (uint32_t i = threadIdx.x; i < nn; i += blockDim.x) {
       s_cnt[i] = 0;
@@ -172,114 +234,146 @@ __global__ void __launch_bounds__(kScanThreads)
       s_sq_hi[i] = 0;
     }
   __syncthreads();
-  const uint32_t tile = s_tile;
-  if (tile >= b.n_tiles) return;
-  const uint32_t inst = b.tile_inst[tile];
-  const u64 tb = b.tile_begin[tile], te = b.tile_end[tile];
-  const u64 ib = b.inst_off[inst];
-  if (sample && tb >= ib + kSampleEvents) return;
-  const u64 se = sample ? min(te, ib + kSampleEvents) : te;
-
-  uint32_t anchor = 0xffffffffu;
-  bool inst_active = do_anchor;
-  if (do_anchor) {
-    const InstState& st = b.inst[inst];
-    anchor = redo ? st.anchor : st.guess;
-    if (redo && !st.redo) inst_active = false;
+  // prologue: fill the ring
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      const uint32_t k = blockIdx.x + s * G;
+      if (k >= n_list) break;
+      u64 tb, te;
+      tile_span(tile_of(k), tb, te);
+      const uint32_t bytes = (uint32_t)((te - tb) * sizeof(cs_event));
+      mbar_expect_tx(&s_bar[s], bytes);
+      if (bytes) bulk_g2s(s_tiles + s * kTileBytes, b.ev + tb, bytes, &s_bar[s]);
+    }
   }
-  NameStat* gstats = b.stats + (u64)inst * b.n_names;
+  uint32_t cur_inst = 0xffffffffu;
+  uint32_t it = 0;
+  for (uint32_t k = blockIdx.x; k < n_list; k += G, ++it) {
+    const int stage = it % kStages;
+    const uint32_t parity = (it / kStages) & 1u;
+    const uint32_t t = tile_of(k);
+    const uint32_t inst = b.tile_inst[t];
+    u64 tb, te;
+    tile_span(t, tb, te);
+    const uint32_t n = (uint32_t)(te - tb);
+    if (do_stats && inst != cur_inst) {
+      if (cur_inst != 0xffffffffu) {
+        __syncthreads();
+        flush_name_stats(b.stats + (u64)cur_inst * b.n_names, nn, s_cnt, s_spn, s_sum, s_sq_lo,
+                         s_sq_hi);
+        __syncthreads();
+        for (uint32_t i = threadIdx.x; i < nn; i += blockDim.x) {
+          s_cnt[i] = 0;
+          s_spn[i] = 0;
+          s_sum[i] = 0;
+          s_sq_lo[i] = 0;
+          s_sq_hi[i] = 0;
+        }
+        __syncthreads();
+      }
+      cur_inst = inst;
+    }
+    uint32_t anchor = 0xffffffffu;
+    bool active = do_anchor;
+    if (do_anchor) {
+      const InstState& st = b.inst[inst];
+      anchor = redo ? st.anchor : st.guess;
+      if (redo && !st.redo) active = false;
+    }
+    NameStat* gstats = b.stats + (u64)inst * b.n_names;
+    mbar_wait(&s_bar[stage], parity);
+    const cs_event* tile = reinterpret_cast<const cs_event*>(s_tiles + stage * kTileBytes);
 
-  uint32_t masks[kScanIters];
-  uint32_t my_count = 0;
+    constexpr int kIt = kTileEvents / kScanThreads;  // 8 iterations of 32 events per warp
+    uint32_t masks[kIt];
+    uint32_t my = 0;
 #pragma unroll
-  for (int k = 0; k < kScanIters; ++k) {
-    const u64 j = tb + (u64)warp * (kScanIters * 32) + (u64)k * 32 + lane;
-    const bool valid = j < se;
-    bool is_anchor = false;
-    if (valid) {
-      const Ev e = load_ev_stream(b.ev + j);
-      const bool span = e.kind == CS_SPAN;
-      if (do_stats && span) {
-        const bool py = e.cat == CS_CAT_PYTHON_CALL;
-        u64 lo = 0, hi = 0;
-        if (py) square_u128(e.dur, lo, hi);
-        if (e.name < nn) {
-          atomicAdd(&s_spn[e.name], 1u);
-          if (py) {
-            atomicAdd(&s_cnt[e.name], 1u);
-            atomicAdd(&s_sum[e.name], (u64)e.dur);
-            atomic_add_u128(&s_sq_lo[e.name], &s_sq_hi[e.name], lo, hi);
-          }
-        } else {
-          NameStat* g = gstats + e.name;
-          atomicAdd(&g->span_count, 1ull);
-          if (py) {
-            atomicAdd(&g->count, 1ull);
-            atomicAdd(&g->sum, (u64)e.dur);
-            atomic_add_u128(&g->sumsq_lo, &g->sumsq_hi, lo, hi);
+    for (int j = 0; j < kIt; ++j) {
+      const uint32_t e_idx = (uint32_t)warp * (kIt * 32) + j * 32 + lane;
+      bool is_anchor = false;
+      if (e_idx < n) {
+        const Ev e = ev_from_smem(tile + e_idx);
+        const bool span = e.kind == CS_SPAN;
+        if (do_stats && span) {
+          const bool py = e.cat == CS_CAT_PYTHON_CALL;
+          u64 lo = 0, hi = 0;
+          if (py) square_u128(e.dur, lo, hi);
+          if (e.name < nn) {
+            atomicAdd(&s_spn[e.name], 1u);
+            if (py) {
+              atomicAdd(&s_cnt[e.name], 1u);
+              atomicAdd(&s_sum[e.name], (u64)e.dur);
+              atomic_add_u128(&s_sq_lo[e.name], &s_sq_hi[e.name], lo, hi);
+            }
+          } else {
+            NameStat* g = gstats + e.name;
+            atomicAdd(&g->span_count, 1ull);
+            if (py) {
+              atomicAdd(&g->count, 1ull);
+              atomicAdd(&g->sum, (u64)e.dur);
+              atomic_add_u128(&g->sumsq_lo, &g->sumsq_hi, lo, hi);
+            }
           }
         }
+        is_anchor = active && span && e.name == anchor;
       }
-      is_anchor = inst_active && span && e.name == anchor;
+      masks[j] = __ballot_sync(0xffffffffu, is_anchor);
+      my += __popc(masks[j]);
     }
-    masks[k] = __ballot_sync(0xffffffffu, is_anchor);
-    my_count += __popc(masks[k]);
-  }
-
-  if (do_anchor) {
-    if (lane == 0) s_warp_cnt[warp] = my_count;
-    __syncthreads();
-    if (warp == 0) {
-      uint32_t c = lane < kScanThreads / 32 ? s_warp_cnt[lane] : 0;
-      // inclusive scan over 8 warp counts
-      for (int o = 1; o < 8; o <<= 1) {
-        uint32_t n = __shfl_up_sync(0xffffffffu, c, o);
-        if (lane >= o) c += n;
-      }
-      const uint32_t total = __shfl_sync(0xffffffffu, c, 7);
-      if (lane < kScanThreads / 32) s_warp_cnt[lane] = c - (lane < 8 ? s_warp_cnt[lane] : 0);
-      const u64 excl = lookback_warp(b.tile_state, tile, b.inst_first_tile[inst], total);
-      if (lane == 0) {
-        s_excl = excl;
-        // last tile of the instance publishes the occurrence count
-        if (inst_active && (tile + 1 == b.n_tiles || b.tile_inst[tile + 1] != inst))
-          b.inst[inst].n_anchors = excl + total;
-      }
-    }
-    __syncthreads();
-    u64 rank = s_excl + s_warp_cnt[warp];
+    if (do_anchor) {
+      if (lane == 0) s_warp_cnt[warp] = my;
+      __syncthreads();
+      uint32_t base = 0, total = 0;
 #pragma unroll
-    for (int k = 0; k < kScanIters; ++k) {
-      const uint32_t m = masks[k];
-      if (m) {
-        if (m & (1u << lane)) {
-          const u64 j = tb + (u64)warp * (kScanIters * 32) + (u64)k * 32 + lane;
-          const u64 r = ib + rank + __popc(m & lanemask_lt());
-          const cs_event* p = b.ev + j;
-          const i64 st = p->start_ts;
-          b.a_pos[r] = j;
-          b.a_start[r] = st;
-          b.a_end[r] = st + p->duration;
+      for (int w = 0; w < kScanThreads / 32; ++w) {
+        const uint32_t c = s_warp_cnt[w];
+        base += w < warp ? c : 0;
+        total += c;
+      }
+      if (active) {
+#pragma unroll
+        for (int j = 0; j < kIt; ++j) {
+          const uint32_t m = masks[j];
+          if (m & (1u << lane)) {
+            const uint32_t e_idx = (uint32_t)warp * (kIt * 32) + j * 32 + lane;
+            const u64 r = tb + base + __popc(m & lanemask_lt());
+            const cs_event* p = tile + e_idx;
+            b.a_pos[r] = tb + e_idx;
+            b.a_start[r] = p->start_ts;
+            b.a_end[r] = p->start_ts + p->duration;
+          }
+          base += __popc(m);
         }
-        rank += __popc(m);
+        if (threadIdx.x == 0) b.tile_cnt[t] = total;
+      }
+    }
+    __syncthreads();  // every thread is done with this stage
+    if (threadIdx.x == 0) {
+      const uint32_t k2 = k + kStages * G;
+      if (k2 < n_list) {
+        u64 nb, ne;
+        tile_span(tile_of(k2), nb, ne);
+        const uint32_t bytes = (uint32_t)((ne - nb) * sizeof(cs_event));
+        fence_proxy_async();
+        mbar_expect_tx(&s_bar[stage], bytes);
+        if (bytes) bulk_g2s(s_tiles + stage * kTileBytes, b.ev + nb, bytes, &s_bar[stage]);
       }
     }
   }
-
-  if (do_stats) {
+  if (do_stats && cur_inst != 0xffffffffu) {
     __syncthreads();
-    for (uint32_t i = threadIdx.x; i < nn; i += blockDim.x) {
-      if (s_spn[i]) {
-        NameStat* g = gstats + i;
-        atomicAdd(&g->span_count, (u64)s_spn[i]);
-        if (s_cnt[i]) {
-          atomicAdd(&g->count, (u64)s_cnt[i]);
-          atomicAdd(&g->sum, s_sum[i]);
-          atomic_add_u128(&g->sumsq_lo, &g->sumsq_hi, s_sq_lo[i], s_sq_hi[i]);
-        }
-      }
-    }
+    flush_name_stats(b.stats + (u64)cur_inst * b.n_names, nn, s_cnt, s_spn, s_sum, s_sq_lo,
+                     s_sq_hi);
   }
+}
+
+// per-instance anchor counts from the tile prefix
+__global__ void k_inst_anchor_counts(DevBuffers b) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= b.n_inst) return;
+  const uint32_t t0 = b.inst_first_tile[i];
+  const uint32_t t1 = i + 1 < b.n_inst ? b.inst_first_tile[i + 1] : b.n_tiles;
+  b.inst[i].n_anchors = b.tile_pref[t1] - b.tile_pref[t0];
 }
 
 // ------------------------------------------------------------ K1r rank
@@ -462,20 +556,34 @@ __device__ __forceinline__ u64 group_start(const cs_event* ev, u64 pos, u64 begi
   return pos;
 }
 
+// anchor k of an instance -> slot in the tile-local anchor arrays
+__device__ __forceinline__ u64 anchor_slot(const DevBuffers& b, uint32_t inst, u64 k) {
+  const uint32_t t0 = b.inst_first_tile[inst];
+  const uint32_t t1 = inst + 1 < b.n_inst ? b.inst_first_tile[inst + 1] : b.n_tiles;
+  const u64 g = b.tile_pref[t0] + k;
+  uint32_t lo = t0, hi = t1;  // last t with tile_pref[t] <= g
+  while (hi - lo > 1) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (b.tile_pref[mid] <= g) lo = mid;
+    else hi = mid;
+  }
+  return b.tile_begin[lo] + (g - b.tile_pref[lo]);
+}
+
 __global__ void k_bounds(DevBuffers b) {
   const u64 g = (u64)blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= b.n_cycles) return;
   const uint32_t inst = upper_bound_u64(b.cyc_off, b.n_inst + 1, g) - 1;
   if (b.inst[inst].no_anchor) return;  // frequency-fallback cycles: k_freq_cycles
   const u64 c = g - b.cyc_off[inst];
-  const u64 base = b.inst_off[inst];
   const u64 ib = b.inst_off[inst];
-  const i64 s = b.a_start[base + c], e = b.a_start[base + c + 1];
-  const u64 p0 = b.a_pos[base + c], p1 = b.a_pos[base + c + 1];
+  const u64 s0 = anchor_slot(b, inst, c), s1 = anchor_slot(b, inst, c + 1);
+  const i64 s = b.a_start[s0], e = b.a_start[s1];
+  const u64 p0 = b.a_pos[s0], p1 = b.a_pos[s1];
   b.c_start[g] = s;
   b.c_end[g] = e;
   b.c_apos[g] = p0;
-  b.c_aend[g] = b.a_end[base + c];
+  b.c_aend[g] = b.a_end[s0];
   b.c_first[g] = group_start(b.ev, p0, ib, s);
   b.c_last[g] = group_start(b.ev, p1, ib, e);
   b.c_inst[g] = inst;
@@ -535,18 +643,35 @@ __global__ void __launch_bounds__(kReduceWarps * 32)
         if (occ && ni.beta_slot >= 0)
           atomicAdd(reinterpret_cast<u64*>(&ws.beta[ni.beta_slot]), (u64)clipped);
         // per-(name, commHash, rank) beta: doubles summed in event order
-        // (rca.cpp:108-115) -> sequential fold by lane 0 in lane order
-        uint32_t m = __ballot_sync(0xffffffffu, occ && e.cat == CS_CAT_COLLECTIVE_COMM &&
-                                                    (e.flags & CS_EV_HAS_COMM));
-        while (m) {
-          const int l = __ffs(m) - 1;
-          m &= m - 1;
-          const uint32_t slot = __shfl_sync(0xffffffffu, (uint32_t)(e.payload >> 32), l);
-          const i64 ov = __shfl_sync(0xffffffffu, clipped, l);
-          if (lane == 0 && slot < (uint32_t)R) {
-            ws.coll[slot] = __dadd_rn(ws.coll[slot], __ddiv_rn((double)ov, (double)dur));
-            ws.colln[slot] += 1;
+        // (rca.cpp:108-115).  Terms are divided in parallel; if every slot has
+        // one contributor in this chunk the adds are independent, otherwise
+        // lane 0 folds the chunk in lane (= event) order.
+        const bool coll = occ && e.cat == CS_CAT_COLLECTIVE_COMM && (e.flags & CS_EV_HAS_COMM);
+        const uint32_t m = __ballot_sync(0xffffffffu, coll);
+        if (m) {
+          const uint32_t slot = coll ? (uint32_t)(e.payload >> 32) : 0xffffffffu;
+          const double term = coll ? __ddiv_rn((double)clipped, (double)dur) : 0.0;
+          const uint32_t same = __match_any_sync(0xffffffffu, slot);
+          const bool unique = !coll || __popc(same & m) == 1;
+          if (__all_sync(0xffffffffu, unique)) {
+            if (coll && slot < (uint32_t)R) {
+              ws.coll[slot] = __dadd_rn(ws.coll[slot], term);
+              ws.colln[slot] += 1;
+            }
+          } else {
+            uint32_t mm = m;
+            while (mm) {
+              const int l = __ffs(mm) - 1;
+              mm &= mm - 1;
+              const uint32_t sl = __shfl_sync(0xffffffffu, slot, l);
+              const double tv = __shfl_sync(0xffffffffu, term, l);
+              if (lane == 0 && sl < (uint32_t)R) {
+                ws.coll[sl] = __dadd_rn(ws.coll[sl], tv);
+                ws.colln[sl] += 1;
+              }
+            }
           }
+          __syncwarp();
         }
       }
       if (!fm_found) {
@@ -795,29 +920,25 @@ __global__ void k_rec_off_tail(DevBuffers b, uint64_t* total) {
 // then ppe (detector.cpp:14-19).  Tile = 8192 records, model staged once per
 // (tile, instance).
 constexpr int kScoreThreads = 256;
-constexpr int kScoreTile = 8192;
+constexpr int kScoreILP = 4;                     // independent records per thread
+constexpr int kScoreTile = kScoreThreads * kScoreILP * 8;
 
+// Exact stand-in for `x <= thr` when x is an integer-valued double with
+// |x| <= 2^53: x <= thr  <=>  (int64)x <= floor(thr) (host-precomputed, with
+// +inf -> INT64_MAX and -inf/NaN -> a value below every such x).
 template <int NF>
-__device__ __forceinline__ double gbdt_predict(const DevModel& m, const double* __restrict__ thr,
-                                               const uint8_t* __restrict__ feat,
-                                               const double* __restrict__ leaf, const double* x) {
-  double v = m.base;
-  const int D = (int)m.depth;
-  const uint32_t ni = (1u << D) - 1, nl = 1u << D;
-  for (uint32_t t = 0; t < m.n_trees; ++t) {
-    const double* tt = thr + (u64)t * ni;
-    const uint8_t* tf = feat + (u64)t * ni;
-    uint32_t node = 0;
-    for (int d = 0; d < D; ++d) {
-      const uint32_t f = tf[node];
-      double xv = x[0];
+__device__ __forceinline__ double pick(const double (&x)[NF > 0 ? NF : 1], uint32_t f) {
+  double v = x[0];
 #pragma unroll
-      for (int k = 1; k < NF; ++k) xv = (f == (uint32_t)k) ? x[k] : xv;
-      node = 2 * node + 1 + (xv <= tt[node] ? 0u : 1u);
-    }
-    v = __dadd_rn(v, __dmul_rn(m.lr, leaf[(u64)t * nl + (node - ni)]));
-  }
-  return m.floor_ < v ? v : m.floor_;
+  for (int k = 1; k < NF; ++k) v = (f == (uint32_t)k) ? x[k] : v;
+  return v;
+}
+template <int NF>
+__device__ __forceinline__ i64 pick_i(const i64 (&x)[NF > 0 ? NF : 1], uint32_t f) {
+  i64 v = x[0];
+#pragma unroll
+  for (int k = 1; k < NF; ++k) v = (f == (uint32_t)k) ? x[k] : v;
+  return v;
 }
 
 template <int NF>
@@ -836,59 +957,122 @@ __global__ void __launch_bounds__(kScoreThreads)
     __syncthreads();
     const uint32_t inst = s_inst;
     const u64 seg_end = min(r1, (u64)b.rec_off[inst + 1]);
-    const DevModel m = b.models[inst];
-    const double* thr = m.thr;
+    const DevModel& m = b.models[inst];
+    const uint32_t D = m.depth, NT = m.n_trees;
+    const uint32_t ni = (1u << D) - 1, nl = 1u << D;
+    const i64* thr = m.thr_i;
     const uint8_t* feat = m.feat;
     const double* leaf = m.leaf;
     if (m.smem_bytes <= smem_cap) {
-      const uint32_t ni = (1u << m.depth) - 1, nl = 1u << m.depth;
-      double* st = reinterpret_cast<double*>(s_model);
-      double* sl = st + (u64)m.n_trees * ni;
-      uint8_t* sf = reinterpret_cast<uint8_t*>(sl + (u64)m.n_trees * nl);
-      for (u64 i = threadIdx.x; i < (u64)m.n_trees * ni; i += blockDim.x) st[i] = m.thr[i];
-      for (u64 i = threadIdx.x; i < (u64)m.n_trees * nl; i += blockDim.x) sl[i] = m.leaf[i];
-      for (u64 i = threadIdx.x; i < (u64)m.n_trees * ni; i += blockDim.x) sf[i] = m.feat[i];
+      i64* st = reinterpret_cast<i64*>(s_model);
+      double* sl = reinterpret_cast<double*>(st + (u64)NT * ni);
+      uint8_t* sf = reinterpret_cast<uint8_t*>(sl + (u64)NT * nl);
+      for (u64 i = threadIdx.x; i < (u64)NT * ni; i += blockDim.x) st[i] = m.thr_i[i];
+      for (u64 i = threadIdx.x; i < (u64)NT * nl; i += blockDim.x) sl[i] = m.leaf[i];
+      for (u64 i = threadIdx.x; i < (u64)NT * ni; i += blockDim.x) sf[i] = m.feat[i];
       thr = st;
       leaf = sl;
       feat = sf;
     }
     __syncthreads();
     const u64 rb = b.rec_off[inst];
-    for (u64 k = r + threadIdx.x; k < seg_end; k += blockDim.x) {
-      const u64 g = b.rec_cycle[k];
-      const cs_workload w = b.wl[b.c_wl[g]];
-      const i64 dur = b.c_end[g] - b.c_start[g];
-      i64 target = dur;
-      if (lat >= 0) {
-        const i64 c = b.c_comp[g * P + lat];
-        if (c > 0) target = c;
-      }
-      const double y = __dmul_rn((double)target, 1e-9);
-      double x[NF > 0 ? NF : 1];
+    const double base = m.base, fl = m.floor_;
+    for (u64 k0 = r + threadIdx.x; k0 < seg_end; k0 += (u64)blockDim.x * kScoreILP) {
+      double x[kScoreILP][NF > 0 ? NF : 1];
+      i64 xi[kScoreILP][NF > 0 ? NF : 1];
+      double y[kScoreILP], v[kScoreILP];
+      bool live[kScoreILP], exact = true;
 #pragma unroll
-      for (int f = 0; f < NF; ++f) {
-        const int id = m.feature_ids[f];
-        double v;
-        switch (id) {
-          case CS_F_BATCH: v = (double)w.batch; break;
-          case CS_F_W_KV: v = (double)(w.batch * (w.input_len + w.output_len)); break;
-          case CS_F_INPUT_LEN: v = (double)w.input_len; break;
-          case CS_F_OUTPUT_LEN: v = (double)w.output_len; break;
-          default: v = b.c_stage[g] == CS_STAGE_PREFILL ? 1.0 : 0.0; break;
+      for (int q = 0; q < kScoreILP; ++q) {
+        const u64 k = k0 + (u64)q * blockDim.x;
+        live[q] = k < seg_end;
+        v[q] = base;
+        y[q] = 1.0;
+        if (!live[q]) {
+#pragma unroll
+          for (int f = 0; f < NF; ++f) {
+            x[q][f] = 0.0;
+            xi[q][f] = 0;
+          }
+          continue;
         }
-        x[f] = v;
+        const u64 g = b.rec_cycle[k];
+        const cs_workload w = b.wl[b.c_wl[g]];
+        i64 target = b.c_end[g] - b.c_start[g];
+        if (lat >= 0) {
+          const i64 c = b.c_comp[g * P + lat];
+          if (c > 0) target = c;
+        }
+        y[q] = __dmul_rn((double)target, 1e-9);  // cycles.cpp:390
+#pragma unroll
+        for (int f = 0; f < NF; ++f) {
+          i64 iv;
+          switch (m.feature_ids[f]) {
+            case CS_F_BATCH: iv = w.batch; break;
+            case CS_F_W_KV: iv = w.batch * (w.input_len + w.output_len); break;
+            case CS_F_INPUT_LEN: iv = w.input_len; break;
+            case CS_F_OUTPUT_LEN: iv = w.output_len; break;
+            default: iv = b.c_stage[g] == CS_STAGE_PREFILL ? 1 : 0; break;
+          }
+          xi[q][f] = iv;
+          x[q][f] = (double)iv;
+          exact &= (iv <= (1ll << 53)) && (iv >= -(1ll << 53));
+        }
       }
-      const double p = gbdt_predict<NF>(m, thr, feat, leaf, x);
-      double res;
-      if (!(y > 0.0)) {
-        atomicMin(reinterpret_cast<u64*>(&b.inst[inst].first_bad_record), (u64)(k - rb));
-        res = __longlong_as_double(0x7ff8000000000000ll);
+      if (exact) {
+        for (uint32_t t = 0; t < NT; ++t) {
+          const i64* tt = thr + (u64)t * ni;
+          const uint8_t* tf = feat + (u64)t * ni;
+          uint32_t node[kScoreILP];
+#pragma unroll
+          for (int q = 0; q < kScoreILP; ++q) node[q] = 0;
+          for (uint32_t d = 0; d < D; ++d) {
+#pragma unroll
+            for (int q = 0; q < kScoreILP; ++q) {
+              const uint32_t f = tf[node[q]];
+              node[q] = 2 * node[q] + 1 + (pick_i<NF>(xi[q], f) <= tt[node[q]] ? 0u : 1u);
+            }
+          }
+          const double* tl = leaf + (u64)t * nl - ni;
+#pragma unroll
+          for (int q = 0; q < kScoreILP; ++q) v[q] = __dadd_rn(v[q], tl[node[q]]);
+        }
       } else {
-        const double q = __ddiv_rn(__dsub_rn(y, p), __dadd_rn(y, eps));
-        res = 0.0 < q ? q : 0.0;
+        // values beyond 2^53: compare the rounded doubles like the reference
+        for (uint32_t t = 0; t < NT; ++t) {
+          const double* tt = m.thr + (u64)t * ni;
+          const uint8_t* tf = m.feat + (u64)t * ni;
+          uint32_t node[kScoreILP];
+#pragma unroll
+          for (int q = 0; q < kScoreILP; ++q) node[q] = 0;
+          for (uint32_t d = 0; d < D; ++d) {
+#pragma unroll
+            for (int q = 0; q < kScoreILP; ++q) {
+              const uint32_t f = tf[node[q]];
+              node[q] = 2 * node[q] + 1 + (pick<NF>(x[q], f) <= tt[node[q]] ? 0u : 1u);
+            }
+          }
+          const double* tl = m.leaf + (u64)t * nl - ni;
+#pragma unroll
+          for (int q = 0; q < kScoreILP; ++q) v[q] = __dadd_rn(v[q], tl[node[q]]);
+        }
       }
-      b.rec_pred[k] = p;
-      b.rec_resid[k] = res;
+#pragma unroll
+      for (int q = 0; q < kScoreILP; ++q) {
+        if (!live[q]) continue;
+        const u64 k = k0 + (u64)q * blockDim.x;
+        const double p = fl < v[q] ? v[q] : fl;
+        double res;
+        if (!(y[q] > 0.0)) {
+          atomicMin(reinterpret_cast<u64*>(&b.inst[inst].first_bad_record), (u64)(k - rb));
+          res = __longlong_as_double(0x7ff8000000000000ll);
+        } else {
+          const double qv = __ddiv_rn(__dsub_rn(y[q], p), __dadd_rn(y[q], eps));
+          res = 0.0 < qv ? qv : 0.0;
+        }
+        b.rec_pred[k] = p;
+        b.rec_resid[k] = res;
+      }
     }
     __syncthreads();
     r = seg_end;
@@ -972,6 +1156,77 @@ __global__ void k_detect_scatter(DevBuffers b, uint64_t n_records) {
   }
   __syncthreads();
   if (alert) b.alert_rec[b.block_tmp[blockIdx.x] + s_w[warp] + __popc(m & lanemask_lt())] = k;
+}
+
+// ------------------------------------------------------------ getters
+// Assemble AoS cs_record / cs_alert rows on the device so a getter is one D2H
+// of exactly the rows asked for.
+__global__ void k_gather_records(DevBuffers b, DevConfig cfg, uint32_t inst, uint64_t r0,
+                                 uint64_t nr, int scored, int det, cs_record* out) {
+  const u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nr) return;
+  const u64 k = r0 + i;
+  const u64 g = b.rec_cycle[k];
+  cs_record r;
+  r.cycle_index = g - b.cyc_off[inst];
+  r.start_ts = b.c_start[g];
+  r.stage = b.c_stage[g];
+  const cs_workload w = b.wl[b.c_wl[g]];
+  r.batch = w.batch;
+  r.input_len = w.input_len;
+  r.output_len = w.output_len;
+  i64 target = b.c_end[g] - b.c_start[g];
+  const int lat = cfg.cyc.latency_phase;
+  if (lat >= 0) {
+    const i64 c = b.c_comp[g * cfg.cyc.n_phases + lat];
+    if (c > 0) target = c;
+  }
+  r.latency_s = __dmul_rn((double)target, 1e-9);
+  r.predicted_s = scored ? b.rec_pred[k] : 0.0;
+  r.residual = scored ? b.rec_resid[k] : 0.0;
+  r.statistic = det ? b.rec_stat[k] : 0.0;
+  const uint8_t f = det ? b.rec_flags[k] : 0;
+  r.armed = f & 1;
+  r.flagged = (f >> 1) & 1;
+  r.alert = (f >> 2) & 1;
+  r.reserved = 0;
+  r.episode_id = 0;
+  out[i] = r;
+}
+
+__global__ void k_gather_alerts(DevBuffers b, DevConfig cfg, uint32_t inst, uint64_t a0,
+                                uint64_t na, cs_alert* out) {
+  const u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= na) return;
+  const u64 k = b.alert_rec[a0 + i];
+  const u64 g = b.rec_cycle[k];
+  const cs_workload w = b.wl[b.c_wl[g]];
+  cs_alert a;
+  a.cycle = g - b.cyc_off[inst];
+  a.ts = b.c_start[g];
+  a.smoothed_error = b.rec_stat[k];
+  a.limit = b.models[inst].ucl;
+  a.strategy = cfg.ctl.strategy;
+  a.reserved = 0;
+  a.batch = w.batch;
+  a.input_len = w.input_len;
+  a.output_len = w.output_len;
+  a.episode_id = i;
+  a.record_index = k - b.rec_off[inst];
+  out[i] = a;
+}
+
+void launch_gather_records(const DevBuffers& b, const DevConfig& cfg, uint32_t inst, uint64_t r0,
+                           uint64_t nr, int scored, int det, cs_record* out, cudaStream_t s) {
+  if (!nr) return;
+  k_gather_records<<<(unsigned)((nr + 255) / 256), 256, 0, s>>>(b, cfg, inst, r0, nr, scored,
+                                                                det, out);
+}
+
+void launch_gather_alerts(const DevBuffers& b, const DevConfig& cfg, uint32_t inst, uint64_t a0,
+                          uint64_t na, cs_alert* out, cudaStream_t s) {
+  if (!na) return;
+  k_gather_alerts<<<(unsigned)((na + 255) / 256), 256, 0, s>>>(b, cfg, inst, a0, na, out);
 }
 
 // --------------------------------------------------- frequency fallback
@@ -1064,10 +1319,29 @@ __global__ void k_freq_cycles(const cs_event* ev, uint64_t begin, uint64_t end, 
 
 // ------------------------------------------------------------ launchers
 void launch_scan_events(const DevBuffers& b, const DevConfig&, int mode, bool sample,
-                        cudaStream_t s, uint64_t* launches) {
-  if (b.n_tiles == 0) return;
-  k_scan_events<<<b.n_tiles, kScanThreads, 0, s>>>(b, mode, sample ? 1 : 0);
+                        const uint32_t* list, uint32_t n_list, cudaStream_t s,
+                        uint64_t* launches) {
+  if (n_list == 0) return;
+  static bool configured = false;
+  const int smem = kStages * (int)kTileBytes;
+  if (!configured) {
+    cudaFuncSetAttribute(k_scan_events, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    configured = true;
+  }
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const uint32_t grid = n_list < (uint32_t)sms ? n_list : (uint32_t)sms;
+  k_scan_events<<<grid, kScanThreads, smem, s>>>(b, mode, list, n_list, sample ? 1 : 0);
   ++*launches;
+}
+
+void launch_tile_prefix(const DevBuffers& b, cudaStream_t s, uint64_t* launches) {
+  cudaMemcpyAsync(b.tile_pref, b.tile_cnt, (size_t)b.n_tiles * sizeof(uint64_t),
+                  cudaMemcpyDeviceToDevice, s);
+  k_scan_exclusive<<<1, 1024, 0, s>>>(b.tile_pref, b.n_tiles, b.tile_pref + b.n_tiles);
+  k_inst_anchor_counts<<<(b.n_inst + 255) / 256, 256, 0, s>>>(b);
+  *launches += 2;
 }
 
 void launch_rank(const DevBuffers& b, const DevConfig& cfg, int final_pass, cudaStream_t s,
