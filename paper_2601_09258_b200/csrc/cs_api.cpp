@@ -57,6 +57,11 @@ struct PackedModel {
   std::vector<uint8_t> feat;
   double base = 0, lr = 0, floor_ = 0, mu = 0, sigma = 0;
   DevBuf d_thr, d_thr_i, d_leaf, d_feat;
+  // compiled ensemble (<= 2 features): distinct thresholds per feature, node
+  // ranks into them, and the per-cell prediction table built on the device
+  bool has_lut = false;
+  std::vector<double> lut_thr[2];
+  DevBuf d_lut_thr[2], d_rank, d_lut;
 };
 
 }  // namespace
@@ -485,6 +490,46 @@ int cs_load_model(cs_ctx* ctx, uint32_t inst, const cs_model* m) {
   if (!pm->thr_i.empty()) cudaMemcpy(ai, pm->thr_i.data(), pm->thr_i.size() * 8, cudaMemcpyHostToDevice);
   if (!pm->leaf.empty()) cudaMemcpy(b, pm->leaf.data(), pm->leaf.size() * 8, cudaMemcpyHostToDevice);
   if (!pm->feat.empty()) cudaMemcpy(c, pm->feat.data(), pm->feat.size(), cudaMemcpyHostToDevice);
+  // compile <= 2-feature ensembles into an exact cell table (k_lut_build)
+  constexpr uint64_t kLutMaxCells = 8ull << 20;
+  if (m->n_features >= 1 && m->n_features <= 2 && m->n_trees > 0) {
+    for (size_t k = 0; k < pm->thr.size(); ++k) {
+      const double t = pm->thr[k];
+      if (std::isfinite(t)) pm->lut_thr[pm->feat[k]].push_back(t);
+    }
+    for (auto& v : pm->lut_thr) {
+      std::sort(v.begin(), v.end());
+      v.erase(std::unique(v.begin(), v.end()), v.end());
+    }
+    const uint64_t n0 = pm->lut_thr[0].size(), n1 = pm->lut_thr[1].size();
+    const uint64_t cells = (n0 + 1) * (n1 + 1);
+    if (cells <= kLutMaxCells) {
+      std::vector<int32_t> rank(pm->thr.size());
+      for (size_t k = 0; k < pm->thr.size(); ++k) {
+        const double t = pm->thr[k];
+        if (std::isnan(t) || t == -std::numeric_limits<double>::infinity()) rank[k] = -1;
+        else if (t == std::numeric_limits<double>::infinity()) rank[k] = INT32_MAX;
+        else {
+          const auto& v = pm->lut_thr[pm->feat[k]];
+          rank[k] = static_cast<int32_t>(std::lower_bound(v.begin(), v.end(), t) - v.begin());
+        }
+      }
+      auto* d0 = static_cast<double*>(pm->d_lut_thr[0].get(std::max<uint64_t>(1, n0) * 8));
+      auto* d1 = static_cast<double*>(pm->d_lut_thr[1].get(std::max<uint64_t>(1, n1) * 8));
+      auto* dr = static_cast<int32_t*>(pm->d_rank.get(std::max<size_t>(1, rank.size()) * 4));
+      auto* dl = static_cast<double*>(pm->d_lut.get(cells * 8));
+      if (d0 && d1 && dr && dl) {
+        if (n0) cudaMemcpy(d0, pm->lut_thr[0].data(), n0 * 8, cudaMemcpyHostToDevice);
+        if (n1) cudaMemcpy(d1, pm->lut_thr[1].data(), n1 * 8, cudaMemcpyHostToDevice);
+        if (!rank.empty()) cudaMemcpy(dr, rank.data(), rank.size() * 4, cudaMemcpyHostToDevice);
+        launch_lut_build(static_cast<const uint8_t*>(pm->d_feat.p), dr,
+                         static_cast<const double*>(pm->d_leaf.p), pm->n_trees, pm->depth,
+                         pm->base, pm->floor_, static_cast<uint32_t>(n0), cells, dl,
+                         ctx->stream);
+        if (cudaStreamSynchronize(ctx->stream) == cudaSuccess) pm->has_lut = true;
+      }
+    }
+  }
   ctx->model_store.push_back(pm);
   const int id = static_cast<int>(ctx->model_store.size() - 1);
   if (inst == UINT32_MAX) {
@@ -776,6 +821,11 @@ int cs_run(cs_ctx* ctx, uint32_t mask) {
       dm.feat = static_cast<const uint8_t*>(pm->d_feat.p);
       dm.smem_bytes = static_cast<uint64_t>(pm->thr_i.size()) * 8 + pm->leaf.size() * 8 +
                       pm->feat.size();
+      dm.lut = pm->has_lut ? static_cast<const double*>(pm->d_lut.p) : nullptr;
+      for (int f = 0; f < 2; ++f) {
+        dm.lut_thr[f] = static_cast<const double*>(pm->d_lut_thr[f].p);
+        dm.lut_n[f] = static_cast<uint32_t>(pm->lut_thr[f].size());
+      }
     }
     auto* dm = dev<DevModel>(ctx->d_models, n_inst);
     if (!dm) return fail(ctx, CS_E_CUDA, "cudaMalloc(models)");

@@ -11,9 +11,9 @@
 namespace csb {
 
 // ------------------------------------------------------------ tiling
-constexpr int kScanThreads = 256;               // 8 warps
+constexpr int kScanThreads = 512;               // 16 warps
 constexpr int kTileEvents = 2048;               // 64 KiB tile, one TMA bulk copy
-constexpr int kSmemNames = 1024;                // name stats staged in smem
+constexpr int kSmemNames = 512;                 // name stats staged in smem
 constexpr int kMaxPhases = 8;
 constexpr int kMaxBetaSlots = 64;
 constexpr int kMaxCommSlots = 64;
@@ -62,6 +62,10 @@ struct DevModel {
   const uint8_t* feat;
   const double* leaf;      // fl(learning_rate * leaf value), as the reference adds
   uint64_t smem_bytes;     // bytes of thr_i+leaf+feat when staged
+  // compiled ensemble (n_features <= 2): lut[k1 * (lut_n[0]+1) + k0]
+  const double* lut;
+  const double* lut_thr[2];
+  uint32_t lut_n[2];
 };
 
 struct DevConfig {
@@ -156,6 +160,9 @@ void launch_freq_cycles(const cs_event* ev, uint64_t begin, uint64_t end, int64_
                         int64_t period, uint64_t n, uint64_t cyc_base, const DevBuffers& b,
                         uint32_t inst, cudaStream_t s, uint64_t* launches);
 
+void launch_lut_build(const uint8_t* feat, const int32_t* rank, const double* leafp,
+                      uint32_t n_trees, uint32_t D, double base, double floor_, uint32_t n0,
+                      uint64_t cells, double* lut, cudaStream_t s);
 void launch_gather_records(const DevBuffers& b, const DevConfig& cfg, uint32_t inst, uint64_t r0,
                            uint64_t nr, int scored, int det, cs_record* out, cudaStream_t s);
 void launch_gather_alerts(const DevBuffers& b, const DevConfig& cfg, uint32_t inst, uint64_t a0,

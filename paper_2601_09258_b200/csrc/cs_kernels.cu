@@ -178,18 +178,90 @@ __device__ __forceinline__ Ev ev_from_smem(const cs_event* p) {
 constexpr int kStages = 3;
 constexpr uint32_t kTileBytes = kTileEvents * sizeof(cs_event);
 
-__device__ void flush_name_stats(NameStat* g, uint32_t nn, const uint32_t* s_cnt,
-                                 const uint32_t* s_spn, const u64* s_sum, const u64* s_lo,
-                                 const u64* s_hi) {
-  for (uint32_t i = threadIdx.x; i < nn; i += blockDim.x) {
-    if (!s_spn[i]) continue;
-    atomicAdd(&g[i].span_count, (u64)s_spn[i]);
-    if (s_cnt[i]) {
-      atomicAdd(&g[i].count, (u64)s_cnt[i]);
-      atomicAdd(&g[i].sum, s_sum[i]);
-      atomic_add_u128(&g[i].sumsq_lo, &g[i].sumsq_hi, s_lo[i], s_hi[i]);
+// Per-name moments of PythonCall spans, staged per warp.  64-bit shared
+// atomics are CAS loops on sm_100a, so each warp owns a small table of
+// (name, count, sum d, sum d^2 as u128) rows: lanes holding the same name are
+// grouped with __match_any_sync, the group leader folds the group and does a
+// plain read-modify-write of its row (no other lane of the warp touches that
+// row in the same step).  Rows are claimed with a 32-bit CAS; a full table
+// spills to global atomics.  Flushed to global when the CTA changes instance.
+constexpr int kWarpNameRows = 16;
+struct WarpNameRow {
+  uint32_t name;  // 0xffffffff = free
+  uint32_t cnt;
+  u64 sum, sq_lo, sq_hi;
+};
+
+__device__ __forceinline__ void rows_zero(WarpNameRow* rows) {
+  for (int i = threadIdx.x; i < (kScanThreads / 32) * kWarpNameRows; i += blockDim.x) {
+    rows[i].name = 0xffffffffu;
+    rows[i].cnt = 0;
+    rows[i].sum = rows[i].sq_lo = rows[i].sq_hi = 0;
+  }
+}
+
+__device__ void rows_flush(NameStat* g, const WarpNameRow* rows) {
+  for (int i = threadIdx.x; i < (kScanThreads / 32) * kWarpNameRows; i += blockDim.x) {
+    const WarpNameRow r = rows[i];
+    if (r.name == 0xffffffffu || !r.cnt) continue;
+    atomicAdd(&g[r.name].count, (u64)r.cnt);
+    atomicAdd(&g[r.name].sum, r.sum);
+    atomic_add_u128(&g[r.name].sumsq_lo, &g[r.name].sumsq_hi, r.sq_lo, r.sq_hi);
+  }
+}
+
+// called by the full warp; `py` lanes contribute (name, d)
+__device__ __forceinline__ void rows_add(WarpNameRow* wrows, NameStat* g, bool py, uint32_t name,
+                                         i64 d) {
+  __syncwarp();  // previous step's row updates are visible to this step's leaders
+  const uint32_t key = py ? name : 0xffffffffu;
+  const uint32_t grp = __match_any_sync(0xffffffffu, key);
+  if (!py) return;
+  const int lane = threadIdx.x & 31;
+  const int leader = __ffs(grp) - 1;
+  u64 lo, hi;
+  square_u128(d, lo, hi);
+  u64 s = (u64)d;
+  uint32_t c = 1;
+  if (grp != (1u << lane)) {  // fold the group (all members run the same loop)
+    uint32_t rest = grp & ~(1u << leader);
+    while (rest) {
+      const int src = __ffs(rest) - 1;
+      rest &= rest - 1;
+      const u64 os = __shfl_sync(grp, s, src);
+      const u64 ol = __shfl_sync(grp, lo, src);
+      const u64 oh = __shfl_sync(grp, hi, src);
+      if (lane == leader) {
+        s += os;
+        const u64 nl = lo + ol;
+        hi += oh + (nl < lo ? 1ull : 0ull);
+        lo = nl;
+        ++c;
+      }
     }
   }
+  if (lane != leader) return;
+  int row = -1;
+  for (int i = 0; i < kWarpNameRows; ++i) {
+    const uint32_t n = wrows[i].name;
+    if (n == name) { row = i; break; }
+    if (n == 0xffffffffu) {
+      const uint32_t old = atomicCAS(&wrows[i].name, 0xffffffffu, name);
+      if (old == 0xffffffffu || old == name) { row = i; break; }
+    }
+  }
+  if (row < 0) {
+    atomicAdd(&g[name].count, (u64)c);
+    atomicAdd(&g[name].sum, s);
+    atomic_add_u128(&g[name].sumsq_lo, &g[name].sumsq_hi, lo, hi);
+    return;
+  }
+  WarpNameRow& r = wrows[row];
+  r.cnt += c;
+  r.sum += s;
+  const u64 nl = r.sq_lo + lo;
+  r.sq_hi += hi + (nl < r.sq_lo ? 1ull : 0ull);
+  r.sq_lo = nl;
 }
 
 __global__ void __launch_bounds__(kScanThreads, 1)
@@ -197,11 +269,7 @@ __global__ void __launch_bounds__(kScanThreads, 1)
                   int sample) {
   extern __shared__ __align__(128) unsigned char s_tiles[];
   __shared__ uint64_t s_bar[kStages];
-  __shared__ uint32_t s_cnt[kSmemNames];
-  __shared__ uint32_t s_spn[kSmemNames];
-  __shared__ u64 s_sum[kSmemNames];
-  __shared__ u64 s_sq_lo[kSmemNames];
-  __shared__ u64 s_sq_hi[kSmemNames];
+  __shared__ WarpNameRow s_rows[(kScanThreads / 32) * kWarpNameRows];
   __shared__ uint32_t s_warp_cnt[kScanThreads / 32];
 
   const bool do_stats = mode & 1;
@@ -210,6 +278,8 @@ __global__ void __launch_bounds__(kScanThreads, 1)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint32_t nn = b.n_names < (uint32_t)kSmemNames ? b.n_names : (uint32_t)kSmemNames;
   const uint32_t G = gridDim.x;
+  constexpr int kWarps = kScanThreads / 32;
+  constexpr int kIt = kTileEvents / kScanThreads;  // 32-event groups per warp per tile
 
   auto tile_of = [&](uint32_t k) { return list ? list[k] : k; };
   auto tile_span = [&](uint32_t t, u64& tb, u64& te) {
@@ -225,16 +295,8 @@ __global__ void __launch_bounds__(kScanThreads, 1)
     for (int s = 0; s < kStages; ++s) mbar_init(&s_bar[s], 1);
     mbar_fence_init();
   }
-  if (do_stats)
-    for (uint32_t i = threadIdx.x; i < nn; i += blockDim.x) {
-      s_cnt[i] = 0;
-      s_spn[i] = 0;
-      s_sum[i] = 0;
-      s_sq_lo[i] = 0;
-      s_sq_hi[i] = 0;
-    }
+  if (do_stats) rows_zero(s_rows);
   __syncthreads();
-  // prologue: fill the ring
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
       const uint32_t k = blockIdx.x + s * G;
@@ -259,16 +321,9 @@ __global__ void __launch_bounds__(kScanThreads, 1)
     if (do_stats && inst != cur_inst) {
       if (cur_inst != 0xffffffffu) {
         __syncthreads();
-        flush_name_stats(b.stats + (u64)cur_inst * b.n_names, nn, s_cnt, s_spn, s_sum, s_sq_lo,
-                         s_sq_hi);
+        rows_flush(b.stats + (u64)cur_inst * b.n_names, s_rows);
         __syncthreads();
-        for (uint32_t i = threadIdx.x; i < nn; i += blockDim.x) {
-          s_cnt[i] = 0;
-          s_spn[i] = 0;
-          s_sum[i] = 0;
-          s_sq_lo[i] = 0;
-          s_sq_hi[i] = 0;
-        }
+        rows_zero(s_rows);
         __syncthreads();
       }
       cur_inst = inst;
@@ -284,39 +339,29 @@ __global__ void __launch_bounds__(kScanThreads, 1)
     mbar_wait(&s_bar[stage], parity);
     const cs_event* tile = reinterpret_cast<const cs_event*>(s_tiles + stage * kTileBytes);
 
-    constexpr int kIt = kTileEvents / kScanThreads;  // 8 iterations of 32 events per warp
     uint32_t masks[kIt];
     uint32_t my = 0;
 #pragma unroll
     for (int j = 0; j < kIt; ++j) {
       const uint32_t e_idx = (uint32_t)warp * (kIt * 32) + j * 32 + lane;
-      bool is_anchor = false;
+      bool is_anchor = false, py = false;
+      uint32_t name = 0;
+      i64 d = 0;
       if (e_idx < n) {
-        const Ev e = ev_from_smem(tile + e_idx);
-        const bool span = e.kind == CS_SPAN;
-        if (do_stats && span) {
-          const bool py = e.cat == CS_CAT_PYTHON_CALL;
-          u64 lo = 0, hi = 0;
-          if (py) square_u128(e.dur, lo, hi);
-          if (e.name < nn) {
-            atomicAdd(&s_spn[e.name], 1u);
-            if (py) {
-              atomicAdd(&s_cnt[e.name], 1u);
-              atomicAdd(&s_sum[e.name], (u64)e.dur);
-              atomic_add_u128(&s_sq_lo[e.name], &s_sq_hi[e.name], lo, hi);
-            }
-          } else {
-            NameStat* g = gstats + e.name;
-            atomicAdd(&g->span_count, 1ull);
-            if (py) {
-              atomicAdd(&g->count, 1ull);
-              atomicAdd(&g->sum, (u64)e.dur);
-              atomic_add_u128(&g->sumsq_lo, &g->sumsq_hi, lo, hi);
-            }
+        const int4 h1 = reinterpret_cast<const int4*>(tile + e_idx)[1];
+        name = (uint32_t)h1.x;
+        const uint32_t kind = (uint32_t)h1.y & 0xffu;
+        const uint32_t cat = ((uint32_t)h1.y >> 8) & 0xffu;
+        if (kind == CS_SPAN) {
+          py = do_stats && cat == CS_CAT_PYTHON_CALL;
+          if (py) {
+            const int4 h0 = reinterpret_cast<const int4*>(tile + e_idx)[0];
+            d = (i64)(((u64)(uint32_t)h0.w << 32) | (uint32_t)h0.z);
           }
+          is_anchor = active && name == anchor;
         }
-        is_anchor = active && span && e.name == anchor;
       }
+      if (do_stats) rows_add(s_rows + warp * kWarpNameRows, gstats, py, name, d);
       masks[j] = __ballot_sync(0xffffffffu, is_anchor);
       my += __popc(masks[j]);
     }
@@ -325,7 +370,7 @@ __global__ void __launch_bounds__(kScanThreads, 1)
       __syncthreads();
       uint32_t base = 0, total = 0;
 #pragma unroll
-      for (int w = 0; w < kScanThreads / 32; ++w) {
+      for (int w = 0; w < kWarps; ++w) {
         const uint32_t c = s_warp_cnt[w];
         base += w < warp ? c : 0;
         total += c;
@@ -362,8 +407,7 @@ __global__ void __launch_bounds__(kScanThreads, 1)
   }
   if (do_stats && cur_inst != 0xffffffffu) {
     __syncthreads();
-    flush_name_stats(b.stats + (u64)cur_inst * b.n_names, nn, s_cnt, s_spn, s_sum, s_sq_lo,
-                     s_sq_hi);
+    rows_flush(b.stats + (u64)cur_inst * b.n_names, s_rows);
   }
 }
 
@@ -488,7 +532,7 @@ __global__ void k_rank(DevBuffers b, DevConfig cfg, int final_pass) {
     if (hint >= 0) {
       // discover_anchor with a hint (cycles.cpp:90-104): the hint wins when it
       // occurs as any Span at all
-      winner = gs[hint].span_count > 0 ? (uint32_t)hint : 0xffffffffu;
+      winner = st.n_anchors > 0 ? (uint32_t)hint : 0xffffffffu;
       amb = false;
     } else if (hint == -2) {
       winner = 0xffffffffu;
@@ -589,6 +633,25 @@ __global__ void k_bounds(DevBuffers b) {
   b.c_inst[g] = inst;
 }
 
+// arr[slot] += v over the warp without shared-memory atomics: lanes with the
+// same slot are grouped (__match_any_sync); each group's leader adds the
+// group total with a plain read-modify-write.  slot < 0: no contribution.
+__device__ __forceinline__ void warp_group_add(i64* arr, int slot, i64 v) {
+  const uint32_t grp = __match_any_sync(0xffffffffu, slot);
+  if (slot < 0) return;
+  const int lane = threadIdx.x & 31;
+  const int leader = __ffs(grp) - 1;
+  i64 acc = v;
+  uint32_t rest = grp & ~(1u << leader);
+  while (rest) {
+    const int src = __ffs(rest) - 1;
+    rest &= rest - 1;
+    const i64 o = __shfl_sync(grp, v, src);
+    if (lane == leader) acc += o;
+  }
+  if (lane == leader) arr[slot] += acc;
+}
+
 // ------------------------------------------------------ K3 cycle reduce
 constexpr int kReduceWarps = 8;
 struct WarpScratch {
@@ -636,12 +699,11 @@ __global__ void __launch_bounds__(kReduceWarps * 32)
       }
       const bool span = valid && e.kind == CS_SPAN;
       const i64 clipped = (e.start + e.dur < ce ? e.start + e.dur : ce) - e.start;
-      if (span && !no_comp && ni.phase >= 0 && clipped > 0)
-        atomicAdd(reinterpret_cast<u64*>(&ws.comp[ni.phase]), (u64)clipped);
+      warp_group_add(ws.comp, (span && !no_comp && ni.phase >= 0 && clipped > 0) ? ni.phase : -1,
+                     clipped);
       if (do_beta) {
         const bool occ = span && e.dur > 0 && clipped > 0;
-        if (occ && ni.beta_slot >= 0)
-          atomicAdd(reinterpret_cast<u64*>(&ws.beta[ni.beta_slot]), (u64)clipped);
+        warp_group_add(ws.beta, (occ && ni.beta_slot >= 0) ? ni.beta_slot : -1, clipped);
         // per-(name, commHash, rank) beta: doubles summed in event order
         // (rca.cpp:108-115).  Terms are divided in parallel; if every slot has
         // one contributor in this chunk the adds are independent, otherwise
@@ -1079,6 +1141,120 @@ __global__ void __launch_bounds__(kScoreThreads)
   }
 }
 
+// -------------------------------------------- K6' compiled-ensemble score
+// For models with <= 2 features the ensemble is piecewise constant on the
+// grid of its distinct split thresholds.  cell (k0, k1), k_f = #{T_f < x_f},
+// decides every node exactly like x <= t does (x <= T_f[j] <=> k_f <= j), so
+// a table built with the reference's sequential tree-order sum per cell is
+// bit-identical to traversing the trees (gbdt.cpp:22-30, 173-184).
+__global__ void k_lut_build(const uint8_t* __restrict__ feat, const int32_t* __restrict__ rank,
+                            const double* __restrict__ leafp, uint32_t n_trees, uint32_t D,
+                            double base, double floor_, uint32_t n0, uint64_t cells,
+                            double* __restrict__ lut) {
+  const u64 c = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= cells) return;
+  const int32_t k0 = (int32_t)(c % (n0 + 1)), k1 = (int32_t)(c / (n0 + 1));
+  const uint32_t ni = (1u << D) - 1, nl = 1u << D;
+  double v = base;
+  for (uint32_t t = 0; t < n_trees; ++t) {
+    uint32_t node = 0;
+    for (uint32_t d = 0; d < D; ++d) {
+      const uint32_t f = feat[(u64)t * ni + node];
+      const int32_t k = f == 0 ? k0 : k1;
+      node = 2 * node + 1 + (k <= rank[(u64)t * ni + node] ? 0u : 1u);
+    }
+    v = __dadd_rn(v, leafp[(u64)t * nl + (node - ni)]);
+  }
+  lut[c] = floor_ < v ? v : floor_;
+}
+
+void launch_lut_build(const uint8_t* feat, const int32_t* rank, const double* leafp,
+                      uint32_t n_trees, uint32_t D, double base, double floor_, uint32_t n0,
+                      uint64_t cells, double* lut, cudaStream_t s) {
+  k_lut_build<<<(unsigned)((cells + 127) / 128), 128, 0, s>>>(feat, rank, leafp, n_trees, D, base,
+                                                              floor_, n0, cells, lut);
+}
+
+__device__ __forceinline__ uint32_t count_less(const double* __restrict__ t, uint32_t n, double x) {
+  uint32_t lo = 0, hi = n;  // lower_bound: first t >= x
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (t[mid] < x) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+constexpr int kLutThreads = 256;
+constexpr int kLutTile = 16384;  // records per CTA
+
+__global__ void __launch_bounds__(kLutThreads)
+    k_score_lut(DevBuffers b, DevConfig cfg, uint64_t n_records, uint64_t smem_cap) {
+  extern __shared__ __align__(16) unsigned char s_thr[];
+  __shared__ uint32_t s_inst;
+  const u64 r0 = (u64)blockIdx.x * kLutTile;
+  const u64 r1 = min(r0 + (u64)kLutTile, (u64)n_records);
+  const double eps = cfg.ctl.epsilon;
+  const int lat = cfg.cyc.latency_phase;
+  const int P = cfg.cyc.n_phases;
+  u64 r = r0;
+  while (r < r1) {
+    if (threadIdx.x == 0) s_inst = upper_bound_u64(b.rec_off, b.n_inst + 1, r) - 1;
+    __syncthreads();
+    const uint32_t inst = s_inst;
+    const u64 seg_end = min(r1, (u64)b.rec_off[inst + 1]);
+    const DevModel& m = b.models[inst];
+    const uint32_t n0 = m.lut_n[0], n1 = m.lut_n[1];
+    const double* t0 = m.lut_thr[0];
+    const double* t1 = m.lut_thr[1];
+    if ((u64)(n0 + n1) * 8 <= smem_cap) {
+      double* s0 = reinterpret_cast<double*>(s_thr);
+      for (uint32_t i = threadIdx.x; i < n0; i += blockDim.x) s0[i] = t0[i];
+      for (uint32_t i = threadIdx.x; i < n1; i += blockDim.x) s0[n0 + i] = t1[i];
+      t0 = s0;
+      t1 = s0 + n0;
+    }
+    __syncthreads();
+    const u64 rb = b.rec_off[inst];
+    const int f0 = m.feature_ids[0], f1 = m.n_features > 1 ? m.feature_ids[1] : -1;
+    for (u64 k = r + threadIdx.x; k < seg_end; k += blockDim.x) {
+      const u64 g = b.rec_cycle[k];
+      const cs_workload w = b.wl[b.c_wl[g]];
+      i64 target = b.c_end[g] - b.c_start[g];
+      if (lat >= 0) {
+        const i64 c = b.c_comp[g * P + lat];
+        if (c > 0) target = c;
+      }
+      const double y = __dmul_rn((double)target, 1e-9);  // cycles.cpp:390
+      const uint8_t stage = b.c_stage[g];
+      auto fval = [&](int id) -> double {
+        switch (id) {
+          case CS_F_BATCH: return (double)w.batch;
+          case CS_F_W_KV: return (double)(w.batch * (w.input_len + w.output_len));
+          case CS_F_INPUT_LEN: return (double)w.input_len;
+          case CS_F_OUTPUT_LEN: return (double)w.output_len;
+          default: return stage == CS_STAGE_PREFILL ? 1.0 : 0.0;
+        }
+      };
+      const uint32_t k0 = count_less(t0, n0, fval(f0));
+      const uint32_t k1 = f1 >= 0 ? count_less(t1, n1, fval(f1)) : 0;
+      const double p = m.lut[(u64)k1 * (n0 + 1) + k0];
+      double res;
+      if (!(y > 0.0)) {
+        atomicMin(reinterpret_cast<u64*>(&b.inst[inst].first_bad_record), (u64)(k - rb));
+        res = __longlong_as_double(0x7ff8000000000000ll);
+      } else {
+        const double q = __ddiv_rn(__dsub_rn(y, p), __dadd_rn(y, eps));
+        res = 0.0 < q ? q : 0.0;
+      }
+      b.rec_pred[k] = p;
+      b.rec_resid[k] = res;
+    }
+    __syncthreads();
+    r = seg_end;
+  }
+}
+
 // ------------------------------------------------------------ K7 detect
 // Detector::step (detector.cpp:91-130) for every record at once:
 //   stat_t  = e_t (FixedPoint) or (sum_{u=max(0,t-W+1)}^{t} e_u, oldest first)/count
@@ -1406,14 +1582,28 @@ void launch_score(const DevBuffers& b, const DevConfig& cfg, uint64_t n_records,
                   const uint64_t*, const int*, const DevModel* h_models, cudaStream_t s,
                   uint64_t* launches) {
   if (!n_records) return;
-  // all instances share the feature count of instance 0's model in this build
-  const uint32_t nf = h_models[0].n_features;
-  uint64_t need = 0;
-  for (uint32_t i = 0; i < b.n_inst; ++i)
-    if (h_models[i].smem_bytes > need) need = h_models[i].smem_bytes;
   int dev = 0, max_optin = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  bool all_lut = true;
+  uint64_t need_lut = 0, need = 0;
+  for (uint32_t i = 0; i < b.n_inst; ++i) {
+    all_lut &= h_models[i].lut != nullptr;
+    const uint64_t nl = (uint64_t)(h_models[i].lut_n[0] + h_models[i].lut_n[1]) * 8;
+    if (nl > need_lut) need_lut = nl;
+    if (h_models[i].smem_bytes > need) need = h_models[i].smem_bytes;
+  }
+  if (all_lut) {
+    uint64_t cap = (uint64_t)max_optin - 1024;
+    if (need_lut < cap) cap = need_lut;
+    cudaFuncSetAttribute(k_score_lut, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cap);
+    const unsigned grid = (unsigned)((n_records + kLutTile - 1) / kLutTile);
+    k_score_lut<<<grid, kLutThreads, cap, s>>>(b, cfg, n_records, cap);
+    ++*launches;
+    return;
+  }
+  // all instances share the feature count of instance 0's model in this build
+  const uint32_t nf = h_models[0].n_features;
   uint64_t cap = (uint64_t)max_optin - 1024;
   if (need < cap) cap = need;
   const unsigned grid = (unsigned)((n_records + kScoreTile - 1) / kScoreTile);
