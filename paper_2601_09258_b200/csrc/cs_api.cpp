@@ -89,8 +89,13 @@ struct cs_ctx {
   DevBuf d_stats, d_inst, d_a_pos, d_a_start, d_a_end;
   std::vector<InstState> h_inst;
   // cycles
-  std::vector<uint64_t> cyc_off;
-  uint64_t n_cycles = 0;
+  std::vector<uint64_t> cyc_off;   // cycle-slot base per instance (+ total)
+  std::vector<uint64_t> n_cyc;     // cycles per instance
+  uint64_t n_cycles = 0;           // cycle slots (fused path: + one hole per instance)
+  uint64_t slot_cap = 0;
+  bool allow_fused = true;
+  bool used_fused = false;
+  DevBuf d_fstate, d_fticket, d_fcnt, d_fpref, d_fixlist, d_fixn, d_fixflags, d_foverflow;
   DevBuf d_cyc_off, c_start, c_end, c_apos, c_aend, c_first, c_last, c_inst, c_stage, c_local,
       c_wl, c_comp, c_beta_tot, c_beta, c_coll, c_coll_n;
   // records
@@ -642,11 +647,123 @@ int cs_run(cs_ctx* ctx, uint32_t mask) {
                        static_cast<uint32_t>(ctx->sample_tiles.size()), s, &ctx->launches);
     launch_rank(b, cfg, 0, s, &ctx->launches);
   }
+  const int P = ctx->cyc.n_phases, C = ctx->cyc.n_beta_slots, R = ctx->cyc.n_comm_slots;
+  auto alloc_cycles = [&](uint64_t n_slots) -> bool {
+    const size_t nc1 = std::max<uint64_t>(1, n_slots);
+    return dev<uint64_t>(ctx->d_cyc_off, n_inst + 1) && dev<int64_t>(ctx->c_start, nc1) &&
+           dev<int64_t>(ctx->c_end, nc1) && dev<uint64_t>(ctx->c_apos, nc1) &&
+           dev<int64_t>(ctx->c_aend, nc1) && dev<uint64_t>(ctx->c_first, nc1) &&
+           dev<uint64_t>(ctx->c_last, nc1) && dev<uint32_t>(ctx->c_inst, nc1) &&
+           dev<uint8_t>(ctx->c_stage, nc1) && dev<uint8_t>(ctx->c_local, nc1) &&
+           dev<int32_t>(ctx->c_wl, nc1) && dev<int64_t>(ctx->c_comp, nc1 * std::max(P, 1)) &&
+           dev<int64_t>(ctx->c_beta_tot, nc1 * std::max(C, 1)) &&
+           dev<double>(ctx->c_beta, nc1 * std::max(C, 1)) &&
+           dev<double>(ctx->c_coll, nc1 * std::max(R, 1)) &&
+           dev<uint8_t>(ctx->c_coll_n, nc1 * std::max(R, 1)) &&
+           dev<uint64_t>(ctx->d_rec_off, n_inst + 1) && dev<uint64_t>(ctx->rec_cycle, nc1) &&
+           dev<double>(ctx->rec_pred, nc1) && dev<double>(ctx->rec_resid, nc1) &&
+           dev<double>(ctx->rec_stat, nc1) && dev<uint8_t>(ctx->rec_flags, nc1) &&
+           dev<uint64_t>(ctx->alert_rec, nc1) && dev<uint64_t>(ctx->d_alert_off, n_inst + 1) &&
+           dev<uint64_t>(ctx->block_tmp, nc1 / 1024 + 16);
+  };
+  ctx->n_cyc.assign(n_inst, 0);
+  ctx->used_fused = false;
+  const std::vector<InstState> h_init = ctx->h_inst;
+  int e1 = -1, e2 = -1;
+  // ---------------- fused single pass (common case)
+  if (ctx->allow_fused) {
+    uint64_t cap = std::max<uint64_t>(ctx->slot_cap, ctx->n_ev / 8 + 1024);
+    const size_t nfix = 2 * std::max<size_t>(1, nt) + 16;
+    FusedMetaHost mh{};
+    for (int attempt = 0; attempt < 2; ++attempt) {
+      if (!alloc_cycles(cap) || !dev<unsigned long long>(ctx->d_fstate, nt) ||
+          !dev<unsigned int>(ctx->d_fticket, 1) || !dev<uint32_t>(ctx->d_fcnt, nt) ||
+          !dev<unsigned long long>(ctx->d_fpref, nt) || !dev<unsigned long long>(ctx->d_fixlist, nfix) ||
+          !dev<unsigned int>(ctx->d_fixn, 1) || !dev<uint32_t>(ctx->d_fixflags, nfix) ||
+          !dev<unsigned int>(ctx->d_foverflow, 1))
+        return fail(ctx, CS_E_CUDA, "cudaMalloc(fused)");
+      ctx->slot_cap = cap;
+      mh = FusedMetaHost{static_cast<unsigned long long*>(ctx->d_fstate.p),
+                         static_cast<unsigned int*>(ctx->d_fticket.p),
+                         static_cast<uint32_t*>(ctx->d_fcnt.p),
+                         static_cast<unsigned long long*>(ctx->d_fpref.p),
+                         static_cast<unsigned long long*>(ctx->d_fixlist.p),
+                         static_cast<unsigned int*>(ctx->d_fixn.p),
+                         static_cast<uint32_t*>(ctx->d_fixflags.p), cap,
+                         static_cast<unsigned int*>(ctx->d_foverflow.p)};
+      if (stats_bytes) CS_CUDA(cudaMemsetAsync(d_stats, 0, stats_bytes, s));
+      CS_CUDA(cudaMemsetAsync(ctx->d_fstate.p, 0, std::max<size_t>(1, nt) * 8, s));
+      CS_CUDA(cudaMemsetAsync(ctx->d_fticket.p, 0, 4, s));
+      CS_CUDA(cudaMemsetAsync(ctx->d_fixn.p, 0, 4, s));
+      CS_CUDA(cudaMemsetAsync(ctx->d_foverflow.p, 0, 4, s));
+      b = make_buffers(ctx);
+      e1 = record_event(ctx, 1);
+      if (launch_fused_segment(b, cfg, mh, (mask & CS_RUN_BETA) ? 1 : 0, s, &ctx->launches) != 0)
+        break;  // configuration too wide for the fused kernel
+      e2 = record_event(ctx, 2);
+      launch_fused_inst(b, mh, static_cast<uint64_t*>(ctx->d_cyc_off.p), s, &ctx->launches);
+      launch_rank(b, cfg, 1, s, &ctx->launches);
+      unsigned int hfix = 0, hover = 0;
+      ctx->cyc_off.assign(n_inst + 1, 0);
+      CS_CUDA(cudaMemcpyAsync(ctx->h_inst.data(), d_inst, n_inst * sizeof(InstState),
+                              cudaMemcpyDeviceToHost, s));
+      CS_CUDA(cudaMemcpyAsync(&hfix, ctx->d_fixn.p, 4, cudaMemcpyDeviceToHost, s));
+      CS_CUDA(cudaMemcpyAsync(&hover, ctx->d_foverflow.p, 4, cudaMemcpyDeviceToHost, s));
+      CS_CUDA(cudaMemcpyAsync(ctx->cyc_off.data(), ctx->d_cyc_off.p, (n_inst + 1) * 8,
+                              cudaMemcpyDeviceToHost, s));
+      CS_CUDA(cudaStreamSynchronize(s));
+      if (hover) {
+        // more anchors than slots: grow to the exact count and run again
+        cap = ctx->cyc_off[n_inst] + 1024;
+        for (uint32_t i = 0; i < n_inst; ++i) {
+          ctx->h_inst[i].n_unknown = 0;
+          ctx->h_inst[i].n_anchors = 0;
+        }
+        CS_CUDA(cudaMemcpyAsync(d_inst, ctx->h_inst.data(), n_inst * sizeof(InstState),
+                                cudaMemcpyHostToDevice, s));
+        continue;
+      }
+      bool ok = true;
+      for (uint32_t i = 0; i < n_inst; ++i) {
+        const auto& st = ctx->h_inst[i];
+        ok &= !st.ambiguous && !st.redo && !st.no_anchor;
+      }
+      if (!ok) break;
+      launch_fixup_cycles(b, cfg, mh, (mask & CS_RUN_BETA) ? 1 : 0, hfix, s, &ctx->launches);
+      ctx->n_cycles = ctx->cyc_off[n_inst];
+      for (uint32_t i = 0; i < n_inst; ++i) {
+        const auto na = ctx->h_inst[i].n_anchors;
+        ctx->n_cyc[i] = na >= 2 ? na - 1 : 0;
+      }
+      ctx->inst_status.assign(n_inst, CS_OK);
+      ctx->used_fallback.assign(n_inst, 0);
+      ctx->fallback_cycles.assign(n_inst, 0);
+      ctx->folded.assign(n_inst, {});
+      ctx->used_fused = true;
+      break;
+    }
+    if (!ctx->used_fused) {
+      // rare: restart on the general multi-kernel path
+      ctx->h_inst = h_init;
+      CS_CUDA(cudaMemcpyAsync(d_inst, ctx->h_inst.data(), n_inst * sizeof(InstState),
+                              cudaMemcpyHostToDevice, s));
+      if (hint == -1) {
+        if (stats_bytes) CS_CUDA(cudaMemsetAsync(d_stats, 0, stats_bytes, s));
+        launch_scan_events(b, cfg, 1, true, static_cast<const uint32_t*>(ctx->d_sample_tiles.p),
+                           static_cast<uint32_t>(ctx->sample_tiles.size()), s, &ctx->launches);
+        launch_rank(b, cfg, 0, s, &ctx->launches);
+      }
+    }
+  }
+  const int e_fused_end = ctx->used_fused ? record_event(ctx, 3) : -1;
+  if (ctx->used_fused) ctx->timed.push_back({"fused_segment", {e1, e2}});
+  int e4 = e_fused_end, e5 = e_fused_end;
+  if (!ctx->used_fused) {
   if (stats_bytes) CS_CUDA(cudaMemsetAsync(d_stats, 0, stats_bytes, s));
   CS_CUDA(cudaMemsetAsync(ctx->d_tile_cnt.p, 0, std::max<size_t>(1, nt) * 8, s));
-  const int e1 = record_event(ctx, 1);
+  e1 = record_event(ctx, 1);
   launch_scan_events(b, cfg, 3, false, nullptr, static_cast<uint32_t>(nt), s, &ctx->launches);
-  const int e2 = record_event(ctx, 2);
+  e2 = record_event(ctx, 2);
   launch_tile_prefix(b, s, &ctx->launches);
   ctx->timed.push_back({"scan_events", {e1, e2}});
   launch_rank(b, cfg, 1, s, &ctx->launches);
@@ -745,27 +862,11 @@ int cs_run(cs_ctx* ctx, uint32_t mask) {
       nc = st.n_anchors >= 2 ? st.n_anchors - 1 : 0;
     }
     ctx->cyc_off[i + 1] = ctx->cyc_off[i] + nc;
+    ctx->n_cyc[i] = nc;
   }
   const uint64_t n_cyc = ctx->cyc_off[n_inst];
   ctx->n_cycles = n_cyc;
-  const int P = ctx->cyc.n_phases, C = ctx->cyc.n_beta_slots, R = ctx->cyc.n_comm_slots;
-  const size_t nc1 = std::max<uint64_t>(1, n_cyc);
-  if (!dev<uint64_t>(ctx->d_cyc_off, n_inst + 1) || !dev<int64_t>(ctx->c_start, nc1) ||
-      !dev<int64_t>(ctx->c_end, nc1) || !dev<uint64_t>(ctx->c_apos, nc1) ||
-      !dev<int64_t>(ctx->c_aend, nc1) || !dev<uint64_t>(ctx->c_first, nc1) ||
-      !dev<uint64_t>(ctx->c_last, nc1) || !dev<uint32_t>(ctx->c_inst, nc1) ||
-      !dev<uint8_t>(ctx->c_stage, nc1) || !dev<uint8_t>(ctx->c_local, nc1) ||
-      !dev<int32_t>(ctx->c_wl, nc1) || !dev<int64_t>(ctx->c_comp, nc1 * std::max(P, 1)) ||
-      !dev<int64_t>(ctx->c_beta_tot, nc1 * std::max(C, 1)) ||
-      !dev<double>(ctx->c_beta, nc1 * std::max(C, 1)) ||
-      !dev<double>(ctx->c_coll, nc1 * std::max(R, 1)) ||
-      !dev<uint8_t>(ctx->c_coll_n, nc1 * std::max(R, 1)) ||
-      !dev<uint64_t>(ctx->d_rec_off, n_inst + 1) || !dev<uint64_t>(ctx->rec_cycle, nc1) ||
-      !dev<double>(ctx->rec_pred, nc1) || !dev<double>(ctx->rec_resid, nc1) ||
-      !dev<double>(ctx->rec_stat, nc1) || !dev<uint8_t>(ctx->rec_flags, nc1) ||
-      !dev<uint64_t>(ctx->alert_rec, nc1) || !dev<uint64_t>(ctx->d_alert_off, n_inst + 1) ||
-      !dev<uint64_t>(ctx->block_tmp, nc1 / 1024 + 16))
-    return fail(ctx, CS_E_CUDA, "cudaMalloc(cycles)");
+  if (!alloc_cycles(n_cyc)) return fail(ctx, CS_E_CUDA, "cudaMalloc(cycles)");
   CS_CUDA(cudaMemcpyAsync(ctx->d_cyc_off.p, ctx->cyc_off.data(), (n_inst + 1) * 8,
                           cudaMemcpyHostToDevice, s));
   b = make_buffers(ctx);
@@ -776,14 +877,16 @@ int cs_run(cs_ctx* ctx, uint32_t mask) {
       launch_freq_cycles(static_cast<const cs_event*>(ctx->d_ev.p), ctx->inst_off[i],
                          ctx->inst_off[i + 1], f_t0[i], f_period[i], ctx->fallback_cycles[i],
                          ctx->cyc_off[i], b, i, s, &ctx->launches);
-  const int e4 = record_event(ctx, 4);
+  e4 = record_event(ctx, 4);
   launch_cycle_reduce(b, cfg, (mask & CS_RUN_BETA) ? 1 : 0, s, &ctx->launches);
-  const int e5 = record_event(ctx, 5);
+  e5 = record_event(ctx, 5);
+  ctx->timed.push_back({"bounds", {e3, e4}});
+  ctx->timed.push_back({"cycle_reduce", {e4, e5}});
+  }  // legacy path
+  b = make_buffers(ctx);
   launch_stage_heuristic(b, cfg, s, &ctx->launches);
   launch_records(b, cfg, 0, s, &ctx->launches);
   const int e6 = record_event(ctx, 6);
-  ctx->timed.push_back({"bounds", {e3, e4}});
-  ctx->timed.push_back({"cycle_reduce", {e4, e5}});
   ctx->timed.push_back({"stage_records", {e5, e6}});
   ctx->rec_off.assign(n_inst + 1, 0);
   CS_CUDA(cudaMemcpyAsync(ctx->rec_off.data(), ctx->d_rec_off.p, (n_inst + 1) * 8,
@@ -876,7 +979,7 @@ int cs_get_summary(cs_ctx* ctx, uint32_t inst, cs_instance_summary* out) {
   const auto& st = ctx->h_inst[inst];
   out->anchor_name_id = ctx->used_fallback[inst] ? UINT32_MAX : st.anchor;
   out->status = ctx->inst_status[inst];
-  out->n_cycles = ctx->cyc_off[inst + 1] - ctx->cyc_off[inst];
+  out->n_cycles = ctx->n_cyc[inst];
   out->n_records = ctx->rec_off[inst + 1] - ctx->rec_off[inst];
   out->n_alerts = ctx->alert_off[inst + 1] - ctx->alert_off[inst];
   out->first_bad_record = st.first_bad_record;
@@ -951,7 +1054,7 @@ extern "C" {
 
 int cs_get_cycles(cs_ctx* ctx, uint32_t inst, cs_cycle* buf, size_t cap, size_t* n) {
   if (!ctx || !ctx->ran || inst >= ctx->n_inst) return CS_E_INVALID_ARGUMENT;
-  const uint64_t c0 = ctx->cyc_off[inst], nc = ctx->cyc_off[inst + 1] - c0;
+  const uint64_t c0 = ctx->cyc_off[inst], nc = ctx->n_cyc[inst];
   if (n) *n = nc;
   if (!buf) return CS_OK;
   if (cap < nc) return fail(ctx, CS_E_INVALID_ARGUMENT, "buffer too small");
@@ -984,7 +1087,7 @@ int cs_get_cycles(cs_ctx* ctx, uint32_t inst, cs_cycle* buf, size_t cap, size_t*
 int cs_get_components(cs_ctx* ctx, uint32_t inst, int64_t* buf, size_t cap, size_t* n) {
   if (!ctx || !ctx->ran || inst >= ctx->n_inst) return CS_E_INVALID_ARGUMENT;
   const uint64_t P = static_cast<uint64_t>(ctx->cyc.n_phases);
-  const uint64_t c0 = ctx->cyc_off[inst], nc = ctx->cyc_off[inst + 1] - c0;
+  const uint64_t c0 = ctx->cyc_off[inst], nc = ctx->n_cyc[inst];
   if (n) *n = nc * P;
   if (!buf) return CS_OK;
   if (cap < nc * P) return fail(ctx, CS_E_INVALID_ARGUMENT, "buffer too small");
@@ -998,7 +1101,7 @@ int cs_get_beta(cs_ctx* ctx, uint32_t inst, int64_t* totals, double* beta, size_
   if (!ctx || !ctx->ran || inst >= ctx->n_inst) return CS_E_INVALID_ARGUMENT;
   if (!(ctx->last_mask & CS_RUN_BETA)) return fail(ctx, CS_E_INVALID_ARGUMENT, "beta not computed");
   const uint64_t Cs = static_cast<uint64_t>(ctx->cyc.n_beta_slots);
-  const uint64_t c0 = ctx->cyc_off[inst], nc = ctx->cyc_off[inst + 1] - c0;
+  const uint64_t c0 = ctx->cyc_off[inst], nc = ctx->n_cyc[inst];
   if (n) *n = nc * Cs;
   if (cap < nc * Cs && (totals || beta)) return fail(ctx, CS_E_INVALID_ARGUMENT, "buffer too small");
   if (totals && nc * Cs)
@@ -1015,7 +1118,7 @@ int cs_get_collective_beta(cs_ctx* ctx, uint32_t inst, double* beta, uint8_t* pr
   if (!ctx || !ctx->ran || inst >= ctx->n_inst) return CS_E_INVALID_ARGUMENT;
   if (!(ctx->last_mask & CS_RUN_BETA)) return fail(ctx, CS_E_INVALID_ARGUMENT, "beta not computed");
   const uint64_t R = static_cast<uint64_t>(ctx->cyc.n_comm_slots);
-  const uint64_t c0 = ctx->cyc_off[inst], nc = ctx->cyc_off[inst + 1] - c0;
+  const uint64_t c0 = ctx->cyc_off[inst], nc = ctx->n_cyc[inst];
   if (n) *n = nc * R;
   if (cap < nc * R && (beta || present)) return fail(ctx, CS_E_INVALID_ARGUMENT, "buffer too small");
   if (beta && nc * R)
@@ -1090,6 +1193,15 @@ int cs_get_alerts(cs_ctx* ctx, uint32_t inst, cs_alert* buf, size_t cap, size_t*
   if (cap < na) return fail(ctx, CS_E_INVALID_ARGUMENT, "buffer too small");
   std::copy(all.begin(), all.begin() + na, buf);
   return CS_OK;
+}
+
+int cs_set_option(cs_ctx* ctx, int option, int64_t value) {
+  if (!ctx) return CS_E_INVALID_ARGUMENT;
+  if (option == CS_OPT_FUSED) {
+    ctx->allow_fused = value != 0;
+    return CS_OK;
+  }
+  return fail(ctx, CS_E_INVALID_ARGUMENT, "unknown option");
 }
 
 int cs_host_alloc(size_t bytes, void** out) {

@@ -12,7 +12,7 @@ namespace csb {
 
 // ------------------------------------------------------------ tiling
 constexpr int kScanThreads = 512;               // 16 warps
-constexpr int kTileEvents = 2048;               // 64 KiB tile, one TMA bulk copy
+constexpr int kTileEvents = 1024;               // 32 KiB tile, one TMA bulk copy
 constexpr int kSmemNames = 512;                 // name stats staged in smem
 constexpr int kMaxPhases = 8;
 constexpr int kMaxBetaSlots = 64;
@@ -127,6 +127,19 @@ struct DevBuffers {
   const DevModel* models;       // per instance (device array)
 };
 
+// fused single-pass segmentation state (k_fused_segment)
+struct FusedMetaHost {
+  unsigned long long* state;
+  unsigned int* ticket;
+  uint32_t* t_cnt;
+  unsigned long long* t_pref;
+  unsigned long long* fix_list;
+  unsigned int* fix_n;
+  uint32_t* fix_flags;
+  unsigned long long capacity;
+  unsigned int* overflow;
+};
+
 // launchers (cs_kernels.cu); all asynchronous on `s`
 void launch_scan_events(const DevBuffers& b, const DevConfig& cfg, int mode, bool sample,
                         const uint32_t* list, uint32_t n_list, cudaStream_t s,
@@ -163,6 +176,12 @@ void launch_freq_cycles(const cs_event* ev, uint64_t begin, uint64_t end, int64_
 void launch_lut_build(const uint8_t* feat, const int32_t* rank, const double* leafp,
                       uint32_t n_trees, uint32_t D, double base, double floor_, uint32_t n0,
                       uint64_t cells, double* lut, cudaStream_t s);
+int launch_fused_segment(const DevBuffers& b, const DevConfig& cfg, const FusedMetaHost& mh,
+                         int do_beta, cudaStream_t s, uint64_t* launches);
+void launch_fused_inst(const DevBuffers& b, const FusedMetaHost& mh, uint64_t* cyc_off,
+                       cudaStream_t s, uint64_t* launches);
+void launch_fixup_cycles(const DevBuffers& b, const DevConfig& cfg, const FusedMetaHost& mh,
+                         int do_beta, uint32_t n_fix, cudaStream_t s, uint64_t* launches);
 void launch_gather_records(const DevBuffers& b, const DevConfig& cfg, uint32_t inst, uint64_t r0,
                            uint64_t nr, int scored, int det, cs_record* out, cudaStream_t s);
 void launch_gather_alerts(const DevBuffers& b, const DevConfig& cfg, uint32_t inst, uint64_t a0,

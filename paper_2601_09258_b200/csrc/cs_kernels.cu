@@ -175,7 +175,7 @@ __device__ __forceinline__ Ev ev_from_smem(const cs_event* p) {
 //               with bit 2) compacted tile-locally: a_*[tile_begin + rank] and
 //               tile_cnt[t]; a prefix over tile_cnt (k_scan_exclusive) then
 //               gives every anchor its instance-global rank.
-constexpr int kStages = 3;
+constexpr int kStages = 6;
 constexpr uint32_t kTileBytes = kTileEvents * sizeof(cs_event);
 
 // Per-name moments of PythonCall spans, staged per warp.  64-bit shared
@@ -1491,6 +1491,484 @@ __global__ void k_freq_cycles(const cs_event* ev, uint64_t begin, uint64_t end, 
   b.c_first[g] = lower(s);
   b.c_last[g] = lower(e);
   b.c_inst[g] = inst;
+}
+
+// ==================================================== fused single pass
+// K123: ONE streaming pass over the events does what k_scan_events + k_bounds
+// + k_cycle_reduce do in three.  Tiles of 1024 events are claimed in order
+// (ticket) and TMA-prefetched kFStages deep; per tile:
+//   1. PythonCall moments (warp name rows) + anchor flags for the guess;
+//   2. decoupled look-back over the anchor counts gives the global rank P of
+//      the tile's first anchor = the global cycle slot of its cycle;
+//   3. every cycle whose two anchors and whole event range lie in the tile is
+//      reduced by ONE thread, sequentially, straight from shared memory:
+//      component durations, first forward_mode, keywords, workload carrier,
+//      beta and event-ordered collective beta (cycles.cpp:157-166, 205-281;
+//      rca.cpp:87-129);
+//   4. cycles that straddle a tile edge (~1 per tile) go to a fixup list that
+//      k_fixup_cycles reduces from global memory with the same routine.
+// Cycle slots are global anchor ranks; the last anchor of an instance owns a
+// "hole" slot (no cycle), marked c_wl = -4.
+constexpr int kFThreads = 512;
+constexpr int kFTile = 1024;
+constexpr int kFStages = 4;
+constexpr uint32_t kFTileBytes = kFTile * sizeof(cs_event);
+constexpr u64 kFlagAggF = 1ull << 62;
+constexpr u64 kFlagPrefixF = 2ull << 62;
+
+__device__ u64 lookback_global(u64* state, uint32_t tile, u64 agg) {
+  const int lane = threadIdx.x & 31;
+  if (tile == 0) {
+    if (lane == 0) st_release(&state[0], kFlagPrefixF | agg);
+    return 0;
+  }
+  if (lane == 0) st_release(&state[tile], kFlagAggF | agg);
+  u64 excl = 0;
+  i64 j = (i64)tile - 1 - lane;
+  while (true) {
+    const bool in = j >= 0;
+    u64 v = 0;
+    if (in) {
+      do {
+        v = ld_acquire(&state[j]);
+      } while ((v >> 62) == 0);
+    }
+    const uint32_t pm = __ballot_sync(0xffffffffu, !in || (v >> 62) == 2);
+    const int stop = pm ? __ffs(pm) - 1 : 32;
+    excl += warp_sum_u64((in && lane <= stop) ? (v & kValMask) : 0);
+    if (pm) break;
+    j -= 32;
+  }
+  if (lane == 0) st_release(&state[tile], kFlagPrefixF | (excl + agg));
+  return excl;
+}
+
+// Sequential per-cycle reduction by one thread over ev[first, last): the
+// reference's own loops, in event order.  Writes every per-cycle output.
+__device__ void reduce_cycle_seq(const DevBuffers& b, const DevConfig& cfg, int do_beta,
+                                 const cs_event* ev, u64 first, u64 last, u64 g, uint32_t inst,
+                                 i64 cs, i64 ce, u64 apos, i64 aend, u64 gfirst, u64 glast,
+                                 i64* comp, i64* beta, double* coll, uint32_t* colln) {
+  const int P = cfg.cyc.n_phases, C = cfg.cyc.n_beta_slots, R = cfg.cyc.n_comm_slots;
+  const i64 dur = ce - cs;
+  const bool no_comp = apos == kNone;
+  for (int i = 0; i < P; ++i) comp[i] = 0;
+  if (do_beta) {
+    for (int i = 0; i < C; ++i) beta[i] = 0;
+    for (int i = 0; i < R; ++i) {
+      coll[i] = 0.0;
+      colln[i] = 0;
+    }
+  }
+  uint32_t fm_cls = 0;
+  bool fm_found = false, pkw = false, dkw = false, batch_found = false;
+  int32_t wl = -1;
+  for (u64 j = first; j < last; ++j) {
+    const int4* q = reinterpret_cast<const int4*>(ev + j);
+    const int4 h0 = q[0], h1 = q[1];
+    const i64 st = (i64)(((u64)(uint32_t)h0.y << 32) | (uint32_t)h0.x);
+    const i64 d = (i64)(((u64)(uint32_t)h0.w << 32) | (uint32_t)h0.z);
+    const uint32_t name = (uint32_t)h1.x;
+    const uint32_t kind = (uint32_t)h1.y & 0xffu;
+    const uint32_t cat = ((uint32_t)h1.y >> 8) & 0xffu;
+    const uint32_t flags = (uint32_t)h1.y >> 16;
+    if (!fm_found && (flags & CS_EV_FM_MASK)) {
+      fm_found = true;
+      fm_cls = flags & CS_EV_FM_MASK;
+    }
+    if (!batch_found && (flags & CS_EV_HAS_BATCH)) {
+      batch_found = true;
+      wl = (flags & CS_EV_WL_OK) ? (int32_t)(uint32_t)h1.z : -2;
+    }
+    if (kind != CS_SPAN) continue;
+    const cs_name_info ni = b.names[name];
+    pkw |= (ni.flags & CS_NAME_PREFILL_KW) != 0;
+    dkw |= (ni.flags & CS_NAME_DECODE_KW) != 0;
+    const i64 end = st + d;
+    const i64 clipped = (end < ce ? end : ce) - st;
+    if (clipped <= 0) continue;
+    if (!no_comp && ni.phase >= 0) comp[ni.phase] += clipped;
+    if (do_beta && d > 0) {
+      if (ni.beta_slot >= 0) beta[ni.beta_slot] += clipped;
+      if (cat == CS_CAT_COLLECTIVE_COMM && (flags & CS_EV_HAS_COMM)) {
+        const uint32_t slot = (uint32_t)h1.w;
+        if (slot < (uint32_t)R) {
+          coll[slot] = __dadd_rn(coll[slot], __ddiv_rn((double)clipped, (double)dur));
+          colln[slot] += 1;
+        }
+      }
+    }
+  }
+  uint8_t stage = CS_STAGE_UNKNOWN;
+  if (fm_cls == CS_EV_FM_PREFILL) stage = CS_STAGE_PREFILL;
+  else if (fm_cls == CS_EV_FM_DECODE) stage = CS_STAGE_DECODE;
+  if (stage == CS_STAGE_UNKNOWN && pkw != dkw) stage = pkw ? CS_STAGE_PREFILL : CS_STAGE_DECODE;
+  b.c_start[g] = cs;
+  b.c_end[g] = ce;
+  b.c_apos[g] = apos;
+  b.c_aend[g] = aend;
+  b.c_first[g] = gfirst;
+  b.c_last[g] = glast;
+  b.c_inst[g] = inst;
+  b.c_local[g] = stage;
+  b.c_stage[g] = stage;
+  b.c_wl[g] = wl;
+  if (stage == CS_STAGE_UNKNOWN) atomicAdd(&b.inst[inst].n_unknown, 1ull);
+  for (int i = 0; i < P; ++i) b.c_comp[g * P + i] = comp[i];
+  if (do_beta) {
+    for (int i = 0; i < C; ++i) {
+      const i64 t = dur > 0 ? beta[i] : 0;
+      b.c_beta_tot[g * C + i] = t;
+      b.c_beta[g * C + i] = t > 0 ? __ddiv_rn((double)t, (double)dur) : 0.0;
+    }
+    for (int i = 0; i < R; ++i) {
+      b.c_coll[g * R + i] = coll[i];
+      b.c_coll_n[g * R + i] = (uint8_t)(colln[i] > 255 ? 255 : colln[i]);
+    }
+  }
+}
+
+struct FusedMeta {
+  u64* state;          // look-back state per tile
+  unsigned int* ticket;
+  uint32_t* t_cnt;     // anchors per tile
+  u64* t_pref;         // global rank of the tile's first anchor
+  u64* fix_list;       // cycle slots needing k_fixup_cycles
+  unsigned int* fix_n;
+  uint32_t* fix_flags; // bit0 needs end/last, bit1 needs first
+  u64 capacity;        // cycle-slot capacity
+  unsigned int* overflow;
+};
+
+__device__ __forceinline__ uint32_t scratch_words(const DevConfig& cfg) {
+  return (uint32_t)(cfg.cyc.n_phases + cfg.cyc.n_beta_slots + cfg.cyc.n_comm_slots) * 2 +
+         (uint32_t)cfg.cyc.n_comm_slots + 1;  // i64/f64 as 2 words, colln as 1
+}
+
+__global__ void __launch_bounds__(kFThreads, 1)
+    k_fused_segment(DevBuffers b, DevConfig cfg, FusedMeta fm, int do_beta,
+                    uint32_t n_cyc_threads) {
+  extern __shared__ __align__(128) unsigned char s_dyn[];
+  __shared__ uint64_t s_bar[kFStages];
+  __shared__ uint32_t s_stage_tile[kFStages];
+  __shared__ WarpNameRow s_rows[(kFThreads / 32) * kWarpNameRows];
+  __shared__ uint16_t s_apos[kFTile];
+  __shared__ i64 s_astart[kFTile];
+  __shared__ i64 s_aend[kFTile];
+  __shared__ uint32_t s_warp_cnt[kFThreads / 32];
+  __shared__ u64 s_P;
+  __shared__ uint32_t s_lead;
+
+  unsigned char* s_tiles = s_dyn;
+  uint32_t* s_scratch = reinterpret_cast<uint32_t*>(s_dyn + kFStages * kFTileBytes);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr int kWarps = kFThreads / 32;
+  constexpr int kIt = kFTile / kFThreads;  // 2 groups of 32 events per warp
+  const int P = cfg.cyc.n_phases, C = cfg.cyc.n_beta_slots, R = cfg.cyc.n_comm_slots;
+  const uint32_t sw = scratch_words(cfg);
+  // per-thread scratch: comp[P] i64 | beta[C] i64 | coll[R] f64 | colln[R] u32
+  i64* my_comp = reinterpret_cast<i64*>(s_scratch + (u64)threadIdx.x * ((sw + 1) & ~1u));
+  i64* my_beta = my_comp + P;
+  double* my_coll = reinterpret_cast<double*>(my_beta + C);
+  uint32_t* my_colln = reinterpret_cast<uint32_t*>(my_coll + R);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kFStages; ++s) mbar_init(&s_bar[s], 1);
+    mbar_fence_init();
+  }
+  rows_zero(s_rows);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kFStages; ++s) {
+      const uint32_t t = atomicAdd(fm.ticket, 1u);
+      s_stage_tile[s] = t;
+      if (t < b.n_tiles) {
+        const u64 tb = b.tile_begin[t], te = b.tile_end[t];
+        const uint32_t bytes = (uint32_t)((te - tb) * sizeof(cs_event));
+        mbar_expect_tx(&s_bar[s], bytes);
+        bulk_g2s(s_tiles + s * kFTileBytes, b.ev + tb, bytes, &s_bar[s]);
+      }
+    }
+  }
+  __syncthreads();
+  uint32_t cur_inst = 0xffffffffu;
+  for (uint32_t it = 0;; ++it) {
+    const int stage = it % kFStages;
+    const uint32_t parity = (it / kFStages) & 1u;
+    const uint32_t t = s_stage_tile[stage];
+    if (t >= b.n_tiles) break;
+    const uint32_t inst = b.tile_inst[t];
+    const u64 tb = b.tile_begin[t], te = b.tile_end[t];
+    const uint32_t n = (uint32_t)(te - tb);
+    const u64 ib = b.inst_off[inst];
+    if (inst != cur_inst) {
+      if (cur_inst != 0xffffffffu) {
+        __syncthreads();
+        rows_flush(b.stats + (u64)cur_inst * b.n_names, s_rows);
+        __syncthreads();
+        rows_zero(s_rows);
+        __syncthreads();
+      }
+      cur_inst = inst;
+    }
+    const uint32_t anchor = b.inst[inst].guess;
+    NameStat* gstats = b.stats + (u64)inst * b.n_names;
+    mbar_wait(&s_bar[stage], parity);
+    const cs_event* tile = reinterpret_cast<const cs_event*>(s_tiles + stage * kFTileBytes);
+
+    // 1. moments + anchor flags
+    uint32_t masks[kIt];
+    uint32_t my = 0;
+#pragma unroll
+    for (int j = 0; j < kIt; ++j) {
+      const uint32_t e_idx = (uint32_t)warp * (kIt * 32) + j * 32 + lane;
+      bool is_anchor = false, py = false;
+      uint32_t name = 0;
+      i64 d = 0;
+      if (e_idx < n) {
+        const int4 h1 = reinterpret_cast<const int4*>(tile + e_idx)[1];
+        name = (uint32_t)h1.x;
+        const uint32_t kind = (uint32_t)h1.y & 0xffu;
+        const uint32_t cat = ((uint32_t)h1.y >> 8) & 0xffu;
+        if (kind == CS_SPAN) {
+          py = cat == CS_CAT_PYTHON_CALL;
+          if (py) {
+            const int4 h0 = reinterpret_cast<const int4*>(tile + e_idx)[0];
+            d = (i64)(((u64)(uint32_t)h0.w << 32) | (uint32_t)h0.z);
+          }
+          is_anchor = name == anchor;
+        }
+      }
+      rows_add(s_rows + warp * kWarpNameRows, gstats, py, name, d);
+      masks[j] = __ballot_sync(0xffffffffu, is_anchor);
+      my += __popc(masks[j]);
+    }
+    if (lane == 0) s_warp_cnt[warp] = my;
+    __syncthreads();
+    uint32_t base = 0, total = 0;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) {
+      const uint32_t c = s_warp_cnt[w];
+      base += w < warp ? c : 0;
+      total += c;
+    }
+    // 2. global rank of the first anchor of this tile
+    if (warp == 0) {
+      const u64 excl = lookback_global(fm.state, t, total);
+      if (lane == 0) {
+        s_P = excl;
+        fm.t_cnt[t] = total;
+        fm.t_pref[t] = excl;
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < kIt; ++j) {
+      const uint32_t m = masks[j];
+      if (m & (1u << lane)) {
+        const uint32_t e_idx = (uint32_t)warp * (kIt * 32) + j * 32 + lane;
+        const uint32_t r = base + __popc(m & lanemask_lt());
+        const cs_event* p = tile + e_idx;
+        s_apos[r] = (uint16_t)e_idx;
+        s_astart[r] = p->start_ts;
+        s_aend[r] = p->start_ts + p->duration;
+      }
+      base += __popc(m);
+    }
+    __syncthreads();
+    const u64 P0 = s_P;
+    if (P0 + total > fm.capacity) {
+      if (threadIdx.x == 0) atomicOr(fm.overflow, 1u);
+    } else if (total > 0) {
+      // lead boundary: the first anchor's equal-start group begins before the tile
+      if (threadIdx.x == 0) {
+        uint32_t p0 = s_apos[0];
+        while (p0 > 0 && tile[p0 - 1].start_ts == s_astart[0]) --p0;
+        s_lead = (p0 == 0 && tb > ib && b.ev[tb - 1].start_ts == s_astart[0]) ? 1u : 0u;
+      }
+      __syncthreads();
+      // 3. local cycles: anchors k and k+1 in the tile
+      for (uint32_t k = threadIdx.x; k < total; k += blockDim.x) {
+        const u64 g = P0 + k;
+        const bool trailing = k + 1 == total;
+        const bool lead = k == 0 && s_lead;
+        const i64 cs = s_astart[k];
+        const u64 apos = tb + s_apos[k];
+        if (trailing || lead) {
+          // k_fixup_cycles completes it; record what is known
+          b.c_start[g] = cs;
+          b.c_apos[g] = apos;
+          b.c_aend[g] = s_aend[k];
+          b.c_inst[g] = inst;
+          if (!trailing) {
+            b.c_end[g] = s_astart[k + 1];
+            uint32_t pl = s_apos[k + 1];
+            while (pl > 0 && tile[pl - 1].start_ts == s_astart[k + 1]) --pl;
+            b.c_last[g] = tb + pl;
+          }
+          const unsigned int slot = atomicAdd(fm.fix_n, 1u);
+          fm.fix_list[slot] = g;
+          fm.fix_flags[slot] = (trailing ? 1u : 0u) | (lead ? 2u : 0u);
+        }
+      }
+      for (uint32_t k = threadIdx.x; k + 1 < total; k += n_cyc_threads) {
+        if (threadIdx.x >= n_cyc_threads) break;
+        if (k == 0 && s_lead) continue;
+        const u64 g = P0 + k;
+        const i64 cs = s_astart[k], ce = s_astart[k + 1];
+        uint32_t pf = s_apos[k];
+        while (pf > 0 && tile[pf - 1].start_ts == cs) --pf;
+        uint32_t pl = s_apos[k + 1];
+        while (pl > 0 && tile[pl - 1].start_ts == ce) --pl;
+        reduce_cycle_seq(b, cfg, do_beta, tile, pf, pl, g, inst, cs, ce, tb + s_apos[k], s_aend[k],
+                         tb + pf, tb + pl, my_comp, my_beta, my_coll, my_colln);
+      }
+    }
+    __syncthreads();  // stage and anchor list consumed
+    if (threadIdx.x == 0) {
+      const uint32_t t2 = atomicAdd(fm.ticket, 1u);
+      s_stage_tile[stage] = t2;
+      if (t2 < b.n_tiles) {
+        const u64 nb = b.tile_begin[t2], ne = b.tile_end[t2];
+        const uint32_t bytes = (uint32_t)((ne - nb) * sizeof(cs_event));
+        fence_proxy_async();
+        mbar_expect_tx(&s_bar[stage], bytes);
+        bulk_g2s(s_tiles + stage * kFTileBytes, b.ev + nb, bytes, &s_bar[stage]);
+      }
+    }
+    __syncthreads();
+  }
+  if (cur_inst != 0xffffffffu) {
+    __syncthreads();
+    rows_flush(b.stats + (u64)cur_inst * b.n_names, s_rows);
+  }
+}
+
+// Per-instance slot base and anchor count from the tile look-back results.
+__global__ void k_fused_inst(DevBuffers b, FusedMeta fm, uint64_t* cyc_off) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i > b.n_inst) return;
+  if (i == b.n_inst) {
+    const uint32_t tl = b.n_tiles;
+    cyc_off[i] = tl ? fm.t_pref[tl - 1] + fm.t_cnt[tl - 1] : 0;
+    return;
+  }
+  const uint32_t t0 = b.inst_first_tile[i];
+  const uint32_t t1 = i + 1 < b.n_inst ? b.inst_first_tile[i + 1] : b.n_tiles;
+  if (t0 >= t1) {  // no events: base = next instance's base (computed by scan below)
+    cyc_off[i] = t0 < b.n_tiles ? fm.t_pref[t0] : (b.n_tiles ? fm.t_pref[b.n_tiles - 1] + fm.t_cnt[b.n_tiles - 1] : 0);
+    b.inst[i].n_anchors = 0;
+    return;
+  }
+  cyc_off[i] = fm.t_pref[t0];
+  b.inst[i].n_anchors = fm.t_pref[t1 - 1] + fm.t_cnt[t1 - 1] - fm.t_pref[t0];
+}
+
+// Boundary cycles: find the missing bounds, then the same sequential
+// reduction over global memory; the instance's last anchor becomes a hole.
+__global__ void k_fixup_cycles(DevBuffers b, DevConfig cfg, FusedMeta fm, int do_beta,
+                               uint32_t n_fix, uint32_t words) {
+  extern __shared__ __align__(16) uint32_t s_fix[];
+  const uint32_t f = blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= n_fix) return;
+  const u64 g = fm.fix_list[f];
+  const uint32_t flags = fm.fix_flags[f];
+  const uint32_t inst = b.c_inst[g];
+  const u64 ib = b.inst_off[inst];
+  const i64 cs = b.c_start[g];
+  const u64 apos = b.c_apos[g];
+  i64 ce;
+  u64 last;
+  if (flags & 1u) {
+    // next anchor = rank g+1: the first anchor of the first later tile with anchors
+    const u64 r = g + 1;
+    uint32_t lo = 0, hi = b.n_tiles;  // last tile with t_pref <= r and t_cnt > 0 ... search
+    while (hi - lo > 1) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (fm.t_pref[mid] <= r) lo = mid;
+      else hi = mid;
+    }
+    // tiles with t_pref == r may have zero anchors: walk forward to one with anchors
+    uint32_t u = lo;
+    while (u < b.n_tiles && (fm.t_cnt[u] == 0 || fm.t_pref[u] + fm.t_cnt[u] <= r)) ++u;
+    if (u >= b.n_tiles || b.tile_inst[u] != inst || fm.t_pref[u] != r) {
+      // last anchor of the instance: hole
+      b.c_wl[g] = -4;
+      b.c_local[g] = 255;
+      b.c_stage[g] = CS_STAGE_UNKNOWN;
+      b.c_end[g] = cs;
+      b.c_first[g] = apos;
+      b.c_last[g] = apos;
+      return;
+    }
+    // first anchor event of tile u: scan the tile for it (it is the anchor)
+    const uint32_t name = b.inst[inst].guess;
+    u64 p = b.tile_begin[u];
+    while (!(b.ev[p].kind == CS_SPAN && b.ev[p].name_id == name)) ++p;
+    ce = b.ev[p].start_ts;
+    last = group_start(b.ev, p, ib, ce);
+    b.c_end[g] = ce;
+    b.c_last[g] = last;
+  } else {
+    ce = b.c_end[g];
+    last = b.c_last[g];
+  }
+  const u64 first = group_start(b.ev, apos, ib, cs);
+  const int P = cfg.cyc.n_phases, C = cfg.cyc.n_beta_slots, R = cfg.cyc.n_comm_slots;
+  i64* comp = reinterpret_cast<i64*>(s_fix + (u64)threadIdx.x * words);
+  i64* beta = comp + P;
+  double* coll = reinterpret_cast<double*>(beta + C);
+  uint32_t* colln = reinterpret_cast<uint32_t*>(coll + R);
+  reduce_cycle_seq(b, cfg, do_beta, b.ev, first, last, g, inst, cs, ce, apos, b.c_aend[g], first,
+                   last, comp, beta, coll, colln);
+}
+
+uint32_t fused_scratch_words(const DevConfig& cfg) {
+  const uint32_t w = (uint32_t)(cfg.cyc.n_phases + cfg.cyc.n_beta_slots + cfg.cyc.n_comm_slots) * 2 +
+                     (uint32_t)cfg.cyc.n_comm_slots + 1;
+  return (w + 1) & ~1u;
+}
+
+int launch_fused_segment(const DevBuffers& b, const DevConfig& cfg, const FusedMetaHost& mh,
+                         int do_beta, cudaStream_t s, uint64_t* launches) {
+  if (b.n_tiles == 0) return 0;
+  FusedMeta fm{mh.state, mh.ticket, mh.t_cnt, mh.t_pref, mh.fix_list, mh.fix_n, mh.fix_flags,
+               mh.capacity, mh.overflow};
+  const uint32_t words = fused_scratch_words(cfg);
+  uint32_t cyc_threads = (uint32_t)(60 * 1024 / (words * 4));
+  cyc_threads = cyc_threads > (uint32_t)kFThreads ? (uint32_t)kFThreads : cyc_threads;
+  cyc_threads &= ~31u;
+  if (cyc_threads < 32) return -1;  // config too wide for the fused path
+  const int smem = kFStages * (int)kFTileBytes + (int)(cyc_threads * words * 4);
+  cudaFuncSetAttribute(k_fused_segment, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const uint32_t grid = b.n_tiles < (uint32_t)sms ? b.n_tiles : (uint32_t)sms;
+  k_fused_segment<<<grid, kFThreads, smem, s>>>(b, cfg, fm, do_beta, cyc_threads);
+  ++*launches;
+  return 0;
+}
+
+void launch_fused_inst(const DevBuffers& b, const FusedMetaHost& mh, uint64_t* cyc_off,
+                       cudaStream_t s, uint64_t* launches) {
+  FusedMeta fm{mh.state, mh.ticket, mh.t_cnt, mh.t_pref, mh.fix_list, mh.fix_n, mh.fix_flags,
+               mh.capacity, mh.overflow};
+  k_fused_inst<<<(b.n_inst + 1 + 255) / 256, 256, 0, s>>>(b, fm, cyc_off);
+  ++*launches;
+}
+
+void launch_fixup_cycles(const DevBuffers& b, const DevConfig& cfg, const FusedMetaHost& mh,
+                         int do_beta, uint32_t n_fix, cudaStream_t s, uint64_t* launches) {
+  if (!n_fix) return;
+  FusedMeta fm{mh.state, mh.ticket, mh.t_cnt, mh.t_pref, mh.fix_list, mh.fix_n, mh.fix_flags,
+               mh.capacity, mh.overflow};
+  const uint32_t words = fused_scratch_words(cfg);
+  const int threads = 64;
+  const int smem = threads * (int)words * 4;
+  cudaFuncSetAttribute(k_fixup_cycles, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  k_fixup_cycles<<<(n_fix + threads - 1) / threads, threads, smem, s>>>(b, cfg, fm, do_beta, n_fix,
+                                                                       words);
+  ++*launches;
 }
 
 // ------------------------------------------------------------ launchers

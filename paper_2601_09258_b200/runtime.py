@@ -64,6 +64,7 @@ def lib():
         getattr(L, fn).argtypes = [vp, u32, vp, sz, psz]
     L.cs_get_beta.argtypes = [vp, u32, vp, vp, sz, psz]
     L.cs_get_collective_beta.argtypes = [vp, u32, vp, vp, sz, psz]
+    L.cs_set_option.argtypes = [vp, C.c_int, C.c_int64]
     L.cs_host_alloc.argtypes = [sz, C.POINTER(vp)]
     L.cs_host_free.argtypes = [vp]
     L.cs_get_timings.argtypes = [vp, vp, sz, psz, C.c_char_p, sz]
@@ -97,7 +98,7 @@ EXPORTED_SYMBOLS = [
     "cs_host_free", "cs_get_timings", "cs_get_launch_count", "cs_fit_latency_model",
     "cs_model_from_json", "cs_model_to_json", "cs_model_view", "cs_model_free",
     "cs_ucl_from_stats", "cs_compute_ucl", "cs_config_from_json", "cs_synth_generate",
-    "cs_synth_view", "cs_synth_names", "cs_synth_free",
+    "cs_synth_view", "cs_synth_names", "cs_synth_free", "cs_set_option",
 ]
 
 
@@ -336,6 +337,9 @@ class Analyzer:
         v = model.view()
         self._keep.append(model)
         self._ck(self.L.cs_load_model(self.h, 0xFFFFFFFF if inst is None else inst, C.byref(v)))
+
+    def set_fused(self, enabled: bool):
+        self._ck(self.L.cs_set_option(self.h, 1, int(bool(enabled))))
 
     def run(self, mask: int = abi.RUN_ALL):
         self._ck(self.L.cs_run(self.h, mask))

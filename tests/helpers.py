@@ -13,9 +13,10 @@ from paper_2601_09258_b200 import runtime as rt
 
 
 def run_product(events, names, workloads, n_comm=0, run_config=None, model_json=None,
-                mask=abi.RUN_ALL, analyzer=None):
+                mask=abi.RUN_ALL, analyzer=None, fused=True):
     """One instance through the C ABI; returns InstanceResult."""
     an = analyzer or rt.Analyzer()
+    an.set_fused(fused)
     span = rt.span_names_mask(events, len(names))
     an.configure(names, span, n_comm_slots=n_comm, run_config=run_config)
     an.upload(events, [0, len(events)], workloads)

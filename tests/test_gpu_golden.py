@@ -28,12 +28,13 @@ def load_golden(path):
     return d
 
 
+@pytest.mark.parametrize("fused", [True, False], ids=["fused", "multikernel"])
 @pytest.mark.parametrize("path", GOLDEN, ids=[os.path.basename(p)[:-4] for p in GOLDEN])
-def test_gpu_matches_golden(path, analyzer):
+def test_gpu_matches_golden(path, fused, analyzer):
     d = load_golden(path)
     got, _ = run_product(d["events"], d["names"], d["workloads"], n_comm=len(d["comm_hash"]),
                          run_config=d["run_config"], model_json=d["model_json"] or None,
-                         analyzer=analyzer)
+                         analyzer=analyzer, fused=fused)
     status = int(d["status"])
     if status:
         assert got.status_type == str(d["err_type"])
@@ -57,11 +58,12 @@ def test_gpu_matches_golden(path, analyzer):
     assert n == len(got.records) or status != 0
 
 
-def test_gpu_matches_c_oracle_on_random_edge_traces(analyzer):
+@pytest.mark.parametrize("fused", [True, False], ids=["fused", "multikernel"])
+def test_gpu_matches_c_oracle_on_random_edge_traces(analyzer, fused):
     """Seeded random traces with equal timestamps, overlapping anchors,
     missing args, duplicates — GPU vs the C restatement."""
     rng = np.random.default_rng(11)
-    for trial in range(12):
+    for trial in range(16):
         spec, t = [], 0
         n = int(rng.integers(5, 400))
         for i in range(n):
@@ -84,7 +86,7 @@ def test_gpu_matches_c_oracle_on_random_edge_traces(analyzer):
         model = json.dumps(traces.TINY_MODEL)
         o = csoracle.analyze(b.events, b.names, b.workloads, b.n_comm, cfg, model)
         got, _ = run_product(b.events, b.names, b.workloads, n_comm=b.n_comm, run_config=cfg,
-                             model_json=model, analyzer=analyzer)
+                             model_json=model, analyzer=analyzer, fused=fused)
         assert np.array_equal(got.cycles, o["cycles"]), trial
         assert np.array_equal(got.components, o["components"]), trial
         assert np.array_equal(got.beta_totals, o["beta_totals"]), trial

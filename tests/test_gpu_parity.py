@@ -18,12 +18,13 @@ FAMILIES = ["cpu_contention", "cpu_freq_drop", "gpu_contention", "gpu_clock_lock
             "memory_thrash", "nvlink_saturation", "pcie_bottleneck", "bus_contention"]
 
 
-def _ref_and_product(refbridge, analyzer, trace, run_config=None, train_cycles=2400, mask=abi.RUN_ALL):
+def _ref_and_product(refbridge, analyzer, trace, run_config=None, train_cycles=2400,
+                     mask=abi.RUN_ALL, fused=True):
     ref = trace.run(run_config, None, train_cycles)
     ex = trace.export(run_config)
     got, _ = run_product(ex.events, ex.names, ex.workloads, n_comm=len(ex.comm_hash),
                          run_config=run_config, model_json=ref.model_json, mask=mask,
-                         analyzer=analyzer)
+                         analyzer=analyzer, fused=fused)
     return ref, got, ex
 
 
@@ -60,11 +61,12 @@ def test_eight_rank_collective_beta(refbridge, analyzer):
     assert cb[2600:2650, 3].mean() > cb[2600:2650, 0].mean()
 
 
-def test_c1_scale_parity(refbridge, analyzer):
+@pytest.mark.parametrize("fused", [True, False], ids=["fused", "multikernel"])
+def test_c1_scale_parity(refbridge, analyzer, fused):
     """BASELINE config 1: 50k cycles, ~1M events, fault at 40000 for 150."""
     t = refbridge.RefTrace.synth(50000, 1, 2, fault="cpu_contention", onset=40000, duration=150)
     assert t.n_events() == 1000001
-    ref, got, _ = _ref_and_product(refbridge, analyzer, t)
+    ref, got, _ = _ref_and_product(refbridge, analyzer, t, fused=fused)
     assert_full_parity(ref, got)
 
 
