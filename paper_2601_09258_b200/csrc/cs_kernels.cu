@@ -1509,9 +1509,9 @@ __global__ void k_freq_cycles(const cs_event* ev, uint64_t begin, uint64_t end, 
 //      k_fixup_cycles reduces from global memory with the same routine.
 // Cycle slots are global anchor ranks; the last anchor of an instance owns a
 // "hole" slot (no cycle), marked c_wl = -4.
-constexpr int kFThreads = 512;
+constexpr int kFThreads = 256;
 constexpr int kFTile = 1024;
-constexpr int kFStages = 4;
+constexpr int kFStages = 2;
 constexpr uint32_t kFTileBytes = kFTile * sizeof(cs_event);
 constexpr u64 kFlagAggF = 1ull << 62;
 constexpr u64 kFlagPrefixF = 2ull << 62;
@@ -1544,15 +1544,27 @@ __device__ u64 lookback_global(u64* state, uint32_t tile, u64 agg) {
 }
 
 // Sequential per-cycle reduction by one thread over ev[first, last): the
-// reference's own loops, in event order.  Writes every per-cycle output.
-__device__ void reduce_cycle_seq(const DevBuffers& b, const DevConfig& cfg, int do_beta,
-                                 const cs_event* ev, u64 first, u64 last, u64 g, uint32_t inst,
-                                 i64 cs, i64 ce, u64 apos, i64 aend, u64 gfirst, u64 glast,
-                                 i64* comp, i64* beta, double* coll, uint32_t* colln) {
-  const int P = cfg.cyc.n_phases, C = cfg.cyc.n_beta_slots, R = cfg.cyc.n_comm_slots;
+// reference's own loops, in event order.  Component sums live in registers
+// (<= kMaxPhases), class occupancy and collective beta in a thread-private
+// shared-memory slice.
+struct CycAcc {
+  i64 comp[kMaxPhases];
+  int32_t wl;
+  uint8_t stage;
+};
+
+template <typename EvPtr>
+__device__ __forceinline__ CycAcc accumulate_cycle(const cs_name_info* __restrict__ names,
+                                                   const DevConfig& cfg, int do_beta,
+                                                   EvPtr ev, u64 first, u64 last, i64 cs, i64 ce,
+                                                   bool no_comp, i64* __restrict__ beta,
+                                                   double* __restrict__ coll,
+                                                   uint32_t* __restrict__ colln) {
+  const int C = cfg.cyc.n_beta_slots, R = cfg.cyc.n_comm_slots;
   const i64 dur = ce - cs;
-  const bool no_comp = apos == kNone;
-  for (int i = 0; i < P; ++i) comp[i] = 0;
+  CycAcc a;
+#pragma unroll
+  for (int i = 0; i < kMaxPhases; ++i) a.comp[i] = 0;
   if (do_beta) {
     for (int i = 0; i < C; ++i) beta[i] = 0;
     for (int i = 0; i < R; ++i) {
@@ -1562,7 +1574,7 @@ __device__ void reduce_cycle_seq(const DevBuffers& b, const DevConfig& cfg, int 
   }
   uint32_t fm_cls = 0;
   bool fm_found = false, pkw = false, dkw = false, batch_found = false;
-  int32_t wl = -1;
+  a.wl = -1;
   for (u64 j = first; j < last; ++j) {
     const int4* q = reinterpret_cast<const int4*>(ev + j);
     const int4 h0 = q[0], h1 = q[1];
@@ -1578,16 +1590,19 @@ __device__ void reduce_cycle_seq(const DevBuffers& b, const DevConfig& cfg, int 
     }
     if (!batch_found && (flags & CS_EV_HAS_BATCH)) {
       batch_found = true;
-      wl = (flags & CS_EV_WL_OK) ? (int32_t)(uint32_t)h1.z : -2;
+      a.wl = (flags & CS_EV_WL_OK) ? (int32_t)(uint32_t)h1.z : -2;
     }
     if (kind != CS_SPAN) continue;
-    const cs_name_info ni = b.names[name];
+    const cs_name_info ni = names[name];
     pkw |= (ni.flags & CS_NAME_PREFILL_KW) != 0;
     dkw |= (ni.flags & CS_NAME_DECODE_KW) != 0;
     const i64 end = st + d;
     const i64 clipped = (end < ce ? end : ce) - st;
     if (clipped <= 0) continue;
-    if (!no_comp && ni.phase >= 0) comp[ni.phase] += clipped;
+    if (!no_comp) {
+#pragma unroll
+      for (int p = 0; p < kMaxPhases; ++p) a.comp[p] += ni.phase == p ? clipped : 0;
+    }
     if (do_beta && d > 0) {
       if (ni.beta_slot >= 0) beta[ni.beta_slot] += clipped;
       if (cat == CS_CAT_COLLECTIVE_COMM && (flags & CS_EV_HAS_COMM)) {
@@ -1599,10 +1614,21 @@ __device__ void reduce_cycle_seq(const DevBuffers& b, const DevConfig& cfg, int 
       }
     }
   }
-  uint8_t stage = CS_STAGE_UNKNOWN;
-  if (fm_cls == CS_EV_FM_PREFILL) stage = CS_STAGE_PREFILL;
-  else if (fm_cls == CS_EV_FM_DECODE) stage = CS_STAGE_DECODE;
-  if (stage == CS_STAGE_UNKNOWN && pkw != dkw) stage = pkw ? CS_STAGE_PREFILL : CS_STAGE_DECODE;
+  a.stage = CS_STAGE_UNKNOWN;
+  if (fm_cls == CS_EV_FM_PREFILL) a.stage = CS_STAGE_PREFILL;
+  else if (fm_cls == CS_EV_FM_DECODE) a.stage = CS_STAGE_DECODE;
+  if (a.stage == CS_STAGE_UNKNOWN && pkw != dkw) a.stage = pkw ? CS_STAGE_PREFILL : CS_STAGE_DECODE;
+  return a;
+}
+
+__device__ __forceinline__ void write_cycle(const DevBuffers& b, const DevConfig& cfg, int do_beta,
+                                            const CycAcc& a, u64 g, uint32_t inst, i64 cs, i64 ce,
+                                            u64 apos, i64 aend, u64 gfirst, u64 glast,
+                                            const i64* __restrict__ beta,
+                                            const double* __restrict__ coll,
+                                            const uint32_t* __restrict__ colln) {
+  const int P = cfg.cyc.n_phases, C = cfg.cyc.n_beta_slots, R = cfg.cyc.n_comm_slots;
+  const i64 dur = ce - cs;
   b.c_start[g] = cs;
   b.c_end[g] = ce;
   b.c_apos[g] = apos;
@@ -1610,11 +1636,13 @@ __device__ void reduce_cycle_seq(const DevBuffers& b, const DevConfig& cfg, int 
   b.c_first[g] = gfirst;
   b.c_last[g] = glast;
   b.c_inst[g] = inst;
-  b.c_local[g] = stage;
-  b.c_stage[g] = stage;
-  b.c_wl[g] = wl;
-  if (stage == CS_STAGE_UNKNOWN) atomicAdd(&b.inst[inst].n_unknown, 1ull);
-  for (int i = 0; i < P; ++i) b.c_comp[g * P + i] = comp[i];
+  b.c_local[g] = a.stage;
+  b.c_stage[g] = a.stage;
+  b.c_wl[g] = a.wl;
+  if (a.stage == CS_STAGE_UNKNOWN) atomicAdd(&b.inst[inst].n_unknown, 1ull);
+#pragma unroll
+  for (int i = 0; i < kMaxPhases; ++i)
+    if (i < P) b.c_comp[g * P + i] = a.comp[i];
   if (do_beta) {
     for (int i = 0; i < C; ++i) {
       const i64 t = dur > 0 ? beta[i] : 0;
@@ -1641,41 +1669,50 @@ struct FusedMeta {
 };
 
 __device__ __forceinline__ uint32_t scratch_words(const DevConfig& cfg) {
-  return (uint32_t)(cfg.cyc.n_phases + cfg.cyc.n_beta_slots + cfg.cyc.n_comm_slots) * 2 +
-         (uint32_t)cfg.cyc.n_comm_slots + 1;  // i64/f64 as 2 words, colln as 1
+  const uint32_t w = (uint32_t)(cfg.cyc.n_beta_slots + cfg.cyc.n_comm_slots) * 2 +
+                     (uint32_t)cfg.cyc.n_comm_slots + 1;
+  return (w + 1) & ~1u;
 }
 
-__global__ void __launch_bounds__(kFThreads, 1)
+constexpr int kFNamesSmem = 256;
+
+__global__ void __launch_bounds__(kFThreads, 2)
     k_fused_segment(DevBuffers b, DevConfig cfg, FusedMeta fm, int do_beta,
                     uint32_t n_cyc_threads) {
   extern __shared__ __align__(128) unsigned char s_dyn[];
   __shared__ uint64_t s_bar[kFStages];
   __shared__ uint32_t s_stage_tile[kFStages];
   __shared__ WarpNameRow s_rows[(kFThreads / 32) * kWarpNameRows];
-  __shared__ uint16_t s_apos[kFTile];
-  __shared__ i64 s_astart[kFTile];
-  __shared__ i64 s_aend[kFTile];
+  __shared__ cs_name_info s_names[kFNamesSmem];
   __shared__ uint32_t s_warp_cnt[kFThreads / 32];
   __shared__ u64 s_P;
-  __shared__ uint32_t s_lead;
+  __shared__ volatile uint32_t s_ready;
 
   unsigned char* s_tiles = s_dyn;
-  uint32_t* s_scratch = reinterpret_cast<uint32_t*>(s_dyn + kFStages * kFTileBytes);
+  uint16_t* s_apos = reinterpret_cast<uint16_t*>(s_dyn + kFStages * kFTileBytes);
+  i64* s_astart = reinterpret_cast<i64*>(s_dyn + kFStages * kFTileBytes + kFTile * 2);
+  i64* s_aend = s_astart + kFTile;
+  uint32_t* s_scratch = reinterpret_cast<uint32_t*>(s_aend + kFTile);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   constexpr int kWarps = kFThreads / 32;
-  constexpr int kIt = kFTile / kFThreads;  // 2 groups of 32 events per warp
-  const int P = cfg.cyc.n_phases, C = cfg.cyc.n_beta_slots, R = cfg.cyc.n_comm_slots;
+  constexpr int kIt = kFTile / kFThreads;
+  const int C = cfg.cyc.n_beta_slots, R = cfg.cyc.n_comm_slots;
   const uint32_t sw = scratch_words(cfg);
-  // per-thread scratch: comp[P] i64 | beta[C] i64 | coll[R] f64 | colln[R] u32
-  i64* my_comp = reinterpret_cast<i64*>(s_scratch + (u64)threadIdx.x * ((sw + 1) & ~1u));
-  i64* my_beta = my_comp + P;
+  // cycle threads: warps 1.. (warp 0 runs the look-back)
+  const int ct = (int)threadIdx.x - 32;
+  const bool is_cyc = ct >= 0 && ct < (int)n_cyc_threads;
+  i64* my_beta = reinterpret_cast<i64*>(s_scratch + (u64)(is_cyc ? ct : 0) * sw);
   double* my_coll = reinterpret_cast<double*>(my_beta + C);
   uint32_t* my_colln = reinterpret_cast<uint32_t*>(my_coll + R);
+  const cs_name_info* names = b.n_names <= (uint32_t)kFNamesSmem ? s_names : b.names;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kFStages; ++s) mbar_init(&s_bar[s], 1);
     mbar_fence_init();
+    s_ready = 0;
   }
+  for (uint32_t i = threadIdx.x; i < b.n_names && i < (uint32_t)kFNamesSmem; i += blockDim.x)
+    s_names[i] = b.names[i];
   rows_zero(s_rows);
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -1752,15 +1789,6 @@ __global__ void __launch_bounds__(kFThreads, 1)
       base += w < warp ? c : 0;
       total += c;
     }
-    // 2. global rank of the first anchor of this tile
-    if (warp == 0) {
-      const u64 excl = lookback_global(fm.state, t, total);
-      if (lane == 0) {
-        s_P = excl;
-        fm.t_cnt[t] = total;
-        fm.t_pref[t] = excl;
-      }
-    }
 #pragma unroll
     for (int j = 0; j < kIt; ++j) {
       const uint32_t m = masks[j];
@@ -1775,28 +1803,26 @@ __global__ void __launch_bounds__(kFThreads, 1)
       base += __popc(m);
     }
     __syncthreads();
-    const u64 P0 = s_P;
-    if (P0 + total > fm.capacity) {
-      if (threadIdx.x == 0) atomicOr(fm.overflow, 1u);
-    } else if (total > 0) {
-      // lead boundary: the first anchor's equal-start group begins before the tile
-      if (threadIdx.x == 0) {
+    if (warp == 0) {
+      // 2. global rank of this tile's first anchor (overlaps the cycle work)
+      const u64 P0 = lookback_global(fm.state, t, total);
+      if (lane == 0) {
+        fm.t_cnt[t] = total;
+        fm.t_pref[t] = P0;
+        if (P0 + total > fm.capacity) atomicOr(fm.overflow, 1u);
+      }
+      // boundary cycles: the trailing one, and k = 0 when its equal-start
+      // group begins before the tile
+      if (lane == 0 && total > 0 && P0 + total <= fm.capacity) {
         uint32_t p0 = s_apos[0];
         while (p0 > 0 && tile[p0 - 1].start_ts == s_astart[0]) --p0;
-        s_lead = (p0 == 0 && tb > ib && b.ev[tb - 1].start_ts == s_astart[0]) ? 1u : 0u;
-      }
-      __syncthreads();
-      // 3. local cycles: anchors k and k+1 in the tile
-      for (uint32_t k = threadIdx.x; k < total; k += blockDim.x) {
-        const u64 g = P0 + k;
-        const bool trailing = k + 1 == total;
-        const bool lead = k == 0 && s_lead;
-        const i64 cs = s_astart[k];
-        const u64 apos = tb + s_apos[k];
-        if (trailing || lead) {
-          // k_fixup_cycles completes it; record what is known
-          b.c_start[g] = cs;
-          b.c_apos[g] = apos;
+        const bool lead = p0 == 0 && tb > ib && b.ev[tb - 1].start_ts == s_astart[0];
+        for (uint32_t k = 0; k < total; ++k) {
+          const bool trailing = k + 1 == total;
+          if (!(trailing || (k == 0 && lead))) continue;
+          const u64 g = P0 + k;
+          b.c_start[g] = s_astart[k];
+          b.c_apos[g] = tb + s_apos[k];
           b.c_aend[g] = s_aend[k];
           b.c_inst[g] = inst;
           if (!trailing) {
@@ -1807,20 +1833,31 @@ __global__ void __launch_bounds__(kFThreads, 1)
           }
           const unsigned int slot = atomicAdd(fm.fix_n, 1u);
           fm.fix_list[slot] = g;
-          fm.fix_flags[slot] = (trailing ? 1u : 0u) | (lead ? 2u : 0u);
+          fm.fix_flags[slot] = (trailing ? 1u : 0u) | ((k == 0 && lead) ? 2u : 0u);
         }
       }
-      for (uint32_t k = threadIdx.x; k + 1 < total; k += n_cyc_threads) {
-        if (threadIdx.x >= n_cyc_threads) break;
-        if (k == 0 && s_lead) continue;
-        const u64 g = P0 + k;
+      if (lane == 0) {
+        s_P = P0;
+        __threadfence_block();
+        s_ready = it + 1;
+      }
+    } else if (is_cyc) {
+      // 3. local cycles, one thread each, from shared memory
+      for (uint32_t k = (uint32_t)ct; k + 1 < total; k += n_cyc_threads) {
         const i64 cs = s_astart[k], ce = s_astart[k + 1];
         uint32_t pf = s_apos[k];
         while (pf > 0 && tile[pf - 1].start_ts == cs) --pf;
+        if (pf == 0 && k == 0 && tb > ib && b.ev[tb - 1].start_ts == cs) continue;  // lead: fixup
         uint32_t pl = s_apos[k + 1];
         while (pl > 0 && tile[pl - 1].start_ts == ce) --pl;
-        reduce_cycle_seq(b, cfg, do_beta, tile, pf, pl, g, inst, cs, ce, tb + s_apos[k], s_aend[k],
-                         tb + pf, tb + pl, my_comp, my_beta, my_coll, my_colln);
+        const CycAcc acc = accumulate_cycle(names, cfg, do_beta, tile, pf, pl, cs, ce, false,
+                                            my_beta, my_coll, my_colln);
+        while (s_ready != it + 1) {
+        }
+        const u64 g = s_P + k;
+        if (g + 1 <= fm.capacity)
+          write_cycle(b, cfg, do_beta, acc, g, inst, cs, ce, tb + s_apos[k], s_aend[k], tb + pf,
+                      tb + pl, my_beta, my_coll, my_colln);
       }
     }
     __syncthreads();  // stage and anchor list consumed
@@ -1913,17 +1950,18 @@ __global__ void k_fixup_cycles(DevBuffers b, DevConfig cfg, FusedMeta fm, int do
     last = b.c_last[g];
   }
   const u64 first = group_start(b.ev, apos, ib, cs);
-  const int P = cfg.cyc.n_phases, C = cfg.cyc.n_beta_slots, R = cfg.cyc.n_comm_slots;
-  i64* comp = reinterpret_cast<i64*>(s_fix + (u64)threadIdx.x * words);
-  i64* beta = comp + P;
+  const int C = cfg.cyc.n_beta_slots, R = cfg.cyc.n_comm_slots;
+  i64* beta = reinterpret_cast<i64*>(s_fix + (u64)threadIdx.x * words);
   double* coll = reinterpret_cast<double*>(beta + C);
   uint32_t* colln = reinterpret_cast<uint32_t*>(coll + R);
-  reduce_cycle_seq(b, cfg, do_beta, b.ev, first, last, g, inst, cs, ce, apos, b.c_aend[g], first,
-                   last, comp, beta, coll, colln);
+  const CycAcc acc = accumulate_cycle(b.names, cfg, do_beta, b.ev, first, last, cs, ce, false,
+                                      beta, coll, colln);
+  write_cycle(b, cfg, do_beta, acc, g, inst, cs, ce, apos, b.c_aend[g], first, last, beta, coll,
+              colln);
 }
 
 uint32_t fused_scratch_words(const DevConfig& cfg) {
-  const uint32_t w = (uint32_t)(cfg.cyc.n_phases + cfg.cyc.n_beta_slots + cfg.cyc.n_comm_slots) * 2 +
+  const uint32_t w = (uint32_t)(cfg.cyc.n_beta_slots + cfg.cyc.n_comm_slots) * 2 +
                      (uint32_t)cfg.cyc.n_comm_slots + 1;
   return (w + 1) & ~1u;
 }
@@ -1934,16 +1972,24 @@ int launch_fused_segment(const DevBuffers& b, const DevConfig& cfg, const FusedM
   FusedMeta fm{mh.state, mh.ticket, mh.t_cnt, mh.t_pref, mh.fix_list, mh.fix_n, mh.fix_flags,
                mh.capacity, mh.overflow};
   const uint32_t words = fused_scratch_words(cfg);
-  uint32_t cyc_threads = (uint32_t)(60 * 1024 / (words * 4));
-  cyc_threads = cyc_threads > (uint32_t)kFThreads ? (uint32_t)kFThreads : cyc_threads;
+  // budget: two CTAs per SM (<= ~113 KB each)
+  const int fixed = kFStages * (int)kFTileBytes + kFTile * (2 + 16);
+  const int budget = 108 * 1024 - fixed;
+  uint32_t cyc_threads = budget > 0 ? (uint32_t)(budget / (int)(words * 4)) : 0;
+  const uint32_t max_ct = (uint32_t)kFThreads - 32;
+  if (cyc_threads > max_ct) cyc_threads = max_ct;
   cyc_threads &= ~31u;
-  if (cyc_threads < 32) return -1;  // config too wide for the fused path
-  const int smem = kFStages * (int)kFTileBytes + (int)(cyc_threads * words * 4);
+  if (cyc_threads < 32) return -1;  // configuration too wide for the fused kernel
+  const int smem = fixed + (int)(cyc_threads * words * 4);
   cudaFuncSetAttribute(k_fused_segment, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const uint32_t grid = b.n_tiles < (uint32_t)sms ? b.n_tiles : (uint32_t)sms;
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fused_segment, kFThreads, smem);
+  if (per_sm < 1) per_sm = 1;
+  const uint32_t want = (uint32_t)(sms * per_sm);
+  const uint32_t grid = b.n_tiles < want ? b.n_tiles : want;
   k_fused_segment<<<grid, kFThreads, smem, s>>>(b, cfg, fm, do_beta, cyc_threads);
   ++*launches;
   return 0;
