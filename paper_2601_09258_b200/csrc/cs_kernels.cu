@@ -193,7 +193,7 @@ struct WarpNameRow {
 };
 
 __device__ __forceinline__ void rows_zero(WarpNameRow* rows) {
-  for (int i = threadIdx.x; i < (kScanThreads / 32) * kWarpNameRows; i += blockDim.x) {
+  for (int i = threadIdx.x; i < (int)(blockDim.x / 32) * kWarpNameRows; i += blockDim.x) {
     rows[i].name = 0xffffffffu;
     rows[i].cnt = 0;
     rows[i].sum = rows[i].sq_lo = rows[i].sq_hi = 0;
@@ -201,7 +201,7 @@ __device__ __forceinline__ void rows_zero(WarpNameRow* rows) {
 }
 
 __device__ void rows_flush(NameStat* g, const WarpNameRow* rows) {
-  for (int i = threadIdx.x; i < (kScanThreads / 32) * kWarpNameRows; i += blockDim.x) {
+  for (int i = threadIdx.x; i < (int)(blockDim.x / 32) * kWarpNameRows; i += blockDim.x) {
     const WarpNameRow r = rows[i];
     if (r.name == 0xffffffffu || !r.cnt) continue;
     atomicAdd(&g[r.name].count, (u64)r.cnt);
@@ -1974,7 +1974,7 @@ int launch_fused_segment(const DevBuffers& b, const DevConfig& cfg, const FusedM
   const uint32_t words = fused_scratch_words(cfg);
   // budget: two CTAs per SM (<= ~113 KB each)
   const int fixed = kFStages * (int)kFTileBytes + kFTile * (2 + 16);
-  const int budget = 108 * 1024 - fixed;
+  const int budget = 100 * 1024 - fixed;
   uint32_t cyc_threads = budget > 0 ? (uint32_t)(budget / (int)(words * 4)) : 0;
   const uint32_t max_ct = (uint32_t)kFThreads - 32;
   if (cyc_threads > max_ct) cyc_threads = max_ct;
