@@ -311,6 +311,12 @@ int cs_get_alerts(cs_ctx* ctx, uint32_t inst, cs_alert* buf, size_t cap, size_t*
 #define CS_OPT_FUSED 1
 int cs_set_option(cs_ctx* ctx, int option, int64_t value);
 
+/* HBM read-streaming microbenchmark (profiling only).
+ * variant 0: vectorised LDG (p0 CTAs/SM, p1 threads, p2 unroll 1|8);
+ * variant 1: 1-D TMA bulk copies (p0 chunk bytes, p1 stages, p2 CTAs/SM). */
+int cs_microbench(int variant, const void* dev_src, uint64_t n_bytes, int p0, int p1, int p2,
+                  int iters, double* ms_out);
+
 /* Pinned host memory helpers (cudaHostAlloc) for the e2e path. */
 int cs_host_alloc(size_t bytes, void** out);
 int cs_host_free(void* p);

@@ -94,6 +94,7 @@ struct cs_ctx {
   uint64_t n_cycles = 0;           // cycle slots (fused path: + one hole per instance)
   uint64_t slot_cap = 0;
   bool allow_fused = true;
+  int fused_debug = 0;
   bool used_fused = false;
   DevBuf d_fstate, d_fticket, d_fcnt, d_fpref, d_fixlist, d_fixn, d_fixflags, d_foverflow;
   DevBuf d_cyc_off, c_start, c_end, c_apos, c_aend, c_first, c_last, c_inst, c_stage, c_local,
@@ -683,7 +684,7 @@ int cs_run(cs_ctx* ctx, uint32_t mask) {
           !dev<unsigned int>(ctx->d_foverflow, 1))
         return fail(ctx, CS_E_CUDA, "cudaMalloc(fused)");
       ctx->slot_cap = cap;
-      mh = FusedMetaHost{static_cast<unsigned long long*>(ctx->d_fstate.p),
+      mh = FusedMetaHost{ctx->fused_debug, static_cast<unsigned long long*>(ctx->d_fstate.p),
                          static_cast<unsigned int*>(ctx->d_fticket.p),
                          static_cast<uint32_t*>(ctx->d_fcnt.p),
                          static_cast<unsigned long long*>(ctx->d_fpref.p),
@@ -1199,6 +1200,10 @@ int cs_set_option(cs_ctx* ctx, int option, int64_t value) {
   if (!ctx) return CS_E_INVALID_ARGUMENT;
   if (option == CS_OPT_FUSED) {
     ctx->allow_fused = value != 0;
+    return CS_OK;
+  }
+  if (option == 99) {  // profiling only (outputs invalid): fused-kernel ablations
+    ctx->fused_debug = static_cast<int>(value);
     return CS_OK;
   }
   return fail(ctx, CS_E_INVALID_ARGUMENT, "unknown option");

@@ -129,6 +129,7 @@ struct DevBuffers {
 
 // fused single-pass segmentation state (k_fused_segment)
 struct FusedMetaHost {
+  int debug;
   unsigned long long* state;
   unsigned int* ticket;
   uint32_t* t_cnt;

@@ -1621,6 +1621,125 @@ __device__ __forceinline__ CycAcc accumulate_cycle(const cs_name_info* __restric
   return a;
 }
 
+// Register-resident variant for the common narrow configurations
+// (<= KC classes, <= KR collective slots): every update is a predicated
+// select-add, no memory round trip, so consecutive events pipeline.
+template <int KC, int KR>
+struct CycAccR {
+  i64 comp[kMaxPhases];
+  i64 beta[KC];
+  double coll[KR];
+  uint32_t colln[KR];
+  int32_t wl;
+  uint8_t stage;
+};
+
+template <int KC, int KR>
+__device__ __forceinline__ void accumulate_cycle_reg(const cs_name_info* __restrict__ names,
+                                                     int do_beta, const cs_event* __restrict__ ev,
+                                                     uint32_t first, uint32_t last, i64 cs,
+                                                     i64 ce, CycAccR<KC, KR>& a) {
+  const i64 dur = ce - cs;
+#pragma unroll
+  for (int i = 0; i < kMaxPhases; ++i) a.comp[i] = 0;
+#pragma unroll
+  for (int i = 0; i < KC; ++i) a.beta[i] = 0;
+#pragma unroll
+  for (int i = 0; i < KR; ++i) {
+    a.coll[i] = 0.0;
+    a.colln[i] = 0;
+  }
+  uint32_t fm_cls = 0;
+  bool fm_found = false, pkw = false, dkw = false, batch_found = false;
+  a.wl = -1;
+#pragma unroll 2
+  for (uint32_t j = first; j < last; ++j) {
+    const int4* q = reinterpret_cast<const int4*>(ev + j);
+    const int4 h0 = q[0], h1 = q[1];
+    const i64 st = (i64)(((u64)(uint32_t)h0.y << 32) | (uint32_t)h0.x);
+    const i64 d = (i64)(((u64)(uint32_t)h0.w << 32) | (uint32_t)h0.z);
+    const uint32_t name = (uint32_t)h1.x;
+    const uint32_t kind = (uint32_t)h1.y & 0xffu;
+    const uint32_t cat = ((uint32_t)h1.y >> 8) & 0xffu;
+    const uint32_t flags = (uint32_t)h1.y >> 16;
+    if (!fm_found && (flags & CS_EV_FM_MASK)) {
+      fm_found = true;
+      fm_cls = flags & CS_EV_FM_MASK;
+    }
+    if (!batch_found && (flags & CS_EV_HAS_BATCH)) {
+      batch_found = true;
+      a.wl = (flags & CS_EV_WL_OK) ? (int32_t)(uint32_t)h1.z : -2;
+    }
+    if (kind != CS_SPAN) continue;
+    const cs_name_info ni = names[name];
+    pkw |= (ni.flags & CS_NAME_PREFILL_KW) != 0;
+    dkw |= (ni.flags & CS_NAME_DECODE_KW) != 0;
+    const i64 end = st + d;
+    const i64 clipped = (end < ce ? end : ce) - st;
+    if (clipped <= 0) continue;
+#pragma unroll
+    for (int p = 0; p < kMaxPhases; ++p) a.comp[p] += ni.phase == p ? clipped : 0;
+    if (do_beta && d > 0) {
+#pragma unroll
+      for (int c = 0; c < KC; ++c) a.beta[c] += ni.beta_slot == c ? clipped : 0;
+      if (cat == CS_CAT_COLLECTIVE_COMM && (flags & CS_EV_HAS_COMM)) {
+        const uint32_t slot = (uint32_t)h1.w;
+        const double term = __ddiv_rn((double)clipped, (double)dur);
+#pragma unroll
+        for (int r = 0; r < KR; ++r)
+          if (slot == (uint32_t)r) {
+            a.coll[r] = __dadd_rn(a.coll[r], term);
+            a.colln[r] += 1;
+          }
+      }
+    }
+  }
+  a.stage = CS_STAGE_UNKNOWN;
+  if (fm_cls == CS_EV_FM_PREFILL) a.stage = CS_STAGE_PREFILL;
+  else if (fm_cls == CS_EV_FM_DECODE) a.stage = CS_STAGE_DECODE;
+  if (a.stage == CS_STAGE_UNKNOWN && pkw != dkw) a.stage = pkw ? CS_STAGE_PREFILL : CS_STAGE_DECODE;
+}
+
+template <int KC, int KR>
+__device__ __forceinline__ void write_cycle_reg(const DevBuffers& b, const DevConfig& cfg,
+                                                int do_beta, const CycAccR<KC, KR>& a, u64 g,
+                                                uint32_t inst, i64 cs, i64 ce, u64 apos, i64 aend,
+                                                u64 gfirst, u64 glast) {
+  const int P = cfg.cyc.n_phases, C = cfg.cyc.n_beta_slots, R = cfg.cyc.n_comm_slots;
+  const i64 dur = ce - cs;
+  b.c_start[g] = cs;
+  b.c_end[g] = ce;
+  b.c_apos[g] = apos;
+  b.c_aend[g] = aend;
+  b.c_first[g] = gfirst;
+  b.c_last[g] = glast;
+  b.c_inst[g] = inst;
+  b.c_local[g] = a.stage;
+  b.c_stage[g] = a.stage;
+  b.c_wl[g] = a.wl;
+  if (a.stage == CS_STAGE_UNKNOWN) atomicAdd(&b.inst[inst].n_unknown, 1ull);
+#pragma unroll
+  for (int i = 0; i < kMaxPhases; ++i)
+    if (i < P) b.c_comp[g * P + i] = a.comp[i];
+  if (do_beta) {
+#pragma unroll
+    for (int i = 0; i < KC; ++i) {
+      if (i < C) {
+        const i64 t = dur > 0 ? a.beta[i] : 0;
+        b.c_beta_tot[g * C + i] = t;
+        b.c_beta[g * C + i] = t > 0 ? __ddiv_rn((double)t, (double)dur) : 0.0;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < KR; ++i) {
+      if (i < R) {
+        b.c_coll[g * R + i] = a.coll[i];
+        b.c_coll_n[g * R + i] = (uint8_t)(a.colln[i] > 255 ? 255 : a.colln[i]);
+      }
+    }
+  }
+}
+
 __device__ __forceinline__ void write_cycle(const DevBuffers& b, const DevConfig& cfg, int do_beta,
                                             const CycAcc& a, u64 g, uint32_t inst, i64 cs, i64 ce,
                                             u64 apos, i64 aend, u64 gfirst, u64 glast,
@@ -1657,6 +1776,7 @@ __device__ __forceinline__ void write_cycle(const DevBuffers& b, const DevConfig
 }
 
 struct FusedMeta {
+  int debug;           // profiling only: bit0 no look-back, bit1 no cycle work
   u64* state;          // look-back state per tile
   unsigned int* ticket;
   uint32_t* t_cnt;     // anchors per tile
@@ -1675,13 +1795,21 @@ __device__ __forceinline__ uint32_t scratch_words(const DevConfig& cfg) {
 }
 
 constexpr int kFNamesSmem = 256;
+constexpr int kFRegC = 16;  // register path: <= 16 span classes
+constexpr int kFRegR = 8;   //                <= 8 collective slots
 
+struct TileMeta {
+  uint32_t t, inst, n, guess;
+  u64 tb, ib;
+};
+
+template <bool kReg>
 __global__ void __launch_bounds__(kFThreads, 2)
     k_fused_segment(DevBuffers b, DevConfig cfg, FusedMeta fm, int do_beta,
                     uint32_t n_cyc_threads) {
   extern __shared__ __align__(128) unsigned char s_dyn[];
   __shared__ uint64_t s_bar[kFStages];
-  __shared__ uint32_t s_stage_tile[kFStages];
+  __shared__ TileMeta s_meta[kFStages];
   __shared__ WarpNameRow s_rows[(kFThreads / 32) * kWarpNameRows];
   __shared__ cs_name_info s_names[kFNamesSmem];
   __shared__ uint32_t s_warp_cnt[kFThreads / 32];
@@ -1698,13 +1826,28 @@ __global__ void __launch_bounds__(kFThreads, 2)
   constexpr int kIt = kFTile / kFThreads;
   const int C = cfg.cyc.n_beta_slots, R = cfg.cyc.n_comm_slots;
   const uint32_t sw = scratch_words(cfg);
-  // cycle threads: warps 1.. (warp 0 runs the look-back)
-  const int ct = (int)threadIdx.x - 32;
+  const int ct = (int)threadIdx.x - 32;  // cycle threads: warps 1..
   const bool is_cyc = ct >= 0 && ct < (int)n_cyc_threads;
-  i64* my_beta = reinterpret_cast<i64*>(s_scratch + (u64)(is_cyc ? ct : 0) * sw);
+  i64* my_beta = reinterpret_cast<i64*>(s_scratch + (u64)(is_cyc && !kReg ? ct : 0) * sw);
   double* my_coll = reinterpret_cast<double*>(my_beta + C);
   uint32_t* my_colln = reinterpret_cast<uint32_t*>(my_coll + R);
-  const cs_name_info* names = b.n_names <= (uint32_t)kFNamesSmem ? s_names : b.names;
+
+  auto issue = [&](int s) {  // thread 0: claim the next tile for stage s
+    const uint32_t t = atomicAdd(fm.ticket, 1u);
+    TileMeta m;
+    m.t = t;
+    if (t < b.n_tiles) {
+      m.inst = b.tile_inst[t];
+      m.tb = b.tile_begin[t];
+      m.n = (uint32_t)(b.tile_end[t] - m.tb);
+      m.ib = b.inst_off[m.inst];
+      m.guess = b.inst[m.inst].guess;
+      const uint32_t bytes = m.n * (uint32_t)sizeof(cs_event);
+      mbar_expect_tx(&s_bar[s], bytes);
+      bulk_g2s(s_tiles + s * kFTileBytes, b.ev + m.tb, bytes, &s_bar[s]);
+    }
+    s_meta[s] = m;
+  };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kFStages; ++s) mbar_init(&s_bar[s], 1);
@@ -1715,30 +1858,16 @@ __global__ void __launch_bounds__(kFThreads, 2)
     s_names[i] = b.names[i];
   rows_zero(s_rows);
   __syncthreads();
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < kFStages; ++s) {
-      const uint32_t t = atomicAdd(fm.ticket, 1u);
-      s_stage_tile[s] = t;
-      if (t < b.n_tiles) {
-        const u64 tb = b.tile_begin[t], te = b.tile_end[t];
-        const uint32_t bytes = (uint32_t)((te - tb) * sizeof(cs_event));
-        mbar_expect_tx(&s_bar[s], bytes);
-        bulk_g2s(s_tiles + s * kFTileBytes, b.ev + tb, bytes, &s_bar[s]);
-      }
-    }
-  }
+  if (threadIdx.x == 0)
+    for (int s = 0; s < kFStages; ++s) issue(s);
   __syncthreads();
   uint32_t cur_inst = 0xffffffffu;
   for (uint32_t it = 0;; ++it) {
     const int stage = it % kFStages;
     const uint32_t parity = (it / kFStages) & 1u;
-    const uint32_t t = s_stage_tile[stage];
-    if (t >= b.n_tiles) break;
-    const uint32_t inst = b.tile_inst[t];
-    const u64 tb = b.tile_begin[t], te = b.tile_end[t];
-    const uint32_t n = (uint32_t)(te - tb);
-    const u64 ib = b.inst_off[inst];
-    if (inst != cur_inst) {
+    const TileMeta m = s_meta[stage];
+    if (m.t >= b.n_tiles) break;
+    if (m.inst != cur_inst) {
       if (cur_inst != 0xffffffffu) {
         __syncthreads();
         rows_flush(b.stats + (u64)cur_inst * b.n_names, s_rows);
@@ -1746,10 +1875,9 @@ __global__ void __launch_bounds__(kFThreads, 2)
         rows_zero(s_rows);
         __syncthreads();
       }
-      cur_inst = inst;
+      cur_inst = m.inst;
     }
-    const uint32_t anchor = b.inst[inst].guess;
-    NameStat* gstats = b.stats + (u64)inst * b.n_names;
+    NameStat* gstats = b.stats + (u64)m.inst * b.n_names;
     mbar_wait(&s_bar[stage], parity);
     const cs_event* tile = reinterpret_cast<const cs_event*>(s_tiles + stage * kFTileBytes);
 
@@ -1762,7 +1890,7 @@ __global__ void __launch_bounds__(kFThreads, 2)
       bool is_anchor = false, py = false;
       uint32_t name = 0;
       i64 d = 0;
-      if (e_idx < n) {
+      if (e_idx < m.n) {
         const int4 h1 = reinterpret_cast<const int4*>(tile + e_idx)[1];
         name = (uint32_t)h1.x;
         const uint32_t kind = (uint32_t)h1.y & 0xffu;
@@ -1773,7 +1901,7 @@ __global__ void __launch_bounds__(kFThreads, 2)
             const int4 h0 = reinterpret_cast<const int4*>(tile + e_idx)[0];
             d = (i64)(((u64)(uint32_t)h0.w << 32) | (uint32_t)h0.z);
           }
-          is_anchor = name == anchor;
+          is_anchor = name == m.guess;
         }
       }
       rows_add(s_rows + warp * kWarpNameRows, gstats, py, name, d);
@@ -1791,45 +1919,45 @@ __global__ void __launch_bounds__(kFThreads, 2)
     }
 #pragma unroll
     for (int j = 0; j < kIt; ++j) {
-      const uint32_t m = masks[j];
-      if (m & (1u << lane)) {
+      const uint32_t mk = masks[j];
+      if (mk & (1u << lane)) {
         const uint32_t e_idx = (uint32_t)warp * (kIt * 32) + j * 32 + lane;
-        const uint32_t r = base + __popc(m & lanemask_lt());
+        const uint32_t r = base + __popc(mk & lanemask_lt());
         const cs_event* p = tile + e_idx;
         s_apos[r] = (uint16_t)e_idx;
         s_astart[r] = p->start_ts;
         s_aend[r] = p->start_ts + p->duration;
       }
-      base += __popc(m);
+      base += __popc(mk);
     }
     __syncthreads();
     if (warp == 0) {
-      // 2. global rank of this tile's first anchor (overlaps the cycle work)
-      const u64 P0 = lookback_global(fm.state, t, total);
+      // 2. global rank of this tile's first anchor, overlapping the cycle work
+      const u64 P0 = (fm.debug & 1) ? 0 : lookback_global(fm.state, m.t, total);
       if (lane == 0) {
-        fm.t_cnt[t] = total;
-        fm.t_pref[t] = P0;
+        fm.t_cnt[m.t] = total;
+        fm.t_pref[m.t] = P0;
         if (P0 + total > fm.capacity) atomicOr(fm.overflow, 1u);
       }
-      // boundary cycles: the trailing one, and k = 0 when its equal-start
-      // group begins before the tile
-      if (lane == 0 && total > 0 && P0 + total <= fm.capacity) {
+      // boundary cycles -> fixup: the trailing one (end anchor in a later
+      // tile) and k = 0 if its equal-start group reaches the tile start
+      if (total > 0 && P0 + total <= fm.capacity) {
         uint32_t p0 = s_apos[0];
         while (p0 > 0 && tile[p0 - 1].start_ts == s_astart[0]) --p0;
-        const bool lead = p0 == 0 && tb > ib && b.ev[tb - 1].start_ts == s_astart[0];
-        for (uint32_t k = 0; k < total; ++k) {
+        const bool lead = p0 == 0 && m.tb > m.ib;
+        for (uint32_t k = lane; k < total; k += 32) {
           const bool trailing = k + 1 == total;
           if (!(trailing || (k == 0 && lead))) continue;
           const u64 g = P0 + k;
           b.c_start[g] = s_astart[k];
-          b.c_apos[g] = tb + s_apos[k];
+          b.c_apos[g] = m.tb + s_apos[k];
           b.c_aend[g] = s_aend[k];
-          b.c_inst[g] = inst;
+          b.c_inst[g] = m.inst;
           if (!trailing) {
             b.c_end[g] = s_astart[k + 1];
             uint32_t pl = s_apos[k + 1];
             while (pl > 0 && tile[pl - 1].start_ts == s_astart[k + 1]) --pl;
-            b.c_last[g] = tb + pl;
+            b.c_last[g] = m.tb + pl;
           }
           const unsigned int slot = atomicAdd(fm.fix_n, 1u);
           fm.fix_list[slot] = g;
@@ -1841,36 +1969,41 @@ __global__ void __launch_bounds__(kFThreads, 2)
         __threadfence_block();
         s_ready = it + 1;
       }
-    } else if (is_cyc) {
+    } else if (is_cyc && !(fm.debug & 2)) {
       // 3. local cycles, one thread each, from shared memory
       for (uint32_t k = (uint32_t)ct; k + 1 < total; k += n_cyc_threads) {
         const i64 cs = s_astart[k], ce = s_astart[k + 1];
         uint32_t pf = s_apos[k];
         while (pf > 0 && tile[pf - 1].start_ts == cs) --pf;
-        if (pf == 0 && k == 0 && tb > ib && b.ev[tb - 1].start_ts == cs) continue;  // lead: fixup
+        if (pf == 0 && k == 0 && m.tb > m.ib) continue;  // lead boundary: fixup
         uint32_t pl = s_apos[k + 1];
         while (pl > 0 && tile[pl - 1].start_ts == ce) --pl;
-        const CycAcc acc = accumulate_cycle(names, cfg, do_beta, tile, pf, pl, cs, ce, false,
-                                            my_beta, my_coll, my_colln);
-        while (s_ready != it + 1) {
+        if constexpr (kReg) {
+          CycAccR<kFRegC, kFRegR> acc;
+          accumulate_cycle_reg<kFRegC, kFRegR>(s_names, do_beta, tile, pf, pl, cs, ce, acc);
+          while (s_ready != it + 1) {
+          }
+          const u64 g = s_P + k;
+          if (g + 1 <= fm.capacity)
+            write_cycle_reg<kFRegC, kFRegR>(b, cfg, do_beta, acc, g, m.inst, cs, ce,
+                                            m.tb + s_apos[k], s_aend[k], m.tb + pf, m.tb + pl);
+        } else {
+          const cs_name_info* names = b.n_names <= (uint32_t)kFNamesSmem ? s_names : b.names;
+          const CycAcc acc = accumulate_cycle(names, cfg, do_beta, tile, pf, pl, cs, ce, false,
+                                              my_beta, my_coll, my_colln);
+          while (s_ready != it + 1) {
+          }
+          const u64 g = s_P + k;
+          if (g + 1 <= fm.capacity)
+            write_cycle(b, cfg, do_beta, acc, g, m.inst, cs, ce, m.tb + s_apos[k], s_aend[k],
+                        m.tb + pf, m.tb + pl, my_beta, my_coll, my_colln);
         }
-        const u64 g = s_P + k;
-        if (g + 1 <= fm.capacity)
-          write_cycle(b, cfg, do_beta, acc, g, inst, cs, ce, tb + s_apos[k], s_aend[k], tb + pf,
-                      tb + pl, my_beta, my_coll, my_colln);
       }
     }
-    __syncthreads();  // stage and anchor list consumed
+    __syncthreads();  // stage, anchor list and meta consumed
     if (threadIdx.x == 0) {
-      const uint32_t t2 = atomicAdd(fm.ticket, 1u);
-      s_stage_tile[stage] = t2;
-      if (t2 < b.n_tiles) {
-        const u64 nb = b.tile_begin[t2], ne = b.tile_end[t2];
-        const uint32_t bytes = (uint32_t)((ne - nb) * sizeof(cs_event));
-        fence_proxy_async();
-        mbar_expect_tx(&s_bar[stage], bytes);
-        bulk_g2s(s_tiles + stage * kFTileBytes, b.ev + nb, bytes, &s_bar[stage]);
-      }
+      fence_proxy_async();
+      issue(stage);
     }
     __syncthreads();
   }
@@ -1969,35 +2102,39 @@ uint32_t fused_scratch_words(const DevConfig& cfg) {
 int launch_fused_segment(const DevBuffers& b, const DevConfig& cfg, const FusedMetaHost& mh,
                          int do_beta, cudaStream_t s, uint64_t* launches) {
   if (b.n_tiles == 0) return 0;
-  FusedMeta fm{mh.state, mh.ticket, mh.t_cnt, mh.t_pref, mh.fix_list, mh.fix_n, mh.fix_flags,
-               mh.capacity, mh.overflow};
+  FusedMeta fm{mh.debug, mh.state, mh.ticket, mh.t_cnt, mh.t_pref, mh.fix_list, mh.fix_n,
+               mh.fix_flags, mh.capacity, mh.overflow};
+  const bool reg = cfg.cyc.n_beta_slots <= kFRegC && cfg.cyc.n_comm_slots <= kFRegR &&
+                   b.n_names <= (uint32_t)kFNamesSmem;
   const uint32_t words = fused_scratch_words(cfg);
-  // budget: two CTAs per SM (<= ~113 KB each)
   const int fixed = kFStages * (int)kFTileBytes + kFTile * (2 + 16);
-  const int budget = 100 * 1024 - fixed;
-  uint32_t cyc_threads = budget > 0 ? (uint32_t)(budget / (int)(words * 4)) : 0;
-  const uint32_t max_ct = (uint32_t)kFThreads - 32;
-  if (cyc_threads > max_ct) cyc_threads = max_ct;
-  cyc_threads &= ~31u;
-  if (cyc_threads < 32) return -1;  // configuration too wide for the fused kernel
-  const int smem = fixed + (int)(cyc_threads * words * 4);
-  cudaFuncSetAttribute(k_fused_segment, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  uint32_t cyc_threads = (uint32_t)kFThreads - 32;
+  int smem = fixed;
+  if (!reg) {
+    const int budget = 100 * 1024 - fixed;
+    uint32_t c = budget > 0 ? (uint32_t)(budget / (int)(words * 4)) : 0;
+    if (c < cyc_threads) cyc_threads = c & ~31u;
+    if (cyc_threads < 32) return -1;  // configuration too wide for the fused kernel
+    smem = fixed + (int)(cyc_threads * words * 4);
+  }
+  auto kern = reg ? k_fused_segment<true> : k_fused_segment<false>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   int per_sm = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fused_segment, kFThreads, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kFThreads, smem);
   if (per_sm < 1) per_sm = 1;
   const uint32_t want = (uint32_t)(sms * per_sm);
   const uint32_t grid = b.n_tiles < want ? b.n_tiles : want;
-  k_fused_segment<<<grid, kFThreads, smem, s>>>(b, cfg, fm, do_beta, cyc_threads);
+  kern<<<grid, kFThreads, smem, s>>>(b, cfg, fm, do_beta, cyc_threads);
   ++*launches;
   return 0;
 }
 
 void launch_fused_inst(const DevBuffers& b, const FusedMetaHost& mh, uint64_t* cyc_off,
                        cudaStream_t s, uint64_t* launches) {
-  FusedMeta fm{mh.state, mh.ticket, mh.t_cnt, mh.t_pref, mh.fix_list, mh.fix_n, mh.fix_flags,
+  FusedMeta fm{mh.debug, mh.state, mh.ticket, mh.t_cnt, mh.t_pref, mh.fix_list, mh.fix_n, mh.fix_flags,
                mh.capacity, mh.overflow};
   k_fused_inst<<<(b.n_inst + 1 + 255) / 256, 256, 0, s>>>(b, fm, cyc_off);
   ++*launches;
@@ -2006,7 +2143,7 @@ void launch_fused_inst(const DevBuffers& b, const FusedMetaHost& mh, uint64_t* c
 void launch_fixup_cycles(const DevBuffers& b, const DevConfig& cfg, const FusedMetaHost& mh,
                          int do_beta, uint32_t n_fix, cudaStream_t s, uint64_t* launches) {
   if (!n_fix) return;
-  FusedMeta fm{mh.state, mh.ticket, mh.t_cnt, mh.t_pref, mh.fix_list, mh.fix_n, mh.fix_flags,
+  FusedMeta fm{mh.debug, mh.state, mh.ticket, mh.t_cnt, mh.t_pref, mh.fix_list, mh.fix_n, mh.fix_flags,
                mh.capacity, mh.overflow};
   const uint32_t words = fused_scratch_words(cfg);
   const int threads = 64;

@@ -65,6 +65,8 @@ def lib():
     L.cs_get_beta.argtypes = [vp, u32, vp, vp, sz, psz]
     L.cs_get_collective_beta.argtypes = [vp, u32, vp, vp, sz, psz]
     L.cs_set_option.argtypes = [vp, C.c_int, C.c_int64]
+    L.cs_microbench.argtypes = [C.c_int, vp, u64, C.c_int, C.c_int, C.c_int, C.c_int,
+                                C.POINTER(C.c_double)]
     L.cs_host_alloc.argtypes = [sz, C.POINTER(vp)]
     L.cs_host_free.argtypes = [vp]
     L.cs_get_timings.argtypes = [vp, vp, sz, psz, C.c_char_p, sz]
@@ -98,7 +100,7 @@ EXPORTED_SYMBOLS = [
     "cs_host_free", "cs_get_timings", "cs_get_launch_count", "cs_fit_latency_model",
     "cs_model_from_json", "cs_model_to_json", "cs_model_view", "cs_model_free",
     "cs_ucl_from_stats", "cs_compute_ucl", "cs_config_from_json", "cs_synth_generate",
-    "cs_synth_view", "cs_synth_names", "cs_synth_free", "cs_set_option",
+    "cs_synth_view", "cs_synth_names", "cs_synth_free", "cs_set_option", "cs_microbench",
 ]
 
 
