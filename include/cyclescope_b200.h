@@ -305,9 +305,10 @@ int cs_get_collective_beta(cs_ctx* ctx, uint32_t inst, double* beta,
 int cs_get_records(cs_ctx* ctx, uint32_t inst, cs_record* buf, size_t cap, size_t* n);
 int cs_get_alerts(cs_ctx* ctx, uint32_t inst, cs_alert* buf, size_t cap, size_t* n);
 
-/* Execution options.  CS_OPT_FUSED (default 1): single-pass fused
- * segmentation (k_fused_segment) when applicable; 0 forces the general
- * multi-kernel path (both are bit-identical; tests run both). */
+/* Execution options.  CS_OPT_FUSED (default 0): 1 selects the single-pass
+ * fused segmentation kernel (k_fused_segment) when applicable; 0 runs the
+ * two-pass path (TMA-staged scan + thread-per-cycle reduce), currently the
+ * faster one.  Both are bit-identical; the tests run both. */
 #define CS_OPT_FUSED 1
 int cs_set_option(cs_ctx* ctx, int option, int64_t value);
 

@@ -93,8 +93,9 @@ struct cs_ctx {
   std::vector<uint64_t> n_cyc;     // cycles per instance
   uint64_t n_cycles = 0;           // cycle slots (fused path: + one hole per instance)
   uint64_t slot_cap = 0;
-  bool allow_fused = true;
+  bool allow_fused = false;  // two-pass path is faster today
   int fused_debug = 0;
+  int reduce_variant = 0;  // 0 thread-per-cycle, 1 warp-per-cycle
   bool used_fused = false;
   DevBuf d_fstate, d_fticket, d_fcnt, d_fpref, d_fixlist, d_fixn, d_fixflags, d_foverflow;
   DevBuf d_cyc_off, c_start, c_end, c_apos, c_aend, c_first, c_last, c_inst, c_stage, c_local,
@@ -879,7 +880,10 @@ int cs_run(cs_ctx* ctx, uint32_t mask) {
                          ctx->inst_off[i + 1], f_t0[i], f_period[i], ctx->fallback_cycles[i],
                          ctx->cyc_off[i], b, i, s, &ctx->launches);
   e4 = record_event(ctx, 4);
-  launch_cycle_reduce(b, cfg, (mask & CS_RUN_BETA) ? 1 : 0, s, &ctx->launches);
+  if (ctx->reduce_variant == 0)
+    launch_cycle_reduce_tpc(b, cfg, (mask & CS_RUN_BETA) ? 1 : 0, s, &ctx->launches);
+  else
+    launch_cycle_reduce(b, cfg, (mask & CS_RUN_BETA) ? 1 : 0, s, &ctx->launches);
   e5 = record_event(ctx, 5);
   ctx->timed.push_back({"bounds", {e3, e4}});
   ctx->timed.push_back({"cycle_reduce", {e4, e5}});
@@ -1200,6 +1204,10 @@ int cs_set_option(cs_ctx* ctx, int option, int64_t value) {
   if (!ctx) return CS_E_INVALID_ARGUMENT;
   if (option == CS_OPT_FUSED) {
     ctx->allow_fused = value != 0;
+    return CS_OK;
+  }
+  if (option == 98) {  // profiling: multi-kernel reduce variant
+    ctx->reduce_variant = static_cast<int>(value);
     return CS_OK;
   }
   if (option == 99) {  // profiling only (outputs invalid): fused-kernel ablations

@@ -154,6 +154,8 @@ void launch_fold(const DevBuffers& b, const DevConfig& cfg, const uint32_t* pair
 void launch_bounds(const DevBuffers& b, cudaStream_t s, uint64_t* launches);
 void launch_cycle_reduce(const DevBuffers& b, const DevConfig& cfg, int do_beta,
                          cudaStream_t s, uint64_t* launches);
+void launch_cycle_reduce_tpc(const DevBuffers& b, const DevConfig& cfg, int do_beta,
+                             cudaStream_t s, uint64_t* launches);
 void launch_stage_heuristic(const DevBuffers& b, const DevConfig& cfg, cudaStream_t s,
                             uint64_t* launches);
 void launch_records(const DevBuffers& b, const DevConfig& cfg, uint64_t n_blocks_cap,

@@ -1516,13 +1516,17 @@ constexpr uint32_t kFTileBytes = kFTile * sizeof(cs_event);
 constexpr u64 kFlagAggF = 1ull << 62;
 constexpr u64 kFlagPrefixF = 2ull << 62;
 
-__device__ u64 lookback_global(u64* state, uint32_t tile, u64 agg) {
+// Aggregate publication is separated from the look-back wait so a CTA can
+// publish a prefetched tile's anchor count the moment its bytes land — long
+// before it processes that tile — and successors never wait on processing.
+__device__ __forceinline__ void publish_aggregate(u64* state, uint32_t tile, u64 agg) {
+  st_release(&state[tile], (tile == 0 ? kFlagPrefixF : kFlagAggF) | agg);
+}
+
+// warp-wide: exclusive prefix of tile `tile` (its aggregate already published)
+__device__ u64 lookback_wait(u64* state, uint32_t tile, u64 agg) {
   const int lane = threadIdx.x & 31;
-  if (tile == 0) {
-    if (lane == 0) st_release(&state[0], kFlagPrefixF | agg);
-    return 0;
-  }
-  if (lane == 0) st_release(&state[tile], kFlagAggF | agg);
+  if (tile == 0) return 0;
   u64 excl = 0;
   i64 j = (i64)tile - 1 - lane;
   while (true) {
@@ -1541,6 +1545,19 @@ __device__ u64 lookback_global(u64* state, uint32_t tile, u64 agg) {
   }
   if (lane == 0) st_release(&state[tile], kFlagPrefixF | (excl + agg));
   return excl;
+}
+
+// warp-wide anchor count of a staged tile
+__device__ __forceinline__ uint32_t warp_count_anchors(const cs_event* tile, uint32_t n,
+                                                       uint32_t guess) {
+  const int lane = threadIdx.x & 31;
+  uint32_t c = 0;
+  for (uint32_t e = lane; e < n; e += 32) {
+    const int4 h1 = reinterpret_cast<const int4*>(tile + e)[1];
+    c += ((((uint32_t)h1.y & 0xffu) == CS_SPAN) && (uint32_t)h1.x == guess) ? 1u : 0u;
+  }
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  return c;
 }
 
 // Sequential per-cycle reduction by one thread over ev[first, last): the
@@ -1861,6 +1878,15 @@ __global__ void __launch_bounds__(kFThreads, 2)
   if (threadIdx.x == 0)
     for (int s = 0; s < kFStages; ++s) issue(s);
   __syncthreads();
+  if (warp == 0 && !(fm.debug & 1)) {  // publish the first tile's aggregate on arrival
+    const TileMeta m0 = s_meta[0];
+    if (m0.t < b.n_tiles) {
+      mbar_wait(&s_bar[0], 0);
+      const uint32_t c = warp_count_anchors(reinterpret_cast<const cs_event*>(s_tiles), m0.n,
+                                            m0.guess);
+      if (lane == 0) publish_aggregate(fm.state, m0.t, c);
+    }
+  }
   uint32_t cur_inst = 0xffffffffu;
   for (uint32_t it = 0;; ++it) {
     const int stage = it % kFStages;
@@ -1932,8 +1958,19 @@ __global__ void __launch_bounds__(kFThreads, 2)
     }
     __syncthreads();
     if (warp == 0) {
-      // 2. global rank of this tile's first anchor, overlapping the cycle work
-      const u64 P0 = (fm.debug & 1) ? 0 : lookback_global(fm.state, m.t, total);
+      // 2a. publish-ahead: the next staged tile's anchor count, as soon as it lands
+      if (!(fm.debug & 1)) {
+        const int ns = (it + 1) % kFStages;
+        const TileMeta mn = s_meta[ns];
+        if (mn.t < b.n_tiles) {
+          mbar_wait(&s_bar[ns], ((it + 1) / kFStages) & 1u);
+          const uint32_t c = warp_count_anchors(
+              reinterpret_cast<const cs_event*>(s_tiles + ns * kFTileBytes), mn.n, mn.guess);
+          if (lane == 0) publish_aggregate(fm.state, mn.t, c);
+        }
+      }
+      // 2b. global rank of this tile's first anchor, overlapping the cycle work
+      const u64 P0 = (fm.debug & 1) ? 0 : lookback_wait(fm.state, m.t, total);
       if (lane == 0) {
         fm.t_cnt[m.t] = total;
         fm.t_pref[m.t] = P0;
@@ -2151,6 +2188,63 @@ void launch_fixup_cycles(const DevBuffers& b, const DevConfig& cfg, const FusedM
   cudaFuncSetAttribute(k_fixup_cycles, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   k_fixup_cycles<<<(n_fix + threads - 1) / threads, threads, smem, s>>>(b, cfg, fm, do_beta, n_fix,
                                                                        words);
+  ++*launches;
+}
+
+// ------------------------------------------ K3' thread-per-cycle reduce
+// One thread per cycle, sequential over its events straight from global
+// memory (each thread's range is contiguous; neighbours' ranges are adjacent,
+// so sectors are consumed from L1 across the warp).  Thousands of cycles in
+// flight per SM hide the latency; no warp-level reductions or atomics.
+template <bool kReg>
+__global__ void __launch_bounds__(256)
+    k_cycle_reduce_tpc(DevBuffers b, DevConfig cfg, int do_beta) {
+  extern __shared__ __align__(16) uint32_t s_scr[];
+  __shared__ cs_name_info s_names[kFNamesSmem];
+  for (uint32_t i = threadIdx.x; i < b.n_names && i < (uint32_t)kFNamesSmem; i += blockDim.x)
+    s_names[i] = b.names[i];
+  __syncthreads();
+  const u64 g = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= b.n_cycles) return;
+  const i64 cs = b.c_start[g], ce = b.c_end[g];
+  const u64 first = b.c_first[g], last = b.c_last[g];
+  const u64 apos = b.c_apos[g];
+  const uint32_t inst = b.c_inst[g];
+  if constexpr (kReg) {
+    CycAccR<kFRegC, kFRegR> acc;
+    accumulate_cycle_reg<kFRegC, kFRegR>(s_names, do_beta, b.ev + first, 0,
+                                         (uint32_t)(last - first), cs, ce, acc);
+    if (apos == kNone)  // frequency-fallback cycles carry no component map
+      for (int i = 0; i < kMaxPhases; ++i) acc.comp[i] = 0;
+    write_cycle_reg<kFRegC, kFRegR>(b, cfg, do_beta, acc, g, inst, cs, ce, apos, b.c_aend[g],
+                                    first, last);
+  } else {
+    const uint32_t sw = scratch_words(cfg);
+    i64* beta = reinterpret_cast<i64*>(s_scr + (u64)threadIdx.x * sw);
+    double* coll = reinterpret_cast<double*>(beta + cfg.cyc.n_beta_slots);
+    uint32_t* colln = reinterpret_cast<uint32_t*>(coll + cfg.cyc.n_comm_slots);
+    const cs_name_info* names = b.n_names <= (uint32_t)kFNamesSmem ? s_names : b.names;
+    const CycAcc acc = accumulate_cycle(names, cfg, do_beta, b.ev, first, last, cs, ce,
+                                        apos == kNone, beta, coll, colln);
+    write_cycle(b, cfg, do_beta, acc, g, inst, cs, ce, apos, b.c_aend[g], first, last, beta, coll,
+                colln);
+  }
+}
+
+void launch_cycle_reduce_tpc(const DevBuffers& b, const DevConfig& cfg, int do_beta,
+                             cudaStream_t s, uint64_t* launches) {
+  if (!b.n_cycles) return;
+  const bool reg = cfg.cyc.n_beta_slots <= kFRegC && cfg.cyc.n_comm_slots <= kFRegR &&
+                   b.n_names <= (uint32_t)kFNamesSmem;
+  const unsigned grid = (unsigned)((b.n_cycles + 255) / 256);
+  if (reg) {
+    k_cycle_reduce_tpc<true><<<grid, 256, 0, s>>>(b, cfg, do_beta);
+  } else {
+    const int smem = 256 * (int)fused_scratch_words(cfg) * 4;
+    cudaFuncSetAttribute(k_cycle_reduce_tpc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         smem);
+    k_cycle_reduce_tpc<false><<<grid, 256, smem, s>>>(b, cfg, do_beta);
+  }
   ++*launches;
 }
 

@@ -13,7 +13,7 @@ from paper_2601_09258_b200 import runtime as rt
 
 
 def run_product(events, names, workloads, n_comm=0, run_config=None, model_json=None,
-                mask=abi.RUN_ALL, analyzer=None, fused=True):
+                mask=abi.RUN_ALL, analyzer=None, fused=False):
     """One instance through the C ABI; returns InstanceResult."""
     an = analyzer or rt.Analyzer()
     an.set_fused(fused)

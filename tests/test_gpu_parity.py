@@ -19,7 +19,7 @@ FAMILIES = ["cpu_contention", "cpu_freq_drop", "gpu_contention", "gpu_clock_lock
 
 
 def _ref_and_product(refbridge, analyzer, trace, run_config=None, train_cycles=2400,
-                     mask=abi.RUN_ALL, fused=True):
+                     mask=abi.RUN_ALL, fused=False):
     ref = trace.run(run_config, None, train_cycles)
     ex = trace.export(run_config)
     got, _ = run_product(ex.events, ex.names, ex.workloads, n_comm=len(ex.comm_hash),

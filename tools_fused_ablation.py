@@ -20,3 +20,7 @@ an.set_fused(False)
 for i in range(4):
     an.run(abi.RUN_SEGMENT | abi.RUN_BETA)
 tm = an.timings(); print("legacy", {k: round(v, 3) for k, v in tm.items()})
+an.L.cs_set_option(an.h, 98, 1)
+for i in range(4):
+    an.run(abi.RUN_SEGMENT | abi.RUN_BETA)
+tm = an.timings(); print("legacy warp-per-cycle", {k: round(v, 3) for k, v in tm.items()})
