@@ -264,104 +264,233 @@ __device__ __forceinline__ void rows_add(WarpNameRow* wrows, NameStat* g, bool p
   r.sq_lo = nl;
 }
 
+// Per-thread cache of PythonCall moments (typical traces have a handful of
+// PythonCall names): no warp synchronisation on the hot loop; a miss falls
+// back to global atomics.  Flushed through the warp rows at instance changes.
+constexpr int kNameCache = 4;
+struct NameCache {
+  uint32_t name[kNameCache];
+  uint32_t cnt[kNameCache];
+  u64 sum[kNameCache], lo[kNameCache], hi[kNameCache];
+};
+
+__device__ __forceinline__ void cache_clear(NameCache& c) {
+#pragma unroll
+  for (int i = 0; i < kNameCache; ++i) {
+    c.name[i] = 0xffffffffu;
+    c.cnt[i] = 0;
+    c.sum[i] = c.lo[i] = c.hi[i] = 0;
+  }
+}
+
+__device__ __forceinline__ void cache_add(NameCache& c, NameStat* g, uint32_t name, i64 d) {
+  u64 lo, hi;
+  square_u128(d, lo, hi);
+  int hit = -1, free_slot = -1;
+#pragma unroll
+  for (int i = 0; i < kNameCache; ++i) {
+    if (c.name[i] == name) hit = i;
+    if (c.name[i] == 0xffffffffu && free_slot < 0) free_slot = i;
+  }
+  if (hit < 0 && free_slot >= 0) {
+    hit = free_slot;
+#pragma unroll
+    for (int i = 0; i < kNameCache; ++i)
+      if (i == free_slot) c.name[i] = name;
+  }
+  if (hit < 0) {
+    atomicAdd(&g[name].count, 1ull);
+    atomicAdd(&g[name].sum, (u64)d);
+    atomic_add_u128(&g[name].sumsq_lo, &g[name].sumsq_hi, lo, hi);
+    return;
+  }
+#pragma unroll
+  for (int i = 0; i < kNameCache; ++i) {
+    if (i == hit) {
+      c.cnt[i] += 1;
+      c.sum[i] += (u64)d;
+      const u64 nl = c.lo[i] + lo;
+      c.hi[i] += hi + (nl < c.lo[i] ? 1ull : 0ull);
+      c.lo[i] = nl;
+    }
+  }
+}
+
+// warp-wide: fold (name, cnt, sum, lo, hi) contributions into the warp's rows
+__device__ __forceinline__ void rows_merge(WarpNameRow* wrows, NameStat* g, bool valid,
+                                           uint32_t name, uint32_t cnt, u64 sum, u64 lo, u64 hi) {
+  __syncwarp();
+  const uint32_t key = valid ? name : 0xffffffffu;
+  const uint32_t grp = __match_any_sync(0xffffffffu, key);
+  if (!valid) return;
+  const int lane = threadIdx.x & 31;
+  const int leader = __ffs(grp) - 1;
+  uint32_t rest = grp & ~(1u << leader);
+  while (rest) {
+    const int src = __ffs(rest) - 1;
+    rest &= rest - 1;
+    const uint32_t oc = __shfl_sync(grp, cnt, src);
+    const u64 os = __shfl_sync(grp, sum, src);
+    const u64 ol = __shfl_sync(grp, lo, src);
+    const u64 oh = __shfl_sync(grp, hi, src);
+    if (lane == leader) {
+      cnt += oc;
+      sum += os;
+      const u64 nl = lo + ol;
+      hi += oh + (nl < lo ? 1ull : 0ull);
+      lo = nl;
+    }
+  }
+  if (lane != leader) return;
+  int row = -1;
+  for (int i = 0; i < kWarpNameRows; ++i) {
+    const uint32_t n = wrows[i].name;
+    if (n == name) { row = i; break; }
+    if (n == 0xffffffffu) {
+      const uint32_t old = atomicCAS(&wrows[i].name, 0xffffffffu, name);
+      if (old == 0xffffffffu || old == name) { row = i; break; }
+    }
+  }
+  if (row < 0) {
+    atomicAdd(&g[name].count, (u64)cnt);
+    atomicAdd(&g[name].sum, sum);
+    atomic_add_u128(&g[name].sumsq_lo, &g[name].sumsq_hi, lo, hi);
+    return;
+  }
+  WarpNameRow& r = wrows[row];
+  r.cnt += cnt;
+  r.sum += sum;
+  const u64 nl = r.sq_lo + lo;
+  r.sq_hi += hi + (nl < r.sq_lo ? 1ull : 0ull);
+  r.sq_lo = nl;
+}
+
+// whole CTA (converged): per-thread caches -> warp rows -> warp 0's rows ->
+// a few global atomics per name and CTA.  Called once per instance switch.
+__device__ void cache_flush(NameCache& c, NameStat* g, WarpNameRow* rows) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nw = blockDim.x / 32;
+  for (int i = threadIdx.x; i < nw * kWarpNameRows; i += blockDim.x) {
+    rows[i].name = 0xffffffffu;
+    rows[i].cnt = 0;
+    rows[i].sum = rows[i].sq_lo = rows[i].sq_hi = 0;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < kNameCache; ++i)
+    rows_merge(rows + warp * kWarpNameRows, g, c.name[i] != 0xffffffffu && c.cnt[i] > 0,
+               c.name[i], c.cnt[i], c.sum[i], c.lo[i], c.hi[i]);
+  __syncthreads();
+  if (warp == 0) {
+    for (int w = 1; w < nw; ++w) {
+      const WarpNameRow r = rows[w * kWarpNameRows + (lane & (kWarpNameRows - 1))];
+      const bool v = lane < kWarpNameRows && r.name != 0xffffffffu && r.cnt > 0;
+      rows_merge(rows, g, v, r.name, r.cnt, r.sum, r.sq_lo, r.sq_hi);
+    }
+    __syncwarp();
+    if (lane < kWarpNameRows) {
+      const WarpNameRow r = rows[lane];
+      if (r.name != 0xffffffffu && r.cnt) {
+        atomicAdd(&g[r.name].count, (u64)r.cnt);
+        atomicAdd(&g[r.name].sum, r.sum);
+        atomic_add_u128(&g[r.name].sumsq_lo, &g[r.name].sumsq_hi, r.sq_lo, r.sq_hi);
+      }
+    }
+  }
+  __syncthreads();
+  cache_clear(c);
+}
+
+struct ScanMeta {
+  uint32_t t, inst, n, anchor, active;
+  u64 tb;
+};
+
 __global__ void __launch_bounds__(kScanThreads, 1)
     k_scan_events(DevBuffers b, int mode, const uint32_t* __restrict__ list, uint32_t n_list,
                   int sample) {
   extern __shared__ __align__(128) unsigned char s_tiles[];
   __shared__ uint64_t s_bar[kStages];
-  __shared__ WarpNameRow s_rows[(kScanThreads / 32) * kWarpNameRows];
+  __shared__ ScanMeta s_meta[kStages];
   __shared__ uint32_t s_warp_cnt[kScanThreads / 32];
+  __shared__ WarpNameRow s_rows[(kScanThreads / 32) * kWarpNameRows];
 
   const bool do_stats = mode & 1;
   const bool do_anchor = (mode & 2) && !sample;
   const bool redo = mode & 4;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const uint32_t nn = b.n_names < (uint32_t)kSmemNames ? b.n_names : (uint32_t)kSmemNames;
   const uint32_t G = gridDim.x;
   constexpr int kWarps = kScanThreads / 32;
-  constexpr int kIt = kTileEvents / kScanThreads;  // 32-event groups per warp per tile
+  constexpr int kIt = kTileEvents / kScanThreads;
 
-  auto tile_of = [&](uint32_t k) { return list ? list[k] : k; };
-  auto tile_span = [&](uint32_t t, u64& tb, u64& te) {
-    tb = b.tile_begin[t];
-    te = b.tile_end[t];
-    if (sample) {
-      const u64 lim = b.inst_off[b.tile_inst[t]] + kSampleEvents;
-      te = te < lim ? te : lim;
-      if (te < tb) te = tb;
+  auto issue = [&](int s, uint32_t k) {  // thread 0
+    ScanMeta m{};
+    m.t = k < n_list ? (list ? list[k] : k) : 0xffffffffu;
+    if (k < n_list) {
+      m.inst = b.tile_inst[m.t];
+      m.tb = b.tile_begin[m.t];
+      u64 te = b.tile_end[m.t];
+      if (sample) {
+        const u64 lim = b.inst_off[m.inst] + kSampleEvents;
+        te = te < lim ? te : lim;
+        if (te < m.tb) te = m.tb;
+      }
+      m.n = (uint32_t)(te - m.tb);
+      m.active = do_anchor;
+      m.anchor = 0xffffffffu;
+      if (do_anchor) {
+        const InstState& st = b.inst[m.inst];
+        m.anchor = redo ? st.anchor : st.guess;
+        if (redo && !st.redo) m.active = 0;
+      }
+      const uint32_t bytes = m.n * (uint32_t)sizeof(cs_event);
+      mbar_expect_tx(&s_bar[s], bytes);
+      if (bytes) bulk_g2s(s_tiles + s * kTileBytes, b.ev + m.tb, bytes, &s_bar[s]);
     }
+    s_meta[s] = m;
   };
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) mbar_init(&s_bar[s], 1);
     mbar_fence_init();
   }
-  if (do_stats) rows_zero(s_rows);
   __syncthreads();
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages; ++s) {
-      const uint32_t k = blockIdx.x + s * G;
-      if (k >= n_list) break;
-      u64 tb, te;
-      tile_span(tile_of(k), tb, te);
-      const uint32_t bytes = (uint32_t)((te - tb) * sizeof(cs_event));
-      mbar_expect_tx(&s_bar[s], bytes);
-      if (bytes) bulk_g2s(s_tiles + s * kTileBytes, b.ev + tb, bytes, &s_bar[s]);
-    }
-  }
+  if (threadIdx.x == 0)
+    for (int s = 0; s < kStages; ++s) issue(s, blockIdx.x + s * G);
+  __syncthreads();
+  NameCache cache;
+  cache_clear(cache);
   uint32_t cur_inst = 0xffffffffu;
   uint32_t it = 0;
   for (uint32_t k = blockIdx.x; k < n_list; k += G, ++it) {
     const int stage = it % kStages;
     const uint32_t parity = (it / kStages) & 1u;
-    const uint32_t t = tile_of(k);
-    const uint32_t inst = b.tile_inst[t];
-    u64 tb, te;
-    tile_span(t, tb, te);
-    const uint32_t n = (uint32_t)(te - tb);
-    if (do_stats && inst != cur_inst) {
-      if (cur_inst != 0xffffffffu) {
-        __syncthreads();
-        rows_flush(b.stats + (u64)cur_inst * b.n_names, s_rows);
-        __syncthreads();
-        rows_zero(s_rows);
-        __syncthreads();
-      }
-      cur_inst = inst;
+    const ScanMeta m = s_meta[stage];
+    if (do_stats && m.inst != cur_inst) {
+      if (cur_inst != 0xffffffffu) cache_flush(cache, b.stats + (u64)cur_inst * b.n_names, s_rows);
+      cur_inst = m.inst;
     }
-    uint32_t anchor = 0xffffffffu;
-    bool active = do_anchor;
-    if (do_anchor) {
-      const InstState& st = b.inst[inst];
-      anchor = redo ? st.anchor : st.guess;
-      if (redo && !st.redo) active = false;
-    }
-    NameStat* gstats = b.stats + (u64)inst * b.n_names;
+    NameStat* gstats = b.stats + (u64)m.inst * b.n_names;
     mbar_wait(&s_bar[stage], parity);
     const cs_event* tile = reinterpret_cast<const cs_event*>(s_tiles + stage * kTileBytes);
-
     uint32_t masks[kIt];
     uint32_t my = 0;
 #pragma unroll
     for (int j = 0; j < kIt; ++j) {
       const uint32_t e_idx = (uint32_t)warp * (kIt * 32) + j * 32 + lane;
-      bool is_anchor = false, py = false;
-      uint32_t name = 0;
-      i64 d = 0;
-      if (e_idx < n) {
+      bool is_anchor = false;
+      if (e_idx < m.n) {
         const int4 h1 = reinterpret_cast<const int4*>(tile + e_idx)[1];
-        name = (uint32_t)h1.x;
+        const uint32_t name = (uint32_t)h1.x;
         const uint32_t kind = (uint32_t)h1.y & 0xffu;
         const uint32_t cat = ((uint32_t)h1.y >> 8) & 0xffu;
         if (kind == CS_SPAN) {
-          py = do_stats && cat == CS_CAT_PYTHON_CALL;
-          if (py) {
+          if (do_stats && cat == CS_CAT_PYTHON_CALL) {
             const int4 h0 = reinterpret_cast<const int4*>(tile + e_idx)[0];
-            d = (i64)(((u64)(uint32_t)h0.w << 32) | (uint32_t)h0.z);
+            cache_add(cache, gstats, name, (i64)(((u64)(uint32_t)h0.w << 32) | (uint32_t)h0.z));
           }
-          is_anchor = active && name == anchor;
+          is_anchor = m.active && name == m.anchor;
         }
       }
-      if (do_stats) rows_add(s_rows + warp * kWarpNameRows, gstats, py, name, d);
       masks[j] = __ballot_sync(0xffffffffu, is_anchor);
       my += __popc(masks[j]);
     }
@@ -375,39 +504,33 @@ __global__ void __launch_bounds__(kScanThreads, 1)
         base += w < warp ? c : 0;
         total += c;
       }
-      if (active) {
+      if (m.active) {
 #pragma unroll
         for (int j = 0; j < kIt; ++j) {
-          const uint32_t m = masks[j];
-          if (m & (1u << lane)) {
+          const uint32_t mk = masks[j];
+          if (mk & (1u << lane)) {
             const uint32_t e_idx = (uint32_t)warp * (kIt * 32) + j * 32 + lane;
-            const u64 r = tb + base + __popc(m & lanemask_lt());
+            const u64 r = m.tb + base + __popc(mk & lanemask_lt());
             const cs_event* p = tile + e_idx;
-            b.a_pos[r] = tb + e_idx;
+            b.a_pos[r] = m.tb + e_idx;
             b.a_start[r] = p->start_ts;
             b.a_end[r] = p->start_ts + p->duration;
           }
-          base += __popc(m);
+          base += __popc(mk);
         }
-        if (threadIdx.x == 0) b.tile_cnt[t] = total;
+        if (threadIdx.x == 0) b.tile_cnt[m.t] = total;
       }
     }
     __syncthreads();  // every thread is done with this stage
     if (threadIdx.x == 0) {
-      const uint32_t k2 = k + kStages * G;
-      if (k2 < n_list) {
-        u64 nb, ne;
-        tile_span(tile_of(k2), nb, ne);
-        const uint32_t bytes = (uint32_t)((ne - nb) * sizeof(cs_event));
-        fence_proxy_async();
-        mbar_expect_tx(&s_bar[stage], bytes);
-        if (bytes) bulk_g2s(s_tiles + stage * kTileBytes, b.ev + nb, bytes, &s_bar[stage]);
-      }
+      fence_proxy_async();
+      issue(stage, k + kStages * G);
     }
   }
-  if (do_stats && cur_inst != 0xffffffffu) {
-    __syncthreads();
-    rows_flush(b.stats + (u64)cur_inst * b.n_names, s_rows);
+  // every thread reaches the flush (uniform control flow across the CTA)
+  if (do_stats && __syncthreads_or(cur_inst != 0xffffffffu)) {
+    if (cur_inst == 0xffffffffu) cache_clear(cache);
+    cache_flush(cache, b.stats + (u64)(cur_inst == 0xffffffffu ? 0 : cur_inst) * b.n_names, s_rows);
   }
 }
 
@@ -1669,45 +1792,59 @@ __device__ __forceinline__ void accumulate_cycle_reg(const cs_name_info* __restr
   uint32_t fm_cls = 0;
   bool fm_found = false, pkw = false, dkw = false, batch_found = false;
   a.wl = -1;
-#pragma unroll 2
-  for (uint32_t j = first; j < last; ++j) {
-    const int4* q = reinterpret_cast<const int4*>(ev + j);
-    const int4 h0 = q[0], h1 = q[1];
-    const i64 st = (i64)(((u64)(uint32_t)h0.y << 32) | (uint32_t)h0.x);
-    const i64 d = (i64)(((u64)(uint32_t)h0.w << 32) | (uint32_t)h0.z);
-    const uint32_t name = (uint32_t)h1.x;
-    const uint32_t kind = (uint32_t)h1.y & 0xffu;
-    const uint32_t cat = ((uint32_t)h1.y >> 8) & 0xffu;
-    const uint32_t flags = (uint32_t)h1.y >> 16;
-    if (!fm_found && (flags & CS_EV_FM_MASK)) {
-      fm_found = true;
-      fm_cls = flags & CS_EV_FM_MASK;
+  constexpr int kB = 4;  // events loaded ahead per step (memory-level parallelism)
+  for (uint32_t j0 = first; j0 < last; j0 += kB) {
+    int4 H0[kB], H1[kB];
+#pragma unroll
+    for (int q = 0; q < kB; ++q) {
+      if (j0 + q < last) {
+        const int4* p = reinterpret_cast<const int4*>(ev + j0 + q);
+        H0[q] = p[0];
+        H1[q] = p[1];
+      } else {
+        H1[q] = make_int4(0, 0x00000003, 0, 0);  // kind = Flow, no flags: ignored
+        H0[q] = make_int4(0, 0, 0, 0);
+      }
     }
-    if (!batch_found && (flags & CS_EV_HAS_BATCH)) {
-      batch_found = true;
-      a.wl = (flags & CS_EV_WL_OK) ? (int32_t)(uint32_t)h1.z : -2;
-    }
-    if (kind != CS_SPAN) continue;
-    const cs_name_info ni = names[name];
-    pkw |= (ni.flags & CS_NAME_PREFILL_KW) != 0;
-    dkw |= (ni.flags & CS_NAME_DECODE_KW) != 0;
-    const i64 end = st + d;
-    const i64 clipped = (end < ce ? end : ce) - st;
-    if (clipped <= 0) continue;
 #pragma unroll
-    for (int p = 0; p < kMaxPhases; ++p) a.comp[p] += ni.phase == p ? clipped : 0;
-    if (do_beta && d > 0) {
+    for (int q = 0; q < kB; ++q) {
+      const int4 h0 = H0[q], h1 = H1[q];
+      const i64 st = (i64)(((u64)(uint32_t)h0.y << 32) | (uint32_t)h0.x);
+      const i64 d = (i64)(((u64)(uint32_t)h0.w << 32) | (uint32_t)h0.z);
+      const uint32_t name = (uint32_t)h1.x;
+      const uint32_t kind = (uint32_t)h1.y & 0xffu;
+      const uint32_t cat = ((uint32_t)h1.y >> 8) & 0xffu;
+      const uint32_t flags = (uint32_t)h1.y >> 16;
+      if (!fm_found && (flags & CS_EV_FM_MASK)) {
+        fm_found = true;
+        fm_cls = flags & CS_EV_FM_MASK;
+      }
+      if (!batch_found && (flags & CS_EV_HAS_BATCH)) {
+        batch_found = true;
+        a.wl = (flags & CS_EV_WL_OK) ? (int32_t)(uint32_t)h1.z : -2;
+      }
+      if (kind != CS_SPAN) continue;
+      const cs_name_info ni = names[name];
+      pkw |= (ni.flags & CS_NAME_PREFILL_KW) != 0;
+      dkw |= (ni.flags & CS_NAME_DECODE_KW) != 0;
+      const i64 end = st + d;
+      const i64 clipped = (end < ce ? end : ce) - st;
+      if (clipped <= 0) continue;
 #pragma unroll
-      for (int c = 0; c < KC; ++c) a.beta[c] += ni.beta_slot == c ? clipped : 0;
-      if (cat == CS_CAT_COLLECTIVE_COMM && (flags & CS_EV_HAS_COMM)) {
-        const uint32_t slot = (uint32_t)h1.w;
-        const double term = __ddiv_rn((double)clipped, (double)dur);
+      for (int p = 0; p < kMaxPhases; ++p) a.comp[p] += ni.phase == p ? clipped : 0;
+      if (do_beta && d > 0) {
 #pragma unroll
-        for (int r = 0; r < KR; ++r)
-          if (slot == (uint32_t)r) {
-            a.coll[r] = __dadd_rn(a.coll[r], term);
-            a.colln[r] += 1;
-          }
+        for (int c = 0; c < KC; ++c) a.beta[c] += ni.beta_slot == c ? clipped : 0;
+        if (cat == CS_CAT_COLLECTIVE_COMM && (flags & CS_EV_HAS_COMM)) {
+          const uint32_t slot = (uint32_t)h1.w;
+          const double term = __ddiv_rn((double)clipped, (double)dur);
+#pragma unroll
+          for (int r = 0; r < KR; ++r)
+            if (slot == (uint32_t)r) {
+              a.coll[r] = __dadd_rn(a.coll[r], term);
+              a.colln[r] += 1;
+            }
+        }
       }
     }
   }
@@ -2197,7 +2334,7 @@ void launch_fixup_cycles(const DevBuffers& b, const DevConfig& cfg, const FusedM
 // so sectors are consumed from L1 across the warp).  Thousands of cycles in
 // flight per SM hide the latency; no warp-level reductions or atomics.
 template <bool kReg>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 2)
     k_cycle_reduce_tpc(DevBuffers b, DevConfig cfg, int do_beta) {
   extern __shared__ __align__(16) uint32_t s_scr[];
   __shared__ cs_name_info s_names[kFNamesSmem];
