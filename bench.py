@@ -172,7 +172,7 @@ def run_ours(args, rank, world, local_rank):
 
     import torch
 
-    from paper_2601_09258_b200 import abi, runtime as rt
+    from paper_2601_09258_b200 import abi, dist as cdist, runtime as rt
 
     dist = None
     if world > 1:
@@ -284,16 +284,8 @@ def run_ours(args, rank, world, local_rank):
         sums = [an.summary(i) for i in range(n_inst)]
         payload = np.concatenate(al).view(np.uint8) if al else np.zeros(0, np.uint8)
         if dist:
-            # final gather of per-shard alerts + summaries to rank 0 (NCCL)
-            t = torch.from_numpy(payload.copy()).cuda(dev)
-            n = torch.tensor([t.numel()], device=f"cuda:{dev}")
-            sizes = [torch.zeros_like(n) for _ in range(world)]
-            dist.all_gather(sizes, n)
-            mx = int(max(s.item() for s in sizes))
-            buf = torch.zeros(max(mx, 1), dtype=torch.uint8, device=f"cuda:{dev}")
-            buf[:t.numel()] = t
-            bufs = [torch.zeros_like(buf) for _ in range(world)]
-            dist.all_gather(bufs, buf)
+            # final gather of per-shard alerts to rank 0 (NCCL over NVLink)
+            cdist.gather_bytes(payload, device=f"cuda:{dev}")
             torch.cuda.synchronize(dev)
         el = (time.perf_counter() - t0) * 1e3
         if k >= args.warmup:
@@ -303,9 +295,8 @@ def run_ours(args, rank, world, local_rank):
     e2e = sum(e2e_ms) / len(e2e_ms)
 
     if dist:
-        tt = torch.tensor([dev_ms, e2e], dtype=torch.float64, device=f"cuda:{dev}")
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        dev_ms, e2e = float(tt[0]), float(tt[1])
+        dev_ms = cdist.max_over_ranks(dev_ms, device=f"cuda:{dev}")
+        e2e = cdist.max_over_ranks(e2e, device=f"cuda:{dev}")
 
     # roofline: dominant kernel measured live (CUDA events on the ctx stream)
     import json as _json
