@@ -127,7 +127,9 @@ typedef struct cs_cycle_config { /* CycleConfig + PipelineOptions */
   int32_t include_prefill;        /* PipelineOptions::include_prefill       */
   int32_t n_beta_slots;           /* number of dense class slots (<= 64)    */
   int32_t n_comm_slots;           /* collective (name,comm,rank) slots      */
-  int32_t reserved;
+  int32_t monitor_from_cycle;     /* records (and the detector stream) start
+                                     at this cycle index: evaluate_trial's
+                                     train/monitor split (simkit.cpp:837-841) */
 } cs_cycle_config;
 
 enum cs_strategy { CS_FIXED_POINT = 0, CS_FIXED_WINDOW = 1, CS_DYNAMIC_WINDOW = 2 };
@@ -304,6 +306,46 @@ int cs_get_collective_beta(cs_ctx* ctx, uint32_t inst, double* beta,
                            uint8_t* present, size_t cap, size_t* n);
 int cs_get_records(cs_ctx* ctx, uint32_t inst, cs_record* buf, size_t cap, size_t* n);
 int cs_get_alerts(cs_ctx* ctx, uint32_t inst, cs_alert* buf, size_t cap, size_t* n);
+
+/* Re-run only the control chart over the residuals of the last cs_run with a
+ * different ControlConfig (strategy / window / warmup / thresholds); the
+ * evaluate_strategies loop of evaluate_trial (simkit.cpp:867-872). */
+int cs_redetect(cs_ctx* ctx, const cs_control_config* control);
+
+/* StrategyMetrics (detector.hpp:138-153) of the last detection for instance
+ * `inst` against per-cycle ground-truth labels (labels[cycle_index] != 0),
+ * computed on the device: confusion counts over armed records from the
+ * flagged bits, lag per contiguous anomaly interval (detector.cpp:166-224). */
+typedef struct cs_strategy_metrics {
+  int32_t strategy;
+  int32_t reserved;
+  double precision, recall, f1, fpr, mean_lag;
+  uint64_t alerts, tp, fp, fn, tn;
+} cs_strategy_metrics;
+int cs_evaluate_strategy(cs_ctx* ctx, uint32_t inst, const uint8_t* cycle_labels,
+                         uint64_t n_labels, cs_strategy_metrics* out);
+
+/* Alert sink of monitor_loop (main.cpp:151-177): Alert::to_json records
+ * (detector.cpp:72-83) as NDJSON, with the Escalator's retain/mode fields on
+ * Sentinel->DeepDive edges (detector.cpp:132-150, EscalationPolicy
+ * pre/post roll).  `buf` receives the text; *n its length + 1. */
+int cs_alerts_to_ndjson(const cs_alert* alerts, uint64_t n_alerts, uint64_t pre_roll,
+                        uint64_t post_roll, char* buf, size_t cap, size_t* n);
+
+/* Streaming (BASELINE config 5; the monitor_loop of main.cpp:151-177 fed by
+ * time-sliced micro-batches).  Between cs_stream_begin and cs_stream_end every
+ * cs_run continues one logical trace per instance:
+ *  - the anchor chosen by the first batch (or the hint) is kept;
+ *  - the detector window, warm-up count, flagged state and episode count
+ *    carry over (windows <= 64), as does the stage heuristic's history;
+ *  - cycle indices and episode ids continue across batches.
+ * The caller resubmits each instance's trailing partial cycle with the next
+ * batch: events [keep_from, n) of the last upload, where cs_stream_tail gives
+ * keep_from.  The result equals one cs_run over the whole trace, minus the
+ * final partial cycle.  cs_redetect is unavailable mid-stream. */
+int cs_stream_begin(cs_ctx* ctx);
+int cs_stream_end(cs_ctx* ctx);
+int cs_stream_tail(cs_ctx* ctx, uint32_t inst, uint64_t* keep_from);
 
 /* Execution options.  CS_OPT_FUSED (default 0): 1 selects the single-pass
  * fused segmentation kernel (k_fused_segment) when applicable; 0 runs the

@@ -68,6 +68,7 @@ struct Results {
   std::vector<cs_record> records;
   std::vector<cs_alert> alerts;
   std::string model_json;
+  std::string ndjson;
   double ucl = 0.0;
   uint64_t first_bad_record = UINT64_MAX;
   double seconds = 0.0;
@@ -306,6 +307,7 @@ void run_reference(Handle& h, const RunConfig& config, const char* model_json,
   // monitor_loop process lambda (main.cpp:151-177), every record in order
   const double ucl = ucl_from_stats(model.mu_train, model.sigma_train, config.detector);
   Detector detector(config.detector, ucl);
+  Escalator escalator(config.escalation);
   R.ucl = detector.limit();  // limit in force (strategy dependent)
   try {
     for (size_t i = 0; i < records.size(); ++i) {
@@ -341,6 +343,15 @@ void run_reference(Handle& h, const RunConfig& config, const char* model_json,
       sample.predicted_s = o.predicted_s;
       sample.error = ppe(rec.latency_s, o.predicted_s, config.detector.epsilon);
       const auto step = detector.step(sample);
+      escalator.on_cycle(rec.cycle_index);  // main.cpp:164
+      if (step.alert) {
+        auto j = step.alert->to_json();
+        if (const auto action = escalator.on_alert(*step.alert)) {
+          j["retain"] = {{"begin", action->retain.begin}, {"end", action->retain.end}};
+          j["mode"] = to_string(escalator.mode());
+        }
+        R.ndjson += j.dump() + "\n";
+      }
       auto& out = R.records.back();
       out.residual = sample.error;
       out.statistic = step.statistic;
@@ -591,6 +602,63 @@ int ref_get_records(void* hv, cs_record* buf, size_t cap, size_t* n) {
 int ref_get_alerts(void* hv, cs_alert* buf, size_t cap, size_t* n) {
   return copy_out(static_cast<Handle*>(hv)->res.alerts, buf, cap, n);
 }
+int ref_get_ndjson(void* hv, char* buf, size_t cap, size_t* n) {
+  auto* h = static_cast<Handle*>(hv);
+  std::vector<char> v(h->res.ndjson.begin(), h->res.ndjson.end());
+  v.push_back('\0');
+  return copy_out(v, buf, cap, n);
+}
+
+// Suite trial dataset exactly like make_trial_fault / make_trial_dataset
+// (simkit.cpp:760-792) with SuiteConfig{} (BASELINE config 4).
+void* ref_trial_dataset(uint64_t trial) {
+  SuiteConfig cfg;
+  const FaultFamily family = cfg.families[trial % cfg.families.size()];
+  FaultSpec fault;
+  fault.family = family;
+  fault.severity = default_severity(family);
+  Rng rng(Rng::substream_seed(cfg.seed, 0xfau + trial));
+  const auto jitter = static_cast<size_t>(
+      rng.uniform_int(0, static_cast<int64_t>(2 * cfg.fault_onset_jitter)));
+  fault.onset = cfg.fault_onset - cfg.fault_onset_jitter + jitter;
+  fault.duration = cfg.fault_duration;
+  if (family == FaultFamily::NvlinkSaturation && cfg.nvlink_ranks > 1)
+    fault.target_rank = static_cast<int>(rng.uniform_int(0, static_cast<int64_t>(cfg.nvlink_ranks) - 1));
+  const auto seed = Rng::substream_seed(cfg.seed, trial);
+  const auto work = generate_workload(cfg.profile, cfg.cycles_per_trial, seed);
+  SynthOptions opt;
+  opt.n_ranks = family == FaultFamily::NvlinkSaturation ? cfg.nvlink_ranks : 1;
+  auto h = std::make_unique<Handle>();
+  h->ds = synthesize_trace(work, cfg.model, {&fault, 1}, opt, Rng::substream_seed(seed, 1));
+  return h.release();
+}
+
+// evaluate_trial (simkit.cpp:796-955): out[s*8 + {tp,fp,fn,tn,alerts,f1,fpr,lag}] per
+// strategy (fixed_point, fixed_window, dynamic_window); returns 0 or 1 on EngineError.
+int ref_evaluate_trial(void* hv, uint64_t trial, double* out, char* err, size_t err_cap) {
+  auto* h = static_cast<Handle*>(hv);
+  SuiteConfig cfg;
+  try {
+    const auto o = evaluate_trial(cfg, h->ds, trial, cfg.families[trial % cfg.families.size()]);
+    for (size_t k = 0; k < o.strategies.size() && k < 3; ++k) {
+      const auto& m = o.strategies[k];
+      double* q = out + 8 * k;
+      q[0] = static_cast<double>(m.true_positives);
+      q[1] = static_cast<double>(m.false_positives);
+      q[2] = static_cast<double>(m.false_negatives);
+      q[3] = static_cast<double>(m.true_negatives);
+      q[4] = static_cast<double>(m.alerts);
+      q[5] = m.f1;
+      q[6] = m.fpr;
+      q[7] = m.mean_lag;
+    }
+  } catch (const EngineError& e) {
+    if (err && err_cap) std::snprintf(err, err_cap, "%s: %s", e.type().c_str(), e.what());
+    return 1;
+  }
+  return 0;
+}
+
 int ref_get_model_json(void* hv, char* buf, size_t cap, size_t* n) {
   auto* h = static_cast<Handle*>(hv);
   std::vector<char> v(h->res.model_json.begin(), h->res.model_json.end());

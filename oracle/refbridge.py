@@ -51,9 +51,13 @@ def lib():
         L.ref_seconds.argtypes = [vp]
         L.ref_first_bad_record.restype = C.c_uint64
         L.ref_first_bad_record.argtypes = [vp]
+        L.ref_trial_dataset.restype = vp
+        L.ref_trial_dataset.argtypes = [C.c_uint64]
+        L.ref_evaluate_trial.argtypes = [vp, C.c_uint64, vp, C.c_char_p, sz]
         for fn in ("ref_get_events", "ref_get_event_ids", "ref_get_workloads", "ref_labels",
                    "ref_get_candidates", "ref_get_cycles", "ref_get_components",
-                   "ref_get_records", "ref_get_alerts", "ref_get_model_json"):
+                   "ref_get_records", "ref_get_alerts", "ref_get_model_json",
+                   "ref_get_ndjson"):
             getattr(L, fn).argtypes = [vp, vp, sz, C.POINTER(sz)]
         L.ref_get_names.argtypes = [vp, vp, sz, C.POINTER(sz), C.POINTER(C.c_uint32)]
         L.ref_get_comm.argtypes = [vp, vp, vp, vp, sz, C.POINTER(sz), C.POINTER(C.c_uint32)]
@@ -167,6 +171,19 @@ class RefTrace:
         t._keep = (events, wl, crank, ids)
         return t
 
+    @classmethod
+    def trial(cls, trial: int):
+        """SuiteConfig{} trial dataset (simkit.cpp:760-792)."""
+        return cls(lib().ref_trial_dataset(trial))
+
+    def evaluate_trial(self, trial: int) -> np.ndarray:
+        """Reference evaluate_trial: 3 x [tp, fp, fn, tn, alerts, f1, fpr, lag]."""
+        out = np.zeros(24, np.float64)
+        err = C.create_string_buffer(512)
+        if lib().ref_evaluate_trial(self.h, trial, out.ctypes.data, err, 512):
+            raise RuntimeError(err.value.decode())
+        return out.reshape(3, 8)
+
     def n_events(self):
         return int(lib().ref_n_events(self.h))
 
@@ -217,6 +234,7 @@ class RefTrace:
             L.ref_get_collective_beta(self.h, cbeta.ctypes.data, cpres.ctypes.data, n.value,
                                       C.byref(n))
         mj = _get(L.ref_get_model_json, self.h, np.uint8)
+        nd = _get(L.ref_get_ndjson, self.h, np.uint8)
         return RefResult(
             status=status, err_type=tb.value.decode(), err_msg=mb.value.decode(),
             anchor=ab.value.decode(), fallback=bool(fb.value),
@@ -228,7 +246,8 @@ class RefTrace:
             alerts=_get(L.ref_get_alerts, self.h, abi.ALERT_DTYPE),
             model_json=bytes(mj[:-1]).decode() if len(mj) else "",
             ucl=L.ref_ucl(self.h), first_bad_record=int(L.ref_first_bad_record(self.h)),
-            seconds=L.ref_seconds(self.h))
+            seconds=L.ref_seconds(self.h),
+            extra={"ndjson": bytes(nd[:-1]).decode() if len(nd) else ""})
 
 
 def ref_fit(x: np.ndarray, y: np.ndarray, feature_names, params=None, options=None) -> str:

@@ -72,7 +72,7 @@ class CycleConfig(C.Structure):
                 ("frequency_bin_ns", C.c_int64), ("n_phases", C.c_int32),
                 ("latency_phase", C.c_int32), ("include_prefill", C.c_int32),
                 ("n_beta_slots", C.c_int32), ("n_comm_slots", C.c_int32),
-                ("reserved", C.c_int32)]
+                ("monitor_from_cycle", C.c_int32)]
 
 
 class ControlConfig(C.Structure):
@@ -124,3 +124,10 @@ def default_fit_options(n_features: int = 2) -> FitOptions:
 def default_control(strategy: int = DYNAMIC_WINDOW) -> ControlConfig:
     """ControlConfig defaults (detector.hpp:25-34)."""
     return ControlConfig(strategy, 0, 10, 0.15, 3.0, 0.18, 0.02, 100, 1e-9)
+
+
+class StrategyMetrics(C.Structure):
+    _fields_ = [("strategy", C.c_int32), ("reserved", C.c_int32), ("precision", C.c_double),
+                ("recall", C.c_double), ("f1", C.c_double), ("fpr", C.c_double),
+                ("mean_lag", C.c_double), ("alerts", C.c_uint64), ("tp", C.c_uint64),
+                ("fp", C.c_uint64), ("fn", C.c_uint64), ("tn", C.c_uint64)]

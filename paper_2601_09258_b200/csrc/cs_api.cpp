@@ -122,6 +122,13 @@ struct cs_ctx {
   std::vector<std::pair<std::string, std::pair<int, int>>> timed;
   uint64_t launches = 0;
   DevBuf d_scratch;
+  // streaming (cs_stream_begin): carry in force for the current batch and the
+  // one being produced for the next
+  bool streaming = false, stream_fresh = false, stream_pending = false;
+  int stream_cur = 0;
+  DevBuf d_stream[2];
+  std::vector<StreamCarry> h_stream;     // carry in force for the last batch
+  std::vector<uint32_t> stream_anchor;   // per instance, fixed after first batch
 
   ~cs_ctx() {
     for (auto* m : model_store) delete m;
@@ -203,6 +210,7 @@ DevBuffers make_buffers(cs_ctx* ctx) {
   b.alert_off = static_cast<uint64_t*>(ctx->d_alert_off.p);
   b.block_tmp = static_cast<uint64_t*>(ctx->block_tmp.p);
   b.models = static_cast<const DevModel*>(ctx->d_models.p);
+  b.stream = ctx->streaming ? static_cast<StreamCarry*>(ctx->d_stream[ctx->stream_cur].p) : nullptr;
   return b;
 }
 
@@ -621,10 +629,40 @@ int cs_run(cs_ctx* ctx, uint32_t mask) {
   if (hint >= static_cast<int64_t>(n_names))
     return fail(ctx, CS_E_INVALID_ARGUMENT, "anchor hint name id out of range");
   if (n_names == 0 && ctx->n_ev) return fail(ctx, CS_E_INVALID_ARGUMENT, "name table not set");
+  // streaming: advance to the carry the previous micro-batch produced
+  bool all_fixed = false;
+  if (ctx->streaming) {
+    if (ctx->ctl.strategy != CS_FIXED_POINT && ctx->ctl.window > kMaxStreamWindow)
+      return fail(ctx, CS_E_UNSUPPORTED, "streaming supports detector windows <= 64");
+    if (ctx->cyc.stage_window > 32)
+      return fail(ctx, CS_E_UNSUPPORTED, "streaming supports stage windows <= 32");
+    if (ctx->stream_fresh || ctx->h_stream.size() != n_inst) {
+      if (!ctx->stream_fresh) return fail(ctx, CS_E_INVALID_ARGUMENT, "instance count changed mid-stream");
+      for (auto& d : ctx->d_stream)
+        if (!dev<StreamCarry>(d, n_inst)) return fail(ctx, CS_E_CUDA, "cudaMalloc(stream)");
+      CS_CUDA(cudaMemsetAsync(ctx->d_stream[0].p, 0, n_inst * sizeof(StreamCarry), s));
+      ctx->stream_cur = 0;
+      ctx->h_stream.assign(n_inst, StreamCarry{});
+      ctx->stream_anchor.assign(n_inst, UINT32_MAX);
+      ctx->stream_fresh = false;
+      ctx->stream_pending = false;
+    }
+    if (ctx->stream_pending) {
+      ctx->stream_cur ^= 1;
+      ctx->stream_pending = false;
+    }
+    all_fixed = true;
+    for (uint32_t a : ctx->stream_anchor) all_fixed &= a != UINT32_MAX;
+  }
   // per-instance state
   ctx->h_inst.assign(n_inst, InstState{});
-  for (auto& st : ctx->h_inst) {
+  for (uint32_t i = 0; i < n_inst; ++i) {
+    auto& st = ctx->h_inst[i];
     st.guess = hint >= 0 ? static_cast<uint32_t>(hint) : UINT32_MAX;
+    if (ctx->streaming && ctx->stream_anchor[i] != UINT32_MAX) {
+      st.guess = ctx->stream_anchor[i];
+      st.fixed_anchor = 1;
+    }
     st.anchor = UINT32_MAX;
     st.first_bad_record = UINT64_MAX;
   }
@@ -642,7 +680,7 @@ int cs_run(cs_ctx* ctx, uint32_t mask) {
   DevBuffers b = make_buffers(ctx);
 
   const int e0 = record_event(ctx, 0);
-  if (hint == -1) {
+  if (hint == -1 && !all_fixed) {
     // speculative anchor from a sample of every instance
     if (stats_bytes) CS_CUDA(cudaMemsetAsync(d_stats, 0, stats_bytes, s));
     launch_scan_events(b, cfg, 1, true, static_cast<const uint32_t*>(ctx->d_sample_tiles.p),
@@ -673,7 +711,7 @@ int cs_run(cs_ctx* ctx, uint32_t mask) {
   const std::vector<InstState> h_init = ctx->h_inst;
   int e1 = -1, e2 = -1;
   // ---------------- fused single pass (common case)
-  if (ctx->allow_fused) {
+  if (ctx->allow_fused && !ctx->streaming) {
     uint64_t cap = std::max<uint64_t>(ctx->slot_cap, ctx->n_ev / 8 + 1024);
     const size_t nfix = 2 * std::max<size_t>(1, nt) + 16;
     FusedMetaHost mh{};
@@ -854,7 +892,9 @@ int cs_run(cs_ctx* ctx, uint32_t mask) {
   for (uint32_t i = 0; i < n_inst; ++i) {
     uint64_t nc = 0;
     const auto& st = ctx->h_inst[i];
-    if (st.no_anchor) {
+    if (st.no_anchor && ctx->streaming) {
+      ctx->inst_status[i] = CS_E_NO_ANCHOR_FOUND;  // no cycles in this micro-batch
+    } else if (st.no_anchor) {
       int rc = frequency_plan(ctx, i, &f_t0[i], &f_period[i], &nc);
       if (rc != CS_OK) return rc;
       ctx->used_fallback[i] = 1;
@@ -955,6 +995,14 @@ int cs_run(cs_ctx* ctx, uint32_t mask) {
       last = e8;
     }
   }
+  if (ctx->streaming) {
+    launch_stream_update(b, cfg, static_cast<StreamCarry*>(ctx->d_stream[ctx->stream_cur ^ 1].p),
+                         (mask & CS_RUN_DETECT) ? 1 : 0, s);
+    ++ctx->launches;
+    ctx->stream_pending = true;
+    CS_CUDA(cudaMemcpyAsync(ctx->h_stream.data(), ctx->d_stream[ctx->stream_cur].p,
+                            n_inst * sizeof(StreamCarry), cudaMemcpyDeviceToHost, s));
+  }
   ctx->timed.push_back({"total", {e0, last}});
   CS_CUDA(cudaMemcpyAsync(ctx->h_inst.data(), d_inst, n_inst * sizeof(InstState),
                           cudaMemcpyDeviceToHost, s));
@@ -968,8 +1016,40 @@ int cs_run(cs_ctx* ctx, uint32_t mask) {
     if (ctx->inst_status[i] == CS_OK && ctx->h_inst[i].first_bad_record != UINT64_MAX &&
         (mask & (CS_RUN_SCORE | CS_RUN_DETECT)))
       ctx->inst_status[i] = CS_E_NON_POSITIVE_LATENCY;
+  if (ctx->streaming)
+    for (uint32_t i = 0; i < n_inst; ++i)
+      if (ctx->stream_anchor[i] == UINT32_MAX && !ctx->h_inst[i].no_anchor &&
+          ctx->h_inst[i].anchor != UINT32_MAX)
+        ctx->stream_anchor[i] = ctx->h_inst[i].anchor;
   ctx->ran = true;
   ctx->last_mask = mask;
+  return CS_OK;
+}
+
+int cs_stream_begin(cs_ctx* ctx) {
+  if (!ctx) return CS_E_INVALID_ARGUMENT;
+  ctx->streaming = true;
+  ctx->stream_fresh = true;
+  return CS_OK;
+}
+
+int cs_stream_end(cs_ctx* ctx) {
+  if (!ctx) return CS_E_INVALID_ARGUMENT;
+  ctx->streaming = false;
+  ctx->stream_pending = false;
+  return CS_OK;
+}
+
+int cs_stream_tail(cs_ctx* ctx, uint32_t inst, uint64_t* keep_from) {
+  if (!ctx || !keep_from || !ctx->ran || inst >= ctx->n_inst) return CS_E_INVALID_ARGUMENT;
+  if (!ctx->streaming) return fail(ctx, CS_E_INVALID_ARGUMENT, "not streaming");
+  *keep_from = 0;
+  if (ctx->n_cyc[inst] == 0) return CS_OK;
+  const uint64_t g = ctx->cyc_off[inst] + ctx->n_cyc[inst] - 1;
+  uint64_t last = 0;
+  CS_CUDA(cudaMemcpy(&last, static_cast<const uint64_t*>(ctx->c_last.p) + g, 8,
+                     cudaMemcpyDeviceToHost));
+  *keep_from = last - ctx->inst_off[inst];
   return CS_OK;
 }
 
@@ -1076,7 +1156,7 @@ int cs_get_cycles(cs_ctx* ctx, uint32_t inst, cs_cycle* buf, size_t cap, size_t*
   const uint64_t ib = ctx->inst_off[inst];
   for (uint64_t k = 0; k < nc; ++k) {
     cs_cycle& c = buf[k];
-    c.index = k;
+    c.index = k + (ctx->streaming ? ctx->h_stream[inst].cycle_off : 0);
     c.start_ts = st[k];
     c.end_ts = en[k];
     c.anchor_pos = ap[k] == UINT64_MAX ? UINT64_MAX : ap[k] - ib;
@@ -1109,10 +1189,10 @@ int cs_get_beta(cs_ctx* ctx, uint32_t inst, int64_t* totals, double* beta, size_
   const uint64_t c0 = ctx->cyc_off[inst], nc = ctx->n_cyc[inst];
   if (n) *n = nc * Cs;
   if (cap < nc * Cs && (totals || beta)) return fail(ctx, CS_E_INVALID_ARGUMENT, "buffer too small");
-  if (totals && nc * Cs)
+  if (totals && nc * Cs != 0)
     CS_CUDA(cudaMemcpy(totals, static_cast<int64_t*>(ctx->c_beta_tot.p) + c0 * Cs, nc * Cs * 8,
                        cudaMemcpyDeviceToHost));
-  if (beta && nc * Cs)
+  if (beta && nc * Cs != 0)
     CS_CUDA(cudaMemcpy(beta, static_cast<double*>(ctx->c_beta.p) + c0 * Cs, nc * Cs * 8,
                        cudaMemcpyDeviceToHost));
   return CS_OK;
@@ -1126,10 +1206,10 @@ int cs_get_collective_beta(cs_ctx* ctx, uint32_t inst, double* beta, uint8_t* pr
   const uint64_t c0 = ctx->cyc_off[inst], nc = ctx->n_cyc[inst];
   if (n) *n = nc * R;
   if (cap < nc * R && (beta || present)) return fail(ctx, CS_E_INVALID_ARGUMENT, "buffer too small");
-  if (beta && nc * R)
+  if (beta && nc * R != 0)
     CS_CUDA(cudaMemcpy(beta, static_cast<double*>(ctx->c_coll.p) + c0 * R, nc * R * 8,
                        cudaMemcpyDeviceToHost));
-  if (present && nc * R) {
+  if (present && nc * R != 0) {
     CS_CUDA(cudaMemcpy(present, static_cast<uint8_t*>(ctx->c_coll_n.p) + c0 * R, nc * R,
                        cudaMemcpyDeviceToHost));
     for (uint64_t k = 0; k < nc * R; ++k) present[k] = present[k] ? 1 : 0;
@@ -1168,7 +1248,7 @@ int cs_get_records(cs_ctx* ctx, uint32_t inst, cs_record* buf, size_t cap, size_
   if (rc) return rc;
   if (ctx->last_mask & CS_RUN_DETECT) {
     // episode ids: running alert count within the instance
-    uint64_t ep = 0;
+    uint64_t ep = ctx->streaming ? ctx->h_stream[inst].episodes : 0;
     for (uint64_t k = 0; k < nr; ++k)
       if (buf[k].alert) buf[k].episode_id = ep++;
   }
@@ -1197,6 +1277,77 @@ int cs_get_alerts(cs_ctx* ctx, uint32_t inst, cs_alert* buf, size_t cap, size_t*
   if (!buf) return CS_OK;
   if (cap < na) return fail(ctx, CS_E_INVALID_ARGUMENT, "buffer too small");
   std::copy(all.begin(), all.begin() + na, buf);
+  return CS_OK;
+}
+
+int cs_redetect(cs_ctx* ctx, const cs_control_config* control) {
+  if (!ctx || !control || !ctx->ran) return CS_E_INVALID_ARGUMENT;
+  if (ctx->streaming) return fail(ctx, CS_E_UNSUPPORTED, "cs_redetect is not available mid-stream");
+  if (!(ctx->last_mask & (CS_RUN_SCORE | CS_RUN_DETECT)))
+    return fail(ctx, CS_E_INVALID_ARGUMENT, "cs_redetect needs a scored run");
+  if (control->strategy < 0 || control->strategy > 2 || control->window == 0)
+    return fail(ctx, CS_E_CONFIG, "invalid control config");
+  CS_CUDA(cudaSetDevice(ctx->device));
+  cudaStream_t s = ctx->stream;
+  ctx->ctl = *control;
+  const uint32_t n_inst = ctx->n_inst;
+  for (uint32_t i = 0; i < n_inst; ++i) {
+    const PackedModel* pm = ctx->model_store[ctx->model_of_inst[i]];
+    ctx->h_models[i].ucl = ctx->ctl.strategy == CS_DYNAMIC_WINDOW
+                               ? ucl_from_stats_host(pm->mu, pm->sigma, ctx->ctl)
+                               : ctx->ctl.fixed_threshold;
+    ctx->h_inst[i].n_alerts = 0;
+  }
+  CS_CUDA(cudaMemcpyAsync(ctx->d_models.p, ctx->h_models.data(), n_inst * sizeof(DevModel),
+                          cudaMemcpyHostToDevice, s));
+  CS_CUDA(cudaMemcpyAsync(ctx->d_inst.p, ctx->h_inst.data(), n_inst * sizeof(InstState),
+                          cudaMemcpyHostToDevice, s));
+  DevConfig cfg{ctx->cyc, ctx->ctl, 0.0};
+  launch_detect(make_buffers(ctx), cfg, ctx->n_records, s, &ctx->launches);
+  CS_CUDA(cudaMemcpyAsync(ctx->alert_off.data(), ctx->d_alert_off.p, (n_inst + 1) * 8,
+                          cudaMemcpyDeviceToHost, s));
+  CS_CUDA(cudaStreamSynchronize(s));
+  ctx->last_mask |= CS_RUN_DETECT;
+  return CS_OK;
+}
+
+int cs_evaluate_strategy(cs_ctx* ctx, uint32_t inst, const uint8_t* labels, uint64_t n_labels,
+                         cs_strategy_metrics* out) {
+  if (!ctx || !out || !ctx->ran || inst >= ctx->n_inst || (n_labels && !labels))
+    return CS_E_INVALID_ARGUMENT;
+  if (!(ctx->last_mask & CS_RUN_DETECT)) return fail(ctx, CS_E_INVALID_ARGUMENT, "detect not run");
+  const uint64_t nr = ctx->rec_off[inst + 1] - ctx->rec_off[inst];
+  if (nr == 0 || n_labels == 0)
+    return fail(ctx, CS_E_NO_LABELS, "labeled stream is empty or label count mismatches");
+  CS_CUDA(cudaSetDevice(ctx->device));
+  DevBuf dl, dout;
+  auto* d_labels = static_cast<uint8_t*>(dl.get(n_labels));
+  auto* d_out = static_cast<unsigned long long*>(dout.get(7 * 8));
+  if (!d_labels || !d_out) return fail(ctx, CS_E_CUDA, "cudaMalloc(eval)");
+  CS_CUDA(cudaMemcpyAsync(d_labels, labels, n_labels, cudaMemcpyHostToDevice, ctx->stream));
+  CS_CUDA(cudaMemsetAsync(d_out, 0, 7 * 8, ctx->stream));
+  launch_eval_strategy(make_buffers(ctx), inst, d_labels, n_labels, ctx->ctl.warmup, d_out,
+                       ctx->stream);
+  unsigned long long h[7];
+  CS_CUDA(cudaMemcpyAsync(h, d_out, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
+  CS_CUDA(cudaStreamSynchronize(ctx->stream));
+  // detector.cpp:193-222, same double arithmetic
+  cs_strategy_metrics m{};
+  m.strategy = ctx->ctl.strategy;
+  m.tp = h[0];
+  m.fp = h[1];
+  m.fn = h[2];
+  m.tn = h[3];
+  m.alerts = h[4];
+  const double tp = static_cast<double>(h[0]), fp = static_cast<double>(h[1]);
+  const double fn = static_cast<double>(h[2]), tn = static_cast<double>(h[3]);
+  m.precision = tp + fp > 0.0 ? tp / (tp + fp) : 0.0;
+  m.recall = tp + fn > 0.0 ? tp / (tp + fn) : 0.0;
+  m.f1 = m.precision + m.recall > 0.0 ? 2.0 * m.precision * m.recall / (m.precision + m.recall)
+                                      : 0.0;
+  m.fpr = fp + tn > 0.0 ? fp / (fp + tn) : 0.0;
+  m.mean_lag = h[6] > 0 ? static_cast<double>(h[5]) / static_cast<double>(h[6]) : 0.0;
+  *out = m;
   return CS_OK;
 }
 

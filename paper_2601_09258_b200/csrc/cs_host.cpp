@@ -381,6 +381,45 @@ int cs_model_view(const cs_fitted_model* m, cs_model* v) {
 
 void cs_model_free(cs_fitted_model* m) { delete m; }
 
+// monitor_loop's alert sink (main.cpp:151-177): Alert::to_json
+// (detector.cpp:72-83) + Escalator (detector.cpp:132-150).  Record cycles are
+// increasing, so the Escalator's on_cycle timeouts between two alerts reduce
+// to checking the alert's own cycle against the deadline.
+int cs_alerts_to_ndjson(const cs_alert* alerts, uint64_t n_alerts, uint64_t pre_roll,
+                        uint64_t post_roll, char* buf, size_t cap, size_t* n) {
+  if (n_alerts && !alerts) return CS_E_INVALID_ARGUMENT;
+  static const char* kStrategy[3] = {"fixed_point", "fixed_window", "dynamic_window"};
+  std::string out;
+  bool deep = false;
+  uint64_t deadline = 0;
+  for (uint64_t i = 0; i < n_alerts; ++i) {
+    const cs_alert& a = alerts[i];
+    if (deep && a.cycle > deadline) deep = false;  // Escalator::on_cycle
+    json rec{{"cycle", a.cycle},
+             {"ts", a.ts},
+             {"ebar", a.smoothed_error},
+             {"ucl", a.limit},
+             {"strategy", kStrategy[a.strategy < 0 || a.strategy > 2 ? 2 : a.strategy]},
+             {"workload",
+              {{"batch", a.batch}, {"input_len", a.input_len}, {"output_len", a.output_len}}},
+             {"episode_id", a.episode_id}};
+    deadline = a.cycle + post_roll;  // Escalator::on_alert
+    if (!deep) {
+      deep = true;
+      rec["retain"] = {{"begin", a.cycle >= pre_roll ? a.cycle - pre_roll : 0},
+                       {"end", a.cycle + post_roll}};
+      rec["mode"] = "deep_dive";
+    }
+    out += rec.dump();
+    out += "\n";
+  }
+  if (n) *n = out.size() + 1;
+  if (!buf) return CS_OK;
+  if (cap < out.size() + 1) return CS_E_INVALID_ARGUMENT;
+  std::memcpy(buf, out.c_str(), out.size() + 1);
+  return CS_OK;
+}
+
 // RunConfig JSON (config.cpp:78-188 schema; unknown keys rejected) ->
 // device configs + per-name table.  `names` are the interned names in id
 // order (lexicographic); name_is_span marks names that occur as Spans

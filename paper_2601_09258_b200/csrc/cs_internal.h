@@ -44,7 +44,8 @@ struct InstState {
   unsigned long long first_bad_record;
   unsigned long long n_records;
   unsigned long long n_alerts;
-  unsigned long long bad_workload;   // reserved
+  uint32_t fixed_anchor;   // streaming: `guess` is this instance's fixed anchor
+  uint32_t reserved;
 };
 
 // flattened model in complete-binary-tree layout (see pack_model)
@@ -66,6 +67,25 @@ struct DevModel {
   const double* lut;
   const double* lut_thr[2];
   uint32_t lut_n[2];
+};
+
+// Streaming (micro-batch) state carried per instance across cs_run calls:
+// the detector's last W-1 residuals, samples seen, flagged state, episode
+// count and the number of cycles already emitted.
+constexpr int kMaxStreamWindow = 64;
+struct StreamCarry {
+  unsigned long long seen;
+  unsigned long long episodes;
+  unsigned long long cycle_off;
+  uint32_t n_hist;
+  uint32_t prev_flag;
+  double hist[kMaxStreamWindow - 1];
+  // stage heuristic (cycles.cpp:204-250): most recent first, <= 32 each
+  double dur_hist[32];
+  double gap_hist[32];
+  uint32_t n_dur, n_gap;
+  long long last_aend;
+  uint32_t has_prev, pad;
 };
 
 struct DevConfig {
@@ -125,6 +145,7 @@ struct DevBuffers {
   uint64_t* alert_off;          // n_inst+1
   uint64_t* block_tmp;          // scratch for scans
   const DevModel* models;       // per instance (device array)
+  StreamCarry* stream;          // per instance, null when not streaming
 };
 
 // fused single-pass segmentation state (k_fused_segment)
@@ -185,6 +206,11 @@ void launch_fused_inst(const DevBuffers& b, const FusedMetaHost& mh, uint64_t* c
                        cudaStream_t s, uint64_t* launches);
 void launch_fixup_cycles(const DevBuffers& b, const DevConfig& cfg, const FusedMetaHost& mh,
                          int do_beta, uint32_t n_fix, cudaStream_t s, uint64_t* launches);
+void launch_eval_strategy(const DevBuffers& b, uint32_t inst, const uint8_t* labels,
+                          uint64_t n_labels, uint64_t warmup, unsigned long long* out,
+                          cudaStream_t s);
+void launch_stream_update(const DevBuffers& b, const DevConfig& cfg, StreamCarry* out, int detected,
+                          cudaStream_t s);
 void launch_gather_records(const DevBuffers& b, const DevConfig& cfg, uint32_t inst, uint64_t r0,
                            uint64_t nr, int scored, int det, cs_record* out, cudaStream_t s);
 void launch_gather_alerts(const DevBuffers& b, const DevConfig& cfg, uint32_t inst, uint64_t a0,

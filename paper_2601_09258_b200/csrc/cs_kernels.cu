@@ -652,10 +652,12 @@ __global__ void k_rank(DevBuffers b, DevConfig cfg, int final_pass) {
 
   if (lane == 0) {
     uint32_t winner = best.name;
-    if (hint >= 0) {
+    if (hint >= 0 || st.fixed_anchor) {
       // discover_anchor with a hint (cycles.cpp:90-104): the hint wins when it
-      // occurs as any Span at all
-      winner = st.n_anchors > 0 ? (uint32_t)hint : 0xffffffffu;
+      // occurs as any Span at all.  A stream keeps the anchor its first
+      // micro-batch chose (fixed_anchor) the same way.
+      const uint32_t h = st.fixed_anchor ? st.guess : (uint32_t)hint;
+      winner = st.n_anchors > 0 ? h : 0xffffffffu;
       amb = false;
     } else if (hint == -2) {
       winner = 0xffffffffu;
@@ -940,6 +942,7 @@ __global__ void k_stage_heuristic(DevBuffers b, DevConfig cfg) {
   const u64 c0 = b.cyc_off[inst], c1 = b.cyc_off[inst + 1];
   const int W = (int)cfg.cyc.stage_window;
   const u64 min_hist = cfg.cyc.stage_min_history;
+  const StreamCarry* sc = b.stream ? b.stream + inst : nullptr;
   for (u64 base = c0; base < c1; base += 32) {
     const u64 g = base + lane;
     uint32_t um = __ballot_sync(0xffffffffu, g < c1 && b.c_local[g] == CS_STAGE_UNKNOWN);
@@ -947,8 +950,8 @@ __global__ void k_stage_heuristic(DevBuffers b, DevConfig cfg) {
       const int l = __ffs(um) - 1;
       um &= um - 1;
       const u64 u = base + l;
-      const double gap =
-          u > c0 ? (double)(b.c_start[u] - b.c_aend[u - 1]) : -1.0;
+      const double gap = u > c0 ? (double)(b.c_start[u] - b.c_aend[u - 1])
+                         : (sc && sc->has_prev) ? (double)(b.c_start[u] - sc->last_aend) : -1.0;
       uint8_t stage = CS_STAGE_UNKNOWN;
       if (gap >= 0.0) {
         // gather windows, most recent first
@@ -963,7 +966,8 @@ __global__ void k_stage_heuristic(DevBuffers b, DevConfig cfg) {
           if (in) {
             nonp = b.c_stage[j] != CS_STAGE_PREFILL;
             jd = (double)(b.c_end[j] - b.c_start[j]);
-            jg = j > (i64)c0 ? (double)(b.c_start[j] - b.c_aend[j - 1]) : -1.0;
+            jg = j > (i64)c0 ? (double)(b.c_start[j] - b.c_aend[j - 1])
+                 : (sc && sc->has_prev) ? (double)(b.c_start[j] - sc->last_aend) : -1.0;
             gok = nonp && jg >= 0.0;
           }
           const uint32_t md = __ballot_sync(0xffffffffu, in && nonp);
@@ -987,6 +991,18 @@ __global__ void k_stage_heuristic(DevBuffers b, DevConfig cfg) {
           }
           nd = min(W, nd + __popc(md));
           ng = min(W, ng + __popc(mg));
+        }
+        if (sc) {  // earlier micro-batches, most recent first
+          if (lane >= nd && lane < W && (uint32_t)(lane - nd) < sc->n_dur) {
+            dv = sc->dur_hist[lane - nd];
+            dh = true;
+          }
+          if (lane >= ng && lane < W && (uint32_t)(lane - ng) < sc->n_gap) {
+            gv = sc->gap_hist[lane - ng];
+            gh = true;
+          }
+          nd = min(W, nd + (int)sc->n_dur);
+          ng = min(W, ng + (int)sc->n_gap);
         }
         if ((u64)nd >= min_hist) {
           const double med_dur = warp_median(dv, dh, nd);
@@ -1016,7 +1032,9 @@ __global__ void k_records_count(DevBuffers b, DevConfig cfg) {
   const u64 g = (u64)blockIdx.x * kRecBlock + threadIdx.x;
   bool ok = false;
   if (g < b.n_cycles)
-    ok = b.c_wl[g] >= 0 && (cfg.cyc.include_prefill || b.c_stage[g] != CS_STAGE_PREFILL);
+    ok = b.c_wl[g] >= 0 && (cfg.cyc.include_prefill || b.c_stage[g] != CS_STAGE_PREFILL) &&
+         g - b.cyc_off[b.c_inst[g]] + (b.stream ? b.stream[b.c_inst[g]].cycle_off : 0) >=
+             (u64)cfg.cyc.monitor_from_cycle;
   const uint32_t m = __ballot_sync(0xffffffffu, ok);
   if ((threadIdx.x & 31) == 0) s_w[threadIdx.x >> 5] = __popc(m);
   __syncthreads();
@@ -1068,7 +1086,9 @@ __global__ void k_records_scatter(DevBuffers b, DevConfig cfg) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   bool ok = false;
   if (g < b.n_cycles)
-    ok = b.c_wl[g] >= 0 && (cfg.cyc.include_prefill || b.c_stage[g] != CS_STAGE_PREFILL);
+    ok = b.c_wl[g] >= 0 && (cfg.cyc.include_prefill || b.c_stage[g] != CS_STAGE_PREFILL) &&
+         g - b.cyc_off[b.c_inst[g]] + (b.stream ? b.stream[b.c_inst[g]].cycle_off : 0) >=
+             (u64)cfg.cyc.monitor_from_cycle;
   const uint32_t m = __ballot_sync(0xffffffffu, ok);
   if (lane == 0) s_w[warp] = __popc(m);
   __syncthreads();
@@ -1394,6 +1414,19 @@ __device__ __forceinline__ double window_stat(const double* e, u64 t, u64 W, int
   return __ddiv_rn(sum, (double)(t - begin + 1));
 }
 
+// Same statistic for stream position T = seen + t: residuals of earlier
+// micro-batches come from the carried history (oldest first).
+__device__ __forceinline__ double window_stat_stream(const double* e, u64 t, u64 W, int strategy,
+                                                     const StreamCarry& c) {
+  const u64 T = c.seen + t;
+  if (strategy == CS_FIXED_POINT) return e[t];
+  const u64 begin = T + 1 >= W ? T + 1 - W : 0;
+  const u64 h0 = c.seen - c.n_hist;  // stream index of hist[0]
+  double sum = 0.0;
+  for (u64 u = begin; u <= T; ++u) sum = __dadd_rn(sum, u < c.seen ? c.hist[u - h0] : e[u - c.seen]);
+  return __ddiv_rn(sum, (double)(T - begin + 1));
+}
+
 __global__ void k_detect_flags(DevBuffers b, DevConfig cfg, uint64_t n_records) {
   __shared__ uint32_t s_w[32];
   const u64 k = (u64)blockIdx.x * kDetBlock + threadIdx.x;
@@ -1404,11 +1437,22 @@ __global__ void k_detect_flags(DevBuffers b, DevConfig cfg, uint64_t n_records) 
     const u64 t = k - rb;
     const double limit = b.models[inst].ucl;
     const double* e = b.rec_resid + rb;
-    const double stat = window_stat(e, t, cfg.ctl.window, cfg.ctl.strategy);
-    const bool armed = t >= cfg.ctl.warmup;
+    const u64 W = cfg.ctl.window, warm = cfg.ctl.warmup;
+    double stat;
+    bool armed, prev = false;
+    if (b.stream) {
+      const StreamCarry& c = b.stream[inst];
+      const u64 T = c.seen + t;
+      stat = window_stat_stream(e, t, W, cfg.ctl.strategy, c);
+      armed = T >= warm;
+      if (t == 0) prev = c.prev_flag != 0;
+      else if (T - 1 >= warm) prev = window_stat_stream(e, t - 1, W, cfg.ctl.strategy, c) > limit;
+    } else {
+      stat = window_stat(e, t, W, cfg.ctl.strategy);
+      armed = t >= warm;
+      if (t >= 1 && t - 1 >= warm) prev = window_stat(e, t - 1, W, cfg.ctl.strategy) > limit;
+    }
     const bool flagged = armed && stat > limit;
-    bool prev = false;
-    if (t >= 1 && t - 1 >= cfg.ctl.warmup) prev = window_stat(e, t - 1, cfg.ctl.window, cfg.ctl.strategy) > limit;
     alert = flagged && !prev;
     b.rec_stat[k] = stat;
     b.rec_flags[k] = (armed ? 1 : 0) | (flagged ? 2 : 0) | (alert ? 4 : 0);
@@ -1422,6 +1466,63 @@ __global__ void k_detect_flags(DevBuffers b, DevConfig cfg, uint64_t n_records) 
     v = warp_sum_u64(v);
     if (threadIdx.x == 0) b.block_tmp[blockIdx.x] = v;
   }
+}
+
+// After a micro-batch: the carry the next one starts from (written to `out`,
+// the carry in force for this batch stays readable for the getters).
+__global__ void k_stream_update(DevBuffers b, DevConfig cfg, StreamCarry* out, int detected) {
+  const uint32_t inst = blockIdx.x * blockDim.x + threadIdx.x;
+  if (inst >= b.n_inst) return;
+  const StreamCarry& c = b.stream[inst];
+  StreamCarry& o = out[inst];
+  // detector window
+  if (detected) {
+    const u64 r0 = b.rec_off[inst], n = b.rec_off[inst + 1] - r0;
+    const u64 keep = cfg.ctl.window > 0 ? cfg.ctl.window - 1 : 0;
+    const u64 total = c.seen + n;
+    const u64 nh = total < keep ? total : keep;
+    const u64 h0 = c.seen - c.n_hist;
+    for (u64 i = 0; i < nh; ++i) {
+      const u64 u = total - nh + i;  // stream index
+      o.hist[i] = u < c.seen ? c.hist[u - h0] : b.rec_resid[r0 + (u - c.seen)];
+    }
+    o.n_hist = (uint32_t)nh;
+    o.prev_flag = n ? ((b.rec_flags[r0 + n - 1] & 2) ? 1u : 0u) : c.prev_flag;
+    o.seen = total;
+    o.episodes = c.episodes + b.inst[inst].n_alerts;
+  } else {
+    o.n_hist = c.n_hist;
+    for (uint32_t i = 0; i < c.n_hist; ++i) o.hist[i] = c.hist[i];
+    o.prev_flag = c.prev_flag;
+    o.seen = c.seen;
+    o.episodes = c.episodes;
+  }
+  // stage-heuristic history: newest cycles of this batch first, then the carry
+  const u64 c0 = b.cyc_off[inst], c1 = b.cyc_off[inst + 1];
+  const uint32_t W = (uint32_t)(cfg.cyc.stage_window < 32 ? cfg.cyc.stage_window : 32);
+  uint32_t nd = 0, ng = 0;
+  for (u64 j = c1; j-- > c0 && (nd < W || ng < W);) {
+    if (b.c_stage[j] == CS_STAGE_PREFILL) continue;
+    if (nd < W) o.dur_hist[nd++] = (double)(b.c_end[j] - b.c_start[j]);
+    const bool has_gap = j > c0 || c.has_prev;
+    if (has_gap && ng < W) {
+      const i64 prev_end = j > c0 ? b.c_aend[j - 1] : c.last_aend;
+      const double g = (double)(b.c_start[j] - prev_end);
+      if (g >= 0.0) o.gap_hist[ng++] = g;
+    }
+  }
+  for (uint32_t i = 0; i < c.n_dur && nd < W; ++i) o.dur_hist[nd++] = c.dur_hist[i];
+  for (uint32_t i = 0; i < c.n_gap && ng < W; ++i) o.gap_hist[ng++] = c.gap_hist[i];
+  o.n_dur = nd;
+  o.n_gap = ng;
+  o.has_prev = (c1 > c0) ? 1u : c.has_prev;
+  o.last_aend = (c1 > c0) ? b.c_aend[c1 - 1] : c.last_aend;
+  o.cycle_off = c.cycle_off + (c1 - c0);
+}
+
+void launch_stream_update(const DevBuffers& b, const DevConfig& cfg, StreamCarry* out, int detected,
+                          cudaStream_t s) {
+  k_stream_update<<<(b.n_inst + 63) / 64, 64, 0, s>>>(b, cfg, out, detected);
 }
 
 __global__ void k_alert_off(DevBuffers b) {
@@ -1457,6 +1558,56 @@ __global__ void k_detect_scatter(DevBuffers b, uint64_t n_records) {
   if (alert) b.alert_rec[b.block_tmp[blockIdx.x] + s_w[warp] + __popc(m & lanemask_lt())] = k;
 }
 
+// ------------------------------------------------- evaluate_strategy
+// detector.cpp:166-224 over one instance's records: confusion counts from the
+// flagged bits of armed records; lag per contiguous anomaly interval that
+// starts at t >= warmup (capped at the interval length).  All counts are
+// integers, so any reduction order is exact; out[0..6] = tp, fp, fn, tn,
+// alerts, lag_sum, intervals.
+__global__ void k_eval_strategy(DevBuffers b, uint32_t inst, const uint8_t* __restrict__ labels,
+                                uint64_t n_labels, uint64_t warmup, unsigned long long* out) {
+  const u64 r0 = b.rec_off[inst], nr = b.rec_off[inst + 1] - r0;
+  const u64 c0 = b.cyc_off[inst];
+  u64 tp = 0, fp = 0, fn = 0, tn = 0, al = 0, lag = 0, iv = 0;
+  auto anomalous = [&](u64 t) {
+    const u64 c = b.rec_cycle[r0 + t] - c0;
+    return c < n_labels && labels[c] != 0;
+  };
+  for (u64 t = (u64)blockIdx.x * blockDim.x + threadIdx.x; t < nr; t += (u64)gridDim.x * blockDim.x) {
+    const uint8_t f = b.rec_flags[r0 + t];
+    const bool an = anomalous(t);
+    if (f & 1) {
+      const bool fl = f & 2;
+      if (f & 4) ++al;
+      if (fl && an) ++tp;
+      else if (fl) ++fp;
+      else if (an) ++fn;
+      else ++tn;
+    }
+    if (t >= warmup && an && (t == warmup || !anomalous(t - 1))) {
+      u64 e = t;
+      while (e < nr && anomalous(e)) ++e;
+      u64 first = e;
+      for (u64 u = t; u < e; ++u)
+        if (b.rec_flags[r0 + u] & 2) { first = u; break; }
+      lag += first - t;
+      ++iv;
+    }
+  }
+  const u64 v[7] = {tp, fp, fn, tn, al, lag, iv};
+#pragma unroll
+  for (int k = 0; k < 7; ++k) {
+    const u64 s = warp_sum_u64(v[k]);
+    if ((threadIdx.x & 31) == 0 && s) atomicAdd(&out[k], s);
+  }
+}
+
+void launch_eval_strategy(const DevBuffers& b, uint32_t inst, const uint8_t* labels,
+                          uint64_t n_labels, uint64_t warmup, unsigned long long* out,
+                          cudaStream_t s) {
+  k_eval_strategy<<<148, 256, 0, s>>>(b, inst, labels, n_labels, warmup, out);
+}
+
 // ------------------------------------------------------------ getters
 // Assemble AoS cs_record / cs_alert rows on the device so a getter is one D2H
 // of exactly the rows asked for.
@@ -1467,7 +1618,7 @@ __global__ void k_gather_records(DevBuffers b, DevConfig cfg, uint32_t inst, uin
   const u64 k = r0 + i;
   const u64 g = b.rec_cycle[k];
   cs_record r;
-  r.cycle_index = g - b.cyc_off[inst];
+  r.cycle_index = g - b.cyc_off[inst] + (b.stream ? b.stream[inst].cycle_off : 0);
   r.start_ts = b.c_start[g];
   r.stage = b.c_stage[g];
   const cs_workload w = b.wl[b.c_wl[g]];
@@ -1501,7 +1652,7 @@ __global__ void k_gather_alerts(DevBuffers b, DevConfig cfg, uint32_t inst, uint
   const u64 g = b.rec_cycle[k];
   const cs_workload w = b.wl[b.c_wl[g]];
   cs_alert a;
-  a.cycle = g - b.cyc_off[inst];
+  a.cycle = g - b.cyc_off[inst] + (b.stream ? b.stream[inst].cycle_off : 0);
   a.ts = b.c_start[g];
   a.smoothed_error = b.rec_stat[k];
   a.limit = b.models[inst].ucl;
@@ -1510,7 +1661,7 @@ __global__ void k_gather_alerts(DevBuffers b, DevConfig cfg, uint32_t inst, uint
   a.batch = w.batch;
   a.input_len = w.input_len;
   a.output_len = w.output_len;
-  a.episode_id = i;
+  a.episode_id = i + (b.stream ? b.stream[inst].episodes : 0);
   a.record_index = k - b.rec_off[inst];
   out[i] = a;
 }

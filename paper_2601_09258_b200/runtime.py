@@ -65,6 +65,12 @@ def lib():
     L.cs_get_beta.argtypes = [vp, u32, vp, vp, sz, psz]
     L.cs_get_collective_beta.argtypes = [vp, u32, vp, vp, sz, psz]
     L.cs_set_option.argtypes = [vp, C.c_int, C.c_int64]
+    L.cs_redetect.argtypes = [vp, C.POINTER(abi.ControlConfig)]
+    L.cs_stream_begin.argtypes = [vp]
+    L.cs_stream_end.argtypes = [vp]
+    L.cs_stream_tail.argtypes = [vp, u32, C.POINTER(C.c_uint64)]
+    L.cs_evaluate_strategy.argtypes = [vp, u32, vp, u64, C.POINTER(abi.StrategyMetrics)]
+    L.cs_alerts_to_ndjson.argtypes = [vp, u64, u64, u64, vp, sz, psz]
     L.cs_microbench.argtypes = [C.c_int, vp, u64, C.c_int, C.c_int, C.c_int, C.c_int,
                                 C.POINTER(C.c_double)]
     L.cs_host_alloc.argtypes = [sz, C.POINTER(vp)]
@@ -101,6 +107,8 @@ EXPORTED_SYMBOLS = [
     "cs_model_from_json", "cs_model_to_json", "cs_model_view", "cs_model_free",
     "cs_ucl_from_stats", "cs_compute_ucl", "cs_config_from_json", "cs_synth_generate",
     "cs_synth_view", "cs_synth_names", "cs_synth_free", "cs_set_option", "cs_microbench",
+    "cs_redetect", "cs_evaluate_strategy", "cs_alerts_to_ndjson", "cs_stream_begin",
+    "cs_stream_end", "cs_stream_tail",
 ]
 
 
@@ -346,6 +354,22 @@ class Analyzer:
     def run(self, mask: int = abi.RUN_ALL):
         self._ck(self.L.cs_run(self.h, mask))
 
+    def redetect(self, control: abi.ControlConfig):
+        """Control chart only, new ControlConfig, same residuals."""
+        self.control = control
+        self._ck(self.L.cs_redetect(self.h, C.byref(control)))
+
+    def stream(self) -> "Stream":
+        """Begin a micro-batched stream on this analyzer (cs_stream_begin)."""
+        return Stream(self)
+
+    def evaluate_strategy(self, labels, inst=0) -> abi.StrategyMetrics:
+        """StrategyMetrics vs per-cycle labels (detector.cpp:166-224)."""
+        lab = np.ascontiguousarray(np.asarray(labels, dtype=np.uint8))
+        m = abi.StrategyMetrics()
+        self._ck(self.L.cs_evaluate_strategy(self.h, inst, _ptr(lab), len(lab), C.byref(m)))
+        return m
+
     def launches(self) -> int:
         n = C.c_uint64()
         self._ck(self.L.cs_get_launch_count(self.h, C.byref(n)))
@@ -428,3 +452,53 @@ def host_alloc(nbytes: int) -> tuple[int, np.ndarray]:
 
 def host_free(ptr: int):
     lib().cs_host_free(C.c_void_p(ptr))
+
+
+def alerts_to_ndjson(alerts: np.ndarray, pre_roll: int = 5, post_roll: int = 20) -> str:
+    """monitor_loop's NDJSON alert sink incl. escalation (main.cpp:151-177)."""
+    a = np.ascontiguousarray(alerts, dtype=abi.ALERT_DTYPE)
+    n = C.c_size_t()
+    L = lib()
+    _check(L.cs_alerts_to_ndjson(_ptr(a), len(a), pre_roll, post_roll, None, 0, C.byref(n)))
+    buf = C.create_string_buffer(n.value)
+    _check(L.cs_alerts_to_ndjson(_ptr(a), len(a), pre_roll, post_roll, buf, n.value, C.byref(n)))
+    return buf.value.decode()
+
+
+class Stream:
+    """monitor_loop over time-sliced micro-batches (BASELINE config 5).
+
+    Each push() uploads, per instance, the carried trailing partial cycle of
+    the previous batch followed by the new events, runs the path, and keeps
+    the new trailing partial cycle (cs_stream_tail).  Detector, stage
+    heuristic, cycle indices and episode ids continue across pushes on the
+    device; the union of all pushes equals one whole-trace run minus the
+    final partial cycle."""
+
+    def __init__(self, analyzer: Analyzer):
+        self.an = analyzer
+        self.tails: list[np.ndarray] | None = None
+        _check(lib().cs_stream_begin(analyzer.h), analyzer.h)
+
+    def push(self, events_per_inst, workloads, mask: int = abi.RUN_ALL):
+        if self.tails is None:
+            self.tails = [np.zeros(0, abi.EVENT_DTYPE) for _ in events_per_inst]
+        if len(events_per_inst) != len(self.tails):
+            raise ValueError("instance count changed mid-stream")
+        parts = [np.concatenate([t, np.asarray(e, dtype=abi.EVENT_DTYPE)])
+                 for t, e in zip(self.tails, events_per_inst)]
+        off = np.zeros(len(parts) + 1, np.uint64)
+        off[1:] = np.cumsum([len(p) for p in parts])
+        ev = np.concatenate(parts) if parts else np.zeros(0, abi.EVENT_DTYPE)
+        self.an.upload(ev, off, workloads)
+        self.an.run(mask)
+        out = [self.an.result(i, beta=bool(mask & abi.RUN_BETA), scored=bool(mask & abi.RUN_DETECT))
+               for i in range(len(parts))]
+        keep = C.c_uint64(0)
+        for i, p in enumerate(parts):
+            _check(lib().cs_stream_tail(self.an.h, i, C.byref(keep)), self.an.h)
+            self.tails[i] = p[keep.value:].copy()
+        return out
+
+    def close(self):
+        _check(lib().cs_stream_end(self.an.h), self.an.h)

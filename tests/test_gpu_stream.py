@@ -1,0 +1,139 @@
+"""GPU: streaming micro-batches (BASELINE config 5; monitor_loop, main.cpp:151-177).
+
+A trace fed as time-sliced micro-batches through cs_stream_* gives exactly the
+cycles, per-cycle beta, records (residual, statistic, flags, episode ids) and
+alerts of one whole-trace cs_run — which the parity suites pin to the
+reference.  Batch-local fields (event positions, record_index) are excluded."""
+import numpy as np
+import pytest
+
+from paper_2601_09258_b200 import abi
+
+pytestmark = pytest.mark.gpu
+
+FM_MASK = 0x3
+
+
+def _traces(rt, n_inst, strip_fm):
+    out = []
+    for i in range(n_inst):
+        t = rt.synth_trace(1200, 31 + i, 57 + i, fault=["cpu_contention", "memory_thrash",
+                                                          "gpu_clock_lock"][i % 3],
+                           onset=700, duration=150, compact_names=False)
+        if strip_fm:
+            t.events["flags"] &= np.uint16(~FM_MASK & 0xFFFF)
+        out.append(t)
+    return out
+
+
+def _merge(traces):
+    evs, wls, offs, base = [], [], [0], 0
+    for t in traces:
+        ev = t.events.copy()
+        has = (ev["flags"] & abi.EV_HAS_BATCH) != 0
+        ev["payload"][has] = (ev["payload"][has] & np.uint64(0xFFFFFFFF00000000)) | \
+            ((ev["payload"][has] & np.uint64(0xFFFFFFFF)) + np.uint64(base))
+        base += len(t.workloads)
+        wls.append(t.workloads)
+        evs.append(ev)
+        offs.append(offs[-1] + len(ev))
+    return evs, np.concatenate(wls), offs
+
+
+def _setup(rt, an, traces):
+    names = traces[0].names
+    evs, wl, offs = _merge(traces)
+    allev = np.concatenate(evs)
+    an.set_fused(False)
+    an.configure(names, rt.span_names_mask(allev, len(names)),
+                 n_comm_slots=max(t.n_comm for t in traces))
+    return evs, wl, offs, allev
+
+
+def _fit(rt, an, n_inst):
+    models = []
+    for i in range(n_inst):
+        recs = an.records(i)
+        tr = recs[recs["cycle_index"] < 500]
+        x = np.stack([tr["batch"].astype(float),
+                      (tr["batch"] * (tr["input_len"] + tr["output_len"])).astype(float)], 1)
+        models.append(rt.fit_latency_model(x, tr["latency_s"]))
+    return models
+
+
+def _cat(parts, dtype):
+    return np.concatenate(parts) if parts else np.zeros(0, dtype)
+
+
+@pytest.mark.parametrize("n_inst,strip_fm,slice_ms,hint", [(1, False, 37.0, True),
+                                                            (3, False, 113.0, False),
+                                                            (2, True, 61.0, False),
+                                                            (1, False, 10.0, True)])
+def test_stream_equals_whole_trace(rt, n_inst, strip_fm, slice_ms, hint):
+    """hint=True: the anchor is given (anchor_hint); False: the first
+    micro-batch (a calibration window of 20% of the trace) discovers it and
+    the stream keeps it."""
+    traces = _traces(rt, n_inst, strip_fm)
+    whole = rt.Analyzer(0)
+    evs, wl, offs, allev = _setup(rt, whole, traces)
+    whole.upload(allev, offs, wl)
+    whole.run(abi.RUN_SEGMENT)
+    models = _fit(rt, whole, n_inst)
+    for i, m in enumerate(models):
+        whole.load_model(m, i)
+    whole.run(abi.RUN_ALL)
+    ref = [whole.result(i) for i in range(n_inst)]
+    assert all(len(r.alerts) >= 1 for r in ref)
+
+    an = rt.Analyzer(0)
+    _setup(rt, an, traces)
+    if hint:
+        anchors = {r.summary.anchor_name_id for r in ref}
+        assert len(anchors) == 1
+        an.cycle.anchor_hint_name = anchors.pop()
+        an.set_config(an.cycle, an.control)
+    for i, m in enumerate(models):
+        an.load_model(m, i)
+    st = an.stream()
+    t_end = max(int(e["start_ts"].max()) for e in evs) + 1
+    t0 = min(int(e["start_ts"].min()) for e in evs)
+    step = int(slice_ms * 1e6)
+    got = [dict(cyc=[], beta=[], rec=[], al=[]) for _ in range(n_inst)]
+    n_batches = 0
+    first = t0 + (0 if hint else (t_end - t0) // 5)
+    bounds = [t0] + list(range(max(first, t0 + step), t_end, step)) + [t_end]
+    for lo, hi in zip(bounds[:-1], bounds[1:]):
+        batch = []
+        for e in evs:
+            a, b = np.searchsorted(e["start_ts"], [lo, hi], side="left")
+            batch.append(e[a:b])
+        res = st.push(batch, wl)
+        n_batches += 1
+        for i, r in enumerate(res):
+            if r.summary.status == 0:
+                got[i]["cyc"].append(r.cycles)
+                got[i]["beta"].append(r.beta)
+                got[i]["rec"].append(r.records)
+                got[i]["al"].append(r.alerts)
+    st.close()
+    assert n_batches > 10
+    for i in range(n_inst):
+        cyc = _cat(got[i]["cyc"], abi.CYCLE_DTYPE)
+        for f in ["index", "start_ts", "end_ts", "anchor_span_end", "stage", "workload_status"]:
+            assert np.array_equal(cyc[f], ref[i].cycles[f]), (i, f)
+        beta = np.concatenate(got[i]["beta"])
+        assert np.array_equal(beta.view(np.uint64), ref[i].beta.view(np.uint64))
+        rec = _cat(got[i]["rec"], abi.RECORD_DTYPE)
+        assert len(rec) == len(ref[i].records)
+        for f in ["cycle_index", "start_ts", "batch", "input_len", "output_len", "stage", "armed",
+                  "flagged", "alert", "episode_id"]:
+            assert np.array_equal(rec[f], ref[i].records[f]), (i, f)
+        for f in ["latency_s", "predicted_s", "residual", "statistic"]:
+            assert np.array_equal(rec[f].view(np.uint64), ref[i].records[f].view(np.uint64)), (i, f)
+        al = _cat(got[i]["al"], abi.ALERT_DTYPE)
+        for f in ["cycle", "ts", "batch", "episode_id"]:
+            assert np.array_equal(al[f], ref[i].alerts[f]), (i, f)
+        assert np.array_equal(al["smoothed_error"].view(np.uint64),
+                              ref[i].alerts["smoothed_error"].view(np.uint64))
+    whole.close()
+    an.close()
