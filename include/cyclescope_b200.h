@@ -278,7 +278,9 @@ int cs_set_name_table(cs_ctx* ctx, uint32_t n_names, const cs_name_info* names);
 int cs_upload(cs_ctx* ctx, uint32_t n_inst, const uint64_t* inst_offsets,
               const cs_event* ev, uint64_t n_workloads, const cs_workload* wl);
 
-/* Latency model for instance `inst` (UINT32_MAX = all instances).
+/* Latency model for instance `inst` (UINT32_MAX = default for every instance
+ * without its own binding).  Bindings are by instance index, may precede the
+ * first cs_upload and survive re-uploads (streams).
  * Replaces LatencyModel::load/predict (baseline.cpp:288-317, gbdt.cpp:173-184). */
 int cs_load_model(cs_ctx* ctx, uint32_t inst, const cs_model* model);
 

@@ -66,6 +66,8 @@ struct PackedModel {
 
 }  // namespace
 
+constexpr uint32_t kMaxBoundInstances = 1u << 24;  // model bindings per ctx
+
 struct cs_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -107,7 +109,12 @@ struct cs_ctx {
   uint64_t n_records = 0;
   // models
   std::vector<PackedModel*> model_store;
-  std::vector<int> model_of_inst;
+  std::vector<int> model_of_inst;  // per instance index; -1: use default_model
+  int default_model = -1;          // cs_load_model(ctx, UINT32_MAX, ...)
+  int model_id(uint32_t i) const {
+    const int id = i < model_of_inst.size() ? model_of_inst[i] : -1;
+    return id >= 0 ? id : default_model;
+  }
   DevBuf d_models;
   std::vector<DevModel> h_models;
   // fold results per instance: name -> (mean, cv, score)
@@ -424,7 +431,8 @@ int cs_upload(cs_ctx* ctx, uint32_t n_inst, const uint64_t* inst_offsets, const 
   }
   CS_CUDA(cudaMemcpyAsync(dft, ctx->inst_first_tile.data(), n_inst * 4, cudaMemcpyHostToDevice,
                           ctx->stream));
-  if (ctx->model_of_inst.size() != n_inst) ctx->model_of_inst.assign(n_inst, -1);
+  // bindings are by instance index and survive re-uploads (streaming pushes)
+  if (ctx->model_of_inst.size() < n_inst) ctx->model_of_inst.resize(n_inst, -1);
   ctx->ran = false;
   return CS_OK;
 }
@@ -548,10 +556,12 @@ int cs_load_model(cs_ctx* ctx, uint32_t inst, const cs_model* m) {
   ctx->model_store.push_back(pm);
   const int id = static_cast<int>(ctx->model_store.size() - 1);
   if (inst == UINT32_MAX) {
-    ctx->model_of_inst.assign(std::max<uint32_t>(ctx->n_inst, 1), id);
+    ctx->default_model = id;
+    ctx->model_of_inst.assign(ctx->model_of_inst.size(), -1);
   } else {
-    if (inst >= ctx->n_inst) return fail(ctx, CS_E_INVALID_ARGUMENT, "instance out of range");
-    if (ctx->model_of_inst.size() != ctx->n_inst) ctx->model_of_inst.assign(ctx->n_inst, -1);
+    // an instance index may be bound before its first upload (streams)
+    if (inst >= kMaxBoundInstances) return fail(ctx, CS_E_INVALID_ARGUMENT, "instance out of range");
+    if (ctx->model_of_inst.size() <= inst) ctx->model_of_inst.resize(inst + 1, -1);
     ctx->model_of_inst[inst] = id;
   }
   return CS_OK;
@@ -944,7 +954,7 @@ int cs_run(cs_ctx* ctx, uint32_t mask) {
     ctx->h_models.assign(n_inst, DevModel{});
     uint32_t nf0 = UINT32_MAX;
     for (uint32_t i = 0; i < n_inst; ++i) {
-      const int id = i < ctx->model_of_inst.size() ? ctx->model_of_inst[i] : -1;
+      const int id = ctx->model_id(i);
       if (id < 0) return fail(ctx, CS_E_INVALID_ARGUMENT, "no model loaded for an instance");
       const PackedModel* pm = ctx->model_store[id];
       if (nf0 == UINT32_MAX) nf0 = pm->n_features;
@@ -1292,7 +1302,7 @@ int cs_redetect(cs_ctx* ctx, const cs_control_config* control) {
   ctx->ctl = *control;
   const uint32_t n_inst = ctx->n_inst;
   for (uint32_t i = 0; i < n_inst; ++i) {
-    const PackedModel* pm = ctx->model_store[ctx->model_of_inst[i]];
+    const PackedModel* pm = ctx->model_store[ctx->model_id(i)];
     ctx->h_models[i].ucl = ctx->ctl.strategy == CS_DYNAMIC_WINDOW
                                ? ucl_from_stats_host(pm->mu, pm->sigma, ctx->ctl)
                                : ctx->ctl.fixed_threshold;
