@@ -2108,234 +2108,550 @@ struct TileMeta {
   u64 tb, ib;
 };
 
-template <bool kReg>
-__global__ void __launch_bounds__(kFThreads, 2)
-    k_fused_segment(DevBuffers b, DevConfig cfg, FusedMeta fm, int do_beta,
-                    uint32_t n_cyc_threads) {
+// Event-parallel single pass (K1+K2+K3 in one read of the events), warp
+// specialised.  A producer warp owns the tile ring: it claims tiles in order
+// (ticket), issues their TMA bulk copies kGStages deep, and when a tile lands
+// counts its anchors, publishes the count and runs the decoupled look-back
+// for the global rank P0 of the tile's first anchor (= its first cycle slot),
+// all off the consumers' critical path.  Sixteen consumer warps process each
+// landed tile:
+//   S1  PythonCall moments (per-thread name cache) + anchor ballots -> the
+//       tile-local anchor list (position, start);
+//   S3  cycle-start marks: group start of every anchor (lower_bound over
+//       equal start_ts, cycles.cpp:137-144) as a bit per tile position, so an
+//       event's local cycle is a popcount over the bitmap;
+//   S4  every event adds its clipped span time into its cycle's row of
+//       shared-memory accumulators with 32-bit atomics (component durations
+//       cycles.cpp:157-166, class occupancy rca.cpp:87-96), the first
+//       forward_mode and workload carrier by atomicMin on the position
+//       (cycles.cpp:205-209, 256-281), keyword bits (222-227) and the
+//       per-(name, comm, rank) collective beta (rca.cpp:108-115): a slot with
+//       a single contribution per cycle is exact (0.0 + term), a cycle with a
+//       repeated slot is re-summed in event order by one thread;
+//   S5  rows -> SoA cycle outputs at slots P0 + k, coalesced.
+// Cycles whose events cross a tile edge (the trailing one of every tile, and
+// leading ones whose equal-start group reaches back into the previous tile)
+// are registered for k_fixup_cycles, which reduces them from global memory.
+// Tiles with more closed cycles than the row capacity run in chunks.
+constexpr int kGConsumerWarps = 16;
+constexpr int kGWork = kGConsumerWarps * 32;   // consumer threads 0..511
+constexpr int kGLookbackWarps = 2;
+constexpr int kGThreads = kGWork + 32 * (1 + kGLookbackWarps);  // + TMA issue + look-back warps
+constexpr int kGTile = kFTile;
+constexpr int kGStages = 5;
+constexpr int kGCycCap = 64;
+constexpr int kGAccWords = 4096;               // 16 KiB of accumulator rows
+constexpr int kGIt = kGTile / kGWork;
+
+struct RowLayout {
+  uint32_t comp, beta, coll, colln, fm, wl, kw, words, cap;
+};
+__device__ __forceinline__ RowLayout row_layout(const DevConfig& cfg, int do_beta) {
+  RowLayout L;
+  const uint32_t P = (uint32_t)cfg.cyc.n_phases;
+  const uint32_t C = do_beta ? (uint32_t)cfg.cyc.n_beta_slots : 0u;
+  const uint32_t R = do_beta ? (uint32_t)cfg.cyc.n_comm_slots : 0u;
+  L.comp = 0;
+  L.beta = 2 * P;
+  L.coll = L.beta + 2 * C;
+  L.colln = L.coll + 2 * R;
+  L.fm = L.colln + R;
+  L.wl = L.fm + 1;
+  L.kw = L.wl + 1;
+  L.words = (L.kw + 2) & ~1u;
+  const uint32_t c = kGAccWords / L.words;
+  L.cap = c < (uint32_t)kGCycCap ? c : (uint32_t)kGCycCap;
+  return L;
+}
+
+// 64-bit add of a positive value into a (lo, hi) pair of 32-bit words with
+// native 32-bit shared atomics (64-bit shared atomics are CAS loops on sm_100a)
+__device__ __forceinline__ void smem_add64(uint32_t* w, i64 v) {
+  const uint32_t lo = (uint32_t)(u64)v, hi = (uint32_t)((u64)v >> 32);
+  const uint32_t old = atomicAdd(w, lo);
+  const uint32_t carry = (old + lo < old) ? 1u : 0u;
+  if (hi | carry) atomicAdd(w + 1, hi + carry);
+}
+__device__ __forceinline__ i64 row_i64(const uint32_t* w) {
+  return (i64)(((u64)w[1] << 32) | w[0]);
+}
+
+__device__ __forceinline__ void bar_work() {  // the 16 consumer warps
+  asm volatile("bar.sync 1, %0;" ::"n"(kGWork) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// consumer-group version of cache_flush (no CTA-wide barrier): per-thread
+// caches -> the warp's rows -> global atomics
+__device__ void cache_flush_warp(NameCache& c, NameStat* g, WarpNameRow* wrows) {
+  const int lane = threadIdx.x & 31;
+  if (lane < kWarpNameRows) {
+    wrows[lane].name = 0xffffffffu;
+    wrows[lane].cnt = 0;
+    wrows[lane].sum = wrows[lane].sq_lo = wrows[lane].sq_hi = 0;
+  }
+  __syncwarp();
+#pragma unroll
+  for (int i = 0; i < kNameCache; ++i)
+    rows_merge(wrows, g, c.name[i] != 0xffffffffu && c.cnt[i] > 0, c.name[i], c.cnt[i], c.sum[i],
+               c.lo[i], c.hi[i]);
+  __syncwarp();
+  if (lane < kWarpNameRows) {
+    const WarpNameRow r = wrows[lane];
+    if (r.name != 0xffffffffu && r.cnt) {
+      atomicAdd(&g[r.name].count, (u64)r.cnt);
+      atomicAdd(&g[r.name].sum, r.sum);
+      atomic_add_u128(&g[r.name].sumsq_lo, &g[r.name].sumsq_hi, r.sq_lo, r.sq_hi);
+    }
+  }
+  __syncwarp();
+  cache_clear(c);
+}
+
+struct TileMetaG {
+  uint32_t t, inst, n, guess;
+  u64 tb, ib;
+};
+
+__global__ void __launch_bounds__(kGThreads, 1)
+    k_segment_pass(DevBuffers b, DevConfig cfg, FusedMeta fm, int do_beta) {
   extern __shared__ __align__(128) unsigned char s_dyn[];
-  __shared__ uint64_t s_bar[kFStages];
-  __shared__ TileMeta s_meta[kFStages];
-  __shared__ WarpNameRow s_rows[(kFThreads / 32) * kWarpNameRows];
-  __shared__ cs_name_info s_names[kFNamesSmem];
-  __shared__ uint32_t s_warp_cnt[kFThreads / 32];
-  __shared__ u64 s_P;
-  __shared__ volatile uint32_t s_ready;
+  __shared__ uint64_t s_full[kGStages], s_empty[kGStages], s_pref[kGStages];
+  __shared__ TileMetaG s_meta[kGStages];
+  __shared__ u64 s_P[kGStages];
+  __shared__ WarpNameRow s_rows[kGConsumerWarps * kWarpNameRows];
+  __shared__ uint32_t s_warp_cnt[kGConsumerWarps];
+  __shared__ uint32_t s_cbits[kGTile / 32];
+  __shared__ uint32_t s_wpre[kGTile / 32];
+  __shared__ uint16_t s_first[kGTile + 1];
+  __shared__ uint32_t s_dup, s_nlead, s_unknown, s_wide, s_reorder;
 
   unsigned char* s_tiles = s_dyn;
-  uint16_t* s_apos = reinterpret_cast<uint16_t*>(s_dyn + kFStages * kFTileBytes);
-  i64* s_astart = reinterpret_cast<i64*>(s_dyn + kFStages * kFTileBytes + kFTile * 2);
-  i64* s_aend = s_astart + kFTile;
-  uint32_t* s_scratch = reinterpret_cast<uint32_t*>(s_aend + kFTile);
+  uint16_t* s_apos = reinterpret_cast<uint16_t*>(s_dyn + kGStages * kFTileBytes);
+  i64* s_astart = reinterpret_cast<i64*>(s_dyn + kGStages * kFTileBytes + kGTile * 2);
+  uint32_t* s_acc = reinterpret_cast<uint32_t*>(s_astart + kGTile);
+
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  constexpr int kWarps = kFThreads / 32;
-  constexpr int kIt = kFTile / kFThreads;
-  const int C = cfg.cyc.n_beta_slots, R = cfg.cyc.n_comm_slots;
-  const uint32_t sw = scratch_words(cfg);
-  const int ct = (int)threadIdx.x - 32;  // cycle threads: warps 1..
-  const bool is_cyc = ct >= 0 && ct < (int)n_cyc_threads;
-  i64* my_beta = reinterpret_cast<i64*>(s_scratch + (u64)(is_cyc && !kReg ? ct : 0) * sw);
-  double* my_coll = reinterpret_cast<double*>(my_beta + C);
-  uint32_t* my_colln = reinterpret_cast<uint32_t*>(my_coll + R);
-
-  auto issue = [&](int s) {  // thread 0: claim the next tile for stage s
-    const uint32_t t = atomicAdd(fm.ticket, 1u);
-    TileMeta m;
-    m.t = t;
-    if (t < b.n_tiles) {
-      m.inst = b.tile_inst[t];
-      m.tb = b.tile_begin[t];
-      m.n = (uint32_t)(b.tile_end[t] - m.tb);
-      m.ib = b.inst_off[m.inst];
-      m.guess = b.inst[m.inst].guess;
-      const uint32_t bytes = m.n * (uint32_t)sizeof(cs_event);
-      mbar_expect_tx(&s_bar[s], bytes);
-      bulk_g2s(s_tiles + s * kFTileBytes, b.ev + m.tb, bytes, &s_bar[s]);
-    }
-    s_meta[s] = m;
-  };
-
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kFStages; ++s) mbar_init(&s_bar[s], 1);
-    mbar_fence_init();
-    s_ready = 0;
-  }
-  for (uint32_t i = threadIdx.x; i < b.n_names && i < (uint32_t)kFNamesSmem; i += blockDim.x)
-    s_names[i] = b.names[i];
-  rows_zero(s_rows);
-  __syncthreads();
-  if (threadIdx.x == 0)
-    for (int s = 0; s < kFStages; ++s) issue(s);
-  __syncthreads();
-  if (warp == 0 && !(fm.debug & 1)) {  // publish the first tile's aggregate on arrival
-    const TileMeta m0 = s_meta[0];
-    if (m0.t < b.n_tiles) {
-      mbar_wait(&s_bar[0], 0);
-      const uint32_t c = warp_count_anchors(reinterpret_cast<const cs_event*>(s_tiles), m0.n,
-                                            m0.guess);
-      if (lane == 0) publish_aggregate(fm.state, m0.t, c);
+    for (int s = 0; s < kGStages; ++s) {
+      mbar_init(&s_full[s], 1);
+      mbar_init(&s_empty[s], 1);
+      mbar_init(&s_pref[s], 1);
     }
+    mbar_fence_init();
   }
+  __syncthreads();
+  // static schedule: this CTA's k-th tile is blockIdx.x + k * gridDim.x, so
+  // the tile metadata can be fetched 32 tiles ahead (all CTAs are resident:
+  // the grid is one CTA per SM)
+  const uint32_t G = gridDim.x;
+  const uint32_t n_mine = b.n_tiles > blockIdx.x ? (b.n_tiles - blockIdx.x + G - 1) / G : 0;
+
+  if (warp == kGConsumerWarps) {
+    // ======================= TMA issue warp
+    TileMetaG pm{};  // lane l: metadata of this CTA's tile (batch + l)
+    for (uint32_t it = 0; it < n_mine + kGLookbackWarps; ++it) {
+      if ((it & 31u) == 0) {
+        const uint32_t k = it + lane;
+        pm.t = k < n_mine ? blockIdx.x + k * G : 0xffffffffu;
+        if (k < n_mine) {
+          pm.inst = b.tile_inst[pm.t];
+          pm.tb = b.tile_begin[pm.t];
+          pm.n = (uint32_t)(b.tile_end[pm.t] - pm.tb);
+          pm.ib = b.inst_off[pm.inst];
+          pm.guess = b.inst[pm.inst].guess;
+        }
+      }
+      const int st = it % kGStages;
+      if (it >= (uint32_t)kGStages) mbar_wait(&s_empty[st], ((it / kGStages) - 1) & 1u);
+      TileMetaG m;
+      const int src = it & 31;
+      m.t = __shfl_sync(0xffffffffu, pm.t, src);
+      m.inst = __shfl_sync(0xffffffffu, pm.inst, src);
+      m.n = __shfl_sync(0xffffffffu, pm.n, src);
+      m.guess = __shfl_sync(0xffffffffu, pm.guess, src);
+      m.tb = __shfl_sync(0xffffffffu, pm.tb, src);
+      m.ib = __shfl_sync(0xffffffffu, pm.ib, src);
+      if (lane == 0) {
+        s_meta[st] = m;
+        if (it < n_mine) {
+          const uint32_t bytes = m.n * (uint32_t)sizeof(cs_event);
+          mbar_expect_tx(&s_full[st], bytes);
+          bulk_g2s(s_tiles + st * kFTileBytes, b.ev + m.tb, bytes, &s_full[st]);
+        } else {
+          mbar_arrive(&s_full[st]);  // sentinel for the consumers / a look-back warp
+        }
+      }
+      __syncwarp();
+    }
+    return;
+  }
+  if (warp > kGConsumerWarps) {
+    // ======================= look-back warps: tiles it = w, w + NW, ...
+    const uint32_t w = (uint32_t)(warp - kGConsumerWarps - 1);
+    for (uint32_t it = w;; it += kGLookbackWarps) {
+      const int st = it % kGStages;
+      mbar_wait(&s_full[st], (it / kGStages) & 1u);
+      const TileMetaG m = s_meta[st];
+      if (m.t >= b.n_tiles) break;
+      u64 P0 = 0;
+      if (!(fm.debug & 1)) {
+        const uint32_t c = warp_count_anchors(reinterpret_cast<const cs_event*>(s_tiles + st * kFTileBytes),
+                                              m.n, m.guess);
+        if (lane == 0) publish_aggregate(fm.state, m.t, c);
+        P0 = lookback_wait(fm.state, m.t, c);
+        if (lane == 0) {
+          fm.t_cnt[m.t] = c;
+          fm.t_pref[m.t] = P0;
+          if (P0 + c > fm.capacity) atomicOr(fm.overflow, 1u);
+        }
+      }
+      if (lane == 0) {
+        s_P[st] = P0;
+        mbar_arrive(&s_pref[st]);
+      }
+      __syncwarp();
+    }
+    return;
+  }
+
+  // ========================= consumer warps
+  // packed per-name info: bits 0-3 phase (15 none), 4-11 beta slot (255 none),
+  // 12-13 keyword bits; names beyond kFNamesSmem are read from global
+  __shared__ uint32_t s_ninfo[kFNamesSmem];
+  const RowLayout L = row_layout(cfg, do_beta);
+  const int P = cfg.cyc.n_phases;
+  const int C = do_beta ? cfg.cyc.n_beta_slots : 0;
+  const int R = do_beta ? cfg.cyc.n_comm_slots : 0;
+  const uint32_t tid = threadIdx.x;
+  auto pack_info = [&](const cs_name_info& ni) -> uint32_t {
+    const uint32_t ph = (ni.phase >= 0 && ni.phase < P) ? (uint32_t)ni.phase : 15u;
+    const uint32_t bs = (ni.beta_slot >= 0 && ni.beta_slot < C) ? (uint32_t)ni.beta_slot : 255u;
+    return ph | (bs << 4) | ((ni.flags & 3u) << 12);
+  };
+  for (uint32_t i = tid; i < b.n_names && i < (uint32_t)kFNamesSmem; i += kGWork)
+    s_ninfo[i] = pack_info(b.names[i]);
+  bar_work();
+  NameCache cache;
+  cache_clear(cache);
   uint32_t cur_inst = 0xffffffffu;
   for (uint32_t it = 0;; ++it) {
-    const int stage = it % kFStages;
-    const uint32_t parity = (it / kFStages) & 1u;
-    const TileMeta m = s_meta[stage];
+    const int stage = it % kGStages;
+    const uint32_t ph = (it / kGStages) & 1u;
+    mbar_wait(&s_full[stage], ph);
+    const TileMetaG m = s_meta[stage];
     if (m.t >= b.n_tiles) break;
     if (m.inst != cur_inst) {
-      if (cur_inst != 0xffffffffu) {
-        __syncthreads();
-        rows_flush(b.stats + (u64)cur_inst * b.n_names, s_rows);
-        __syncthreads();
-        rows_zero(s_rows);
-        __syncthreads();
-      }
+      if (cur_inst != 0xffffffffu)
+        cache_flush_warp(cache, b.stats + (u64)cur_inst * b.n_names, s_rows + warp * kWarpNameRows);
       cur_inst = m.inst;
     }
     NameStat* gstats = b.stats + (u64)m.inst * b.n_names;
-    mbar_wait(&s_bar[stage], parity);
-    const cs_event* tile = reinterpret_cast<const cs_event*>(s_tiles + stage * kFTileBytes);
+    const int4* t4 = reinterpret_cast<const int4*>(s_tiles + stage * kFTileBytes);
 
-    // 1. moments + anchor flags
-    uint32_t masks[kIt];
+    // ---- S1: this thread's events stay in registers through S4
+    int4 H0[kGIt], H1[kGIt];
+    uint32_t masks[kGIt];
+#pragma unroll
+    for (int q = 0; q < kGIt; ++q) {
+      const uint32_t j = (uint32_t)warp * (kGIt * 32) + q * 32 + lane;
+      bool is_anchor = false;
+      if (j < m.n) {
+        H0[q] = t4[2 * j];
+        H1[q] = t4[2 * j + 1];
+        if (((uint32_t)H1[q].y & 0xffu) == CS_SPAN) {
+          if ((((uint32_t)H1[q].y >> 8) & 0xffu) == CS_CAT_PYTHON_CALL)
+            cache_add(cache, gstats, (uint32_t)H1[q].x,
+                      (i64)(((u64)(uint32_t)H0[q].w << 32) | (uint32_t)H0[q].z));
+          is_anchor = (uint32_t)H1[q].x == m.guess;
+        }
+      } else {
+        H0[q] = make_int4(0, 0, 0, 0);
+        H1[q] = make_int4(0, CS_FLOW, 0, 0);  // ignored
+      }
+      masks[q] = __ballot_sync(0xffffffffu, is_anchor);
+    }
     uint32_t my = 0;
 #pragma unroll
-    for (int j = 0; j < kIt; ++j) {
-      const uint32_t e_idx = (uint32_t)warp * (kIt * 32) + j * 32 + lane;
-      bool is_anchor = false, py = false;
-      uint32_t name = 0;
-      i64 d = 0;
-      if (e_idx < m.n) {
-        const int4 h1 = reinterpret_cast<const int4*>(tile + e_idx)[1];
-        name = (uint32_t)h1.x;
-        const uint32_t kind = (uint32_t)h1.y & 0xffu;
-        const uint32_t cat = ((uint32_t)h1.y >> 8) & 0xffu;
-        if (kind == CS_SPAN) {
-          py = cat == CS_CAT_PYTHON_CALL;
-          if (py) {
-            const int4 h0 = reinterpret_cast<const int4*>(tile + e_idx)[0];
-            d = (i64)(((u64)(uint32_t)h0.w << 32) | (uint32_t)h0.z);
-          }
-          is_anchor = name == m.guess;
-        }
-      }
-      rows_add(s_rows + warp * kWarpNameRows, gstats, py, name, d);
-      masks[j] = __ballot_sync(0xffffffffu, is_anchor);
-      my += __popc(masks[j]);
-    }
+    for (int q = 0; q < kGIt; ++q) my += __popc(masks[q]);
     if (lane == 0) s_warp_cnt[warp] = my;
-    __syncthreads();
-    uint32_t base = 0, total = 0;
+    if (tid < kGTile / 32) s_cbits[tid] = 0u;
+    if (tid == 0) {
+      s_dup = 0u;
+      s_nlead = 0u;
+      s_unknown = 0u;
+      s_wide = 0u;
+      s_reorder = 0u;
+    }
+    bar_work();
+    uint32_t base, total;
+    {
+      const uint32_t c = lane < kGConsumerWarps ? s_warp_cnt[lane] : 0u;
+      uint32_t incl = c;
 #pragma unroll
-    for (int w = 0; w < kWarps; ++w) {
-      const uint32_t c = s_warp_cnt[w];
-      base += w < warp ? c : 0;
-      total += c;
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+      }
+      base = __shfl_sync(0xffffffffu, incl - c, warp);
+      total = __shfl_sync(0xffffffffu, incl, 31);
     }
 #pragma unroll
-    for (int j = 0; j < kIt; ++j) {
-      const uint32_t mk = masks[j];
+    for (int q = 0; q < kGIt; ++q) {
+      const uint32_t mk = masks[q];
       if (mk & (1u << lane)) {
-        const uint32_t e_idx = (uint32_t)warp * (kIt * 32) + j * 32 + lane;
         const uint32_t r = base + __popc(mk & lanemask_lt());
-        const cs_event* p = tile + e_idx;
-        s_apos[r] = (uint16_t)e_idx;
-        s_astart[r] = p->start_ts;
-        s_aend[r] = p->start_ts + p->duration;
+        s_apos[r] = (uint16_t)((uint32_t)warp * (kGIt * 32) + q * 32 + lane);
+        s_astart[r] = (i64)(((u64)(uint32_t)H0[q].y << 32) | (uint32_t)H0[q].x);
       }
       base += __popc(mk);
     }
-    __syncthreads();
+    const uint32_t n_loc = total >= 1 ? total - 1 : 0;  // cycles closed inside the tile
+    const uint32_t n_chunks = n_loc ? (n_loc + L.cap - 1) / L.cap : 0;
+    bar_work();
+    // ---- S3: cycle-start marks, 32-bit safety, rows of the first chunk zeroed
+    for (uint32_t k = tid; k < total; k += kGWork) {
+      uint32_t pf = s_apos[k];
+      const i64 a = s_astart[k];
+      while (pf > 0 && reinterpret_cast<const i64*>(t4 + 2 * (pf - 1))[0] == a) --pf;
+      s_first[k] = (uint16_t)pf;
+      const uint32_t bit = 1u << (pf & 31);
+      if (atomicOr(&s_cbits[pf >> 5], bit) & bit) s_dup = 1u;  // equal-start anchors
+      if (pf == 0 && m.tb > m.ib) atomicAdd(&s_nlead, 1u);
+    }
+    {
+      const uint32_t nw = (n_loc < L.cap ? n_loc : L.cap) * L.words;
+      for (uint32_t i = tid; i < nw; i += kGWork) {
+        const uint32_t f = i % L.words;
+        s_acc[i] = (f == L.fm || f == L.wl) ? 0xffffffffu : 0u;
+      }
+    }
+    bar_work();
     if (warp == 0) {
-      // 2a. publish-ahead: the next staged tile's anchor count, as soon as it lands
-      if (!(fm.debug & 1)) {
-        const int ns = (it + 1) % kFStages;
-        const TileMeta mn = s_meta[ns];
-        if (mn.t < b.n_tiles) {
-          mbar_wait(&s_bar[ns], ((it + 1) / kFStages) & 1u);
-          const uint32_t c = warp_count_anchors(
-              reinterpret_cast<const cs_event*>(s_tiles + ns * kFTileBytes), mn.n, mn.guess);
-          if (lane == 0) publish_aggregate(fm.state, mn.t, c);
+      const uint32_t c = __popc(s_cbits[lane]);
+      uint32_t incl = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+      }
+      s_wpre[lane] = incl - c;
+    }
+    // per-(cycle, slot) sums fit 32 bits when events x duration < 2^32
+    for (uint32_t k = tid; k < n_loc; k += kGWork) {
+      const u64 dur = (u64)(s_astart[k + 1] - s_astart[k]);
+      const u64 nev = (u64)(s_first[k + 1] - s_first[k]);
+      if (dur >= (1ull << 32) || dur * nev >= (1ull << 32)) s_wide = 1u;
+    }
+    bar_work();
+    const uint32_t nlead = s_nlead;
+    const bool dup = s_dup != 0u;
+    const bool wide = s_wide != 0u;
+    bool have_p = false;
+    u64 P0 = 0;
+    for (uint32_t ch = 0; ch < n_chunks; ++ch) {
+      const uint32_t c0 = ch * L.cap;
+      const uint32_t c1 = min(n_loc, c0 + L.cap);
+      if (ch > 0) {
+        const uint32_t nw = (c1 - c0) * L.words;
+        for (uint32_t i = tid; i < nw; i += kGWork) {
+          const uint32_t f = i % L.words;
+          s_acc[i] = (f == L.fm || f == L.wl) ? 0xffffffffu : 0u;
         }
+        bar_work();
       }
-      // 2b. global rank of this tile's first anchor, overlapping the cycle work
-      const u64 P0 = (fm.debug & 1) ? 0 : lookback_wait(fm.state, m.t, total);
-      if (lane == 0) {
-        fm.t_cnt[m.t] = total;
-        fm.t_pref[m.t] = P0;
-        if (P0 + total > fm.capacity) atomicOr(fm.overflow, 1u);
-      }
-      // boundary cycles -> fixup: the trailing one (end anchor in a later
-      // tile) and k = 0 if its equal-start group reaches the tile start
-      if (total > 0 && P0 + total <= fm.capacity) {
-        uint32_t p0 = s_apos[0];
-        while (p0 > 0 && tile[p0 - 1].start_ts == s_astart[0]) --p0;
-        const bool lead = p0 == 0 && m.tb > m.ib;
-        for (uint32_t k = lane; k < total; k += 32) {
-          const bool trailing = k + 1 == total;
-          if (!(trailing || (k == 0 && lead))) continue;
-          const u64 g = P0 + k;
-          b.c_start[g] = s_astart[k];
-          b.c_apos[g] = m.tb + s_apos[k];
-          b.c_aend[g] = s_aend[k];
-          b.c_inst[g] = m.inst;
-          if (!trailing) {
-            b.c_end[g] = s_astart[k + 1];
-            uint32_t pl = s_apos[k + 1];
-            while (pl > 0 && tile[pl - 1].start_ts == s_astart[k + 1]) --pl;
-            b.c_last[g] = m.tb + pl;
+      // ---- S4: this thread's events into their cycles' rows
+#pragma unroll
+      for (int q = 0; q < kGIt; ++q) {
+        if (fm.debug & 2) break;
+        const uint32_t j = (uint32_t)warp * (kGIt * 32) + q * 32 + lane;
+        uint32_t k;
+        if (!dup) {
+          const uint32_t w = j >> 5;
+          k = s_wpre[w] + __popc(s_cbits[w] & ((2u << (j & 31)) - 1u)) - 1u;
+        } else {  // upper_bound over the group starts
+          uint32_t a = 0, z = total;
+          while (a < z) {
+            const uint32_t mid = (a + z) >> 1;
+            if (s_first[mid] <= j) a = mid + 1;
+            else z = mid;
           }
-          const unsigned int slot = atomicAdd(fm.fix_n, 1u);
-          fm.fix_list[slot] = g;
-          fm.fix_flags[slot] = (trailing ? 1u : 0u) | ((k == 0 && lead) ? 2u : 0u);
+          k = a - 1;
         }
-      }
-      if (lane == 0) {
-        s_P = P0;
-        __threadfence_block();
-        s_ready = it + 1;
-      }
-    } else if (is_cyc && !(fm.debug & 2)) {
-      // 3. local cycles, one thread each, from shared memory
-      for (uint32_t k = (uint32_t)ct; k + 1 < total; k += n_cyc_threads) {
-        const i64 cs = s_astart[k], ce = s_astart[k + 1];
-        uint32_t pf = s_apos[k];
-        while (pf > 0 && tile[pf - 1].start_ts == cs) --pf;
-        if (pf == 0 && k == 0 && m.tb > m.ib) continue;  // lead boundary: fixup
-        uint32_t pl = s_apos[k + 1];
-        while (pl > 0 && tile[pl - 1].start_ts == ce) --pl;
-        if constexpr (kReg) {
-          CycAccR<kFRegC, kFRegR> acc;
-          accumulate_cycle_reg<kFRegC, kFRegR>(s_names, do_beta, tile, pf, pl, cs, ce, acc);
-          while (s_ready != it + 1) {
-          }
-          const u64 g = s_P + k;
-          if (g + 1 <= fm.capacity)
-            write_cycle_reg<kFRegC, kFRegR>(b, cfg, do_beta, acc, g, m.inst, cs, ce,
-                                            m.tb + s_apos[k], s_aend[k], m.tb + pf, m.tb + pl);
+        if (j >= m.n || k < c0 || k >= c1 || k < nlead) continue;
+        uint32_t* row = s_acc + (k - c0) * L.words;
+        const int4 h0 = H0[q], h1 = H1[q];
+        const uint32_t flags = (uint32_t)h1.y >> 16;
+        const uint32_t kind = (uint32_t)h1.y & 0xffu;
+        const uint32_t name = (uint32_t)h1.x;
+        const uint32_t info = name < (uint32_t)kFNamesSmem ? s_ninfo[name] : pack_info(b.names[name]);
+        const i64 st = (i64)(((u64)(uint32_t)h0.y << 32) | (uint32_t)h0.x);
+        const i64 d = (i64)(((u64)(uint32_t)h0.w << 32) | (uint32_t)h0.z);
+        const i64 ce = s_astart[k + 1];
+        const i64 end = st + d;
+        const i64 clipped = (end < ce ? end : ce) - st;
+        const bool span = kind == CS_SPAN;
+        const bool pos = span && clipped > 0;
+        const uint32_t phs = info & 15u, bs = (info >> 4) & 255u;
+        if (!wide) {
+          if (pos && phs != 15u) atomicAdd(&row[L.comp + 2 * phs], (uint32_t)clipped);
+          if (pos && d > 0 && bs != 255u) atomicAdd(&row[L.beta + 2 * bs], (uint32_t)clipped);
         } else {
-          const cs_name_info* names = b.n_names <= (uint32_t)kFNamesSmem ? s_names : b.names;
-          const CycAcc acc = accumulate_cycle(names, cfg, do_beta, tile, pf, pl, cs, ce, false,
-                                              my_beta, my_coll, my_colln);
-          while (s_ready != it + 1) {
+          if (pos && phs != 15u) smem_add64(&row[L.comp + 2 * phs], clipped);
+          if (pos && d > 0 && bs != 255u) smem_add64(&row[L.beta + 2 * bs], clipped);
+        }
+        if (flags & (CS_EV_FM_MASK | CS_EV_HAS_BATCH)) {
+          if (flags & CS_EV_FM_MASK) atomicMin(&row[L.fm], (j << 2) | (flags & CS_EV_FM_MASK));
+          if (flags & CS_EV_HAS_BATCH) atomicMin(&row[L.wl], j);
+        }
+        if (span && (info & (3u << 12))) atomicOr(&row[L.kw], (info >> 12) & 3u);
+        if (pos && d > 0 && (flags & CS_EV_HAS_COMM) &&
+            (((uint32_t)h1.y >> 8) & 0xffu) == CS_CAT_COLLECTIVE_COMM) {
+          const uint32_t slot = (uint32_t)h1.w;
+          if (slot < (uint32_t)R) {
+            const uint32_t n0 = atomicAdd(&row[L.colln + slot], 1u);
+            if (n0 == 0u) {
+              const double term = __ddiv_rn((double)clipped, (double)(ce - s_astart[k]));
+              *reinterpret_cast<double*>(&row[L.coll + 2 * slot]) = term;
+            } else {
+              atomicOr(&row[L.kw], 0x80000000u);  // repeated slot: ordered re-sum
+              s_reorder = 1u;
+            }
           }
-          const u64 g = s_P + k;
-          if (g + 1 <= fm.capacity)
-            write_cycle(b, cfg, do_beta, acc, g, m.inst, cs, ce, m.tb + s_apos[k], s_aend[k],
-                        m.tb + pf, m.tb + pl, my_beta, my_coll, my_colln);
         }
       }
+      if (!have_p && warp == 0) mbar_wait(&s_pref[stage], ph);
+      bar_work();
+      if (!have_p) {
+        P0 = s_P[stage];
+        have_p = true;
+      }
+      // repeated collective slots: the reference's event-ordered sum (rca.cpp:112-113)
+      if (s_reorder) {
+        for (uint32_t k = c0 + tid; k < c1; k += kGWork) {
+          uint32_t* row = s_acc + (k - c0) * L.words;
+          if (!(row[L.kw] & 0x80000000u) || k < nlead) continue;
+          double* coll = reinterpret_cast<double*>(&row[L.coll]);
+          for (int r = 0; r < R; ++r) coll[r] = 0.0;
+          const i64 cs = s_astart[k], ce = s_astart[k + 1];
+          for (uint32_t j = s_first[k]; j < s_first[k + 1]; ++j) {
+            const int4 h0 = t4[2 * j], h1 = t4[2 * j + 1];
+            if (((uint32_t)h1.y & 0xffu) != CS_SPAN) continue;
+            const uint32_t flags = (uint32_t)h1.y >> 16;
+            if ((((uint32_t)h1.y >> 8) & 0xffu) != CS_CAT_COLLECTIVE_COMM || !(flags & CS_EV_HAS_COMM))
+              continue;
+            const i64 st = (i64)(((u64)(uint32_t)h0.y << 32) | (uint32_t)h0.x);
+            const i64 d = (i64)(((u64)(uint32_t)h0.w << 32) | (uint32_t)h0.z);
+            const i64 end = st + d;
+            const i64 clipped = (end < ce ? end : ce) - st;
+            if (d <= 0 || clipped <= 0) continue;
+            const uint32_t slot = (uint32_t)h1.w;
+            if (slot < (uint32_t)R)
+              coll[slot] = __dadd_rn(coll[slot], __ddiv_rn((double)clipped, (double)(ce - cs)));
+          }
+        }
+        bar_work();
+      }
+      // ---- S5: rows -> cycle outputs (coalesced over the chunk's cycles)
+      if (P0 + total <= fm.capacity && !(fm.debug & 4)) {
+        const uint32_t ncc = c1 - c0;
+        for (uint32_t i = tid; i < ncc; i += kGWork) {
+          const uint32_t k = c0 + i;
+          if (k < nlead) continue;
+          const uint32_t* row = s_acc + i * L.words;
+          const u64 g = P0 + k;
+          const i64 cs = s_astart[k];
+          const uint32_t ap = s_apos[k];
+          b.c_start[g] = cs;
+          b.c_end[g] = s_astart[k + 1];
+          b.c_apos[g] = m.tb + ap;
+          b.c_aend[g] = cs + reinterpret_cast<const i64*>(t4 + 2 * ap)[1];
+          b.c_first[g] = m.tb + s_first[k];
+          b.c_last[g] = m.tb + s_first[k + 1];
+          b.c_inst[g] = m.inst;
+          const uint32_t fmw = row[L.fm];
+          const uint32_t fm_cls = fmw == 0xffffffffu ? 0u : (fmw & CS_EV_FM_MASK);
+          const uint32_t kw = row[L.kw];
+          const bool pkw = kw & CS_NAME_PREFILL_KW, dkw = kw & CS_NAME_DECODE_KW;
+          uint8_t stg = CS_STAGE_UNKNOWN;
+          if (fm_cls == CS_EV_FM_PREFILL) stg = CS_STAGE_PREFILL;
+          else if (fm_cls == CS_EV_FM_DECODE) stg = CS_STAGE_DECODE;
+          if (stg == CS_STAGE_UNKNOWN && pkw != dkw) stg = pkw ? CS_STAGE_PREFILL : CS_STAGE_DECODE;
+          b.c_local[g] = stg;
+          b.c_stage[g] = stg;
+          const uint32_t wj = row[L.wl];
+          int32_t wl = -1;
+          if (wj != 0xffffffffu) {
+            const int4 h1 = t4[2 * wj + 1];
+            wl = ((uint32_t)h1.y >> 16) & CS_EV_WL_OK ? (int32_t)(uint32_t)h1.z : -2;
+          }
+          b.c_wl[g] = wl;
+          if (stg == CS_STAGE_UNKNOWN) atomicAdd(&s_unknown, 1u);
+        }
+        for (uint32_t f = tid; f < ncc * (uint32_t)P; f += kGWork) {
+          const uint32_t i = f / (uint32_t)P, p = f - i * (uint32_t)P;
+          if (c0 + i < nlead) continue;
+          b.c_comp[(P0 + c0) * P + f] = row_i64(s_acc + i * L.words + L.comp + 2 * p);
+        }
+        for (uint32_t f = tid; f < ncc * (uint32_t)C; f += kGWork) {
+          const uint32_t i = f / (uint32_t)C, c = f - i * (uint32_t)C;
+          const uint32_t k = c0 + i;
+          if (k < nlead) continue;
+          const i64 dur = s_astart[k + 1] - s_astart[k];
+          const i64 t = dur > 0 ? row_i64(s_acc + i * L.words + L.beta + 2 * c) : 0;
+          b.c_beta_tot[(P0 + c0) * C + f] = t;
+          b.c_beta[(P0 + c0) * C + f] = t > 0 ? __ddiv_rn((double)t, (double)dur) : 0.0;
+        }
+        for (uint32_t f = tid; f < ncc * (uint32_t)R; f += kGWork) {
+          const uint32_t i = f / (uint32_t)R, r = f - i * (uint32_t)R;
+          if (c0 + i < nlead) continue;
+          const uint32_t* row = s_acc + i * L.words;
+          const uint32_t n = row[L.colln + r];
+          b.c_coll[(P0 + c0) * R + f] = n ? *reinterpret_cast<const double*>(&row[L.coll + 2 * r]) : 0.0;
+          b.c_coll_n[(P0 + c0) * R + f] = (uint8_t)(n > 255u ? 255u : n);
+        }
+      }
+      if (ch + 1 < n_chunks) bar_work();  // rows are reused by the next chunk
     }
-    __syncthreads();  // stage, anchor list and meta consumed
-    if (threadIdx.x == 0) {
+    if (!have_p) {
+      if (warp == 0) mbar_wait(&s_pref[stage], ph);
+      bar_work();
+      P0 = s_P[stage];
+    }
+    // boundary cycles -> k_fixup_cycles: leading ones whose group reaches the
+    // previous tile, and the trailing one (its end anchor lies in a later tile)
+    if (P0 + total <= fm.capacity && total > 0) {
+      const uint32_t nb = (nlead < total ? nlead : total - 1) + 1;  // leads + trailing
+      for (uint32_t i = tid; i < nb; i += kGWork) {
+        const bool trailing = i + 1 == nb;
+        const uint32_t k = trailing ? total - 1 : i;
+        const bool lead = k < nlead;
+        const u64 g = P0 + k;
+        const uint32_t ap = s_apos[k];
+        b.c_start[g] = s_astart[k];
+        b.c_apos[g] = m.tb + ap;
+        b.c_aend[g] = s_astart[k] + reinterpret_cast<const i64*>(t4 + 2 * ap)[1];
+        b.c_inst[g] = m.inst;
+        if (!trailing) {
+          b.c_end[g] = s_astart[k + 1];
+          b.c_last[g] = m.tb + s_first[k + 1];
+        }
+        const unsigned int slot = atomicAdd(fm.fix_n, 1u);
+        fm.fix_list[slot] = g;
+        fm.fix_flags[slot] = (trailing ? 1u : 0u) | (lead ? 2u : 0u);
+      }
+    }
+    bar_work();  // stage, anchor list, rows consumed
+    if (tid == 0) {
+      if (s_unknown) atomicAdd(&b.inst[m.inst].n_unknown, (u64)s_unknown);
       fence_proxy_async();
-      issue(stage);
+      mbar_arrive(&s_empty[stage]);
     }
-    __syncthreads();
   }
-  if (cur_inst != 0xffffffffu) {
-    __syncthreads();
-    rows_flush(b.stats + (u64)cur_inst * b.n_names, s_rows);
-  }
+  if (cur_inst != 0xffffffffu)
+    cache_flush_warp(cache, b.stats + (u64)cur_inst * b.n_names, s_rows + warp * kWarpNameRows);
 }
 
 // Per-instance slot base and anchor count from the tile look-back results.
@@ -2429,30 +2745,21 @@ int launch_fused_segment(const DevBuffers& b, const DevConfig& cfg, const FusedM
   if (b.n_tiles == 0) return 0;
   FusedMeta fm{mh.debug, mh.state, mh.ticket, mh.t_cnt, mh.t_pref, mh.fix_list, mh.fix_n,
                mh.fix_flags, mh.capacity, mh.overflow};
-  const bool reg = cfg.cyc.n_beta_slots <= kFRegC && cfg.cyc.n_comm_slots <= kFRegR &&
-                   b.n_names <= (uint32_t)kFNamesSmem;
-  const uint32_t words = fused_scratch_words(cfg);
-  const int fixed = kFStages * (int)kFTileBytes + kFTile * (2 + 16);
-  uint32_t cyc_threads = (uint32_t)kFThreads - 32;
-  int smem = fixed;
-  if (!reg) {
-    const int budget = 100 * 1024 - fixed;
-    uint32_t c = budget > 0 ? (uint32_t)(budget / (int)(words * 4)) : 0;
-    if (c < cyc_threads) cyc_threads = c & ~31u;
-    if (cyc_threads < 32) return -1;  // configuration too wide for the fused kernel
-    smem = fixed + (int)(cyc_threads * words * 4);
+  const int smem = kGStages * (int)kFTileBytes + kGTile * (2 + 8) + kGAccWords * 4;  // 186 KiB
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(k_segment_pass, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    configured = true;
   }
-  auto kern = reg ? k_fused_segment<true> : k_fused_segment<false>;
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   int per_sm = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kFThreads, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_segment_pass, kGThreads, smem);
   if (per_sm < 1) per_sm = 1;
   const uint32_t want = (uint32_t)(sms * per_sm);
   const uint32_t grid = b.n_tiles < want ? b.n_tiles : want;
-  kern<<<grid, kFThreads, smem, s>>>(b, cfg, fm, do_beta, cyc_threads);
+  k_segment_pass<<<grid, kGThreads, smem, s>>>(b, cfg, fm, do_beta);
   ++*launches;
   return 0;
 }

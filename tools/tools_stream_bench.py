@@ -1,6 +1,6 @@
 """HBM streaming microbenchmark: LDG vs TMA bulk (profiling helper)."""
 import ctypes as C, os, sys
-sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_2601_09258_b200 import runtime as rt
 L = rt.lib()
