@@ -762,6 +762,7 @@ int cs_run(cs_ctx* ctx, uint32_t mask) {
       CS_CUDA(cudaMemcpyAsync(ctx->cyc_off.data(), ctx->d_cyc_off.p, (n_inst + 1) * 8,
                               cudaMemcpyDeviceToHost, s));
       CS_CUDA(cudaStreamSynchronize(s));
+      CS_CUDA(cudaGetLastError());  // launch failures surface here, not as bad counts
       if (hover) {
         // more anchors than slots: grow to the exact count and run again
         cap = ctx->cyc_off[n_inst] + 1024;
@@ -820,6 +821,7 @@ int cs_run(cs_ctx* ctx, uint32_t mask) {
   CS_CUDA(cudaMemcpyAsync(ctx->h_inst.data(), d_inst, n_inst * sizeof(InstState),
                           cudaMemcpyDeviceToHost, s));
   CS_CUDA(cudaStreamSynchronize(s));
+  CS_CUDA(cudaGetLastError());  // launch failures surface here, not as bad counts
 
   // ---- rare paths: ordered fold for uncertified rankings
   ctx->folded.assign(n_inst, {});
@@ -947,6 +949,7 @@ int cs_run(cs_ctx* ctx, uint32_t mask) {
   CS_CUDA(cudaMemcpyAsync(ctx->rec_off.data(), ctx->d_rec_off.p, (n_inst + 1) * 8,
                           cudaMemcpyDeviceToHost, s));
   CS_CUDA(cudaStreamSynchronize(s));
+  CS_CUDA(cudaGetLastError());
   ctx->n_records = ctx->rec_off[n_inst];
   int last = e6;
   // ---- score + detect

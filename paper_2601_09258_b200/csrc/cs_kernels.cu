@@ -401,6 +401,169 @@ __device__ void cache_flush(NameCache& c, NameStat* g, WarpNameRow* rows) {
   cache_clear(c);
 }
 
+// consumer-group version of cache_flush (no CTA-wide barrier): per-thread
+// caches -> the warp's rows -> global atomics
+__device__ void cache_flush_warp(NameCache& c, NameStat* g, WarpNameRow* wrows) {
+  const int lane = threadIdx.x & 31;
+  if (lane < kWarpNameRows) {
+    wrows[lane].name = 0xffffffffu;
+    wrows[lane].cnt = 0;
+    wrows[lane].sum = wrows[lane].sq_lo = wrows[lane].sq_hi = 0;
+  }
+  __syncwarp();
+#pragma unroll
+  for (int i = 0; i < kNameCache; ++i)
+    rows_merge(wrows, g, c.name[i] != 0xffffffffu && c.cnt[i] > 0, c.name[i], c.cnt[i], c.sum[i],
+               c.lo[i], c.hi[i]);
+  __syncwarp();
+  if (lane < kWarpNameRows) {
+    const WarpNameRow r = wrows[lane];
+    if (r.name != 0xffffffffu && r.cnt) {
+      atomicAdd(&g[r.name].count, (u64)r.cnt);
+      atomicAdd(&g[r.name].sum, r.sum);
+      atomic_add_u128(&g[r.name].sumsq_lo, &g[r.name].sumsq_hi, r.sq_lo, r.sq_hi);
+    }
+  }
+  __syncwarp();
+  cache_clear(c);
+}
+
+// --------------------------------------- K1 / K12 event scan (warp streaming)
+// One warp per tile (instance-aligned, <= kTileEvents events), warps
+// persistent over tiles with a static schedule.  The warp streams its tile
+// with coalesced 256-bit loads (one 32-B record per lane per load, kScanUnroll
+// records per lane in flight), folds PythonCall moments into a per-thread name
+// cache (cycles.cpp:50-59; exact integer sums, so order-free) and compacts
+// the tile's anchor occurrences (Spans named the guessed/final anchor,
+// cycles.cpp:127-131) warp-locally to a_*[tile_begin + rank] with the
+// tile's count in tile_cnt[t].  No shared-memory staging, no CTA barriers.
+constexpr int kScanWarpThreads = 256;
+constexpr int kScanUnroll = 4;
+
+struct Ev8 {
+  u64 a, b, c, d;  // start, duration, (name | kind/cat/flags << 32), payload
+};
+__device__ __forceinline__ Ev8 ldg256(const cs_event* p) {
+  Ev8 e;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u64 {%0,%1,%2,%3}, [%4];"
+               : "=l"(e.a), "=l"(e.b), "=l"(e.c), "=l"(e.d)
+               : "l"(p));
+  return e;
+}
+
+__global__ void __launch_bounds__(kScanWarpThreads, 3)
+    k_scan_warp(DevBuffers b, int mode, const uint32_t* __restrict__ list, uint32_t n_list,
+                int sample) {
+  constexpr int kW = kScanWarpThreads / 32;
+  __shared__ WarpNameRow s_rows[kW * kWarpNameRows];
+  // PythonCall spans are ~1 event in 9: they are compacted per warp and
+  // folded into the per-thread name caches 32 at a time, so the cache update
+  // runs once per PythonCall span instead of predicated on every lane
+  __shared__ uint32_t s_pn[kW][64];
+  __shared__ i64 s_pd[kW][64];
+  const bool do_stats = mode & 1;
+  const bool do_anchor = (mode & 2) && !sample;
+  const bool redo = mode & 4;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  WarpNameRow* wrows = s_rows + warp * kWarpNameRows;
+  uint32_t* pn = s_pn[warp];
+  i64* pd = s_pd[warp];
+  const uint32_t gw = blockIdx.x * kW + warp;
+  const uint32_t nw = gridDim.x * kW;
+  NameCache cache;
+  cache_clear(cache);
+  uint32_t cur_inst = 0xffffffffu, npend = 0;
+  NameStat* gstats = b.stats;
+  auto drain = [&](uint32_t take) {  // fold entries [0, take) and shift the rest down
+    __syncwarp();
+    if ((uint32_t)lane < take) cache_add(cache, gstats, pn[lane], pd[lane]);
+    __syncwarp();
+    const uint32_t rest = npend - take;
+    uint32_t mv_n = 0;
+    i64 mv_d = 0;
+    if ((uint32_t)lane < rest) {
+      mv_n = pn[take + lane];
+      mv_d = pd[take + lane];
+    }
+    __syncwarp();
+    if ((uint32_t)lane < rest) {
+      pn[lane] = mv_n;
+      pd[lane] = mv_d;
+    }
+    npend = rest;
+    __syncwarp();
+  };
+  for (uint32_t k = gw; k < n_list; k += nw) {
+    const uint32_t t = list ? list[k] : k;
+    const uint32_t inst = b.tile_inst[t];
+    const u64 tb = b.tile_begin[t];
+    u64 te = b.tile_end[t];
+    if (sample) {
+      const u64 lim = b.inst_off[inst] + kSampleEvents;
+      te = te < lim ? te : lim;
+      if (te < tb) te = tb;
+    }
+    bool active = do_anchor;
+    uint32_t anchor = 0xffffffffu;
+    if (do_anchor) {
+      const InstState& st = b.inst[inst];
+      anchor = redo ? st.anchor : st.guess;
+      if (redo && !st.redo) active = false;
+    }
+    if (do_stats && inst != cur_inst) {
+      if (cur_inst != 0xffffffffu) {
+        drain(npend);
+        cache_flush_warp(cache, gstats, wrows);
+      }
+      cur_inst = inst;
+      gstats = b.stats + (u64)inst * b.n_names;
+    }
+    const uint32_t n = (uint32_t)(te - tb);
+    uint32_t cnt = 0;
+    for (uint32_t j0 = 0; j0 < n; j0 += 32 * kScanUnroll) {
+      Ev8 e[kScanUnroll];
+#pragma unroll
+      for (int q = 0; q < kScanUnroll; ++q) {
+        const uint32_t j = j0 + q * 32 + lane;
+        if (j < n) e[q] = ldg256(b.ev + tb + j);
+        else e[q].c = (u64)CS_FLOW << 32;  // ignored
+      }
+#pragma unroll
+      for (int q = 0; q < kScanUnroll; ++q) {
+        const uint32_t name = (uint32_t)e[q].c;
+        const uint32_t kc = (uint32_t)(e[q].c >> 32);
+        const bool span = (kc & 0xffu) == CS_SPAN;
+        if (do_stats) {
+          const bool py = span && ((kc >> 8) & 0xffu) == CS_CAT_PYTHON_CALL;
+          const uint32_t pm = __ballot_sync(0xffffffffu, py);
+          if (py) {
+            const uint32_t slot = npend + __popc(pm & lanemask_lt());
+            pn[slot] = name;
+            pd[slot] = (i64)e[q].b;
+          }
+          npend += __popc(pm);
+          if (npend >= 32) drain(32);
+        }
+        const bool is_anchor = active && span && name == anchor;
+        const uint32_t mk = __ballot_sync(0xffffffffu, is_anchor);
+        if (is_anchor) {
+          const u64 r = tb + cnt + __popc(mk & lanemask_lt());
+          b.a_pos[r] = tb + j0 + q * 32 + lane;
+          b.a_start[r] = (i64)e[q].a;
+          b.a_end[r] = (i64)e[q].a + (i64)e[q].b;
+        }
+        cnt += __popc(mk);
+      }
+    }
+    if (active && lane == 0) b.tile_cnt[t] = cnt;
+  }
+  if (do_stats && cur_inst != 0xffffffffu) {
+    drain(npend);
+    cache_flush_warp(cache, gstats, wrows);
+  }
+}
+
+
 struct ScanMeta {
   uint32_t t, inst, n, anchor, active;
   u64 tb;
@@ -758,6 +921,42 @@ __global__ void k_bounds(DevBuffers b) {
   b.c_inst[g] = inst;
 }
 
+// Cycle bounds by scatter from each tile's anchor list (warp per tile): the
+// anchor of global rank r opens cycle r - base(inst) and closes the previous
+// one; first/last events by lower_bound over equal start_ts
+// (cycles.cpp:135-156).  Replaces a binary search per cycle.
+__global__ void __launch_bounds__(256) k_bounds_tile(DevBuffers b) {
+  const int lane = threadIdx.x & 31;
+  const u64 t = (u64)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (t >= b.n_tiles) return;
+  const uint32_t inst = b.tile_inst[t];
+  if (b.inst[inst].no_anchor) return;  // frequency-fallback cycles: k_freq_cycles
+  const u64 cnt = b.tile_cnt[t];
+  const u64 base = b.tile_pref[b.inst_first_tile[inst]];
+  const u64 ib = b.inst_off[inst];
+  const u64 c0 = b.cyc_off[inst], c1 = b.cyc_off[inst + 1];
+  const u64 tb = b.tile_begin[t];
+  for (u64 r = lane; r < cnt; r += 32) {
+    const u64 rank = b.tile_pref[t] + r - base;  // anchor index within the instance
+    const u64 s = tb + r;
+    const i64 a = b.a_start[s];
+    const u64 p = b.a_pos[s];
+    const u64 f = group_start(b.ev, p, ib, a);
+    const u64 g = c0 + rank;
+    if (g < c1) {  // opens cycle `rank`
+      b.c_start[g] = a;
+      b.c_apos[g] = p;
+      b.c_aend[g] = b.a_end[s];
+      b.c_first[g] = f;
+      b.c_inst[g] = inst;
+    }
+    if (rank > 0 && g - 1 < c1) {  // closes cycle rank - 1
+      b.c_end[g - 1] = a;
+      b.c_last[g - 1] = f;
+    }
+  }
+}
+
 // arr[slot] += v over the warp without shared-memory atomics: lanes with the
 // same slot are grouped (__match_any_sync); each group's leader adds the
 // group total with a plain read-modify-write.  slot < 0: no contribution.
@@ -1045,17 +1244,26 @@ __global__ void k_records_count(DevBuffers b, DevConfig cfg) {
   }
 }
 
-// single-CTA exclusive scan of n u64 values in place; total to *total
-__global__ void k_scan_exclusive(uint64_t* v, uint64_t n, uint64_t* total) {
+// single-CTA exclusive scan of n u64 values in place; total to *total.
+// kScanItems consecutive values per thread per round (n ~ 1e5 in a few rounds).
+constexpr int kScanItems = 8;
+__global__ void __launch_bounds__(1024, 1) k_scan_exclusive(uint64_t* v, uint64_t n, uint64_t* total) {
   __shared__ u64 s_part[32];
   __shared__ u64 s_carry;
   if (threadIdx.x == 0) s_carry = 0;
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (u64 base = 0; base < n; base += blockDim.x) {
-    const u64 i = base + threadIdx.x;
-    u64 x = i < n ? v[i] : 0;
-    u64 incl = x;
+  const u64 per_round = (u64)blockDim.x * kScanItems;
+  for (u64 base = 0; base < n; base += per_round) {
+    const u64 i0 = base + (u64)threadIdx.x * kScanItems;
+    u64 x[kScanItems];
+    u64 sum = 0;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+      x[k] = i0 + k < n ? v[i0 + k] : 0;
+      sum += x[k];
+    }
+    u64 incl = sum;
     for (int o = 1; o < 32; o <<= 1) {
       const u64 y = __shfl_up_sync(0xffffffffu, incl, o);
       if (lane >= o) incl += y;
@@ -1071,8 +1279,12 @@ __global__ void k_scan_exclusive(uint64_t* v, uint64_t n, uint64_t* total) {
       s_part[lane] = p;
     }
     __syncthreads();
-    const u64 warp_base = warp ? s_part[warp - 1] : 0;
-    if (i < n) v[i] = s_carry + warp_base + incl - x;
+    u64 run = s_carry + (warp ? s_part[warp - 1] : 0) + incl - sum;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+      if (i0 + k < n) v[i0 + k] = run;
+      run += x[k];
+    }
     __syncthreads();
     if (threadIdx.x == 0) s_carry += s_part[blockDim.x / 32 - 1];
     __syncthreads();
@@ -2183,33 +2395,6 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
-// consumer-group version of cache_flush (no CTA-wide barrier): per-thread
-// caches -> the warp's rows -> global atomics
-__device__ void cache_flush_warp(NameCache& c, NameStat* g, WarpNameRow* wrows) {
-  const int lane = threadIdx.x & 31;
-  if (lane < kWarpNameRows) {
-    wrows[lane].name = 0xffffffffu;
-    wrows[lane].cnt = 0;
-    wrows[lane].sum = wrows[lane].sq_lo = wrows[lane].sq_hi = 0;
-  }
-  __syncwarp();
-#pragma unroll
-  for (int i = 0; i < kNameCache; ++i)
-    rows_merge(wrows, g, c.name[i] != 0xffffffffu && c.cnt[i] > 0, c.name[i], c.cnt[i], c.sum[i],
-               c.lo[i], c.hi[i]);
-  __syncwarp();
-  if (lane < kWarpNameRows) {
-    const WarpNameRow r = wrows[lane];
-    if (r.name != 0xffffffffu && r.cnt) {
-      atomicAdd(&g[r.name].count, (u64)r.cnt);
-      atomicAdd(&g[r.name].sum, r.sum);
-      atomic_add_u128(&g[r.name].sumsq_lo, &g[r.name].sumsq_hi, r.sq_lo, r.sq_hi);
-    }
-  }
-  __syncwarp();
-  cache_clear(c);
-}
-
 struct TileMetaG {
   uint32_t t, inst, n, guess;
   u64 tb, ib;
@@ -2826,21 +3011,118 @@ __global__ void __launch_bounds__(256, 2)
   }
 }
 
-void launch_cycle_reduce_tpc(const DevBuffers& b, const DevConfig& cfg, int do_beta,
-                             cudaStream_t s, uint64_t* launches) {
-  if (!b.n_cycles) return;
-  const bool reg = cfg.cyc.n_beta_slots <= kFRegC && cfg.cyc.n_comm_slots <= kFRegR &&
-                   b.n_names <= (uint32_t)kFNamesSmem;
-  const unsigned grid = (unsigned)((b.n_cycles + 255) / 256);
-  if (reg) {
-    k_cycle_reduce_tpc<true><<<grid, 256, 0, s>>>(b, cfg, do_beta);
-  } else {
-    const int smem = 256 * (int)fused_scratch_words(cfg) * 4;
-    cudaFuncSetAttribute(k_cycle_reduce_tpc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         smem);
-    k_cycle_reduce_tpc<false><<<grid, 256, smem, s>>>(b, cfg, do_beta);
+// ------------------------------------- K3'' thread-per-cycle reduce, v2
+// One thread per cycle walks its events in order (the reference's own loops:
+// cycles.cpp:157-166, 205-229, 256-281; rca.cpp:87-129) with one 256-bit
+// load per 32-B record, kRedUnroll records in flight per thread.  The
+// per-cycle accumulators (component durations, class occupancy, event-ordered
+// collective beta) live in shared memory as [slot][thread] arrays: an update
+// is one load/add/store whose bank depends only on the lane, and the cost per
+// event no longer grows with the number of slots.
+constexpr int kRedUnroll = 4;
+
+__global__ void __launch_bounds__(256, 3) k_cycle_reduce_v2(DevBuffers b, DevConfig cfg, int do_beta) {
+  extern __shared__ __align__(16) unsigned char s_red[];
+  __shared__ uint32_t s_ninfo[kFNamesSmem];
+  const int P = cfg.cyc.n_phases;
+  const int C = do_beta ? cfg.cyc.n_beta_slots : 0;
+  const int R = do_beta ? cfg.cyc.n_comm_slots : 0;
+  const uint32_t NT = blockDim.x, tid = threadIdx.x;
+  auto pack_info = [&](const cs_name_info& ni) -> uint32_t {
+    const uint32_t ph = (ni.phase >= 0 && ni.phase < P) ? (uint32_t)ni.phase : 15u;
+    const uint32_t bs = (ni.beta_slot >= 0 && ni.beta_slot < C) ? (uint32_t)ni.beta_slot : 255u;
+    return ph | (bs << 4) | ((ni.flags & 3u) << 12);
+  };
+  for (uint32_t i = tid; i < b.n_names && i < (uint32_t)kFNamesSmem; i += NT)
+    s_ninfo[i] = pack_info(b.names[i]);
+  __syncthreads();
+  i64* comp = reinterpret_cast<i64*>(s_red);            // [P][NT]
+  i64* beta = comp + (u64)P * NT;                       // [C][NT]
+  double* coll = reinterpret_cast<double*>(beta + (u64)C * NT);  // [R][NT]
+  uint32_t* colln = reinterpret_cast<uint32_t*>(coll + (u64)R * NT);  // [R][NT]
+  const u64 g = (u64)blockIdx.x * NT + tid;
+  const bool live = g < b.n_cycles;
+  uint8_t stage = CS_STAGE_UNKNOWN;
+  if (live) {
+    const i64 cs = b.c_start[g], ce = b.c_end[g];
+    const u64 first = b.c_first[g], last = b.c_last[g];
+    const bool no_comp = b.c_apos[g] == kNone;  // frequency-fallback cycle (cycles.cpp:332-340)
+    const i64 dur = ce - cs;
+    for (int p = 0; p < P; ++p) comp[p * NT + tid] = 0;
+    for (int c = 0; c < C; ++c) beta[c * NT + tid] = 0;
+    for (int r = 0; r < R; ++r) {
+      coll[r * NT + tid] = 0.0;
+      colln[r * NT + tid] = 0u;
+    }
+    uint32_t fm_cls = 0, kw = 0;
+    bool fm_found = false, batch_found = false;
+    int32_t wl = -1;
+    for (u64 j0 = first; j0 < last; j0 += kRedUnroll) {
+      Ev8 e[kRedUnroll];
+#pragma unroll
+      for (int q = 0; q < kRedUnroll; ++q) {
+        if (j0 + q < last) e[q] = ldg256(b.ev + j0 + q);
+        else e[q].c = (u64)CS_FLOW << 32;  // ignored
+      }
+#pragma unroll
+      for (int q = 0; q < kRedUnroll; ++q) {
+        const uint32_t name = (uint32_t)e[q].c;
+        const uint32_t kc = (uint32_t)(e[q].c >> 32);
+        const uint32_t flags = kc >> 16;
+        if (!fm_found && (flags & CS_EV_FM_MASK)) {
+          fm_found = true;
+          fm_cls = flags & CS_EV_FM_MASK;
+        }
+        if (!batch_found && (flags & CS_EV_HAS_BATCH)) {
+          batch_found = true;
+          wl = (flags & CS_EV_WL_OK) ? (int32_t)(uint32_t)e[q].d : -2;
+        }
+        if ((kc & 0xffu) != CS_SPAN) continue;
+        const uint32_t info = name < (uint32_t)kFNamesSmem ? s_ninfo[name] : pack_info(b.names[name]);
+        kw |= (info >> 12) & 3u;
+        const i64 st = (i64)e[q].a, d = (i64)e[q].b;
+        const i64 end = st + d;
+        const i64 clipped = (end < ce ? end : ce) - st;
+        if (clipped <= 0) continue;
+        const uint32_t ph = info & 15u, bs = (info >> 4) & 255u;
+        if (ph != 15u && !no_comp) comp[ph * NT + tid] += clipped;
+        if (do_beta && d > 0) {
+          if (bs != 255u) beta[bs * NT + tid] += clipped;
+          if (((kc >> 8) & 0xffu) == CS_CAT_COLLECTIVE_COMM && (flags & CS_EV_HAS_COMM)) {
+            const uint32_t slot = (uint32_t)(e[q].d >> 32);
+            if (slot < (uint32_t)R) {
+              coll[slot * NT + tid] =
+                  __dadd_rn(coll[slot * NT + tid], __ddiv_rn((double)clipped, (double)dur));
+              colln[slot * NT + tid] += 1u;
+            }
+          }
+        }
+      }
+    }
+    // classify_stages local signals (cycles.cpp:205-229)
+    if (fm_cls == CS_EV_FM_PREFILL) stage = CS_STAGE_PREFILL;
+    else if (fm_cls == CS_EV_FM_DECODE) stage = CS_STAGE_DECODE;
+    const bool pkw = kw & CS_NAME_PREFILL_KW, dkw = kw & CS_NAME_DECODE_KW;
+    if (stage == CS_STAGE_UNKNOWN && pkw != dkw) stage = pkw ? CS_STAGE_PREFILL : CS_STAGE_DECODE;
+    b.c_local[g] = stage;
+    b.c_stage[g] = stage;
+    b.c_wl[g] = wl;
+    for (int p = 0; p < P; ++p) b.c_comp[g * P + p] = comp[p * NT + tid];
+    for (int c = 0; c < C; ++c) {
+      const i64 t = dur > 0 ? beta[c * NT + tid] : 0;
+      b.c_beta_tot[g * C + c] = t;
+      b.c_beta[g * C + c] = t > 0 ? __ddiv_rn((double)t, (double)dur) : 0.0;
+    }
+    for (int r = 0; r < R; ++r) {
+      b.c_coll[g * R + r] = coll[r * NT + tid];
+      const uint32_t n = colln[r * NT + tid];
+      b.c_coll_n[g * R + r] = (uint8_t)(n > 255u ? 255u : n);
+    }
   }
-  ++*launches;
+  const bool unk = live && stage == CS_STAGE_UNKNOWN;
+  const uint32_t inst = unk ? b.c_inst[g] : 0xffffffffu;
+  const uint32_t grp = __match_any_sync(0xffffffffu, inst);
+  if (unk && (tid & 31) == (uint32_t)(__ffs(grp) - 1)) atomicAdd(&b.inst[inst].n_unknown, (u64)__popc(grp));
 }
 
 // ------------------------------------------------------------ launchers
@@ -2848,17 +3130,32 @@ void launch_scan_events(const DevBuffers& b, const DevConfig&, int mode, bool sa
                         const uint32_t* list, uint32_t n_list, cudaStream_t s,
                         uint64_t* launches) {
   if (n_list == 0) return;
-  static bool configured = false;
-  const int smem = kStages * (int)kTileBytes;
-  if (!configured) {
-    cudaFuncSetAttribute(k_scan_events, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    configured = true;
-  }
-  int dev = 0, sms = 148;
+  int dev = 0, sms = 148, per_sm = 1;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const uint32_t grid = n_list < (uint32_t)sms ? n_list : (uint32_t)sms;
-  k_scan_events<<<grid, kScanThreads, smem, s>>>(b, mode, list, n_list, sample ? 1 : 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_scan_warp, kScanWarpThreads, 0);
+  if (per_sm < 1) per_sm = 1;
+  const uint32_t warps = kScanWarpThreads / 32;
+  uint32_t grid = (uint32_t)sms * (uint32_t)per_sm;
+  const uint32_t need = (n_list + warps - 1) / warps;
+  if (need < grid) grid = need;
+  k_scan_warp<<<grid, kScanWarpThreads, 0, s>>>(b, mode, list, n_list, sample ? 1 : 0);
+  ++*launches;
+}
+
+void launch_cycle_reduce_tpc(const DevBuffers& b, const DevConfig& cfg, int do_beta,
+                             cudaStream_t s, uint64_t* launches) {
+  if (!b.n_cycles) return;
+  const int P = cfg.cyc.n_phases;
+  const int C = do_beta ? cfg.cyc.n_beta_slots : 0;
+  const int R = do_beta ? cfg.cyc.n_comm_slots : 0;
+  const int per_thread = (P + C + R) * 8 + R * 4;
+  int nt = 256;
+  while (nt > 32 && nt * per_thread > 100 * 1024) nt >>= 1;
+  const int smem = nt * per_thread;
+  cudaFuncSetAttribute(k_cycle_reduce_v2, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  const unsigned grid = (unsigned)((b.n_cycles + nt - 1) / nt);
+  k_cycle_reduce_v2<<<grid, nt, smem, s>>>(b, cfg, do_beta);
   ++*launches;
 }
 
@@ -2886,7 +3183,8 @@ void launch_fold(const DevBuffers& b, const DevConfig&, const uint32_t* pi, cons
 
 void launch_bounds(const DevBuffers& b, cudaStream_t s, uint64_t* launches) {
   if (!b.n_cycles) return;
-  k_bounds<<<(unsigned)((b.n_cycles + 255) / 256), 256, 0, s>>>(b);
+  if (!b.n_tiles) return;
+  k_bounds_tile<<<(unsigned)((b.n_tiles + 7) / 8), 256, 0, s>>>(b);
   ++*launches;
 }
 

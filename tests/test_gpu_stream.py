@@ -65,6 +65,44 @@ def _cat(parts, dtype):
     return np.concatenate(parts) if parts else np.zeros(0, dtype)
 
 
+def _calibration_anchors(rt, traces, first):
+    """The anchor each instance's first micro-batch (events before `first`)
+    discovers; the stream keeps it for the rest of the trace."""
+    cal = rt.Analyzer(0)
+    evs, wl, offs, _ = _setup(rt, cal, traces)
+    head = [e[e["start_ts"] < first] for e in evs]
+    off = np.zeros(len(head) + 1, np.uint64)
+    off[1:] = np.cumsum([len(h) for h in head])
+    cal.upload(np.concatenate(head), off, wl)
+    cal.run(abi.RUN_SEGMENT)
+    out = [cal.summary(i).anchor_name_id for i in range(len(traces))]
+    cal.close()
+    return out
+
+
+def _whole_trace_reference(rt, traces, anchors):
+    """One whole-trace run per distinct anchor (anchor_hint), models fit on
+    its records; returns (results, models) per instance."""
+    n_inst = len(traces)
+    ref, models = [None] * n_inst, [None] * n_inst
+    for a in sorted(set(anchors)):
+        whole = rt.Analyzer(0)
+        evs, wl, offs, allev = _setup(rt, whole, traces)
+        whole.cycle.anchor_hint_name = a
+        whole.set_config(whole.cycle, whole.control)
+        whole.upload(allev, offs, wl)
+        whole.run(abi.RUN_SEGMENT)
+        fitted = _fit(rt, whole, n_inst)
+        for i, m in enumerate(fitted):
+            whole.load_model(m, i)
+        whole.run(abi.RUN_ALL)
+        for i in range(n_inst):
+            if anchors[i] == a:
+                ref[i], models[i] = whole.result(i), fitted[i]
+        whole.close()
+    return ref, models
+
+
 @pytest.mark.parametrize("n_inst,strip_fm,slice_ms,hint", [(1, False, 37.0, True),
                                                             (3, False, 113.0, False),
                                                             (2, True, 61.0, False),
@@ -72,35 +110,38 @@ def _cat(parts, dtype):
 def test_stream_equals_whole_trace(rt, n_inst, strip_fm, slice_ms, hint):
     """hint=True: the anchor is given (anchor_hint); False: the first
     micro-batch (a calibration window of 20% of the trace) discovers it and
-    the stream keeps it."""
+    the stream keeps it, so the whole-trace reference runs with that anchor
+    (the calibration window may rank candidates differently from the whole
+    trace: memory_thrash does)."""
     traces = _traces(rt, n_inst, strip_fm)
-    whole = rt.Analyzer(0)
-    evs, wl, offs, allev = _setup(rt, whole, traces)
-    whole.upload(allev, offs, wl)
-    whole.run(abi.RUN_SEGMENT)
-    models = _fit(rt, whole, n_inst)
-    for i, m in enumerate(models):
-        whole.load_model(m, i)
-    whole.run(abi.RUN_ALL)
-    ref = [whole.result(i) for i in range(n_inst)]
+    evs = [t.events for t in traces]
+    t_end = max(int(e["start_ts"].max()) for e in evs) + 1
+    t0 = min(int(e["start_ts"].min()) for e in evs)
+    first = t0 + (0 if hint else (t_end - t0) // 5)
+    if hint:
+        whole = rt.Analyzer(0)
+        _, wl, offs, allev = _setup(rt, whole, traces)
+        whole.upload(allev, offs, wl)
+        whole.run(abi.RUN_SEGMENT)
+        anchors = [whole.summary(i).anchor_name_id for i in range(n_inst)]
+        whole.close()
+        assert len(set(anchors)) == 1
+    else:
+        anchors = _calibration_anchors(rt, traces, max(first, t0 + int(slice_ms * 1e6)))
+    ref, models = _whole_trace_reference(rt, traces, anchors)
     assert all(len(r.alerts) >= 1 for r in ref)
 
     an = rt.Analyzer(0)
-    _setup(rt, an, traces)
+    evs, wl, offs, allev = _setup(rt, an, traces)
     if hint:
-        anchors = {r.summary.anchor_name_id for r in ref}
-        assert len(anchors) == 1
-        an.cycle.anchor_hint_name = anchors.pop()
+        an.cycle.anchor_hint_name = anchors[0]
         an.set_config(an.cycle, an.control)
     for i, m in enumerate(models):
         an.load_model(m, i)
     st = an.stream()
-    t_end = max(int(e["start_ts"].max()) for e in evs) + 1
-    t0 = min(int(e["start_ts"].min()) for e in evs)
     step = int(slice_ms * 1e6)
     got = [dict(cyc=[], beta=[], rec=[], al=[]) for _ in range(n_inst)]
     n_batches = 0
-    first = t0 + (0 if hint else (t_end - t0) // 5)
     bounds = [t0] + list(range(max(first, t0 + step), t_end, step)) + [t_end]
     for lo, hi in zip(bounds[:-1], bounds[1:]):
         batch = []
@@ -135,5 +176,4 @@ def test_stream_equals_whole_trace(rt, n_inst, strip_fm, slice_ms, hint):
             assert np.array_equal(al[f], ref[i].alerts[f]), (i, f)
         assert np.array_equal(al["smoothed_error"].view(np.uint64),
                               ref[i].alerts["smoothed_error"].view(np.uint64))
-    whole.close()
     an.close()
