@@ -97,7 +97,7 @@ struct cs_ctx {
   uint64_t slot_cap = 0;
   bool allow_fused = false;  // two-pass path is faster today
   int fused_debug = 0;
-  int reduce_variant = 0;  // 0 thread-per-cycle, 1 warp-per-cycle
+  int reduce_variant = 0;  // profiling hook (single variant today)
   bool used_fused = false;
   DevBuf d_fstate, d_fticket, d_fcnt, d_fpref, d_fixlist, d_fixn, d_fixflags, d_foverflow;
   DevBuf d_cyc_off, c_start, c_end, c_apos, c_aend, c_first, c_last, c_inst, c_stage, c_local,
@@ -932,10 +932,8 @@ int cs_run(cs_ctx* ctx, uint32_t mask) {
                          ctx->inst_off[i + 1], f_t0[i], f_period[i], ctx->fallback_cycles[i],
                          ctx->cyc_off[i], b, i, s, &ctx->launches);
   e4 = record_event(ctx, 4);
-  if (ctx->reduce_variant == 0)
-    launch_cycle_reduce_tpc(b, cfg, (mask & CS_RUN_BETA) ? 1 : 0, s, &ctx->launches);
-  else
-    launch_cycle_reduce(b, cfg, (mask & CS_RUN_BETA) ? 1 : 0, s, &ctx->launches);
+  launch_cycle_reduce_tpc(b, cfg, (mask & CS_RUN_BETA) ? 1 : 0, s, &ctx->launches,
+                          ctx->reduce_variant);
   e5 = record_event(ctx, 5);
   ctx->timed.push_back({"bounds", {e3, e4}});
   ctx->timed.push_back({"cycle_reduce", {e4, e5}});

@@ -173,10 +173,8 @@ void launch_fold(const DevBuffers& b, const DevConfig& cfg, const uint32_t* pair
                  const uint32_t* pairs_name, uint32_t n_pairs, double* out_scores,
                  cudaStream_t s, uint64_t* launches);
 void launch_bounds(const DevBuffers& b, cudaStream_t s, uint64_t* launches);
-void launch_cycle_reduce(const DevBuffers& b, const DevConfig& cfg, int do_beta,
-                         cudaStream_t s, uint64_t* launches);
 void launch_cycle_reduce_tpc(const DevBuffers& b, const DevConfig& cfg, int do_beta,
-                             cudaStream_t s, uint64_t* launches);
+                             cudaStream_t s, uint64_t* launches, int variant);
 void launch_stage_heuristic(const DevBuffers& b, const DevConfig& cfg, cudaStream_t s,
                             uint64_t* launches);
 void launch_records(const DevBuffers& b, const DevConfig& cfg, uint64_t n_blocks_cap,

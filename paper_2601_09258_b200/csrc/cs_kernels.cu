@@ -1,26 +1,28 @@
 // cs_kernels.cu — hand-written sm_100a kernels of the trace-analysis hot path.
 //
 // Data flow (one cs_run over a batch of instances):
-//   K1s  k_scan_events<sample>   name moments over the first 1 Mi events of each
+//   K1s  k_scan_warp<sample>     name moments over the first 1 Mi events of each
 //                                instance -> speculative anchor guess
 //   K1r  k_rank                  exact-moment anchor ranking (cycles.cpp:47-110)
-//   K12  k_scan_events           ONE pass over all events: exact per-name moments
-//                                (cycles.cpp:50-59) + anchor-occurrence
-//                                compaction for the guessed anchor
-//                                (cycles.cpp:127-131) via decoupled look-back
+//   K12  k_scan_warp             ONE pass over all events, warp per tile: exact
+//                                per-name moments (cycles.cpp:50-59) + tile-local
+//                                compaction of the guessed anchor's occurrences
+//                                (cycles.cpp:127-131)
 //   K1r  k_rank(final)           winner; redo flag when the guess was wrong
-//   K2   k_bounds                cycle bounds, lower_bound group starts
-//                                (cycles.cpp:135-156)
-//   K3   k_cycle_reduce          warp per cycle: component durations
+//   K2   k_bounds_tile           cycle bounds scattered from each tile's anchors,
+//                                lower_bound group starts (cycles.cpp:135-156)
+//   K3   k_cycle_reduce_v2       thread per cycle: component durations
 //                                (cycles.cpp:157-166), forward_mode / keyword
 //                                stage signals (205-229), workload carrier
 //                                (256-281), class occupancy beta and per-rank
 //                                collective beta (rca.cpp:71-130)
+//   K123 k_segment_pass          (optional, CS_OPT_FUSED) K1+K2+K3 in one
+//                                warp-specialised pass with decoupled look-back
 //   K4   k_stage_heuristic       trailing-median heuristic for Unknown cycles
 //                                only (cycles.cpp:230-250), warp selection
 //   K5   k_records_*             record compaction (cycles.cpp:366-409)
-//   K6   k_score                 GBDT in shared memory + PPE (gbdt.cpp:22-30,
-//                                173-184; detector.cpp:14-19)
+//   K6   k_score_lut / k_score   GBDT (compiled cell table or traversal) + PPE
+//                                (gbdt.cpp:22-30, 173-184; detector.cpp:14-19)
 //   K7   k_detect_*              control chart, episode ids, alert compaction
 //                                (detector.cpp:91-130)
 // All f64 arithmetic that must match the reference bit for bit is written with
@@ -71,20 +73,6 @@ struct Ev {
 
 // 32-byte record as two 16-byte vector loads; streaming (evict-first) since
 // every event is read exactly once per pass.
-__device__ __forceinline__ Ev load_ev_stream(const cs_event* p) {
-  const int4* q = reinterpret_cast<const int4*>(p);
-  int4 a = __ldcs(q);
-  int4 b = __ldcs(q + 1);
-  Ev e;
-  e.start = (i64)(((u64)(uint32_t)a.y << 32) | (uint32_t)a.x);
-  e.dur = (i64)(((u64)(uint32_t)a.w << 32) | (uint32_t)a.z);
-  e.name = (uint32_t)b.x;
-  e.kind = (uint32_t)b.y & 0xffu;
-  e.cat = ((uint32_t)b.y >> 8) & 0xffu;
-  e.flags = (uint32_t)b.y >> 16;
-  e.payload = ((u64)(uint32_t)b.w << 32) | (uint32_t)b.z;
-  return e;
-}
 __device__ __forceinline__ Ev load_ev(const cs_event* p) {
   const int4* q = reinterpret_cast<const int4*>(p);
   int4 a = __ldg(q);
@@ -164,105 +152,20 @@ __device__ __forceinline__ Ev ev_from_smem(const cs_event* p) {
   return e;
 }
 
-// --------------------------------------------------- K1 / K12 event scan
-// Persistent CTAs stream instance-aligned tiles of 2048 events (64 KiB)
-// through a kStages-deep ring of TMA bulk copies, so ~kStages x 64 KiB per SM
-// are in flight.  Per tile:
-//   mode bit 0: exact per-(instance, name) moments of PythonCall spans
-//               (count, sum d, sum d^2 as u128) in shared memory, flushed to
-//               global atomics when the CTA moves to another instance;
-//   mode bit 1: anchor occurrences (Spans named inst[].guess, or inst[].anchor
-//               with bit 2) compacted tile-locally: a_*[tile_begin + rank] and
-//               tile_cnt[t]; a prefix over tile_cnt (k_scan_exclusive) then
-//               gives every anchor its instance-global rank.
-constexpr int kStages = 6;
+// --------------------------------------------------- K1 / K12 helpers
 constexpr uint32_t kTileBytes = kTileEvents * sizeof(cs_event);
 
-// Per-name moments of PythonCall spans, staged per warp.  64-bit shared
-// atomics are CAS loops on sm_100a, so each warp owns a small table of
-// (name, count, sum d, sum d^2 as u128) rows: lanes holding the same name are
-// grouped with __match_any_sync, the group leader folds the group and does a
-// plain read-modify-write of its row (no other lane of the warp touches that
-// row in the same step).  Rows are claimed with a 32-bit CAS; a full table
-// spills to global atomics.  Flushed to global when the CTA changes instance.
+// Per-warp staging rows for flushing per-thread moment caches.  64-bit shared
+// atomics are CAS loops on sm_100a, so lanes holding the same name are grouped
+// with __match_any_sync and the group leader does a plain read-modify-write
+// of its row.  Rows are claimed with a 32-bit CAS; a full table spills to
+// global atomics.
 constexpr int kWarpNameRows = 16;
 struct WarpNameRow {
   uint32_t name;  // 0xffffffff = free
   uint32_t cnt;
   u64 sum, sq_lo, sq_hi;
 };
-
-__device__ __forceinline__ void rows_zero(WarpNameRow* rows) {
-  for (int i = threadIdx.x; i < (int)(blockDim.x / 32) * kWarpNameRows; i += blockDim.x) {
-    rows[i].name = 0xffffffffu;
-    rows[i].cnt = 0;
-    rows[i].sum = rows[i].sq_lo = rows[i].sq_hi = 0;
-  }
-}
-
-__device__ void rows_flush(NameStat* g, const WarpNameRow* rows) {
-  for (int i = threadIdx.x; i < (int)(blockDim.x / 32) * kWarpNameRows; i += blockDim.x) {
-    const WarpNameRow r = rows[i];
-    if (r.name == 0xffffffffu || !r.cnt) continue;
-    atomicAdd(&g[r.name].count, (u64)r.cnt);
-    atomicAdd(&g[r.name].sum, r.sum);
-    atomic_add_u128(&g[r.name].sumsq_lo, &g[r.name].sumsq_hi, r.sq_lo, r.sq_hi);
-  }
-}
-
-// called by the full warp; `py` lanes contribute (name, d)
-__device__ __forceinline__ void rows_add(WarpNameRow* wrows, NameStat* g, bool py, uint32_t name,
-                                         i64 d) {
-  __syncwarp();  // previous step's row updates are visible to this step's leaders
-  const uint32_t key = py ? name : 0xffffffffu;
-  const uint32_t grp = __match_any_sync(0xffffffffu, key);
-  if (!py) return;
-  const int lane = threadIdx.x & 31;
-  const int leader = __ffs(grp) - 1;
-  u64 lo, hi;
-  square_u128(d, lo, hi);
-  u64 s = (u64)d;
-  uint32_t c = 1;
-  if (grp != (1u << lane)) {  // fold the group (all members run the same loop)
-    uint32_t rest = grp & ~(1u << leader);
-    while (rest) {
-      const int src = __ffs(rest) - 1;
-      rest &= rest - 1;
-      const u64 os = __shfl_sync(grp, s, src);
-      const u64 ol = __shfl_sync(grp, lo, src);
-      const u64 oh = __shfl_sync(grp, hi, src);
-      if (lane == leader) {
-        s += os;
-        const u64 nl = lo + ol;
-        hi += oh + (nl < lo ? 1ull : 0ull);
-        lo = nl;
-        ++c;
-      }
-    }
-  }
-  if (lane != leader) return;
-  int row = -1;
-  for (int i = 0; i < kWarpNameRows; ++i) {
-    const uint32_t n = wrows[i].name;
-    if (n == name) { row = i; break; }
-    if (n == 0xffffffffu) {
-      const uint32_t old = atomicCAS(&wrows[i].name, 0xffffffffu, name);
-      if (old == 0xffffffffu || old == name) { row = i; break; }
-    }
-  }
-  if (row < 0) {
-    atomicAdd(&g[name].count, (u64)c);
-    atomicAdd(&g[name].sum, s);
-    atomic_add_u128(&g[name].sumsq_lo, &g[name].sumsq_hi, lo, hi);
-    return;
-  }
-  WarpNameRow& r = wrows[row];
-  r.cnt += c;
-  r.sum += s;
-  const u64 nl = r.sq_lo + lo;
-  r.sq_hi += hi + (nl < r.sq_lo ? 1ull : 0ull);
-  r.sq_lo = nl;
-}
 
 // Per-thread cache of PythonCall moments (typical traces have a handful of
 // PythonCall names): no warp synchronisation on the hot loop; a miss falls
@@ -564,139 +467,6 @@ __global__ void __launch_bounds__(kScanWarpThreads, 3)
 }
 
 
-struct ScanMeta {
-  uint32_t t, inst, n, anchor, active;
-  u64 tb;
-};
-
-__global__ void __launch_bounds__(kScanThreads, 1)
-    k_scan_events(DevBuffers b, int mode, const uint32_t* __restrict__ list, uint32_t n_list,
-                  int sample) {
-  extern __shared__ __align__(128) unsigned char s_tiles[];
-  __shared__ uint64_t s_bar[kStages];
-  __shared__ ScanMeta s_meta[kStages];
-  __shared__ uint32_t s_warp_cnt[kScanThreads / 32];
-  __shared__ WarpNameRow s_rows[(kScanThreads / 32) * kWarpNameRows];
-
-  const bool do_stats = mode & 1;
-  const bool do_anchor = (mode & 2) && !sample;
-  const bool redo = mode & 4;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const uint32_t G = gridDim.x;
-  constexpr int kWarps = kScanThreads / 32;
-  constexpr int kIt = kTileEvents / kScanThreads;
-
-  auto issue = [&](int s, uint32_t k) {  // thread 0
-    ScanMeta m{};
-    m.t = k < n_list ? (list ? list[k] : k) : 0xffffffffu;
-    if (k < n_list) {
-      m.inst = b.tile_inst[m.t];
-      m.tb = b.tile_begin[m.t];
-      u64 te = b.tile_end[m.t];
-      if (sample) {
-        const u64 lim = b.inst_off[m.inst] + kSampleEvents;
-        te = te < lim ? te : lim;
-        if (te < m.tb) te = m.tb;
-      }
-      m.n = (uint32_t)(te - m.tb);
-      m.active = do_anchor;
-      m.anchor = 0xffffffffu;
-      if (do_anchor) {
-        const InstState& st = b.inst[m.inst];
-        m.anchor = redo ? st.anchor : st.guess;
-        if (redo && !st.redo) m.active = 0;
-      }
-      const uint32_t bytes = m.n * (uint32_t)sizeof(cs_event);
-      mbar_expect_tx(&s_bar[s], bytes);
-      if (bytes) bulk_g2s(s_tiles + s * kTileBytes, b.ev + m.tb, bytes, &s_bar[s]);
-    }
-    s_meta[s] = m;
-  };
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages; ++s) mbar_init(&s_bar[s], 1);
-    mbar_fence_init();
-  }
-  __syncthreads();
-  if (threadIdx.x == 0)
-    for (int s = 0; s < kStages; ++s) issue(s, blockIdx.x + s * G);
-  __syncthreads();
-  NameCache cache;
-  cache_clear(cache);
-  uint32_t cur_inst = 0xffffffffu;
-  uint32_t it = 0;
-  for (uint32_t k = blockIdx.x; k < n_list; k += G, ++it) {
-    const int stage = it % kStages;
-    const uint32_t parity = (it / kStages) & 1u;
-    const ScanMeta m = s_meta[stage];
-    if (do_stats && m.inst != cur_inst) {
-      if (cur_inst != 0xffffffffu) cache_flush(cache, b.stats + (u64)cur_inst * b.n_names, s_rows);
-      cur_inst = m.inst;
-    }
-    NameStat* gstats = b.stats + (u64)m.inst * b.n_names;
-    mbar_wait(&s_bar[stage], parity);
-    const cs_event* tile = reinterpret_cast<const cs_event*>(s_tiles + stage * kTileBytes);
-    uint32_t masks[kIt];
-    uint32_t my = 0;
-#pragma unroll
-    for (int j = 0; j < kIt; ++j) {
-      const uint32_t e_idx = (uint32_t)warp * (kIt * 32) + j * 32 + lane;
-      bool is_anchor = false;
-      if (e_idx < m.n) {
-        const int4 h1 = reinterpret_cast<const int4*>(tile + e_idx)[1];
-        const uint32_t name = (uint32_t)h1.x;
-        const uint32_t kind = (uint32_t)h1.y & 0xffu;
-        const uint32_t cat = ((uint32_t)h1.y >> 8) & 0xffu;
-        if (kind == CS_SPAN) {
-          if (do_stats && cat == CS_CAT_PYTHON_CALL) {
-            const int4 h0 = reinterpret_cast<const int4*>(tile + e_idx)[0];
-            cache_add(cache, gstats, name, (i64)(((u64)(uint32_t)h0.w << 32) | (uint32_t)h0.z));
-          }
-          is_anchor = m.active && name == m.anchor;
-        }
-      }
-      masks[j] = __ballot_sync(0xffffffffu, is_anchor);
-      my += __popc(masks[j]);
-    }
-    if (do_anchor) {
-      if (lane == 0) s_warp_cnt[warp] = my;
-      __syncthreads();
-      uint32_t base = 0, total = 0;
-#pragma unroll
-      for (int w = 0; w < kWarps; ++w) {
-        const uint32_t c = s_warp_cnt[w];
-        base += w < warp ? c : 0;
-        total += c;
-      }
-      if (m.active) {
-#pragma unroll
-        for (int j = 0; j < kIt; ++j) {
-          const uint32_t mk = masks[j];
-          if (mk & (1u << lane)) {
-            const uint32_t e_idx = (uint32_t)warp * (kIt * 32) + j * 32 + lane;
-            const u64 r = m.tb + base + __popc(mk & lanemask_lt());
-            const cs_event* p = tile + e_idx;
-            b.a_pos[r] = m.tb + e_idx;
-            b.a_start[r] = p->start_ts;
-            b.a_end[r] = p->start_ts + p->duration;
-          }
-          base += __popc(mk);
-        }
-        if (threadIdx.x == 0) b.tile_cnt[m.t] = total;
-      }
-    }
-    __syncthreads();  // every thread is done with this stage
-    if (threadIdx.x == 0) {
-      fence_proxy_async();
-      issue(stage, k + kStages * G);
-    }
-  }
-  // every thread reaches the flush (uniform control flow across the CTA)
-  if (do_stats && __syncthreads_or(cur_inst != 0xffffffffu)) {
-    if (cur_inst == 0xffffffffu) cache_clear(cache);
-    cache_flush(cache, b.stats + (u64)(cur_inst == 0xffffffffu ? 0 : cur_inst) * b.n_names, s_rows);
-  }
-}
-
 // per-instance anchor counts from the tile prefix
 __global__ void k_inst_anchor_counts(DevBuffers b) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -902,25 +672,6 @@ __device__ __forceinline__ u64 anchor_slot(const DevBuffers& b, uint32_t inst, u
   return b.tile_begin[lo] + (g - b.tile_pref[lo]);
 }
 
-__global__ void k_bounds(DevBuffers b) {
-  const u64 g = (u64)blockIdx.x * blockDim.x + threadIdx.x;
-  if (g >= b.n_cycles) return;
-  const uint32_t inst = upper_bound_u64(b.cyc_off, b.n_inst + 1, g) - 1;
-  if (b.inst[inst].no_anchor) return;  // frequency-fallback cycles: k_freq_cycles
-  const u64 c = g - b.cyc_off[inst];
-  const u64 ib = b.inst_off[inst];
-  const u64 s0 = anchor_slot(b, inst, c), s1 = anchor_slot(b, inst, c + 1);
-  const i64 s = b.a_start[s0], e = b.a_start[s1];
-  const u64 p0 = b.a_pos[s0], p1 = b.a_pos[s1];
-  b.c_start[g] = s;
-  b.c_end[g] = e;
-  b.c_apos[g] = p0;
-  b.c_aend[g] = b.a_end[s0];
-  b.c_first[g] = group_start(b.ev, p0, ib, s);
-  b.c_last[g] = group_start(b.ev, p1, ib, e);
-  b.c_inst[g] = inst;
-}
-
 // Cycle bounds by scatter from each tile's anchor list (warp per tile): the
 // anchor of global rank r opens cycle r - base(inst) and closes the previous
 // one; first/last events by lower_bound over equal start_ts
@@ -954,158 +705,6 @@ __global__ void __launch_bounds__(256) k_bounds_tile(DevBuffers b) {
       b.c_end[g - 1] = a;
       b.c_last[g - 1] = f;
     }
-  }
-}
-
-// arr[slot] += v over the warp without shared-memory atomics: lanes with the
-// same slot are grouped (__match_any_sync); each group's leader adds the
-// group total with a plain read-modify-write.  slot < 0: no contribution.
-__device__ __forceinline__ void warp_group_add(i64* arr, int slot, i64 v) {
-  const uint32_t grp = __match_any_sync(0xffffffffu, slot);
-  if (slot < 0) return;
-  const int lane = threadIdx.x & 31;
-  const int leader = __ffs(grp) - 1;
-  i64 acc = v;
-  uint32_t rest = grp & ~(1u << leader);
-  while (rest) {
-    const int src = __ffs(rest) - 1;
-    rest &= rest - 1;
-    const i64 o = __shfl_sync(grp, v, src);
-    if (lane == leader) acc += o;
-  }
-  if (lane == leader) arr[slot] += acc;
-}
-
-// ------------------------------------------------------ K3 cycle reduce
-constexpr int kReduceWarps = 8;
-struct WarpScratch {
-  i64 comp[kMaxPhases];
-  i64 beta[kMaxBetaSlots];
-  double coll[kMaxCommSlots];
-  uint32_t colln[kMaxCommSlots];
-};
-
-__global__ void __launch_bounds__(kReduceWarps * 32)
-    k_cycle_reduce(DevBuffers b, DevConfig cfg, int do_beta) {
-  __shared__ WarpScratch s_ws[kReduceWarps];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  WarpScratch& ws = s_ws[warp];
-  const int P = cfg.cyc.n_phases, C = cfg.cyc.n_beta_slots, R = cfg.cyc.n_comm_slots;
-  const int lat = cfg.cyc.latency_phase;
-  const u64 n_warps = (u64)gridDim.x * kReduceWarps;
-
-  for (u64 g = (u64)blockIdx.x * kReduceWarps + warp; g < b.n_cycles; g += n_warps) {
-    const i64 cs = b.c_start[g], ce = b.c_end[g];
-    const u64 first = b.c_first[g], last = b.c_last[g];
-    const i64 dur = ce - cs;
-    // frequency-fallback cycles carry no component map (cycles.cpp:332-340)
-    const bool no_comp = b.c_apos[g] == kNone;
-    for (int i = lane; i < kMaxPhases; i += 32) ws.comp[i] = 0;
-    if (do_beta) {
-      for (int i = lane; i < C; i += 32) ws.beta[i] = 0;
-      for (int i = lane; i < R; i += 32) {
-        ws.coll[i] = 0.0;
-        ws.colln[i] = 0;
-      }
-    }
-    __syncwarp();
-    uint32_t fm_cls = 0;
-    bool fm_found = false, pkw = false, dkw = false, batch_found = false;
-    int32_t wl = -1;
-    for (u64 base = first; base < last; base += 32) {
-      const u64 j = base + lane;
-      const bool valid = j < last;
-      Ev e{};
-      cs_name_info ni{0, -1, -1, 0};
-      if (valid) {
-        e = load_ev_stream(b.ev + j);
-        ni = b.names[e.name];
-      }
-      const bool span = valid && e.kind == CS_SPAN;
-      const i64 clipped = (e.start + e.dur < ce ? e.start + e.dur : ce) - e.start;
-      warp_group_add(ws.comp, (span && !no_comp && ni.phase >= 0 && clipped > 0) ? ni.phase : -1,
-                     clipped);
-      if (do_beta) {
-        const bool occ = span && e.dur > 0 && clipped > 0;
-        warp_group_add(ws.beta, (occ && ni.beta_slot >= 0) ? ni.beta_slot : -1, clipped);
-        // per-(name, commHash, rank) beta: doubles summed in event order
-        // (rca.cpp:108-115).  Terms are divided in parallel; if every slot has
-        // one contributor in this chunk the adds are independent, otherwise
-        // lane 0 folds the chunk in lane (= event) order.
-        const bool coll = occ && e.cat == CS_CAT_COLLECTIVE_COMM && (e.flags & CS_EV_HAS_COMM);
-        const uint32_t m = __ballot_sync(0xffffffffu, coll);
-        if (m) {
-          const uint32_t slot = coll ? (uint32_t)(e.payload >> 32) : 0xffffffffu;
-          const double term = coll ? __ddiv_rn((double)clipped, (double)dur) : 0.0;
-          const uint32_t same = __match_any_sync(0xffffffffu, slot);
-          const bool unique = !coll || __popc(same & m) == 1;
-          if (__all_sync(0xffffffffu, unique)) {
-            if (coll && slot < (uint32_t)R) {
-              ws.coll[slot] = __dadd_rn(ws.coll[slot], term);
-              ws.colln[slot] += 1;
-            }
-          } else {
-            uint32_t mm = m;
-            while (mm) {
-              const int l = __ffs(mm) - 1;
-              mm &= mm - 1;
-              const uint32_t sl = __shfl_sync(0xffffffffu, slot, l);
-              const double tv = __shfl_sync(0xffffffffu, term, l);
-              if (lane == 0 && sl < (uint32_t)R) {
-                ws.coll[sl] = __dadd_rn(ws.coll[sl], tv);
-                ws.colln[sl] += 1;
-              }
-            }
-          }
-          __syncwarp();
-        }
-      }
-      if (!fm_found) {
-        const uint32_t m = __ballot_sync(0xffffffffu, valid && (e.flags & CS_EV_FM_MASK));
-        if (m) {
-          fm_found = true;
-          fm_cls = __shfl_sync(0xffffffffu, e.flags & CS_EV_FM_MASK, __ffs(m) - 1);
-        }
-      }
-      pkw |= __any_sync(0xffffffffu, span && (ni.flags & CS_NAME_PREFILL_KW));
-      dkw |= __any_sync(0xffffffffu, span && (ni.flags & CS_NAME_DECODE_KW));
-      if (!batch_found) {
-        const uint32_t m = __ballot_sync(0xffffffffu, valid && (e.flags & CS_EV_HAS_BATCH));
-        if (m) {
-          batch_found = true;
-          const int l = __ffs(m) - 1;
-          const uint32_t ok = __shfl_sync(0xffffffffu, e.flags & CS_EV_WL_OK, l);
-          const uint32_t idx = __shfl_sync(0xffffffffu, (uint32_t)(e.payload & 0xffffffffu), l);
-          wl = ok ? (int32_t)idx : -2;
-        }
-      }
-    }
-    __syncwarp();
-    // classify_stages local signals (cycles.cpp:205-229)
-    uint8_t stage = CS_STAGE_UNKNOWN;
-    if (fm_cls == CS_EV_FM_PREFILL) stage = CS_STAGE_PREFILL;
-    else if (fm_cls == CS_EV_FM_DECODE) stage = CS_STAGE_DECODE;
-    if (stage == CS_STAGE_UNKNOWN && pkw != dkw) stage = pkw ? CS_STAGE_PREFILL : CS_STAGE_DECODE;
-    if (lane == 0) {
-      b.c_local[g] = stage;
-      b.c_stage[g] = stage;
-      b.c_wl[g] = wl;
-      if (stage == CS_STAGE_UNKNOWN) atomicAdd(&b.inst[b.c_inst[g]].n_unknown, 1ull);
-    }
-    if (lane < P) b.c_comp[g * P + lane] = ws.comp[lane];
-    (void)lat;
-    if (do_beta) {
-      for (int i = lane; i < C; i += 32) {
-        const i64 t = dur > 0 ? ws.beta[i] : 0;
-        b.c_beta_tot[g * C + i] = t;
-        b.c_beta[g * C + i] = t > 0 ? __ddiv_rn((double)t, (double)dur) : 0.0;
-      }
-      for (int i = lane; i < R; i += 32) {
-        b.c_coll[g * R + i] = ws.coll[i];
-        b.c_coll_n[g * R + i] = (uint8_t)(ws.colln[i] > 255 ? 255 : ws.colln[i]);
-      }
-    }
-    __syncwarp();
   }
 }
 
@@ -2124,139 +1723,6 @@ __device__ __forceinline__ CycAcc accumulate_cycle(const cs_name_info* __restric
   return a;
 }
 
-// Register-resident variant for the common narrow configurations
-// (<= KC classes, <= KR collective slots): every update is a predicated
-// select-add, no memory round trip, so consecutive events pipeline.
-template <int KC, int KR>
-struct CycAccR {
-  i64 comp[kMaxPhases];
-  i64 beta[KC];
-  double coll[KR];
-  uint32_t colln[KR];
-  int32_t wl;
-  uint8_t stage;
-};
-
-template <int KC, int KR>
-__device__ __forceinline__ void accumulate_cycle_reg(const cs_name_info* __restrict__ names,
-                                                     int do_beta, const cs_event* __restrict__ ev,
-                                                     uint32_t first, uint32_t last, i64 cs,
-                                                     i64 ce, CycAccR<KC, KR>& a) {
-  const i64 dur = ce - cs;
-#pragma unroll
-  for (int i = 0; i < kMaxPhases; ++i) a.comp[i] = 0;
-#pragma unroll
-  for (int i = 0; i < KC; ++i) a.beta[i] = 0;
-#pragma unroll
-  for (int i = 0; i < KR; ++i) {
-    a.coll[i] = 0.0;
-    a.colln[i] = 0;
-  }
-  uint32_t fm_cls = 0;
-  bool fm_found = false, pkw = false, dkw = false, batch_found = false;
-  a.wl = -1;
-  constexpr int kB = 4;  // events loaded ahead per step (memory-level parallelism)
-  for (uint32_t j0 = first; j0 < last; j0 += kB) {
-    int4 H0[kB], H1[kB];
-#pragma unroll
-    for (int q = 0; q < kB; ++q) {
-      if (j0 + q < last) {
-        const int4* p = reinterpret_cast<const int4*>(ev + j0 + q);
-        H0[q] = p[0];
-        H1[q] = p[1];
-      } else {
-        H1[q] = make_int4(0, 0x00000003, 0, 0);  // kind = Flow, no flags: ignored
-        H0[q] = make_int4(0, 0, 0, 0);
-      }
-    }
-#pragma unroll
-    for (int q = 0; q < kB; ++q) {
-      const int4 h0 = H0[q], h1 = H1[q];
-      const i64 st = (i64)(((u64)(uint32_t)h0.y << 32) | (uint32_t)h0.x);
-      const i64 d = (i64)(((u64)(uint32_t)h0.w << 32) | (uint32_t)h0.z);
-      const uint32_t name = (uint32_t)h1.x;
-      const uint32_t kind = (uint32_t)h1.y & 0xffu;
-      const uint32_t cat = ((uint32_t)h1.y >> 8) & 0xffu;
-      const uint32_t flags = (uint32_t)h1.y >> 16;
-      if (!fm_found && (flags & CS_EV_FM_MASK)) {
-        fm_found = true;
-        fm_cls = flags & CS_EV_FM_MASK;
-      }
-      if (!batch_found && (flags & CS_EV_HAS_BATCH)) {
-        batch_found = true;
-        a.wl = (flags & CS_EV_WL_OK) ? (int32_t)(uint32_t)h1.z : -2;
-      }
-      if (kind != CS_SPAN) continue;
-      const cs_name_info ni = names[name];
-      pkw |= (ni.flags & CS_NAME_PREFILL_KW) != 0;
-      dkw |= (ni.flags & CS_NAME_DECODE_KW) != 0;
-      const i64 end = st + d;
-      const i64 clipped = (end < ce ? end : ce) - st;
-      if (clipped <= 0) continue;
-#pragma unroll
-      for (int p = 0; p < kMaxPhases; ++p) a.comp[p] += ni.phase == p ? clipped : 0;
-      if (do_beta && d > 0) {
-#pragma unroll
-        for (int c = 0; c < KC; ++c) a.beta[c] += ni.beta_slot == c ? clipped : 0;
-        if (cat == CS_CAT_COLLECTIVE_COMM && (flags & CS_EV_HAS_COMM)) {
-          const uint32_t slot = (uint32_t)h1.w;
-          const double term = __ddiv_rn((double)clipped, (double)dur);
-#pragma unroll
-          for (int r = 0; r < KR; ++r)
-            if (slot == (uint32_t)r) {
-              a.coll[r] = __dadd_rn(a.coll[r], term);
-              a.colln[r] += 1;
-            }
-        }
-      }
-    }
-  }
-  a.stage = CS_STAGE_UNKNOWN;
-  if (fm_cls == CS_EV_FM_PREFILL) a.stage = CS_STAGE_PREFILL;
-  else if (fm_cls == CS_EV_FM_DECODE) a.stage = CS_STAGE_DECODE;
-  if (a.stage == CS_STAGE_UNKNOWN && pkw != dkw) a.stage = pkw ? CS_STAGE_PREFILL : CS_STAGE_DECODE;
-}
-
-template <int KC, int KR>
-__device__ __forceinline__ void write_cycle_reg(const DevBuffers& b, const DevConfig& cfg,
-                                                int do_beta, const CycAccR<KC, KR>& a, u64 g,
-                                                uint32_t inst, i64 cs, i64 ce, u64 apos, i64 aend,
-                                                u64 gfirst, u64 glast) {
-  const int P = cfg.cyc.n_phases, C = cfg.cyc.n_beta_slots, R = cfg.cyc.n_comm_slots;
-  const i64 dur = ce - cs;
-  b.c_start[g] = cs;
-  b.c_end[g] = ce;
-  b.c_apos[g] = apos;
-  b.c_aend[g] = aend;
-  b.c_first[g] = gfirst;
-  b.c_last[g] = glast;
-  b.c_inst[g] = inst;
-  b.c_local[g] = a.stage;
-  b.c_stage[g] = a.stage;
-  b.c_wl[g] = a.wl;
-  if (a.stage == CS_STAGE_UNKNOWN) atomicAdd(&b.inst[inst].n_unknown, 1ull);
-#pragma unroll
-  for (int i = 0; i < kMaxPhases; ++i)
-    if (i < P) b.c_comp[g * P + i] = a.comp[i];
-  if (do_beta) {
-#pragma unroll
-    for (int i = 0; i < KC; ++i) {
-      if (i < C) {
-        const i64 t = dur > 0 ? a.beta[i] : 0;
-        b.c_beta_tot[g * C + i] = t;
-        b.c_beta[g * C + i] = t > 0 ? __ddiv_rn((double)t, (double)dur) : 0.0;
-      }
-    }
-#pragma unroll
-    for (int i = 0; i < KR; ++i) {
-      if (i < R) {
-        b.c_coll[g * R + i] = a.coll[i];
-        b.c_coll_n[g * R + i] = (uint8_t)(a.colln[i] > 255 ? 255 : a.colln[i]);
-      }
-    }
-  }
-}
-
 __device__ __forceinline__ void write_cycle(const DevBuffers& b, const DevConfig& cfg, int do_beta,
                                             const CycAcc& a, u64 g, uint32_t inst, i64 cs, i64 ce,
                                             u64 apos, i64 aend, u64 gfirst, u64 glast,
@@ -2305,20 +1771,9 @@ struct FusedMeta {
   unsigned int* overflow;
 };
 
-__device__ __forceinline__ uint32_t scratch_words(const DevConfig& cfg) {
-  const uint32_t w = (uint32_t)(cfg.cyc.n_beta_slots + cfg.cyc.n_comm_slots) * 2 +
-                     (uint32_t)cfg.cyc.n_comm_slots + 1;
-  return (w + 1) & ~1u;
-}
-
 constexpr int kFNamesSmem = 256;
 constexpr int kFRegC = 16;  // register path: <= 16 span classes
 constexpr int kFRegR = 8;   //                <= 8 collective slots
-
-struct TileMeta {
-  uint32_t t, inst, n, guess;
-  u64 tb, ib;
-};
 
 // Event-parallel single pass (K1+K2+K3 in one read of the events), warp
 // specialised.  A producer warp owns the tile ring: it claims tiles in order
@@ -2971,46 +2426,6 @@ void launch_fixup_cycles(const DevBuffers& b, const DevConfig& cfg, const FusedM
   ++*launches;
 }
 
-// ------------------------------------------ K3' thread-per-cycle reduce
-// One thread per cycle, sequential over its events straight from global
-// memory (each thread's range is contiguous; neighbours' ranges are adjacent,
-// so sectors are consumed from L1 across the warp).  Thousands of cycles in
-// flight per SM hide the latency; no warp-level reductions or atomics.
-template <bool kReg>
-__global__ void __launch_bounds__(256, 2)
-    k_cycle_reduce_tpc(DevBuffers b, DevConfig cfg, int do_beta) {
-  extern __shared__ __align__(16) uint32_t s_scr[];
-  __shared__ cs_name_info s_names[kFNamesSmem];
-  for (uint32_t i = threadIdx.x; i < b.n_names && i < (uint32_t)kFNamesSmem; i += blockDim.x)
-    s_names[i] = b.names[i];
-  __syncthreads();
-  const u64 g = (u64)blockIdx.x * blockDim.x + threadIdx.x;
-  if (g >= b.n_cycles) return;
-  const i64 cs = b.c_start[g], ce = b.c_end[g];
-  const u64 first = b.c_first[g], last = b.c_last[g];
-  const u64 apos = b.c_apos[g];
-  const uint32_t inst = b.c_inst[g];
-  if constexpr (kReg) {
-    CycAccR<kFRegC, kFRegR> acc;
-    accumulate_cycle_reg<kFRegC, kFRegR>(s_names, do_beta, b.ev + first, 0,
-                                         (uint32_t)(last - first), cs, ce, acc);
-    if (apos == kNone)  // frequency-fallback cycles carry no component map
-      for (int i = 0; i < kMaxPhases; ++i) acc.comp[i] = 0;
-    write_cycle_reg<kFRegC, kFRegR>(b, cfg, do_beta, acc, g, inst, cs, ce, apos, b.c_aend[g],
-                                    first, last);
-  } else {
-    const uint32_t sw = scratch_words(cfg);
-    i64* beta = reinterpret_cast<i64*>(s_scr + (u64)threadIdx.x * sw);
-    double* coll = reinterpret_cast<double*>(beta + cfg.cyc.n_beta_slots);
-    uint32_t* colln = reinterpret_cast<uint32_t*>(coll + cfg.cyc.n_comm_slots);
-    const cs_name_info* names = b.n_names <= (uint32_t)kFNamesSmem ? s_names : b.names;
-    const CycAcc acc = accumulate_cycle(names, cfg, do_beta, b.ev, first, last, cs, ce,
-                                        apos == kNone, beta, coll, colln);
-    write_cycle(b, cfg, do_beta, acc, g, inst, cs, ce, apos, b.c_aend[g], first, last, beta, coll,
-                colln);
-  }
-}
-
 // ------------------------------------- K3'' thread-per-cycle reduce, v2
 // One thread per cycle walks its events in order (the reference's own loops:
 // cycles.cpp:157-166, 205-229, 256-281; rca.cpp:87-129) with one 256-bit
@@ -3019,8 +2434,10 @@ __global__ void __launch_bounds__(256, 2)
 // collective beta) live in shared memory as [slot][thread] arrays: an update
 // is one load/add/store whose bank depends only on the lane, and the cost per
 // event no longer grows with the number of slots.
+// Measured on B200 (configs[1]): an L2 bulk prefetch of the cycle's range,
+// 8 records in flight (spills) and a warp-cooperative coalesced variant (2x
+// the instructions: consecutive records of mixed kinds diverge) were all slower.
 constexpr int kRedUnroll = 4;
-
 __global__ void __launch_bounds__(256, 3) k_cycle_reduce_v2(DevBuffers b, DevConfig cfg, int do_beta) {
   extern __shared__ __align__(16) unsigned char s_red[];
   __shared__ uint32_t s_ninfo[kFNamesSmem];
@@ -3144,7 +2561,7 @@ void launch_scan_events(const DevBuffers& b, const DevConfig&, int mode, bool sa
 }
 
 void launch_cycle_reduce_tpc(const DevBuffers& b, const DevConfig& cfg, int do_beta,
-                             cudaStream_t s, uint64_t* launches) {
+                             cudaStream_t s, uint64_t* launches, int variant) {
   if (!b.n_cycles) return;
   const int P = cfg.cyc.n_phases;
   const int C = do_beta ? cfg.cyc.n_beta_slots : 0;
@@ -3153,6 +2570,7 @@ void launch_cycle_reduce_tpc(const DevBuffers& b, const DevConfig& cfg, int do_b
   int nt = 256;
   while (nt > 32 && nt * per_thread > 100 * 1024) nt >>= 1;
   const int smem = nt * per_thread;
+  (void)variant;
   cudaFuncSetAttribute(k_cycle_reduce_v2, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   const unsigned grid = (unsigned)((b.n_cycles + nt - 1) / nt);
   k_cycle_reduce_v2<<<grid, nt, smem, s>>>(b, cfg, do_beta);
@@ -3185,19 +2603,6 @@ void launch_bounds(const DevBuffers& b, cudaStream_t s, uint64_t* launches) {
   if (!b.n_cycles) return;
   if (!b.n_tiles) return;
   k_bounds_tile<<<(unsigned)((b.n_tiles + 7) / 8), 256, 0, s>>>(b);
-  ++*launches;
-}
-
-void launch_cycle_reduce(const DevBuffers& b, const DevConfig& cfg, int do_beta, cudaStream_t s,
-                         uint64_t* launches) {
-  if (!b.n_cycles) return;
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  u64 blocks = (b.n_cycles + kReduceWarps - 1) / kReduceWarps;
-  const u64 cap = (u64)sms * 8;
-  if (blocks > cap) blocks = cap;
-  k_cycle_reduce<<<(unsigned)blocks, kReduceWarps * 32, 0, s>>>(b, cfg, do_beta);
   ++*launches;
 }
 
