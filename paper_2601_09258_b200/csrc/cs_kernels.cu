@@ -341,6 +341,7 @@ __device__ void cache_flush_warp(NameCache& c, NameStat* g, WarpNameRow* wrows) 
 // cycles.cpp:127-131) warp-locally to a_*[tile_begin + rank] with the
 // tile's count in tile_cnt[t].  No shared-memory staging, no CTA barriers.
 constexpr int kScanWarpThreads = 256;
+constexpr u64 kWalk = 1ull << 63;  // a_pos flag: the group start needs a walk back
 constexpr int kScanUnroll = 4;
 
 struct Ev8 {
@@ -449,9 +450,15 @@ __global__ void __launch_bounds__(kScanWarpThreads, 3)
         }
         const bool is_anchor = active && span && name == anchor;
         const uint32_t mk = __ballot_sync(0xffffffffu, is_anchor);
+        // group start (lower_bound over equal start_ts, cycles.cpp:137-144):
+        // the anchor opens its group unless the previous record shares its
+        // start; kWalk marks the rare anchors k_bounds_tile must walk back for
+        const u64 prev = __shfl_up_sync(0xffffffffu, e[q].a, 1);
         if (is_anchor) {
           const u64 r = tb + cnt + __popc(mk & lanemask_lt());
-          b.a_pos[r] = tb + j0 + q * 32 + lane;
+          const uint32_t jj = j0 + q * 32 + lane;
+          const bool walk = jj == 0 ? tb > b.inst_off[inst] : (lane == 0 || prev == e[q].a);
+          b.a_pos[r] = (tb + jj) | (walk ? kWalk : 0ull);
           b.a_start[r] = (i64)e[q].a;
           b.a_end[r] = (i64)e[q].a + (i64)e[q].b;
         }
@@ -691,8 +698,9 @@ __global__ void __launch_bounds__(256) k_bounds_tile(DevBuffers b) {
     const u64 rank = b.tile_pref[t] + r - base;  // anchor index within the instance
     const u64 s = tb + r;
     const i64 a = b.a_start[s];
-    const u64 p = b.a_pos[s];
-    const u64 f = group_start(b.ev, p, ib, a);
+    const u64 pw = b.a_pos[s];
+    const u64 p = pw & ~kWalk;
+    const u64 f = (pw & kWalk) ? group_start(b.ev, p, ib, a) : p;
     const u64 g = c0 + rank;
     if (g < c1) {  // opens cycle `rank`
       b.c_start[g] = a;
@@ -843,52 +851,40 @@ __global__ void k_records_count(DevBuffers b, DevConfig cfg) {
   }
 }
 
-// single-CTA exclusive scan of n u64 values in place; total to *total.
-// kScanItems consecutive values per thread per round (n ~ 1e5 in a few rounds).
-constexpr int kScanItems = 8;
+// single-CTA exclusive scan of n u64 values in place; total to *total.  One
+// round: thread t owns the contiguous chunk [t*c, (t+1)*c), c = ceil(n/threads)
+// (independent loads, no per-round barriers).
 __global__ void __launch_bounds__(1024, 1) k_scan_exclusive(uint64_t* v, uint64_t n, uint64_t* total) {
   __shared__ u64 s_part[32];
-  __shared__ u64 s_carry;
-  if (threadIdx.x == 0) s_carry = 0;
-  __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const u64 per_round = (u64)blockDim.x * kScanItems;
-  for (u64 base = 0; base < n; base += per_round) {
-    const u64 i0 = base + (u64)threadIdx.x * kScanItems;
-    u64 x[kScanItems];
-    u64 sum = 0;
-#pragma unroll
-    for (int k = 0; k < kScanItems; ++k) {
-      x[k] = i0 + k < n ? v[i0 + k] : 0;
-      sum += x[k];
-    }
-    u64 incl = sum;
-    for (int o = 1; o < 32; o <<= 1) {
-      const u64 y = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += y;
-    }
-    if (lane == 31) s_part[warp] = incl;
-    __syncthreads();
-    if (warp == 0) {
-      u64 p = lane < (int)(blockDim.x / 32) ? s_part[lane] : 0;
-      for (int o = 1; o < 32; o <<= 1) {
-        const u64 y = __shfl_up_sync(0xffffffffu, p, o);
-        if (lane >= o) p += y;
-      }
-      s_part[lane] = p;
-    }
-    __syncthreads();
-    u64 run = s_carry + (warp ? s_part[warp - 1] : 0) + incl - sum;
-#pragma unroll
-    for (int k = 0; k < kScanItems; ++k) {
-      if (i0 + k < n) v[i0 + k] = run;
-      run += x[k];
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) s_carry += s_part[blockDim.x / 32 - 1];
-    __syncthreads();
+  const u64 c = (n + blockDim.x - 1) / blockDim.x;
+  const u64 i0 = (u64)threadIdx.x * c;
+  const u64 i1 = min(i0 + c, (u64)n);
+  u64 sum = 0;
+  for (u64 i = i0; i < i1; ++i) sum += v[i];
+  u64 incl = sum;
+  for (int o = 1; o < 32; o <<= 1) {
+    const u64 y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
   }
-  if (threadIdx.x == 0 && total) *total = s_carry;
+  if (lane == 31) s_part[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    u64 p = lane < (int)(blockDim.x / 32) ? s_part[lane] : 0;
+    for (int o = 1; o < 32; o <<= 1) {
+      const u64 y = __shfl_up_sync(0xffffffffu, p, o);
+      if (lane >= o) p += y;
+    }
+    s_part[lane] = p;
+  }
+  __syncthreads();
+  u64 run = (warp ? s_part[warp - 1] : 0) + incl - sum;
+  for (u64 i = i0; i < i1; ++i) {
+    const u64 x = v[i];
+    v[i] = run;
+    run += x;
+  }
+  if (threadIdx.x == 0 && total) *total = s_part[blockDim.x / 32 - 1];
 }
 
 __global__ void k_records_scatter(DevBuffers b, DevConfig cfg) {
@@ -1140,7 +1136,7 @@ __device__ __forceinline__ uint32_t count_less(const double* __restrict__ t, uin
 }
 
 constexpr int kLutThreads = 256;
-constexpr int kLutTile = 16384;  // records per CTA
+constexpr int kLutTile = 2048;  // records per CTA (>= 10 CTAs per SM at configs[1])
 
 __global__ void __launch_bounds__(kLutThreads)
     k_score_lut(DevBuffers b, DevConfig cfg, uint64_t n_records, uint64_t smem_cap) {
