@@ -278,6 +278,50 @@ int cs_set_name_table(cs_ctx* ctx, uint32_t n_names, const cs_name_info* names);
 int cs_upload(cs_ctx* ctx, uint32_t n_inst, const uint64_t* inst_offsets,
               const cs_event* ev, uint64_t n_workloads, const cs_workload* wl);
 
+/* ------------------------------------------------- wire format (host link)
+ * 16-byte packed record for the host->device leg: the H2D copy is what bounds
+ * an end-to-end run, so the producer (ingest / collector) emits this instead
+ * of cs_event and the device expands it in HBM.  Events are grouped in
+ * instance-aligned blocks of CS_WIRE_BLOCK records (block b of instance i
+ * covers events [inst_offsets[i] + b*CS_WIRE_BLOCK, ...)); block_base[] holds
+ * each block's first start_ts, and t_off is start_ts - block_base (events are
+ * canonically ordered, so t_off >= 0).
+ *   dur      duration (ns); for CS_EV_HAS_VALUE counters the index of the
+ *            f64 `value` in values[] instead
+ *   payload  CS_EV_HAS_COMM: collective slot (cs_event.payload >> 32);
+ *            otherwise cs_event.payload (workload index)
+ * Records that do not fit (offset or duration >= 2^32, negative duration,
+ * name_id >= 65535, kind/category >= 16, both HAS_COMM and a low payload)
+ * set CS_WIRE_ESCAPE and carry an index into escapes[] (full cs_event). */
+#define CS_WIRE_BLOCK 1024u
+#define CS_WIRE_ESCAPE 0x80u
+typedef struct cs_wire_event {
+  uint32_t t_off;
+  uint32_t dur;
+  uint16_t name_id;
+  uint8_t kind_cat;   /* kind | category << 4 */
+  uint8_t flags;      /* CS_EV_* (bits 0-5) | CS_WIRE_ESCAPE */
+  uint32_t payload;
+} cs_wire_event;
+
+/* Upload a batch in the wire format (same instance layout and semantics as
+ * cs_upload; expanded on the device into the same cs_event records). */
+int cs_upload_wire(cs_ctx* ctx, uint32_t n_inst, const uint64_t* inst_offsets,
+                   const cs_wire_event* ev, const int64_t* block_base, const double* values,
+                   uint64_t n_values, const cs_event* escapes, uint64_t n_escapes,
+                   uint64_t n_workloads, const cs_workload* wl);
+
+/* Host encoder (multi-threaded) from cs_event to the wire format; the
+ * producer side of cs_upload_wire.  Buffers are owned by the returned
+ * object; cs_wire_view exposes them. */
+typedef struct cs_wire_trace cs_wire_trace;
+int cs_wire_pack(uint32_t n_inst, const uint64_t* inst_offsets, const cs_event* ev,
+                 uint32_t n_threads, cs_wire_trace** out);
+int cs_wire_view(const cs_wire_trace* w, const cs_wire_event** ev, uint64_t* n_ev,
+                 const int64_t** block_base, uint64_t* n_blocks, const double** values,
+                 uint64_t* n_values, const cs_event** escapes, uint64_t* n_escapes);
+void cs_wire_free(cs_wire_trace* w);
+
 /* Latency model for instance `inst` (UINT32_MAX = default for every instance
  * without its own binding).  Bindings are by instance index, may precede the
  * first cs_upload and survive re-uploads (streams).

@@ -14,6 +14,14 @@ EVENT_DTYPE = np.dtype(
      ("category", "u1"), ("flags", "<u2"), ("payload", "<u8")], align=True)
 assert EVENT_DTYPE.itemsize == 32
 
+# 16-byte wire record (cs_wire_event): the host->device format
+WIRE_DTYPE = np.dtype(
+    [("t_off", "<u4"), ("dur", "<u4"), ("name_id", "<u2"), ("kind_cat", "u1"), ("flags", "u1"),
+     ("payload", "<u4")])
+assert WIRE_DTYPE.itemsize == 16
+WIRE_BLOCK = 1024
+WIRE_ESCAPE = 0x80
+
 WORKLOAD_DTYPE = np.dtype([("batch", "<i8"), ("input_len", "<i8"), ("output_len", "<i8")])
 NAME_INFO_DTYPE = np.dtype(
     [("flags", "<u4"), ("phase", "<i4"), ("beta_slot", "<i4"), ("reserved", "<u4")])

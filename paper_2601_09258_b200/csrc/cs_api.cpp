@@ -81,6 +81,7 @@ struct cs_ctx {
   uint64_t n_ev = 0, n_wl = 0;
   std::vector<uint64_t> inst_off;
   DevBuf d_ev, d_wl, d_names, d_inst_off;
+  DevBuf d_wire, d_wire_base, d_wire_values, d_wire_esc;  // cs_upload_wire staging
   // tiles
   std::vector<uint32_t> tile_inst, inst_first_tile;
   std::vector<uint64_t> tile_begin, tile_end;
@@ -368,8 +369,15 @@ int cs_set_name_table(cs_ctx* ctx, uint32_t n_names, const cs_name_info* names) 
   return CS_OK;
 }
 
-int cs_upload(cs_ctx* ctx, uint32_t n_inst, const uint64_t* inst_offsets, const cs_event* ev,
-              uint64_t n_workloads, const cs_workload* wl) {
+}  // extern "C"
+
+namespace {
+
+// Shared by cs_upload / cs_upload_wire: validates the instance layout,
+// allocates the event array, uploads workloads and offsets, and builds the
+// instance-aligned tiles (= wire blocks).  The caller fills d_ev.
+int upload_layout(cs_ctx* ctx, uint32_t n_inst, const uint64_t* inst_offsets, bool have_ev,
+                  uint64_t n_workloads, const cs_workload* wl) {
   if (!ctx || !inst_offsets || n_inst == 0) return CS_E_INVALID_ARGUMENT;
   cudaSetDevice(ctx->device);
   if (inst_offsets[0] != 0) return fail(ctx, CS_E_INVALID_ARGUMENT, "inst_offsets[0] must be 0");
@@ -377,7 +385,7 @@ int cs_upload(cs_ctx* ctx, uint32_t n_inst, const uint64_t* inst_offsets, const 
     if (inst_offsets[i + 1] < inst_offsets[i])
       return fail(ctx, CS_E_INVALID_ARGUMENT, "inst_offsets must be non-decreasing");
   const uint64_t n_ev = inst_offsets[n_inst];
-  if (n_ev && !ev) return CS_E_INVALID_ARGUMENT;
+  if (n_ev && !have_ev) return CS_E_INVALID_ARGUMENT;
   if (n_workloads && !wl) return CS_E_INVALID_ARGUMENT;
   ctx->n_inst = n_inst;
   ctx->n_ev = n_ev;
@@ -387,8 +395,6 @@ int cs_upload(cs_ctx* ctx, uint32_t n_inst, const uint64_t* inst_offsets, const 
   void* dw = ctx->d_wl.get(std::max<uint64_t>(1, n_workloads) * sizeof(cs_workload));
   void* doff = ctx->d_inst_off.get((n_inst + 1) * sizeof(uint64_t));
   if (!de || !dw || !doff) return fail(ctx, CS_E_CUDA, "cudaMalloc(events)");
-  if (n_ev) CS_CUDA(cudaMemcpyAsync(de, ev, n_ev * sizeof(cs_event), cudaMemcpyHostToDevice,
-                                    ctx->stream));
   if (n_workloads)
     CS_CUDA(cudaMemcpyAsync(dw, wl, n_workloads * sizeof(cs_workload), cudaMemcpyHostToDevice,
                             ctx->stream));
@@ -434,6 +440,53 @@ int cs_upload(cs_ctx* ctx, uint32_t n_inst, const uint64_t* inst_offsets, const 
   // bindings are by instance index and survive re-uploads (streaming pushes)
   if (ctx->model_of_inst.size() < n_inst) ctx->model_of_inst.resize(n_inst, -1);
   ctx->ran = false;
+  return CS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int cs_upload(cs_ctx* ctx, uint32_t n_inst, const uint64_t* inst_offsets, const cs_event* ev,
+              uint64_t n_workloads, const cs_workload* wl) {
+  const int rc = upload_layout(ctx, n_inst, inst_offsets, ev != nullptr, n_workloads, wl);
+  if (rc != CS_OK) return rc;
+  if (ctx->n_ev)
+    CS_CUDA(cudaMemcpyAsync(ctx->d_ev.p, ev, ctx->n_ev * sizeof(cs_event), cudaMemcpyHostToDevice,
+                            ctx->stream));
+  return CS_OK;
+}
+
+int cs_upload_wire(cs_ctx* ctx, uint32_t n_inst, const uint64_t* inst_offsets,
+                   const cs_wire_event* ev, const int64_t* block_base, const double* values,
+                   uint64_t n_values, const cs_event* escapes, uint64_t n_escapes,
+                   uint64_t n_workloads, const cs_workload* wl) {
+  const int rc = upload_layout(ctx, n_inst, inst_offsets, ev != nullptr && block_base != nullptr,
+                               n_workloads, wl);
+  if (rc != CS_OK) return rc;
+  if ((n_values && !values) || (n_escapes && !escapes)) return CS_E_INVALID_ARGUMENT;
+  const uint64_t n = ctx->n_ev;
+  const size_t nt = ctx->tile_inst.size();
+  void* dw = ctx->d_wire.get(std::max<uint64_t>(1, n) * sizeof(cs_wire_event));
+  void* db = ctx->d_wire_base.get(std::max<size_t>(1, nt) * sizeof(int64_t));
+  void* dv = ctx->d_wire_values.get(std::max<uint64_t>(1, n_values) * sizeof(double));
+  void* dx = ctx->d_wire_esc.get(std::max<uint64_t>(1, n_escapes) * sizeof(cs_event));
+  if (!dw || !db || !dv || !dx) return fail(ctx, CS_E_CUDA, "cudaMalloc(wire)");
+  if (n) {
+    CS_CUDA(cudaMemcpyAsync(dw, ev, n * sizeof(cs_wire_event), cudaMemcpyHostToDevice, ctx->stream));
+    CS_CUDA(cudaMemcpyAsync(db, block_base, nt * sizeof(int64_t), cudaMemcpyHostToDevice, ctx->stream));
+  }
+  if (n_values)
+    CS_CUDA(cudaMemcpyAsync(dv, values, n_values * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+  if (n_escapes)
+    CS_CUDA(cudaMemcpyAsync(dx, escapes, n_escapes * sizeof(cs_event), cudaMemcpyHostToDevice,
+                            ctx->stream));
+  launch_wire_expand(static_cast<const cs_wire_event*>(dw), static_cast<const int64_t*>(db),
+                     static_cast<const double*>(dv), static_cast<const cs_event*>(dx),
+                     static_cast<const uint64_t*>(ctx->d_tile_begin.p),
+                     static_cast<const uint64_t*>(ctx->d_tile_end.p), static_cast<uint32_t>(nt),
+                     static_cast<cs_event*>(ctx->d_ev.p), ctx->stream);
+  CS_CUDA(cudaGetLastError());
   return CS_OK;
 }
 

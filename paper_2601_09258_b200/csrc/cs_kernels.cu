@@ -2538,6 +2538,50 @@ __global__ void __launch_bounds__(256, 3) k_cycle_reduce_v2(DevBuffers b, DevCon
   if (unk && (tid & 31) == (uint32_t)(__ffs(grp) - 1)) atomicAdd(&b.inst[inst].n_unknown, (u64)__popc(grp));
 }
 
+// ---------------------------------------------------- wire-format expand
+// 16-B wire records (cs_wire_event) -> canonical 32-B cs_event in HBM, one
+// CTA per instance-aligned block (= tile): 128-bit coalesced loads, 256-bit
+// stores; counter values from the side array, escaped records copied whole.
+__global__ void __launch_bounds__(256) k_wire_expand(const cs_wire_event* __restrict__ w,
+                                                     const int64_t* __restrict__ base,
+                                                     const double* __restrict__ values,
+                                                     const cs_event* __restrict__ esc,
+                                                     const uint64_t* __restrict__ tile_begin,
+                                                     const uint64_t* __restrict__ tile_end,
+                                                     cs_event* __restrict__ out) {
+  const uint32_t t = blockIdx.x;
+  const u64 tb = tile_begin[t], te = tile_end[t];
+  const i64 b0 = base[t];
+  for (u64 j = tb + threadIdx.x; j < te; j += blockDim.x) {
+    const uint4 r = __ldcs(reinterpret_cast<const uint4*>(w + j));
+    const uint32_t t_off = r.x, dur = r.y, payload = r.w;
+    const uint32_t name = r.z & 0xffffu, kc = (r.z >> 16) & 0xffu, flags = r.z >> 24;
+    u64 a, d, c, p;
+    if (flags & CS_WIRE_ESCAPE) {
+      const cs_event& e = esc[payload];
+      a = (u64)e.start_ts;
+      d = (u64)e.duration;
+      c = (u64)e.name_id | ((u64)e.kind << 32) | ((u64)e.category << 40) | ((u64)e.flags << 48);
+      p = e.payload;
+    } else {
+      a = (u64)(b0 + (i64)t_off);
+      d = (flags & CS_EV_HAS_VALUE) ? (u64)__double_as_longlong(values[dur]) : (u64)dur;
+      c = (u64)name | ((u64)(kc & 15u) << 32) | ((u64)(kc >> 4) << 40) | ((u64)flags << 48);
+      p = (flags & CS_EV_HAS_COMM) ? ((u64)payload << 32) : (u64)payload;
+    }
+    asm volatile("st.global.v4.u64 [%0], {%1, %2, %3, %4};" ::"l"(out + j), "l"(a), "l"(d), "l"(c),
+                 "l"(p)
+                 : "memory");
+  }
+}
+
+void launch_wire_expand(const cs_wire_event* w, const int64_t* base, const double* values,
+                        const cs_event* esc, const uint64_t* tile_begin, const uint64_t* tile_end,
+                        uint32_t n_tiles, cs_event* out, cudaStream_t s) {
+  if (!n_tiles) return;
+  k_wire_expand<<<n_tiles, 256, 0, s>>>(w, base, values, esc, tile_begin, tile_end, out);
+}
+
 // ------------------------------------------------------------ launchers
 void launch_scan_events(const DevBuffers& b, const DevConfig&, int mode, bool sample,
                         const uint32_t* list, uint32_t n_list, cudaStream_t s,

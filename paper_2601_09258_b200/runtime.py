@@ -55,6 +55,11 @@ def lib():
     L.cs_set_config.argtypes = [vp, C.POINTER(abi.CycleConfig), C.POINTER(abi.ControlConfig)]
     L.cs_set_name_table.argtypes = [vp, u32, vp]
     L.cs_upload.argtypes = [vp, u32, vp, vp, u64, vp]
+    L.cs_upload_wire.argtypes = [vp, u32, vp, vp, vp, vp, u64, vp, u64, u64, vp]
+    L.cs_wire_pack.argtypes = [u32, vp, vp, u32, C.POINTER(vp)]
+    L.cs_wire_view.argtypes = [vp, C.POINTER(vp), C.POINTER(u64), C.POINTER(vp), C.POINTER(u64),
+                               C.POINTER(vp), C.POINTER(u64), C.POINTER(vp), C.POINTER(u64)]
+    L.cs_wire_free.argtypes = [vp]
     L.cs_load_model.argtypes = [vp, u32, C.POINTER(abi.Model)]
     L.cs_run.argtypes = [vp, u32]
     L.cs_sync.argtypes = [vp]
@@ -100,7 +105,8 @@ def lib():
 
 EXPORTED_SYMBOLS = [
     "cs_abi_version", "cs_status_type", "cs_ctx_create", "cs_ctx_destroy", "cs_last_error",
-    "cs_set_config", "cs_set_name_table", "cs_upload", "cs_load_model", "cs_run", "cs_sync",
+    "cs_set_config", "cs_set_name_table", "cs_upload", "cs_upload_wire", "cs_wire_pack",
+    "cs_wire_view", "cs_wire_free", "cs_load_model", "cs_run", "cs_sync",
     "cs_get_summary", "cs_get_candidates", "cs_get_cycles", "cs_get_components", "cs_get_beta",
     "cs_get_collective_beta", "cs_get_records", "cs_get_alerts", "cs_host_alloc",
     "cs_host_free", "cs_get_timings", "cs_get_launch_count", "cs_fit_latency_model",
@@ -275,6 +281,46 @@ def synth_trace(n_cycles, workload_seed, synth_seed, fault=None, onset=0, durati
         L.cs_synth_free(h)
 
 
+@dataclass
+class WireTrace:
+    """A batch of instances in the 16-byte wire format (cs_wire_pack)."""
+    events: np.ndarray       # WIRE_DTYPE
+    block_base: np.ndarray   # int64 per instance-aligned block of WIRE_BLOCK records
+    values: np.ndarray       # float64 counter values
+    escapes: np.ndarray      # EVENT_DTYPE records that do not fit the packed fields
+    inst_offsets: np.ndarray
+
+    @property
+    def nbytes(self) -> int:
+        return self.events.nbytes + self.block_base.nbytes + self.values.nbytes + self.escapes.nbytes
+
+
+def wire_pack(events: np.ndarray, inst_offsets, n_threads=None) -> WireTrace:
+    """cs_wire_pack: cs_event records -> wire format (the producer side)."""
+    events = np.ascontiguousarray(events, dtype=abi.EVENT_DTYPE)
+    off = np.ascontiguousarray(np.asarray(inst_offsets, dtype=np.uint64))
+    L = lib()
+    h = C.c_void_p()
+    _check(L.cs_wire_pack(len(off) - 1, off.ctypes.data, _ptr(events), n_threads or os.cpu_count() or 1,
+                          C.byref(h)))
+    try:
+        pe, pb, pv, px = C.c_void_p(), C.c_void_p(), C.c_void_p(), C.c_void_p()
+        ne, nb, nv, nx = C.c_uint64(), C.c_uint64(), C.c_uint64(), C.c_uint64()
+        _check(L.cs_wire_view(h, C.byref(pe), C.byref(ne), C.byref(pb), C.byref(nb), C.byref(pv),
+                              C.byref(nv), C.byref(px), C.byref(nx)))
+
+        def arr(ptr, n, dtype):
+            if n == 0:
+                return np.zeros(0, dtype=dtype)
+            nbytes = n * np.dtype(dtype).itemsize
+            return np.frombuffer((C.c_char * nbytes).from_address(ptr.value), dtype=dtype).copy()
+
+        return WireTrace(arr(pe, ne.value, abi.WIRE_DTYPE), arr(pb, nb.value, np.int64),
+                         arr(pv, nv.value, np.float64), arr(px, nx.value, abi.EVENT_DTYPE), off)
+    finally:
+        L.cs_wire_free(h)
+
+
 # ---------------------------------------------------------------- analyzer
 @dataclass
 class InstanceResult:
@@ -342,6 +388,15 @@ class Analyzer:
         self._ck(self.L.cs_upload(self.h, len(off) - 1, off.ctypes.data, _ptr(events), len(wl),
                                   _ptr(wl)))
         self.n_inst = len(off) - 1
+
+    def upload_wire(self, w: WireTrace, workloads: np.ndarray):
+        """cs_upload_wire: same batch as upload(), sent in the 16-byte format."""
+        wl = np.ascontiguousarray(workloads, dtype=abi.WORKLOAD_DTYPE)
+        self._ck(self.L.cs_upload_wire(self.h, len(w.inst_offsets) - 1, w.inst_offsets.ctypes.data,
+                                       _ptr(w.events), _ptr(w.block_base), _ptr(w.values),
+                                       len(w.values), _ptr(w.escapes), len(w.escapes), len(wl),
+                                       _ptr(wl)))
+        self.n_inst = len(w.inst_offsets) - 1
 
     def load_model(self, model: LatencyModel, inst: int | None = None):
         v = model.view()
