@@ -1,4 +1,2 @@
-timeout 600 python -m pytest tests/test_wire.py -x -q > gpurun_out/pytest_wire.log 2>&1; echo wire=$?
-tail -3 gpurun_out/pytest_wire.log
-timeout 900 python bench.py --no-cpu-baseline > gpurun_out/bench.log 2>&1; echo bench=$?
-tail -1 gpurun_out/bench.log
+timeout 600 python tools/tools_variants.py 3700000 0,1,2,3,4,5 > gpurun_out/variants.log 2>&1; echo var=$?
+cat gpurun_out/variants.log
