@@ -86,6 +86,7 @@ struct cs_ctx {
   std::vector<uint32_t> tile_inst, inst_first_tile;
   std::vector<uint64_t> tile_begin, tile_end;
   DevBuf d_tile_inst, d_tile_begin, d_tile_end, d_inst_first_tile, d_tile_cnt, d_tile_pref;
+  DevBuf d_scan_tmp;
   std::vector<uint32_t> sample_tiles;
   DevBuf d_sample_tiles, d_redo_tiles;
   // state
@@ -188,6 +189,7 @@ DevBuffers make_buffers(cs_ctx* ctx) {
   b.inst = static_cast<InstState*>(ctx->d_inst.p);
   b.tile_cnt = static_cast<uint64_t*>(ctx->d_tile_cnt.p);
   b.tile_pref = static_cast<uint64_t*>(ctx->d_tile_pref.p);
+  b.scan_tmp = static_cast<uint64_t*>(ctx->d_scan_tmp.p);
   b.a_pos = static_cast<uint64_t*>(ctx->d_a_pos.p);
   b.a_start = static_cast<int64_t*>(ctx->d_a_start.p);
   b.a_end = static_cast<int64_t*>(ctx->d_a_end.p);
@@ -425,7 +427,7 @@ int upload_layout(cs_ctx* ctx, uint32_t n_inst, const uint64_t* inst_offsets, bo
       ctx->sample_tiles.push_back(static_cast<uint32_t>(t));
   auto* dst = dev<uint32_t>(ctx->d_sample_tiles, ctx->sample_tiles.size());
   if (!dti || !dtb || !dte || !dft || !dst || !dev<uint64_t>(ctx->d_tile_cnt, nt) ||
-      !dev<uint64_t>(ctx->d_tile_pref, nt + 1))
+      !dev<uint64_t>(ctx->d_tile_pref, nt + 1) || !dev<uint64_t>(ctx->d_scan_tmp, nt / 1024 + 2))
     return fail(ctx, CS_E_CUDA, "cudaMalloc(tiles)");
   if (!ctx->sample_tiles.empty())
     CS_CUDA(cudaMemcpyAsync(dst, ctx->sample_tiles.data(), ctx->sample_tiles.size() * 4,
@@ -871,6 +873,9 @@ int cs_run(cs_ctx* ctx, uint32_t mask) {
   launch_tile_prefix(b, s, &ctx->launches);
   ctx->timed.push_back({"scan_events", {e1, e2}});
   launch_rank(b, cfg, 1, s, &ctx->launches);
+  const int e9 = record_event(ctx, 9);
+  ctx->timed.push_back({"sample_and_setup", {e0, e1}});
+  ctx->timed.push_back({"prefix_rank", {e2, e9}});
   CS_CUDA(cudaMemcpyAsync(ctx->h_inst.data(), d_inst, n_inst * sizeof(InstState),
                           cudaMemcpyDeviceToHost, s));
   CS_CUDA(cudaStreamSynchronize(s));
@@ -978,6 +983,7 @@ int cs_run(cs_ctx* ctx, uint32_t mask) {
                           cudaMemcpyHostToDevice, s));
   b = make_buffers(ctx);
   const int e3 = record_event(ctx, 3);
+  ctx->timed.push_back({"host_sizing", {e9, e3}});
   launch_bounds(b, s, &ctx->launches);
   for (uint32_t i = 0; i < n_inst; ++i)
     if (ctx->used_fallback[i] && ctx->fallback_cycles[i])
@@ -996,12 +1002,10 @@ int cs_run(cs_ctx* ctx, uint32_t mask) {
   launch_records(b, cfg, 0, s, &ctx->launches);
   const int e6 = record_event(ctx, 6);
   ctx->timed.push_back({"stage_records", {e5, e6}});
+  // record counts stay on the device: scoring and detection launch over the
+  // cycle count as capacity and clamp to rec_off[n_inst] (no host round trip)
+  const uint64_t rec_cap = ctx->n_cycles;
   ctx->rec_off.assign(n_inst + 1, 0);
-  CS_CUDA(cudaMemcpyAsync(ctx->rec_off.data(), ctx->d_rec_off.p, (n_inst + 1) * 8,
-                          cudaMemcpyDeviceToHost, s));
-  CS_CUDA(cudaStreamSynchronize(s));
-  CS_CUDA(cudaGetLastError());
-  ctx->n_records = ctx->rec_off[n_inst];
   int last = e6;
   // ---- score + detect
   if (mask & (CS_RUN_SCORE | CS_RUN_DETECT)) {
@@ -1044,16 +1048,16 @@ int cs_run(cs_ctx* ctx, uint32_t mask) {
     CS_CUDA(cudaMemcpyAsync(dm, ctx->h_models.data(), n_inst * sizeof(DevModel),
                             cudaMemcpyHostToDevice, s));
     b = make_buffers(ctx);
-    if (!dev<uint64_t>(ctx->block_tmp, ctx->n_records / 1024 + 16))
+    if (!dev<uint64_t>(ctx->block_tmp, rec_cap / 1024 + 16))
       return fail(ctx, CS_E_CUDA, "cudaMalloc(block_tmp)");
     b = make_buffers(ctx);
-    launch_score(b, cfg, ctx->n_records, ctx->rec_off.data(), ctx->model_of_inst.data(),
+    launch_score(b, cfg, rec_cap, ctx->rec_off.data(), ctx->model_of_inst.data(),
                  ctx->h_models.data(), s, &ctx->launches);
     const int e7 = record_event(ctx, 7);
     ctx->timed.push_back({"score", {e6, e7}});
     last = e7;
     if (mask & CS_RUN_DETECT) {
-      launch_detect(b, cfg, ctx->n_records, s, &ctx->launches);
+      launch_detect(b, cfg, rec_cap, s, &ctx->launches);
       const int e8 = record_event(ctx, 8);
       ctx->timed.push_back({"detect", {e7, e8}});
       last = e8;
@@ -1074,8 +1078,11 @@ int cs_run(cs_ctx* ctx, uint32_t mask) {
   if (mask & CS_RUN_DETECT)
     CS_CUDA(cudaMemcpyAsync(ctx->alert_off.data(), ctx->d_alert_off.p, (n_inst + 1) * 8,
                             cudaMemcpyDeviceToHost, s));
+  CS_CUDA(cudaMemcpyAsync(ctx->rec_off.data(), ctx->d_rec_off.p, (n_inst + 1) * 8,
+                          cudaMemcpyDeviceToHost, s));
   CS_CUDA(cudaStreamSynchronize(s));
   CS_CUDA(cudaGetLastError());
+  ctx->n_records = ctx->rec_off[n_inst];
   for (uint32_t i = 0; i < n_inst; ++i)
     if (ctx->inst_status[i] == CS_OK && ctx->h_inst[i].first_bad_record != UINT64_MAX &&
         (mask & (CS_RUN_SCORE | CS_RUN_DETECT)))

@@ -112,6 +112,7 @@ struct DevBuffers {
   InstState* inst;
   uint64_t* tile_cnt;           // anchors per tile (tile-local compaction)
   uint64_t* tile_pref;          // exclusive prefix of tile_cnt, n_tiles+1
+  uint64_t* scan_tmp;           // block sums of the multi-CTA scan (n_tiles/1024 + 2)
   // anchors (capacity = events; instance i at inst_off[i])
   uint64_t* a_pos;
   int64_t* a_start;

@@ -887,6 +887,61 @@ __global__ void __launch_bounds__(1024, 1) k_scan_exclusive(uint64_t* v, uint64_
   if (threadIdx.x == 0 && total) *total = s_part[blockDim.x / 32 - 1];
 }
 
+// Multi-CTA exclusive scan for large arrays (tile prefixes: ~1e5 entries):
+// k_scan_totals writes each 1024-element block's sum, k_scan_exclusive scans
+// the (few) block sums, k_scan_apply scans within each block and adds its
+// block's prefix.  Coalesced, one element per thread.
+constexpr int kScanBlk = 1024;
+__device__ __forceinline__ u64 block_incl_scan(u64 x, u64* s_w, u64* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  u64 incl = x;
+  for (int o = 1; o < 32; o <<= 1) {
+    const u64 y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) s_w[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    u64 p = lane < (int)(blockDim.x / 32) ? s_w[lane] : 0;
+    for (int o = 1; o < 32; o <<= 1) {
+      const u64 y = __shfl_up_sync(0xffffffffu, p, o);
+      if (lane >= o) p += y;
+    }
+    s_w[lane] = p;
+  }
+  __syncthreads();
+  if (total) *total = s_w[blockDim.x / 32 - 1];
+  return incl + (warp ? s_w[warp - 1] : 0);
+}
+__global__ void __launch_bounds__(kScanBlk) k_scan_totals(const uint64_t* v, uint64_t n, uint64_t* part) {
+  __shared__ u64 s_w[32];
+  const u64 i = (u64)blockIdx.x * kScanBlk + threadIdx.x;
+  u64 t;
+  block_incl_scan(i < n ? v[i] : 0, s_w, &t);
+  if (threadIdx.x == 0) part[blockIdx.x] = t;
+}
+__global__ void __launch_bounds__(kScanBlk) k_scan_apply(uint64_t* v, uint64_t n, const uint64_t* part) {
+  __shared__ u64 s_w[32];
+  const u64 i = (u64)blockIdx.x * kScanBlk + threadIdx.x;
+  const u64 x = i < n ? v[i] : 0;
+  const u64 incl = block_incl_scan(x, s_w, nullptr);
+  if (i < n) v[i] = part[blockIdx.x] + incl - x;
+}
+
+void launch_exclusive_scan(uint64_t* v, uint64_t n, uint64_t* total, uint64_t* tmp, cudaStream_t s,
+                           uint64_t* launches) {
+  if (n <= 16 * kScanBlk || !tmp) {
+    k_scan_exclusive<<<1, 1024, 0, s>>>(v, n, total);
+    ++*launches;
+    return;
+  }
+  const u64 nb = (n + kScanBlk - 1) / kScanBlk;
+  k_scan_totals<<<(unsigned)nb, kScanBlk, 0, s>>>(v, n, tmp);
+  k_scan_exclusive<<<1, 1024, 0, s>>>(tmp, nb, total);
+  k_scan_apply<<<(unsigned)nb, kScanBlk, 0, s>>>(v, n, tmp);
+  *launches += 3;
+}
+
 __global__ void k_records_scatter(DevBuffers b, DevConfig cfg) {
   __shared__ uint32_t s_w[32];
   const u64 g = (u64)blockIdx.x * kRecBlock + threadIdx.x;
@@ -953,11 +1008,20 @@ __device__ __forceinline__ i64 pick_i(const i64 (&x)[NF > 0 ? NF : 1], uint32_t 
   return v;
 }
 
+// Records are counted on the device (rec_off[n_inst]); record kernels are
+// launched over a capacity (the cycle count) and clamp to the device count,
+// so cs_run needs no host round trip between records and scoring.
+__device__ __forceinline__ u64 records_on_device(const DevBuffers& b, u64 cap) {
+  const u64 n = b.rec_off[b.n_inst];
+  return n < cap ? n : cap;
+}
+
 template <int NF>
 __global__ void __launch_bounds__(kScoreThreads)
     k_score(DevBuffers b, DevConfig cfg, uint64_t n_records, uint64_t smem_cap) {
   extern __shared__ __align__(16) unsigned char s_model[];
   __shared__ uint32_t s_inst;
+  n_records = records_on_device(b, n_records);
   const u64 r0 = (u64)blockIdx.x * kScoreTile;
   const u64 r1 = min(r0 + (u64)kScoreTile, (u64)n_records);
   const double eps = cfg.ctl.epsilon;
@@ -1142,6 +1206,7 @@ __global__ void __launch_bounds__(kLutThreads)
     k_score_lut(DevBuffers b, DevConfig cfg, uint64_t n_records, uint64_t smem_cap) {
   extern __shared__ __align__(16) unsigned char s_thr[];
   __shared__ uint32_t s_inst;
+  n_records = records_on_device(b, n_records);
   const u64 r0 = (u64)blockIdx.x * kLutTile;
   const u64 r1 = min(r0 + (u64)kLutTile, (u64)n_records);
   const double eps = cfg.ctl.epsilon;
@@ -1236,6 +1301,7 @@ __device__ __forceinline__ double window_stat_stream(const double* e, u64 t, u64
 
 __global__ void k_detect_flags(DevBuffers b, DevConfig cfg, uint64_t n_records) {
   __shared__ uint32_t s_w[32];
+  n_records = records_on_device(b, n_records);
   const u64 k = (u64)blockIdx.x * kDetBlock + threadIdx.x;
   bool alert = false;
   if (k < n_records) {
@@ -1346,6 +1412,7 @@ __global__ void k_alert_off(DevBuffers b) {
 
 __global__ void k_detect_scatter(DevBuffers b, uint64_t n_records) {
   __shared__ uint32_t s_w[32];
+  n_records = records_on_device(b, n_records);
   const u64 k = (u64)blockIdx.x * kDetBlock + threadIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const bool alert = k < n_records && (b.rec_flags[k] & 4);
@@ -2620,9 +2687,9 @@ void launch_cycle_reduce_tpc(const DevBuffers& b, const DevConfig& cfg, int do_b
 void launch_tile_prefix(const DevBuffers& b, cudaStream_t s, uint64_t* launches) {
   cudaMemcpyAsync(b.tile_pref, b.tile_cnt, (size_t)b.n_tiles * sizeof(uint64_t),
                   cudaMemcpyDeviceToDevice, s);
-  k_scan_exclusive<<<1, 1024, 0, s>>>(b.tile_pref, b.n_tiles, b.tile_pref + b.n_tiles);
+  launch_exclusive_scan(b.tile_pref, b.n_tiles, b.tile_pref + b.n_tiles, b.scan_tmp, s, launches);
   k_inst_anchor_counts<<<(b.n_inst + 255) / 256, 256, 0, s>>>(b);
-  *launches += 2;
+  *launches += 1;
 }
 
 void launch_rank(const DevBuffers& b, const DevConfig& cfg, int final_pass, cudaStream_t s,
