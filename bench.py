@@ -344,6 +344,19 @@ def run_ours(args, rank, world, local_rank):
         dom = (("cycle_reduce", reduce_bytes, red_t) if red_t >= scan_t
                else ("scan_events", scan_bytes, scan_t))
     achieved = dom[1] / (dom[2] * 1e-3) / 1e9
+    # dram bytes of the dominant kernel from the committed ncu --set full
+    # capture of this same command (profiles/r1_ncu_traffic.json); only for
+    # the default workload it was taken on
+    traffic = None
+    kname = {"cycle_reduce": "k_cycle_reduce_v2", "scan_events": "k_scan_warp",
+             "fused_segment": "k_segment_pass"}[dom[0]]
+    try:
+        with open(os.path.join(ROOT, "profiles", "r1_ncu_traffic.json")) as f:
+            tr = json.load(f).get(kname)
+        if tr and args.workload == "c2":
+            traffic = tr["dram_read_bytes"] + tr["dram_write_bytes"]
+    except (OSError, ValueError):
+        pass
     path_bytes = 44.5 * n_events  # SURVEY §8d per-event figure
     line = {
         "metric": METRIC,
@@ -365,7 +378,8 @@ def run_ours(args, rank, world, local_rank):
                    "model_fit_s": round(fit_s, 3), "setup_s": round(setup_s, 1)},
         "roofline": {"bound": "hbm", "kernel": dom[0], "achieved": achieved, "peak": peak,
                      "peak_source": peak_src, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": None,
+                     "traffic": traffic, "algorithmic_bytes": dom[1],
+                     "traffic_source": "profiles/r1_ncu_traffic.json (ncu --set full, dram read+write)",
                      "kernel_ms": dom[2], "event_pass_ms": scan_t, "cycle_reduce_ms": red_t,
                      "path_frac_44p5B_per_event": path_bytes / (dev_ms * 1e-3) / 1e9 / peak},
         "e2e": {"value": world * n_events / (e2e * 1e-3), "unit": UNIT,
