@@ -277,6 +277,7 @@ int cs_set_name_table(cs_ctx* ctx, uint32_t n_names, const cs_name_info* names);
  * host buffers may be pinned (cs_host_alloc) for full link bandwidth. */
 int cs_upload(cs_ctx* ctx, uint32_t n_inst, const uint64_t* inst_offsets,
               const cs_event* ev, uint64_t n_workloads, const cs_workload* wl);
+/* (n_workloads = 0 with wl = NULL keeps the previously uploaded workload table.) */
 
 /* ------------------------------------------------- wire format (host link)
  * 16-byte packed record for the host->device leg: the H2D copy is what bounds
@@ -392,6 +393,16 @@ int cs_alerts_to_ndjson(const cs_alert* alerts, uint64_t n_alerts, uint64_t pre_
 int cs_stream_begin(cs_ctx* ctx);
 int cs_stream_end(cs_ctx* ctx);
 int cs_stream_tail(cs_ctx* ctx, uint32_t inst, uint64_t* keep_from);
+/* One micro-batch of monitor_loop (main.cpp:151-177) natively: per instance,
+ * the carried trailing partial cycle of the previous push is prepended to the
+ * new events ev[offsets[i] .. offsets[i+1]), the batch is uploaded and run
+ * with `stage_mask`, the new trailing partial cycle is kept, and the alerts
+ * of every instance (instance order) are copied to `alerts`.  Passing
+ * n_workloads = 0 and wl = NULL keeps the previously uploaded workload table
+ * (event payloads index it).  Per-batch alert latency = this call. */
+int cs_stream_push(cs_ctx* ctx, uint32_t n_inst, const uint64_t* offsets, const cs_event* ev,
+                   uint64_t n_workloads, const cs_workload* wl, uint32_t stage_mask,
+                   cs_alert* alerts, size_t cap, size_t* n_alerts);
 
 /* Execution options.  CS_OPT_FUSED (default 0): 1 selects the single-pass
  * fused segmentation kernel (k_fused_segment) when applicable; 0 runs the

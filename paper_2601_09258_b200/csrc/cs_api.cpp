@@ -87,6 +87,12 @@ struct cs_ctx {
   std::vector<uint64_t> tile_begin, tile_end;
   DevBuf d_tile_inst, d_tile_begin, d_tile_end, d_inst_first_tile, d_tile_cnt, d_tile_pref;
   DevBuf d_scan_tmp;
+  // cs_stream_push: carried trailing partial cycle per instance + pinned staging
+  std::vector<std::vector<cs_event>> tails;
+  cs_event* stage_host = nullptr;
+  size_t stage_cap = 0;
+  std::vector<uint64_t> stage_off;
+  DevBuf d_keep;
   std::vector<uint32_t> sample_tiles;
   DevBuf d_sample_tiles, d_redo_tiles;
   // state
@@ -324,6 +330,7 @@ void cs_ctx_destroy(cs_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
+  if (ctx->stage_host) cudaFreeHost(ctx->stage_host);
   delete ctx;
 }
 
@@ -391,7 +398,7 @@ int upload_layout(cs_ctx* ctx, uint32_t n_inst, const uint64_t* inst_offsets, bo
   if (n_workloads && !wl) return CS_E_INVALID_ARGUMENT;
   ctx->n_inst = n_inst;
   ctx->n_ev = n_ev;
-  ctx->n_wl = n_workloads;
+  if (n_workloads || wl) ctx->n_wl = n_workloads;  // none given: keep the previous table
   ctx->inst_off.assign(inst_offsets, inst_offsets + n_inst + 1);
   void* de = ctx->d_ev.get(std::max<uint64_t>(1, n_ev) * sizeof(cs_event));
   void* dw = ctx->d_wl.get(std::max<uint64_t>(1, n_workloads) * sizeof(cs_workload));
@@ -1100,6 +1107,7 @@ int cs_run(cs_ctx* ctx, uint32_t mask) {
 int cs_stream_begin(cs_ctx* ctx) {
   if (!ctx) return CS_E_INVALID_ARGUMENT;
   ctx->streaming = true;
+  ctx->tails.clear();
   ctx->stream_fresh = true;
   return CS_OK;
 }
@@ -1121,6 +1129,88 @@ int cs_stream_tail(cs_ctx* ctx, uint32_t inst, uint64_t* keep_from) {
   CS_CUDA(cudaMemcpy(&last, static_cast<const uint64_t*>(ctx->c_last.p) + g, 8,
                      cudaMemcpyDeviceToHost));
   *keep_from = last - ctx->inst_off[inst];
+  return CS_OK;
+}
+
+int cs_stream_push(cs_ctx* ctx, uint32_t n_inst, const uint64_t* offsets, const cs_event* ev,
+                   uint64_t n_workloads, const cs_workload* wl, uint32_t mask, cs_alert* alerts,
+                   size_t cap, size_t* n_alerts) {
+  if (!ctx || !offsets || n_inst == 0) return CS_E_INVALID_ARGUMENT;
+  if (!ctx->streaming) return fail(ctx, CS_E_INVALID_ARGUMENT, "not streaming (cs_stream_begin)");
+  if (offsets[0] != 0) return fail(ctx, CS_E_INVALID_ARGUMENT, "offsets[0] must be 0");
+  if (ctx->tails.size() != n_inst) {
+    if (!ctx->tails.empty() && !ctx->stream_fresh)
+      return fail(ctx, CS_E_INVALID_ARGUMENT, "instance count changed mid-stream");
+    ctx->tails.assign(n_inst, {});
+  }
+  // carried trailing partial cycle + the new events, per instance, staged pinned
+  ctx->stage_off.assign(n_inst + 1, 0);
+  for (uint32_t i = 0; i < n_inst; ++i) {
+    if (offsets[i + 1] < offsets[i]) return fail(ctx, CS_E_INVALID_ARGUMENT, "offsets must be non-decreasing");
+    ctx->stage_off[i + 1] = ctx->stage_off[i] + ctx->tails[i].size() + (offsets[i + 1] - offsets[i]);
+  }
+  const uint64_t total = ctx->stage_off[n_inst];
+  if (total > ctx->stage_cap) {
+    if (ctx->stage_host) cudaFreeHost(ctx->stage_host);
+    ctx->stage_host = nullptr;
+    ctx->stage_cap = 0;
+    const size_t want = std::max<size_t>(total + total / 2, 1 << 16);
+    if (cudaHostAlloc(reinterpret_cast<void**>(&ctx->stage_host), want * sizeof(cs_event),
+                      cudaHostAllocDefault) != cudaSuccess)
+      return fail(ctx, CS_E_CUDA, "cudaHostAlloc(stream staging)");
+    ctx->stage_cap = want;
+  }
+  for (uint32_t i = 0; i < n_inst; ++i) {
+    cs_event* dst = ctx->stage_host + ctx->stage_off[i];
+    std::copy(ctx->tails[i].begin(), ctx->tails[i].end(), dst);
+    std::copy(ev + offsets[i], ev + offsets[i + 1], dst + ctx->tails[i].size());
+  }
+  int rc = cs_upload(ctx, n_inst, ctx->stage_off.data(), ctx->stage_host, n_workloads, wl);
+  if (rc != CS_OK) return rc;
+  rc = cs_run(ctx, mask);
+  if (rc != CS_OK) return rc;
+  // new tails: everything from the last closed cycle's end (cycles.cpp:147)
+  auto* dk = dev<uint64_t>(ctx->d_keep, n_inst);
+  if (!dk) return fail(ctx, CS_E_CUDA, "cudaMalloc(keep)");
+  launch_stream_keep(make_buffers(ctx), dk, ctx->stream);
+  std::vector<uint64_t> keep(n_inst);
+  CS_CUDA(cudaMemcpyAsync(keep.data(), dk, n_inst * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  // alerts of every instance, in instance order
+  size_t na = 0;
+  const bool det = (mask & CS_RUN_DETECT) != 0;
+  std::vector<cs_alert> all;
+  if (det && ctx->alert_off[n_inst]) {
+    const uint64_t n_all = ctx->alert_off[n_inst];
+    auto* d = dev<cs_alert>(ctx->d_scratch, n_all);
+    if (!d) return fail(ctx, CS_E_CUDA, "cudaMalloc(alerts)");
+    DevConfig cfg{ctx->cyc, ctx->ctl, 0.0};
+    const DevBuffers b = make_buffers(ctx);
+    for (uint32_t i = 0; i < n_inst; ++i) {
+      const uint64_t a0 = ctx->alert_off[i], ni = ctx->alert_off[i + 1] - a0;
+      if (ni) launch_gather_alerts(b, cfg, i, a0, ni, d + a0, ctx->stream);
+    }
+    all.resize(n_all);
+    CS_CUDA(cudaMemcpyAsync(all.data(), d, n_all * sizeof(cs_alert), cudaMemcpyDeviceToHost,
+                            ctx->stream));
+  }
+  CS_CUDA(cudaStreamSynchronize(ctx->stream));
+  for (uint32_t i = 0; i < n_inst && det; ++i) {
+    // monitor_loop stops at the first NonPositiveLatency (main.cpp:162)
+    const uint64_t bad = ctx->h_inst[i].first_bad_record;
+    for (uint64_t a = ctx->alert_off[i]; a < ctx->alert_off[i + 1]; ++a) {
+      if (all[a].record_index >= bad) break;
+      if (alerts && na < cap) alerts[na] = all[a];
+      ++na;
+    }
+  }
+  for (uint32_t i = 0; i < n_inst; ++i) {
+    const cs_event* part = ctx->stage_host + ctx->stage_off[i];
+    const uint64_t len = ctx->stage_off[i + 1] - ctx->stage_off[i];
+    const uint64_t k = std::min(keep[i], len);
+    ctx->tails[i].assign(part + k, part + len);
+  }
+  if (n_alerts) *n_alerts = na;
+  if (alerts && na > cap) return fail(ctx, CS_E_INVALID_ARGUMENT, "alert buffer too small");
   return CS_OK;
 }
 

@@ -199,6 +199,7 @@ void launch_freq_cycles(const cs_event* ev, uint64_t begin, uint64_t end, int64_
 void launch_wire_expand(const cs_wire_event* w, const int64_t* base, const double* values,
                         const cs_event* esc, const uint64_t* tile_begin, const uint64_t* tile_end,
                         uint32_t n_tiles, cs_event* out, cudaStream_t s);
+void launch_stream_keep(const DevBuffers& b, uint64_t* keep, cudaStream_t s);
 void launch_lut_build(const uint8_t* feat, const int32_t* rank, const double* leafp,
                       uint32_t n_trees, uint32_t D, double base, double floor_, uint32_t n0,
                       uint64_t cells, double* lut, cudaStream_t s);

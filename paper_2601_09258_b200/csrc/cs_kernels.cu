@@ -1303,27 +1303,40 @@ __global__ void k_detect_flags(DevBuffers b, DevConfig cfg, uint64_t n_records) 
   __shared__ uint32_t s_w[32];
   n_records = records_on_device(b, n_records);
   const u64 k = (u64)blockIdx.x * kDetBlock + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const bool valid = k < n_records;
   bool alert = false;
-  if (k < n_records) {
-    const uint32_t inst = upper_bound_u64(b.rec_off, b.n_inst + 1, k) - 1;
-    const u64 rb = b.rec_off[inst];
-    const u64 t = k - rb;
+  uint32_t inst = 0xffffffffu;
+  u64 t = 0, rb = 0;
+  double stat = 0.0;
+  const u64 W = cfg.ctl.window, warm = cfg.ctl.warmup;
+  if (valid) {
+    inst = upper_bound_u64(b.rec_off, b.n_inst + 1, k) - 1;
+    rb = b.rec_off[inst];
+    t = k - rb;
+    stat = b.stream ? window_stat_stream(b.rec_resid + rb, t, W, cfg.ctl.strategy, b.stream[inst])
+                    : window_stat(b.rec_resid + rb, t, W, cfg.ctl.strategy);
+  }
+  // statistic of record k-1: the neighbouring lane's, unless it is in another
+  // warp or instance (then recomputed, identically)
+  const double up_stat = __shfl_up_sync(0xffffffffu, stat, 1);
+  const uint32_t up_inst = __shfl_up_sync(0xffffffffu, inst, 1);
+  if (valid) {
     const double limit = b.models[inst].ucl;
     const double* e = b.rec_resid + rb;
-    const u64 W = cfg.ctl.window, warm = cfg.ctl.warmup;
-    double stat;
     bool armed, prev = false;
+    const bool have_up = lane > 0 && up_inst == inst;
     if (b.stream) {
       const StreamCarry& c = b.stream[inst];
       const u64 T = c.seen + t;
-      stat = window_stat_stream(e, t, W, cfg.ctl.strategy, c);
       armed = T >= warm;
       if (t == 0) prev = c.prev_flag != 0;
-      else if (T - 1 >= warm) prev = window_stat_stream(e, t - 1, W, cfg.ctl.strategy, c) > limit;
+      else if (T - 1 >= warm)
+        prev = (have_up ? up_stat : window_stat_stream(e, t - 1, W, cfg.ctl.strategy, c)) > limit;
     } else {
-      stat = window_stat(e, t, W, cfg.ctl.strategy);
       armed = t >= warm;
-      if (t >= 1 && t - 1 >= warm) prev = window_stat(e, t - 1, W, cfg.ctl.strategy) > limit;
+      if (t >= 1 && t - 1 >= warm)
+        prev = (have_up ? up_stat : window_stat(e, t - 1, W, cfg.ctl.strategy)) > limit;
     }
     const bool flagged = armed && stat > limit;
     alert = flagged && !prev;
@@ -2647,6 +2660,21 @@ void launch_wire_expand(const cs_wire_event* w, const int64_t* base, const doubl
                         uint32_t n_tiles, cs_event* out, cudaStream_t s) {
   if (!n_tiles) return;
   k_wire_expand<<<n_tiles, 256, 0, s>>>(w, base, values, esc, tile_begin, tile_end, out);
+}
+
+// Streaming: per instance, the position (relative to the instance's first
+// uploaded event) from which events are carried into the next micro-batch:
+// the last closed cycle's end group start (cycles.cpp:147 drops the trailing
+// partial cycle; it is completed by the next batch).
+__global__ void k_stream_keep(DevBuffers b, uint64_t* keep) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= b.n_inst) return;
+  const u64 c0 = b.cyc_off[i], c1 = b.cyc_off[i + 1];
+  keep[i] = c1 > c0 ? b.c_last[c1 - 1] - b.inst_off[i] : 0;
+}
+
+void launch_stream_keep(const DevBuffers& b, uint64_t* keep, cudaStream_t s) {
+  if (b.n_inst) k_stream_keep<<<(b.n_inst + 127) / 128, 128, 0, s>>>(b, keep);
 }
 
 // ------------------------------------------------------------ launchers

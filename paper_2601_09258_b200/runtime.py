@@ -74,6 +74,7 @@ def lib():
     L.cs_stream_begin.argtypes = [vp]
     L.cs_stream_end.argtypes = [vp]
     L.cs_stream_tail.argtypes = [vp, u32, C.POINTER(C.c_uint64)]
+    L.cs_stream_push.argtypes = [vp, u32, vp, vp, u64, vp, u32, vp, sz, psz]
     L.cs_evaluate_strategy.argtypes = [vp, u32, vp, u64, C.POINTER(abi.StrategyMetrics)]
     L.cs_alerts_to_ndjson.argtypes = [vp, u64, u64, u64, vp, sz, psz]
     L.cs_microbench.argtypes = [C.c_int, vp, u64, C.c_int, C.c_int, C.c_int, C.c_int,
@@ -114,7 +115,7 @@ EXPORTED_SYMBOLS = [
     "cs_ucl_from_stats", "cs_compute_ucl", "cs_config_from_json", "cs_synth_generate",
     "cs_synth_view", "cs_synth_names", "cs_synth_free", "cs_set_option", "cs_microbench",
     "cs_redetect", "cs_evaluate_strategy", "cs_alerts_to_ndjson", "cs_stream_begin",
-    "cs_stream_end", "cs_stream_tail",
+    "cs_stream_end", "cs_stream_tail", "cs_stream_push",
 ]
 
 
@@ -554,6 +555,28 @@ class Stream:
             _check(lib().cs_stream_tail(self.an.h, i, C.byref(keep)), self.an.h)
             self.tails[i] = p[keep.value:].copy()
         return out
+
+    def push_native(self, events_per_inst, workloads=None, mask: int = abi.RUN_ALL,
+                    max_alerts: int = 1 << 16) -> np.ndarray:
+        """cs_stream_push: the same micro-batch step done in the library (tails,
+        upload, run, alert gather in one call); returns every instance's alerts
+        in instance order.  workloads=None keeps the uploaded table."""
+        parts = [np.asarray(e, dtype=abi.EVENT_DTYPE) for e in events_per_inst]
+        off = np.zeros(len(parts) + 1, np.uint64)
+        off[1:] = np.cumsum([len(p) for p in parts])
+        ev = np.ascontiguousarray(np.concatenate(parts)) if parts else np.zeros(0, abi.EVENT_DTYPE)
+        return self.push_packed(ev, off, workloads, mask, max_alerts)
+
+    def push_packed(self, ev: np.ndarray, off: np.ndarray, workloads=None, mask: int = abi.RUN_ALL,
+                    max_alerts: int = 1 << 16) -> np.ndarray:
+        """push_native with the batch already concatenated (ev, per-instance offsets)."""
+        wl = None if workloads is None else np.ascontiguousarray(workloads, dtype=abi.WORKLOAD_DTYPE)
+        out = np.zeros(max_alerts, abi.ALERT_DTYPE)
+        n = C.c_size_t()
+        _check(lib().cs_stream_push(self.an.h, len(off) - 1, off.ctypes.data, _ptr(ev) or None,
+                                    0 if wl is None else len(wl), _ptr(wl), mask, _ptr(out),
+                                    max_alerts, C.byref(n)), self.an.h)
+        return out[:n.value].copy()
 
     def close(self):
         _check(lib().cs_stream_end(self.an.h), self.an.h)

@@ -177,3 +177,43 @@ def test_stream_equals_whole_trace(rt, n_inst, strip_fm, slice_ms, hint):
         assert np.array_equal(al["smoothed_error"].view(np.uint64),
                               ref[i].alerts["smoothed_error"].view(np.uint64))
     an.close()
+
+
+def test_native_push_equals_python_push(rt):
+    """cs_stream_push (tails, upload, run and alert gather in the library)
+    gives the alerts of the Python-driven micro-batch loop, and the union of
+    its alerts equals the whole-trace run's."""
+    traces = _traces(rt, 3, False)
+    evs = [t.events for t in traces]
+    t_end = max(int(e["start_ts"].max()) for e in evs) + 1
+    t0 = min(int(e["start_ts"].min()) for e in evs)
+    first = t0 + (t_end - t0) // 5  # calibration window: the first push discovers the anchors
+    anchors = _calibration_anchors(rt, traces, first)
+    ref, models = _whole_trace_reference(rt, traces, anchors)
+    step = int(23e6)
+    bounds = [t0] + list(range(first, t_end, step)) + [t_end]
+    got = {}
+    for native in (False, True):
+        an = rt.Analyzer(0)
+        evs, wl2, _, _ = _setup(rt, an, traces)  # payloads remapped into the merged table
+        for i, m in enumerate(models):
+            an.load_model(m, i)
+        st = an.stream()
+        alerts = []
+        for k, (lo, hi) in enumerate(zip(bounds[:-1], bounds[1:])):  # noqa: B007
+            batch = []
+            for e in evs:
+                a, b = np.searchsorted(e["start_ts"], [lo, hi], side="left")
+                batch.append(e[a:b])
+            if native:
+                alerts.append(st.push_native(batch, wl2 if k == 0 else None))
+            else:
+                res = st.push(batch, wl2)
+                alerts += [r.alerts for r in res if r.summary.status == 0]
+        st.close()
+        an.close()
+        got[native] = np.concatenate(alerts)
+    key = lambda a: sorted(zip(a["cycle"].tolist(), a["ts"].tolist(), a["episode_id"].tolist()))
+    assert key(got[True]) == key(got[False])
+    whole_alerts = np.concatenate([r.alerts for r in ref])
+    assert key(got[True]) == key(whole_alerts)
