@@ -499,6 +499,7 @@ def run_stream(args, rank, world, local_rank):
             lat.append(el * 1e3)
             n_ev += len(ev)
             n_alerts += len(al)
+    phase_ms = {k: round(v, 4) for k, v in an.timings().items()}  # device phases of the last slice
     st.close()
     total_s = sum(lat) / 1e3
     if dist:
@@ -517,6 +518,7 @@ def run_stream(args, rank, world, local_rank):
                        "max": lat_s[-1],
                        "timer": "host wall clock: events on host -> alerts on host"},
         "alerts": n_alerts,
+        "device_phase_ms_last_slice": phase_ms,
     }
     if rank == 0:
         print(json.dumps(line))

@@ -90,6 +90,8 @@ struct cs_ctx {
   // cs_stream_push: carried trailing partial cycle per instance + pinned staging
   std::vector<std::vector<cs_event>> tails;
   cs_event* stage_host = nullptr;
+  void* pin_models = nullptr;  // pinned staging of the per-instance DevModel array
+  size_t pin_models_cap = 0;
   size_t stage_cap = 0;
   std::vector<uint64_t> stage_off;
   DevBuf d_keep;
@@ -331,6 +333,7 @@ void cs_ctx_destroy(cs_ctx* ctx) {
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
   if (ctx->stage_host) cudaFreeHost(ctx->stage_host);
+  if (ctx->pin_models) cudaFreeHost(ctx->pin_models);
   delete ctx;
 }
 
@@ -1052,8 +1055,18 @@ int cs_run(cs_ctx* ctx, uint32_t mask) {
     }
     auto* dm = dev<DevModel>(ctx->d_models, n_inst);
     if (!dm) return fail(ctx, CS_E_CUDA, "cudaMalloc(models)");
-    CS_CUDA(cudaMemcpyAsync(dm, ctx->h_models.data(), n_inst * sizeof(DevModel),
-                            cudaMemcpyHostToDevice, s));
+    // pinned staging: a pageable copy here would stall the host on the stream
+    const size_t mbytes = n_inst * sizeof(DevModel);
+    if (mbytes > ctx->pin_models_cap) {
+      if (ctx->pin_models) cudaFreeHost(ctx->pin_models);
+      ctx->pin_models = nullptr;
+      ctx->pin_models_cap = 0;
+      if (cudaHostAlloc(&ctx->pin_models, mbytes, cudaHostAllocDefault) != cudaSuccess)
+        return fail(ctx, CS_E_CUDA, "cudaHostAlloc(models)");
+      ctx->pin_models_cap = mbytes;
+    }
+    std::memcpy(ctx->pin_models, ctx->h_models.data(), mbytes);
+    CS_CUDA(cudaMemcpyAsync(dm, ctx->pin_models, mbytes, cudaMemcpyHostToDevice, s));
     b = make_buffers(ctx);
     if (!dev<uint64_t>(ctx->block_tmp, rec_cap / 1024 + 16))
       return fail(ctx, CS_E_CUDA, "cudaMalloc(block_tmp)");

@@ -1027,6 +1027,7 @@ __global__ void __launch_bounds__(kScoreThreads)
   const double eps = cfg.ctl.epsilon;
   const int lat = cfg.cyc.latency_phase;
   const int P = cfg.cyc.n_phases;
+  const void* staged = nullptr;
   u64 r = r0;
   while (r < r1) {
     if (threadIdx.x == 0) s_inst = upper_bound_u64(b.rec_off, b.n_inst + 1, r) - 1;
@@ -1043,9 +1044,12 @@ __global__ void __launch_bounds__(kScoreThreads)
       i64* st = reinterpret_cast<i64*>(s_model);
       double* sl = reinterpret_cast<double*>(st + (u64)NT * ni);
       uint8_t* sf = reinterpret_cast<uint8_t*>(sl + (u64)NT * nl);
-      for (u64 i = threadIdx.x; i < (u64)NT * ni; i += blockDim.x) st[i] = m.thr_i[i];
-      for (u64 i = threadIdx.x; i < (u64)NT * nl; i += blockDim.x) sl[i] = m.leaf[i];
-      for (u64 i = threadIdx.x; i < (u64)NT * ni; i += blockDim.x) sf[i] = m.feat[i];
+      if (m.thr_i != staged) {  // instances sharing a model reuse the staged copy
+        for (u64 i = threadIdx.x; i < (u64)NT * ni; i += blockDim.x) st[i] = m.thr_i[i];
+        for (u64 i = threadIdx.x; i < (u64)NT * nl; i += blockDim.x) sl[i] = m.leaf[i];
+        for (u64 i = threadIdx.x; i < (u64)NT * ni; i += blockDim.x) sf[i] = m.feat[i];
+        staged = m.thr_i;
+      }
       thr = st;
       leaf = sl;
       feat = sf;
@@ -1199,6 +1203,50 @@ __device__ __forceinline__ uint32_t count_less(const double* __restrict__ t, uin
   return lo;
 }
 
+// One record through the compiled cell table: latency target (cycles.cpp:
+// 384-390), features (baseline.cpp:61-62), prediction (gbdt.cpp:173-184),
+// ppe (detector.cpp:14-19).
+__device__ __forceinline__ void score_one_lut(const DevBuffers& b, const DevConfig& cfg,
+                                              const DevModel& m, uint32_t inst, u64 rb, u64 k,
+                                              const double* t0, const double* t1) {
+  const double eps = cfg.ctl.epsilon;
+  const int lat = cfg.cyc.latency_phase;
+  const int P = cfg.cyc.n_phases;
+  const uint32_t n0 = m.lut_n[0], n1 = m.lut_n[1];
+  const int f0 = m.feature_ids[0], f1 = m.n_features > 1 ? m.feature_ids[1] : -1;
+  const u64 g = b.rec_cycle[k];
+  const cs_workload w = b.wl[b.c_wl[g]];
+  i64 target = b.c_end[g] - b.c_start[g];
+  if (lat >= 0) {
+    const i64 c = b.c_comp[g * P + lat];
+    if (c > 0) target = c;
+  }
+  const double y = __dmul_rn((double)target, 1e-9);  // cycles.cpp:390
+  const uint8_t stage = b.c_stage[g];
+  auto fval = [&](int id) -> double {
+    switch (id) {
+      case CS_F_BATCH: return (double)w.batch;
+      case CS_F_W_KV: return (double)(w.batch * (w.input_len + w.output_len));
+      case CS_F_INPUT_LEN: return (double)w.input_len;
+      case CS_F_OUTPUT_LEN: return (double)w.output_len;
+      default: return stage == CS_STAGE_PREFILL ? 1.0 : 0.0;
+    }
+  };
+  const uint32_t k0 = count_less(t0, n0, fval(f0));
+  const uint32_t k1 = f1 >= 0 ? count_less(t1, n1, fval(f1)) : 0;
+  const double p = m.lut[(u64)k1 * (n0 + 1) + k0];
+  double res;
+  if (!(y > 0.0)) {
+    atomicMin(reinterpret_cast<u64*>(&b.inst[inst].first_bad_record), (u64)(k - rb));
+    res = __longlong_as_double(0x7ff8000000000000ll);
+  } else {
+    const double q = __ddiv_rn(__dsub_rn(y, p), __dadd_rn(y, eps));
+    res = 0.0 < q ? q : 0.0;
+  }
+  b.rec_pred[k] = p;
+  b.rec_resid[k] = res;
+}
+
 constexpr int kLutThreads = 256;
 constexpr int kLutTile = 2048;  // records per CTA (>= 10 CTAs per SM at configs[1])
 
@@ -1212,6 +1260,7 @@ __global__ void __launch_bounds__(kLutThreads)
   const double eps = cfg.ctl.epsilon;
   const int lat = cfg.cyc.latency_phase;
   const int P = cfg.cyc.n_phases;
+  const void* staged = nullptr;
   u64 r = r0;
   while (r < r1) {
     if (threadIdx.x == 0) s_inst = upper_bound_u64(b.rec_off, b.n_inst + 1, r) - 1;
@@ -1224,50 +1273,35 @@ __global__ void __launch_bounds__(kLutThreads)
     const double* t1 = m.lut_thr[1];
     if ((u64)(n0 + n1) * 8 <= smem_cap) {
       double* s0 = reinterpret_cast<double*>(s_thr);
-      for (uint32_t i = threadIdx.x; i < n0; i += blockDim.x) s0[i] = t0[i];
-      for (uint32_t i = threadIdx.x; i < n1; i += blockDim.x) s0[n0 + i] = t1[i];
+      if (m.lut_thr[0] != staged) {  // instances sharing a model reuse the staged copy
+        for (uint32_t i = threadIdx.x; i < n0; i += blockDim.x) s0[i] = t0[i];
+        for (uint32_t i = threadIdx.x; i < n1; i += blockDim.x) s0[n0 + i] = t1[i];
+        staged = m.lut_thr[0];
+      }
       t0 = s0;
       t1 = s0 + n0;
     }
     __syncthreads();
     const u64 rb = b.rec_off[inst];
     const int f0 = m.feature_ids[0], f1 = m.n_features > 1 ? m.feature_ids[1] : -1;
-    for (u64 k = r + threadIdx.x; k < seg_end; k += blockDim.x) {
-      const u64 g = b.rec_cycle[k];
-      const cs_workload w = b.wl[b.c_wl[g]];
-      i64 target = b.c_end[g] - b.c_start[g];
-      if (lat >= 0) {
-        const i64 c = b.c_comp[g * P + lat];
-        if (c > 0) target = c;
-      }
-      const double y = __dmul_rn((double)target, 1e-9);  // cycles.cpp:390
-      const uint8_t stage = b.c_stage[g];
-      auto fval = [&](int id) -> double {
-        switch (id) {
-          case CS_F_BATCH: return (double)w.batch;
-          case CS_F_W_KV: return (double)(w.batch * (w.input_len + w.output_len));
-          case CS_F_INPUT_LEN: return (double)w.input_len;
-          case CS_F_OUTPUT_LEN: return (double)w.output_len;
-          default: return stage == CS_STAGE_PREFILL ? 1.0 : 0.0;
-        }
-      };
-      const uint32_t k0 = count_less(t0, n0, fval(f0));
-      const uint32_t k1 = f1 >= 0 ? count_less(t1, n1, fval(f1)) : 0;
-      const double p = m.lut[(u64)k1 * (n0 + 1) + k0];
-      double res;
-      if (!(y > 0.0)) {
-        atomicMin(reinterpret_cast<u64*>(&b.inst[inst].first_bad_record), (u64)(k - rb));
-        res = __longlong_as_double(0x7ff8000000000000ll);
-      } else {
-        const double q = __ddiv_rn(__dsub_rn(y, p), __dadd_rn(y, eps));
-        res = 0.0 < q ? q : 0.0;
-      }
-      b.rec_pred[k] = p;
-      b.rec_resid[k] = res;
-    }
+    for (u64 k = r + threadIdx.x; k < seg_end; k += blockDim.x)
+      score_one_lut(b, cfg, m, inst, rb, k, t0, t1);
     __syncthreads();
     r = seg_end;
   }
+}
+
+
+// Fleets with few records per instance: thread per record, its instance by
+// binary search (independent across threads), thresholds read through L1.
+__global__ void __launch_bounds__(kLutThreads)
+    k_score_lut_flat(DevBuffers b, DevConfig cfg, uint64_t n_records) {
+  n_records = records_on_device(b, n_records);
+  const u64 k = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n_records) return;
+  const uint32_t inst = upper_bound_u64(b.rec_off, b.n_inst + 1, k) - 1;
+  const DevModel& m = b.models[inst];
+  score_one_lut(b, cfg, m, inst, b.rec_off[inst], k, m.lut_thr[0], m.lut_thr[1]);
 }
 
 // ------------------------------------------------------------ K7 detect
@@ -1411,15 +1445,21 @@ void launch_stream_update(const DevBuffers& b, const DevConfig& cfg, StreamCarry
   k_stream_update<<<(b.n_inst + 63) / 64, 64, 0, s>>>(b, cfg, out, detected);
 }
 
-__global__ void k_alert_off(DevBuffers b) {
-  // exclusive scan over instances of n_alerts (n_inst is small: one CTA)
-  if (threadIdx.x == 0) {
-    u64 acc = 0;
-    for (uint32_t i = 0; i < b.n_inst; ++i) {
-      b.alert_off[i] = acc;
-      acc += b.inst[i].n_alerts;
-    }
-    b.alert_off[b.n_inst] = acc;
+// exclusive scan over instances of n_alerts: one CTA, kScanItems per thread per round
+__global__ void __launch_bounds__(1024) k_alert_off(DevBuffers b) {
+  __shared__ u64 s_w[32];
+  __shared__ u64 s_carry;
+  if (threadIdx.x == 0) s_carry = 0;
+  __syncthreads();
+  for (uint32_t base = 0; base <= b.n_inst; base += blockDim.x) {
+    const uint32_t i = base + threadIdx.x;
+    const u64 x = i < b.n_inst ? b.inst[i].n_alerts : 0;
+    u64 t;
+    const u64 incl = block_incl_scan(x, s_w, &t);
+    if (i <= b.n_inst) b.alert_off[i] = s_carry + incl - x;
+    __syncthreads();
+    if (threadIdx.x == 0) s_carry += t;
+    __syncthreads();
   }
 }
 
@@ -2781,6 +2821,12 @@ void launch_score(const DevBuffers& b, const DevConfig& cfg, uint64_t n_records,
     if (nl > need_lut) need_lut = nl;
     if (h_models[i].smem_bytes > need) need = h_models[i].smem_bytes;
   }
+  if (all_lut && n_records < (u64)b.n_inst * 512) {  // short instance segments
+    k_score_lut_flat<<<(unsigned)((n_records + kLutThreads - 1) / kLutThreads), kLutThreads, 0, s>>>(
+        b, cfg, n_records);
+    ++*launches;
+    return;
+  }
   if (all_lut) {
     uint64_t cap = (uint64_t)max_optin - 1024;
     if (need_lut < cap) cap = need_lut;
@@ -2826,7 +2872,7 @@ void launch_detect(const DevBuffers& b, const DevConfig& cfg, uint64_t n_records
   }
   k_scan_exclusive<<<1, 1024, 0, s>>>(b.block_tmp, nb, b.block_tmp + nb);
   ++*launches;
-  k_alert_off<<<1, 32, 0, s>>>(b);
+  k_alert_off<<<1, 1024, 0, s>>>(b);
   ++*launches;
   if (nb) {
     k_detect_scatter<<<(unsigned)nb, kDetBlock, 0, s>>>(b, n_records);
