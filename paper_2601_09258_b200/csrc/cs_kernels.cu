@@ -1,7 +1,7 @@
 // cs_kernels.cu — hand-written sm_100a kernels of the trace-analysis hot path.
 //
 // Data flow (one cs_run over a batch of instances):
-//   K1s  k_scan_warp<sample>     name moments over the first 1 Mi events of each
+//   K1s  k_scan_warp<sample>     name moments over the first 256 Ki events of each
 //                                instance -> speculative anchor guess
 //   K1r  k_rank                  exact-moment anchor ranking (cycles.cpp:47-110)
 //   K12  k_scan_warp             ONE pass over all events, warp per tile: exact
