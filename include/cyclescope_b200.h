@@ -106,7 +106,8 @@ typedef struct cs_name_info {
   uint32_t flags;      /* CS_NAME_* */
   int32_t phase;       /* index into CycleConfig::phase_functions, -1 none */
   int32_t beta_slot;   /* dense class slot for stage attribution, -1 none  */
-  uint32_t reserved;
+  uint32_t metric;     /* 1 + name id of the counter series MetricMap maps this
+                          class to (rca.cpp:55-69, RunConfig metric_map); 0 none */
 } cs_name_info;
 #define CS_NAME_PREFILL_KW 0x1u /* name contains a prefill keyword (174-179) */
 #define CS_NAME_DECODE_KW  0x2u /* name contains a decode keyword            */
@@ -256,6 +257,9 @@ typedef struct cs_ctx cs_ctx;
 #define CS_RUN_SCORE     0x4u  /* GBDT predict + ppe                     */
 #define CS_RUN_DETECT    0x8u  /* control chart + alerts                 */
 #define CS_RUN_ALL       0xFu
+#define CS_RUN_MU        0x10u /* counter-weighted mu per (cycle, class):
+                                  cycle_stats with a CounterTable
+                                  (rca.cpp:97-106, 123-126); implies BETA  */
 
 int cs_abi_version(void);
 const char* cs_status_type(int status);
@@ -351,6 +355,12 @@ int cs_get_beta(cs_ctx* ctx, uint32_t inst, int64_t* totals, double* beta,
  * presence mask: n_cycles x n_comm_slots uint8 */
 int cs_get_collective_beta(cs_ctx* ctx, uint32_t inst, double* beta,
                            uint8_t* present, size_t cap, size_t* n);
+/* Counter-weighted mean per (cycle, class slot) (CS_RUN_MU): for every Span of
+ * the class with duration > 0 and positive clipped overlap whose class maps
+ * to a counter series of the instance, interpolate_mean over [start,
+ * clipped end) (rca.cpp:17-53) weighted by the overlap, divided by the class
+ * total (ClassStat::mu); has[k] = 0 where the reference leaves mu unset. */
+int cs_get_mu(cs_ctx* ctx, uint32_t inst, double* mu, uint8_t* has, size_t cap, size_t* n);
 int cs_get_records(cs_ctx* ctx, uint32_t inst, cs_record* buf, size_t cap, size_t* n);
 int cs_get_alerts(cs_ctx* ctx, uint32_t inst, cs_alert* buf, size_t cap, size_t* n);
 

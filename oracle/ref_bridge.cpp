@@ -64,6 +64,8 @@ struct Results {
   std::vector<int64_t> beta_totals; // n_cycles x n_slots
   std::vector<double> beta;
   std::vector<double> coll_beta;    // n_cycles x n_comm
+  std::vector<double> mu;           // n_cycles x n_slots (do_beta & 2: CounterTable)
+  std::vector<uint8_t> mu_has;
   std::vector<uint8_t> coll_present;
   std::vector<cs_record> records;
   std::vector<cs_alert> alerts;
@@ -266,13 +268,24 @@ void run_reference(Handle& h, const RunConfig& config, const char* model_json,
     R.beta.assign(cycles.size() * ns, 0.0);
     R.coll_beta.assign(cycles.size() * nc, 0.0);
     R.coll_present.assign(cycles.size() * nc, 0);
-    const CounterTable no_counters;
-    const MetricMap no_metrics;
+    // do_beta & 2: the mu branch too, with the trace's CounterTable and the
+    // RunConfig metric map (cmd_diagnose, main.cpp:285-293)
+    const bool with_mu = (do_beta & 2) != 0;
+    const CounterTable counters = with_mu ? CounterTable::from_trace(trace) : CounterTable{};
+    const MetricMap metrics = with_mu ? config.metric_map : MetricMap{};
+    if (with_mu) {
+      R.mu.assign(cycles.size() * ns, 0.0);
+      R.mu_has.assign(cycles.size() * ns, 0);
+    }
     for (size_t ci = 0; ci < cycles.size(); ++ci) {
-      const auto st = cycle_stats(cycles[ci], trace, no_counters, no_metrics);
+      const auto st = cycle_stats(cycles[ci], trace, counters, metrics);
       for (const auto& [name, cs] : st.classes) {
         R.beta_totals[ci * ns + beta_slot[name]] = cs.total_duration;
         R.beta[ci * ns + beta_slot[name]] = cs.beta;
+        if (with_mu && cs.mu) {
+          R.mu[ci * ns + beta_slot[name]] = *cs.mu;
+          R.mu_has[ci * ns + beta_slot[name]] = 1;
+        }
       }
       for (const auto& [key, b] : st.collective_rank_beta) {
         const int s = comm_slot[key];
@@ -590,6 +603,11 @@ int ref_get_beta(void* hv, int64_t* totals, double* beta, size_t cap, size_t* n)
   auto* h = static_cast<Handle*>(hv);
   if (copy_out(h->res.beta_totals, totals, cap, n)) return 1;
   return copy_out(h->res.beta, beta, cap, n);
+}
+int ref_get_mu(void* hv, double* mu, uint8_t* has, size_t cap, size_t* n) {
+  auto* h = static_cast<Handle*>(hv);
+  if (copy_out(h->res.mu, mu, cap, n)) return 1;
+  return copy_out(h->res.mu_has, has, cap, n);
 }
 int ref_get_collective_beta(void* hv, double* beta, uint8_t* present, size_t cap, size_t* n) {
   auto* h = static_cast<Handle*>(hv);

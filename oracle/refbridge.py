@@ -63,6 +63,7 @@ def lib():
         L.ref_get_comm.argtypes = [vp, vp, vp, vp, sz, C.POINTER(sz), C.POINTER(C.c_uint32)]
         L.ref_get_beta.argtypes = [vp, vp, vp, sz, C.POINTER(sz)]
         L.ref_get_collective_beta.argtypes = [vp, vp, vp, sz, C.POINTER(sz)]
+        L.ref_get_mu.argtypes = [vp, vp, vp, sz, C.POINTER(sz)]
         L.ref_fit.argtypes = [C.c_uint64, C.c_uint32, C.c_char_p, vp, vp, vp, vp, vp, sz,
                               C.POINTER(sz), C.c_char_p, sz]
         L.ref_cpu_prepare.restype = vp
@@ -213,10 +214,12 @@ class RefTrace:
                         [h.decode() for h in hashes])
 
     def run(self, run_config: dict | None = None, model_json: str | None = None,
-            train_cycles: int = 2400, beta: bool = True) -> RefResult:
+            train_cycles: int = 2400, beta: bool = True, mu: bool = False) -> RefResult:
+        """mu=True: cycle_stats with the trace's CounterTable (O(cycles x samples)
+        in the reference: keep traces small)."""
         L = lib()
         L.ref_run(self.h, json.dumps(run_config or {}).encode(),
-                  (model_json or "").encode(), train_cycles, int(beta))
+                  (model_json or "").encode(), train_cycles, int(beta) | (2 if mu else 0))
         tb, mb = C.create_string_buffer(256), C.create_string_buffer(4096)
         status = L.ref_status(self.h, tb, 256, mb, 4096)
         ab, fb = C.create_string_buffer(4096), C.c_int(0)
@@ -233,6 +236,11 @@ class RefTrace:
         if n.value:
             L.ref_get_collective_beta(self.h, cbeta.ctypes.data, cpres.ctypes.data, n.value,
                                       C.byref(n))
+        L.ref_get_mu(self.h, None, None, 0, C.byref(n))
+        mu_v = np.zeros(n.value, np.float64)
+        mu_h = np.zeros(n.value, np.uint8)
+        if n.value:
+            L.ref_get_mu(self.h, mu_v.ctypes.data, mu_h.ctypes.data, n.value, C.byref(n))
         mj = _get(L.ref_get_model_json, self.h, np.uint8)
         nd = _get(L.ref_get_ndjson, self.h, np.uint8)
         return RefResult(
@@ -247,7 +255,8 @@ class RefTrace:
             model_json=bytes(mj[:-1]).decode() if len(mj) else "",
             ucl=L.ref_ucl(self.h), first_bad_record=int(L.ref_first_bad_record(self.h)),
             seconds=L.ref_seconds(self.h),
-            extra={"ndjson": bytes(nd[:-1]).decode() if len(nd) else ""})
+            extra={"ndjson": bytes(nd[:-1]).decode() if len(nd) else "", "mu": mu_v,
+                   "mu_has": mu_h})
 
 
 def ref_fit(x: np.ndarray, y: np.ndarray, feature_names, params=None, options=None) -> str:

@@ -24,7 +24,7 @@ WIRE_ESCAPE = 0x80
 
 WORKLOAD_DTYPE = np.dtype([("batch", "<i8"), ("input_len", "<i8"), ("output_len", "<i8")])
 NAME_INFO_DTYPE = np.dtype(
-    [("flags", "<u4"), ("phase", "<i4"), ("beta_slot", "<i4"), ("reserved", "<u4")])
+    [("flags", "<u4"), ("phase", "<i4"), ("beta_slot", "<i4"), ("metric", "<u4")])
 
 CYCLE_DTYPE = np.dtype(
     [("index", "<u8"), ("start_ts", "<i8"), ("end_ts", "<i8"), ("anchor_pos", "<u8"),
@@ -61,6 +61,7 @@ FEATURE_IDS = {"batch": F_BATCH, "w_kv": F_W_KV, "input_len": F_INPUT_LEN,
                "output_len": F_OUTPUT_LEN, "stage": F_STAGE}
 
 RUN_SEGMENT, RUN_BETA, RUN_SCORE, RUN_DETECT, RUN_ALL = 0x1, 0x2, 0x4, 0x8, 0xF
+RUN_MU = 0x10  # counter-weighted mu (cycle_stats with a CounterTable)
 
 STATUS_TYPES = {
     0: "ok", 1: "invalid_argument", 2: "no_device", 3: "cuda_error",

@@ -87,6 +87,9 @@ struct cs_ctx {
   std::vector<uint64_t> tile_begin, tile_end;
   DevBuf d_tile_inst, d_tile_begin, d_tile_end, d_inst_first_tile, d_tile_cnt, d_tile_pref;
   DevBuf d_scan_tmp;
+  // counter-weighted mu: metric slots derived from the name table
+  uint32_t n_metrics = 0;
+  DevBuf d_series_slot, d_class_metric, d_m_off, d_s_ts, d_s_val, d_mu, d_mu_has;
   // cs_stream_push: carried trailing partial cycle per instance + pinned staging
   std::vector<std::vector<cs_event>> tails;
   cs_event* stage_host = nullptr;
@@ -228,6 +231,14 @@ DevBuffers make_buffers(cs_ctx* ctx) {
   b.alert_off = static_cast<uint64_t*>(ctx->d_alert_off.p);
   b.block_tmp = static_cast<uint64_t*>(ctx->block_tmp.p);
   b.models = static_cast<const DevModel*>(ctx->d_models.p);
+  b.series_slot = static_cast<const int8_t*>(ctx->d_series_slot.p);
+  b.class_metric = static_cast<const int8_t*>(ctx->d_class_metric.p);
+  b.n_metrics = ctx->n_metrics;
+  b.m_off = static_cast<uint64_t*>(ctx->d_m_off.p);
+  b.s_ts = static_cast<int64_t*>(ctx->d_s_ts.p);
+  b.s_val = static_cast<double*>(ctx->d_s_val.p);
+  b.c_mu = static_cast<double*>(ctx->d_mu.p);
+  b.c_mu_has = static_cast<uint8_t*>(ctx->d_mu_has.p);
   b.stream = ctx->streaming ? static_cast<StreamCarry*>(ctx->d_stream[ctx->stream_cur].p) : nullptr;
   return b;
 }
@@ -378,6 +389,28 @@ int cs_set_name_table(cs_ctx* ctx, uint32_t n_names, const cs_name_info* names) 
   if (!d) return fail(ctx, CS_E_CUDA, "cudaMalloc(names)");
   if (n_names) CS_CUDA(cudaMemcpyAsync(d, names, n_names * sizeof(cs_name_info),
                                        cudaMemcpyHostToDevice, ctx->stream));
+  // metric slots for the counter-weighted mu: one per counter name a class maps to
+  std::vector<int8_t> series(std::max<uint32_t>(1, n_names), -1), cls(std::max<uint32_t>(1, n_names), -1);
+  std::map<uint32_t, int> slot_of;
+  for (uint32_t i = 0; i < n_names; ++i) {
+    const uint32_t m = names[i].metric;
+    if (m == 0) continue;
+    if (m > n_names) return fail(ctx, CS_E_INVALID_ARGUMENT, "metric name id out of range");
+    auto it = slot_of.find(m - 1);
+    if (it == slot_of.end()) {
+      if (slot_of.size() >= static_cast<size_t>(kMaxMetrics))
+        return fail(ctx, CS_E_UNSUPPORTED, "at most 16 counter metrics");
+      it = slot_of.emplace(m - 1, static_cast<int>(slot_of.size())).first;
+      series[m - 1] = static_cast<int8_t>(it->second);
+    }
+    cls[i] = static_cast<int8_t>(it->second);
+  }
+  ctx->n_metrics = static_cast<uint32_t>(slot_of.size());
+  void* ds = ctx->d_series_slot.get(series.size());
+  void* dc = ctx->d_class_metric.get(cls.size());
+  if (!ds || !dc) return fail(ctx, CS_E_CUDA, "cudaMalloc(metrics)");
+  CS_CUDA(cudaMemcpy(ds, series.data(), series.size(), cudaMemcpyHostToDevice));
+  CS_CUDA(cudaMemcpy(dc, cls.data(), cls.size(), cudaMemcpyHostToDevice));
   return CS_OK;
 }
 
@@ -692,6 +725,9 @@ extern "C" {
 
 int cs_run(cs_ctx* ctx, uint32_t mask) {
   if (!ctx) return CS_E_INVALID_ARGUMENT;
+  if (mask & CS_RUN_MU) mask |= CS_RUN_BETA;  // mu divides by the class totals
+  if ((mask & CS_RUN_MU) && ctx->streaming)
+    return fail(ctx, CS_E_UNSUPPORTED, "mu needs whole-trace counter series (not per micro-batch)");
   if (!(mask & CS_RUN_SEGMENT)) return fail(ctx, CS_E_INVALID_ARGUMENT, "CS_RUN_SEGMENT required");
   if (ctx->n_inst == 0) return fail(ctx, CS_E_INVALID_ARGUMENT, "nothing uploaded");
   CS_CUDA(cudaSetDevice(ctx->device));
@@ -1010,8 +1046,32 @@ int cs_run(cs_ctx* ctx, uint32_t mask) {
   b = make_buffers(ctx);
   launch_stage_heuristic(b, cfg, s, &ctx->launches);
   launch_records(b, cfg, 0, s, &ctx->launches);
-  const int e6 = record_event(ctx, 6);
-  ctx->timed.push_back({"stage_records", {e5, e6}});
+  const int e6m = record_event(ctx, 6);
+  ctx->timed.push_back({"stage_records", {e5, e6m}});
+  int e6 = e6m;
+  // ---- counter-weighted mu (cycle_stats with a CounterTable, rca.cpp:97-126)
+  if ((mask & CS_RUN_MU) && ctx->n_metrics && nt) {
+    const uint64_t nm = static_cast<uint64_t>(ctx->n_metrics) * nt;
+    if (!dev<uint64_t>(ctx->d_m_off, nm + 1) || !dev<uint64_t>(ctx->d_scan_tmp, nm / 1024 + 2))
+      return fail(ctx, CS_E_CUDA, "cudaMalloc(counter series)");
+    b = make_buffers(ctx);
+    launch_counter_series(b, s, &ctx->launches);
+    uint64_t n_samples = 0;
+    CS_CUDA(cudaMemcpyAsync(&n_samples, static_cast<uint64_t*>(ctx->d_m_off.p) + nm, 8,
+                            cudaMemcpyDeviceToHost, s));
+    CS_CUDA(cudaStreamSynchronize(s));
+    const size_t C = std::max<int32_t>(1, ctx->cyc.n_beta_slots);
+    if (!dev<int64_t>(ctx->d_s_ts, std::max<uint64_t>(1, n_samples)) ||
+        !dev<double>(ctx->d_s_val, std::max<uint64_t>(1, n_samples)) ||
+        !dev<double>(ctx->d_mu, std::max<uint64_t>(1, ctx->n_cycles) * C) ||
+        !dev<uint8_t>(ctx->d_mu_has, std::max<uint64_t>(1, ctx->n_cycles) * C))
+      return fail(ctx, CS_E_CUDA, "cudaMalloc(mu)");
+    b = make_buffers(ctx);
+    launch_counter_scatter(b, s, &ctx->launches);
+    launch_cycle_mu(b, cfg, s, &ctx->launches);
+    e6 = record_event(ctx, 10);
+    ctx->timed.push_back({"mu", {e6m, e6}});
+  }
   // record counts stay on the device: scoring and detection launch over the
   // cycle count as capacity and clamp to rec_off[n_inst] (no host round trip)
   const uint64_t rec_cap = ctx->n_cycles;
@@ -1388,6 +1448,25 @@ int cs_get_collective_beta(cs_ctx* ctx, uint32_t inst, double* beta, uint8_t* pr
                        cudaMemcpyDeviceToHost));
     for (uint64_t k = 0; k < nc * R; ++k) present[k] = present[k] ? 1 : 0;
   }
+  return CS_OK;
+}
+
+int cs_get_mu(cs_ctx* ctx, uint32_t inst, double* mu, uint8_t* has, size_t cap, size_t* n) {
+  if (!ctx || !ctx->ran || inst >= ctx->n_inst) return CS_E_INVALID_ARGUMENT;
+  if (!(ctx->last_mask & CS_RUN_MU)) return fail(ctx, CS_E_INVALID_ARGUMENT, "mu not computed");
+  const uint64_t C = static_cast<uint64_t>(ctx->cyc.n_beta_slots);
+  const uint64_t c0 = ctx->cyc_off[inst], nc = ctx->n_cyc[inst];
+  if (n) *n = nc * C;
+  if (cap < nc * C && (mu || has)) return fail(ctx, CS_E_INVALID_ARGUMENT, "buffer too small");
+  if (!ctx->n_metrics) {  // no class maps to a counter: beta-only entries everywhere
+    if (mu) std::fill(mu, mu + nc * C, 0.0);
+    if (has) std::fill(has, has + nc * C, 0);
+    return CS_OK;
+  }
+  if (mu && nc * C)
+    CS_CUDA(cudaMemcpy(mu, static_cast<double*>(ctx->d_mu.p) + c0 * C, nc * C * 8, cudaMemcpyDeviceToHost));
+  if (has && nc * C)
+    CS_CUDA(cudaMemcpy(has, static_cast<uint8_t*>(ctx->d_mu_has.p) + c0 * C, nc * C, cudaMemcpyDeviceToHost));
   return CS_OK;
 }
 

@@ -7,6 +7,7 @@
 //  * RunConfig JSON (config.cpp:78-188 schema) -> cs_* configs + name table.
 // Compiled with -ffp-contract=off: no FMA, like the reference's objects.
 #include <algorithm>
+#include <map>
 #include <cmath>
 #include <cstring>
 #include <numeric>
@@ -492,6 +493,15 @@ int cs_config_from_json(const char* run_config_json, uint32_t n_names,
       ctl.warmup = d.value("warmup", ctl.warmup);
       ctl.epsilon = d.value("epsilon", ctl.epsilon);
     }
+    // MetricMap (rca.cpp:55-69): event class -> counter metric
+    std::map<std::string, std::string> metric_map = {
+        {"oncpu", "cpu_usage"},           {"gemm_kernel", "gpu_usage"},
+        {"attn_kernel", "gpu_clock"},     {"reduce", "tx_bytes"},
+        {"memcpy_h2d", "pcie_util"},      {"memcpy_d2d", "bus_util"},
+        {"run_batch", "gpu_usage"},       {"process_batch_result", "cpu_usage"},
+        {"get_next_batch_to_run", "cpu_usage"}};
+    if (j.contains("metric_map"))
+      metric_map = j["metric_map"].get<std::map<std::string, std::string>>();
     // dedup phases, first occurrence (component_durations is a map)
     std::vector<std::string> uph;
     for (const auto& p : phases)
@@ -524,6 +534,11 @@ int cs_config_from_json(const char* run_config_json, uint32_t n_names,
       for (const auto& kw : dkw)
         if (nm.find(kw) != std::string::npos) ni.flags |= CS_NAME_DECODE_KW;
       ni.beta_slot = name_is_span[i] ? slot++ : -1;
+      ni.metric = 0;
+      const auto mm = metric_map.find(nm);
+      if (mm != metric_map.end())
+        for (uint32_t k = 0; k < n_names; ++k)
+          if (mm->second == names[k]) ni.metric = k + 1;
       if (!hint.empty() && nm == hint) cyc.anchor_hint_name = i;
     }
     if (!hint.empty() && cyc.anchor_hint_name < 0) cyc.anchor_hint_name = -2;

@@ -146,6 +146,15 @@ struct DevBuffers {
   uint64_t* alert_off;          // n_inst+1
   uint64_t* block_tmp;          // scratch for scans
   const DevModel* models;       // per instance (device array)
+  // counter-weighted mu (CS_RUN_MU)
+  const int8_t* series_slot;    // per name: metric slot of a counter series name, -1
+  const int8_t* class_metric;   // per name: metric slot its class maps to, -1
+  uint32_t n_metrics;
+  uint64_t* m_off;              // [metric][tile] counts, then exclusive offsets (+ total)
+  int64_t* s_ts;                // samples, metric-major, instances in tile order
+  double* s_val;
+  double* c_mu;                 // n_cycles x n_beta
+  uint8_t* c_mu_has;
   StreamCarry* stream;          // per instance, null when not streaming
 };
 
@@ -200,6 +209,10 @@ void launch_wire_expand(const cs_wire_event* w, const int64_t* base, const doubl
                         const cs_event* esc, const uint64_t* tile_begin, const uint64_t* tile_end,
                         uint32_t n_tiles, cs_event* out, cudaStream_t s);
 void launch_stream_keep(const DevBuffers& b, uint64_t* keep, cudaStream_t s);
+void launch_counter_series(const DevBuffers& b, cudaStream_t s, uint64_t* launches);
+void launch_counter_scatter(const DevBuffers& b, cudaStream_t s, uint64_t* launches);
+void launch_cycle_mu(const DevBuffers& b, const DevConfig& cfg, cudaStream_t s, uint64_t* launches);
+constexpr int kMaxMetrics = 16;
 void launch_lut_build(const uint8_t* feat, const int32_t* rank, const double* leafp,
                       uint32_t n_trees, uint32_t D, double base, double floor_, uint32_t n0,
                       uint64_t cells, double* lut, cudaStream_t s);

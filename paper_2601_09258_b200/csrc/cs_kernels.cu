@@ -2717,6 +2717,177 @@ void launch_stream_keep(const DevBuffers& b, uint64_t* keep, cudaStream_t s) {
   if (b.n_inst) k_stream_keep<<<(b.n_inst + 127) / 128, 128, 0, s>>>(b, keep);
 }
 
+// ------------------------------------------- counter-weighted mu (§8f #1)
+// CounterTable::from_trace (trace.cpp:111-131): per (instance, metric) the
+// Counter events with a numeric value, stable-sorted by ts = their canonical
+// event order.  Compacted here by metric: k_counter_count counts per (metric,
+// tile), an exclusive scan over [metric][tile] gives offsets, and
+// k_counter_scatter writes (ts, value) in event order.  Instance i's series
+// for metric m is [m_off[m*nt + first_tile(i)], m_off[m*nt + first_tile(i+1)]).
+__device__ __forceinline__ int counter_slot(const DevBuffers& b, const Ev8& e) {
+  const uint32_t kc = (uint32_t)(e.c >> 32);
+  if ((kc & 0xffu) != CS_COUNTER || !((kc >> 16) & CS_EV_HAS_VALUE)) return -1;
+  const uint32_t name = (uint32_t)e.c;
+  return name < b.n_names ? (int)b.series_slot[name] : -1;
+}
+
+__global__ void __launch_bounds__(256) k_counter_count(DevBuffers b) {
+  __shared__ uint32_t s_cnt[8][kMaxMetrics];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const u64 t = (u64)blockIdx.x * 8 + warp;
+  if (lane < kMaxMetrics) s_cnt[warp][lane] = 0;
+  __syncwarp();
+  if (t >= b.n_tiles) return;
+  const u64 tb = b.tile_begin[t], te = b.tile_end[t];
+  for (u64 j0 = tb; j0 < te; j0 += 32) {
+    const u64 j = j0 + lane;
+    const int m = j < te ? counter_slot(b, ldg256(b.ev + j)) : -1;
+    const uint32_t grp = __match_any_sync(0xffffffffu, m);
+    if (m >= 0 && lane == __ffs(grp) - 1) s_cnt[warp][m] += __popc(grp);
+    __syncwarp();
+  }
+  if (lane < (int)b.n_metrics) b.m_off[(u64)lane * b.n_tiles + t] = s_cnt[warp][lane];
+}
+
+__global__ void __launch_bounds__(256) k_counter_scatter(DevBuffers b) {
+  __shared__ uint32_t s_run[8][kMaxMetrics];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const u64 t = (u64)blockIdx.x * 8 + warp;
+  if (lane < kMaxMetrics) s_run[warp][lane] = 0;
+  __syncwarp();
+  if (t >= b.n_tiles) return;
+  const u64 tb = b.tile_begin[t], te = b.tile_end[t];
+  for (u64 j0 = tb; j0 < te; j0 += 32) {
+    const u64 j = j0 + lane;
+    Ev8 e{};
+    int m = -1;
+    if (j < te) {
+      e = ldg256(b.ev + j);
+      m = counter_slot(b, e);
+    }
+    const uint32_t grp = __match_any_sync(0xffffffffu, m);
+    if (m >= 0) {
+      const u64 pos = b.m_off[(u64)m * b.n_tiles + t] + s_run[warp][m] + __popc(grp & lanemask_lt());
+      b.s_ts[pos] = (i64)e.a;
+      b.s_val[pos] = __longlong_as_double((long long)e.b);  // the f64 `value` (cs_event.duration)
+    }
+    __syncwarp();
+    if (m >= 0 && lane == __ffs(grp) - 1) s_run[warp][m] += __popc(grp);
+    __syncwarp();
+  }
+}
+
+// interpolate_mean (rca.cpp:17-53), operation for operation: knots t0, the
+// sample timestamps strictly inside (t0, t1), t1; trapezoids summed in knot
+// order; value_at by lower_bound over the samples' double timestamps.
+__device__ double interpolate_mean_dev(const int64_t* __restrict__ ts, const double* __restrict__ val,
+                                       u64 n, i64 t0i, i64 t1i) {
+  const double t0 = (double)t0i, t1 = (double)t1i;
+  auto lower = [&](double t) -> u64 {  // first sample with (double)ts >= t
+    u64 lo = 0, hi = n;
+    while (lo < hi) {
+      const u64 mid = (lo + hi) >> 1;
+      if ((double)ts[mid] < t) lo = mid + 1;
+      else hi = mid;
+    }
+    return lo;
+  };
+  auto value_at = [&](double t) -> double {
+    if (t <= (double)ts[0]) return val[0];
+    if (t >= (double)ts[n - 1]) return val[n - 1];
+    const u64 h = lower(t);
+    const double f = __ddiv_rn(__dsub_rn(t, (double)ts[h - 1]), (double)(ts[h] - ts[h - 1]));
+    return __dadd_rn(val[h - 1], __dmul_rn(f, __dsub_rn(val[h], val[h - 1])));
+  };
+  // interior knots: samples with t0 < (double)ts < t1, a contiguous range
+  u64 k0 = 0, hi = n;
+  while (k0 < hi) {  // first with (double)ts > t0
+    const u64 mid = (k0 + hi) >> 1;
+    if ((double)ts[mid] <= t0) k0 = mid + 1;
+    else hi = mid;
+  }
+  const u64 k1 = lower(t1);
+  double integral = 0.0, a = t0, va = value_at(t0);
+  for (u64 i = k0; i < k1; ++i) {
+    const double kt = (double)ts[i], vb = value_at(kt);
+    integral = __dadd_rn(integral, __dmul_rn(__dmul_rn(0.5, __dadd_rn(va, vb)), __dsub_rn(kt, a)));
+    a = kt;
+    va = vb;
+  }
+  const double vb = value_at(t1);
+  integral = __dadd_rn(integral, __dmul_rn(__dmul_rn(0.5, __dadd_rn(va, vb)), __dsub_rn(t1, a)));
+  return __ddiv_rn(integral, __dsub_rn(t1, t0));
+}
+
+// cycle_stats' mu branch (rca.cpp:97-106, 123-126), one thread per cycle in
+// event order: weighted_mu[class] += interpolate_mean(series, start,
+// clipped_end) * overlap; mu = weighted_mu / total overlap (the beta totals).
+__global__ void __launch_bounds__(256) k_cycle_mu(DevBuffers b, DevConfig cfg) {
+  extern __shared__ __align__(16) unsigned char s_mu[];
+  const int C = cfg.cyc.n_beta_slots;
+  const uint32_t NT = blockDim.x, tid = threadIdx.x;
+  double* acc = reinterpret_cast<double*>(s_mu);  // [C][NT]
+  const u64 g = (u64)blockIdx.x * NT + tid;
+  if (g >= b.n_cycles) return;
+  const i64 cs = b.c_start[g], ce = b.c_end[g];
+  const i64 dur = ce - cs;
+  const u64 first = b.c_first[g], last = b.c_last[g];
+  const uint32_t inst = b.c_inst[g];
+  const uint32_t ft = b.inst_first_tile[inst];
+  const uint32_t lt = inst + 1 < b.n_inst ? b.inst_first_tile[inst + 1] : b.n_tiles;
+  for (int c = 0; c < C; ++c) acc[c * NT + tid] = 0.0;
+  u64 has = 0;
+  if (dur > 0) {  // cycle_stats returns empty stats otherwise (rca.cpp:77)
+    for (u64 j = first; j < last; ++j) {
+      const Ev8 e = ldg256(b.ev + j);
+      const uint32_t kc = (uint32_t)(e.c >> 32);
+      const i64 st = (i64)e.a, d = (i64)e.b;
+      if ((kc & 0xffu) != CS_SPAN || d <= 0) continue;
+      const i64 end = st + d;
+      const i64 clipped = (end < ce ? end : ce) - st;
+      if (clipped <= 0) continue;
+      const uint32_t name = (uint32_t)e.c;
+      const int m = b.class_metric[name];
+      const int bs = b.names[name].beta_slot;
+      if (m < 0 || bs < 0 || bs >= C) continue;
+      const u64 lo = b.m_off[(u64)m * b.n_tiles + ft], hi = b.m_off[(u64)m * b.n_tiles + lt];
+      if (hi <= lo) continue;  // counters.find(metric) == nullptr: beta-only entry
+      const double mu = interpolate_mean_dev(b.s_ts + lo, b.s_val + lo, hi - lo, st, st + clipped);
+      acc[bs * NT + tid] = __dadd_rn(acc[bs * NT + tid], __dmul_rn(mu, (double)clipped));
+      has |= 1ull << bs;
+    }
+  }
+  for (int c = 0; c < C; ++c) {
+    const i64 tot = b.c_beta_tot[g * C + c];
+    const bool h = ((has >> c) & 1ull) && tot > 0;
+    b.c_mu[g * C + c] = h ? __ddiv_rn(acc[c * NT + tid], (double)tot) : 0.0;
+    b.c_mu_has[g * C + c] = h ? 1 : 0;
+  }
+}
+
+void launch_counter_series(const DevBuffers& b, cudaStream_t s, uint64_t* launches) {
+  if (!b.n_tiles || !b.n_metrics) return;
+  k_counter_count<<<(unsigned)((b.n_tiles + 7) / 8), 256, 0, s>>>(b);
+  const u64 n = (u64)b.n_metrics * b.n_tiles;
+  launch_exclusive_scan(b.m_off, n, b.m_off + n, b.scan_tmp, s, launches);
+  ++*launches;
+}
+void launch_counter_scatter(const DevBuffers& b, cudaStream_t s, uint64_t* launches) {
+  if (!b.n_tiles || !b.n_metrics) return;
+  k_counter_scatter<<<(unsigned)((b.n_tiles + 7) / 8), 256, 0, s>>>(b);
+  ++*launches;
+}
+void launch_cycle_mu(const DevBuffers& b, const DevConfig& cfg, cudaStream_t s, uint64_t* launches) {
+  if (!b.n_cycles) return;
+  int nt = 256;
+  const int C = cfg.cyc.n_beta_slots > 0 ? cfg.cyc.n_beta_slots : 1;
+  while (nt > 32 && nt * C * 8 > 96 * 1024) nt >>= 1;
+  const int smem = nt * C * 8;
+  cudaFuncSetAttribute(k_cycle_mu, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  k_cycle_mu<<<(unsigned)((b.n_cycles + nt - 1) / nt), nt, smem, s>>>(b, cfg);
+  ++*launches;
+}
+
 // ------------------------------------------------------------ launchers
 void launch_scan_events(const DevBuffers& b, const DevConfig&, int mode, bool sample,
                         const uint32_t* list, uint32_t n_list, cudaStream_t s,

@@ -69,6 +69,7 @@ def lib():
         getattr(L, fn).argtypes = [vp, u32, vp, sz, psz]
     L.cs_get_beta.argtypes = [vp, u32, vp, vp, sz, psz]
     L.cs_get_collective_beta.argtypes = [vp, u32, vp, vp, sz, psz]
+    L.cs_get_mu.argtypes = [vp, u32, vp, vp, sz, psz]
     L.cs_set_option.argtypes = [vp, C.c_int, C.c_int64]
     L.cs_redetect.argtypes = [vp, C.POINTER(abi.ControlConfig)]
     L.cs_stream_begin.argtypes = [vp]
@@ -109,7 +110,7 @@ EXPORTED_SYMBOLS = [
     "cs_set_config", "cs_set_name_table", "cs_upload", "cs_upload_wire", "cs_wire_pack",
     "cs_wire_view", "cs_wire_free", "cs_load_model", "cs_run", "cs_sync",
     "cs_get_summary", "cs_get_candidates", "cs_get_cycles", "cs_get_components", "cs_get_beta",
-    "cs_get_collective_beta", "cs_get_records", "cs_get_alerts", "cs_host_alloc",
+    "cs_get_collective_beta", "cs_get_mu", "cs_get_records", "cs_get_alerts", "cs_host_alloc",
     "cs_host_free", "cs_get_timings", "cs_get_launch_count", "cs_fit_latency_model",
     "cs_model_from_json", "cs_model_to_json", "cs_model_view", "cs_model_free",
     "cs_ucl_from_stats", "cs_compute_ucl", "cs_config_from_json", "cs_synth_generate",
@@ -486,6 +487,16 @@ class Analyzer:
             self._ck(self.L.cs_get_collective_beta(self.h, inst, b.ctypes.data, p.ctypes.data,
                                                    n.value, C.byref(n)))
         return b, p
+
+    def mu(self, inst=0):
+        """Counter-weighted mu per (cycle, class slot) and its presence (CS_RUN_MU)."""
+        n = C.c_size_t()
+        self._ck(self.L.cs_get_mu(self.h, inst, None, None, 0, C.byref(n)))
+        m = np.zeros(n.value, np.float64)
+        h = np.zeros(n.value, np.uint8)
+        if n.value:
+            self._ck(self.L.cs_get_mu(self.h, inst, m.ctypes.data, h.ctypes.data, n.value, C.byref(n)))
+        return m, h
 
     def result(self, inst=0, beta=True, scored=True) -> InstanceResult:
         s = self.summary(inst)

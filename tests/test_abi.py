@@ -185,3 +185,17 @@ def test_ucl_from_stats():
     c.theta_max = 0.18
     assert rt.ucl_from_stats(0.2, 0.2, c) == pytest.approx(0.18)
     assert rt.ucl_from_stats(0.0, 0.0, c) == pytest.approx(0.02)
+
+
+def test_metric_map_interned_into_name_table():
+    """RunConfig metric_map (rca.cpp:55-69 defaults) -> cs_name_info.metric =
+    1 + name id of the counter series, 0 when unmapped or absent."""
+    names = ["cpu_usage", "gemm_kernel", "oncpu", "run_batch", "x"]
+    span = [0, 1, 1, 1, 1]
+    _, _, table = rt.configs_from_json(None, names, span)
+    assert table["metric"][names.index("oncpu")] == names.index("cpu_usage") + 1
+    assert table["metric"][names.index("gemm_kernel")] == 0  # gpu_usage not in the trace
+    assert table["metric"][names.index("x")] == 0
+    _, _, table = rt.configs_from_json({"metric_map": {"x": "cpu_usage"}}, names, span)
+    assert table["metric"][names.index("x")] == names.index("cpu_usage") + 1
+    assert table["metric"][names.index("oncpu")] == 0  # a given map replaces the defaults

@@ -98,3 +98,31 @@ def test_gpu_matches_c_oracle_on_random_edge_traces(analyzer, fused):
             k = int(o["first_bad_record"])
             assert got.summary.first_bad_record == k
             assert np.array_equal(got.records[:k], o["records"][:k]), trial
+
+
+def test_mu_known_answer(analyzer):
+    """test_rca.cpp:121-155: oncpu 1 ms where cpu_usage reads 10, 3 ms where
+    it reads 30 -> mu = (1*10 + 3*30) / 4 = 25 (exact here)."""
+    import traces
+    from traces import ev
+    spec = [ev("run_batch", 0, 9_800_000), ev("run_batch", 10_000_000, 9_800_000),
+            ev("oncpu", 1_000_000, 1_000_000, cat="os_sched"),
+            ev("oncpu", 5_000_000, 3_000_000, cat="os_sched"),
+            ev("cpu_usage", 0, kind="counter", cat="counter_telemetry", value=10.0),
+            ev("cpu_usage", 3_000_000, kind="counter", cat="counter_telemetry", value=10.0),
+            ev("cpu_usage", 4_000_000, kind="counter", cat="counter_telemetry", value=30.0)]
+    b = traces.build(spec)
+    got, an = run_product(b.events, b.names, b.workloads, mask=abi.RUN_SEGMENT | abi.RUN_MU,
+                          run_config={"cycle": {"anchor_hint": "run_batch"}}, analyzer=analyzer)
+    mu, has = an.mu(0)
+    C = an.cycle.n_beta_slots
+    slots = {n: i for i, n in enumerate(n for n, s in zip(b.names, rt_span(b)) if s)}
+    assert len(got.cycles) == 1
+    assert has[slots["oncpu"]] == 1 and mu[slots["oncpu"]] == 25.0
+    assert has[slots["run_batch"]] == 0  # gpu_usage has no series: beta-only entry
+    assert len(mu) == C
+
+
+def rt_span(b):
+    from paper_2601_09258_b200 import runtime as rt
+    return rt.span_names_mask(b.events, len(b.names))

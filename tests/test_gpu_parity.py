@@ -135,3 +135,37 @@ def test_product_fit_drives_same_alerts(refbridge, analyzer, rt):
     an.run(abi.RUN_ALL)
     from helpers import assert_alerts_equal
     assert_alerts_equal(ref.alerts, an.alerts(0))
+
+
+@pytest.mark.parametrize("family,ranks,fused", [("cpu_contention", 1, False),
+                                                ("memory_thrash", 1, True),
+                                                ("nvlink_saturation", 4, False),
+                                                ("gpu_clock_lock", 8, False)])
+def test_counter_weighted_mu_parity(refbridge, analyzer, family, ranks, fused):
+    """cycle_stats' mu with the trace's CounterTable and the
+    default MetricMap (rca.cpp:17-53, 97-126) — bit-equal to the reference."""
+    t = refbridge.RefTrace.synth(900, 3 + ranks, 4, fault=family, onset=600, duration=150,
+                                 n_ranks=ranks, target_rank=ranks - 1)
+    ref = t.run(None, None, 400, beta=True, mu=True)
+    ex = t.export(None)
+    got, an = run_product(ex.events, ex.names, ex.workloads, n_comm=len(ex.comm_hash),
+                          mask=abi.RUN_SEGMENT | abi.RUN_MU, analyzer=analyzer, fused=fused)
+    mu, has = an.mu(0)
+    assert ref.status == 0
+    assert has.sum() > len(got.cycles)  # several mapped classes per cycle
+    assert np.array_equal(has, ref.extra["mu_has"])
+    assert np.array_equal(mu.view(np.uint64), ref.extra["mu"].view(np.uint64))
+
+
+def test_counter_weighted_mu_custom_metric_map(refbridge, analyzer):
+    cfg = {"metric_map": {"attn_kernel": "frequency", "oncpu": "page_activity",
+                          "reduce": "bus_util", "run_batch": "no_such_counter"}}
+    t = refbridge.RefTrace.synth(700, 31, 32, fault="bus_contention", onset=500, duration=100,
+                                 n_ranks=2, target_rank=1)
+    ref = t.run(cfg, None, 300, beta=True, mu=True)
+    ex = t.export(cfg)
+    got, an = run_product(ex.events, ex.names, ex.workloads, n_comm=len(ex.comm_hash),
+                          run_config=cfg, mask=abi.RUN_SEGMENT | abi.RUN_MU, analyzer=analyzer)
+    mu, has = an.mu(0)
+    assert np.array_equal(has, ref.extra["mu_has"])
+    assert np.array_equal(mu.view(np.uint64), ref.extra["mu"].view(np.uint64))
