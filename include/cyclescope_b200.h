@@ -284,47 +284,58 @@ int cs_upload(cs_ctx* ctx, uint32_t n_inst, const uint64_t* inst_offsets,
 /* (n_workloads = 0 with wl = NULL keeps the previously uploaded workload table.) */
 
 /* ------------------------------------------------- wire format (host link)
- * 16-byte packed record for the host->device leg: the H2D copy is what bounds
+ * Columnar wire format for the host->device leg: the H2D copy is what bounds
  * an end-to-end run, so the producer (ingest / collector) emits this instead
- * of cs_event and the device expands it in HBM.  Events are grouped in
- * instance-aligned blocks of CS_WIRE_BLOCK records (block b of instance i
- * covers events [inst_offsets[i] + b*CS_WIRE_BLOCK, ...)); block_base[] holds
- * each block's first start_ts, and t_off is start_ts - block_base (events are
- * canonically ordered, so t_off >= 0).
- *   dur      duration (ns); for CS_EV_HAS_VALUE counters the index of the
- *            f64 `value` in values[] instead
- *   payload  CS_EV_HAS_COMM: collective slot (cs_event.payload >> 32);
- *            otherwise cs_event.payload (workload index)
- * Records that do not fit (offset or duration >= 2^32, negative duration,
- * name_id >= 65535, kind/category >= 16, both HAS_COMM and a low payload)
- * set CS_WIRE_ESCAPE and carry an index into escapes[] (full cs_event). */
+ * of cs_event and the device expands it in HBM (k_wire_expand).  Events are
+ * grouped in instance-aligned blocks of CS_WIRE_BLOCK records (block b of
+ * instance i covers events [inst_offsets[i] + b*CS_WIRE_BLOCK, ...)).
+ *   events[]     8-byte header per event: t_off = start_ts - block_base[b]
+ *                (events are canonically ordered, so >= 0) and the packed
+ *                name id (16 bits) | kind (4) | category (4) | CS_EV_* flags
+ *                (6) | CS_WIRE_ESCAPE;
+ *   durations[]  one u32 per Span, in event order;
+ *   payloads[]   one u32 per event with CS_EV_HAS_BATCH (workload index) or
+ *                CS_EV_HAS_COMM (collective slot = cs_event.payload >> 32);
+ *   values[]     one f64 per Counter with CS_EV_HAS_VALUE;
+ *   block_cols[] per block, the index of its first entry in durations,
+ *                payloads and values (3 x u64);
+ *   escapes[]    full cs_event for records that do not fit (offset or span
+ *                duration >= 2^32, negative duration, a non-Span duration,
+ *                name id >= 65535, kind/category >= 16, both HAS_BATCH and
+ *                HAS_COMM): their header carries the escape index in t_off. */
 #define CS_WIRE_BLOCK 1024u
-#define CS_WIRE_ESCAPE 0x80u
+#define CS_WIRE_ESCAPE (1u << 30)
 typedef struct cs_wire_event {
   uint32_t t_off;
-  uint32_t dur;
-  uint16_t name_id;
-  uint8_t kind_cat;   /* kind | category << 4 */
-  uint8_t flags;      /* CS_EV_* (bits 0-5) | CS_WIRE_ESCAPE */
-  uint32_t payload;
+  uint32_t info;      /* name_id | kind << 16 | category << 20 | flags << 24 | CS_WIRE_ESCAPE */
 } cs_wire_event;
+
+typedef struct cs_wire_batch {
+  const cs_wire_event* events;   /* inst_offsets[n_inst] headers */
+  const int64_t* block_base;     /* n_blocks */
+  const uint64_t* block_cols;    /* 3 * n_blocks */
+  const uint32_t* durations;
+  uint64_t n_durations;
+  const uint32_t* payloads;
+  uint64_t n_payloads;
+  const double* values;
+  uint64_t n_values;
+  const cs_event* escapes;
+  uint64_t n_escapes;
+} cs_wire_batch;
 
 /* Upload a batch in the wire format (same instance layout and semantics as
  * cs_upload; expanded on the device into the same cs_event records). */
 int cs_upload_wire(cs_ctx* ctx, uint32_t n_inst, const uint64_t* inst_offsets,
-                   const cs_wire_event* ev, const int64_t* block_base, const double* values,
-                   uint64_t n_values, const cs_event* escapes, uint64_t n_escapes,
-                   uint64_t n_workloads, const cs_workload* wl);
+                   const cs_wire_batch* wire, uint64_t n_workloads, const cs_workload* wl);
 
 /* Host encoder (multi-threaded) from cs_event to the wire format; the
  * producer side of cs_upload_wire.  Buffers are owned by the returned
- * object; cs_wire_view exposes them. */
+ * object; cs_wire_view fills a cs_wire_batch pointing at them. */
 typedef struct cs_wire_trace cs_wire_trace;
 int cs_wire_pack(uint32_t n_inst, const uint64_t* inst_offsets, const cs_event* ev,
                  uint32_t n_threads, cs_wire_trace** out);
-int cs_wire_view(const cs_wire_trace* w, const cs_wire_event** ev, uint64_t* n_ev,
-                 const int64_t** block_base, uint64_t* n_blocks, const double** values,
-                 uint64_t* n_values, const cs_event** escapes, uint64_t* n_escapes);
+int cs_wire_view(const cs_wire_trace* w, cs_wire_batch* out, uint64_t* n_blocks);
 void cs_wire_free(cs_wire_trace* w);
 
 /* Latency model for instance `inst` (UINT32_MAX = default for every instance

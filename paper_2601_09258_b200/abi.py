@@ -14,13 +14,11 @@ EVENT_DTYPE = np.dtype(
      ("category", "u1"), ("flags", "<u2"), ("payload", "<u8")], align=True)
 assert EVENT_DTYPE.itemsize == 32
 
-# 16-byte wire record (cs_wire_event): the host->device format
-WIRE_DTYPE = np.dtype(
-    [("t_off", "<u4"), ("dur", "<u4"), ("name_id", "<u2"), ("kind_cat", "u1"), ("flags", "u1"),
-     ("payload", "<u4")])
-assert WIRE_DTYPE.itemsize == 16
+# wire format (cs_wire_event header, 8 bytes): the host->device format
+WIRE_DTYPE = np.dtype([("t_off", "<u4"), ("info", "<u4")])
+assert WIRE_DTYPE.itemsize == 8
 WIRE_BLOCK = 1024
-WIRE_ESCAPE = 0x80
+WIRE_ESCAPE = 1 << 30
 
 WORKLOAD_DTYPE = np.dtype([("batch", "<i8"), ("input_len", "<i8"), ("output_len", "<i8")])
 NAME_INFO_DTYPE = np.dtype(
@@ -133,6 +131,14 @@ def default_fit_options(n_features: int = 2) -> FitOptions:
 def default_control(strategy: int = DYNAMIC_WINDOW) -> ControlConfig:
     """ControlConfig defaults (detector.hpp:25-34)."""
     return ControlConfig(strategy, 0, 10, 0.15, 3.0, 0.18, 0.02, 100, 1e-9)
+
+
+class WireBatch(C.Structure):  # cs_wire_batch
+    _fields_ = [("events", C.c_void_p), ("block_base", C.c_void_p), ("block_cols", C.c_void_p),
+                ("durations", C.c_void_p), ("n_durations", C.c_uint64),
+                ("payloads", C.c_void_p), ("n_payloads", C.c_uint64),
+                ("values", C.c_void_p), ("n_values", C.c_uint64),
+                ("escapes", C.c_void_p), ("n_escapes", C.c_uint64)]
 
 
 class StrategyMetrics(C.Structure):

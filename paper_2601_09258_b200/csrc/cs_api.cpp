@@ -81,7 +81,7 @@ struct cs_ctx {
   uint64_t n_ev = 0, n_wl = 0;
   std::vector<uint64_t> inst_off;
   DevBuf d_ev, d_wl, d_names, d_inst_off;
-  DevBuf d_wire, d_wire_base, d_wire_values, d_wire_esc;  // cs_upload_wire staging
+  DevBuf d_wire;  // cs_upload_wire staging (all columns in one allocation)
   // tiles
   std::vector<uint32_t> tile_inst, inst_first_tile;
   std::vector<uint64_t> tile_begin, tile_end;
@@ -503,32 +503,41 @@ int cs_upload(cs_ctx* ctx, uint32_t n_inst, const uint64_t* inst_offsets, const 
 }
 
 int cs_upload_wire(cs_ctx* ctx, uint32_t n_inst, const uint64_t* inst_offsets,
-                   const cs_wire_event* ev, const int64_t* block_base, const double* values,
-                   uint64_t n_values, const cs_event* escapes, uint64_t n_escapes,
-                   uint64_t n_workloads, const cs_workload* wl) {
-  const int rc = upload_layout(ctx, n_inst, inst_offsets, ev != nullptr && block_base != nullptr,
-                               n_workloads, wl);
+                   const cs_wire_batch* w, uint64_t n_workloads, const cs_workload* wl) {
+  if (!w) return CS_E_INVALID_ARGUMENT;
+  const int rc = upload_layout(ctx, n_inst, inst_offsets,
+                               w->events != nullptr && w->block_base && w->block_cols, n_workloads, wl);
   if (rc != CS_OK) return rc;
-  if ((n_values && !values) || (n_escapes && !escapes)) return CS_E_INVALID_ARGUMENT;
+  if ((w->n_durations && !w->durations) || (w->n_payloads && !w->payloads) ||
+      (w->n_values && !w->values) || (w->n_escapes && !w->escapes))
+    return CS_E_INVALID_ARGUMENT;
   const uint64_t n = ctx->n_ev;
   const size_t nt = ctx->tile_inst.size();
-  void* dw = ctx->d_wire.get(std::max<uint64_t>(1, n) * sizeof(cs_wire_event));
-  void* db = ctx->d_wire_base.get(std::max<size_t>(1, nt) * sizeof(int64_t));
-  void* dv = ctx->d_wire_values.get(std::max<uint64_t>(1, n_values) * sizeof(double));
-  void* dx = ctx->d_wire_esc.get(std::max<uint64_t>(1, n_escapes) * sizeof(cs_event));
-  if (!dw || !db || !dv || !dx) return fail(ctx, CS_E_CUDA, "cudaMalloc(wire)");
-  if (n) {
-    CS_CUDA(cudaMemcpyAsync(dw, ev, n * sizeof(cs_wire_event), cudaMemcpyHostToDevice, ctx->stream));
-    CS_CUDA(cudaMemcpyAsync(db, block_base, nt * sizeof(int64_t), cudaMemcpyHostToDevice, ctx->stream));
-  }
-  if (n_values)
-    CS_CUDA(cudaMemcpyAsync(dv, values, n_values * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
-  if (n_escapes)
-    CS_CUDA(cudaMemcpyAsync(dx, escapes, n_escapes * sizeof(cs_event), cudaMemcpyHostToDevice,
-                            ctx->stream));
-  launch_wire_expand(static_cast<const cs_wire_event*>(dw), static_cast<const int64_t*>(db),
-                     static_cast<const double*>(dv), static_cast<const cs_event*>(dx),
-                     static_cast<const uint64_t*>(ctx->d_tile_begin.p),
+  // one staging allocation, sections 16-B aligned
+  auto al = [](size_t x) { return (x + 15) & ~size_t{15}; };
+  const size_t s_ev = al(n * sizeof(cs_wire_event)), s_base = al(nt * 8), s_cols = al(nt * 24),
+               s_dur = al(w->n_durations * 4), s_pay = al(w->n_payloads * 4),
+               s_val = al(w->n_values * 8), s_esc = al(w->n_escapes * sizeof(cs_event));
+  auto* d = static_cast<unsigned char*>(
+      ctx->d_wire.get(std::max<size_t>(16, s_ev + s_base + s_cols + s_dur + s_pay + s_val + s_esc)));
+  if (!d) return fail(ctx, CS_E_CUDA, "cudaMalloc(wire)");
+  WireDev dv;
+  size_t o = 0;
+  auto put = [&](const void* src, size_t bytes, size_t span) -> void* {
+    void* dst = d + o;
+    if (bytes) cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx->stream);
+    o += span;
+    return dst;
+  };
+  dv.events = static_cast<const uint2*>(put(w->events, n * sizeof(cs_wire_event), s_ev));
+  dv.block_base = static_cast<const int64_t*>(put(w->block_base, nt * 8, s_base));
+  dv.block_cols = static_cast<const uint64_t*>(put(w->block_cols, nt * 24, s_cols));
+  dv.durations = static_cast<const uint32_t*>(put(w->durations, w->n_durations * 4, s_dur));
+  dv.payloads = static_cast<const uint32_t*>(put(w->payloads, w->n_payloads * 4, s_pay));
+  dv.values = static_cast<const double*>(put(w->values, w->n_values * 8, s_val));
+  dv.escapes = static_cast<const cs_event*>(put(w->escapes, w->n_escapes * sizeof(cs_event), s_esc));
+  CS_CUDA(cudaGetLastError());
+  launch_wire_expand(dv, static_cast<const uint64_t*>(ctx->d_tile_begin.p),
                      static_cast<const uint64_t*>(ctx->d_tile_end.p), static_cast<uint32_t>(nt),
                      static_cast<cs_event*>(ctx->d_ev.p), ctx->stream);
   CS_CUDA(cudaGetLastError());

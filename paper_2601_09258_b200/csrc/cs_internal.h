@@ -205,8 +205,17 @@ void launch_freq_cycles(const cs_event* ev, uint64_t begin, uint64_t end, int64_
                         int64_t period, uint64_t n, uint64_t cyc_base, const DevBuffers& b,
                         uint32_t inst, cudaStream_t s, uint64_t* launches);
 
-void launch_wire_expand(const cs_wire_event* w, const int64_t* base, const double* values,
-                        const cs_event* esc, const uint64_t* tile_begin, const uint64_t* tile_end,
+// device copies of a cs_wire_batch (cs_upload_wire)
+struct WireDev {
+  const uint2* events;
+  const int64_t* block_base;
+  const uint64_t* block_cols;
+  const uint32_t* durations;
+  const uint32_t* payloads;
+  const double* values;
+  const cs_event* escapes;
+};
+void launch_wire_expand(const WireDev& w, const uint64_t* tile_begin, const uint64_t* tile_end,
                         uint32_t n_tiles, cs_event* out, cudaStream_t s);
 void launch_stream_keep(const DevBuffers& b, uint64_t* keep, cudaStream_t s);
 void launch_counter_series(const DevBuffers& b, cudaStream_t s, uint64_t* launches);

@@ -2659,47 +2659,74 @@ __global__ void __launch_bounds__(256, 3) k_cycle_reduce_v2(DevBuffers b, DevCon
 }
 
 // ---------------------------------------------------- wire-format expand
-// 16-B wire records (cs_wire_event) -> canonical 32-B cs_event in HBM, one
-// CTA per instance-aligned block (= tile): 128-bit coalesced loads, 256-bit
-// stores; counter values from the side array, escaped records copied whole.
-__global__ void __launch_bounds__(256) k_wire_expand(const cs_wire_event* __restrict__ w,
-                                                     const int64_t* __restrict__ base,
-                                                     const double* __restrict__ values,
-                                                     const cs_event* __restrict__ esc,
-                                                     const uint64_t* __restrict__ tile_begin,
-                                                     const uint64_t* __restrict__ tile_end,
-                                                     cs_event* __restrict__ out) {
+// Columnar wire records -> canonical 32-B cs_event in HBM, one CTA per
+// instance-aligned block (= tile), 4 consecutive events per thread: each
+// thread counts its events' entries in the duration / payload / value
+// columns, a block-wide exclusive scan (three 21-bit counts packed in a u64)
+// gives their column positions, escaped records are copied whole.
+constexpr int kWireThreads = 256;
+__global__ void __launch_bounds__(kWireThreads) k_wire_expand(WireDev w, const uint64_t* __restrict__ tile_begin,
+                                                              const uint64_t* __restrict__ tile_end,
+                                                              cs_event* __restrict__ out) {
+  __shared__ u64 s_w[32];
   const uint32_t t = blockIdx.x;
   const u64 tb = tile_begin[t], te = tile_end[t];
-  const i64 b0 = base[t];
-  for (u64 j = tb + threadIdx.x; j < te; j += blockDim.x) {
-    const uint4 r = __ldcs(reinterpret_cast<const uint4*>(w + j));
-    const uint32_t t_off = r.x, dur = r.y, payload = r.w;
-    const uint32_t name = r.z & 0xffffu, kc = (r.z >> 16) & 0xffu, flags = r.z >> 24;
+  const i64 b0 = w.block_base[t];
+  const u64 j0 = tb + 4u * threadIdx.x;
+  uint32_t off[4], info[4];
+  u64 mine = 0;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    off[q] = 0;
+    info[q] = CS_WIRE_ESCAPE;  // ignored below
+    if (j0 + q < te) {
+      const uint2 h = w.events[j0 + q];
+      off[q] = h.x;
+      info[q] = h.y;
+      if (!(h.y & CS_WIRE_ESCAPE)) {
+        const uint32_t kind = (h.y >> 16) & 15u, flags = (h.y >> 24) & 0x3fu;
+        mine += (kind == CS_SPAN ? 1ull : 0ull) +
+                ((flags & (CS_EV_HAS_BATCH | CS_EV_HAS_COMM)) ? (1ull << 21) : 0ull) +
+                ((kind == CS_COUNTER && (flags & CS_EV_HAS_VALUE)) ? (1ull << 42) : 0ull);
+      }
+    }
+  }
+  const u64 excl = block_incl_scan(mine, s_w, nullptr) - mine;
+  u64 dpos = w.block_cols[3 * t + 0] + (excl & 0x1fffffull);
+  u64 ppos = w.block_cols[3 * t + 1] + ((excl >> 21) & 0x1fffffull);
+  u64 vpos = w.block_cols[3 * t + 2] + (excl >> 42);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    if (j0 + q >= te) break;
     u64 a, d, c, p;
-    if (flags & CS_WIRE_ESCAPE) {
-      const cs_event& e = esc[payload];
+    if (info[q] & CS_WIRE_ESCAPE) {
+      const cs_event& e = w.escapes[off[q]];
       a = (u64)e.start_ts;
       d = (u64)e.duration;
       c = (u64)e.name_id | ((u64)e.kind << 32) | ((u64)e.category << 40) | ((u64)e.flags << 48);
       p = e.payload;
     } else {
-      a = (u64)(b0 + (i64)t_off);
-      d = (flags & CS_EV_HAS_VALUE) ? (u64)__double_as_longlong(values[dur]) : (u64)dur;
-      c = (u64)name | ((u64)(kc & 15u) << 32) | ((u64)(kc >> 4) << 40) | ((u64)flags << 48);
-      p = (flags & CS_EV_HAS_COMM) ? ((u64)payload << 32) : (u64)payload;
+      const uint32_t name = info[q] & 0xffffu, kind = (info[q] >> 16) & 15u;
+      const uint32_t cat = (info[q] >> 20) & 15u, flags = (info[q] >> 24) & 0x3fu;
+      a = (u64)(b0 + (i64)off[q]);
+      d = 0;
+      if (kind == CS_SPAN) d = (u64)w.durations[dpos++];
+      else if (kind == CS_COUNTER && (flags & CS_EV_HAS_VALUE)) d = (u64)__double_as_longlong(w.values[vpos++]);
+      p = 0;
+      if (flags & CS_EV_HAS_COMM) p = (u64)w.payloads[ppos++] << 32;
+      else if (flags & CS_EV_HAS_BATCH) p = (u64)w.payloads[ppos++];
+      c = (u64)name | ((u64)kind << 32) | ((u64)cat << 40) | ((u64)flags << 48);
     }
-    asm volatile("st.global.v4.u64 [%0], {%1, %2, %3, %4};" ::"l"(out + j), "l"(a), "l"(d), "l"(c),
-                 "l"(p)
+    asm volatile("st.global.v4.u64 [%0], {%1, %2, %3, %4};" ::"l"(out + j0 + q), "l"(a), "l"(d),
+                 "l"(c), "l"(p)
                  : "memory");
   }
 }
 
-void launch_wire_expand(const cs_wire_event* w, const int64_t* base, const double* values,
-                        const cs_event* esc, const uint64_t* tile_begin, const uint64_t* tile_end,
+void launch_wire_expand(const WireDev& w, const uint64_t* tile_begin, const uint64_t* tile_end,
                         uint32_t n_tiles, cs_event* out, cudaStream_t s) {
   if (!n_tiles) return;
-  k_wire_expand<<<n_tiles, 256, 0, s>>>(w, base, values, esc, tile_begin, tile_end, out);
+  k_wire_expand<<<n_tiles, kWireThreads, 0, s>>>(w, tile_begin, tile_end, out);
 }
 
 // Streaming: per instance, the position (relative to the instance's first

@@ -55,10 +55,9 @@ def lib():
     L.cs_set_config.argtypes = [vp, C.POINTER(abi.CycleConfig), C.POINTER(abi.ControlConfig)]
     L.cs_set_name_table.argtypes = [vp, u32, vp]
     L.cs_upload.argtypes = [vp, u32, vp, vp, u64, vp]
-    L.cs_upload_wire.argtypes = [vp, u32, vp, vp, vp, vp, u64, vp, u64, u64, vp]
+    L.cs_upload_wire.argtypes = [vp, u32, vp, C.POINTER(abi.WireBatch), u64, vp]
     L.cs_wire_pack.argtypes = [u32, vp, vp, u32, C.POINTER(vp)]
-    L.cs_wire_view.argtypes = [vp, C.POINTER(vp), C.POINTER(u64), C.POINTER(vp), C.POINTER(u64),
-                               C.POINTER(vp), C.POINTER(u64), C.POINTER(vp), C.POINTER(u64)]
+    L.cs_wire_view.argtypes = [vp, C.POINTER(abi.WireBatch), C.POINTER(u64)]
     L.cs_wire_free.argtypes = [vp]
     L.cs_load_model.argtypes = [vp, u32, C.POINTER(abi.Model)]
     L.cs_run.argtypes = [vp, u32]
@@ -285,16 +284,27 @@ def synth_trace(n_cycles, workload_seed, synth_seed, fault=None, onset=0, durati
 
 @dataclass
 class WireTrace:
-    """A batch of instances in the 16-byte wire format (cs_wire_pack)."""
-    events: np.ndarray       # WIRE_DTYPE
+    """A batch of instances in the columnar wire format (cs_wire_pack)."""
+    events: np.ndarray       # WIRE_DTYPE headers, one per event
     block_base: np.ndarray   # int64 per instance-aligned block of WIRE_BLOCK records
-    values: np.ndarray       # float64 counter values
-    escapes: np.ndarray      # EVENT_DTYPE records that do not fit the packed fields
+    block_cols: np.ndarray   # uint64 (n_blocks, 3): first duration / payload / value index
+    durations: np.ndarray    # uint32, one per Span
+    payloads: np.ndarray     # uint32, one per batch/collective event
+    values: np.ndarray       # float64, one per valued Counter
+    escapes: np.ndarray      # EVENT_DTYPE records that do not fit
     inst_offsets: np.ndarray
+
+    COLUMNS = ("events", "block_base", "block_cols", "durations", "payloads", "values", "escapes")
 
     @property
     def nbytes(self) -> int:
-        return self.events.nbytes + self.block_base.nbytes + self.values.nbytes + self.escapes.nbytes
+        return sum(getattr(self, c).nbytes for c in self.COLUMNS)
+
+    def batch(self) -> abi.WireBatch:
+        return abi.WireBatch(_ptr(self.events), _ptr(self.block_base), _ptr(self.block_cols),
+                             _ptr(self.durations), len(self.durations), _ptr(self.payloads),
+                             len(self.payloads), _ptr(self.values), len(self.values),
+                             _ptr(self.escapes), len(self.escapes))
 
 
 def wire_pack(events: np.ndarray, inst_offsets, n_threads=None) -> WireTrace:
@@ -306,19 +316,22 @@ def wire_pack(events: np.ndarray, inst_offsets, n_threads=None) -> WireTrace:
     _check(L.cs_wire_pack(len(off) - 1, off.ctypes.data, _ptr(events), n_threads or os.cpu_count() or 1,
                           C.byref(h)))
     try:
-        pe, pb, pv, px = C.c_void_p(), C.c_void_p(), C.c_void_p(), C.c_void_p()
-        ne, nb, nv, nx = C.c_uint64(), C.c_uint64(), C.c_uint64(), C.c_uint64()
-        _check(L.cs_wire_view(h, C.byref(pe), C.byref(ne), C.byref(pb), C.byref(nb), C.byref(pv),
-                              C.byref(nv), C.byref(px), C.byref(nx)))
+        v, nb = abi.WireBatch(), C.c_uint64()
+        _check(L.cs_wire_view(h, C.byref(v), C.byref(nb)))
 
         def arr(ptr, n, dtype):
-            if n == 0:
+            if n == 0 or not ptr:
                 return np.zeros(0, dtype=dtype)
             nbytes = n * np.dtype(dtype).itemsize
-            return np.frombuffer((C.c_char * nbytes).from_address(ptr.value), dtype=dtype).copy()
+            return np.frombuffer((C.c_char * nbytes).from_address(ptr), dtype=dtype).copy()
 
-        return WireTrace(arr(pe, ne.value, abi.WIRE_DTYPE), arr(pb, nb.value, np.int64),
-                         arr(pv, nv.value, np.float64), arr(px, nx.value, abi.EVENT_DTYPE), off)
+        n = int(off[-1])
+        return WireTrace(arr(v.events, n, abi.WIRE_DTYPE), arr(v.block_base, nb.value, np.int64),
+                         arr(v.block_cols, 3 * nb.value, np.uint64).reshape(-1, 3),
+                         arr(v.durations, v.n_durations, np.uint32),
+                         arr(v.payloads, v.n_payloads, np.uint32),
+                         arr(v.values, v.n_values, np.float64),
+                         arr(v.escapes, v.n_escapes, abi.EVENT_DTYPE), off)
     finally:
         L.cs_wire_free(h)
 
@@ -394,10 +407,9 @@ class Analyzer:
     def upload_wire(self, w: WireTrace, workloads: np.ndarray):
         """cs_upload_wire: same batch as upload(), sent in the 16-byte format."""
         wl = np.ascontiguousarray(workloads, dtype=abi.WORKLOAD_DTYPE)
+        b = w.batch()
         self._ck(self.L.cs_upload_wire(self.h, len(w.inst_offsets) - 1, w.inst_offsets.ctypes.data,
-                                       _ptr(w.events), _ptr(w.block_base), _ptr(w.values),
-                                       len(w.values), _ptr(w.escapes), len(w.escapes), len(wl),
-                                       _ptr(wl)))
+                                       C.byref(b), len(wl), _ptr(wl)))
         self.n_inst = len(w.inst_offsets) - 1
 
     def load_model(self, model: LatencyModel, inst: int | None = None):

@@ -22,23 +22,30 @@ def unpack(w):
         block[off[i]:off[i + 1]] = b + np.arange(m) // abi.WIRE_BLOCK
         b += nb
     assert b == len(w.block_base)
-    e = w.events
-    out = np.zeros(n, abi.EVENT_DTYPE)
-    esc = (e["flags"] & abi.WIRE_ESCAPE) != 0
+    info = w.events["info"].astype(np.int64)
+    esc = (info & abi.WIRE_ESCAPE) != 0
     ok = ~esc
-    out["start_ts"][ok] = w.block_base[block[ok]] + e["t_off"][ok].astype(np.int64)
-    val = ok & ((e["flags"] & 0x20) != 0)
-    dur = e["dur"].astype(np.int64)
-    out["duration"][ok] = dur[ok]
-    out["duration"][val] = w.values[e["dur"][val]].view(np.int64)
-    out["name_id"][ok] = e["name_id"][ok]
-    out["kind"][ok] = e["kind_cat"][ok] & 15
-    out["category"][ok] = e["kind_cat"][ok] >> 4
-    out["flags"][ok] = e["flags"][ok]
-    comm = ok & ((e["flags"] & 0x10) != 0)
-    out["payload"][ok] = e["payload"][ok]
-    out["payload"][comm] = e["payload"][comm].astype(np.uint64) << np.uint64(32)
-    out[esc] = w.escapes[e["payload"][esc]]
+    kind = (info >> 16) & 15
+    flags = (info >> 24) & 0x3F
+    span = ok & (kind == abi.SPAN)
+    val = ok & (kind == abi.COUNTER) & ((flags & 0x20) != 0)
+    pay = ok & ((flags & 0x14) != 0)
+    # column positions: running counts in event order (block_cols = block starts)
+    out = np.zeros(n, abi.EVENT_DTYPE)
+    out["start_ts"][ok] = w.block_base[block[ok]] + w.events["t_off"][ok].astype(np.int64)
+    assert span.sum() == len(w.durations) and pay.sum() == len(w.payloads) and val.sum() == len(w.values)
+    assert np.array_equal(w.block_cols[:, 0], np.concatenate([[0], np.cumsum(np.bincount(block[span], minlength=b))])[:b])
+    out["duration"][span] = w.durations.astype(np.int64)
+    out["duration"][val] = w.values.view(np.int64)
+    out["name_id"][ok] = info[ok] & 0xFFFF
+    out["kind"][ok] = kind[ok]
+    out["category"][ok] = (info[ok] >> 20) & 15
+    out["flags"][ok] = flags[ok]
+    p = w.payloads.astype(np.uint64)
+    comm = (flags[pay] & 0x10) != 0
+    p[comm] <<= np.uint64(32)
+    out["payload"][pay] = p
+    out[esc] = w.escapes[w.events["t_off"][esc]]
     return out
 
 
@@ -61,8 +68,9 @@ def test_wire_roundtrip_simkit(rt):
     t = rt.synth_trace(3000, 1, 2, n_ranks=8, fault="nvlink_saturation", onset=2000,
                        duration=150, target_rank=3, compact_names=False)
     w = rt.wire_pack(t.events, [0, len(t.events)])
-    assert w.events.nbytes == 16 * len(t.events)
+    assert w.events.nbytes == 8 * len(t.events)
     assert len(w.escapes) == 0
+    assert w.nbytes < 16 * len(t.events)
     assert np.array_equal(unpack(w).view(np.uint8), t.events.view(np.uint8))
 
 
