@@ -14,7 +14,10 @@
  *   frequency_cycles     cycles.cpp:283-343
  *   classify             cycles.cpp:190-254 (median 181-186)
  *   workload_of          cycles.cpp:256-281
- *   beta_of              rca.cpp:71-130 (beta / collective part; mu is §8f)
+ *   beta_of              rca.cpp:71-130 (beta / collective part)
+ *   counter_series       trace.cpp:111-131 (CounterTable::from_trace)
+ *   interpolate_mean     rca.cpp:17-53
+ *   mu_of                rca.cpp:97-106, 123-126 (mu part of cycle_stats)
  *   records              cycles.cpp:359-409
  *   predict              gbdt.cpp:22-30, 173-184
  *   ppe / detector       detector.cpp:14-19, 57-60, 85-130
@@ -39,6 +42,8 @@ typedef struct cso_out {
   double* beta;
   double* coll;        /* n_cycles x n_comm   */
   uint8_t* coll_present;
+  double* mu;          /* n_cycles x n_beta   */
+  uint8_t* mu_has;
   uint64_t n_records;
   cs_record* records;
   uint64_t n_alerts;
@@ -325,6 +330,107 @@ static void beta_of(const cs_event* ev, const cs_name_info* names, int C, int R,
   }
 }
 
+
+/* --------------------------------------------- counter-weighted mu (§8f) */
+typedef struct {
+  uint64_t n;
+  int64_t* ts;
+  double* v;
+} Series;
+
+/* CounterTable::from_trace: per counter name, the valued Counter events in
+ * event order (the reference's stable sort by ts keeps that order). */
+static Series* counter_series(const cs_event* ev, uint64_t n, uint32_t n_names) {
+  Series* s = zalloc(sizeof(Series) * (n_names ? n_names : 1));
+  for (uint64_t j = 0; j < n; ++j)
+    if (ev[j].kind == CS_COUNTER && (ev[j].flags & CS_EV_HAS_VALUE)) ++s[ev[j].name_id].n;
+  for (uint32_t k = 0; k < n_names; ++k) {
+    s[k].ts = zalloc(sizeof(int64_t) * s[k].n);
+    s[k].v = zalloc(sizeof(double) * s[k].n);
+    s[k].n = 0;
+  }
+  for (uint64_t j = 0; j < n; ++j) {
+    if (ev[j].kind != CS_COUNTER || !(ev[j].flags & CS_EV_HAS_VALUE)) continue;
+    Series* x = &s[ev[j].name_id];
+    x->ts[x->n] = ev[j].start_ts;
+    memcpy(&x->v[x->n], &ev[j].duration, sizeof(double));
+    ++x->n;
+  }
+  return s;
+}
+
+static double value_at(const Series* s, double t) {
+  if (t <= (double)s->ts[0]) return s->v[0];
+  if (t >= (double)s->ts[s->n - 1]) return s->v[s->n - 1];
+  uint64_t lo = 0, hi = s->n; /* lower_bound: first sample with ts >= t */
+  while (lo < hi) {
+    const uint64_t mid = (lo + hi) / 2;
+    if ((double)s->ts[mid] < t) lo = mid + 1;
+    else hi = mid;
+  }
+  const double f = (t - (double)s->ts[lo - 1]) / (double)(s->ts[lo] - s->ts[lo - 1]);
+  return s->v[lo - 1] + f * (s->v[lo] - s->v[lo - 1]);
+}
+
+static double interpolate_mean(const Series* s, int64_t t0, int64_t t1) {
+  double* knots = zalloc(sizeof(double) * (s->n + 2));
+  uint64_t nk = 0;
+  knots[nk++] = (double)t0;
+  for (uint64_t i = 0; i < s->n; ++i) {
+    const double ts = (double)s->ts[i];
+    if (ts > (double)t0 && ts < (double)t1) knots[nk++] = ts;
+  }
+  knots[nk++] = (double)t1;
+  double integral = 0.0;
+  for (uint64_t i = 0; i + 1 < nk; ++i) {
+    const double a = knots[i], b = knots[i + 1];
+    integral += 0.5 * (value_at(s, a) + value_at(s, b)) * (b - a);
+  }
+  free(knots);
+  return integral / ((double)t1 - (double)t0);
+}
+
+static void mu_of(const cs_event* ev, uint64_t n, const cs_name_info* names, uint32_t n_names,
+                  int C, cso_out* o) {
+  o->mu = zalloc(sizeof(double) * o->n_cycles * (C ? C : 1));
+  o->mu_has = zalloc(o->n_cycles * (C ? C : 1));
+  Series* series = counter_series(ev, n, n_names);
+  double* w = zalloc(sizeof(double) * (C ? C : 1));
+  uint8_t* has = zalloc(C ? C : 1);
+  for (uint64_t i = 0; i < o->n_cycles; ++i) {
+    const cs_cycle* c = &o->cycles[i];
+    const int64_t dur = c->end_ts - c->start_ts;
+    if (dur <= 0) continue;
+    memset(w, 0, sizeof(double) * (C ? C : 1));
+    memset(has, 0, C ? C : 1);
+    for (uint64_t j = c->first_event; j < c->last_event; ++j) {
+      const cs_event* e = &ev[j];
+      if (e->kind != CS_SPAN || e->duration <= 0) continue;
+      const int64_t end = e->start_ts + e->duration;
+      const int64_t clipped_end = end < c->end_ts ? end : c->end_ts;
+      const int64_t ov = clipped_end - e->start_ts;
+      if (ov <= 0) continue;
+      const int s = names[e->name_id].beta_slot;
+      const uint32_t m = names[e->name_id].metric;
+      if (s < 0 || m == 0 || m > n_names || series[m - 1].n == 0) continue;
+      w[s] += interpolate_mean(&series[m - 1], e->start_ts, clipped_end) * (double)ov;
+      has[s] = 1;
+    }
+    for (int s = 0; s < C; ++s)
+      if (has[s] && o->beta_tot[i * C + s] > 0) {
+        o->mu[i * C + s] = w[s] / (double)o->beta_tot[i * C + s];
+        o->mu_has[i * C + s] = 1;
+      }
+  }
+  for (uint32_t k = 0; k < n_names; ++k) {
+    free(series[k].ts);
+    free(series[k].v);
+  }
+  free(series);
+  free(w);
+  free(has);
+}
+
 /* ----------------------------------------------------------- model eval */
 static double predict(const cs_model* m, const double* x) {
   double v = m->base;
@@ -366,6 +472,7 @@ int cso_analyze(const cs_event* ev, uint64_t n, const cs_workload* wl, uint32_t 
     if (o->n_cycles == 0) {
       o->status = CS_E_NO_ANCHOR_FOUND;
       beta_of(ev, names, C, R, o);
+      mu_of(ev, n, names, n_names, C, o);
       o->records = zalloc(sizeof(cs_record));
       o->alerts = zalloc(sizeof(cs_alert));
       return o->status;
@@ -376,6 +483,7 @@ int cso_analyze(const cs_event* ev, uint64_t n, const cs_workload* wl, uint32_t 
   for (uint64_t i = 0; i < o->n_cycles; ++i)
     o->cycles[i].workload_status = workload_of(ev, &o->cycles[i], &wl_idx[i]);
   beta_of(ev, names, C, R, o);
+  mu_of(ev, n, names, n_names, C, o);
   /* records (cycles.cpp:366-409) */
   o->records = zalloc(sizeof(cs_record) * (o->n_cycles ? o->n_cycles : 1));
   o->alerts = zalloc(sizeof(cs_alert) * (o->n_cycles ? o->n_cycles : 1));
@@ -471,6 +579,8 @@ void cso_free(cso_out* o) {
   free(o->beta);
   free(o->coll);
   free(o->coll_present);
+  free(o->mu);
+  free(o->mu_has);
   free(o->records);
   free(o->alerts);
   free(o);
@@ -491,6 +601,8 @@ const int64_t* cso_beta_totals(const cso_out* o) { return o->beta_tot; }
 const double* cso_beta(const cso_out* o) { return o->beta; }
 const double* cso_coll(const cso_out* o) { return o->coll; }
 const uint8_t* cso_coll_present(const cso_out* o) { return o->coll_present; }
+const double* cso_mu(const cso_out* o) { return o->mu; }
+const uint8_t* cso_mu_has(const cso_out* o) { return o->mu_has; }
 uint64_t cso_n_records(const cso_out* o) { return o->n_records; }
 const cs_record* cso_records(const cso_out* o) { return o->records; }
 uint64_t cso_n_alerts(const cso_out* o) { return o->n_alerts; }

@@ -43,7 +43,8 @@ def lib():
                        ("cso_n_alerts", C.c_uint64)] + \
                 [(f, vp) for f in ("cso_candidates", "cso_cycles", "cso_components",
                                    "cso_beta_totals", "cso_beta", "cso_coll",
-                                   "cso_coll_present", "cso_records", "cso_alerts")]:
+                                   "cso_coll_present", "cso_mu", "cso_mu_has", "cso_records",
+                                   "cso_alerts")]:
             getattr(L, fn).restype = rt
             getattr(L, fn).argtypes = [vp]
         _lib = L
@@ -64,9 +65,17 @@ def derive_config(run_config, names, name_is_span, n_comm):
             phases.append(p)
     pkw = cy.get("prefill_keywords", ["forward_prefill"])
     dkw = cy.get("decode_keywords", ["process_batch_result_decode"])
+    # MetricMap::defaults (rca.cpp:55-69), replaced by RunConfig metric_map
+    metric_map = rc.get("metric_map", {
+        "oncpu": "cpu_usage", "gemm_kernel": "gpu_usage", "attn_kernel": "gpu_clock",
+        "reduce": "tx_bytes", "memcpy_h2d": "pcie_util", "memcpy_d2d": "bus_util",
+        "run_batch": "gpu_usage", "process_batch_result": "cpu_usage",
+        "get_next_batch_to_run": "cpu_usage"})
     table = np.zeros(len(names), dtype=abi.NAME_INFO_DTYPE)
     slot = 0
     for i, n in enumerate(names):
+        m = metric_map.get(n)
+        table[i]["metric"] = names.index(m) + 1 if m in names else 0
         table[i]["phase"] = phases.index(n) if n in phases else -1
         flags = 0
         if any(k in n for k in pkw):
@@ -153,6 +162,8 @@ def analyze(events, names, workloads, n_comm=0, run_config=None, model_json=None
             beta=_arr(L.cso_beta(out), nc * Cs, np.float64),
             coll_beta=_arr(L.cso_coll(out), nc * R, np.float64),
             coll_present=_arr(L.cso_coll_present(out), nc * R, np.uint8),
+            mu=_arr(L.cso_mu(out), nc * Cs, np.float64),
+            mu_has=_arr(L.cso_mu_has(out), nc * Cs, np.uint8),
             records=_arr(L.cso_records(out), L.cso_n_records(out), abi.RECORD_DTYPE),
             alerts=_arr(L.cso_alerts(out), L.cso_n_alerts(out), abi.ALERT_DTYPE))
     finally:

@@ -73,6 +73,11 @@ def test_gpu_matches_c_oracle_on_random_edge_traces(analyzer, fused):
                                   input_len=int(rng.integers(0, 500)),
                                   output_len=None if rng.random() < 0.05 else int(rng.integers(0, 50))))
             for k in range(int(rng.integers(0, 40))):
+                if rng.random() < 0.2:  # counter samples feeding mu (equal timestamps included)
+                    spec.append(traces.ev(["cpu_usage", "gpu_usage", "tx_bytes"][int(rng.integers(0, 3))],
+                                          t + int(rng.integers(0, 2500)) // 100 * 100, kind="counter",
+                                          cat="counter_telemetry", value=float(rng.normal(50, 20))))
+                    continue
                 nm = ["oncpu", "gemm_kernel", "reduce", "process_batch_result", "forward_prefill",
                       "get_next_batch_to_run"][int(rng.integers(0, 6))]
                 cat = {"oncpu": "os_sched", "gemm_kernel": "gpu_kernel",
@@ -85,8 +90,12 @@ def test_gpu_matches_c_oracle_on_random_edge_traces(analyzer, fused):
         cfg = {"detector": {"warmup": int(rng.integers(0, 20)), "window": int(rng.integers(1, 12))}}
         model = json.dumps(traces.TINY_MODEL)
         o = csoracle.analyze(b.events, b.names, b.workloads, b.n_comm, cfg, model)
-        got, _ = run_product(b.events, b.names, b.workloads, n_comm=b.n_comm, run_config=cfg,
-                             model_json=model, analyzer=analyzer, fused=fused)
+        got, an = run_product(b.events, b.names, b.workloads, n_comm=b.n_comm, run_config=cfg,
+                              model_json=model, analyzer=analyzer, fused=fused,
+                              mask=abi.RUN_ALL | abi.RUN_MU)
+        mu, has = an.mu(0)
+        assert np.array_equal(has, o["mu_has"]), trial
+        assert np.array_equal(mu.view(np.uint64), o["mu"].view(np.uint64)), trial
         assert np.array_equal(got.cycles, o["cycles"]), trial
         assert np.array_equal(got.components, o["components"]), trial
         assert np.array_equal(got.beta_totals, o["beta_totals"]), trial

@@ -179,3 +179,33 @@ def test_reference_equivalence_fixtures(refbridge):
         assert np.array_equal(r.cycles, o["cycles"]), name
         assert np.array_equal(r.components, o["components"]), name
         assert np.array_equal(r.records, o["records"][:len(r.records)]), name
+
+
+def test_c_oracle_mu_matches_reference(refbridge):
+    """The C restatement's counter-weighted mu (rca.cpp:17-53, 97-126) equals
+    the reference's cycle_stats with a CounterTable, bit for bit."""
+    for seed, ranks, fault in ((3, 1, "cpu_contention"), (5, 4, "nvlink_saturation")):
+        t = refbridge.RefTrace.synth(500, seed, seed + 1, fault=fault, onset=300, duration=100,
+                                     n_ranks=ranks, target_rank=ranks - 1)
+        ref = t.run(None, None, 250, beta=True, mu=True)
+        ex = t.export(None)
+        o = csoracle.analyze(ex.events, ex.names, ex.workloads, n_comm=len(ex.comm_hash))
+        assert o["mu_has"].sum() > 0
+        assert np.array_equal(o["mu_has"], ref.extra["mu_has"])
+        assert np.array_equal(o["mu"].view(np.uint64), ref.extra["mu"].view(np.uint64))
+
+
+def test_c_oracle_mu_known_answer():  # test_rca.cpp:121-155
+    from traces import build, ev
+    spec = [ev("run_batch", 0, 9_800_000), ev("run_batch", 10_000_000, 9_800_000),
+            ev("oncpu", 1_000_000, 1_000_000, cat="os_sched"),
+            ev("oncpu", 5_000_000, 3_000_000, cat="os_sched"),
+            ev("cpu_usage", 0, kind="counter", cat="counter_telemetry", value=10.0),
+            ev("cpu_usage", 3_000_000, kind="counter", cat="counter_telemetry", value=10.0),
+            ev("cpu_usage", 4_000_000, kind="counter", cat="counter_telemetry", value=30.0)]
+    b = build(spec)
+    o = csoracle.analyze(b.events, b.names, b.workloads,
+                         run_config={"cycle": {"anchor_hint": "run_batch"}})
+    span_names = [n for n in b.names if n in ("oncpu", "run_batch")]
+    k = span_names.index("oncpu")
+    assert o["mu_has"][k] == 1 and o["mu"][k] == 25.0
