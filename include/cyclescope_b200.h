@@ -338,6 +338,32 @@ int cs_wire_pack(uint32_t n_inst, const uint64_t* inst_offsets, const cs_event* 
 int cs_wire_view(const cs_wire_trace* w, cs_wire_batch* out, uint64_t* n_blocks);
 void cs_wire_free(cs_wire_trace* w);
 
+/* ------------------------------------------- Chrome-trace JSON ingest
+ * Native replacement of parse_trace_json (trace_io.cpp:162-206) + the
+ * interning every exporter does: a Chrome-trace JSON document (an event array
+ * or an object with "traceEvents") -> canonically ordered cs_event records,
+ * event ids, names (lexicographic, packed NUL-separated), workload table and
+ * (name, commHash, rank) collective slots.  Records parse in parallel on
+ * n_threads host threads; semantics (number classification, duplicate keys,
+ * args flattening, us -> ns rounding, fallback ids, skipped records) follow
+ * the reference as built with nlohmann/json.  n_issues counts the reference's
+ * ValidationIssue entries (an invalid document: empty trace, one issue). */
+typedef struct cs_ingest_keys { /* CycleConfig arg keys (cycles.hpp:28-39); NULL = default */
+  const char* forward_mode;
+  const char* batch_size;
+  const char* input_len;
+  const char* output_len;
+} cs_ingest_keys;
+typedef struct cs_ingest_result cs_ingest_result;
+int cs_ingest_chrome_json(const char* text, size_t len, const cs_ingest_keys* keys,
+                          uint32_t n_threads, cs_ingest_result** out);
+int cs_ingest_view(const cs_ingest_result* r, const cs_event** ev, const uint64_t** event_ids,
+                   uint64_t* n_ev, const cs_workload** wl, uint64_t* n_wl, const char** names,
+                   size_t* names_bytes, uint32_t* n_names, const int32_t** comm_name,
+                   const int32_t** comm_rank, const char** comm_hash, size_t* comm_bytes,
+                   uint32_t* n_comm, uint64_t* n_issues);
+void cs_ingest_free(cs_ingest_result* r);
+
 /* Latency model for instance `inst` (UINT32_MAX = default for every instance
  * without its own binding).  Bindings are by instance index, may precede the
  * first cs_upload and survive re-uploads (streams).

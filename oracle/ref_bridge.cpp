@@ -35,6 +35,7 @@
 #include "cyclescope/rng.hpp"
 #include "cyclescope/simkit.hpp"
 #include "cyclescope/trace.hpp"
+#include "cyclescope/trace_io.hpp"
 #include "cyclescope_b200.h"
 
 using namespace cyclescope;
@@ -437,6 +438,27 @@ void* ref_synth(const ref_synth_params* p) {
   SynthOptions opt;
   opt.n_ranks = p->n_ranks;
   h->ds = synthesize_trace(workloads, model, faults, opt, p->synth_seed);
+  return h.release();
+}
+
+// The reference's own Chrome-trace JSON (trace_io.cpp): serialize_trace_json
+// of this handle's trace, and a handle from parse_trace_json of a document
+// (its issues count in *n_issues).
+int ref_to_json(void* hv, char* buf, size_t cap, size_t* n) {
+  auto* h = static_cast<Handle*>(hv);
+  const std::string text = serialize_trace_json(h->ds.trace);
+  if (n) *n = text.size();
+  if (!buf) return 0;
+  if (cap < text.size()) return 1;
+  std::memcpy(buf, text.data(), text.size());
+  return 0;
+}
+
+void* ref_from_json(const char* text, size_t len, uint64_t* n_issues) {
+  auto h = std::make_unique<Handle>();
+  auto parsed = parse_trace_json(std::string(text, len));
+  if (n_issues) *n_issues = parsed.issues.size();
+  h->ds.trace = std::move(parsed.trace);
   return h.release();
 }
 

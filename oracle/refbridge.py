@@ -35,6 +35,9 @@ def lib():
         vp, sz = C.c_void_p, C.c_size_t
         L.ref_synth.restype = vp
         L.ref_synth.argtypes = [C.c_void_p]
+        L.ref_to_json.argtypes = [vp, C.c_char_p, sz, C.POINTER(sz)]
+        L.ref_from_json.restype = vp
+        L.ref_from_json.argtypes = [C.c_char_p, sz, C.POINTER(C.c_uint64)]
         L.ref_build.restype = vp
         L.ref_build.argtypes = [C.c_uint64, vp, vp, C.c_uint32, C.c_char_p, vp, C.c_uint32,
                                 C.c_char_p, vp, C.c_int]
@@ -153,6 +156,21 @@ class RefTrace:
         p = SynthParams(n_cycles, workload_seed, synth_seed, fam, target_rank, onset, duration,
                         severity, n_ranks, noise)
         return cls(lib().ref_synth(C.byref(p)))
+
+    def to_json(self) -> bytes:
+        """The reference's serialize_trace_json of this trace."""
+        L = lib()
+        n = C.c_size_t(0)
+        L.ref_to_json(self.h, None, 0, C.byref(n))
+        buf = C.create_string_buffer(n.value)
+        L.ref_to_json(self.h, buf, n.value, C.byref(n))
+        return buf.raw[:n.value]
+
+    @classmethod
+    def from_json(cls, text: bytes):
+        """A trace from the reference's parse_trace_json; returns (trace, n_issues)."""
+        iss = C.c_uint64(0)
+        return cls(lib().ref_from_json(text, len(text), C.byref(iss))), iss.value
 
     @classmethod
     def build(cls, events, names, workloads=None, comm_hash=(), comm_rank=(), event_ids=None,

@@ -1472,9 +1472,9 @@ int cs_get_mu(cs_ctx* ctx, uint32_t inst, double* mu, uint8_t* has, size_t cap, 
     if (has) std::fill(has, has + nc * C, 0);
     return CS_OK;
   }
-  if (mu && nc * C)
+  if (mu && nc * C != 0)
     CS_CUDA(cudaMemcpy(mu, static_cast<double*>(ctx->d_mu.p) + c0 * C, nc * C * 8, cudaMemcpyDeviceToHost));
-  if (has && nc * C)
+  if (has && nc * C != 0)
     CS_CUDA(cudaMemcpy(has, static_cast<uint8_t*>(ctx->d_mu_has.p) + c0 * C, nc * C, cudaMemcpyDeviceToHost));
   return CS_OK;
 }

@@ -59,6 +59,12 @@ def lib():
     L.cs_wire_pack.argtypes = [u32, vp, vp, u32, C.POINTER(vp)]
     L.cs_wire_view.argtypes = [vp, C.POINTER(abi.WireBatch), C.POINTER(u64)]
     L.cs_wire_free.argtypes = [vp]
+    L.cs_ingest_chrome_json.argtypes = [C.c_char_p, sz, vp, u32, C.POINTER(vp)]
+    L.cs_ingest_view.argtypes = [vp] + [C.POINTER(vp)] * 2 + [C.POINTER(u64), C.POINTER(vp),
+                                 C.POINTER(u64), C.POINTER(vp), psz, C.POINTER(u32),
+                                 C.POINTER(vp), C.POINTER(vp), C.POINTER(vp), psz, C.POINTER(u32),
+                                 C.POINTER(u64)]
+    L.cs_ingest_free.argtypes = [vp]
     L.cs_load_model.argtypes = [vp, u32, C.POINTER(abi.Model)]
     L.cs_run.argtypes = [vp, u32]
     L.cs_sync.argtypes = [vp]
@@ -107,7 +113,7 @@ def lib():
 EXPORTED_SYMBOLS = [
     "cs_abi_version", "cs_status_type", "cs_ctx_create", "cs_ctx_destroy", "cs_last_error",
     "cs_set_config", "cs_set_name_table", "cs_upload", "cs_upload_wire", "cs_wire_pack",
-    "cs_wire_view", "cs_wire_free", "cs_load_model", "cs_run", "cs_sync",
+    "cs_wire_view", "cs_wire_free", "cs_ingest_chrome_json", "cs_ingest_view", "cs_ingest_free", "cs_load_model", "cs_run", "cs_sync",
     "cs_get_summary", "cs_get_candidates", "cs_get_cycles", "cs_get_components", "cs_get_beta",
     "cs_get_collective_beta", "cs_get_mu", "cs_get_records", "cs_get_alerts", "cs_host_alloc",
     "cs_host_free", "cs_get_timings", "cs_get_launch_count", "cs_fit_latency_model",
@@ -280,6 +286,54 @@ def synth_trace(n_cycles, workload_seed, synth_seed, fault=None, onset=0, durati
         return SynthTrace(events, event_ids, workloads, labels, names, nc.value)
     finally:
         L.cs_synth_free(h)
+
+
+@dataclass
+class IngestedTrace:
+    """cs_ingest_chrome_json output: what an exporter produces from a Trace."""
+    events: np.ndarray
+    event_ids: np.ndarray
+    workloads: np.ndarray
+    names: list
+    comm_name: np.ndarray
+    comm_rank: np.ndarray
+    comm_hash: list
+    n_issues: int
+
+    @property
+    def n_comm(self) -> int:
+        return len(self.comm_name)
+
+
+def ingest_chrome_json(text: bytes, n_threads=None) -> IngestedTrace:
+    """Native Chrome-trace JSON ingest (parse_trace_json + interning)."""
+    L = lib()
+    h = C.c_void_p()
+    _check(L.cs_ingest_chrome_json(text, len(text), None, n_threads or os.cpu_count() or 1,
+                                   C.byref(h)))
+    try:
+        ev, ids, wl, nm, cn, cr, ch = (C.c_void_p() for _ in range(7))
+        nev, nwl, iss = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        nb, cb = C.c_size_t(), C.c_size_t()
+        nn, nc = C.c_uint32(), C.c_uint32()
+        _check(L.cs_ingest_view(h, C.byref(ev), C.byref(ids), C.byref(nev), C.byref(wl), C.byref(nwl),
+                                C.byref(nm), C.byref(nb), C.byref(nn), C.byref(cn), C.byref(cr),
+                                C.byref(ch), C.byref(cb), C.byref(nc), C.byref(iss)))
+
+        def arr(ptr, n, dtype):
+            if n == 0 or not ptr.value:
+                return np.zeros(0, dtype=dtype)
+            nbytes = n * np.dtype(dtype).itemsize
+            return np.frombuffer((C.c_char * nbytes).from_address(ptr.value), dtype=dtype).copy()
+
+        names = C.string_at(nm, nb.value).split(b"\0")[:nn.value] if nb.value else []
+        hashes = C.string_at(ch, cb.value).split(b"\0")[:nc.value] if cb.value else []
+        return IngestedTrace(arr(ev, nev.value, abi.EVENT_DTYPE), arr(ids, nev.value, np.uint64),
+                             arr(wl, nwl.value, abi.WORKLOAD_DTYPE), [x.decode() for x in names],
+                             arr(cn, nc.value, np.int32), arr(cr, nc.value, np.int32),
+                             [x.decode() for x in hashes], iss.value)
+    finally:
+        L.cs_ingest_free(h)
 
 
 @dataclass

@@ -1,0 +1,151 @@
+"""Native Chrome-trace JSON ingest (cs_ingest_chrome_json)
+vs the reference's own parse_trace_json (trace_io.cpp:87-206) followed by
+the oracle-side exporter (oracle/ref_bridge.cpp): identical records, event
+ids, names, workload table, collective slots and issue counts, on simkit
+traces serialized by the reference and on hand-written edge documents."""
+import json
+
+import numpy as np
+import pytest
+
+from paper_2601_09258_b200 import runtime as rt
+
+
+def _compare(refbridge, text: bytes):
+    ref, n_issues = refbridge.RefTrace.from_json(text)
+    ex = ref.export(None)
+    got = rt.ingest_chrome_json(text, n_threads=4)
+    assert got.n_issues == n_issues
+    assert got.names == ex.names
+    assert got.events.tobytes() == ex.events.tobytes()
+    assert np.array_equal(got.event_ids, ex.event_ids)
+    assert got.workloads.tobytes() == ex.workloads.tobytes()
+    assert got.comm_hash == ex.comm_hash
+    assert list(got.comm_rank) == list(ex.comm_rank)
+    return got
+
+
+@pytest.mark.parametrize("ranks,fault", [(1, "cpu_contention"), (4, "nvlink_saturation"),
+                                         (8, "pcie_bottleneck")])
+def test_simkit_round_trip(refbridge, ranks, fault):
+    t = refbridge.RefTrace.synth(1500, 3, 4, n_ranks=ranks, fault=fault, onset=1000, duration=100,
+                                 target_rank=ranks - 1)
+    text = t.to_json()
+    got = _compare(refbridge, text)
+    assert len(got.events) > 1500 * 19
+    wrapped = b'{"displayTimeUnit": "ns", "traceEvents": ' + text + b', "x": [1, {"y": null}]}'
+    _compare(refbridge, wrapped)
+
+
+def _doc(records, wrap=False):
+    body = "[" + ",\n".join(r if isinstance(r, str) else json.dumps(r) for r in records) + "]"
+    return (('{"traceEvents": ' + body + '}') if wrap else body).encode()
+
+
+EDGE = [
+    # phases, metadata, malformed records
+    {"ph": "M", "name": "process_name", "args": {"name": "x"}},
+    {"ph": "B", "name": "unsupported", "ts": 1},
+    {"name": "no_phase", "ts": 2},
+    '5',
+    {"ph": "X", "name": "run_batch", "ts": 10, "dur": 4.5, "args": {"forward_mode": "DECODE",
+                                                                     "batch_size": 3,
+                                                                     "input_len": 7,
+                                                                     "output_len": 1}},
+    {"ph": "X", "name": "run_batch", "ts": 20.0004, "dur": 3, "eid": 100,
+     "args": {"forward_mode": "Extend", "batch_size": 2.9, "input_len": True, "output_len": 0}},
+    {"ph": "X", "name": "run_batch", "ts": 20.0004, "dur": 1, "eid": 7},   # equal ts, lower id
+    {"ph": "X", "name": "gemm_kernel", "ts": 12, "dur": 1, "cat": "gpu_kernel"},
+    {"ph": "X", "name": "oddcat", "ts": 13, "dur": 1, "cat": "not_a_category"},
+    {"ph": "X", "name": "badcat", "ts": 13, "dur": 1, "cat": 5},          # type error: dropped
+    {"ph": "X", "name": 17, "ts": 14},                                    # type error: dropped
+    {"ph": "X", "name": "str_ts", "ts": "15"},                            # type error: dropped
+    {"ph": "X", "name": "bool_ts", "ts": True},                           # type error: dropped
+    {"ph": "X", "name": "pid_str", "ts": 16, "pid": "a"},                 # type error: dropped
+    {"ph": "X", "name": "eid_float", "ts": 17, "eid": 9.7},
+    {"ph": "i", "name": "inst", "ts": 18, "dur": 5, "args": {"forward_mode": "prefill"}},
+    {"ph": "C", "name": "cpu_usage", "ts": 19, "args": {"value": 3}},
+    {"ph": "C", "name": "cpu_usage", "ts": 19.5, "args": {"value": 2.25}},
+    {"ph": "C", "name": "gpu_usage", "ts": 19.7, "args": {"other": 1}},
+    {"ph": "C", "name": "bool_value", "ts": 19.8, "args": {"value": False}},
+    {"ph": "X", "name": "reduce", "ts": 21, "dur": 2, "cat": "collective_comm",
+     "args": {"commHash": "abc", "rank": 3}},
+    {"ph": "X", "name": "reduce", "ts": 22, "dur": 2, "cat": "collective_comm",
+     "args": {"commHash": "abc", "rank": 1.9}},
+    {"ph": "X", "name": "reduce", "ts": 23, "dur": 2, "cat": "collective_comm",
+     "args": {"commHash": 5, "rank": 1}},
+    {"ph": "s", "name": "flow", "ts": 24, "id": 1},
+    {"ph": "f", "name": "flow", "ts": 25, "args": {"flow": "zz"}},
+    # args: nesting, arrays, nulls, duplicate keys, keys that flatten alike
+    '{"ph": "X", "name": "nest", "ts": 26, "dur": 1, "args": {"a": {"forward_mode": "decode"},'
+    ' "b": [1, {"c": 2}], "z": null, "batch_size": 4, "batch_size": 5, "input_len": 1,'
+    ' "output_len": 2}}',
+    '{"ph": "X", "name": "flat", "ts": 27, "dur": 1, "args": {"x": {"batch_size": 9},'
+    ' "x.batch_size": 8, "batch_size": {"a": 1}}}',
+    '{"ph": "X", "name": "dupkey", "ts": 28, "ph": "i", "dur": 3, "name": "dup2"}',
+    # strings, numbers
+    {"ph": "X", "name": "café \U0001F600 \"q\" \\ /", "ts": 29, "dur": 1},
+    '{"ph": "X", "name": "esc\\u00e9\\ud83d\\ude00\\t", "ts": 30, "dur": 1e0, "tid": -0}',
+    '{"ph": "X", "name": "bigint", "ts": 31, "dur": 1, "eid": 18446744073709551615,'
+    ' "args": {"batch_size": 9223372036854775808, "input_len": -5, "output_len": 1E2}}',
+    '{"ph": "X", "name": "tiny", "ts": 32, "dur": 1, "args": {"batch_size": 1e-400}}',
+    {"ph": "X", "name": "neg_dur", "ts": 33, "dur": -2.5},
+    {"ph": "X", "name": "round", "ts": 0.0005, "dur": 0.0015},
+]
+
+
+@pytest.mark.parametrize("wrap", [False, True])
+def test_edge_records(refbridge, wrap):
+    got = _compare(refbridge, _doc(EDGE, wrap))
+    assert got.n_issues > 5
+
+
+@pytest.mark.parametrize("text", [
+    b'[{"ph": "X", "ts": 1,}]', b'[{"ph": "X", "ts": 01}]', b'[{"ph": "X", "name": "a\x01"}]',
+    b'[{"ph": "X", "name": "\xff"}]', b'[{"ph": "X"}] trailing', b'{"traceEvents": 5}',
+    b'"just a string"', b'[{"ph": "X", "ts": 1e}]', b'[{"ph": "X", "name": "\\x"}]',
+    b'[{"ph": "X", "name": "\\ud800"}]', b'', b'[{"ph": "X", "ts": -}]', b'{}',
+    b'{"traceEvents": [{"ph": "X", "ts": 1}], "traceEvents": [{"ph": "i", "ts": 2}]}'])
+def test_invalid_and_odd_documents(refbridge, text):
+    _compare(refbridge, text)
+
+
+def test_float_overflow_rejects_the_document():
+    """nlohmann throws out_of_range.406 on 1e400, which the reference's
+    parse_trace_json does not catch (the process terminates); the native
+    ingest treats it as an invalid document instead."""
+    got = rt.ingest_chrome_json(b'[{"ph": "X", "ts": 1, "args": {"v": 1e400}}, {"ph": "X", "ts": 2}]')
+    assert got.n_issues == 1 and len(got.events) == 0
+
+
+def _nasty(seed, n):
+    """Records whose strings hold quotes, backslash runs, brackets and commas,
+    at random lengths so the splitter's chunk boundaries land inside them."""
+    rng = np.random.default_rng(seed)
+    alphabet = ['"', '\\', '[', ']', '{', '}', ',', ':', 'a', ' ', '\\\\', '\\"']
+    recs = []
+    for i in range(n):
+        k = int(rng.integers(0, 40))
+        name = "".join(alphabet[j] for j in rng.integers(0, len(alphabet), k))
+        r = {"ph": "X", "name": name[:6] or "n", "ts": int(rng.integers(0, 10**6)), "dur": 1,
+             "args": {"note": name, "deep": [[{"s": name}], {"t": [name, 1]}],
+                      "batch_size": int(rng.integers(1, 9))}}
+        recs.append(r)
+    return recs
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_parallel_split_adversarial_strings(refbridge, seed):
+    text = _doc(_nasty(seed, 12000), wrap=bool(seed))
+    assert len(text) > 1 << 21
+    got = _compare(refbridge, text)
+    for nt in (1, 3, 8):
+        alt = rt.ingest_chrome_json(text, n_threads=nt)
+        assert alt.events.tobytes() == got.events.tobytes() and alt.names == got.names
+    # a stray backslash outside any string, deep in the document, rejects it
+    cut = len(text) // 2
+    pos = text.index(b'"ts"', cut)
+    bad = text[:pos] + b'\\' + text[pos:]
+    for nt in (1, 8):
+        r = rt.ingest_chrome_json(bad, n_threads=nt)
+        assert r.n_issues == 1 and len(r.events) == 0
