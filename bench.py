@@ -278,7 +278,7 @@ def run_ours(args, rank, world, local_rank):
     dev_ms = sum(step_ms) / len(step_ms)
 
     # e2e through the public API with host buffers: the producer emits the
-    # 16-byte wire format (cs_wire_pack, outside the timed region, as ingest
+    # columnar wire format (cs_wire_pack, outside the timed region, as ingest
     # would); every step uploads it from pinned memory (cs_upload_wire: H2D +
     # device expand), runs the path and reads alerts + summaries back
     wt = rt.wire_pack(pin_ev, offs, n_threads=threads)

@@ -289,34 +289,47 @@ int cs_upload(cs_ctx* ctx, uint32_t n_inst, const uint64_t* inst_offsets,
  * of cs_event and the device expands it in HBM (k_wire_expand).  Events are
  * grouped in instance-aligned blocks of CS_WIRE_BLOCK records (block b of
  * instance i covers events [inst_offsets[i] + b*CS_WIRE_BLOCK, ...)).
- *   events[]     8-byte header per event: t_off = start_ts - block_base[b]
- *                (events are canonically ordered, so >= 0) and the packed
- *                name id (16 bits) | kind (4) | category (4) | CS_EV_* flags
- *                (6) | CS_WIRE_ESCAPE;
- *   durations[]  one u32 per Span, in event order;
- *   payloads[]   one u32 per event with CS_EV_HAS_BATCH (workload index) or
- *                CS_EV_HAS_COMM (collective slot = cs_event.payload >> 32);
+ *   events[]     one 32-bit word per event: code << 24 | dt, where code
+ *                indexes dict[] (the packed name id (16 bits) | kind << 16 |
+ *                category << 20 | CS_EV_* flags << 24 of the event) or is
+ *                CS_WIRE_ESCAPE, and dt = start_ts - the previous event's
+ *                start_ts in the block (the block's first event: start_ts -
+ *                blocks[b].base_ts, which the encoder makes 0).  Events are
+ *                canonically ordered, so dt >= 0;
+ *   dur_lo[], dur_hi[]  one 24-bit duration per Span in event order (low
+ *                16 bits, high 8 bits);
+ *   payloads[]   one u16 per event with CS_EV_HAS_COMM (collective slot =
+ *                cs_event.payload >> 32) or CS_EV_HAS_BATCH (workload index
+ *                - blocks[b].batch_base);
  *   values[]     one f64 per Counter with CS_EV_HAS_VALUE;
- *   block_cols[] per block, the index of its first entry in durations,
- *                payloads and values (3 x u64);
- *   escapes[]    full cs_event for records that do not fit (offset or span
- *                duration >= 2^32, negative duration, a non-Span duration,
- *                name id >= 65535, kind/category >= 16, both HAS_BATCH and
- *                HAS_COMM): their header carries the escape index in t_off. */
+ *   blocks[]     per block: base timestamp, batch_base, and the index of its
+ *                first entry in the duration, payload, value and escape
+ *                columns;
+ *   escapes[]    full cs_event, in event order, for records that do not fit
+ *                (dt or span duration >= 2^24, negative duration, a non-Span
+ *                non-value duration, info not in dict, payload out of range,
+ *                both HAS_BATCH and HAS_COMM).  The next event's dt is taken
+ *                from an escaped event's start_ts like any other. */
 #define CS_WIRE_BLOCK 1024u
-#define CS_WIRE_ESCAPE (1u << 30)
-typedef struct cs_wire_event {
-  uint32_t t_off;
-  uint32_t info;      /* name_id | kind << 16 | category << 20 | flags << 24 | CS_WIRE_ESCAPE */
-} cs_wire_event;
+#define CS_WIRE_ESCAPE 0xffu
+#define CS_WIRE_MAX_DICT 255u
+typedef struct cs_wire_block {
+  int64_t base_ts;
+  uint64_t dur, pay, val, esc;  /* first entry of the block in each column */
+  uint32_t batch_base;
+  uint32_t reserved;
+} cs_wire_block;
 
 typedef struct cs_wire_batch {
-  const cs_wire_event* events;   /* inst_offsets[n_inst] headers */
-  const int64_t* block_base;     /* n_blocks */
-  const uint64_t* block_cols;    /* 3 * n_blocks */
-  const uint32_t* durations;
+  const uint32_t* events;        /* inst_offsets[n_inst] words */
+  const uint32_t* dict;          /* n_dict <= CS_WIRE_MAX_DICT info words */
+  uint32_t n_dict;
+  uint32_t reserved;
+  const cs_wire_block* blocks;   /* n_blocks */
+  const uint16_t* dur_lo;
+  const uint8_t* dur_hi;
   uint64_t n_durations;
-  const uint32_t* payloads;
+  const uint16_t* payloads;
   uint64_t n_payloads;
   const double* values;
   uint64_t n_values;

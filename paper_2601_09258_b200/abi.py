@@ -15,10 +15,12 @@ EVENT_DTYPE = np.dtype(
 assert EVENT_DTYPE.itemsize == 32
 
 # wire format (cs_wire_event header, 8 bytes): the host->device format
-WIRE_DTYPE = np.dtype([("t_off", "<u4"), ("info", "<u4")])
-assert WIRE_DTYPE.itemsize == 8
 WIRE_BLOCK = 1024
-WIRE_ESCAPE = 1 << 30
+WIRE_ESCAPE = 0xFF          # dictionary code of an escaped event
+WIRE_MAX_DICT = 255
+WIRE_BLOCK_DTYPE = np.dtype([("base_ts", "<i8"), ("dur", "<u8"), ("pay", "<u8"), ("val", "<u8"),
+                             ("esc", "<u8"), ("batch_base", "<u4"), ("reserved", "<u4")])
+assert WIRE_BLOCK_DTYPE.itemsize == 48
 
 WORKLOAD_DTYPE = np.dtype([("batch", "<i8"), ("input_len", "<i8"), ("output_len", "<i8")])
 NAME_INFO_DTYPE = np.dtype(
@@ -134,8 +136,9 @@ def default_control(strategy: int = DYNAMIC_WINDOW) -> ControlConfig:
 
 
 class WireBatch(C.Structure):  # cs_wire_batch
-    _fields_ = [("events", C.c_void_p), ("block_base", C.c_void_p), ("block_cols", C.c_void_p),
-                ("durations", C.c_void_p), ("n_durations", C.c_uint64),
+    _fields_ = [("events", C.c_void_p), ("dict", C.c_void_p), ("n_dict", C.c_uint32),
+                ("reserved", C.c_uint32), ("blocks", C.c_void_p),
+                ("dur_lo", C.c_void_p), ("dur_hi", C.c_void_p), ("n_durations", C.c_uint64),
                 ("payloads", C.c_void_p), ("n_payloads", C.c_uint64),
                 ("values", C.c_void_p), ("n_values", C.c_uint64),
                 ("escapes", C.c_void_p), ("n_escapes", C.c_uint64)]

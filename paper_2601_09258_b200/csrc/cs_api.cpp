@@ -505,21 +505,22 @@ int cs_upload(cs_ctx* ctx, uint32_t n_inst, const uint64_t* inst_offsets, const 
 int cs_upload_wire(cs_ctx* ctx, uint32_t n_inst, const uint64_t* inst_offsets,
                    const cs_wire_batch* w, uint64_t n_workloads, const cs_workload* wl) {
   if (!w) return CS_E_INVALID_ARGUMENT;
-  const int rc = upload_layout(ctx, n_inst, inst_offsets,
-                               w->events != nullptr && w->block_base && w->block_cols, n_workloads, wl);
+  const int rc = upload_layout(ctx, n_inst, inst_offsets, w->events != nullptr && w->blocks,
+                               n_workloads, wl);
   if (rc != CS_OK) return rc;
-  if ((w->n_durations && !w->durations) || (w->n_payloads && !w->payloads) ||
-      (w->n_values && !w->values) || (w->n_escapes && !w->escapes))
+  if ((w->n_durations && (!w->dur_lo || !w->dur_hi)) || (w->n_payloads && !w->payloads) ||
+      (w->n_values && !w->values) || (w->n_escapes && !w->escapes) ||
+      w->n_dict > CS_WIRE_MAX_DICT || (w->n_dict && !w->dict))
     return CS_E_INVALID_ARGUMENT;
   const uint64_t n = ctx->n_ev;
   const size_t nt = ctx->tile_inst.size();
   // one staging allocation, sections 16-B aligned
   auto al = [](size_t x) { return (x + 15) & ~size_t{15}; };
-  const size_t s_ev = al(n * sizeof(cs_wire_event)), s_base = al(nt * 8), s_cols = al(nt * 24),
-               s_dur = al(w->n_durations * 4), s_pay = al(w->n_payloads * 4),
+  const size_t s_ev = al(n * 4), s_dict = al(w->n_dict * 4), s_blk = al(nt * sizeof(cs_wire_block)),
+               s_lo = al(w->n_durations * 2), s_hi = al(w->n_durations), s_pay = al(w->n_payloads * 2),
                s_val = al(w->n_values * 8), s_esc = al(w->n_escapes * sizeof(cs_event));
-  auto* d = static_cast<unsigned char*>(
-      ctx->d_wire.get(std::max<size_t>(16, s_ev + s_base + s_cols + s_dur + s_pay + s_val + s_esc)));
+  auto* d = static_cast<unsigned char*>(ctx->d_wire.get(
+      std::max<size_t>(16, s_ev + s_dict + s_blk + s_lo + s_hi + s_pay + s_val + s_esc)));
   if (!d) return fail(ctx, CS_E_CUDA, "cudaMalloc(wire)");
   WireDev dv;
   size_t o = 0;
@@ -529,11 +530,13 @@ int cs_upload_wire(cs_ctx* ctx, uint32_t n_inst, const uint64_t* inst_offsets,
     o += span;
     return dst;
   };
-  dv.events = static_cast<const uint2*>(put(w->events, n * sizeof(cs_wire_event), s_ev));
-  dv.block_base = static_cast<const int64_t*>(put(w->block_base, nt * 8, s_base));
-  dv.block_cols = static_cast<const uint64_t*>(put(w->block_cols, nt * 24, s_cols));
-  dv.durations = static_cast<const uint32_t*>(put(w->durations, w->n_durations * 4, s_dur));
-  dv.payloads = static_cast<const uint32_t*>(put(w->payloads, w->n_payloads * 4, s_pay));
+  dv.events = static_cast<const uint32_t*>(put(w->events, n * 4, s_ev));
+  dv.dict = static_cast<const uint32_t*>(put(w->dict, w->n_dict * 4, s_dict));
+  dv.n_dict = w->n_dict;
+  dv.blocks = static_cast<const cs_wire_block*>(put(w->blocks, nt * sizeof(cs_wire_block), s_blk));
+  dv.dur_lo = static_cast<const uint16_t*>(put(w->dur_lo, w->n_durations * 2, s_lo));
+  dv.dur_hi = static_cast<const uint8_t*>(put(w->dur_hi, w->n_durations, s_hi));
+  dv.payloads = static_cast<const uint16_t*>(put(w->payloads, w->n_payloads * 2, s_pay));
   dv.values = static_cast<const double*>(put(w->values, w->n_values * 8, s_val));
   dv.escapes = static_cast<const cs_event*>(put(w->escapes, w->n_escapes * sizeof(cs_event), s_esc));
   CS_CUDA(cudaGetLastError());

@@ -207,11 +207,13 @@ void launch_freq_cycles(const cs_event* ev, uint64_t begin, uint64_t end, int64_
 
 // device copies of a cs_wire_batch (cs_upload_wire)
 struct WireDev {
-  const uint2* events;
-  const int64_t* block_base;
-  const uint64_t* block_cols;
-  const uint32_t* durations;
-  const uint32_t* payloads;
+  const uint32_t* events;
+  const uint32_t* dict;
+  uint32_t n_dict;
+  const cs_wire_block* blocks;
+  const uint16_t* dur_lo;
+  const uint8_t* dur_hi;
+  const uint16_t* payloads;
   const double* values;
   const cs_event* escapes;
 };

@@ -2661,60 +2661,131 @@ __global__ void __launch_bounds__(256, 3) k_cycle_reduce_v2(DevBuffers b, DevCon
 // ---------------------------------------------------- wire-format expand
 // Columnar wire records -> canonical 32-B cs_event in HBM, one CTA per
 // instance-aligned block (= tile), 4 consecutive events per thread: each
-// thread counts its events' entries in the duration / payload / value
-// columns, a block-wide exclusive scan (three 21-bit counts packed in a u64)
-// gives their column positions, escaped records are copied whole.
+// thread decodes its events' dictionary codes (dictionary in shared memory)
+// and counts their entries in the duration / payload / value / escape
+// columns; a block-wide exclusive scan (four 16-bit counts packed in a u64)
+// gives their column positions, and a segmented scan of the 24-bit start_ts
+// deltas (restarted at escaped records, which are copied whole) gives the
+// timestamps.
 constexpr int kWireThreads = 256;
 __global__ void __launch_bounds__(kWireThreads) k_wire_expand(WireDev w, const uint64_t* __restrict__ tile_begin,
                                                               const uint64_t* __restrict__ tile_end,
                                                               cs_event* __restrict__ out) {
   __shared__ u64 s_w[32];
+  __shared__ uint32_t s_dict[256];
+  __shared__ i64 s_x[kWireThreads];
+  __shared__ uint8_t s_f[kWireThreads];
+  __shared__ i64 s_wx[32];
+  __shared__ uint8_t s_wf[32];
   const uint32_t t = blockIdx.x;
+  for (uint32_t i = threadIdx.x; i < 256; i += kWireThreads) s_dict[i] = i < w.n_dict ? w.dict[i] : 0u;
   const u64 tb = tile_begin[t], te = tile_end[t];
-  const i64 b0 = w.block_base[t];
+  const cs_wire_block& B = w.blocks[t];
+  const i64 b0 = B.base_ts;
+  const uint32_t batch_base = B.batch_base;
   const u64 j0 = tb + 4u * threadIdx.x;
-  uint32_t off[4], info[4];
-  u64 mine = 0;
+  uint32_t word[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) word[q] = j0 + q < te ? __ldg(w.events + j0 + q) : 0u;
+  __syncthreads();  // s_dict
+  uint32_t info[4];
+  u64 mine = 0;  // [durations, payloads, values, escapes] 16 bits each
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
-    off[q] = 0;
-    info[q] = CS_WIRE_ESCAPE;  // ignored below
-    if (j0 + q < te) {
-      const uint2 h = w.events[j0 + q];
-      off[q] = h.x;
-      info[q] = h.y;
-      if (!(h.y & CS_WIRE_ESCAPE)) {
-        const uint32_t kind = (h.y >> 16) & 15u, flags = (h.y >> 24) & 0x3fu;
-        mine += (kind == CS_SPAN ? 1ull : 0ull) +
-                ((flags & (CS_EV_HAS_BATCH | CS_EV_HAS_COMM)) ? (1ull << 21) : 0ull) +
-                ((kind == CS_COUNTER && (flags & CS_EV_HAS_VALUE)) ? (1ull << 42) : 0ull);
+    info[q] = 0;
+    if (j0 + q >= te) continue;
+    const uint32_t code = word[q] >> 24;
+    if (code == CS_WIRE_ESCAPE) {
+      mine += 1ull << 48;
+      continue;
+    }
+    info[q] = s_dict[code];
+    const uint32_t kind = (info[q] >> 16) & 15u, flags = (info[q] >> 24) & 0x3fu;
+    mine += (kind == CS_SPAN ? 1ull : 0ull) +
+            ((flags & (CS_EV_HAS_BATCH | CS_EV_HAS_COMM)) ? (1ull << 16) : 0ull) +
+            ((kind == CS_COUNTER && (flags & CS_EV_HAS_VALUE)) ? (1ull << 32) : 0ull);
+  }
+  const u64 excl = block_incl_scan(mine, s_w, nullptr) - mine;
+  u64 dpos = B.dur + (excl & 0xffffull);
+  u64 ppos = B.pay + ((excl >> 16) & 0xffffull);
+  u64 vpos = B.val + ((excl >> 32) & 0xffffull);
+  u64 epos = B.esc + (excl >> 48);
+  // start_ts: a segmented prefix sum of the deltas, restarted at each escaped
+  // event's absolute start_ts (the aggregate (f, x) of a run: f = it holds an
+  // escape, x = offset from b0 after it)
+  uint8_t f = 0;
+  i64 x = 0;
+  {
+    u64 e = epos;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (j0 + q >= te) break;
+      if ((word[q] >> 24) == CS_WIRE_ESCAPE) {
+        f = 1;
+        x = w.escapes[e++].start_ts - b0;
+      } else {
+        x += (i64)(word[q] & 0xffffffu);
       }
     }
   }
-  const u64 excl = block_incl_scan(mine, s_w, nullptr) - mine;
-  u64 dpos = w.block_cols[3 * t + 0] + (excl & 0x1fffffull);
-  u64 ppos = w.block_cols[3 * t + 1] + ((excl >> 21) & 0x1fffffull);
-  u64 vpos = w.block_cols[3 * t + 2] + (excl >> 42);
+  {
+    const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+    for (int o = 1; o < 32; o <<= 1) {
+      const i64 yx = __shfl_up_sync(0xffffffffu, x, o);
+      const uint32_t yf = __shfl_up_sync(0xffffffffu, (uint32_t)f, o);
+      if (lane >= o) {
+        if (!f) x += yx;
+        f |= (uint8_t)yf;
+      }
+    }
+    if (lane == 31) s_wx[wp] = x, s_wf[wp] = f;
+    __syncthreads();
+    if (wp == 0) {
+      constexpr int kW = kWireThreads / 32;
+      i64 px = lane < kW ? s_wx[lane] : 0;
+      uint32_t pf = lane < kW ? s_wf[lane] : 0u;
+      for (int o = 1; o < kW; o <<= 1) {
+        const i64 yx = __shfl_up_sync(0xffffffffu, px, o);
+        const uint32_t yf = __shfl_up_sync(0xffffffffu, pf, o);
+        if (lane >= o) {
+          if (!pf) px += yx;
+          pf |= yf;
+        }
+      }
+      if (lane < kW) s_wx[lane] = px, s_wf[lane] = (uint8_t)pf;
+    }
+    __syncthreads();
+    if (wp > 0 && !f) x += s_wx[wp - 1];
+    s_x[threadIdx.x] = x;  // inclusive
+    __syncthreads();
+  }
+  i64 run = threadIdx.x ? s_x[threadIdx.x - 1] : 0;
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     if (j0 + q >= te) break;
     u64 a, d, c, p;
-    if (info[q] & CS_WIRE_ESCAPE) {
-      const cs_event& e = w.escapes[off[q]];
+    if ((word[q] >> 24) == CS_WIRE_ESCAPE) {
+      const cs_event& e = w.escapes[epos++];
+      run = e.start_ts - b0;
       a = (u64)e.start_ts;
       d = (u64)e.duration;
       c = (u64)e.name_id | ((u64)e.kind << 32) | ((u64)e.category << 40) | ((u64)e.flags << 48);
       p = e.payload;
     } else {
+      run += (i64)(word[q] & 0xffffffu);
       const uint32_t name = info[q] & 0xffffu, kind = (info[q] >> 16) & 15u;
       const uint32_t cat = (info[q] >> 20) & 15u, flags = (info[q] >> 24) & 0x3fu;
-      a = (u64)(b0 + (i64)off[q]);
+      a = (u64)(b0 + run);
       d = 0;
-      if (kind == CS_SPAN) d = (u64)w.durations[dpos++];
-      else if (kind == CS_COUNTER && (flags & CS_EV_HAS_VALUE)) d = (u64)__double_as_longlong(w.values[vpos++]);
+      if (kind == CS_SPAN) {
+        d = (u64)w.dur_lo[dpos] | ((u64)w.dur_hi[dpos] << 16);
+        ++dpos;
+      } else if (kind == CS_COUNTER && (flags & CS_EV_HAS_VALUE)) {
+        d = (u64)__double_as_longlong(w.values[vpos++]);
+      }
       p = 0;
       if (flags & CS_EV_HAS_COMM) p = (u64)w.payloads[ppos++] << 32;
-      else if (flags & CS_EV_HAS_BATCH) p = (u64)w.payloads[ppos++];
+      else if (flags & CS_EV_HAS_BATCH) p = (u64)((uint32_t)w.payloads[ppos++] + batch_base);
       c = (u64)name | ((u64)kind << 32) | ((u64)cat << 40) | ((u64)flags << 48);
     }
     asm volatile("st.global.v4.u64 [%0], {%1, %2, %3, %4};" ::"l"(out + j0 + q), "l"(a), "l"(d),

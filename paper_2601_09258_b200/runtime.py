@@ -339,26 +339,27 @@ def ingest_chrome_json(text: bytes, n_threads=None) -> IngestedTrace:
 @dataclass
 class WireTrace:
     """A batch of instances in the columnar wire format (cs_wire_pack)."""
-    events: np.ndarray       # WIRE_DTYPE headers, one per event
-    block_base: np.ndarray   # int64 per instance-aligned block of WIRE_BLOCK records
-    block_cols: np.ndarray   # uint64 (n_blocks, 3): first duration / payload / value index
-    durations: np.ndarray    # uint32, one per Span
-    payloads: np.ndarray     # uint32, one per batch/collective event
+    events: np.ndarray       # uint32 per event: dictionary code << 24 | start_ts delta
+    dict: np.ndarray         # uint32 info words (name | kind << 16 | category << 20 | flags << 24)
+    blocks: np.ndarray       # WIRE_BLOCK_DTYPE per instance-aligned block of WIRE_BLOCK records
+    dur_lo: np.ndarray       # uint16, one per Span
+    dur_hi: np.ndarray       # uint8, one per Span
+    payloads: np.ndarray     # uint16, one per batch/collective event
     values: np.ndarray       # float64, one per valued Counter
     escapes: np.ndarray      # EVENT_DTYPE records that do not fit
     inst_offsets: np.ndarray
 
-    COLUMNS = ("events", "block_base", "block_cols", "durations", "payloads", "values", "escapes")
+    COLUMNS = ("events", "dict", "blocks", "dur_lo", "dur_hi", "payloads", "values", "escapes")
 
     @property
     def nbytes(self) -> int:
         return sum(getattr(self, c).nbytes for c in self.COLUMNS)
 
     def batch(self) -> abi.WireBatch:
-        return abi.WireBatch(_ptr(self.events), _ptr(self.block_base), _ptr(self.block_cols),
-                             _ptr(self.durations), len(self.durations), _ptr(self.payloads),
-                             len(self.payloads), _ptr(self.values), len(self.values),
-                             _ptr(self.escapes), len(self.escapes))
+        return abi.WireBatch(_ptr(self.events), _ptr(self.dict), len(self.dict), 0, _ptr(self.blocks),
+                             _ptr(self.dur_lo), _ptr(self.dur_hi), len(self.dur_lo),
+                             _ptr(self.payloads), len(self.payloads), _ptr(self.values),
+                             len(self.values), _ptr(self.escapes), len(self.escapes))
 
 
 def wire_pack(events: np.ndarray, inst_offsets, n_threads=None) -> WireTrace:
@@ -380,11 +381,10 @@ def wire_pack(events: np.ndarray, inst_offsets, n_threads=None) -> WireTrace:
             return np.frombuffer((C.c_char * nbytes).from_address(ptr), dtype=dtype).copy()
 
         n = int(off[-1])
-        return WireTrace(arr(v.events, n, abi.WIRE_DTYPE), arr(v.block_base, nb.value, np.int64),
-                         arr(v.block_cols, 3 * nb.value, np.uint64).reshape(-1, 3),
-                         arr(v.durations, v.n_durations, np.uint32),
-                         arr(v.payloads, v.n_payloads, np.uint32),
-                         arr(v.values, v.n_values, np.float64),
+        return WireTrace(arr(v.events, n, np.uint32), arr(v.dict, v.n_dict, np.uint32),
+                         arr(v.blocks, nb.value, abi.WIRE_BLOCK_DTYPE),
+                         arr(v.dur_lo, v.n_durations, np.uint16), arr(v.dur_hi, v.n_durations, np.uint8),
+                         arr(v.payloads, v.n_payloads, np.uint16), arr(v.values, v.n_values, np.float64),
                          arr(v.escapes, v.n_escapes, abi.EVENT_DTYPE), off)
     finally:
         L.cs_wire_free(h)
@@ -459,7 +459,7 @@ class Analyzer:
         self.n_inst = len(off) - 1
 
     def upload_wire(self, w: WireTrace, workloads: np.ndarray):
-        """cs_upload_wire: same batch as upload(), sent in the 16-byte format."""
+        """cs_upload_wire: same batch as upload(), sent in the columnar wire format."""
         wl = np.ascontiguousarray(workloads, dtype=abi.WORKLOAD_DTYPE)
         b = w.batch()
         self._ck(self.L.cs_upload_wire(self.h, len(w.inst_offsets) - 1, w.inst_offsets.ctypes.data,

@@ -1,4 +1,4 @@
-"""The 16-byte wire format (cs_wire_event, include/cyclescope_b200.h).
+"""The columnar wire format (cs_wire_batch, include/cyclescope_b200.h).
 
 CPU: cs_wire_pack round-trips every cs_event field exactly (decoded here in
 numpy, the inverse of the device's k_wire_expand), escapes included.
@@ -15,27 +15,44 @@ def unpack(w):
     off = w.inst_offsets.astype(np.int64)
     n = int(off[-1])
     block = np.empty(n, np.int64)
+    bstart = []
     b = 0
     for i in range(len(off) - 1):
         m = int(off[i + 1] - off[i])
         nb = (m + abi.WIRE_BLOCK - 1) // abi.WIRE_BLOCK
         block[off[i]:off[i + 1]] = b + np.arange(m) // abi.WIRE_BLOCK
+        bstart += [int(off[i]) + k * abi.WIRE_BLOCK for k in range(nb)]
         b += nb
-    assert b == len(w.block_base)
-    info = w.events["info"].astype(np.int64)
-    esc = (info & abi.WIRE_ESCAPE) != 0
+    assert b == len(w.blocks) and len(w.dict) <= abi.WIRE_MAX_DICT
+    bstart = np.asarray(bstart, np.int64)
+    code = (w.events >> 24).astype(np.int64)
+    esc = code == abi.WIRE_ESCAPE
     ok = ~esc
+    info = np.zeros(n, np.int64)
+    info[ok] = w.dict[code[ok]].astype(np.int64)
     kind = (info >> 16) & 15
     flags = (info >> 24) & 0x3F
     span = ok & (kind == abi.SPAN)
     val = ok & (kind == abi.COUNTER) & ((flags & 0x20) != 0)
     pay = ok & ((flags & 0x14) != 0)
-    # column positions: running counts in event order (block_cols = block starts)
+    assert span.sum() == len(w.dur_lo) and pay.sum() == len(w.payloads) and val.sum() == len(w.values)
+    assert esc.sum() == len(w.escapes)
+    for col, mask in (("dur", span), ("pay", pay), ("val", val), ("esc", esc)):
+        starts = np.concatenate([[0], np.cumsum(np.bincount(block[mask], minlength=b))])[:b]
+        assert np.array_equal(w.blocks[col].astype(np.int64), starts), col
+    # start_ts: per-block prefix sums of the deltas, restarted at escaped records
+    dt = (w.events & 0xFFFFFF).astype(np.int64)
+    dt[esc] = 0
+    cs = np.cumsum(dt)
+    cs -= (cs - dt)[bstart][block]                 # inclusive sum within the block
     out = np.zeros(n, abi.EVENT_DTYPE)
-    out["start_ts"][ok] = w.block_base[block[ok]] + w.events["t_off"][ok].astype(np.int64)
-    assert span.sum() == len(w.durations) and pay.sum() == len(w.payloads) and val.sum() == len(w.values)
-    assert np.array_equal(w.block_cols[:, 0], np.concatenate([[0], np.cumsum(np.bincount(block[span], minlength=b))])[:b])
-    out["duration"][span] = w.durations.astype(np.int64)
+    out[esc] = w.escapes
+    last = np.maximum.accumulate(np.where(esc, np.arange(n), -1))
+    restarted = last >= bstart[block]
+    base = w.blocks["base_ts"][block].astype(np.int64)
+    base[restarted] = out["start_ts"][last[restarted]] - cs[last[restarted]]
+    out["start_ts"][ok] = (base + cs)[ok]
+    out["duration"][span] = w.dur_lo.astype(np.int64) | (w.dur_hi.astype(np.int64) << 16)
     out["duration"][val] = w.values.view(np.int64)
     out["name_id"][ok] = info[ok] & 0xFFFF
     out["kind"][ok] = kind[ok]
@@ -44,8 +61,8 @@ def unpack(w):
     p = w.payloads.astype(np.uint64)
     comm = (flags[pay] & 0x10) != 0
     p[comm] <<= np.uint64(32)
+    p[~comm] += w.blocks["batch_base"][block[pay][~comm]].astype(np.uint64)
     out["payload"][pay] = p
-    out[esc] = w.escapes[w.events["t_off"][esc]]
     return out
 
 
@@ -59,8 +76,10 @@ def _edge_events(rt):
     ev["payload"][k[20:30]] |= np.uint64(1 << 40)                 # high payload bits
     sp = np.nonzero(ev["kind"] == 0)[0]
     ev["duration"][sp[:5]] = -3                                   # negative span duration
-    # a gap > 4.29 s inside one block
+    # a gap > 4.29 s inside one block, and one of 2^24 ns exactly (escape)
     ev["start_ts"][2000:] += (1 << 33)
+    ev["start_ts"][3001:] += (1 << 24) - int(ev["start_ts"][3001] - ev["start_ts"][3000])
+    ev["duration"][sp[5:9]] = [(1 << 24) - 1, 1 << 24, 1 << 24 + 5, 0]  # 24-bit limit
     return t, ev
 
 
@@ -68,9 +87,9 @@ def test_wire_roundtrip_simkit(rt):
     t = rt.synth_trace(3000, 1, 2, n_ranks=8, fault="nvlink_saturation", onset=2000,
                        duration=150, target_rank=3, compact_names=False)
     w = rt.wire_pack(t.events, [0, len(t.events)])
-    assert w.events.nbytes == 8 * len(t.events)
-    assert len(w.escapes) == 0
-    assert w.nbytes < 16 * len(t.events)
+    assert w.events.nbytes == 4 * len(t.events)
+    assert len(w.escapes) < 1e-3 * len(t.events)  # run_batch spans >= 16.8 ms under the fault
+    assert w.nbytes < 10 * len(t.events)
     assert np.array_equal(unpack(w).view(np.uint8), t.events.view(np.uint8))
 
 
@@ -79,6 +98,22 @@ def test_wire_roundtrip_escapes_and_instances(rt):
     cut = [0, 1500, 1500, len(ev)]  # includes an empty instance
     w = rt.wire_pack(ev, cut, n_threads=3)
     assert len(w.escapes) > 20
+    assert np.array_equal(unpack(w).view(np.uint8), ev.view(np.uint8))
+
+
+def test_wire_dictionary_overflow_and_payload_range(rt):
+    """More distinct info words than the dictionary holds (the rarest ones
+    escape), batch payloads below the block's base or 2^16 above it."""
+    t = rt.synth_trace(600, 5, 6, n_ranks=2, compact_names=False)
+    ev = t.events.copy()
+    inst = np.nonzero(ev["kind"] == abi.INSTANT)[0]
+    ev["name_id"][inst[:400]] = 1000 + np.arange(400) % 300        # 300 extra info words
+    bat = np.nonzero((ev["flags"] & abi.EV_HAS_BATCH) != 0)[0]
+    ev["payload"][bat[3]] = 0                                       # below the block's base
+    ev["payload"][bat[7]] = ev["payload"][bat[6]] + np.uint64(70000)
+    w = rt.wire_pack(ev, [0, len(ev)], n_threads=2)
+    assert len(w.dict) == abi.WIRE_MAX_DICT
+    assert len(w.escapes) >= 300 - abi.WIRE_MAX_DICT  # the rarest words escape
     assert np.array_equal(unpack(w).view(np.uint8), ev.view(np.uint8))
 
 
@@ -95,8 +130,12 @@ def test_upload_wire_matches_upload(rt):
     sel = has & second
     ev["payload"][sel] = ev["payload"][sel] + np.uint64(len(traces[0].workloads))
     wl = np.concatenate([t.workloads for t in traces])
-    # a few escapes on span durations inside cycles
+    # escapes inside cycles: span durations of 2^24 ns and more, a 2^24 ns gap
+    sp = np.nonzero((ev["kind"] == abi.SPAN) & second)[0]
+    ev["duration"][sp[100:140]] += np.int64(1 << 24)
+    ev["start_ts"][sp[300]:int(off[2])] += np.int64(1 << 24)
     w = rt.wire_pack(ev, off)
+    assert len(w.escapes) >= 40
     names = traces[0].names
     out = []
     for kind in ("upload", "wire"):
