@@ -377,6 +377,33 @@ int cs_ingest_view(const cs_ingest_result* r, const cs_event** ev, const uint64_
                    uint32_t* n_comm, uint64_t* n_issues);
 void cs_ingest_free(cs_ingest_result* r);
 
+/* The ingest's ValidationReport (trace.hpp:129-148): the parse issues in
+ * document order followed by validate_trace's checks (trace.cpp:239-276:
+ * duplicate event ids, negative span durations, correlation ids, counter
+ * values and per-series monotonicity) in canonical event order, as
+ * (severity, stable code, event id).  category_counts is indexed by
+ * cs_category; a report with n_errors == 0 is what load_validated
+ * (main.cpp:41-56) accepts. */
+enum cs_issue_code {
+  CS_ISSUE_MALFORMED_EVENT = 0,
+  CS_ISSUE_MALFORMED_ARGS = 1,
+  CS_ISSUE_DUPLICATE_EVENT_ID = 2,
+  CS_ISSUE_NEGATIVE_DURATION = 3,
+  CS_ISSUE_DUPLICATE_CORRELATION = 4,
+  CS_ISSUE_UNMATCHED_CORRELATION = 5,
+  CS_ISSUE_NON_MONOTONE_COUNTER = 6
+};
+enum cs_severity { CS_SEV_ERROR = 0, CS_SEV_WARNING = 1 };
+typedef struct cs_ingest_issue {
+  uint8_t severity;      /* cs_severity */
+  uint8_t code;          /* cs_issue_code */
+  uint8_t has_event_id;
+  uint8_t reserved[5];
+  uint64_t event_id;
+} cs_ingest_issue;
+int cs_ingest_report(const cs_ingest_result* r, const cs_ingest_issue** issues, uint64_t* n_issues,
+                     uint64_t* n_parse_issues, uint64_t category_counts[8], uint64_t* n_errors);
+
 /* Latency model for instance `inst` (UINT32_MAX = default for every instance
  * without its own binding).  Bindings are by instance index, may precede the
  * first cs_upload and survive re-uploads (streams).

@@ -79,6 +79,7 @@ struct Results {
 
 struct Handle {
   LabeledDataset ds;
+  std::vector<ValidationIssue> parse_issues;  // from parse_trace_json
   Exported ex;
   bool exported = false;
   Results res;
@@ -459,7 +460,40 @@ void* ref_from_json(const char* text, size_t len, uint64_t* n_issues) {
   auto parsed = parse_trace_json(std::string(text, len));
   if (n_issues) *n_issues = parsed.issues.size();
   h->ds.trace = std::move(parsed.trace);
+  h->parse_issues = std::move(parsed.issues);
   return h.release();
+}
+
+// validate_trace(trace, parse issues) (trace.cpp:243-276): the report as
+// (severity, code, event id) records (cs_ingest_issue layout), per-category
+// counts and the error count.
+int ref_validate(void* hv, cs_ingest_issue* out, size_t cap, size_t* n, uint64_t* cats,
+                 uint64_t* n_errors) {
+  auto* h = static_cast<Handle*>(hv);
+  const ValidationReport rep = validate_trace(h->ds.trace, h->parse_issues);
+  static const char* kCodes[] = {"malformed_event",       "malformed_args",        "duplicate_event_id",
+                                 "negative_duration",     "duplicate_correlation", "unmatched_correlation",
+                                 "non_monotone_counter"};
+  if (n) *n = rep.issues.size();
+  if (n_errors) *n_errors = rep.error_count();
+  if (cats) {
+    for (int c = 0; c < 8; ++c) cats[c] = 0;
+    for (const auto& [c, k] : rep.category_counts) cats[static_cast<int>(c)] = k;
+  }
+  if (!out) return 0;
+  if (cap < rep.issues.size()) return 1;
+  for (size_t i = 0; i < rep.issues.size(); ++i) {
+    const auto& x = rep.issues[i];
+    cs_ingest_issue o{};
+    o.severity = x.severity == ValidationIssue::Severity::Error ? CS_SEV_ERROR : CS_SEV_WARNING;
+    o.code = 255;
+    for (uint8_t c = 0; c < 7; ++c)
+      if (x.code == kCodes[c]) o.code = c;
+    o.has_event_id = x.event_id ? 1 : 0;
+    o.event_id = x.event_id ? *x.event_id : 0;
+    out[i] = o;
+  }
+  return 0;
 }
 
 // Inverse ingest: binary records -> reference Trace.  forward_mode classes map

@@ -38,6 +38,7 @@ def lib():
         L.ref_to_json.argtypes = [vp, C.c_char_p, sz, C.POINTER(sz)]
         L.ref_from_json.restype = vp
         L.ref_from_json.argtypes = [C.c_char_p, sz, C.POINTER(C.c_uint64)]
+        L.ref_validate.argtypes = [vp, vp, sz, C.POINTER(sz), vp, C.POINTER(C.c_uint64)]
         L.ref_build.restype = vp
         L.ref_build.argtypes = [C.c_uint64, vp, vp, C.c_uint32, C.c_char_p, vp, C.c_uint32,
                                 C.c_char_p, vp, C.c_int]
@@ -165,6 +166,16 @@ class RefTrace:
         buf = C.create_string_buffer(n.value)
         L.ref_to_json(self.h, buf, n.value, C.byref(n))
         return buf.raw[:n.value]
+
+    def validate(self):
+        """validate_trace with the parse issues: (ISSUE_DTYPE records, category counts, n_errors)."""
+        L = lib()
+        n, ne = C.c_size_t(0), C.c_uint64(0)
+        cats = np.zeros(8, np.uint64)
+        L.ref_validate(self.h, None, 0, C.byref(n), cats.ctypes.data, C.byref(ne))
+        out = np.zeros(n.value, abi.ISSUE_DTYPE)
+        assert L.ref_validate(self.h, out.ctypes.data, n.value, C.byref(n), None, None) == 0
+        return out, cats, ne.value
 
     @classmethod
     def from_json(cls, text: bytes):

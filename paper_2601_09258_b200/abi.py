@@ -15,6 +15,13 @@ EVENT_DTYPE = np.dtype(
 assert EVENT_DTYPE.itemsize == 32
 
 # wire format (cs_wire_event header, 8 bytes): the host->device format
+ISSUE_DTYPE = np.dtype([("severity", "u1"), ("code", "u1"), ("has_event_id", "u1"),
+                        ("reserved", "u1", (5,)), ("event_id", "<u8")])
+assert ISSUE_DTYPE.itemsize == 16
+SEV_ERROR, SEV_WARNING = 0, 1
+ISSUE_CODES = ("malformed_event", "malformed_args", "duplicate_event_id", "negative_duration",
+               "duplicate_correlation", "unmatched_correlation", "non_monotone_counter")
+
 WIRE_BLOCK = 1024
 WIRE_ESCAPE = 0xFF          # dictionary code of an escaped event
 WIRE_MAX_DICT = 255

@@ -54,7 +54,19 @@ struct cs_ingest_result {
   uint32_t n_names = 0;
   std::vector<int32_t> comm_name, comm_rank;
   std::string comm_hash_packed;
-  uint64_t n_issues = 0;
+  uint64_t n_issues = 0;  // parse issues
+  std::vector<cs_ingest_issue> issues;  // parse issues, then validate_trace's
+  uint64_t categories[8] = {};
+  uint64_t n_errors = 0;
+  void issue(uint8_t sev, uint8_t code, bool has_id, uint64_t id) {
+    cs_ingest_issue x{};
+    x.severity = sev;
+    x.code = code;
+    x.has_event_id = has_id ? 1 : 0;
+    x.event_id = has_id ? id : 0;
+    issues.push_back(x);
+    n_errors += sev == CS_SEV_ERROR;
+  }
 };
 
 namespace {
@@ -552,7 +564,7 @@ struct Keys {
 
 // the args the path reads, after flattening (later writes win)
 struct Args {
-  Arg fm, batch, in, out, comm, rank, value;
+  Arg fm, batch, in, out, comm, rank, value, corr;
   uint64_t dropped = 0;
   Arg* slot(std::string_view k, const Keys& keys) {
     using namespace std::string_view_literals;
@@ -563,6 +575,7 @@ struct Args {
     if (k == "commHash"sv) return &comm;
     if (k == "rank"sv) return &rank;
     if (k == "value"sv) return &value;
+    if (k == "correlation_id"sv) return &corr;
     return nullptr;
   }
 };
@@ -716,7 +729,13 @@ const std::string_view* arg_string(const Arg& a) { return a.t == Arg::Str ? &a.s
 // ------------------------------------------------------------ records
 struct Rec {
   bool keep = false;
-  uint64_t issues = 0;
+  // parse issues, in the order parse_record pushes them: a leading one that
+  // ends the record (1 = not an event object / no "ph": error, 2 =
+  // unsupported phase: warning), or an unknown-category warning, one
+  // malformed_args warning per dropped args key, and a type error last
+  uint8_t lead = 0;
+  bool cat_warn = false, type_err = false;
+  uint32_t dropped = 0;
   bool has_eid = false;
   uint64_t eid = 0;
   int kind = 0, category = 0;
@@ -767,7 +786,7 @@ void parse_record(const char* b, const char* e, Rec& r, const Keys& keys, Arena&
     s.skip();
     s.ws();
     if (s.p != s.end) throw BadJson{};
-    r.issues = 1;  // "record is not an event object"
+    r.lead = 1;  // "record is not an event object"
     return;
   }
   ++s.p;
@@ -797,7 +816,7 @@ void parse_record(const char* b, const char* e, Rec& r, const Keys& keys, Arena&
   if (s.p != s.end) throw BadJson{};  // spans come from the parallel splitter, untrimmed
   try {
     if (!pos[kPh]) {
-      r.issues = 1;
+      r.lead = 1;
       return;
     }
     std::string buf;
@@ -805,7 +824,7 @@ void parse_record(const char* b, const char* e, Rec& r, const Keys& keys, Arena&
     if (ph == "M") return;
     r.kind = kind_from_phase(ph);
     if (r.kind < 0) {
-      r.issues = 1;
+      r.lead = 2;
       return;
     }
     if (pos[kEid]) {
@@ -828,7 +847,7 @@ void parse_record(const char* b, const char* e, Rec& r, const Keys& keys, Arena&
     r.category = r.kind == CS_COUNTER ? CS_CAT_COUNTER_TELEMETRY : CS_CAT_PYTHON_CALL;
     if (pos[kCat]) {
       const int c = category_from_string(as_string(pos[kCat], e, buf));
-      if (c < 0) ++r.issues;  // unknown category: warning, default kept
+      if (c < 0) r.cat_warn = true;  // unknown category: warning, default kept
       else r.category = c;
     }
     if (pos[kSrc]) {
@@ -855,12 +874,12 @@ void parse_record(const char* b, const char* e, Rec& r, const Keys& keys, Arena&
     }
     if (pos[kArgs]) {
       parse_args(pos[kArgs], e, r.args, keys, arena);
-      r.issues += r.args.dropped;
+      r.dropped = static_cast<uint32_t>(r.args.dropped);
     }
     r.keep = true;
   } catch (const TypeError&) {
     r.keep = false;
-    r.issues += 1;
+    r.type_err = true;
   }
 }
 
@@ -994,6 +1013,104 @@ const char* split_array(const char* a, const char* end, uint32_t n_threads,
   throw BadJson{};  // unterminated array
 }
 
+// validate_trace (trace.cpp:239-276) over the canonical record order: per
+// event a duplicate id (at its second occurrence), a negative span duration,
+// a non-span duration; then check_correlations (158-201) and check_counters
+// (203-235).  Duplicate ids are found in parallel (one hash partition of the
+// ids per thread, all scanning in event order) unless the ids increase.
+void validate(cs_ingest_result& res, const std::vector<std::pair<size_t, uint64_t>>& corr,
+              uint32_t n_threads) {
+  const size_t n = res.events.size();
+  const uint64_t* ids = res.event_ids.data();
+  for (const cs_event& e : res.events) ++res.categories[e.category & 7];
+  std::vector<uint8_t> dup2(n, 0);
+  bool increasing = true;
+  uint64_t lo = n ? ids[0] : 0, hi = lo;
+  for (size_t i = 1; i < n; ++i) {
+    increasing = increasing && ids[i] > ids[i - 1];
+    lo = std::min(lo, ids[i]);
+    hi = std::max(hi, ids[i]);
+  }
+  if (!increasing) {
+    // each thread owns a slice of the id space and scans every event in order
+    const bool dense = hi - lo < 8 * static_cast<uint64_t>(n) + 64;
+    parallel_for(n_threads, n_threads, [&](size_t t0, size_t t1, uint32_t) {
+      for (size_t t = t0; t < t1; ++t) {
+        if (dense) {
+          const uint64_t span = hi - lo + 1;
+          const uint64_t a = lo + span * t / n_threads, b = lo + span * (t + 1) / n_threads;
+          std::vector<uint64_t> once((b - a + 63) / 64, 0), twice((b - a + 63) / 64, 0);
+          for (size_t i = 0; i < n; ++i) {
+            const uint64_t x = ids[i];
+            if (x < a || x >= b) continue;
+            const uint64_t k = x - a, w = k >> 6, m = 1ull << (k & 63);
+            if (!(once[w] & m)) {
+              once[w] |= m;
+            } else if (!(twice[w] & m)) {
+              twice[w] |= m;
+              dup2[i] = 1;
+            }
+          }
+        } else {
+          std::unordered_map<uint64_t, uint32_t> seen;
+          for (size_t i = 0; i < n; ++i) {
+            if ((ids[i] * 0x9E3779B97F4A7C15ull >> 40) % n_threads != t) continue;
+            if (++seen[ids[i]] == 2) dup2[i] = 1;
+          }
+        }
+      }
+    });
+  }
+  for (size_t i = 0; i < n; ++i) {
+    const cs_event& e = res.events[i];
+    if (dup2[i]) res.issue(CS_SEV_ERROR, CS_ISSUE_DUPLICATE_EVENT_ID, true, ids[i]);
+    if (e.kind == CS_SPAN && e.duration < 0)
+      res.issue(CS_SEV_ERROR, CS_ISSUE_NEGATIVE_DURATION, true, ids[i]);
+    if (e.kind != CS_SPAN && e.kind != CS_COUNTER && e.duration != 0)
+      res.issue(CS_SEV_ERROR, CS_ISSUE_MALFORMED_EVENT, true, ids[i]);
+  }
+  // correlations: host side = RuntimeApi, device side = GpuKernel / MemCopy
+  if (!corr.empty()) {
+    std::unordered_map<uint64_t, int> host, device;
+    auto is_dev = [&](size_t i) {
+      return res.events[i].category == CS_CAT_GPU_KERNEL || res.events[i].category == CS_CAT_MEM_COPY;
+    };
+    for (const auto& [i, c] : corr) {
+      if (res.events[i].category == CS_CAT_RUNTIME_API) ++host[c];
+      else if (is_dev(i)) ++device[c];
+    }
+    for (const auto& [i, c] : corr) {
+      if (is_dev(i)) {
+        if (device[c] > 1) res.issue(CS_SEV_ERROR, CS_ISSUE_DUPLICATE_CORRELATION, true, ids[i]);
+        else if (!host.count(c)) res.issue(CS_SEV_WARNING, CS_ISSUE_UNMATCHED_CORRELATION, true, ids[i]);
+      } else if (res.events[i].category == CS_CAT_RUNTIME_API && host[c] > 1) {
+        res.issue(CS_SEV_ERROR, CS_ISSUE_DUPLICATE_CORRELATION, true, ids[i]);
+      }
+    }
+  }
+  // counters: a numeric, finite value; strictly increasing ts per series name
+  std::vector<int64_t> last(res.n_names, 0);
+  std::vector<uint8_t> has_last(res.n_names, 0), flagged(res.n_names, 0);
+  for (size_t i = 0; i < n; ++i) {
+    const cs_event& e = res.events[i];
+    if (e.kind != CS_COUNTER) continue;
+    if (!(e.flags & CS_EV_HAS_VALUE)) {
+      res.issue(CS_SEV_ERROR, CS_ISSUE_MALFORMED_ARGS, true, ids[i]);
+      continue;
+    }
+    double v;
+    std::memcpy(&v, &e.duration, sizeof v);
+    if (!std::isfinite(v)) res.issue(CS_SEV_ERROR, CS_ISSUE_MALFORMED_ARGS, true, ids[i]);
+    const uint32_t k = e.name_id;
+    if (has_last[k] && e.start_ts <= last[k] && !flagged[k]) {
+      res.issue(CS_SEV_ERROR, CS_ISSUE_NON_MONOTONE_COUNTER, true, ids[i]);
+      flagged[k] = 1;
+    }
+    last[k] = e.start_ts;
+    has_last[k] = 1;
+  }
+}
+
 struct CommKey {
   std::string_view name, hash;
   int rank;
@@ -1024,6 +1141,7 @@ int cs_ingest_chrome_json(const char* text, size_t len, const cs_ingest_keys* ke
   auto* res = new cs_ingest_result();
   auto reject = [&]() {
     res->n_issues = 1;  // parse_error: empty trace, one issue
+    res->issue(CS_SEV_ERROR, CS_ISSUE_MALFORMED_EVENT, false, 0);
     *out = res;
     return CS_OK;
   };
@@ -1087,6 +1205,7 @@ int cs_ingest_chrome_json(const char* text, size_t len, const cs_ingest_keys* ke
     }
     if (not_events) {
       res->n_issues = 1;  // neither an event array nor an object with traceEvents
+      res->issue(CS_SEV_ERROR, CS_ISSUE_MALFORMED_EVENT, false, 0);
       *out = res;
       return CS_OK;
     }
@@ -1119,10 +1238,19 @@ int cs_ingest_chrome_json(const char* text, size_t len, const cs_ingest_keys* ke
   // ---- fallback ids in document order, then the canonical stable sort
   std::vector<Rec*> kept;
   kept.reserve(spans.size());
-  uint64_t next_id = 1, issues = 0;
+  uint64_t next_id = 1;
   for (uint32_t t = 0; t < n_threads; ++t)
     for (Rec& r : chunks[t]) {
-      issues += r.issues;
+      // parse issues; event_id as parse_record saw it (eid, or the fallback)
+      const uint64_t id_now = r.has_eid ? r.eid : next_id;
+      if (r.lead) {
+        res->issue(r.lead == 1 ? CS_SEV_ERROR : CS_SEV_WARNING, CS_ISSUE_MALFORMED_EVENT, false, 0);
+      } else {
+        if (r.cat_warn) res->issue(CS_SEV_WARNING, CS_ISSUE_MALFORMED_EVENT, true, id_now);
+        for (uint32_t q = 0; q < r.dropped; ++q)
+          res->issue(CS_SEV_WARNING, CS_ISSUE_MALFORMED_ARGS, true, id_now);
+        if (r.type_err) res->issue(CS_SEV_ERROR, CS_ISSUE_MALFORMED_EVENT, false, 0);
+      }
       if (!r.keep) continue;
       if (!r.has_eid) r.eid = next_id;
       next_id = std::max(next_id, r.eid) + 1;
@@ -1190,9 +1318,12 @@ int cs_ingest_chrome_json(const char* text, size_t len, const cs_ingest_keys* ke
   res->events.resize(kept.size());
   res->event_ids.resize(kept.size());
   std::vector<uint8_t> carries(kept.size(), 0);
-  parallel_for(kept.size(), n_threads, [&](size_t k0, size_t k1, uint32_t) {
+  // correlation ids (integer args.correlation_id, trace_io.cpp:151-156), per worker in order
+  std::vector<std::vector<std::pair<size_t, uint64_t>>> tcorr(n_threads);
+  parallel_for(kept.size(), n_threads, [&](size_t k0, size_t k1, uint32_t t) {
     for (size_t i = k0; i < k1; ++i) {
       const Rec& r = *kept[i];
+      if (r.args.corr.t == Arg::Int) tcorr[t].push_back({i, static_cast<uint64_t>(r.args.corr.i)});
       cs_event& o = res->events[i];
       std::memset(&o, 0, sizeof o);
       o.start_ts = r.start;
@@ -1245,7 +1376,10 @@ int cs_ingest_chrome_json(const char* text, size_t len, const cs_ingest_keys* ke
     res->events[i].payload |= static_cast<uint64_t>(res->workloads.size());
     res->workloads.push_back({*b, in ? *in : INT64_MIN, ou ? *ou : INT64_MIN});
   }
-  res->n_issues = issues;
+  res->n_issues = res->issues.size();
+  std::vector<std::pair<size_t, uint64_t>> corr;
+  for (const auto& v : tcorr) corr.insert(corr.end(), v.begin(), v.end());
+  validate(*res, corr, n_threads);
   *out = res;
   return CS_OK;
 }
@@ -1270,6 +1404,17 @@ int cs_ingest_view(const cs_ingest_result* r, const cs_event** ev, const uint64_
   if (comm_bytes) *comm_bytes = r->comm_hash_packed.size();
   if (n_comm) *n_comm = static_cast<uint32_t>(r->comm_name.size());
   if (n_issues) *n_issues = r->n_issues;
+  return CS_OK;
+}
+
+int cs_ingest_report(const cs_ingest_result* r, const cs_ingest_issue** issues, uint64_t* n_issues,
+                     uint64_t* n_parse_issues, uint64_t category_counts[8], uint64_t* n_errors) {
+  if (!r) return CS_E_INVALID_ARGUMENT;
+  if (issues) *issues = r->issues.data();
+  if (n_issues) *n_issues = r->issues.size();
+  if (n_parse_issues) *n_parse_issues = r->n_issues;
+  if (category_counts) std::memcpy(category_counts, r->categories, sizeof r->categories);
+  if (n_errors) *n_errors = r->n_errors;
   return CS_OK;
 }
 

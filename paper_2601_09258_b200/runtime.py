@@ -65,6 +65,7 @@ def lib():
                                  C.POINTER(vp), C.POINTER(vp), C.POINTER(vp), psz, C.POINTER(u32),
                                  C.POINTER(u64)]
     L.cs_ingest_free.argtypes = [vp]
+    L.cs_ingest_report.argtypes = [vp, C.POINTER(vp), C.POINTER(u64), C.POINTER(u64), vp, C.POINTER(u64)]
     L.cs_load_model.argtypes = [vp, u32, C.POINTER(abi.Model)]
     L.cs_run.argtypes = [vp, u32]
     L.cs_sync.argtypes = [vp]
@@ -113,7 +114,7 @@ def lib():
 EXPORTED_SYMBOLS = [
     "cs_abi_version", "cs_status_type", "cs_ctx_create", "cs_ctx_destroy", "cs_last_error",
     "cs_set_config", "cs_set_name_table", "cs_upload", "cs_upload_wire", "cs_wire_pack",
-    "cs_wire_view", "cs_wire_free", "cs_ingest_chrome_json", "cs_ingest_view", "cs_ingest_free", "cs_load_model", "cs_run", "cs_sync",
+    "cs_wire_view", "cs_wire_free", "cs_ingest_chrome_json", "cs_ingest_view", "cs_ingest_free", "cs_ingest_report", "cs_load_model", "cs_run", "cs_sync",
     "cs_get_summary", "cs_get_candidates", "cs_get_cycles", "cs_get_components", "cs_get_beta",
     "cs_get_collective_beta", "cs_get_mu", "cs_get_records", "cs_get_alerts", "cs_host_alloc",
     "cs_host_free", "cs_get_timings", "cs_get_launch_count", "cs_fit_latency_model",
@@ -298,7 +299,15 @@ class IngestedTrace:
     comm_name: np.ndarray
     comm_rank: np.ndarray
     comm_hash: list
-    n_issues: int
+    n_issues: int                  # parse issues (parse_trace_json's ValidationIssue count)
+    issues: np.ndarray = None      # ISSUE_DTYPE: parse issues, then validate_trace's
+    category_counts: np.ndarray = None
+    n_errors: int = 0
+
+    @property
+    def ok(self) -> bool:
+        """ValidationReport::ok(): what load_validated (main.cpp:41-56) accepts."""
+        return self.n_errors == 0
 
     @property
     def n_comm(self) -> int:
@@ -328,10 +337,14 @@ def ingest_chrome_json(text: bytes, n_threads=None) -> IngestedTrace:
 
         names = C.string_at(nm, nb.value).split(b"\0")[:nn.value] if nb.value else []
         hashes = C.string_at(ch, cb.value).split(b"\0")[:nc.value] if cb.value else []
+        ip, ni, npi, ne = C.c_void_p(), C.c_uint64(), C.c_uint64(), C.c_uint64()
+        cats = np.zeros(8, np.uint64)
+        _check(L.cs_ingest_report(h, C.byref(ip), C.byref(ni), C.byref(npi), cats.ctypes.data, C.byref(ne)))
         return IngestedTrace(arr(ev, nev.value, abi.EVENT_DTYPE), arr(ids, nev.value, np.uint64),
                              arr(wl, nwl.value, abi.WORKLOAD_DTYPE), [x.decode() for x in names],
                              arr(cn, nc.value, np.int32), arr(cr, nc.value, np.int32),
-                             [x.decode() for x in hashes], iss.value)
+                             [x.decode() for x in hashes], iss.value,
+                             arr(ip, ni.value, abi.ISSUE_DTYPE), cats, ne.value)
     finally:
         L.cs_ingest_free(h)
 

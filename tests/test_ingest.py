@@ -8,7 +8,7 @@ import json
 import numpy as np
 import pytest
 
-from paper_2601_09258_b200 import runtime as rt
+from paper_2601_09258_b200 import abi, runtime as rt
 
 
 def _compare(refbridge, text: bytes):
@@ -22,6 +22,11 @@ def _compare(refbridge, text: bytes):
     assert got.workloads.tobytes() == ex.workloads.tobytes()
     assert got.comm_hash == ex.comm_hash
     assert list(got.comm_rank) == list(ex.comm_rank)
+    # the ValidationReport (validate_trace with the parse issues)
+    iss, cats, n_err = ref.validate()
+    assert got.issues.tobytes() == iss.tobytes()
+    assert np.array_equal(got.category_counts, cats)
+    assert got.n_errors == n_err and got.ok == (n_err == 0)
     return got
 
 
@@ -149,3 +154,50 @@ def test_parallel_split_adversarial_strings(refbridge, seed):
     for nt in (1, 8):
         r = rt.ingest_chrome_json(bad, n_threads=nt)
         assert r.n_issues == 1 and len(r.events) == 0
+
+
+VALIDATION = [
+    # duplicate ids (reported once, at the second occurrence), negative spans
+    {"ph": "X", "name": "a", "ts": 1, "dur": 1, "eid": 5},
+    {"ph": "X", "name": "b", "ts": 2, "dur": 1, "eid": 5},
+    {"ph": "i", "name": "c", "ts": 3, "eid": 5},
+    {"ph": "X", "name": "neg", "ts": 4, "dur": -1},
+    # correlations: matched, unmatched device, duplicate device / host, float ids
+    {"ph": "X", "name": "launch", "ts": 5, "dur": 1, "cat": "runtime_api", "args": {"correlation_id": 1}},
+    {"ph": "X", "name": "k1", "ts": 6, "dur": 1, "cat": "gpu_kernel", "args": {"correlation_id": 1}},
+    {"ph": "X", "name": "k2", "ts": 7, "dur": 1, "cat": "gpu_kernel", "args": {"correlation_id": 2}},
+    {"ph": "X", "name": "m1", "ts": 8, "dur": 1, "cat": "mem_copy", "args": {"correlation_id": 3}},
+    {"ph": "X", "name": "m2", "ts": 9, "dur": 1, "cat": "mem_copy", "args": {"correlation_id": 3}},
+    {"ph": "X", "name": "l2", "ts": 10, "dur": 1, "cat": "runtime_api", "args": {"correlation_id": 4}},
+    {"ph": "X", "name": "l3", "ts": 11, "dur": 1, "cat": "runtime_api", "args": {"correlation_id": 4}},
+    {"ph": "X", "name": "kf", "ts": 12, "dur": 1, "cat": "gpu_kernel", "args": {"correlation_id": 9.5}},
+    {"ph": "X", "name": "py", "ts": 13, "dur": 1, "args": {"correlation_id": 77}},
+    # counters: missing / non-numeric value, non-increasing series (flagged once)
+    {"ph": "C", "name": "cpu", "ts": 20, "args": {"value": 1}},
+    {"ph": "C", "name": "cpu", "ts": 20, "args": {"value": 2}},
+    {"ph": "C", "name": "cpu", "ts": 19, "args": {"value": 3}},
+    {"ph": "C", "name": "gpu", "ts": 21, "args": {"other": 1}},
+    {"ph": "C", "name": "gpu", "ts": 22, "args": {"value": "x"}},
+    {"ph": "C", "name": "mem", "ts": 23, "args": {"value": True}},
+    # parse-side issues with event ids (unknown category, dropped null args)
+    {"ph": "X", "name": "odd", "ts": 24, "dur": 1, "cat": "zzz", "args": {"p": None, "q": None}},
+    {"ph": "X", "name": "odd2", "ts": 25, "dur": 1, "cat": "zzz", "eid": 900, "src": {"collector": 3}},
+]
+
+
+@pytest.mark.parametrize("wrap", [False, True])
+def test_validation_report(refbridge, wrap):
+    got = _compare(refbridge, _doc(VALIDATION, wrap))
+    codes = {abi.ISSUE_CODES[c] for c in got.issues["code"]}
+    assert {"duplicate_event_id", "negative_duration", "duplicate_correlation",
+            "unmatched_correlation", "non_monotone_counter", "malformed_args"} <= codes
+    assert not got.ok
+
+
+def test_validation_many_duplicate_ids(refbridge):
+    """Out-of-order, repeating explicit ids (the parallel duplicate search)."""
+    rng = np.random.default_rng(3)
+    recs = [{"ph": "X", "name": f"n{i % 7}", "ts": int(t), "dur": 1, "eid": int(e)}
+            for i, (t, e) in enumerate(zip(rng.integers(0, 5000, 20000), rng.integers(0, 15000, 20000)))]
+    got = _compare(refbridge, _doc(recs))
+    assert (got.issues["code"] == 2).sum() > 1000
