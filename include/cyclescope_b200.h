@@ -539,6 +539,21 @@ int cs_fit_latency_model(uint64_t n, uint32_t n_features, const int32_t* feature
                          const double* x, const double* y,
                          const cs_gbdt_params* params, const cs_fit_options* opt,
                          cs_fitted_model** out, char* err, size_t err_cap);
+/* Batched fit_latency_model on the device: n_models
+ * independent sample sets (model m: rows [offsets[m], offsets[m+1]) of x / y,
+ * x row-major), each fitted exactly as cs_fit_latency_model would (the model
+ * JSON is byte-identical).  Checks, split_calibration and the holdout
+ * statistics run on n_threads host threads; the boosting rounds of every
+ * model run in one kernel, one CTA per model (k_gbdt_fit: libstdc++'s sort
+ * order restated for the split search, sequential sums kept sequential).
+ * status[m] is model m's cs_status; out[m] is NULL unless it is CS_OK.
+ * device_ms (optional) receives the kernel time.  Supports max_depth <= 8 and
+ * 1..8 features (CS_E_UNSUPPORTED otherwise). */
+int cs_fit_latency_models(int device, uint32_t n_models, const uint64_t* offsets,
+                          uint32_t n_features, const int32_t* feature_ids, const double* x,
+                          const double* y, const cs_gbdt_params* params, const cs_fit_options* opt,
+                          uint32_t n_threads, cs_fitted_model** out, int32_t* status,
+                          float* device_ms);
 /* Parse a LatencyModel JSON document (baseline.cpp:288-302). */
 int cs_model_from_json(const char* json, cs_fitted_model** out, char* err, size_t err_cap);
 /* Serialize to the reference's LatencyModel JSON (baseline.cpp:277-286). */

@@ -15,8 +15,11 @@
 #include <utility>
 #include <vector>
 
+#include <thread>
+
 #include <nlohmann/json.hpp>
 
+#include "cs_fit.h"
 #include "cyclescope_b200.h"
 
 using nlohmann::json;
@@ -227,6 +230,64 @@ void rebuild_flat(cs_fitted_model& m) {
   for (const auto& n : m.feature_names) m.feature_ids.push_back(feature_id_of(n));
 }
 
+// fit_latency_model's checks and split_calibration (baseline.cpp:118-149,
+// 168-180): training and holdout rows, each in chronological order
+void split_rows(uint64_t n, uint32_t n_features, const double* x, const double* y,
+                const cs_gbdt_params* params, const cs_fit_options* opt, std::vector<uint32_t>& train,
+                std::vector<uint32_t>& calib) {
+  const uint64_t min_required = std::max<uint64_t>(opt->min_samples, 2 * params->min_samples_leaf);
+  if (n < min_required)
+    throw FitError{CS_E_INSUFFICIENT_DATA, "need at least " + std::to_string(min_required) +
+                                               " samples, got " + std::to_string(n)};
+  for (uint64_t i = 0; i < n; ++i)
+    if (!(y[i] > 0.0) || !std::isfinite(y[i]))
+      throw FitError{CS_E_INSUFFICIENT_DATA, "targets must be positive and finite"};
+  const uint32_t sc = (opt->stratify_col >= 0 && static_cast<uint32_t>(opt->stratify_col) < n_features)
+                          ? static_cast<uint32_t>(opt->stratify_col)
+                          : 0u;
+  std::vector<uint32_t> order(n);
+  std::iota(order.begin(), order.end(), 0u);
+  std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) {
+    return x[static_cast<uint64_t>(a) * n_features + sc] < x[static_cast<uint64_t>(b) * n_features + sc];
+  });
+  const uint64_t stride =
+      opt->calibration_fraction > 0.0
+          ? std::max<uint64_t>(2, static_cast<uint64_t>(std::llround(1.0 / opt->calibration_fraction)))
+          : n + 1;
+  for (uint64_t pos = 0; pos < n; ++pos)
+    (pos % stride == stride - 1 ? calib : train).push_back(order[pos]);
+  std::sort(train.begin(), train.end());
+  std::sort(calib.begin(), calib.end());
+}
+
+// holdout residual statistics (baseline.cpp:186-205)
+void holdout_stats(cs_fitted_model& m, const double* x, const double* y, uint32_t n_features,
+                   const std::vector<uint32_t>& calib, const cs_fit_options* opt) {
+  std::vector<double> res;
+  for (uint32_t r : calib) {
+    const double p = clamp_predict(m, x + static_cast<uint64_t>(r) * n_features);
+    res.push_back(std::max(0.0, (y[r] - p) / (y[r] + opt->ppe_epsilon)));
+  }
+  m.calibration_size = res.size();
+  if (!res.empty()) {
+    double mean = 0.0;
+    for (double v : res) mean += v;
+    mean /= static_cast<double>(res.size());
+    double var = 0.0;
+    for (double v : res) var += (v - mean) * (v - mean);
+    var = res.size() > 1 ? var / static_cast<double>(res.size() - 1) : 0.0;
+    m.mu = mean;
+    m.sigma = std::sqrt(var);
+  }
+}
+
+void set_features(cs_fitted_model& m, uint32_t n_features, const int32_t* feature_ids) {
+  for (uint32_t f = 0; f < n_features; ++f) {
+    if (feature_ids[f] < 0 || feature_ids[f] > 4) throw FitError{CS_E_FEATURE_MISMATCH, "unknown feature id"};
+    m.feature_names.push_back(kFeatureNames[feature_ids[f]]);
+  }
+}
+
 }  // namespace
 
 extern "C" {
@@ -240,36 +301,9 @@ int cs_fit_latency_model(uint64_t n, uint32_t n_features, const int32_t* feature
   auto m = new cs_fitted_model();
   try {
     m->params = *params;
-    for (uint32_t f = 0; f < n_features; ++f) {
-      if (feature_ids[f] < 0 || feature_ids[f] > 4) throw FitError{CS_E_FEATURE_MISMATCH, "unknown feature id"};
-      m->feature_names.push_back(kFeatureNames[feature_ids[f]]);
-    }
-    // fit_latency_model (baseline.cpp:168-208)
-    const uint64_t min_required = std::max<uint64_t>(opt->min_samples, 2 * params->min_samples_leaf);
-    if (n < min_required)
-      throw FitError{CS_E_INSUFFICIENT_DATA, "need at least " + std::to_string(min_required) +
-                                                 " samples, got " + std::to_string(n)};
-    for (uint64_t i = 0; i < n; ++i)
-      if (!(y[i] > 0.0) || !std::isfinite(y[i]))
-        throw FitError{CS_E_INSUFFICIENT_DATA, "targets must be positive and finite"};
-    // split_calibration (118-149): round robin over a stable w_kv order
-    const uint32_t sc = (opt->stratify_col >= 0 && static_cast<uint32_t>(opt->stratify_col) < n_features)
-                            ? static_cast<uint32_t>(opt->stratify_col)
-                            : 0u;
-    std::vector<uint32_t> order(n);
-    std::iota(order.begin(), order.end(), 0u);
-    std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) {
-      return x[static_cast<uint64_t>(a) * n_features + sc] < x[static_cast<uint64_t>(b) * n_features + sc];
-    });
-    const uint64_t stride =
-        opt->calibration_fraction > 0.0
-            ? std::max<uint64_t>(2, static_cast<uint64_t>(std::llround(1.0 / opt->calibration_fraction)))
-            : n + 1;
+    set_features(*m, n_features, feature_ids);
     std::vector<uint32_t> train, calib;
-    for (uint64_t pos = 0; pos < n; ++pos)
-      (pos % stride == stride - 1 ? calib : train).push_back(order[pos]);
-    std::sort(train.begin(), train.end());
-    std::sort(calib.begin(), calib.end());
+    split_rows(n, n_features, x, y, params, opt, train, calib);
     Matrix tx;
     tx.cols = n_features;
     tx.rows = train.size();
@@ -280,22 +314,7 @@ int cs_fit_latency_model(uint64_t n, uint32_t n_features, const int32_t* feature
       ty.push_back(y[r]);
     }
     fit_gbdt_into(*m, tx, ty);
-    std::vector<double> res;
-    for (uint32_t r : calib) {
-      const double p = clamp_predict(*m, x + static_cast<uint64_t>(r) * n_features);
-      res.push_back(std::max(0.0, (y[r] - p) / (y[r] + opt->ppe_epsilon)));
-    }
-    m->calibration_size = res.size();
-    if (!res.empty()) {
-      double mean = 0.0;
-      for (double v : res) mean += v;
-      mean /= static_cast<double>(res.size());
-      double var = 0.0;
-      for (double v : res) var += (v - mean) * (v - mean);
-      var = res.size() > 1 ? var / static_cast<double>(res.size() - 1) : 0.0;
-      m->mu = mean;
-      m->sigma = std::sqrt(var);
-    }
+    holdout_stats(*m, x, y, n_features, calib, opt);
     rebuild_flat(*m);
   } catch (const FitError& e) {
     set_err(err, err_cap, e.msg);
@@ -303,6 +322,92 @@ int cs_fit_latency_model(uint64_t n, uint32_t n_features, const int32_t* feature
     return e.code;
   }
   *out = m;
+  return CS_OK;
+}
+
+int cs_fit_latency_models(int device, uint32_t n_models, const uint64_t* offsets,
+                          uint32_t n_features, const int32_t* feature_ids, const double* x,
+                          const double* y, const cs_gbdt_params* params, const cs_fit_options* opt,
+                          uint32_t n_threads, cs_fitted_model** out, int32_t* status,
+                          float* device_ms) {
+  if (!out || !status || !params || !opt || !feature_ids || !offsets || n_features == 0)
+    return CS_E_INVALID_ARGUMENT;
+  if (offsets[0] != 0) return CS_E_INVALID_ARGUMENT;
+  for (uint32_t m = 0; m < n_models; ++m)
+    if (offsets[m + 1] < offsets[m]) return CS_E_INVALID_ARGUMENT;
+  if (offsets[n_models] && (!x || !y)) return CS_E_INVALID_ARGUMENT;
+  if (n_threads == 0) n_threads = 1;
+  for (uint32_t m = 0; m < n_models; ++m) {
+    out[m] = nullptr;
+    status[m] = CS_OK;
+  }
+  // host: checks and holdout split per model (parallel over models)
+  std::vector<std::vector<uint32_t>> train(n_models), calib(n_models);
+  auto par = [&](auto body) {
+    std::vector<std::thread> th;
+    const uint32_t nt = std::max<uint32_t>(1, std::min(n_threads, n_models));
+    for (uint32_t t = 0; t < nt; ++t)
+      th.emplace_back([&, t] {
+        for (uint32_t m = t; m < n_models; m += nt) body(m);
+      });
+    for (auto& h : th) h.join();
+  };
+  par([&](uint32_t m) {
+    const uint64_t o = offsets[m], n = offsets[m + 1] - o;
+    try {
+      cs_fitted_model probe;
+      set_features(probe, n_features, feature_ids);
+      split_rows(n, n_features, x + o * n_features, y + o, params, opt, train[m], calib[m]);
+    } catch (const FitError& e) {
+      status[m] = e.code;
+    }
+  });
+  // device: fit_gbdt of every model's training rows
+  GbdtBatch b;
+  b.n_features = n_features;
+  b.params = *params;
+  b.off.assign(n_models + 1, 0);
+  for (uint32_t m = 0; m < n_models; ++m)
+    b.off[m + 1] = b.off[m] + (status[m] == CS_OK ? train[m].size() : 0);
+  b.x_col.resize(b.off[n_models] * n_features);
+  b.y.resize(b.off[n_models]);
+  par([&](uint32_t m) {
+    if (status[m] != CS_OK) return;
+    const uint64_t o = offsets[m], to = b.off[m], tn = train[m].size();
+    for (uint64_t k = 0; k < tn; ++k) {
+      const uint64_t r = o + train[m][k];
+      for (uint32_t f = 0; f < n_features; ++f) b.x_col[to * n_features + f * tn + k] = x[r * n_features + f];
+      b.y[to + k] = y[r];
+    }
+  });
+  std::string err;
+  const int rc = gbdt_fit_device(device, b, err);
+  if (rc != CS_OK) return rc;
+  if (device_ms) *device_ms = b.device_ms;
+  // host: models and holdout statistics
+  par([&](uint32_t m) {
+    if (status[m] != CS_OK) return;
+    auto* fm = new cs_fitted_model();
+    fm->params = *params;
+    set_features(*fm, n_features, feature_ids);
+    fm->n_features = n_features;
+    fm->base = b.base[m];
+    fm->degenerate = b.degenerate[m] != 0;
+    fm->importance.assign(b.importance.begin() + static_cast<size_t>(m) * n_features,
+                          b.importance.begin() + static_cast<size_t>(m + 1) * n_features);
+    if (!fm->degenerate) {
+      for (uint64_t t = 0; t < params->n_trees; ++t) {
+        const cs_tree_node* src = &b.nodes[(static_cast<size_t>(m) * params->n_trees + t) * b.node_stride];
+        std::vector<FitNode> tree(b.n_nodes[static_cast<size_t>(m) * params->n_trees + t]);
+        for (size_t k = 0; k < tree.size(); ++k)
+          tree[k] = FitNode{src[k].feature, src[k].threshold, src[k].left, src[k].right, src[k].value};
+        fm->trees.push_back(std::move(tree));
+      }
+    }
+    holdout_stats(*fm, x + offsets[m] * n_features, y + offsets[m], n_features, calib[m], opt);
+    rebuild_flat(*fm);
+    out[m] = fm;
+  });
   return CS_OK;
 }
 

@@ -90,6 +90,8 @@ def lib():
     L.cs_host_free.argtypes = [vp]
     L.cs_get_timings.argtypes = [vp, vp, sz, psz, C.c_char_p, sz]
     L.cs_get_launch_count.argtypes = [vp, C.POINTER(u64)]
+    L.cs_fit_latency_models.argtypes = [C.c_int, u32, vp, u32, vp, vp, vp, C.POINTER(abi.GbdtParams),
+                                        C.POINTER(abi.FitOptions), u32, vp, vp, C.POINTER(C.c_float)]
     L.cs_fit_latency_model.argtypes = [u64, u32, vp, vp, vp, C.POINTER(abi.GbdtParams),
                                        C.POINTER(abi.FitOptions), C.POINTER(vp), C.c_char_p, sz]
     L.cs_model_from_json.argtypes = [C.c_char_p, C.POINTER(vp), C.c_char_p, sz]
@@ -117,7 +119,7 @@ EXPORTED_SYMBOLS = [
     "cs_wire_view", "cs_wire_free", "cs_ingest_chrome_json", "cs_ingest_view", "cs_ingest_free", "cs_ingest_report", "cs_load_model", "cs_run", "cs_sync",
     "cs_get_summary", "cs_get_candidates", "cs_get_cycles", "cs_get_components", "cs_get_beta",
     "cs_get_collective_beta", "cs_get_mu", "cs_get_records", "cs_get_alerts", "cs_host_alloc",
-    "cs_host_free", "cs_get_timings", "cs_get_launch_count", "cs_fit_latency_model",
+    "cs_host_free", "cs_get_timings", "cs_get_launch_count", "cs_fit_latency_model", "cs_fit_latency_models",
     "cs_model_from_json", "cs_model_to_json", "cs_model_view", "cs_model_free",
     "cs_ucl_from_stats", "cs_compute_ucl", "cs_config_from_json", "cs_synth_generate",
     "cs_synth_view", "cs_synth_names", "cs_synth_free", "cs_set_option", "cs_microbench",
@@ -198,6 +200,35 @@ def fit_latency_model(x: np.ndarray, y: np.ndarray, feature_names=("batch", "w_k
     if rc:
         raise EngineError(rc, err.value.decode())
     return LatencyModel(h)
+
+
+def fit_latency_models(xs, ys, feature_names=("batch", "w_kv"),
+                       params: abi.GbdtParams | None = None,
+                       options: abi.FitOptions | None = None, device: int = 0, n_threads=None):
+    """Batched fit_latency_model on the device (cs_fit_latency_models): one model
+    per (x, y) pair, each identical to fit_latency_model's.  Returns (models,
+    device_ms); a model that cannot be fitted is an EngineError in the list."""
+    ids = np.array([abi.FEATURE_IDS[n] for n in feature_names], dtype=np.int32)
+    params = params or abi.default_gbdt_params()
+    if options is None:
+        options = abi.default_fit_options(len(ids))
+        options.stratify_col = list(feature_names).index("w_kv") if "w_kv" in feature_names else 0
+    xs = [np.ascontiguousarray(x, dtype=np.float64).reshape(-1, len(ids)) for x in xs]
+    ys = [np.ascontiguousarray(y, dtype=np.float64) for y in ys]
+    off = np.concatenate([[0], np.cumsum([len(y) for y in ys])]).astype(np.uint64)
+    x = np.ascontiguousarray(np.concatenate(xs) if xs else np.zeros((0, len(ids))))
+    y = np.ascontiguousarray(np.concatenate(ys) if ys else np.zeros(0))
+    M = len(ys)
+    out = (C.c_void_p * max(M, 1))()
+    status = np.zeros(max(M, 1), np.int32)
+    ms = C.c_float(0)
+    _check(lib().cs_fit_latency_models(device, M, off.ctypes.data, len(ids), ids.ctypes.data, _ptr(x),
+                                       _ptr(y), C.byref(params), C.byref(options),
+                                       n_threads or os.cpu_count() or 1, out, status.ctypes.data,
+                                       C.byref(ms)))
+    models = [LatencyModel(C.c_void_p(out[m])) if status[m] == 0 else EngineError(int(status[m]), "fit failed")
+              for m in range(M)]
+    return models, ms.value
 
 
 def ucl_from_stats(mu: float, sigma: float, control: abi.ControlConfig) -> float:
