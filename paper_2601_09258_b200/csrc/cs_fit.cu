@@ -24,6 +24,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <string>
 
 #include "cs_fit.h"
@@ -31,7 +33,8 @@
 
 namespace {
 
-constexpr int kFitThreads = 256;
+constexpr int kFitThreads = 512;
+constexpr int kFitWarps = kFitThreads / 32;
 constexpr int kMaxDepth = 8;  // node table: 2^(kMaxDepth+1) - 1 entries
 
 struct BNode {
@@ -43,12 +46,22 @@ struct BNode {
   double thr, gain;
 };
 
+// the sorted element: (feature value, row) — the reference sorts (feature
+// value, residual) pairs with a comparator on the value only
+struct KP {
+  double key;
+  uint32_t row, pad;
+};
+struct KPLess {
+  __device__ __forceinline__ bool operator()(const KP& a, const KP& b) const { return a.key < b.key; }
+};
+
 struct FitArgs {
   uint32_t n_models, F;
   const uint64_t* off;
   const double* x;      // column-major per model
   const double* y;
-  double* pred;         // per row
+  KP* root;             // per row and feature: the root's sorted (value, row) pairs
   uint8_t* scratch;     // global working memory for models beyond the smem budget
   const uint64_t* scratch_off;  // per model; UINT64_MAX = shared memory
   uint32_t n_trees, max_depth, min_leaf, node_stride;
@@ -58,58 +71,165 @@ struct FitArgs {
   double* base;
   uint8_t* degenerate;
   double* importance;
+  unsigned long long* prof;  // optional per-phase cycle totals (block 0), CS_FIT_PROFILE
 };
 
 __host__ __device__ inline uint64_t align16(uint64_t x) { return (x + 15) & ~uint64_t{15}; }
+__host__ __device__ inline uint64_t work_cap(uint64_t n, uint64_t F) { return F * n / 16 + 64; }
+__host__ __device__ inline uint64_t final_cap(uint64_t n, uint64_t F) { return F * n / 2 + 64; }
 
 // working-memory layout of one model with n rows, F features
 struct Layout {
-  uint64_t r, keys, perm, root, idx_a, idx_b, nodes, total;
+  uint64_t r, pred, kp, g, idx_a, idx_b, nodes, work_a, work_b, fin, total;
   __host__ __device__ Layout(uint64_t n, uint64_t F, uint64_t max_nodes) {
     uint64_t o = 0;
-    r = o;
-    o = align16(o + 8 * n);
-    keys = o;
-    o = align16(o + 8 * F * n);
-    perm = o;
-    o = align16(o + 4 * F * n);
-    root = o;
-    o = align16(o + 4 * F * n);
-    idx_a = o;
-    o = align16(o + 4 * n);
-    idx_b = o;
-    o = align16(o + 4 * n);
-    nodes = o;
-    o = align16(o + sizeof(BNode) * max_nodes);
+    auto take = [&](uint64_t bytes) {
+      const uint64_t at = o;
+      o = align16(o + bytes);
+      return at;
+    };
+    r = take(8 * n);
+    pred = take(8 * n);
+    kp = take(sizeof(KP) * F * n);
+    g = take(8 * F * n);
+    idx_a = take(4 * n);
+    idx_b = take(4 * n);
+    nodes = take(sizeof(BNode) * max_nodes);
+    work_a = take(sizeof(cs_sort::Range) * work_cap(n, F));
+    work_b = take(sizeof(cs_sort::Range) * work_cap(n, F));
+    fin = take(sizeof(cs_sort::Range) * final_cap(n, F));
     total = o;
   }
 };
 
-__global__ void __launch_bounds__(kFitThreads) k_gbdt_fit(FitArgs a) {
+// libstdc++'s __unguarded_partition_pivot (cs_introsort.h) on kp[first, last)
+// by one warp.  The sequential scans swap the i-th left stopper (ascending,
+// key >= pivot) with the i-th right stopper (descending, key <= pivot) while
+// l_i < r_i; for those i every position a scan passes is still unmodified
+// (earlier swaps touched only l_j < l_i and r_j > r_i), so the stoppers are
+// those of the input.  The warp lists both stopper sequences of the input
+// with ballots, finds K = the first i with l_i >= r_i, performs the K swaps
+// in parallel and returns min(l_{K+1}, r_K), where the sequential scan stops.
+// `scratch` holds 2 * (last - first) u32 (the range's slice of the gain array).
+__device__ uint32_t warp_partition(KP* kp, uint32_t first, uint32_t last, uint32_t* scratch, int lane) {
+  const KPLess lt;
+  if (lane == 0) cs_sort::move_median_to_first(kp, first, first + 1, first + (last - first) / 2, last - 1, lt);
+  __syncwarp();
+  const double pv = kp[first].key;
+  const uint32_t m = last - first;
+  uint32_t* Ls = scratch;
+  uint32_t* Rs = scratch + m;
+  const uint32_t below = (1u << lane) - 1u;
+  uint32_t nL = 0, nR = 0;
+  for (uint32_t b = first + 1; b < last; b += 32) {
+    const uint32_t p = b + lane;
+    const bool f = p < last && !(kp[p].key < pv);
+    const uint32_t bal = __ballot_sync(0xffffffffu, f);
+    if (f) Ls[nL + __popc(bal & below)] = p;
+    nL += __popc(bal);
+  }
+  for (uint32_t e = last; e > first + 1; e = e > first + 33 ? e - 32 : first + 1) {
+    const bool valid = e - 1 >= first + 1 + (uint32_t)lane && (uint32_t)lane < e - 1 - first;
+    const uint32_t p = valid ? e - 1 - lane : first;
+    const bool f = valid && !(pv < kp[p].key);
+    const uint32_t bal = __ballot_sync(0xffffffffu, f);
+    if (f) Rs[nR + __popc(bal & below)] = p;
+    nR += __popc(bal);
+  }
+  __syncwarp();
+  const uint32_t np = nL < nR ? nL : nR;
+  uint32_t K = 0;
+  for (uint32_t i0 = 0; i0 < np; i0 += 32) {  // l_i < r_i holds for a prefix of i
+    const uint32_t i = i0 + lane;
+    const uint32_t bal = __ballot_sync(0xffffffffu, i < np && Ls[i] < Rs[i]);
+    K += __popc(bal);
+    if (bal != 0xffffffffu) break;
+  }
+  for (uint32_t i = lane; i < K; i += 32) {
+    const KP t = kp[Ls[i]];
+    kp[Ls[i]] = kp[Rs[i]];
+    kp[Rs[i]] = t;
+  }
+  uint32_t cut = K < nL ? Ls[K] : last;
+  if (K > 0 && Rs[K - 1] < cut) cut = Rs[K - 1];
+  __syncwarp();
+  return cut;
+}
+
+// s = ((s + v[0]) + v[1]) + ... in order; loads are issued 8 ahead
+__device__ __forceinline__ double seq_sum(const double* v, uint32_t len) {
+  double s = 0.0;
+  uint32_t k = 0;
+  for (; k + 8 <= len; k += 8) {
+    double t[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) t[u] = v[k + u];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) s += t[u];
+  }
+  for (; k < len; ++k) s += v[k];
+  return s;
+}
+// v[k] = v[0] + ... + v[k] (sequential left-to-right sums), in place
+__device__ __forceinline__ void seq_prefix(double* v, uint32_t len) {
+  double s = 0.0;
+  uint32_t k = 0;
+  for (; k + 8 <= len; k += 8) {
+    double t[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) t[u] = v[k + u];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      s += t[u];
+      v[k + u] = s;
+    }
+  }
+  for (; k < len; ++k) {
+    s += v[k];
+    v[k] = s;
+  }
+}
+
+__global__ void __launch_bounds__(kFitThreads, 1) k_gbdt_fit(FitArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
+  long long t_mark = clock64();
+  auto mark = [&](int phase) {
+    if (a.prof && blockIdx.x == 0 && threadIdx.x == 0) {
+      const long long now = clock64();
+      a.prof[phase] += (unsigned long long)(now - t_mark);
+      t_mark = now;
+    }
+  };
   __shared__ double s_mean, s_lo, s_hi;
-  __shared__ uint32_t s_nn, s_lvl;
+  __shared__ uint32_t s_nn, s_lvl, s_nwork[2], s_nfin;
   const uint32_t m = blockIdx.x;
   const uint64_t o = a.off[m];
   const uint32_t n = (uint32_t)(a.off[m + 1] - o);
   const uint32_t F = a.F, D = a.max_depth, min_leaf = a.min_leaf;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  // sequential tasks (one per thread) are dealt to lane 0 of every warp
+  // first, then lane 1, ...: tasks on lanes of one warp diverge and run one
+  // after another, tasks on different warps run side by side
+  const uint32_t task = (uint32_t)lane * kFitWarps + (uint32_t)warp;
   const double* xm = a.x + o * F;  // feature f: xm + f * n
   const double* ym = a.y + o;
-  double* pred = a.pred + o;
+  KP* root = a.root + o * F;
   const uint32_t max_nodes = (2u << D) - 1u;
   const Layout L(n, F, max_nodes);
   uint8_t* w = a.scratch_off[m] == ~0ull ? smem : a.scratch + a.scratch_off[m];
   double* r = (double*)(w + L.r);
-  double* keys = (double*)(w + L.keys);
-  uint32_t* perm = (uint32_t*)(w + L.perm);
-  uint32_t* root = (uint32_t*)(w + L.root);
+  double* pred = (double*)(w + L.pred);
+  KP* kp = (KP*)(w + L.kp);
+  double* g = (double*)(w + L.g);
   uint32_t* idx = (uint32_t*)(w + L.idx_a);
   uint32_t* idx_next = (uint32_t*)(w + L.idx_b);
   BNode* nd = (BNode*)(w + L.nodes);
+  cs_sort::Range* work[2] = {(cs_sort::Range*)(w + L.work_a), (cs_sort::Range*)(w + L.work_b)};
+  cs_sort::Range* fin = (cs_sort::Range*)(w + L.fin);
   cs_tree_node* out_nodes = a.nodes + (uint64_t)m * a.n_trees * a.node_stride;
   uint32_t* out_count = a.n_nodes + (uint64_t)m * a.n_trees;
   double* imp = a.importance + (uint64_t)m * F;
+  const KPLess lt;
 
   if (tid == 0) {  // base = mean(y), degenerate when every target is equal (gbdt.cpp:132-143)
     double s = 0.0, lo = n ? ym[0] : 0.0, hi = lo;
@@ -139,10 +259,10 @@ __global__ void __launch_bounds__(kFitThreads) k_gbdt_fit(FitArgs a) {
   }
   const double mean = s_mean;
   for (uint32_t i = tid; i < n; i += kFitThreads) pred[i] = mean;
-  // the root's sort permutation: same input (rows in order) for every tree
-  for (uint32_t q = tid; q < F * n; q += kFitThreads) root[q] = q % n;
+  // the root's sorted pairs: same input (rows in order) for every tree
+  for (uint32_t q = tid; q < F * n; q += kFitThreads) root[q] = KP{xm[q], q % n, 0u};
   __syncthreads();
-  for (uint32_t f = tid; f < F; f += kFitThreads) cs_sort::sort(root + (uint64_t)f * n, n, xm + (uint64_t)f * n);
+  for (uint32_t f = task; f < F; f += kFitThreads) cs_sort::sort_with(root + (uint64_t)f * n, n, lt);
   __syncthreads();
 
   for (uint32_t t = 0; t < a.n_trees; ++t) {
@@ -156,77 +276,189 @@ __global__ void __launch_bounds__(kFitThreads) k_gbdt_fit(FitArgs a) {
       s_lvl = 0;
     }
     __syncthreads();
+    mark(0);
     for (uint32_t d = 0;; ++d) {
       const uint32_t lb = s_lvl, le = s_nn;
       if (lb == le) break;
-      // (A) node totals, row order (gbdt.cpp:51-53)
-      for (uint32_t j = lb + tid; j < le; j += kFitThreads) {
+      auto splittable = [&](uint32_t j) { return d < D && (uint64_t)nd[j].len >= 2ull * min_leaf; };
+      // (A) node totals in row order (gbdt.cpp:51-53): residuals gathered
+      // into row order first, then one sequential sum per node
+      for (uint32_t j = lb; j < le; ++j) {
         const uint32_t s0 = nd[j].start, len = nd[j].len;
-        double s = 0.0;
-        for (uint32_t k = 0; k < len; ++k) s += r[idx[s0 + k]];
-        nd[j].sum = s;
+        for (uint32_t k = tid; k < len; k += kFitThreads) g[s0 + k] = r[idx[s0 + k]];
+      }
+      if (tid == 0) {
+        s_nwork[0] = 0;
+        s_nfin = 0;
+      }
+      __syncthreads();
+      for (uint32_t j = lb + task; j < le; j += kFitThreads) {
+        nd[j].sum = seq_sum(g + nd[j].start, nd[j].len);
         nd[j].feature = -1;
       }
       __syncthreads();
-      auto splittable = [&](uint32_t j) { return d < D && (uint64_t)nd[j].len >= 2ull * min_leaf; };
-      // (B) per feature: keys in row order and the sort permutation
+      mark(1);
+      // (B) per feature: (value, row) pairs in row order, the sort's input;
+      // the root's are sorted once per model
       for (uint32_t j = lb; j < le; ++j) {
         if (!splittable(j)) continue;
         const uint32_t s0 = nd[j].start, len = nd[j].len;
         for (uint32_t q = tid; q < F * len; q += kFitThreads) {
           const uint32_t f = q / len, k = q - f * len;
-          keys[(uint64_t)f * n + s0 + k] = xm[(uint64_t)f * n + idx[s0 + k]];
-          perm[(uint64_t)f * n + s0 + k] = d == 0 ? root[(uint64_t)f * n + k] : k;
+          if (d == 0) {
+            kp[(uint64_t)f * n + k] = root[(uint64_t)f * n + k];
+          } else {
+            const uint32_t row = idx[s0 + k];
+            kp[(uint64_t)f * n + s0 + k] = KP{xm[(uint64_t)f * n + row], row, 0u};
+          }
+        }
+        if (d > 0 && tid < (int)F) {
+          const uint32_t b0 = (uint32_t)tid * n + s0;
+          if (len > (uint32_t)cs_sort::kThreshold) work[0][atomicAdd(&s_nwork[0], 1u)] = cs_sort::start(b0, len);
+          else if (len > 1) fin[atomicAdd(&s_nfin, 1u)] = cs_sort::Range{b0, b0 + len, 0u};
         }
       }
       __syncthreads();
+      mark(2);
       if (d > 0) {
-        for (uint32_t q = tid; q < (le - lb) * F; q += kFitThreads) {
-          const uint32_t j = lb + q / F, f = q % F;
-          if (!splittable(j)) continue;
-          const uint32_t s0 = nd[j].start;
-          cs_sort::sort(perm + (uint64_t)f * n + s0, nd[j].len, keys + (uint64_t)f * n + s0);
+        // (S) std::sort of every (node, feature) segment as independent range
+        // steps (cs_introsort.h): the partition tree level by level, then
+        // every final range's insertion sort
+        int cur = 0;
+        while (true) {
+          const uint32_t nw = s_nwork[cur];
+          if (nw == 0) break;
+          if (tid == 0) s_nwork[cur ^ 1] = 0;
+          __syncthreads();
+          for (uint32_t q = warp; q < nw; q += kFitWarps) {  // a warp per range
+            const cs_sort::Range rg = work[cur][q];
+            if (rg.depth == 0) {  // depth limit: heap sort (sorted, nothing left)
+              if (lane == 0) cs_sort::heap_sort(kp + rg.first, rg.last - rg.first, lt);
+              continue;
+            }
+            const uint32_t cut = warp_partition(kp, rg.first, rg.last, (uint32_t*)(g + rg.first), lane);
+            if (lane == 0) {
+              const cs_sort::Range out[2] = {{rg.first, cut, rg.depth - 1}, {cut, rg.last, rg.depth - 1}};
+              for (int i = 0; i < 2; ++i) {
+                const uint32_t len = out[i].last - out[i].first;
+                if (len > (uint32_t)cs_sort::kThreshold) work[cur ^ 1][atomicAdd(&s_nwork[cur ^ 1], 1u)] = out[i];
+                else if (len > 1) fin[atomicAdd(&s_nfin, 1u)] = out[i];
+              }
+            }
+          }
+          __syncthreads();
+          cur ^= 1;
         }
+        mark(3);
+        const uint32_t nf = s_nfin;
+        for (uint32_t q = task; q < nf; q += kFitThreads)
+          cs_sort::insertion_sort(kp, fin[q].first, fin[q].last, lt);
         __syncthreads();
+        mark(4);
       }
-      // (C) exact greedy split, features in order with the running best (gbdt.cpp:57-90)
-      for (uint32_t j = lb + tid; j < le; j += kFitThreads) {
+      // (C1) left prefix sums in sorted order (gbdt.cpp:65-67): residuals
+      // gathered into sorted order, then one sequential sum per (node, feature)
+      for (uint32_t j = lb; j < le; ++j) {
+        if (!splittable(j)) continue;
+        const uint32_t s0 = nd[j].start, len = nd[j].len;
+        for (uint32_t q = tid; q < F * len; q += kFitThreads) {
+          const uint32_t f = q / len, k = q - f * len;
+          g[(uint64_t)f * n + s0 + k] = r[kp[(uint64_t)f * n + s0 + k].row];
+        }
+      }
+      __syncthreads();
+      for (uint32_t q = task; q < (le - lb) * F; q += kFitThreads) {
+        const uint32_t j = lb + q / F, f = q % F;
+        if (!splittable(j)) continue;
+        seq_prefix(g + (uint64_t)f * n + nd[j].start, nd[j].len - 1);
+      }
+      __syncthreads();
+      mark(5);
+      // (C2) candidate gains, all in parallel (gbdt.cpp:68-80); -1 marks a non-candidate
+      for (uint32_t j = lb; j < le; ++j) {
         if (!splittable(j)) continue;
         const uint32_t s0 = nd[j].start, len = nd[j].len;
         const double sum = nd[j].sum, cnt = (double)len;
-        double best_gain = 0.0, best_thr = 0.0;
-        int best_f = -1;
-        for (uint32_t f = 0; f < F; ++f) {
-          const uint32_t* P = perm + (uint64_t)f * n + s0;
-          const double* K = keys + (uint64_t)f * n + s0;
-          double lsum = 0.0;
-          uint32_t p = P[0];
-          for (uint32_t k = 0; k + 1 < len; ++k) {
-            const uint32_t pn = P[k + 1];
-            lsum += r[idx[s0 + p]];
-            const double kp = K[p], kn = K[pn];
-            p = pn;
-            if (kp == kn) continue;
-            const uint32_t ln = k + 1, rn = len - ln;
-            if (ln < min_leaf || rn < min_leaf) continue;
-            const double rsum = sum - lsum;
-            const double gain = lsum * lsum / (double)ln + rsum * rsum / (double)rn - sum * sum / cnt;
-            if (gain > best_gain + 1e-12) {
-              best_gain = gain;
-              best_f = (int)f;
-              best_thr = 0.5 * (kp + kn);
+        for (uint32_t q = tid; q < F * (len - 1); q += kFitThreads) {
+          const uint32_t f = q / (len - 1), k = q - f * (len - 1);
+          const KP* P = kp + (uint64_t)f * n + s0;
+          double* G = g + (uint64_t)f * n + s0;
+          const uint32_t ln = k + 1, rn = len - ln;
+          double gv = -1.0;
+          if (P[k].key != P[k + 1].key && ln >= min_leaf && rn >= min_leaf) {
+            const double lsum = G[k], rsum = sum - lsum;
+            gv = lsum * lsum / (double)ln + rsum * rsum / (double)rn - sum * sum / cnt;
+          }
+          G[k] = gv;
+        }
+      }
+      __syncthreads();
+      mark(6);
+      // (C3) the reference's running best over features then positions
+      // (gbdt.cpp:83-88): best is replaced when g > best + 1e-12.  Every
+      // earlier candidate c satisfied c <= best + 1e-12 at its turn, so best
+      // >= (max of earlier candidates) - 1e-12 and an accepted candidate is a
+      // strict prefix maximum.  A warp per node scans the candidates with a
+      // running max and replays the chain on the strict prefix maxima only,
+      // in order, which gives the sequential result.
+      for (uint32_t j = lb + warp; j < le; j += kFitWarps) {
+        if (!splittable(j)) continue;
+        const uint32_t s0 = nd[j].start, len = nd[j].len, per = len - 1, total = F * per;
+        double best_gain = 0.0, run_max = -1.0;
+        uint32_t best_q = 0;
+        bool found = false;
+        for (uint32_t q0 = 0; q0 < total; q0 += 32) {
+          const uint32_t q = q0 + lane;
+          double gv = -1.0;
+          if (q < total) {
+            const uint32_t f = q / per, k = q - f * per;
+            gv = g[(uint64_t)f * n + s0 + k];
+          }
+          double incl = gv;  // inclusive max scan over the chunk
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const double y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl = fmax(incl, y);
+          }
+          double excl = __shfl_up_sync(0xffffffffu, incl, 1);
+          if (lane == 0) excl = -1.0;
+          excl = fmax(excl, run_max);
+          uint32_t cand = __ballot_sync(0xffffffffu, q < total && gv > excl);
+          // every strict prefix maximum clears the previous one by more than
+          // the margin: each is accepted, the last one ends the chunk
+          // (best <= max(earlier candidates, 0): the chain starts at 0)
+          const uint32_t wide = __ballot_sync(0xffffffffu, q < total && gv > fmax(excl, 0.0) + 1e-12);
+          if (cand && wide == cand) {
+            const int l = 31 - __clz(cand);
+            best_gain = __shfl_sync(0xffffffffu, gv, l);
+            best_q = q0 + l;
+            found = true;
+            cand = 0;
+          }
+          while (cand) {  // replay the chain on the strict prefix maxima, in order
+            const int l = __ffs(cand) - 1;
+            cand &= cand - 1;
+            const double c = __shfl_sync(0xffffffffu, gv, l);
+            if (c > best_gain + 1e-12) {
+              best_gain = c;
+              best_q = q0 + l;
+              found = true;
             }
           }
+          run_max = fmax(run_max, __shfl_sync(0xffffffffu, incl, 31));
         }
-        if (best_f >= 0 && best_gain > 1e-12) {
-          nd[j].feature = best_f;
-          nd[j].thr = best_thr;
+        if (lane == 0 && found && best_gain > 1e-12) {
+          const uint32_t bf = best_q / per, bk = best_q - bf * per;
+          const KP* P = kp + (uint64_t)bf * n + s0;
+          nd[j].feature = (int32_t)bf;
+          nd[j].thr = 0.5 * (P[bk].key + P[bk + 1].key);
           nd[j].gain = best_gain;
         }
       }
       __syncthreads();
+      mark(7);
       // (D) stable split of each internal node's rows (gbdt.cpp:97-104), warp per node
-      for (uint32_t j = lb + warp; j < le; j += kFitThreads / 32) {
+      for (uint32_t j = lb + warp; j < le; j += kFitWarps) {
         if (nd[j].feature < 0) continue;
         const uint32_t s0 = nd[j].start, len = nd[j].len;
         const double* X = xm + (uint64_t)nd[j].feature * n;
@@ -252,6 +484,7 @@ __global__ void __launch_bounds__(kFitThreads) k_gbdt_fit(FitArgs a) {
         if (lane == 0) nd[j].n_left = nl;
       }
       __syncthreads();
+      mark(8);
       if (tid == 0) {  // children in BFS order
         uint32_t nn = le;
         for (uint32_t j = lb; j < le; ++j) {
@@ -270,6 +503,7 @@ __global__ void __launch_bounds__(kFitThreads) k_gbdt_fit(FitArgs a) {
       idx = idx_next;
       idx_next = tmp;
       __syncthreads();
+      mark(9);
     }
     // pre-order ids and importance (the reference's recursion order)
     if (tid == 0) {
@@ -314,6 +548,7 @@ __global__ void __launch_bounds__(kFitThreads) k_gbdt_fit(FitArgs a) {
       pred[i] = pred[i] + a.lr * (nd[j].sum / (double)nd[j].len);
     }
     __syncthreads();
+    mark(10);
   }
 }
 
@@ -366,11 +601,11 @@ int gbdt_fit_device(int device, GbdtBatch& b, std::string& err) {
     }
   }
   const uint64_t rows = b.off[M];
-  DevMem d_off, d_x, d_y, d_pred, d_scr, d_scr_off, d_nodes, d_cnt, d_base, d_deg, d_imp;
+  DevMem d_off, d_x, d_y, d_root, d_scr, d_scr_off, d_nodes, d_cnt, d_base, d_deg, d_imp;
   auto alloc = [&](DevMem& x, size_t bytes) { return cudaMalloc(&x.p, std::max<size_t>(bytes, 16)) == cudaSuccess; };
   const size_t node_count = static_cast<size_t>(M) * b.params.n_trees * max_nodes;
   if (!alloc(d_off, (M + 1) * 8) || !alloc(d_x, rows * F * 8) || !alloc(d_y, rows * 8) ||
-      !alloc(d_pred, rows * 8) || !alloc(d_scr, scratch_total) || !alloc(d_scr_off, M * 8) ||
+      !alloc(d_root, rows * F * sizeof(KP)) || !alloc(d_scr, scratch_total) || !alloc(d_scr_off, M * 8) ||
       !alloc(d_nodes, node_count * sizeof(cs_tree_node)) ||
       !alloc(d_cnt, static_cast<size_t>(M) * b.params.n_trees * 4) || !alloc(d_base, M * 8) ||
       !alloc(d_deg, M) || !alloc(d_imp, static_cast<size_t>(M) * F * 8)) {
@@ -387,7 +622,7 @@ int gbdt_fit_device(int device, GbdtBatch& b, std::string& err) {
   a.off = static_cast<const uint64_t*>(d_off.p);
   a.x = static_cast<const double*>(d_x.p);
   a.y = static_cast<const double*>(d_y.p);
-  a.pred = static_cast<double*>(d_pred.p);
+  a.root = static_cast<KP*>(d_root.p);
   a.scratch = static_cast<uint8_t*>(d_scr.p);
   a.scratch_off = static_cast<const uint64_t*>(d_scr_off.p);
   a.n_trees = static_cast<uint32_t>(b.params.n_trees);
@@ -400,6 +635,12 @@ int gbdt_fit_device(int device, GbdtBatch& b, std::string& err) {
   a.base = static_cast<double*>(d_base.p);
   a.degenerate = static_cast<uint8_t*>(d_deg.p);
   a.importance = static_cast<double*>(d_imp.p);
+  DevMem d_prof;
+  const bool prof = std::getenv("CS_FIT_PROFILE") != nullptr;
+  if (prof && alloc(d_prof, 16 * 8)) {
+    cudaMemset(d_prof.p, 0, 16 * 8);
+    a.prof = static_cast<unsigned long long*>(d_prof.p);
+  }
   cudaFuncSetAttribute(k_gbdt_fit, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_need));
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
@@ -414,6 +655,13 @@ int gbdt_fit_device(int device, GbdtBatch& b, std::string& err) {
   if (ce != cudaSuccess || cudaGetLastError() != cudaSuccess) {
     err = std::string("k_gbdt_fit: ") + cudaGetErrorString(ce);
     return CS_E_CUDA;
+  }
+  if (a.prof) {
+    unsigned long long h[16];
+    cudaMemcpy(h, a.prof, sizeof h, cudaMemcpyDeviceToHost);
+    static const char* kPhase[] = {"residuals", "sums", "gather", "sort", "insertion", "prefix",
+                                   "gains", "select", "partition", "children", "tree_out+predict"};
+    for (int i = 0; i < 11; ++i) std::fprintf(stderr, "fit phase %-16s %12llu cycles\n", kPhase[i], h[i]);
   }
   b.base.resize(M);
   b.degenerate.resize(M);

@@ -19,6 +19,9 @@
 
 namespace cs_sort {
 
+// Element-generic restatement: E is the moved element, lt(E, E) the
+// comparator.  Index sorts use E = uint32_t with Less (key[a] < key[b]);
+// the device fit sorts (key, row) pairs directly.
 struct Less {
   const double* key;
   CS_HD bool operator()(uint32_t a, uint32_t b) const { return key[a] < key[b]; }
@@ -33,14 +36,16 @@ CS_HD int lg(int64_t n) {  // std::__lg
   return k;
 }
 
-CS_HD void swap(uint32_t* a, int64_t i, int64_t j) {
-  const uint32_t t = a[i];
+template <typename E>
+CS_HD void swap(E* a, int64_t i, int64_t j) {
+  const E t = a[i];
   a[i] = a[j];
   a[j] = t;
 }
 
 // ---- heap (stl_heap.h)
-CS_HD void push_heap(uint32_t* a, int64_t hole, int64_t top, uint32_t value, const Less& lt) {
+template <typename E, typename Lt>
+CS_HD void push_heap(E* a, int64_t hole, int64_t top, E value, const Lt& lt) {
   int64_t parent = (hole - 1) / 2;
   while (hole > top && lt(a[parent], value)) {
     a[hole] = a[parent];
@@ -50,7 +55,8 @@ CS_HD void push_heap(uint32_t* a, int64_t hole, int64_t top, uint32_t value, con
   a[hole] = value;
 }
 
-CS_HD void adjust_heap(uint32_t* a, int64_t hole, int64_t len, uint32_t value, const Less& lt) {
+template <typename E, typename Lt>
+CS_HD void adjust_heap(E* a, int64_t hole, int64_t len, E value, const Lt& lt) {
   const int64_t top = hole;
   int64_t child = hole;
   while (child < (len - 1) / 2) {
@@ -67,7 +73,8 @@ CS_HD void adjust_heap(uint32_t* a, int64_t hole, int64_t len, uint32_t value, c
   push_heap(a, hole, top, value, lt);
 }
 
-CS_HD void make_heap(uint32_t* a, int64_t len, const Less& lt) {
+template <typename E, typename Lt>
+CS_HD void make_heap(E* a, int64_t len, const Lt& lt) {
   if (len < 2) return;
   int64_t parent = (len - 2) / 2;
   while (true) {
@@ -78,19 +85,20 @@ CS_HD void make_heap(uint32_t* a, int64_t len, const Less& lt) {
 }
 
 // __partial_sort(first, last, last): __heap_select (make_heap only) + __sort_heap
-CS_HD void heap_sort(uint32_t* a, int64_t len, const Less& lt) {
+template <typename E, typename Lt>
+CS_HD void heap_sort(E* a, int64_t len, const Lt& lt) {
   make_heap(a, len, lt);
   while (len > 1) {
     --len;
-    const uint32_t value = a[len];
+    const E value = a[len];
     a[len] = a[0];
     adjust_heap(a, 0, len, value, lt);
   }
 }
 
 // ---- partition
-CS_HD void move_median_to_first(uint32_t* a, int64_t result, int64_t x, int64_t y, int64_t z,
-                                const Less& lt) {
+template <typename E, typename Lt>
+CS_HD void move_median_to_first(E* a, int64_t result, int64_t x, int64_t y, int64_t z, const Lt& lt) {
   if (lt(a[x], a[y])) {
     if (lt(a[y], a[z])) swap(a, result, y);
     else if (lt(a[x], a[z])) swap(a, result, z);
@@ -104,26 +112,32 @@ CS_HD void move_median_to_first(uint32_t* a, int64_t result, int64_t x, int64_t 
   }
 }
 
-CS_HD int64_t unguarded_partition(uint32_t* a, int64_t first, int64_t last, int64_t pivot, const Less& lt) {
+// the pivot sits outside [first, last) and is never moved by the scan, so
+// its value is held in a register
+template <typename E, typename Lt>
+CS_HD int64_t unguarded_partition(E* a, int64_t first, int64_t last, int64_t pivot, const Lt& lt) {
+  const E pv = a[pivot];
   while (true) {
-    while (lt(a[first], a[pivot])) ++first;
+    while (lt(a[first], pv)) ++first;
     --last;
-    while (lt(a[pivot], a[last])) --last;
+    while (lt(pv, a[last])) --last;
     if (!(first < last)) return first;
     swap(a, first, last);
     ++first;
   }
 }
 
-CS_HD int64_t partition_pivot(uint32_t* a, int64_t first, int64_t last, const Less& lt) {
+template <typename E, typename Lt>
+CS_HD int64_t partition_pivot(E* a, int64_t first, int64_t last, const Lt& lt) {
   const int64_t mid = first + (last - first) / 2;
   move_median_to_first(a, first, first + 1, mid, last - 1, lt);
   return unguarded_partition(a, first + 1, last, first, lt);
 }
 
 // ---- insertion sorts
-CS_HD void unguarded_linear_insert(uint32_t* a, int64_t last, const Less& lt) {
-  const uint32_t val = a[last];
+template <typename E, typename Lt>
+CS_HD void unguarded_linear_insert(E* a, int64_t last, const Lt& lt) {
+  const E val = a[last];
   int64_t next = last - 1;
   while (lt(val, a[next])) {
     a[last] = a[next];
@@ -133,11 +147,12 @@ CS_HD void unguarded_linear_insert(uint32_t* a, int64_t last, const Less& lt) {
   a[last] = val;
 }
 
-CS_HD void insertion_sort(uint32_t* a, int64_t first, int64_t last, const Less& lt) {
+template <typename E, typename Lt>
+CS_HD void insertion_sort(E* a, int64_t first, int64_t last, const Lt& lt) {
   if (first == last) return;
   for (int64_t i = first + 1; i != last; ++i) {
     if (lt(a[i], a[first])) {
-      const uint32_t val = a[i];
+      const E val = a[i];
       for (int64_t k = i; k > first; --k) a[k] = a[k - 1];
       a[first] = val;
     } else {
@@ -149,8 +164,10 @@ CS_HD void insertion_sort(uint32_t* a, int64_t first, int64_t last, const Less& 
 constexpr int64_t kThreshold = 16;
 
 // __introsort_loop, with the recursion on the right part made explicit (a
-// stack of pending [first, last, depth) ranges processed in the same order)
-CS_HD void introsort_loop(uint32_t* a, int64_t first0, int64_t last0, int depth0, const Less& lt) {
+// stack of pending [first, last, depth) ranges).  The ranges are disjoint,
+// so the order in which they are processed does not change the result.
+template <typename E, typename Lt>
+CS_HD void introsort_loop(E* a, int64_t first0, int64_t last0, int depth0, const Lt& lt) {
   struct Range {
     int64_t first, last;
     int depth;
@@ -160,13 +177,9 @@ CS_HD void introsort_loop(uint32_t* a, int64_t first0, int64_t last0, int depth0
   stack[sp++] = {first0, last0, depth0};
   while (sp) {
     Range r = stack[--sp];
-    // a call: loop on [first, last); each cut's right part is a nested call
-    // that completes before this call continues with the left part, so the
-    // left part is pushed first and the right part on top of it
     while (r.last - r.first > kThreshold) {
       if (r.depth == 0) {
         heap_sort(a + r.first, r.last - r.first, lt);
-        r.last = r.first;  // this call returns
         break;
       }
       --r.depth;
@@ -177,11 +190,11 @@ CS_HD void introsort_loop(uint32_t* a, int64_t first0, int64_t last0, int depth0
   }
 }
 
-// std::sort(a, a + n, key-less-than)
-CS_HD void sort(uint32_t* a, int64_t n, const double* key) {
-  const Less lt{key};
-  if (n <= 1) return;
-  introsort_loop(a, 0, n, 2 * lg(n), lt);
+// __final_insertion_sort.  After the partitions no element is smaller than
+// anything in an earlier partition range (left part <= pivot <= right part),
+// so this is also an independent insertion sort of each final range.
+template <typename E, typename Lt>
+CS_HD void final_insertion_sort(E* a, int64_t n, const Lt& lt) {
   if (n > kThreshold) {
     insertion_sort(a, 0, kThreshold, lt);
     for (int64_t i = kThreshold; i < n; ++i) unguarded_linear_insert(a, i, lt);
@@ -189,5 +202,43 @@ CS_HD void sort(uint32_t* a, int64_t n, const double* key) {
     insertion_sort(a, 0, n, lt);
   }
 }
+
+// ---- the same sort as independent range steps (the device fit runs the
+// partition tree level by level, then the final ranges in parallel):
+// start(n) -> one work range or one final range; step(range) -> heap sort
+// (depth exhausted: sorted, nothing left to do) or a partition into two
+// children, each a work range (> kThreshold) or a final range; finally
+// insertion_sort(a, first, last) of every final range.
+struct Range {
+  uint32_t first, last, depth;
+};
+// returns the number of children written to out[0..1]; *final_mask bit i
+// set when out[i] is a final range
+template <typename E, typename Lt>
+CS_HD int step(E* a, const Range& r, const Lt& lt, Range out[2], unsigned* final_mask) {
+  *final_mask = 0;
+  if (r.depth == 0) {
+    heap_sort(a + r.first, r.last - r.first, lt);
+    return 0;
+  }
+  const uint32_t cut = (uint32_t)partition_pivot(a, r.first, r.last, lt);
+  out[0] = Range{r.first, cut, r.depth - 1};
+  out[1] = Range{cut, r.last, r.depth - 1};
+  if (cut - r.first <= (uint32_t)kThreshold) *final_mask |= 1u;
+  if (r.last - cut <= (uint32_t)kThreshold) *final_mask |= 2u;
+  return 2;
+}
+CS_HD Range start(uint32_t first, uint32_t n) { return Range{first, first + n, (uint32_t)(2 * lg(n))}; }
+
+// std::sort(a, a + n, lt)
+template <typename E, typename Lt>
+CS_HD void sort_with(E* a, int64_t n, const Lt& lt) {
+  if (n <= 1) return;
+  introsort_loop(a, 0, n, 2 * lg(n), lt);
+  final_insertion_sort(a, n, lt);
+}
+
+// std::sort of positions by key[position]
+CS_HD void sort(uint32_t* a, int64_t n, const double* key) { sort_with(a, n, Less{key}); }
 
 }  // namespace cs_sort
