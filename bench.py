@@ -9,8 +9,9 @@ instance, ~100 M events (3.70 M cycles x 27 events), mixed prefill/decode,
 NvlinkSaturation x18 straggler on rank 3 — synthetic, produced by the simkit
 restatement (cs_synth.cpp, byte-identical to the reference generator per
 chunk; 64 chunks with substream seeds, generated on all host cores).  The
-latency model is fit once in setup (host C++, bit-identical to the
-reference's fit) on the first 2400 cycles.
+latency model is fit once in setup (one device batch over every instance,
+cs_fit_latency_models, byte-identical to the reference's fit) on the first
+2400 cycles.
 
 A step = one cs_run over the whole instance: anchor discovery, segmentation,
 stage classification, beta stage attribution, records, GBDT predict + ppe,
@@ -237,15 +238,21 @@ def run_ours(args, rank, world, local_rank):
     an.upload(pin_ev, offs, pin_wl)
     # setup: fit the model on the first 2400 cycles of each instance (A17, host)
     an.run(abi.RUN_SEGMENT)
-    fit_s = 0.0
+    # one device batch for every instance's model (cs_fit_latency_models,
+    # byte-identical to the reference's per-instance fit)
+    xs, ys = [], []
     for i in range(n_inst):
         recs = an.records(i)
         tr = recs[recs["cycle_index"] < 2400]
-        x = np.stack([tr["batch"].astype(float),
-                      (tr["batch"] * (tr["input_len"] + tr["output_len"])).astype(float)], 1)
-        t0 = time.time()
-        model = rt.fit_latency_model(x, tr["latency_s"])
-        fit_s += time.time() - t0
+        xs.append(np.stack([tr["batch"].astype(float),
+                            (tr["batch"] * (tr["input_len"] + tr["output_len"])).astype(float)], 1))
+        ys.append(tr["latency_s"])
+    t0 = time.time()
+    models, _ = rt.fit_latency_models(xs, ys, device=dev, n_threads=threads)
+    fit_s = time.time() - t0
+    for i, model in enumerate(models):
+        if isinstance(model, Exception):
+            raise model
         an.load_model(model, inst=i)
     setup_s = time.time() - t_setup
 

@@ -50,7 +50,8 @@ enum cs_status {
   CS_E_MODEL_FORMAT = 11,      /* "model_format_error"     errors.hpp:80-82  */
   CS_E_UNSUPPORTED = 12,       /* "unsupported": outside the device limits   */
   CS_E_CONFIG = 13,            /* "config_error"           errors.hpp:77-79  */
-  CS_E_INTERNAL = 14           /* "internal"                                 */
+  CS_E_INTERNAL = 14,          /* "internal"                                 */
+  CS_E_INSUFFICIENT_CYCLES = 15 /* "insufficient_cycles"   errors.hpp:68-70  */
 };
 
 /* ------------------------------------------------------- event record (A1)
@@ -440,6 +441,58 @@ int cs_get_collective_beta(cs_ctx* ctx, uint32_t inst, double* beta,
 int cs_get_mu(cs_ctx* ctx, uint32_t inst, double* mu, uint8_t* has, size_t cap, size_t* n);
 int cs_get_records(cs_ctx* ctx, uint32_t inst, cs_record* buf, size_t cap, size_t* n);
 int cs_get_alerts(cs_ctx* ctx, uint32_t inst, cs_alert* buf, size_t cap, size_t* n);
+
+/* ------------------------------------------- post-alert root cause (§8f #4)
+ * suspicion_rank + attribute_straggler (rca.cpp:220-353) over a normal and an
+ * abnormal window of cycles, from the stage attribution of the last cs_run
+ * (CS_RUN_BETA; CS_RUN_MU for the mu terms).  One entry per event class (beta
+ * slot) present in either window, sorted by score (descending), ties by class
+ * name; welch_p is the two-sided Welch test on beta.  Collective classes get
+ * the rank whose mean per-rank beta shifted most between the windows, within
+ * communicator groups with >= 2 ranks in the abnormal window.
+ * CS_E_INSUFFICIENT_CYCLES below 10 normal / 3 abnormal cycles. */
+typedef struct cs_suspect {
+  int32_t beta_slot;           /* event class (its name = the slot's name)      */
+  int32_t metric;              /* 1 + name id of the counter behind mu, 0 none  */
+  double beta_norm, beta_abn, delta_beta, z_beta, z_log_mu, score;
+  double mu_norm, mu_abn, delta_mu, welch_p;
+  int32_t straggler_slot;      /* comm slot (class, commHash, rank), -1 none    */
+  int32_t straggler_location;  /* comm_location[straggler_slot], -1 unmapped    */
+  double rank_beta_shift;
+} cs_suspect;
+/* Host form, on window rows (row c = one cycle of the window, in window order):
+ * totals / beta / mu / mu_has: n_cycles x n_slots; coll / coll_present:
+ * n_cycles x n_comm. */
+typedef struct cs_rca_window {
+  uint64_t n_cycles;
+  const int64_t* totals;
+  const double* beta;
+  const double* mu;            /* NULL: no mu terms */
+  const uint8_t* mu_has;
+  const double* coll;
+  const uint8_t* coll_present;
+} cs_rca_window;
+typedef struct cs_rca_layout {
+  uint32_t n_slots;
+  uint32_t n_comm;
+  const int32_t* slot_metric;    /* per beta slot: 1 + metric name id, 0 none  */
+  const int32_t* comm_class;     /* per comm slot: beta slot of its name       */
+  const int32_t* comm_group;     /* per comm slot: equal for equal (name, hash) */
+  const int32_t* comm_rank;      /* per comm slot: rank                        */
+  const int32_t* comm_location;  /* per comm slot: caller's (node, device) id, -1 unmapped; may be NULL */
+} cs_rca_layout;
+int cs_rank_suspects(const cs_rca_window* normal, const cs_rca_window* abnormal,
+                     const cs_rca_layout* layout, cs_suspect* out, size_t cap, size_t* n_out);
+/* Device form: the windows are cycle indices of instance `inst`; the rows are
+ * gathered from the device.  comm_group / comm_rank / comm_location describe
+ * the comm slots (comm_class comes from the name table). */
+int cs_suspicion_rank(cs_ctx* ctx, uint32_t inst, const uint64_t* normal_cycles, size_t n_normal,
+                      const uint64_t* abnormal_cycles, size_t n_abnormal, const int32_t* comm_name,
+                      const int32_t* comm_group, const int32_t* comm_rank,
+                      const int32_t* comm_location, cs_suspect* out, size_t cap, size_t* n_out);
+/* welch_p_value (rca.cpp:206-218). */
+double cs_welch_p_value(double mean_a, double var_a, uint64_t n_a, double mean_b, double var_b,
+                        uint64_t n_b);
 
 /* Re-run only the control chart over the residuals of the last cs_run with a
  * different ControlConfig (strategy / window / warmup / thresholds); the

@@ -80,6 +80,8 @@ struct Results {
 struct Handle {
   LabeledDataset ds;
   std::vector<ValidationIssue> parse_issues;  // from parse_trace_json
+  std::vector<Cycle> cycles;                  // of the last ref_run
+  MetricMap metric_map;
   Exported ex;
   bool exported = false;
   Results res;
@@ -239,6 +241,8 @@ void run_reference(Handle& h, const RunConfig& config, const char* model_json,
     set_error(R, e);
     return;
   }
+  h.cycles = cycles;
+  h.metric_map = config.metric_map;
   for (const auto& c : cycles) {
     cs_cycle o{};
     o.index = c.index;
@@ -462,6 +466,67 @@ void* ref_from_json(const char* text, size_t len, uint64_t* n_issues) {
   h->ds.trace = std::move(parsed.trace);
   h->parse_issues = std::move(parsed.issues);
   return h.release();
+}
+
+// The reference's post-alert ranking (cmd_diagnose, main.cpp:285-303):
+// cycle_stats of the windows' cycles (by cycle index, from the last ref_run),
+// suspicion_rank, attribute_straggler with resolve_topology; the JSON report
+// (render_json_report) in buf.  Returns 2 with the error type in err on an
+// EngineError.
+int ref_rca(void* hv, const uint64_t* normal, size_t n_normal, const uint64_t* abnormal,
+            size_t n_abnormal, int with_mu, char* buf, size_t cap, size_t* n, char* err,
+            size_t err_cap) {
+  auto* h = static_cast<Handle*>(hv);
+  const Trace& trace = h->ds.trace;
+  try {
+    const CounterTable counters = with_mu ? CounterTable::from_trace(trace) : CounterTable{};
+    const MetricMap metrics = with_mu ? h->metric_map : MetricMap{};
+    std::map<std::size_t, const Cycle*> by_index;
+    for (const auto& c : h->cycles) by_index[c.index] = &c;
+    auto stats_for = [&](const uint64_t* idx, size_t k) {
+      std::vector<CycleClassStats> st;
+      for (size_t i = 0; i < k; ++i)
+        if (auto it = by_index.find(idx[i]); it != by_index.end())
+          st.push_back(cycle_stats(*it->second, trace, counters, metrics));
+      return st;
+    };
+    const auto ns = stats_for(normal, n_normal), as = stats_for(abnormal, n_abnormal);
+    auto entries = suspicion_rank(ns, as);
+    attribute_straggler(entries, resolve_topology(trace), ns, as);
+    const std::string j = render_json_report(entries).dump();
+    if (n) *n = j.size();
+    if (buf) {
+      if (cap < j.size()) return 1;
+      std::memcpy(buf, j.data(), j.size());
+    }
+    return 0;
+  } catch (const EngineError& e) {
+    if (err && err_cap) {
+      std::strncpy(err, e.type().c_str(), err_cap - 1);
+      err[err_cap - 1] = 0;
+    }
+    return 2;
+  }
+}
+
+// resolve_topology (align.cpp:178-191) per exported comm slot: a JSON array
+// of [node, device] or null (unmapped)
+int ref_topology(void* hv, char* buf, size_t cap, size_t* n) {
+  auto* h = static_cast<Handle*>(hv);
+  const TopologyMap topo = resolve_topology(h->ds.trace);
+  json arr = json::array();
+  for (const auto& [name, hash, rank] : h->ex.comm) {
+    (void)name;
+    if (const auto* loc = topo.find(hash, rank)) arr.push_back(json::array({loc->node, loc->device}));
+    else arr.push_back(nullptr);
+  }
+  const std::string j = arr.dump();
+  if (n) *n = j.size();
+  if (buf) {
+    if (cap < j.size()) return 1;
+    std::memcpy(buf, j.data(), j.size());
+  }
+  return 0;
 }
 
 // validate_trace(trace, parse issues) (trace.cpp:243-276): the report as

@@ -38,6 +38,8 @@ def lib():
         L.ref_to_json.argtypes = [vp, C.c_char_p, sz, C.POINTER(sz)]
         L.ref_from_json.restype = vp
         L.ref_from_json.argtypes = [C.c_char_p, sz, C.POINTER(C.c_uint64)]
+        L.ref_rca.argtypes = [vp, vp, sz, vp, sz, C.c_int, C.c_char_p, sz, C.POINTER(sz), C.c_char_p, sz]
+        L.ref_topology.argtypes = [vp, C.c_char_p, sz, C.POINTER(sz)]
         L.ref_validate.argtypes = [vp, vp, sz, C.POINTER(sz), vp, C.POINTER(C.c_uint64)]
         L.ref_build.restype = vp
         L.ref_build.argtypes = [C.c_uint64, vp, vp, C.c_uint32, C.c_char_p, vp, C.c_uint32,
@@ -166,6 +168,32 @@ class RefTrace:
         buf = C.create_string_buffer(n.value)
         L.ref_to_json(self.h, buf, n.value, C.byref(n))
         return buf.raw[:n.value]
+
+    def rca(self, normal, abnormal, mu=False):
+        """suspicion_rank + attribute_straggler over cycle-index windows of the
+        last run(): the parsed render_json_report, or ("error", type)."""
+        L = lib()
+        nrm = np.ascontiguousarray(np.asarray(normal, dtype=np.uint64))
+        abn = np.ascontiguousarray(np.asarray(abnormal, dtype=np.uint64))
+        n = C.c_size_t(0)
+        err = C.create_string_buffer(256)
+        rc = L.ref_rca(self.h, nrm.ctypes.data, len(nrm), abn.ctypes.data, len(abn), int(mu), None, 0,
+                       C.byref(n), err, 256)
+        if rc == 2:
+            return ("error", err.value.decode())
+        buf = C.create_string_buffer(n.value + 1)
+        assert L.ref_rca(self.h, nrm.ctypes.data, len(nrm), abn.ctypes.data, len(abn), int(mu), buf,
+                         n.value, C.byref(n), err, 256) == 0
+        return json.loads(buf.raw[:n.value])
+
+    def topology(self):
+        """resolve_topology per exported comm slot: [node, device] or None."""
+        L = lib()
+        n = C.c_size_t(0)
+        L.ref_topology(self.h, None, 0, C.byref(n))
+        buf = C.create_string_buffer(n.value + 1)
+        L.ref_topology(self.h, buf, n.value, C.byref(n))
+        return json.loads(buf.raw[:n.value])
 
     def validate(self):
         """validate_trace with the parse issues: (ISSUE_DTYPE records, category counts, n_errors)."""

@@ -75,7 +75,7 @@ STATUS_TYPES = {
     4: "no_anchor_found", 5: "missing_workload_args", 6: "feature_mismatch",
     7: "non_positive_latency", 8: "insufficient_data", 9: "insufficient_calibration",
     10: "no_labels", 11: "model_format_error", 12: "unsupported", 13: "config_error",
-    14: "internal",
+    14: "internal", 15: "insufficient_cycles",
 }
 U64_MAX = (1 << 64) - 1
 U32_MAX = (1 << 32) - 1
@@ -149,6 +149,35 @@ class WireBatch(C.Structure):  # cs_wire_batch
                 ("payloads", C.c_void_p), ("n_payloads", C.c_uint64),
                 ("values", C.c_void_p), ("n_values", C.c_uint64),
                 ("escapes", C.c_void_p), ("n_escapes", C.c_uint64)]
+
+
+SUSPECT_DTYPE = np.dtype([("beta_slot", "<i4"), ("metric", "<i4"), ("beta_norm", "<f8"),
+                          ("beta_abn", "<f8"), ("delta_beta", "<f8"), ("z_beta", "<f8"),
+                          ("z_log_mu", "<f8"), ("score", "<f8"), ("mu_norm", "<f8"), ("mu_abn", "<f8"),
+                          ("delta_mu", "<f8"), ("welch_p", "<f8"), ("straggler_slot", "<i4"),
+                          ("straggler_location", "<i4"), ("rank_beta_shift", "<f8")])
+assert SUSPECT_DTYPE.itemsize == 104
+
+
+class Suspect(C.Structure):  # cs_suspect
+    _fields_ = [("beta_slot", C.c_int32), ("metric", C.c_int32), ("beta_norm", C.c_double),
+                ("beta_abn", C.c_double), ("delta_beta", C.c_double), ("z_beta", C.c_double),
+                ("z_log_mu", C.c_double), ("score", C.c_double), ("mu_norm", C.c_double),
+                ("mu_abn", C.c_double), ("delta_mu", C.c_double), ("welch_p", C.c_double),
+                ("straggler_slot", C.c_int32), ("straggler_location", C.c_int32),
+                ("rank_beta_shift", C.c_double)]
+
+
+class RcaWindow(C.Structure):  # cs_rca_window
+    _fields_ = [("n_cycles", C.c_uint64), ("totals", C.c_void_p), ("beta", C.c_void_p),
+                ("mu", C.c_void_p), ("mu_has", C.c_void_p), ("coll", C.c_void_p),
+                ("coll_present", C.c_void_p)]
+
+
+class RcaLayout(C.Structure):  # cs_rca_layout
+    _fields_ = [("n_slots", C.c_uint32), ("n_comm", C.c_uint32), ("slot_metric", C.c_void_p),
+                ("comm_class", C.c_void_p), ("comm_group", C.c_void_p), ("comm_rank", C.c_void_p),
+                ("comm_location", C.c_void_p)]
 
 
 class StrategyMetrics(C.Structure):

@@ -297,6 +297,7 @@ const char* cs_status_type(int status) {
     case CS_E_MODEL_FORMAT: return "model_format_error";
     case CS_E_UNSUPPORTED: return "unsupported";
     case CS_E_CONFIG: return "config_error";
+    case CS_E_INSUFFICIENT_CYCLES: return "insufficient_cycles";
     default: return "internal";
   }
 }
@@ -1461,6 +1462,97 @@ int cs_get_collective_beta(cs_ctx* ctx, uint32_t inst, double* beta, uint8_t* pr
     for (uint64_t k = 0; k < nc * R; ++k) present[k] = present[k] ? 1 : 0;
   }
   return CS_OK;
+}
+
+int cs_suspicion_rank(cs_ctx* ctx, uint32_t inst, const uint64_t* normal_cycles, size_t n_normal,
+                      const uint64_t* abnormal_cycles, size_t n_abnormal, const int32_t* comm_name,
+                      const int32_t* comm_group, const int32_t* comm_rank,
+                      const int32_t* comm_location, cs_suspect* out, size_t cap, size_t* n_out) {
+  if (!ctx || !ctx->ran || inst >= ctx->n_inst || !n_out) return CS_E_INVALID_ARGUMENT;
+  if (!(ctx->last_mask & CS_RUN_BETA)) return fail(ctx, CS_E_INVALID_ARGUMENT, "beta not computed");
+  if ((n_normal && !normal_cycles) || (n_abnormal && !abnormal_cycles)) return CS_E_INVALID_ARGUMENT;
+  cudaSetDevice(ctx->device);
+  const uint32_t S = static_cast<uint32_t>(ctx->cyc.n_beta_slots), R = static_cast<uint32_t>(ctx->cyc.n_comm_slots);
+  if (R && (!comm_name || !comm_group || !comm_rank)) return CS_E_INVALID_ARGUMENT;
+  const uint64_t c0 = ctx->cyc_off[inst], nc = ctx->n_cyc[inst];
+  const bool with_mu = (ctx->last_mask & CS_RUN_MU) != 0;
+  // window rows, gathered cycle by cycle (windows are a few hundred cycles)
+  struct Rows {
+    std::vector<int64_t> totals;
+    std::vector<double> beta, mu, coll;
+    std::vector<uint8_t> mu_has, coll_n;
+  };
+  auto gather = [&](const uint64_t* idx, size_t n, Rows& w) -> int {
+    w.totals.resize(n * S);
+    w.beta.resize(n * S);
+    w.coll.resize(n * R);
+    w.coll_n.resize(n * R);
+    if (with_mu) {
+      w.mu.resize(n * S);
+      w.mu_has.resize(n * S);
+    }
+    for (size_t k = 0; k < n; ++k) {
+      if (idx[k] >= nc) return CS_E_INVALID_ARGUMENT;
+      const uint64_t c = c0 + idx[k];
+      if (S) {
+        CS_CUDA(cudaMemcpy(&w.totals[k * S], static_cast<int64_t*>(ctx->c_beta_tot.p) + c * S, S * 8,
+                           cudaMemcpyDeviceToHost));
+        CS_CUDA(cudaMemcpy(&w.beta[k * S], static_cast<double*>(ctx->c_beta.p) + c * S, S * 8,
+                           cudaMemcpyDeviceToHost));
+        if (with_mu) {
+          CS_CUDA(cudaMemcpy(&w.mu[k * S], static_cast<double*>(ctx->d_mu.p) + c * S, S * 8,
+                             cudaMemcpyDeviceToHost));
+          CS_CUDA(cudaMemcpy(&w.mu_has[k * S], static_cast<uint8_t*>(ctx->d_mu_has.p) + c * S, S,
+                             cudaMemcpyDeviceToHost));
+        }
+      }
+      if (R) {
+        CS_CUDA(cudaMemcpy(&w.coll[k * R], static_cast<double*>(ctx->c_coll.p) + c * R, R * 8,
+                           cudaMemcpyDeviceToHost));
+        CS_CUDA(cudaMemcpy(&w.coll_n[k * R], static_cast<uint8_t*>(ctx->c_coll_n.p) + c * R, R,
+                           cudaMemcpyDeviceToHost));
+      }
+    }
+    for (auto& x : w.coll_n) x = x ? 1 : 0;
+    return CS_OK;
+  };
+  Rows rn, ra;
+  int rc = gather(normal_cycles, n_normal, rn);
+  if (rc == CS_OK) rc = gather(abnormal_cycles, n_abnormal, ra);
+  if (rc != CS_OK) return fail(ctx, rc, "cycle index out of range");
+  auto window = [&](Rows& w, size_t n) {
+    cs_rca_window v{};
+    v.n_cycles = n;
+    v.totals = w.totals.data();
+    v.beta = w.beta.data();
+    v.mu = with_mu ? w.mu.data() : nullptr;
+    v.mu_has = with_mu ? w.mu_has.data() : nullptr;
+    v.coll = w.coll.data();
+    v.coll_present = w.coll_n.data();
+    return v;
+  };
+  const cs_rca_window wn = window(rn, n_normal), wa = window(ra, n_abnormal);
+  // per beta slot: its name's metric; per comm slot: its name's beta slot
+  std::vector<int32_t> slot_metric(std::max<uint32_t>(S, 1), 0), comm_class(std::max<uint32_t>(R, 1), -1);
+  for (const auto& ni : ctx->names)
+    if (ni.beta_slot >= 0 && static_cast<uint32_t>(ni.beta_slot) < S) slot_metric[ni.beta_slot] = static_cast<int32_t>(ni.metric);
+  for (uint32_t k = 0; k < R; ++k) {
+    if (comm_name[k] < 0 || static_cast<size_t>(comm_name[k]) >= ctx->names.size()) return CS_E_INVALID_ARGUMENT;
+    comm_class[k] = ctx->names[comm_name[k]].beta_slot;
+  }
+  cs_rca_layout lay{};
+  lay.n_slots = S;
+  lay.n_comm = R;
+  lay.slot_metric = slot_metric.data();
+  lay.comm_class = comm_class.data();
+  lay.comm_group = comm_group;
+  lay.comm_rank = comm_rank;
+  lay.comm_location = comm_location;
+  rc = cs_rank_suspects(&wn, &wa, &lay, out, cap, n_out);
+  if (rc == CS_E_INSUFFICIENT_CYCLES)
+    return fail(ctx, rc, "need >= 10 normal and >= 3 abnormal cycles, got " + std::to_string(n_normal) + "/" +
+                             std::to_string(n_abnormal));
+  return rc;
 }
 
 int cs_get_mu(cs_ctx* ctx, uint32_t inst, double* mu, uint8_t* has, size_t cap, size_t* n) {

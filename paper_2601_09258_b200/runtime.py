@@ -65,6 +65,12 @@ def lib():
                                  C.POINTER(vp), C.POINTER(vp), C.POINTER(vp), psz, C.POINTER(u32),
                                  C.POINTER(u64)]
     L.cs_ingest_free.argtypes = [vp]
+    L.cs_rank_suspects.argtypes = [C.POINTER(abi.RcaWindow), C.POINTER(abi.RcaWindow),
+                                   C.POINTER(abi.RcaLayout), vp, C.c_size_t, C.POINTER(C.c_size_t)]
+    L.cs_suspicion_rank.argtypes = [vp, u32, vp, C.c_size_t, vp, C.c_size_t, vp, vp, vp, vp, vp,
+                                    C.c_size_t, C.POINTER(C.c_size_t)]
+    L.cs_welch_p_value.restype = C.c_double
+    L.cs_welch_p_value.argtypes = [C.c_double, C.c_double, u64, C.c_double, C.c_double, u64]
     L.cs_ingest_report.argtypes = [vp, C.POINTER(vp), C.POINTER(u64), C.POINTER(u64), vp, C.POINTER(u64)]
     L.cs_load_model.argtypes = [vp, u32, C.POINTER(abi.Model)]
     L.cs_run.argtypes = [vp, u32]
@@ -116,7 +122,8 @@ def lib():
 EXPORTED_SYMBOLS = [
     "cs_abi_version", "cs_status_type", "cs_ctx_create", "cs_ctx_destroy", "cs_last_error",
     "cs_set_config", "cs_set_name_table", "cs_upload", "cs_upload_wire", "cs_wire_pack",
-    "cs_wire_view", "cs_wire_free", "cs_ingest_chrome_json", "cs_ingest_view", "cs_ingest_free", "cs_ingest_report", "cs_load_model", "cs_run", "cs_sync",
+    "cs_wire_view", "cs_wire_free", "cs_ingest_chrome_json", "cs_ingest_view", "cs_ingest_free", "cs_ingest_report", "cs_rank_suspects",
+    "cs_suspicion_rank", "cs_welch_p_value", "cs_load_model", "cs_run", "cs_sync",
     "cs_get_summary", "cs_get_candidates", "cs_get_cycles", "cs_get_components", "cs_get_beta",
     "cs_get_collective_beta", "cs_get_mu", "cs_get_records", "cs_get_alerts", "cs_host_alloc",
     "cs_host_free", "cs_get_timings", "cs_get_launch_count", "cs_fit_latency_model", "cs_fit_latency_models",
@@ -229,6 +236,95 @@ def fit_latency_models(xs, ys, feature_names=("batch", "w_kv"),
     models = [LatencyModel(C.c_void_p(out[m])) if status[m] == 0 else EngineError(int(status[m]), "fit failed")
               for m in range(M)]
     return models, ms.value
+
+
+def _i32(a, n):
+    return np.ascontiguousarray(np.asarray(a if a is not None else np.full(n, -1), dtype=np.int32))
+
+
+def comm_groups(comm_name, comm_hash) -> np.ndarray:
+    """Group id per comm slot: equal for equal (name, commHash) (cs_rca_layout)."""
+    out, last, g = np.zeros(len(comm_name), np.int32), None, -1
+    for k, key in enumerate(zip(comm_name, comm_hash)):
+        if key != last:
+            g, last = g + 1, key
+        out[k] = g
+    return out
+
+
+def rank_suspects(normal: dict, abnormal: dict, n_slots: int, n_comm: int, slot_metric=None,
+                  comm_class=None, comm_group=None, comm_rank=None, comm_location=None) -> np.ndarray:
+    """cs_rank_suspects on window rows: dicts with totals, beta, [mu, mu_has],
+    coll, coll_present (rows = cycles of the window, in window order)."""
+    keep = []
+
+    def win(d):
+        arrs = {k: np.ascontiguousarray(d[k]) for k in d if d[k] is not None}
+        keep.append(arrs)
+        n = len(arrs["totals"]) // max(n_slots, 1) if n_slots else len(arrs.get("coll", [])) // max(n_comm, 1)
+        return abi.RcaWindow(n, _ptr(arrs["totals"]), _ptr(arrs["beta"]), _ptr(arrs.get("mu")),
+                             _ptr(arrs.get("mu_has")), _ptr(arrs.get("coll")), _ptr(arrs.get("coll_present")))
+
+    wn, wa = win(normal), win(abnormal)
+    lay_arrs = [_i32(slot_metric, n_slots) if slot_metric is not None else None, _i32(comm_class, n_comm),
+                _i32(comm_group, n_comm), _i32(comm_rank, n_comm),
+                _i32(comm_location, n_comm) if comm_location is not None else None]
+    lay = abi.RcaLayout(n_slots, n_comm, *[_ptr(a) if a is not None else None for a in lay_arrs])
+    n = C.c_size_t(0)
+    _check(lib().cs_rank_suspects(C.byref(wn), C.byref(wa), C.byref(lay), None, 0, C.byref(n)))
+    out = np.zeros(n.value, abi.SUSPECT_DTYPE)
+    _check(lib().cs_rank_suspects(C.byref(wn), C.byref(wa), C.byref(lay), _ptr(out), n.value, C.byref(n)))
+    return out
+
+
+def suspects_report(entries: np.ndarray, slot_names, names, comm_hash=(), comm_rank=(), locations=()):
+    """render_json_report's "suspects" list (rca.cpp:355-385) from cs_suspect records."""
+    out = []
+    for e in entries:
+        d = {"class": slot_names[e["beta_slot"]], "beta_norm": float(e["beta_norm"]),
+             "beta_abn": float(e["beta_abn"]), "delta_beta": float(e["delta_beta"]),
+             "delta_beta_pct": 100.0 * float(e["delta_beta"]), "z_beta": float(e["z_beta"]),
+             "z_log_mu": float(e["z_log_mu"]), "score": float(e["score"]),
+             "metric": names[e["metric"] - 1] if e["metric"] > 0 else "",
+             "mu_norm": float(e["mu_norm"]), "mu_abn": float(e["mu_abn"]), "delta_mu": float(e["delta_mu"]),
+             "p_value": float(e["welch_p"])}
+        k = int(e["straggler_slot"])
+        if k >= 0:
+            st = {"comm": comm_hash[k], "rank": int(comm_rank[k]), "beta_shift": float(e["rank_beta_shift"])}
+            loc = locations[e["straggler_location"]] if e["straggler_location"] >= 0 else None
+            if loc is None:
+                st["node"] = "unmapped"
+            else:
+                st["node"], st["device"] = loc
+            d["straggler"] = st
+        out.append(d)
+    return out
+
+
+def diagnose_windows(records: np.ndarray, episode: int = 0, max_normal: int = 300):
+    """cmd_diagnose's windows (main.cpp:262-298) from detector records in
+    order: flagged runs are episodes, armed unflagged cycles are normal (the
+    last max_normal kept).  Returns (normal, abnormal) cycle indices."""
+    episodes, normal, open_ = [], [], False
+    for r in records:
+        if r["flagged"]:
+            if not open_:
+                episodes.append([])
+            open_ = True
+            episodes[-1].append(int(r["cycle_index"]))
+        else:
+            open_ = False
+            if r["armed"]:
+                normal.append(int(r["cycle_index"]))
+    if not episodes:
+        raise EngineError(15, "no alert episodes found in this trace")
+    if episode >= len(episodes):
+        raise EngineError(13, f"episode {episode} out of range, {len(episodes)} episode(s) found")
+    return normal[-max_normal:], episodes[episode]
+
+
+def welch_p_value(mean_a, var_a, n_a, mean_b, var_b, n_b) -> float:
+    return lib().cs_welch_p_value(mean_a, var_a, n_a, mean_b, var_b, n_b)
 
 
 def ucl_from_stats(mu: float, sigma: float, control: abi.ControlConfig) -> float:
@@ -571,6 +667,21 @@ class Analyzer:
 
     def records(self, inst=0):
         return self._get(self.L.cs_get_records, inst, abi.RECORD_DTYPE)
+
+    def suspicion_rank(self, normal_cycles, abnormal_cycles, comm_name=(), comm_group=(),
+                       comm_rank=(), comm_location=None, inst=0) -> np.ndarray:
+        """cs_suspicion_rank: suspects over two windows of cycle indices."""
+        nrm = np.ascontiguousarray(np.asarray(normal_cycles, dtype=np.uint64))
+        abn = np.ascontiguousarray(np.asarray(abnormal_cycles, dtype=np.uint64))
+        cn, cg, cr = (np.ascontiguousarray(np.asarray(a, dtype=np.int32)) for a in (comm_name, comm_group, comm_rank))
+        cl = None if comm_location is None else np.ascontiguousarray(np.asarray(comm_location, dtype=np.int32))
+        n = C.c_size_t(0)
+        args = [self.h, inst, _ptr(nrm), len(nrm), _ptr(abn), len(abn), _ptr(cn), _ptr(cg), _ptr(cr),
+                _ptr(cl) if cl is not None else None]
+        self._ck(self.L.cs_suspicion_rank(*args, None, 0, C.byref(n)))
+        out = np.zeros(n.value, abi.SUSPECT_DTYPE)
+        self._ck(self.L.cs_suspicion_rank(*args, _ptr(out), n.value, C.byref(n)))
+        return out
 
     def alerts(self, inst=0):
         return self._get(self.L.cs_get_alerts, inst, abi.ALERT_DTYPE)
