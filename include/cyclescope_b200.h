@@ -402,6 +402,13 @@ typedef struct cs_ingest_issue {
   uint8_t reserved[5];
   uint64_t event_id;
 } cs_ingest_issue;
+/* resolve_topology (align.cpp:178-191) from the same records: a location per
+ * comm slot (index into the locations, -1 unmapped); locations are distinct
+ * (hostname, device) pairs, hostnames NUL-separated.  *conflicting != 0 when a
+ * (commHash, rank) maps to two locations (the reference's ConflictingTopology). */
+int cs_ingest_topology(const cs_ingest_result* r, const int32_t** comm_location,
+                       const char** loc_nodes, size_t* loc_nodes_bytes, const int32_t** loc_device,
+                       uint32_t* n_locations, int* conflicting);
 int cs_ingest_report(const cs_ingest_result* r, const cs_ingest_issue** issues, uint64_t* n_issues,
                      uint64_t* n_parse_issues, uint64_t category_counts[8], uint64_t* n_errors);
 

@@ -53,6 +53,10 @@ struct cs_ingest_result {
   std::string names_packed;
   uint32_t n_names = 0;
   std::vector<int32_t> comm_name, comm_rank;
+  // resolve_topology (align.cpp:178-191): per comm slot a location, -1 unmapped
+  std::vector<int32_t> comm_location, loc_device;
+  std::string loc_nodes_packed;
+  int topology_conflict = 0;
   std::string comm_hash_packed;
   uint64_t n_issues = 0;  // parse issues
   std::vector<cs_ingest_issue> issues;  // parse issues, then validate_trace's
@@ -564,7 +568,7 @@ struct Keys {
 
 // the args the path reads, after flattening (later writes win)
 struct Args {
-  Arg fm, batch, in, out, comm, rank, value, corr;
+  Arg fm, batch, in, out, comm, rank, value, corr, host, dev;
   uint64_t dropped = 0;
   Arg* slot(std::string_view k, const Keys& keys) {
     using namespace std::string_view_literals;
@@ -576,6 +580,8 @@ struct Args {
     if (k == "rank"sv) return &rank;
     if (k == "value"sv) return &value;
     if (k == "correlation_id"sv) return &corr;
+    if (k == "hostname"sv) return &host;
+    if (k == "device"sv) return &dev;
     return nullptr;
   }
 };
@@ -1314,6 +1320,46 @@ int cs_ingest_chrome_json(const char* text, size_t len, const cs_ingest_keys* ke
     res->comm_hash_packed.append(ck.hash);
     res->comm_hash_packed.push_back('\0');
   }
+  // ---- topology: (commHash, rank) -> (hostname, device) from every
+  // CollectiveComm record carrying all four args; a key mapped to two
+  // locations is the reference's ConflictingTopology
+  {
+    using Key = std::pair<std::string_view, int>;
+    using Loc = std::pair<std::string_view, int>;
+    std::vector<std::vector<std::pair<Key, Loc>>> tl(n_threads);
+    parallel_for(kept.size(), n_threads, [&](size_t k0, size_t k1, uint32_t t) {
+      for (size_t k = k0; k < k1; ++k) {
+        const Rec& r = *kept[k];
+        if (r.category != CS_CAT_COLLECTIVE_COMM) continue;
+        const std::string_view* comm = arg_string(r.args.comm);
+        const std::string_view* host = arg_string(r.args.host);
+        const auto rank = arg_int(r.args.rank), dev = arg_int(r.args.dev);
+        if (comm && rank && host && dev)
+          tl[t].push_back({{*comm, static_cast<int>(*rank)}, {*host, static_cast<int>(*dev)}});
+      }
+    });
+    std::map<Key, Loc> topo;
+    for (const auto& v : tl)
+      for (const auto& [key, loc] : v) {
+        const auto [it, inserted] = topo.emplace(key, loc);
+        if (!inserted && it->second != loc) res->topology_conflict = 1;
+      }
+    std::vector<Loc> locs;
+    for (const auto& kv : topo) locs.push_back(kv.second);
+    std::sort(locs.begin(), locs.end());
+    locs.erase(std::unique(locs.begin(), locs.end()), locs.end());
+    for (const auto& l : locs) {
+      res->loc_nodes_packed.append(l.first);
+      res->loc_nodes_packed.push_back('\0');
+      res->loc_device.push_back(l.second);
+    }
+    for (const auto& ck : comms) {
+      const auto it = topo.find({ck.hash, ck.rank});
+      res->comm_location.push_back(
+          it == topo.end() ? -1
+                           : static_cast<int32_t>(std::lower_bound(locs.begin(), locs.end(), it->second) - locs.begin()));
+    }
+  }
   // ---- records (the exporters' contract, include/cyclescope_b200.h)
   res->events.resize(kept.size());
   res->event_ids.resize(kept.size());
@@ -1404,6 +1450,19 @@ int cs_ingest_view(const cs_ingest_result* r, const cs_event** ev, const uint64_
   if (comm_bytes) *comm_bytes = r->comm_hash_packed.size();
   if (n_comm) *n_comm = static_cast<uint32_t>(r->comm_name.size());
   if (n_issues) *n_issues = r->n_issues;
+  return CS_OK;
+}
+
+int cs_ingest_topology(const cs_ingest_result* r, const int32_t** comm_location,
+                       const char** loc_nodes, size_t* loc_nodes_bytes, const int32_t** loc_device,
+                       uint32_t* n_locations, int* conflicting) {
+  if (!r) return CS_E_INVALID_ARGUMENT;
+  if (comm_location) *comm_location = r->comm_location.data();
+  if (loc_nodes) *loc_nodes = r->loc_nodes_packed.data();
+  if (loc_nodes_bytes) *loc_nodes_bytes = r->loc_nodes_packed.size();
+  if (loc_device) *loc_device = r->loc_device.data();
+  if (n_locations) *n_locations = static_cast<uint32_t>(r->loc_device.size());
+  if (conflicting) *conflicting = r->topology_conflict;
   return CS_OK;
 }
 

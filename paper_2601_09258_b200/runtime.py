@@ -71,6 +71,8 @@ def lib():
                                     C.c_size_t, C.POINTER(C.c_size_t)]
     L.cs_welch_p_value.restype = C.c_double
     L.cs_welch_p_value.argtypes = [C.c_double, C.c_double, u64, C.c_double, C.c_double, u64]
+    L.cs_ingest_topology.argtypes = [vp, C.POINTER(vp), C.POINTER(vp), C.POINTER(C.c_size_t), C.POINTER(vp),
+                                     C.POINTER(u32), C.POINTER(C.c_int)]
     L.cs_ingest_report.argtypes = [vp, C.POINTER(vp), C.POINTER(u64), C.POINTER(u64), vp, C.POINTER(u64)]
     L.cs_load_model.argtypes = [vp, u32, C.POINTER(abi.Model)]
     L.cs_run.argtypes = [vp, u32]
@@ -122,7 +124,7 @@ def lib():
 EXPORTED_SYMBOLS = [
     "cs_abi_version", "cs_status_type", "cs_ctx_create", "cs_ctx_destroy", "cs_last_error",
     "cs_set_config", "cs_set_name_table", "cs_upload", "cs_upload_wire", "cs_wire_pack",
-    "cs_wire_view", "cs_wire_free", "cs_ingest_chrome_json", "cs_ingest_view", "cs_ingest_free", "cs_ingest_report", "cs_rank_suspects",
+    "cs_wire_view", "cs_wire_free", "cs_ingest_chrome_json", "cs_ingest_view", "cs_ingest_free", "cs_ingest_report", "cs_ingest_topology", "cs_rank_suspects",
     "cs_suspicion_rank", "cs_welch_p_value", "cs_load_model", "cs_run", "cs_sync",
     "cs_get_summary", "cs_get_candidates", "cs_get_cycles", "cs_get_components", "cs_get_beta",
     "cs_get_collective_beta", "cs_get_mu", "cs_get_records", "cs_get_alerts", "cs_host_alloc",
@@ -430,6 +432,9 @@ class IngestedTrace:
     issues: np.ndarray = None      # ISSUE_DTYPE: parse issues, then validate_trace's
     category_counts: np.ndarray = None
     n_errors: int = 0
+    comm_location: np.ndarray = None  # per comm slot: index into locations, -1 unmapped
+    locations: list = None            # (hostname, device)
+    topology_conflict: bool = False
 
     @property
     def ok(self) -> bool:
@@ -467,11 +472,19 @@ def ingest_chrome_json(text: bytes, n_threads=None) -> IngestedTrace:
         ip, ni, npi, ne = C.c_void_p(), C.c_uint64(), C.c_uint64(), C.c_uint64()
         cats = np.zeros(8, np.uint64)
         _check(L.cs_ingest_report(h, C.byref(ip), C.byref(ni), C.byref(npi), cats.ctypes.data, C.byref(ne)))
+        cl, lnp, ld = C.c_void_p(), C.c_void_p(), C.c_void_p()
+        lnb, nloc, conf = C.c_size_t(), C.c_uint32(), C.c_int()
+        _check(L.cs_ingest_topology(h, C.byref(cl), C.byref(lnp), C.byref(lnb), C.byref(ld), C.byref(nloc),
+                                    C.byref(conf)))
+        nodes = C.string_at(lnp, lnb.value).split(b"\0")[:nloc.value] if lnb.value else []
+        devs = arr(ld, nloc.value, np.int32)
         return IngestedTrace(arr(ev, nev.value, abi.EVENT_DTYPE), arr(ids, nev.value, np.uint64),
                              arr(wl, nwl.value, abi.WORKLOAD_DTYPE), [x.decode() for x in names],
                              arr(cn, nc.value, np.int32), arr(cr, nc.value, np.int32),
                              [x.decode() for x in hashes], iss.value,
-                             arr(ip, ni.value, abi.ISSUE_DTYPE), cats, ne.value)
+                             arr(ip, ni.value, abi.ISSUE_DTYPE), cats, ne.value,
+                             arr(cl, nc.value, np.int32), [(x.decode(), int(d)) for x, d in zip(nodes, devs)],
+                             bool(conf.value))
     finally:
         L.cs_ingest_free(h)
 

@@ -27,6 +27,10 @@ def _compare(refbridge, text: bytes):
     assert got.issues.tobytes() == iss.tobytes()
     assert np.array_equal(got.category_counts, cats)
     assert got.n_errors == n_err and got.ok == (n_err == 0)
+    # resolve_topology per comm slot (align.cpp:178-191)
+    if not got.topology_conflict:
+        topo = ref.topology()
+        assert [list(got.locations[i]) if i >= 0 else None for i in got.comm_location] == topo
     return got
 
 
@@ -201,3 +205,20 @@ def test_validation_many_duplicate_ids(refbridge):
             for i, (t, e) in enumerate(zip(rng.integers(0, 5000, 20000), rng.integers(0, 15000, 20000)))]
     got = _compare(refbridge, _doc(recs))
     assert (got.issues["code"] == 2).sum() > 1000
+
+
+def test_topology_and_conflict(refbridge):
+    recs = [{"ph": "X", "name": "reduce", "ts": 1 + r, "dur": 1, "cat": "collective_comm",
+             "args": {"commHash": h, "rank": r, "hostname": f"n{r // 2}", "device": r % 2}}
+            for h in ("a", "b") for r in range(4)]
+    recs.append({"ph": "i", "name": "reduce", "ts": 9, "cat": "collective_comm",  # instants count too
+                 "args": {"commHash": "c", "rank": 0, "hostname": "n9", "device": 3}})
+    recs.append({"ph": "X", "name": "reduce", "ts": 10, "dur": 1, "cat": "collective_comm",
+                 "args": {"commHash": "c", "rank": 0}})                          # unmapped slot? no: mapped
+    recs.append({"ph": "X", "name": "reduce", "ts": 11, "dur": 1, "cat": "collective_comm",
+                 "args": {"commHash": "d", "rank": 1}})                          # unmapped
+    got = _compare(refbridge, _doc(recs))
+    assert not got.topology_conflict and -1 in list(got.comm_location)
+    recs.append({"ph": "X", "name": "reduce", "ts": 12, "dur": 1, "cat": "collective_comm",
+                 "args": {"commHash": "a", "rank": 0, "hostname": "elsewhere", "device": 0}})
+    assert rt.ingest_chrome_json(_doc(recs)).topology_conflict
