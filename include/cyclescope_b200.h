@@ -51,7 +51,10 @@ enum cs_status {
   CS_E_UNSUPPORTED = 12,       /* "unsupported": outside the device limits   */
   CS_E_CONFIG = 13,            /* "config_error"           errors.hpp:77-79  */
   CS_E_INTERNAL = 14,          /* "internal"                                 */
-  CS_E_INSUFFICIENT_CYCLES = 15 /* "insufficient_cycles"   errors.hpp:68-70  */
+  CS_E_INSUFFICIENT_CYCLES = 15, /* "insufficient_cycles"  errors.hpp:68-70  */
+  CS_E_NO_BEACONS = 16,         /* "no_beacons"             errors.hpp:26-28  */
+  CS_E_INCONSISTENT_BEACONS = 17, /* "inconsistent_beacons" errors.hpp:29-31  */
+  CS_E_ALREADY_CALIBRATED = 18  /* "already_calibrated"     errors.hpp:32-34  */
 };
 
 /* ------------------------------------------------------- event record (A1)
@@ -402,6 +405,26 @@ typedef struct cs_ingest_issue {
   uint8_t reserved[5];
   uint64_t event_id;
 } cs_ingest_issue;
+/* cmd_ingest's clock unification (main.cpp:80-97): the inputs' inline beacons
+ * (Instant "beacon" events with an integer args.reference_ts, extract_beacons)
+ * calibrate every clock domain (src.clock; calibrate, align.cpp:22-84: offset
+ * from one beacon, the mean offset, or a least-squares drift fit), each input
+ * is mapped onto the reference timeline (apply_calibration, 97-113:
+ * llround(offset + drift * ts), span durations scaled by drift) and re-sorted,
+ * and the inputs are merged (merge_traces, 193-206: stable canonical sort,
+ * event ids renumbered from 1).  *out is a new ingest result for the merged
+ * trace (names, collective slots, workloads and topology re-interned; no
+ * ValidationReport); CS_E_NO_BEACONS / CS_E_INCONSISTENT_BEACONS /
+ * CS_E_ALREADY_CALIBRATED as the reference throws them. */
+typedef struct cs_calibration_options { /* CalibrationOptions (align.hpp) */
+  const char* reference_domain;  /* NULL = "reference" */
+  double tolerance_ns;           /* 1000 */
+  int32_t estimate_drift;        /* 0 */
+  int32_t reserved;
+} cs_calibration_options;
+int cs_ingest_merge(const cs_ingest_result* const* inputs, uint32_t n_inputs,
+                    const cs_calibration_options* options, uint32_t n_threads,
+                    cs_ingest_result** out, char* err, size_t err_cap);
 /* resolve_topology (align.cpp:178-191) from the same records: a location per
  * comm slot (index into the locations, -1 unmapped); locations are distinct
  * (hostname, device) pairs, hostnames NUL-separated.  *conflicting != 0 when a

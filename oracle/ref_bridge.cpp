@@ -509,6 +509,38 @@ int ref_rca(void* hv, const uint64_t* normal, size_t n_normal, const uint64_t* a
   }
 }
 
+// cmd_ingest (main.cpp:80-97) without the validation gate and the file
+// write: parse each document, extract_beacons, calibrate, apply_calibration,
+// merge_traces.  A handle on the merged trace, or NULL with the error type.
+void* ref_merge(const char* const* texts, const size_t* lens, uint32_t n, const char* ref_domain,
+                double tolerance_ns, int estimate_drift, char* err, size_t err_cap) {
+  try {
+    std::vector<Trace> traces;
+    std::vector<Beacon> beacons;
+    for (uint32_t i = 0; i < n; ++i) {
+      auto parsed = parse_trace_json(std::string(texts[i], lens[i]));
+      auto b = extract_beacons(parsed.trace);
+      beacons.insert(beacons.end(), b.begin(), b.end());
+      traces.push_back(std::move(parsed.trace));
+    }
+    CalibrationOptions opt;
+    if (ref_domain) opt.reference_domain = ref_domain;
+    opt.tolerance_ns = tolerance_ns;
+    opt.estimate_drift = estimate_drift != 0;
+    const auto calibration = calibrate(beacons, opt);
+    for (auto& t : traces) apply_calibration(t, calibration);
+    auto h = std::make_unique<Handle>();
+    h->ds.trace = merge_traces(std::move(traces));
+    return h.release();
+  } catch (const EngineError& e) {
+    if (err && err_cap) {
+      std::strncpy(err, e.type().c_str(), err_cap - 1);
+      err[err_cap - 1] = 0;
+    }
+    return nullptr;
+  }
+}
+
 // resolve_topology (align.cpp:178-191) per exported comm slot: a JSON array
 // of [node, device] or null (unmapped)
 int ref_topology(void* hv, char* buf, size_t cap, size_t* n) {

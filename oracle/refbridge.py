@@ -39,6 +39,8 @@ def lib():
         L.ref_from_json.restype = vp
         L.ref_from_json.argtypes = [C.c_char_p, sz, C.POINTER(C.c_uint64)]
         L.ref_rca.argtypes = [vp, vp, sz, vp, sz, C.c_int, C.c_char_p, sz, C.POINTER(sz), C.c_char_p, sz]
+        L.ref_merge.restype = vp
+        L.ref_merge.argtypes = [vp, vp, C.c_uint32, C.c_char_p, C.c_double, C.c_int, C.c_char_p, sz]
         L.ref_topology.argtypes = [vp, C.c_char_p, sz, C.POINTER(sz)]
         L.ref_validate.argtypes = [vp, vp, sz, C.POINTER(sz), vp, C.POINTER(C.c_uint64)]
         L.ref_build.restype = vp
@@ -204,6 +206,21 @@ class RefTrace:
         out = np.zeros(n.value, abi.ISSUE_DTYPE)
         assert L.ref_validate(self.h, out.ctypes.data, n.value, C.byref(n), None, None) == 0
         return out, cats, ne.value
+
+    @classmethod
+    def merge(cls, texts, reference_domain="reference", tolerance_ns=1000.0, estimate_drift=False):
+        """The reference's cmd_ingest pipeline on documents: a RefTrace of the
+        merged trace, or ("error", type)."""
+        L = lib()
+        bufs = [C.create_string_buffer(t, len(t)) for t in texts]
+        ptrs = (C.c_void_p * max(1, len(texts)))(*[C.addressof(b) for b in bufs])
+        lens = (C.c_size_t * max(1, len(texts)))(*[len(t) for t in texts])
+        err = C.create_string_buffer(256)
+        h = L.ref_merge(ptrs, lens, len(texts), reference_domain.encode(), tolerance_ns,
+                        int(estimate_drift), err, 256)
+        if not h:
+            return ("error", err.value.decode())
+        return cls(h)
 
     @classmethod
     def from_json(cls, text: bytes):

@@ -75,7 +75,8 @@ STATUS_TYPES = {
     4: "no_anchor_found", 5: "missing_workload_args", 6: "feature_mismatch",
     7: "non_positive_latency", 8: "insufficient_data", 9: "insufficient_calibration",
     10: "no_labels", 11: "model_format_error", 12: "unsupported", 13: "config_error",
-    14: "internal", 15: "insufficient_cycles",
+    14: "internal", 15: "insufficient_cycles", 16: "no_beacons", 17: "inconsistent_beacons",
+    18: "already_calibrated",
 }
 U64_MAX = (1 << 64) - 1
 U32_MAX = (1 << 32) - 1
@@ -166,6 +167,11 @@ class Suspect(C.Structure):  # cs_suspect
                 ("mu_abn", C.c_double), ("delta_mu", C.c_double), ("welch_p", C.c_double),
                 ("straggler_slot", C.c_int32), ("straggler_location", C.c_int32),
                 ("rank_beta_shift", C.c_double)]
+
+
+class CalibrationOptions(C.Structure):  # cs_calibration_options
+    _fields_ = [("reference_domain", C.c_char_p), ("tolerance_ns", C.c_double),
+                ("estimate_drift", C.c_int32), ("reserved", C.c_int32)]
 
 
 class RcaWindow(C.Structure):  # cs_rca_window

@@ -298,6 +298,9 @@ const char* cs_status_type(int status) {
     case CS_E_UNSUPPORTED: return "unsupported";
     case CS_E_CONFIG: return "config_error";
     case CS_E_INSUFFICIENT_CYCLES: return "insufficient_cycles";
+    case CS_E_NO_BEACONS: return "no_beacons";
+    case CS_E_INCONSISTENT_BEACONS: return "inconsistent_beacons";
+    case CS_E_ALREADY_CALIBRATED: return "already_calibrated";
     default: return "internal";
   }
 }

@@ -57,6 +57,14 @@ struct cs_ingest_result {
   std::vector<int32_t> comm_location, loc_device;
   std::string loc_nodes_packed;
   int topology_conflict = 0;
+  std::vector<std::tuple<std::string, int, std::string, int>> topo;  // (hash, rank, node, device)
+  // clock domains (src.clock, default "reference") and inline beacons
+  // (extract_beacons, align.cpp:86-95): per event a domain id, the sorted
+  // domain names, and (event index, reference_ts) in event order
+  std::vector<uint16_t> domain;
+  std::vector<std::string> domains;
+  std::vector<std::pair<uint64_t, int64_t>> beacons;
+  bool calibrated = false;
   std::string comm_hash_packed;
   uint64_t n_issues = 0;  // parse issues
   std::vector<cs_ingest_issue> issues;  // parse issues, then validate_trace's
@@ -568,7 +576,7 @@ struct Keys {
 
 // the args the path reads, after flattening (later writes win)
 struct Args {
-  Arg fm, batch, in, out, comm, rank, value, corr, host, dev;
+  Arg fm, batch, in, out, comm, rank, value, corr, host, dev, ref_ts;
   uint64_t dropped = 0;
   Arg* slot(std::string_view k, const Keys& keys) {
     using namespace std::string_view_literals;
@@ -582,6 +590,7 @@ struct Args {
     if (k == "correlation_id"sv) return &corr;
     if (k == "hostname"sv) return &host;
     if (k == "device"sv) return &dev;
+    if (k == "reference_ts"sv) return &ref_ts;
     return nullptr;
   }
 };
@@ -746,6 +755,7 @@ struct Rec {
   uint64_t eid = 0;
   int kind = 0, category = 0;
   std::string_view name;  // into the document, or into the worker's arena
+  std::string_view domain = "reference";  // source.clock_domain
   int64_t start = 0, dur = 0;
   Args args;
   uint32_t name_id = 0;
@@ -875,6 +885,10 @@ void parse_record(const char* b, const char* e, Rec& r, const Keys& keys, Arena&
           }
           for (const char* q : sp)
             if (q) as_string(q, e, buf);
+          if (sp[1]) {
+            const std::string_view v = as_string(sp[1], e, buf);
+            r.domain = v.data() == buf.data() ? arena.keep(buf) : v;
+          }
         }
       }
     }
@@ -1344,6 +1358,8 @@ int cs_ingest_chrome_json(const char* text, size_t len, const cs_ingest_keys* ke
         const auto [it, inserted] = topo.emplace(key, loc);
         if (!inserted && it->second != loc) res->topology_conflict = 1;
       }
+    for (const auto& [key, loc] : topo)
+      res->topo.emplace_back(std::string(key.first), key.second, std::string(loc.first), loc.second);
     std::vector<Loc> locs;
     for (const auto& kv : topo) locs.push_back(kv.second);
     std::sort(locs.begin(), locs.end());
@@ -1422,6 +1438,31 @@ int cs_ingest_chrome_json(const char* text, size_t len, const cs_ingest_keys* ke
     res->events[i].payload |= static_cast<uint64_t>(res->workloads.size());
     res->workloads.push_back({*b, in ? *in : INT64_MIN, ou ? *ou : INT64_MIN});
   }
+  // clock domains (interned in name order) and inline beacons, in event order
+  {
+    std::vector<std::unordered_set<std::string_view>> td(n_threads);
+    std::vector<std::vector<std::pair<uint64_t, int64_t>>> tb(n_threads);
+    parallel_for(kept.size(), n_threads, [&](size_t k0, size_t k1, uint32_t t) {
+      for (size_t k = k0; k < k1; ++k) {
+        const Rec& r = *kept[k];
+        td[t].insert(r.domain);
+        if (r.kind == CS_INSTANT && r.name == "beacon")
+          if (const auto ref = arg_int(r.args.ref_ts)) tb[t].push_back({k, *ref});
+      }
+    });
+    std::set<std::string_view> ds;
+    for (const auto& v : td) ds.insert(v.begin(), v.end());
+    std::unordered_map<std::string_view, uint16_t> did;
+    for (const auto& d : ds) {
+      did[d] = static_cast<uint16_t>(res->domains.size());
+      res->domains.emplace_back(d);
+    }
+    res->domain.resize(kept.size());
+    parallel_for(kept.size(), n_threads, [&](size_t k0, size_t k1, uint32_t) {
+      for (size_t k = k0; k < k1; ++k) res->domain[k] = did.at(kept[k]->domain);
+    });
+    for (const auto& v : tb) res->beacons.insert(res->beacons.end(), v.begin(), v.end());
+  }
   res->n_issues = res->issues.size();
   std::vector<std::pair<size_t, uint64_t>> corr;
   for (const auto& v : tcorr) corr.insert(corr.end(), v.begin(), v.end());
@@ -1450,6 +1491,230 @@ int cs_ingest_view(const cs_ingest_result* r, const cs_event** ev, const uint64_
   if (comm_bytes) *comm_bytes = r->comm_hash_packed.size();
   if (n_comm) *n_comm = static_cast<uint32_t>(r->comm_name.size());
   if (n_issues) *n_issues = r->n_issues;
+  return CS_OK;
+}
+
+int cs_ingest_merge(const cs_ingest_result* const* in, uint32_t n_in, const cs_calibration_options* opt,
+                    uint32_t n_threads, cs_ingest_result** out, char* err, size_t err_cap) {
+  if (!out || (n_in && !in)) return CS_E_INVALID_ARGUMENT;
+  *out = nullptr;
+  for (uint32_t t = 0; t < n_in; ++t)
+    if (!in[t]) return CS_E_INVALID_ARGUMENT;
+  if (n_threads == 0) n_threads = 1;
+  auto failure = [&](int code, const std::string& msg) {
+    if (err && err_cap) {
+      std::strncpy(err, msg.c_str(), err_cap - 1);
+      err[err_cap - 1] = 0;
+    }
+    return code;
+  };
+  // ---- calibrate (align.cpp:22-84) from every input's beacons, input order
+  const std::string ref_dom = opt && opt->reference_domain ? opt->reference_domain : "reference";
+  const double tol = opt ? opt->tolerance_ns : 1000.0;
+  const bool fit_drift = opt && opt->estimate_drift;
+  struct Beacon {
+    std::string_view domain;
+    int64_t local, ref;
+  };
+  std::map<std::string_view, std::vector<Beacon>> groups;
+  for (uint32_t t = 0; t < n_in; ++t)
+    for (const auto& [i, ref] : in[t]->beacons) {
+      const std::string_view d = in[t]->domains[in[t]->domain[i]];
+      if (d != ref_dom) groups[d].push_back({d, in[t]->events[i].start_ts, ref});
+    }
+  struct Clock {
+    double offset = 0.0, drift = 1.0;
+    bool identity() const { return offset == 0.0 && drift == 1.0; }
+  };
+  std::map<std::string, Clock, std::less<>> clocks;
+  clocks[ref_dom] = Clock{};
+  for (const auto& [dom, g] : groups) {
+    Clock c;
+    const double n = static_cast<double>(g.size());
+    if (g.size() == 1) {
+      c.offset = static_cast<double>(g[0].ref - g[0].local);
+    } else if (!fit_drift) {
+      double sum = 0.0;
+      for (const auto& b : g) sum += static_cast<double>(b.ref - b.local);
+      c.offset = sum / n;
+    } else {  // least squares: ref = offset + drift * local
+      double ml = 0.0, mr = 0.0;
+      for (const auto& b : g) {
+        ml += static_cast<double>(b.local);
+        mr += static_cast<double>(b.ref);
+      }
+      ml /= n;
+      mr /= n;
+      double cov = 0.0, var = 0.0;
+      for (const auto& b : g) {
+        const double dl = static_cast<double>(b.local) - ml, dr = static_cast<double>(b.ref) - mr;
+        cov += dl * dr;
+        var += dl * dl;
+      }
+      c.drift = var > 0.0 ? cov / var : 1.0;
+      c.offset = mr - c.drift * ml;
+    }
+    double worst = 0.0;
+    for (const auto& b : g)
+      worst = std::max(worst, std::abs(c.offset + c.drift * static_cast<double>(b.local) - static_cast<double>(b.ref)));
+    if (worst > tol)
+      return failure(CS_E_INCONSISTENT_BEACONS, "domain '" + std::string(dom) + "' max beacon residual " +
+                                                    std::to_string(worst) + " ns exceeds tolerance");
+    clocks[std::string(dom)] = c;
+  }
+  // ---- apply_calibration per input (align.cpp:97-113), then merge_traces (193-206)
+  struct Item {
+    int64_t ts;
+    uint64_t eid;
+    uint32_t t;
+    uint64_t i;
+  };
+  std::vector<std::vector<Item>> items(n_in);
+  std::vector<std::vector<cs_event>> evs(n_in);
+  for (uint32_t t = 0; t < n_in; ++t) {
+    const cs_ingest_result& r = *in[t];
+    if (r.calibrated) return failure(CS_E_ALREADY_CALIBRATED, "trace timestamps are already on the unified timeline");
+    std::vector<const Clock*> of(r.domains.size(), nullptr);
+    for (size_t d = 0; d < r.domains.size(); ++d) {
+      const auto it = clocks.find(r.domains[d]);
+      if (it != clocks.end()) of[d] = &it->second;
+    }
+    for (size_t i = 0; i < r.events.size(); ++i)
+      if (!of[r.domain[i]])
+        return failure(CS_E_NO_BEACONS, "no calibration for clock domain '" + r.domains[r.domain[i]] + "'");
+    evs[t] = r.events;
+    items[t].resize(r.events.size());
+    parallel_for(r.events.size(), n_threads, [&](size_t k0, size_t k1, uint32_t) {
+      for (size_t i = k0; i < k1; ++i) {
+        cs_event& e = evs[t][i];
+        const Clock& c = *of[r.domain[i]];
+        if (!c.identity()) {
+          const int64_t start = static_cast<int64_t>(std::llround(c.offset + c.drift * static_cast<double>(e.start_ts)));
+          if (e.kind == CS_SPAN)
+            e.duration = static_cast<int64_t>(std::llround(c.drift * static_cast<double>(e.duration)));
+          e.start_ts = start;
+        }
+        items[t][i] = Item{e.start_ts, r.event_ids[i], t, i};
+      }
+    });
+  }
+  auto less = [](const Item& a, const Item& b) { return a.ts != b.ts ? a.ts < b.ts : a.eid < b.eid; };
+  std::vector<Item> all;
+  for (uint32_t t = 0; t < n_in; ++t) {
+    std::stable_sort(items[t].begin(), items[t].end(), less);  // trace.sort_events()
+    all.insert(all.end(), items[t].begin(), items[t].end());
+  }
+  std::stable_sort(all.begin(), all.end(), less);
+  // ---- the merged trace's tables: names, collective slots, domains, topology
+  auto* res = new cs_ingest_result();
+  std::vector<std::vector<std::string>> tnames(n_in);
+  std::set<std::string> name_set;
+  for (uint32_t t = 0; t < n_in; ++t) {
+    const std::string& p = in[t]->names_packed;
+    size_t a = 0;
+    for (uint32_t k = 0; k < in[t]->n_names; ++k) {
+      const size_t b = p.find('\0', a);
+      tnames[t].push_back(p.substr(a, b - a));
+      a = b + 1;
+    }
+    name_set.insert(tnames[t].begin(), tnames[t].end());
+  }
+  std::vector<std::string> names(name_set.begin(), name_set.end());
+  std::vector<std::vector<uint32_t>> name_map(n_in);
+  for (uint32_t t = 0; t < n_in; ++t)
+    for (const auto& nm : tnames[t])
+      name_map[t].push_back(static_cast<uint32_t>(std::lower_bound(names.begin(), names.end(), nm) - names.begin()));
+  for (const auto& nm : names) {
+    res->names_packed.append(nm);
+    res->names_packed.push_back('\0');
+  }
+  res->n_names = static_cast<uint32_t>(names.size());
+  using CK = std::tuple<std::string, std::string, int>;
+  std::vector<std::vector<CK>> tcomm(n_in);
+  std::set<CK> comm_set;
+  for (uint32_t t = 0; t < n_in; ++t) {
+    const std::string& p = in[t]->comm_hash_packed;
+    size_t a = 0;
+    for (size_t k = 0; k < in[t]->comm_name.size(); ++k) {
+      const size_t b = p.find('\0', a);
+      tcomm[t].emplace_back(tnames[t][in[t]->comm_name[k]], p.substr(a, b - a), in[t]->comm_rank[k]);
+      a = b + 1;
+    }
+    comm_set.insert(tcomm[t].begin(), tcomm[t].end());
+  }
+  std::vector<CK> comms(comm_set.begin(), comm_set.end());
+  std::vector<std::vector<uint32_t>> comm_map(n_in);
+  for (uint32_t t = 0; t < n_in; ++t)
+    for (const auto& ck : tcomm[t])
+      comm_map[t].push_back(static_cast<uint32_t>(std::lower_bound(comms.begin(), comms.end(), ck) - comms.begin()));
+  for (const auto& [nm, h, rk] : comms) {
+    res->comm_name.push_back(static_cast<int32_t>(std::lower_bound(names.begin(), names.end(), nm) - names.begin()));
+    res->comm_rank.push_back(rk);
+    res->comm_hash_packed.append(h);
+    res->comm_hash_packed.push_back('\0');
+  }
+  std::set<std::string> dom_set;
+  for (uint32_t t = 0; t < n_in; ++t) dom_set.insert(in[t]->domains.begin(), in[t]->domains.end());
+  res->domains.assign(dom_set.begin(), dom_set.end());
+  std::map<std::pair<std::string, int>, std::pair<std::string, int>> topo;
+  for (uint32_t t = 0; t < n_in; ++t) {
+    if (in[t]->topology_conflict) res->topology_conflict = 1;
+    for (const auto& [h, rk, node, dev] : in[t]->topo) {
+      const auto [it, inserted] = topo.emplace(std::make_pair(h, rk), std::make_pair(node, dev));
+      if (!inserted && it->second != std::make_pair(node, dev)) res->topology_conflict = 1;
+    }
+  }
+  std::vector<std::pair<std::string, int>> locs;
+  for (const auto& [key, loc] : topo) {
+    res->topo.emplace_back(key.first, key.second, loc.first, loc.second);
+    locs.push_back(loc);
+  }
+  std::sort(locs.begin(), locs.end());
+  locs.erase(std::unique(locs.begin(), locs.end()), locs.end());
+  for (const auto& l : locs) {
+    res->loc_nodes_packed.append(l.first);
+    res->loc_nodes_packed.push_back('\0');
+    res->loc_device.push_back(l.second);
+  }
+  for (const auto& [nm, h, rk] : comms) {
+    (void)nm;
+    const auto it = topo.find({h, rk});
+    res->comm_location.push_back(
+        it == topo.end() ? -1
+                         : static_cast<int32_t>(std::lower_bound(locs.begin(), locs.end(), it->second) - locs.begin()));
+  }
+  // ---- merged records: remapped ids, event ids 1..n (merge_traces), workload
+  // table rebuilt in the merged order, beacons re-extracted
+  const size_t n = all.size();
+  res->events.resize(n);
+  res->event_ids.resize(n);
+  res->domain.resize(n);
+  for (size_t k = 0; k < n; ++k) {
+    const Item& it = all[k];
+    const cs_ingest_result& r = *in[it.t];
+    cs_event e = evs[it.t][it.i];
+    e.name_id = name_map[it.t][e.name_id];
+    if (e.flags & CS_EV_HAS_COMM)
+      e.payload = (e.payload & 0xffffffffull) | (static_cast<uint64_t>(comm_map[it.t][e.payload >> 32]) << 32);
+    if (e.flags & CS_EV_HAS_BATCH) {
+      const uint64_t w = e.payload & 0xffffffffull;
+      e.payload = (e.payload & ~0xffffffffull) | static_cast<uint64_t>(res->workloads.size());
+      res->workloads.push_back(r.workloads[w]);
+    }
+    res->events[k] = e;
+    res->event_ids[k] = k + 1;
+    res->domain[k] = static_cast<uint16_t>(
+        std::lower_bound(res->domains.begin(), res->domains.end(), r.domains[r.domain[it.i]]) - res->domains.begin());
+  }
+  std::vector<std::unordered_map<uint64_t, int64_t>> bmap(n_in);
+  for (uint32_t t = 0; t < n_in; ++t) bmap[t].insert(in[t]->beacons.begin(), in[t]->beacons.end());
+  for (size_t k = 0; k < n; ++k) {
+    const auto it = bmap[all[k].t].find(all[k].i);
+    if (it != bmap[all[k].t].end()) res->beacons.push_back({k, it->second});
+  }
+  for (const cs_event& e : res->events) ++res->categories[e.category & 7];
+  res->calibrated = true;
+  *out = res;
   return CS_OK;
 }
 

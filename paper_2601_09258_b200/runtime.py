@@ -73,6 +73,8 @@ def lib():
     L.cs_welch_p_value.argtypes = [C.c_double, C.c_double, u64, C.c_double, C.c_double, u64]
     L.cs_ingest_topology.argtypes = [vp, C.POINTER(vp), C.POINTER(vp), C.POINTER(C.c_size_t), C.POINTER(vp),
                                      C.POINTER(u32), C.POINTER(C.c_int)]
+    L.cs_ingest_merge.argtypes = [vp, u32, C.POINTER(abi.CalibrationOptions), u32, C.POINTER(vp),
+                                  C.c_char_p, C.c_size_t]
     L.cs_ingest_report.argtypes = [vp, C.POINTER(vp), C.POINTER(u64), C.POINTER(u64), vp, C.POINTER(u64)]
     L.cs_load_model.argtypes = [vp, u32, C.POINTER(abi.Model)]
     L.cs_run.argtypes = [vp, u32]
@@ -124,7 +126,7 @@ def lib():
 EXPORTED_SYMBOLS = [
     "cs_abi_version", "cs_status_type", "cs_ctx_create", "cs_ctx_destroy", "cs_last_error",
     "cs_set_config", "cs_set_name_table", "cs_upload", "cs_upload_wire", "cs_wire_pack",
-    "cs_wire_view", "cs_wire_free", "cs_ingest_chrome_json", "cs_ingest_view", "cs_ingest_free", "cs_ingest_report", "cs_ingest_topology", "cs_rank_suspects",
+    "cs_wire_view", "cs_wire_free", "cs_ingest_chrome_json", "cs_ingest_view", "cs_ingest_free", "cs_ingest_report", "cs_ingest_topology", "cs_ingest_merge", "cs_rank_suspects",
     "cs_suspicion_rank", "cs_welch_p_value", "cs_load_model", "cs_run", "cs_sync",
     "cs_get_summary", "cs_get_candidates", "cs_get_cycles", "cs_get_components", "cs_get_beta",
     "cs_get_collective_beta", "cs_get_mu", "cs_get_records", "cs_get_alerts", "cs_host_alloc",
@@ -453,40 +455,74 @@ def ingest_chrome_json(text: bytes, n_threads=None) -> IngestedTrace:
     _check(L.cs_ingest_chrome_json(text, len(text), None, n_threads or os.cpu_count() or 1,
                                    C.byref(h)))
     try:
-        ev, ids, wl, nm, cn, cr, ch = (C.c_void_p() for _ in range(7))
-        nev, nwl, iss = C.c_uint64(), C.c_uint64(), C.c_uint64()
-        nb, cb = C.c_size_t(), C.c_size_t()
-        nn, nc = C.c_uint32(), C.c_uint32()
-        _check(L.cs_ingest_view(h, C.byref(ev), C.byref(ids), C.byref(nev), C.byref(wl), C.byref(nwl),
-                                C.byref(nm), C.byref(nb), C.byref(nn), C.byref(cn), C.byref(cr),
-                                C.byref(ch), C.byref(cb), C.byref(nc), C.byref(iss)))
-
-        def arr(ptr, n, dtype):
-            if n == 0 or not ptr.value:
-                return np.zeros(0, dtype=dtype)
-            nbytes = n * np.dtype(dtype).itemsize
-            return np.frombuffer((C.c_char * nbytes).from_address(ptr.value), dtype=dtype).copy()
-
-        names = C.string_at(nm, nb.value).split(b"\0")[:nn.value] if nb.value else []
-        hashes = C.string_at(ch, cb.value).split(b"\0")[:nc.value] if cb.value else []
-        ip, ni, npi, ne = C.c_void_p(), C.c_uint64(), C.c_uint64(), C.c_uint64()
-        cats = np.zeros(8, np.uint64)
-        _check(L.cs_ingest_report(h, C.byref(ip), C.byref(ni), C.byref(npi), cats.ctypes.data, C.byref(ne)))
-        cl, lnp, ld = C.c_void_p(), C.c_void_p(), C.c_void_p()
-        lnb, nloc, conf = C.c_size_t(), C.c_uint32(), C.c_int()
-        _check(L.cs_ingest_topology(h, C.byref(cl), C.byref(lnp), C.byref(lnb), C.byref(ld), C.byref(nloc),
-                                    C.byref(conf)))
-        nodes = C.string_at(lnp, lnb.value).split(b"\0")[:nloc.value] if lnb.value else []
-        devs = arr(ld, nloc.value, np.int32)
-        return IngestedTrace(arr(ev, nev.value, abi.EVENT_DTYPE), arr(ids, nev.value, np.uint64),
-                             arr(wl, nwl.value, abi.WORKLOAD_DTYPE), [x.decode() for x in names],
-                             arr(cn, nc.value, np.int32), arr(cr, nc.value, np.int32),
-                             [x.decode() for x in hashes], iss.value,
-                             arr(ip, ni.value, abi.ISSUE_DTYPE), cats, ne.value,
-                             arr(cl, nc.value, np.int32), [(x.decode(), int(d)) for x, d in zip(nodes, devs)],
-                             bool(conf.value))
+        return _ingest_extract(h)
     finally:
         L.cs_ingest_free(h)
+
+
+def ingest_merge(texts, reference_domain="reference", tolerance_ns=1000.0, estimate_drift=False,
+                 n_threads=None) -> IngestedTrace:
+    """cmd_ingest (main.cpp:80-97) natively: ingest each document, calibrate
+    the clock domains from their beacons, apply, merge (cs_ingest_merge)."""
+    L = lib()
+    nt = n_threads or os.cpu_count() or 1
+    hs = []
+    try:
+        for t in texts:
+            h = C.c_void_p()
+            _check(L.cs_ingest_chrome_json(t, len(t), None, nt, C.byref(h)))
+            hs.append(h)
+        arr = (C.c_void_p * max(1, len(hs)))(*[h.value for h in hs])
+        opt = abi.CalibrationOptions(reference_domain.encode(), tolerance_ns, int(estimate_drift), 0)
+        out = C.c_void_p()
+        err = C.create_string_buffer(512)
+        rc = L.cs_ingest_merge(arr, len(hs), C.byref(opt), nt, C.byref(out), err, 512)
+        if rc:
+            raise EngineError(rc, err.value.decode())
+        try:
+            return _ingest_extract(out)
+        finally:
+            L.cs_ingest_free(out)
+    finally:
+        for h in hs:
+            L.cs_ingest_free(h)
+
+
+def _ingest_extract(h) -> IngestedTrace:
+    """IngestedTrace from a cs_ingest_result handle (copied out)."""
+    L = lib()
+    ev, ids, wl, nm, cn, cr, ch = (C.c_void_p() for _ in range(7))
+    nev, nwl, iss = C.c_uint64(), C.c_uint64(), C.c_uint64()
+    nb, cb = C.c_size_t(), C.c_size_t()
+    nn, nc = C.c_uint32(), C.c_uint32()
+    _check(L.cs_ingest_view(h, C.byref(ev), C.byref(ids), C.byref(nev), C.byref(wl), C.byref(nwl),
+                            C.byref(nm), C.byref(nb), C.byref(nn), C.byref(cn), C.byref(cr),
+                            C.byref(ch), C.byref(cb), C.byref(nc), C.byref(iss)))
+
+    def arr(ptr, n, dtype):
+        if n == 0 or not ptr.value:
+            return np.zeros(0, dtype=dtype)
+        nbytes = n * np.dtype(dtype).itemsize
+        return np.frombuffer((C.c_char * nbytes).from_address(ptr.value), dtype=dtype).copy()
+
+    names = C.string_at(nm, nb.value).split(b"\0")[:nn.value] if nb.value else []
+    hashes = C.string_at(ch, cb.value).split(b"\0")[:nc.value] if cb.value else []
+    ip, ni, npi, ne = C.c_void_p(), C.c_uint64(), C.c_uint64(), C.c_uint64()
+    cats = np.zeros(8, np.uint64)
+    _check(L.cs_ingest_report(h, C.byref(ip), C.byref(ni), C.byref(npi), cats.ctypes.data, C.byref(ne)))
+    cl, lnp, ld = C.c_void_p(), C.c_void_p(), C.c_void_p()
+    lnb, nloc, conf = C.c_size_t(), C.c_uint32(), C.c_int()
+    _check(L.cs_ingest_topology(h, C.byref(cl), C.byref(lnp), C.byref(lnb), C.byref(ld), C.byref(nloc),
+                                C.byref(conf)))
+    nodes = C.string_at(lnp, lnb.value).split(b"\0")[:nloc.value] if lnb.value else []
+    devs = arr(ld, nloc.value, np.int32)
+    return IngestedTrace(arr(ev, nev.value, abi.EVENT_DTYPE), arr(ids, nev.value, np.uint64),
+                         arr(wl, nwl.value, abi.WORKLOAD_DTYPE), [x.decode() for x in names],
+                         arr(cn, nc.value, np.int32), arr(cr, nc.value, np.int32),
+                         [x.decode() for x in hashes], iss.value,
+                         arr(ip, ni.value, abi.ISSUE_DTYPE), cats, ne.value,
+                         arr(cl, nc.value, np.int32), [(x.decode(), int(d)) for x, d in zip(nodes, devs)],
+                         bool(conf.value))
 
 
 @dataclass
