@@ -325,8 +325,51 @@ def run_ours(args, rank, world, local_rank):
                 n_al = sum(len(a) for a in al)
         return sum(times) / len(times), d2h_b, n_al
 
-    e2e, d2h, alerts_total = e2e_leg(lambda: an.upload_wire(wire, wire_wl))
+    e2e_seq, d2h, alerts_total = e2e_leg(lambda: an.upload_wire(wire, wire_wl))
     e2e32, _, _ = e2e_leg(lambda: an.upload(pin_ev, offs, pin_wl))
+
+    # Serving pattern (N=1): two contexts on their own non-blocking streams,
+    # one host thread each taking alternate steps, so one step's upload over
+    # PCIe overlaps the other's analysis.  Every step still copies its inputs
+    # from pinned memory and reads its alerts and summaries back inside the
+    # timed region; ms_per_step = wall time / steps.
+    e2e, pipeline = e2e_seq, 1
+    if not dist:
+        import threading
+        an2 = rt.Analyzer(dev)
+        an2.configure(names, span, n_comm_slots=n_comm)
+        for i, model in enumerate(models):
+            an2.load_model(model, inst=i)
+        ctxs = [an, an2]
+
+        def step(a):
+            a.upload_wire(wire, wire_wl)
+            a.run(mask)
+            al = [a.alerts(i) for i in range(n_inst)]
+            _ = [a.summary(i) for i in range(n_inst)]
+            return al
+
+        for a in ctxs:
+            for _ in range(max(1, args.warmup // 2)):
+                step(a)
+        results = [None, None]
+
+        def worker(j, n_steps):
+            for _ in range(n_steps):
+                results[j] = step(ctxs[j])
+
+        n0 = (args.steps + 1) // 2
+        th = [threading.Thread(target=worker, args=(0, n0)),
+              threading.Thread(target=worker, args=(1, args.steps - n0))]
+        t0 = time.perf_counter()
+        for x in th:
+            x.start()
+        for x in th:
+            x.join()
+        e2e = (time.perf_counter() - t0) * 1e3 / args.steps
+        pipeline = 2
+        assert sum(len(x) for x in results[0]) == alerts_total
+        an2.close()
     rt.host_free(wptr)
 
     if dist:
@@ -402,6 +445,7 @@ def run_ours(args, rank, world, local_rank):
                 "h2d_bytes_per_step": wire_bytes, "d2h_bytes_per_step": d2h,
                 "ms_per_step": e2e, "input": f"columnar wire format (cs_upload_wire, {wire_bytes_per_event:.1f} B/event incl. workloads) from pinned memory",
                 "timer": "host wall clock around the synchronous API calls",
+                "pipeline": pipeline, "ms_per_step_one_context": e2e_seq,
                 "cs_event_32B": {"value": world * n_events / (e2e32 * 1e-3), "ms_per_step": e2e32,
                                  "h2d_bytes_per_step": ev_bytes + wl_bytes}},
         "gpu_launches": launches,
