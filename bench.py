@@ -329,8 +329,9 @@ def run_ours(args, rank, world, local_rank):
     e2e32, _, _ = e2e_leg(lambda: an.upload(pin_ev, offs, pin_wl))
 
     # Serving pattern (N=1): two contexts on their own non-blocking streams,
-    # one host thread each taking alternate steps, so one step's upload over
-    # PCIe overlaps the other's analysis.  Every step still copies its inputs
+    # one host thread each taking alternate steps, uploads issued one at a
+    # time (cs_upload_wire returns when its copies are done), so one step's
+    # upload over PCIe overlaps the other's analysis.  Every step still copies its inputs
     # from pinned memory and reads its alerts and summaries back inside the
     # timed region; ms_per_step = wall time / steps.
     e2e, pipeline = e2e_seq, 1
@@ -342,8 +343,11 @@ def run_ours(args, rank, world, local_rank):
             an2.load_model(model, inst=i)
         ctxs = [an, an2]
 
+        link = threading.Lock()  # one upload on the host link at a time
+
         def step(a):
-            a.upload_wire(wire, wire_wl)
+            with link:
+                a.upload_wire(wire, wire_wl)  # returns when its copies are done
             a.run(mask)
             al = [a.alerts(i) for i in range(n_inst)]
             _ = [a.summary(i) for i in range(n_inst)]

@@ -342,7 +342,11 @@ typedef struct cs_wire_batch {
 } cs_wire_batch;
 
 /* Upload a batch in the wire format (same instance layout and semantics as
- * cs_upload; expanded on the device into the same cs_event records). */
+ * cs_upload; expanded on the device into the same cs_event records).
+ * cs_upload and cs_upload_wire return once the host->device copies have
+ * completed (the host buffers may be reused); the expansion and everything
+ * queued after it run asynchronously.  Two contexts whose uploads are issued
+ * one after the other keep the host link busy while the other analyses. */
 int cs_upload_wire(cs_ctx* ctx, uint32_t n_inst, const uint64_t* inst_offsets,
                    const cs_wire_batch* wire, uint64_t n_workloads, const cs_workload* wl);
 

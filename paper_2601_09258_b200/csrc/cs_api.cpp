@@ -139,6 +139,7 @@ struct cs_ctx {
   uint32_t last_mask = 0;
   // timing
   cudaEvent_t ev[16]{};
+  cudaEvent_t ev_copied = nullptr;  // end of the last upload's host->device copies
   std::vector<std::pair<std::string, std::pair<int, int>>> timed;
   uint64_t launches = 0;
   DevBuf d_scratch;
@@ -154,6 +155,7 @@ struct cs_ctx {
     for (auto* m : model_store) delete m;
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
+    if (ev_copied) cudaEventDestroy(ev_copied);
     if (stream) cudaStreamDestroy(stream);
   }
 };
@@ -496,6 +498,16 @@ int upload_layout(cs_ctx* ctx, uint32_t n_inst, const uint64_t* inst_offsets, bo
 
 extern "C" {
 
+// An upload returns once its host->device copies have completed: the
+// caller's buffers may be reused, and a caller driving two contexts can hand
+// the link to the other context's upload while this one's analysis runs.
+int wait_copied(cs_ctx* ctx) {
+  if (!ctx->ev_copied && cudaEventCreateWithFlags(&ctx->ev_copied, cudaEventDisableTiming) != cudaSuccess)
+    return fail(ctx, CS_E_CUDA, "cudaEventCreate");
+  CS_CUDA(cudaEventRecord(ctx->ev_copied, ctx->stream));
+  return CS_OK;
+}
+
 int cs_upload(cs_ctx* ctx, uint32_t n_inst, const uint64_t* inst_offsets, const cs_event* ev,
               uint64_t n_workloads, const cs_workload* wl) {
   const int rc = upload_layout(ctx, n_inst, inst_offsets, ev != nullptr, n_workloads, wl);
@@ -503,6 +515,8 @@ int cs_upload(cs_ctx* ctx, uint32_t n_inst, const uint64_t* inst_offsets, const 
   if (ctx->n_ev)
     CS_CUDA(cudaMemcpyAsync(ctx->d_ev.p, ev, ctx->n_ev * sizeof(cs_event), cudaMemcpyHostToDevice,
                             ctx->stream));
+  if (wait_copied(ctx) != CS_OK) return CS_E_CUDA;
+  CS_CUDA(cudaEventSynchronize(ctx->ev_copied));
   return CS_OK;
 }
 
@@ -544,10 +558,12 @@ int cs_upload_wire(cs_ctx* ctx, uint32_t n_inst, const uint64_t* inst_offsets,
   dv.values = static_cast<const double*>(put(w->values, w->n_values * 8, s_val));
   dv.escapes = static_cast<const cs_event*>(put(w->escapes, w->n_escapes * sizeof(cs_event), s_esc));
   CS_CUDA(cudaGetLastError());
+  if (wait_copied(ctx) != CS_OK) return CS_E_CUDA;
   launch_wire_expand(dv, static_cast<const uint64_t*>(ctx->d_tile_begin.p),
                      static_cast<const uint64_t*>(ctx->d_tile_end.p), static_cast<uint32_t>(nt),
                      static_cast<cs_event*>(ctx->d_ev.p), ctx->stream);
   CS_CUDA(cudaGetLastError());
+  CS_CUDA(cudaEventSynchronize(ctx->ev_copied));  // the expand keeps running
   return CS_OK;
 }
 

@@ -655,6 +655,10 @@ class Analyzer:
                                        C.byref(b), len(wl), _ptr(wl)))
         self.n_inst = len(w.inst_offsets) - 1
 
+    def sync(self):
+        """cs_sync: wait for the context's queued work."""
+        self._ck(self.L.cs_sync(self.h))
+
     def load_model(self, model: LatencyModel, inst: int | None = None):
         v = model.view()
         self._keep.append(model)
