@@ -288,8 +288,10 @@ def run_ours(args, rank, world, local_rank):
     # columnar wire format (cs_wire_pack, outside the timed region, as ingest
     # would); every step uploads it from pinned memory (cs_upload_wire: H2D +
     # device expand), runs the path and reads alerts + summaries back
-    wt = rt.wire_pack(pin_ev, offs, n_threads=threads)
-    cols = [getattr(wt, c) for c in rt.WireTrace.COLUMNS] + [pin_wl]
+    wt = rt.wire_pack(pin_ev, offs, pin_wl, n_threads=threads)
+    cols = [getattr(wt, c) for c in rt.WireTrace.COLUMNS]
+    if wt.workloads32 is None:  # a workload value that does not fit u32: the i64 table travels
+        cols[-1] = pin_wl
     wire_bytes = sum(a.nbytes for a in cols)
     wptr, wpin = rt.host_alloc(max(1, wire_bytes + 16 * len(cols)))
     views, o = [], 0
@@ -298,8 +300,12 @@ def run_ours(args, rank, world, local_rank):
         wpin[o:o + a.nbytes] = a.view(np.uint8).reshape(-1)
         views.append(wpin[o:o + a.nbytes].view(a.dtype).reshape(a.shape))
         o += a.nbytes
-    wire = rt.WireTrace(*views[:-1], wt.inst_offsets)
-    wire_wl = views[-1]
+    if wt.workloads32 is None:
+        wire = rt.WireTrace(*views[:-1], None, wt.inst_offsets)
+        wire_wl = views[-1]
+    else:
+        wire = rt.WireTrace(*views, wt.inst_offsets)
+        wire_wl = None
     wire_bytes_per_event = wire_bytes / n_events
     del wt, cols
 

@@ -293,52 +293,66 @@ int cs_upload(cs_ctx* ctx, uint32_t n_inst, const uint64_t* inst_offsets,
  * of cs_event and the device expands it in HBM (k_wire_expand).  Events are
  * grouped in instance-aligned blocks of CS_WIRE_BLOCK records (block b of
  * instance i covers events [inst_offsets[i] + b*CS_WIRE_BLOCK, ...)).
- *   events[]     one 32-bit word per event: code << 24 | dt, where code
- *                indexes dict[] (the packed name id (16 bits) | kind << 16 |
- *                category << 20 | CS_EV_* flags << 24 of the event) or is
- *                CS_WIRE_ESCAPE, and dt = start_ts - the previous event's
- *                start_ts in the block (the block's first event: start_ts -
- *                blocks[b].base_ts, which the encoder makes 0).  Events are
- *                canonically ordered, so dt >= 0;
+ *   codes[]      one byte per event: a dict code (< n_dict) or CS_WIRE_ESCAPE,
+ *                | CS_WIRE_LONG_DT when the start_ts delta needs 17..24 bits;
+ *   dt_lo[]      one u16 per event: the low 16 bits of dt = start_ts - the
+ *                previous event's start_ts in the block (the block's first
+ *                event: start_ts - blocks[b].base_ts, which the encoder makes
+ *                0).  Events are canonically ordered, so dt >= 0;
+ *   dt_hi[]      one byte per CS_WIRE_LONG_DT event: dt >> 16;
+ *   dict[]       the packed name id (16 bits) | kind << 16 | category << 20 |
+ *                CS_EV_* flags << 24 | CS_WIRE_WIDE (payload in pay16) of
+ *                each code;
  *   dur_lo[], dur_hi[]  one 24-bit duration per Span in event order (low
  *                16 bits, high 8 bits);
- *   payloads[]   one u16 per event with CS_EV_HAS_COMM (collective slot =
- *                cs_event.payload >> 32) or CS_EV_HAS_BATCH (workload index
- *                - blocks[b].batch_base);
+ *   pay8[], pay16[]  one entry per event with CS_EV_HAS_COMM (collective
+ *                slot = cs_event.payload >> 32) or CS_EV_HAS_BATCH (workload
+ *                index - blocks[b].batch_base), in the column its code's
+ *                CS_WIRE_WIDE bit selects;
  *   values[]     one f64 per Counter with CS_EV_HAS_VALUE;
  *   blocks[]     per block: base timestamp, batch_base, and the index of its
- *                first entry in the duration, payload, value and escape
- *                columns;
+ *                first entry in every column;
  *   escapes[]    full cs_event, in event order, for records that do not fit
  *                (dt or span duration >= 2^24, negative duration, a non-Span
  *                non-value duration, info not in dict, payload out of range,
  *                both HAS_BATCH and HAS_COMM).  The next event's dt is taken
- *                from an escaped event's start_ts like any other. */
+ *                from an escaped event's start_ts like any other;
+ *   workloads32[]  optional: the workload table as (batch, input_len,
+ *                output_len) u32 triples, 0xffffffff = absent (INT64_MIN). */
 #define CS_WIRE_BLOCK 1024u
-#define CS_WIRE_ESCAPE 0xffu
-#define CS_WIRE_MAX_DICT 255u
+#define CS_WIRE_ESCAPE 0x7fu
+#define CS_WIRE_LONG_DT 0x80u
+#define CS_WIRE_MAX_DICT 127u
+#define CS_WIRE_WIDE (1u << 30)
 typedef struct cs_wire_block {
   int64_t base_ts;
-  uint64_t dur, pay, val, esc;  /* first entry of the block in each column */
+  uint64_t dur, pay8, pay16, val, dt_hi, esc;  /* first entry of the block per column */
   uint32_t batch_base;
   uint32_t reserved;
 } cs_wire_block;
 
 typedef struct cs_wire_batch {
-  const uint32_t* events;        /* inst_offsets[n_inst] words */
-  const uint32_t* dict;          /* n_dict <= CS_WIRE_MAX_DICT info words */
+  const uint8_t* codes;          /* inst_offsets[n_inst] each */
+  const uint16_t* dt_lo;
+  const uint8_t* dt_hi;
+  uint64_t n_dt_hi;
+  const uint32_t* dict;          /* n_dict <= CS_WIRE_MAX_DICT */
   uint32_t n_dict;
   uint32_t reserved;
   const cs_wire_block* blocks;   /* n_blocks */
   const uint16_t* dur_lo;
   const uint8_t* dur_hi;
   uint64_t n_durations;
-  const uint16_t* payloads;
-  uint64_t n_payloads;
+  const uint8_t* pay8;
+  uint64_t n_pay8;
+  const uint16_t* pay16;
+  uint64_t n_pay16;
   const double* values;
   uint64_t n_values;
   const cs_event* escapes;
   uint64_t n_escapes;
+  const uint32_t* workloads32;   /* NULL: the cs_upload_wire workload arguments */
+  uint64_t n_workloads32;
 } cs_wire_batch;
 
 /* Upload a batch in the wire format (same instance layout and semantics as
@@ -346,7 +360,8 @@ typedef struct cs_wire_batch {
  * cs_upload and cs_upload_wire return once the host->device copies have
  * completed (the host buffers may be reused); the expansion and everything
  * queued after it run asynchronously.  Two contexts whose uploads are issued
- * one after the other keep the host link busy while the other analyses. */
+ * one after the other keep the host link busy while the other analyses.
+ * With wire->workloads32 set, n_workloads / wl must be 0 / NULL. */
 int cs_upload_wire(cs_ctx* ctx, uint32_t n_inst, const uint64_t* inst_offsets,
                    const cs_wire_batch* wire, uint64_t n_workloads, const cs_workload* wl);
 
@@ -355,7 +370,8 @@ int cs_upload_wire(cs_ctx* ctx, uint32_t n_inst, const uint64_t* inst_offsets,
  * object; cs_wire_view fills a cs_wire_batch pointing at them. */
 typedef struct cs_wire_trace cs_wire_trace;
 int cs_wire_pack(uint32_t n_inst, const uint64_t* inst_offsets, const cs_event* ev,
-                 uint32_t n_threads, cs_wire_trace** out);
+                 uint64_t n_workloads, const cs_workload* workloads, uint32_t n_threads,
+                 cs_wire_trace** out);
 int cs_wire_view(const cs_wire_trace* w, cs_wire_batch* out, uint64_t* n_blocks);
 void cs_wire_free(cs_wire_trace* w);
 

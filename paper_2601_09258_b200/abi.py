@@ -23,11 +23,14 @@ ISSUE_CODES = ("malformed_event", "malformed_args", "duplicate_event_id", "negat
                "duplicate_correlation", "unmatched_correlation", "non_monotone_counter")
 
 WIRE_BLOCK = 1024
-WIRE_ESCAPE = 0xFF          # dictionary code of an escaped event
-WIRE_MAX_DICT = 255
-WIRE_BLOCK_DTYPE = np.dtype([("base_ts", "<i8"), ("dur", "<u8"), ("pay", "<u8"), ("val", "<u8"),
-                             ("esc", "<u8"), ("batch_base", "<u4"), ("reserved", "<u4")])
-assert WIRE_BLOCK_DTYPE.itemsize == 48
+WIRE_ESCAPE = 0x7F          # code of an escaped event
+WIRE_LONG_DT = 0x80         # code bit: the delta's high byte is in dt_hi
+WIRE_MAX_DICT = 127
+WIRE_WIDE = 1 << 30         # dictionary bit: the payload is in pay16
+WIRE_BLOCK_DTYPE = np.dtype([("base_ts", "<i8"), ("dur", "<u8"), ("pay8", "<u8"), ("pay16", "<u8"),
+                             ("val", "<u8"), ("dt_hi", "<u8"), ("esc", "<u8"), ("batch_base", "<u4"),
+                             ("reserved", "<u4")])
+assert WIRE_BLOCK_DTYPE.itemsize == 64
 
 WORKLOAD_DTYPE = np.dtype([("batch", "<i8"), ("input_len", "<i8"), ("output_len", "<i8")])
 NAME_INFO_DTYPE = np.dtype(
@@ -144,12 +147,13 @@ def default_control(strategy: int = DYNAMIC_WINDOW) -> ControlConfig:
 
 
 class WireBatch(C.Structure):  # cs_wire_batch
-    _fields_ = [("events", C.c_void_p), ("dict", C.c_void_p), ("n_dict", C.c_uint32),
-                ("reserved", C.c_uint32), ("blocks", C.c_void_p),
-                ("dur_lo", C.c_void_p), ("dur_hi", C.c_void_p), ("n_durations", C.c_uint64),
-                ("payloads", C.c_void_p), ("n_payloads", C.c_uint64),
-                ("values", C.c_void_p), ("n_values", C.c_uint64),
-                ("escapes", C.c_void_p), ("n_escapes", C.c_uint64)]
+    _fields_ = [("codes", C.c_void_p), ("dt_lo", C.c_void_p), ("dt_hi", C.c_void_p), ("n_dt_hi", C.c_uint64),
+                ("dict", C.c_void_p), ("n_dict", C.c_uint32), ("reserved", C.c_uint32),
+                ("blocks", C.c_void_p), ("dur_lo", C.c_void_p), ("dur_hi", C.c_void_p),
+                ("n_durations", C.c_uint64), ("pay8", C.c_void_p), ("n_pay8", C.c_uint64),
+                ("pay16", C.c_void_p), ("n_pay16", C.c_uint64), ("values", C.c_void_p),
+                ("n_values", C.c_uint64), ("escapes", C.c_void_p), ("n_escapes", C.c_uint64),
+                ("workloads32", C.c_void_p), ("n_workloads32", C.c_uint64)]
 
 
 SUSPECT_DTYPE = np.dtype([("beta_slot", "<i4"), ("metric", "<i4"), ("beta_norm", "<f8"),

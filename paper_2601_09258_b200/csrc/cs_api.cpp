@@ -523,22 +523,26 @@ int cs_upload(cs_ctx* ctx, uint32_t n_inst, const uint64_t* inst_offsets, const 
 int cs_upload_wire(cs_ctx* ctx, uint32_t n_inst, const uint64_t* inst_offsets,
                    const cs_wire_batch* w, uint64_t n_workloads, const cs_workload* wl) {
   if (!w) return CS_E_INVALID_ARGUMENT;
-  const int rc = upload_layout(ctx, n_inst, inst_offsets, w->events != nullptr && w->blocks,
+  const bool wl32 = w->workloads32 != nullptr;
+  if (wl32 && (n_workloads || wl)) return CS_E_INVALID_ARGUMENT;
+  const int rc = upload_layout(ctx, n_inst, inst_offsets, w->codes != nullptr && w->dt_lo && w->blocks,
                                n_workloads, wl);
   if (rc != CS_OK) return rc;
-  if ((w->n_durations && (!w->dur_lo || !w->dur_hi)) || (w->n_payloads && !w->payloads) ||
-      (w->n_values && !w->values) || (w->n_escapes && !w->escapes) ||
-      w->n_dict > CS_WIRE_MAX_DICT || (w->n_dict && !w->dict))
+  if ((w->n_durations && (!w->dur_lo || !w->dur_hi)) || (w->n_pay8 && !w->pay8) ||
+      (w->n_pay16 && !w->pay16) || (w->n_values && !w->values) || (w->n_escapes && !w->escapes) ||
+      (w->n_dt_hi && !w->dt_hi) || w->n_dict > CS_WIRE_MAX_DICT || (w->n_dict && !w->dict))
     return CS_E_INVALID_ARGUMENT;
   const uint64_t n = ctx->n_ev;
   const size_t nt = ctx->tile_inst.size();
+  const uint64_t n_wl32 = wl32 ? w->n_workloads32 : 0;
   // one staging allocation, sections 16-B aligned
   auto al = [](size_t x) { return (x + 15) & ~size_t{15}; };
-  const size_t s_ev = al(n * 4), s_dict = al(w->n_dict * 4), s_blk = al(nt * sizeof(cs_wire_block)),
-               s_lo = al(w->n_durations * 2), s_hi = al(w->n_durations), s_pay = al(w->n_payloads * 2),
-               s_val = al(w->n_values * 8), s_esc = al(w->n_escapes * sizeof(cs_event));
-  auto* d = static_cast<unsigned char*>(ctx->d_wire.get(
-      std::max<size_t>(16, s_ev + s_dict + s_blk + s_lo + s_hi + s_pay + s_val + s_esc)));
+  const size_t s_code = al(n), s_dtl = al(n * 2), s_dth = al(w->n_dt_hi), s_dict = al(w->n_dict * 4),
+               s_blk = al(nt * sizeof(cs_wire_block)), s_lo = al(w->n_durations * 2), s_hi = al(w->n_durations),
+               s_p8 = al(w->n_pay8), s_p16 = al(w->n_pay16 * 2), s_val = al(w->n_values * 8),
+               s_esc = al(w->n_escapes * sizeof(cs_event)), s_wl = al(n_wl32 * 12);
+  auto* d = static_cast<unsigned char*>(ctx->d_wire.get(std::max<size_t>(
+      16, s_code + s_dtl + s_dth + s_dict + s_blk + s_lo + s_hi + s_p8 + s_p16 + s_val + s_esc + s_wl)));
   if (!d) return fail(ctx, CS_E_CUDA, "cudaMalloc(wire)");
   WireDev dv;
   size_t o = 0;
@@ -548,17 +552,27 @@ int cs_upload_wire(cs_ctx* ctx, uint32_t n_inst, const uint64_t* inst_offsets,
     o += span;
     return dst;
   };
-  dv.events = static_cast<const uint32_t*>(put(w->events, n * 4, s_ev));
+  dv.codes = static_cast<const uint8_t*>(put(w->codes, n, s_code));
+  dv.dt_lo = static_cast<const uint16_t*>(put(w->dt_lo, n * 2, s_dtl));
+  dv.dt_hi = static_cast<const uint8_t*>(put(w->dt_hi, w->n_dt_hi, s_dth));
   dv.dict = static_cast<const uint32_t*>(put(w->dict, w->n_dict * 4, s_dict));
   dv.n_dict = w->n_dict;
   dv.blocks = static_cast<const cs_wire_block*>(put(w->blocks, nt * sizeof(cs_wire_block), s_blk));
   dv.dur_lo = static_cast<const uint16_t*>(put(w->dur_lo, w->n_durations * 2, s_lo));
   dv.dur_hi = static_cast<const uint8_t*>(put(w->dur_hi, w->n_durations, s_hi));
-  dv.payloads = static_cast<const uint16_t*>(put(w->payloads, w->n_payloads * 2, s_pay));
+  dv.pay8 = static_cast<const uint8_t*>(put(w->pay8, w->n_pay8, s_p8));
+  dv.pay16 = static_cast<const uint16_t*>(put(w->pay16, w->n_pay16 * 2, s_p16));
   dv.values = static_cast<const double*>(put(w->values, w->n_values * 8, s_val));
   dv.escapes = static_cast<const cs_event*>(put(w->escapes, w->n_escapes * sizeof(cs_event), s_esc));
+  const uint32_t* dwl32 = static_cast<const uint32_t*>(put(w->workloads32, n_wl32 * 12, s_wl));
   CS_CUDA(cudaGetLastError());
   if (wait_copied(ctx) != CS_OK) return CS_E_CUDA;
+  if (wl32) {
+    void* dw = ctx->d_wl.get(std::max<uint64_t>(1, n_wl32) * sizeof(cs_workload));
+    if (!dw) return fail(ctx, CS_E_CUDA, "cudaMalloc(workloads)");
+    ctx->n_wl = n_wl32;
+    launch_wl32_expand(dwl32, n_wl32, static_cast<cs_workload*>(dw), ctx->stream);
+  }
   launch_wire_expand(dv, static_cast<const uint64_t*>(ctx->d_tile_begin.p),
                      static_cast<const uint64_t*>(ctx->d_tile_end.p), static_cast<uint32_t>(nt),
                      static_cast<cs_event*>(ctx->d_ev.p), ctx->stream);

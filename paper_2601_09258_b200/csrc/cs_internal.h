@@ -207,16 +207,20 @@ void launch_freq_cycles(const cs_event* ev, uint64_t begin, uint64_t end, int64_
 
 // device copies of a cs_wire_batch (cs_upload_wire)
 struct WireDev {
-  const uint32_t* events;
+  const uint8_t* codes;
+  const uint16_t* dt_lo;
+  const uint8_t* dt_hi;
   const uint32_t* dict;
   uint32_t n_dict;
   const cs_wire_block* blocks;
   const uint16_t* dur_lo;
   const uint8_t* dur_hi;
-  const uint16_t* payloads;
+  const uint8_t* pay8;
+  const uint16_t* pay16;
   const double* values;
   const cs_event* escapes;
 };
+void launch_wl32_expand(const uint32_t* wl32, uint64_t n, cs_workload* out, cudaStream_t s);
 void launch_wire_expand(const WireDev& w, const uint64_t* tile_begin, const uint64_t* tile_end,
                         uint32_t n_tiles, cs_event* out, cudaStream_t s);
 void launch_stream_keep(const DevBuffers& b, uint64_t* keep, cudaStream_t s);

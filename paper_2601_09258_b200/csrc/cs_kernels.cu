@@ -2662,9 +2662,9 @@ __global__ void __launch_bounds__(256, 3) k_cycle_reduce_v2(DevBuffers b, DevCon
 // Columnar wire records -> canonical 32-B cs_event in HBM, one CTA per
 // instance-aligned block (= tile), 4 consecutive events per thread: each
 // thread decodes its events' dictionary codes (dictionary in shared memory)
-// and counts their entries in the duration / payload / value / escape
-// columns; a block-wide exclusive scan (four 16-bit counts packed in a u64)
-// gives their column positions, and a segmented scan of the 24-bit start_ts
+// and counts their entries in the duration / payload / value / long-delta /
+// escape columns; two block-wide exclusive scans (16-bit counts packed in
+// u64s) give their column positions, and a segmented scan of the start_ts
 // deltas (restarted at escaped records, which are copied whole) gives the
 // timestamps.
 constexpr int kWireThreads = 256;
@@ -2672,44 +2672,60 @@ __global__ void __launch_bounds__(kWireThreads) k_wire_expand(WireDev w, const u
                                                               const uint64_t* __restrict__ tile_end,
                                                               cs_event* __restrict__ out) {
   __shared__ u64 s_w[32];
-  __shared__ uint32_t s_dict[256];
+  __shared__ uint32_t s_dict[128];
   __shared__ i64 s_x[kWireThreads];
-  __shared__ uint8_t s_f[kWireThreads];
   __shared__ i64 s_wx[32];
   __shared__ uint8_t s_wf[32];
   const uint32_t t = blockIdx.x;
-  for (uint32_t i = threadIdx.x; i < 256; i += kWireThreads) s_dict[i] = i < w.n_dict ? w.dict[i] : 0u;
+  if (threadIdx.x < 128) s_dict[threadIdx.x] = threadIdx.x < w.n_dict ? w.dict[threadIdx.x] : 0u;
   const u64 tb = tile_begin[t], te = tile_end[t];
   const cs_wire_block& B = w.blocks[t];
   const i64 b0 = B.base_ts;
   const uint32_t batch_base = B.batch_base;
   const u64 j0 = tb + 4u * threadIdx.x;
-  uint32_t word[4];
+  uint32_t code[4], dtl[4];
 #pragma unroll
-  for (int q = 0; q < 4; ++q) word[q] = j0 + q < te ? __ldg(w.events + j0 + q) : 0u;
+  for (int q = 0; q < 4; ++q) {
+    const bool in = j0 + q < te;
+    code[q] = in ? (uint32_t)__ldg(w.codes + j0 + q) : (uint32_t)CS_WIRE_ESCAPE;
+    dtl[q] = in ? (uint32_t)__ldg(w.dt_lo + j0 + q) : 0u;
+  }
   __syncthreads();  // s_dict
   uint32_t info[4];
-  u64 mine = 0;  // [durations, payloads, values, escapes] 16 bits each
+  u64 ca = 0, cb = 0;  // [dur, pay8, pay16, val] and [dt_hi, esc], 16 bits each
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     info[q] = 0;
     if (j0 + q >= te) continue;
-    const uint32_t code = word[q] >> 24;
-    if (code == CS_WIRE_ESCAPE) {
-      mine += 1ull << 48;
+    const uint32_t c = code[q] & 0x7fu;
+    if (c == CS_WIRE_ESCAPE) {
+      cb += 1ull << 16;
       continue;
     }
-    info[q] = s_dict[code];
+    info[q] = s_dict[c];
     const uint32_t kind = (info[q] >> 16) & 15u, flags = (info[q] >> 24) & 0x3fu;
-    mine += (kind == CS_SPAN ? 1ull : 0ull) +
-            ((flags & (CS_EV_HAS_BATCH | CS_EV_HAS_COMM)) ? (1ull << 16) : 0ull) +
-            ((kind == CS_COUNTER && (flags & CS_EV_HAS_VALUE)) ? (1ull << 32) : 0ull);
+    const bool pay = (flags & (CS_EV_HAS_BATCH | CS_EV_HAS_COMM)) != 0;
+    ca += (kind == CS_SPAN ? 1ull : 0ull) + (pay ? ((info[q] & CS_WIRE_WIDE) ? (1ull << 32) : (1ull << 16)) : 0ull) +
+          ((kind == CS_COUNTER && (flags & CS_EV_HAS_VALUE)) ? (1ull << 48) : 0ull);
+    cb += (code[q] & CS_WIRE_LONG_DT) ? 1ull : 0ull;
   }
-  const u64 excl = block_incl_scan(mine, s_w, nullptr) - mine;
-  u64 dpos = B.dur + (excl & 0xffffull);
-  u64 ppos = B.pay + ((excl >> 16) & 0xffffull);
-  u64 vpos = B.val + ((excl >> 32) & 0xffffull);
-  u64 epos = B.esc + (excl >> 48);
+  const u64 xa = block_incl_scan(ca, s_w, nullptr) - ca;
+  __syncthreads();  // s_w reuse
+  const u64 xb = block_incl_scan(cb, s_w, nullptr) - cb;
+  u64 dpos = B.dur + (xa & 0xffffull);
+  u64 p8 = B.pay8 + ((xa >> 16) & 0xffffull);
+  u64 p16 = B.pay16 + ((xa >> 32) & 0xffffull);
+  u64 vpos = B.val + (xa >> 48);
+  u64 hpos = B.dt_hi + (xb & 0xffffull);
+  u64 epos = B.esc + (xb >> 16);
+  // full deltas (low 16 bits + the high byte of long ones)
+  {
+    u64 h = hpos;
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (j0 + q < te && (code[q] & 0x7fu) != CS_WIRE_ESCAPE && (code[q] & CS_WIRE_LONG_DT))
+        dtl[q] |= (uint32_t)__ldg(w.dt_hi + h++) << 16;
+  }
   // start_ts: a segmented prefix sum of the deltas, restarted at each escaped
   // event's absolute start_ts (the aggregate (f, x) of a run: f = it holds an
   // escape, x = offset from b0 after it)
@@ -2720,11 +2736,11 @@ __global__ void __launch_bounds__(kWireThreads) k_wire_expand(WireDev w, const u
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       if (j0 + q >= te) break;
-      if ((word[q] >> 24) == CS_WIRE_ESCAPE) {
+      if ((code[q] & 0x7fu) == CS_WIRE_ESCAPE) {
         f = 1;
         x = w.escapes[e++].start_ts - b0;
       } else {
-        x += (i64)(word[q] & 0xffffffu);
+        x += (i64)dtl[q];
       }
     }
   }
@@ -2764,7 +2780,7 @@ __global__ void __launch_bounds__(kWireThreads) k_wire_expand(WireDev w, const u
   for (int q = 0; q < 4; ++q) {
     if (j0 + q >= te) break;
     u64 a, d, c, p;
-    if ((word[q] >> 24) == CS_WIRE_ESCAPE) {
+    if ((code[q] & 0x7fu) == CS_WIRE_ESCAPE) {
       const cs_event& e = w.escapes[epos++];
       run = e.start_ts - b0;
       a = (u64)e.start_ts;
@@ -2772,7 +2788,7 @@ __global__ void __launch_bounds__(kWireThreads) k_wire_expand(WireDev w, const u
       c = (u64)e.name_id | ((u64)e.kind << 32) | ((u64)e.category << 40) | ((u64)e.flags << 48);
       p = e.payload;
     } else {
-      run += (i64)(word[q] & 0xffffffu);
+      run += (i64)dtl[q];
       const uint32_t name = info[q] & 0xffffu, kind = (info[q] >> 16) & 15u;
       const uint32_t cat = (info[q] >> 20) & 15u, flags = (info[q] >> 24) & 0x3fu;
       a = (u64)(b0 + run);
@@ -2784,14 +2800,28 @@ __global__ void __launch_bounds__(kWireThreads) k_wire_expand(WireDev w, const u
         d = (u64)__double_as_longlong(w.values[vpos++]);
       }
       p = 0;
-      if (flags & CS_EV_HAS_COMM) p = (u64)w.payloads[ppos++] << 32;
-      else if (flags & CS_EV_HAS_BATCH) p = (u64)((uint32_t)w.payloads[ppos++] + batch_base);
+      if (flags & (CS_EV_HAS_COMM | CS_EV_HAS_BATCH)) {
+        const uint32_t v = (info[q] & CS_WIRE_WIDE) ? (uint32_t)w.pay16[p16++] : (uint32_t)w.pay8[p8++];
+        p = (flags & CS_EV_HAS_COMM) ? (u64)v << 32 : (u64)(v + batch_base);
+      }
       c = (u64)name | ((u64)kind << 32) | ((u64)cat << 40) | ((u64)flags << 48);
     }
     asm volatile("st.global.v4.u64 [%0], {%1, %2, %3, %4};" ::"l"(out + j0 + q), "l"(a), "l"(d),
                  "l"(c), "l"(p)
                  : "memory");
   }
+}
+
+// workload table from u32 triples (0xffffffff = absent -> INT64_MIN)
+__global__ void k_wl32_expand(const uint32_t* __restrict__ wl32, uint64_t n, cs_workload* __restrict__ out) {
+  const u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  auto dec = [](uint32_t v) -> int64_t { return v == 0xffffffffu ? INT64_MIN : (int64_t)v; };
+  out[i] = cs_workload{dec(wl32[3 * i]), dec(wl32[3 * i + 1]), dec(wl32[3 * i + 2])};
+}
+
+void launch_wl32_expand(const uint32_t* wl32, uint64_t n, cs_workload* out, cudaStream_t s) {
+  if (n) k_wl32_expand<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(wl32, n, out);
 }
 
 void launch_wire_expand(const WireDev& w, const uint64_t* tile_begin, const uint64_t* tile_end,

@@ -56,7 +56,7 @@ def lib():
     L.cs_set_name_table.argtypes = [vp, u32, vp]
     L.cs_upload.argtypes = [vp, u32, vp, vp, u64, vp]
     L.cs_upload_wire.argtypes = [vp, u32, vp, C.POINTER(abi.WireBatch), u64, vp]
-    L.cs_wire_pack.argtypes = [u32, vp, vp, u32, C.POINTER(vp)]
+    L.cs_wire_pack.argtypes = [u32, vp, vp, u64, vp, u32, C.POINTER(vp)]
     L.cs_wire_view.argtypes = [vp, C.POINTER(abi.WireBatch), C.POINTER(u64)]
     L.cs_wire_free.argtypes = [vp]
     L.cs_ingest_chrome_json.argtypes = [C.c_char_p, sz, vp, u32, C.POINTER(vp)]
@@ -528,37 +528,47 @@ def _ingest_extract(h) -> IngestedTrace:
 @dataclass
 class WireTrace:
     """A batch of instances in the columnar wire format (cs_wire_pack)."""
-    events: np.ndarray       # uint32 per event: dictionary code << 24 | start_ts delta
-    dict: np.ndarray         # uint32 info words (name | kind << 16 | category << 20 | flags << 24)
+    codes: np.ndarray        # uint8 per event: dictionary code | WIRE_LONG_DT (WIRE_ESCAPE: escaped)
+    dt_lo: np.ndarray        # uint16 per event: low 16 bits of the start_ts delta
+    dt_hi: np.ndarray        # uint8 per long-delta event: delta >> 16
+    dict: np.ndarray         # uint32 info words (name | kind << 16 | category << 20 | flags << 24 | WIDE)
     blocks: np.ndarray       # WIRE_BLOCK_DTYPE per instance-aligned block of WIRE_BLOCK records
     dur_lo: np.ndarray       # uint16, one per Span
     dur_hi: np.ndarray       # uint8, one per Span
-    payloads: np.ndarray     # uint16, one per batch/collective event
+    pay8: np.ndarray         # uint8 payloads (narrow codes)
+    pay16: np.ndarray        # uint16 payloads (WIDE codes)
     values: np.ndarray       # float64, one per valued Counter
     escapes: np.ndarray      # EVENT_DTYPE records that do not fit
+    workloads32: np.ndarray  # uint32 (n, 3) workload table, or None (the i64 table is sent)
     inst_offsets: np.ndarray
 
-    COLUMNS = ("events", "dict", "blocks", "dur_lo", "dur_hi", "payloads", "values", "escapes")
+    COLUMNS = ("codes", "dt_lo", "dt_hi", "dict", "blocks", "dur_lo", "dur_hi", "pay8", "pay16",
+               "values", "escapes", "workloads32")
 
     @property
     def nbytes(self) -> int:
-        return sum(getattr(self, c).nbytes for c in self.COLUMNS)
+        return sum(getattr(self, c).nbytes for c in self.COLUMNS if getattr(self, c) is not None)
 
     def batch(self) -> abi.WireBatch:
-        return abi.WireBatch(_ptr(self.events), _ptr(self.dict), len(self.dict), 0, _ptr(self.blocks),
-                             _ptr(self.dur_lo), _ptr(self.dur_hi), len(self.dur_lo),
-                             _ptr(self.payloads), len(self.payloads), _ptr(self.values),
-                             len(self.values), _ptr(self.escapes), len(self.escapes))
+        w32 = self.workloads32
+        return abi.WireBatch(_ptr(self.codes), _ptr(self.dt_lo), _ptr(self.dt_hi), len(self.dt_hi),
+                             _ptr(self.dict), len(self.dict), 0, _ptr(self.blocks), _ptr(self.dur_lo),
+                             _ptr(self.dur_hi), len(self.dur_lo), _ptr(self.pay8), len(self.pay8),
+                             _ptr(self.pay16), len(self.pay16), _ptr(self.values), len(self.values),
+                             _ptr(self.escapes), len(self.escapes),
+                             _ptr(w32) if w32 is not None else None, 0 if w32 is None else len(w32))
 
 
-def wire_pack(events: np.ndarray, inst_offsets, n_threads=None) -> WireTrace:
-    """cs_wire_pack: cs_event records -> wire format (the producer side)."""
+def wire_pack(events: np.ndarray, inst_offsets, workloads=None, n_threads=None) -> WireTrace:
+    """cs_wire_pack: cs_event records (+ workload table) -> wire format (the producer side)."""
     events = np.ascontiguousarray(events, dtype=abi.EVENT_DTYPE)
     off = np.ascontiguousarray(np.asarray(inst_offsets, dtype=np.uint64))
+    wl = np.ascontiguousarray(workloads if workloads is not None else np.zeros(0, abi.WORKLOAD_DTYPE),
+                              dtype=abi.WORKLOAD_DTYPE)
     L = lib()
     h = C.c_void_p()
-    _check(L.cs_wire_pack(len(off) - 1, off.ctypes.data, _ptr(events), n_threads or os.cpu_count() or 1,
-                          C.byref(h)))
+    _check(L.cs_wire_pack(len(off) - 1, off.ctypes.data, _ptr(events), len(wl), _ptr(wl),
+                          n_threads or os.cpu_count() or 1, C.byref(h)))
     try:
         v, nb = abi.WireBatch(), C.c_uint64()
         _check(L.cs_wire_view(h, C.byref(v), C.byref(nb)))
@@ -570,11 +580,13 @@ def wire_pack(events: np.ndarray, inst_offsets, n_threads=None) -> WireTrace:
             return np.frombuffer((C.c_char * nbytes).from_address(ptr), dtype=dtype).copy()
 
         n = int(off[-1])
-        return WireTrace(arr(v.events, n, np.uint32), arr(v.dict, v.n_dict, np.uint32),
-                         arr(v.blocks, nb.value, abi.WIRE_BLOCK_DTYPE),
+        w32 = arr(v.workloads32, 3 * v.n_workloads32, np.uint32).reshape(-1, 3) if v.workloads32 else None
+        return WireTrace(arr(v.codes, n, np.uint8), arr(v.dt_lo, n, np.uint16), arr(v.dt_hi, v.n_dt_hi, np.uint8),
+                         arr(v.dict, v.n_dict, np.uint32), arr(v.blocks, nb.value, abi.WIRE_BLOCK_DTYPE),
                          arr(v.dur_lo, v.n_durations, np.uint16), arr(v.dur_hi, v.n_durations, np.uint8),
-                         arr(v.payloads, v.n_payloads, np.uint16), arr(v.values, v.n_values, np.float64),
-                         arr(v.escapes, v.n_escapes, abi.EVENT_DTYPE), off)
+                         arr(v.pay8, v.n_pay8, np.uint8), arr(v.pay16, v.n_pay16, np.uint16),
+                         arr(v.values, v.n_values, np.float64), arr(v.escapes, v.n_escapes, abi.EVENT_DTYPE),
+                         w32, off)
     finally:
         L.cs_wire_free(h)
 
@@ -647,12 +659,18 @@ class Analyzer:
                                   _ptr(wl)))
         self.n_inst = len(off) - 1
 
-    def upload_wire(self, w: WireTrace, workloads: np.ndarray):
-        """cs_upload_wire: same batch as upload(), sent in the columnar wire format."""
-        wl = np.ascontiguousarray(workloads, dtype=abi.WORKLOAD_DTYPE)
+    def upload_wire(self, w: WireTrace, workloads: np.ndarray | None = None):
+        """cs_upload_wire: same batch as upload(), sent in the columnar wire
+        format (the workload table travels in it when packed with one)."""
         b = w.batch()
-        self._ck(self.L.cs_upload_wire(self.h, len(w.inst_offsets) - 1, w.inst_offsets.ctypes.data,
-                                       C.byref(b), len(wl), _ptr(wl)))
+        if w.workloads32 is not None:
+            self._ck(self.L.cs_upload_wire(self.h, len(w.inst_offsets) - 1, w.inst_offsets.ctypes.data,
+                                           C.byref(b), 0, None))
+        else:
+            wl = np.ascontiguousarray(workloads if workloads is not None else np.zeros(0, abi.WORKLOAD_DTYPE),
+                                      dtype=abi.WORKLOAD_DTYPE)
+            self._ck(self.L.cs_upload_wire(self.h, len(w.inst_offsets) - 1, w.inst_offsets.ctypes.data,
+                                           C.byref(b), len(wl), _ptr(wl) if len(wl) else None))
         self.n_inst = len(w.inst_offsets) - 1
 
     def sync(self):

@@ -25,23 +25,28 @@ def unpack(w):
         b += nb
     assert b == len(w.blocks) and len(w.dict) <= abi.WIRE_MAX_DICT
     bstart = np.asarray(bstart, np.int64)
-    code = (w.events >> 24).astype(np.int64)
+    code = (w.codes & 0x7F).astype(np.int64)
     esc = code == abi.WIRE_ESCAPE
     ok = ~esc
+    longdt = ok & ((w.codes & abi.WIRE_LONG_DT) != 0)
     info = np.zeros(n, np.int64)
     info[ok] = w.dict[code[ok]].astype(np.int64)
     kind = (info >> 16) & 15
     flags = (info >> 24) & 0x3F
+    wide = (info & abi.WIRE_WIDE) != 0
     span = ok & (kind == abi.SPAN)
     val = ok & (kind == abi.COUNTER) & ((flags & 0x20) != 0)
     pay = ok & ((flags & 0x14) != 0)
-    assert span.sum() == len(w.dur_lo) and pay.sum() == len(w.payloads) and val.sum() == len(w.values)
-    assert esc.sum() == len(w.escapes)
-    for col, mask in (("dur", span), ("pay", pay), ("val", val), ("esc", esc)):
+    assert span.sum() == len(w.dur_lo) and val.sum() == len(w.values)
+    assert (pay & ~wide).sum() == len(w.pay8) and (pay & wide).sum() == len(w.pay16)
+    assert esc.sum() == len(w.escapes) and longdt.sum() == len(w.dt_hi)
+    for col, mask in (("dur", span), ("pay8", pay & ~wide), ("pay16", pay & wide), ("val", val),
+                      ("dt_hi", longdt), ("esc", esc)):
         starts = np.concatenate([[0], np.cumsum(np.bincount(block[mask], minlength=b))])[:b]
         assert np.array_equal(w.blocks[col].astype(np.int64), starts), col
     # start_ts: per-block prefix sums of the deltas, restarted at escaped records
-    dt = (w.events & 0xFFFFFF).astype(np.int64)
+    dt = w.dt_lo.astype(np.int64)
+    dt[longdt] |= w.dt_hi.astype(np.int64) << 16
     dt[esc] = 0
     cs = np.cumsum(dt)
     cs -= (cs - dt)[bstart][block]                 # inclusive sum within the block
@@ -58,11 +63,22 @@ def unpack(w):
     out["kind"][ok] = kind[ok]
     out["category"][ok] = (info[ok] >> 20) & 15
     out["flags"][ok] = flags[ok]
-    p = w.payloads.astype(np.uint64)
-    comm = (flags[pay] & 0x10) != 0
+    p = np.zeros(n, np.uint64)
+    p[pay & ~wide] = w.pay8
+    p[pay & wide] = w.pay16
+    comm = pay & ((flags & 0x10) != 0)
+    batch = pay & ~comm
     p[comm] <<= np.uint64(32)
-    p[~comm] += w.blocks["batch_base"][block[pay][~comm]].astype(np.uint64)
-    out["payload"][pay] = p
+    p[batch] += w.blocks["batch_base"][block[batch]].astype(np.uint64)
+    out["payload"][pay] = p[pay]
+    return out
+
+
+def unpack_workloads(w):
+    x = w.workloads32.astype(np.int64)
+    x[w.workloads32 == 0xFFFFFFFF] = np.iinfo(np.int64).min
+    out = np.zeros(len(x), abi.WORKLOAD_DTYPE)
+    out["batch"], out["input_len"], out["output_len"] = x[:, 0], x[:, 1], x[:, 2]
     return out
 
 
@@ -86,10 +102,11 @@ def _edge_events(rt):
 def test_wire_roundtrip_simkit(rt):
     t = rt.synth_trace(3000, 1, 2, n_ranks=8, fault="nvlink_saturation", onset=2000,
                        duration=150, target_rank=3, compact_names=False)
-    w = rt.wire_pack(t.events, [0, len(t.events)])
-    assert w.events.nbytes == 4 * len(t.events)
+    w = rt.wire_pack(t.events, [0, len(t.events)], t.workloads)
+    assert w.codes.nbytes + w.dt_lo.nbytes == 3 * len(t.events)
+    assert unpack_workloads(w).tobytes() == t.workloads.tobytes()
     assert len(w.escapes) < 1e-3 * len(t.events)  # run_batch spans >= 16.8 ms under the fault
-    assert w.nbytes < 10 * len(t.events)
+    assert w.nbytes < 9 * len(t.events)
     assert np.array_equal(unpack(w).view(np.uint8), t.events.view(np.uint8))
 
 
@@ -135,16 +152,18 @@ def test_upload_wire_matches_upload(rt):
     ev["duration"][sp[100:140]] += np.int64(1 << 24)
     ev["start_ts"][sp[300]:int(off[2])] += np.int64(1 << 24)
     w = rt.wire_pack(ev, off)
+    w32 = rt.wire_pack(ev, off, wl)  # the workload table inside the wire batch
+    assert w32.workloads32 is not None
     assert len(w.escapes) >= 40
     names = traces[0].names
     out = []
-    for kind in ("upload", "wire"):
+    for kind in ("upload", "wire", "wire32"):
         an = rt.Analyzer(0)
         an.configure(names, rt.span_names_mask(ev, len(names)), n_comm_slots=4)
         if kind == "upload":
             an.upload(ev, off, wl)
         else:
-            an.upload_wire(w, wl)
+            an.upload_wire(w, wl) if kind == "wire" else an.upload_wire(w32)
         an.run(abi.RUN_SEGMENT)
         recs = an.records(0)
         tr = recs[recs["cycle_index"] < 1500]
@@ -154,7 +173,7 @@ def test_upload_wire_matches_upload(rt):
         an.run(abi.RUN_ALL)
         out.append([an.result(i) for i in range(2)])
         an.close()
-    for a, b in zip(*out):
+    for a, b in list(zip(out[0], out[1])) + list(zip(out[0], out[2])):
         assert a.cycles.tobytes() == b.cycles.tobytes()
         assert a.beta.tobytes() == b.beta.tobytes()
         assert a.records.tobytes() == b.records.tobytes()

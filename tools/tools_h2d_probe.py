@@ -32,8 +32,8 @@ for parts in (2, 9, 32):
 del d, h
 
 tr = rt.synth_trace(400_000, 1, 2, n_ranks=8, n_chunks=16, n_threads=os.cpu_count(), compact_names=False)
-wt = rt.wire_pack(tr.events, [0, len(tr.events)])
-cols = [getattr(wt, c) for c in rt.WireTrace.COLUMNS] + [tr.workloads]
+wt = rt.wire_pack(tr.events, [0, len(tr.events)], tr.workloads)
+cols = [getattr(wt, c) for c in rt.WireTrace.COLUMNS]
 nb = sum(a.nbytes for a in cols)
 ptr, pin = rt.host_alloc(nb + 16 * len(cols))
 views, o = [], 0
@@ -42,15 +42,15 @@ for a in cols:
     pin[o:o + a.nbytes] = a.view(np.uint8).reshape(-1)
     views.append(pin[o:o + a.nbytes].view(a.dtype).reshape(a.shape))
     o += a.nbytes
-wire = rt.WireTrace(*views[:-1], wt.inst_offsets)
+wire = rt.WireTrace(*views, wt.inst_offsets)
 an = rt.Analyzer(0)
 an.configure(tr.names, rt.span_names_mask(tr.events, len(tr.names)), n_comm_slots=tr.n_comm)
 for _ in range(3):
-    an.upload_wire(wire, views[-1])
+    an.upload_wire(wire)
     an.sync()
 t0 = time.perf_counter()
 for _ in range(5):
-    an.upload_wire(wire, views[-1])
+    an.upload_wire(wire)
     an.sync()
 el = (time.perf_counter() - t0) / 5
 print(f"wire upload+expand: {len(tr.events)} events, {nb / 1e6:.0f} MB, {el * 1e3:.2f} ms, {nb / el / 1e9:.1f} GB/s")

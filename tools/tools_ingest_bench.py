@@ -63,8 +63,8 @@ def main():
 
     def pipeline():
         g = rt.ingest_chrome_json(text, n_threads=nt)
-        w = rt.wire_pack(g.events, offs, n_threads=nt)
-        an.upload_wire(w, g.workloads)
+        w = rt.wire_pack(g.events, offs, g.workloads, n_threads=nt)
+        an.upload_wire(w)
         an.run(abi.RUN_ALL)
         return an.alerts(0)
 
