@@ -546,12 +546,19 @@ def run_stream(args, rank, world, local_rank):
     first = t0 + 20 * slice_ns  # skip the start-up
     cuts = [[int(np.searchsorted(e["start_ts"], first + k * slice_ns)) for k in range(n_slices + 1)]
             for e in evs]
-    batches = []
+    # each slice's events sit in pinned host memory, as a producer writing
+    # into a pinned ring would leave them (staged outside the timer)
+    batches, pins = [], []
     for k in range(n_slices):
         parts = [fleet[i][cuts[i % n_distinct][k]:cuts[i % n_distinct][k + 1]] for i in range(n_inst)]
         off = np.zeros(n_inst + 1, np.uint64)
         off[1:] = np.cumsum([len(p) for p in parts])
-        batches.append((np.ascontiguousarray(np.concatenate(parts)), off))
+        cat = np.concatenate(parts)
+        ptr, buf = rt.host_alloc(max(1, cat.nbytes))
+        pins.append(ptr)
+        ev_pin = buf[:cat.nbytes].view(abi.EVENT_DTYPE)
+        ev_pin[:] = cat
+        batches.append((ev_pin, off))
     st = an.stream()
     head = np.concatenate([f[:cuts[i % n_distinct][0]] for i, f in enumerate(fleet)])
     hoff = np.zeros(n_inst + 1, np.uint64)
@@ -571,6 +578,9 @@ def run_stream(args, rank, world, local_rank):
             n_alerts += len(al)
     phase_ms = {k: round(v, 4) for k, v in an.timings().items()}  # device phases of the last slice
     st.close()
+    del batches
+    for ptr in pins:
+        rt.host_free(ptr)
     total_s = sum(lat) / 1e3
     if dist:
         total_s = cdist.max_over_ranks(total_s, device=f"cuda:{dev}")

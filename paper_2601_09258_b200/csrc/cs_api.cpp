@@ -30,17 +30,25 @@ namespace {
 struct DevBuf {
   void* p = nullptr;
   size_t cap = 0;
+  // a first allocation is exact; a buffer that has to grow again (streaming
+  // batches of varying size) grows by half at least, so reallocations (and
+  // the device synchronisation cudaFree implies) die out
   void* get(size_t bytes) {
     if (bytes > cap) {
+      const size_t want = cap ? std::max(bytes, cap + cap / 2) : bytes;
       if (p) cudaFree(p);
       p = nullptr;
       cap = 0;
       if (bytes == 0) return nullptr;
-      if (cudaMalloc(&p, bytes) != cudaSuccess) {
-        p = nullptr;
-        return nullptr;
+      if (cudaMalloc(&p, want) != cudaSuccess) {
+        if (want == bytes || cudaMalloc(&p, bytes) != cudaSuccess) {
+          p = nullptr;
+          return nullptr;
+        }
+        cap = bytes;
+        return p;
       }
-      cap = bytes;
+      cap = want;
     }
     return p;
   }
@@ -90,13 +98,15 @@ struct cs_ctx {
   // counter-weighted mu: metric slots derived from the name table
   uint32_t n_metrics = 0;
   DevBuf d_series_slot, d_class_metric, d_m_off, d_s_ts, d_s_val, d_mu, d_mu_has;
-  // cs_stream_push: carried trailing partial cycle per instance + pinned staging
-  std::vector<std::vector<cs_event>> tails;
-  cs_event* stage_host = nullptr;
+  // cs_stream_push: the carried trailing partial cycle of every instance stays
+  // in the previous batch's event buffer (d_ev_prev); per instance its start
+  // and length there
+  std::vector<uint64_t> tail_start, tail_len;
+  bool tails_on_device = false;
+  DevBuf d_ev_prev, d_new_ev, d_assemble;
   void* pin_models = nullptr;  // pinned staging of the per-instance DevModel array
   size_t pin_models_cap = 0;
-  size_t stage_cap = 0;
-  std::vector<uint64_t> stage_off;
+  std::vector<uint64_t> stage_off, assemble_host;
   DevBuf d_keep;
   std::vector<uint32_t> sample_tiles;
   DevBuf d_sample_tiles, d_redo_tiles;
@@ -349,7 +359,6 @@ void cs_ctx_destroy(cs_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
-  if (ctx->stage_host) cudaFreeHost(ctx->stage_host);
   if (ctx->pin_models) cudaFreeHost(ctx->pin_models);
   delete ctx;
 }
@@ -510,6 +519,7 @@ int wait_copied(cs_ctx* ctx) {
 
 int cs_upload(cs_ctx* ctx, uint32_t n_inst, const uint64_t* inst_offsets, const cs_event* ev,
               uint64_t n_workloads, const cs_workload* wl) {
+  if (ctx) ctx->tails_on_device = false;
   const int rc = upload_layout(ctx, n_inst, inst_offsets, ev != nullptr, n_workloads, wl);
   if (rc != CS_OK) return rc;
   if (ctx->n_ev)
@@ -522,7 +532,8 @@ int cs_upload(cs_ctx* ctx, uint32_t n_inst, const uint64_t* inst_offsets, const 
 
 int cs_upload_wire(cs_ctx* ctx, uint32_t n_inst, const uint64_t* inst_offsets,
                    const cs_wire_batch* w, uint64_t n_workloads, const cs_workload* wl) {
-  if (!w) return CS_E_INVALID_ARGUMENT;
+  if (!w || !ctx) return CS_E_INVALID_ARGUMENT;
+  ctx->tails_on_device = false;
   const bool wl32 = w->workloads32 != nullptr;
   if (wl32 && (n_workloads || wl)) return CS_E_INVALID_ARGUMENT;
   const int rc = upload_layout(ctx, n_inst, inst_offsets, w->codes != nullptr && w->dt_lo && w->blocks,
@@ -1226,7 +1237,9 @@ int cs_run(cs_ctx* ctx, uint32_t mask) {
 int cs_stream_begin(cs_ctx* ctx) {
   if (!ctx) return CS_E_INVALID_ARGUMENT;
   ctx->streaming = true;
-  ctx->tails.clear();
+  ctx->tail_len.clear();
+  ctx->tail_start.clear();
+  ctx->tails_on_device = false;
   ctx->stream_fresh = true;
   return CS_OK;
 }
@@ -1257,35 +1270,47 @@ int cs_stream_push(cs_ctx* ctx, uint32_t n_inst, const uint64_t* offsets, const 
   if (!ctx || !offsets || n_inst == 0) return CS_E_INVALID_ARGUMENT;
   if (!ctx->streaming) return fail(ctx, CS_E_INVALID_ARGUMENT, "not streaming (cs_stream_begin)");
   if (offsets[0] != 0) return fail(ctx, CS_E_INVALID_ARGUMENT, "offsets[0] must be 0");
-  if (ctx->tails.size() != n_inst) {
-    if (!ctx->tails.empty() && !ctx->stream_fresh)
+  if (ctx->tail_len.size() != n_inst) {
+    if (!ctx->tail_len.empty() && !ctx->stream_fresh)
       return fail(ctx, CS_E_INVALID_ARGUMENT, "instance count changed mid-stream");
-    ctx->tails.assign(n_inst, {});
+    ctx->tail_len.assign(n_inst, 0);
+    ctx->tail_start.assign(n_inst, 0);
   }
-  // carried trailing partial cycle + the new events, per instance, staged pinned
+  uint64_t carried = 0;
+  for (uint32_t i = 0; i < n_inst; ++i) carried += ctx->tail_len[i];
+  if (carried && !ctx->tails_on_device)
+    return fail(ctx, CS_E_INVALID_ARGUMENT, "stream tails were replaced by cs_upload (use one streaming API)");
+  // new layout: per instance the carried tail, then the new events
   ctx->stage_off.assign(n_inst + 1, 0);
   for (uint32_t i = 0; i < n_inst; ++i) {
     if (offsets[i + 1] < offsets[i]) return fail(ctx, CS_E_INVALID_ARGUMENT, "offsets must be non-decreasing");
-    ctx->stage_off[i + 1] = ctx->stage_off[i] + ctx->tails[i].size() + (offsets[i + 1] - offsets[i]);
+    ctx->stage_off[i + 1] = ctx->stage_off[i] + ctx->tail_len[i] + (offsets[i + 1] - offsets[i]);
   }
-  const uint64_t total = ctx->stage_off[n_inst];
-  if (total > ctx->stage_cap) {
-    if (ctx->stage_host) cudaFreeHost(ctx->stage_host);
-    ctx->stage_host = nullptr;
-    ctx->stage_cap = 0;
-    const size_t want = std::max<size_t>(total + total / 2, 1 << 16);
-    if (cudaHostAlloc(reinterpret_cast<void**>(&ctx->stage_host), want * sizeof(cs_event),
-                      cudaHostAllocDefault) != cudaSuccess)
-      return fail(ctx, CS_E_CUDA, "cudaHostAlloc(stream staging)");
-    ctx->stage_cap = want;
-  }
-  for (uint32_t i = 0; i < n_inst; ++i) {
-    cs_event* dst = ctx->stage_host + ctx->stage_off[i];
-    std::copy(ctx->tails[i].begin(), ctx->tails[i].end(), dst);
-    std::copy(ev + offsets[i], ev + offsets[i + 1], dst + ctx->tails[i].size());
-  }
-  int rc = cs_upload(ctx, n_inst, ctx->stage_off.data(), ctx->stage_host, n_workloads, wl);
+  const uint64_t n_new = offsets[n_inst];
+  if (n_new && !ev) return CS_E_INVALID_ARGUMENT;
+  // the previous batch's events (holding the tails) move to d_ev_prev; the
+  // new batch is assembled on the device from them and the uploaded events
+  std::swap(ctx->d_ev.p, ctx->d_ev_prev.p);
+  std::swap(ctx->d_ev.cap, ctx->d_ev_prev.cap);
+  int rc = upload_layout(ctx, n_inst, ctx->stage_off.data(), true, n_workloads, wl);
   if (rc != CS_OK) return rc;
+  auto* d_new = dev<cs_event>(ctx->d_new_ev, std::max<uint64_t>(1, n_new));
+  auto* d_meta = dev<uint64_t>(ctx->d_assemble, 4ull * n_inst);
+  if (!d_new || !d_meta) return fail(ctx, CS_E_CUDA, "cudaMalloc(stream)");
+  if (n_new)
+    CS_CUDA(cudaMemcpyAsync(d_new, ev, n_new * sizeof(cs_event), cudaMemcpyHostToDevice, ctx->stream));
+  std::vector<uint64_t>& meta = ctx->assemble_host;
+  meta.resize(4ull * n_inst);
+  for (uint32_t i = 0; i < n_inst; ++i) {
+    meta[4 * i + 0] = ctx->stage_off[i];
+    meta[4 * i + 1] = ctx->tail_start[i];
+    meta[4 * i + 2] = ctx->tail_len[i];
+    meta[4 * i + 3] = offsets[i];
+  }
+  CS_CUDA(cudaMemcpyAsync(d_meta, meta.data(), meta.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
+  launch_stream_assemble(static_cast<const cs_event*>(ctx->d_ev_prev.p), d_new, d_meta, n_inst,
+                         ctx->stage_off[n_inst], static_cast<cs_event*>(ctx->d_ev.p), ctx->stream);
+  CS_CUDA(cudaGetLastError());
   rc = cs_run(ctx, mask);
   if (rc != CS_OK) return rc;
   // new tails: everything from the last closed cycle's end (cycles.cpp:147)
@@ -1323,11 +1348,12 @@ int cs_stream_push(cs_ctx* ctx, uint32_t n_inst, const uint64_t* offsets, const 
     }
   }
   for (uint32_t i = 0; i < n_inst; ++i) {
-    const cs_event* part = ctx->stage_host + ctx->stage_off[i];
     const uint64_t len = ctx->stage_off[i + 1] - ctx->stage_off[i];
     const uint64_t k = std::min(keep[i], len);
-    ctx->tails[i].assign(part + k, part + len);
+    ctx->tail_start[i] = ctx->stage_off[i] + k;
+    ctx->tail_len[i] = len - k;
   }
+  ctx->tails_on_device = true;
   if (n_alerts) *n_alerts = na;
   if (alerts && na > cap) return fail(ctx, CS_E_INVALID_ARGUMENT, "alert buffer too small");
   return CS_OK;

@@ -224,6 +224,11 @@ void launch_wl32_expand(const uint32_t* wl32, uint64_t n, cs_workload* out, cuda
 void launch_wire_expand(const WireDev& w, const uint64_t* tile_begin, const uint64_t* tile_end,
                         uint32_t n_tiles, cs_event* out, cudaStream_t s);
 void launch_stream_keep(const DevBuffers& b, uint64_t* keep, cudaStream_t s);
+// streaming batch assembly: per instance i (meta[4i..4i+3] = dst offset, tail
+// start in prev, tail length, new-event offset) out[dst..] = prev tail, then
+// the instance's new events
+void launch_stream_assemble(const cs_event* prev, const cs_event* fresh, const uint64_t* meta,
+                            uint32_t n_inst, uint64_t total, cs_event* out, cudaStream_t s);
 void launch_counter_series(const DevBuffers& b, cudaStream_t s, uint64_t* launches);
 void launch_counter_scatter(const DevBuffers& b, cudaStream_t s, uint64_t* launches);
 void launch_cycle_mu(const DevBuffers& b, const DevConfig& cfg, cudaStream_t s, uint64_t* launches);

@@ -2841,6 +2841,27 @@ __global__ void k_stream_keep(DevBuffers b, uint64_t* keep) {
   keep[i] = c1 > c0 ? b.c_last[c1 - 1] - b.inst_off[i] : 0;
 }
 
+// one CTA per instance: its carried tail (from the previous batch's buffer)
+// followed by its new events, 16 bytes per lane-step
+__global__ void __launch_bounds__(128) k_stream_assemble(const cs_event* __restrict__ prev,
+                                                         const cs_event* __restrict__ fresh,
+                                                         const uint64_t* __restrict__ meta, uint64_t total,
+                                                         uint32_t n_inst, cs_event* __restrict__ out) {
+  const uint32_t i = blockIdx.x;
+  const u64 dst = meta[4 * i], ts = meta[4 * i + 1], tl = meta[4 * i + 2], ns = meta[4 * i + 3];
+  const u64 end = i + 1 < n_inst ? meta[4 * (i + 1)] : total;
+  const uint4* p4 = reinterpret_cast<const uint4*>(prev + ts);
+  const uint4* f4 = reinterpret_cast<const uint4*>(fresh + ns);
+  uint4* o4 = reinterpret_cast<uint4*>(out + dst);
+  const u64 n2 = 2 * (end - dst), t2 = 2 * tl;  // 16-B halves of 32-B records
+  for (u64 k = threadIdx.x; k < n2; k += blockDim.x) o4[k] = k < t2 ? p4[k] : f4[k - t2];
+}
+
+void launch_stream_assemble(const cs_event* prev, const cs_event* fresh, const uint64_t* meta,
+                            uint32_t n_inst, uint64_t total, cs_event* out, cudaStream_t s) {
+  if (n_inst) k_stream_assemble<<<n_inst, 128, 0, s>>>(prev, fresh, meta, total, n_inst, out);
+}
+
 void launch_stream_keep(const DevBuffers& b, uint64_t* keep, cudaStream_t s) {
   if (b.n_inst) k_stream_keep<<<(b.n_inst + 127) / 128, 128, 0, s>>>(b, keep);
 }
