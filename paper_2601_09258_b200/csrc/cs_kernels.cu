@@ -2926,44 +2926,85 @@ __global__ void __launch_bounds__(256) k_counter_scatter(DevBuffers b) {
   }
 }
 
+// First index h in [0, n] with (double)ts[h] >= t (strict: > t), found by
+// galloping from `hint` and finishing with a binary search.  The answer is
+// unique (ts is sorted), so the hint only changes how many loads it takes.
+__device__ __forceinline__ u64 search_from(const int64_t* __restrict__ ts, u64 n, double t, bool strict,
+                                           u64 hint) {
+  auto at_or_after = [&](u64 i) {
+    const double x = (double)ts[i];
+    return strict ? x > t : x >= t;
+  };
+  u64 lo, hi;  // the answer is in [lo, hi]; hi == n or at_or_after(hi)
+  if (hint >= n || at_or_after(hint)) {
+    hi = hint < n ? hint : n;
+    u64 step = 1;
+    while (true) {
+      if (hi < step) {
+        lo = 0;
+        break;
+      }
+      const u64 c = hi - step;
+      if (at_or_after(c)) {
+        hi = c;
+        step <<= 1;
+      } else {
+        lo = c + 1;
+        break;
+      }
+    }
+  } else {
+    lo = hint + 1;
+    u64 step = 1;
+    while (true) {
+      const u64 c = lo + step - 1;
+      if (c >= n) {
+        hi = n;
+        break;
+      }
+      if (at_or_after(c)) {
+        hi = c;
+        break;
+      }
+      lo = c + 1;
+      step <<= 1;
+    }
+  }
+  while (lo < hi) {
+    const u64 mid = (lo + hi) >> 1;
+    if (at_or_after(mid)) hi = mid;
+    else lo = mid + 1;
+  }
+  return lo;
+}
+
 // interpolate_mean (rca.cpp:17-53), operation for operation: knots t0, the
 // sample timestamps strictly inside (t0, t1), t1; trapezoids summed in knot
-// order; value_at by lower_bound over the samples' double timestamps.
+// order; value_at by lower_bound over the samples' double timestamps.  Every
+// search starts from `*hint` (the previous span's first interior knot of this
+// metric), which moves to this span's.
 __device__ double interpolate_mean_dev(const int64_t* __restrict__ ts, const double* __restrict__ val,
-                                       u64 n, i64 t0i, i64 t1i) {
+                                       u64 n, i64 t0i, i64 t1i, u64* hint) {
   const double t0 = (double)t0i, t1 = (double)t1i;
-  auto lower = [&](double t) -> u64 {  // first sample with (double)ts >= t
-    u64 lo = 0, hi = n;
-    while (lo < hi) {
-      const u64 mid = (lo + hi) >> 1;
-      if ((double)ts[mid] < t) lo = mid + 1;
-      else hi = mid;
-    }
-    return lo;
-  };
-  auto value_at = [&](double t) -> double {
+  auto value_at = [&](double t, u64 near) -> double {
     if (t <= (double)ts[0]) return val[0];
     if (t >= (double)ts[n - 1]) return val[n - 1];
-    const u64 h = lower(t);
+    const u64 h = search_from(ts, n, t, false, near);
     const double f = __ddiv_rn(__dsub_rn(t, (double)ts[h - 1]), (double)(ts[h] - ts[h - 1]));
     return __dadd_rn(val[h - 1], __dmul_rn(f, __dsub_rn(val[h], val[h - 1])));
   };
   // interior knots: samples with t0 < (double)ts < t1, a contiguous range
-  u64 k0 = 0, hi = n;
-  while (k0 < hi) {  // first with (double)ts > t0
-    const u64 mid = (k0 + hi) >> 1;
-    if ((double)ts[mid] <= t0) k0 = mid + 1;
-    else hi = mid;
-  }
-  const u64 k1 = lower(t1);
-  double integral = 0.0, a = t0, va = value_at(t0);
+  const u64 k0 = search_from(ts, n, t0, true, *hint);
+  const u64 k1 = search_from(ts, n, t1, false, k0);
+  *hint = k0;
+  double integral = 0.0, a = t0, va = value_at(t0, k0);
   for (u64 i = k0; i < k1; ++i) {
-    const double kt = (double)ts[i], vb = value_at(kt);
+    const double kt = (double)ts[i], vb = value_at(kt, i);
     integral = __dadd_rn(integral, __dmul_rn(__dmul_rn(0.5, __dadd_rn(va, vb)), __dsub_rn(kt, a)));
     a = kt;
     va = vb;
   }
-  const double vb = value_at(t1);
+  const double vb = value_at(t1, k1);
   integral = __dadd_rn(integral, __dmul_rn(__dmul_rn(0.5, __dadd_rn(va, vb)), __dsub_rn(t1, a)));
   return __ddiv_rn(integral, __dsub_rn(t1, t0));
 }
@@ -2986,6 +3027,8 @@ __global__ void __launch_bounds__(256) k_cycle_mu(DevBuffers b, DevConfig cfg) {
   const uint32_t lt = inst + 1 < b.n_inst ? b.inst_first_tile[inst + 1] : b.n_tiles;
   for (int c = 0; c < C; ++c) acc[c * NT + tid] = 0.0;
   u64 has = 0;
+  u64 hint[kMaxMetrics];  // per metric: where the previous span's knots started
+  for (int m = 0; m < kMaxMetrics; ++m) hint[m] = ~0ull;
   if (dur > 0) {  // cycle_stats returns empty stats otherwise (rca.cpp:77)
     for (u64 j = first; j < last; ++j) {
       const Ev8 e = ldg256(b.ev + j);
@@ -3001,7 +3044,9 @@ __global__ void __launch_bounds__(256) k_cycle_mu(DevBuffers b, DevConfig cfg) {
       if (m < 0 || bs < 0 || bs >= C) continue;
       const u64 lo = b.m_off[(u64)m * b.n_tiles + ft], hi = b.m_off[(u64)m * b.n_tiles + lt];
       if (hi <= lo) continue;  // counters.find(metric) == nullptr: beta-only entry
-      const double mu = interpolate_mean_dev(b.s_ts + lo, b.s_val + lo, hi - lo, st, st + clipped);
+      u64& h = hint[m];
+      if (h == ~0ull) h = (hi - lo) >> 1;
+      const double mu = interpolate_mean_dev(b.s_ts + lo, b.s_val + lo, hi - lo, st, st + clipped, &h);
       acc[bs * NT + tid] = __dadd_rn(acc[bs * NT + tid], __dmul_rn(mu, (double)clipped));
       has |= 1ull << bs;
     }
