@@ -2569,11 +2569,17 @@ __global__ void __launch_bounds__(256, 3) k_cycle_reduce_v2(DevBuffers b, DevCon
   for (uint32_t i = tid; i < b.n_names && i < (uint32_t)kFNamesSmem; i += NT)
     s_ninfo[i] = pack_info(b.names[i]);
   __syncthreads();
-  i64* comp = reinterpret_cast<i64*>(s_red);            // [P][NT]
-  i64* beta = comp + (u64)P * NT;                       // [C][NT]
-  double* coll = reinterpret_cast<double*>(beta + (u64)C * NT);  // [R][NT]
-  uint32_t* colln = reinterpret_cast<uint32_t*>(coll + (u64)R * NT);  // [R][NT]
-  const u64 g = (u64)blockIdx.x * NT + tid;
+  // [slot][thread] accumulators, row stride SN = NT + 1: the per-event
+  // updates (a thread's own column) and the transposed write-out below are
+  // both (nearly) bank-conflict free
+  const uint32_t SN = NT + 1;
+  i64* comp = reinterpret_cast<i64*>(s_red);            // [P][SN]
+  i64* beta = comp + (u64)P * SN;                       // [C][SN]
+  double* coll = reinterpret_cast<double*>(beta + (u64)C * SN);  // [R][SN]
+  i64* s_dur = reinterpret_cast<i64*>(coll + (u64)R * SN);       // [NT]
+  uint32_t* colln = reinterpret_cast<uint32_t*>(s_dur + NT);     // [R][SN]
+  const u64 g0 = (u64)blockIdx.x * NT;
+  const u64 g = g0 + tid;
   const bool live = g < b.n_cycles;
   uint8_t stage = CS_STAGE_UNKNOWN;
   if (live) {
@@ -2581,11 +2587,12 @@ __global__ void __launch_bounds__(256, 3) k_cycle_reduce_v2(DevBuffers b, DevCon
     const u64 first = b.c_first[g], last = b.c_last[g];
     const bool no_comp = b.c_apos[g] == kNone;  // frequency-fallback cycle (cycles.cpp:332-340)
     const i64 dur = ce - cs;
-    for (int p = 0; p < P; ++p) comp[p * NT + tid] = 0;
-    for (int c = 0; c < C; ++c) beta[c * NT + tid] = 0;
+    s_dur[tid] = dur;
+    for (int p = 0; p < P; ++p) comp[p * SN + tid] = 0;
+    for (int c = 0; c < C; ++c) beta[c * SN + tid] = 0;
     for (int r = 0; r < R; ++r) {
-      coll[r * NT + tid] = 0.0;
-      colln[r * NT + tid] = 0u;
+      coll[r * SN + tid] = 0.0;
+      colln[r * SN + tid] = 0u;
     }
     uint32_t fm_cls = 0, kw = 0;
     bool fm_found = false, batch_found = false;
@@ -2618,15 +2625,15 @@ __global__ void __launch_bounds__(256, 3) k_cycle_reduce_v2(DevBuffers b, DevCon
         const i64 clipped = (end < ce ? end : ce) - st;
         if (clipped <= 0) continue;
         const uint32_t ph = info & 15u, bs = (info >> 4) & 255u;
-        if (ph != 15u && !no_comp) comp[ph * NT + tid] += clipped;
+        if (ph != 15u && !no_comp) comp[ph * SN + tid] += clipped;
         if (do_beta && d > 0) {
-          if (bs != 255u) beta[bs * NT + tid] += clipped;
+          if (bs != 255u) beta[bs * SN + tid] += clipped;
           if (((kc >> 8) & 0xffu) == CS_CAT_COLLECTIVE_COMM && (flags & CS_EV_HAS_COMM)) {
             const uint32_t slot = (uint32_t)(e[q].d >> 32);
             if (slot < (uint32_t)R) {
-              coll[slot * NT + tid] =
-                  __dadd_rn(coll[slot * NT + tid], __ddiv_rn((double)clipped, (double)dur));
-              colln[slot * NT + tid] += 1u;
+              coll[slot * SN + tid] =
+                  __dadd_rn(coll[slot * SN + tid], __ddiv_rn((double)clipped, (double)dur));
+              colln[slot * SN + tid] += 1u;
             }
           }
         }
@@ -2640,16 +2647,30 @@ __global__ void __launch_bounds__(256, 3) k_cycle_reduce_v2(DevBuffers b, DevCon
     b.c_local[g] = stage;
     b.c_stage[g] = stage;
     b.c_wl[g] = wl;
-    for (int p = 0; p < P; ++p) b.c_comp[g * P + p] = comp[p * NT + tid];
-    for (int c = 0; c < C; ++c) {
-      const i64 t = dur > 0 ? beta[c * NT + tid] : 0;
-      b.c_beta_tot[g * C + c] = t;
-      b.c_beta[g * C + c] = t > 0 ? __ddiv_rn((double)t, (double)dur) : 0.0;
+  }
+  // the CTA's rows [g0, g0 + n_live) of every per-(cycle, slot) output are
+  // contiguous: written cooperatively, consecutive threads on consecutive
+  // addresses (a thread-per-row store would touch 32 partial sectors per
+  // warp instruction)
+  __syncthreads();
+  {
+    const uint32_t n_live = (uint32_t)(b.n_cycles - g0 < (u64)NT ? b.n_cycles - g0 : (u64)NT);
+    for (uint32_t idx = tid; idx < n_live * (uint32_t)P; idx += NT) {
+      const uint32_t lc = idx / (uint32_t)P, p = idx - lc * (uint32_t)P;
+      b.c_comp[g0 * P + idx] = comp[p * SN + lc];
     }
-    for (int r = 0; r < R; ++r) {
-      b.c_coll[g * R + r] = coll[r * NT + tid];
-      const uint32_t n = colln[r * NT + tid];
-      b.c_coll_n[g * R + r] = (uint8_t)(n > 255u ? 255u : n);
+    for (uint32_t idx = tid; idx < n_live * (uint32_t)C; idx += NT) {
+      const uint32_t lc = idx / (uint32_t)C, c = idx - lc * (uint32_t)C;
+      const i64 dur = s_dur[lc];
+      const i64 t = dur > 0 ? beta[c * SN + lc] : 0;
+      b.c_beta_tot[g0 * C + idx] = t;
+      b.c_beta[g0 * C + idx] = t > 0 ? __ddiv_rn((double)t, (double)dur) : 0.0;
+    }
+    for (uint32_t idx = tid; idx < n_live * (uint32_t)R; idx += NT) {
+      const uint32_t lc = idx / (uint32_t)R, r = idx - lc * (uint32_t)R;
+      b.c_coll[g0 * R + idx] = coll[r * SN + lc];
+      const uint32_t n = colln[r * SN + lc];
+      b.c_coll_n[g0 * R + idx] = (uint8_t)(n > 255u ? 255u : n);
     }
   }
   const bool unk = live && stage == CS_STAGE_UNKNOWN;
@@ -3108,8 +3129,8 @@ void launch_cycle_reduce_tpc(const DevBuffers& b, const DevConfig& cfg, int do_b
   const int R = do_beta ? cfg.cyc.n_comm_slots : 0;
   const int per_thread = (P + C + R) * 8 + R * 4;
   int nt = 256;
-  while (nt > 32 && nt * per_thread > 100 * 1024) nt >>= 1;
-  const int smem = nt * per_thread;
+  while (nt > 32 && (nt + 1) * per_thread + nt * 8 > 100 * 1024) nt >>= 1;
+  const int smem = (nt + 1) * per_thread + nt * 8;  // padded [slot][thread] rows + durations
   (void)variant;
   cudaFuncSetAttribute(k_cycle_reduce_v2, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   const unsigned grid = (unsigned)((b.n_cycles + nt - 1) / nt);
