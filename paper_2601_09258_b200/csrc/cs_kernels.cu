@@ -3036,47 +3036,56 @@ __device__ double interpolate_mean_dev(const int64_t* __restrict__ ts, const dou
 __global__ void __launch_bounds__(256) k_cycle_mu(DevBuffers b, DevConfig cfg) {
   extern __shared__ __align__(16) unsigned char s_mu[];
   const int C = cfg.cyc.n_beta_slots;
-  const uint32_t NT = blockDim.x, tid = threadIdx.x;
-  double* acc = reinterpret_cast<double*>(s_mu);  // [C][NT]
-  const u64 g = (u64)blockIdx.x * NT + tid;
-  if (g >= b.n_cycles) return;
-  const i64 cs = b.c_start[g], ce = b.c_end[g];
-  const i64 dur = ce - cs;
-  const u64 first = b.c_first[g], last = b.c_last[g];
-  const uint32_t inst = b.c_inst[g];
-  const uint32_t ft = b.inst_first_tile[inst];
-  const uint32_t lt = inst + 1 < b.n_inst ? b.inst_first_tile[inst + 1] : b.n_tiles;
-  for (int c = 0; c < C; ++c) acc[c * NT + tid] = 0.0;
+  const uint32_t NT = blockDim.x, tid = threadIdx.x, SN = NT + 1;
+  double* acc = reinterpret_cast<double*>(s_mu);  // [C][SN]
+  u64* s_has = reinterpret_cast<u64*>(acc + (u64)C * SN);  // [NT]
+  const u64 g0 = (u64)blockIdx.x * NT;
+  const u64 g = g0 + tid;
+  const bool live = g < b.n_cycles;
+  for (int c = 0; c < C; ++c) acc[c * SN + tid] = 0.0;
   u64 has = 0;
-  u64 hint[kMaxMetrics];  // per metric: where the previous span's knots started
-  for (int m = 0; m < kMaxMetrics; ++m) hint[m] = ~0ull;
-  if (dur > 0) {  // cycle_stats returns empty stats otherwise (rca.cpp:77)
-    for (u64 j = first; j < last; ++j) {
-      const Ev8 e = ldg256(b.ev + j);
-      const uint32_t kc = (uint32_t)(e.c >> 32);
-      const i64 st = (i64)e.a, d = (i64)e.b;
-      if ((kc & 0xffu) != CS_SPAN || d <= 0) continue;
-      const i64 end = st + d;
-      const i64 clipped = (end < ce ? end : ce) - st;
-      if (clipped <= 0) continue;
-      const uint32_t name = (uint32_t)e.c;
-      const int m = b.class_metric[name];
-      const int bs = b.names[name].beta_slot;
-      if (m < 0 || bs < 0 || bs >= C) continue;
-      const u64 lo = b.m_off[(u64)m * b.n_tiles + ft], hi = b.m_off[(u64)m * b.n_tiles + lt];
-      if (hi <= lo) continue;  // counters.find(metric) == nullptr: beta-only entry
-      u64& h = hint[m];
-      if (h == ~0ull) h = (hi - lo) >> 1;
-      const double mu = interpolate_mean_dev(b.s_ts + lo, b.s_val + lo, hi - lo, st, st + clipped, &h);
-      acc[bs * NT + tid] = __dadd_rn(acc[bs * NT + tid], __dmul_rn(mu, (double)clipped));
-      has |= 1ull << bs;
+  if (live) {
+    const i64 cs = b.c_start[g], ce = b.c_end[g];
+    const i64 dur = ce - cs;
+    const u64 first = b.c_first[g], last = b.c_last[g];
+    const uint32_t inst = b.c_inst[g];
+    const uint32_t ft = b.inst_first_tile[inst];
+    const uint32_t lt = inst + 1 < b.n_inst ? b.inst_first_tile[inst + 1] : b.n_tiles;
+    u64 hint[kMaxMetrics];  // per metric: where the previous span's knots started
+    for (int m = 0; m < kMaxMetrics; ++m) hint[m] = ~0ull;
+    if (dur > 0) {  // cycle_stats returns empty stats otherwise (rca.cpp:77)
+      for (u64 j = first; j < last; ++j) {
+        const Ev8 e = ldg256(b.ev + j);
+        const uint32_t kc = (uint32_t)(e.c >> 32);
+        const i64 st = (i64)e.a, d = (i64)e.b;
+        if ((kc & 0xffu) != CS_SPAN || d <= 0) continue;
+        const i64 end = st + d;
+        const i64 clipped = (end < ce ? end : ce) - st;
+        if (clipped <= 0) continue;
+        const uint32_t name = (uint32_t)e.c;
+        const int m = b.class_metric[name];
+        const int bs = b.names[name].beta_slot;
+        if (m < 0 || bs < 0 || bs >= C) continue;
+        const u64 lo = b.m_off[(u64)m * b.n_tiles + ft], hi = b.m_off[(u64)m * b.n_tiles + lt];
+        if (hi <= lo) continue;  // counters.find(metric) == nullptr: beta-only entry
+        u64& h = hint[m];
+        if (h == ~0ull) h = (hi - lo) >> 1;
+        const double mu = interpolate_mean_dev(b.s_ts + lo, b.s_val + lo, hi - lo, st, st + clipped, &h);
+        acc[bs * SN + tid] = __dadd_rn(acc[bs * SN + tid], __dmul_rn(mu, (double)clipped));
+        has |= 1ull << bs;
+      }
     }
-  }
-  for (int c = 0; c < C; ++c) {
-    const i64 tot = b.c_beta_tot[g * C + c];
-    const bool h = ((has >> c) & 1ull) && tot > 0;
-    b.c_mu[g * C + c] = h ? __ddiv_rn(acc[c * NT + tid], (double)tot) : 0.0;
-    b.c_mu_has[g * C + c] = h ? 1 : 0;
+  }  // live
+  s_has[tid] = has;
+  __syncthreads();
+  // the CTA's rows written cooperatively (consecutive threads, consecutive addresses)
+  const uint32_t n_live = (uint32_t)(b.n_cycles - g0 < (u64)NT ? b.n_cycles - g0 : (u64)NT);
+  for (uint32_t idx = tid; idx < n_live * (uint32_t)C; idx += NT) {
+    const uint32_t lc = idx / (uint32_t)C, c = idx - lc * (uint32_t)C;
+    const i64 tot = b.c_beta_tot[g0 * C + idx];
+    const bool h = ((s_has[lc] >> c) & 1ull) && tot > 0;
+    b.c_mu[g0 * C + idx] = h ? __ddiv_rn(acc[c * SN + lc], (double)tot) : 0.0;
+    b.c_mu_has[g0 * C + idx] = h ? 1 : 0;
   }
 }
 
@@ -3097,7 +3106,7 @@ void launch_cycle_mu(const DevBuffers& b, const DevConfig& cfg, cudaStream_t s, 
   int nt = 256;
   const int C = cfg.cyc.n_beta_slots > 0 ? cfg.cyc.n_beta_slots : 1;
   while (nt > 32 && nt * C * 8 > 96 * 1024) nt >>= 1;
-  const int smem = nt * C * 8;
+  const int smem = (nt + 1) * C * 8 + nt * 8;  // padded [class][thread] rows + has masks
   cudaFuncSetAttribute(k_cycle_mu, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   k_cycle_mu<<<(unsigned)((b.n_cycles + nt - 1) / nt), nt, smem, s>>>(b, cfg);
   ++*launches;
