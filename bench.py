@@ -419,11 +419,15 @@ def run_ours(args, rank, world, local_rank):
     traffic = None
     kname = {"cycle_reduce": "k_cycle_reduce_v2", "scan_events": "k_scan_warp",
              "fused_segment": "k_segment_pass"}[dom[0]]
+    step_dram = None  # ncu DRAM bytes of the step's captured kernels (the full capture)
     try:
         with open(os.path.join(ROOT, "profiles", "r1_ncu_traffic.json")) as f:
-            tr = json.load(f).get(kname)
+            allk = json.load(f)
+        tr = allk.get(kname)
         if tr and args.workload == "c2":
             traffic = tr["dram_read_bytes"] + tr["dram_write_bytes"]
+            step_dram = sum(v["dram_read_bytes"] + v["dram_write_bytes"] for k, v in allk.items()
+                            if not k.endswith("_2"))  # one launch per kernel of one step
     except (OSError, ValueError):
         pass
     path_bytes = 44.5 * n_events  # SURVEY §8d per-event figure
@@ -450,7 +454,10 @@ def run_ours(args, rank, world, local_rank):
                      "traffic": traffic, "algorithmic_bytes": dom[1],
                      "traffic_source": "profiles/r1_ncu_traffic.json (ncu --set full, dram read+write)",
                      "kernel_ms": dom[2], "event_pass_ms": scan_t, "cycle_reduce_ms": red_t,
-                     "path_frac_44p5B_per_event": path_bytes / (dev_ms * 1e-3) / 1e9 / peak},
+                     "path_frac_44p5B_per_event": path_bytes / (dev_ms * 1e-3) / 1e9 / peak,
+                     "step_dram_frac_ncu": (step_dram / (dev_ms * 1e-3) / 1e9 / peak) if step_dram else None,
+                     "step_dram_note": "ncu DRAM read+write of one launch of each captured kernel "
+                                       "(scan, bounds, reduce, score, detect) over the measured step time"},
         "e2e": {"value": world * n_events / (e2e * 1e-3), "unit": UNIT,
                 "h2d_bytes_per_step": wire_bytes, "d2h_bytes_per_step": d2h,
                 "ms_per_step": e2e, "input": f"columnar wire format (cs_upload_wire, {wire_bytes_per_event:.1f} B/event incl. workloads) from pinned memory",
