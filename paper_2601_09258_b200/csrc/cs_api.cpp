@@ -20,10 +20,19 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "cs_internal.h"
 #include "cyclescope_b200.h"
 
 using namespace csb;
+
+// an NVTX range for the rest of the enclosing scope
+struct NvtxScope {
+  explicit NvtxScope(const char* name) { nvtxRangePushA(name); }
+  ~NvtxScope() { nvtxRangePop(); }
+};
+#define CS_NVTX_SCOPE(name) NvtxScope nvtx_scope_(name)
 
 namespace {
 
@@ -150,6 +159,7 @@ struct cs_ctx {
   // timing
   cudaEvent_t ev[16]{};
   cudaEvent_t ev_copied = nullptr;  // end of the last upload's host->device copies
+  bool nvtx_phase_open = false;
   std::vector<std::pair<std::string, std::pair<int, int>>> timed;
   uint64_t launches = 0;
   DevBuf d_scratch;
@@ -519,6 +529,7 @@ int wait_copied(cs_ctx* ctx) {
 
 int cs_upload(cs_ctx* ctx, uint32_t n_inst, const uint64_t* inst_offsets, const cs_event* ev,
               uint64_t n_workloads, const cs_workload* wl) {
+  CS_NVTX_SCOPE("cs_upload");
   if (ctx) ctx->tails_on_device = false;
   const int rc = upload_layout(ctx, n_inst, inst_offsets, ev != nullptr, n_workloads, wl);
   if (rc != CS_OK) return rc;
@@ -533,6 +544,7 @@ int cs_upload(cs_ctx* ctx, uint32_t n_inst, const uint64_t* inst_offsets, const 
 int cs_upload_wire(cs_ctx* ctx, uint32_t n_inst, const uint64_t* inst_offsets,
                    const cs_wire_batch* w, uint64_t n_workloads, const cs_workload* wl) {
   if (!w || !ctx) return CS_E_INVALID_ARGUMENT;
+  CS_NVTX_SCOPE("cs_upload_wire");
   ctx->tails_on_device = false;
   const bool wl32 = w->workloads32 != nullptr;
   if (wl32 && (n_workloads || wl)) return CS_E_INVALID_ARGUMENT;
@@ -726,10 +738,29 @@ int cs_load_model(cs_ctx* ctx, uint32_t inst, const cs_model* m) {
 
 namespace {
 
+// Each timing event also moves the NVTX range (nsys / ncu --nvtx): the
+// range opened here names the phase whose launches follow the event.
+const char* const kPhaseAfterEvent[16] = {"sample_and_setup", "scan_events", "prefix_rank", "bounds",
+                                          "cycle_reduce", "stage_records", "score", "detect",
+                                          "finish", "host_sizing", nullptr};
 int record_event(cs_ctx* ctx, int idx) {
   cudaEventRecord(ctx->ev[idx], ctx->stream);
+  if (ctx->nvtx_phase_open) nvtxRangePop();
+  ctx->nvtx_phase_open = kPhaseAfterEvent[idx] != nullptr;
+  if (ctx->nvtx_phase_open) nvtxRangePushA(kPhaseAfterEvent[idx]);
   return idx;
 }
+
+// cs_run's outer NVTX range; closes the phase range on every exit path
+struct NvtxRun {
+  cs_ctx* ctx;
+  explicit NvtxRun(cs_ctx* c) : ctx(c) { nvtxRangePushA("cs_run"); }
+  ~NvtxRun() {
+    if (ctx->nvtx_phase_open) nvtxRangePop();
+    ctx->nvtx_phase_open = false;
+    nvtxRangePop();
+  }
+};
 
 // NoAnchorFound -> segment_by_frequency (cycles.cpp:283-343) for one instance.
 // Returns the number of cycles (0 = still NoAnchorFound); fills t0/period.
@@ -782,6 +813,7 @@ extern "C" {
 
 int cs_run(cs_ctx* ctx, uint32_t mask) {
   if (!ctx) return CS_E_INVALID_ARGUMENT;
+  NvtxRun nvtx_run(ctx);
   if (mask & CS_RUN_MU) mask |= CS_RUN_BETA;  // mu divides by the class totals
   if ((mask & CS_RUN_MU) && ctx->streaming)
     return fail(ctx, CS_E_UNSUPPORTED, "mu needs whole-trace counter series (not per micro-batch)");

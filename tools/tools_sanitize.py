@@ -1,0 +1,45 @@
+"""Small workload touching most kernels, for compute-sanitizer (memcheck /
+racecheck / synccheck): analysis with mu and beta, wire upload,
+batched device fit, streaming push, root-cause ranking."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+
+from paper_2601_09258_b200 import abi, runtime as rt
+
+tr = rt.synth_trace(700, 3, 4, n_ranks=4, fault="nvlink_saturation", onset=560, duration=80, target_rank=1)
+an = rt.Analyzer(0)
+an.configure(tr.names, rt.span_names_mask(tr.events, len(tr.names)), n_comm_slots=tr.n_comm)
+an.upload(tr.events, [0, len(tr.events)], tr.workloads)
+an.run(abi.RUN_SEGMENT)
+recs = an.records(0)
+train = recs[recs["cycle_index"] < 500]
+x = np.stack([train["batch"].astype(float),
+              (train["batch"] * (train["input_len"] + train["output_len"])).astype(float)], 1)
+models, _ = rt.fit_latency_models([x, x[:300]], [train["latency_s"], train["latency_s"][:300]])
+an.load_model(models[0])
+an.run(abi.RUN_ALL | abi.RUN_MU)
+res = an.result(0)
+an.upload_wire(rt.wire_pack(tr.events, [0, len(tr.events)], tr.workloads))
+an.run(abi.RUN_ALL)
+recs = an.records(0)
+normal = [int(c) for c in recs["cycle_index"][(recs["armed"] == 1) & (recs["flagged"] == 0)]][-100:]
+abnormal = [int(c) for c in recs["cycle_index"][recs["flagged"] == 1]][:50]
+if len(normal) >= 10 and len(abnormal) >= 3:
+    groups = np.arange(tr.n_comm, dtype=np.int32)
+    an.suspicion_rank(normal, abnormal, np.zeros(tr.n_comm, np.int32), groups, np.arange(tr.n_comm), None)
+an.close()
+# streaming micro-batches
+an = rt.Analyzer(0)
+an.configure(tr.names, rt.span_names_mask(tr.events, len(tr.names)), n_comm_slots=tr.n_comm)
+an.load_model(models[0])
+st = an.stream()
+cut = np.linspace(0, len(tr.events), 6).astype(np.int64)
+for k in range(5):
+    ev = np.ascontiguousarray(tr.events[cut[k]:cut[k + 1]])
+    st.push_packed(ev, np.array([0, len(ev)], np.uint64), tr.workloads if k == 0 else None)
+st.close()
+an.close()
+print("sanitize workload ok:", len(tr.events), "events,", len(res.cycles), "cycles,", len(res.alerts), "alerts")
