@@ -397,7 +397,16 @@ __global__ void __launch_bounds__(kScanWarpThreads, 3)
     npend = rest;
     __syncwarp();
   };
-  for (uint32_t k = gw; k < n_list; k += nw) {
+  // Many-instance batches: each warp takes a contiguous run of tiles, which
+  // mostly belong to one instance, so its name-moment cache is flushed once
+  // per instance it meets instead of on every tile.  One instance: tiles
+  // strided across warps (all warps stream neighbouring tiles).
+  const bool runs = b.n_inst > 1;
+  const uint32_t per_warp = runs ? (n_list + nw - 1) / nw : 0u;
+  const uint32_t k0 = runs ? gw * per_warp : gw;
+  const uint32_t k_end = runs ? ((gw + 1) * per_warp < n_list ? (gw + 1) * per_warp : n_list) : n_list;
+  const uint32_t k_step = runs ? 1u : nw;
+  for (uint32_t k = k0; k < k_end; k += k_step) {
     const uint32_t t = list ? list[k] : k;
     const uint32_t inst = b.tile_inst[t];
     const u64 tb = b.tile_begin[t];
