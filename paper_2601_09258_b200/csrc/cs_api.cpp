@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <new>
 #include <array>
 #include <cmath>
 #include <cstdio>
@@ -35,6 +36,30 @@ struct NvtxScope {
 #define CS_NVTX_SCOPE(name) NvtxScope nvtx_scope_(name)
 
 namespace {
+
+// Pinned host memory for the small host mirrors a run copies to / from the
+// device (instance states, offsets, stream carries): their copies then run
+// asynchronously instead of being staged through pageable memory.
+template <typename T>
+struct PinnedAlloc {
+  using value_type = T;
+  PinnedAlloc() = default;
+  template <typename U>
+  PinnedAlloc(const PinnedAlloc<U>&) {}
+  T* allocate(size_t n) {
+    void* p = nullptr;
+    if (cudaHostAlloc(&p, std::max<size_t>(1, n) * sizeof(T), cudaHostAllocDefault) != cudaSuccess)
+      throw std::bad_alloc();
+    return static_cast<T*>(p);
+  }
+  void deallocate(T* p, size_t) { cudaFreeHost(p); }
+  template <typename U>
+  bool operator==(const PinnedAlloc<U>&) const { return true; }
+  template <typename U>
+  bool operator!=(const PinnedAlloc<U>&) const { return false; }
+};
+template <typename T>
+using pinned_vector = std::vector<T, PinnedAlloc<T>>;
 
 struct DevBuf {
   void* p = nullptr;
@@ -121,9 +146,9 @@ struct cs_ctx {
   DevBuf d_sample_tiles, d_redo_tiles;
   // state
   DevBuf d_stats, d_inst, d_a_pos, d_a_start, d_a_end;
-  std::vector<InstState> h_inst;
+  pinned_vector<InstState> h_inst;
   // cycles
-  std::vector<uint64_t> cyc_off;   // cycle-slot base per instance (+ total)
+  pinned_vector<uint64_t> cyc_off;   // cycle-slot base per instance (+ total)
   std::vector<uint64_t> n_cyc;     // cycles per instance
   uint64_t n_cycles = 0;           // cycle slots (fused path: + one hole per instance)
   uint64_t slot_cap = 0;
@@ -137,7 +162,7 @@ struct cs_ctx {
   // records
   DevBuf d_rec_off, rec_cycle, rec_pred, rec_resid, rec_stat, rec_flags, alert_rec, d_alert_off,
       block_tmp;
-  std::vector<uint64_t> rec_off, alert_off;
+  pinned_vector<uint64_t> rec_off, alert_off;
   uint64_t n_records = 0;
   // models
   std::vector<PackedModel*> model_store;
@@ -168,7 +193,7 @@ struct cs_ctx {
   bool streaming = false, stream_fresh = false, stream_pending = false;
   int stream_cur = 0;
   DevBuf d_stream[2];
-  std::vector<StreamCarry> h_stream;     // carry in force for the last batch
+  pinned_vector<StreamCarry> h_stream;   // carry in force for the last batch
   std::vector<uint32_t> stream_anchor;   // per instance, fixed after first batch
 
   ~cs_ctx() {
@@ -908,7 +933,7 @@ int cs_run(cs_ctx* ctx, uint32_t mask) {
   };
   ctx->n_cyc.assign(n_inst, 0);
   ctx->used_fused = false;
-  const std::vector<InstState> h_init = ctx->h_inst;
+  const std::vector<InstState> h_init(ctx->h_inst.begin(), ctx->h_inst.end());
   int e1 = -1, e2 = -1;
   // ---------------- fused single pass (common case)
   if (ctx->allow_fused && !ctx->streaming) {
@@ -985,7 +1010,7 @@ int cs_run(cs_ctx* ctx, uint32_t mask) {
     }
     if (!ctx->used_fused) {
       // rare: restart on the general multi-kernel path
-      ctx->h_inst = h_init;
+      ctx->h_inst.assign(h_init.begin(), h_init.end());
       CS_CUDA(cudaMemcpyAsync(d_inst, ctx->h_inst.data(), n_inst * sizeof(InstState),
                               cudaMemcpyHostToDevice, s));
       if (hint == -1) {
