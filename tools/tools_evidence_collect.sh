@@ -1,4 +1,4 @@
-# Copy one tools_gpu9.sh run (gpurun_out/) into profiles/: bench lines, fit
+# Copy one tools_evidence_gpu.sh run (gpurun_out/) into profiles/: bench lines, fit
 # and ingest benches, launch list + summary, ncu summary, raw metrics and the
 # dominant kernels' DRAM traffic (profiles/r1_ncu_traffic.json, read by bench.py).
 set -e
