@@ -121,6 +121,22 @@ def cpu_cores() -> int:
         return os.cpu_count() or 1
 
 
+def dist_setup(dist, local_rank):
+    """One process per GPU over NCCL: returns (device index, collective device).
+    CS_BENCH_DIST_BACKEND=gloo with CS_BENCH_FORCE_DEVICE=0 runs every rank on
+    one GPU with CPU collectives: a functional check of the N > 1 path on a
+    single-GPU box (not a measurement)."""
+    import torch
+    backend = os.environ.get("CS_BENCH_DIST_BACKEND", "nccl")
+    dev = int(os.environ.get("CS_BENCH_FORCE_DEVICE", local_rank))
+    torch.cuda.set_device(dev)
+    if backend == "nccl":
+        dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        return dev, f"cuda:{dev}"
+    dist.init_process_group(backend)
+    return dev, None
+
+
 def run_reference(args, rank, world):
     """--impl reference: the reference CPU analyzer (oracle/_ref, compiled
     unmodified from /root/reference) on this box's host cores, rank 0 only."""
@@ -180,9 +196,9 @@ def run_ours(args, rank, world, local_rank):
     dist = None
     if world > 1:
         import torch.distributed as dist
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    dev = local_rank
+        dev, cdev = dist_setup(dist, local_rank)
+    else:
+        dev, cdev = local_rank, f"cuda:{local_rank}"
     threads = max(1, cpu_cores() // max(1, env_int("LOCAL_WORLD_SIZE", world)))
 
     t_setup = time.time()
@@ -322,7 +338,7 @@ def run_ours(args, rank, world, local_rank):
             payload = np.concatenate(al).view(np.uint8) if al else np.zeros(0, np.uint8)
             if dist:
                 # final gather of per-shard alerts to rank 0 (NCCL over NVLink)
-                cdist.gather_bytes(payload, device=f"cuda:{dev}")
+                cdist.gather_bytes(payload, device=cdev)
                 torch.cuda.synchronize(dev)
             el = (time.perf_counter() - t0) * 1e3
             if k >= args.warmup:
@@ -383,9 +399,9 @@ def run_ours(args, rank, world, local_rank):
     rt.host_free(wptr)
 
     if dist:
-        dev_ms = cdist.max_over_ranks(dev_ms, device=f"cuda:{dev}")
-        e2e = cdist.max_over_ranks(e2e, device=f"cuda:{dev}")
-        e2e32 = cdist.max_over_ranks(e2e32, device=f"cuda:{dev}")
+        dev_ms = cdist.max_over_ranks(dev_ms, device=cdev)
+        e2e = cdist.max_over_ranks(e2e, device=cdev)
+        e2e32 = cdist.max_over_ranks(e2e32, device=cdev)
 
     # roofline: dominant kernel measured live (CUDA events on the ctx stream)
     import json as _json
@@ -511,9 +527,9 @@ def run_stream(args, rank, world, local_rank):
     dist = None
     if world > 1:
         import torch.distributed as dist
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    dev = local_rank
+        dev, cdev = dist_setup(dist, local_rank)
+    else:
+        dev, cdev = local_rank, f"cuda:{local_rank}"
     cyc = WORKLOADS["c5"][0]
     n_distinct, tile = 64, 16
     with cf.ThreadPoolExecutor(max(1, cpu_cores())) as ex:
@@ -590,7 +606,7 @@ def run_stream(args, rank, world, local_rank):
         rt.host_free(ptr)
     total_s = sum(lat) / 1e3
     if dist:
-        total_s = cdist.max_over_ranks(total_s, device=f"cuda:{dev}")
+        total_s = cdist.max_over_ranks(total_s, device=cdev)
     value = world * n_ev / total_s
     lat_s = sorted(lat)
     line = {
