@@ -350,58 +350,70 @@ def run_ours(args, rank, world, local_rank):
     e2e_seq, d2h, alerts_total = e2e_leg(lambda: an.upload_wire(wire, wire_wl))
     e2e32, _, _ = e2e_leg(lambda: an.upload(pin_ev, offs, pin_wl))
 
-    # Serving pattern (N=1): two contexts on their own non-blocking streams,
-    # one host thread each taking alternate steps, uploads issued one at a
-    # time (cs_upload_wire returns when its copies are done), so one step's
-    # upload over PCIe overlaps the other's analysis.  Every step still copies its inputs
-    # from pinned memory and reads its alerts and summaries back inside the
-    # timed region; ms_per_step = wall time / steps.
-    e2e, pipeline = e2e_seq, 1
-    if not dist:
-        import threading
-        an2 = rt.Analyzer(dev)
-        an2.configure(names, span, n_comm_slots=n_comm)
-        for i, model in enumerate(models):
-            an2.load_model(model, inst=i)
-        ctxs = [an, an2]
+    # Serving pattern: two contexts on their own non-blocking streams, one
+    # host thread each taking alternate steps, uploads issued one at a time
+    # (cs_upload_wire returns when its copies are done), so one step's upload
+    # over PCIe overlaps the other's analysis.  Every step still copies its
+    # inputs from pinned memory and reads its alerts and summaries back inside
+    # the timed region; ms_per_step = wall time / steps.  With N > 1 the
+    # per-step gather of each step's alerts to rank 0 is issued by the main
+    # thread, in step order (one communicator, one issuing thread, the same
+    # collective sequence on every rank).
+    import threading
+    an2 = rt.Analyzer(dev)
+    an2.configure(names, span, n_comm_slots=n_comm)
+    for i, model in enumerate(models):
+        an2.load_model(model, inst=i)
+    ctxs = [an, an2]
+    link = threading.Lock()  # one upload on the host link at a time
 
-        link = threading.Lock()  # one upload on the host link at a time
+    def step(a):
+        with link:
+            a.upload_wire(wire, wire_wl)  # returns when its copies are done
+        a.run(mask)
+        al = [a.alerts(i) for i in range(n_inst)]
+        _ = [a.summary(i) for i in range(n_inst)]
+        return al
 
-        def step(a):
-            with link:
-                a.upload_wire(wire, wire_wl)  # returns when its copies are done
-            a.run(mask)
-            al = [a.alerts(i) for i in range(n_inst)]
-            _ = [a.summary(i) for i in range(n_inst)]
-            return al
+    for a in ctxs:
+        for _ in range(max(1, args.warmup // 2)):
+            step(a)
+    done = [threading.Event() for _ in range(args.steps)]
+    payloads = [None] * args.steps
+    n_alerts_step = [0] * args.steps
 
-        for a in ctxs:
-            for _ in range(max(1, args.warmup // 2)):
-                step(a)
-        results = [None, None]
+    def worker(j):
+        for k in range(j, args.steps, 2):
+            al = step(ctxs[j])
+            n_alerts_step[k] = sum(len(x) for x in al)
+            payloads[k] = np.concatenate(al).view(np.uint8) if al else np.zeros(0, np.uint8)
+            done[k].set()
 
-        def worker(j, n_steps):
-            for _ in range(n_steps):
-                results[j] = step(ctxs[j])
-
-        n0 = (args.steps + 1) // 2
-        th = [threading.Thread(target=worker, args=(0, n0)),
-              threading.Thread(target=worker, args=(1, args.steps - n0))]
-        t0 = time.perf_counter()
-        for x in th:
-            x.start()
-        for x in th:
-            x.join()
-        e2e = (time.perf_counter() - t0) * 1e3 / args.steps
-        pipeline = 2
-        assert sum(len(x) for x in results[0]) == alerts_total
-        an2.close()
+    if dist:
+        dist.barrier()
+    th = [threading.Thread(target=worker, args=(j,)) for j in range(2)]
+    t0 = time.perf_counter()
+    for x in th:
+        x.start()
+    for k in range(args.steps):
+        done[k].wait()
+        if dist:
+            cdist.gather_bytes(payloads[k], device=cdev)
+    for x in th:
+        x.join()
+    if dist and cdev is not None:
+        torch.cuda.synchronize(dev)
+    e2e = (time.perf_counter() - t0) * 1e3 / args.steps
+    pipeline = 2
+    assert all(n == alerts_total for n in n_alerts_step)
+    an2.close()
     rt.host_free(wptr)
 
     if dist:
         dev_ms = cdist.max_over_ranks(dev_ms, device=cdev)
         e2e = cdist.max_over_ranks(e2e, device=cdev)
         e2e32 = cdist.max_over_ranks(e2e32, device=cdev)
+        e2e_seq = cdist.max_over_ranks(e2e_seq, device=cdev)
 
     # roofline: dominant kernel measured live (CUDA events on the ctx stream)
     import json as _json
