@@ -20,6 +20,7 @@
 #include <nlohmann/json.hpp>
 
 #include "cs_fit.h"
+#include "cs_parallel.h"
 #include "cyclescope_b200.h"
 
 using nlohmann::json;
@@ -344,13 +345,9 @@ int cs_fit_latency_models(int device, uint32_t n_models, const uint64_t* offsets
   // host: checks and holdout split per model (parallel over models)
   std::vector<std::vector<uint32_t>> train(n_models), calib(n_models);
   auto par = [&](auto body) {
-    std::vector<std::thread> th;
-    const uint32_t nt = std::max<uint32_t>(1, std::min(n_threads, n_models));
-    for (uint32_t t = 0; t < nt; ++t)
-      th.emplace_back([&, t] {
-        for (uint32_t m = t; m < n_models; m += nt) body(m);
-      });
-    for (auto& h : th) h.join();
+    cs_host::parallel_for(n_models, n_threads, [&](size_t m0, size_t m1, uint32_t) {
+      for (size_t m = m0; m < m1; ++m) body(static_cast<uint32_t>(m));
+    });
   };
   par([&](uint32_t m) {
     const uint64_t o = offsets[m], n = offsets[m + 1] - o;

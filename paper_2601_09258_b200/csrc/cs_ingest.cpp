@@ -44,6 +44,7 @@
 
 #include <emmintrin.h>
 
+#include "cs_parallel.h"
 #include "cyclescope_b200.h"
 
 struct cs_ingest_result {
@@ -903,14 +904,7 @@ void parse_record(const char* b, const char* e, Rec& r, const Keys& keys, Arena&
   }
 }
 
-template <typename F>
-void parallel_for(size_t n, uint32_t n_threads, F f) {
-  const uint32_t nt = std::max<uint32_t>(1, std::min<size_t>(n_threads, n ? n : 1));
-  std::vector<std::thread> th;
-  for (uint32_t t = 0; t < nt; ++t)
-    th.emplace_back([&, t] { f(n * t / nt, n * (t + 1) / nt, t); });
-  for (auto& x : th) x.join();
-}
+using cs_host::parallel_for;
 
 // Split the array whose '[' is at a into element spans, in parallel; returns
 // one past its ']'.  Two passes over fixed chunks of the remaining text:

@@ -18,6 +18,7 @@
 #include <unordered_map>
 #include <vector>
 
+#include "cs_parallel.h"
 #include "cyclescope_b200.h"
 
 struct cs_wire_trace {
@@ -96,14 +97,7 @@ uint32_t encode_code(const cs_event& e, int64_t prev_ts, uint32_t batch_base, co
   return dix.get(key_of(e, batch_base));
 }
 
-template <typename F>
-void parallel_for(size_t n, uint32_t n_threads, F f) {
-  const uint32_t nt = std::max<uint32_t>(1, std::min<size_t>(n_threads, n ? n : 1));
-  std::vector<std::thread> th;
-  for (uint32_t t = 0; t < nt; ++t)
-    th.emplace_back([&, t] { f(n * t / nt, n * (t + 1) / nt, t); });
-  for (auto& x : th) x.join();
-}
+using cs_host::parallel_for;
 
 // column entry counts of one event: [dur, pay8, pay16, val, dt_hi, esc]
 void count_event(const cs_event& e, uint32_t code, int64_t dt, uint32_t key, uint64_t c[6]) {
