@@ -24,6 +24,7 @@
 #include <nvtx3/nvToolsExt.h>
 
 #include "cs_internal.h"
+#include "cs_guard.h"
 #include "cyclescope_b200.h"
 
 using namespace csb;
@@ -427,7 +428,7 @@ int cs_set_config(cs_ctx* ctx, const cs_cycle_config* cycle, const cs_control_co
   return CS_OK;
 }
 
-int cs_set_name_table(cs_ctx* ctx, uint32_t n_names, const cs_name_info* names) {
+static int cs_set_name_table_impl(cs_ctx* ctx, uint32_t n_names, const cs_name_info* names) {
   if (!ctx || (n_names && !names)) return CS_E_INVALID_ARGUMENT;
   cudaSetDevice(ctx->device);
   ctx->names.assign(names, names + n_names);
@@ -462,6 +463,10 @@ int cs_set_name_table(cs_ctx* ctx, uint32_t n_names, const cs_name_info* names) 
   CS_CUDA(cudaMemcpy(ds, series.data(), series.size(), cudaMemcpyHostToDevice));
   CS_CUDA(cudaMemcpy(dc, cls.data(), cls.size(), cudaMemcpyHostToDevice));
   return CS_OK;
+}
+
+int cs_set_name_table(cs_ctx* ctx, uint32_t n_names, const cs_name_info* names) {
+  return cs_guard([&] { return cs_set_name_table_impl(ctx, n_names, names); });
 }
 
 }  // extern "C"
@@ -552,7 +557,7 @@ int wait_copied(cs_ctx* ctx) {
   return CS_OK;
 }
 
-int cs_upload(cs_ctx* ctx, uint32_t n_inst, const uint64_t* inst_offsets, const cs_event* ev,
+static int cs_upload_impl(cs_ctx* ctx, uint32_t n_inst, const uint64_t* inst_offsets, const cs_event* ev,
               uint64_t n_workloads, const cs_workload* wl) {
   CS_NVTX_SCOPE("cs_upload");
   if (ctx) ctx->tails_on_device = false;
@@ -566,7 +571,12 @@ int cs_upload(cs_ctx* ctx, uint32_t n_inst, const uint64_t* inst_offsets, const 
   return CS_OK;
 }
 
-int cs_upload_wire(cs_ctx* ctx, uint32_t n_inst, const uint64_t* inst_offsets,
+int cs_upload(cs_ctx* ctx, uint32_t n_inst, const uint64_t* inst_offsets, const cs_event* ev,
+              uint64_t n_workloads, const cs_workload* wl) {
+  return cs_guard([&] { return cs_upload_impl(ctx, n_inst, inst_offsets, ev, n_workloads, wl); });
+}
+
+static int cs_upload_wire_impl(cs_ctx* ctx, uint32_t n_inst, const uint64_t* inst_offsets,
                    const cs_wire_batch* w, uint64_t n_workloads, const cs_workload* wl) {
   if (!w || !ctx) return CS_E_INVALID_ARGUMENT;
   CS_NVTX_SCOPE("cs_upload_wire");
@@ -629,7 +639,12 @@ int cs_upload_wire(cs_ctx* ctx, uint32_t n_inst, const uint64_t* inst_offsets,
   return CS_OK;
 }
 
-int cs_load_model(cs_ctx* ctx, uint32_t inst, const cs_model* m) {
+int cs_upload_wire(cs_ctx* ctx, uint32_t n_inst, const uint64_t* inst_offsets,
+                   const cs_wire_batch* w, uint64_t n_workloads, const cs_workload* wl) {
+  return cs_guard([&] { return cs_upload_wire_impl(ctx, n_inst, inst_offsets, w, n_workloads, wl); });
+}
+
+static int cs_load_model_impl(cs_ctx* ctx, uint32_t inst, const cs_model* m) {
   if (!ctx || !m) return CS_E_INVALID_ARGUMENT;
   cudaSetDevice(ctx->device);
   if (m->n_features > static_cast<uint32_t>(kMaxFeatures))
@@ -759,6 +774,10 @@ int cs_load_model(cs_ctx* ctx, uint32_t inst, const cs_model* m) {
   return CS_OK;
 }
 
+int cs_load_model(cs_ctx* ctx, uint32_t inst, const cs_model* m) {
+  return cs_guard([&] { return cs_load_model_impl(ctx, inst, m); });
+}
+
 }  // extern "C"
 
 namespace {
@@ -836,7 +855,7 @@ int frequency_plan(cs_ctx* ctx, uint32_t i, int64_t* t0, int64_t* period, uint64
 
 extern "C" {
 
-int cs_run(cs_ctx* ctx, uint32_t mask) {
+static int cs_run_impl(cs_ctx* ctx, uint32_t mask) {
   if (!ctx) return CS_E_INVALID_ARGUMENT;
   NvtxRun nvtx_run(ctx);
   if (mask & CS_RUN_MU) mask |= CS_RUN_BETA;  // mu divides by the class totals
@@ -1291,6 +1310,10 @@ int cs_run(cs_ctx* ctx, uint32_t mask) {
   return CS_OK;
 }
 
+int cs_run(cs_ctx* ctx, uint32_t mask) {
+  return cs_guard([&] { return cs_run_impl(ctx, mask); });
+}
+
 int cs_stream_begin(cs_ctx* ctx) {
   if (!ctx) return CS_E_INVALID_ARGUMENT;
   ctx->streaming = true;
@@ -1321,7 +1344,7 @@ int cs_stream_tail(cs_ctx* ctx, uint32_t inst, uint64_t* keep_from) {
   return CS_OK;
 }
 
-int cs_stream_push(cs_ctx* ctx, uint32_t n_inst, const uint64_t* offsets, const cs_event* ev,
+static int cs_stream_push_impl(cs_ctx* ctx, uint32_t n_inst, const uint64_t* offsets, const cs_event* ev,
                    uint64_t n_workloads, const cs_workload* wl, uint32_t mask, cs_alert* alerts,
                    size_t cap, size_t* n_alerts) {
   if (!ctx || !offsets || n_inst == 0) return CS_E_INVALID_ARGUMENT;
@@ -1414,6 +1437,12 @@ int cs_stream_push(cs_ctx* ctx, uint32_t n_inst, const uint64_t* offsets, const 
   if (n_alerts) *n_alerts = na;
   if (alerts && na > cap) return fail(ctx, CS_E_INVALID_ARGUMENT, "alert buffer too small");
   return CS_OK;
+}
+
+int cs_stream_push(cs_ctx* ctx, uint32_t n_inst, const uint64_t* offsets, const cs_event* ev,
+                   uint64_t n_workloads, const cs_workload* wl, uint32_t mask, cs_alert* alerts,
+                   size_t cap, size_t* n_alerts) {
+  return cs_guard([&] { return cs_stream_push_impl(ctx, n_inst, offsets, ev, n_workloads, wl, mask, alerts, cap, n_alerts); });
 }
 
 int cs_sync(cs_ctx* ctx) {
@@ -1580,7 +1609,7 @@ int cs_get_collective_beta(cs_ctx* ctx, uint32_t inst, double* beta, uint8_t* pr
   return CS_OK;
 }
 
-int cs_suspicion_rank(cs_ctx* ctx, uint32_t inst, const uint64_t* normal_cycles, size_t n_normal,
+static int cs_suspicion_rank_impl(cs_ctx* ctx, uint32_t inst, const uint64_t* normal_cycles, size_t n_normal,
                       const uint64_t* abnormal_cycles, size_t n_abnormal, const int32_t* comm_name,
                       const int32_t* comm_group, const int32_t* comm_rank,
                       const int32_t* comm_location, cs_suspect* out, size_t cap, size_t* n_out) {
@@ -1669,6 +1698,13 @@ int cs_suspicion_rank(cs_ctx* ctx, uint32_t inst, const uint64_t* normal_cycles,
     return fail(ctx, rc, "need >= 10 normal and >= 3 abnormal cycles, got " + std::to_string(n_normal) + "/" +
                              std::to_string(n_abnormal));
   return rc;
+}
+
+int cs_suspicion_rank(cs_ctx* ctx, uint32_t inst, const uint64_t* normal_cycles, size_t n_normal,
+                      const uint64_t* abnormal_cycles, size_t n_abnormal, const int32_t* comm_name,
+                      const int32_t* comm_group, const int32_t* comm_rank,
+                      const int32_t* comm_location, cs_suspect* out, size_t cap, size_t* n_out) {
+  return cs_guard([&] { return cs_suspicion_rank_impl(ctx, inst, normal_cycles, n_normal, abnormal_cycles, n_abnormal, comm_name, comm_group, comm_rank, comm_location, out, cap, n_out); });
 }
 
 int cs_get_mu(cs_ctx* ctx, uint32_t inst, double* mu, uint8_t* has, size_t cap, size_t* n) {

@@ -21,6 +21,7 @@
 
 #include "cs_fit.h"
 #include "cs_parallel.h"
+#include "cs_guard.h"
 #include "cyclescope_b200.h"
 
 using nlohmann::json;
@@ -293,7 +294,7 @@ void set_features(cs_fitted_model& m, uint32_t n_features, const int32_t* featur
 
 extern "C" {
 
-int cs_fit_latency_model(uint64_t n, uint32_t n_features, const int32_t* feature_ids,
+static int cs_fit_latency_model_impl(uint64_t n, uint32_t n_features, const int32_t* feature_ids,
                          const double* x, const double* y, const cs_gbdt_params* params,
                          const cs_fit_options* opt, cs_fitted_model** out, char* err,
                          size_t err_cap) {
@@ -326,7 +327,14 @@ int cs_fit_latency_model(uint64_t n, uint32_t n_features, const int32_t* feature
   return CS_OK;
 }
 
-int cs_fit_latency_models(int device, uint32_t n_models, const uint64_t* offsets,
+int cs_fit_latency_model(uint64_t n, uint32_t n_features, const int32_t* feature_ids,
+                         const double* x, const double* y, const cs_gbdt_params* params,
+                         const cs_fit_options* opt, cs_fitted_model** out, char* err,
+                         size_t err_cap) {
+  return cs_guard([&] { return cs_fit_latency_model_impl(n, n_features, feature_ids, x, y, params, opt, out, err, err_cap); });
+}
+
+static int cs_fit_latency_models_impl(int device, uint32_t n_models, const uint64_t* offsets,
                           uint32_t n_features, const int32_t* feature_ids, const double* x,
                           const double* y, const cs_gbdt_params* params, const cs_fit_options* opt,
                           uint32_t n_threads, cs_fitted_model** out, int32_t* status,
@@ -408,7 +416,15 @@ int cs_fit_latency_models(int device, uint32_t n_models, const uint64_t* offsets
   return CS_OK;
 }
 
-int cs_model_from_json(const char* text, cs_fitted_model** out, char* err, size_t err_cap) {
+int cs_fit_latency_models(int device, uint32_t n_models, const uint64_t* offsets,
+                          uint32_t n_features, const int32_t* feature_ids, const double* x,
+                          const double* y, const cs_gbdt_params* params, const cs_fit_options* opt,
+                          uint32_t n_threads, cs_fitted_model** out, int32_t* status,
+                          float* device_ms) {
+  return cs_guard([&] { return cs_fit_latency_models_impl(device, n_models, offsets, n_features, feature_ids, x, y, params, opt, n_threads, out, status, device_ms); });
+}
+
+static int cs_model_from_json_impl(const char* text, cs_fitted_model** out, char* err, size_t err_cap) {
   if (!text || !out) return CS_E_INVALID_ARGUMENT;
   *out = nullptr;
   auto m = new cs_fitted_model();
@@ -453,6 +469,10 @@ int cs_model_from_json(const char* text, cs_fitted_model** out, char* err, size_
   }
   *out = m;
   return CS_OK;
+}
+
+int cs_model_from_json(const char* text, cs_fitted_model** out, char* err, size_t err_cap) {
+  return cs_guard([&] { return cs_model_from_json_impl(text, out, err, err_cap); });
 }
 
 int cs_model_to_json(const cs_fitted_model* m, char* buf, size_t cap, size_t* n) {
@@ -527,7 +547,7 @@ int cs_alerts_to_ndjson(const cs_alert* alerts, uint64_t n_alerts, uint64_t pre_
 // device configs + per-name table.  `names` are the interned names in id
 // order (lexicographic); name_is_span marks names that occur as Spans
 // (dense beta slots in name order).
-int cs_config_from_json(const char* run_config_json, uint32_t n_names,
+static int cs_config_from_json_impl(const char* run_config_json, uint32_t n_names,
                         const char* const* names, const uint8_t* name_is_span,
                         uint32_t n_comm_slots, cs_name_info* out_names,
                         cs_cycle_config* out_cycle, cs_control_config* out_control, char* err,
@@ -656,6 +676,14 @@ int cs_config_from_json(const char* run_config_json, uint32_t n_names,
     return CS_E_CONFIG;
   }
   return CS_OK;
+}
+
+int cs_config_from_json(const char* run_config_json, uint32_t n_names,
+                        const char* const* names, const uint8_t* name_is_span,
+                        uint32_t n_comm_slots, cs_name_info* out_names,
+                        cs_cycle_config* out_cycle, cs_control_config* out_control, char* err,
+                        size_t err_cap) {
+  return cs_guard([&] { return cs_config_from_json_impl(run_config_json, n_names, names, name_is_span, n_comm_slots, out_names, out_cycle, out_control, err, err_cap); });
 }
 
 }  // extern "C"

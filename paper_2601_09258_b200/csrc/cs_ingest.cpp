@@ -45,6 +45,7 @@
 #include <emmintrin.h>
 
 #include "cs_parallel.h"
+#include "cs_guard.h"
 #include "cyclescope_b200.h"
 
 struct cs_ingest_result {
@@ -1140,7 +1141,7 @@ struct CommKey {
 
 extern "C" {
 
-int cs_ingest_chrome_json(const char* text, size_t len, const cs_ingest_keys* keys_in,
+static int cs_ingest_chrome_json_impl(const char* text, size_t len, const cs_ingest_keys* keys_in,
                           uint32_t n_threads, cs_ingest_result** out) {
   if (!out || (len && !text)) return CS_E_INVALID_ARGUMENT;
   *out = nullptr;
@@ -1465,6 +1466,11 @@ int cs_ingest_chrome_json(const char* text, size_t len, const cs_ingest_keys* ke
   return CS_OK;
 }
 
+int cs_ingest_chrome_json(const char* text, size_t len, const cs_ingest_keys* keys_in,
+                          uint32_t n_threads, cs_ingest_result** out) {
+  return cs_guard([&] { return cs_ingest_chrome_json_impl(text, len, keys_in, n_threads, out); });
+}
+
 int cs_ingest_view(const cs_ingest_result* r, const cs_event** ev, const uint64_t** event_ids,
                    uint64_t* n_ev, const cs_workload** wl, uint64_t* n_wl, const char** names,
                    size_t* names_bytes, uint32_t* n_names, const int32_t** comm_name,
@@ -1488,7 +1494,7 @@ int cs_ingest_view(const cs_ingest_result* r, const cs_event** ev, const uint64_
   return CS_OK;
 }
 
-int cs_ingest_merge(const cs_ingest_result* const* in, uint32_t n_in, const cs_calibration_options* opt,
+static int cs_ingest_merge_impl(const cs_ingest_result* const* in, uint32_t n_in, const cs_calibration_options* opt,
                     uint32_t n_threads, cs_ingest_result** out, char* err, size_t err_cap) {
   if (!out || (n_in && !in)) return CS_E_INVALID_ARGUMENT;
   *out = nullptr;
@@ -1710,6 +1716,11 @@ int cs_ingest_merge(const cs_ingest_result* const* in, uint32_t n_in, const cs_c
   res->calibrated = true;
   *out = res;
   return CS_OK;
+}
+
+int cs_ingest_merge(const cs_ingest_result* const* in, uint32_t n_in, const cs_calibration_options* opt,
+                    uint32_t n_threads, cs_ingest_result** out, char* err, size_t err_cap) {
+  return cs_guard([&] { return cs_ingest_merge_impl(in, n_in, opt, n_threads, out, err, err_cap); });
 }
 
 int cs_ingest_topology(const cs_ingest_result* r, const int32_t** comm_location,

@@ -14,6 +14,7 @@
 #include <map>
 #include <vector>
 
+#include "cs_guard.h"
 #include "cyclescope_b200.h"
 
 namespace {
@@ -101,7 +102,7 @@ double cs_welch_p_value(double mean_a, double var_a, uint64_t n_a, double mean_b
   return welch_p(mean_a, var_a, n_a, mean_b, var_b, n_b);
 }
 
-int cs_rank_suspects(const cs_rca_window* normal, const cs_rca_window* abnormal,
+static int cs_rank_suspects_impl(const cs_rca_window* normal, const cs_rca_window* abnormal,
                      const cs_rca_layout* lay, cs_suspect* out, size_t cap, size_t* n_out) {
   if (!normal || !abnormal || !lay || !n_out) return CS_E_INVALID_ARGUMENT;
   *n_out = 0;
@@ -217,6 +218,11 @@ int cs_rank_suspects(const cs_rca_window* normal, const cs_rca_window* abnormal,
     std::memcpy(out, entries.data(), entries.size() * sizeof(cs_suspect));
   }
   return CS_OK;
+}
+
+int cs_rank_suspects(const cs_rca_window* normal, const cs_rca_window* abnormal,
+                     const cs_rca_layout* lay, cs_suspect* out, size_t cap, size_t* n_out) {
+  return cs_guard([&] { return cs_rank_suspects_impl(normal, abnormal, lay, out, cap, n_out); });
 }
 
 }  // extern "C"

@@ -19,6 +19,7 @@
 #include <vector>
 
 #include "cs_parallel.h"
+#include "cs_guard.h"
 #include "cyclescope_b200.h"
 
 struct cs_wire_trace {
@@ -115,7 +116,7 @@ void count_event(const cs_event& e, uint32_t code, int64_t dt, uint32_t key, uin
 
 extern "C" {
 
-int cs_wire_pack(uint32_t n_inst, const uint64_t* off, const cs_event* ev, uint64_t n_workloads,
+static int cs_wire_pack_impl(uint32_t n_inst, const uint64_t* off, const cs_event* ev, uint64_t n_workloads,
                  const cs_workload* wl, uint32_t n_threads, cs_wire_trace** out) {
   if (!out || !off || n_inst == 0 || off[0] != 0 || (n_workloads && !wl)) return CS_E_INVALID_ARGUMENT;
   *out = nullptr;
@@ -258,6 +259,11 @@ int cs_wire_pack(uint32_t n_inst, const uint64_t* off, const cs_event* ev, uint6
   if (!w->has_wl32) w->wl32.clear();
   *out = w;
   return CS_OK;
+}
+
+int cs_wire_pack(uint32_t n_inst, const uint64_t* off, const cs_event* ev, uint64_t n_workloads,
+                 const cs_workload* wl, uint32_t n_threads, cs_wire_trace** out) {
+  return cs_guard([&] { return cs_wire_pack_impl(n_inst, off, ev, n_workloads, wl, n_threads, out); });
 }
 
 int cs_wire_view(const cs_wire_trace* w, cs_wire_batch* out, uint64_t* n_blocks) {
