@@ -1250,27 +1250,84 @@ static int cs_ingest_chrome_json_impl(const char* text, size_t len, const cs_ing
   });
   for (uint8_t x : bad)
     if (x) return reject();
-  // ---- fallback ids in document order, then the canonical stable sort
-  std::vector<Rec*> kept;
-  kept.reserve(spans.size());
-  uint64_t next_id = 1;
-  for (uint32_t t = 0; t < n_threads; ++t)
+  // ---- fallback ids in document order, then the canonical stable sort.
+  // next_id evolves as x -> max(x, eid) + 1 per kept record (a fallback id is
+  // x itself), i.e. x -> max(x + a, b): such maps compose, so each chunk's map
+  // is built in parallel, chained sequentially (one per chunk), and the ids
+  // assigned in parallel.  A chunk holding an id that could wrap the uint64
+  // arithmetic is done sequentially instead (the reference wraps too).
+  const uint32_t nchunk = n_threads;
+  struct Affine {
+    uint64_t a = 0, b = 0;  // x -> max(x + a, b); b = 0 is "no bound" (x >= 1)
+    bool wraps = false;
+  };
+  std::vector<Affine> maps(nchunk);
+  parallel_for(nchunk, nchunk, [&](size_t t0, size_t t1, uint32_t) {
+    for (size_t t = t0; t < t1; ++t) {
+      Affine m;
+      for (const Rec& r : chunks[t]) {
+        if (!r.keep) continue;
+        if (r.has_eid && r.eid >= (UINT64_MAX >> 1)) m.wraps = true;
+        m.b = r.has_eid ? std::max(m.b + 1, r.eid + 1) : m.b + 1;
+        m.a += 1;
+      }
+      maps[t] = m;
+    }
+  });
+  bool any_wrap = false;
+  for (const auto& m : maps) any_wrap |= m.wraps;
+  std::vector<uint64_t> next_in(nchunk + 1, 1);
+  for (uint32_t t = 0; t < nchunk && !any_wrap; ++t)
+    next_in[t + 1] = std::max(next_in[t] + maps[t].a, maps[t].b);
+  // per chunk: ids, parse issues (with the id each record had at its turn), kept records
+  std::vector<std::vector<cs_ingest_issue>> tiss(nchunk);
+  std::vector<std::vector<Rec*>> tkept(nchunk);
+  auto chunk_ids = [&](uint32_t t, uint64_t& next_id) {
+    auto issue = [&](uint8_t sev, uint8_t code, bool has_id, uint64_t id) {
+      cs_ingest_issue x{};
+      x.severity = sev;
+      x.code = code;
+      x.has_event_id = has_id ? 1 : 0;
+      x.event_id = has_id ? id : 0;
+      tiss[t].push_back(x);
+    };
+    tkept[t].reserve(chunks[t].size());
     for (Rec& r : chunks[t]) {
-      // parse issues; event_id as parse_record saw it (eid, or the fallback)
       const uint64_t id_now = r.has_eid ? r.eid : next_id;
       if (r.lead) {
-        res->issue(r.lead == 1 ? CS_SEV_ERROR : CS_SEV_WARNING, CS_ISSUE_MALFORMED_EVENT, false, 0);
+        issue(r.lead == 1 ? CS_SEV_ERROR : CS_SEV_WARNING, CS_ISSUE_MALFORMED_EVENT, false, 0);
       } else {
-        if (r.cat_warn) res->issue(CS_SEV_WARNING, CS_ISSUE_MALFORMED_EVENT, true, id_now);
-        for (uint32_t q = 0; q < r.dropped; ++q)
-          res->issue(CS_SEV_WARNING, CS_ISSUE_MALFORMED_ARGS, true, id_now);
-        if (r.type_err) res->issue(CS_SEV_ERROR, CS_ISSUE_MALFORMED_EVENT, false, 0);
+        if (r.cat_warn) issue(CS_SEV_WARNING, CS_ISSUE_MALFORMED_EVENT, true, id_now);
+        for (uint32_t q = 0; q < r.dropped; ++q) issue(CS_SEV_WARNING, CS_ISSUE_MALFORMED_ARGS, true, id_now);
+        if (r.type_err) issue(CS_SEV_ERROR, CS_ISSUE_MALFORMED_EVENT, false, 0);
       }
       if (!r.keep) continue;
       if (!r.has_eid) r.eid = next_id;
       next_id = std::max(next_id, r.eid) + 1;
-      kept.push_back(&r);
+      tkept[t].push_back(&r);
     }
+  };
+  if (any_wrap) {
+    uint64_t next_id = 1;
+    for (uint32_t t = 0; t < nchunk; ++t) chunk_ids(t, next_id);
+  } else {
+    parallel_for(nchunk, nchunk, [&](size_t t0, size_t t1, uint32_t) {
+      for (size_t t = t0; t < t1; ++t) {
+        uint64_t next_id = next_in[t];
+        chunk_ids(static_cast<uint32_t>(t), next_id);
+      }
+    });
+  }
+  std::vector<Rec*> kept;
+  {
+    size_t nk = 0;
+    for (const auto& v : tkept) nk += v.size();
+    kept.reserve(nk);
+  }
+  for (uint32_t t = 0; t < nchunk; ++t) {
+    for (const auto& x : tiss[t]) res->issue(x.severity, x.code, x.has_event_id != 0, x.event_id);
+    kept.insert(kept.end(), tkept[t].begin(), tkept[t].end());
+  }
   (void)rec;
   {
     struct Key {
@@ -1278,12 +1335,23 @@ static int cs_ingest_chrome_json_impl(const char* text, size_t len, const cs_ing
       uint64_t eid;
       Rec* idx;
     };
-    std::vector<Key> keys_v(kept.size());
-    for (size_t i = 0; i < kept.size(); ++i) keys_v[i] = {kept[i]->start, kept[i]->eid, kept[i]};
     auto less = [](const Key& a, const Key& b) {
       return a.start != b.start ? a.start < b.start : a.eid < b.eid;
     };
-    if (!std::is_sorted(keys_v.begin(), keys_v.end(), less)) {
+    std::vector<Key> keys_v(kept.size());
+    std::vector<uint8_t> unsorted(n_threads, 0);
+    parallel_for(kept.size(), n_threads, [&](size_t k0, size_t k1, uint32_t t) {
+      for (size_t i = k0; i < k1; ++i) keys_v[i] = {kept[i]->start, kept[i]->eid, kept[i]};
+      for (size_t i = k0 + 1; i < k1 && !unsorted[t]; ++i) unsorted[t] = less(keys_v[i], keys_v[i - 1]);
+    });
+    bool sorted = true;
+    for (uint8_t u : unsorted) sorted = sorted && !u;
+    if (sorted)  // chunk boundaries
+      for (uint32_t t = 1; t < n_threads && sorted; ++t) {
+        const size_t i = kept.size() * t / std::max<size_t>(1, std::min<size_t>(n_threads, kept.size() ? kept.size() : 1));
+        if (i > 0 && i < kept.size()) sorted = !less(keys_v[i], keys_v[i - 1]);
+      }
+    if (!sorted) {
       std::stable_sort(keys_v.begin(), keys_v.end(), less);
       for (size_t i = 0; i < kept.size(); ++i) kept[i] = keys_v[i].idx;
     }
