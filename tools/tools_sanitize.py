@@ -42,4 +42,29 @@ for k in range(5):
     st.push_packed(ev, np.array([0, len(ev)], np.uint64), tr.workloads if k == 0 else None)
 st.close()
 an.close()
-print("sanitize workload ok:", len(tr.events), "events,", len(res.cycles), "cycles,", len(res.alerts), "alerts")
+# a multi-instance batch (uneven sizes, an empty instance) through the wire format
+parts = [rt.synth_trace(n, 20 + i, 30 + i, n_ranks=1 + i % 3, fault="cpu_contention" if i == 1 else None,
+                        onset=n - 100, duration=60, compact_names=False) for i, n in enumerate((300, 900, 150))]
+names = parts[0].names
+evs = [p.events for p in parts]
+evs.insert(2, evs[0][:0])  # empty instance
+off = np.concatenate([[0], np.cumsum([len(e) for e in evs])]).astype(np.uint64)
+ev = np.concatenate(evs)
+wl = np.concatenate([p.workloads for p in parts])
+base = 0
+for k, e in enumerate(evs):
+    lo, hi = int(off[k]), int(off[k + 1])
+    has = (ev["flags"][lo:hi] & abi.EV_HAS_BATCH) != 0
+    ev["payload"][lo:hi][has] += np.uint64(base)
+    src = [p for p in parts][k - (1 if k > 2 else 0)] if k != 2 else None
+    if src is not None:
+        base += len(src.workloads)
+an = rt.Analyzer(0)
+an.configure(names, rt.span_names_mask(ev, len(names)), n_comm_slots=max(p.n_comm for p in parts))
+an.load_model(models[0])
+an.upload_wire(rt.wire_pack(ev, off, wl))
+an.run(abi.RUN_ALL | abi.RUN_MU)
+n_cyc = sum(an.summary(i).n_cycles for i in range(len(evs)))
+an.close()
+print("sanitize workload ok:", len(tr.events), "events,", len(res.cycles), "cycles,", len(res.alerts),
+      "alerts; multi-instance batch", len(ev), "events,", n_cyc, "cycles")
