@@ -490,6 +490,13 @@ int cs_get_collective_beta(cs_ctx* ctx, uint32_t inst, double* beta,
  * total (ClassStat::mu); has[k] = 0 where the reference leaves mu unset. */
 int cs_get_mu(cs_ctx* ctx, uint32_t inst, double* mu, uint8_t* has, size_t cap, size_t* n);
 int cs_get_records(cs_ctx* ctx, uint32_t inst, cs_record* buf, size_t cap, size_t* n);
+/* Row ranges [first, first + count) of the cycle / record tables above (the
+ * same rows, `index` and `episode_id` as the whole-table getters).  Used by
+ * the sharded single-instance run (halo.py) to read a shard's halo and tail
+ * without copying its whole tables; no reference counterpart.  count rows
+ * must fit in buf; a range past the table is CS_E_INVALID_ARGUMENT. */
+int cs_get_cycle_range(cs_ctx* ctx, uint32_t inst, uint64_t first, uint64_t count, cs_cycle* buf);
+int cs_get_record_range(cs_ctx* ctx, uint32_t inst, uint64_t first, uint64_t count, cs_record* buf);
 int cs_get_alerts(cs_ctx* ctx, uint32_t inst, cs_alert* buf, size_t cap, size_t* n);
 
 /* ------------------------------------------- post-alert root cause (§8f #4)

@@ -132,13 +132,17 @@ def _arr(ptr, n, dtype):
     return np.frombuffer((C.c_char * nbytes).from_address(ptr), dtype=dtype).copy()
 
 
-def analyze(events, names, workloads, n_comm=0, run_config=None, model_json=None):
-    """The whole hot path on one instance; returns a dict of numpy arrays."""
+def analyze(events, names, workloads, n_comm=0, run_config=None, model_json=None, span=None):
+    """The whole hot path on one instance; returns a dict of numpy arrays.
+    `span`: which names are span names (beta slots); default: those with a
+    span event in `events` (a shard of a trace passes the whole trace's)."""
     L = lib()
     events = np.ascontiguousarray(events, dtype=abi.EVENT_DTYPE)
     workloads = np.ascontiguousarray(workloads, dtype=abi.WORKLOAD_DTYPE)
-    span = np.zeros(len(names), np.uint8)
-    span[np.unique(events["name_id"][events["kind"] == abi.SPAN])] = 1
+    if span is None:
+        span = np.zeros(len(names), np.uint8)
+        span[np.unique(events["name_id"][events["kind"] == abi.SPAN])] = 1
+    span = np.ascontiguousarray(span, dtype=np.uint8)
     cyc, ctl, table = derive_config(run_config, names, span, n_comm)
     mp = None
     if model_json:

@@ -1529,12 +1529,26 @@ int d2h(cs_ctx* ctx, std::vector<T>& v, const DevBuf& b, uint64_t off, uint64_t 
 
 extern "C" {
 
+static int cycles_to_host(cs_ctx* ctx, uint32_t inst, uint64_t first, uint64_t nc, cs_cycle* buf);
+
 int cs_get_cycles(cs_ctx* ctx, uint32_t inst, cs_cycle* buf, size_t cap, size_t* n) {
   if (!ctx || !ctx->ran || inst >= ctx->n_inst) return CS_E_INVALID_ARGUMENT;
-  const uint64_t c0 = ctx->cyc_off[inst], nc = ctx->n_cyc[inst];
+  const uint64_t nc = ctx->n_cyc[inst];
   if (n) *n = nc;
   if (!buf) return CS_OK;
   if (cap < nc) return fail(ctx, CS_E_INVALID_ARGUMENT, "buffer too small");
+  return cycles_to_host(ctx, inst, 0, nc, buf);
+}
+
+int cs_get_cycle_range(cs_ctx* ctx, uint32_t inst, uint64_t first, uint64_t count, cs_cycle* buf) {
+  if (!ctx || !ctx->ran || inst >= ctx->n_inst || (count && !buf)) return CS_E_INVALID_ARGUMENT;
+  if (first > ctx->n_cyc[inst] || count > ctx->n_cyc[inst] - first)
+    return fail(ctx, CS_E_INVALID_ARGUMENT, "cycle range out of bounds");
+  return cycles_to_host(ctx, inst, first, count, buf);
+}
+
+static int cycles_to_host(cs_ctx* ctx, uint32_t inst, uint64_t first, uint64_t nc, cs_cycle* buf) {
+  const uint64_t c0 = ctx->cyc_off[inst] + first;
   std::vector<int64_t> st, en, ae;
   std::vector<uint64_t> ap, fi, la;
   std::vector<uint8_t> sg;
@@ -1548,7 +1562,7 @@ int cs_get_cycles(cs_ctx* ctx, uint32_t inst, cs_cycle* buf, size_t cap, size_t*
   const uint64_t ib = ctx->inst_off[inst];
   for (uint64_t k = 0; k < nc; ++k) {
     cs_cycle& c = buf[k];
-    c.index = k + (ctx->streaming ? ctx->h_stream[inst].cycle_off : 0);
+    c.index = first + k + (ctx->streaming ? ctx->h_stream[inst].cycle_off : 0);
     c.start_ts = st[k];
     c.end_ts = en[k];
     c.anchor_pos = ap[k] == UINT64_MAX ? UINT64_MAX : ap[k] - ib;
@@ -1760,6 +1774,30 @@ int cs_get_records(cs_ctx* ctx, uint32_t inst, cs_record* buf, size_t cap, size_
     uint64_t ep = ctx->streaming ? ctx->h_stream[inst].episodes : 0;
     for (uint64_t k = 0; k < nr; ++k)
       if (buf[k].alert) buf[k].episode_id = ep++;
+  }
+  return CS_OK;
+}
+
+int cs_get_record_range(cs_ctx* ctx, uint32_t inst, uint64_t first, uint64_t count, cs_record* buf) {
+  if (!ctx || !ctx->ran || inst >= ctx->n_inst || (count && !buf)) return CS_E_INVALID_ARGUMENT;
+  const uint64_t r0 = ctx->rec_off[inst], nr = ctx->rec_off[inst + 1] - r0;
+  if (first > nr || count > nr - first) return fail(ctx, CS_E_INVALID_ARGUMENT, "record range out of bounds");
+  int rc = gather_records(ctx, inst, r0 + first, count, buf);
+  if (rc) return rc;
+  if ((ctx->last_mask & CS_RUN_DETECT) && count) {
+    bool any = false;
+    for (uint64_t k = 0; k < count && !any; ++k) any = buf[k].alert;
+    if (any) {
+      // episode ids: alerts before the range (the alerts are few)
+      size_t na = 0;
+      if ((rc = cs_get_alerts(ctx, inst, nullptr, 0, &na))) return rc;
+      std::vector<cs_alert> al(na);
+      if (na && (rc = cs_get_alerts(ctx, inst, al.data(), na, &na))) return rc;
+      uint64_t ep = ctx->streaming ? ctx->h_stream[inst].episodes : 0;
+      for (const cs_alert& a : al) ep += a.record_index < first;
+      for (uint64_t k = 0; k < count; ++k)
+        if (buf[k].alert) buf[k].episode_id = ep++;
+    }
   }
   return CS_OK;
 }

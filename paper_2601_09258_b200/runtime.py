@@ -55,6 +55,8 @@ def lib():
     L.cs_set_config.argtypes = [vp, C.POINTER(abi.CycleConfig), C.POINTER(abi.ControlConfig)]
     L.cs_set_name_table.argtypes = [vp, u32, vp]
     L.cs_upload.argtypes = [vp, u32, vp, vp, u64, vp]
+    L.cs_get_cycle_range.argtypes = [vp, u32, u64, u64, vp]
+    L.cs_get_record_range.argtypes = [vp, u32, u64, u64, vp]
     L.cs_upload_wire.argtypes = [vp, u32, vp, C.POINTER(abi.WireBatch), u64, vp]
     L.cs_wire_pack.argtypes = [u32, vp, vp, u64, vp, u32, C.POINTER(vp)]
     L.cs_wire_view.argtypes = [vp, C.POINTER(abi.WireBatch), C.POINTER(u64)]
@@ -738,6 +740,18 @@ class Analyzer:
 
     def records(self, inst=0):
         return self._get(self.L.cs_get_records, inst, abi.RECORD_DTYPE)
+
+    def cycle_range(self, first: int, count: int, inst=0):
+        """Rows [first, first + count) of cycles() (cs_get_cycle_range)."""
+        out = np.zeros(count, abi.CYCLE_DTYPE)
+        self._ck(self.L.cs_get_cycle_range(self.h, inst, first, count, out.ctypes.data if count else None))
+        return out
+
+    def record_range(self, first: int, count: int, inst=0):
+        """Rows [first, first + count) of records() (cs_get_record_range)."""
+        out = np.zeros(count, abi.RECORD_DTYPE)
+        self._ck(self.L.cs_get_record_range(self.h, inst, first, count, out.ctypes.data if count else None))
+        return out
 
     def suspicion_rank(self, normal_cycles, abnormal_cycles, comm_name=(), comm_group=(),
                        comm_rank=(), comm_location=None, inst=0) -> np.ndarray:
