@@ -2,7 +2,7 @@
 """Benchmark: trace events/sec analysed on B200 (BASELINE.json metric).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                  [--workload c2|c1|c3]
+                  [--workload c2|c1|c3|c5] [--c2-split replicas|halo]
 
 Workload (default c2 = BASELINE configs[1]): one 8-rank tensor-parallel serving
 instance, ~100 M events (3.70 M cycles x 27 events), mixed prefill/decode,
@@ -642,6 +642,155 @@ def run_stream(args, rank, world, local_rank):
         dist.destroy_process_group()
 
 
+def run_halo(args, rank, world, local_rank):
+    """--c2-split halo: configs[1]'s single instance split into N cycle-range
+    shards, one per GPU, each with a 1024-cycle halo (halo.py):
+    strong scaling of one instance.  A step = cs_run on the resident shard
+    (device time, CUDA events), then the exchange: the shard's halo / tail rows
+    and alerts read back (split_device), one all-gather of the tails (a few
+    KB), the halo acceptance check and the alert gather to rank 0.  `value`
+    = the instance's events / max over ranks of the device time; the
+    exchange is reported beside it and is inside `e2e` (wire upload of the
+    shard + step + exchange, wall clock)."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2601_09258_b200 import abi, dist as cdist, halo as hl, runtime as rt
+
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dev, cdev = dist_setup(dist, local_rank)
+    else:
+        dev, cdev = local_rank, f"cuda:{local_rank}"
+    threads = max(1, cpu_cores() // max(1, env_int("LOCAL_WORLD_SIZE", world)))
+
+    def allgather(obj):
+        if not dist:
+            return [obj]
+        out = [None] * world
+        dist.all_gather_object(out, obj)
+        return out
+
+    t_setup = time.time()
+    tr = make_instance(rt, "c2", 7, threads)  # the same instance on every rank
+    ev, wl, names = tr.events, tr.workloads, list(tr.names)
+    n_events = len(ev)
+    span = rt.span_names_mask(ev, len(names))
+    an = rt.Analyzer(dev)
+    an.configure(names, span, n_comm_slots=tr.n_comm)
+    # setup: the whole-trace anchor discovery and the model fit on the first
+    # 2400 cycles, identical on every rank; then the anchor is fixed
+    an.upload(ev, [0, n_events], wl)
+    an.run(abi.RUN_SEGMENT)
+    anchor = int(an.summary(0).anchor_name_id)
+    recs = an.records(0)
+    recs = recs[recs["cycle_index"] < 2400]
+    x = np.stack([recs["batch"].astype(float),
+                  (recs["batch"] * (recs["input_len"] + recs["output_len"])).astype(float)], 1)
+    model = rt.fit_latency_model(x, recs["latency_s"])
+    an.configure(names, span, n_comm_slots=tr.n_comm, run_config={"cycle": {"anchor_hint": names[anchor]}})
+    an.load_model(model)
+    halo = 1024
+    _, specs = hl.plan(ev, anchor, world, halo)
+    spec = specs[rank]
+    loc = np.ascontiguousarray(ev[spec.lo:spec.hi])
+    an.upload(loc, [0, len(loc)], wl)
+    cfg = hl.CheckConfig(stage_window=an.cycle.stage_window, window=an.control.window,
+                         warmup=an.control.warmup)
+    wt = rt.wire_pack(loc, [0, len(loc)], wl, n_threads=threads)
+    if wt.workloads32 is None:
+        raise RuntimeError("configs[1] workloads fit the u32 wire column")
+    cols = [getattr(wt, c) for c in rt.WireTrace.COLUMNS]
+    wire_bytes = sum(a.nbytes for a in cols)
+    wptr, wpin = rt.host_alloc(wire_bytes + 16 * len(cols))  # pinned, as in run_ours
+    views, o = [], 0
+    for a in cols:
+        o = (o + 15) & ~15
+        wpin[o:o + a.nbytes] = a.view(np.uint8).reshape(-1)
+        views.append(wpin[o:o + a.nbytes].view(a.dtype).reshape(a.shape))
+        o += a.nbytes
+    wire = rt.WireTrace(*views, wt.inst_offsets)
+    del tr, wt, cols
+    setup_s = time.time() - t_setup
+
+    def exchange():
+        owned, view, tail = hl.split_device(spec, an, halo)
+        info = allgather((view, tail))
+        ok = all(hl.halo_ok(specs[r], info[r][0], [i[1] for i in info[:r]], cfg) for r in range(world))
+        if not ok:  # the synthetic configs[1] trace has explicit stages: never expected
+            raise RuntimeError("halo rejected; run halo.ShardedRun for the full-prefix fallback")
+        counts = allgather(owned.n_records)
+        payload = owned.alerts.view(np.uint8)
+        got = cdist.gather_bytes(payload, device=cdev) if dist else [payload]
+        return owned, counts, got
+
+    for _ in range(args.warmup):
+        an.run(abi.RUN_ALL)
+        exchange()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    clocks = ClockSampler(dev)
+    clocks.start()
+    time.sleep(0.3)
+    dev_ms, ex_ms, launches = [], [], 0
+    for _ in range(args.steps):
+        an.run(abi.RUN_ALL)
+        dev_ms.append(an.timings()["total"])
+        launches += an.launches()
+        t0 = time.perf_counter()
+        _, _, got = exchange()
+        ex_ms.append((time.perf_counter() - t0) * 1e3)
+    torch.cuda.synchronize(dev)
+    if dist:
+        dist.barrier()
+    clk = clocks.stop()
+    # e2e: the shard's wire columns from host memory each step
+    e2e = []
+    for k in range(args.warmup + args.steps):
+        if dist:
+            dist.barrier()
+        t0 = time.perf_counter()
+        an.upload_wire(wire)
+        an.run(abi.RUN_ALL)
+        _, _, got = exchange()
+        if k >= args.warmup:
+            e2e.append((time.perf_counter() - t0) * 1e3)
+    d_ms, x_ms, e_ms = statistics.median(dev_ms), statistics.median(ex_ms), statistics.median(e2e)
+    if dist:
+        d_ms = cdist.max_over_ranks(d_ms, device=cdev)
+        x_ms = cdist.max_over_ranks(x_ms, device=cdev)
+        e_ms = cdist.max_over_ranks(e_ms, device=cdev)
+    n_alerts = sum(len(g) // abi.ALERT_DTYPE.itemsize for g in got) if got else 0
+    # split_device's reads: halo + tail cycle and record rows, summary, alerts
+    d2h = (2 * halo * (abi.CYCLE_DTYPE.itemsize + abi.RECORD_DTYPE.itemsize)
+           + C.sizeof(abi.InstanceSummary) + n_alerts * abi.ALERT_DTYPE.itemsize)
+    rt.host_free(wptr)
+    line = {
+        "metric": METRIC, "value": n_events / (d_ms * 1e-3), "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": d_ms, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "int64+f64",
+        "data": "synthetic (simkit restatement, byte-identical to the reference generator per chunk)",
+        "config": {"workload": WORKLOADS["c2"][6] + "; one instance split into cycle-range shards",
+                   "events_total": n_events, "events_this_rank": int(len(loc)), "halo_cycles": halo,
+                   "parallelism": f"cycle-range shards x{world} with a verified halo",
+                   "l2": "inputs larger than L2; no flush needed", "setup_s": round(setup_s, 1)},
+        "exchange_ms": x_ms,
+        "e2e": {"value": n_events / (e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": wire_bytes,
+                "d2h_bytes_per_step": d2h, "ms_per_step": e_ms,
+                "input": "the shard's columnar wire format from host memory (cs_upload_wire)",
+                "timer": "host wall clock: upload + cs_run + exchange + alert gather"},
+        "gpu_launches": launches, "clocks": clk, "alerts_per_step": n_alerts,
+    }
+    if rank == 0:
+        print(json.dumps(line))
+    an.close()
+    if dist:
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -650,6 +799,9 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--c2-split", choices=["replicas", "halo"], default="replicas",
+                    help="N > 1 on configs[1]: N independent instances (default) or one "
+                         "instance split into cycle-range shards with a verified halo")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     rank = env_int("RANK", 0)
@@ -659,6 +811,8 @@ def main():
         run_reference(args, rank, world)
     elif args.workload == "c5":
         run_stream(args, rank, world, local_rank)
+    elif args.workload == "c2" and args.c2_split == "halo":
+        run_halo(args, rank, world, local_rank)
     else:
         run_ours(args, rank, world, local_rank)
 
