@@ -382,35 +382,24 @@ class ShardedRun:
         spec = specs[self.rank]
         tail_n = max(self.halo, 1)
         owned, view, tail = split(spec, analyze(spec), tail_n)
-        accepted = [False] * self.world
         while True:
-            info = allgather((spec, view, tail, accepted[self.rank]))
+            info = allgather((spec, view, tail))
             specs = [i[0] for i in info]
             views = [i[1] for i in info]
             tails = [i[2] for i in info]
-            # acceptance chain, left to right
-            acc = [False] * self.world
-            for r in range(self.world):
-                ok = halo_ok(specs[r], views[r], tails[:r], self.cfg)
-                acc[r] = ok and (r == 0 or acc[r - 1])
-                if not acc[r]:
-                    break
-            if all(acc):
+            # acceptance chain, left to right: the first shard whose halo
+            # fails against its accepted predecessors re-runs with the halo
+            # reaching the start of the trace (exact), then the chain is
+            # re-checked against its new tail (at most `world` rounds)
+            first = next((r for r in range(self.world)
+                          if not halo_ok(specs[r], views[r], tails[:r], self.cfg)), None)
+            if first is None:
                 return owned, specs
-            first = acc.index(False)
-            if not halo_ok(specs[first], views[first], tails[:first], self.cfg) and self.rank == first:
-                # re-run this shard with the halo reaching the start of the trace
+            if self.rank == first:
                 pos = anchor_positions(self.events, self.anchor)
                 spec = shard_spec(self.events, pos, self.rank, spec.c0, spec.c1, None)
                 self.reruns.append(self.rank)
                 owned, view, tail = split(spec, analyze(spec), tail_n)
-            elif self.rank == first:
-                raise RuntimeError("halo acceptance chain stalled")
-
-
-def local_allgather(objs_by_rank):
-    """In-process all-gather for running every shard in one process."""
-    return objs_by_rank
 
 
 def run_all_in_process(events, anchor, world, cfg, analyze_at, halo=1024):

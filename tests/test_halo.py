@@ -139,13 +139,13 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, heuristic, halo):
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        ev, names, wl, n_comm, span = _trace(n_cycles=2000, seed=13)
+        ev, names, wl, n_comm, span = _trace(n_cycles=2000, seed=13, heuristic=heuristic)
         model = _model(ev, names, wl, n_comm, span)
 
         def allgather(obj):
@@ -153,13 +153,15 @@ def _worker(rank, world, port, q):
             dist.all_gather_object(out, obj)
             return out
 
-        run = hl.ShardedRun(ev, names.index("run_batch"), world, rank, _cfg(), halo=200)
+        run = hl.ShardedRun(ev, names.index("run_batch"), world, rank, _cfg(), halo=halo)
         owned, specs = run.run(_oracle_at(ev, names, wl, n_comm, span, model), allgather)
         parts = allgather(owned)
         if rank == 0:
             whole = csoracle.analyze(ev, names, wl, n_comm, RUN_CONFIG, model, span=span)
             _check_equal(whole, hl.merge(parts))
-            q.put(("ok", len(whole["alerts"]), run.reruns))
+            q.put(("ok", len(whole["alerts"]), allgather(run.reruns)))
+        else:
+            allgather(run.reruns)
     except Exception as e:  # surface the failure to the parent
         q.put(("error", repr(e), None))
         raise
@@ -167,16 +169,18 @@ def _worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-def test_sharded_run_world2_gloo():
+@pytest.mark.parametrize("heuristic,halo,want_reruns", [(False, 200, [[], []]), (True, 16, [[], [1]])],
+                         ids=["accepted", "rerun"])
+def test_sharded_run_world2_gloo(heuristic, halo, want_reruns):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q, heuristic, halo)) for r in range(2)]
     for p in procs:
         p.start()
     status, n_alerts, reruns = q.get(timeout=300)
     for p in procs:
         p.join(timeout=60)
     assert status == "ok", n_alerts
-    assert reruns == []
+    assert reruns == want_reruns
     assert all(p.exitcode == 0 for p in procs)
