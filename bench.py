@@ -21,7 +21,9 @@ same through the public C ABI with host buffers: H2D of the step's events
 from pinned memory + cs_run + D2H of alerts and summary.
 N > 1: one process per GPU, each analysing its own instance (instances shard
 with no data-path collective: "weak" scaling); the per-shard alert lists and
-summaries are gathered to rank 0 over NCCL.
+summaries are gathered to rank 0 over NCCL.  `--c2-split halo` instead splits
+configs[1]'s one instance into N cycle-range shards with a verified halo
+(halo.py; "strong" scaling; one all-gather of shard tails per step).
 """
 from __future__ import annotations
 
