@@ -601,7 +601,7 @@ def run_stream(args, rank, world, local_rank):
     hoff = np.zeros(n_inst + 1, np.uint64)
     hoff[1:] = np.cumsum([cuts[i % n_distinct][0] for i in range(n_inst)])
     st.push_packed(head, hoff, wl)  # history up to the first slice (uploads the workload table)
-    lat, n_ev, n_alerts = [], 0, 0
+    lat, n_ev, n_alerts, launches, dev_ms = [], 0, 0, 0, []
     torch.cuda.synchronize(dev)
     for k, (ev, off) in enumerate(batches):
         if dist:
@@ -613,6 +613,8 @@ def run_stream(args, rank, world, local_rank):
             lat.append(el * 1e3)
             n_ev += len(ev)
             n_alerts += len(al)
+            launches += an.launches()
+            dev_ms.append(an.timings()["total"])
     phase_ms = {k: round(v, 4) for k, v in an.timings().items()}  # device phases of the last slice
     st.close()
     del batches
@@ -636,6 +638,13 @@ def run_stream(args, rank, world, local_rank):
                        "timer": "host wall clock: events on host -> alerts on host"},
         "alerts": n_alerts,
         "device_phase_ms_last_slice": phase_ms,
+        "device_ms_per_slice_median": statistics.median(dev_ms),
+        # the line is already measured host to host through cs_stream_push
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": int(32 * n_ev / len(lat)),
+                "d2h_bytes_per_step": int(abi.ALERT_DTYPE.itemsize * n_alerts / len(lat)),
+                "ms_per_step": sum(lat) / len(lat),
+                "input": "each slice's 32-B events in pinned host memory (cs_stream_push)"},
+        "gpu_launches": launches,
     }
     if rank == 0:
         print(json.dumps(line))

@@ -10,6 +10,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <new>
 #include <array>
 #include <cmath>
@@ -35,6 +38,29 @@ struct NvtxScope {
   ~NvtxScope() { nvtxRangePop(); }
 };
 #define CS_NVTX_SCOPE(name) NvtxScope nvtx_scope_(name)
+
+// CS_HOST_PROFILE=1: host-side phase times of each push on stderr (tools) and of each cs_run
+struct HostPhases {
+  const char* label;
+  bool on = false;
+  std::chrono::steady_clock::time_point t0;
+  std::string line;
+  explicit HostPhases(const char* l) : label(l) {
+    const char* e = std::getenv("CS_HOST_PROFILE");
+    on = e && *e == '1';
+    if (on) t0 = std::chrono::steady_clock::now();
+  }
+  void mark(const char* name) {
+    if (!on) return;
+    const auto t = std::chrono::steady_clock::now();
+    line += std::string(name) + "=" +
+            std::to_string(std::chrono::duration<double, std::micro>(t - t0).count()) + " ";
+  }
+  ~HostPhases() {
+    if (on) std::fprintf(stderr, "%s_us %s\n", label, line.c_str());
+  }
+};
+
 
 namespace {
 
@@ -856,6 +882,7 @@ int frequency_plan(cs_ctx* ctx, uint32_t i, int64_t* t0, int64_t* period, uint64
 extern "C" {
 
 static int cs_run_impl(cs_ctx* ctx, uint32_t mask) {
+  HostPhases hp("cs_run");
   if (!ctx) return CS_E_INVALID_ARGUMENT;
   NvtxRun nvtx_run(ctx);
   if (mask & CS_RUN_MU) mask |= CS_RUN_BETA;  // mu divides by the class totals
@@ -1057,7 +1084,9 @@ static int cs_run_impl(cs_ctx* ctx, uint32_t mask) {
   ctx->timed.push_back({"prefix_rank", {e2, e9}});
   CS_CUDA(cudaMemcpyAsync(ctx->h_inst.data(), d_inst, n_inst * sizeof(InstState),
                           cudaMemcpyDeviceToHost, s));
+  hp.mark("scan_issued");
   CS_CUDA(cudaStreamSynchronize(s));
+  hp.mark("scan_sync");
   CS_CUDA(cudaGetLastError());  // launch failures surface here, not as bad counts
 
   // ---- rare paths: ordered fold for uncertified rankings
@@ -1293,7 +1322,9 @@ static int cs_run_impl(cs_ctx* ctx, uint32_t mask) {
                             cudaMemcpyDeviceToHost, s));
   CS_CUDA(cudaMemcpyAsync(ctx->rec_off.data(), ctx->d_rec_off.p, (n_inst + 1) * 8,
                           cudaMemcpyDeviceToHost, s));
+  hp.mark("all_issued");
   CS_CUDA(cudaStreamSynchronize(s));
+  hp.mark("final_sync");
   CS_CUDA(cudaGetLastError());
   ctx->n_records = ctx->rec_off[n_inst];
   for (uint32_t i = 0; i < n_inst; ++i)
@@ -1347,6 +1378,7 @@ int cs_stream_tail(cs_ctx* ctx, uint32_t inst, uint64_t* keep_from) {
 static int cs_stream_push_impl(cs_ctx* ctx, uint32_t n_inst, const uint64_t* offsets, const cs_event* ev,
                    uint64_t n_workloads, const cs_workload* wl, uint32_t mask, cs_alert* alerts,
                    size_t cap, size_t* n_alerts) {
+  HostPhases hp("cs_stream_push");
   if (!ctx || !offsets || n_inst == 0) return CS_E_INVALID_ARGUMENT;
   if (!ctx->streaming) return fail(ctx, CS_E_INVALID_ARGUMENT, "not streaming (cs_stream_begin)");
   if (offsets[0] != 0) return fail(ctx, CS_E_INVALID_ARGUMENT, "offsets[0] must be 0");
@@ -1372,8 +1404,10 @@ static int cs_stream_push_impl(cs_ctx* ctx, uint32_t n_inst, const uint64_t* off
   // new batch is assembled on the device from them and the uploaded events
   std::swap(ctx->d_ev.p, ctx->d_ev_prev.p);
   std::swap(ctx->d_ev.cap, ctx->d_ev_prev.cap);
+  hp.mark("pre");
   int rc = upload_layout(ctx, n_inst, ctx->stage_off.data(), true, n_workloads, wl);
   if (rc != CS_OK) return rc;
+  hp.mark("layout");
   auto* d_new = dev<cs_event>(ctx->d_new_ev, std::max<uint64_t>(1, n_new));
   auto* d_meta = dev<uint64_t>(ctx->d_assemble, 4ull * n_inst);
   if (!d_new || !d_meta) return fail(ctx, CS_E_CUDA, "cudaMalloc(stream)");
@@ -1391,8 +1425,10 @@ static int cs_stream_push_impl(cs_ctx* ctx, uint32_t n_inst, const uint64_t* off
   launch_stream_assemble(static_cast<const cs_event*>(ctx->d_ev_prev.p), d_new, d_meta, n_inst,
                          ctx->stage_off[n_inst], static_cast<cs_event*>(ctx->d_ev.p), ctx->stream);
   CS_CUDA(cudaGetLastError());
+  hp.mark("copy_assemble");
   rc = cs_run(ctx, mask);
   if (rc != CS_OK) return rc;
+  hp.mark("run");
   // new tails: everything from the last closed cycle's end (cycles.cpp:147)
   auto* dk = dev<uint64_t>(ctx->d_keep, n_inst);
   if (!dk) return fail(ctx, CS_E_CUDA, "cudaMalloc(keep)");
@@ -1417,7 +1453,9 @@ static int cs_stream_push_impl(cs_ctx* ctx, uint32_t n_inst, const uint64_t* off
     CS_CUDA(cudaMemcpyAsync(all.data(), d, n_all * sizeof(cs_alert), cudaMemcpyDeviceToHost,
                             ctx->stream));
   }
+  hp.mark("alerts_issued");
   CS_CUDA(cudaStreamSynchronize(ctx->stream));
+  hp.mark("sync");
   for (uint32_t i = 0; i < n_inst && det; ++i) {
     // monitor_loop stops at the first NonPositiveLatency (main.cpp:162)
     const uint64_t bad = ctx->h_inst[i].first_bad_record;
@@ -1434,6 +1472,7 @@ static int cs_stream_push_impl(cs_ctx* ctx, uint32_t n_inst, const uint64_t* off
     ctx->tail_len[i] = len - k;
   }
   ctx->tails_on_device = true;
+  hp.mark("end");
   if (n_alerts) *n_alerts = na;
   if (alerts && na > cap) return fail(ctx, CS_E_INVALID_ARGUMENT, "alert buffer too small");
   return CS_OK;

@@ -888,7 +888,11 @@ class Stream:
                     max_alerts: int = 1 << 16) -> np.ndarray:
         """push_native with the batch already concatenated (ev, per-instance offsets)."""
         wl = None if workloads is None else np.ascontiguousarray(workloads, dtype=abi.WORKLOAD_DTYPE)
-        out = np.zeros(max_alerts, abi.ALERT_DTYPE)
+        # one alert buffer per stream, reused (a fresh 5 MB zeroed array per
+        # push cost ~0.2 ms of a ~0.55 ms micro-batch)
+        out = getattr(self, "_alert_buf", None)
+        if out is None or len(out) < max_alerts:
+            out = self._alert_buf = np.empty(max_alerts, abi.ALERT_DTYPE)
         n = C.c_size_t()
         _check(lib().cs_stream_push(self.an.h, len(off) - 1, off.ctypes.data, _ptr(ev) or None,
                                     0 if wl is None else len(wl), _ptr(wl), mask, _ptr(out),
