@@ -221,6 +221,7 @@ struct cs_ctx {
   int stream_cur = 0;
   DevBuf d_stream[2];
   pinned_vector<StreamCarry> h_stream;   // carry in force for the last batch
+  pinned_vector<uint64_t> h_cyc_stage;   // pinned staging of cycle-table reads
   std::vector<uint32_t> stream_anchor;   // per instance, fixed after first batch
 
   ~cs_ctx() {
@@ -1587,21 +1588,38 @@ int cs_get_cycle_range(cs_ctx* ctx, uint32_t inst, uint64_t first, uint64_t coun
 }
 
 static int cycles_to_host(cs_ctx* ctx, uint32_t inst, uint64_t first, uint64_t nc, cs_cycle* buf) {
+  if (!nc) return CS_OK;
   const uint64_t c0 = ctx->cyc_off[inst] + first;
-  std::vector<int64_t> st, en, ae;
-  std::vector<uint64_t> ap, fi, la;
-  std::vector<uint8_t> sg;
-  std::vector<int32_t> wl;
-  int rc;
-  if ((rc = d2h(ctx, st, ctx->c_start, c0, nc)) || (rc = d2h(ctx, en, ctx->c_end, c0, nc)) ||
-      (rc = d2h(ctx, ae, ctx->c_aend, c0, nc)) || (rc = d2h(ctx, ap, ctx->c_apos, c0, nc)) ||
-      (rc = d2h(ctx, fi, ctx->c_first, c0, nc)) || (rc = d2h(ctx, la, ctx->c_last, c0, nc)) ||
-      (rc = d2h(ctx, sg, ctx->c_stage, c0, nc)) || (rc = d2h(ctx, wl, ctx->c_wl, c0, nc)))
-    return rc;
+  // the eight columns land in one pinned staging area: async copies on the
+  // ctx stream and one synchronize (pageable copies would each round-trip)
+  ctx->h_cyc_stage.resize(7 * nc + (nc + 7) / 8 + 1);
+  uint64_t* base = ctx->h_cyc_stage.data();
+  auto* st = reinterpret_cast<int64_t*>(base);
+  int64_t* en = st + nc;
+  int64_t* ae = en + nc;
+  auto* ap = reinterpret_cast<uint64_t*>(ae + nc);
+  uint64_t* fi = ap + nc;
+  uint64_t* la = fi + nc;
+  auto* wl = reinterpret_cast<int32_t*>(la + nc);
+  auto* sg = reinterpret_cast<uint8_t*>(wl + nc);
+  auto col = [&](void* dst, const DevBuf& src, size_t elem) {
+    return cudaMemcpyAsync(dst, static_cast<const uint8_t*>(src.p) + c0 * elem, nc * elem,
+                           cudaMemcpyDeviceToHost, ctx->stream);
+  };
+  CS_CUDA(col(st, ctx->c_start, 8));
+  CS_CUDA(col(en, ctx->c_end, 8));
+  CS_CUDA(col(ae, ctx->c_aend, 8));
+  CS_CUDA(col(ap, ctx->c_apos, 8));
+  CS_CUDA(col(fi, ctx->c_first, 8));
+  CS_CUDA(col(la, ctx->c_last, 8));
+  CS_CUDA(col(wl, ctx->c_wl, 4));
+  CS_CUDA(col(sg, ctx->c_stage, 1));
+  CS_CUDA(cudaStreamSynchronize(ctx->stream));
   const uint64_t ib = ctx->inst_off[inst];
+  const uint64_t idx0 = first + (ctx->streaming ? ctx->h_stream[inst].cycle_off : 0);
   for (uint64_t k = 0; k < nc; ++k) {
     cs_cycle& c = buf[k];
-    c.index = first + k + (ctx->streaming ? ctx->h_stream[inst].cycle_off : 0);
+    c.index = idx0 + k;
     c.start_ts = st[k];
     c.end_ts = en[k];
     c.anchor_pos = ap[k] == UINT64_MAX ? UINT64_MAX : ap[k] - ib;
@@ -1845,6 +1863,11 @@ int cs_get_alerts(cs_ctx* ctx, uint32_t inst, cs_alert* buf, size_t cap, size_t*
   if (!ctx || !ctx->ran || inst >= ctx->n_inst) return CS_E_INVALID_ARGUMENT;
   if (!(ctx->last_mask & CS_RUN_DETECT)) return fail(ctx, CS_E_INVALID_ARGUMENT, "detect not run");
   const uint64_t a0 = ctx->alert_off[inst], na_all = ctx->alert_off[inst + 1] - a0;
+  const uint64_t bad = ctx->h_inst[inst].first_bad_record;
+  if (!buf && bad == UINT64_MAX) {  // a count query: no truncation to apply
+    if (n) *n = na_all;
+    return CS_OK;
+  }
   std::vector<cs_alert> all(na_all);
   if (na_all) {
     auto* d = dev<cs_alert>(ctx->d_scratch, na_all);
@@ -1856,7 +1879,6 @@ int cs_get_alerts(cs_ctx* ctx, uint32_t inst, cs_alert* buf, size_t cap, size_t*
     CS_CUDA(cudaStreamSynchronize(ctx->stream));
   }
   // monitor_loop stops at the first NonPositiveLatency (main.cpp:162)
-  const uint64_t bad = ctx->h_inst[inst].first_bad_record;
   uint64_t na = 0;
   while (na < na_all && all[na].record_index < bad) ++na;
   if (n) *n = na;
