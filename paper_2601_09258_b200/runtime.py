@@ -827,6 +827,38 @@ def host_free(ptr: int):
     lib().cs_host_free(C.c_void_p(ptr))
 
 
+def pool_strategy_metrics(per_trial) -> np.ndarray:
+    """evaluate_suite's aggregate (simkit.cpp:1038-1068): confusion counts
+    pooled over trials per strategy, precision / recall / F1 / FPR from the
+    pooled counts, mean lag averaged over trials (in trial order).
+
+    per_trial: per trial, 3 rows (strategies in order) of
+    [tp, fp, fn, tn, alerts, ..., mean_lag] — StrategyMetrics or array rows
+    with mean_lag last.  Returns (3, 10) float64:
+    [tp, fp, fn, tn, alerts, precision, recall, f1, fpr, mean_lag]."""
+    out = np.zeros((3, 10), np.float64)
+    n = len(per_trial)
+    for s in range(3):
+        tp = fp = fn = tn = alerts = 0
+        lag_sum = 0.0
+        for rows in per_trial:
+            m = rows[s]
+            if isinstance(m, abi.StrategyMetrics):
+                v = (m.tp, m.fp, m.fn, m.tn, m.alerts, m.mean_lag)
+            else:
+                v = (int(m[0]), int(m[1]), int(m[2]), int(m[3]), int(m[4]), float(m[-1]))
+            tp, fp, fn, tn, alerts = tp + v[0], fp + v[1], fn + v[2], tn + v[3], alerts + v[4]
+            lag_sum += v[5]
+        tpf, fpf, fnf, tnf = float(tp), float(fp), float(fn), float(tn)
+        precision = tpf / (tpf + fpf) if tpf + fpf > 0.0 else 0.0
+        recall = tpf / (tpf + fnf) if tpf + fnf > 0.0 else 0.0
+        f1 = 2.0 * precision * recall / (precision + recall) if precision + recall > 0.0 else 0.0
+        fpr = fpf / (fpf + tnf) if fpf + tnf > 0.0 else 0.0
+        lag = lag_sum / float(n) if n else 0.0
+        out[s] = [tp, fp, fn, tn, alerts, precision, recall, f1, fpr, lag]
+    return out
+
+
 def alerts_to_ndjson(alerts: np.ndarray, pre_roll: int = 5, post_roll: int = 20) -> str:
     """monitor_loop's NDJSON alert sink incl. escalation (main.cpp:151-177)."""
     a = np.ascontiguousarray(alerts, dtype=abi.ALERT_DTYPE)

@@ -83,3 +83,69 @@ def test_ndjson_alert_sink_matches_monitor_loop(refbridge, analyzer, rt, family,
     text = rt.alerts_to_ndjson(got.alerts, 5, 20)
     assert text == ref.extra["ndjson"]
     assert len(text.splitlines()) == len(ref.alerts) >= 1
+
+
+def suite_metrics(refbridge, rt, an, n_trials=20, timer=None):
+    """BASELINE config 4 end to end: every SuiteConfig{} trial segmented on the
+    device, the 20 latency models fitted in one device batch
+    (cs_fit_latency_models), monitored from cycle 2400 under the three
+    strategies, pooled as evaluate_suite does.  Returns (ours, reference)
+    per-trial metric rows and the trials the reference's own gate skipped."""
+    import time
+    tick = timer if timer is not None else {}
+    prepared, ref_rows, skipped = [], [], []
+    for trial in range(n_trials):
+        t = refbridge.RefTrace.trial(trial)
+        t0 = time.perf_counter()
+        try:
+            ref = t.evaluate_trial(trial)
+        except RuntimeError:
+            skipped.append(trial)
+            continue
+        tick["reference_s"] = tick.get("reference_s", 0.0) + time.perf_counter() - t0
+        prepared.append((trial, t.export(), t.labels().astype(np.uint8)))
+        ref_rows.append(ref)
+    t0 = time.perf_counter()
+    xs, ys, cfgs = [], [], []
+    for _, ex, _ in prepared:
+        span = rt.span_names_mask(ex.events, len(ex.names))
+        cyc, ctl, table = rt.configs_from_json({}, ex.names, span, len(ex.comm_hash))
+        an.set_config(cyc, ctl)
+        an.set_name_table(table)
+        an.upload(ex.events, [0, len(ex.events)], ex.workloads)
+        an.run(abi.RUN_SEGMENT)
+        recs = an.records(0)
+        tr = recs[recs["cycle_index"] < 2400]
+        xs.append(np.stack([tr["batch"].astype(float),
+                            (tr["batch"] * (tr["input_len"] + tr["output_len"])).astype(float)], 1))
+        ys.append(tr["latency_s"])
+        cfgs.append((cyc, ctl, table))
+    models, _ = rt.fit_latency_models(xs, ys)
+    ours = []
+    for (_, ex, labels), model, (cyc, ctl, table) in zip(prepared, models, cfgs):
+        cyc.monitor_from_cycle = 2400
+        an.set_config(cyc, ctl)
+        an.set_name_table(table)
+        an.upload(ex.events, [0, len(ex.events)], ex.workloads)
+        an.load_model(model)
+        an.run(abi.RUN_ALL)
+        rows = []
+        for strategy in (abi.FIXED_POINT, abi.FIXED_WINDOW, abi.DYNAMIC_WINDOW):
+            an.redetect(abi.default_control(strategy))
+            rows.append(an.evaluate_strategy(labels))
+        ours.append(rows)
+    tick["ours_s"] = time.perf_counter() - t0
+    return ours, ref_rows, skipped
+
+
+def test_config4_suite_aggregate_equals_reference(refbridge, analyzer, rt):
+    analyzer.set_fused(False)
+    ours, ref_rows, skipped = suite_metrics(refbridge, rt, analyzer)
+    assert len(ours) + len(skipped) == 20 and len(ours) >= 16
+    for o, r in zip(ours, ref_rows):
+        assert [[m.tp, m.fp, m.fn, m.tn, m.alerts] for m in o] == r[:, :5].astype(int).tolist()
+    got = rt.pool_strategy_metrics(ours)
+    want = rt.pool_strategy_metrics(ref_rows)
+    assert np.array_equal(got.view(np.uint64), want.view(np.uint64))
+    # the suite's Dynamic Window strategy detects (SURVEY §8d C4: F1 0.972)
+    assert got[2, 7] > 0.9

@@ -87,3 +87,16 @@ def test_welch_p_value_edges():
     assert rt.welch_p_value(1.0, 0.0, 5, 2.0, 0.0, 5) == 0.0
     p = rt.welch_p_value(0.30, 0.01, 40, 0.25, 0.012, 300)
     assert 0.0 < p < 0.01
+
+
+def test_pool_strategy_metrics_matches_evaluate_suite_arithmetic():
+    # two trials x three strategies: [tp, fp, fn, tn, alerts, f1, fpr, lag]
+    from paper_2601_09258_b200 import runtime as rt
+    t1 = np.array([[10, 2, 1, 100, 1, 0, 0, 1.5], [0, 0, 5, 80, 0, 0, 0, 0.0], [3, 1, 0, 50, 2, 0, 0, 0.25]], float)
+    t2 = np.array([[5, 0, 3, 90, 1, 0, 0, 2.0], [1, 1, 1, 1, 1, 0, 0, 4.0], [0, 0, 0, 60, 0, 0, 0, 0.0]], float)
+    got = rt.pool_strategy_metrics([t1, t2])
+    tp, fp, fn, tn = 15.0, 2.0, 4.0, 190.0
+    p, r = tp / (tp + fp), tp / (tp + fn)
+    assert got[0].tolist() == [15, 2, 4, 190, 2, p, r, 2.0 * p * r / (p + r), fp / (fp + tn), (1.5 + 2.0) / 2.0]
+    assert got[1, 5] == 0.5 and got[1, 6] == 1.0 / 7.0   # tp=1 fp=1 fn=6
+    assert got[2, 0] == 3 and got[2, 8] == 1.0 / 111.0
