@@ -3,10 +3,13 @@
 # dominant kernels' DRAM traffic (profiles/r1_ncu_traffic.json, read by bench.py).
 set -e
 cd "$(dirname "$0")/.."
-for f in bench:r1_bench_c2 bench_ref:r1_bench_ref bench_c3:r1_bench_c3 bench_c5:r1_bench_c5; do
+for f in bench:r1_bench_c2 bench_ref:r1_bench_ref bench_c3:r1_bench_c3 bench_c5:r1_bench_c5 \
+         bench_c1:r1_bench_c1 bench_c1_ref:r1_bench_c1_ref bench_c2_halo:r1_bench_c2_halo_n1; do
   tail -1 gpurun_out/${f%%:*}.log > profiles/${f##*:}.json
 done
 cp gpurun_out/fit_bench.json profiles/r1_fit_bench.json
+cp gpurun_out/halo_bench.json profiles/r1_halo_bench.json
+cp gpurun_out/suite_bench.json profiles/r1_suite_bench.json
 cp gpurun_out/ingest_bench.json profiles/r1_ingest_bench.json
 cp gpurun_out/launches.csv profiles/r1_launches.csv
 python tools/tools_launches.py gpurun_out/launches.csv > profiles/r1_launches_summary.txt
