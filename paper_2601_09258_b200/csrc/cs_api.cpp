@@ -201,6 +201,15 @@ struct cs_ctx {
   }
   DevBuf d_models;
   std::vector<DevModel> h_models;
+  // the per-instance model table on the device is rebuilt only when what it
+  // is made of changes: the instance -> model binding, a model load (model_gen)
+  // or the control config (cs_redetect also invalidates it)
+  uint64_t model_gen = 0;
+  bool mt_valid = false;
+  uint64_t mt_gen = 0;
+  uint32_t mt_n_inst = 0;
+  cs_control_config mt_ctl{};
+  std::vector<int> mt_ids;
   // fold results per instance: name -> (mean, cv, score)
   std::vector<std::map<uint32_t, std::array<double, 3>>> folded;
   std::vector<int> inst_status;
@@ -788,6 +797,7 @@ static int cs_load_model_impl(cs_ctx* ctx, uint32_t inst, const cs_model* m) {
     }
   }
   ctx->model_store.push_back(pm);
+  ++ctx->model_gen;
   const int id = static_cast<int>(ctx->model_store.size() - 1);
   if (inst == UINT32_MAX) {
     ctx->default_model = id;
@@ -1242,6 +1252,12 @@ static int cs_run_impl(cs_ctx* ctx, uint32_t mask) {
   int last = e6;
   // ---- score + detect
   if (mask & (CS_RUN_SCORE | CS_RUN_DETECT)) {
+    bool reuse = ctx->mt_valid && ctx->mt_gen == ctx->model_gen && ctx->mt_n_inst == n_inst &&
+                 ctx->h_models.size() == n_inst &&
+                 std::memcmp(&ctx->mt_ctl, &ctx->ctl, sizeof(cs_control_config)) == 0;
+    for (uint32_t i = 0; i < n_inst && reuse; ++i) reuse = ctx->mt_ids[i] == ctx->model_id(i);
+    if (!reuse) {
+    ctx->mt_valid = false;
     ctx->h_models.assign(n_inst, DevModel{});
     uint32_t nf0 = UINT32_MAX;
     for (uint32_t i = 0; i < n_inst; ++i) {
@@ -1290,6 +1306,13 @@ static int cs_run_impl(cs_ctx* ctx, uint32_t mask) {
     }
     std::memcpy(ctx->pin_models, ctx->h_models.data(), mbytes);
     CS_CUDA(cudaMemcpyAsync(dm, ctx->pin_models, mbytes, cudaMemcpyHostToDevice, s));
+    ctx->mt_ids.resize(n_inst);
+    for (uint32_t i = 0; i < n_inst; ++i) ctx->mt_ids[i] = ctx->model_id(i);
+    ctx->mt_gen = ctx->model_gen;
+    ctx->mt_n_inst = n_inst;
+    ctx->mt_ctl = ctx->ctl;
+    ctx->mt_valid = true;
+    }  // rebuild
     b = make_buffers(ctx);
     if (!dev<uint64_t>(ctx->block_tmp, rec_cap / 1024 + 16))
       return fail(ctx, CS_E_CUDA, "cudaMalloc(block_tmp)");
@@ -1898,6 +1921,7 @@ int cs_redetect(cs_ctx* ctx, const cs_control_config* control) {
   CS_CUDA(cudaSetDevice(ctx->device));
   cudaStream_t s = ctx->stream;
   ctx->ctl = *control;
+  ctx->mt_valid = false;  // the table below gets this config's limits
   const uint32_t n_inst = ctx->n_inst;
   for (uint32_t i = 0; i < n_inst; ++i) {
     const PackedModel* pm = ctx->model_store[ctx->model_id(i)];
