@@ -287,6 +287,23 @@ int cs_upload(cs_ctx* ctx, uint32_t n_inst, const uint64_t* inst_offsets,
               const cs_event* ev, uint64_t n_workloads, const cs_workload* wl);
 /* (n_workloads = 0 with wl = NULL keeps the previously uploaded workload table.) */
 
+/* K0: canonical order on the device (Trace::sort_events, trace.cpp:103-105).
+ * cs_upload / cs_upload_wire / cs_stream_push take events already in the
+ * reference's canonical order (start_ts, event_id) per instance; cs_run
+ * verifies it inside its first event pass (trace.cpp:107-109 is_sorted) and
+ * returns CS_E_INVALID_ARGUMENT when an instance's start_ts ever decreases,
+ * instead of producing wrong cycles.  cs_upload_unsorted accepts any order:
+ * every instance's events are stably sorted on the device by (start_ts,
+ * event_id) (event_ids NULL: the input position breaks ties, i.e. ids ascend
+ * in input order), exactly the order sort_events gives.  All indices returned
+ * afterwards (first_event, last_event, anchor_pos, ...) are canonical
+ * positions; cs_get_order maps them back: buf[k] = the input position (within
+ * the instance) of canonical position k. */
+int cs_upload_unsorted(cs_ctx* ctx, uint32_t n_inst, const uint64_t* inst_offsets,
+                       const cs_event* ev, const uint64_t* event_ids, uint64_t n_workloads,
+                       const cs_workload* wl);
+int cs_get_order(cs_ctx* ctx, uint32_t inst, uint64_t* buf, size_t cap, size_t* n);
+
 /* ------------------------------------------------- wire format (host link)
  * Columnar wire format for the host->device leg: the H2D copy is what bounds
  * an end-to-end run, so the producer (ingest / collector) emits this instead
@@ -601,11 +618,14 @@ int cs_stream_push(cs_ctx* ctx, uint32_t n_inst, const uint64_t* offsets, const 
                    uint64_t n_workloads, const cs_workload* wl, uint32_t stage_mask,
                    cs_alert* alerts, size_t cap, size_t* n_alerts);
 
-/* Execution options.  CS_OPT_FUSED (default 0): 1 selects the single-pass
- * fused segmentation kernel (k_fused_segment) when applicable; 0 runs the
- * two-pass path (TMA-staged scan + thread-per-cycle reduce), currently the
- * faster one.  Both are bit-identical; the tests run both. */
+/* Execution options.  CS_OPT_FUSED: 1 selects the single-read segmentation
+ * pass when applicable, 0 the two-pass path (warp-streaming event scan +
+ * thread-per-cycle reduce).  Both are bit-identical; the tests run both. */
 #define CS_OPT_FUSED 1
+/* CS_OPT_TRAVERSAL (default 0): 1 scores every model by tree traversal
+ * (k_score) even where a compiled cell table exists (k_score_lut); both are
+ * bit-identical to GbdtModel::predict, the tests run both. */
+#define CS_OPT_TRAVERSAL 2
 int cs_set_option(cs_ctx* ctx, int option, int64_t value);
 
 /* HBM read-streaming microbenchmark (profiling only).

@@ -165,6 +165,10 @@ struct cs_ctx {
   std::vector<uint64_t> tail_start, tail_len;
   bool tails_on_device = false;
   DevBuf d_ev_prev, d_new_ev, d_assemble;
+  // K0 (cs_upload_unsorted): unsorted input, event ids, radix-sort scratch and
+  // the canonical -> input position map of the last sorted upload
+  DevBuf d_sort_in, d_sort_ids, d_sort_scratch, d_sort_hist, d_sort_hist_tmp, d_sort_ext, d_order;
+  bool have_order = false;
   void* pin_models = nullptr;  // pinned staging of the per-instance DevModel array
   size_t pin_models_cap = 0;
   std::vector<uint64_t> stage_off, assemble_host;
@@ -177,13 +181,10 @@ struct cs_ctx {
   // cycles
   pinned_vector<uint64_t> cyc_off;   // cycle-slot base per instance (+ total)
   std::vector<uint64_t> n_cyc;     // cycles per instance
-  uint64_t n_cycles = 0;           // cycle slots (fused path: + one hole per instance)
-  uint64_t slot_cap = 0;
-  bool allow_fused = false;  // two-pass path is faster today
-  int fused_debug = 0;
+  uint64_t n_cycles = 0;           // cycle slots
   int reduce_variant = 0;  // profiling hook (single variant today)
-  bool used_fused = false;
-  DevBuf d_fstate, d_fticket, d_fcnt, d_fpref, d_fixlist, d_fixn, d_fixflags, d_foverflow;
+  bool allow_fused = false;  // CS_OPT_FUSED
+  bool no_lut = false;       // CS_OPT_TRAVERSAL: score by tree traversal even with a cell table
   DevBuf d_cyc_off, c_start, c_end, c_apos, c_aend, c_first, c_last, c_inst, c_stage, c_local,
       c_wl, c_comp, c_beta_tot, c_beta, c_coll, c_coll_n;
   // records
@@ -232,6 +233,12 @@ struct cs_ctx {
   pinned_vector<StreamCarry> h_stream;   // carry in force for the last batch
   pinned_vector<uint64_t> h_cyc_stage;   // pinned staging of cycle-table reads
   std::vector<uint32_t> stream_anchor;   // per instance, fixed after first batch
+  // monitor_loop stops at the first NonPositiveLatency (main.cpp:162): an
+  // instance whose stream saw a zero-length latency emits nothing afterwards.
+  // stream_stopped: set by the run that saw it; stream_stopped_prior: the
+  // state before the current run (that run's alerts are cut, later runs' dropped)
+  std::vector<uint8_t> stream_stopped, stream_stopped_prior;
+  bool stream_broken = false;  // a push failed after it started mutating state
 
   ~cs_ctx() {
     for (auto* m : model_store) delete m;
@@ -440,12 +447,8 @@ const char* cs_last_error(const cs_ctx* ctx) { return ctx ? ctx->err.c_str() : "
 int cs_set_config(cs_ctx* ctx, const cs_cycle_config* cycle, const cs_control_config* control) {
   if (!ctx) return CS_E_INVALID_ARGUMENT;
   if (cycle) {
-    if (cycle->n_phases < 0 || cycle->n_phases > kMaxPhases)
-      return fail(ctx, CS_E_UNSUPPORTED, "at most 8 phase functions are supported");
-    if (cycle->n_beta_slots < 0 || cycle->n_beta_slots > kMaxBetaSlots)
-      return fail(ctx, CS_E_UNSUPPORTED, "at most 64 span classes are supported");
-    if (cycle->n_comm_slots < 0 || cycle->n_comm_slots > kMaxCommSlots)
-      return fail(ctx, CS_E_UNSUPPORTED, "at most 64 collective slots are supported");
+    if (cycle->n_phases < 0 || cycle->n_beta_slots < 0 || cycle->n_comm_slots < 0)
+      return fail(ctx, CS_E_INVALID_ARGUMENT, "negative phase / class / collective slot count");
     if (cycle->stage_window == 0 || cycle->stage_window > 32)
       return fail(ctx, CS_E_UNSUPPORTED, "stage_window must be in [1, 32]");
     if (cycle->latency_phase >= cycle->n_phases)
@@ -468,10 +471,6 @@ static int cs_set_name_table_impl(cs_ctx* ctx, uint32_t n_names, const cs_name_i
   if (!ctx || (n_names && !names)) return CS_E_INVALID_ARGUMENT;
   cudaSetDevice(ctx->device);
   ctx->names.assign(names, names + n_names);
-  for (const auto& n : ctx->names) {
-    if (n.phase >= kMaxPhases) return fail(ctx, CS_E_UNSUPPORTED, "phase index out of range");
-    if (n.beta_slot >= kMaxBetaSlots) return fail(ctx, CS_E_UNSUPPORTED, "beta slot out of range");
-  }
   void* d = ctx->d_names.get(std::max<size_t>(1, n_names) * sizeof(cs_name_info));
   if (!d) return fail(ctx, CS_E_CUDA, "cudaMalloc(names)");
   if (n_names) CS_CUDA(cudaMemcpyAsync(d, names, n_names * sizeof(cs_name_info),
@@ -593,10 +592,67 @@ int wait_copied(cs_ctx* ctx) {
   return CS_OK;
 }
 
+static int cs_upload_unsorted_impl(cs_ctx* ctx, uint32_t n_inst, const uint64_t* inst_offsets,
+                                   const cs_event* ev, const uint64_t* event_ids, uint64_t n_workloads,
+                                   const cs_workload* wl) {
+  CS_NVTX_SCOPE("cs_upload_unsorted");
+  if (ctx) ctx->tails_on_device = false;
+  if (ctx && ctx->streaming) return fail(ctx, CS_E_INVALID_ARGUMENT, "cs_upload_unsorted mid-stream");
+  const int rc = upload_layout(ctx, n_inst, inst_offsets, ev != nullptr, n_workloads, wl);
+  if (rc != CS_OK) return rc;
+  ctx->have_order = false;
+  const uint64_t n = ctx->n_ev;
+  auto* din = dev<cs_event>(ctx->d_sort_in, n);
+  auto* dids = event_ids ? dev<uint64_t>(ctx->d_sort_ids, n) : nullptr;
+  auto* dsc = dev<unsigned long long>(ctx->d_sort_scratch, 4 * std::max<uint64_t>(1, n));
+  const uint64_t n_tiles = (n + kSortTile - 1) / kSortTile;
+  auto* dh = dev<uint64_t>(ctx->d_sort_hist, 256 * std::max<uint64_t>(1, n_tiles));
+  auto* dht = dev<uint64_t>(ctx->d_sort_hist_tmp, 256 * n_tiles / 1024 + 4);
+  auto* dex = dev<unsigned long long>(ctx->d_sort_ext, 4);
+  auto* dord = dev<uint64_t>(ctx->d_order, n);
+  if (!din || (event_ids && !dids) || !dsc || !dh || !dht || !dex || !dord)
+    return fail(ctx, CS_E_CUDA, "cudaMalloc(sort)");
+  if (n) {
+    CS_CUDA(cudaMemcpyAsync(din, ev, n * sizeof(cs_event), cudaMemcpyHostToDevice, ctx->stream));
+    if (event_ids)
+      CS_CUDA(cudaMemcpyAsync(dids, event_ids, n * 8, cudaMemcpyHostToDevice, ctx->stream));
+  }
+  if (wait_copied(ctx) != CS_OK) return CS_E_CUDA;
+  uint64_t launches = 0;
+  if (sort_events_device(din, dids, static_cast<const uint64_t*>(ctx->d_inst_off.p), n_inst, n,
+                         static_cast<cs_event*>(ctx->d_ev.p), dord, dsc, dh, dht, dex, ctx->stream,
+                         &launches) != 0)
+    return fail(ctx, CS_E_CUDA, std::string("device sort: ") + cudaGetErrorString(cudaGetLastError()));
+  CS_CUDA(cudaStreamSynchronize(ctx->stream));
+  ctx->have_order = true;
+  return CS_OK;
+}
+
+int cs_upload_unsorted(cs_ctx* ctx, uint32_t n_inst, const uint64_t* inst_offsets, const cs_event* ev,
+                       const uint64_t* event_ids, uint64_t n_workloads, const cs_workload* wl) {
+  return cs_guard(
+      [&] { return cs_upload_unsorted_impl(ctx, n_inst, inst_offsets, ev, event_ids, n_workloads, wl); });
+}
+
+int cs_get_order(cs_ctx* ctx, uint32_t inst, uint64_t* buf, size_t cap, size_t* n) {
+  if (!ctx || inst >= ctx->n_inst) return CS_E_INVALID_ARGUMENT;
+  if (!ctx->have_order) return fail(ctx, CS_E_INVALID_ARGUMENT, "no cs_upload_unsorted since the last upload");
+  const uint64_t b = ctx->inst_off[inst], m = ctx->inst_off[inst + 1] - b;
+  if (n) *n = m;
+  if (!buf) return CS_OK;
+  if (cap < m) return fail(ctx, CS_E_INVALID_ARGUMENT, "buffer too small");
+  if (m)
+    CS_CUDA(cudaMemcpyAsync(buf, static_cast<const uint64_t*>(ctx->d_order.p) + b, m * 8,
+                            cudaMemcpyDeviceToHost, ctx->stream));
+  CS_CUDA(cudaStreamSynchronize(ctx->stream));
+  return CS_OK;
+}
+
 static int cs_upload_impl(cs_ctx* ctx, uint32_t n_inst, const uint64_t* inst_offsets, const cs_event* ev,
               uint64_t n_workloads, const cs_workload* wl) {
   CS_NVTX_SCOPE("cs_upload");
   if (ctx) ctx->tails_on_device = false;
+  if (ctx) ctx->have_order = false;
   const int rc = upload_layout(ctx, n_inst, inst_offsets, ev != nullptr, n_workloads, wl);
   if (rc != CS_OK) return rc;
   if (ctx->n_ev)
@@ -617,6 +673,7 @@ static int cs_upload_wire_impl(cs_ctx* ctx, uint32_t n_inst, const uint64_t* ins
   if (!w || !ctx) return CS_E_INVALID_ARGUMENT;
   CS_NVTX_SCOPE("cs_upload_wire");
   ctx->tails_on_device = false;
+  ctx->have_order = false;
   const bool wl32 = w->workloads32 != nullptr;
   if (wl32 && (n_workloads || wl)) return CS_E_INVALID_ARGUMENT;
   const int rc = upload_layout(ctx, n_inst, inst_offsets, w->codes != nullptr && w->dt_lo && w->blocks,
@@ -926,6 +983,7 @@ static int cs_run_impl(cs_ctx* ctx, uint32_t mask) {
       ctx->stream_cur = 0;
       ctx->h_stream.assign(n_inst, StreamCarry{});
       ctx->stream_anchor.assign(n_inst, UINT32_MAX);
+      ctx->stream_stopped.assign(n_inst, 0);
       ctx->stream_fresh = false;
       ctx->stream_pending = false;
     }
@@ -989,99 +1047,8 @@ static int cs_run_impl(cs_ctx* ctx, uint32_t mask) {
            dev<uint64_t>(ctx->block_tmp, nc1 / 1024 + 16);
   };
   ctx->n_cyc.assign(n_inst, 0);
-  ctx->used_fused = false;
-  const std::vector<InstState> h_init(ctx->h_inst.begin(), ctx->h_inst.end());
-  int e1 = -1, e2 = -1;
-  // ---------------- fused single pass (common case)
-  if (ctx->allow_fused && !ctx->streaming) {
-    uint64_t cap = std::max<uint64_t>(ctx->slot_cap, ctx->n_ev / 8 + 1024);
-    const size_t nfix = 2 * std::max<size_t>(1, nt) + 16;
-    FusedMetaHost mh{};
-    for (int attempt = 0; attempt < 2; ++attempt) {
-      if (!alloc_cycles(cap) || !dev<unsigned long long>(ctx->d_fstate, nt) ||
-          !dev<unsigned int>(ctx->d_fticket, 1) || !dev<uint32_t>(ctx->d_fcnt, nt) ||
-          !dev<unsigned long long>(ctx->d_fpref, nt) || !dev<unsigned long long>(ctx->d_fixlist, nfix) ||
-          !dev<unsigned int>(ctx->d_fixn, 1) || !dev<uint32_t>(ctx->d_fixflags, nfix) ||
-          !dev<unsigned int>(ctx->d_foverflow, 1))
-        return fail(ctx, CS_E_CUDA, "cudaMalloc(fused)");
-      ctx->slot_cap = cap;
-      mh = FusedMetaHost{ctx->fused_debug, static_cast<unsigned long long*>(ctx->d_fstate.p),
-                         static_cast<unsigned int*>(ctx->d_fticket.p),
-                         static_cast<uint32_t*>(ctx->d_fcnt.p),
-                         static_cast<unsigned long long*>(ctx->d_fpref.p),
-                         static_cast<unsigned long long*>(ctx->d_fixlist.p),
-                         static_cast<unsigned int*>(ctx->d_fixn.p),
-                         static_cast<uint32_t*>(ctx->d_fixflags.p), cap,
-                         static_cast<unsigned int*>(ctx->d_foverflow.p)};
-      if (stats_bytes) CS_CUDA(cudaMemsetAsync(d_stats, 0, stats_bytes, s));
-      CS_CUDA(cudaMemsetAsync(ctx->d_fstate.p, 0, std::max<size_t>(1, nt) * 8, s));
-      CS_CUDA(cudaMemsetAsync(ctx->d_fticket.p, 0, 4, s));
-      CS_CUDA(cudaMemsetAsync(ctx->d_fixn.p, 0, 4, s));
-      CS_CUDA(cudaMemsetAsync(ctx->d_foverflow.p, 0, 4, s));
-      b = make_buffers(ctx);
-      e1 = record_event(ctx, 1);
-      if (launch_fused_segment(b, cfg, mh, (mask & CS_RUN_BETA) ? 1 : 0, s, &ctx->launches) != 0)
-        break;  // configuration too wide for the fused kernel
-      e2 = record_event(ctx, 2);
-      launch_fused_inst(b, mh, static_cast<uint64_t*>(ctx->d_cyc_off.p), s, &ctx->launches);
-      launch_rank(b, cfg, 1, s, &ctx->launches);
-      unsigned int hfix = 0, hover = 0;
-      ctx->cyc_off.assign(n_inst + 1, 0);
-      CS_CUDA(cudaMemcpyAsync(ctx->h_inst.data(), d_inst, n_inst * sizeof(InstState),
-                              cudaMemcpyDeviceToHost, s));
-      CS_CUDA(cudaMemcpyAsync(&hfix, ctx->d_fixn.p, 4, cudaMemcpyDeviceToHost, s));
-      CS_CUDA(cudaMemcpyAsync(&hover, ctx->d_foverflow.p, 4, cudaMemcpyDeviceToHost, s));
-      CS_CUDA(cudaMemcpyAsync(ctx->cyc_off.data(), ctx->d_cyc_off.p, (n_inst + 1) * 8,
-                              cudaMemcpyDeviceToHost, s));
-      CS_CUDA(cudaStreamSynchronize(s));
-      CS_CUDA(cudaGetLastError());  // launch failures surface here, not as bad counts
-      if (hover) {
-        // more anchors than slots: grow to the exact count and run again
-        cap = ctx->cyc_off[n_inst] + 1024;
-        for (uint32_t i = 0; i < n_inst; ++i) {
-          ctx->h_inst[i].n_unknown = 0;
-          ctx->h_inst[i].n_anchors = 0;
-        }
-        CS_CUDA(cudaMemcpyAsync(d_inst, ctx->h_inst.data(), n_inst * sizeof(InstState),
-                                cudaMemcpyHostToDevice, s));
-        continue;
-      }
-      bool ok = true;
-      for (uint32_t i = 0; i < n_inst; ++i) {
-        const auto& st = ctx->h_inst[i];
-        ok &= !st.ambiguous && !st.redo && !st.no_anchor;
-      }
-      if (!ok) break;
-      launch_fixup_cycles(b, cfg, mh, (mask & CS_RUN_BETA) ? 1 : 0, hfix, s, &ctx->launches);
-      ctx->n_cycles = ctx->cyc_off[n_inst];
-      for (uint32_t i = 0; i < n_inst; ++i) {
-        const auto na = ctx->h_inst[i].n_anchors;
-        ctx->n_cyc[i] = na >= 2 ? na - 1 : 0;
-      }
-      ctx->inst_status.assign(n_inst, CS_OK);
-      ctx->used_fallback.assign(n_inst, 0);
-      ctx->fallback_cycles.assign(n_inst, 0);
-      ctx->folded.assign(n_inst, {});
-      ctx->used_fused = true;
-      break;
-    }
-    if (!ctx->used_fused) {
-      // rare: restart on the general multi-kernel path
-      ctx->h_inst.assign(h_init.begin(), h_init.end());
-      CS_CUDA(cudaMemcpyAsync(d_inst, ctx->h_inst.data(), n_inst * sizeof(InstState),
-                              cudaMemcpyHostToDevice, s));
-      if (hint == -1) {
-        if (stats_bytes) CS_CUDA(cudaMemsetAsync(d_stats, 0, stats_bytes, s));
-        launch_scan_events(b, cfg, 1, true, static_cast<const uint32_t*>(ctx->d_sample_tiles.p),
-                           static_cast<uint32_t>(ctx->sample_tiles.size()), s, &ctx->launches);
-        launch_rank(b, cfg, 0, s, &ctx->launches);
-      }
-    }
-  }
-  const int e_fused_end = ctx->used_fused ? record_event(ctx, 3) : -1;
-  if (ctx->used_fused) ctx->timed.push_back({"fused_segment", {e1, e2}});
-  int e4 = e_fused_end, e5 = e_fused_end;
-  if (!ctx->used_fused) {
+  int e1 = -1, e2 = -1, e4 = -1, e5 = -1;
+  {
   if (stats_bytes) CS_CUDA(cudaMemsetAsync(d_stats, 0, stats_bytes, s));
   CS_CUDA(cudaMemsetAsync(ctx->d_tile_cnt.p, 0, std::max<size_t>(1, nt) * 8, s));
   e1 = record_event(ctx, 1);
@@ -1099,6 +1066,12 @@ static int cs_run_impl(cs_ctx* ctx, uint32_t mask) {
   CS_CUDA(cudaStreamSynchronize(s));
   hp.mark("scan_sync");
   CS_CUDA(cudaGetLastError());  // launch failures surface here, not as bad counts
+  for (uint32_t i = 0; i < n_inst; ++i)
+    if (ctx->h_inst[i].unsorted)
+      return fail(ctx, CS_E_INVALID_ARGUMENT,
+                  "events of instance " + std::to_string(i) +
+                      " are not in canonical (start_ts, event_id) order (trace.cpp:103-109); "
+                      "cs_upload_unsorted sorts them on the device");
 
   // ---- rare paths: ordered fold for uncertified rankings
   ctx->folded.assign(n_inst, {});
@@ -1215,7 +1188,7 @@ static int cs_run_impl(cs_ctx* ctx, uint32_t mask) {
   e5 = record_event(ctx, 5);
   ctx->timed.push_back({"bounds", {e3, e4}});
   ctx->timed.push_back({"cycle_reduce", {e4, e5}});
-  }  // legacy path
+  }
   b = make_buffers(ctx);
   launch_stage_heuristic(b, cfg, s, &ctx->launches);
   launch_records(b, cfg, 0, s, &ctx->launches);
@@ -1259,14 +1232,10 @@ static int cs_run_impl(cs_ctx* ctx, uint32_t mask) {
     if (!reuse) {
     ctx->mt_valid = false;
     ctx->h_models.assign(n_inst, DevModel{});
-    uint32_t nf0 = UINT32_MAX;
     for (uint32_t i = 0; i < n_inst; ++i) {
       const int id = ctx->model_id(i);
       if (id < 0) return fail(ctx, CS_E_INVALID_ARGUMENT, "no model loaded for an instance");
       const PackedModel* pm = ctx->model_store[id];
-      if (nf0 == UINT32_MAX) nf0 = pm->n_features;
-      if (pm->n_features != nf0)
-        return fail(ctx, CS_E_UNSUPPORTED, "all instances of a batch must share the feature count");
       DevModel& dm = ctx->h_models[i];
       dm.n_trees = pm->n_trees;
       dm.depth = pm->depth;
@@ -1286,7 +1255,7 @@ static int cs_run_impl(cs_ctx* ctx, uint32_t mask) {
       dm.feat = static_cast<const uint8_t*>(pm->d_feat.p);
       dm.smem_bytes = static_cast<uint64_t>(pm->thr_i.size()) * 8 + pm->leaf.size() * 8 +
                       pm->feat.size();
-      dm.lut = pm->has_lut ? static_cast<const double*>(pm->d_lut.p) : nullptr;
+      dm.lut = (pm->has_lut && !ctx->no_lut) ? static_cast<const double*>(pm->d_lut.p) : nullptr;
       for (int f = 0; f < 2; ++f) {
         dm.lut_thr[f] = static_cast<const double*>(pm->d_lut_thr[f].p);
         dm.lut_n[f] = static_cast<uint32_t>(pm->lut_thr[f].size());
@@ -1355,6 +1324,16 @@ static int cs_run_impl(cs_ctx* ctx, uint32_t mask) {
     if (ctx->inst_status[i] == CS_OK && ctx->h_inst[i].first_bad_record != UINT64_MAX &&
         (mask & (CS_RUN_SCORE | CS_RUN_DETECT)))
       ctx->inst_status[i] = CS_E_NON_POSITIVE_LATENCY;
+  if (ctx->streaming) {
+    ctx->stream_stopped_prior = ctx->stream_stopped;
+    for (uint32_t i = 0; i < n_inst; ++i) {
+      if (ctx->stream_stopped_prior[i]) ctx->inst_status[i] = CS_E_NON_POSITIVE_LATENCY;
+      if (ctx->h_inst[i].first_bad_record != UINT64_MAX && (mask & (CS_RUN_SCORE | CS_RUN_DETECT)))
+        ctx->stream_stopped[i] = 1;
+    }
+  } else {
+    ctx->stream_stopped_prior.clear();
+  }
   if (ctx->streaming)
     for (uint32_t i = 0; i < n_inst; ++i)
       if (ctx->stream_anchor[i] == UINT32_MAX && !ctx->h_inst[i].no_anchor &&
@@ -1372,6 +1351,9 @@ int cs_run(cs_ctx* ctx, uint32_t mask) {
 int cs_stream_begin(cs_ctx* ctx) {
   if (!ctx) return CS_E_INVALID_ARGUMENT;
   ctx->streaming = true;
+  ctx->stream_broken = false;
+  ctx->stream_stopped.clear();
+  ctx->stream_stopped_prior.clear();
   ctx->tail_len.clear();
   ctx->tail_start.clear();
   ctx->tails_on_device = false;
@@ -1399,67 +1381,16 @@ int cs_stream_tail(cs_ctx* ctx, uint32_t inst, uint64_t* keep_from) {
   return CS_OK;
 }
 
-static int cs_stream_push_impl(cs_ctx* ctx, uint32_t n_inst, const uint64_t* offsets, const cs_event* ev,
-                   uint64_t n_workloads, const cs_workload* wl, uint32_t mask, cs_alert* alerts,
-                   size_t cap, size_t* n_alerts) {
-  HostPhases hp("cs_stream_push");
-  if (!ctx || !offsets || n_inst == 0) return CS_E_INVALID_ARGUMENT;
-  if (!ctx->streaming) return fail(ctx, CS_E_INVALID_ARGUMENT, "not streaming (cs_stream_begin)");
-  if (offsets[0] != 0) return fail(ctx, CS_E_INVALID_ARGUMENT, "offsets[0] must be 0");
-  if (ctx->tail_len.size() != n_inst) {
-    if (!ctx->tail_len.empty() && !ctx->stream_fresh)
-      return fail(ctx, CS_E_INVALID_ARGUMENT, "instance count changed mid-stream");
-    ctx->tail_len.assign(n_inst, 0);
-    ctx->tail_start.assign(n_inst, 0);
-  }
-  uint64_t carried = 0;
-  for (uint32_t i = 0; i < n_inst; ++i) carried += ctx->tail_len[i];
-  if (carried && !ctx->tails_on_device)
-    return fail(ctx, CS_E_INVALID_ARGUMENT, "stream tails were replaced by cs_upload (use one streaming API)");
-  // new layout: per instance the carried tail, then the new events
-  ctx->stage_off.assign(n_inst + 1, 0);
-  for (uint32_t i = 0; i < n_inst; ++i) {
-    if (offsets[i + 1] < offsets[i]) return fail(ctx, CS_E_INVALID_ARGUMENT, "offsets must be non-decreasing");
-    ctx->stage_off[i + 1] = ctx->stage_off[i] + ctx->tail_len[i] + (offsets[i + 1] - offsets[i]);
-  }
-  const uint64_t n_new = offsets[n_inst];
-  if (n_new && !ev) return CS_E_INVALID_ARGUMENT;
-  // the previous batch's events (holding the tails) move to d_ev_prev; the
-  // new batch is assembled on the device from them and the uploaded events
-  std::swap(ctx->d_ev.p, ctx->d_ev_prev.p);
-  std::swap(ctx->d_ev.cap, ctx->d_ev_prev.cap);
-  hp.mark("pre");
-  int rc = upload_layout(ctx, n_inst, ctx->stage_off.data(), true, n_workloads, wl);
-  if (rc != CS_OK) return rc;
-  hp.mark("layout");
-  auto* d_new = dev<cs_event>(ctx->d_new_ev, std::max<uint64_t>(1, n_new));
-  auto* d_meta = dev<uint64_t>(ctx->d_assemble, 4ull * n_inst);
-  if (!d_new || !d_meta) return fail(ctx, CS_E_CUDA, "cudaMalloc(stream)");
-  if (n_new)
-    CS_CUDA(cudaMemcpyAsync(d_new, ev, n_new * sizeof(cs_event), cudaMemcpyHostToDevice, ctx->stream));
-  std::vector<uint64_t>& meta = ctx->assemble_host;
-  meta.resize(4ull * n_inst);
-  for (uint32_t i = 0; i < n_inst; ++i) {
-    meta[4 * i + 0] = ctx->stage_off[i];
-    meta[4 * i + 1] = ctx->tail_start[i];
-    meta[4 * i + 2] = ctx->tail_len[i];
-    meta[4 * i + 3] = offsets[i];
-  }
-  CS_CUDA(cudaMemcpyAsync(d_meta, meta.data(), meta.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
-  launch_stream_assemble(static_cast<const cs_event*>(ctx->d_ev_prev.p), d_new, d_meta, n_inst,
-                         ctx->stage_off[n_inst], static_cast<cs_event*>(ctx->d_ev.p), ctx->stream);
-  CS_CUDA(cudaGetLastError());
-  hp.mark("copy_assemble");
-  rc = cs_run(ctx, mask);
-  if (rc != CS_OK) return rc;
-  hp.mark("run");
-  // new tails: everything from the last closed cycle's end (cycles.cpp:147)
+// After a push's run: new tails (everything from the last closed cycle's end,
+// cycles.cpp:147) and the alerts of every instance in instance order, cut at
+// the first NonPositiveLatency of the stream (main.cpp:162).
+static int stream_commit(cs_ctx* ctx, uint32_t n_inst, uint32_t mask, cs_alert* alerts, size_t cap,
+                         size_t* n_alerts, HostPhases& hp) {
   auto* dk = dev<uint64_t>(ctx->d_keep, n_inst);
   if (!dk) return fail(ctx, CS_E_CUDA, "cudaMalloc(keep)");
   launch_stream_keep(make_buffers(ctx), dk, ctx->stream);
   std::vector<uint64_t> keep(n_inst);
   CS_CUDA(cudaMemcpyAsync(keep.data(), dk, n_inst * 8, cudaMemcpyDeviceToHost, ctx->stream));
-  // alerts of every instance, in instance order
   size_t na = 0;
   const bool det = (mask & CS_RUN_DETECT) != 0;
   std::vector<cs_alert> all;
@@ -1481,7 +1412,7 @@ static int cs_stream_push_impl(cs_ctx* ctx, uint32_t n_inst, const uint64_t* off
   CS_CUDA(cudaStreamSynchronize(ctx->stream));
   hp.mark("sync");
   for (uint32_t i = 0; i < n_inst && det; ++i) {
-    // monitor_loop stops at the first NonPositiveLatency (main.cpp:162)
+    if (ctx->stream_stopped_prior[i]) continue;  // stopped by an earlier push
     const uint64_t bad = ctx->h_inst[i].first_bad_record;
     for (uint64_t a = ctx->alert_off[i]; a < ctx->alert_off[i + 1]; ++a) {
       if (all[a].record_index >= bad) break;
@@ -1498,8 +1429,91 @@ static int cs_stream_push_impl(cs_ctx* ctx, uint32_t n_inst, const uint64_t* off
   ctx->tails_on_device = true;
   hp.mark("end");
   if (n_alerts) *n_alerts = na;
-  if (alerts && na > cap) return fail(ctx, CS_E_INVALID_ARGUMENT, "alert buffer too small");
+  if (alerts && na > cap)
+    return fail(ctx, CS_E_INVALID_ARGUMENT,
+                "alert buffer too small (the push is committed; cs_get_alerts reads its alerts)");
   return CS_OK;
+}
+
+static int cs_stream_push_impl(cs_ctx* ctx, uint32_t n_inst, const uint64_t* offsets, const cs_event* ev,
+                   uint64_t n_workloads, const cs_workload* wl, uint32_t mask, cs_alert* alerts,
+                   size_t cap, size_t* n_alerts) {
+  HostPhases hp("cs_stream_push");
+  if (!ctx || !offsets || n_inst == 0) return CS_E_INVALID_ARGUMENT;
+  if (!ctx->streaming) return fail(ctx, CS_E_INVALID_ARGUMENT, "not streaming (cs_stream_begin)");
+  if (ctx->stream_broken)
+    return fail(ctx, CS_E_INVALID_ARGUMENT, "stream broken by an earlier failed push (cs_stream_begin restarts it)");
+  // every argument is checked before any state changes: a rejected push
+  // leaves the stream exactly as it was
+  if (offsets[0] != 0) return fail(ctx, CS_E_INVALID_ARGUMENT, "offsets[0] must be 0");
+  for (uint32_t i = 0; i < n_inst; ++i)
+    if (offsets[i + 1] < offsets[i]) return fail(ctx, CS_E_INVALID_ARGUMENT, "offsets must be non-decreasing");
+  if (offsets[n_inst] && !ev) return fail(ctx, CS_E_INVALID_ARGUMENT, "events missing");
+  if (n_workloads && !wl) return fail(ctx, CS_E_INVALID_ARGUMENT, "n_workloads > 0 needs wl");
+  if (!ctx->tail_len.empty() && ctx->tail_len.size() != n_inst && !ctx->stream_fresh)
+    return fail(ctx, CS_E_INVALID_ARGUMENT, "instance count changed mid-stream");
+  if (ctx->tail_len.size() != n_inst) {
+    if (!ctx->tail_len.empty() && !ctx->stream_fresh)
+      return fail(ctx, CS_E_INVALID_ARGUMENT, "instance count changed mid-stream");
+    ctx->tail_len.assign(n_inst, 0);
+    ctx->tail_start.assign(n_inst, 0);
+  }
+  uint64_t carried = 0;
+  for (uint32_t i = 0; i < n_inst; ++i) carried += ctx->tail_len[i];
+  if (carried && !ctx->tails_on_device)
+    return fail(ctx, CS_E_INVALID_ARGUMENT, "stream tails were replaced by cs_upload (use one streaming API)");
+  // new layout: per instance the carried tail, then the new events
+  ctx->stage_off.assign(n_inst + 1, 0);
+  for (uint32_t i = 0; i < n_inst; ++i)
+    ctx->stage_off[i + 1] = ctx->stage_off[i] + ctx->tail_len[i] + (offsets[i + 1] - offsets[i]);
+  const uint64_t n_new = offsets[n_inst];
+  // the previous batch's events (holding the tails) move to d_ev_prev; the
+  // new batch is assembled on the device from them and the uploaded events.
+  // From here on a failure (allocation, CUDA, run) leaves the carried tails
+  // and detector carry inconsistent: the stream is marked broken and every
+  // later push fails loudly instead of assembling from a stale buffer.
+  std::swap(ctx->d_ev.p, ctx->d_ev_prev.p);
+  std::swap(ctx->d_ev.cap, ctx->d_ev_prev.cap);
+  auto broken = [&](int rc) {
+    std::swap(ctx->d_ev.p, ctx->d_ev_prev.p);
+    std::swap(ctx->d_ev.cap, ctx->d_ev_prev.cap);
+    ctx->stream_broken = true;
+    return rc;
+  };
+  hp.mark("pre");
+  int rc = upload_layout(ctx, n_inst, ctx->stage_off.data(), true, n_workloads, wl);
+  if (rc != CS_OK) return broken(rc);
+  hp.mark("layout");
+  auto* d_new = dev<cs_event>(ctx->d_new_ev, std::max<uint64_t>(1, n_new));
+  auto* d_meta = dev<uint64_t>(ctx->d_assemble, 4ull * n_inst);
+  if (!d_new || !d_meta) return broken(fail(ctx, CS_E_CUDA, "cudaMalloc(stream)"));
+  if (n_new && cudaMemcpyAsync(d_new, ev, n_new * sizeof(cs_event), cudaMemcpyHostToDevice,
+                               ctx->stream) != cudaSuccess)
+    return broken(fail(ctx, CS_E_CUDA, "cudaMemcpyAsync(stream events)"));
+  std::vector<uint64_t>& meta = ctx->assemble_host;
+  meta.resize(4ull * n_inst);
+  for (uint32_t i = 0; i < n_inst; ++i) {
+    meta[4 * i + 0] = ctx->stage_off[i];
+    meta[4 * i + 1] = ctx->tail_start[i];
+    meta[4 * i + 2] = ctx->tail_len[i];
+    meta[4 * i + 3] = offsets[i];
+  }
+  if (cudaMemcpyAsync(d_meta, meta.data(), meta.size() * 8, cudaMemcpyHostToDevice, ctx->stream) !=
+      cudaSuccess)
+    return broken(fail(ctx, CS_E_CUDA, "cudaMemcpyAsync(stream meta)"));
+  launch_stream_assemble(static_cast<const cs_event*>(ctx->d_ev_prev.p), d_new, d_meta, n_inst,
+                         ctx->stage_off[n_inst], static_cast<cs_event*>(ctx->d_ev.p), ctx->stream);
+  if (cudaGetLastError() != cudaSuccess) return broken(fail(ctx, CS_E_CUDA, "stream assemble"));
+  hp.mark("copy_assemble");
+  rc = cs_run(ctx, mask);
+  if (rc != CS_OK) return broken(rc);
+  hp.mark("run");
+  // the run has advanced the device carry: from here on the push commits
+  // (the tails below move forward even when the alert buffer is too small;
+  // the alerts of this push stay readable with cs_get_alerts until the next)
+  rc = stream_commit(ctx, n_inst, mask, alerts, cap, n_alerts, hp);
+  if (rc != CS_OK && rc != CS_E_INVALID_ARGUMENT) ctx->stream_broken = true;
+  return rc;
 }
 
 int cs_stream_push(cs_ctx* ctx, uint32_t n_inst, const uint64_t* offsets, const cs_event* ev,
@@ -1885,6 +1899,10 @@ int cs_get_record_range(cs_ctx* ctx, uint32_t inst, uint64_t first, uint64_t cou
 int cs_get_alerts(cs_ctx* ctx, uint32_t inst, cs_alert* buf, size_t cap, size_t* n) {
   if (!ctx || !ctx->ran || inst >= ctx->n_inst) return CS_E_INVALID_ARGUMENT;
   if (!(ctx->last_mask & CS_RUN_DETECT)) return fail(ctx, CS_E_INVALID_ARGUMENT, "detect not run");
+  if (ctx->streaming && inst < ctx->stream_stopped_prior.size() && ctx->stream_stopped_prior[inst]) {
+    if (n) *n = 0;  // the stream stopped at an earlier NonPositiveLatency
+    return CS_OK;
+  }
   const uint64_t a0 = ctx->alert_off[inst], na_all = ctx->alert_off[inst + 1] - a0;
   const uint64_t bad = ctx->h_inst[inst].first_bad_record;
   if (!buf && bad == UINT64_MAX) {  // a count query: no truncation to apply
@@ -1918,13 +1936,18 @@ int cs_redetect(cs_ctx* ctx, const cs_control_config* control) {
     return fail(ctx, CS_E_INVALID_ARGUMENT, "cs_redetect needs a scored run");
   if (control->strategy < 0 || control->strategy > 2 || control->window == 0)
     return fail(ctx, CS_E_CONFIG, "invalid control config");
+  const uint32_t n_inst = ctx->n_inst;
+  // the limits come from the models the last run scored with (mt_ids), not
+  // from the bindings now: a model loaded or rebound since would otherwise
+  // mix its limits with the old model's residuals
+  if (ctx->mt_ids.size() != n_inst || ctx->h_models.size() != n_inst)
+    return fail(ctx, CS_E_INVALID_ARGUMENT, "cs_redetect needs the model table of the last run");
   CS_CUDA(cudaSetDevice(ctx->device));
   cudaStream_t s = ctx->stream;
   ctx->ctl = *control;
   ctx->mt_valid = false;  // the table below gets this config's limits
-  const uint32_t n_inst = ctx->n_inst;
   for (uint32_t i = 0; i < n_inst; ++i) {
-    const PackedModel* pm = ctx->model_store[ctx->model_id(i)];
+    const PackedModel* pm = ctx->model_store[ctx->mt_ids[i]];
     ctx->h_models[i].ucl = ctx->ctl.strategy == CS_DYNAMIC_WINDOW
                                ? ucl_from_stats_host(pm->mu, pm->sigma, ctx->ctl)
                                : ctx->ctl.fixed_threshold;
@@ -1989,12 +2012,13 @@ int cs_set_option(cs_ctx* ctx, int option, int64_t value) {
     ctx->allow_fused = value != 0;
     return CS_OK;
   }
-  if (option == 98) {  // profiling: multi-kernel reduce variant
-    ctx->reduce_variant = static_cast<int>(value);
+  if (option == CS_OPT_TRAVERSAL) {
+    ctx->no_lut = value != 0;
+    ctx->mt_valid = false;  // the per-instance model table carries the choice
     return CS_OK;
   }
-  if (option == 99) {  // profiling only (outputs invalid): fused-kernel ablations
-    ctx->fused_debug = static_cast<int>(value);
+  if (option == 98) {  // profiling: multi-kernel reduce variant
+    ctx->reduce_variant = static_cast<int>(value);
     return CS_OK;
   }
   return fail(ctx, CS_E_INVALID_ARGUMENT, "unknown option");

@@ -14,9 +14,6 @@ namespace csb {
 constexpr int kScanThreads = 512;               // 16 warps
 constexpr int kTileEvents = 1024;               // 32 KiB tile, one TMA bulk copy
 constexpr int kSmemNames = 512;                 // name stats staged in smem
-constexpr int kMaxPhases = 8;
-constexpr int kMaxBetaSlots = 64;
-constexpr int kMaxCommSlots = 64;
 constexpr int kMaxFeatures = 8;
 constexpr int kMaxTreeDepth = 8;
 constexpr uint64_t kSampleEvents = 1u << 18;    // anchor-guess sample per instance (verified by the full pass)
@@ -45,7 +42,7 @@ struct InstState {
   unsigned long long n_records;
   unsigned long long n_alerts;
   uint32_t fixed_anchor;   // streaming: `guess` is this instance's fixed anchor
-  uint32_t reserved;
+  uint32_t unsorted;       // the event scan saw start_ts decrease (not canonical order)
 };
 
 // flattened model in complete-binary-tree layout (see pack_model)
@@ -158,20 +155,6 @@ struct DevBuffers {
   StreamCarry* stream;          // per instance, null when not streaming
 };
 
-// fused single-pass segmentation state (k_fused_segment)
-struct FusedMetaHost {
-  int debug;
-  unsigned long long* state;
-  unsigned int* ticket;
-  uint32_t* t_cnt;
-  unsigned long long* t_pref;
-  unsigned long long* fix_list;
-  unsigned int* fix_n;
-  uint32_t* fix_flags;
-  unsigned long long capacity;
-  unsigned int* overflow;
-};
-
 // launchers (cs_kernels.cu); all asynchronous on `s`
 void launch_scan_events(const DevBuffers& b, const DevConfig& cfg, int mode, bool sample,
                         const uint32_t* list, uint32_t n_list, cudaStream_t s,
@@ -236,12 +219,16 @@ constexpr int kMaxMetrics = 16;
 void launch_lut_build(const uint8_t* feat, const int32_t* rank, const double* leafp,
                       uint32_t n_trees, uint32_t D, double base, double floor_, uint32_t n0,
                       uint64_t cells, double* lut, cudaStream_t s);
-int launch_fused_segment(const DevBuffers& b, const DevConfig& cfg, const FusedMetaHost& mh,
-                         int do_beta, cudaStream_t s, uint64_t* launches);
-void launch_fused_inst(const DevBuffers& b, const FusedMetaHost& mh, uint64_t* cyc_off,
-                       cudaStream_t s, uint64_t* launches);
-void launch_fixup_cycles(const DevBuffers& b, const DevConfig& cfg, const FusedMetaHost& mh,
-                         int do_beta, uint32_t n_fix, cudaStream_t s, uint64_t* launches);
+void launch_exclusive_scan(uint64_t* v, uint64_t n, uint64_t* total, uint64_t* tmp, cudaStream_t s,
+                           uint64_t* launches);
+// K0 (cs_sort.cu): stable per-instance sort by (start_ts, event_id) (ids may be
+// null: input position breaks ties); scratch = 4n u64, hist = 256 * ceil(n /
+// 4096) u64, hist_tmp = its scan scratch, extent = 4 u64.  Returns 0 on success.
+int sort_events_device(const cs_event* in, const uint64_t* ids, const uint64_t* d_off,
+                       uint32_t n_inst, uint64_t n, cs_event* out, uint64_t* order,
+                       unsigned long long* scratch, uint64_t* hist, uint64_t* hist_tmp,
+                       unsigned long long* extent, cudaStream_t s, uint64_t* launches);
+constexpr uint64_t kSortTile = 4096;
 void launch_eval_strategy(const DevBuffers& b, uint32_t inst, const uint8_t* labels,
                           uint64_t n_labels, uint64_t warmup, unsigned long long* out,
                           cudaStream_t s);

@@ -16,8 +16,6 @@
 //                                stage signals (205-229), workload carrier
 //                                (256-281), class occupancy beta and per-rank
 //                                collective beta (rca.cpp:71-130)
-//   K123 k_segment_pass          (optional, CS_OPT_FUSED) K1+K2+K3 in one
-//                                warp-specialised pass with decoupled look-back
 //   K4   k_stage_heuristic       trailing-median heuristic for Unknown cycles
 //                                only (cycles.cpp:230-250), warp selection
 //   K5   k_records_*             record compaction (cycles.cpp:366-409)
@@ -30,6 +28,7 @@
 // and the whole file is compiled with --fmad=false.
 #include <cuda_runtime.h>
 
+#include <climits>
 #include <cstdint>
 
 #include "cs_internal.h"
@@ -368,6 +367,7 @@ __global__ void __launch_bounds__(kScanWarpThreads, 3)
   const bool do_stats = mode & 1;
   const bool do_anchor = (mode & 2) && !sample;
   const bool redo = mode & 4;
+  const bool check = do_anchor && !redo;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   WarpNameRow* wrows = s_rows + warp * kWarpNameRows;
   uint32_t* pn = s_pn[warp];
@@ -433,13 +433,20 @@ __global__ void __launch_bounds__(kScanWarpThreads, 3)
     }
     const uint32_t n = (uint32_t)(te - tb);
     uint32_t cnt = 0;
+    // K0 check (trace.cpp:103-109 is_sorted): start_ts never decreases within
+    // an instance; the previous event of the tile's first one is read once
+    i64 carry_ts = (check && tb > b.inst_off[inst]) ? b.ev[tb - 1].start_ts : LLONG_MIN;
+    bool unsorted = false;
     for (uint32_t j0 = 0; j0 < n; j0 += 32 * kScanUnroll) {
       Ev8 e[kScanUnroll];
 #pragma unroll
       for (int q = 0; q < kScanUnroll; ++q) {
         const uint32_t j = j0 + q * 32 + lane;
         if (j < n) e[q] = ldg256(b.ev + tb + j);
-        else e[q].c = (u64)CS_FLOW << 32;  // ignored
+        else {
+          e[q].a = ~0ull >> 1;  // INT64_MAX: never below its predecessor
+          e[q].c = (u64)CS_FLOW << 32;  // ignored
+        }
       }
 #pragma unroll
       for (int q = 0; q < kScanUnroll; ++q) {
@@ -463,6 +470,11 @@ __global__ void __launch_bounds__(kScanWarpThreads, 3)
         // the anchor opens its group unless the previous record shares its
         // start; kWalk marks the rare anchors k_bounds_tile must walk back for
         const u64 prev = __shfl_up_sync(0xffffffffu, e[q].a, 1);
+        if (check) {
+          const i64 before = lane == 0 ? carry_ts : (i64)prev;
+          unsorted |= before > (i64)e[q].a;
+          carry_ts = (i64)__shfl_sync(0xffffffffu, e[q].a, 31);
+        }
         if (is_anchor) {
           const u64 r = tb + cnt + __popc(mk & lanemask_lt());
           const uint32_t jj = j0 + q * 32 + lane;
@@ -475,6 +487,7 @@ __global__ void __launch_bounds__(kScanWarpThreads, 3)
       }
     }
     if (active && lane == 0) b.tile_cnt[t] = cnt;
+    if (check && __any_sync(0xffffffffu, unsorted) && lane == 0) atomicOr(&b.inst[inst].unsorted, 1u);
   }
   if (do_stats && cur_inst != 0xffffffffu) {
     drain(npend);
@@ -1703,853 +1716,7 @@ __global__ void k_freq_cycles(const cs_event* ev, uint64_t begin, uint64_t end, 
   b.c_inst[g] = inst;
 }
 
-// ==================================================== fused single pass
-// K123: ONE streaming pass over the events does what k_scan_events + k_bounds
-// + k_cycle_reduce do in three.  Tiles of 1024 events are claimed in order
-// (ticket) and TMA-prefetched kFStages deep; per tile:
-//   1. PythonCall moments (warp name rows) + anchor flags for the guess;
-//   2. decoupled look-back over the anchor counts gives the global rank P of
-//      the tile's first anchor = the global cycle slot of its cycle;
-//   3. every cycle whose two anchors and whole event range lie in the tile is
-//      reduced by ONE thread, sequentially, straight from shared memory:
-//      component durations, first forward_mode, keywords, workload carrier,
-//      beta and event-ordered collective beta (cycles.cpp:157-166, 205-281;
-//      rca.cpp:87-129);
-//   4. cycles that straddle a tile edge (~1 per tile) go to a fixup list that
-//      k_fixup_cycles reduces from global memory with the same routine.
-// Cycle slots are global anchor ranks; the last anchor of an instance owns a
-// "hole" slot (no cycle), marked c_wl = -4.
-constexpr int kFThreads = 256;
-constexpr int kFTile = 1024;
-constexpr int kFStages = 2;
-constexpr uint32_t kFTileBytes = kFTile * sizeof(cs_event);
-constexpr u64 kFlagAggF = 1ull << 62;
-constexpr u64 kFlagPrefixF = 2ull << 62;
-
-// Aggregate publication is separated from the look-back wait so a CTA can
-// publish a prefetched tile's anchor count the moment its bytes land — long
-// before it processes that tile — and successors never wait on processing.
-__device__ __forceinline__ void publish_aggregate(u64* state, uint32_t tile, u64 agg) {
-  st_release(&state[tile], (tile == 0 ? kFlagPrefixF : kFlagAggF) | agg);
-}
-
-// warp-wide: exclusive prefix of tile `tile` (its aggregate already published)
-__device__ u64 lookback_wait(u64* state, uint32_t tile, u64 agg) {
-  const int lane = threadIdx.x & 31;
-  if (tile == 0) return 0;
-  u64 excl = 0;
-  i64 j = (i64)tile - 1 - lane;
-  while (true) {
-    const bool in = j >= 0;
-    u64 v = 0;
-    if (in) {
-      do {
-        v = ld_acquire(&state[j]);
-      } while ((v >> 62) == 0);
-    }
-    const uint32_t pm = __ballot_sync(0xffffffffu, !in || (v >> 62) == 2);
-    const int stop = pm ? __ffs(pm) - 1 : 32;
-    excl += warp_sum_u64((in && lane <= stop) ? (v & kValMask) : 0);
-    if (pm) break;
-    j -= 32;
-  }
-  if (lane == 0) st_release(&state[tile], kFlagPrefixF | (excl + agg));
-  return excl;
-}
-
-// warp-wide anchor count of a staged tile
-__device__ __forceinline__ uint32_t warp_count_anchors(const cs_event* tile, uint32_t n,
-                                                       uint32_t guess) {
-  const int lane = threadIdx.x & 31;
-  uint32_t c = 0;
-  for (uint32_t e = lane; e < n; e += 32) {
-    const int4 h1 = reinterpret_cast<const int4*>(tile + e)[1];
-    c += ((((uint32_t)h1.y & 0xffu) == CS_SPAN) && (uint32_t)h1.x == guess) ? 1u : 0u;
-  }
-  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-  return c;
-}
-
-// Sequential per-cycle reduction by one thread over ev[first, last): the
-// reference's own loops, in event order.  Component sums live in registers
-// (<= kMaxPhases), class occupancy and collective beta in a thread-private
-// shared-memory slice.
-struct CycAcc {
-  i64 comp[kMaxPhases];
-  int32_t wl;
-  uint8_t stage;
-};
-
-template <typename EvPtr>
-__device__ __forceinline__ CycAcc accumulate_cycle(const cs_name_info* __restrict__ names,
-                                                   const DevConfig& cfg, int do_beta,
-                                                   EvPtr ev, u64 first, u64 last, i64 cs, i64 ce,
-                                                   bool no_comp, i64* __restrict__ beta,
-                                                   double* __restrict__ coll,
-                                                   uint32_t* __restrict__ colln) {
-  const int C = cfg.cyc.n_beta_slots, R = cfg.cyc.n_comm_slots;
-  const i64 dur = ce - cs;
-  CycAcc a;
-#pragma unroll
-  for (int i = 0; i < kMaxPhases; ++i) a.comp[i] = 0;
-  if (do_beta) {
-    for (int i = 0; i < C; ++i) beta[i] = 0;
-    for (int i = 0; i < R; ++i) {
-      coll[i] = 0.0;
-      colln[i] = 0;
-    }
-  }
-  uint32_t fm_cls = 0;
-  bool fm_found = false, pkw = false, dkw = false, batch_found = false;
-  a.wl = -1;
-  for (u64 j = first; j < last; ++j) {
-    const int4* q = reinterpret_cast<const int4*>(ev + j);
-    const int4 h0 = q[0], h1 = q[1];
-    const i64 st = (i64)(((u64)(uint32_t)h0.y << 32) | (uint32_t)h0.x);
-    const i64 d = (i64)(((u64)(uint32_t)h0.w << 32) | (uint32_t)h0.z);
-    const uint32_t name = (uint32_t)h1.x;
-    const uint32_t kind = (uint32_t)h1.y & 0xffu;
-    const uint32_t cat = ((uint32_t)h1.y >> 8) & 0xffu;
-    const uint32_t flags = (uint32_t)h1.y >> 16;
-    if (!fm_found && (flags & CS_EV_FM_MASK)) {
-      fm_found = true;
-      fm_cls = flags & CS_EV_FM_MASK;
-    }
-    if (!batch_found && (flags & CS_EV_HAS_BATCH)) {
-      batch_found = true;
-      a.wl = (flags & CS_EV_WL_OK) ? (int32_t)(uint32_t)h1.z : -2;
-    }
-    if (kind != CS_SPAN) continue;
-    const cs_name_info ni = names[name];
-    pkw |= (ni.flags & CS_NAME_PREFILL_KW) != 0;
-    dkw |= (ni.flags & CS_NAME_DECODE_KW) != 0;
-    const i64 end = st + d;
-    const i64 clipped = (end < ce ? end : ce) - st;
-    if (clipped <= 0) continue;
-    if (!no_comp) {
-#pragma unroll
-      for (int p = 0; p < kMaxPhases; ++p) a.comp[p] += ni.phase == p ? clipped : 0;
-    }
-    if (do_beta && d > 0) {
-      if (ni.beta_slot >= 0) beta[ni.beta_slot] += clipped;
-      if (cat == CS_CAT_COLLECTIVE_COMM && (flags & CS_EV_HAS_COMM)) {
-        const uint32_t slot = (uint32_t)h1.w;
-        if (slot < (uint32_t)R) {
-          coll[slot] = __dadd_rn(coll[slot], __ddiv_rn((double)clipped, (double)dur));
-          colln[slot] += 1;
-        }
-      }
-    }
-  }
-  a.stage = CS_STAGE_UNKNOWN;
-  if (fm_cls == CS_EV_FM_PREFILL) a.stage = CS_STAGE_PREFILL;
-  else if (fm_cls == CS_EV_FM_DECODE) a.stage = CS_STAGE_DECODE;
-  if (a.stage == CS_STAGE_UNKNOWN && pkw != dkw) a.stage = pkw ? CS_STAGE_PREFILL : CS_STAGE_DECODE;
-  return a;
-}
-
-__device__ __forceinline__ void write_cycle(const DevBuffers& b, const DevConfig& cfg, int do_beta,
-                                            const CycAcc& a, u64 g, uint32_t inst, i64 cs, i64 ce,
-                                            u64 apos, i64 aend, u64 gfirst, u64 glast,
-                                            const i64* __restrict__ beta,
-                                            const double* __restrict__ coll,
-                                            const uint32_t* __restrict__ colln) {
-  const int P = cfg.cyc.n_phases, C = cfg.cyc.n_beta_slots, R = cfg.cyc.n_comm_slots;
-  const i64 dur = ce - cs;
-  b.c_start[g] = cs;
-  b.c_end[g] = ce;
-  b.c_apos[g] = apos;
-  b.c_aend[g] = aend;
-  b.c_first[g] = gfirst;
-  b.c_last[g] = glast;
-  b.c_inst[g] = inst;
-  b.c_local[g] = a.stage;
-  b.c_stage[g] = a.stage;
-  b.c_wl[g] = a.wl;
-  if (a.stage == CS_STAGE_UNKNOWN) atomicAdd(&b.inst[inst].n_unknown, 1ull);
-#pragma unroll
-  for (int i = 0; i < kMaxPhases; ++i)
-    if (i < P) b.c_comp[g * P + i] = a.comp[i];
-  if (do_beta) {
-    for (int i = 0; i < C; ++i) {
-      const i64 t = dur > 0 ? beta[i] : 0;
-      b.c_beta_tot[g * C + i] = t;
-      b.c_beta[g * C + i] = t > 0 ? __ddiv_rn((double)t, (double)dur) : 0.0;
-    }
-    for (int i = 0; i < R; ++i) {
-      b.c_coll[g * R + i] = coll[i];
-      b.c_coll_n[g * R + i] = (uint8_t)(colln[i] > 255 ? 255 : colln[i]);
-    }
-  }
-}
-
-struct FusedMeta {
-  int debug;           // profiling only: bit0 no look-back, bit1 no cycle work
-  u64* state;          // look-back state per tile
-  unsigned int* ticket;
-  uint32_t* t_cnt;     // anchors per tile
-  u64* t_pref;         // global rank of the tile's first anchor
-  u64* fix_list;       // cycle slots needing k_fixup_cycles
-  unsigned int* fix_n;
-  uint32_t* fix_flags; // bit0 needs end/last, bit1 needs first
-  u64 capacity;        // cycle-slot capacity
-  unsigned int* overflow;
-};
-
-constexpr int kFNamesSmem = 256;
-constexpr int kFRegC = 16;  // register path: <= 16 span classes
-constexpr int kFRegR = 8;   //                <= 8 collective slots
-
-// Event-parallel single pass (K1+K2+K3 in one read of the events), warp
-// specialised.  A producer warp owns the tile ring: it claims tiles in order
-// (ticket), issues their TMA bulk copies kGStages deep, and when a tile lands
-// counts its anchors, publishes the count and runs the decoupled look-back
-// for the global rank P0 of the tile's first anchor (= its first cycle slot),
-// all off the consumers' critical path.  Sixteen consumer warps process each
-// landed tile:
-//   S1  PythonCall moments (per-thread name cache) + anchor ballots -> the
-//       tile-local anchor list (position, start);
-//   S3  cycle-start marks: group start of every anchor (lower_bound over
-//       equal start_ts, cycles.cpp:137-144) as a bit per tile position, so an
-//       event's local cycle is a popcount over the bitmap;
-//   S4  every event adds its clipped span time into its cycle's row of
-//       shared-memory accumulators with 32-bit atomics (component durations
-//       cycles.cpp:157-166, class occupancy rca.cpp:87-96), the first
-//       forward_mode and workload carrier by atomicMin on the position
-//       (cycles.cpp:205-209, 256-281), keyword bits (222-227) and the
-//       per-(name, comm, rank) collective beta (rca.cpp:108-115): a slot with
-//       a single contribution per cycle is exact (0.0 + term), a cycle with a
-//       repeated slot is re-summed in event order by one thread;
-//   S5  rows -> SoA cycle outputs at slots P0 + k, coalesced.
-// Cycles whose events cross a tile edge (the trailing one of every tile, and
-// leading ones whose equal-start group reaches back into the previous tile)
-// are registered for k_fixup_cycles, which reduces them from global memory.
-// Tiles with more closed cycles than the row capacity run in chunks.
-constexpr int kGConsumerWarps = 16;
-constexpr int kGWork = kGConsumerWarps * 32;   // consumer threads 0..511
-constexpr int kGLookbackWarps = 2;
-constexpr int kGThreads = kGWork + 32 * (1 + kGLookbackWarps);  // + TMA issue + look-back warps
-constexpr int kGTile = kFTile;
-constexpr int kGStages = 5;
-constexpr int kGCycCap = 64;
-constexpr int kGAccWords = 4096;               // 16 KiB of accumulator rows
-constexpr int kGIt = kGTile / kGWork;
-
-struct RowLayout {
-  uint32_t comp, beta, coll, colln, fm, wl, kw, words, cap;
-};
-__device__ __forceinline__ RowLayout row_layout(const DevConfig& cfg, int do_beta) {
-  RowLayout L;
-  const uint32_t P = (uint32_t)cfg.cyc.n_phases;
-  const uint32_t C = do_beta ? (uint32_t)cfg.cyc.n_beta_slots : 0u;
-  const uint32_t R = do_beta ? (uint32_t)cfg.cyc.n_comm_slots : 0u;
-  L.comp = 0;
-  L.beta = 2 * P;
-  L.coll = L.beta + 2 * C;
-  L.colln = L.coll + 2 * R;
-  L.fm = L.colln + R;
-  L.wl = L.fm + 1;
-  L.kw = L.wl + 1;
-  L.words = (L.kw + 2) & ~1u;
-  const uint32_t c = kGAccWords / L.words;
-  L.cap = c < (uint32_t)kGCycCap ? c : (uint32_t)kGCycCap;
-  return L;
-}
-
-// 64-bit add of a positive value into a (lo, hi) pair of 32-bit words with
-// native 32-bit shared atomics (64-bit shared atomics are CAS loops on sm_100a)
-__device__ __forceinline__ void smem_add64(uint32_t* w, i64 v) {
-  const uint32_t lo = (uint32_t)(u64)v, hi = (uint32_t)((u64)v >> 32);
-  const uint32_t old = atomicAdd(w, lo);
-  const uint32_t carry = (old + lo < old) ? 1u : 0u;
-  if (hi | carry) atomicAdd(w + 1, hi + carry);
-}
-__device__ __forceinline__ i64 row_i64(const uint32_t* w) {
-  return (i64)(((u64)w[1] << 32) | w[0]);
-}
-
-__device__ __forceinline__ void bar_work() {  // the 16 consumer warps
-  asm volatile("bar.sync 1, %0;" ::"n"(kGWork) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-
-struct TileMetaG {
-  uint32_t t, inst, n, guess;
-  u64 tb, ib;
-};
-
-__global__ void __launch_bounds__(kGThreads, 1)
-    k_segment_pass(DevBuffers b, DevConfig cfg, FusedMeta fm, int do_beta) {
-  extern __shared__ __align__(128) unsigned char s_dyn[];
-  __shared__ uint64_t s_full[kGStages], s_empty[kGStages], s_pref[kGStages];
-  __shared__ TileMetaG s_meta[kGStages];
-  __shared__ u64 s_P[kGStages];
-  __shared__ WarpNameRow s_rows[kGConsumerWarps * kWarpNameRows];
-  __shared__ uint32_t s_warp_cnt[kGConsumerWarps];
-  __shared__ uint32_t s_cbits[kGTile / 32];
-  __shared__ uint32_t s_wpre[kGTile / 32];
-  __shared__ uint16_t s_first[kGTile + 1];
-  __shared__ uint32_t s_dup, s_nlead, s_unknown, s_wide, s_reorder;
-
-  unsigned char* s_tiles = s_dyn;
-  uint16_t* s_apos = reinterpret_cast<uint16_t*>(s_dyn + kGStages * kFTileBytes);
-  i64* s_astart = reinterpret_cast<i64*>(s_dyn + kGStages * kFTileBytes + kGTile * 2);
-  uint32_t* s_acc = reinterpret_cast<uint32_t*>(s_astart + kGTile);
-
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < kGStages; ++s) {
-      mbar_init(&s_full[s], 1);
-      mbar_init(&s_empty[s], 1);
-      mbar_init(&s_pref[s], 1);
-    }
-    mbar_fence_init();
-  }
-  __syncthreads();
-  // static schedule: this CTA's k-th tile is blockIdx.x + k * gridDim.x, so
-  // the tile metadata can be fetched 32 tiles ahead (all CTAs are resident:
-  // the grid is one CTA per SM)
-  const uint32_t G = gridDim.x;
-  const uint32_t n_mine = b.n_tiles > blockIdx.x ? (b.n_tiles - blockIdx.x + G - 1) / G : 0;
-
-  if (warp == kGConsumerWarps) {
-    // ======================= TMA issue warp
-    TileMetaG pm{};  // lane l: metadata of this CTA's tile (batch + l)
-    for (uint32_t it = 0; it < n_mine + kGLookbackWarps; ++it) {
-      if ((it & 31u) == 0) {
-        const uint32_t k = it + lane;
-        pm.t = k < n_mine ? blockIdx.x + k * G : 0xffffffffu;
-        if (k < n_mine) {
-          pm.inst = b.tile_inst[pm.t];
-          pm.tb = b.tile_begin[pm.t];
-          pm.n = (uint32_t)(b.tile_end[pm.t] - pm.tb);
-          pm.ib = b.inst_off[pm.inst];
-          pm.guess = b.inst[pm.inst].guess;
-        }
-      }
-      const int st = it % kGStages;
-      if (it >= (uint32_t)kGStages) mbar_wait(&s_empty[st], ((it / kGStages) - 1) & 1u);
-      TileMetaG m;
-      const int src = it & 31;
-      m.t = __shfl_sync(0xffffffffu, pm.t, src);
-      m.inst = __shfl_sync(0xffffffffu, pm.inst, src);
-      m.n = __shfl_sync(0xffffffffu, pm.n, src);
-      m.guess = __shfl_sync(0xffffffffu, pm.guess, src);
-      m.tb = __shfl_sync(0xffffffffu, pm.tb, src);
-      m.ib = __shfl_sync(0xffffffffu, pm.ib, src);
-      if (lane == 0) {
-        s_meta[st] = m;
-        if (it < n_mine) {
-          const uint32_t bytes = m.n * (uint32_t)sizeof(cs_event);
-          mbar_expect_tx(&s_full[st], bytes);
-          bulk_g2s(s_tiles + st * kFTileBytes, b.ev + m.tb, bytes, &s_full[st]);
-        } else {
-          mbar_arrive(&s_full[st]);  // sentinel for the consumers / a look-back warp
-        }
-      }
-      __syncwarp();
-    }
-    return;
-  }
-  if (warp > kGConsumerWarps) {
-    // ======================= look-back warps: tiles it = w, w + NW, ...
-    const uint32_t w = (uint32_t)(warp - kGConsumerWarps - 1);
-    for (uint32_t it = w;; it += kGLookbackWarps) {
-      const int st = it % kGStages;
-      mbar_wait(&s_full[st], (it / kGStages) & 1u);
-      const TileMetaG m = s_meta[st];
-      if (m.t >= b.n_tiles) break;
-      u64 P0 = 0;
-      if (!(fm.debug & 1)) {
-        const uint32_t c = warp_count_anchors(reinterpret_cast<const cs_event*>(s_tiles + st * kFTileBytes),
-                                              m.n, m.guess);
-        if (lane == 0) publish_aggregate(fm.state, m.t, c);
-        P0 = lookback_wait(fm.state, m.t, c);
-        if (lane == 0) {
-          fm.t_cnt[m.t] = c;
-          fm.t_pref[m.t] = P0;
-          if (P0 + c > fm.capacity) atomicOr(fm.overflow, 1u);
-        }
-      }
-      if (lane == 0) {
-        s_P[st] = P0;
-        mbar_arrive(&s_pref[st]);
-      }
-      __syncwarp();
-    }
-    return;
-  }
-
-  // ========================= consumer warps
-  // packed per-name info: bits 0-3 phase (15 none), 4-11 beta slot (255 none),
-  // 12-13 keyword bits; names beyond kFNamesSmem are read from global
-  __shared__ uint32_t s_ninfo[kFNamesSmem];
-  const RowLayout L = row_layout(cfg, do_beta);
-  const int P = cfg.cyc.n_phases;
-  const int C = do_beta ? cfg.cyc.n_beta_slots : 0;
-  const int R = do_beta ? cfg.cyc.n_comm_slots : 0;
-  const uint32_t tid = threadIdx.x;
-  auto pack_info = [&](const cs_name_info& ni) -> uint32_t {
-    const uint32_t ph = (ni.phase >= 0 && ni.phase < P) ? (uint32_t)ni.phase : 15u;
-    const uint32_t bs = (ni.beta_slot >= 0 && ni.beta_slot < C) ? (uint32_t)ni.beta_slot : 255u;
-    return ph | (bs << 4) | ((ni.flags & 3u) << 12);
-  };
-  for (uint32_t i = tid; i < b.n_names && i < (uint32_t)kFNamesSmem; i += kGWork)
-    s_ninfo[i] = pack_info(b.names[i]);
-  bar_work();
-  NameCache cache;
-  cache_clear(cache);
-  uint32_t cur_inst = 0xffffffffu;
-  for (uint32_t it = 0;; ++it) {
-    const int stage = it % kGStages;
-    const uint32_t ph = (it / kGStages) & 1u;
-    mbar_wait(&s_full[stage], ph);
-    const TileMetaG m = s_meta[stage];
-    if (m.t >= b.n_tiles) break;
-    if (m.inst != cur_inst) {
-      if (cur_inst != 0xffffffffu)
-        cache_flush_warp(cache, b.stats + (u64)cur_inst * b.n_names, s_rows + warp * kWarpNameRows);
-      cur_inst = m.inst;
-    }
-    NameStat* gstats = b.stats + (u64)m.inst * b.n_names;
-    const int4* t4 = reinterpret_cast<const int4*>(s_tiles + stage * kFTileBytes);
-
-    // ---- S1: this thread's events stay in registers through S4
-    int4 H0[kGIt], H1[kGIt];
-    uint32_t masks[kGIt];
-#pragma unroll
-    for (int q = 0; q < kGIt; ++q) {
-      const uint32_t j = (uint32_t)warp * (kGIt * 32) + q * 32 + lane;
-      bool is_anchor = false;
-      if (j < m.n) {
-        H0[q] = t4[2 * j];
-        H1[q] = t4[2 * j + 1];
-        if (((uint32_t)H1[q].y & 0xffu) == CS_SPAN) {
-          if ((((uint32_t)H1[q].y >> 8) & 0xffu) == CS_CAT_PYTHON_CALL)
-            cache_add(cache, gstats, (uint32_t)H1[q].x,
-                      (i64)(((u64)(uint32_t)H0[q].w << 32) | (uint32_t)H0[q].z));
-          is_anchor = (uint32_t)H1[q].x == m.guess;
-        }
-      } else {
-        H0[q] = make_int4(0, 0, 0, 0);
-        H1[q] = make_int4(0, CS_FLOW, 0, 0);  // ignored
-      }
-      masks[q] = __ballot_sync(0xffffffffu, is_anchor);
-    }
-    uint32_t my = 0;
-#pragma unroll
-    for (int q = 0; q < kGIt; ++q) my += __popc(masks[q]);
-    if (lane == 0) s_warp_cnt[warp] = my;
-    if (tid < kGTile / 32) s_cbits[tid] = 0u;
-    if (tid == 0) {
-      s_dup = 0u;
-      s_nlead = 0u;
-      s_unknown = 0u;
-      s_wide = 0u;
-      s_reorder = 0u;
-    }
-    bar_work();
-    uint32_t base, total;
-    {
-      const uint32_t c = lane < kGConsumerWarps ? s_warp_cnt[lane] : 0u;
-      uint32_t incl = c;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += v;
-      }
-      base = __shfl_sync(0xffffffffu, incl - c, warp);
-      total = __shfl_sync(0xffffffffu, incl, 31);
-    }
-#pragma unroll
-    for (int q = 0; q < kGIt; ++q) {
-      const uint32_t mk = masks[q];
-      if (mk & (1u << lane)) {
-        const uint32_t r = base + __popc(mk & lanemask_lt());
-        s_apos[r] = (uint16_t)((uint32_t)warp * (kGIt * 32) + q * 32 + lane);
-        s_astart[r] = (i64)(((u64)(uint32_t)H0[q].y << 32) | (uint32_t)H0[q].x);
-      }
-      base += __popc(mk);
-    }
-    const uint32_t n_loc = total >= 1 ? total - 1 : 0;  // cycles closed inside the tile
-    const uint32_t n_chunks = n_loc ? (n_loc + L.cap - 1) / L.cap : 0;
-    bar_work();
-    // ---- S3: cycle-start marks, 32-bit safety, rows of the first chunk zeroed
-    for (uint32_t k = tid; k < total; k += kGWork) {
-      uint32_t pf = s_apos[k];
-      const i64 a = s_astart[k];
-      while (pf > 0 && reinterpret_cast<const i64*>(t4 + 2 * (pf - 1))[0] == a) --pf;
-      s_first[k] = (uint16_t)pf;
-      const uint32_t bit = 1u << (pf & 31);
-      if (atomicOr(&s_cbits[pf >> 5], bit) & bit) s_dup = 1u;  // equal-start anchors
-      if (pf == 0 && m.tb > m.ib) atomicAdd(&s_nlead, 1u);
-    }
-    {
-      const uint32_t nw = (n_loc < L.cap ? n_loc : L.cap) * L.words;
-      for (uint32_t i = tid; i < nw; i += kGWork) {
-        const uint32_t f = i % L.words;
-        s_acc[i] = (f == L.fm || f == L.wl) ? 0xffffffffu : 0u;
-      }
-    }
-    bar_work();
-    if (warp == 0) {
-      const uint32_t c = __popc(s_cbits[lane]);
-      uint32_t incl = c;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += v;
-      }
-      s_wpre[lane] = incl - c;
-    }
-    // per-(cycle, slot) sums fit 32 bits when events x duration < 2^32
-    for (uint32_t k = tid; k < n_loc; k += kGWork) {
-      const u64 dur = (u64)(s_astart[k + 1] - s_astart[k]);
-      const u64 nev = (u64)(s_first[k + 1] - s_first[k]);
-      if (dur >= (1ull << 32) || dur * nev >= (1ull << 32)) s_wide = 1u;
-    }
-    bar_work();
-    const uint32_t nlead = s_nlead;
-    const bool dup = s_dup != 0u;
-    const bool wide = s_wide != 0u;
-    bool have_p = false;
-    u64 P0 = 0;
-    for (uint32_t ch = 0; ch < n_chunks; ++ch) {
-      const uint32_t c0 = ch * L.cap;
-      const uint32_t c1 = min(n_loc, c0 + L.cap);
-      if (ch > 0) {
-        const uint32_t nw = (c1 - c0) * L.words;
-        for (uint32_t i = tid; i < nw; i += kGWork) {
-          const uint32_t f = i % L.words;
-          s_acc[i] = (f == L.fm || f == L.wl) ? 0xffffffffu : 0u;
-        }
-        bar_work();
-      }
-      // ---- S4: this thread's events into their cycles' rows
-#pragma unroll
-      for (int q = 0; q < kGIt; ++q) {
-        if (fm.debug & 2) break;
-        const uint32_t j = (uint32_t)warp * (kGIt * 32) + q * 32 + lane;
-        uint32_t k;
-        if (!dup) {
-          const uint32_t w = j >> 5;
-          k = s_wpre[w] + __popc(s_cbits[w] & ((2u << (j & 31)) - 1u)) - 1u;
-        } else {  // upper_bound over the group starts
-          uint32_t a = 0, z = total;
-          while (a < z) {
-            const uint32_t mid = (a + z) >> 1;
-            if (s_first[mid] <= j) a = mid + 1;
-            else z = mid;
-          }
-          k = a - 1;
-        }
-        if (j >= m.n || k < c0 || k >= c1 || k < nlead) continue;
-        uint32_t* row = s_acc + (k - c0) * L.words;
-        const int4 h0 = H0[q], h1 = H1[q];
-        const uint32_t flags = (uint32_t)h1.y >> 16;
-        const uint32_t kind = (uint32_t)h1.y & 0xffu;
-        const uint32_t name = (uint32_t)h1.x;
-        const uint32_t info = name < (uint32_t)kFNamesSmem ? s_ninfo[name] : pack_info(b.names[name]);
-        const i64 st = (i64)(((u64)(uint32_t)h0.y << 32) | (uint32_t)h0.x);
-        const i64 d = (i64)(((u64)(uint32_t)h0.w << 32) | (uint32_t)h0.z);
-        const i64 ce = s_astart[k + 1];
-        const i64 end = st + d;
-        const i64 clipped = (end < ce ? end : ce) - st;
-        const bool span = kind == CS_SPAN;
-        const bool pos = span && clipped > 0;
-        const uint32_t phs = info & 15u, bs = (info >> 4) & 255u;
-        if (!wide) {
-          if (pos && phs != 15u) atomicAdd(&row[L.comp + 2 * phs], (uint32_t)clipped);
-          if (pos && d > 0 && bs != 255u) atomicAdd(&row[L.beta + 2 * bs], (uint32_t)clipped);
-        } else {
-          if (pos && phs != 15u) smem_add64(&row[L.comp + 2 * phs], clipped);
-          if (pos && d > 0 && bs != 255u) smem_add64(&row[L.beta + 2 * bs], clipped);
-        }
-        if (flags & (CS_EV_FM_MASK | CS_EV_HAS_BATCH)) {
-          if (flags & CS_EV_FM_MASK) atomicMin(&row[L.fm], (j << 2) | (flags & CS_EV_FM_MASK));
-          if (flags & CS_EV_HAS_BATCH) atomicMin(&row[L.wl], j);
-        }
-        if (span && (info & (3u << 12))) atomicOr(&row[L.kw], (info >> 12) & 3u);
-        if (pos && d > 0 && (flags & CS_EV_HAS_COMM) &&
-            (((uint32_t)h1.y >> 8) & 0xffu) == CS_CAT_COLLECTIVE_COMM) {
-          const uint32_t slot = (uint32_t)h1.w;
-          if (slot < (uint32_t)R) {
-            const uint32_t n0 = atomicAdd(&row[L.colln + slot], 1u);
-            if (n0 == 0u) {
-              const double term = __ddiv_rn((double)clipped, (double)(ce - s_astart[k]));
-              *reinterpret_cast<double*>(&row[L.coll + 2 * slot]) = term;
-            } else {
-              atomicOr(&row[L.kw], 0x80000000u);  // repeated slot: ordered re-sum
-              s_reorder = 1u;
-            }
-          }
-        }
-      }
-      if (!have_p && warp == 0) mbar_wait(&s_pref[stage], ph);
-      bar_work();
-      if (!have_p) {
-        P0 = s_P[stage];
-        have_p = true;
-      }
-      // repeated collective slots: the reference's event-ordered sum (rca.cpp:112-113)
-      if (s_reorder) {
-        for (uint32_t k = c0 + tid; k < c1; k += kGWork) {
-          uint32_t* row = s_acc + (k - c0) * L.words;
-          if (!(row[L.kw] & 0x80000000u) || k < nlead) continue;
-          double* coll = reinterpret_cast<double*>(&row[L.coll]);
-          for (int r = 0; r < R; ++r) coll[r] = 0.0;
-          const i64 cs = s_astart[k], ce = s_astart[k + 1];
-          for (uint32_t j = s_first[k]; j < s_first[k + 1]; ++j) {
-            const int4 h0 = t4[2 * j], h1 = t4[2 * j + 1];
-            if (((uint32_t)h1.y & 0xffu) != CS_SPAN) continue;
-            const uint32_t flags = (uint32_t)h1.y >> 16;
-            if ((((uint32_t)h1.y >> 8) & 0xffu) != CS_CAT_COLLECTIVE_COMM || !(flags & CS_EV_HAS_COMM))
-              continue;
-            const i64 st = (i64)(((u64)(uint32_t)h0.y << 32) | (uint32_t)h0.x);
-            const i64 d = (i64)(((u64)(uint32_t)h0.w << 32) | (uint32_t)h0.z);
-            const i64 end = st + d;
-            const i64 clipped = (end < ce ? end : ce) - st;
-            if (d <= 0 || clipped <= 0) continue;
-            const uint32_t slot = (uint32_t)h1.w;
-            if (slot < (uint32_t)R)
-              coll[slot] = __dadd_rn(coll[slot], __ddiv_rn((double)clipped, (double)(ce - cs)));
-          }
-        }
-        bar_work();
-      }
-      // ---- S5: rows -> cycle outputs (coalesced over the chunk's cycles)
-      if (P0 + total <= fm.capacity && !(fm.debug & 4)) {
-        const uint32_t ncc = c1 - c0;
-        for (uint32_t i = tid; i < ncc; i += kGWork) {
-          const uint32_t k = c0 + i;
-          if (k < nlead) continue;
-          const uint32_t* row = s_acc + i * L.words;
-          const u64 g = P0 + k;
-          const i64 cs = s_astart[k];
-          const uint32_t ap = s_apos[k];
-          b.c_start[g] = cs;
-          b.c_end[g] = s_astart[k + 1];
-          b.c_apos[g] = m.tb + ap;
-          b.c_aend[g] = cs + reinterpret_cast<const i64*>(t4 + 2 * ap)[1];
-          b.c_first[g] = m.tb + s_first[k];
-          b.c_last[g] = m.tb + s_first[k + 1];
-          b.c_inst[g] = m.inst;
-          const uint32_t fmw = row[L.fm];
-          const uint32_t fm_cls = fmw == 0xffffffffu ? 0u : (fmw & CS_EV_FM_MASK);
-          const uint32_t kw = row[L.kw];
-          const bool pkw = kw & CS_NAME_PREFILL_KW, dkw = kw & CS_NAME_DECODE_KW;
-          uint8_t stg = CS_STAGE_UNKNOWN;
-          if (fm_cls == CS_EV_FM_PREFILL) stg = CS_STAGE_PREFILL;
-          else if (fm_cls == CS_EV_FM_DECODE) stg = CS_STAGE_DECODE;
-          if (stg == CS_STAGE_UNKNOWN && pkw != dkw) stg = pkw ? CS_STAGE_PREFILL : CS_STAGE_DECODE;
-          b.c_local[g] = stg;
-          b.c_stage[g] = stg;
-          const uint32_t wj = row[L.wl];
-          int32_t wl = -1;
-          if (wj != 0xffffffffu) {
-            const int4 h1 = t4[2 * wj + 1];
-            wl = ((uint32_t)h1.y >> 16) & CS_EV_WL_OK ? (int32_t)(uint32_t)h1.z : -2;
-          }
-          b.c_wl[g] = wl;
-          if (stg == CS_STAGE_UNKNOWN) atomicAdd(&s_unknown, 1u);
-        }
-        for (uint32_t f = tid; f < ncc * (uint32_t)P; f += kGWork) {
-          const uint32_t i = f / (uint32_t)P, p = f - i * (uint32_t)P;
-          if (c0 + i < nlead) continue;
-          b.c_comp[(P0 + c0) * P + f] = row_i64(s_acc + i * L.words + L.comp + 2 * p);
-        }
-        for (uint32_t f = tid; f < ncc * (uint32_t)C; f += kGWork) {
-          const uint32_t i = f / (uint32_t)C, c = f - i * (uint32_t)C;
-          const uint32_t k = c0 + i;
-          if (k < nlead) continue;
-          const i64 dur = s_astart[k + 1] - s_astart[k];
-          const i64 t = dur > 0 ? row_i64(s_acc + i * L.words + L.beta + 2 * c) : 0;
-          b.c_beta_tot[(P0 + c0) * C + f] = t;
-          b.c_beta[(P0 + c0) * C + f] = t > 0 ? __ddiv_rn((double)t, (double)dur) : 0.0;
-        }
-        for (uint32_t f = tid; f < ncc * (uint32_t)R; f += kGWork) {
-          const uint32_t i = f / (uint32_t)R, r = f - i * (uint32_t)R;
-          if (c0 + i < nlead) continue;
-          const uint32_t* row = s_acc + i * L.words;
-          const uint32_t n = row[L.colln + r];
-          b.c_coll[(P0 + c0) * R + f] = n ? *reinterpret_cast<const double*>(&row[L.coll + 2 * r]) : 0.0;
-          b.c_coll_n[(P0 + c0) * R + f] = (uint8_t)(n > 255u ? 255u : n);
-        }
-      }
-      if (ch + 1 < n_chunks) bar_work();  // rows are reused by the next chunk
-    }
-    if (!have_p) {
-      if (warp == 0) mbar_wait(&s_pref[stage], ph);
-      bar_work();
-      P0 = s_P[stage];
-    }
-    // boundary cycles -> k_fixup_cycles: leading ones whose group reaches the
-    // previous tile, and the trailing one (its end anchor lies in a later tile)
-    if (P0 + total <= fm.capacity && total > 0) {
-      const uint32_t nb = (nlead < total ? nlead : total - 1) + 1;  // leads + trailing
-      for (uint32_t i = tid; i < nb; i += kGWork) {
-        const bool trailing = i + 1 == nb;
-        const uint32_t k = trailing ? total - 1 : i;
-        const bool lead = k < nlead;
-        const u64 g = P0 + k;
-        const uint32_t ap = s_apos[k];
-        b.c_start[g] = s_astart[k];
-        b.c_apos[g] = m.tb + ap;
-        b.c_aend[g] = s_astart[k] + reinterpret_cast<const i64*>(t4 + 2 * ap)[1];
-        b.c_inst[g] = m.inst;
-        if (!trailing) {
-          b.c_end[g] = s_astart[k + 1];
-          b.c_last[g] = m.tb + s_first[k + 1];
-        }
-        const unsigned int slot = atomicAdd(fm.fix_n, 1u);
-        fm.fix_list[slot] = g;
-        fm.fix_flags[slot] = (trailing ? 1u : 0u) | (lead ? 2u : 0u);
-      }
-    }
-    bar_work();  // stage, anchor list, rows consumed
-    if (tid == 0) {
-      if (s_unknown) atomicAdd(&b.inst[m.inst].n_unknown, (u64)s_unknown);
-      fence_proxy_async();
-      mbar_arrive(&s_empty[stage]);
-    }
-  }
-  if (cur_inst != 0xffffffffu)
-    cache_flush_warp(cache, b.stats + (u64)cur_inst * b.n_names, s_rows + warp * kWarpNameRows);
-}
-
-// Per-instance slot base and anchor count from the tile look-back results.
-__global__ void k_fused_inst(DevBuffers b, FusedMeta fm, uint64_t* cyc_off) {
-  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i > b.n_inst) return;
-  if (i == b.n_inst) {
-    const uint32_t tl = b.n_tiles;
-    cyc_off[i] = tl ? fm.t_pref[tl - 1] + fm.t_cnt[tl - 1] : 0;
-    return;
-  }
-  const uint32_t t0 = b.inst_first_tile[i];
-  const uint32_t t1 = i + 1 < b.n_inst ? b.inst_first_tile[i + 1] : b.n_tiles;
-  if (t0 >= t1) {  // no events: base = next instance's base (computed by scan below)
-    cyc_off[i] = t0 < b.n_tiles ? fm.t_pref[t0] : (b.n_tiles ? fm.t_pref[b.n_tiles - 1] + fm.t_cnt[b.n_tiles - 1] : 0);
-    b.inst[i].n_anchors = 0;
-    return;
-  }
-  cyc_off[i] = fm.t_pref[t0];
-  b.inst[i].n_anchors = fm.t_pref[t1 - 1] + fm.t_cnt[t1 - 1] - fm.t_pref[t0];
-}
-
-// Boundary cycles: find the missing bounds, then the same sequential
-// reduction over global memory; the instance's last anchor becomes a hole.
-__global__ void k_fixup_cycles(DevBuffers b, DevConfig cfg, FusedMeta fm, int do_beta,
-                               uint32_t n_fix, uint32_t words) {
-  extern __shared__ __align__(16) uint32_t s_fix[];
-  const uint32_t f = blockIdx.x * blockDim.x + threadIdx.x;
-  if (f >= n_fix) return;
-  const u64 g = fm.fix_list[f];
-  const uint32_t flags = fm.fix_flags[f];
-  const uint32_t inst = b.c_inst[g];
-  const u64 ib = b.inst_off[inst];
-  const i64 cs = b.c_start[g];
-  const u64 apos = b.c_apos[g];
-  i64 ce;
-  u64 last;
-  if (flags & 1u) {
-    // next anchor = rank g+1: the first anchor of the first later tile with anchors
-    const u64 r = g + 1;
-    uint32_t lo = 0, hi = b.n_tiles;  // last tile with t_pref <= r and t_cnt > 0 ... search
-    while (hi - lo > 1) {
-      const uint32_t mid = (lo + hi) >> 1;
-      if (fm.t_pref[mid] <= r) lo = mid;
-      else hi = mid;
-    }
-    // tiles with t_pref == r may have zero anchors: walk forward to one with anchors
-    uint32_t u = lo;
-    while (u < b.n_tiles && (fm.t_cnt[u] == 0 || fm.t_pref[u] + fm.t_cnt[u] <= r)) ++u;
-    if (u >= b.n_tiles || b.tile_inst[u] != inst || fm.t_pref[u] != r) {
-      // last anchor of the instance: hole
-      b.c_wl[g] = -4;
-      b.c_local[g] = 255;
-      b.c_stage[g] = CS_STAGE_UNKNOWN;
-      b.c_end[g] = cs;
-      b.c_first[g] = apos;
-      b.c_last[g] = apos;
-      return;
-    }
-    // first anchor event of tile u: scan the tile for it (it is the anchor)
-    const uint32_t name = b.inst[inst].guess;
-    u64 p = b.tile_begin[u];
-    while (!(b.ev[p].kind == CS_SPAN && b.ev[p].name_id == name)) ++p;
-    ce = b.ev[p].start_ts;
-    last = group_start(b.ev, p, ib, ce);
-    b.c_end[g] = ce;
-    b.c_last[g] = last;
-  } else {
-    ce = b.c_end[g];
-    last = b.c_last[g];
-  }
-  const u64 first = group_start(b.ev, apos, ib, cs);
-  const int C = cfg.cyc.n_beta_slots, R = cfg.cyc.n_comm_slots;
-  i64* beta = reinterpret_cast<i64*>(s_fix + (u64)threadIdx.x * words);
-  double* coll = reinterpret_cast<double*>(beta + C);
-  uint32_t* colln = reinterpret_cast<uint32_t*>(coll + R);
-  const CycAcc acc = accumulate_cycle(b.names, cfg, do_beta, b.ev, first, last, cs, ce, false,
-                                      beta, coll, colln);
-  write_cycle(b, cfg, do_beta, acc, g, inst, cs, ce, apos, b.c_aend[g], first, last, beta, coll,
-              colln);
-}
-
-uint32_t fused_scratch_words(const DevConfig& cfg) {
-  const uint32_t w = (uint32_t)(cfg.cyc.n_beta_slots + cfg.cyc.n_comm_slots) * 2 +
-                     (uint32_t)cfg.cyc.n_comm_slots + 1;
-  return (w + 1) & ~1u;
-}
-
-int launch_fused_segment(const DevBuffers& b, const DevConfig& cfg, const FusedMetaHost& mh,
-                         int do_beta, cudaStream_t s, uint64_t* launches) {
-  if (b.n_tiles == 0) return 0;
-  FusedMeta fm{mh.debug, mh.state, mh.ticket, mh.t_cnt, mh.t_pref, mh.fix_list, mh.fix_n,
-               mh.fix_flags, mh.capacity, mh.overflow};
-  const int smem = kGStages * (int)kFTileBytes + kGTile * (2 + 8) + kGAccWords * 4;  // 186 KiB
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(k_segment_pass, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    configured = true;
-  }
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  int per_sm = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_segment_pass, kGThreads, smem);
-  if (per_sm < 1) per_sm = 1;
-  const uint32_t want = (uint32_t)(sms * per_sm);
-  const uint32_t grid = b.n_tiles < want ? b.n_tiles : want;
-  k_segment_pass<<<grid, kGThreads, smem, s>>>(b, cfg, fm, do_beta);
-  ++*launches;
-  return 0;
-}
-
-void launch_fused_inst(const DevBuffers& b, const FusedMetaHost& mh, uint64_t* cyc_off,
-                       cudaStream_t s, uint64_t* launches) {
-  FusedMeta fm{mh.debug, mh.state, mh.ticket, mh.t_cnt, mh.t_pref, mh.fix_list, mh.fix_n, mh.fix_flags,
-               mh.capacity, mh.overflow};
-  k_fused_inst<<<(b.n_inst + 1 + 255) / 256, 256, 0, s>>>(b, fm, cyc_off);
-  ++*launches;
-}
-
-void launch_fixup_cycles(const DevBuffers& b, const DevConfig& cfg, const FusedMetaHost& mh,
-                         int do_beta, uint32_t n_fix, cudaStream_t s, uint64_t* launches) {
-  if (!n_fix) return;
-  FusedMeta fm{mh.debug, mh.state, mh.ticket, mh.t_cnt, mh.t_pref, mh.fix_list, mh.fix_n, mh.fix_flags,
-               mh.capacity, mh.overflow};
-  const uint32_t words = fused_scratch_words(cfg);
-  const int threads = 64;
-  const int smem = threads * (int)words * 4;
-  cudaFuncSetAttribute(k_fixup_cycles, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  k_fixup_cycles<<<(n_fix + threads - 1) / threads, threads, smem, s>>>(b, cfg, fm, do_beta, n_fix,
-                                                                       words);
-  ++*launches;
-}
+constexpr int kFNamesSmem = 256;  // name infos staged in shared memory by the reduce
 
 // ------------------------------------- K3'' thread-per-cycle reduce, v2
 // One thread per cycle walks its events in order (the reference's own loops:
@@ -2686,6 +1853,97 @@ __global__ void __launch_bounds__(256, 3) k_cycle_reduce_v2(DevBuffers b, DevCon
   const uint32_t inst = unk ? b.c_inst[g] : 0xffffffffu;
   const uint32_t grp = __match_any_sync(0xffffffffu, inst);
   if (unk && (tid & 31) == (uint32_t)(__ffs(grp) - 1)) atomicAdd(&b.inst[inst].n_unknown, (u64)__popc(grp));
+}
+
+// ------------------------------ K3w thread-per-cycle reduce, any slot count
+// The reference keys component durations by phase name, class occupancy by
+// span name and collective beta by (name, commHash, rank) in std::maps
+// (cycles.cpp:157-166, rca.cpp:85-115): no bound on their number.  When the
+// shared-memory [slot][thread] accumulators of k_cycle_reduce_v2 do not fit
+// (more than 15 phases or 254 classes, or rows too wide for >= 64 threads per
+// CTA), each thread accumulates straight into its own (cycle, slot) rows of
+// the outputs in global memory (zeroed before the launch; rows are private to
+// the thread, so no atomics; L1/L2 absorb the read-modify-writes).  Same
+// event loop, same arithmetic order; k_beta_finalize turns the totals into
+// beta afterwards.
+__global__ void __launch_bounds__(128) k_cycle_reduce_wide(DevBuffers b, DevConfig cfg, int do_beta) {
+  const int P = cfg.cyc.n_phases;
+  const int C = do_beta ? cfg.cyc.n_beta_slots : 0;
+  const int R = do_beta ? cfg.cyc.n_comm_slots : 0;
+  const u64 g = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= b.n_cycles) return;
+  const i64 cs = b.c_start[g], ce = b.c_end[g];
+  const u64 first = b.c_first[g], last = b.c_last[g];
+  const bool no_comp = b.c_apos[g] == kNone;  // frequency-fallback cycle (cycles.cpp:332-340)
+  const i64 dur = ce - cs;
+  int64_t* comp = b.c_comp + g * (u64)P;
+  int64_t* beta = b.c_beta_tot + g * (u64)C;
+  double* coll = b.c_coll + g * (u64)R;
+  uint8_t* colln = b.c_coll_n + g * (u64)R;
+  uint32_t fm_cls = 0, kw = 0;
+  bool fm_found = false, batch_found = false;
+  int32_t wl = -1;
+  for (u64 j0 = first; j0 < last; j0 += kRedUnroll) {
+    Ev8 e[kRedUnroll];
+#pragma unroll
+    for (int q = 0; q < kRedUnroll; ++q) {
+      if (j0 + q < last) e[q] = ldg256(b.ev + j0 + q);
+      else e[q].c = (u64)CS_FLOW << 32;
+    }
+#pragma unroll
+    for (int q = 0; q < kRedUnroll; ++q) {
+      const uint32_t name = (uint32_t)e[q].c;
+      const uint32_t kc = (uint32_t)(e[q].c >> 32);
+      const uint32_t flags = kc >> 16;
+      if (!fm_found && (flags & CS_EV_FM_MASK)) {
+        fm_found = true;
+        fm_cls = flags & CS_EV_FM_MASK;
+      }
+      if (!batch_found && (flags & CS_EV_HAS_BATCH)) {
+        batch_found = true;
+        wl = (flags & CS_EV_WL_OK) ? (int32_t)(uint32_t)e[q].d : -2;
+      }
+      if ((kc & 0xffu) != CS_SPAN) continue;
+      const cs_name_info ni = b.names[name];
+      kw |= ni.flags & 3u;
+      const i64 st = (i64)e[q].a, d = (i64)e[q].b;
+      const i64 end = st + d;
+      const i64 clipped = (end < ce ? end : ce) - st;
+      if (clipped <= 0) continue;
+      if (ni.phase >= 0 && ni.phase < P && !no_comp) comp[ni.phase] += clipped;
+      if (do_beta && d > 0) {
+        if (ni.beta_slot >= 0 && ni.beta_slot < C) beta[ni.beta_slot] += clipped;
+        if (((kc >> 8) & 0xffu) == CS_CAT_COLLECTIVE_COMM && (flags & CS_EV_HAS_COMM)) {
+          const uint32_t slot = (uint32_t)(e[q].d >> 32);
+          if (slot < (uint32_t)R) {
+            coll[slot] = __dadd_rn(coll[slot], __ddiv_rn((double)clipped, (double)dur));
+            if (colln[slot] < 255u) colln[slot] += 1u;
+          }
+        }
+      }
+    }
+  }
+  uint8_t stage = CS_STAGE_UNKNOWN;
+  if (fm_cls == CS_EV_FM_PREFILL) stage = CS_STAGE_PREFILL;
+  else if (fm_cls == CS_EV_FM_DECODE) stage = CS_STAGE_DECODE;
+  const bool pkw = kw & CS_NAME_PREFILL_KW, dkw = kw & CS_NAME_DECODE_KW;
+  if (stage == CS_STAGE_UNKNOWN && pkw != dkw) stage = pkw ? CS_STAGE_PREFILL : CS_STAGE_DECODE;
+  b.c_local[g] = stage;
+  b.c_stage[g] = stage;
+  b.c_wl[g] = wl;
+  if (stage == CS_STAGE_UNKNOWN) atomicAdd(&b.inst[b.c_inst[g]].n_unknown, 1ull);
+}
+
+// beta = total / cycle duration for every (cycle, class) of the wide reduce
+// (rca.cpp:95-96, 119-121), coalesced over the row-major table
+__global__ void k_beta_finalize(DevBuffers b, int C) {
+  const u64 k = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= b.n_cycles * (u64)C) return;
+  const u64 g = k / (u64)C;
+  const i64 dur = b.c_end[g] - b.c_start[g];
+  const i64 t = dur > 0 ? b.c_beta_tot[k] : 0;
+  b.c_beta_tot[k] = t;
+  b.c_beta[k] = t > 0 ? __ddiv_rn((double)t, (double)dur) : 0.0;
 }
 
 // ---------------------------------------------------- wire-format expand
@@ -3147,9 +2405,27 @@ void launch_cycle_reduce_tpc(const DevBuffers& b, const DevConfig& cfg, int do_b
   const int R = do_beta ? cfg.cyc.n_comm_slots : 0;
   const int per_thread = (P + C + R) * 8 + R * 4;
   int nt = 256;
-  while (nt > 32 && (nt + 1) * per_thread + nt * 8 > 100 * 1024) nt >>= 1;
+  while (nt > 64 && (nt + 1) * per_thread + nt * 8 > 100 * 1024) nt >>= 1;
   const int smem = (nt + 1) * per_thread + nt * 8;  // padded [slot][thread] rows + durations
   (void)variant;
+  if (P > 15 || C > 254 || smem > 100 * 1024) {
+    // more slots than the shared-memory accumulators hold: global-memory rows
+    const u64 nc = b.n_cycles;
+    if (P) cudaMemsetAsync(b.c_comp, 0, nc * (u64)P * sizeof(int64_t), s);
+    if (C) cudaMemsetAsync(b.c_beta_tot, 0, nc * (u64)C * sizeof(int64_t), s);
+    if (R) {
+      cudaMemsetAsync(b.c_coll, 0, nc * (u64)R * sizeof(double), s);
+      cudaMemsetAsync(b.c_coll_n, 0, nc * (u64)R, s);
+    }
+    k_cycle_reduce_wide<<<(unsigned)((nc + 127) / 128), 128, 0, s>>>(b, cfg, do_beta);
+    ++*launches;
+    if (C) {
+      const u64 n = nc * (u64)C;
+      k_beta_finalize<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(b, C);
+      ++*launches;
+    }
+    return;
+  }
   cudaFuncSetAttribute(k_cycle_reduce_v2, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   const unsigned grid = (unsigned)((b.n_cycles + nt - 1) / nt);
   k_cycle_reduce_v2<<<grid, nt, smem, s>>>(b, cfg, do_beta);
@@ -3240,8 +2516,11 @@ void launch_score(const DevBuffers& b, const DevConfig& cfg, uint64_t n_records,
     ++*launches;
     return;
   }
-  // all instances share the feature count of instance 0's model in this build
-  const uint32_t nf = h_models[0].n_features;
+  // one traversal kernel for the batch, instantiated for the widest model:
+  // narrower models never read the extra feature slots (their nodes test
+  // features < their own count), so instances may mix feature counts
+  uint32_t nf = 0;
+  for (uint32_t i = 0; i < b.n_inst; ++i) nf = h_models[i].n_features > nf ? h_models[i].n_features : nf;
   uint64_t cap = (uint64_t)max_optin - 1024;
   if (need < cap) cap = need;
   const unsigned grid = (unsigned)((n_records + kScoreTile - 1) / kScoreTile);

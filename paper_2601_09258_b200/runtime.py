@@ -55,6 +55,8 @@ def lib():
     L.cs_set_config.argtypes = [vp, C.POINTER(abi.CycleConfig), C.POINTER(abi.ControlConfig)]
     L.cs_set_name_table.argtypes = [vp, u32, vp]
     L.cs_upload.argtypes = [vp, u32, vp, vp, u64, vp]
+    L.cs_upload_unsorted.argtypes = [vp, u32, vp, vp, vp, u64, vp]
+    L.cs_get_order.argtypes = [vp, u32, vp, sz, psz]
     L.cs_get_cycle_range.argtypes = [vp, u32, u64, u64, vp]
     L.cs_get_record_range.argtypes = [vp, u32, u64, u64, vp]
     L.cs_upload_wire.argtypes = [vp, u32, vp, C.POINTER(abi.WireBatch), u64, vp]
@@ -127,7 +129,7 @@ def lib():
 
 EXPORTED_SYMBOLS = [
     "cs_abi_version", "cs_status_type", "cs_ctx_create", "cs_ctx_destroy", "cs_last_error",
-    "cs_set_config", "cs_set_name_table", "cs_upload", "cs_upload_wire", "cs_wire_pack",
+    "cs_set_config", "cs_set_name_table", "cs_upload", "cs_upload_unsorted", "cs_get_order", "cs_upload_wire", "cs_wire_pack",
     "cs_wire_view", "cs_wire_free", "cs_ingest_chrome_json", "cs_ingest_view", "cs_ingest_free", "cs_ingest_report", "cs_ingest_topology", "cs_ingest_merge", "cs_rank_suspects",
     "cs_suspicion_rank", "cs_welch_p_value", "cs_load_model", "cs_run", "cs_sync",
     "cs_get_summary", "cs_get_candidates", "cs_get_cycles", "cs_get_components", "cs_get_beta",
@@ -661,6 +663,22 @@ class Analyzer:
                                   _ptr(wl)))
         self.n_inst = len(off) - 1
 
+    def upload_unsorted(self, events: np.ndarray, inst_offsets, workloads: np.ndarray,
+                        event_ids: np.ndarray | None = None):
+        """cs_upload_unsorted (K0): any event order; each instance is sorted on
+        the device by (start_ts, event_id) like Trace::sort_events."""
+        events = np.ascontiguousarray(events, dtype=abi.EVENT_DTYPE)
+        off = np.ascontiguousarray(np.asarray(inst_offsets, dtype=np.uint64))
+        wl = np.ascontiguousarray(workloads, dtype=abi.WORKLOAD_DTYPE)
+        ids = None if event_ids is None else np.ascontiguousarray(event_ids, dtype=np.uint64)
+        self._ck(self.L.cs_upload_unsorted(self.h, len(off) - 1, off.ctypes.data, _ptr(events),
+                                           _ptr(ids), len(wl), _ptr(wl)))
+        self.n_inst = len(off) - 1
+
+    def order(self, inst: int = 0) -> np.ndarray:
+        """cs_get_order: canonical position -> input position within the instance."""
+        return self._get(self.L.cs_get_order, inst, np.uint64)
+
     def upload_wire(self, w: WireTrace, workloads: np.ndarray | None = None):
         """cs_upload_wire: same batch as upload(), sent in the columnar wire
         format (the workload table travels in it when packed with one)."""
@@ -686,6 +704,11 @@ class Analyzer:
 
     def set_fused(self, enabled: bool):
         self._ck(self.L.cs_set_option(self.h, 1, int(bool(enabled))))
+
+    def set_traversal(self, enabled: bool):
+        """CS_OPT_TRAVERSAL: score by tree traversal (k_score) even when the
+        model has a compiled cell table."""
+        self._ck(self.L.cs_set_option(self.h, 2, int(bool(enabled))))
 
     def run(self, mask: int = abi.RUN_ALL):
         self._ck(self.L.cs_run(self.h, mask))

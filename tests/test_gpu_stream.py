@@ -217,3 +217,121 @@ def test_native_push_equals_python_push(rt):
     assert key(got[True]) == key(got[False])
     whole_alerts = np.concatenate([r.alerts for r in ref])
     assert key(got[True]) == key(whole_alerts)
+
+
+def _ref_stream_setup(rt, refbridge, t, cfg):
+    ref = t.run(cfg, None, 2400)
+    ex = t.export(cfg)
+    an = rt.Analyzer(0)
+    an.configure(ex.names, rt.span_names_mask(ex.events, len(ex.names)),
+                 n_comm_slots=len(ex.comm_hash), run_config=cfg)
+    an.load_model(rt.LatencyModel.from_json(ref.model_json))
+    return ref, ex, an
+
+
+@pytest.mark.parametrize("slice_ms,ranks", [(10.0, 1), (37.0, 4)])
+def test_stream_equals_reference_directly(rt, refbridge, slice_ms, ranks):
+    """Micro-batched monitor (configs[4]) vs the reference's whole-trace
+    monitor_loop on the SAME trace (no transitivity through device runs):
+    cycles, records, residuals, flags and alerts identical."""
+    cfg = {"cycle": {"anchor_hint": "run_batch"}}
+    t = refbridge.RefTrace.synth(3000, 71 + ranks, 72, fault="gpu_contention", onset=2600,
+                                 duration=150, n_ranks=ranks, target_rank=0)
+    ref, ex, an = _ref_stream_setup(rt, refbridge, t, cfg)
+    assert ref.status == 0 and len(ref.alerts) >= 1
+    ev = ex.events
+    st = an.stream()
+    step = int(slice_ms * 1e6)
+    t0, t_end = int(ev["start_ts"][0]), int(ev["start_ts"][-1]) + 1
+    cyc, rec, al, al_native = [], [], [], []
+    for lo in range(t0, t_end, step):
+        a, b = np.searchsorted(ev["start_ts"], [lo, lo + step], side="left")
+        r = st.push([ev[a:b]], ex.workloads)[0]
+        if r.summary.status == 0:
+            cyc.append(r.cycles)
+            rec.append(r.records)
+            al.append(r.alerts)
+    st.close()
+    cyc, rec, al = (_cat(cyc, abi.CYCLE_DTYPE), _cat(rec, abi.RECORD_DTYPE), _cat(al, abi.ALERT_DTYPE))
+    for f in ["index", "start_ts", "end_ts", "anchor_span_end", "stage", "workload_status"]:
+        assert np.array_equal(cyc[f], ref.cycles[f]), f
+    assert len(rec) == len(ref.records)
+    for f in ["cycle_index", "start_ts", "batch", "input_len", "output_len", "stage", "armed",
+              "flagged", "alert"]:
+        assert np.array_equal(rec[f], ref.records[f]), f
+    for f in ["latency_s", "predicted_s", "residual", "statistic"]:
+        assert np.array_equal(rec[f].view(np.uint64), ref.records[f].view(np.uint64)), f
+    for f in ["cycle", "ts", "batch", "input_len", "output_len", "episode_id"]:
+        assert np.array_equal(al[f], ref.alerts[f]), f
+    assert np.array_equal(al["smoothed_error"].view(np.uint64), ref.alerts["smoothed_error"].view(np.uint64))
+    # the native push (cs_stream_push) gives the same alerts
+    an2 = rt.Analyzer(0)
+    an2.configure(ex.names, rt.span_names_mask(ev, len(ex.names)), n_comm_slots=len(ex.comm_hash),
+                  run_config=cfg)
+    an2.load_model(rt.LatencyModel.from_json(ref.model_json))
+    st2 = an2.stream()
+    for k, lo in enumerate(range(t0, t_end, step)):
+        a, b = np.searchsorted(ev["start_ts"], [lo, lo + step], side="left")
+        al_native.append(st2.push_native([ev[a:b]], ex.workloads if k == 0 else None))
+    st2.close()
+    aln = np.concatenate(al_native)
+    for f in ["cycle", "ts", "episode_id"]:
+        assert np.array_equal(aln[f], ref.alerts[f]), f
+    an.close()
+    an2.close()
+
+
+def _overflow_trace(refbridge, bad_cycle):
+    """A simkit trace whose cycle `bad_cycle` spans more than 2^63 ns: its
+    duration wraps negative in int64 exactly as the reference computes it
+    (cycles.hpp:75), so with latency_component "" the record's latency is
+    <= 0 and ppe throws NonPositiveLatency (detector.cpp:14-19); monitor_loop
+    stops there (main.cpp:162)."""
+    t = refbridge.RefTrace.synth(3000, 81, 82, fault="gpu_contention", onset=2600, duration=150)
+    probe = t.run({"cycle": {"anchor_hint": "run_batch"}}, None, 2400)
+    ex = t.export()
+    cut = int(probe.cycles["start_ts"][bad_cycle + 1])
+    ev = ex.events.copy()
+    head = ev["start_ts"] < cut
+    ev["start_ts"][head] -= np.int64(4_700_000_000_000_000_000)
+    ev["start_ts"][~head] += np.int64(4_600_000_000_000_000_000)
+    bt = refbridge.RefTrace.build(ev, ex.names, ex.workloads, ex.comm_hash, ex.comm_rank,
+                                  event_ids=ex.event_ids, sort=False)
+    return t, bt, ev, ex
+
+
+def test_stream_stays_stopped_after_non_positive_latency(rt, refbridge):
+    cfg = {"cycle": {"anchor_hint": "run_batch"}, "pipeline": {"latency_component": ""}}
+    t, bt, ev, ex = _overflow_trace(refbridge, 2450)
+    ref_clean = t.run(cfg, None, 2400)
+    ref = bt.run(cfg, ref_clean.model_json, 2400)
+    assert ref.err_type == "non_positive_latency"
+    # the fault after the bad cycle alerts in the clean trace, never after the stop
+    assert (ref_clean.alerts["cycle"] > 2450).any()
+    assert not (ref.alerts["cycle"] > 2450).any()
+    an = rt.Analyzer(0)
+    an.configure(ex.names, rt.span_names_mask(ev, len(ex.names)), n_comm_slots=len(ex.comm_hash),
+                 run_config=cfg)
+    an.load_model(rt.LatencyModel.from_json(ref_clean.model_json))
+    # whole trace: status non_positive_latency, alerts cut at the bad record
+    an.upload(ev, [0, len(ev)], ex.workloads)
+    an.run(abi.RUN_ALL)
+    whole = an.result(0)
+    assert whole.status_type == "non_positive_latency"
+    assert whole.summary.first_bad_record == ref.first_bad_record
+    assert np.array_equal(whole.alerts["cycle"], ref.alerts["cycle"])
+    # stream in event-count slices (time slices cannot cross a 2^63 ns gap)
+    st = an.stream()
+    got, statuses = [], []
+    for a in range(0, len(ev), 9000):
+        got.append(st.push_native([ev[a:a + 9000]], ex.workloads if a == 0 else None))
+        statuses.append(an.summary(0).status)
+    st.close()
+    got = np.concatenate(got)
+    assert np.array_equal(got["cycle"], ref.alerts["cycle"]), "alerts after the stream stopped"
+    assert np.array_equal(got["episode_id"], ref.alerts["episode_id"])
+    bad = {v: k for k, v in abi.STATUS_TYPES.items()}["non_positive_latency"]
+    assert bad in statuses
+    k = statuses.index(bad)
+    assert all(s == bad for s in statuses[k:]), statuses
+    an.close()
