@@ -251,6 +251,7 @@ def run_ours(args, rank, world, local_rank):
     del events
 
     an = rt.Analyzer(dev)
+    an.set_fused(os.environ.get("CS_BENCH_FUSED", "1") != "0")
     span = rt.span_names_mask(pin_ev, len(names))
     an.configure(names, span, n_comm_slots=n_comm)
     an.upload(pin_ev, offs, pin_wl)
@@ -289,8 +290,8 @@ def run_ours(args, rank, world, local_rank):
         tm = an.timings()
         phase_hist.append(tm)
         step_ms.append(tm["total"])
-        if "fused_segment" in tm:
-            scan_ms.append(tm["fused_segment"])
+        if "segment_range" in tm:
+            scan_ms.append(tm["segment_range"])
             reduce_ms.append(0.0)
         else:
             scan_ms.append(tm["scan_events"])
@@ -363,6 +364,7 @@ def run_ours(args, rank, world, local_rank):
     # collective sequence on every rank).
     import threading
     an2 = rt.Analyzer(dev)
+    an2.set_fused(os.environ.get("CS_BENCH_FUSED", "1") != "0")
     an2.configure(names, span, n_comm_slots=n_comm)
     for i, model in enumerate(models):
         an2.load_model(model, inst=i)
@@ -435,8 +437,8 @@ def run_ours(args, rank, world, local_rank):
     cyc_out = n_cycles * (48 + 4 + 2 + 4 + 8 * P + 16 * Cs + 9 * R)  # per-cycle outputs
     scan_t = sum(scan_ms) / len(scan_ms)
     red_t = sum(reduce_ms) / len(reduce_ms)
-    if red_t == 0.0:  # fused single pass: events read once, cycle outputs written once
-        dom = ("fused_segment", 32 * n_events + cyc_out, scan_t)
+    if red_t == 0.0:  # single-read segmentation: events read once, cycle outputs written once
+        dom = ("segment_range", 32 * n_events + cyc_out + 24 * n_cycles, scan_t)
     else:
         scan_bytes = 32 * n_events + 24 * (n_cycles + n_inst)
         reduce_bytes = 32 * n_events + 32 * n_cycles + cyc_out
@@ -448,7 +450,7 @@ def run_ours(args, rank, world, local_rank):
     # the default workload it was taken on
     traffic = None
     kname = {"cycle_reduce": "k_cycle_reduce_v2", "scan_events": "k_scan_warp",
-             "fused_segment": "k_segment_pass"}[dom[0]]
+             "segment_range": "k_segment_range"}[dom[0]]
     step_dram = None  # ncu DRAM bytes of the step's captured kernels (the full capture)
     try:
         with open(os.path.join(ROOT, "profiles", "r1_ncu_traffic.json")) as f:

@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define CS_ABI_VERSION 1
+#define CS_ABI_VERSION 2
 
 /* ------------------------------------------------------------------ status */
 enum cs_status {
@@ -238,6 +238,8 @@ typedef struct cs_anchor_candidate { /* AnchorCandidate (cycles.hpp:45-52) */
   double mean_duration_ns;
   double duration_cv;
   double score;
+  double periodicity;  /* 1 / (1 + CV of inter-start gaps) (cycles.cpp:76);
+                          cs_get_candidates_exact only (NaN otherwise) */
 } cs_anchor_candidate;
 
 typedef struct cs_instance_summary {
@@ -261,6 +263,14 @@ typedef struct cs_ctx cs_ctx;
 #define CS_RUN_SCORE     0x4u  /* GBDT predict + ppe                     */
 #define CS_RUN_DETECT    0x8u  /* control chart + alerts                 */
 #define CS_RUN_ALL       0xFu
+#define CS_RUN_GIVEN     0x20u /* use the cs_set_cycles table instead of anchor
+                                  discovery + segmentation (one instance):
+                                  local stage signals, workloads, components,
+                                  beta / mu, records, score and detect run on
+                                  the caller's cycles                      */
+#define CS_RUN_CLASSIFY  0x40u /* with CS_RUN_GIVEN: classify_stages from
+                                  scratch (cycles.cpp:190-254); without it the
+                                  given cycles keep their stage            */
 #define CS_RUN_MU        0x10u /* counter-weighted mu per (cycle, class):
                                   cycle_stats with a CounterTable
                                   (rca.cpp:97-106, 123-126); implies BETA  */
@@ -486,9 +496,27 @@ int cs_load_model(cs_ctx* ctx, uint32_t inst, const cs_model* model);
 int cs_run(cs_ctx* ctx, uint32_t stage_mask);
 int cs_sync(cs_ctx* ctx);
 
+/* Caller-given cycles for the next cs_run(CS_RUN_GIVEN | ...): the span
+ * overloads of the reference (build_cycle_records(trace, span<const Cycle>,
+ * ...) cycles.cpp:366-409, classify_stages 190-254, extract_workload 256-281,
+ * cycle_stats rca.cpp:71-130) take cycles the caller built or edited.  Event
+ * positions are canonical indices of the uploaded instance 0; anchor_pos =
+ * UINT64_MAX marks a cycle without components (frequency fallback).
+ * `components` (n x n_phases, may be NULL) are the cycles' own
+ * component_durations, used for the latency target instead of recomputing
+ * them.  Getters report the given `index` values. */
+int cs_set_cycles(cs_ctx* ctx, const cs_cycle* cycles, uint64_t n, const int64_t* components);
+
 int cs_get_summary(cs_ctx* ctx, uint32_t inst, cs_instance_summary* out);
+/* Anchor candidates of the last run (cycles.cpp:47-87), best first.  The
+ * scores come from the exact integer moments (within a few ulps of the
+ * reference's ordered sums); cs_get_candidates_exact recomputes every
+ * candidate with the reference's own sequential arithmetic on the device
+ * (incl. periodicity) and is bit-identical to rank_anchor_candidates. */
 int cs_get_candidates(cs_ctx* ctx, uint32_t inst, cs_anchor_candidate* buf,
                       size_t cap, size_t* n);
+int cs_get_candidates_exact(cs_ctx* ctx, uint32_t inst, cs_anchor_candidate* buf,
+                            size_t cap, size_t* n);
 int cs_get_cycles(cs_ctx* ctx, uint32_t inst, cs_cycle* buf, size_t cap, size_t* n);
 /* component_durations: n_cycles x n_phases int64, row-major */
 int cs_get_components(cs_ctx* ctx, uint32_t inst, int64_t* buf, size_t cap, size_t* n);
@@ -585,6 +613,17 @@ typedef struct cs_strategy_metrics {
 } cs_strategy_metrics;
 int cs_evaluate_strategy(cs_ctx* ctx, uint32_t inst, const uint8_t* cycle_labels,
                          uint64_t n_labels, cs_strategy_metrics* out);
+
+/* Detector::step over a residual stream (detector.cpp:85-130; one Detector,
+ * samples in order) and, with per-sample labels, evaluate_strategy
+ * (detector.cpp:166-224) — the batched detector of evaluate_trial / the
+ * drop-in's evaluate_strategy.  The limit is dynamic_ucl for DynamicWindow and
+ * ctl->fixed_threshold otherwise (the Detector constructor).  Optional
+ * outputs: the statistic and flags (bit0 armed, bit1 flagged, bit2 alert) per
+ * sample, metrics (needs labels; CS_E_NO_LABELS for an empty stream). */
+int cs_detect_residuals(cs_ctx* ctx, const double* residuals, uint64_t n, const cs_control_config* ctl,
+                        double dynamic_ucl, const uint8_t* labels, double* statistic, uint8_t* flags,
+                        cs_strategy_metrics* metrics);
 
 /* Alert sink of monitor_loop (main.cpp:151-177): Alert::to_json records
  * (detector.cpp:72-83) as NDJSON, with the Escalator's retain/mode fields on

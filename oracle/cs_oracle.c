@@ -59,6 +59,8 @@ typedef struct {
   uint64_t count;
   double sum, sum_sq;
   uint64_t spans_any;
+  int64_t prev_start;     /* gap_cv (cycles.cpp:30-43): sequential gap sums */
+  double gap_sum, gap_sq;
 } NameAcc;
 
 static int cand_cmp(const void* a, const void* b) {
@@ -76,6 +78,12 @@ static void rank_candidates(const cs_event* ev, uint64_t n, uint32_t n_names,
     acc[e->name_id].spans_any++;
     if (e->category != CS_CAT_PYTHON_CALL) continue;
     NameAcc* s = &acc[e->name_id];
+    if (s->count > 0) {
+      const double gap = (double)(e->start_ts - s->prev_start);
+      s->gap_sum += gap;
+      s->gap_sq += gap * gap;
+    }
+    s->prev_start = e->start_ts;
     s->count++;
     const double d = (double)e->duration;
     s->sum += d;
@@ -99,6 +107,17 @@ static void rank_candidates(const cs_event* ev, uint64_t n, uint32_t n_names,
     }
     c.duration_cv = cv;
     c.score = (double)s->count / (1.0 + cv);
+    double gcv = 0.0;
+    if (s->count >= 3) {
+      const double ng = (double)(s->count - 1);
+      const double gm = s->gap_sum / ng;
+      if (gm > 0.0) {
+        double var = s->gap_sq / ng - gm * gm;
+        if (!(0.0 < var)) var = 0.0;
+        gcv = sqrt(var) / gm;
+      }
+    }
+    c.periodicity = 1.0 / (1.0 + gcv);
     o->cand[o->n_cand++] = c;
   }
   qsort(o->cand, o->n_cand, sizeof(cs_anchor_candidate), cand_cmp);

@@ -226,6 +226,7 @@ void run_reference(Handle& h, const RunConfig& config, const char* model_json,
         a.mean_duration_ns = c.mean_duration_ns;
         a.duration_cv = c.duration_cv;
         a.score = c.score;
+        a.periodicity = c.periodicity;
         R.candidates.push_back(a);
       }
       const auto anchor = discover_anchor(trace, config.cycle);

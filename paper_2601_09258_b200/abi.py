@@ -52,7 +52,8 @@ ALERT_DTYPE = np.dtype(
      ("output_len", "<i8"), ("episode_id", "<u8"), ("record_index", "<u8")], align=True)
 CANDIDATE_DTYPE = np.dtype(
     [("name_id", "<u4"), ("reserved", "<u4"), ("call_count", "<u8"),
-     ("mean_duration_ns", "<f8"), ("duration_cv", "<f8"), ("score", "<f8")], align=True)
+     ("mean_duration_ns", "<f8"), ("duration_cv", "<f8"), ("score", "<f8"),
+     ("periodicity", "<f8")], align=True)
 TREE_NODE_DTYPE = np.dtype(
     [("feature", "<i4"), ("left", "<i4"), ("right", "<i4"), ("reserved", "<i4"),
      ("threshold", "<f8"), ("value", "<f8")], align=True)
@@ -72,6 +73,10 @@ FEATURE_IDS = {"batch": F_BATCH, "w_kv": F_W_KV, "input_len": F_INPUT_LEN,
 
 RUN_SEGMENT, RUN_BETA, RUN_SCORE, RUN_DETECT, RUN_ALL = 0x1, 0x2, 0x4, 0x8, 0xF
 RUN_MU = 0x10  # counter-weighted mu (cycle_stats with a CounterTable)
+RUN_GIVEN = 0x20  # caller-given cycles (cs_set_cycles) instead of segmentation
+RUN_CLASSIFY = 0x40  # with RUN_GIVEN: classify_stages from scratch
+
+CS_ABI_VERSION = 2  # include/cyclescope_b200.h
 
 STATUS_TYPES = {
     0: "ok", 1: "invalid_argument", 2: "no_device", 3: "cuda_error",

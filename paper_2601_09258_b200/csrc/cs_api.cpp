@@ -135,6 +135,12 @@ struct PackedModel {
 
 }  // namespace
 
+// cs_detect_residuals: a one-instance record table of its own
+struct DetScratch {
+  DevBuf resid, stat, flags, rec_off, rec_cycle, cyc_off, alert_rec, alert_off, block_tmp, inst,
+      model, labels, out;
+};
+
 constexpr uint32_t kMaxBoundInstances = 1u << 24;  // model bindings per ctx
 
 struct cs_ctx {
@@ -184,6 +190,23 @@ struct cs_ctx {
   uint64_t n_cycles = 0;           // cycle slots
   int reduce_variant = 0;  // profiling hook (single variant today)
   bool allow_fused = false;  // CS_OPT_FUSED
+  bool used_fused = false;   // the last run segmented with k_segment_range
+  // cs_set_cycles: caller-given cycles of instance 0 (CS_RUN_GIVEN)
+  std::vector<cs_cycle> given;
+  std::vector<int64_t> given_comp;   // n x n_phases, empty = recompute
+  bool given_run = false;            // the last run used them (indices map through `given`)
+  DetScratch det;                    // cs_detect_residuals
+  uint64_t slot_cap = 0;     // cycle-slot capacity of the fused pass (grows to the last count)
+  // k_segment_range ranges (<= range_events events of one instance), built by
+  // the first fused run after an upload for the range size in force
+  uint64_t ranges_built_for = 0;
+  int64_t opt_range_events = 0;   // 0: ~kSegCycles cycles per range from the last run's density
+  int64_t opt_prefetch = -1;      // bytes of the next-round range prefetched into L2; -1: whole range
+  double ev_per_cycle = 0.0;      // events per cycle slot of the last run
+  std::vector<uint64_t> range_begin, range_end;
+  std::vector<uint32_t> range_inst, inst_first_range;
+  DevBuf d_range_begin, d_range_end, d_range_inst, d_inst_first_range, d_lb_state, d_range_prefix,
+      d_seg_ctl;
   bool no_lut = false;       // CS_OPT_TRAVERSAL: score by tree traversal even with a cell table
   DevBuf d_cyc_off, c_start, c_end, c_apos, c_aend, c_first, c_last, c_inst, c_stage, c_local,
       c_wl, c_comp, c_beta_tot, c_beta, c_coll, c_coll_n;
@@ -212,7 +235,7 @@ struct cs_ctx {
   cs_control_config mt_ctl{};
   std::vector<int> mt_ids;
   // fold results per instance: name -> (mean, cv, score)
-  std::vector<std::map<uint32_t, std::array<double, 3>>> folded;
+  std::vector<std::map<uint32_t, std::array<double, 4>>> folded;
   std::vector<int> inst_status;
   std::vector<int> used_fallback;
   std::vector<uint64_t> fallback_cycles;
@@ -572,6 +595,7 @@ int upload_layout(cs_ctx* ctx, uint32_t n_inst, const uint64_t* inst_offsets, bo
   }
   CS_CUDA(cudaMemcpyAsync(dft, ctx->inst_first_tile.data(), n_inst * 4, cudaMemcpyHostToDevice,
                           ctx->stream));
+  ctx->ranges_built_for = 0;  // k_segment_range ranges are rebuilt by the next fused run
   // bindings are by instance index and survive re-uploads (streaming pushes)
   if (ctx->model_of_inst.size() < n_inst) ctx->model_of_inst.resize(n_inst, -1);
   ctx->ran = false;
@@ -645,6 +669,14 @@ int cs_get_order(cs_ctx* ctx, uint32_t inst, uint64_t* buf, size_t cap, size_t* 
     CS_CUDA(cudaMemcpyAsync(buf, static_cast<const uint64_t*>(ctx->d_order.p) + b, m * 8,
                             cudaMemcpyDeviceToHost, ctx->stream));
   CS_CUDA(cudaStreamSynchronize(ctx->stream));
+  return CS_OK;
+}
+
+int cs_set_cycles(cs_ctx* ctx, const cs_cycle* cycles, uint64_t n, const int64_t* components) {
+  if (!ctx || (n && !cycles)) return CS_E_INVALID_ARGUMENT;
+  ctx->given.assign(cycles, cycles + n);
+  if (components) ctx->given_comp.assign(components, components + n * static_cast<uint64_t>(ctx->cyc.n_phases));
+  else ctx->given_comp.clear();
   return CS_OK;
 }
 
@@ -900,6 +932,45 @@ struct NvtxRun {
   }
 };
 
+// Ranges of the single-read segmentation: consecutive events of one instance,
+// about one cycle per thread of the CTA each (the thread-per-cycle reduce then
+// keeps every thread busy), multiples of 256 events, built once per upload and
+// range size.
+int build_ranges(cs_ctx* ctx, uint64_t range_events) {
+  if (ctx->ranges_built_for == range_events) return CS_OK;
+  const uint32_t n_inst = ctx->n_inst;
+  ctx->range_begin.clear();
+  ctx->range_end.clear();
+  ctx->range_inst.clear();
+  ctx->inst_first_range.assign(n_inst + 1, 0);
+  for (uint32_t i = 0; i < n_inst; ++i) {
+    ctx->inst_first_range[i] = static_cast<uint32_t>(ctx->range_inst.size());
+    for (uint64_t t = ctx->inst_off[i]; t < ctx->inst_off[i + 1]; t += range_events) {
+      ctx->range_begin.push_back(t);
+      ctx->range_end.push_back(std::min<uint64_t>(t + range_events, ctx->inst_off[i + 1]));
+      ctx->range_inst.push_back(i);
+    }
+  }
+  ctx->inst_first_range[n_inst] = static_cast<uint32_t>(ctx->range_inst.size());
+  const size_t nr = ctx->range_inst.size();
+  if (nr > 0x7fffffffull) return fail(ctx, CS_E_UNSUPPORTED, "too many segmentation ranges");
+  auto* rb = dev<uint64_t>(ctx->d_range_begin, nr);
+  auto* re = dev<uint64_t>(ctx->d_range_end, nr);
+  auto* ri = dev<uint32_t>(ctx->d_range_inst, nr);
+  auto* rf = dev<uint32_t>(ctx->d_inst_first_range, n_inst + 1);
+  if (!rb || !re || !ri || !rf) return fail(ctx, CS_E_CUDA, "cudaMalloc(ranges)");
+  if (nr) {
+    CS_CUDA(cudaMemcpyAsync(rb, ctx->range_begin.data(), nr * 8, cudaMemcpyHostToDevice, ctx->stream));
+    CS_CUDA(cudaMemcpyAsync(re, ctx->range_end.data(), nr * 8, cudaMemcpyHostToDevice, ctx->stream));
+    CS_CUDA(cudaMemcpyAsync(ri, ctx->range_inst.data(), nr * 4, cudaMemcpyHostToDevice, ctx->stream));
+  }
+  CS_CUDA(cudaMemcpyAsync(rf, ctx->inst_first_range.data(), (n_inst + 1) * 4, cudaMemcpyHostToDevice,
+                          ctx->stream));
+  CS_CUDA(cudaStreamSynchronize(ctx->stream));  // host vectors may change before the copies ran
+  ctx->ranges_built_for = range_events;
+  return CS_OK;
+}
+
 // NoAnchorFound -> segment_by_frequency (cycles.cpp:283-343) for one instance.
 // Returns the number of cycles (0 = still NoAnchorFound); fills t0/period.
 int frequency_plan(cs_ctx* ctx, uint32_t i, int64_t* t0, int64_t* period, uint64_t* n) {
@@ -956,7 +1027,8 @@ static int cs_run_impl(cs_ctx* ctx, uint32_t mask) {
   if (mask & CS_RUN_MU) mask |= CS_RUN_BETA;  // mu divides by the class totals
   if ((mask & CS_RUN_MU) && ctx->streaming)
     return fail(ctx, CS_E_UNSUPPORTED, "mu needs whole-trace counter series (not per micro-batch)");
-  if (!(mask & CS_RUN_SEGMENT)) return fail(ctx, CS_E_INVALID_ARGUMENT, "CS_RUN_SEGMENT required");
+  if (!(mask & (CS_RUN_SEGMENT | CS_RUN_GIVEN)))
+    return fail(ctx, CS_E_INVALID_ARGUMENT, "CS_RUN_SEGMENT (or CS_RUN_GIVEN) required");
   if (ctx->n_inst == 0) return fail(ctx, CS_E_INVALID_ARGUMENT, "nothing uploaded");
   CS_CUDA(cudaSetDevice(ctx->device));
   cudaStream_t s = ctx->stream;
@@ -1020,7 +1092,7 @@ static int cs_run_impl(cs_ctx* ctx, uint32_t mask) {
   DevBuffers b = make_buffers(ctx);
 
   const int e0 = record_event(ctx, 0);
-  if (hint == -1 && !all_fixed) {
+  if (hint == -1 && !all_fixed && !(mask & CS_RUN_GIVEN)) {
     // speculative anchor from a sample of every instance
     if (stats_bytes) CS_CUDA(cudaMemsetAsync(d_stats, 0, stats_bytes, s));
     launch_scan_events(b, cfg, 1, true, static_cast<const uint32_t*>(ctx->d_sample_tiles.p),
@@ -1048,12 +1120,177 @@ static int cs_run_impl(cs_ctx* ctx, uint32_t mask) {
   };
   ctx->n_cyc.assign(n_inst, 0);
   int e1 = -1, e2 = -1, e4 = -1, e5 = -1;
-  {
+  ctx->used_fused = false;
+  ctx->given_run = false;
+  // ---------------- caller-given cycles (CS_RUN_GIVEN): no anchor discovery or
+  // segmentation; the cycle table is the caller's (cycles.hpp:62-77)
+  if (mask & CS_RUN_GIVEN) {
+    if (n_inst != 1) return fail(ctx, CS_E_INVALID_ARGUMENT, "CS_RUN_GIVEN needs exactly one instance");
+    if (ctx->streaming) return fail(ctx, CS_E_INVALID_ARGUMENT, "CS_RUN_GIVEN mid-stream");
+    const uint64_t nc = ctx->given.size();
+    for (const cs_cycle& c : ctx->given)
+      if (c.first_event > c.last_event || c.last_event > ctx->n_ev ||
+          (c.anchor_pos != UINT64_MAX && c.anchor_pos >= ctx->n_ev))
+        return fail(ctx, CS_E_INVALID_ARGUMENT, "given cycle event range out of bounds");
+    if (!alloc_cycles(nc)) return fail(ctx, CS_E_CUDA, "cudaMalloc(cycles)");
+    ctx->cyc_off.assign({0, nc});
+    ctx->n_cyc[0] = nc;
+    ctx->n_cycles = nc;
+    ctx->inst_status.assign(1, CS_OK);
+    ctx->used_fallback.assign(1, 0);
+    ctx->fallback_cycles.assign(1, 0);
+    ctx->folded.assign(1, {});
+    std::vector<int64_t> st(nc), en(nc), ae(nc);
+    std::vector<uint64_t> ap(nc), fi(nc), la(nc);
+    std::vector<uint8_t> sg(nc);
+    for (uint64_t k = 0; k < nc; ++k) {
+      const cs_cycle& c = ctx->given[k];
+      st[k] = c.start_ts;
+      en[k] = c.end_ts;
+      ae[k] = c.anchor_span_end;
+      ap[k] = c.anchor_pos == UINT64_MAX ? UINT64_MAX : c.anchor_pos;
+      fi[k] = c.first_event;
+      la[k] = c.last_event;
+      sg[k] = static_cast<uint8_t>(c.stage);
+    }
+    if (nc) {
+      CS_CUDA(cudaMemcpyAsync(ctx->c_start.p, st.data(), nc * 8, cudaMemcpyHostToDevice, s));
+      CS_CUDA(cudaMemcpyAsync(ctx->c_end.p, en.data(), nc * 8, cudaMemcpyHostToDevice, s));
+      CS_CUDA(cudaMemcpyAsync(ctx->c_aend.p, ae.data(), nc * 8, cudaMemcpyHostToDevice, s));
+      CS_CUDA(cudaMemcpyAsync(ctx->c_apos.p, ap.data(), nc * 8, cudaMemcpyHostToDevice, s));
+      CS_CUDA(cudaMemcpyAsync(ctx->c_first.p, fi.data(), nc * 8, cudaMemcpyHostToDevice, s));
+      CS_CUDA(cudaMemcpyAsync(ctx->c_last.p, la.data(), nc * 8, cudaMemcpyHostToDevice, s));
+      CS_CUDA(cudaMemsetAsync(ctx->c_inst.p, 0, nc * 4, s));
+    }
+    CS_CUDA(cudaMemcpyAsync(ctx->d_cyc_off.p, ctx->cyc_off.data(), 16, cudaMemcpyHostToDevice, s));
+    b = make_buffers(ctx);
+    e1 = e2 = e4 = record_event(ctx, 4);
+    launch_cycle_reduce_tpc(b, cfg, (mask & CS_RUN_BETA) ? 1 : 0, s, &ctx->launches, ctx->reduce_variant);
+    if (!ctx->given_comp.empty() && P)
+      CS_CUDA(cudaMemcpyAsync(ctx->c_comp.p, ctx->given_comp.data(), nc * P * 8, cudaMemcpyHostToDevice, s));
+    if (!(mask & CS_RUN_CLASSIFY) && nc)  // build_cycle_records(span): the caller's stages
+      CS_CUDA(cudaMemcpyAsync(ctx->c_stage.p, sg.data(), nc, cudaMemcpyHostToDevice, s));
+    e5 = record_event(ctx, 5);
+    ctx->timed.push_back({"cycle_reduce", {e4, e5}});
+    ctx->given_run = true;
+    CS_CUDA(cudaStreamSynchronize(s));  // the host staging vectors above go out of scope
+  }
+  // ---------------- single-read segmentation (k_segment_range)
+  if (!ctx->given_run && ctx->allow_fused && !ctx->streaming && ctx->n_ev &&
+      segment_range_smem(cfg, (mask & CS_RUN_BETA) ? 1 : 0) >= 0) {
+    uint64_t range_events = static_cast<uint64_t>(ctx->opt_range_events);
+    if (!range_events) {
+      const double epc = ctx->ev_per_cycle > 0.0 ? ctx->ev_per_cycle : 16.0;
+      range_events = static_cast<uint64_t>(epc * kSegCycles);
+    }
+    range_events = std::min<uint64_t>(std::max<uint64_t>((range_events + 255) / 256 * 256, 1024), 65536);
+    const int rc = build_ranges(ctx, range_events);
+    if (rc != CS_OK) return rc;
+  }
+  const uint32_t n_ranges = static_cast<uint32_t>(ctx->range_inst.size());
+  if (!ctx->given_run && ctx->allow_fused && !ctx->streaming && n_ranges && ctx->ranges_built_for &&
+      segment_range_smem(cfg, (mask & CS_RUN_BETA) ? 1 : 0) >= 0) {
+    const std::vector<InstState> h_init(ctx->h_inst.begin(), ctx->h_inst.end());
+    uint64_t cap = std::max<uint64_t>(ctx->slot_cap, ctx->n_ev / 8 + 1024);
+    for (int attempt = 0; attempt < 2 && !ctx->used_fused; ++attempt) {
+      if (!alloc_cycles(cap) || !dev<unsigned long long>(ctx->d_lb_state, n_ranges) ||
+          !dev<uint64_t>(ctx->d_range_prefix, n_ranges) || !dev<unsigned int>(ctx->d_seg_ctl, 2))
+        return fail(ctx, CS_E_CUDA, "cudaMalloc(segment)");
+      ctx->slot_cap = cap;
+      if (attempt) {  // overflow: back to the state after the anchor guess
+        for (uint32_t i = 0; i < n_inst; ++i) {
+          ctx->h_inst[i].n_anchors = ctx->h_inst[i].n_unknown = 0;
+          ctx->h_inst[i].unsorted = 0;
+        }
+        CS_CUDA(cudaMemcpyAsync(d_inst, ctx->h_inst.data(), n_inst * sizeof(InstState),
+                                cudaMemcpyHostToDevice, s));
+      }
+      if (stats_bytes) CS_CUDA(cudaMemsetAsync(d_stats, 0, stats_bytes, s));
+      CS_CUDA(cudaMemsetAsync(ctx->d_lb_state.p, 0, n_ranges * 8ull, s));
+      CS_CUDA(cudaMemsetAsync(ctx->d_seg_ctl.p, 0, 8, s));
+      b = make_buffers(ctx);
+      SegMeta sm{static_cast<const uint64_t*>(ctx->d_range_begin.p),
+                 static_cast<const uint64_t*>(ctx->d_range_end.p),
+                 static_cast<const uint32_t*>(ctx->d_range_inst.p), n_ranges,
+                 static_cast<unsigned long long*>(ctx->d_lb_state.p),
+                 static_cast<uint64_t*>(ctx->d_range_prefix.p),
+                 static_cast<unsigned int*>(ctx->d_seg_ctl.p),
+                 static_cast<unsigned int*>(ctx->d_seg_ctl.p) + 1, cap,
+                 static_cast<uint32_t>(ctx->opt_prefetch < 0 ? ctx->ranges_built_for * sizeof(cs_event)
+                                                             : static_cast<uint64_t>(ctx->opt_prefetch))};
+      e1 = record_event(ctx, 1);
+      launch_segment_range(b, cfg, sm, (mask & CS_RUN_BETA) ? 1 : 0, s, &ctx->launches);
+      e2 = record_event(ctx, 2);
+      launch_range_inst(b, sm, static_cast<const uint32_t*>(ctx->d_inst_first_range.p),
+                        static_cast<uint64_t*>(ctx->d_cyc_off.p), s, &ctx->launches);
+      launch_rank(b, cfg, 1, s, &ctx->launches);
+      const int e9 = record_event(ctx, 9);
+      e5 = e9;
+      ctx->timed.push_back({"segment_range", {e1, e2}});
+      ctx->timed.push_back({"sample_and_setup", {e0, e1}});
+      ctx->timed.push_back({"prefix_rank", {e2, e9}});
+      unsigned int ctl[2] = {0, 0};
+      CS_CUDA(cudaMemcpyAsync(ctx->h_inst.data(), d_inst, n_inst * sizeof(InstState),
+                              cudaMemcpyDeviceToHost, s));
+      CS_CUDA(cudaMemcpyAsync(ctl, ctx->d_seg_ctl.p, 8, cudaMemcpyDeviceToHost, s));
+      hp.mark("segment_issued");
+      CS_CUDA(cudaStreamSynchronize(s));
+      hp.mark("segment_sync");
+      CS_CUDA(cudaGetLastError());
+      for (uint32_t i = 0; i < n_inst; ++i)
+        if (ctx->h_inst[i].unsorted)
+          return fail(ctx, CS_E_INVALID_ARGUMENT,
+                      "events of instance " + std::to_string(i) +
+                          " are not in canonical (start_ts, event_id) order (trace.cpp:103-109); "
+                          "cs_upload_unsorted sorts them on the device");
+      uint64_t slots = 0;
+      for (uint32_t i = 0; i < n_inst; ++i) slots += ctx->h_inst[i].n_anchors;
+      if (ctl[1]) {  // more anchors than slots: exact capacity, once more
+        cap = slots + 1024;
+        continue;
+      }
+      bool ok = true;
+      for (uint32_t i = 0; i < n_inst; ++i) {
+        const auto& st = ctx->h_inst[i];
+        ok &= !st.ambiguous && !st.redo && !st.no_anchor;
+      }
+      if (!ok) break;  // wrong guess / uncertified ranking / no anchor: two-pass path
+      ctx->cyc_off.assign(n_inst + 1, 0);
+      for (uint32_t i = 0; i < n_inst; ++i) {
+        const uint64_t na = ctx->h_inst[i].n_anchors;
+        ctx->cyc_off[i + 1] = ctx->cyc_off[i] + na;  // slots: cycles + the hole
+        ctx->n_cyc[i] = na >= 2 ? na - 1 : 0;
+      }
+      ctx->n_cycles = slots;
+      if (slots) ctx->ev_per_cycle = static_cast<double>(ctx->n_ev) / static_cast<double>(slots);
+      ctx->inst_status.assign(n_inst, CS_OK);
+      ctx->used_fallback.assign(n_inst, 0);
+      ctx->fallback_cycles.assign(n_inst, 0);
+      ctx->folded.assign(n_inst, {});
+      ctx->used_fused = true;
+    }
+    if (!ctx->used_fused) {
+      // rare: redo on the two-pass path from a fresh anchor guess
+      ctx->timed.clear();
+      ctx->h_inst.assign(h_init.begin(), h_init.end());
+      CS_CUDA(cudaMemcpyAsync(d_inst, ctx->h_inst.data(), n_inst * sizeof(InstState),
+                              cudaMemcpyHostToDevice, s));
+      b = make_buffers(ctx);
+      if (hint == -1) {
+        if (stats_bytes) CS_CUDA(cudaMemsetAsync(d_stats, 0, stats_bytes, s));
+        launch_scan_events(b, cfg, 1, true, static_cast<const uint32_t*>(ctx->d_sample_tiles.p),
+                           static_cast<uint32_t>(ctx->sample_tiles.size()), s, &ctx->launches);
+        launch_rank(b, cfg, 0, s, &ctx->launches);
+      }
+    }
+  }
+  if (!ctx->used_fused && !ctx->given_run) {
   if (stats_bytes) CS_CUDA(cudaMemsetAsync(d_stats, 0, stats_bytes, s));
   CS_CUDA(cudaMemsetAsync(ctx->d_tile_cnt.p, 0, std::max<size_t>(1, nt) * 8, s));
   e1 = record_event(ctx, 1);
   launch_scan_events(b, cfg, 3, false, nullptr, static_cast<uint32_t>(nt), s, &ctx->launches);
   e2 = record_event(ctx, 2);
+  launch_tile_order(b, s, &ctx->launches);
   launch_tile_prefix(b, s, &ctx->launches);
   ctx->timed.push_back({"scan_events", {e1, e2}});
   launch_rank(b, cfg, 1, s, &ctx->launches);
@@ -1095,20 +1332,20 @@ static int cs_run_impl(cs_ctx* ctx, uint32_t mask) {
     DevBuf dpi, dpn, dout;
     auto* a = static_cast<uint32_t*>(dpi.get(pi.size() * 4));
     auto* c = static_cast<uint32_t*>(dpn.get(pn.size() * 4));
-    auto* o = static_cast<double*>(dout.get(pi.size() * 24));
+    auto* o = static_cast<double*>(dout.get(pi.size() * 32));
     if (!a || !c || !o) return fail(ctx, CS_E_CUDA, "cudaMalloc(fold)");
     CS_CUDA(cudaMemcpy(a, pi.data(), pi.size() * 4, cudaMemcpyHostToDevice));
     CS_CUDA(cudaMemcpy(c, pn.data(), pn.size() * 4, cudaMemcpyHostToDevice));
     launch_fold(b, cfg, a, c, static_cast<uint32_t>(pi.size()), o, s, &ctx->launches);
-    std::vector<double> res(pi.size() * 3);
+    std::vector<double> res(pi.size() * 4);
     CS_CUDA(cudaMemcpyAsync(res.data(), o, res.size() * 8, cudaMemcpyDeviceToHost, s));
     CS_CUDA(cudaStreamSynchronize(s));
     std::vector<double> best_score(n_inst, -1.0);
     std::vector<uint32_t> best_name(n_inst, UINT32_MAX);
     for (size_t k = 0; k < pi.size(); ++k) {
       const uint32_t i = pi[k];
-      ctx->folded[i][pn[k]] = {res[3 * k], res[3 * k + 1], res[3 * k + 2]};
-      const double sc = res[3 * k + 2];
+      ctx->folded[i][pn[k]] = {res[4 * k], res[4 * k + 1], res[4 * k + 2], res[4 * k + 3]};
+      const double sc = res[4 * k + 2];
       // std::sort by score desc then name asc (cycles.cpp:81-85)
       if (sc > best_score[i] || (sc == best_score[i] && pn[k] < best_name[i])) {
         best_score[i] = sc;
@@ -1170,6 +1407,7 @@ static int cs_run_impl(cs_ctx* ctx, uint32_t mask) {
   }
   const uint64_t n_cyc = ctx->cyc_off[n_inst];
   ctx->n_cycles = n_cyc;
+  if (n_cyc) ctx->ev_per_cycle = static_cast<double>(ctx->n_ev) / static_cast<double>(n_cyc);
   if (!alloc_cycles(n_cyc)) return fail(ctx, CS_E_CUDA, "cudaMalloc(cycles)");
   CS_CUDA(cudaMemcpyAsync(ctx->d_cyc_off.p, ctx->cyc_off.data(), (n_inst + 1) * 8,
                           cudaMemcpyHostToDevice, s));
@@ -1190,7 +1428,7 @@ static int cs_run_impl(cs_ctx* ctx, uint32_t mask) {
   ctx->timed.push_back({"cycle_reduce", {e4, e5}});
   }
   b = make_buffers(ctx);
-  launch_stage_heuristic(b, cfg, s, &ctx->launches);
+  if (!ctx->given_run || (mask & CS_RUN_CLASSIFY)) launch_stage_heuristic(b, cfg, s, &ctx->launches);
   launch_records(b, cfg, 0, s, &ctx->launches);
   const int e6m = record_event(ctx, 6);
   ctx->timed.push_back({"stage_records", {e5, e6m}});
@@ -1563,6 +1801,7 @@ int cs_get_candidates(cs_ctx* ctx, uint32_t inst, cs_anchor_candidate* buf, size
       c.mean_duration_ns = it->second[0];
       c.duration_cv = it->second[1];
       c.score = it->second[2];
+      c.periodicity = it->second[3];
     } else {
       // exact moments; within a few ulps of the reference's ordered sums
       const double nd = static_cast<double>(s.count);
@@ -1576,8 +1815,65 @@ int cs_get_candidates(cs_ctx* ctx, uint32_t inst, cs_anchor_candidate* buf, size
       }
       c.duration_cv = cv;
       c.score = nd / (1.0 + cv);
+      c.periodicity = std::numeric_limits<double>::quiet_NaN();  // cs_get_candidates_exact
     }
     out.push_back(c);
+  }
+  std::sort(out.begin(), out.end(), [](const cs_anchor_candidate& a, const cs_anchor_candidate& b) {
+    if (a.score != b.score) return a.score > b.score;
+    return a.name_id < b.name_id;
+  });
+  if (n) *n = out.size();
+  if (!buf) return CS_OK;
+  if (cap < out.size()) return fail(ctx, CS_E_INVALID_ARGUMENT, "buffer too small");
+  std::copy(out.begin(), out.end(), buf);
+  return CS_OK;
+}
+
+// rank_anchor_candidates (cycles.cpp:47-87) bit for bit: the ordered fold of
+// every candidate name of the instance on the device (k_fold, warp per name:
+// the reference's sequential sums of d, d*d and the start gaps), then the
+// reference's sort (score desc, name asc).
+int cs_get_candidates_exact(cs_ctx* ctx, uint32_t inst, cs_anchor_candidate* buf, size_t cap,
+                            size_t* n) {
+  if (!ctx || !ctx->ran || inst >= ctx->n_inst) return CS_E_INVALID_ARGUMENT;
+  CS_CUDA(cudaSetDevice(ctx->device));
+  const uint32_t nn = static_cast<uint32_t>(ctx->names.size());
+  std::vector<NameStat> hs(nn);
+  if (nn)
+    CS_CUDA(cudaMemcpy(hs.data(), static_cast<NameStat*>(ctx->d_stats.p) + static_cast<size_t>(inst) * nn,
+                       nn * sizeof(NameStat), cudaMemcpyDeviceToHost));
+  std::vector<uint32_t> pi, pn;
+  for (uint32_t k = 0; k < nn; ++k)
+    if (hs[k].count >= ctx->cyc.min_anchor_calls && hs[k].count > 0) {
+      pi.push_back(inst);
+      pn.push_back(k);
+    }
+  std::vector<cs_anchor_candidate> out(pi.size());
+  if (!pi.empty()) {
+    DevBuf dpi, dpn, dout;
+    auto* a = static_cast<uint32_t*>(dpi.get(pi.size() * 4));
+    auto* c = static_cast<uint32_t*>(dpn.get(pn.size() * 4));
+    auto* o = static_cast<double*>(dout.get(pi.size() * 32));
+    if (!a || !c || !o) return fail(ctx, CS_E_CUDA, "cudaMalloc(fold)");
+    CS_CUDA(cudaMemcpy(a, pi.data(), pi.size() * 4, cudaMemcpyHostToDevice));
+    CS_CUDA(cudaMemcpy(c, pn.data(), pn.size() * 4, cudaMemcpyHostToDevice));
+    DevConfig cfg{ctx->cyc, ctx->ctl, 0.0};
+    launch_fold(make_buffers(ctx), cfg, a, c, static_cast<uint32_t>(pi.size()), o, ctx->stream,
+                &ctx->launches);
+    std::vector<double> res(pi.size() * 4);
+    CS_CUDA(cudaMemcpyAsync(res.data(), o, res.size() * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    CS_CUDA(cudaStreamSynchronize(ctx->stream));
+    for (size_t k = 0; k < pi.size(); ++k) {
+      cs_anchor_candidate& x = out[k];
+      x = cs_anchor_candidate{};
+      x.name_id = pn[k];
+      x.call_count = hs[pn[k]].count;
+      x.mean_duration_ns = res[4 * k];
+      x.duration_cv = res[4 * k + 1];
+      x.score = res[4 * k + 2];
+      x.periodicity = res[4 * k + 3];
+    }
   }
   std::sort(out.begin(), out.end(), [](const cs_anchor_candidate& a, const cs_anchor_candidate& b) {
     if (a.score != b.score) return a.score > b.score;
@@ -1656,7 +1952,7 @@ static int cycles_to_host(cs_ctx* ctx, uint32_t inst, uint64_t first, uint64_t n
   const uint64_t idx0 = first + (ctx->streaming ? ctx->h_stream[inst].cycle_off : 0);
   for (uint64_t k = 0; k < nc; ++k) {
     cs_cycle& c = buf[k];
-    c.index = idx0 + k;
+    c.index = ctx->given_run ? ctx->given[first + k].index : idx0 + k;
     c.start_ts = st[k];
     c.end_ts = en[k];
     c.anchor_pos = ap[k] == UINT64_MAX ? UINT64_MAX : ap[k] - ib;
@@ -1863,6 +2159,8 @@ int cs_get_records(cs_ctx* ctx, uint32_t inst, cs_record* buf, size_t cap, size_
   if (cap < nr) return fail(ctx, CS_E_INVALID_ARGUMENT, "buffer too small");
   int rc = gather_records(ctx, inst, r0, nr, buf);
   if (rc) return rc;
+  if (ctx->given_run)
+    for (uint64_t k = 0; k < nr; ++k) buf[k].cycle_index = ctx->given[buf[k].cycle_index].index;
   if (ctx->last_mask & CS_RUN_DETECT) {
     // episode ids: running alert count within the instance
     uint64_t ep = ctx->streaming ? ctx->h_stream[inst].episodes : 0;
@@ -1919,6 +2217,8 @@ int cs_get_alerts(cs_ctx* ctx, uint32_t inst, cs_alert* buf, size_t cap, size_t*
                             ctx->stream));
     CS_CUDA(cudaStreamSynchronize(ctx->stream));
   }
+  if (ctx->given_run)
+    for (auto& a : all) a.cycle = ctx->given[a.cycle].index;
   // monitor_loop stops at the first NonPositiveLatency (main.cpp:162)
   uint64_t na = 0;
   while (na < na_all && all[na].record_index < bad) ++na;
@@ -1966,6 +2266,95 @@ int cs_redetect(cs_ctx* ctx, const cs_control_config* control) {
   return CS_OK;
 }
 
+// StrategyMetrics from the device counts (tp, fp, fn, tn, alerts, lag sum,
+// intervals): detector.cpp:193-222, same double arithmetic
+static void fill_metrics(const unsigned long long* h, int32_t strategy, cs_strategy_metrics* out) {
+  cs_strategy_metrics m{};
+  m.strategy = strategy;
+  m.tp = h[0];
+  m.fp = h[1];
+  m.fn = h[2];
+  m.tn = h[3];
+  m.alerts = h[4];
+  const double tp = static_cast<double>(h[0]), fp = static_cast<double>(h[1]);
+  const double fn = static_cast<double>(h[2]), tn = static_cast<double>(h[3]);
+  m.precision = tp + fp > 0.0 ? tp / (tp + fp) : 0.0;
+  m.recall = tp + fn > 0.0 ? tp / (tp + fn) : 0.0;
+  m.f1 = m.precision + m.recall > 0.0 ? 2.0 * m.precision * m.recall / (m.precision + m.recall)
+                                      : 0.0;
+  m.fpr = fp + tn > 0.0 ? fp / (fp + tn) : 0.0;
+  m.mean_lag = h[6] > 0 ? static_cast<double>(h[5]) / static_cast<double>(h[6]) : 0.0;
+  *out = m;
+}
+
+// Detector::step over a caller's residual stream (detector.cpp:85-130) and
+// evaluate_strategy (166-224) on the device, with the run's kernels
+// (k_detect_flags / k_detect_scatter / k_eval_strategy) on a one-instance
+// table whose record t is stream sample t.
+int cs_detect_residuals(cs_ctx* ctx, const double* residuals, uint64_t n, const cs_control_config* ctl,
+                        double dynamic_ucl, const uint8_t* labels, double* statistic, uint8_t* flags,
+                        cs_strategy_metrics* metrics) {
+  if (!ctx || !ctl || (n && !residuals)) return CS_E_INVALID_ARGUMENT;
+  if (ctl->strategy < 0 || ctl->strategy > 2 || ctl->window == 0)
+    return fail(ctx, CS_E_CONFIG, "invalid control config");
+  if (metrics && (!labels || n == 0))
+    return fail(ctx, CS_E_NO_LABELS, "labeled stream is empty or label count mismatches");
+  CS_CUDA(cudaSetDevice(ctx->device));
+  cudaStream_t s = ctx->stream;
+  const uint64_t n1 = std::max<uint64_t>(1, n);
+  DetScratch& d = ctx->det;
+  if (!dev<double>(d.resid, n1) || !dev<double>(d.stat, n1) || !dev<uint8_t>(d.flags, n1) ||
+      !dev<uint64_t>(d.rec_off, 2) || !dev<uint64_t>(d.rec_cycle, n1) || !dev<uint64_t>(d.cyc_off, 2) ||
+      !dev<uint64_t>(d.alert_rec, n1) || !dev<uint64_t>(d.alert_off, 2) ||
+      !dev<uint64_t>(d.block_tmp, n1 / 1024 + 16) || !dev<InstState>(d.inst, 1) ||
+      !dev<DevModel>(d.model, 1) || !dev<uint8_t>(d.labels, n1) || !dev<unsigned long long>(d.out, 8))
+    return fail(ctx, CS_E_CUDA, "cudaMalloc(detect)");
+  const uint64_t off[2] = {0, n};
+  std::vector<uint64_t> iota(n);
+  for (uint64_t k = 0; k < n; ++k) iota[k] = k;
+  InstState st{};
+  st.first_bad_record = UINT64_MAX;
+  DevModel m{};
+  m.ucl = ctl->strategy == CS_DYNAMIC_WINDOW ? dynamic_ucl : ctl->fixed_threshold;
+  if (n) {
+    CS_CUDA(cudaMemcpyAsync(d.resid.p, residuals, n * 8, cudaMemcpyHostToDevice, s));
+    CS_CUDA(cudaMemcpyAsync(d.rec_cycle.p, iota.data(), n * 8, cudaMemcpyHostToDevice, s));
+  }
+  CS_CUDA(cudaMemcpyAsync(d.rec_off.p, off, 16, cudaMemcpyHostToDevice, s));
+  CS_CUDA(cudaMemsetAsync(d.cyc_off.p, 0, 16, s));
+  CS_CUDA(cudaMemcpyAsync(d.inst.p, &st, sizeof st, cudaMemcpyHostToDevice, s));
+  CS_CUDA(cudaMemcpyAsync(d.model.p, &m, sizeof m, cudaMemcpyHostToDevice, s));
+  DevBuffers b{};
+  b.n_inst = 1;
+  b.rec_off = static_cast<uint64_t*>(d.rec_off.p);
+  b.rec_cycle = static_cast<uint64_t*>(d.rec_cycle.p);
+  b.rec_resid = static_cast<double*>(d.resid.p);
+  b.rec_stat = static_cast<double*>(d.stat.p);
+  b.rec_flags = static_cast<uint8_t*>(d.flags.p);
+  b.alert_rec = static_cast<uint64_t*>(d.alert_rec.p);
+  b.alert_off = static_cast<uint64_t*>(d.alert_off.p);
+  b.block_tmp = static_cast<uint64_t*>(d.block_tmp.p);
+  b.inst = static_cast<InstState*>(d.inst.p);
+  b.models = static_cast<const DevModel*>(d.model.p);
+  b.cyc_off = static_cast<const uint64_t*>(d.cyc_off.p);
+  DevConfig cfg{ctx->cyc, *ctl, 0.0};
+  launch_detect(b, cfg, n, s, &ctx->launches);
+  if (statistic && n) CS_CUDA(cudaMemcpyAsync(statistic, d.stat.p, n * 8, cudaMemcpyDeviceToHost, s));
+  if (flags && n) CS_CUDA(cudaMemcpyAsync(flags, d.flags.p, n, cudaMemcpyDeviceToHost, s));
+  unsigned long long h[8] = {0};
+  if (metrics) {
+    CS_CUDA(cudaMemcpyAsync(d.labels.p, labels, n, cudaMemcpyHostToDevice, s));
+    CS_CUDA(cudaMemsetAsync(d.out.p, 0, sizeof h, s));
+    launch_eval_strategy(b, 0, static_cast<const uint8_t*>(d.labels.p), n, ctl->warmup,
+                         static_cast<unsigned long long*>(d.out.p), s);
+    CS_CUDA(cudaMemcpyAsync(h, d.out.p, sizeof h, cudaMemcpyDeviceToHost, s));
+  }
+  CS_CUDA(cudaStreamSynchronize(s));
+  CS_CUDA(cudaGetLastError());
+  if (metrics) fill_metrics(h, ctl->strategy, metrics);
+  return CS_OK;
+}
+
 int cs_evaluate_strategy(cs_ctx* ctx, uint32_t inst, const uint8_t* labels, uint64_t n_labels,
                          cs_strategy_metrics* out) {
   if (!ctx || !out || !ctx->ran || inst >= ctx->n_inst || (n_labels && !labels))
@@ -1986,23 +2375,7 @@ int cs_evaluate_strategy(cs_ctx* ctx, uint32_t inst, const uint8_t* labels, uint
   unsigned long long h[7];
   CS_CUDA(cudaMemcpyAsync(h, d_out, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
   CS_CUDA(cudaStreamSynchronize(ctx->stream));
-  // detector.cpp:193-222, same double arithmetic
-  cs_strategy_metrics m{};
-  m.strategy = ctx->ctl.strategy;
-  m.tp = h[0];
-  m.fp = h[1];
-  m.fn = h[2];
-  m.tn = h[3];
-  m.alerts = h[4];
-  const double tp = static_cast<double>(h[0]), fp = static_cast<double>(h[1]);
-  const double fn = static_cast<double>(h[2]), tn = static_cast<double>(h[3]);
-  m.precision = tp + fp > 0.0 ? tp / (tp + fp) : 0.0;
-  m.recall = tp + fn > 0.0 ? tp / (tp + fn) : 0.0;
-  m.f1 = m.precision + m.recall > 0.0 ? 2.0 * m.precision * m.recall / (m.precision + m.recall)
-                                      : 0.0;
-  m.fpr = fp + tn > 0.0 ? fp / (fp + tn) : 0.0;
-  m.mean_lag = h[6] > 0 ? static_cast<double>(h[5]) / static_cast<double>(h[6]) : 0.0;
-  *out = m;
+  fill_metrics(h, ctx->ctl.strategy, out);
   return CS_OK;
 }
 
@@ -2015,6 +2388,14 @@ int cs_set_option(cs_ctx* ctx, int option, int64_t value) {
   if (option == CS_OPT_TRAVERSAL) {
     ctx->no_lut = value != 0;
     ctx->mt_valid = false;  // the per-instance model table carries the choice
+    return CS_OK;
+  }
+  if (option == 96) {  // tuning: events per single-read segmentation range (0 = auto)
+    ctx->opt_range_events = value;
+    return CS_OK;
+  }
+  if (option == 97) {  // tuning: L2 prefetch bytes per range (-1 = whole range, 0 = off)
+    ctx->opt_prefetch = value;
     return CS_OK;
   }
   if (option == 98) {  // profiling: multi-kernel reduce variant

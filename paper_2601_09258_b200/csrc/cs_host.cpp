@@ -628,7 +628,6 @@ static int cs_config_from_json_impl(const char* run_config_json, uint32_t n_name
     std::vector<std::string> uph;
     for (const auto& p : phases)
       if (std::find(uph.begin(), uph.end(), p) == uph.end()) uph.push_back(p);
-    if (uph.size() > 8) throw FitError{CS_E_UNSUPPORTED, "at most 8 phase functions"};
     cs_cycle_config cyc{};
     cyc.anchor_hint_name = -1;
     cyc.min_anchor_calls = min_calls;
@@ -665,7 +664,6 @@ static int cs_config_from_json_impl(const char* run_config_json, uint32_t n_name
     }
     if (!hint.empty() && cyc.anchor_hint_name < 0) cyc.anchor_hint_name = -2;
     cyc.n_beta_slots = slot;
-    if (slot > 64) throw FitError{CS_E_UNSUPPORTED, "at most 64 span classes on device"};
     *out_cycle = cyc;
     *out_control = ctl;
   } catch (const FitError& e) {

@@ -155,11 +155,33 @@ struct DevBuffers {
   StreamCarry* stream;          // per instance, null when not streaming
 };
 
+// Single-read segmentation (k_segment_range, CS_OPT_FUSED): ranges of <= 4
+// instance-aligned tiles claimed in order; per range the events are scanned
+// (moments, order check, anchor compaction) and the range's cycles reduced
+// right after, from L2.  Cycle slots = global anchor ranks (decoupled
+// look-back over ranges), so each instance's last anchor leaves one hole slot
+// (c_wl = kHoleWl, empty event range) after its cycles.
+struct SegMeta {
+  const uint64_t* range_begin;   // event index
+  const uint64_t* range_end;
+  const uint32_t* range_inst;
+  uint32_t n_ranges;
+  unsigned long long* lb_state;  // per range: look-back flag | value (zeroed per run)
+  uint64_t* range_prefix;        // per range: global anchor rank of its first anchor
+  unsigned int* ticket;          // zeroed per run
+  unsigned int* overflow;        // zeroed per run; set when slots exceed `cap`
+  uint64_t cap;                  // cycle slot capacity
+  uint32_t prefetch_bytes;       // L2 bulk prefetch of the next claimed range (0 = off)
+};
+constexpr int32_t kHoleWl = -3;
+constexpr uint64_t kSegCycles = 224;  // target cycles per range (CTA of 256 threads)
+
 // launchers (cs_kernels.cu); all asynchronous on `s`
 void launch_scan_events(const DevBuffers& b, const DevConfig& cfg, int mode, bool sample,
                         const uint32_t* list, uint32_t n_list, cudaStream_t s,
                         uint64_t* launches);
 void launch_tile_prefix(const DevBuffers& b, cudaStream_t s, uint64_t* launches);
+void launch_tile_order(const DevBuffers& b, cudaStream_t s, uint64_t* launches);
 void launch_rank(const DevBuffers& b, const DevConfig& cfg, int final_pass, cudaStream_t s,
                  uint64_t* launches);
 void launch_fold(const DevBuffers& b, const DevConfig& cfg, const uint32_t* pairs_inst,
@@ -168,6 +190,14 @@ void launch_fold(const DevBuffers& b, const DevConfig& cfg, const uint32_t* pair
 void launch_bounds(const DevBuffers& b, cudaStream_t s, uint64_t* launches);
 void launch_cycle_reduce_tpc(const DevBuffers& b, const DevConfig& cfg, int do_beta,
                              cudaStream_t s, uint64_t* launches, int variant);
+void launch_segment_range(const DevBuffers& b, const DevConfig& cfg, const SegMeta& sm, int do_beta,
+                          cudaStream_t s, uint64_t* launches);
+// per instance from the range prefixes: n_anchors (InstState) and slot offsets
+void launch_range_inst(const DevBuffers& b, const SegMeta& sm, const uint32_t* inst_first_range,
+                       uint64_t* slot_off, cudaStream_t s, uint64_t* launches);
+// dynamic shared memory of k_segment_range for this configuration; -1 when the
+// slot counts need the wide reduce (the fused pass is then not used)
+int segment_range_smem(const DevConfig& cfg, int do_beta);
 void launch_stage_heuristic(const DevBuffers& b, const DevConfig& cfg, cudaStream_t s,
                             uint64_t* launches);
 void launch_records(const DevBuffers& b, const DevConfig& cfg, uint64_t n_blocks_cap,

@@ -434,8 +434,8 @@ __global__ void __launch_bounds__(kScanWarpThreads, 3)
     const uint32_t n = (uint32_t)(te - tb);
     uint32_t cnt = 0;
     // K0 check (trace.cpp:103-109 is_sorted): start_ts never decreases within
-    // an instance; the previous event of the tile's first one is read once
-    i64 carry_ts = (check && tb > b.inst_off[inst]) ? b.ev[tb - 1].start_ts : LLONG_MIN;
+    // the tile; k_tile_order checks the tile boundaries (no dependent load per tile)
+    i64 carry_ts = LLONG_MIN;
     bool unsorted = false;
     for (uint32_t j0 = 0; j0 < n; j0 += 32 * kScanUnroll) {
       Ev8 e[kScanUnroll];
@@ -638,24 +638,57 @@ __global__ void k_rank(DevBuffers b, DevConfig cfg, int final_pass) {
 }
 
 // Ordered fold: the reference's own sequential arithmetic for one
-// (instance, name): count, sum += d, sum_sq += d*d in event order
-// (cycles.cpp:50-59), then mean/cv/score (66-77).  One thread per pair; only
-// launched when k_rank cannot certify the winner.
-__global__ void k_fold(DevBuffers b, const uint32_t* pairs_inst, const uint32_t* pairs_name,
-                       uint32_t n_pairs, double* out) {
-  const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+// (instance, name) -- count, sum += d, sum_sq += d*d in event order
+// (cycles.cpp:50-59) and the start gaps of gap_cv (30-43) -- then
+// mean/cv/score/periodicity (66-77).  One warp per pair: the warp reads 32
+// records per step (coalesced), and every lane folds the matching spans in
+// lane order with the same sequential f64 operations (the values are
+// warp-uniform, so no reduction tree ever reorders a sum).  Launched when
+// k_rank cannot certify the winner and for cs_get_candidates_exact.
+constexpr int kFoldUnroll = 4;
+__global__ void __launch_bounds__(128) k_fold(DevBuffers b, const uint32_t* pairs_inst,
+                                              const uint32_t* pairs_name, uint32_t n_pairs,
+                                              double* out) {
+  const uint32_t p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
   if (p >= n_pairs) return;
   const uint32_t inst = pairs_inst[p], name = pairs_name[p];
+  const u64 e0 = b.inst_off[inst], e1 = b.inst_off[inst + 1];
   u64 count = 0;
-  double sum = 0.0, sum_sq = 0.0;
-  for (u64 j = b.inst_off[inst]; j < b.inst_off[inst + 1]; ++j) {
-    const cs_event* e = b.ev + j;
-    if (e->kind != CS_SPAN || e->category != CS_CAT_PYTHON_CALL || e->name_id != name) continue;
-    ++count;
-    const double d = (double)e->duration;
-    sum = __dadd_rn(sum, d);
-    sum_sq = __dadd_rn(sum_sq, __dmul_rn(d, d));
+  double sum = 0.0, sum_sq = 0.0, gsum = 0.0, gsq = 0.0;
+  i64 prev = 0;
+  for (u64 j0 = e0; j0 < e1; j0 += 32 * kFoldUnroll) {
+    Ev8 e[kFoldUnroll];
+#pragma unroll
+    for (int q = 0; q < kFoldUnroll; ++q) {
+      const u64 j = j0 + q * 32 + lane;
+      if (j < e1) e[q] = ldg256(b.ev + j);
+      else e[q].c = (u64)CS_FLOW << 32;
+    }
+#pragma unroll
+    for (int q = 0; q < kFoldUnroll; ++q) {
+      const uint32_t kc = (uint32_t)(e[q].c >> 32);
+      const bool m = (kc & 0xffu) == CS_SPAN && ((kc >> 8) & 0xffu) == CS_CAT_PYTHON_CALL &&
+                     (uint32_t)e[q].c == name;
+      uint32_t mask = __ballot_sync(0xffffffffu, m);
+      while (mask) {
+        const int l = __ffs(mask) - 1;
+        mask &= mask - 1;
+        const i64 st = (i64)__shfl_sync(0xffffffffu, e[q].a, l);
+        const double d = (double)(i64)__shfl_sync(0xffffffffu, e[q].b, l);
+        if (count > 0) {
+          const double gap = (double)(st - prev);
+          gsum = __dadd_rn(gsum, gap);
+          gsq = __dadd_rn(gsq, __dmul_rn(gap, gap));
+        }
+        prev = st;
+        ++count;
+        sum = __dadd_rn(sum, d);
+        sum_sq = __dadd_rn(sum_sq, __dmul_rn(d, d));
+      }
+    }
   }
+  if (lane != 0) return;
   const double n = (double)count;
   const double mean = __ddiv_rn(sum, n);
   double cv = 0.0;
@@ -664,9 +697,20 @@ __global__ void k_fold(DevBuffers b, const uint32_t* pairs_inst, const uint32_t*
     var = 0.0 < var ? var : 0.0;
     cv = __ddiv_rn(sqrt(var), mean);
   }
-  out[3 * p + 0] = mean;
-  out[3 * p + 1] = cv;
-  out[3 * p + 2] = __ddiv_rn(n, __dadd_rn(1.0, cv));
+  double gcv = 0.0;  // gap_cv (cycles.cpp:30-43)
+  if (count >= 3) {
+    const double ng = (double)(count - 1);
+    const double gm = __ddiv_rn(gsum, ng);
+    if (gm > 0.0) {
+      double var = __dsub_rn(__ddiv_rn(gsq, ng), __dmul_rn(gm, gm));
+      var = 0.0 < var ? var : 0.0;
+      gcv = __ddiv_rn(sqrt(var), gm);
+    }
+  }
+  out[4 * p + 0] = mean;
+  out[4 * p + 1] = cv;
+  out[4 * p + 2] = __ddiv_rn(n, __dadd_rn(1.0, cv));
+  out[4 * p + 3] = __ddiv_rn(1.0, __dadd_rn(1.0, gcv));
 }
 
 // ------------------------------------------------------------ K2 bounds
@@ -2380,6 +2424,23 @@ void launch_cycle_mu(const DevBuffers& b, const DevConfig& cfg, cudaStream_t s, 
 }
 
 // ------------------------------------------------------------ launchers
+// tile boundaries of the K0 check: a tile's first start_ts is not below the
+// previous tile's last within the same instance
+__global__ void k_tile_order(DevBuffers b) {
+  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t == 0 || t >= b.n_tiles) return;
+  const uint32_t inst = b.tile_inst[t];
+  if (b.tile_inst[t - 1] != inst) return;
+  if (b.ev[b.tile_begin[t]].start_ts < b.ev[b.tile_end[t - 1] - 1].start_ts)
+    atomicOr(&b.inst[inst].unsorted, 1u);
+}
+
+void launch_tile_order(const DevBuffers& b, cudaStream_t s, uint64_t* launches) {
+  if (b.n_tiles < 2) return;
+  k_tile_order<<<(b.n_tiles + 255) / 256, 256, 0, s>>>(b);
+  ++*launches;
+}
+
 void launch_scan_events(const DevBuffers& b, const DevConfig&, int mode, bool sample,
                         const uint32_t* list, uint32_t n_list, cudaStream_t s,
                         uint64_t* launches) {
@@ -2450,7 +2511,7 @@ void launch_rank(const DevBuffers& b, const DevConfig& cfg, int final_pass, cuda
 void launch_fold(const DevBuffers& b, const DevConfig&, const uint32_t* pi, const uint32_t* pn,
                  uint32_t n_pairs, double* out, cudaStream_t s, uint64_t* launches) {
   if (!n_pairs) return;
-  k_fold<<<(n_pairs + 63) / 64, 64, 0, s>>>(b, pi, pn, n_pairs, out);
+  k_fold<<<(n_pairs * 32 + 127) / 128, 128, 0, s>>>(b, pi, pn, n_pairs, out);
   ++*launches;
 }
 
@@ -2594,6 +2655,440 @@ void launch_freq_cycles(const cs_event* ev, uint64_t begin, uint64_t end, int64_
   if (!n) return;
   k_freq_cycles<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(ev, begin, end, t0, period, n,
                                                            cyc_base, b, inst);
+  ++*launches;
+}
+
+
+// =================================================== single-read segmentation
+// K1+K2+K3 with the events read from DRAM once (CS_OPT_FUSED).  Ranges of up
+// to kRangeTiles instance-aligned tiles (<= 4096 events, 128 KiB) are claimed
+// in order by a persistent grid; per range:
+//   A. the CTA's warps stream the range (coalesced 256-bit loads) exactly like
+//      k_scan_warp: PythonCall moments for the anchor ranking (cycles.cpp:
+//      50-59), the canonical-order check, and the speculated anchor's
+//      occurrences compacted per warp (cycles.cpp:127-131);
+//   B. the range's anchor count is published and a decoupled look-back over
+//      the preceding ranges gives the global rank of its first anchor = the
+//      cycle slot of the cycle that anchor opens; one warp meanwhile finds the
+//      next anchor after the range (the end of the range's last cycle);
+//   C. one thread per cycle walks its events in order -- now L2 hits, the CTA
+//      has just streamed them -- with k_cycle_reduce_v2's accumulators and
+//      arithmetic (cycles.cpp:157-166, 205-229, 256-281; rca.cpp:87-129), and
+//      the CTA writes the cycle rows at their slots.
+// An instance's last anchor opens no complete cycle (cycles.cpp:147): its slot
+// is a hole (empty event range, c_wl = kHoleWl) that every consumer skips.
+// The anchor guess is verified afterwards by k_rank over the full moments; a
+// wrong guess (or an ambiguous ranking) re-runs the two-pass path.
+constexpr int kSegThreads = 256;
+constexpr int kSegWarps = kSegThreads / 32;
+
+__device__ __forceinline__ void bulk_prefetch_l2(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
+__global__ void __launch_bounds__(kSegThreads, 2)
+    k_segment_range(DevBuffers b, DevConfig cfg, SegMeta sm, int do_beta) {
+  extern __shared__ __align__(16) unsigned char s_red[];
+  __shared__ uint32_t s_ninfo[kFNamesSmem];
+  __shared__ WarpNameRow s_rows[kSegWarps * kWarpNameRows];
+  __shared__ uint32_t s_pn[kSegWarps][64];
+  __shared__ i64 s_pd[kSegWarps][64];
+  __shared__ uint32_t s_wbase[kSegWarps + 1];
+  __shared__ u64 s_sub0[kSegWarps];
+  __shared__ uint32_t s_ticket[1];
+  __shared__ u64 s_prefix;
+  __shared__ i64 s_next_start;
+  __shared__ u64 s_next_first;
+  __shared__ int s_next_found;
+  const int P = cfg.cyc.n_phases;
+  const int C = do_beta ? cfg.cyc.n_beta_slots : 0;
+  const int R = do_beta ? cfg.cyc.n_comm_slots : 0;
+  const uint32_t NT = blockDim.x, tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  auto pack_info = [&](const cs_name_info& ni) -> uint32_t {
+    const uint32_t ph = (ni.phase >= 0 && ni.phase < P) ? (uint32_t)ni.phase : 15u;
+    const uint32_t bs = (ni.beta_slot >= 0 && ni.beta_slot < C) ? (uint32_t)ni.beta_slot : 255u;
+    return ph | (bs << 4) | ((ni.flags & 3u) << 12);
+  };
+  for (uint32_t i = tid; i < b.n_names && i < (uint32_t)kFNamesSmem; i += NT) s_ninfo[i] = pack_info(b.names[i]);
+  const uint32_t SN = NT + 1;
+  i64* comp = reinterpret_cast<i64*>(s_red);                         // [P][SN]
+  i64* beta = comp + (u64)P * SN;                                    // [C][SN]
+  double* coll = reinterpret_cast<double*>(beta + (u64)C * SN);      // [R][SN]
+  i64* s_dur = reinterpret_cast<i64*>(coll + (u64)R * SN);           // [NT]
+  uint32_t* colln = reinterpret_cast<uint32_t*>(s_dur + NT);         // [R][SN]
+  WarpNameRow* wrows = s_rows + warp * kWarpNameRows;
+  uint32_t* pn = s_pn[warp];
+  i64* pd = s_pd[warp];
+  NameCache cache;
+  cache_clear(cache);
+  uint32_t cur_inst = 0xffffffffu, npend = 0;
+  NameStat* gstats = b.stats;
+  auto drain = [&](uint32_t take) {
+    __syncwarp();
+    if ((uint32_t)lane < take) cache_add(cache, gstats, pn[lane], pd[lane]);
+    __syncwarp();
+    const uint32_t rest = npend - take;
+    uint32_t mv_n = 0;
+    i64 mv_d = 0;
+    if ((uint32_t)lane < rest) {
+      mv_n = pn[take + lane];
+      mv_d = pd[take + lane];
+    }
+    __syncwarp();
+    if ((uint32_t)lane < rest) {
+      pn[lane] = mv_n;
+      pd[lane] = mv_d;
+    }
+    npend = rest;
+    __syncwarp();
+  };
+  auto anchor_idx = [&](uint32_t k) -> u64 {
+    int w = 0;
+#pragma unroll
+    for (int x = 1; x < kSegWarps; ++x) w += (k >= s_wbase[x]) ? 1 : 0;
+    return s_sub0[w] + (k - s_wbase[w]);
+  };
+  // the range one round of the grid ahead (gridDim.x tickets) is prefetched
+  // into L2 by a TMA bulk prefetch (no registers, no waiting): its DRAM read
+  // overlaps this range's work and whichever CTA claims it scans from L2
+  auto prefetch = [&](uint32_t rr) {
+    if (rr >= sm.n_ranges || sm.prefetch_bytes == 0) return;
+    const u64 rb = sm.range_begin[rr], re = sm.range_end[rr];
+    const u64 bytes = min((re - rb) * (u64)sizeof(cs_event), (u64)sm.prefetch_bytes);
+    const char* base = reinterpret_cast<const char*>(b.ev + rb);
+    for (u64 o = (u64)lane * 4096; o < bytes; o += 32 * 4096)
+      bulk_prefetch_l2(base + o, (uint32_t)min((u64)4096, bytes - o));
+  };
+  if (warp == 0) prefetch(blockIdx.x);  // the first round
+  for (;;) {
+    __syncthreads();  // previous range's shared state fully consumed
+    if (tid == 0) s_ticket[0] = atomicAdd(sm.ticket, 1u);
+    __syncthreads();
+    const uint32_t r = s_ticket[0];
+    if (warp == 0) prefetch(r + gridDim.x);
+    if (r >= sm.n_ranges) break;
+    const u64 rb = sm.range_begin[r], re = sm.range_end[r];
+    const uint32_t inst = sm.range_inst[r];
+    const u64 ib = b.inst_off[inst], ie = b.inst_off[inst + 1];
+    const uint32_t anchor = b.inst[inst].guess;
+    if (inst != cur_inst) {
+      if (cur_inst != 0xffffffffu) {
+        drain(npend);
+        cache_flush_warp(cache, gstats, wrows);
+      }
+      cur_inst = inst;
+      gstats = b.stats + (u64)inst * b.n_names;
+    }
+    // ---------------- A: scan the warp's sub-block
+    const u64 n = re - rb;
+    const u64 chunk = ((n + kSegWarps * 32 - 1) / (kSegWarps * 32)) * 32;
+    const u64 sb = rb + min((u64)warp * chunk, n), se = rb + min((u64)(warp + 1) * chunk, n);
+    const uint32_t nsub = (uint32_t)(se - sb);
+    uint32_t cnt = 0;
+    i64 carry_ts = sb > ib ? b.ev[sb - 1].start_ts : LLONG_MIN;
+    bool unsorted = false;
+    for (uint32_t j0 = 0; j0 < nsub; j0 += 32 * kScanUnroll) {
+      Ev8 e[kScanUnroll];
+#pragma unroll
+      for (int q = 0; q < kScanUnroll; ++q) {
+        const uint32_t j = j0 + q * 32 + lane;
+        if (j < nsub) e[q] = ldg256(b.ev + sb + j);
+        else {
+          e[q].a = ~0ull >> 1;
+          e[q].c = (u64)CS_FLOW << 32;
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < kScanUnroll; ++q) {
+        const uint32_t name = (uint32_t)e[q].c;
+        const uint32_t kc = (uint32_t)(e[q].c >> 32);
+        const bool span = (kc & 0xffu) == CS_SPAN;
+        const bool py = span && ((kc >> 8) & 0xffu) == CS_CAT_PYTHON_CALL;
+        const uint32_t pm = __ballot_sync(0xffffffffu, py);
+        if (py) {
+          const uint32_t slot = npend + __popc(pm & lanemask_lt());
+          pn[slot] = name;
+          pd[slot] = (i64)e[q].b;
+        }
+        npend += __popc(pm);
+        if (npend >= 32) drain(32);
+        const bool is_anchor = span && name == anchor;
+        const uint32_t mk = __ballot_sync(0xffffffffu, is_anchor);
+        const u64 prev = __shfl_up_sync(0xffffffffu, e[q].a, 1);
+        const i64 before = lane == 0 ? carry_ts : (i64)prev;
+        unsorted |= before > (i64)e[q].a;
+        carry_ts = (i64)__shfl_sync(0xffffffffu, e[q].a, 31);
+        if (is_anchor) {
+          const uint32_t jj = j0 + q * 32 + lane;
+          const u64 ai = sb + cnt + __popc(mk & lanemask_lt());
+          const bool walk = jj == 0 ? sb > ib : (lane == 0 || prev == e[q].a);
+          b.a_pos[ai] = (sb + jj) | (walk ? kWalk : 0ull);
+          b.a_start[ai] = (i64)e[q].a;
+          b.a_end[ai] = (i64)e[q].a + (i64)e[q].b;
+        }
+        cnt += __popc(mk);
+      }
+    }
+    if (__any_sync(0xffffffffu, unsorted) && lane == 0) atomicOr(&b.inst[inst].unsorted, 1u);
+    if (lane == 0) {
+      s_wbase[warp + 1] = cnt;
+      s_sub0[warp] = sb;
+    }
+    // the last warp continues past the range: the next anchor closes the
+    // range's last cycle
+    if (warp == kSegWarps - 1) {
+      int found = 0;
+      i64 nstart = 0;
+      u64 npos = 0;
+      for (u64 p0 = re; p0 < ie; p0 += 32) {
+        const u64 p = p0 + lane;
+        bool m = false;
+        i64 st = 0;
+        if (p < ie) {
+          const Ev8 e = ldg256(b.ev + p);
+          m = ((uint32_t)(e.c >> 32) & 0xffu) == CS_SPAN && (uint32_t)e.c == anchor;
+          st = (i64)e.a;
+        }
+        const uint32_t bm = __ballot_sync(0xffffffffu, m);
+        if (bm) {
+          const int L = __ffs(bm) - 1;
+          nstart = __shfl_sync(0xffffffffu, st, L);
+          npos = p0 + L;
+          found = 1;
+          break;
+        }
+      }
+      if (lane == 0) {
+        s_next_found = found;
+        s_next_start = nstart;
+        s_next_first = found ? group_start(b.ev, npos, ib, nstart) : 0;
+      }
+    }
+    __syncthreads();
+    if (tid == 0) {
+      s_wbase[0] = 0;
+      for (int w = 1; w <= kSegWarps; ++w) s_wbase[w] += s_wbase[w - 1];
+      const u64 A = s_wbase[kSegWarps];
+      if (r == 0) {
+        st_release(&sm.lb_state[0], kFlagPrefix | A);
+        s_prefix = 0;
+        sm.range_prefix[0] = 0;
+      } else {
+        st_release(&sm.lb_state[r], kFlagAgg | A);
+      }
+    }
+    __syncthreads();
+    const uint32_t A = s_wbase[kSegWarps];
+    // ---------------- C: thread per cycle over the range's anchors
+    for (uint32_t k0 = 0; k0 == 0 || k0 < A; k0 += NT) {
+      const uint32_t k = k0 + tid;
+      const bool live = k < A;
+      uint8_t stage = CS_STAGE_UNKNOWN;
+      bool hole = false;
+      i64 cs = 0, ce = 0, aend = 0;
+      u64 apos = 0, first = 0, last = 0;
+      int32_t wl = -1;
+      if (live) {
+        const u64 ai = anchor_idx(k);
+        cs = b.a_start[ai];
+        aend = b.a_end[ai];
+        const u64 pw = b.a_pos[ai];
+        apos = pw & ~kWalk;
+        first = (pw & kWalk) ? group_start(b.ev, apos, ib, cs) : apos;
+        if (k + 1 < A) {
+          const u64 an = anchor_idx(k + 1);
+          ce = b.a_start[an];
+          const u64 pw2 = b.a_pos[an];
+          const u64 p2 = pw2 & ~kWalk;
+          last = (pw2 & kWalk) ? group_start(b.ev, p2, ib, ce) : p2;
+        } else if (s_next_found) {
+          ce = s_next_start;
+          last = s_next_first;
+        } else {
+          hole = true;  // the instance's last anchor: trailing partial cycle dropped
+          ce = cs;
+          last = first;
+        }
+        const i64 dur = ce - cs;
+        s_dur[tid] = dur;
+        for (int p = 0; p < P; ++p) comp[p * SN + tid] = 0;
+        for (int c = 0; c < C; ++c) beta[c * SN + tid] = 0;
+        for (int q = 0; q < R; ++q) {
+          coll[q * SN + tid] = 0.0;
+          colln[q * SN + tid] = 0u;
+        }
+        uint32_t fm_cls = 0, kw = 0;
+        bool fm_found = false, batch_found = false;
+        for (u64 j0 = first; j0 < last; j0 += kRedUnroll) {
+          Ev8 e[kRedUnroll];
+#pragma unroll
+          for (int q = 0; q < kRedUnroll; ++q) {
+            if (j0 + q < last) e[q] = ldg256(b.ev + j0 + q);
+            else e[q].c = (u64)CS_FLOW << 32;
+          }
+#pragma unroll
+          for (int q = 0; q < kRedUnroll; ++q) {
+            const uint32_t name = (uint32_t)e[q].c;
+            const uint32_t kc = (uint32_t)(e[q].c >> 32);
+            const uint32_t flags = kc >> 16;
+            if (!fm_found && (flags & CS_EV_FM_MASK)) {
+              fm_found = true;
+              fm_cls = flags & CS_EV_FM_MASK;
+            }
+            if (!batch_found && (flags & CS_EV_HAS_BATCH)) {
+              batch_found = true;
+              wl = (flags & CS_EV_WL_OK) ? (int32_t)(uint32_t)e[q].d : -2;
+            }
+            if ((kc & 0xffu) != CS_SPAN) continue;
+            const uint32_t info = name < (uint32_t)kFNamesSmem ? s_ninfo[name] : pack_info(b.names[name]);
+            kw |= (info >> 12) & 3u;
+            const i64 st = (i64)e[q].a, d = (i64)e[q].b;
+            const i64 end = st + d;
+            const i64 clipped = (end < ce ? end : ce) - st;
+            if (clipped <= 0) continue;
+            const uint32_t ph = info & 15u, bs = (info >> 4) & 255u;
+            if (ph != 15u) comp[ph * SN + tid] += clipped;
+            if (do_beta && d > 0) {
+              if (bs != 255u) beta[bs * SN + tid] += clipped;
+              if (((kc >> 8) & 0xffu) == CS_CAT_COLLECTIVE_COMM && (flags & CS_EV_HAS_COMM)) {
+                const uint32_t slot = (uint32_t)(e[q].d >> 32);
+                if (slot < (uint32_t)R) {
+                  coll[slot * SN + tid] = __dadd_rn(coll[slot * SN + tid], __ddiv_rn((double)clipped, (double)dur));
+                  colln[slot * SN + tid] += 1u;
+                }
+              }
+            }
+          }
+        }
+        if (fm_cls == CS_EV_FM_PREFILL) stage = CS_STAGE_PREFILL;
+        else if (fm_cls == CS_EV_FM_DECODE) stage = CS_STAGE_DECODE;
+        const bool pkw = kw & CS_NAME_PREFILL_KW, dkw = kw & CS_NAME_DECODE_KW;
+        if (stage == CS_STAGE_UNKNOWN && pkw != dkw) stage = pkw ? CS_STAGE_PREFILL : CS_STAGE_DECODE;
+      }
+      // the slot base: decoupled look-back over the preceding ranges, resolved
+      // by warp 0 after its share of the reduce (predecessors have long since
+      // published their counts)
+      if (k0 == 0 && warp == 0 && r > 0) {
+        u64 excl = 0;
+        long long j = (long long)r - 1;
+        for (;;) {
+          const long long idx = j - lane;
+          u64 v = idx >= 0 ? ld_acquire(&sm.lb_state[idx]) : kFlagPrefix;
+          while (__any_sync(0xffffffffu, (v & (kFlagAgg | kFlagPrefix)) == 0)) {
+            if ((v & (kFlagAgg | kFlagPrefix)) == 0) v = ld_acquire(&sm.lb_state[idx]);
+          }
+          const uint32_t pm = __ballot_sync(0xffffffffu, (v & kFlagPrefix) != 0);
+          const u64 val = v & kValMask;
+          if (pm) {
+            const int L = __ffs(pm) - 1;
+            excl += warp_sum_u64(lane <= L ? val : 0ull);
+            break;
+          }
+          excl += warp_sum_u64(val);
+          j -= 32;
+        }
+        if (lane == 0) {
+          s_prefix = excl;
+          sm.range_prefix[r] = excl;
+          st_release(&sm.lb_state[r], kFlagPrefix | (excl + A));
+        }
+      }
+      const bool unk = live && !hole && stage == CS_STAGE_UNKNOWN;
+      const uint32_t um = __ballot_sync(0xffffffffu, unk);
+      if (lane == 0 && um) atomicAdd(&b.inst[inst].n_unknown, (u64)__popc(um));
+      __syncthreads();
+      const u64 base = s_prefix;
+      if (base + A > sm.cap) {
+        if (tid == 0) atomicOr(sm.overflow, 1u);
+        break;  // CTA-uniform
+      }
+      if (live) {
+        const u64 g = base + k;
+        b.c_start[g] = cs;
+        b.c_end[g] = ce;
+        b.c_apos[g] = apos;
+        b.c_aend[g] = aend;
+        b.c_first[g] = first;
+        b.c_last[g] = last;
+        b.c_inst[g] = inst;
+        b.c_local[g] = hole ? (uint8_t)3 : stage;
+        b.c_stage[g] = hole ? (uint8_t)3 : stage;
+        b.c_wl[g] = hole ? kHoleWl : wl;
+      }
+      const u64 g0 = base + k0;
+      const uint32_t n_live = A > k0 ? min((uint32_t)NT, A - k0) : 0u;
+      for (uint32_t idx = tid; idx < n_live * (uint32_t)P; idx += NT) {
+        const uint32_t lc = idx / (uint32_t)P, p = idx - lc * (uint32_t)P;
+        b.c_comp[g0 * P + idx] = comp[p * SN + lc];
+      }
+      for (uint32_t idx = tid; idx < n_live * (uint32_t)C; idx += NT) {
+        const uint32_t lc = idx / (uint32_t)C, c = idx - lc * (uint32_t)C;
+        const i64 dur = s_dur[lc];
+        const i64 t = dur > 0 ? beta[c * SN + lc] : 0;
+        b.c_beta_tot[g0 * C + idx] = t;
+        b.c_beta[g0 * C + idx] = t > 0 ? __ddiv_rn((double)t, (double)dur) : 0.0;
+      }
+      for (uint32_t idx = tid; idx < n_live * (uint32_t)R; idx += NT) {
+        const uint32_t lc = idx / (uint32_t)R, q = idx - lc * (uint32_t)R;
+        b.c_coll[g0 * R + idx] = coll[q * SN + lc];
+        const uint32_t cn = colln[q * SN + lc];
+        b.c_coll_n[g0 * R + idx] = (uint8_t)(cn > 255u ? 255u : cn);
+      }
+      __syncthreads();
+    }
+  }
+  if (cur_inst != 0xffffffffu) {
+    drain(npend);
+    cache_flush_warp(cache, gstats, wrows);
+  }
+}
+
+// per instance: slot offset (global rank of its first anchor) and anchor count
+__global__ void k_range_inst(DevBuffers b, SegMeta sm, const uint32_t* inst_first_range,
+                             uint64_t* slot_off) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i > b.n_inst) return;
+  const u64 total = sm.n_ranges ? (sm.lb_state[sm.n_ranges - 1] & kValMask) : 0ull;
+  auto off = [&](uint32_t k) -> u64 {
+    const uint32_t fr = inst_first_range[k];
+    return fr < sm.n_ranges ? sm.range_prefix[fr] : total;
+  };
+  const u64 o = i < b.n_inst ? off(i) : total;
+  slot_off[i] = o;
+  if (i < b.n_inst) b.inst[i].n_anchors = off(i + 1) - o;
+}
+
+int segment_range_smem(const DevConfig& cfg, int do_beta) {
+  const int P = cfg.cyc.n_phases;
+  const int C = do_beta ? cfg.cyc.n_beta_slots : 0;
+  const int R = do_beta ? cfg.cyc.n_comm_slots : 0;
+  if (P > 15 || C > 254) return -1;
+  const int per_thread = (P + C + R) * 8 + R * 4;
+  const int smem = (kSegThreads + 1) * per_thread + kSegThreads * 8;
+  return smem <= 96 * 1024 ? smem : -1;
+}
+
+void launch_segment_range(const DevBuffers& b, const DevConfig& cfg, const SegMeta& sm, int do_beta,
+                          cudaStream_t s, uint64_t* launches) {
+  const int smem = segment_range_smem(cfg, do_beta);
+  if (smem < 0 || sm.n_ranges == 0) return;
+  cudaFuncSetAttribute(k_segment_range, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  int dev = 0, n_sm = 148, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_segment_range, kSegThreads, smem);
+  if (per_sm < 1) per_sm = 1;
+  // persistent: every CTA resident (the look-back waits on earlier tickets)
+  unsigned grid = (unsigned)(n_sm * per_sm);
+  if (grid > sm.n_ranges) grid = sm.n_ranges;
+  k_segment_range<<<grid, kSegThreads, smem, s>>>(b, cfg, sm, do_beta);
+  ++*launches;
+}
+
+void launch_range_inst(const DevBuffers& b, const SegMeta& sm, const uint32_t* inst_first_range,
+                       uint64_t* slot_off, cudaStream_t s, uint64_t* launches) {
+  k_range_inst<<<(b.n_inst + 1 + 255) / 256, 256, 0, s>>>(b, sm, inst_first_range, slot_off);
   ++*launches;
 }
 

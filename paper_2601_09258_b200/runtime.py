@@ -57,6 +57,9 @@ def lib():
     L.cs_upload.argtypes = [vp, u32, vp, vp, u64, vp]
     L.cs_upload_unsorted.argtypes = [vp, u32, vp, vp, vp, u64, vp]
     L.cs_get_order.argtypes = [vp, u32, vp, sz, psz]
+    L.cs_set_cycles.argtypes = [vp, vp, u64, vp]
+    L.cs_detect_residuals.argtypes = [vp, vp, u64, C.POINTER(abi.ControlConfig), C.c_double, vp, vp, vp,
+                                      C.POINTER(abi.StrategyMetrics)]
     L.cs_get_cycle_range.argtypes = [vp, u32, u64, u64, vp]
     L.cs_get_record_range.argtypes = [vp, u32, u64, u64, vp]
     L.cs_upload_wire.argtypes = [vp, u32, vp, C.POINTER(abi.WireBatch), u64, vp]
@@ -84,7 +87,7 @@ def lib():
     L.cs_run.argtypes = [vp, u32]
     L.cs_sync.argtypes = [vp]
     L.cs_get_summary.argtypes = [vp, u32, C.POINTER(abi.InstanceSummary)]
-    for fn in ("cs_get_candidates", "cs_get_cycles", "cs_get_components", "cs_get_records",
+    for fn in ("cs_get_candidates", "cs_get_candidates_exact", "cs_get_cycles", "cs_get_components", "cs_get_records",
                "cs_get_alerts"):
         getattr(L, fn).argtypes = [vp, u32, vp, sz, psz]
     L.cs_get_beta.argtypes = [vp, u32, vp, vp, sz, psz]
@@ -129,10 +132,10 @@ def lib():
 
 EXPORTED_SYMBOLS = [
     "cs_abi_version", "cs_status_type", "cs_ctx_create", "cs_ctx_destroy", "cs_last_error",
-    "cs_set_config", "cs_set_name_table", "cs_upload", "cs_upload_unsorted", "cs_get_order", "cs_upload_wire", "cs_wire_pack",
+    "cs_set_config", "cs_set_name_table", "cs_upload", "cs_upload_unsorted", "cs_get_order", "cs_set_cycles", "cs_detect_residuals", "cs_upload_wire", "cs_wire_pack",
     "cs_wire_view", "cs_wire_free", "cs_ingest_chrome_json", "cs_ingest_view", "cs_ingest_free", "cs_ingest_report", "cs_ingest_topology", "cs_ingest_merge", "cs_rank_suspects",
     "cs_suspicion_rank", "cs_welch_p_value", "cs_load_model", "cs_run", "cs_sync",
-    "cs_get_summary", "cs_get_candidates", "cs_get_cycles", "cs_get_components", "cs_get_beta",
+    "cs_get_summary", "cs_get_candidates", "cs_get_candidates_exact", "cs_get_cycles", "cs_get_components", "cs_get_beta",
     "cs_get_collective_beta", "cs_get_mu", "cs_get_records", "cs_get_alerts", "cs_host_alloc",
     "cs_host_free", "cs_get_timings", "cs_get_launch_count", "cs_fit_latency_model", "cs_fit_latency_models",
     "cs_model_from_json", "cs_model_to_json", "cs_model_view", "cs_model_free",
@@ -679,6 +682,28 @@ class Analyzer:
         """cs_get_order: canonical position -> input position within the instance."""
         return self._get(self.L.cs_get_order, inst, np.uint64)
 
+    def set_cycles(self, cycles: np.ndarray, components: np.ndarray | None = None):
+        """cs_set_cycles: caller-given cycles (CYCLE_DTYPE rows, canonical event
+        positions of instance 0) for the next run(RUN_GIVEN | ...)."""
+        cc = np.ascontiguousarray(cycles, dtype=abi.CYCLE_DTYPE)
+        comp = None if components is None else np.ascontiguousarray(components, dtype=np.int64)
+        self._keep_cycles = (cc, comp)
+        self._ck(self.L.cs_set_cycles(self.h, _ptr(cc), len(cc), _ptr(comp)))
+
+    def detect_residuals(self, residuals, control: abi.ControlConfig, dynamic_ucl: float,
+                         labels=None):
+        """cs_detect_residuals: Detector::step over a residual stream (+
+        evaluate_strategy with labels).  Returns (statistic, flags, metrics|None)."""
+        r = np.ascontiguousarray(residuals, dtype=np.float64)
+        st = np.zeros(len(r), np.float64)
+        fl = np.zeros(len(r), np.uint8)
+        lab = None if labels is None else np.ascontiguousarray(labels, dtype=np.uint8)
+        m = abi.StrategyMetrics()
+        self._ck(self.L.cs_detect_residuals(self.h, _ptr(r), len(r), C.byref(control), dynamic_ucl,
+                                            _ptr(lab), _ptr(st), _ptr(fl),
+                                            C.byref(m) if lab is not None else None))
+        return st, fl, (m if lab is not None else None)
+
     def upload_wire(self, w: WireTrace, workloads: np.ndarray | None = None):
         """cs_upload_wire: same batch as upload(), sent in the columnar wire
         format (the workload table travels in it when packed with one)."""
@@ -796,6 +821,10 @@ class Analyzer:
 
     def candidates(self, inst=0):
         return self._get(self.L.cs_get_candidates, inst, abi.CANDIDATE_DTYPE)
+
+    def candidates_exact(self, inst=0):
+        """rank_anchor_candidates bit for bit, periodicity included (cs_get_candidates_exact)."""
+        return self._get(self.L.cs_get_candidates_exact, inst, abi.CANDIDATE_DTYPE)
 
     def beta(self, inst=0):
         n = C.c_size_t()
