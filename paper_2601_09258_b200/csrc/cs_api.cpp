@@ -162,6 +162,7 @@ struct cs_ctx {
   std::vector<uint64_t> tile_begin, tile_end;
   DevBuf d_tile_inst, d_tile_begin, d_tile_end, d_inst_first_tile, d_tile_cnt, d_tile_pref;
   DevBuf d_scan_tmp;
+  DevBuf d_stage2, d_stage_changed, d_stage_lb, d_stage_ctl;  // k_stage_jacobi
   // counter-weighted mu: metric slots derived from the name table
   uint32_t n_metrics = 0;
   DevBuf d_series_slot, d_class_metric, d_m_off, d_s_ts, d_s_val, d_mu, d_mu_has;
@@ -472,8 +473,8 @@ int cs_set_config(cs_ctx* ctx, const cs_cycle_config* cycle, const cs_control_co
   if (cycle) {
     if (cycle->n_phases < 0 || cycle->n_beta_slots < 0 || cycle->n_comm_slots < 0)
       return fail(ctx, CS_E_INVALID_ARGUMENT, "negative phase / class / collective slot count");
-    if (cycle->stage_window == 0 || cycle->stage_window > 32)
-      return fail(ctx, CS_E_UNSUPPORTED, "stage_window must be in [1, 32]");
+    if (cycle->stage_window == 0 || cycle->stage_window > 1600)
+      return fail(ctx, CS_E_UNSUPPORTED, "stage_window must be in [1, 1600]");
     if (cycle->latency_phase >= cycle->n_phases)
       return fail(ctx, CS_E_INVALID_ARGUMENT, "latency_phase out of range");
     if (cycle->frequency_bin_ns <= 0)
@@ -1428,7 +1429,22 @@ static int cs_run_impl(cs_ctx* ctx, uint32_t mask) {
   ctx->timed.push_back({"cycle_reduce", {e4, e5}});
   }
   b = make_buffers(ctx);
-  if (!ctx->given_run || (mask & CS_RUN_CLASSIFY)) launch_stage_heuristic(b, cfg, s, &ctx->launches);
+  if ((!ctx->given_run || (mask & CS_RUN_CLASSIFY)) && ctx->n_cycles) {
+    const uint64_t nch = (ctx->n_cycles + kStageChunkCycles - 1) / kStageChunkCycles;
+    if (!dev<uint8_t>(ctx->d_stage2, ctx->n_cycles) || !dev<int32_t>(ctx->d_stage_changed, nch) ||
+        !dev<uint64_t>(ctx->d_stage_lb, nch) || !dev<unsigned int>(ctx->d_stage_ctl, 8))
+      return fail(ctx, CS_E_CUDA, "cudaMalloc(stage heuristic)");
+    CS_CUDA(cudaMemcpyAsync(ctx->d_stage2.p, ctx->c_stage.p, ctx->n_cycles, cudaMemcpyDeviceToDevice, s));
+    CS_CUDA(cudaMemsetAsync(ctx->d_stage_changed.p, 0xff, nch * 4, s));
+    CS_CUDA(cudaMemsetAsync(ctx->d_stage_ctl.p, 0, 32, s));
+    auto* ctl = static_cast<unsigned int*>(ctx->d_stage_ctl.p);
+    StageMeta sm{{static_cast<uint8_t*>(ctx->c_stage.p), static_cast<uint8_t*>(ctx->d_stage2.p)},
+                 static_cast<uint32_t>(nch), static_cast<int32_t*>(ctx->d_stage_changed.p),
+                 static_cast<uint64_t*>(ctx->d_stage_lb.p), ctl, ctl + 2, ctl + 3, ctl + 4,
+                 static_cast<int>(nch) + 2};
+    if (launch_stage_heuristic(b, cfg, sm, s, &ctx->launches) != 0)
+      return fail(ctx, CS_E_UNSUPPORTED, "stage_window too large for the device heuristic (<= 1600)");
+  }
   launch_records(b, cfg, 0, s, &ctx->launches);
   const int e6m = record_event(ctx, 6);
   ctx->timed.push_back({"stage_records", {e5, e6m}});

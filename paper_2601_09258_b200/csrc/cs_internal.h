@@ -198,8 +198,24 @@ void launch_range_inst(const DevBuffers& b, const SegMeta& sm, const uint32_t* i
 // dynamic shared memory of k_segment_range for this configuration; -1 when the
 // slot counts need the wide reduce (the fused pass is then not used)
 int segment_range_smem(const DevConfig& cfg, int do_beta);
-void launch_stage_heuristic(const DevBuffers& b, const DevConfig& cfg, cudaStream_t s,
-                            uint64_t* launches);
+// K4' (k_stage_jacobi): the stage heuristic over chunks of cycle slots with
+// Jacobi refinement; st[0] = c_stage (holding the local stages), st[1] a
+// scratch copy; *final_parity = index of the array with the result
+// (0xffffffff: no fixed point within max_iter).
+struct StageMeta {
+  uint8_t* st[2];
+  uint32_t n_chunks;
+  int32_t* changed_iter;      // per chunk, zero-initialised to -1
+  uint64_t* lookback_lo;      // per chunk
+  unsigned int* any_changed;  // [2], zeroed
+  unsigned int* bar_count;    // zeroed
+  unsigned int* bar_gen;
+  unsigned int* final_parity;
+  int max_iter;
+};
+constexpr uint32_t kStageChunkCycles = 256;
+int launch_stage_heuristic(const DevBuffers& b, const DevConfig& cfg, const StageMeta& m, cudaStream_t s,
+                           uint64_t* launches);
 void launch_records(const DevBuffers& b, const DevConfig& cfg, uint64_t n_blocks_cap,
                     cudaStream_t s, uint64_t* launches);
 void launch_score(const DevBuffers& b, const DevConfig& cfg, uint64_t n_records_total,

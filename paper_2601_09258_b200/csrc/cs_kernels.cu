@@ -782,117 +782,6 @@ __global__ void __launch_bounds__(256) k_bounds_tile(DevBuffers b) {
   }
 }
 
-// --------------------------------------------------- K4 stage heuristic
-// One warp per instance; only Unknown cycles are decided, in order
-// (cycles.cpp:230-250).  For each, the trailing windows (<= 32 most recent
-// non-Prefill durations; <= 32 most recent non-Prefill idle gaps >= 0) are
-// gathered by a backward ballot scan over already-final stages, and the
-// medians come from a 32-lane rank selection.
-__device__ double warp_median(double v, bool has, int n) {
-  // rank of each lane's value among valid lanes (stable on ties)
-  const int lane = threadIdx.x & 31;
-  int rank = 0;
-  for (int l = 0; l < 32; ++l) {
-    const double o = __shfl_sync(0xffffffffu, v, l);
-    const bool oh = __shfl_sync(0xffffffffu, has, l);
-    if (has && oh && (o < v || (o == v && l < lane))) ++rank;
-  }
-  const int want_hi = n / 2;
-  const uint32_t mhi = __ballot_sync(0xffffffffu, has && rank == want_hi);
-  const double hi = __shfl_sync(0xffffffffu, v, __ffs(mhi) - 1);
-  if (n % 2 == 1) return hi;
-  const uint32_t mlo = __ballot_sync(0xffffffffu, has && rank == want_hi - 1);
-  const double lo = __shfl_sync(0xffffffffu, v, __ffs(mlo) - 1);
-  return __dmul_rn(0.5, __dadd_rn(lo, hi));
-}
-
-__global__ void k_stage_heuristic(DevBuffers b, DevConfig cfg) {
-  const int lane = threadIdx.x & 31;
-  const uint32_t inst = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
-  if (inst >= b.n_inst) return;
-  if (b.inst[inst].n_unknown == 0) return;
-  const u64 c0 = b.cyc_off[inst], c1 = b.cyc_off[inst + 1];
-  const int W = (int)cfg.cyc.stage_window;
-  const u64 min_hist = cfg.cyc.stage_min_history;
-  const StreamCarry* sc = b.stream ? b.stream + inst : nullptr;
-  for (u64 base = c0; base < c1; base += 32) {
-    const u64 g = base + lane;
-    uint32_t um = __ballot_sync(0xffffffffu, g < c1 && b.c_local[g] == CS_STAGE_UNKNOWN);
-    while (um) {
-      const int l = __ffs(um) - 1;
-      um &= um - 1;
-      const u64 u = base + l;
-      const double gap = u > c0 ? (double)(b.c_start[u] - b.c_aend[u - 1])
-                         : (sc && sc->has_prev) ? (double)(b.c_start[u] - sc->last_aend) : -1.0;
-      uint8_t stage = CS_STAGE_UNKNOWN;
-      if (gap >= 0.0) {
-        // gather windows, most recent first
-        double dv = 0.0, gv = 0.0;
-        bool dh = false, gh = false;
-        int nd = 0, ng = 0;
-        for (i64 top = (i64)u - 1; top >= (i64)c0 && (nd < W || ng < W); top -= 32) {
-          const i64 j = top - lane;
-          const bool in = j >= (i64)c0;
-          bool nonp = false, gok = false;
-          double jd = 0.0, jg = -1.0;
-          if (in) {
-            nonp = b.c_stage[j] != CS_STAGE_PREFILL;
-            jd = (double)(b.c_end[j] - b.c_start[j]);
-            jg = j > (i64)c0 ? (double)(b.c_start[j] - b.c_aend[j - 1])
-                 : (sc && sc->has_prev) ? (double)(b.c_start[j] - sc->last_aend) : -1.0;
-            gok = nonp && jg >= 0.0;
-          }
-          const uint32_t md = __ballot_sync(0xffffffffu, in && nonp);
-          const uint32_t mg = __ballot_sync(0xffffffffu, in && gok);
-          // k-th collected value goes to lane (nd + k)
-          const int kd = __popc(md & lanemask_lt());
-          const int kg = __popc(mg & lanemask_lt());
-          for (int src = 0; src < 32; ++src) {
-            const double sd = __shfl_sync(0xffffffffu, jd, src);
-            const double sg = __shfl_sync(0xffffffffu, jg, src);
-            const int skd = __shfl_sync(0xffffffffu, kd, src);
-            const int skg = __shfl_sync(0xffffffffu, kg, src);
-            if ((md >> src) & 1u) {
-              const int slot = nd + skd;
-              if (slot < W && slot == lane) { dv = sd; dh = true; }
-            }
-            if ((mg >> src) & 1u) {
-              const int slot = ng + skg;
-              if (slot < W && slot == lane) { gv = sg; gh = true; }
-            }
-          }
-          nd = min(W, nd + __popc(md));
-          ng = min(W, ng + __popc(mg));
-        }
-        if (sc) {  // earlier micro-batches, most recent first
-          if (lane >= nd && lane < W && (uint32_t)(lane - nd) < sc->n_dur) {
-            dv = sc->dur_hist[lane - nd];
-            dh = true;
-          }
-          if (lane >= ng && lane < W && (uint32_t)(lane - ng) < sc->n_gap) {
-            gv = sc->gap_hist[lane - ng];
-            gh = true;
-          }
-          nd = min(W, nd + (int)sc->n_dur);
-          ng = min(W, ng + (int)sc->n_gap);
-        }
-        if ((u64)nd >= min_hist) {
-          const double med_dur = warp_median(dv, dh, nd);
-          double med_gap = ng > 0 ? warp_median(gv, gh, ng) : 0.0;
-          med_gap = 1.0 < med_gap ? med_gap : 1.0;
-          const double cdur = (double)(b.c_end[u] - b.c_start[u]);
-          const bool long_cycle = cdur > __dmul_rn(cfg.cyc.prefill_duration_factor, med_dur);
-          const bool long_gap = gap > __dmul_rn(cfg.cyc.prefill_gap_factor, med_gap);
-          stage = (long_cycle && long_gap) ? CS_STAGE_PREFILL : CS_STAGE_DECODE;
-        }
-      }
-      if (lane == 0) b.c_stage[u] = stage;
-      __syncwarp();
-      __threadfence_block();
-    }
-  }
-}
-
 // ------------------------------------------------------------ K5 records
 // record := cycle with (include_prefill || stage != Prefill) && workload ok
 // (cycles.cpp:372-383).  Global compaction in cycle order; instance i's
@@ -2522,11 +2411,256 @@ void launch_bounds(const DevBuffers& b, cudaStream_t s, uint64_t* launches) {
   ++*launches;
 }
 
-void launch_stage_heuristic(const DevBuffers& b, const DevConfig& cfg, cudaStream_t s,
-                            uint64_t* launches) {
-  if (!b.n_inst) return;
-  k_stage_heuristic<<<(b.n_inst + 3) / 4, 128, 0, s>>>(b, cfg);
+// ------------------------------------------- K4' parallel stage heuristic
+// classify_stages' trailing-window heuristic (cycles.cpp:190-254) in parallel.
+// The cycle slots are cut into chunks of kStageChunk; a warp runs the
+// reference's sequential loop over its chunk (windows = sorted arrays + FIFO
+// rings in shared memory, exact medians) after rebuilding the windows at the
+// chunk start from the stages of the cycles before it.  Those stages are
+// speculated (Unknown cycles count as non-Prefill, i.e. the local stage) and
+// refined by Jacobi iteration: iteration k reads the stages of iteration k-1
+// and recomputes only chunks whose look-back region changed Prefill-ness.
+// Stages depend only on earlier cycles, so iteration k makes at least the
+// first k chunks exact and the fixed point is the sequential result.  One
+// persistent grid, a grid barrier between iterations.
+constexpr int kStageChunk = 256;
+constexpr int kStageWarps = 4;
+
+struct Win {  // one trailing window in the warp's shared memory
+  double* sorted;
+  double* ring;
+  uint32_t n, head, cap;
+};
+
+__device__ __forceinline__ void win_insert(Win& w, double x) {
+  const int lane = threadIdx.x & 31;
+  uint32_t cnt = 0;
+  for (uint32_t i = lane; i < w.n; i += 32) cnt += w.sorted[i] <= x ? 1u : 0u;
+  for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+  const uint32_t p = cnt;
+  for (int64_t base = (int64_t)w.n - 1; base >= (int64_t)p; base -= 32) {
+    const int64_t idx = base - lane;
+    double v = 0.0;
+    if (idx >= (int64_t)p) v = w.sorted[idx];
+    __syncwarp();
+    if (idx >= (int64_t)p) w.sorted[idx + 1] = v;
+    __syncwarp();
+  }
+  if (lane == 0) w.sorted[p] = x;
+  __syncwarp();
+  ++w.n;
+}
+
+__device__ __forceinline__ void win_remove(Win& w, double y) {
+  const int lane = threadIdx.x & 31;
+  uint32_t q = w.n;
+  for (uint32_t base = 0; base < w.n && q == w.n; base += 32) {
+    const uint32_t i = base + lane;
+    const uint32_t m = __ballot_sync(0xffffffffu, i < w.n && w.sorted[i] == y);
+    if (m) q = base + __ffs(m) - 1;
+  }
+  for (uint32_t base = q; base + 1 < w.n; base += 32) {
+    const uint32_t idx = base + 1 + lane;
+    double v = 0.0;
+    if (idx < w.n) v = w.sorted[idx];
+    __syncwarp();
+    if (idx < w.n) w.sorted[idx - 1] = v;
+    __syncwarp();
+  }
+  --w.n;
+}
+
+// push_back + pop_front beyond the capacity (cycles.cpp:245-249)
+__device__ __forceinline__ void win_push(Win& w, double x) {
+  const int lane = threadIdx.x & 31;
+  if (w.n == w.cap) {
+    const double oldest = w.ring[w.head];
+    win_remove(w, oldest);
+    w.head = w.head + 1 == w.cap ? 0 : w.head + 1;
+  }
+  uint32_t tail = w.head + w.n;
+  if (tail >= w.cap) tail -= w.cap;
+  if (lane == 0) w.ring[tail] = x;
+  __syncwarp();
+  win_insert(w, x);
+}
+
+// median of the sorted window (cycles.cpp:181-186)
+__device__ __forceinline__ double win_median(const Win& w) {
+  const uint32_t n = w.n;
+  if (n % 2 == 1) return w.sorted[n / 2];
+  return __dmul_rn(0.5, __dadd_rn(w.sorted[n / 2 - 1], w.sorted[n / 2]));
+}
+
+__device__ __forceinline__ void grid_barrier(unsigned int* count, unsigned int* gen) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned int g = *(volatile unsigned int*)gen;
+    __threadfence();
+    if (atomicAdd(count, 1u) == gridDim.x - 1) {
+      *(volatile unsigned int*)count = 0;
+      __threadfence();
+      atomicAdd(gen, 1u);
+    } else {
+      while (*(volatile unsigned int*)gen == g) {
+      }
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(kStageWarps * 32)
+    k_stage_jacobi(DevBuffers b, DevConfig cfg, StageMeta m) {
+  extern __shared__ __align__(16) double s_win[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t W = (uint32_t)cfg.cyc.stage_window;
+  const u64 min_hist = cfg.cyc.stage_min_history;
+  double* mine = s_win + (u64)warp * 4 * W;
+  const uint32_t gw = blockIdx.x * kStageWarps + warp, nw = gridDim.x * kStageWarps;
+  for (int it = 0; it < m.max_iter; ++it) {
+    const uint8_t* in = m.st[it & 1];
+    uint8_t* out = m.st[(it + 1) & 1];
+    for (uint32_t c = gw; c < m.n_chunks; c += nw) {
+      const u64 lo = (u64)c * kStageChunk;
+      const u64 hi = min(lo + (u64)kStageChunk, (u64)b.n_cycles);
+      // chunks of instances without Unknown cycles keep their local stages
+      bool any_unknown = false;
+      for (uint32_t i = b.c_inst[lo]; i <= b.c_inst[hi - 1] && !any_unknown; ++i)
+        any_unknown = b.inst[i].n_unknown != 0;
+      // recompute only when something before the chunk changed last iteration
+      bool dirty = it == 0 && any_unknown;
+      if (!dirty && it > 0 && any_unknown) {
+        const u64 lb = __ldcg(&m.lookback_lo[c]);
+        for (u64 cc = lb / kStageChunk; cc < c && !dirty; ++cc)
+          dirty = __ldcg(&m.changed_iter[cc]) == it - 1;
+      }
+      if (!dirty) {  // carry the values over into this iteration's array
+        for (u64 u = lo + lane; u < hi; u += 32) out[u] = __ldcg(&in[u]);
+        continue;
+      }
+      bool changed = false;
+      uint32_t cur_inst = 0xffffffffu;
+      Win dw{mine, mine + W, 0, 0, W}, gwin{mine + 2 * W, mine + 3 * W, 0, 0, W};
+      u64 c0 = 0;
+      const StreamCarry* sc = nullptr;
+      u64 lb_lo = lo;
+      for (u64 u = lo; u < hi; ++u) {
+        const uint8_t local = b.c_local[u];
+        if (local == 3) {  // hole slot of the single-read pass: not a cycle
+          if (lane == 0) out[u] = local;
+          continue;
+        }
+        const uint32_t inst = b.c_inst[u];
+        if (inst != cur_inst) {
+          // (re)build the windows from the cycles before u in its instance
+          cur_inst = inst;
+          c0 = b.cyc_off[inst];
+          sc = b.stream ? b.stream + inst : nullptr;
+          dw.n = dw.head = gwin.n = gwin.head = 0;
+          // collect most recent first in the rings' upper halves, then insert oldest first
+          uint32_t nd = 0, ng = 0;
+          i64 top = (i64)u - 1;
+          for (; top >= (i64)c0 && (nd < W || ng < W); top -= 32) {
+            const i64 j = top - lane;
+            const bool inr = j >= (i64)c0;
+            bool nonp = false, gok = false;
+            double jd = 0.0, jg = -1.0;
+            if (inr && b.c_local[j] != 3) {
+              nonp = __ldcg(&in[j]) != CS_STAGE_PREFILL;
+              jd = (double)(b.c_end[j] - b.c_start[j]);
+              jg = j > (i64)c0 ? (double)(b.c_start[j] - b.c_aend[j - 1])
+                   : (sc && sc->has_prev) ? (double)(b.c_start[j] - sc->last_aend) : -1.0;
+              gok = nonp && jg >= 0.0;
+            }
+            const uint32_t md = __ballot_sync(0xffffffffu, inr && nonp);
+            const uint32_t mg = __ballot_sync(0xffffffffu, inr && gok);
+            const uint32_t kd = nd + __popc(md & lanemask_lt());
+            const uint32_t kg = ng + __popc(mg & lanemask_lt());
+            if (inr && nonp && kd < W) dw.sorted[kd] = jd;  // staging: most recent first
+            if (inr && gok && kg < W) gwin.sorted[kg] = jg;
+            nd = min(W, nd + __popc(md));
+            ng = min(W, ng + __popc(mg));
+            if (u == lo) lb_lo = (u64)max((i64)c0, top - 31);
+          }
+          if (u == lo && top < (i64)c0) lb_lo = c0;
+          __syncwarp();
+          // earlier micro-batches (streaming carry), most recent first
+          if (sc) {
+            for (uint32_t k = lane; k < sc->n_dur && nd + k < W; k += 32) dw.sorted[nd + k] = sc->dur_hist[k];
+            for (uint32_t k = lane; k < sc->n_gap && ng + k < W; k += 32) gwin.sorted[ng + k] = sc->gap_hist[k];
+            nd = min(W, nd + sc->n_dur);
+            ng = min(W, ng + sc->n_gap);
+          }
+          __syncwarp();
+          // oldest first into the rings, then sort
+          for (uint32_t k = lane; k < nd; k += 32) dw.ring[k] = dw.sorted[nd - 1 - k];
+          for (uint32_t k = lane; k < ng; k += 32) gwin.ring[k] = gwin.sorted[ng - 1 - k];
+          __syncwarp();
+          for (uint32_t k = 0; k < nd; ++k) win_insert(dw, dw.ring[k]);
+          for (uint32_t k = 0; k < ng; ++k) win_insert(gwin, gwin.ring[k]);
+          dw.head = 0;
+          gwin.head = 0;
+        }
+        const double gap = u > c0 ? (double)(b.c_start[u] - b.c_aend[u - 1])
+                           : (sc && sc->has_prev) ? (double)(b.c_start[u] - sc->last_aend) : -1.0;
+        uint8_t stage = local;
+        if (stage == CS_STAGE_UNKNOWN && (u64)dw.n >= min_hist && gap >= 0.0) {
+          const double med_dur = win_median(dw);
+          double med_gap = gwin.n ? win_median(gwin) : 0.0;
+          med_gap = 1.0 < med_gap ? med_gap : 1.0;
+          const double cdur = (double)(b.c_end[u] - b.c_start[u]);
+          const bool long_cycle = cdur > __dmul_rn(cfg.cyc.prefill_duration_factor, med_dur);
+          const bool long_gap = gap > __dmul_rn(cfg.cyc.prefill_gap_factor, med_gap);
+          stage = (long_cycle && long_gap) ? CS_STAGE_PREFILL : CS_STAGE_DECODE;
+        }
+        changed |= (stage == CS_STAGE_PREFILL) != (__ldcg(&in[u]) == CS_STAGE_PREFILL);
+        if (lane == 0) out[u] = stage;
+        if (stage != CS_STAGE_PREFILL) {
+          win_push(dw, (double)(b.c_end[u] - b.c_start[u]));
+          if (gap >= 0.0) win_push(gwin, gap);
+        }
+      }
+      if (lane == 0) {
+        m.lookback_lo[c] = lb_lo;
+        if (changed) {
+          m.changed_iter[c] = it;
+          atomicOr(m.any_changed + (it & 1), 1u);
+        }
+      }
+    }
+    grid_barrier(m.bar_count, m.bar_gen);
+    const bool more = __ldcg(m.any_changed + (it & 1)) != 0;
+    grid_barrier(m.bar_count, m.bar_gen);  // everyone has read the flag
+    if (blockIdx.x == 0 && threadIdx.x == 0) m.any_changed[it & 1] = 0;
+    if (!more) {
+      if ((it + 1) & 1)  // the result is in the scratch array: back into c_stage
+        for (u64 u = (u64)blockIdx.x * blockDim.x + threadIdx.x; u < b.n_cycles; u += (u64)gridDim.x * blockDim.x)
+          m.st[0][u] = __ldcg(&m.st[1][u]);
+      if (blockIdx.x == 0 && threadIdx.x == 0) *m.final_parity = 0;
+      return;
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) *m.final_parity = 0xffffffffu;  // did not converge
+}
+
+int launch_stage_heuristic(const DevBuffers& b, const DevConfig& cfg, const StageMeta& m, cudaStream_t s,
+                           uint64_t* launches) {
+  if (!b.n_cycles || m.n_chunks == 0) return 0;
+  const size_t smem = (size_t)kStageWarps * 4 * cfg.cyc.stage_window * sizeof(double);
+  if (smem > 200 * 1024) return -1;
+  cudaFuncSetAttribute(k_stage_jacobi, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int dev = 0, n_sm = 148, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_stage_jacobi, kStageWarps * 32, smem);
+  if (per_sm < 1) per_sm = 1;
+  uint64_t grid = (uint64_t)n_sm * per_sm;  // persistent: every CTA resident (grid barrier)
+  const uint64_t need = (m.n_chunks + kStageWarps - 1) / kStageWarps;
+  if (grid > need) grid = need;
+  k_stage_jacobi<<<(unsigned)grid, kStageWarps * 32, smem, s>>>(b, cfg, m);
   ++*launches;
+  return 0;
 }
 
 void launch_records(const DevBuffers& b, const DevConfig& cfg, uint64_t, cudaStream_t s,
