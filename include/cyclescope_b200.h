@@ -151,9 +151,12 @@ typedef struct cs_control_config { /* ControlConfig detector.hpp:25-34 */
   double epsilon;          /* 1e-9 */
 } cs_control_config;
 
-/* Feature ids a model may request (main.cpp:59-78 features_by_name). */
+/* Feature ids a model may request (main.cpp:59-78 features_by_name).  Any
+ * other feature name is a record `extra` (the post_* args of the Full feature
+ * set, cycles.cpp:392-405 / baseline.cpp:43-76), resolved by name against the
+ * extras keys of the uploaded trace (cs_upload_extras) when a run scores. */
 enum cs_feature { CS_F_BATCH = 0, CS_F_W_KV = 1, CS_F_INPUT_LEN = 2,
-                  CS_F_OUTPUT_LEN = 3, CS_F_STAGE = 4 };
+                  CS_F_OUTPUT_LEN = 3, CS_F_STAGE = 4, CS_F_EXTRA = -1 };
 
 /* Flattened GbdtModel (gbdt.hpp:33-84) + LatencyModel stats (baseline.hpp:50-67).
  * Trees are concatenated node arrays; tree t owns nodes
@@ -180,6 +183,8 @@ typedef struct cs_model {
   double sigma_train;
   int32_t degenerate;
   int32_t reserved;
+  const char* const* feature_names; /* n_features names (NULL: ids only); needed
+                                       for CS_F_EXTRA features */
 } cs_model;
 
 /* ------------------------------------------------------------- outputs */
@@ -248,7 +253,9 @@ typedef struct cs_instance_summary {
   uint64_t n_cycles;
   uint64_t n_records;
   uint64_t n_alerts;
-  uint64_t first_bad_record; /* record whose latency <= 0 (UINT64_MAX none) */
+  uint64_t first_bad_record; /* first record where monitor_loop stops: latency
+                                <= 0 (NonPositiveLatency) or a model feature the
+                                record lacks (FeatureMismatch); UINT64_MAX none */
   double ucl;                /* detector limit in force                   */
   int32_t used_frequency_fallback;
   int32_t anchor_ambiguous;  /* exact-stat ranking needed the ordered fold */
@@ -482,6 +489,30 @@ int cs_ingest_topology(const cs_ingest_result* r, const int32_t** comm_location,
 int cs_ingest_report(const cs_ingest_result* r, const cs_ingest_issue** issues, uint64_t* n_issues,
                      uint64_t* n_parse_issues, uint64_t category_counts[8], uint64_t* n_errors);
 
+/* Record extras (PipelineOptions::extra_args_prefix, cycles.cpp:392-405): the
+ * numeric args with the prefix ("post_" by default) of the uploaded events, as
+ * a side table sorted by event: refs[k] = {canonical event index (batch-wide),
+ * first value, count}, values = {key id, value} with key ids into the n_keys
+ * keys (lexicographic order, `keys` NUL-separated).  A record's extra[key] is
+ * the value of the LAST event of its cycle carrying the key (map assignment in
+ * event order).  Call after the events' upload (an upload clears the table). */
+typedef struct cs_extra_ref {
+  uint64_t event;
+  uint32_t first;
+  uint32_t count;
+} cs_extra_ref;
+typedef struct cs_extra_value {
+  uint32_t key;
+  uint32_t reserved;
+  double value;
+} cs_extra_value;
+int cs_upload_extras(cs_ctx* ctx, uint32_t n_keys, const char* keys, const cs_extra_ref* refs,
+                     uint64_t n_refs, const cs_extra_value* values, uint64_t n_values);
+/* The records' extras of the last run: n_records x n_keys values and presence
+ * bytes (present == 0: the record's cycle has no event with that key). */
+int cs_get_record_extras(cs_ctx* ctx, uint32_t inst, double* values, uint8_t* present, size_t cap,
+                         size_t* n);
+
 /* Latency model for instance `inst` (UINT32_MAX = default for every instance
  * without its own binding).  Bindings are by instance index, may precede the
  * first cs_upload and survive re-uploads (streams).
@@ -708,6 +739,12 @@ int cs_fit_latency_model(uint64_t n, uint32_t n_features, const int32_t* feature
                          const double* x, const double* y,
                          const cs_gbdt_params* params, const cs_fit_options* opt,
                          cs_fitted_model** out, char* err, size_t err_cap);
+/* The same fit with feature NAMES (the Full feature set's extras columns,
+ * to_sample_set baseline.cpp:43-78): names are stored in the model as given. */
+int cs_fit_latency_model_named(uint64_t n, uint32_t n_features, const char* const* feature_names,
+                               const double* x, const double* y, const cs_gbdt_params* params,
+                               const cs_fit_options* opt, cs_fitted_model** out, char* err,
+                               size_t err_cap);
 /* Batched fit_latency_model on the device: n_models
  * independent sample sets (model m: rows [offsets[m], offsets[m+1]) of x / y,
  * x row-major), each fitted exactly as cs_fit_latency_model would (the model

@@ -52,6 +52,11 @@ struct Exported {
   std::vector<int32_t> comm_name, comm_rank;
   std::string comm_hash_packed;
   std::vector<uint64_t> event_ids;
+  // record extras side table (cycles.cpp:392-405): prefixed numeric args
+  std::vector<std::string> extra_keys;
+  std::string extra_keys_packed;
+  std::vector<cs_extra_ref> extra_refs;
+  std::vector<cs_extra_value> extra_vals;
 };
 
 struct Results {
@@ -70,6 +75,9 @@ struct Results {
   std::vector<uint8_t> coll_present;
   std::vector<cs_record> records;
   std::vector<cs_alert> alerts;
+  std::vector<std::string> rec_extra_keys;  // sorted union of the records' extra keys
+  std::vector<double> rec_extra;            // n_records x keys
+  std::vector<uint8_t> rec_extra_has;
   std::string model_json;
   std::string ndjson;
   double ucl = 0.0;
@@ -98,7 +106,7 @@ int stage_code(Stage s) {
 
 // The oracle-side ingest: Trace -> 32-byte records.  Written independently of
 // the product's ingest; the shared contract is include/cyclescope_b200.h.
-void export_trace(Handle& h, const CycleConfig& cfg) {
+void export_trace(Handle& h, const CycleConfig& cfg, const std::string& extra_prefix = "post_") {
   Exported& ex = h.ex;
   ex = Exported{};
   const auto& ev = h.ds.trace.events;
@@ -175,6 +183,34 @@ void export_trace(Handle& h, const CycleConfig& cfg) {
     }
     r.flags = flags;
     ex.event_ids[i] = e.event_id;
+  }
+  // extras: every numeric arg with the prefix, per event in key order
+  if (!extra_prefix.empty()) {
+    std::set<std::string> keys;
+    for (const auto& e : ev)
+      for (const auto& [k, v] : e.args)
+        if (k.rfind(extra_prefix, 0) == 0 && !std::holds_alternative<std::string>(v)) keys.insert(k);
+    ex.extra_keys.assign(keys.begin(), keys.end());
+    for (const auto& k : ex.extra_keys) {
+      ex.extra_keys_packed += k;
+      ex.extra_keys_packed.push_back('\0');
+    }
+    for (size_t i = 0; i < ev.size(); ++i) {
+      cs_extra_ref ref{i, static_cast<uint32_t>(ex.extra_vals.size()), 0};
+      for (const auto& [k, v] : ev[i].args) {
+        if (k.rfind(extra_prefix, 0) != 0) continue;
+        double d;
+        if (const auto* x = std::get_if<double>(&v)) d = *x;
+        else if (const auto* n = std::get_if<std::int64_t>(&v)) d = static_cast<double>(*n);
+        else if (const auto* b = std::get_if<bool>(&v)) d = *b ? 1.0 : 0.0;
+        else continue;
+        const uint32_t key = static_cast<uint32_t>(
+            std::lower_bound(ex.extra_keys.begin(), ex.extra_keys.end(), k) - ex.extra_keys.begin());
+        ex.extra_vals.push_back({key, 0, d});
+        ++ref.count;
+      }
+      if (ref.count) ex.extra_refs.push_back(ref);
+    }
   }
   h.exported = true;
 }
@@ -308,6 +344,22 @@ void run_reference(Handle& h, const RunConfig& config, const char* model_json,
     set_error(R, e);
     return;
   }
+  {  // the records' extras (post_* args), columns in key order
+    std::set<std::string> keys;
+    for (const auto& r : records)
+      for (const auto& [k, v] : r.extra) keys.insert(k);
+    R.rec_extra_keys.assign(keys.begin(), keys.end());
+    const size_t K = R.rec_extra_keys.size();
+    R.rec_extra.assign(records.size() * K, 0.0);
+    R.rec_extra_has.assign(records.size() * K, 0);
+    for (size_t i = 0; i < records.size(); ++i)
+      for (const auto& [k, v] : records[i].extra) {
+        const size_t c = std::lower_bound(R.rec_extra_keys.begin(), R.rec_extra_keys.end(), k) -
+                         R.rec_extra_keys.begin();
+        R.rec_extra[i * K + c] = v;
+        R.rec_extra_has[i * K + c] = 1;
+      }
+  }
   LatencyModel model;
   try {
     if (model_json && *model_json) {
@@ -347,7 +399,14 @@ void run_reference(Handle& h, const RunConfig& config, const char* model_json,
         else if (name == "input_len") row.push_back(static_cast<double>(rec.workload.input_len));
         else if (name == "output_len") row.push_back(static_cast<double>(rec.workload.output_len));
         else if (name == "stage") row.push_back(rec.stage == Stage::Prefill ? 1.0 : 0.0);
-        else throw FeatureMismatch("input lacks feature '" + name + "'");
+        else {  // features_by_name (main.cpp:70-75)
+          auto it = rec.extra.find(name);
+          if (it == rec.extra.end()) {
+            R.first_bad_record = i;
+            throw FeatureMismatch("input lacks feature '" + name + "'");
+          }
+          row.push_back(it->second);
+        }
       }
       o.predicted_s = model.predict(row);
       R.records.push_back(o);
@@ -666,7 +725,7 @@ int ref_export(void* hv, const char* run_config_json) {
     RunConfig cfg = (run_config_json && *run_config_json)
                         ? RunConfig::from_json(json::parse(run_config_json))
                         : RunConfig{};
-    export_trace(*h, cfg.cycle);
+    export_trace(*h, cfg.cycle, cfg.pipeline.extra_args_prefix);
   } catch (const std::exception&) {
     return 1;
   }
@@ -681,6 +740,35 @@ int ref_get_event_ids(void* hv, uint64_t* buf, size_t cap, size_t* n) {
 }
 int ref_get_workloads(void* hv, cs_workload* buf, size_t cap, size_t* n) {
   return copy_out(static_cast<Handle*>(hv)->ex.workloads, buf, cap, n);
+}
+int ref_get_extra_keys(void* hv, char* buf, size_t cap, size_t* n_bytes, uint32_t* n_keys) {
+  auto* h = static_cast<Handle*>(hv);
+  if (n_keys) *n_keys = static_cast<uint32_t>(h->ex.extra_keys.size());
+  std::vector<char> v(h->ex.extra_keys_packed.begin(), h->ex.extra_keys_packed.end());
+  return copy_out(v, buf, cap, n_bytes);
+}
+int ref_get_extra_refs(void* hv, cs_extra_ref* buf, size_t cap, size_t* n) {
+  return copy_out(static_cast<Handle*>(hv)->ex.extra_refs, buf, cap, n);
+}
+int ref_get_extra_values(void* hv, cs_extra_value* buf, size_t cap, size_t* n) {
+  return copy_out(static_cast<Handle*>(hv)->ex.extra_vals, buf, cap, n);
+}
+int ref_get_record_extras(void* hv, char* keys, size_t keys_cap, size_t* keys_bytes, double* vals,
+                          uint8_t* has, size_t cap, size_t* n) {
+  auto* h = static_cast<Handle*>(hv);
+  std::string packed;
+  for (const auto& k : h->res.rec_extra_keys) {
+    packed += k;
+    packed.push_back('\0');
+  }
+  std::vector<char> kv(packed.begin(), packed.end());
+  if (copy_out(kv, keys, keys_cap, keys_bytes)) return 1;
+  if (n) *n = h->res.rec_extra.size();
+  if (!vals) return 0;
+  if (cap < h->res.rec_extra.size()) return 1;
+  std::copy(h->res.rec_extra.begin(), h->res.rec_extra.end(), vals);
+  std::copy(h->res.rec_extra_has.begin(), h->res.rec_extra_has.end(), has);
+  return 0;
 }
 int ref_get_names(void* hv, char* buf, size_t cap, size_t* n_bytes, uint32_t* n_names) {
   auto* h = static_cast<Handle*>(hv);

@@ -68,6 +68,10 @@ def lib():
                    "ref_get_ndjson"):
             getattr(L, fn).argtypes = [vp, vp, sz, C.POINTER(sz)]
         L.ref_get_names.argtypes = [vp, vp, sz, C.POINTER(sz), C.POINTER(C.c_uint32)]
+        L.ref_get_extra_keys.argtypes = [vp, vp, sz, C.POINTER(sz), C.POINTER(C.c_uint32)]
+        L.ref_get_extra_refs.argtypes = [vp, vp, sz, C.POINTER(sz)]
+        L.ref_get_extra_values.argtypes = [vp, vp, sz, C.POINTER(sz)]
+        L.ref_get_record_extras.argtypes = [vp, vp, sz, C.POINTER(sz), vp, vp, sz, C.POINTER(sz)]
         L.ref_get_comm.argtypes = [vp, vp, vp, vp, sz, C.POINTER(sz), C.POINTER(C.c_uint32)]
         L.ref_get_beta.argtypes = [vp, vp, vp, sz, C.POINTER(sz)]
         L.ref_get_collective_beta.argtypes = [vp, vp, vp, sz, C.POINTER(sz)]
@@ -118,6 +122,9 @@ class Exported:
     comm_name: np.ndarray
     comm_rank: np.ndarray
     comm_hash: list
+    extra_keys: list = field(default_factory=list)
+    extra_refs: np.ndarray = None
+    extra_values: np.ndarray = None
 
 
 @dataclass
@@ -284,8 +291,15 @@ class RefTrace:
         L.ref_get_comm(self.h, cn.ctypes.data, cr.ctypes.data, cbuf, cb.value, C.byref(cb),
                        C.byref(nc))
         hashes = cbuf.raw[:cb.value].split(b"\0")[:nc.value]
+        kb, nk = C.c_size_t(0), C.c_uint32(0)
+        L.ref_get_extra_keys(self.h, None, 0, C.byref(kb), C.byref(nk))
+        kbuf = C.create_string_buffer(kb.value + 1)
+        L.ref_get_extra_keys(self.h, kbuf, kb.value, C.byref(kb), C.byref(nk))
+        keys = [k.decode() for k in kbuf.raw[:kb.value].split(b"\0")[:nk.value]]
         return Exported(ev, ids, wl, [n.decode() for n in names], cn, cr,
-                        [h.decode() for h in hashes])
+                        [h.decode() for h in hashes], keys,
+                        _get(L.ref_get_extra_refs, self.h, abi.EXTRA_REF_DTYPE),
+                        _get(L.ref_get_extra_values, self.h, abi.EXTRA_VALUE_DTYPE))
 
     def run(self, run_config: dict | None = None, model_json: str | None = None,
             train_cycles: int = 2400, beta: bool = True, mu: bool = False) -> RefResult:
@@ -315,6 +329,14 @@ class RefTrace:
         mu_h = np.zeros(n.value, np.uint8)
         if n.value:
             L.ref_get_mu(self.h, mu_v.ctypes.data, mu_h.ctypes.data, n.value, C.byref(n))
+        kb, nx = C.c_size_t(0), C.c_size_t(0)
+        L.ref_get_record_extras(self.h, None, 0, C.byref(kb), None, None, 0, C.byref(nx))
+        kbuf = C.create_string_buffer(kb.value + 1)
+        rx = np.zeros(nx.value, np.float64)
+        rh = np.zeros(nx.value, np.uint8)
+        L.ref_get_record_extras(self.h, kbuf, kb.value, C.byref(kb), rx.ctypes.data, rh.ctypes.data, nx.value,
+                                C.byref(nx))
+        rkeys = [k.decode() for k in kbuf.raw[:kb.value].split(b"\0") if k]
         mj = _get(L.ref_get_model_json, self.h, np.uint8)
         nd = _get(L.ref_get_ndjson, self.h, np.uint8)
         return RefResult(
@@ -330,7 +352,9 @@ class RefTrace:
             ucl=L.ref_ucl(self.h), first_bad_record=int(L.ref_first_bad_record(self.h)),
             seconds=L.ref_seconds(self.h),
             extra={"ndjson": bytes(nd[:-1]).decode() if len(nd) else "", "mu": mu_v,
-                   "mu_has": mu_h})
+                   "mu_has": mu_h, "rec_extra_keys": rkeys,
+                   "rec_extra": rx.reshape(-1, len(rkeys)) if rkeys else rx.reshape(0, 0),
+                   "rec_extra_has": rh.reshape(-1, len(rkeys)) if rkeys else rh.reshape(0, 0)})
 
 
 def ref_fit(x: np.ndarray, y: np.ndarray, feature_names, params=None, options=None) -> str:

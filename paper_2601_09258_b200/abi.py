@@ -33,6 +33,8 @@ WIRE_BLOCK_DTYPE = np.dtype([("base_ts", "<i8"), ("dur", "<u8"), ("pay8", "<u8")
 assert WIRE_BLOCK_DTYPE.itemsize == 64
 
 WORKLOAD_DTYPE = np.dtype([("batch", "<i8"), ("input_len", "<i8"), ("output_len", "<i8")])
+EXTRA_REF_DTYPE = np.dtype([("event", "<u8"), ("first", "<u4"), ("count", "<u4")])
+EXTRA_VALUE_DTYPE = np.dtype([("key", "<u4"), ("reserved", "<u4"), ("value", "<f8")])
 NAME_INFO_DTYPE = np.dtype(
     [("flags", "<u4"), ("phase", "<i4"), ("beta_slot", "<i4"), ("metric", "<u4")])
 
@@ -113,7 +115,7 @@ class Model(C.Structure):
                 ("nodes", C.c_void_p), ("base", C.c_double), ("learning_rate", C.c_double),
                 ("prediction_floor", C.c_double), ("mu_train", C.c_double),
                 ("sigma_train", C.c_double), ("degenerate", C.c_int32),
-                ("reserved", C.c_int32)]
+                ("reserved", C.c_int32), ("feature_names", C.POINTER(C.c_char_p))]
 
 
 class InstanceSummary(C.Structure):

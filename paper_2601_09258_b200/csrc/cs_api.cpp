@@ -120,7 +120,8 @@ struct DevBuf {
 
 struct PackedModel {
   uint32_t n_trees = 0, depth = 0, n_features = 0, degenerate = 0;
-  std::vector<int32_t> feature_ids;
+  std::vector<int32_t> feature_ids;  // CS_F_* or CS_F_EXTRA (resolved by name per run)
+  std::vector<std::string> feature_names;
   std::vector<double> thr, leaf;   // leaf holds fl(lr * value)
   std::vector<int64_t> thr_i;       // floor(thr) for exact integer compares
   std::vector<uint8_t> feat;
@@ -162,6 +163,10 @@ struct cs_ctx {
   std::vector<uint64_t> tile_begin, tile_end;
   DevBuf d_tile_inst, d_tile_begin, d_tile_end, d_inst_first_tile, d_tile_cnt, d_tile_pref;
   DevBuf d_scan_tmp;
+  // record extras (cs_upload_extras)
+  std::vector<std::string> extra_keys;
+  uint64_t n_extra_refs = 0;
+  DevBuf d_extra_refs, d_extra_vals, d_rec_extra, d_rec_extra_has;
   DevBuf d_stage2, d_stage_changed, d_stage_lb, d_stage_ctl;  // k_stage_jacobi
   // counter-weighted mu: metric slots derived from the name table
   uint32_t n_metrics = 0;
@@ -355,6 +360,12 @@ DevBuffers make_buffers(cs_ctx* ctx) {
   b.c_mu = static_cast<double*>(ctx->d_mu.p);
   b.c_mu_has = static_cast<uint8_t*>(ctx->d_mu_has.p);
   b.stream = ctx->streaming ? static_cast<StreamCarry*>(ctx->d_stream[ctx->stream_cur].p) : nullptr;
+  b.extra_refs = static_cast<const cs_extra_ref*>(ctx->d_extra_refs.p);
+  b.n_extra_refs = ctx->n_extra_refs;
+  b.extra_vals = static_cast<const cs_extra_value*>(ctx->d_extra_vals.p);
+  b.n_extra_keys = static_cast<uint32_t>(ctx->extra_keys.size());
+  b.rec_extra = static_cast<double*>(ctx->d_rec_extra.p);
+  b.rec_extra_has = static_cast<uint8_t*>(ctx->d_rec_extra_has.p);
   return b;
 }
 
@@ -597,6 +608,9 @@ int upload_layout(cs_ctx* ctx, uint32_t n_inst, const uint64_t* inst_offsets, bo
   CS_CUDA(cudaMemcpyAsync(dft, ctx->inst_first_tile.data(), n_inst * 4, cudaMemcpyHostToDevice,
                           ctx->stream));
   ctx->ranges_built_for = 0;  // k_segment_range ranges are rebuilt by the next fused run
+  if (!ctx->extra_keys.empty()) ctx->mt_valid = false;  // extras resolve per upload
+  ctx->extra_keys.clear();
+  ctx->n_extra_refs = 0;
   // bindings are by instance index and survive re-uploads (streaming pushes)
   if (ctx->model_of_inst.size() < n_inst) ctx->model_of_inst.resize(n_inst, -1);
   ctx->ran = false;
@@ -670,6 +684,57 @@ int cs_get_order(cs_ctx* ctx, uint32_t inst, uint64_t* buf, size_t cap, size_t* 
     CS_CUDA(cudaMemcpyAsync(buf, static_cast<const uint64_t*>(ctx->d_order.p) + b, m * 8,
                             cudaMemcpyDeviceToHost, ctx->stream));
   CS_CUDA(cudaStreamSynchronize(ctx->stream));
+  return CS_OK;
+}
+
+int cs_upload_extras(cs_ctx* ctx, uint32_t n_keys, const char* keys, const cs_extra_ref* refs,
+                     uint64_t n_refs, const cs_extra_value* values, uint64_t n_values) {
+  if (!ctx || (n_keys && !keys) || (n_refs && !refs) || (n_values && !values)) return CS_E_INVALID_ARGUMENT;
+  std::vector<std::string> k;
+  const char* p = keys;
+  for (uint32_t i = 0; i < n_keys; ++i) {
+    k.emplace_back(p);
+    p += k.back().size() + 1;
+    if (i && !(k[i - 1] < k[i])) return fail(ctx, CS_E_INVALID_ARGUMENT, "extras keys must be sorted and distinct");
+  }
+  for (uint64_t r = 0; r < n_refs; ++r) {
+    if (refs[r].event >= ctx->n_ev || (r && refs[r].event <= refs[r - 1].event))
+      return fail(ctx, CS_E_INVALID_ARGUMENT, "extras refs must be sorted by event and inside the upload");
+    if (static_cast<uint64_t>(refs[r].first) + refs[r].count > n_values)
+      return fail(ctx, CS_E_INVALID_ARGUMENT, "extras ref out of range");
+  }
+  for (uint64_t v = 0; v < n_values; ++v)
+    if (values[v].key >= n_keys) return fail(ctx, CS_E_INVALID_ARGUMENT, "extras key id out of range");
+  CS_CUDA(cudaSetDevice(ctx->device));
+  void* dr = ctx->d_extra_refs.get(std::max<uint64_t>(1, n_refs) * sizeof(cs_extra_ref));
+  void* dv = ctx->d_extra_vals.get(std::max<uint64_t>(1, n_values) * sizeof(cs_extra_value));
+  if (!dr || !dv) return fail(ctx, CS_E_CUDA, "cudaMalloc(extras)");
+  if (n_refs) CS_CUDA(cudaMemcpyAsync(dr, refs, n_refs * sizeof(cs_extra_ref), cudaMemcpyHostToDevice, ctx->stream));
+  if (n_values)
+    CS_CUDA(cudaMemcpyAsync(dv, values, n_values * sizeof(cs_extra_value), cudaMemcpyHostToDevice, ctx->stream));
+  CS_CUDA(cudaStreamSynchronize(ctx->stream));
+  ctx->extra_keys = std::move(k);
+  ctx->n_extra_refs = n_refs;
+  ctx->mt_valid = false;  // model extras resolve against these keys
+  return CS_OK;
+}
+
+int cs_get_record_extras(cs_ctx* ctx, uint32_t inst, double* values, uint8_t* present, size_t cap,
+                         size_t* n) {
+  if (!ctx || !ctx->ran || inst >= ctx->n_inst) return CS_E_INVALID_ARGUMENT;
+  const uint64_t K = ctx->extra_keys.size();
+  const uint64_t r0 = ctx->rec_off[inst], nr = ctx->rec_off[inst + 1] - r0;
+  if (n) *n = nr * K;
+  if (!values && !present) return CS_OK;
+  if (cap < nr * K) return fail(ctx, CS_E_INVALID_ARGUMENT, "buffer too small");
+  if (nr * K != 0) {
+    if (values)
+      CS_CUDA(cudaMemcpy(values, static_cast<const double*>(ctx->d_rec_extra.p) + r0 * K, nr * K * 8,
+                         cudaMemcpyDeviceToHost));
+    if (present)
+      CS_CUDA(cudaMemcpy(present, static_cast<const uint8_t*>(ctx->d_rec_extra_has.p) + r0 * K, nr * K,
+                         cudaMemcpyDeviceToHost));
+  }
   return CS_OK;
 }
 
@@ -786,12 +851,19 @@ static int cs_load_model_impl(cs_ctx* ctx, uint32_t inst, const cs_model* m) {
   pm->sigma = m->sigma_train;
   for (uint32_t f = 0; f < m->n_features; ++f) {
     const int32_t id = m->feature_ids[f];
+    const char* nm = m->feature_names ? m->feature_names[f] : nullptr;
     if (id < CS_F_BATCH || id > CS_F_STAGE) {
-      delete pm;
-      return fail(ctx, CS_E_FEATURE_MISMATCH,
-                  "model feature is not one of batch/w_kv/input_len/output_len/stage");
+      // a record extra (main.cpp:70-75), resolved by name when a run scores
+      if (!nm || !*nm) {
+        delete pm;
+        return fail(ctx, CS_E_FEATURE_MISMATCH,
+                    "model feature is not one of batch/w_kv/input_len/output_len/stage and has no name");
+      }
+      pm->feature_ids.push_back(CS_F_EXTRA);
+    } else {
+      pm->feature_ids.push_back(id);
     }
-    pm->feature_ids.push_back(id);
+    pm->feature_names.push_back(nm ? nm : "");
   }
   int D = 0;
   for (uint32_t t = 0; t < m->n_trees; ++t) {
@@ -810,9 +882,11 @@ static int cs_load_model_impl(cs_ctx* ctx, uint32_t inst, const cs_model* m) {
     }
     D = std::max(D, dmax);
   }
-  if (D > kMaxTreeDepth) {
+  // complete-tree layout (2^D - 1 internal + 2^D leaves per tree) in HBM
+  const double layout_bytes = static_cast<double>(m->n_trees) * std::ldexp(1.0, D) * 25.0;
+  if (D > kMaxTreeDepth || layout_bytes > 4e9) {
     delete pm;
-    return fail(ctx, CS_E_UNSUPPORTED, "tree depth > 8 is not supported on device");
+    return fail(ctx, CS_E_UNSUPPORTED, "tree too deep for the complete-tree device layout");
   }
   pm->depth = static_cast<uint32_t>(D);
   const uint32_t ni = (1u << D) - 1, nl = 1u << D;
@@ -1078,6 +1152,7 @@ static int cs_run_impl(cs_ctx* ctx, uint32_t mask) {
     }
     st.anchor = UINT32_MAX;
     st.first_bad_record = UINT64_MAX;
+    st.first_missing_record = UINT64_MAX;
   }
   auto* d_inst = dev<InstState>(ctx->d_inst, n_inst);
   auto* d_stats = dev<NameStat>(ctx->d_stats, static_cast<size_t>(n_inst) * std::max(1u, n_names));
@@ -1446,6 +1521,13 @@ static int cs_run_impl(cs_ctx* ctx, uint32_t mask) {
       return fail(ctx, CS_E_UNSUPPORTED, "stage_window too large for the device heuristic (<= 1600)");
   }
   launch_records(b, cfg, 0, s, &ctx->launches);
+  if (!ctx->extra_keys.empty() && ctx->n_cycles) {
+    const uint64_t K = ctx->extra_keys.size();
+    if (!dev<double>(ctx->d_rec_extra, ctx->n_cycles * K) || !dev<uint8_t>(ctx->d_rec_extra_has, ctx->n_cycles * K))
+      return fail(ctx, CS_E_CUDA, "cudaMalloc(record extras)");
+    b = make_buffers(ctx);
+    launch_record_extras(b, ctx->n_cycles, s, &ctx->launches);
+  }
   const int e6m = record_event(ctx, 6);
   ctx->timed.push_back({"stage_records", {e5, e6m}});
   int e6 = e6m;
@@ -1495,7 +1577,16 @@ static int cs_run_impl(cs_ctx* ctx, uint32_t mask) {
       dm.depth = pm->depth;
       dm.n_features = pm->n_features;
       dm.degenerate = pm->degenerate;
-      for (uint32_t f = 0; f < pm->n_features; ++f) dm.feature_ids[f] = pm->feature_ids[f];
+      for (uint32_t f = 0; f < pm->n_features; ++f) {
+        int32_t id = pm->feature_ids[f];
+        if (id == CS_F_EXTRA) {
+          auto it = std::lower_bound(ctx->extra_keys.begin(), ctx->extra_keys.end(), pm->feature_names[f]);
+          id = (it != ctx->extra_keys.end() && *it == pm->feature_names[f])
+                   ? kFeatExtra + static_cast<int32_t>(it - ctx->extra_keys.begin())
+                   : kFeatMissing;  // every record lacks it: FeatureMismatch at the first
+        }
+        dm.feature_ids[f] = id;
+      }
       dm.base = pm->base;
       dm.lr = pm->lr;
       dm.floor_ = pm->floor_;
@@ -1574,16 +1665,23 @@ static int cs_run_impl(cs_ctx* ctx, uint32_t mask) {
   hp.mark("final_sync");
   CS_CUDA(cudaGetLastError());
   ctx->n_records = ctx->rec_off[n_inst];
-  for (uint32_t i = 0; i < n_inst; ++i)
-    if (ctx->inst_status[i] == CS_OK && ctx->h_inst[i].first_bad_record != UINT64_MAX &&
-        (mask & (CS_RUN_SCORE | CS_RUN_DETECT)))
-      ctx->inst_status[i] = CS_E_NON_POSITIVE_LATENCY;
+  for (uint32_t i = 0; i < n_inst; ++i) {
+    // monitor_loop stops at the first record whose features are missing
+    // (FeatureMismatch, checked before ppe) or whose latency is <= 0
+    InstState& st = ctx->h_inst[i];
+    if (!(mask & (CS_RUN_SCORE | CS_RUN_DETECT))) continue;
+    const bool miss = st.first_missing_record != UINT64_MAX && st.first_missing_record <= st.first_bad_record;
+    if (miss) st.first_bad_record = st.first_missing_record;
+    if (ctx->inst_status[i] == CS_OK && st.first_bad_record != UINT64_MAX)
+      ctx->inst_status[i] = miss ? CS_E_FEATURE_MISMATCH : CS_E_NON_POSITIVE_LATENCY;
+  }
   if (ctx->streaming) {
     ctx->stream_stopped_prior = ctx->stream_stopped;
     for (uint32_t i = 0; i < n_inst; ++i) {
-      if (ctx->stream_stopped_prior[i]) ctx->inst_status[i] = CS_E_NON_POSITIVE_LATENCY;
-      if (ctx->h_inst[i].first_bad_record != UINT64_MAX && (mask & (CS_RUN_SCORE | CS_RUN_DETECT)))
-        ctx->stream_stopped[i] = 1;
+      if (ctx->stream_stopped_prior[i]) ctx->inst_status[i] = ctx->stream_stopped_prior[i];
+      if (!ctx->stream_stopped[i] && ctx->h_inst[i].first_bad_record != UINT64_MAX &&
+          (mask & (CS_RUN_SCORE | CS_RUN_DETECT)))
+        ctx->stream_stopped[i] = static_cast<uint8_t>(ctx->inst_status[i]);  // the stop's status
     }
   } else {
     ctx->stream_stopped_prior.clear();

@@ -47,6 +47,7 @@ struct cs_fitted_model {
   // flattened view storage
   std::vector<uint32_t> offsets;
   std::vector<cs_tree_node> flat;
+  std::vector<const char*> name_ptrs;  // cs_model::feature_names
 };
 
 namespace {
@@ -297,13 +298,20 @@ extern "C" {
 static int cs_fit_latency_model_impl(uint64_t n, uint32_t n_features, const int32_t* feature_ids,
                          const double* x, const double* y, const cs_gbdt_params* params,
                          const cs_fit_options* opt, cs_fitted_model** out, char* err,
-                         size_t err_cap) {
-  if (!out || !params || !opt || !feature_ids || (n && (!x || !y))) return CS_E_INVALID_ARGUMENT;
+                         size_t err_cap, const char* const* names = nullptr) {
+  if (!out || !params || !opt || (!feature_ids && !names) || (n && (!x || !y))) return CS_E_INVALID_ARGUMENT;
   *out = nullptr;
   auto m = new cs_fitted_model();
   try {
     m->params = *params;
-    set_features(*m, n_features, feature_ids);
+    if (names) {
+      for (uint32_t f = 0; f < n_features; ++f) {
+        if (!names[f]) throw FitError{CS_E_INVALID_ARGUMENT, "null feature name"};
+        m->feature_names.push_back(names[f]);
+      }
+    } else {
+      set_features(*m, n_features, feature_ids);
+    }
     std::vector<uint32_t> train, calib;
     split_rows(n, n_features, x, y, params, opt, train, calib);
     Matrix tx;
@@ -332,6 +340,17 @@ int cs_fit_latency_model(uint64_t n, uint32_t n_features, const int32_t* feature
                          const cs_fit_options* opt, cs_fitted_model** out, char* err,
                          size_t err_cap) {
   return cs_guard([&] { return cs_fit_latency_model_impl(n, n_features, feature_ids, x, y, params, opt, out, err, err_cap); });
+}
+
+int cs_fit_latency_model_named(uint64_t n, uint32_t n_features, const char* const* feature_names,
+                               const double* x, const double* y, const cs_gbdt_params* params,
+                               const cs_fit_options* opt, cs_fitted_model** out, char* err,
+                               size_t err_cap) {
+  if (!feature_names && n_features) return CS_E_INVALID_ARGUMENT;
+  return cs_guard([&] {
+    return cs_fit_latency_model_impl(n, n_features, nullptr, x, y, params, opt, out, err, err_cap,
+                                     feature_names);
+  });
 }
 
 static int cs_fit_latency_models_impl(int device, uint32_t n_models, const uint64_t* offsets,
@@ -491,6 +510,10 @@ int cs_model_view(const cs_fitted_model* m, cs_model* v) {
   v->n_features = static_cast<uint32_t>(m->feature_names.size());
   v->n_trees = static_cast<uint32_t>(m->trees.size());
   v->feature_ids = m->feature_ids.data();
+  auto& np = const_cast<cs_fitted_model*>(m)->name_ptrs;
+  np.clear();
+  for (const auto& nm : m->feature_names) np.push_back(nm.c_str());
+  v->feature_names = np.data();
   v->tree_offsets = m->offsets.data();
   v->nodes = m->flat.data();
   v->base = m->base;

@@ -15,7 +15,7 @@ constexpr int kScanThreads = 512;               // 16 warps
 constexpr int kTileEvents = 1024;               // 32 KiB tile, one TMA bulk copy
 constexpr int kSmemNames = 512;                 // name stats staged in smem
 constexpr int kMaxFeatures = 8;
-constexpr int kMaxTreeDepth = 8;
+constexpr int kMaxTreeDepth = 24;  // bounded in practice by the layout size (cs_load_model)
 constexpr uint64_t kSampleEvents = 1u << 18;    // anchor-guess sample per instance (verified by the full pass)
 
 // name-stat accumulator (per instance x name); exact integer moments
@@ -43,9 +43,14 @@ struct InstState {
   unsigned long long n_alerts;
   uint32_t fixed_anchor;   // streaming: `guess` is this instance's fixed anchor
   uint32_t unsorted;       // the event scan saw start_ts decrease (not canonical order)
+  unsigned long long first_missing_record;  // FeatureMismatch: a model extra the record lacks
 };
 
 // flattened model in complete-binary-tree layout (see pack_model)
+// feature ids in DevModel: CS_F_* (0..4), kFeatExtra + key for a record extra,
+// kFeatMissing for an extra name the uploaded trace has no key for
+constexpr int32_t kFeatExtra = 16;
+constexpr int32_t kFeatMissing = 15;
 struct DevModel {
   uint32_t n_trees;
   uint32_t depth;          // padded depth D: 2^D-1 internal, 2^D leaves per tree
@@ -153,6 +158,14 @@ struct DevBuffers {
   double* c_mu;                 // n_cycles x n_beta
   uint8_t* c_mu_has;
   StreamCarry* stream;          // per instance, null when not streaming
+  // record extras (cs_upload_extras): side table sorted by event, and the
+  // per-record values / presence (n_records x n_extra_keys)
+  const cs_extra_ref* extra_refs;
+  uint64_t n_extra_refs;
+  const cs_extra_value* extra_vals;
+  uint32_t n_extra_keys;
+  double* rec_extra;
+  uint8_t* rec_extra_has;
 };
 
 // Single-read segmentation (k_segment_range, CS_OPT_FUSED): ranges of <= 4
@@ -218,6 +231,8 @@ int launch_stage_heuristic(const DevBuffers& b, const DevConfig& cfg, const Stag
                            uint64_t* launches);
 void launch_records(const DevBuffers& b, const DevConfig& cfg, uint64_t n_blocks_cap,
                     cudaStream_t s, uint64_t* launches);
+// per record: the extras of its cycle (last event carrying each key wins)
+void launch_record_extras(const DevBuffers& b, uint64_t n_records_cap, cudaStream_t s, uint64_t* launches);
 void launch_score(const DevBuffers& b, const DevConfig& cfg, uint64_t n_records_total,
                   const uint64_t* h_rec_off, const int* h_model_of_inst, const DevModel* h_models,
                   cudaStream_t s, uint64_t* launches);

@@ -971,6 +971,47 @@ __device__ __forceinline__ u64 records_on_device(const DevBuffers& b, u64 cap) {
   return n < cap ? n : cap;
 }
 
+// record extras (cycles.cpp:392-405): thread per record; the cycle's events
+// carrying extras are found by binary search in the event-sorted side table,
+// and each key keeps the value of the last such event (map assignment order)
+__global__ void k_record_extras(DevBuffers b, uint64_t n_records) {
+  n_records = records_on_device(b, n_records);
+  const u64 k = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n_records) return;
+  const uint32_t K = b.n_extra_keys;
+  double* vals = b.rec_extra + k * K;
+  uint8_t* has = b.rec_extra_has + k * K;
+  for (uint32_t j = 0; j < K; ++j) {
+    vals[j] = 0.0;
+    has[j] = 0;
+  }
+  const u64 g = b.rec_cycle[k];
+  const u64 first = b.c_first[g], last = b.c_last[g];
+  u64 lo = 0, hi = b.n_extra_refs;  // first ref with event >= first
+  while (lo < hi) {
+    const u64 mid = (lo + hi) >> 1;
+    if (b.extra_refs[mid].event < first) lo = mid + 1;
+    else hi = mid;
+  }
+  for (u64 r = lo; r < b.n_extra_refs && b.extra_refs[r].event < last; ++r) {
+    const cs_extra_ref ref = b.extra_refs[r];
+    for (uint32_t v = 0; v < ref.count; ++v) {
+      const cs_extra_value ev = b.extra_vals[ref.first + v];
+      if (ev.key < K) {
+        vals[ev.key] = ev.value;
+        has[ev.key] = 1;
+      }
+    }
+  }
+}
+
+void launch_record_extras(const DevBuffers& b, uint64_t n_records_cap, cudaStream_t s, uint64_t* launches) {
+  if (!n_records_cap || !b.n_extra_keys) return;
+  k_record_extras<<<(unsigned)((n_records_cap + 127) / 128), 128, 0, s>>>(b, n_records_cap);
+  ++*launches;
+}
+
+
 template <int NF>
 __global__ void __launch_bounds__(kScoreThreads)
     k_score(DevBuffers b, DevConfig cfg, uint64_t n_records, uint64_t smem_cap) {
@@ -1041,8 +1082,22 @@ __global__ void __launch_bounds__(kScoreThreads)
         y[q] = __dmul_rn((double)target, 1e-9);  // cycles.cpp:390
 #pragma unroll
         for (int f = 0; f < NF; ++f) {
-          i64 iv;
-          switch (m.feature_ids[f]) {
+          i64 iv = 0;
+          const int32_t id = m.feature_ids[f];
+          if (id >= kFeatExtra || id == kFeatMissing) {
+            // a record extra (main.cpp:70-75): double-valued, compared as such
+            const u64 ke = k * (u64)b.n_extra_keys + (u64)(id - kFeatExtra);
+            if (id == kFeatMissing || !b.rec_extra_has[ke]) {
+              atomicMin(reinterpret_cast<u64*>(&b.inst[inst].first_missing_record), (u64)(k - rb));
+              x[q][f] = 0.0;
+            } else {
+              x[q][f] = b.rec_extra[ke];
+            }
+            xi[q][f] = 0;
+            exact = false;
+            continue;
+          }
+          switch (id) {
             case CS_F_BATCH: iv = w.batch; break;
             case CS_F_W_KV: iv = w.batch * (w.input_len + w.output_len); break;
             case CS_F_INPUT_LEN: iv = w.input_len; break;
@@ -1179,6 +1234,14 @@ __device__ __forceinline__ void score_one_lut(const DevBuffers& b, const DevConf
   const double y = __dmul_rn((double)target, 1e-9);  // cycles.cpp:390
   const uint8_t stage = b.c_stage[g];
   auto fval = [&](int id) -> double {
+    if (id >= kFeatExtra || id == kFeatMissing) {
+      const u64 ke = k * (u64)b.n_extra_keys + (u64)(id - kFeatExtra);
+      if (id == kFeatMissing || !b.rec_extra_has[ke]) {
+        atomicMin(reinterpret_cast<u64*>(&b.inst[inst].first_missing_record), (u64)(k - rb));
+        return 0.0;
+      }
+      return b.rec_extra[ke];
+    }
     switch (id) {
       case CS_F_BATCH: return (double)w.batch;
       case CS_F_W_KV: return (double)(w.batch * (w.input_len + w.output_len));

@@ -58,6 +58,11 @@ def lib():
     L.cs_upload_unsorted.argtypes = [vp, u32, vp, vp, vp, u64, vp]
     L.cs_get_order.argtypes = [vp, u32, vp, sz, psz]
     L.cs_set_cycles.argtypes = [vp, vp, u64, vp]
+    L.cs_upload_extras.argtypes = [vp, u32, C.c_char_p, vp, u64, vp, u64]
+    L.cs_get_record_extras.argtypes = [vp, u32, vp, vp, sz, psz]
+    L.cs_fit_latency_model_named.argtypes = [u64, u32, C.POINTER(C.c_char_p), vp, vp,
+                                             C.POINTER(abi.GbdtParams), C.POINTER(abi.FitOptions),
+                                             C.POINTER(vp), C.c_char_p, sz]
     L.cs_detect_residuals.argtypes = [vp, vp, u64, C.POINTER(abi.ControlConfig), C.c_double, vp, vp, vp,
                                       C.POINTER(abi.StrategyMetrics)]
     L.cs_get_cycle_range.argtypes = [vp, u32, u64, u64, vp]
@@ -132,7 +137,8 @@ def lib():
 
 EXPORTED_SYMBOLS = [
     "cs_abi_version", "cs_status_type", "cs_ctx_create", "cs_ctx_destroy", "cs_last_error",
-    "cs_set_config", "cs_set_name_table", "cs_upload", "cs_upload_unsorted", "cs_get_order", "cs_set_cycles", "cs_detect_residuals", "cs_upload_wire", "cs_wire_pack",
+    "cs_set_config", "cs_set_name_table", "cs_upload", "cs_upload_unsorted", "cs_get_order", "cs_set_cycles", "cs_detect_residuals", "cs_upload_extras", "cs_get_record_extras",
+    "cs_fit_latency_model_named", "cs_upload_wire", "cs_wire_pack",
     "cs_wire_view", "cs_wire_free", "cs_ingest_chrome_json", "cs_ingest_view", "cs_ingest_free", "cs_ingest_report", "cs_ingest_topology", "cs_ingest_merge", "cs_rank_suspects",
     "cs_suspicion_rank", "cs_welch_p_value", "cs_load_model", "cs_run", "cs_sync",
     "cs_get_summary", "cs_get_candidates", "cs_get_candidates_exact", "cs_get_cycles", "cs_get_components", "cs_get_beta",
@@ -203,18 +209,26 @@ class LatencyModel:
 def fit_latency_model(x: np.ndarray, y: np.ndarray, feature_names=("batch", "w_kv"),
                       params: abi.GbdtParams | None = None,
                       options: abi.FitOptions | None = None) -> LatencyModel:
-    """fit_latency_model (baseline.cpp:168-208): deterministic host C++ fit."""
+    """fit_latency_model (baseline.cpp:168-208): deterministic host C++ fit.
+    Feature names outside batch/w_kv/input_len/output_len/stage are record
+    extras (the Full feature set's post_* columns)."""
     x = np.ascontiguousarray(x, dtype=np.float64)
     y = np.ascontiguousarray(y, dtype=np.float64)
-    ids = np.array([abi.FEATURE_IDS[n] for n in feature_names], dtype=np.int32)
+    names = list(feature_names)
     params = params or abi.default_gbdt_params()
     if options is None:
-        options = abi.default_fit_options(len(ids))
-        options.stratify_col = list(feature_names).index("w_kv") if "w_kv" in feature_names else 0
+        options = abi.default_fit_options(len(names))
+        options.stratify_col = names.index("w_kv") if "w_kv" in names else 0
     h = C.c_void_p()
     err = C.create_string_buffer(1024)
-    rc = lib().cs_fit_latency_model(len(y), len(ids), ids.ctypes.data, _ptr(x), _ptr(y),
-                                    C.byref(params), C.byref(options), C.byref(h), err, 1024)
+    if all(n in abi.FEATURE_IDS for n in names):
+        ids = np.array([abi.FEATURE_IDS[n] for n in names], dtype=np.int32)
+        rc = lib().cs_fit_latency_model(len(y), len(ids), ids.ctypes.data, _ptr(x), _ptr(y),
+                                        C.byref(params), C.byref(options), C.byref(h), err, 1024)
+    else:
+        arr = (C.c_char_p * len(names))(*[n.encode() for n in names])
+        rc = lib().cs_fit_latency_model_named(len(y), len(names), arr, _ptr(x), _ptr(y),
+                                              C.byref(params), C.byref(options), C.byref(h), err, 1024)
     if rc:
         raise EngineError(rc, err.value.decode())
     return LatencyModel(h)
@@ -681,6 +695,28 @@ class Analyzer:
     def order(self, inst: int = 0) -> np.ndarray:
         """cs_get_order: canonical position -> input position within the instance."""
         return self._get(self.L.cs_get_order, inst, np.uint64)
+
+    def upload_extras(self, keys, refs: np.ndarray, values: np.ndarray):
+        """cs_upload_extras: the record-extras side table of the uploaded events
+        (keys sorted, refs sorted by event, values per ref)."""
+        packed = b"".join(k.encode() + b"\0" for k in keys) or b"\0"
+        r = np.ascontiguousarray(refs, dtype=abi.EXTRA_REF_DTYPE)
+        v = np.ascontiguousarray(values, dtype=abi.EXTRA_VALUE_DTYPE)
+        self._keep_extras = (packed, r, v)
+        self._ck(self.L.cs_upload_extras(self.h, len(keys), packed, _ptr(r), len(r), _ptr(v), len(v)))
+        self.extra_keys = list(keys)
+
+    def record_extras(self, inst=0):
+        """cs_get_record_extras: (values, present), n_records x n_keys."""
+        n = C.c_size_t()
+        self._ck(self.L.cs_get_record_extras(self.h, inst, None, None, 0, C.byref(n)))
+        k = len(getattr(self, "extra_keys", []))
+        vals = np.zeros(n.value, np.float64)
+        has = np.zeros(n.value, np.uint8)
+        if n.value:
+            self._ck(self.L.cs_get_record_extras(self.h, inst, vals.ctypes.data, has.ctypes.data, n.value,
+                                                 C.byref(n)))
+        return vals.reshape(-1, k) if k else vals.reshape(0, 0), has.reshape(-1, k) if k else has.reshape(0, 0)
 
     def set_cycles(self, cycles: np.ndarray, components: np.ndarray | None = None):
         """cs_set_cycles: caller-given cycles (CYCLE_DTYPE rows, canonical event

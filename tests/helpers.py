@@ -13,13 +13,16 @@ from paper_2601_09258_b200 import runtime as rt
 
 
 def run_product(events, names, workloads, n_comm=0, run_config=None, model_json=None,
-                mask=abi.RUN_ALL, analyzer=None, fused=False):
-    """One instance through the C ABI; returns InstanceResult."""
+                mask=abi.RUN_ALL, analyzer=None, fused=False, extras=None):
+    """One instance through the C ABI; returns InstanceResult.  extras =
+    (keys, refs, values) of the record-extras side table (cs_upload_extras)."""
     an = analyzer or rt.Analyzer()
     an.set_fused(fused)
     span = rt.span_names_mask(events, len(names))
     an.configure(names, span, n_comm_slots=n_comm, run_config=run_config)
     an.upload(events, [0, len(events)], workloads)
+    if extras is not None:
+        an.upload_extras(*extras)
     if model_json and (mask & (abi.RUN_SCORE | abi.RUN_DETECT)):
         an.load_model(rt.LatencyModel.from_json(model_json))
     an.run(mask)
