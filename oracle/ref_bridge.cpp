@@ -980,6 +980,7 @@ struct CpuBaseline {
   std::vector<LatencyModel> models;
   uint64_t events = 0;
   double fit_seconds = 0.0;
+  std::string anchor_hint;  // slices of one trace: the anchor the whole trace uses
 };
 
 void* ref_cpu_prepare(uint32_t n_instances, uint32_t n_threads, uint64_t cycles_per_instance,
@@ -1029,6 +1030,34 @@ double ref_cpu_fit_seconds(void* h) { return static_cast<CpuBaseline*>(h)->fit_s
 void ref_cpu_free(void* h) { delete static_cast<CpuBaseline*>(h); }
 
 // Returns wall seconds of one timed pass over all prepared instances.
+// Cycle-aligned slices of ONE trace (the GPU arm's benchmarked instance), one
+// reference Trace per slice built on n_threads threads; every slice is
+// analysed with the whole trace's anchor (anchor_hint) and one model.
+void* ref_cpu_prepare_slices(uint64_t n, const cs_event* ev, const uint64_t* event_ids, uint32_t n_names,
+                             const char* names_packed, const cs_workload* wl, uint32_t n_comm,
+                             const char* comm_hash_packed, const int32_t* comm_rank, uint32_t n_slices,
+                             const uint64_t* bounds, const char* model_json, const char* anchor_hint,
+                             uint32_t n_threads) {
+  auto* cb = new CpuBaseline();
+  cb->inst.resize(n_slices);
+  cb->anchor_hint = anchor_hint ? anchor_hint : "";
+  const LatencyModel model = LatencyModel::from_json(json::parse(model_json));
+  cb->models.assign(n_slices, model);
+  std::vector<std::thread> th;
+  for (uint32_t t = 0; t < std::max(1u, n_threads); ++t)
+    th.emplace_back([&, t] {
+      for (uint32_t i = t; i < n_slices; i += std::max(1u, n_threads)) {
+        const uint64_t lo = bounds[i], hi = std::min<uint64_t>(bounds[i + 1], n);
+        cb->inst[i].reset(static_cast<Handle*>(ref_build(hi - lo, ev + lo, event_ids ? event_ids + lo : nullptr,
+                                                         n_names, names_packed, wl, n_comm, comm_hash_packed,
+                                                         comm_rank, 0)));
+      }
+    });
+  for (auto& x : th) x.join();
+  for (uint32_t i = 0; i < n_slices; ++i) cb->events += cb->inst[i]->ds.trace.events.size();
+  return cb;
+}
+
 double ref_cpu_run(void* h, uint32_t n_threads, uint64_t* n_alerts_out) {
   auto* cb = static_cast<CpuBaseline*>(h);
   const uint32_t n = static_cast<uint32_t>(cb->inst.size());
@@ -1036,6 +1065,7 @@ double ref_cpu_run(void* h, uint32_t n_threads, uint64_t* n_alerts_out) {
   auto work = [&](uint32_t i) {
     const Trace& tr = cb->inst[i]->ds.trace;
     CycleConfig cc;
+    cc.anchor_hint = cb->anchor_hint;
     PipelineOptions po;
     ControlConfig dc;
     const auto cycles = segment_and_classify(tr, cc);

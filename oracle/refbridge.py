@@ -81,6 +81,10 @@ def lib():
         L.ref_cpu_prepare.restype = vp
         L.ref_cpu_prepare.argtypes = [C.c_uint32, C.c_uint32, C.c_uint64, C.c_uint64,
                                       C.c_uint64]
+        L.ref_cpu_prepare_slices.restype = vp
+        L.ref_cpu_prepare_slices.argtypes = [C.c_uint64, vp, vp, C.c_uint32, C.c_char_p, vp, C.c_uint32,
+                                             C.c_char_p, vp, C.c_uint32, vp, C.c_char_p, C.c_char_p,
+                                             C.c_uint32]
         L.ref_cpu_events.restype = C.c_uint64
         L.ref_cpu_events.argtypes = [vp]
         L.ref_cpu_fit_seconds.restype = C.c_double
@@ -384,6 +388,29 @@ class CpuBaseline:
         self.h = lib().ref_cpu_prepare(n_instances, n_threads, cycles_per_instance, n_ranks, seed)
         self.events = int(lib().ref_cpu_events(self.h))
         self.fit_seconds = lib().ref_cpu_fit_seconds(self.h)
+
+    @classmethod
+    def slices(cls, events, event_ids, names, workloads, comm_hash, comm_rank, bounds, model_json,
+               anchor, n_threads):
+        """Cycle-aligned slices [bounds[k], bounds[k+1]) of ONE trace, one
+        reference Trace each (analysed on its own thread with `anchor` as the
+        hint and one model)."""
+        self = cls.__new__(cls)
+        self.n_threads = n_threads
+        ev = np.ascontiguousarray(events, dtype=abi.EVENT_DTYPE)
+        ids = np.ascontiguousarray(event_ids, dtype=np.uint64)
+        wl = np.ascontiguousarray(workloads, dtype=abi.WORKLOAD_DTYPE)
+        b = np.ascontiguousarray(bounds, dtype=np.uint64)
+        packed = b"".join(n.encode() + b"\0" for n in names)
+        cpacked = b"".join(c.encode() + b"\0" for c in comm_hash) or b"\0"
+        crank = np.ascontiguousarray(np.asarray(comm_rank, dtype=np.int32))
+        self.h = lib().ref_cpu_prepare_slices(len(ev), ev.ctypes.data, ids.ctypes.data, len(names), packed,
+                                              wl.ctypes.data, len(comm_hash), cpacked,
+                                              crank.ctypes.data if len(crank) else None, len(b) - 1,
+                                              b.ctypes.data, model_json.encode(), anchor.encode(), n_threads)
+        self.events = int(lib().ref_cpu_events(self.h))
+        self.fit_seconds = 0.0
+        return self
 
     def run(self):
         """One timed pass; returns (seconds, alerts)."""

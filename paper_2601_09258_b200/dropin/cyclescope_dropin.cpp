@@ -51,7 +51,41 @@ struct Ingested {
   std::vector<std::string> names;
   std::vector<uint8_t> is_span;
   std::vector<std::tuple<std::string, std::string, int>> comm;
+  // record extras (PipelineOptions::extra_args_prefix args, cycles.cpp:392-405)
+  std::string extra_prefix;
+  std::vector<std::string> extra_keys;
+  std::vector<cs_extra_ref> extra_refs;
+  std::vector<cs_extra_value> extra_vals;
 };
+
+// the numeric args with the prefix, per event in key order (map iteration)
+void ingest_extras(Ingested& in, const Trace& trace, const std::string& prefix) {
+  in.extra_prefix = prefix;
+  in.extra_keys.clear();
+  in.extra_refs.clear();
+  in.extra_vals.clear();
+  if (prefix.empty()) return;
+  std::set<std::string> keys;
+  for (const auto& e : trace.events)
+    for (const auto& [k, v] : e.args)
+      if (k.rfind(prefix, 0) == 0 && !std::holds_alternative<std::string>(v)) keys.insert(k);
+  in.extra_keys.assign(keys.begin(), keys.end());
+  for (size_t i = 0; i < trace.events.size(); ++i) {
+    cs_extra_ref ref{i, static_cast<uint32_t>(in.extra_vals.size()), 0};
+    for (const auto& [k, v] : trace.events[i].args) {
+      if (k.rfind(prefix, 0) != 0) continue;
+      double d;
+      if (const auto* x = std::get_if<double>(&v)) d = *x;
+      else if (const auto* n = std::get_if<std::int64_t>(&v)) d = static_cast<double>(*n);
+      else if (const auto* b = std::get_if<bool>(&v)) d = *b ? 1.0 : 0.0;
+      else continue;
+      const auto key = std::lower_bound(in.extra_keys.begin(), in.extra_keys.end(), k) - in.extra_keys.begin();
+      in.extra_vals.push_back({static_cast<uint32_t>(key), 0, d});
+      ++ref.count;
+    }
+    if (ref.count) in.extra_refs.push_back(ref);
+  }
+}
 
 Ingested ingest(const Trace& trace, const CycleConfig& cfg) {
   Ingested in;
@@ -159,6 +193,7 @@ struct Session {
   Ctx ctx;
   std::vector<std::string> phases;  // device phase index -> name (last config applied)
   std::vector<std::string> slot_names;
+  bool extras_uploaded = false;
 };
 
 uint64_t fingerprint(const Trace& t) {
@@ -300,9 +335,34 @@ std::vector<Cycle> cycles_of(const Session& S, const Trace& trace, bool classifi
   return out;
 }
 
+// the device extras table follows the PipelineOptions prefix in force
+void sync_extras(Session& S, const Trace& trace, const PipelineOptions& opt) {
+  if (S.in.extra_prefix == opt.extra_args_prefix && S.extras_uploaded) return;
+  ingest_extras(S.in, trace, opt.extra_args_prefix);
+  std::string packed;
+  for (const auto& k : S.in.extra_keys) {
+    packed += k;
+    packed.push_back('\0');
+  }
+  S.ctx.check(cs_upload_extras(S.ctx.c, static_cast<uint32_t>(S.in.extra_keys.size()), packed.c_str(),
+                               S.in.extra_refs.data(), S.in.extra_refs.size(), S.in.extra_vals.data(),
+                               S.in.extra_vals.size()));
+  S.extras_uploaded = true;
+}
+
 std::vector<CycleRecord> records_of(const Session& S) {
   const auto rr = fetch<cs_record>(S, cs_get_records);
   std::vector<CycleRecord> out(rr.size());
+  const size_t K = S.in.extra_keys.size();
+  std::vector<double> xv;
+  std::vector<uint8_t> xh;
+  if (K) {
+    size_t n = 0;
+    S.ctx.check(cs_get_record_extras(S.ctx.c, 0, nullptr, nullptr, 0, &n));
+    xv.resize(n);
+    xh.resize(n);
+    if (n) S.ctx.check(cs_get_record_extras(S.ctx.c, 0, xv.data(), xh.data(), n, &n));
+  }
   for (size_t i = 0; i < rr.size(); ++i) {
     out[i].cycle_index = rr[i].cycle_index;
     out[i].start_ts = rr[i].start_ts;
@@ -312,6 +372,8 @@ std::vector<CycleRecord> records_of(const Session& S) {
     out[i].workload.output_len = rr[i].output_len;
     out[i].workload.stage = out[i].stage;
     out[i].latency_s = rr[i].latency_s;
+    for (size_t k = 0; k < K; ++k)
+      if (xh[i * K + k]) out[i].extra[S.in.extra_keys[k]] = xv[i * K + k];
   }
   return out;
 }
@@ -461,12 +523,12 @@ std::vector<Cycle> segment_and_classify(const Trace& trace, const CycleConfig& c
   return cycles_of(S, trace, true);
 }
 
-// build_cycle_records (cycles.cpp:359-364).  `extra` (post_* args, the Full
-// feature set) is not harvested by the device path.
+// build_cycle_records (cycles.cpp:359-364), `extra` (post_* args) included
 std::vector<CycleRecord> build_cycle_records(const Trace& trace, const CycleConfig& config,
                                              const PipelineOptions& options) {
   Session& S = session(trace, config);
   apply_config(S, config, options);
+  sync_extras(S, trace, options);
   S.ctx.check(cs_run(S.ctx.c, CS_RUN_SEGMENT));
   if (summary(S).status == CS_E_NO_ANCHOR_FOUND) rethrow(CS_E_NO_ANCHOR_FOUND, "no anchor and no periodic GPU kernels");
   return records_of(S);
@@ -479,6 +541,7 @@ std::vector<CycleRecord> build_cycle_records(const Trace& trace, std::span<const
   if (cycles.empty()) return {};
   Session& S = session(trace, config);
   apply_config(S, config, options);
+  sync_extras(S, trace, options);
   set_cycles(S, cycles, true);
   S.ctx.check(cs_run(S.ctx.c, CS_RUN_GIVEN));
   return records_of(S);
