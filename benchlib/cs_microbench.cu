@@ -6,7 +6,7 @@
 
 #include <cstdint>
 
-#include "cyclescope_b200.h"
+#include "cs_bench.h"
 
 namespace {
 

@@ -19,7 +19,7 @@
 #include <thread>
 #include <vector>
 
-#include "cyclescope_b200.h"
+#include "cs_bench.h"
 
 namespace {
 

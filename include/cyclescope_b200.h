@@ -698,12 +698,6 @@ int cs_stream_push(cs_ctx* ctx, uint32_t n_inst, const uint64_t* offsets, const 
 #define CS_OPT_TRAVERSAL 2
 int cs_set_option(cs_ctx* ctx, int option, int64_t value);
 
-/* HBM read-streaming microbenchmark (profiling only).
- * variant 0: vectorised LDG (p0 CTAs/SM, p1 threads, p2 unroll 1|8);
- * variant 1: 1-D TMA bulk copies (p0 chunk bytes, p1 stages, p2 CTAs/SM). */
-int cs_microbench(int variant, const void* dev_src, uint64_t n_bytes, int p0, int p1, int p2,
-                  int iters, double* ms_out);
-
 /* Pinned host memory helpers (cudaHostAlloc) for the e2e path. */
 int cs_host_alloc(size_t bytes, void** out);
 int cs_host_free(void* p);
@@ -784,33 +778,6 @@ int cs_config_from_json(const char* run_config_json, uint32_t n_names,
                         uint32_t n_comm_slots, cs_name_info* out_names,
                         cs_cycle_config* out_cycle, cs_control_config* out_control,
                         char* err, size_t err_cap);
-
-/* ------------------------------------------------- synthetic trace producer
- * Restatement of the reference's simkit generator (simkit.cpp:34-86,
- * 195-246, 276-506) writing cs_event records directly; benchmark input only.
- * n_chunks > 1 concatenates independent generator calls (substream seeds per
- * chunk) in time so large instances can be produced on all host cores. */
-typedef struct cs_synth_params {
-  uint64_t n_cycles;
-  uint64_t workload_seed;
-  uint64_t synth_seed;
-  int32_t fault_family;    /* -1 none, else FaultFamily enum (simkit.hpp:70-79) */
-  int32_t target_rank;
-  uint64_t fault_onset;    /* global cycle index */
-  uint64_t fault_duration;
-  double severity;         /* <= 0: default_severity (simkit.cpp:134-146) */
-  uint64_t n_ranks;
-  double noise;            /* < 0: GroundTruthModel default 0.05 */
-} cs_synth_params;
-typedef struct cs_synth_trace cs_synth_trace;
-int cs_synth_generate(const cs_synth_params* p, uint32_t n_chunks, uint32_t n_threads,
-                      int compact_names, cs_synth_trace** out);
-int cs_synth_view(const cs_synth_trace* t, const cs_event** ev, uint64_t* n_ev,
-                  const uint64_t** event_ids, const cs_workload** wl, uint64_t* n_wl,
-                  const uint8_t** labels, uint64_t* n_cycles);
-int cs_synth_names(const cs_synth_trace* t, const char** packed, size_t* n_bytes,
-                   uint32_t* n_names, uint32_t* n_comm);
-void cs_synth_free(cs_synth_trace* t);
 
 #ifdef __cplusplus
 }

@@ -106,8 +106,6 @@ def lib():
     L.cs_stream_push.argtypes = [vp, u32, vp, vp, u64, vp, u32, vp, sz, psz]
     L.cs_evaluate_strategy.argtypes = [vp, u32, vp, u64, C.POINTER(abi.StrategyMetrics)]
     L.cs_alerts_to_ndjson.argtypes = [vp, u64, u64, u64, vp, sz, psz]
-    L.cs_microbench.argtypes = [C.c_int, vp, u64, C.c_int, C.c_int, C.c_int, C.c_int,
-                                C.POINTER(C.c_double)]
     L.cs_host_alloc.argtypes = [sz, C.POINTER(vp)]
     L.cs_host_free.argtypes = [vp]
     L.cs_get_timings.argtypes = [vp, vp, sz, psz, C.c_char_p, sz]
@@ -125,12 +123,6 @@ def lib():
     L.cs_config_from_json.argtypes = [C.c_char_p, u32, vp, vp, u32, vp,
                                       C.POINTER(abi.CycleConfig), C.POINTER(abi.ControlConfig),
                                       C.c_char_p, sz]
-    L.cs_synth_generate.argtypes = [vp, u32, u32, C.c_int, C.POINTER(vp)]
-    L.cs_synth_view.argtypes = [vp] + [C.POINTER(vp), C.POINTER(u64), C.POINTER(vp),
-                                       C.POINTER(vp), C.POINTER(u64), C.POINTER(vp),
-                                       C.POINTER(u64)]
-    L.cs_synth_names.argtypes = [vp, C.POINTER(C.c_char_p), psz, C.POINTER(u32), C.POINTER(u32)]
-    L.cs_synth_free.argtypes = [vp]
     _lib = L
     return L
 
@@ -145,8 +137,7 @@ EXPORTED_SYMBOLS = [
     "cs_get_collective_beta", "cs_get_mu", "cs_get_records", "cs_get_alerts", "cs_host_alloc",
     "cs_host_free", "cs_get_timings", "cs_get_launch_count", "cs_fit_latency_model", "cs_fit_latency_models",
     "cs_model_from_json", "cs_model_to_json", "cs_model_view", "cs_model_free",
-    "cs_ucl_from_stats", "cs_compute_ucl", "cs_config_from_json", "cs_synth_generate",
-    "cs_synth_view", "cs_synth_names", "cs_synth_free", "cs_set_option", "cs_microbench",
+    "cs_ucl_from_stats", "cs_compute_ucl", "cs_config_from_json", "cs_set_option",
     "cs_redetect", "cs_evaluate_strategy", "cs_alerts_to_ndjson", "cs_stream_begin",
     "cs_stream_end", "cs_stream_tail", "cs_stream_push",
 ]
@@ -405,6 +396,31 @@ FAULT_FAMILIES = ["cpu_contention", "cpu_freq_drop", "gpu_contention", "gpu_cloc
                   "memory_thrash", "nvlink_saturation", "pcie_bottleneck", "bus_contention"]
 
 
+BENCH_LIB_PATH = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "benchlib",
+                              "libcs_bench.so")
+_bench = None
+
+
+def bench_lib():
+    """benchlib/libcs_bench.so: the synthetic trace producer and the HBM
+    microbenchmark (benchmark support; never part of the analysis path)."""
+    global _bench
+    if _bench is None:
+        if not os.path.exists(BENCH_LIB_PATH):
+            raise RuntimeError(f"{BENCH_LIB_PATH} missing: build it with __graft_entry__.build()")
+        B = C.CDLL(BENCH_LIB_PATH)
+        vp, sz, u32, u64 = C.c_void_p, C.c_size_t, C.c_uint32, C.c_uint64
+        B.cs_synth_generate.argtypes = [vp, u32, u32, C.c_int, C.POINTER(vp)]
+        B.cs_synth_view.argtypes = [vp] + [C.POINTER(vp), C.POINTER(u64), C.POINTER(vp),
+                                           C.POINTER(vp), C.POINTER(u64), C.POINTER(vp), C.POINTER(u64)]
+        B.cs_synth_names.argtypes = [vp, C.POINTER(C.c_char_p), C.POINTER(sz), C.POINTER(u32), C.POINTER(u32)]
+        B.cs_synth_free.argtypes = [vp]
+        B.cs_microbench.argtypes = [C.c_int, vp, u64, C.c_int, C.c_int, C.c_int, C.c_int,
+                                    C.POINTER(C.c_double)]
+        _bench = B
+    return _bench
+
+
 def synth_trace(n_cycles, workload_seed, synth_seed, fault=None, onset=0, duration=0,
                 severity=-1.0, target_rank=0, n_ranks=1, noise=-1.0, n_chunks=1,
                 n_threads=None, compact_names=True) -> SynthTrace:
@@ -412,7 +428,7 @@ def synth_trace(n_cycles, workload_seed, synth_seed, fault=None, onset=0, durati
     fam = -1 if fault is None else (FAULT_FAMILIES.index(fault) if isinstance(fault, str) else int(fault))
     p = SynthParams(n_cycles, workload_seed, synth_seed, fam, target_rank, onset, duration,
                     severity, n_ranks, noise)
-    L = lib()
+    L = bench_lib()
     h = C.c_void_p()
     _check(L.cs_synth_generate(C.byref(p), n_chunks, n_threads or os.cpu_count() or 1,
                                int(compact_names), C.byref(h)))

@@ -18,9 +18,9 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 GOLDEN = os.path.join(ROOT, "tests", "golden")
 
 
-def declared_functions():
+def declared_functions(header="cyclescope_b200.h"):
     names = []
-    for h in glob.glob(os.path.join(ROOT, "include", "*.h")):
+    for h in glob.glob(os.path.join(ROOT, "include", header)):
         text = open(h).read()
         text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
         names += re.findall(r"^\s*(?:const\s+)?[a-z_0-9]+\s*\**\s*(cs_[a-z_0-9]+)\s*\(", text, re.M)
@@ -34,7 +34,12 @@ def test_library_exports_every_declared_symbol():
     for name in decl:
         assert hasattr(L, name), name
     assert set(rt.EXPORTED_SYMBOLS) <= set(decl)
-    assert L.cs_abi_version() == abi.CS_ABI_VERSION if hasattr(abi, "CS_ABI_VERSION") else 1
+    assert L.cs_abi_version() == abi.CS_ABI_VERSION
+    # benchmark support lives in its own library, never in the product one
+    B = rt.bench_lib()
+    bench = declared_functions("cs_bench.h")
+    assert bench and all(hasattr(B, n) for n in bench)
+    assert not any(hasattr(L, n) for n in bench)
 
 
 def test_status_strings_match_reference_error_types():

@@ -10,7 +10,7 @@ buf.fill_(1)
 torch.cuda.synchronize()
 def run(v, p0, p1, p2):
     ms = C.c_double()
-    rc = L.cs_microbench(v, C.c_void_p(buf.data_ptr()), nbytes, p0, p1, p2, 5, C.byref(ms))
+    rc = rt.bench_lib().cs_microbench(v, C.c_void_p(buf.data_ptr()), nbytes, p0, p1, p2, 5, C.byref(ms))
     return rc, ms.value, nbytes / ms.value / 1e6
 for cfg in [(0, 4, 256, 8), (0, 8, 256, 8), (0, 2, 512, 8), (0, 8, 256, 1), (0, 16, 256, 1)]:
     print("LDG ctas/sm,threads,unroll", cfg[1:], "-> rc %d %.3f ms %.0f GB/s" % run(*cfg))
