@@ -1030,14 +1030,14 @@ double ref_cpu_fit_seconds(void* h) { return static_cast<CpuBaseline*>(h)->fit_s
 void ref_cpu_free(void* h) { delete static_cast<CpuBaseline*>(h); }
 
 // Returns wall seconds of one timed pass over all prepared instances.
-// Cycle-aligned slices of ONE trace (the GPU arm's benchmarked instance), one
+// Cycle-aligned slices [slice_lo[k], slice_hi[k]) of ONE trace (the GPU arm's benchmarked instance), one
 // reference Trace per slice built on n_threads threads; every slice is
 // analysed with the whole trace's anchor (anchor_hint) and one model.
 void* ref_cpu_prepare_slices(uint64_t n, const cs_event* ev, const uint64_t* event_ids, uint32_t n_names,
                              const char* names_packed, const cs_workload* wl, uint32_t n_comm,
                              const char* comm_hash_packed, const int32_t* comm_rank, uint32_t n_slices,
-                             const uint64_t* bounds, const char* model_json, const char* anchor_hint,
-                             uint32_t n_threads) {
+                             const uint64_t* slice_lo, const uint64_t* slice_hi, const char* model_json,
+                             const char* anchor_hint, uint32_t n_threads) {
   auto* cb = new CpuBaseline();
   cb->inst.resize(n_slices);
   cb->anchor_hint = anchor_hint ? anchor_hint : "";
@@ -1047,7 +1047,7 @@ void* ref_cpu_prepare_slices(uint64_t n, const cs_event* ev, const uint64_t* eve
   for (uint32_t t = 0; t < std::max(1u, n_threads); ++t)
     th.emplace_back([&, t] {
       for (uint32_t i = t; i < n_slices; i += std::max(1u, n_threads)) {
-        const uint64_t lo = bounds[i], hi = std::min<uint64_t>(bounds[i + 1], n);
+        const uint64_t lo = std::min<uint64_t>(slice_lo[i], n), hi = std::min<uint64_t>(slice_hi[i], n);
         cb->inst[i].reset(static_cast<Handle*>(ref_build(hi - lo, ev + lo, event_ids ? event_ids + lo : nullptr,
                                                          n_names, names_packed, wl, n_comm, comm_hash_packed,
                                                          comm_rank, 0)));

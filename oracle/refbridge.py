@@ -83,7 +83,7 @@ def lib():
                                       C.c_uint64]
         L.ref_cpu_prepare_slices.restype = vp
         L.ref_cpu_prepare_slices.argtypes = [C.c_uint64, vp, vp, C.c_uint32, C.c_char_p, vp, C.c_uint32,
-                                             C.c_char_p, vp, C.c_uint32, vp, C.c_char_p, C.c_char_p,
+                                             C.c_char_p, vp, C.c_uint32, vp, vp, C.c_char_p, C.c_char_p,
                                              C.c_uint32]
         L.ref_cpu_events.restype = C.c_uint64
         L.ref_cpu_events.argtypes = [vp]
@@ -390,24 +390,27 @@ class CpuBaseline:
         self.fit_seconds = lib().ref_cpu_fit_seconds(self.h)
 
     @classmethod
-    def slices(cls, events, event_ids, names, workloads, comm_hash, comm_rank, bounds, model_json,
+    def slices(cls, events, event_ids, names, workloads, comm_hash, comm_rank, lo, hi, model_json,
                anchor, n_threads):
-        """Cycle-aligned slices [bounds[k], bounds[k+1]) of ONE trace, one
-        reference Trace each (analysed on its own thread with `anchor` as the
-        hint and one model)."""
+        """Cycle-aligned slices [lo[k], hi[k]) of ONE trace, one reference
+        Trace each (analysed on its own thread with `anchor` as the hint and
+        one model)."""
         self = cls.__new__(cls)
         self.n_threads = n_threads
         ev = np.ascontiguousarray(events, dtype=abi.EVENT_DTYPE)
-        ids = np.ascontiguousarray(event_ids, dtype=np.uint64)
+        ids = None if event_ids is None else np.ascontiguousarray(event_ids, dtype=np.uint64)
         wl = np.ascontiguousarray(workloads, dtype=abi.WORKLOAD_DTYPE)
-        b = np.ascontiguousarray(bounds, dtype=np.uint64)
+        lo = np.ascontiguousarray(lo, dtype=np.uint64)
+        hi = np.ascontiguousarray(hi, dtype=np.uint64)
         packed = b"".join(n.encode() + b"\0" for n in names)
         cpacked = b"".join(c.encode() + b"\0" for c in comm_hash) or b"\0"
         crank = np.ascontiguousarray(np.asarray(comm_rank, dtype=np.int32))
-        self.h = lib().ref_cpu_prepare_slices(len(ev), ev.ctypes.data, ids.ctypes.data, len(names), packed,
+        self.h = lib().ref_cpu_prepare_slices(len(ev), ev.ctypes.data, None if ids is None else ids.ctypes.data,
+                                              len(names), packed,
                                               wl.ctypes.data, len(comm_hash), cpacked,
-                                              crank.ctypes.data if len(crank) else None, len(b) - 1,
-                                              b.ctypes.data, model_json.encode(), anchor.encode(), n_threads)
+                                              crank.ctypes.data if len(crank) else None, len(lo),
+                                              lo.ctypes.data, hi.ctypes.data, model_json.encode(),
+                                              anchor.encode(), n_threads)
         self.events = int(lib().ref_cpu_events(self.h))
         self.fit_seconds = 0.0
         return self
