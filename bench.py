@@ -390,7 +390,7 @@ def run_ours(args, rank, world, local_rank):
     del events
 
     an = rt.Analyzer(dev)
-    an.set_fused(os.environ.get("CS_BENCH_FUSED", "1") != "0")
+    an.set_fused(os.environ.get("CS_BENCH_FUSED", "0") != "0")
     span = rt.span_names_mask(pin_ev, len(names))
     an.configure(names, span, n_comm_slots=n_comm)
     an.upload(pin_ev, offs, pin_wl)

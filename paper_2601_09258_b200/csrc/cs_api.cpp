@@ -168,6 +168,7 @@ struct cs_ctx {
   uint64_t n_extra_refs = 0;
   DevBuf d_extra_refs, d_extra_vals, d_rec_extra, d_rec_extra_has;
   DevBuf d_stage2, d_stage_changed, d_stage_lb, d_stage_ctl;  // k_stage_jacobi
+  DevBuf d_any_unknown;
   // counter-weighted mu: metric slots derived from the name table
   uint32_t n_metrics = 0;
   DevBuf d_series_slot, d_class_metric, d_m_off, d_s_ts, d_s_val, d_mu, d_mu_has;
@@ -360,6 +361,7 @@ DevBuffers make_buffers(cs_ctx* ctx) {
   b.c_mu = static_cast<double*>(ctx->d_mu.p);
   b.c_mu_has = static_cast<uint8_t*>(ctx->d_mu_has.p);
   b.stream = ctx->streaming ? static_cast<StreamCarry*>(ctx->d_stream[ctx->stream_cur].p) : nullptr;
+  b.any_unknown = static_cast<unsigned int*>(ctx->d_any_unknown.p);
   b.extra_refs = static_cast<const cs_extra_ref*>(ctx->d_extra_refs.p);
   b.n_extra_refs = ctx->n_extra_refs;
   b.extra_vals = static_cast<const cs_extra_value*>(ctx->d_extra_vals.p);
@@ -1008,9 +1010,8 @@ struct NvtxRun {
 };
 
 // Ranges of the single-read segmentation: consecutive events of one instance,
-// about one cycle per thread of the CTA each (the thread-per-cycle reduce then
-// keeps every thread busy), multiples of 256 events, built once per upload and
-// range size.
+// about one cycle per lane of the warp that takes the range (the lane-per-cycle
+// reduce then keeps every lane busy), built once per upload and range size.
 int build_ranges(cs_ctx* ctx, uint64_t range_events) {
   if (ctx->ranges_built_for == range_events) return CS_OK;
   const uint32_t n_inst = ctx->n_inst;
@@ -1162,6 +1163,8 @@ static int cs_run_impl(cs_ctx* ctx, uint32_t mask) {
     return fail(ctx, CS_E_CUDA, "cudaMalloc(state)");
   CS_CUDA(cudaMemcpyAsync(d_inst, ctx->h_inst.data(), n_inst * sizeof(InstState),
                           cudaMemcpyHostToDevice, s));
+  if (!dev<unsigned int>(ctx->d_any_unknown, 1)) return fail(ctx, CS_E_CUDA, "cudaMalloc(flag)");
+  CS_CUDA(cudaMemsetAsync(ctx->d_any_unknown.p, 0, 4, s));
   const size_t stats_bytes = static_cast<size_t>(n_inst) * n_names * sizeof(NameStat);
   const size_t nt = ctx->tile_inst.size();
   DevConfig cfg{ctx->cyc, ctx->ctl, 0.0};
@@ -1259,7 +1262,7 @@ static int cs_run_impl(cs_ctx* ctx, uint32_t mask) {
       const double epc = ctx->ev_per_cycle > 0.0 ? ctx->ev_per_cycle : 16.0;
       range_events = static_cast<uint64_t>(epc * kSegCycles);
     }
-    range_events = std::min<uint64_t>(std::max<uint64_t>((range_events + 255) / 256 * 256, 1024), 65536);
+    range_events = std::min<uint64_t>(std::max<uint64_t>((range_events + 31) / 32 * 32, 128), 65536);
     const int rc = build_ranges(ctx, range_events);
     if (rc != CS_OK) return rc;
   }

@@ -158,6 +158,7 @@ struct DevBuffers {
   double* c_mu;                 // n_cycles x n_beta
   uint8_t* c_mu_has;
   StreamCarry* stream;          // per instance, null when not streaming
+  unsigned int* any_unknown;    // set by the reduces when any cycle's local stage is Unknown
   // record extras (cs_upload_extras): side table sorted by event, and the
   // per-record values / presence (n_records x n_extra_keys)
   const cs_extra_ref* extra_refs;
@@ -187,7 +188,7 @@ struct SegMeta {
   uint32_t prefetch_bytes;       // L2 bulk prefetch of the next claimed range (0 = off)
 };
 constexpr int32_t kHoleWl = -3;
-constexpr uint64_t kSegCycles = 224;  // target cycles per range (CTA of 256 threads)
+constexpr uint64_t kSegCycles = 30;  // target cycles per range (one warp, one cycle per lane)
 
 // launchers (cs_kernels.cu); all asynchronous on `s`
 void launch_scan_events(const DevBuffers& b, const DevConfig& cfg, int mode, bool sample,

@@ -1848,7 +1848,10 @@ __global__ void __launch_bounds__(256, 3) k_cycle_reduce_v2(DevBuffers b, DevCon
   const bool unk = live && stage == CS_STAGE_UNKNOWN;
   const uint32_t inst = unk ? b.c_inst[g] : 0xffffffffu;
   const uint32_t grp = __match_any_sync(0xffffffffu, inst);
-  if (unk && (tid & 31) == (uint32_t)(__ffs(grp) - 1)) atomicAdd(&b.inst[inst].n_unknown, (u64)__popc(grp));
+  if (unk && (tid & 31) == (uint32_t)(__ffs(grp) - 1)) {
+    atomicAdd(&b.inst[inst].n_unknown, (u64)__popc(grp));
+    *b.any_unknown = 1u;
+  }
 }
 
 // ------------------------------ K3w thread-per-cycle reduce, any slot count
@@ -1927,7 +1930,10 @@ __global__ void __launch_bounds__(128) k_cycle_reduce_wide(DevBuffers b, DevConf
   b.c_local[g] = stage;
   b.c_stage[g] = stage;
   b.c_wl[g] = wl;
-  if (stage == CS_STAGE_UNKNOWN) atomicAdd(&b.inst[b.c_inst[g]].n_unknown, 1ull);
+  if (stage == CS_STAGE_UNKNOWN) {
+    atomicAdd(&b.inst[b.c_inst[g]].n_unknown, 1ull);
+    *b.any_unknown = 1u;
+  }
 }
 
 // beta = total / cycle duration for every (cycle, class) of the wide reduce
@@ -2581,6 +2587,12 @@ __global__ void __launch_bounds__(kStageWarps * 32)
   const u64 min_hist = cfg.cyc.stage_min_history;
   double* mine = s_win + (u64)warp * 4 * W;
   const uint32_t gw = blockIdx.x * kStageWarps + warp, nw = gridDim.x * kStageWarps;
+  // no Unknown cycle anywhere (the common forward_mode case): nothing to do;
+  // every CTA reads the same flag, so none waits at a barrier
+  if (__ldcg(b.any_unknown) == 0u) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) *m.final_parity = 0;
+    return;
+  }
   for (int it = 0; it < m.max_iter; ++it) {
     const uint8_t* in = m.st[it & 1];
     uint8_t* out = m.st[(it + 1) & 1];
@@ -2857,21 +2869,23 @@ void launch_freq_cycles(const cs_event* ev, uint64_t begin, uint64_t end, int64_
 
 
 // =================================================== single-read segmentation
-// K1+K2+K3 with the events read from DRAM once (CS_OPT_FUSED).  Ranges of up
-// to kRangeTiles instance-aligned tiles (<= 4096 events, 128 KiB) are claimed
-// in order by a persistent grid; per range:
-//   A. the CTA's warps stream the range (coalesced 256-bit loads) exactly like
-//      k_scan_warp: PythonCall moments for the anchor ranking (cycles.cpp:
-//      50-59), the canonical-order check, and the speculated anchor's
-//      occurrences compacted per warp (cycles.cpp:127-131);
-//   B. the range's anchor count is published and a decoupled look-back over
-//      the preceding ranges gives the global rank of its first anchor = the
-//      cycle slot of the cycle that anchor opens; one warp meanwhile finds the
-//      next anchor after the range (the end of the range's last cycle);
-//   C. one thread per cycle walks its events in order -- now L2 hits, the CTA
-//      has just streamed them -- with k_cycle_reduce_v2's accumulators and
-//      arithmetic (cycles.cpp:157-166, 205-229, 256-281; rca.cpp:87-129), and
-//      the CTA writes the cycle rows at their slots.
+// K1+K2+K3 with the events read from DRAM once (CS_OPT_FUSED).  Work unit: a
+// WARP RANGE of consecutive events of one instance, sized for ~32 cycles (one
+// per lane), claimed in order by a persistent grid.  Every warp is independent
+// (no CTA barriers), so one warp's DRAM-bound scan overlaps its neighbours'
+// L2-bound reduce.  Per range:
+//   A. the warp streams its events (coalesced 256-bit loads): PythonCall
+//      moments for the anchor ranking (cycles.cpp:50-59), the canonical-order
+//      check, and the speculated anchor's occurrences compacted in order
+//      (cycles.cpp:127-131); it publishes its anchor count and keeps reading
+//      past the range to the next anchor, which closes its last cycle;
+//   B. lane k reduces the cycle opened by anchor k, walking its events in
+//      order -- L2 hits, the warp has just streamed them -- with the
+//      accumulators and arithmetic of k_cycle_reduce_v2 (cycles.cpp:157-166,
+//      205-229, 256-281; rca.cpp:87-129);
+//   C. a decoupled look-back over the preceding ranges gives the global rank
+//      of the range's first anchor = the slot of its first cycle, and the warp
+//      writes its cycle rows.
 // An instance's last anchor opens no complete cycle (cycles.cpp:147): its slot
 // is a hole (empty event range, c_wl = kHoleWl) that every consumer skips.
 // The anchor guess is verified afterwards by k_rank over the full moments; a
@@ -2879,41 +2893,34 @@ void launch_freq_cycles(const cs_event* ev, uint64_t begin, uint64_t end, int64_
 constexpr int kSegThreads = 256;
 constexpr int kSegWarps = kSegThreads / 32;
 
-__device__ __forceinline__ void bulk_prefetch_l2(const void* p, uint32_t bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
-}
-
 __global__ void __launch_bounds__(kSegThreads, 2)
     k_segment_range(DevBuffers b, DevConfig cfg, SegMeta sm, int do_beta) {
-  extern __shared__ __align__(16) unsigned char s_red[];
+  extern __shared__ __align__(16) unsigned char s_dyn[];
   __shared__ uint32_t s_ninfo[kFNamesSmem];
   __shared__ WarpNameRow s_rows[kSegWarps * kWarpNameRows];
   __shared__ uint32_t s_pn[kSegWarps][64];
   __shared__ i64 s_pd[kSegWarps][64];
-  __shared__ uint32_t s_wbase[kSegWarps + 1];
-  __shared__ u64 s_sub0[kSegWarps];
-  __shared__ uint32_t s_ticket[1];
-  __shared__ u64 s_prefix;
-  __shared__ i64 s_next_start;
-  __shared__ u64 s_next_first;
-  __shared__ int s_next_found;
   const int P = cfg.cyc.n_phases;
   const int C = do_beta ? cfg.cyc.n_beta_slots : 0;
   const int R = do_beta ? cfg.cyc.n_comm_slots : 0;
-  const uint32_t NT = blockDim.x, tid = threadIdx.x;
-  const int lane = tid & 31, warp = tid >> 5;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   auto pack_info = [&](const cs_name_info& ni) -> uint32_t {
     const uint32_t ph = (ni.phase >= 0 && ni.phase < P) ? (uint32_t)ni.phase : 15u;
     const uint32_t bs = (ni.beta_slot >= 0 && ni.beta_slot < C) ? (uint32_t)ni.beta_slot : 255u;
     return ph | (bs << 4) | ((ni.flags & 3u) << 12);
   };
-  for (uint32_t i = tid; i < b.n_names && i < (uint32_t)kFNamesSmem; i += NT) s_ninfo[i] = pack_info(b.names[i]);
-  const uint32_t SN = NT + 1;
-  i64* comp = reinterpret_cast<i64*>(s_red);                         // [P][SN]
-  i64* beta = comp + (u64)P * SN;                                    // [C][SN]
-  double* coll = reinterpret_cast<double*>(beta + (u64)C * SN);      // [R][SN]
-  i64* s_dur = reinterpret_cast<i64*>(coll + (u64)R * SN);           // [NT]
-  uint32_t* colln = reinterpret_cast<uint32_t*>(s_dur + NT);         // [R][SN]
+  for (uint32_t i = threadIdx.x; i < b.n_names && i < (uint32_t)kFNamesSmem; i += blockDim.x)
+    s_ninfo[i] = pack_info(b.names[i]);
+  __syncthreads();  // the only CTA barrier: warps are independent from here on
+  // per-warp [slot][lane] accumulator columns (row stride 33)
+  const uint32_t SN = 33;
+  const uint32_t words = (uint32_t)(P + C + R) * SN * 2 + (uint32_t)R * SN + 64;  // 4-byte words
+  uint32_t* wbase = reinterpret_cast<uint32_t*>(s_dyn) + (u64)warp * words;
+  i64* comp = reinterpret_cast<i64*>(wbase);
+  i64* beta = comp + (u64)P * SN;
+  double* coll = reinterpret_cast<double*>(beta + (u64)C * SN);
+  i64* s_dur = reinterpret_cast<i64*>(coll + (u64)R * SN);     // [32]
+  uint32_t* colln = reinterpret_cast<uint32_t*>(s_dur + 32);    // [R][SN]
   WarpNameRow* wrows = s_rows + warp * kWarpNameRows;
   uint32_t* pn = s_pn[warp];
   i64* pd = s_pd[warp];
@@ -2940,30 +2947,10 @@ __global__ void __launch_bounds__(kSegThreads, 2)
     npend = rest;
     __syncwarp();
   };
-  auto anchor_idx = [&](uint32_t k) -> u64 {
-    int w = 0;
-#pragma unroll
-    for (int x = 1; x < kSegWarps; ++x) w += (k >= s_wbase[x]) ? 1 : 0;
-    return s_sub0[w] + (k - s_wbase[w]);
-  };
-  // the range one round of the grid ahead (gridDim.x tickets) is prefetched
-  // into L2 by a TMA bulk prefetch (no registers, no waiting): its DRAM read
-  // overlaps this range's work and whichever CTA claims it scans from L2
-  auto prefetch = [&](uint32_t rr) {
-    if (rr >= sm.n_ranges || sm.prefetch_bytes == 0) return;
-    const u64 rb = sm.range_begin[rr], re = sm.range_end[rr];
-    const u64 bytes = min((re - rb) * (u64)sizeof(cs_event), (u64)sm.prefetch_bytes);
-    const char* base = reinterpret_cast<const char*>(b.ev + rb);
-    for (u64 o = (u64)lane * 4096; o < bytes; o += 32 * 4096)
-      bulk_prefetch_l2(base + o, (uint32_t)min((u64)4096, bytes - o));
-  };
-  if (warp == 0) prefetch(blockIdx.x);  // the first round
   for (;;) {
-    __syncthreads();  // previous range's shared state fully consumed
-    if (tid == 0) s_ticket[0] = atomicAdd(sm.ticket, 1u);
-    __syncthreads();
-    const uint32_t r = s_ticket[0];
-    if (warp == 0) prefetch(r + gridDim.x);
+    uint32_t r = 0;
+    if (lane == 0) r = atomicAdd(sm.ticket, 1u);
+    r = __shfl_sync(0xffffffffu, r, 0);
     if (r >= sm.n_ranges) break;
     const u64 rb = sm.range_begin[r], re = sm.range_end[r];
     const uint32_t inst = sm.range_inst[r];
@@ -2977,20 +2964,17 @@ __global__ void __launch_bounds__(kSegThreads, 2)
       cur_inst = inst;
       gstats = b.stats + (u64)inst * b.n_names;
     }
-    // ---------------- A: scan the warp's sub-block
-    const u64 n = re - rb;
-    const u64 chunk = ((n + kSegWarps * 32 - 1) / (kSegWarps * 32)) * 32;
-    const u64 sb = rb + min((u64)warp * chunk, n), se = rb + min((u64)(warp + 1) * chunk, n);
-    const uint32_t nsub = (uint32_t)(se - sb);
+    // ---------------- A: stream the range
+    const uint32_t n = (uint32_t)(re - rb);
     uint32_t cnt = 0;
-    i64 carry_ts = sb > ib ? b.ev[sb - 1].start_ts : LLONG_MIN;
-    bool unsorted = false;
-    for (uint32_t j0 = 0; j0 < nsub; j0 += 32 * kScanUnroll) {
+    i64 carry_ts = LLONG_MIN;  // the range's first pair is checked by k_tile_order-like look at rb-1 below
+    bool unsorted = rb > ib && b.ev[rb - 1].start_ts > b.ev[rb].start_ts;
+    for (uint32_t j0 = 0; j0 < n; j0 += 32 * kScanUnroll) {
       Ev8 e[kScanUnroll];
 #pragma unroll
       for (int q = 0; q < kScanUnroll; ++q) {
         const uint32_t j = j0 + q * 32 + lane;
-        if (j < nsub) e[q] = ldg256(b.ev + sb + j);
+        if (j < n) e[q] = ldg256(b.ev + rb + j);
         else {
           e[q].a = ~0ull >> 1;
           e[q].c = (u64)CS_FLOW << 32;
@@ -3018,9 +3002,9 @@ __global__ void __launch_bounds__(kSegThreads, 2)
         carry_ts = (i64)__shfl_sync(0xffffffffu, e[q].a, 31);
         if (is_anchor) {
           const uint32_t jj = j0 + q * 32 + lane;
-          const u64 ai = sb + cnt + __popc(mk & lanemask_lt());
-          const bool walk = jj == 0 ? sb > ib : (lane == 0 || prev == e[q].a);
-          b.a_pos[ai] = (sb + jj) | (walk ? kWalk : 0ull);
+          const u64 ai = rb + cnt + __popc(mk & lanemask_lt());
+          const bool walk = jj == 0 ? rb > ib : (lane == 0 || prev == e[q].a);
+          b.a_pos[ai] = (rb + jj) | (walk ? kWalk : 0ull);
           b.a_start[ai] = (i64)e[q].a;
           b.a_end[ai] = (i64)e[q].a + (i64)e[q].b;
         }
@@ -3028,15 +3012,20 @@ __global__ void __launch_bounds__(kSegThreads, 2)
       }
     }
     if (__any_sync(0xffffffffu, unsorted) && lane == 0) atomicOr(&b.inst[inst].unsorted, 1u);
+    const uint32_t A = cnt;
     if (lane == 0) {
-      s_wbase[warp + 1] = cnt;
-      s_sub0[warp] = sb;
+      if (r == 0) {
+        st_release(&sm.lb_state[0], kFlagPrefix | (u64)A);
+        sm.range_prefix[0] = 0;
+      } else {
+        st_release(&sm.lb_state[r], kFlagAgg | (u64)A);
+      }
     }
-    // the last warp continues past the range: the next anchor closes the
-    // range's last cycle
-    if (warp == kSegWarps - 1) {
-      int found = 0;
-      i64 nstart = 0;
+    // the next anchor after the range closes its last cycle
+    int next_found = 0;
+    i64 next_start = 0;
+    u64 next_first = 0;
+    if (A > 0) {
       u64 npos = 0;
       for (u64 p0 = re; p0 < ie; p0 += 32) {
         const u64 p = p0 + lane;
@@ -3050,36 +3039,19 @@ __global__ void __launch_bounds__(kSegThreads, 2)
         const uint32_t bm = __ballot_sync(0xffffffffu, m);
         if (bm) {
           const int L = __ffs(bm) - 1;
-          nstart = __shfl_sync(0xffffffffu, st, L);
+          next_start = __shfl_sync(0xffffffffu, st, L);
           npos = p0 + L;
-          found = 1;
+          next_found = 1;
           break;
         }
       }
-      if (lane == 0) {
-        s_next_found = found;
-        s_next_start = nstart;
-        s_next_first = found ? group_start(b.ev, npos, ib, nstart) : 0;
-      }
+      if (next_found) next_first = group_start(b.ev, npos, ib, next_start);
     }
-    __syncthreads();
-    if (tid == 0) {
-      s_wbase[0] = 0;
-      for (int w = 1; w <= kSegWarps; ++w) s_wbase[w] += s_wbase[w - 1];
-      const u64 A = s_wbase[kSegWarps];
-      if (r == 0) {
-        st_release(&sm.lb_state[0], kFlagPrefix | A);
-        s_prefix = 0;
-        sm.range_prefix[0] = 0;
-      } else {
-        st_release(&sm.lb_state[r], kFlagAgg | A);
-      }
-    }
-    __syncthreads();
-    const uint32_t A = s_wbase[kSegWarps];
-    // ---------------- C: thread per cycle over the range's anchors
-    for (uint32_t k0 = 0; k0 == 0 || k0 < A; k0 += NT) {
-      const uint32_t k = k0 + tid;
+    // ---------------- B + C: lane per cycle, 32 cycles per round
+    u64 base = 0;
+    bool have_base = r == 0;
+    for (uint32_t k0 = 0; k0 == 0 || k0 < A; k0 += 32) {
+      const uint32_t k = k0 + lane;
       const bool live = k < A;
       uint8_t stage = CS_STAGE_UNKNOWN;
       bool hole = false;
@@ -3087,33 +3059,32 @@ __global__ void __launch_bounds__(kSegThreads, 2)
       u64 apos = 0, first = 0, last = 0;
       int32_t wl = -1;
       if (live) {
-        const u64 ai = anchor_idx(k);
+        const u64 ai = rb + k;
         cs = b.a_start[ai];
         aend = b.a_end[ai];
         const u64 pw = b.a_pos[ai];
         apos = pw & ~kWalk;
         first = (pw & kWalk) ? group_start(b.ev, apos, ib, cs) : apos;
         if (k + 1 < A) {
-          const u64 an = anchor_idx(k + 1);
-          ce = b.a_start[an];
-          const u64 pw2 = b.a_pos[an];
+          ce = b.a_start[ai + 1];
+          const u64 pw2 = b.a_pos[ai + 1];
           const u64 p2 = pw2 & ~kWalk;
           last = (pw2 & kWalk) ? group_start(b.ev, p2, ib, ce) : p2;
-        } else if (s_next_found) {
-          ce = s_next_start;
-          last = s_next_first;
+        } else if (next_found) {
+          ce = next_start;
+          last = next_first;
         } else {
           hole = true;  // the instance's last anchor: trailing partial cycle dropped
           ce = cs;
           last = first;
         }
         const i64 dur = ce - cs;
-        s_dur[tid] = dur;
-        for (int p = 0; p < P; ++p) comp[p * SN + tid] = 0;
-        for (int c = 0; c < C; ++c) beta[c * SN + tid] = 0;
+        s_dur[lane] = dur;
+        for (int p = 0; p < P; ++p) comp[p * SN + lane] = 0;
+        for (int c = 0; c < C; ++c) beta[c * SN + lane] = 0;
         for (int q = 0; q < R; ++q) {
-          coll[q * SN + tid] = 0.0;
-          colln[q * SN + tid] = 0u;
+          coll[q * SN + lane] = 0.0;
+          colln[q * SN + lane] = 0u;
         }
         uint32_t fm_cls = 0, kw = 0;
         bool fm_found = false, batch_found = false;
@@ -3145,14 +3116,14 @@ __global__ void __launch_bounds__(kSegThreads, 2)
             const i64 clipped = (end < ce ? end : ce) - st;
             if (clipped <= 0) continue;
             const uint32_t ph = info & 15u, bs = (info >> 4) & 255u;
-            if (ph != 15u) comp[ph * SN + tid] += clipped;
+            if (ph != 15u) comp[ph * SN + lane] += clipped;
             if (do_beta && d > 0) {
-              if (bs != 255u) beta[bs * SN + tid] += clipped;
+              if (bs != 255u) beta[bs * SN + lane] += clipped;
               if (((kc >> 8) & 0xffu) == CS_CAT_COLLECTIVE_COMM && (flags & CS_EV_HAS_COMM)) {
                 const uint32_t slot = (uint32_t)(e[q].d >> 32);
                 if (slot < (uint32_t)R) {
-                  coll[slot * SN + tid] = __dadd_rn(coll[slot * SN + tid], __ddiv_rn((double)clipped, (double)dur));
-                  colln[slot * SN + tid] += 1u;
+                  coll[slot * SN + lane] = __dadd_rn(coll[slot * SN + lane], __ddiv_rn((double)clipped, (double)dur));
+                  colln[slot * SN + lane] += 1u;
                 }
               }
             }
@@ -3163,10 +3134,9 @@ __global__ void __launch_bounds__(kSegThreads, 2)
         const bool pkw = kw & CS_NAME_PREFILL_KW, dkw = kw & CS_NAME_DECODE_KW;
         if (stage == CS_STAGE_UNKNOWN && pkw != dkw) stage = pkw ? CS_STAGE_PREFILL : CS_STAGE_DECODE;
       }
-      // the slot base: decoupled look-back over the preceding ranges, resolved
-      // by warp 0 after its share of the reduce (predecessors have long since
-      // published their counts)
-      if (k0 == 0 && warp == 0 && r > 0) {
+      // slot base: decoupled look-back over the preceding ranges (they
+      // published their counts long ago, when their scans finished)
+      if (!have_base) {
         u64 excl = 0;
         long long j = (long long)r - 1;
         for (;;) {
@@ -3185,20 +3155,21 @@ __global__ void __launch_bounds__(kSegThreads, 2)
           excl += warp_sum_u64(val);
           j -= 32;
         }
+        base = excl;
+        have_base = true;
         if (lane == 0) {
-          s_prefix = excl;
           sm.range_prefix[r] = excl;
           st_release(&sm.lb_state[r], kFlagPrefix | (excl + A));
         }
       }
-      const bool unk = live && !hole && stage == CS_STAGE_UNKNOWN;
-      const uint32_t um = __ballot_sync(0xffffffffu, unk);
-      if (lane == 0 && um) atomicAdd(&b.inst[inst].n_unknown, (u64)__popc(um));
-      __syncthreads();
-      const u64 base = s_prefix;
+      const uint32_t um = __ballot_sync(0xffffffffu, live && !hole && stage == CS_STAGE_UNKNOWN);
+      if (lane == 0 && um) {
+        atomicAdd(&b.inst[inst].n_unknown, (u64)__popc(um));
+        *b.any_unknown = 1u;
+      }
       if (base + A > sm.cap) {
-        if (tid == 0) atomicOr(sm.overflow, 1u);
-        break;  // CTA-uniform
+        if (lane == 0) atomicOr(sm.overflow, 1u);
+        break;  // warp-uniform
       }
       if (live) {
         const u64 g = base + k;
@@ -3213,26 +3184,27 @@ __global__ void __launch_bounds__(kSegThreads, 2)
         b.c_stage[g] = hole ? (uint8_t)3 : stage;
         b.c_wl[g] = hole ? kHoleWl : wl;
       }
+      __syncwarp();
       const u64 g0 = base + k0;
-      const uint32_t n_live = A > k0 ? min((uint32_t)NT, A - k0) : 0u;
-      for (uint32_t idx = tid; idx < n_live * (uint32_t)P; idx += NT) {
+      const uint32_t n_live = A > k0 ? min(32u, A - k0) : 0u;
+      for (uint32_t idx = lane; idx < n_live * (uint32_t)P; idx += 32) {
         const uint32_t lc = idx / (uint32_t)P, p = idx - lc * (uint32_t)P;
         b.c_comp[g0 * P + idx] = comp[p * SN + lc];
       }
-      for (uint32_t idx = tid; idx < n_live * (uint32_t)C; idx += NT) {
+      for (uint32_t idx = lane; idx < n_live * (uint32_t)C; idx += 32) {
         const uint32_t lc = idx / (uint32_t)C, c = idx - lc * (uint32_t)C;
         const i64 dur = s_dur[lc];
         const i64 t = dur > 0 ? beta[c * SN + lc] : 0;
         b.c_beta_tot[g0 * C + idx] = t;
         b.c_beta[g0 * C + idx] = t > 0 ? __ddiv_rn((double)t, (double)dur) : 0.0;
       }
-      for (uint32_t idx = tid; idx < n_live * (uint32_t)R; idx += NT) {
+      for (uint32_t idx = lane; idx < n_live * (uint32_t)R; idx += 32) {
         const uint32_t lc = idx / (uint32_t)R, q = idx - lc * (uint32_t)R;
         b.c_coll[g0 * R + idx] = coll[q * SN + lc];
         const uint32_t cn = colln[q * SN + lc];
         b.c_coll_n[g0 * R + idx] = (uint8_t)(cn > 255u ? 255u : cn);
       }
-      __syncthreads();
+      __syncwarp();
     }
   }
   if (cur_inst != 0xffffffffu) {
@@ -3261,8 +3233,8 @@ int segment_range_smem(const DevConfig& cfg, int do_beta) {
   const int C = do_beta ? cfg.cyc.n_beta_slots : 0;
   const int R = do_beta ? cfg.cyc.n_comm_slots : 0;
   if (P > 15 || C > 254) return -1;
-  const int per_thread = (P + C + R) * 8 + R * 4;
-  const int smem = (kSegThreads + 1) * per_thread + kSegThreads * 8;
+  const int words = (P + C + R) * 33 * 2 + R * 33 + 64;  // per warp (k_segment_range)
+  const int smem = kSegWarps * words * 4;
   return smem <= 96 * 1024 ? smem : -1;
 }
 
