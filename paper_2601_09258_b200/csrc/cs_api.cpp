@@ -1195,7 +1195,7 @@ static int cs_run_impl(cs_ctx* ctx, uint32_t mask) {
            dev<double>(ctx->rec_pred, nc1) && dev<double>(ctx->rec_resid, nc1) &&
            dev<double>(ctx->rec_stat, nc1) && dev<uint8_t>(ctx->rec_flags, nc1) &&
            dev<uint64_t>(ctx->alert_rec, nc1) && dev<uint64_t>(ctx->d_alert_off, n_inst + 1) &&
-           dev<uint64_t>(ctx->block_tmp, nc1 / 1024 + 16);
+           dev<uint64_t>(ctx->block_tmp, nc1 / 256 + 16);
   };
   ctx->n_cyc.assign(n_inst, 0);
   int e1 = -1, e2 = -1, e4 = -1, e5 = -1;
@@ -1631,7 +1631,7 @@ static int cs_run_impl(cs_ctx* ctx, uint32_t mask) {
     ctx->mt_valid = true;
     }  // rebuild
     b = make_buffers(ctx);
-    if (!dev<uint64_t>(ctx->block_tmp, rec_cap / 1024 + 16))
+    if (!dev<uint64_t>(ctx->block_tmp, rec_cap / 256 + 16))
       return fail(ctx, CS_E_CUDA, "cudaMalloc(block_tmp)");
     b = make_buffers(ctx);
     launch_score(b, cfg, rec_cap, ctx->rec_off.data(), ctx->model_of_inst.data(),
@@ -2423,7 +2423,7 @@ int cs_detect_residuals(cs_ctx* ctx, const double* residuals, uint64_t n, const 
   if (!dev<double>(d.resid, n1) || !dev<double>(d.stat, n1) || !dev<uint8_t>(d.flags, n1) ||
       !dev<uint64_t>(d.rec_off, 2) || !dev<uint64_t>(d.rec_cycle, n1) || !dev<uint64_t>(d.cyc_off, 2) ||
       !dev<uint64_t>(d.alert_rec, n1) || !dev<uint64_t>(d.alert_off, 2) ||
-      !dev<uint64_t>(d.block_tmp, n1 / 1024 + 16) || !dev<InstState>(d.inst, 1) ||
+      !dev<uint64_t>(d.block_tmp, n1 / 256 + 16) || !dev<InstState>(d.inst, 1) ||
       !dev<DevModel>(d.model, 1) || !dev<uint8_t>(d.labels, n1) || !dev<unsigned long long>(d.out, 8))
     return fail(ctx, CS_E_CUDA, "cudaMalloc(detect)");
   const uint64_t off[2] = {0, n};

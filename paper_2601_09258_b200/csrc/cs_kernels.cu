@@ -1328,7 +1328,7 @@ __global__ void __launch_bounds__(kLutThreads)
 //   armed_t = t >= warmup;  flagged_t = armed_t && stat_t > limit
 //   alert_t = flagged_t && !flagged_{t-1}   (in_episode == flagged_{t-1})
 // Episode id = alerts before t in the instance (exclusive scan).
-constexpr int kDetBlock = 1024;
+constexpr int kDetBlock = 256;  // 6 CTAs/SM at 40 registers (1024-thread CTAs: 1, half occupancy)
 
 __device__ __forceinline__ double window_stat(const double* e, u64 t, u64 W, int strategy) {
   if (strategy == CS_FIXED_POINT) return e[t];
@@ -1400,7 +1400,7 @@ __global__ void k_detect_flags(DevBuffers b, DevConfig cfg, uint64_t n_records) 
   if ((threadIdx.x & 31) == 0) s_w[threadIdx.x >> 5] = __popc(m);
   __syncthreads();
   if (threadIdx.x < 32) {
-    u64 v = s_w[threadIdx.x];
+    u64 v = threadIdx.x < kDetBlock / 32 ? s_w[threadIdx.x] : 0u;
     v = warp_sum_u64(v);
     if (threadIdx.x == 0) b.block_tmp[blockIdx.x] = v;
   }
@@ -2914,7 +2914,7 @@ __global__ void __launch_bounds__(kSegThreads, 2)
   __syncthreads();  // the only CTA barrier: warps are independent from here on
   // per-warp [slot][lane] accumulator columns (row stride 33)
   const uint32_t SN = 33;
-  const uint32_t words = (uint32_t)(P + C + R) * SN * 2 + (uint32_t)R * SN + 64;  // 4-byte words
+  const uint32_t words = ((uint32_t)(P + C + R) * SN * 2 + (uint32_t)R * SN + 64 + 3) & ~3u;  // 16-B aligned
   uint32_t* wbase = reinterpret_cast<uint32_t*>(s_dyn) + (u64)warp * words;
   i64* comp = reinterpret_cast<i64*>(wbase);
   i64* beta = comp + (u64)P * SN;
@@ -3233,7 +3233,7 @@ int segment_range_smem(const DevConfig& cfg, int do_beta) {
   const int C = do_beta ? cfg.cyc.n_beta_slots : 0;
   const int R = do_beta ? cfg.cyc.n_comm_slots : 0;
   if (P > 15 || C > 254) return -1;
-  const int words = (P + C + R) * 33 * 2 + R * 33 + 64;  // per warp (k_segment_range)
+  const int words = ((P + C + R) * 33 * 2 + R * 33 + 64 + 3) & ~3;  // per warp (k_segment_range)
   const int smem = kSegWarps * words * 4;
   return smem <= 96 * 1024 ? smem : -1;
 }
