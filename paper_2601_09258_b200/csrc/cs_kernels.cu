@@ -1328,7 +1328,7 @@ __global__ void __launch_bounds__(kLutThreads)
 //   armed_t = t >= warmup;  flagged_t = armed_t && stat_t > limit
 //   alert_t = flagged_t && !flagged_{t-1}   (in_episode == flagged_{t-1})
 // Episode id = alerts before t in the instance (exclusive scan).
-constexpr int kDetBlock = 256;  // 6 CTAs/SM at 40 registers (1024-thread CTAs: 1, half occupancy)
+constexpr int kDetBlock = 1024;  // records per detect block (both flag kernels, the scatter)
 
 __device__ __forceinline__ double window_stat(const double* e, u64 t, u64 W, int strategy) {
   if (strategy == CS_FIXED_POINT) return e[t];
@@ -1403,6 +1403,101 @@ __global__ void k_detect_flags(DevBuffers b, DevConfig cfg, uint64_t n_records) 
     u64 v = threadIdx.x < kDetBlock / 32 ? s_w[threadIdx.x] : 0u;
     v = warp_sum_u64(v);
     if (threadIdx.x == 0) b.block_tmp[blockIdx.x] = v;
+  }
+}
+
+// Register-blocked control chart for whole runs (no stream carry) with W <=
+// kDetMaxW: a thread takes kDetK consecutive records and loads the residuals
+// of their windows once (kDetMaxW + kDetK values); every statistic is still
+// the sequential oldest-to-newest sum of its own window (detector.cpp:96-104),
+// the previous record's statistic comes from the same registers.  256-thread
+// CTAs of 1024 records (= kDetBlock, so k_detect_scatter's blocks match).
+constexpr int kDetK = 4;
+constexpr int kDetMaxW = 16;
+__global__ void __launch_bounds__(kDetBlock / kDetK) k_detect_flags_blk(DevBuffers b, DevConfig cfg,
+                                                                        uint64_t n_records) {
+  __shared__ uint32_t s_w[kDetBlock / kDetK / 32];
+  n_records = records_on_device(b, n_records);
+  const u64 k0 = (u64)blockIdx.x * kDetBlock + (u64)threadIdx.x * kDetK;
+  const long long W = (long long)cfg.ctl.window;
+  const bool fixed_point = cfg.ctl.strategy == CS_FIXED_POINT;
+  const u64 warm = cfg.ctl.warmup;
+  uint32_t n_alert = 0;
+  if (k0 < n_records) {
+    uint32_t inst = upper_bound_u64(b.rec_off, b.n_inst + 1, k0) - 1;
+    u64 rb = b.rec_off[inst];
+    u64 re = b.rec_off[inst + 1];
+    const double* e = b.rec_resid;
+    double v[kDetMaxW + kDetK];  // v[j] = e[k0 - kDetMaxW + j] inside the instance
+#pragma unroll
+    for (int j = 0; j < kDetMaxW + kDetK; ++j) {
+      const long long a = (long long)k0 - kDetMaxW + j;
+      v[j] = (a >= (long long)rb && (u64)a < re && (u64)a < n_records) ? e[a] : 0.0;
+    }
+    // statistic of record k0 + q (q >= -1), instance-relative index t
+    auto stat_of = [&](int q) -> double {
+      if (fixed_point) return v[kDetMaxW + q];
+      const long long t = (long long)(k0 + q) - (long long)rb;
+      const long long begin = t + 1 >= W ? t + 1 - W : 0;
+      const long long a0 = (long long)k0 - kDetMaxW - (long long)rb;  // relative index of v[0]
+      double sum = 0.0;
+#pragma unroll
+      for (int j = 0; j < kDetMaxW + kDetK; ++j) {
+        const long long a = a0 + j;
+        if (a >= begin && a <= t) sum = __dadd_rn(sum, v[j]);
+      }
+      return __ddiv_rn(sum, (double)(t - begin + 1));
+    };
+    double limit = b.models[inst].ucl;
+    double prev_stat = k0 > rb ? stat_of(-1) : 0.0;
+    bool crossed = false;
+#pragma unroll
+    for (int q = 0; q < kDetK; ++q) {
+      const u64 k = k0 + q;
+      if (k >= n_records) break;
+      if (crossed || k >= re) {  // the block crosses into the next instance: per-record from here
+        crossed = true;
+        inst = upper_bound_u64(b.rec_off, b.n_inst + 1, k) - 1;
+        rb = b.rec_off[inst];
+        re = b.rec_off[inst + 1];
+        limit = b.models[inst].ucl;
+        const double* ei = e + rb;
+        const u64 t = k - rb;
+        const double st = window_stat(ei, t, (u64)W, cfg.ctl.strategy);
+        const bool armed = t >= warm;
+        const bool prev = t >= 1 && t - 1 >= warm && window_stat(ei, t - 1, (u64)W, cfg.ctl.strategy) > limit;
+        const bool flagged = armed && st > limit;
+        const bool alert = flagged && !prev;
+        b.rec_stat[k] = st;
+        b.rec_flags[k] = (armed ? 1 : 0) | (flagged ? 2 : 0) | (alert ? 4 : 0);
+        if (alert) {
+          atomicAdd(&b.inst[inst].n_alerts, 1ull);
+          ++n_alert;
+        }
+        continue;
+      }
+      const u64 t = k - rb;
+      const double st = stat_of(q);
+      const bool armed = t >= warm;
+      const bool prev = t >= 1 && t - 1 >= warm && prev_stat > limit;
+      const bool flagged = armed && st > limit;
+      const bool alert = flagged && !prev;
+      b.rec_stat[k] = st;
+      b.rec_flags[k] = (armed ? 1 : 0) | (flagged ? 2 : 0) | (alert ? 4 : 0);
+      if (alert) {
+        atomicAdd(&b.inst[inst].n_alerts, 1ull);
+        ++n_alert;
+      }
+      prev_stat = st;
+    }
+  }
+  const uint32_t wsum = (uint32_t)warp_sum_u64(n_alert);
+  if ((threadIdx.x & 31) == 0) s_w[threadIdx.x >> 5] = wsum;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    u64 t = 0;
+    for (int w = 0; w < kDetBlock / kDetK / 32; ++w) t += s_w[w];
+    b.block_tmp[blockIdx.x] = t;
   }
 }
 
@@ -2820,7 +2915,10 @@ void launch_detect(const DevBuffers& b, const DevConfig& cfg, uint64_t n_records
                    uint64_t* launches) {
   const u64 nb = (n_records + kDetBlock - 1) / kDetBlock;
   if (nb) {
-    k_detect_flags<<<(unsigned)nb, kDetBlock, 0, s>>>(b, cfg, n_records);
+    if (!b.stream && (cfg.ctl.strategy == CS_FIXED_POINT || cfg.ctl.window <= (u64)kDetMaxW))
+      k_detect_flags_blk<<<(unsigned)nb, kDetBlock / kDetK, 0, s>>>(b, cfg, n_records);
+    else
+      k_detect_flags<<<(unsigned)nb, kDetBlock, 0, s>>>(b, cfg, n_records);
     ++*launches;
   }
   k_scan_exclusive<<<1, 1024, 0, s>>>(b.block_tmp, nb, b.block_tmp + nb);
