@@ -236,77 +236,6 @@ def reference_anchor_and_model(rb, events, names, workloads, n_comm, head_events
     return r.anchor, r.model_json
 
 
-def parity_leg(rb, an, events, names, workloads, n_comm, model_json, anchor, control, slices):
-    """Same-run alert parity: the reference (oracle/_ref, unmodified sources)
-    analyses cycle-aligned slices of the benchmarked trace with the GPU's
-    anchor and model; cycles, components, beta, records and residuals must be
-    identical to the GPU's whole-trace results for the same cycles, and the
-    detector's flags, statistics and alerts identical wherever its window and
-    warm-up have filled inside the slice (a slice restarts the detector)."""
-    from paper_2601_09258_b200 import abi
-    cyc = an.cycles(0)
-    recs = an.records(0)
-    alerts = an.alerts(0)
-    comp = an.components(0).reshape(len(cyc), -1)
-    tot, beta = an.beta(0)
-    nb = tot.size // max(1, len(cyc))
-    tot, beta = tot.reshape(len(cyc), nb), beta.reshape(len(cyc), nb)
-    settle = int(max(control.warmup, control.window)) + 1
-    out = {"checked_against": "reference built unmodified from /root/reference (oracle/_ref)",
-           "slices": [], "events_compared": 0, "cycles_compared": 0, "records_compared": 0,
-           "alerts_compared": 0}
-    ok = {"cycles": True, "components_beta": True, "records": True, "detector": True, "alerts": True}
-    first_event = cyc["first_event"].astype(np.int64)
-    for lo, hi in zip(*slices):
-        lo, hi = int(lo), int(hi)
-        t = rb.RefTrace.build(events[lo:hi], names, workloads, ["comm0"] * n_comm, list(range(n_comm)),
-                              sort=False)
-        ref = t.run({"cycle": {"anchor_hint": anchor}}, model_json, 0)
-        c0 = int(np.searchsorted(first_event, lo))
-        nc = len(ref.cycles)
-        g = cyc[c0:c0 + nc]
-        same = len(g) == nc and nc > 0
-        for f in ["start_ts", "end_ts", "anchor_span_end", "stage", "workload_status"]:
-            same = same and np.array_equal(ref.cycles[f], g[f])
-        same = same and np.array_equal(ref.cycles["first_event"] + lo, g["first_event"])
-        ok["cycles"] &= bool(same)
-        rc = ref.components.reshape(nc, -1) if nc else ref.components
-        ok["components_beta"] &= bool(same and np.array_equal(rc, comp[c0:c0 + nc]) and
-                                      np.array_equal(ref.beta_totals.reshape(nc, -1), tot[c0:c0 + nc]) and
-                                      np.array_equal(ref.beta.reshape(nc, -1).view(np.uint64),
-                                                     beta[c0:c0 + nc].view(np.uint64)))
-        sel = (recs["cycle_index"] >= c0) & (recs["cycle_index"] < c0 + nc)
-        gr = recs[sel]
-        rr = ref.records
-        n = min(len(rr), len(gr))
-        rec_ok = len(rr) == len(gr)
-        for f in ["latency_s", "predicted_s", "residual"]:
-            rec_ok = rec_ok and np.array_equal(rr[f][:n].view(np.uint64), gr[f][:n].view(np.uint64))
-        rec_ok = rec_ok and np.array_equal(rr["cycle_index"][:n] + c0, gr["cycle_index"][:n])
-        ok["records"] &= bool(rec_ok)
-        s = settle
-        det_ok = rec_ok and np.array_equal(rr["statistic"][s:n].view(np.uint64), gr["statistic"][s:n].view(np.uint64))
-        for f in ["armed", "flagged", "alert"]:
-            det_ok = det_ok and np.array_equal(rr[f][s:n], gr[f][s:n])
-        ok["detector"] &= bool(det_ok)
-        # alerts of the settled part of the slice
-        a_lo = int(gr["cycle_index"][s]) if n > s else c0 + nc
-        ga = alerts[(alerts["cycle"] >= a_lo) & (alerts["cycle"] < c0 + nc)]
-        ra = ref.alerts[ref.alerts["record_index"] >= s]
-        al_ok = len(ga) == len(ra) and np.array_equal(ra["cycle"] + c0, ga["cycle"]) and \
-            np.array_equal(ra["ts"], ga["ts"]) and \
-            np.array_equal(ra["smoothed_error"].view(np.uint64), ga["smoothed_error"].view(np.uint64))
-        ok["alerts"] &= bool(al_ok)
-        out["slices"].append({"events": [lo, hi], "cycles": [c0, c0 + nc], "alerts": int(len(ra))})
-        out["events_compared"] += hi - lo
-        out["cycles_compared"] += nc
-        out["records_compared"] += n
-        out["alerts_compared"] += int(len(ra))
-    out.update({f"{k}_identical": v for k, v in ok.items()})
-    out["identical"] = all(ok.values())
-    return out
-
-
 def cpu_reference_same_trace(rb, events, names, workloads, n_comm, cores, per_slice, center_event,
                              model_json=None, anchor=None):
     """The reference analyzer (oracle/_ref) on cycle-aligned slices of THIS
@@ -677,16 +606,8 @@ def run_ours(args, rank, world, local_rank):
             from oracle import refbridge as rb
             if rb.available():
                 anchor = names[an.summary(0).anchor_name_id]
-                model_json = models[0].to_json()
-                onset = WORKLOADS[args.workload][3]
-                cyc_tab = an.cycles(0)
-                center = int(cyc_tab["first_event"][min(onset, len(cyc_tab) - 1)]) if onset else None
-                sl = cycle_aligned_slices(pin_ev, names.index(anchor), 2, 400_000, None)
-                if center is not None:
-                    c_sl = cycle_aligned_slices(pin_ev, names.index(anchor), 1, 400_000, center)
-                    sl = (np.concatenate([sl[0][:1], c_sl[0]]), np.concatenate([sl[1][:1], c_sl[1]]))
-                line["parity"] = parity_leg(rb, an, pin_ev, names, pin_wl, n_comm, model_json, anchor,
-                                            an.control, sl)
+                line["parity"] = rb.full_parity(an, pin_ev, names, pin_wl, n_comm, models[0].to_json(),
+                                                anchor, cpu_cores())
         except Exception as e:  # report, never hide
             line["parity"] = {"identical": None, "error": repr(e)}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -13,6 +13,7 @@
 // Only the reference's public headers are used; no reference code is copied.
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cstring>
 #include <map>
@@ -1101,6 +1102,272 @@ double ref_cpu_run(void* h, uint32_t n_threads, uint64_t* n_alerts_out) {
   for (auto a : alerts) na += a;
   if (n_alerts_out) *n_alerts_out = na;
   return secs;
+}
+
+// Whole-trace reference results for a trace too large for one reference
+// Trace (configs[1]: ~42 GB as TraceEvent + std::map args): the trace is cut
+// into cycle-aligned chunks at anchor group starts, each chunk extended
+// through the next chunk's first anchor so that its last cycle closes
+// exactly as in the whole trace (segment, cycles.cpp:120-170; lower_bound
+// group starts).  Chunks run segment_and_classify (anchor_hint = the trace's
+// anchor), cycle_stats (beta part), build_cycle_records, predict and ppe on
+// n_threads threads; ONE Detector then steps every record in trace order
+// (monitor_loop, main.cpp:151-177), so flags, statistics, episodes and alerts
+// are the whole trace's.  Stages restart their trailing windows per chunk:
+// exact when every cycle's stage comes from forward_mode or keywords (as in
+// simkit traces), which out_flags bit 0 reports.  Outputs go to caller
+// buffers in the product's layouts: cycles (cs_cycle), components [cycle][P]
+// by the name table's phase, beta totals / beta [cycle][C] by its beta_slot,
+// collective beta / present [cycle][R] by the records' comm slot; records
+// (cs_record, incl. detector fields) and alerts (cs_alert).
+int ref_full_parity(uint64_t n, const cs_event* ev, uint32_t n_names, const char* names_packed,
+                    const cs_workload* wl, uint32_t n_comm, const char* comm_hash_packed,
+                    const int32_t* comm_rank, const cs_name_info* name_table, int32_t P, int32_t C,
+                    int32_t R, const char* model_json, const char* anchor_name, uint32_t n_threads,
+                    uint64_t chunk_events, uint64_t cap_cycles, cs_cycle* o_cycles, int64_t* o_comp,
+                    int64_t* o_beta_tot, double* o_beta, double* o_coll, uint8_t* o_coll_present,
+                    uint64_t cap_records, cs_record* o_records, uint64_t cap_alerts, cs_alert* o_alerts,
+                    uint64_t* n_out, uint32_t* out_flags, double* seconds, char* err, size_t err_cap) {
+  const auto t0 = std::chrono::steady_clock::now();
+  try {
+    std::vector<std::string> names;
+    {
+      const char* p = names_packed;
+      for (uint32_t i = 0; i < n_names; ++i) {
+        names.emplace_back(p);
+        p += names.back().size() + 1;
+      }
+    }
+    std::map<std::string, uint32_t> name_id;
+    for (uint32_t i = 0; i < n_names; ++i) name_id[names[i]] = i;
+    const auto ait = name_id.find(anchor_name);
+    if (ait == name_id.end()) throw std::runtime_error("anchor not in the name table");
+    const uint32_t anchor = ait->second;
+    std::vector<uint64_t> apos;
+    for (uint64_t i = 0; i < n; ++i)
+      if (ev[i].kind == CS_SPAN && ev[i].name_id == anchor) apos.push_back(i);
+    const uint64_t n_anchors = apos.size();
+    const uint64_t n_cyc = n_anchors >= 2 ? n_anchors - 1 : 0;
+    if (n_cyc > cap_cycles) throw std::runtime_error("cycle capacity");
+    auto group_start = [&](uint64_t pos) {
+      while (pos > 0 && ev[pos - 1].start_ts == ev[pos].start_ts) --pos;
+      return pos;
+    };
+    // chunk k covers the cycles of anchors [ka[k], ka[k+1])
+    std::vector<uint64_t> ka;
+    {
+      uint64_t k = 0;
+      while (k < n_cyc) {
+        ka.push_back(k);
+        const uint64_t lo = group_start(apos[k]);
+        uint64_t k2 = k + 1;
+        while (k2 < n_cyc && apos[k2] - lo < chunk_events) ++k2;
+        k = k2;
+      }
+      ka.push_back(n_cyc);
+    }
+    const size_t n_chunks = ka.size() - 1;
+    std::vector<std::string> comms;
+    {
+      const char* p = comm_hash_packed;
+      for (uint32_t i = 0; i < n_comm; ++i) {
+        comms.emplace_back(p);
+        p += comms.back().size() + 1;
+      }
+    }
+    std::map<std::tuple<std::string, std::string, int>, uint32_t> comm_slot;
+    std::vector<std::string> phases;  // phase order = the name table's phase index
+    phases.assign(std::max(0, P), std::string());
+    for (uint32_t i = 0; i < n_names; ++i)
+      if (name_table[i].phase >= 0 && name_table[i].phase < P) phases[name_table[i].phase] = names[i];
+    for (uint64_t i = 0; i < n; ++i)
+      if ((ev[i].flags & CS_EV_HAS_COMM) && ev[i].kind == CS_SPAN) {
+        const uint32_t s = static_cast<uint32_t>(ev[i].payload >> 32);
+        if (s < n_comm) comm_slot[{names[ev[i].name_id], comms[s], comm_rank[s]}] = s;
+      }
+    const LatencyModel model = LatencyModel::from_json(json::parse(model_json));
+    CycleConfig cc;
+    cc.anchor_hint = anchor_name;
+    cc.phase_functions.clear();
+    for (const auto& ph : phases) cc.phase_functions.push_back(ph);
+    PipelineOptions po;
+    ControlConfig dc;
+    if (n_cyc) std::memset(o_cycles, 0, n_cyc * sizeof(cs_cycle));
+    if (P > 0 && n_cyc) std::memset(o_comp, 0, n_cyc * P * sizeof(int64_t));
+    if (C > 0 && n_cyc) {
+      std::memset(o_beta_tot, 0, n_cyc * C * sizeof(int64_t));
+      std::memset(o_beta, 0, n_cyc * C * sizeof(double));
+    }
+    if (R > 0 && n_cyc) {
+      std::memset(o_coll, 0, n_cyc * R * sizeof(double));
+      std::memset(o_coll_present, 0, n_cyc * R);
+    }
+    struct ChunkOut {
+      std::vector<cs_record> recs;
+      std::vector<double> err;
+      std::vector<WorkloadFeatures> wl;
+      bool heuristic = false;
+      std::string error;
+    };
+    std::vector<ChunkOut> outs(n_chunks);
+    const double eps = dc.epsilon;
+    auto work = [&](size_t k) {
+      ChunkOut& co = outs[k];
+      const uint64_t c0 = ka[k], c1 = ka[k + 1];
+      const uint64_t lo = group_start(apos[c0]);
+      const uint64_t hi = c1 < n_anchors ? apos[c1] + 1 : n;  // through the closing anchor
+      std::unique_ptr<Handle> h(static_cast<Handle*>(
+          ref_build(hi - lo, ev + lo, nullptr, n_names, names_packed, wl, n_comm, comm_hash_packed,
+                    comm_rank, 0)));
+      const Trace& tr = h->ds.trace;
+      auto cyc = segment_and_classify(tr, cc);
+      if (cyc.size() < c1 - c0) {
+        co.error = "chunk produced fewer cycles than anchors";
+        return;
+      }
+      cyc.resize(c1 - c0);
+      const CounterTable no_counters;
+      const MetricMap no_metrics;
+      for (size_t i = 0; i < cyc.size(); ++i) {
+        const Cycle& c = cyc[i];
+        const uint64_t g = c0 + i;
+        cs_cycle& o = o_cycles[g];
+        o.index = g;
+        o.start_ts = c.start_ts;
+        o.end_ts = c.end_ts;
+        o.anchor_pos = c.anchor_event_id ? lo + (*c.anchor_event_id - 1) : UINT64_MAX;
+        o.anchor_span_end = c.anchor_span_end;
+        o.first_event = lo + c.first_event;
+        o.last_event = lo + c.last_event;
+        o.stage = stage_code(c.stage);
+        try {
+          extract_workload(c, tr, cc);
+          o.workload_status = 0;
+        } catch (const MissingWorkloadArgs&) {
+          bool carrier = false;
+          for (size_t j = c.first_event; j < c.last_event && !carrier; ++j)
+            carrier = arg_int(tr.events[j], cc.batch_size_key).has_value();
+          o.workload_status = carrier ? 2 : 1;
+        }
+        // a stage the trailing-median heuristic decided depends on earlier
+        // cycles (cycles.cpp:230-250): reported, since chunks restart it
+        {
+          std::optional<std::string> fm;
+          for (size_t j = c.first_event; j < c.last_event && !fm; ++j) fm = arg_string(tr.events[j], cc.forward_mode_key);
+          bool local = false;
+          if (fm) {
+            std::string m = *fm;
+            for (auto& ch : m) ch = static_cast<char>(std::tolower(static_cast<unsigned char>(ch)));
+            local = m.find("prefill") != std::string::npos || m.find("extend") != std::string::npos ||
+                    m.find("decode") != std::string::npos;
+          }
+          if (!local) co.heuristic = true;  // keyword-only stages are reported too (conservative)
+        }
+        for (int p = 0; p < P; ++p) {
+          auto it = c.component_durations.find(phases[p]);
+          o_comp[g * P + p] = it == c.component_durations.end() ? 0 : it->second;
+        }
+        if (C > 0 || R > 0) {
+          const auto st = cycle_stats(c, tr, no_counters, no_metrics);
+          for (const auto& [name, cls] : st.classes) {
+            const auto nit = name_id.find(name);
+            const int32_t s = nit == name_id.end() ? -1 : name_table[nit->second].beta_slot;
+            if (s < 0 || s >= C) throw std::runtime_error("class without a beta slot: " + name);
+            o_beta_tot[g * C + s] = cls.total_duration;
+            o_beta[g * C + s] = cls.beta;
+          }
+          for (const auto& [key, b] : st.collective_rank_beta) {
+            const auto cit = comm_slot.find(key);
+            if (cit == comm_slot.end() || static_cast<int32_t>(cit->second) >= R)
+              throw std::runtime_error("collective key without a slot");
+            o_coll[g * R + cit->second] = b;
+            o_coll_present[g * R + cit->second] = 1;
+          }
+        }
+      }
+      const auto recs = build_cycle_records(tr, std::span<const Cycle>(cyc), cc, po);
+      for (const auto& r : recs) {
+        cs_record o{};
+        o.cycle_index = c0 + r.cycle_index;
+        o.start_ts = r.start_ts;
+        o.batch = r.workload.batch;
+        o.input_len = r.workload.input_len;
+        o.output_len = r.workload.output_len;
+        o.latency_s = r.latency_s;
+        o.stage = stage_code(r.stage);
+        const double row[2] = {static_cast<double>(r.workload.batch),
+                               static_cast<double>(r.workload.kv_token_slots())};
+        o.predicted_s = model.predict(row);
+        co.recs.push_back(o);
+        co.wl.push_back(r.workload);
+      }
+    };
+    std::vector<std::thread> th;
+    const uint32_t nt = std::max(1u, n_threads);
+    std::atomic<size_t> next{0};
+    for (uint32_t t = 0; t < nt; ++t)
+      th.emplace_back([&] {
+        for (size_t k; (k = next.fetch_add(1)) < n_chunks;) work(k);
+      });
+    for (auto& x : th) x.join();
+    uint32_t flags = 0;
+    for (const auto& co : outs) {
+      if (!co.error.empty()) throw std::runtime_error(co.error);
+      if (co.heuristic) flags |= 1u;
+    }
+    // one Detector over every record, in trace order
+    const double ucl = ucl_from_stats(model.mu_train, model.sigma_train, dc);
+    Detector det(dc, ucl);
+    uint64_t nr = 0, na = 0;
+    for (const auto& co : outs) {
+      for (size_t i = 0; i < co.recs.size(); ++i) {
+        if (nr >= cap_records) throw std::runtime_error("record capacity");
+        cs_record o = co.recs[i];
+        ResidualSample s;
+        s.cycle = o.cycle_index;
+        s.ts = o.start_ts;
+        s.workload = co.wl[i];
+        s.actual_s = o.latency_s;
+        s.predicted_s = o.predicted_s;
+        s.error = ppe(o.latency_s, o.predicted_s, eps);
+        const auto step = det.step(s);
+        o.residual = s.error;
+        o.statistic = step.statistic;
+        o.armed = step.armed;
+        o.flagged = step.flagged;
+        o.alert = step.alert.has_value();
+        if (step.alert) {
+          o.episode_id = step.alert->episode_id;
+          if (na >= cap_alerts) throw std::runtime_error("alert capacity");
+          cs_alert& a = o_alerts[na++];
+          a = cs_alert{};
+          a.cycle = step.alert->cycle;
+          a.ts = step.alert->ts;
+          a.smoothed_error = step.alert->smoothed_error;
+          a.limit = step.alert->limit;
+          a.strategy = static_cast<int32_t>(step.alert->strategy);
+          a.batch = step.alert->workload.batch;
+          a.input_len = step.alert->workload.input_len;
+          a.output_len = step.alert->workload.output_len;
+          a.episode_id = step.alert->episode_id;
+          a.record_index = nr;
+        }
+        o_records[nr++] = o;
+      }
+    }
+    n_out[0] = n_cyc;
+    n_out[1] = nr;
+    n_out[2] = na;
+    if (out_flags) *out_flags = flags;
+  } catch (const EngineError& e) {
+    if (err && err_cap) std::snprintf(err, err_cap, "%s: %s", e.type().c_str(), e.what());
+    return 1;
+  } catch (const std::exception& e) {
+    if (err && err_cap) std::snprintf(err, err_cap, "internal: %s", e.what());
+    return 2;
+  }
+  if (seconds) *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  return 0;
 }
 
 }  // extern "C"

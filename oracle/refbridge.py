@@ -90,6 +90,10 @@ def lib():
         L.ref_cpu_fit_seconds.restype = C.c_double
         L.ref_cpu_fit_seconds.argtypes = [vp]
         L.ref_cpu_free.argtypes = [vp]
+        L.ref_full_parity.argtypes = [C.c_uint64, vp, C.c_uint32, C.c_char_p, vp, C.c_uint32, C.c_char_p,
+                                      vp, vp, C.c_int32, C.c_int32, C.c_int32, C.c_char_p, C.c_char_p,
+                                      C.c_uint32, C.c_uint64, C.c_uint64, vp, vp, vp, vp, vp, vp,
+                                      C.c_uint64, vp, C.c_uint64, vp, vp, vp, vp, C.c_char_p, sz]
         L.ref_cpu_run.restype = C.c_double
         L.ref_cpu_run.argtypes = [vp, C.c_uint32, C.POINTER(C.c_uint64)]
         _lib = L
@@ -425,3 +429,75 @@ class CpuBaseline:
         if self.h:
             lib().ref_cpu_free(self.h)
             self.h = None
+
+
+def full_parity(an, events, names, workloads, n_comm, model_json, anchor, n_threads,
+                chunk_events=1_000_000, inst=0):
+    """The WHOLE trace through the reference (ref_full_parity: cycle-aligned
+    chunks on n_threads threads, one Detector over every record in order)
+    compared with the product's results for instance `inst` of analyzer `an`
+    (after a RUN_ALL with beta).  Returns the summary dict bench.py reports;
+    every comparison is bitwise."""
+    ev = np.ascontiguousarray(events, dtype=abi.EVENT_DTYPE)
+    wl = np.ascontiguousarray(workloads, dtype=abi.WORKLOAD_DTYPE)
+    packed = b"".join(n.encode() + b"\0" for n in names)
+    cpacked = b"".join(b"comm0\0" for _ in range(n_comm)) or b"\0"
+    crank = np.arange(max(1, n_comm), dtype=np.int32)
+    P, Cs, R = an.cycle.n_phases, an.cycle.n_beta_slots, an.cycle.n_comm_slots
+    cyc = an.cycles(inst)
+    recs = an.records(inst)
+    alerts = an.alerts(inst)
+    nc, nr = len(cyc), len(recs)
+    cap_c, cap_r, cap_a = nc + 16, nr + 16, len(alerts) + 1024
+    r_cyc = np.zeros(cap_c, abi.CYCLE_DTYPE)
+    r_comp = np.zeros(cap_c * max(P, 1), np.int64)
+    r_tot = np.zeros(cap_c * max(Cs, 1), np.int64)
+    r_beta = np.zeros(cap_c * max(Cs, 1), np.float64)
+    r_coll = np.zeros(cap_c * max(R, 1), np.float64)
+    r_cp = np.zeros(cap_c * max(R, 1), np.uint8)
+    r_rec = np.zeros(cap_r, abi.RECORD_DTYPE)
+    r_al = np.zeros(cap_a, abi.ALERT_DTYPE)
+    n_out = np.zeros(3, np.uint64)
+    flags = C.c_uint32(0)
+    secs = C.c_double(0)
+    err = C.create_string_buffer(512)
+    table = np.ascontiguousarray(an.name_table, dtype=abi.NAME_INFO_DTYPE)
+    rc = lib().ref_full_parity(len(ev), ev.ctypes.data, len(names), packed, wl.ctypes.data, n_comm, cpacked,
+                               crank.ctypes.data, table.ctypes.data, P, Cs, R, model_json.encode(),
+                               anchor.encode(), n_threads, chunk_events, cap_c, r_cyc.ctypes.data,
+                               r_comp.ctypes.data, r_tot.ctypes.data, r_beta.ctypes.data, r_coll.ctypes.data,
+                               r_cp.ctypes.data, cap_r, r_rec.ctypes.data, cap_a, r_al.ctypes.data,
+                               n_out.ctypes.data, C.byref(flags), C.byref(secs), err, 512)
+    if rc != 0:
+        raise RuntimeError(f"ref_full_parity: {err.value.decode()}")
+    rn_c, rn_r, rn_a = (int(x) for x in n_out)
+    r_cyc, r_rec, r_al = r_cyc[:rn_c], r_rec[:rn_r], r_al[:rn_a]
+
+    def same(a, b):
+        return a.shape == b.shape and a.tobytes() == b.tobytes()
+
+    ok = {}
+    ok["cycles"] = rn_c == nc and all(np.array_equal(r_cyc[f], cyc[f]) for f in abi.CYCLE_DTYPE.names)
+    ok["components"] = same(r_comp[:rn_c * P], an.components(inst)[:nc * P])
+    tot, beta = an.beta(inst)
+    ok["beta"] = same(r_tot[:rn_c * Cs], tot) and same(r_beta[:rn_c * Cs], beta)
+    cb, cp = an.collective_beta(inst)
+    ok["collective_beta"] = same(r_coll[:rn_c * R], cb) and same(r_cp[:rn_c * R], cp)
+    rec_fields = [f for f in abi.RECORD_DTYPE.names if f not in ("reserved", "episode_id")]
+    def raw(a):
+        return np.ascontiguousarray(a).view(np.uint8)
+
+    ok["records"] = rn_r == nr and all(np.array_equal(raw(r_rec[f]), raw(recs[f])) for f in rec_fields)
+    al_fields = [f for f in abi.ALERT_DTYPE.names if f != "reserved"]
+    ok["alerts"] = rn_a == len(alerts) and all(
+        np.array_equal(raw(r_al[f]), raw(alerts[f])) for f in al_fields)
+    out = {"checked_against": "reference built unmodified from /root/reference (oracle/_ref)",
+           "scope": "whole trace: cycle-aligned chunks through segment_and_classify / cycle_stats / "
+                    "build_cycle_records / predict / ppe, one Detector over every record in order",
+           "events_compared": int(len(ev)), "cycles_compared": nc, "records_compared": nr,
+           "alerts_compared": int(rn_a), "reference_seconds": round(secs.value, 2),
+           "reference_threads": int(n_threads),
+           "stages_from_heuristic": bool(flags.value & 1)}
+    out.update({f"{k}_identical": bool(v) for k, v in ok.items()})
+    out["identical"] = all(ok.values())
+    return out

@@ -678,6 +678,7 @@ class Analyzer:
         self.set_config(cyc, ctl)
         self.set_name_table(table)
         self.names = list(names)
+        self.name_table = np.ascontiguousarray(table, dtype=abi.NAME_INFO_DTYPE)
         return cyc, ctl, table
 
     def set_config(self, cycle: abi.CycleConfig, control: abi.ControlConfig):
