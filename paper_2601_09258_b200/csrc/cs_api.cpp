@@ -155,12 +155,13 @@ struct cs_ctx {
   // inputs
   uint32_t n_inst = 0;
   uint64_t n_ev = 0, n_wl = 0;
-  std::vector<uint64_t> inst_off;
+  pinned_vector<uint64_t> inst_off;
   DevBuf d_ev, d_wl, d_names, d_inst_off;
   DevBuf d_wire;  // cs_upload_wire staging (all columns in one allocation)
   // tiles
-  std::vector<uint32_t> tile_inst, inst_first_tile;
-  std::vector<uint64_t> tile_begin, tile_end;
+  // pinned: the layout's host->device copies are asynchronous (streaming pushes)
+  pinned_vector<uint32_t> tile_inst, inst_first_tile;
+  pinned_vector<uint64_t> tile_begin, tile_end;
   DevBuf d_tile_inst, d_tile_begin, d_tile_end, d_inst_first_tile, d_tile_cnt, d_tile_pref;
   DevBuf d_scan_tmp;
   // record extras (cs_upload_extras)
@@ -184,9 +185,13 @@ struct cs_ctx {
   bool have_order = false;
   void* pin_models = nullptr;  // pinned staging of the per-instance DevModel array
   size_t pin_models_cap = 0;
-  std::vector<uint64_t> stage_off, assemble_host;
+  std::vector<uint64_t> stage_off;
+  pinned_vector<uint64_t> assemble_host, h_new_anchors;
+  pinned_vector<uint32_t> h_anchor_ids;
+  DevBuf d_anchor_ids, d_new_anchors;
+  cudaEvent_t ev_counted = nullptr;  // the new events' anchor counts are on the host
   DevBuf d_keep;
-  std::vector<uint32_t> sample_tiles;
+  pinned_vector<uint32_t> sample_tiles;
   DevBuf d_sample_tiles, d_redo_tiles;
   // state
   DevBuf d_stats, d_inst, d_a_pos, d_a_start, d_a_end;
@@ -269,12 +274,21 @@ struct cs_ctx {
   // state before the current run (that run's alerts are cut, later runs' dropped)
   std::vector<uint8_t> stream_stopped, stream_stopped_prior;
   bool stream_broken = false;  // a push failed after it started mutating state
+  // steady-state micro-batches: anchor occurrences per instance predicted on
+  // the host (carried tail + the new events, the anchor being fixed), so the
+  // run sizes its cycle tables without waiting for the event scan; verified
+  // against the device's count at the run's final synchronisation
+  std::vector<uint64_t> tail_anchors;    // anchor occurrences in each carried tail
+  pinned_vector<uint64_t> h_keep;        // tail starts + tail anchor counts (stream_commit)
+  pinned_vector<cs_alert> h_alerts_all;  // a push's alerts (stream_commit)
+  std::vector<uint64_t> pred_anchors;    // for the run in flight (empty: no prediction)
 
   ~cs_ctx() {
     for (auto* m : model_store) delete m;
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
     if (ev_copied) cudaEventDestroy(ev_copied);
+    if (ev_counted) cudaEventDestroy(ev_counted);
     if (stream) cudaStreamDestroy(stream);
   }
 };
@@ -1142,6 +1156,10 @@ static int cs_run_impl(cs_ctx* ctx, uint32_t mask) {
     all_fixed = true;
     for (uint32_t a : ctx->stream_anchor) all_fixed &= a != UINT32_MAX;
   }
+  // a host prediction of the anchor counts applies to this run only
+  std::vector<uint64_t> pred;
+  pred.swap(ctx->pred_anchors);
+  const bool predicted = ctx->streaming && all_fixed && pred.size() == n_inst && !(mask & CS_RUN_GIVEN);
   // per-instance state
   ctx->h_inst.assign(n_inst, InstState{});
   for (uint32_t i = 0; i < n_inst; ++i) {
@@ -1165,6 +1183,7 @@ static int cs_run_impl(cs_ctx* ctx, uint32_t mask) {
                           cudaMemcpyHostToDevice, s));
   if (!dev<unsigned int>(ctx->d_any_unknown, 1)) return fail(ctx, CS_E_CUDA, "cudaMalloc(flag)");
   CS_CUDA(cudaMemsetAsync(ctx->d_any_unknown.p, 0, 4, s));
+  hp.mark("state_up");
   const size_t stats_bytes = static_cast<size_t>(n_inst) * n_names * sizeof(NameStat);
   const size_t nt = ctx->tile_inst.size();
   DevConfig cfg{ctx->cyc, ctx->ctl, 0.0};
@@ -1369,13 +1388,28 @@ static int cs_run_impl(cs_ctx* ctx, uint32_t mask) {
   e1 = record_event(ctx, 1);
   launch_scan_events(b, cfg, 3, false, nullptr, static_cast<uint32_t>(nt), s, &ctx->launches);
   e2 = record_event(ctx, 2);
+  hp.mark("scan");
   launch_tile_order(b, s, &ctx->launches);
   launch_tile_prefix(b, s, &ctx->launches);
+  hp.mark("tiles");
   ctx->timed.push_back({"scan_events", {e1, e2}});
   launch_rank(b, cfg, 1, s, &ctx->launches);
   const int e9 = record_event(ctx, 9);
   ctx->timed.push_back({"sample_and_setup", {e0, e1}});
   ctx->timed.push_back({"prefix_rank", {e2, e9}});
+  // steady-state stream: every anchor is fixed and the host predicted the
+  // occurrence counts, so the ranking cannot be ambiguous or redone and the
+  // sizing needs nothing from the device (checked after the final sync)
+  if (predicted) {
+    for (uint32_t i = 0; i < n_inst; ++i) {
+      auto& st = ctx->h_inst[i];
+      st.n_anchors = pred[i];
+      st.anchor = st.n_anchors ? st.guess : UINT32_MAX;
+      st.no_anchor = st.n_anchors ? 0u : 1u;
+      st.ambiguous = st.redo = 0;
+    }
+    hp.mark("scan_issued");
+  } else {
   CS_CUDA(cudaMemcpyAsync(ctx->h_inst.data(), d_inst, n_inst * sizeof(InstState),
                           cudaMemcpyDeviceToHost, s));
   hp.mark("scan_issued");
@@ -1388,6 +1422,7 @@ static int cs_run_impl(cs_ctx* ctx, uint32_t mask) {
                   "events of instance " + std::to_string(i) +
                       " are not in canonical (start_ts, event_id) order (trace.cpp:103-109); "
                       "cs_upload_unsorted sorts them on the device");
+  }
 
   // ---- rare paths: ordered fold for uncertified rankings
   ctx->folded.assign(n_inst, {});
@@ -1493,6 +1528,7 @@ static int cs_run_impl(cs_ctx* ctx, uint32_t mask) {
   b = make_buffers(ctx);
   const int e3 = record_event(ctx, 3);
   ctx->timed.push_back({"host_sizing", {e9, e3}});
+  hp.mark("sized");
   launch_bounds(b, s, &ctx->launches);
   for (uint32_t i = 0; i < n_inst; ++i)
     if (ctx->used_fallback[i] && ctx->fallback_cycles[i])
@@ -1503,6 +1539,7 @@ static int cs_run_impl(cs_ctx* ctx, uint32_t mask) {
   launch_cycle_reduce_tpc(b, cfg, (mask & CS_RUN_BETA) ? 1 : 0, s, &ctx->launches,
                           ctx->reduce_variant);
   e5 = record_event(ctx, 5);
+  hp.mark("reduce");
   ctx->timed.push_back({"bounds", {e3, e4}});
   ctx->timed.push_back({"cycle_reduce", {e4, e5}});
   }
@@ -1523,7 +1560,9 @@ static int cs_run_impl(cs_ctx* ctx, uint32_t mask) {
     if (launch_stage_heuristic(b, cfg, sm, s, &ctx->launches) != 0)
       return fail(ctx, CS_E_UNSUPPORTED, "stage_window too large for the device heuristic (<= 1600)");
   }
+  hp.mark("stage");
   launch_records(b, cfg, 0, s, &ctx->launches);
+  hp.mark("records");
   if (!ctx->extra_keys.empty() && ctx->n_cycles) {
     const uint64_t K = ctx->extra_keys.size();
     if (!dev<double>(ctx->d_rec_extra, ctx->n_cycles * K) || !dev<uint8_t>(ctx->d_rec_extra_has, ctx->n_cycles * K))
@@ -1634,13 +1673,16 @@ static int cs_run_impl(cs_ctx* ctx, uint32_t mask) {
     if (!dev<uint64_t>(ctx->block_tmp, rec_cap / 256 + 16))
       return fail(ctx, CS_E_CUDA, "cudaMalloc(block_tmp)");
     b = make_buffers(ctx);
+    hp.mark("models");
     launch_score(b, cfg, rec_cap, ctx->rec_off.data(), ctx->model_of_inst.data(),
                  ctx->h_models.data(), s, &ctx->launches);
+    hp.mark("score");
     const int e7 = record_event(ctx, 7);
     ctx->timed.push_back({"score", {e6, e7}});
     last = e7;
     if (mask & CS_RUN_DETECT) {
       launch_detect(b, cfg, rec_cap, s, &ctx->launches);
+      hp.mark("detect");
       const int e8 = record_event(ctx, 8);
       ctx->timed.push_back({"detect", {e7, e8}});
       last = e8;
@@ -1667,6 +1709,16 @@ static int cs_run_impl(cs_ctx* ctx, uint32_t mask) {
   CS_CUDA(cudaStreamSynchronize(s));
   hp.mark("final_sync");
   CS_CUDA(cudaGetLastError());
+  if (predicted) {
+    for (uint32_t i = 0; i < n_inst; ++i) {
+      if (ctx->h_inst[i].unsorted)
+        return fail(ctx, CS_E_INVALID_ARGUMENT,
+                    "events of instance " + std::to_string(i) +
+                        " are not in canonical (start_ts, event_id) order (trace.cpp:103-109)");
+      if (ctx->h_inst[i].n_anchors != pred[i])
+        return fail(ctx, CS_E_INTERNAL, "micro-batch anchor count differs from the host prediction");
+    }
+  }
   ctx->n_records = ctx->rec_off[n_inst];
   for (uint32_t i = 0; i < n_inst; ++i) {
     // monitor_loop stops at the first record whose features are missing
@@ -1696,6 +1748,7 @@ static int cs_run_impl(cs_ctx* ctx, uint32_t mask) {
         ctx->stream_anchor[i] = ctx->h_inst[i].anchor;
   ctx->ran = true;
   ctx->last_mask = mask;
+  hp.mark("done");
   return CS_OK;
 }
 
@@ -1711,6 +1764,8 @@ int cs_stream_begin(cs_ctx* ctx) {
   ctx->stream_stopped_prior.clear();
   ctx->tail_len.clear();
   ctx->tail_start.clear();
+  ctx->tail_anchors.clear();
+  ctx->pred_anchors.clear();
   ctx->tails_on_device = false;
   ctx->stream_fresh = true;
   return CS_OK;
@@ -1741,24 +1796,21 @@ int cs_stream_tail(cs_ctx* ctx, uint32_t inst, uint64_t* keep_from) {
 // the first NonPositiveLatency of the stream (main.cpp:162).
 static int stream_commit(cs_ctx* ctx, uint32_t n_inst, uint32_t mask, cs_alert* alerts, size_t cap,
                          size_t* n_alerts, HostPhases& hp) {
-  auto* dk = dev<uint64_t>(ctx->d_keep, n_inst);
+  auto* dk = dev<uint64_t>(ctx->d_keep, 2ull * n_inst);
   if (!dk) return fail(ctx, CS_E_CUDA, "cudaMalloc(keep)");
   launch_stream_keep(make_buffers(ctx), dk, ctx->stream);
-  std::vector<uint64_t> keep(n_inst);
-  CS_CUDA(cudaMemcpyAsync(keep.data(), dk, n_inst * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  pinned_vector<uint64_t>& keep = ctx->h_keep;
+  keep.resize(2ull * n_inst);
+  CS_CUDA(cudaMemcpyAsync(keep.data(), dk, 2ull * n_inst * 8, cudaMemcpyDeviceToHost, ctx->stream));
   size_t na = 0;
   const bool det = (mask & CS_RUN_DETECT) != 0;
-  std::vector<cs_alert> all;
+  pinned_vector<cs_alert>& all = ctx->h_alerts_all;
   if (det && ctx->alert_off[n_inst]) {
     const uint64_t n_all = ctx->alert_off[n_inst];
     auto* d = dev<cs_alert>(ctx->d_scratch, n_all);
     if (!d) return fail(ctx, CS_E_CUDA, "cudaMalloc(alerts)");
     DevConfig cfg{ctx->cyc, ctx->ctl, 0.0};
-    const DevBuffers b = make_buffers(ctx);
-    for (uint32_t i = 0; i < n_inst; ++i) {
-      const uint64_t a0 = ctx->alert_off[i], ni = ctx->alert_off[i + 1] - a0;
-      if (ni) launch_gather_alerts(b, cfg, i, a0, ni, d + a0, ctx->stream);
-    }
+    launch_gather_alerts_all(make_buffers(ctx), cfg, n_all, d, ctx->stream);
     all.resize(n_all);
     CS_CUDA(cudaMemcpyAsync(all.data(), d, n_all * sizeof(cs_alert), cudaMemcpyDeviceToHost,
                             ctx->stream));
@@ -1775,11 +1827,13 @@ static int stream_commit(cs_ctx* ctx, uint32_t n_inst, uint32_t mask, cs_alert* 
       ++na;
     }
   }
+  ctx->tail_anchors.resize(n_inst);
   for (uint32_t i = 0; i < n_inst; ++i) {
     const uint64_t len = ctx->stage_off[i + 1] - ctx->stage_off[i];
     const uint64_t k = std::min(keep[i], len);
     ctx->tail_start[i] = ctx->stage_off[i] + k;
     ctx->tail_len[i] = len - k;
+    ctx->tail_anchors[i] = keep[n_inst + i];
   }
   ctx->tails_on_device = true;
   hp.mark("end");
@@ -1836,16 +1890,16 @@ static int cs_stream_push_impl(cs_ctx* ctx, uint32_t n_inst, const uint64_t* off
     return rc;
   };
   hp.mark("pre");
-  int rc = upload_layout(ctx, n_inst, ctx->stage_off.data(), true, n_workloads, wl);
-  if (rc != CS_OK) return broken(rc);
-  hp.mark("layout");
+  // the new events go up first; in steady state (every anchor fixed) a tiny
+  // kernel counts their anchor occurrences while the host prepares the batch
+  // layout, so the run can size its cycle tables without a mid-run sync
   auto* d_new = dev<cs_event>(ctx->d_new_ev, std::max<uint64_t>(1, n_new));
   auto* d_meta = dev<uint64_t>(ctx->d_assemble, 4ull * n_inst);
   if (!d_new || !d_meta) return broken(fail(ctx, CS_E_CUDA, "cudaMalloc(stream)"));
   if (n_new && cudaMemcpyAsync(d_new, ev, n_new * sizeof(cs_event), cudaMemcpyHostToDevice,
                                ctx->stream) != cudaSuccess)
     return broken(fail(ctx, CS_E_CUDA, "cudaMemcpyAsync(stream events)"));
-  std::vector<uint64_t>& meta = ctx->assemble_host;
+  auto& meta = ctx->assemble_host;
   meta.resize(4ull * n_inst);
   for (uint32_t i = 0; i < n_inst; ++i) {
     meta[4 * i + 0] = ctx->stage_off[i];
@@ -1856,10 +1910,35 @@ static int cs_stream_push_impl(cs_ctx* ctx, uint32_t n_inst, const uint64_t* off
   if (cudaMemcpyAsync(d_meta, meta.data(), meta.size() * 8, cudaMemcpyHostToDevice, ctx->stream) !=
       cudaSuccess)
     return broken(fail(ctx, CS_E_CUDA, "cudaMemcpyAsync(stream meta)"));
+  bool predict = ctx->tail_anchors.size() == n_inst && ctx->stream_anchor.size() == n_inst && !ctx->stream_fresh;
+  for (uint32_t i = 0; i < n_inst && predict; ++i) predict = ctx->stream_anchor[i] != UINT32_MAX;
+  if (predict) {
+    ctx->h_anchor_ids.assign(ctx->stream_anchor.begin(), ctx->stream_anchor.end());
+    ctx->h_new_anchors.resize(n_inst);
+    auto* da = dev<uint32_t>(ctx->d_anchor_ids, n_inst);
+    auto* dc = dev<uint64_t>(ctx->d_new_anchors, n_inst);
+    if (!da || !dc) return broken(fail(ctx, CS_E_CUDA, "cudaMalloc(stream count)"));
+    if (!ctx->ev_counted && cudaEventCreateWithFlags(&ctx->ev_counted, cudaEventDisableTiming) != cudaSuccess)
+      return broken(fail(ctx, CS_E_CUDA, "cudaEventCreate"));
+    CS_CUDA(cudaMemcpyAsync(da, ctx->h_anchor_ids.data(), n_inst * 4ull, cudaMemcpyHostToDevice, ctx->stream));
+    launch_stream_count(d_new, d_meta, da, n_inst, n_new, dc, ctx->stream);
+    CS_CUDA(cudaMemcpyAsync(ctx->h_new_anchors.data(), dc, n_inst * 8ull, cudaMemcpyDeviceToHost, ctx->stream));
+    CS_CUDA(cudaEventRecord(ctx->ev_counted, ctx->stream));
+  }
+  hp.mark("upload_new");
+  int rc = upload_layout(ctx, n_inst, ctx->stage_off.data(), true, n_workloads, wl);
+  if (rc != CS_OK) return broken(rc);
+  hp.mark("layout");
   launch_stream_assemble(static_cast<const cs_event*>(ctx->d_ev_prev.p), d_new, d_meta, n_inst,
                          ctx->stage_off[n_inst], static_cast<cs_event*>(ctx->d_ev.p), ctx->stream);
   if (cudaGetLastError() != cudaSuccess) return broken(fail(ctx, CS_E_CUDA, "stream assemble"));
-  hp.mark("copy_assemble");
+  ctx->pred_anchors.clear();
+  if (predict) {
+    CS_CUDA(cudaEventSynchronize(ctx->ev_counted));
+    ctx->pred_anchors.assign(ctx->tail_anchors.begin(), ctx->tail_anchors.end());
+    for (uint32_t i = 0; i < n_inst; ++i) ctx->pred_anchors[i] += ctx->h_new_anchors[i];
+  }
+  hp.mark("assemble_count");
   rc = cs_run(ctx, mask);
   if (rc != CS_OK) return broken(rc);
   hp.mark("run");

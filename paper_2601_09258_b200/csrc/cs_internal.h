@@ -269,6 +269,8 @@ void launch_wl32_expand(const uint32_t* wl32, uint64_t n, cs_workload* out, cuda
 void launch_wire_expand(const WireDev& w, const uint64_t* tile_begin, const uint64_t* tile_end,
                         uint32_t n_tiles, cs_event* out, cudaStream_t s);
 void launch_stream_keep(const DevBuffers& b, uint64_t* keep, cudaStream_t s);
+void launch_stream_count(const cs_event* fresh, const uint64_t* meta, const uint32_t* anchor, uint32_t n_inst,
+                         uint64_t n_new, uint64_t* out, cudaStream_t s);
 // streaming batch assembly: per instance i (meta[4i..4i+3] = dst offset, tail
 // start in prev, tail length, new-event offset) out[dst..] = prev tail, then
 // the instance's new events
@@ -300,5 +302,7 @@ void launch_gather_records(const DevBuffers& b, const DevConfig& cfg, uint32_t i
                            uint64_t nr, int scored, int det, cs_record* out, cudaStream_t s);
 void launch_gather_alerts(const DevBuffers& b, const DevConfig& cfg, uint32_t inst, uint64_t a0,
                           uint64_t na, cs_alert* out, cudaStream_t s);
+void launch_gather_alerts_all(const DevBuffers& b, const DevConfig& cfg, uint64_t n_all, cs_alert* out,
+                              cudaStream_t s);
 
 }  // namespace csb

@@ -1503,8 +1503,16 @@ __global__ void __launch_bounds__(kDetBlock / kDetK) k_detect_flags_blk(DevBuffe
 
 // After a micro-batch: the carry the next one starts from (written to `out`,
 // the carry in force for this batch stays readable for the getters).
-__global__ void k_stream_update(DevBuffers b, DevConfig cfg, StreamCarry* out, int detected) {
-  const uint32_t inst = blockIdx.x * blockDim.x + threadIdx.x;
+// One warp per instance: the carry the next micro-batch starts from.  The
+// detector keeps the last W-1 residuals, the flag of the last record and the
+// episode count (detector.cpp:91-130); the stage heuristic its two trailing
+// windows, newest first (cycles.cpp:204-250).  Lanes copy the windows and
+// take the batch's cycles 32 at a time (ballot compaction keeps the
+// reference's newest-first order).
+__global__ void __launch_bounds__(128) k_stream_update(DevBuffers b, DevConfig cfg, StreamCarry* out,
+                                                       int detected) {
+  const uint32_t inst = blockIdx.x * 4 + (threadIdx.x >> 5);
+  const uint32_t lane = threadIdx.x & 31;
   if (inst >= b.n_inst) return;
   const StreamCarry& c = b.stream[inst];
   StreamCarry& o = out[inst];
@@ -1515,47 +1523,66 @@ __global__ void k_stream_update(DevBuffers b, DevConfig cfg, StreamCarry* out, i
     const u64 total = c.seen + n;
     const u64 nh = total < keep ? total : keep;
     const u64 h0 = c.seen - c.n_hist;
-    for (u64 i = 0; i < nh; ++i) {
+    for (u64 i = lane; i < nh; i += 32) {
       const u64 u = total - nh + i;  // stream index
       o.hist[i] = u < c.seen ? c.hist[u - h0] : b.rec_resid[r0 + (u - c.seen)];
     }
-    o.n_hist = (uint32_t)nh;
-    o.prev_flag = n ? ((b.rec_flags[r0 + n - 1] & 2) ? 1u : 0u) : c.prev_flag;
-    o.seen = total;
-    o.episodes = c.episodes + b.inst[inst].n_alerts;
+    if (lane == 0) {
+      o.n_hist = (uint32_t)nh;
+      o.prev_flag = n ? ((b.rec_flags[r0 + n - 1] & 2) ? 1u : 0u) : c.prev_flag;
+      o.seen = total;
+      o.episodes = c.episodes + b.inst[inst].n_alerts;
+    }
   } else {
-    o.n_hist = c.n_hist;
-    for (uint32_t i = 0; i < c.n_hist; ++i) o.hist[i] = c.hist[i];
-    o.prev_flag = c.prev_flag;
-    o.seen = c.seen;
-    o.episodes = c.episodes;
+    for (uint32_t i = lane; i < c.n_hist; i += 32) o.hist[i] = c.hist[i];
+    if (lane == 0) {
+      o.n_hist = c.n_hist;
+      o.prev_flag = c.prev_flag;
+      o.seen = c.seen;
+      o.episodes = c.episodes;
+    }
   }
   // stage-heuristic history: newest cycles of this batch first, then the carry
   const u64 c0 = b.cyc_off[inst], c1 = b.cyc_off[inst + 1];
   const uint32_t W = (uint32_t)(cfg.cyc.stage_window < 32 ? cfg.cyc.stage_window : 32);
   uint32_t nd = 0, ng = 0;
-  for (u64 j = c1; j-- > c0 && (nd < W || ng < W);) {
-    if (b.c_stage[j] == CS_STAGE_PREFILL) continue;
-    if (nd < W) o.dur_hist[nd++] = (double)(b.c_end[j] - b.c_start[j]);
-    const bool has_gap = j > c0 || c.has_prev;
-    if (has_gap && ng < W) {
-      const i64 prev_end = j > c0 ? b.c_aend[j - 1] : c.last_aend;
-      const double g = (double)(b.c_start[j] - prev_end);
-      if (g >= 0.0) o.gap_hist[ng++] = g;
+  const uint32_t lt = (1u << lane) - 1u;
+  for (u64 top = c1; top > c0 && (nd < W || ng < W); top = top > c0 + 32 ? top - 32 : c0) {
+    const bool have = top > c0 + lane;
+    const u64 j = have ? top - 1 - lane : c0;
+    bool np = false, gv = false;
+    double dur = 0.0, g = 0.0;
+    if (have && b.c_stage[j] != CS_STAGE_PREFILL) {
+      np = true;
+      dur = (double)(b.c_end[j] - b.c_start[j]);
+      if (j > c0 || c.has_prev) {
+        const i64 prev_end = j > c0 ? b.c_aend[j - 1] : c.last_aend;
+        g = (double)(b.c_start[j] - prev_end);
+        gv = g >= 0.0;
+      }
     }
+    const uint32_t dm = __ballot_sync(0xffffffffu, np);
+    const uint32_t gm = __ballot_sync(0xffffffffu, gv);
+    const uint32_t di = nd + __popc(dm & lt), gi = ng + __popc(gm & lt);
+    if (np && di < W) o.dur_hist[di] = dur;
+    if (gv && gi < W) o.gap_hist[gi] = g;
+    nd = min(W, nd + __popc(dm));
+    ng = min(W, ng + __popc(gm));
   }
-  for (uint32_t i = 0; i < c.n_dur && nd < W; ++i) o.dur_hist[nd++] = c.dur_hist[i];
-  for (uint32_t i = 0; i < c.n_gap && ng < W; ++i) o.gap_hist[ng++] = c.gap_hist[i];
-  o.n_dur = nd;
-  o.n_gap = ng;
-  o.has_prev = (c1 > c0) ? 1u : c.has_prev;
-  o.last_aend = (c1 > c0) ? b.c_aend[c1 - 1] : c.last_aend;
-  o.cycle_off = c.cycle_off + (c1 - c0);
+  for (uint32_t i = lane; i < c.n_dur && nd + i < W; i += 32) o.dur_hist[nd + i] = c.dur_hist[i];
+  for (uint32_t i = lane; i < c.n_gap && ng + i < W; i += 32) o.gap_hist[ng + i] = c.gap_hist[i];
+  if (lane == 0) {
+    o.n_dur = min(W, nd + c.n_dur);
+    o.n_gap = min(W, ng + c.n_gap);
+    o.has_prev = (c1 > c0) ? 1u : c.has_prev;
+    o.last_aend = (c1 > c0) ? b.c_aend[c1 - 1] : c.last_aend;
+    o.cycle_off = c.cycle_off + (c1 - c0);
+  }
 }
 
 void launch_stream_update(const DevBuffers& b, const DevConfig& cfg, StreamCarry* out, int detected,
                           cudaStream_t s) {
-  k_stream_update<<<(b.n_inst + 63) / 64, 64, 0, s>>>(b, cfg, out, detected);
+  k_stream_update<<<(b.n_inst + 3) / 4, 128, 0, s>>>(b, cfg, out, detected);
 }
 
 // exclusive scan over instances of n_alerts: one CTA, kScanItems per thread per round
@@ -1684,11 +1711,8 @@ __global__ void k_gather_records(DevBuffers b, DevConfig cfg, uint32_t inst, uin
   out[i] = r;
 }
 
-__global__ void k_gather_alerts(DevBuffers b, DevConfig cfg, uint32_t inst, uint64_t a0,
-                                uint64_t na, cs_alert* out) {
-  const u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= na) return;
-  const u64 k = b.alert_rec[a0 + i];
+__device__ __forceinline__ cs_alert make_alert(const DevBuffers& b, const DevConfig& cfg, uint32_t inst,
+                                               u64 i /* within the instance */, u64 k) {
   const u64 g = b.rec_cycle[k];
   const cs_workload w = b.wl[b.c_wl[g]];
   cs_alert a;
@@ -1703,7 +1727,34 @@ __global__ void k_gather_alerts(DevBuffers b, DevConfig cfg, uint32_t inst, uint
   a.output_len = w.output_len;
   a.episode_id = i + (b.stream ? b.stream[inst].episodes : 0);
   a.record_index = k - b.rec_off[inst];
-  out[i] = a;
+  return a;
+}
+
+__global__ void k_gather_alerts(DevBuffers b, DevConfig cfg, uint32_t inst, uint64_t a0,
+                                uint64_t na, cs_alert* out) {
+  const u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= na) return;
+  out[i] = make_alert(b, cfg, inst, i, b.alert_rec[a0 + i]);
+}
+
+// every instance's alerts in one launch (alert_off on the device gives each
+// alert its instance); out[a] for a in [0, n_all)
+__global__ void k_gather_alerts_all(DevBuffers b, DevConfig cfg, uint64_t n_all, cs_alert* out) {
+  const u64 a = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (a >= n_all) return;
+  uint32_t lo = 0, hi = b.n_inst;  // last instance with alert_off[inst] <= a
+  while (hi - lo > 1) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (b.alert_off[mid] <= a) lo = mid;
+    else hi = mid;
+  }
+  out[a] = make_alert(b, cfg, lo, a - b.alert_off[lo], b.alert_rec[a]);
+}
+
+void launch_gather_alerts_all(const DevBuffers& b, const DevConfig& cfg, uint64_t n_all, cs_alert* out,
+                              cudaStream_t s) {
+  if (!n_all) return;
+  k_gather_alerts_all<<<(unsigned)((n_all + 255) / 256), 256, 0, s>>>(b, cfg, n_all, out);
 }
 
 void launch_gather_records(const DevBuffers& b, const DevConfig& cfg, uint32_t inst, uint64_t r0,
@@ -2219,11 +2270,25 @@ void launch_wire_expand(const WireDev& w, const uint64_t* tile_begin, const uint
 // uploaded event) from which events are carried into the next micro-batch:
 // the last closed cycle's end group start (cycles.cpp:147 drops the trailing
 // partial cycle; it is completed by the next batch).
-__global__ void k_stream_keep(DevBuffers b, uint64_t* keep) {
-  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+// per instance: where its carried tail starts (the last closed cycle's end,
+// cycles.cpp:147) and, in keep[n_inst + i], the anchor occurrences in that
+// tail (the next micro-batch's host-side sizing starts from them)
+__global__ void __launch_bounds__(128) k_stream_keep(DevBuffers b, uint64_t* keep) {
+  const uint32_t i = blockIdx.x * 4 + (threadIdx.x >> 5);
+  const uint32_t lane = threadIdx.x & 31;
   if (i >= b.n_inst) return;
   const u64 c0 = b.cyc_off[i], c1 = b.cyc_off[i + 1];
-  keep[i] = c1 > c0 ? b.c_last[c1 - 1] - b.inst_off[i] : 0;
+  const u64 k = c1 > c0 ? b.c_last[c1 - 1] - b.inst_off[i] : 0;
+  const uint32_t anchor = b.inst[i].anchor;
+  u64 n = 0;
+  if (anchor != 0xffffffffu)
+    for (u64 p = b.inst_off[i] + k + lane; p < b.inst_off[i + 1]; p += 32)
+      n += (b.ev[p].kind == CS_SPAN && b.ev[p].name_id == anchor) ? 1ull : 0ull;
+  n = warp_sum_u64(n);
+  if (lane == 0) {
+    keep[i] = k;
+    keep[b.n_inst + i] = n;
+  }
 }
 
 // one CTA per instance: its carried tail (from the previous batch's buffer)
@@ -2247,8 +2312,30 @@ void launch_stream_assemble(const cs_event* prev, const cs_event* fresh, const u
   if (n_inst) k_stream_assemble<<<n_inst, 128, 0, s>>>(prev, fresh, meta, total, n_inst, out);
 }
 
+// anchor occurrences among each instance's NEW events of a micro-batch (warp
+// per instance; meta as for k_stream_assemble, anchor ids per instance)
+__global__ void __launch_bounds__(128) k_stream_count(const cs_event* __restrict__ fresh,
+                                                      const uint64_t* __restrict__ meta,
+                                                      const uint32_t* __restrict__ anchor, uint32_t n_inst,
+                                                      uint64_t n_new, uint64_t* out) {
+  const uint32_t i = blockIdx.x * 4 + (threadIdx.x >> 5);
+  const uint32_t lane = threadIdx.x & 31;
+  if (i >= n_inst) return;
+  const u64 b0 = meta[4 * i + 3], b1 = i + 1 < n_inst ? meta[4 * (i + 1) + 3] : n_new;
+  const uint32_t a = anchor[i];
+  u64 n = 0;
+  for (u64 p = b0 + lane; p < b1; p += 32) n += (fresh[p].kind == CS_SPAN && fresh[p].name_id == a) ? 1ull : 0ull;
+  n = warp_sum_u64(n);
+  if (lane == 0) out[i] = n;
+}
+
+void launch_stream_count(const cs_event* fresh, const uint64_t* meta, const uint32_t* anchor, uint32_t n_inst,
+                         uint64_t n_new, uint64_t* out, cudaStream_t s) {
+  if (n_inst) k_stream_count<<<(n_inst + 3) / 4, 128, 0, s>>>(fresh, meta, anchor, n_inst, n_new, out);
+}
+
 void launch_stream_keep(const DevBuffers& b, uint64_t* keep, cudaStream_t s) {
-  if (b.n_inst) k_stream_keep<<<(b.n_inst + 127) / 128, 128, 0, s>>>(b, keep);
+  if (b.n_inst) k_stream_keep<<<(b.n_inst + 3) / 4, 128, 0, s>>>(b, keep);
 }
 
 // ------------------------------------------- counter-weighted mu (§8f #1)
