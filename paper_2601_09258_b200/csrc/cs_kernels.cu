@@ -342,6 +342,7 @@ __device__ void cache_flush_warp(NameCache& c, NameStat* g, WarpNameRow* wrows) 
 constexpr int kScanWarpThreads = 256;
 constexpr u64 kWalk = 1ull << 63;  // a_pos flag: the group start needs a walk back
 constexpr int kScanUnroll = 4;
+constexpr uint32_t kSampleSplit = 4;  // sub-ranges per tile in the sample pass
 
 struct Ev8 {
   u64 a, b, c, d;  // start, duration, (name | kind/cat/flags << 32), payload
@@ -407,13 +408,19 @@ __global__ void __launch_bounds__(kScanWarpThreads, 3)
   const uint32_t k_end = runs ? ((gw + 1) * per_warp < n_list ? (gw + 1) * per_warp : n_list) : n_list;
   const uint32_t k_step = runs ? 1u : nw;
   for (uint32_t k = k0; k < k_end; k += k_step) {
-    const uint32_t t = list ? list[k] : k;
+    // the sample pass splits each tile into kSampleSplit sub-ranges (moments
+    // only, order-free), so its few tiles still spread over the whole GPU
+    const uint32_t t = sample ? list[k / kSampleSplit] : (list ? list[k] : k);
     const uint32_t inst = b.tile_inst[t];
-    const u64 tb = b.tile_begin[t];
+    u64 tb = b.tile_begin[t];
     u64 te = b.tile_end[t];
     if (sample) {
       const u64 lim = b.inst_off[inst] + kSampleEvents;
       te = te < lim ? te : lim;
+      const u64 sub = (u64)(k % kSampleSplit) * (kTileEvents / kSampleSplit);
+      const u64 sb = tb + sub, se = sb + kTileEvents / kSampleSplit;
+      tb = sb;
+      te = te < se ? te : se;
       if (te < tb) te = tb;
     }
     bool active = do_anchor;
@@ -788,21 +795,38 @@ __global__ void __launch_bounds__(256) k_bounds_tile(DevBuffers b) {
 // records are contiguous and start at rec_off[i].
 constexpr int kRecBlock = 1024;
 
-__global__ void k_records_count(DevBuffers b, DevConfig cfg) {
-  __shared__ uint32_t s_w[32];
-  const u64 g = (u64)blockIdx.x * kRecBlock + threadIdx.x;
-  bool ok = false;
-  if (g < b.n_cycles)
-    ok = b.c_wl[g] >= 0 && (cfg.cyc.include_prefill || b.c_stage[g] != CS_STAGE_PREFILL) &&
-         g - b.cyc_off[b.c_inst[g]] + (b.stream ? b.stream[b.c_inst[g]].cycle_off : 0) >=
-             (u64)cfg.cyc.monitor_from_cycle;
-  const uint32_t m = __ballot_sync(0xffffffffu, ok);
-  if ((threadIdx.x & 31) == 0) s_w[threadIdx.x >> 5] = __popc(m);
+// cycle g yields a record (cycles.cpp:372-383); the instance-relative index
+// test (monitor_from_cycle, streaming offsets) only loads the instance when
+// it can matter
+__device__ __forceinline__ bool rec_ok(const DevBuffers& b, const DevConfig& cfg, u64 g, bool need_index) {
+  if (!(b.c_wl[g] >= 0 && (cfg.cyc.include_prefill || b.c_stage[g] != CS_STAGE_PREFILL))) return false;
+  if (!need_index) return true;
+  const uint32_t inst = b.c_inst[g];
+  return g - b.cyc_off[inst] + (b.stream ? b.stream[inst].cycle_off : 0) >= (u64)cfg.cyc.monitor_from_cycle;
+}
+
+// kRecBlock cycles per CTA of kRecThreads, kRecBlock / kRecThreads per thread
+// (thread stride: coalesced), independent loads in flight
+constexpr int kRecThreads = 256;
+constexpr int kRecPer = kRecBlock / kRecThreads;
+
+__global__ void __launch_bounds__(kRecThreads) k_records_count(DevBuffers b, DevConfig cfg) {
+  __shared__ uint32_t s_w[kRecThreads / 32];
+  const bool need_index = cfg.cyc.monitor_from_cycle > 0 || b.stream;
+  const u64 g0 = (u64)blockIdx.x * kRecBlock + threadIdx.x;
+  uint32_t n = 0;
+#pragma unroll
+  for (int r = 0; r < kRecPer; ++r) {
+    const u64 g = g0 + (u64)r * kRecThreads;
+    n += (g < b.n_cycles && rec_ok(b, cfg, g, need_index)) ? 1u : 0u;
+  }
+  n = (uint32_t)warp_sum_u64(n);
+  if ((threadIdx.x & 31) == 0) s_w[threadIdx.x >> 5] = n;
   __syncthreads();
-  if (threadIdx.x < 32) {
-    u64 v = s_w[threadIdx.x];
-    v = warp_sum_u64(v);
-    if (threadIdx.x == 0) b.block_tmp[blockIdx.x] = v;
+  if (threadIdx.x == 0) {
+    u64 t = 0;
+    for (int w = 0; w < kRecThreads / 32; ++w) t += s_w[w];
+    b.block_tmp[blockIdx.x] = t;
   }
 }
 
@@ -897,37 +921,52 @@ void launch_exclusive_scan(uint64_t* v, uint64_t n, uint64_t* total, uint64_t* t
   *launches += 3;
 }
 
-__global__ void k_records_scatter(DevBuffers b, DevConfig cfg) {
-  __shared__ uint32_t s_w[32];
-  const u64 g = (u64)blockIdx.x * kRecBlock + threadIdx.x;
+__global__ void __launch_bounds__(kRecThreads) k_records_scatter(DevBuffers b, DevConfig cfg) {
+  __shared__ uint32_t s_w[kRecPer][kRecThreads / 32];
+  __shared__ uint32_t s_rank[kRecBlock];  // exclusive record rank of each cycle in the block
+  const bool need_index = cfg.cyc.monitor_from_cycle > 0 || b.stream;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  bool ok = false;
-  if (g < b.n_cycles)
-    ok = b.c_wl[g] >= 0 && (cfg.cyc.include_prefill || b.c_stage[g] != CS_STAGE_PREFILL) &&
-         g - b.cyc_off[b.c_inst[g]] + (b.stream ? b.stream[b.c_inst[g]].cycle_off : 0) >=
-             (u64)cfg.cyc.monitor_from_cycle;
-  const uint32_t m = __ballot_sync(0xffffffffu, ok);
-  if (lane == 0) s_w[warp] = __popc(m);
-  __syncthreads();
-  if (warp == 0) {
-    uint32_t c = lane < kRecBlock / 32 ? s_w[lane] : 0;
-    const uint32_t x = c;
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(0xffffffffu, c, o);
-      if (lane >= o) c += y;
-    }
-    s_w[lane] = c - x;
+  const u64 gb = (u64)blockIdx.x * kRecBlock;
+  bool ok[kRecPer];
+  uint32_t m[kRecPer];
+#pragma unroll
+  for (int r = 0; r < kRecPer; ++r) {
+    const u64 g = gb + threadIdx.x + (u64)r * kRecThreads;
+    ok[r] = g < b.n_cycles && rec_ok(b, cfg, g, need_index);
+    m[r] = __ballot_sync(0xffffffffu, ok[r]);
+    if (lane == 0) s_w[r][warp] = __popc(m[r]);
   }
   __syncthreads();
-  const u64 rank = b.block_tmp[blockIdx.x] + s_w[warp] + __popc(m & lanemask_lt());
-  if (ok) b.rec_cycle[rank] = g;
-  // per-instance record offsets: rank of the instance's first cycle
-  if (g < b.n_cycles) {
-    const uint32_t inst = b.c_inst[g];
-    if (g == b.cyc_off[inst]) {
-      // every instance with cycles starting here (empty instances share it)
-      for (i64 i = inst; i >= 0 && b.cyc_off[i] == g; --i) b.rec_off[i] = rank;
+  if (threadIdx.x == 0) {  // exclusive prefix over (row, warp) in cycle order
+    uint32_t c = 0;
+    for (int r = 0; r < kRecPer; ++r)
+      for (int w = 0; w < kRecThreads / 32; ++w) {
+        const uint32_t x = s_w[r][w];
+        s_w[r][w] = c;
+        c += x;
+      }
+  }
+  __syncthreads();
+  const u64 base = b.block_tmp[blockIdx.x];
+#pragma unroll
+  for (int r = 0; r < kRecPer; ++r) {
+    const uint32_t local = s_w[r][warp] + __popc(m[r] & lanemask_lt());
+    s_rank[threadIdx.x + r * kRecThreads] = local;
+    if (ok[r]) b.rec_cycle[base + local] = gb + threadIdx.x + (u64)r * kRecThreads;
+  }
+  __syncthreads();
+  // per-instance record offsets: the rank of each instance's first cycle that
+  // falls in this block (empty instances share it)
+  if (threadIdx.x == 0) {
+    const u64 ge = gb + kRecBlock < b.n_cycles ? gb + kRecBlock : b.n_cycles;
+    uint32_t lo = 0, hi = b.n_inst + 1;  // first i with cyc_off[i] >= gb
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (b.cyc_off[mid] < gb) lo = mid + 1;
+      else hi = mid;
     }
+    for (uint32_t i = lo; i < b.n_inst && b.cyc_off[i] < ge; ++i)
+      b.rec_off[i] = base + s_rank[b.cyc_off[i] - gb];
   }
 }
 
@@ -1406,89 +1445,77 @@ __global__ void k_detect_flags(DevBuffers b, DevConfig cfg, uint64_t n_records) 
   }
 }
 
-// Register-blocked control chart for whole runs (no stream carry) with W <=
-// kDetMaxW: a thread takes kDetK consecutive records and loads the residuals
-// of their windows once (kDetMaxW + kDetK values); every statistic is still
-// the sequential oldest-to-newest sum of its own window (detector.cpp:96-104),
-// the previous record's statistic comes from the same registers.  256-thread
-// CTAs of 1024 records (= kDetBlock, so k_detect_scatter's blocks match).
-constexpr int kDetK = 4;
+// Control chart for whole runs (no stream carry), window length W <= kDetMaxW
+// as a template parameter (FixedPoint: W = 0).  A CTA takes kDetBlock
+// consecutive records: their residuals plus the W before them are staged in
+// shared memory with coalesced loads; each statistic is still the sequential
+// oldest-to-newest sum of its own window (detector.cpp:96-104) -- W ordered
+// adds, unrolled, and one division -- and the previous record's statistic
+// (in_episode = armed && flagged at t-1, detector.cpp:107-128) comes from the
+// CTA's statistics in shared memory.  Stores are coalesced (thread stride).
 constexpr int kDetMaxW = 16;
-__global__ void __launch_bounds__(kDetBlock / kDetK) k_detect_flags_blk(DevBuffers b, DevConfig cfg,
-                                                                        uint64_t n_records) {
-  __shared__ uint32_t s_w[kDetBlock / kDetK / 32];
+constexpr int kDetThreads = 256;
+template <int W>
+__global__ void __launch_bounds__(kDetThreads) k_detect_win(DevBuffers b, DevConfig cfg, uint64_t n_records) {
+  __shared__ double s_e[kDetBlock + kDetMaxW];
+  __shared__ double s_st[kDetBlock + 1];
+  __shared__ uint32_t s_w[kDetThreads / 32];
   n_records = records_on_device(b, n_records);
-  const u64 k0 = (u64)blockIdx.x * kDetBlock + (u64)threadIdx.x * kDetK;
-  const long long W = (long long)cfg.ctl.window;
-  const bool fixed_point = cfg.ctl.strategy == CS_FIXED_POINT;
+  const u64 k0 = (u64)blockIdx.x * kDetBlock;
+  if (k0 >= n_records) {
+    if (threadIdx.x == 0) b.block_tmp[blockIdx.x] = 0;
+    return;
+  }
+  const u64 kend = k0 + kDetBlock < n_records ? k0 + kDetBlock : n_records;
+  constexpr u64 kHalo = W > 0 ? (u64)W : 1u;  // the window of the record before the block
+  const u64 base = k0 >= kHalo ? k0 - kHalo : 0;  // s_e[i] = e[base + i]
+  const u64 need = kend - base;
+  for (u64 i = threadIdx.x; i < need; i += kDetThreads) s_e[i] = b.rec_resid[base + i];
+  __syncthreads();
   const u64 warm = cfg.ctl.warmup;
-  uint32_t n_alert = 0;
-  if (k0 < n_records) {
-    uint32_t inst = upper_bound_u64(b.rec_off, b.n_inst + 1, k0) - 1;
-    u64 rb = b.rec_off[inst];
-    u64 re = b.rec_off[inst + 1];
-    const double* e = b.rec_resid;
-    double v[kDetMaxW + kDetK];  // v[j] = e[k0 - kDetMaxW + j] inside the instance
+  // instance of the block's first record (one search per thread, cached)
+  uint32_t inst0 = upper_bound_u64(b.rec_off, b.n_inst + 1, k0) - 1;
+  auto stat_at = [&](u64 k, u64 rb) -> double {
+    if (W == 0) return s_e[k - base];
+    const u64 lo = k + 1 >= rb + W ? k + 1 - W : rb;
+    double sum = 0.0;
+    if (k + 1 - lo == (u64)W) {
+      const double* p = s_e + (k + 1 - W - base);
 #pragma unroll
-    for (int j = 0; j < kDetMaxW + kDetK; ++j) {
-      const long long a = (long long)k0 - kDetMaxW + j;
-      v[j] = (a >= (long long)rb && (u64)a < re && (u64)a < n_records) ? e[a] : 0.0;
+      for (int u = 0; u < W; ++u) sum = __dadd_rn(sum, p[u]);
+    } else {
+      for (u64 u = lo; u <= k; ++u) sum = __dadd_rn(sum, s_e[u - base]);
     }
-    // statistic of record k0 + q (q >= -1), instance-relative index t
-    auto stat_of = [&](int q) -> double {
-      if (fixed_point) return v[kDetMaxW + q];
-      const long long t = (long long)(k0 + q) - (long long)rb;
-      const long long begin = t + 1 >= W ? t + 1 - W : 0;
-      const long long a0 = (long long)k0 - kDetMaxW - (long long)rb;  // relative index of v[0]
-      double sum = 0.0;
-#pragma unroll
-      for (int j = 0; j < kDetMaxW + kDetK; ++j) {
-        const long long a = a0 + j;
-        if (a >= begin && a <= t) sum = __dadd_rn(sum, v[j]);
-      }
-      return __ddiv_rn(sum, (double)(t - begin + 1));
-    };
-    double limit = b.models[inst].ucl;
-    double prev_stat = k0 > rb ? stat_of(-1) : 0.0;
-    bool crossed = false;
-#pragma unroll
-    for (int q = 0; q < kDetK; ++q) {
-      const u64 k = k0 + q;
-      if (k >= n_records) break;
-      if (crossed || k >= re) {  // the block crosses into the next instance: per-record from here
-        crossed = true;
-        inst = upper_bound_u64(b.rec_off, b.n_inst + 1, k) - 1;
-        rb = b.rec_off[inst];
-        re = b.rec_off[inst + 1];
-        limit = b.models[inst].ucl;
-        const double* ei = e + rb;
-        const u64 t = k - rb;
-        const double st = window_stat(ei, t, (u64)W, cfg.ctl.strategy);
-        const bool armed = t >= warm;
-        const bool prev = t >= 1 && t - 1 >= warm && window_stat(ei, t - 1, (u64)W, cfg.ctl.strategy) > limit;
-        const bool flagged = armed && st > limit;
-        const bool alert = flagged && !prev;
-        b.rec_stat[k] = st;
-        b.rec_flags[k] = (armed ? 1 : 0) | (flagged ? 2 : 0) | (alert ? 4 : 0);
-        if (alert) {
-          atomicAdd(&b.inst[inst].n_alerts, 1ull);
-          ++n_alert;
-        }
-        continue;
-      }
-      const u64 t = k - rb;
-      const double st = stat_of(q);
-      const bool armed = t >= warm;
-      const bool prev = t >= 1 && t - 1 >= warm && prev_stat > limit;
-      const bool flagged = armed && st > limit;
-      const bool alert = flagged && !prev;
-      b.rec_stat[k] = st;
-      b.rec_flags[k] = (armed ? 1 : 0) | (flagged ? 2 : 0) | (alert ? 4 : 0);
-      if (alert) {
-        atomicAdd(&b.inst[inst].n_alerts, 1ull);
-        ++n_alert;
-      }
-      prev_stat = st;
+    return __ddiv_rn(sum, (double)(k + 1 - lo));
+  };
+  // statistics of the block's records (and of the record before the block)
+  for (u64 k = k0 + threadIdx.x; k < kend; k += kDetThreads) {
+    uint32_t inst = inst0;
+    while (b.rec_off[inst + 1] <= k) ++inst;
+    s_st[1 + (k - k0)] = stat_at(k, b.rec_off[inst]);
+  }
+  if (threadIdx.x == 0 && k0 > 0) {
+    const u64 k = k0 - 1;
+    const uint32_t inst = upper_bound_u64(b.rec_off, b.n_inst + 1, k) - 1;
+    s_st[0] = stat_at(k, b.rec_off[inst]);
+  }
+  __syncthreads();
+  uint32_t n_alert = 0;
+  for (u64 k = k0 + threadIdx.x; k < kend; k += kDetThreads) {
+    uint32_t inst = inst0;
+    while (b.rec_off[inst + 1] <= k) ++inst;
+    const u64 t = k - b.rec_off[inst];
+    const double limit = b.models[inst].ucl;
+    const double st = s_st[1 + (k - k0)];
+    const bool armed = t >= warm;
+    const bool prev = t >= 1 && t - 1 >= warm && s_st[k - k0] > limit;
+    const bool flagged = armed && st > limit;
+    const bool alert = flagged && !prev;
+    b.rec_stat[k] = st;
+    b.rec_flags[k] = (armed ? 1 : 0) | (flagged ? 2 : 0) | (alert ? 4 : 0);
+    if (alert) {
+      atomicAdd(&b.inst[inst].n_alerts, 1ull);
+      ++n_alert;
     }
   }
   const uint32_t wsum = (uint32_t)warp_sum_u64(n_alert);
@@ -1496,7 +1523,7 @@ __global__ void __launch_bounds__(kDetBlock / kDetK) k_detect_flags_blk(DevBuffe
   __syncthreads();
   if (threadIdx.x == 0) {
     u64 t = 0;
-    for (int w = 0; w < kDetBlock / kDetK / 32; ++w) t += s_w[w];
+    for (int w = 0; w < kDetThreads / 32; ++w) t += s_w[w];
     b.block_tmp[blockIdx.x] = t;
   }
 }
@@ -2585,6 +2612,7 @@ void launch_scan_events(const DevBuffers& b, const DevConfig&, int mode, bool sa
                         const uint32_t* list, uint32_t n_list, cudaStream_t s,
                         uint64_t* launches) {
   if (n_list == 0) return;
+  if (sample) n_list *= kSampleSplit;
   int dev = 0, sms = 148, per_sm = 1;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -2924,14 +2952,14 @@ void launch_records(const DevBuffers& b, const DevConfig& cfg, uint64_t, cudaStr
                     uint64_t* launches) {
   const u64 nb = (b.n_cycles + kRecBlock - 1) / kRecBlock;
   if (nb) {
-    k_records_count<<<(unsigned)nb, kRecBlock, 0, s>>>(b, cfg);
+    k_records_count<<<(unsigned)nb, kRecThreads, 0, s>>>(b, cfg);
     ++*launches;
   }
   // block_tmp[nb] receives the total
   k_scan_exclusive<<<1, 1024, 0, s>>>(b.block_tmp, nb, b.block_tmp + nb);
   ++*launches;
   if (nb) {
-    k_records_scatter<<<(unsigned)nb, kRecBlock, 0, s>>>(b, cfg);
+    k_records_scatter<<<(unsigned)nb, kRecThreads, 0, s>>>(b, cfg);
     ++*launches;
   }
   k_rec_off_tail<<<1, 1, 0, s>>>(b, b.block_tmp + nb);
@@ -3002,10 +3030,19 @@ void launch_detect(const DevBuffers& b, const DevConfig& cfg, uint64_t n_records
                    uint64_t* launches) {
   const u64 nb = (n_records + kDetBlock - 1) / kDetBlock;
   if (nb) {
-    if (!b.stream && (cfg.ctl.strategy == CS_FIXED_POINT || cfg.ctl.window <= (u64)kDetMaxW))
-      k_detect_flags_blk<<<(unsigned)nb, kDetBlock / kDetK, 0, s>>>(b, cfg, n_records);
-    else
+    const int W = cfg.ctl.strategy == CS_FIXED_POINT ? 0 : (int)cfg.ctl.window;
+    if (!b.stream && W <= kDetMaxW) {
+#define CS_DET_CASE(N)   case N:                  k_detect_win<N><<<(unsigned)nb, kDetThreads, 0, s>>>(b, cfg, n_records);     break;
+      switch (W) {
+        CS_DET_CASE(0) CS_DET_CASE(1) CS_DET_CASE(2) CS_DET_CASE(3) CS_DET_CASE(4) CS_DET_CASE(5)
+        CS_DET_CASE(6) CS_DET_CASE(7) CS_DET_CASE(8) CS_DET_CASE(9) CS_DET_CASE(10) CS_DET_CASE(11)
+        CS_DET_CASE(12) CS_DET_CASE(13) CS_DET_CASE(14) CS_DET_CASE(15) CS_DET_CASE(16)
+        default: break;
+      }
+#undef CS_DET_CASE
+    } else {
       k_detect_flags<<<(unsigned)nb, kDetBlock, 0, s>>>(b, cfg, n_records);
+    }
     ++*launches;
   }
   k_scan_exclusive<<<1, 1024, 0, s>>>(b.block_tmp, nb, b.block_tmp + nb);
