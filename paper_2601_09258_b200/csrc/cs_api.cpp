@@ -221,7 +221,7 @@ struct cs_ctx {
       d_seg_ctl;
   bool no_lut = false;       // CS_OPT_TRAVERSAL: score by tree traversal even with a cell table
   DevBuf d_cyc_off, c_start, c_end, c_apos, c_aend, c_first, c_last, c_inst, c_stage, c_local,
-      c_wl, c_comp, c_beta_tot, c_beta, c_coll, c_coll_n;
+      c_wl, c_comp, c_beta_tot, c_coll, c_coll_n;
   // records
   DevBuf d_rec_off, rec_cycle, rec_pred, rec_resid, rec_stat, rec_flags, alert_rec, d_alert_off,
       block_tmp;
@@ -353,7 +353,6 @@ DevBuffers make_buffers(cs_ctx* ctx) {
   b.c_wl = static_cast<int32_t*>(ctx->c_wl.p);
   b.c_comp = static_cast<int64_t*>(ctx->c_comp.p);
   b.c_beta_tot = static_cast<int64_t*>(ctx->c_beta_tot.p);
-  b.c_beta = static_cast<double*>(ctx->c_beta.p);
   b.c_coll = static_cast<double*>(ctx->c_coll.p);
   b.c_coll_n = static_cast<uint8_t*>(ctx->c_coll_n.p);
   b.rec_off = static_cast<uint64_t*>(ctx->d_rec_off.p);
@@ -1207,7 +1206,6 @@ static int cs_run_impl(cs_ctx* ctx, uint32_t mask) {
            dev<uint8_t>(ctx->c_stage, nc1) && dev<uint8_t>(ctx->c_local, nc1) &&
            dev<int32_t>(ctx->c_wl, nc1) && dev<int64_t>(ctx->c_comp, nc1 * std::max(P, 1)) &&
            dev<int64_t>(ctx->c_beta_tot, nc1 * std::max(C, 1)) &&
-           dev<double>(ctx->c_beta, nc1 * std::max(C, 1)) &&
            dev<double>(ctx->c_coll, nc1 * std::max(R, 1)) &&
            dev<uint8_t>(ctx->c_coll_n, nc1 * std::max(R, 1)) &&
            dev<uint64_t>(ctx->d_rec_off, n_inst + 1) && dev<uint64_t>(ctx->rec_cycle, nc1) &&
@@ -1275,7 +1273,7 @@ static int cs_run_impl(cs_ctx* ctx, uint32_t mask) {
   }
   // ---------------- single-read segmentation (k_segment_range)
   if (!ctx->given_run && ctx->allow_fused && !ctx->streaming && ctx->n_ev &&
-      segment_range_smem(cfg, (mask & CS_RUN_BETA) ? 1 : 0) >= 0) {
+      segment_range_smem(cfg, (mask & CS_RUN_BETA) ? 1 : 0, static_cast<uint32_t>(ctx->names.size())) >= 0) {
     uint64_t range_events = static_cast<uint64_t>(ctx->opt_range_events);
     if (!range_events) {
       const double epc = ctx->ev_per_cycle > 0.0 ? ctx->ev_per_cycle : 16.0;
@@ -1287,7 +1285,7 @@ static int cs_run_impl(cs_ctx* ctx, uint32_t mask) {
   }
   const uint32_t n_ranges = static_cast<uint32_t>(ctx->range_inst.size());
   if (!ctx->given_run && ctx->allow_fused && !ctx->streaming && n_ranges && ctx->ranges_built_for &&
-      segment_range_smem(cfg, (mask & CS_RUN_BETA) ? 1 : 0) >= 0) {
+      segment_range_smem(cfg, (mask & CS_RUN_BETA) ? 1 : 0, static_cast<uint32_t>(ctx->names.size())) >= 0) {
     const std::vector<InstState> h_init(ctx->h_inst.begin(), ctx->h_inst.end());
     uint64_t cap = std::max<uint64_t>(ctx->slot_cap, ctx->n_ev / 8 + 1024);
     for (int attempt = 0; attempt < 2 && !ctx->used_fused; ++attempt) {
@@ -1343,6 +1341,7 @@ static int cs_run_impl(cs_ctx* ctx, uint32_t mask) {
                           "cs_upload_unsorted sorts them on the device");
       uint64_t slots = 0;
       for (uint32_t i = 0; i < n_inst; ++i) slots += ctx->h_inst[i].n_anchors;
+      if (ctl[1] & 2u) break;  // a range denser than its anchor list: two-pass path
       if (ctl[1]) {  // more anchors than slots: exact capacity, once more
         cap = slots + 1024;
         continue;
@@ -2184,9 +2183,25 @@ int cs_get_beta(cs_ctx* ctx, uint32_t inst, int64_t* totals, double* beta, size_
   if (totals && nc * Cs != 0)
     CS_CUDA(cudaMemcpy(totals, static_cast<int64_t*>(ctx->c_beta_tot.p) + c0 * Cs, nc * Cs * 8,
                        cudaMemcpyDeviceToHost));
-  if (beta && nc * Cs != 0)
-    CS_CUDA(cudaMemcpy(beta, static_cast<double*>(ctx->c_beta.p) + c0 * Cs, nc * Cs * 8,
-                       cudaMemcpyDeviceToHost));
+  if (beta && nc * Cs != 0) {
+    // beta = total / cycle duration (rca.cpp:95-96, 119-121), formed here from
+    // the device's totals (masked to positive durations) and cycle bounds:
+    // one IEEE division, the same bits as a device __ddiv_rn
+    std::vector<int64_t> tot(totals ? 0 : nc * Cs), st(nc), en(nc);
+    int64_t* t = totals ? totals : tot.data();
+    if (!totals)
+      CS_CUDA(cudaMemcpy(t, static_cast<int64_t*>(ctx->c_beta_tot.p) + c0 * Cs, nc * Cs * 8,
+                         cudaMemcpyDeviceToHost));
+    CS_CUDA(cudaMemcpy(st.data(), static_cast<int64_t*>(ctx->c_start.p) + c0, nc * 8, cudaMemcpyDeviceToHost));
+    CS_CUDA(cudaMemcpy(en.data(), static_cast<int64_t*>(ctx->c_end.p) + c0, nc * 8, cudaMemcpyDeviceToHost));
+    for (uint64_t k = 0; k < nc; ++k) {
+      const double dur = static_cast<double>(en[k] - st[k]);
+      for (uint64_t c = 0; c < Cs; ++c) {
+        const int64_t v = t[k * Cs + c];
+        beta[k * Cs + c] = v > 0 ? static_cast<double>(v) / dur : 0.0;
+      }
+    }
+  }
   return CS_OK;
 }
 
@@ -2242,8 +2257,13 @@ static int cs_suspicion_rank_impl(cs_ctx* ctx, uint32_t inst, const uint64_t* no
       if (S) {
         CS_CUDA(cudaMemcpy(&w.totals[k * S], static_cast<int64_t*>(ctx->c_beta_tot.p) + c * S, S * 8,
                            cudaMemcpyDeviceToHost));
-        CS_CUDA(cudaMemcpy(&w.beta[k * S], static_cast<double*>(ctx->c_beta.p) + c * S, S * 8,
-                           cudaMemcpyDeviceToHost));
+        int64_t se[2];
+        CS_CUDA(cudaMemcpy(&se[0], static_cast<int64_t*>(ctx->c_start.p) + c, 8, cudaMemcpyDeviceToHost));
+        CS_CUDA(cudaMemcpy(&se[1], static_cast<int64_t*>(ctx->c_end.p) + c, 8, cudaMemcpyDeviceToHost));
+        for (uint32_t q = 0; q < S; ++q) {  // beta = total / duration, formed on read
+          const int64_t v = w.totals[k * S + q];
+          w.beta[k * S + q] = v > 0 ? static_cast<double>(v) / static_cast<double>(se[1] - se[0]) : 0.0;
+        }
         if (with_mu) {
           CS_CUDA(cudaMemcpy(&w.mu[k * S], static_cast<double*>(ctx->d_mu.p) + c * S, S * 8,
                              cudaMemcpyDeviceToHost));

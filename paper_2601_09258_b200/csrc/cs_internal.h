@@ -134,7 +134,6 @@ struct DevBuffers {
   int32_t* c_wl;                // workload index, -1 no carrier, -2 invalid carrier
   int64_t* c_comp;              // n_cycles x n_phases
   int64_t* c_beta_tot;          // n_cycles x n_beta
-  double* c_beta;               // n_cycles x n_beta
   double* c_coll;               // n_cycles x n_comm
   uint8_t* c_coll_n;            // contributions per (cycle, comm slot)
   // records (instance i at rec_off[i], device-computed)
@@ -211,7 +210,7 @@ void launch_range_inst(const DevBuffers& b, const SegMeta& sm, const uint32_t* i
                        uint64_t* slot_off, cudaStream_t s, uint64_t* launches);
 // dynamic shared memory of k_segment_range for this configuration; -1 when the
 // slot counts need the wide reduce (the fused pass is then not used)
-int segment_range_smem(const DevConfig& cfg, int do_beta);
+int segment_range_smem(const DevConfig& cfg, int do_beta, uint32_t n_names);
 // K4' (k_stage_jacobi): the stage heuristic over chunks of cycle slots with
 // Jacobi refinement; st[0] = c_stage (holding the local stages), st[1] a
 // scratch copy; *final_parity = index of the array with the result

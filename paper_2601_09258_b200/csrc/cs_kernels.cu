@@ -52,6 +52,16 @@ __device__ __forceinline__ u64 ld_acquire(const u64* p) {
 __device__ __forceinline__ void st_release(u64* p, u64 v) {
   asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
+// look-back words that carry nothing but their own value: relaxed is enough
+// (no MEMBAR behind the warp's row stores, no L1 invalidation)
+__device__ __forceinline__ u64 ld_relaxed(const u64* p) {
+  u64 v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed(u64* p, u64 v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
 __device__ __forceinline__ u64 warp_sum_u64(u64 v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -60,6 +70,11 @@ __device__ __forceinline__ u64 warp_sum_u64(u64 v) {
 __device__ __forceinline__ uint32_t lanemask_lt() {
   uint32_t m;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+__device__ __forceinline__ uint32_t lanemask_le() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_le;" : "=r"(m));
   return m;
 }
 
@@ -317,6 +332,89 @@ __device__ void cache_flush_warp(NameCache& c, NameStat* g, WarpNameRow* wrows) 
   for (int i = 0; i < kNameCache; ++i)
     rows_merge(wrows, g, c.name[i] != 0xffffffffu && c.cnt[i] > 0, c.name[i], c.cnt[i], c.sum[i],
                c.lo[i], c.hi[i]);
+  __syncwarp();
+  if (lane < kWarpNameRows) {
+    const WarpNameRow r = wrows[lane];
+    if (r.name != 0xffffffffu && r.cnt) {
+      atomicAdd(&g[r.name].count, (u64)r.cnt);
+      atomicAdd(&g[r.name].sum, r.sum);
+      atomic_add_u128(&g[r.name].sumsq_lo, &g[r.name].sumsq_hi, r.sq_lo, r.sq_hi);
+    }
+  }
+  __syncwarp();
+  cache_clear(c);
+}
+
+// Shared-memory variant of NameCache for kernels short of registers: lane
+// columns [entry][32] of one warp's block; same semantics as NameCache.
+struct SNameCache {
+  uint32_t* name;  // [kNameCache][32]
+  uint32_t* cnt;
+  u64 *sum, *lo, *hi;
+  int lane;
+  __device__ static SNameCache at(void* base, int lane) {
+    SNameCache c;
+    c.sum = reinterpret_cast<u64*>(base);
+    c.lo = c.sum + kNameCache * 32;
+    c.hi = c.lo + kNameCache * 32;
+    c.name = reinterpret_cast<uint32_t*>(c.hi + kNameCache * 32);
+    c.cnt = c.name + kNameCache * 32;
+    c.lane = lane;
+    return c;
+  }
+  static constexpr int kBytes = kNameCache * 32 * (3 * 8 + 2 * 4);
+};
+
+__device__ __forceinline__ void cache_clear(SNameCache& c) {
+#pragma unroll
+  for (int i = 0; i < kNameCache; ++i) {
+    c.name[i * 32 + c.lane] = 0xffffffffu;
+    c.cnt[i * 32 + c.lane] = 0;
+    c.sum[i * 32 + c.lane] = c.lo[i * 32 + c.lane] = c.hi[i * 32 + c.lane] = 0;
+  }
+}
+
+__device__ __forceinline__ void cache_add(SNameCache& c, NameStat* g, uint32_t name, i64 d) {
+  u64 lo, hi;
+  square_u128(d, lo, hi);
+  int hit = -1, free_slot = -1;
+#pragma unroll
+  for (int i = 0; i < kNameCache; ++i) {
+    const uint32_t n = c.name[i * 32 + c.lane];
+    if (n == name && hit < 0) hit = i;
+    if (n == 0xffffffffu && free_slot < 0) free_slot = i;
+  }
+  if (hit < 0 && free_slot >= 0) {
+    hit = free_slot;
+    c.name[hit * 32 + c.lane] = name;
+  }
+  if (hit < 0) {
+    atomicAdd(&g[name].count, 1ull);
+    atomicAdd(&g[name].sum, (u64)d);
+    atomic_add_u128(&g[name].sumsq_lo, &g[name].sumsq_hi, lo, hi);
+    return;
+  }
+  const int k = hit * 32 + c.lane;
+  c.cnt[k] += 1;
+  c.sum[k] += (u64)d;
+  const u64 ol = c.lo[k], nl = ol + lo;
+  c.hi[k] += hi + (nl < ol ? 1ull : 0ull);
+  c.lo[k] = nl;
+}
+
+__device__ void cache_flush_warp(SNameCache& c, NameStat* g, WarpNameRow* wrows) {
+  const int lane = c.lane;
+  if (lane < kWarpNameRows) {
+    wrows[lane].name = 0xffffffffu;
+    wrows[lane].cnt = 0;
+    wrows[lane].sum = wrows[lane].sq_lo = wrows[lane].sq_hi = 0;
+  }
+  __syncwarp();
+  for (int i = 0; i < kNameCache; ++i) {
+    const int k = i * 32 + lane;
+    const uint32_t n = c.name[k], cn = c.cnt[k];
+    rows_merge(wrows, g, n != 0xffffffffu && cn > 0, n, cn, c.sum[k], c.lo[k], c.hi[k]);
+  }
   __syncwarp();
   if (lane < kWarpNameRows) {
     const WarpNameRow r = wrows[lane];
@@ -2009,7 +2107,6 @@ __global__ void __launch_bounds__(256, 3) k_cycle_reduce_v2(DevBuffers b, DevCon
       const i64 dur = s_dur[lc];
       const i64 t = dur > 0 ? beta[c * SN + lc] : 0;
       b.c_beta_tot[g0 * C + idx] = t;
-      b.c_beta[g0 * C + idx] = t > 0 ? __ddiv_rn((double)t, (double)dur) : 0.0;
     }
     for (uint32_t idx = tid; idx < n_live * (uint32_t)R; idx += NT) {
       const uint32_t lc = idx / (uint32_t)R, r = idx - lc * (uint32_t)R;
@@ -2109,8 +2206,8 @@ __global__ void __launch_bounds__(128) k_cycle_reduce_wide(DevBuffers b, DevConf
   }
 }
 
-// beta = total / cycle duration for every (cycle, class) of the wide reduce
-// (rca.cpp:95-96, 119-121), coalesced over the row-major table
+// class totals of the wide reduce masked to cycles with a positive duration
+// (rca.cpp:95-96, 119-121); beta = total / duration is formed on read
 __global__ void k_beta_finalize(DevBuffers b, int C) {
   const u64 k = (u64)blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= b.n_cycles * (u64)C) return;
@@ -2118,7 +2215,6 @@ __global__ void k_beta_finalize(DevBuffers b, int C) {
   const i64 dur = b.c_end[g] - b.c_start[g];
   const i64 t = dur > 0 ? b.c_beta_tot[k] : 0;
   b.c_beta_tot[k] = t;
-  b.c_beta[k] = t > 0 ? __ddiv_rn((double)t, (double)dur) : 0.0;
 }
 
 // ---------------------------------------------------- wire-format expand
@@ -3092,79 +3188,177 @@ void launch_freq_cycles(const cs_event* ev, uint64_t begin, uint64_t end, int64_
 
 // =================================================== single-read segmentation
 // K1+K2+K3 with the events read from DRAM once (CS_OPT_FUSED).  Work unit: a
-// WARP RANGE of consecutive events of one instance, sized for ~32 cycles (one
-// per lane), claimed in order by a persistent grid.  Every warp is independent
-// (no CTA barriers), so one warp's DRAM-bound scan overlaps its neighbours'
-// L2-bound reduce.  Per range:
+// WARP RANGE of consecutive events of one instance, sized for ~32 cycles,
+// claimed in order by a persistent grid.  Every warp is independent (no CTA
+// barriers), so one warp's DRAM-bound scan overlaps its neighbours' L2-bound
+// reduce.  Per range:
 //   A. the warp streams its events (coalesced 256-bit loads): PythonCall
 //      moments for the anchor ranking (cycles.cpp:50-59), the canonical-order
-//      check, and the speculated anchor's occurrences compacted in order
+//      check, and the speculated anchor's occurrences listed in shared memory
 //      (cycles.cpp:127-131); it publishes its anchor count and keeps reading
 //      past the range to the next anchor, which closes its last cycle;
 //   B. lane k reduces the cycle opened by anchor k, walking its events in
-//      order -- L2 hits, the warp has just streamed them -- with the
-//      accumulators and arithmetic of k_cycle_reduce_v2 (cycles.cpp:157-166,
-//      205-229, 256-281; rca.cpp:87-129);
+//      order (L2 hits: the warp has just streamed them), branch-free: every
+//      event adds its clipped duration to lane-private shared-memory rows
+//      (class occupancy, collective occupancy and count; a per-lane dummy row
+//      absorbs the events that add nothing), so the warp executes one path
+//      whatever mix of event kinds its lanes meet (cycles.cpp:157-166, 205-229,
+//      256-281; rca.cpp:87-129).  Component durations are the class rows of
+//      the phase functions' names (a clipped term > 0 implies duration > 0,
+//      so both sums take the same terms).  Collective beta is a sum of
+//      quotients in event order (rca.cpp:108-115): a (cycle, slot) with one
+//      contribution is 0.0 + q = q, the quotient of its integer sum; one with
+//      several is re-summed in order by its lane.  Rows are 32-bit when the
+//      batch proves duration x events < 2^32 for each cycle, 64-bit otherwise;
 //   C. a decoupled look-back over the preceding ranges gives the global rank
 //      of the range's first anchor = the slot of its first cycle, and the warp
 //      writes its cycle rows.
 // An instance's last anchor opens no complete cycle (cycles.cpp:147): its slot
 // is a hole (empty event range, c_wl = kHoleWl) that every consumer skips.
 // The anchor guess is verified afterwards by k_rank over the full moments; a
-// wrong guess (or an ambiguous ranking) re-runs the two-pass path.
+// wrong guess, an ambiguous ranking, a range with more than kSegList anchors
+// or an equal-timestamp group at an anchor (lower_bound before the anchor's
+// position) re-runs the two-pass path.
 constexpr int kSegThreads = 256;
 constexpr int kSegWarps = kSegThreads / 32;
+constexpr int kSegList = 128;      // anchors of one range listed in shared memory
+constexpr int kSegNames = 1024;    // name table staged in shared memory
+constexpr uint32_t kSegTie = 0x80000000u;  // apos flag: equal start_ts before the anchor
+
+// u64 accumulator rows [row][33]: [0, C) classes, [C, C+R) collectives
+// (count << 48 | integer sum), [C+R, C+R+P) components of phases without a
+// class row, then one dummy row
+constexpr int kCollShift = 48;
+__host__ __device__ constexpr uint32_t seg_rows(int P, int C, int R) {
+  return (uint32_t)(C + R + P + 3);  // + dummy rows for classes, components, collectives
+}
+__host__ __device__ constexpr uint32_t seg_words(int P, int C, int R) {
+  return seg_rows(P, C, R) * 33u * 2u;
+}
+
+struct SegWarpSmem {  // fixed-size per-warp state (static shared memory)
+  i64 ats[kSegList];        // range anchors: start_ts
+  uint32_t apos[kSegList];  // range anchors: offset in the range | kSegTie
+  uint32_t pn[64];          // PythonCall compaction (name, duration)
+  i64 pd[64];
+  i64 dur[32];              // batch cycles: duration
+};
+
+// one cycle's events in order, branch-free (cycles.cpp:157-166, 205-229,
+// 256-281; rca.cpp:87-129): every event adds its clipped duration to the
+// lane's rows named by its name, or to a dummy row when none applies.  The
+// three rows one event touches are distinct (class rows / dummy 0, component
+// rows / dummy 1, collective rows / dummy 2), so their read-modify-writes
+// overlap; consecutive events may share rows and stay in order.
+template <bool kGuard>
+__device__ __forceinline__ void seg_walk_step(const cs_event* __restrict__ ev, u64 j0, u64 last, i64 ce,
+                                              const uint32_t* __restrict__ s_ninfo, u64* acc, uint32_t dummy,
+                                              uint32_t C, uint32_t R, uint32_t& fm, uint32_t& kw, int32_t& wl,
+                                              bool& wl_found) {
+  const uint32_t SN = 33;
+  Ev8 e[kRedUnroll];
+#pragma unroll
+  for (int q = 0; q < kRedUnroll; ++q) {
+    if (!kGuard || j0 + q < last) e[q] = ldg256(ev + j0 + q);
+    else {
+      e[q].a = 0;
+      e[q].b = 0;
+      e[q].c = (u64)CS_FLOW << 32;
+      e[q].d = 0;
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < kRedUnroll; ++q) {
+    const uint32_t name = (uint32_t)e[q].c;
+    const uint32_t kc = (uint32_t)(e[q].c >> 32);
+    const uint32_t flags = kc >> 16;
+    const bool span = (kc & 0xffu) == CS_SPAN;
+    const uint32_t info = span ? s_ninfo[name] : (dummy | ((dummy + 1u) << 8));
+    kw |= info >> 30;
+    // clipped = max(0, min(st + d, ce) - st) = min(d, ce - st) when d > 0
+    const i64 d = (i64)e[q].b;
+    const i64 rem = ce - (i64)e[q].a;
+    const u64 c = d > 0 ? (u64)(d < rem ? d : rem) : 0ull;
+    const uint32_t slot = (uint32_t)(e[q].d >> 32);
+    const bool cl = span && ((kc >> 8) & 0xffu) == CS_CAT_COLLECTIVE_COMM && (flags & CS_EV_HAS_COMM) &&
+                    slot < R && d > 0;
+    u64* pb = acc + (info & 0xffu) * SN;
+    u64* pp = acc + ((info >> 8) & 0xffu) * SN;
+    u64* pc = acc + (cl ? C + slot : dummy + 2u) * SN;
+    const u64 vb = *pb, vp = *pp, vc = *pc;
+    *pb = vb + c;
+    *pp = vp + c;
+    *pc = vc + c + (1ull << kCollShift);
+    fm = (fm == 0u && (flags & CS_EV_FM_MASK)) ? (4u | (flags & CS_EV_FM_MASK)) : fm;
+    const bool hb = (flags & CS_EV_HAS_BATCH) != 0;
+    wl = (!wl_found && hb) ? ((flags & CS_EV_WL_OK) ? (int32_t)(uint32_t)e[q].d : -2) : wl;
+    wl_found |= hb;
+  }
+}
+
+__device__ __forceinline__ void seg_walk(const cs_event* __restrict__ ev, u64 first, u64 last, i64 ce,
+                                         const uint32_t* __restrict__ s_ninfo, u64* acc, uint32_t dummy,
+                                         uint32_t C, uint32_t R, uint32_t& fm, uint32_t& kw, int32_t& wl) {
+  bool wl_found = false;
+  u64 j0 = first;
+  for (; j0 + kRedUnroll <= last; j0 += kRedUnroll)
+    seg_walk_step<false>(ev, j0, last, ce, s_ninfo, acc, dummy, C, R, fm, kw, wl, wl_found);
+  if (j0 < last) seg_walk_step<true>(ev, j0, last, ce, s_ninfo, acc, dummy, C, R, fm, kw, wl, wl_found);
+}
 
 __global__ void __launch_bounds__(kSegThreads, 2)
     k_segment_range(DevBuffers b, DevConfig cfg, SegMeta sm, int do_beta) {
   extern __shared__ __align__(16) unsigned char s_dyn[];
-  __shared__ uint32_t s_ninfo[kFNamesSmem];
+  __shared__ uint32_t s_ninfo[kSegNames];
+  __shared__ int32_t s_pbs[16];  // phase -> class row of its name (-1: own component row)
   __shared__ WarpNameRow s_rows[kSegWarps * kWarpNameRows];
-  __shared__ uint32_t s_pn[kSegWarps][64];
-  __shared__ i64 s_pd[kSegWarps][64];
+  __shared__ SegWarpSmem s_w[kSegWarps];
   const int P = cfg.cyc.n_phases;
   const int C = do_beta ? cfg.cyc.n_beta_slots : 0;
   const int R = do_beta ? cfg.cyc.n_comm_slots : 0;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  auto pack_info = [&](const cs_name_info& ni) -> uint32_t {
-    const uint32_t ph = (ni.phase >= 0 && ni.phase < P) ? (uint32_t)ni.phase : 15u;
-    const uint32_t bs = (ni.beta_slot >= 0 && ni.beta_slot < C) ? (uint32_t)ni.beta_slot : 255u;
-    return ph | (bs << 4) | ((ni.flags & 3u) << 12);
-  };
-  for (uint32_t i = threadIdx.x; i < b.n_names && i < (uint32_t)kFNamesSmem; i += blockDim.x)
-    s_ninfo[i] = pack_info(b.names[i]);
-  __syncthreads();  // the only CTA barrier: warps are independent from here on
-  // per-warp [slot][lane] accumulator columns (row stride 33)
+  const uint32_t NR = seg_rows(P, C, R), dummy = NR - 3;
+  if (threadIdx.x < 16) s_pbs[threadIdx.x] = -1;
+  __syncthreads();
+  // name -> (class row | component row << 8 | keyword bits << 30); a phase
+  // name with a class row accumulates once, into the class row
+  for (uint32_t i = threadIdx.x; i < b.n_names; i += blockDim.x) {
+    const cs_name_info ni = b.names[i];
+    const bool ph = ni.phase >= 0 && ni.phase < P;
+    const bool bs = ni.beta_slot >= 0 && ni.beta_slot < C;
+    const uint32_t brow = bs ? (uint32_t)ni.beta_slot : dummy;
+    const uint32_t prow = (ph && !bs) ? (uint32_t)(C + R + ni.phase) : dummy + 1u;
+    s_ninfo[i] = brow | (prow << 8) | ((ni.flags & 3u) << 30);
+    if (ph && bs) s_pbs[ni.phase] = ni.beta_slot;
+  }
+  __syncthreads();  // the only CTA barriers: warps are independent from here on
   const uint32_t SN = 33;
-  const uint32_t words = ((uint32_t)(P + C + R) * SN * 2 + (uint32_t)R * SN + 64 + 3) & ~3u;  // 16-B aligned
-  uint32_t* wbase = reinterpret_cast<uint32_t*>(s_dyn) + (u64)warp * words;
-  i64* comp = reinterpret_cast<i64*>(wbase);
-  i64* beta = comp + (u64)P * SN;
-  double* coll = reinterpret_cast<double*>(beta + (u64)C * SN);
-  i64* s_dur = reinterpret_cast<i64*>(coll + (u64)R * SN);     // [32]
-  uint32_t* colln = reinterpret_cast<uint32_t*>(s_dur + 32);    // [R][SN]
+  u64* acc = reinterpret_cast<u64*>(s_dyn) + (u64)warp * NR * SN;
+  SegWarpSmem& w = s_w[warp];
   WarpNameRow* wrows = s_rows + warp * kWarpNameRows;
-  uint32_t* pn = s_pn[warp];
-  i64* pd = s_pd[warp];
-  NameCache cache;
+  const u64 mP = P ? ((1ull << 32) + (u64)P - 1) / (u64)P : 0;
+  const u64 mC = C ? ((1ull << 32) + (u64)C - 1) / (u64)C : 0;
+  const u64 mR = R ? ((1ull << 32) + (u64)R - 1) / (u64)R : 0;
+  SNameCache cache = SNameCache::at(s_dyn + (u64)kSegWarps * seg_words(P, C, R) * 4 + (u64)warp * SNameCache::kBytes, lane);
   cache_clear(cache);
+  __syncwarp();
   uint32_t cur_inst = 0xffffffffu, npend = 0;
   NameStat* gstats = b.stats;
   auto drain = [&](uint32_t take) {
     __syncwarp();
-    if ((uint32_t)lane < take) cache_add(cache, gstats, pn[lane], pd[lane]);
+    if ((uint32_t)lane < take) cache_add(cache, gstats, w.pn[lane], w.pd[lane]);
     __syncwarp();
     const uint32_t rest = npend - take;
     uint32_t mv_n = 0;
     i64 mv_d = 0;
     if ((uint32_t)lane < rest) {
-      mv_n = pn[take + lane];
-      mv_d = pd[take + lane];
+      mv_n = w.pn[take + lane];
+      mv_d = w.pd[take + lane];
     }
     __syncwarp();
     if ((uint32_t)lane < rest) {
-      pn[lane] = mv_n;
-      pd[lane] = mv_d;
+      w.pn[lane] = mv_n;
+      w.pd[lane] = mv_d;
     }
     npend = rest;
     __syncwarp();
@@ -3174,9 +3368,10 @@ __global__ void __launch_bounds__(kSegThreads, 2)
     if (lane == 0) r = atomicAdd(sm.ticket, 1u);
     r = __shfl_sync(0xffffffffu, r, 0);
     if (r >= sm.n_ranges) break;
-    const u64 rb = sm.range_begin[r], re = sm.range_end[r];
+    const u64 rb = sm.range_begin[r];
+    const uint32_t n = (uint32_t)(sm.range_end[r] - rb);
     const uint32_t inst = sm.range_inst[r];
-    const u64 ib = b.inst_off[inst], ie = b.inst_off[inst + 1];
+    const u64 ib = b.inst_off[inst];
     const uint32_t anchor = b.inst[inst].guess;
     if (inst != cur_inst) {
       if (cur_inst != 0xffffffffu) {
@@ -3187,48 +3382,55 @@ __global__ void __launch_bounds__(kSegThreads, 2)
       gstats = b.stats + (u64)inst * b.n_names;
     }
     // ---------------- A: stream the range
-    const uint32_t n = (uint32_t)(re - rb);
     uint32_t cnt = 0;
-    i64 carry_ts = LLONG_MIN;  // the range's first pair is checked by k_tile_order-like look at rb-1 below
-    bool unsorted = rb > ib && b.ev[rb - 1].start_ts > b.ev[rb].start_ts;
+    // ts of the event before the range: the first pair's order check and the
+    // equal-timestamp test of an anchor at the range start
+    i64 carry_ts = rb > ib ? b.ev[rb - 1].start_ts : LLONG_MIN;
+    bool unsorted = false;
+    const cs_event* pl = b.ev + rb + lane;
     for (uint32_t j0 = 0; j0 < n; j0 += 32 * kScanUnroll) {
       Ev8 e[kScanUnroll];
+      if (j0 + 32 * kScanUnroll <= n) {
 #pragma unroll
-      for (int q = 0; q < kScanUnroll; ++q) {
-        const uint32_t j = j0 + q * 32 + lane;
-        if (j < n) e[q] = ldg256(b.ev + rb + j);
-        else {
-          e[q].a = ~0ull >> 1;
-          e[q].c = (u64)CS_FLOW << 32;
+        for (int q = 0; q < kScanUnroll; ++q) e[q] = ldg256(pl + j0 + q * 32);
+      } else {
+#pragma unroll
+        for (int q = 0; q < kScanUnroll; ++q) {
+          if (j0 + q * 32 + lane < n) e[q] = ldg256(pl + j0 + q * 32);
+          else {
+            e[q].a = ~0ull >> 1;
+            e[q].c = (u64)CS_FLOW << 32;
+          }
         }
       }
 #pragma unroll
       for (int q = 0; q < kScanUnroll; ++q) {
         const uint32_t name = (uint32_t)e[q].c;
         const uint32_t kc = (uint32_t)(e[q].c >> 32);
-        const bool span = (kc & 0xffu) == CS_SPAN;
-        const bool py = span && ((kc >> 8) & 0xffu) == CS_CAT_PYTHON_CALL;
+        const bool py = (kc & 0xffffu) == (((uint32_t)CS_CAT_PYTHON_CALL << 8) | CS_SPAN);
         const uint32_t pm = __ballot_sync(0xffffffffu, py);
-        if (py) {
-          const uint32_t slot = npend + __popc(pm & lanemask_lt());
-          pn[slot] = name;
-          pd[slot] = (i64)e[q].b;
+        if (pm) {
+          if (py) {
+            const uint32_t slot = npend + __popc(pm & lanemask_lt());
+            w.pn[slot] = name;
+            w.pd[slot] = (i64)e[q].b;
+          }
+          npend += __popc(pm);
+          if (npend >= 32) drain(32);
         }
-        npend += __popc(pm);
-        if (npend >= 32) drain(32);
-        const bool is_anchor = span && name == anchor;
+        const bool is_anchor = (kc & 0xffu) == CS_SPAN && name == anchor;
         const uint32_t mk = __ballot_sync(0xffffffffu, is_anchor);
-        const u64 prev = __shfl_up_sync(0xffffffffu, e[q].a, 1);
-        const i64 before = lane == 0 ? carry_ts : (i64)prev;
-        unsorted |= before > (i64)e[q].a;
-        carry_ts = (i64)__shfl_sync(0xffffffffu, e[q].a, 31);
+        const i64 ts = (i64)e[q].a;
+        const i64 prev = __shfl_up_sync(0xffffffffu, ts, 1);
+        const i64 before = lane == 0 ? carry_ts : prev;
+        unsorted |= before > ts;
+        carry_ts = __shfl_sync(0xffffffffu, ts, 31);
         if (is_anchor) {
-          const uint32_t jj = j0 + q * 32 + lane;
-          const u64 ai = rb + cnt + __popc(mk & lanemask_lt());
-          const bool walk = jj == 0 ? rb > ib : (lane == 0 || prev == e[q].a);
-          b.a_pos[ai] = (rb + jj) | (walk ? kWalk : 0ull);
-          b.a_start[ai] = (i64)e[q].a;
-          b.a_end[ai] = (i64)e[q].a + (i64)e[q].b;
+          const uint32_t ai = cnt + __popc(mk & lanemask_lt());
+          if (ai < (uint32_t)kSegList) {
+            w.apos[ai] = (j0 + q * 32 + lane) | (before == ts ? kSegTie : 0u);
+            w.ats[ai] = ts;
+          }
         }
         cnt += __popc(mk);
       }
@@ -3237,19 +3439,24 @@ __global__ void __launch_bounds__(kSegThreads, 2)
     const uint32_t A = cnt;
     if (lane == 0) {
       if (r == 0) {
-        st_release(&sm.lb_state[0], kFlagPrefix | (u64)A);
+        st_relaxed(&sm.lb_state[0], kFlagPrefix | (u64)A);
         sm.range_prefix[0] = 0;
       } else {
-        st_release(&sm.lb_state[r], kFlagAgg | (u64)A);
+        st_relaxed(&sm.lb_state[r], kFlagAgg | (u64)A);
       }
     }
+    if (A > (uint32_t)kSegList) {  // too dense for the list: the host re-runs two-pass
+      if (lane == 0) atomicOr(sm.overflow, 2u);
+      continue;
+    }
+    __syncwarp();
     // the next anchor after the range closes its last cycle
-    int next_found = 0;
+    bool next_found = false, next_tie = false;
     i64 next_start = 0;
-    u64 next_first = 0;
+    u64 npos = 0;
     if (A > 0) {
-      u64 npos = 0;
-      for (u64 p0 = re; p0 < ie; p0 += 32) {
+      const u64 ie = b.inst_off[inst + 1];
+      for (u64 p0 = rb + n; p0 < ie; p0 += 32) {
         const u64 p = p0 + lane;
         bool m = false;
         i64 st = 0;
@@ -3263,94 +3470,59 @@ __global__ void __launch_bounds__(kSegThreads, 2)
           const int L = __ffs(bm) - 1;
           next_start = __shfl_sync(0xffffffffu, st, L);
           npos = p0 + L;
-          next_found = 1;
+          next_found = true;
           break;
         }
       }
-      if (next_found) next_first = group_start(b.ev, npos, ib, next_start);
+      if (next_found) next_tie = b.ev[npos - 1].start_ts == next_start;
     }
-    // ---------------- B + C: lane per cycle, 32 cycles per round
+    // ---------------- B + C: 32 cycles per batch, lane owns cycle k0 + lane
     u64 base = 0;
     bool have_base = r == 0;
     for (uint32_t k0 = 0; k0 == 0 || k0 < A; k0 += 32) {
       const uint32_t k = k0 + lane;
       const bool live = k < A;
-      uint8_t stage = CS_STAGE_UNKNOWN;
-      bool hole = false;
-      i64 cs = 0, ce = 0, aend = 0;
-      u64 apos = 0, first = 0, last = 0;
-      int32_t wl = -1;
+      bool hole = false, tie = false, fits = true;
+      i64 cs = 0, ce = 0;
+      u64 apos = 0, last = 0;
       if (live) {
-        const u64 ai = rb + k;
-        cs = b.a_start[ai];
-        aend = b.a_end[ai];
-        const u64 pw = b.a_pos[ai];
-        apos = pw & ~kWalk;
-        first = (pw & kWalk) ? group_start(b.ev, apos, ib, cs) : apos;
+        const uint32_t pw = w.apos[k];
+        cs = w.ats[k];
+        apos = rb + (pw & ~kSegTie);
+        tie = (pw & kSegTie) != 0;
         if (k + 1 < A) {
-          ce = b.a_start[ai + 1];
-          const u64 pw2 = b.a_pos[ai + 1];
-          const u64 p2 = pw2 & ~kWalk;
-          last = (pw2 & kWalk) ? group_start(b.ev, p2, ib, ce) : p2;
+          const uint32_t pw2 = w.apos[k + 1];
+          ce = w.ats[k + 1];
+          last = rb + (pw2 & ~kSegTie);
+          tie |= (pw2 & kSegTie) != 0;
         } else if (next_found) {
           ce = next_start;
-          last = next_first;
+          last = npos;
+          tie |= next_tie;
         } else {
           hole = true;  // the instance's last anchor: trailing partial cycle dropped
           ce = cs;
-          last = first;
+          last = apos;
         }
-        const i64 dur = ce - cs;
-        s_dur[lane] = dur;
-        for (int p = 0; p < P; ++p) comp[p * SN + lane] = 0;
-        for (int c = 0; c < C; ++c) beta[c * SN + lane] = 0;
-        for (int q = 0; q < R; ++q) {
-          coll[q * SN + lane] = 0.0;
-          colln[q * SN + lane] = 0u;
-        }
-        uint32_t fm_cls = 0, kw = 0;
-        bool fm_found = false, batch_found = false;
-        for (u64 j0 = first; j0 < last; j0 += kRedUnroll) {
-          Ev8 e[kRedUnroll];
-#pragma unroll
-          for (int q = 0; q < kRedUnroll; ++q) {
-            if (j0 + q < last) e[q] = ldg256(b.ev + j0 + q);
-            else e[q].c = (u64)CS_FLOW << 32;
-          }
-#pragma unroll
-          for (int q = 0; q < kRedUnroll; ++q) {
-            const uint32_t name = (uint32_t)e[q].c;
-            const uint32_t kc = (uint32_t)(e[q].c >> 32);
-            const uint32_t flags = kc >> 16;
-            if (!fm_found && (flags & CS_EV_FM_MASK)) {
-              fm_found = true;
-              fm_cls = flags & CS_EV_FM_MASK;
-            }
-            if (!batch_found && (flags & CS_EV_HAS_BATCH)) {
-              batch_found = true;
-              wl = (flags & CS_EV_WL_OK) ? (int32_t)(uint32_t)e[q].d : -2;
-            }
-            if ((kc & 0xffu) != CS_SPAN) continue;
-            const uint32_t info = name < (uint32_t)kFNamesSmem ? s_ninfo[name] : pack_info(b.names[name]);
-            kw |= (info >> 12) & 3u;
-            const i64 st = (i64)e[q].a, d = (i64)e[q].b;
-            const i64 end = st + d;
-            const i64 clipped = (end < ce ? end : ce) - st;
-            if (clipped <= 0) continue;
-            const uint32_t ph = info & 15u, bs = (info >> 4) & 255u;
-            if (ph != 15u) comp[ph * SN + lane] += clipped;
-            if (do_beta && d > 0) {
-              if (bs != 255u) beta[bs * SN + lane] += clipped;
-              if (((kc >> 8) & 0xffu) == CS_CAT_COLLECTIVE_COMM && (flags & CS_EV_HAS_COMM)) {
-                const uint32_t slot = (uint32_t)(e[q].d >> 32);
-                if (slot < (uint32_t)R) {
-                  coll[slot * SN + lane] = __dadd_rn(coll[slot * SN + lane], __ddiv_rn((double)clipped, (double)dur));
-                  colln[slot * SN + lane] += 1u;
-                }
-              }
-            }
-          }
-        }
+        // collective rows hold count << 48 | sum: sum <= events x duration
+        const u64 dur = (u64)(ce - cs), ne = last - apos;
+        fits = dur < (1ull << 32) && ne < (1ull << 16) && dur * ne < (1ull << kCollShift);
+        w.dur[lane] = (i64)dur;
+      }
+      if (__any_sync(0xffffffffu, tie || !fits)) {
+        // an equal-ts group at an anchor (lower_bound before the anchor's
+        // position) or a cycle too long for the packed rows: two-pass path
+        if (lane == 0) atomicOr(sm.overflow, 2u);
+        break;
+      }
+      uint32_t fm = 0, kw = 0;
+      int32_t wl = -1;
+      for (uint32_t q = 0; q < NR; ++q) acc[q * SN + lane] = 0;
+      if (live) seg_walk(b.ev, apos, last, ce, s_ninfo, acc + lane, dummy, (uint32_t)C, (uint32_t)R, fm, kw, wl);
+      auto row = [&](uint32_t q, uint32_t lc) -> u64 { return acc[q * SN + lc]; };
+      uint8_t stage = CS_STAGE_UNKNOWN;
+      if (live) {
+        const uint32_t fm_cls = fm & 3u;
         if (fm_cls == CS_EV_FM_PREFILL) stage = CS_STAGE_PREFILL;
         else if (fm_cls == CS_EV_FM_DECODE) stage = CS_STAGE_DECODE;
         const bool pkw = kw & CS_NAME_PREFILL_KW, dkw = kw & CS_NAME_DECODE_KW;
@@ -3363,9 +3535,9 @@ __global__ void __launch_bounds__(kSegThreads, 2)
         long long j = (long long)r - 1;
         for (;;) {
           const long long idx = j - lane;
-          u64 v = idx >= 0 ? ld_acquire(&sm.lb_state[idx]) : kFlagPrefix;
+          u64 v = idx >= 0 ? ld_relaxed(&sm.lb_state[idx]) : kFlagPrefix;
           while (__any_sync(0xffffffffu, (v & (kFlagAgg | kFlagPrefix)) == 0)) {
-            if ((v & (kFlagAgg | kFlagPrefix)) == 0) v = ld_acquire(&sm.lb_state[idx]);
+            if ((v & (kFlagAgg | kFlagPrefix)) == 0) v = ld_relaxed(&sm.lb_state[idx]);
           }
           const uint32_t pm = __ballot_sync(0xffffffffu, (v & kFlagPrefix) != 0);
           const u64 val = v & kValMask;
@@ -3381,7 +3553,7 @@ __global__ void __launch_bounds__(kSegThreads, 2)
         have_base = true;
         if (lane == 0) {
           sm.range_prefix[r] = excl;
-          st_release(&sm.lb_state[r], kFlagPrefix | (excl + A));
+          st_relaxed(&sm.lb_state[r], kFlagPrefix | (excl + A));
         }
       }
       const uint32_t um = __ballot_sync(0xffffffffu, live && !hole && stage == CS_STAGE_UNKNOWN);
@@ -3398,8 +3570,8 @@ __global__ void __launch_bounds__(kSegThreads, 2)
         b.c_start[g] = cs;
         b.c_end[g] = ce;
         b.c_apos[g] = apos;
-        b.c_aend[g] = aend;
-        b.c_first[g] = first;
+        b.c_aend[g] = cs + b.ev[apos].duration;
+        b.c_first[g] = apos;
         b.c_last[g] = last;
         b.c_inst[g] = inst;
         b.c_local[g] = hole ? (uint8_t)3 : stage;
@@ -3407,24 +3579,50 @@ __global__ void __launch_bounds__(kSegThreads, 2)
         b.c_wl[g] = hole ? kHoleWl : wl;
       }
       __syncwarp();
+      // rows [g0, g0 + nb) of every per-(cycle, slot) output are contiguous:
+      // consecutive lanes store consecutive elements.  idx / n as
+      // floor(idx * ceil(2^32 / n) / 2^32), exact for idx < 2^24
+      const uint32_t nb = A > k0 ? min(32u, A - k0) : 0u;
       const u64 g0 = base + k0;
-      const uint32_t n_live = A > k0 ? min(32u, A - k0) : 0u;
-      for (uint32_t idx = lane; idx < n_live * (uint32_t)P; idx += 32) {
-        const uint32_t lc = idx / (uint32_t)P, p = idx - lc * (uint32_t)P;
-        b.c_comp[g0 * P + idx] = comp[p * SN + lc];
+      for (uint32_t idx = lane; idx < nb * (uint32_t)P; idx += 32) {
+        const uint32_t lc = (uint32_t)(((u64)idx * mP) >> 32), p = idx - lc * (uint32_t)P;
+        const int pb = p < 16u ? s_pbs[p] : -1;
+        b.c_comp[g0 * P + idx] = (i64)row(pb >= 0 ? (uint32_t)pb : (uint32_t)(C + R) + p, lc);
       }
-      for (uint32_t idx = lane; idx < n_live * (uint32_t)C; idx += 32) {
-        const uint32_t lc = idx / (uint32_t)C, c = idx - lc * (uint32_t)C;
-        const i64 dur = s_dur[lc];
-        const i64 t = dur > 0 ? beta[c * SN + lc] : 0;
+      for (uint32_t idx = lane; idx < nb * (uint32_t)C; idx += 32) {
+        const uint32_t lc = (uint32_t)(((u64)idx * mC) >> 32), c = idx - lc * (uint32_t)C;
+        const i64 dur = w.dur[lc];
+        const i64 t = dur > 0 ? (i64)row(c, lc) : 0;
         b.c_beta_tot[g0 * C + idx] = t;
-        b.c_beta[g0 * C + idx] = t > 0 ? __ddiv_rn((double)t, (double)dur) : 0.0;
       }
-      for (uint32_t idx = lane; idx < n_live * (uint32_t)R; idx += 32) {
-        const uint32_t lc = idx / (uint32_t)R, q = idx - lc * (uint32_t)R;
-        b.c_coll[g0 * R + idx] = coll[q * SN + lc];
-        const uint32_t cn = colln[q * SN + lc];
+      // collective beta (rca.cpp:108-115, summed in event order): one
+      // contribution is 0.0 + q = q, the quotient of the integer sum; several
+      // are re-summed in order below by the cycle's lane
+      for (uint32_t idx = lane; idx < nb * (uint32_t)R; idx += 32) {
+        const uint32_t lc = (uint32_t)(((u64)idx * mR) >> 32), q = idx - lc * (uint32_t)R;
+        const u64 v = row((uint32_t)C + q, lc), cn = v >> kCollShift;
+        b.c_coll[g0 * R + idx] = cn == 1u ? __ddiv_rn((double)(v & ((1ull << kCollShift) - 1)), (double)w.dur[lc]) : 0.0;
         b.c_coll_n[g0 * R + idx] = (uint8_t)(cn > 255u ? 255u : cn);
+      }
+      __syncwarp();
+      if (live && R) {
+        bool multi = false;
+        for (int q = 0; q < R; ++q) multi |= (row((uint32_t)(C + q), lane) >> kCollShift) > 1u;
+        if (multi) {
+          const i64 dur = ce - cs;
+          double* out = b.c_coll + (base + k) * R;
+          for (u64 j = apos; j < last; ++j) {
+            const cs_event& ev = b.ev[j];
+            if (ev.kind != CS_SPAN || ev.category != CS_CAT_COLLECTIVE_COMM || !(ev.flags & CS_EV_HAS_COMM) ||
+                ev.duration <= 0)
+              continue;
+            const uint32_t slot = (uint32_t)(ev.payload >> 32);
+            if (slot >= (uint32_t)R || (row((uint32_t)C + slot, lane) >> kCollShift) < 2u) continue;
+            const i64 end = ev.start_ts + ev.duration;
+            const i64 clipped = (end < ce ? end : ce) - ev.start_ts;
+            out[slot] = __dadd_rn(out[slot], __ddiv_rn((double)clipped, (double)dur));
+          }
+        }
       }
       __syncwarp();
     }
@@ -3450,19 +3648,18 @@ __global__ void k_range_inst(DevBuffers b, SegMeta sm, const uint32_t* inst_firs
   if (i < b.n_inst) b.inst[i].n_anchors = off(i + 1) - o;
 }
 
-int segment_range_smem(const DevConfig& cfg, int do_beta) {
+int segment_range_smem(const DevConfig& cfg, int do_beta, uint32_t n_names) {
   const int P = cfg.cyc.n_phases;
   const int C = do_beta ? cfg.cyc.n_beta_slots : 0;
   const int R = do_beta ? cfg.cyc.n_comm_slots : 0;
-  if (P > 15 || C > 254) return -1;
-  const int words = ((P + C + R) * 33 * 2 + R * 33 + 64 + 3) & ~3;  // per warp (k_segment_range)
-  const int smem = kSegWarps * words * 4;
-  return smem <= 96 * 1024 ? smem : -1;
+  if (P > 16 || (int)seg_rows(P, C, R) > 255 || n_names > (uint32_t)kSegNames) return -1;
+  const int smem = kSegWarps * ((int)seg_words(P, C, R) * 4 + SNameCache::kBytes);
+  return smem <= 150 * 1024 ? smem : -1;
 }
 
 void launch_segment_range(const DevBuffers& b, const DevConfig& cfg, const SegMeta& sm, int do_beta,
                           cudaStream_t s, uint64_t* launches) {
-  const int smem = segment_range_smem(cfg, do_beta);
+  const int smem = segment_range_smem(cfg, do_beta, b.n_names);
   if (smem < 0 || sm.n_ranges == 0) return;
   cudaFuncSetAttribute(k_segment_range, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   int dev = 0, n_sm = 148, per_sm = 0;
