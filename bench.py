@@ -319,7 +319,7 @@ def run_ours(args, rank, world, local_rank):
     del events
 
     an = rt.Analyzer(dev)
-    an.set_fused(os.environ.get("CS_BENCH_FUSED", "0") != "0")
+    an.set_fused(os.environ.get("CS_BENCH_FUSED", "1") != "0")
     span = rt.span_names_mask(pin_ev, len(names))
     an.configure(names, span, n_comm_slots=n_comm)
     an.upload(pin_ev, offs, pin_wl)
@@ -443,7 +443,7 @@ def run_ours(args, rank, world, local_rank):
     # the same collective sequence on every rank).
     import threading
     an2 = rt.Analyzer(dev)
-    an2.set_fused(os.environ.get("CS_BENCH_FUSED", "0") != "0")
+    an2.set_fused(os.environ.get("CS_BENCH_FUSED", "1") != "0")
     an2.configure(names, span, n_comm_slots=n_comm)
     for i, model in enumerate(models):
         an2.load_model(model, inst=i)

@@ -688,9 +688,12 @@ int cs_stream_push(cs_ctx* ctx, uint32_t n_inst, const uint64_t* offsets, const 
                    uint64_t n_workloads, const cs_workload* wl, uint32_t stage_mask,
                    cs_alert* alerts, size_t cap, size_t* n_alerts);
 
-/* Execution options.  CS_OPT_FUSED: 1 selects the single-read segmentation
- * pass when applicable, 0 the two-pass path (warp-streaming event scan +
- * thread-per-cycle reduce).  Both are bit-identical; the tests run both. */
+/* Execution options.  CS_OPT_FUSED (default 1): the single-read segmentation
+ * pass (events read from HBM once per run) when applicable, 0 the two-pass
+ * path (warp-streaming event scan + thread-per-cycle reduce).  The single-read
+ * pass falls back to the two-pass path by itself for a wrong anchor guess,
+ * equal-timestamp groups at anchors, ranges denser than its anchor list and
+ * streaming pushes.  Both are bit-identical; the tests run both. */
 #define CS_OPT_FUSED 1
 /* CS_OPT_TRAVERSAL (default 0): 1 scores every model by tree traversal
  * (k_score) even where a compiled cell table exists (k_score_lut); both are

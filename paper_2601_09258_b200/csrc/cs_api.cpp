@@ -201,7 +201,7 @@ struct cs_ctx {
   std::vector<uint64_t> n_cyc;     // cycles per instance
   uint64_t n_cycles = 0;           // cycle slots
   int reduce_variant = 0;  // profiling hook (single variant today)
-  bool allow_fused = false;  // CS_OPT_FUSED
+  bool allow_fused = true;   // CS_OPT_FUSED (default on; 0 selects the two-pass path)
   bool used_fused = false;   // the last run segmented with k_segment_range
   // cs_set_cycles: caller-given cycles of instance 0 (CS_RUN_GIVEN)
   std::vector<cs_cycle> given;
@@ -213,7 +213,7 @@ struct cs_ctx {
   // the first fused run after an upload for the range size in force
   uint64_t ranges_built_for = 0;
   int64_t opt_range_events = 0;   // 0: ~kSegCycles cycles per range from the last run's density
-  int64_t opt_prefetch = -1;      // bytes of the next-round range prefetched into L2; -1: whole range
+  int64_t opt_prefetch = 0;       // L2 prefetch lookahead in ranges (0: the claimed range only; -1: the grid's warp count)
   double ev_per_cycle = 0.0;      // events per cycle slot of the last run
   std::vector<uint64_t> range_begin, range_end;
   std::vector<uint32_t> range_inst, inst_first_range;
@@ -1312,8 +1312,7 @@ static int cs_run_impl(cs_ctx* ctx, uint32_t mask) {
                  static_cast<uint64_t*>(ctx->d_range_prefix.p),
                  static_cast<unsigned int*>(ctx->d_seg_ctl.p),
                  static_cast<unsigned int*>(ctx->d_seg_ctl.p) + 1, cap,
-                 static_cast<uint32_t>(ctx->opt_prefetch < 0 ? ctx->ranges_built_for * sizeof(cs_event)
-                                                             : static_cast<uint64_t>(ctx->opt_prefetch))};
+                 static_cast<uint32_t>(ctx->opt_prefetch < 0 ? 0xffffffffu : ctx->opt_prefetch)};
       e1 = record_event(ctx, 1);
       launch_segment_range(b, cfg, sm, (mask & CS_RUN_BETA) ? 1 : 0, s, &ctx->launches);
       e2 = record_event(ctx, 2);
@@ -2610,7 +2609,7 @@ int cs_set_option(cs_ctx* ctx, int option, int64_t value) {
     ctx->opt_range_events = value;
     return CS_OK;
   }
-  if (option == 97) {  // tuning: L2 prefetch bytes per range (-1 = whole range, 0 = off)
+  if (option == 97) {  // tuning: L2 prefetch lookahead in ranges (-1 = the grid's warps, 0 = the claimed range only)
     ctx->opt_prefetch = value;
     return CS_OK;
   }

@@ -184,7 +184,7 @@ struct SegMeta {
   unsigned int* ticket;          // zeroed per run
   unsigned int* overflow;        // zeroed per run; set when slots exceed `cap`
   uint64_t cap;                  // cycle slot capacity
-  uint32_t prefetch_bytes;       // L2 bulk prefetch of the next claimed range (0 = off)
+  uint32_t prefetch_ahead;       // also prefetch range r + this into L2 (0xffffffff: the grid's warps)
 };
 constexpr int32_t kHoleWl = -3;
 constexpr uint64_t kSegCycles = 30;  // target cycles per range (one warp, one cycle per lane)

@@ -72,6 +72,7 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
   return m;
 }
+__device__ __forceinline__ u64 umin64(u64 a, u64 b) { return a < b ? a : b; }
 __device__ __forceinline__ uint32_t lanemask_le() {
   uint32_t m;
   asm("mov.u32 %0, %%lanemask_le;" : "=r"(m));
@@ -3219,18 +3220,31 @@ void launch_freq_cycles(const cs_event* ev, uint64_t begin, uint64_t end, int64_
 // wrong guess, an ambiguous ranking, a range with more than kSegList anchors
 // or an equal-timestamp group at an anchor (lower_bound before the anchor's
 // position) re-runs the two-pass path.
+#ifndef CS_SEG_SCAN_UNROLL
+#define CS_SEG_SCAN_UNROLL 4
+#endif
+#ifndef CS_SEG_PREFETCH
+#define CS_SEG_PREFETCH 1
+#endif
+#ifndef CS_SEG_WALK_UNROLL
+#define CS_SEG_WALK_UNROLL 4
+#endif
+constexpr int kSegScanUnroll = CS_SEG_SCAN_UNROLL;  // phase A: 256-bit loads in flight per lane
+constexpr int kSegWalkUnroll = CS_SEG_WALK_UNROLL;  // phase B: events in flight per lane
 constexpr int kSegThreads = 256;
 constexpr int kSegWarps = kSegThreads / 32;
 constexpr int kSegList = 128;      // anchors of one range listed in shared memory
 constexpr int kSegNames = 1024;    // name table staged in shared memory
 constexpr uint32_t kSegTie = 0x80000000u;  // apos flag: equal start_ts before the anchor
 
-// u64 accumulator rows [row][33]: [0, C) classes, [C, C+R) collectives
-// (count << 48 | integer sum), [C+R, C+R+P) components of phases without a
-// class row, then one dummy row
+// per-warp accumulator rows [row][33] (lane-private columns): u64 collective
+// rows [0, R) as count << 48 | integer sum, then a dummy row; then class and
+// component rows [0, C) classes, [C, C+P) components of phases without a
+// class row, two dummy rows -- u32 when the batch proves every sum < 2^32,
+// else u64
 constexpr int kCollShift = 48;
 __host__ __device__ constexpr uint32_t seg_rows(int P, int C, int R) {
-  return (uint32_t)(C + R + P + 3);  // + dummy rows for classes, components, collectives
+  return (uint32_t)(R + 1 + C + P + 2);
 }
 __host__ __device__ constexpr uint32_t seg_words(int P, int C, int R) {
   return seg_rows(P, C, R) * 33u * 2u;
@@ -3244,68 +3258,6 @@ struct SegWarpSmem {  // fixed-size per-warp state (static shared memory)
   i64 dur[32];              // batch cycles: duration
 };
 
-// one cycle's events in order, branch-free (cycles.cpp:157-166, 205-229,
-// 256-281; rca.cpp:87-129): every event adds its clipped duration to the
-// lane's rows named by its name, or to a dummy row when none applies.  The
-// three rows one event touches are distinct (class rows / dummy 0, component
-// rows / dummy 1, collective rows / dummy 2), so their read-modify-writes
-// overlap; consecutive events may share rows and stay in order.
-template <bool kGuard>
-__device__ __forceinline__ void seg_walk_step(const cs_event* __restrict__ ev, u64 j0, u64 last, i64 ce,
-                                              const uint32_t* __restrict__ s_ninfo, u64* acc, uint32_t dummy,
-                                              uint32_t C, uint32_t R, uint32_t& fm, uint32_t& kw, int32_t& wl,
-                                              bool& wl_found) {
-  const uint32_t SN = 33;
-  Ev8 e[kRedUnroll];
-#pragma unroll
-  for (int q = 0; q < kRedUnroll; ++q) {
-    if (!kGuard || j0 + q < last) e[q] = ldg256(ev + j0 + q);
-    else {
-      e[q].a = 0;
-      e[q].b = 0;
-      e[q].c = (u64)CS_FLOW << 32;
-      e[q].d = 0;
-    }
-  }
-#pragma unroll
-  for (int q = 0; q < kRedUnroll; ++q) {
-    const uint32_t name = (uint32_t)e[q].c;
-    const uint32_t kc = (uint32_t)(e[q].c >> 32);
-    const uint32_t flags = kc >> 16;
-    const bool span = (kc & 0xffu) == CS_SPAN;
-    const uint32_t info = span ? s_ninfo[name] : (dummy | ((dummy + 1u) << 8));
-    kw |= info >> 30;
-    // clipped = max(0, min(st + d, ce) - st) = min(d, ce - st) when d > 0
-    const i64 d = (i64)e[q].b;
-    const i64 rem = ce - (i64)e[q].a;
-    const u64 c = d > 0 ? (u64)(d < rem ? d : rem) : 0ull;
-    const uint32_t slot = (uint32_t)(e[q].d >> 32);
-    const bool cl = span && ((kc >> 8) & 0xffu) == CS_CAT_COLLECTIVE_COMM && (flags & CS_EV_HAS_COMM) &&
-                    slot < R && d > 0;
-    u64* pb = acc + (info & 0xffu) * SN;
-    u64* pp = acc + ((info >> 8) & 0xffu) * SN;
-    u64* pc = acc + (cl ? C + slot : dummy + 2u) * SN;
-    const u64 vb = *pb, vp = *pp, vc = *pc;
-    *pb = vb + c;
-    *pp = vp + c;
-    *pc = vc + c + (1ull << kCollShift);
-    fm = (fm == 0u && (flags & CS_EV_FM_MASK)) ? (4u | (flags & CS_EV_FM_MASK)) : fm;
-    const bool hb = (flags & CS_EV_HAS_BATCH) != 0;
-    wl = (!wl_found && hb) ? ((flags & CS_EV_WL_OK) ? (int32_t)(uint32_t)e[q].d : -2) : wl;
-    wl_found |= hb;
-  }
-}
-
-__device__ __forceinline__ void seg_walk(const cs_event* __restrict__ ev, u64 first, u64 last, i64 ce,
-                                         const uint32_t* __restrict__ s_ninfo, u64* acc, uint32_t dummy,
-                                         uint32_t C, uint32_t R, uint32_t& fm, uint32_t& kw, int32_t& wl) {
-  bool wl_found = false;
-  u64 j0 = first;
-  for (; j0 + kRedUnroll <= last; j0 += kRedUnroll)
-    seg_walk_step<false>(ev, j0, last, ce, s_ninfo, acc, dummy, C, R, fm, kw, wl, wl_found);
-  if (j0 < last) seg_walk_step<true>(ev, j0, last, ce, s_ninfo, acc, dummy, C, R, fm, kw, wl, wl_found);
-}
-
 __global__ void __launch_bounds__(kSegThreads, 2)
     k_segment_range(DevBuffers b, DevConfig cfg, SegMeta sm, int do_beta) {
   extern __shared__ __align__(16) unsigned char s_dyn[];
@@ -3317,23 +3269,92 @@ __global__ void __launch_bounds__(kSegThreads, 2)
   const int C = do_beta ? cfg.cyc.n_beta_slots : 0;
   const int R = do_beta ? cfg.cyc.n_comm_slots : 0;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const uint32_t NR = seg_rows(P, C, R), dummy = NR - 3;
+  const uint32_t NR = seg_rows(P, C, R);
+  const uint32_t db = (uint32_t)(C + P), dp = db + 1u;  // dummy class / component rows
   if (threadIdx.x < 16) s_pbs[threadIdx.x] = -1;
   __syncthreads();
   // name -> (class row | component row << 8 | keyword bits << 30); a phase
-  // name with a class row accumulates once, into the class row
+  // name with a class row accumulates once, into the class row (a clipped
+  // term > 0 implies duration > 0, so both sums take the same terms)
   for (uint32_t i = threadIdx.x; i < b.n_names; i += blockDim.x) {
     const cs_name_info ni = b.names[i];
     const bool ph = ni.phase >= 0 && ni.phase < P;
     const bool bs = ni.beta_slot >= 0 && ni.beta_slot < C;
-    const uint32_t brow = bs ? (uint32_t)ni.beta_slot : dummy;
-    const uint32_t prow = (ph && !bs) ? (uint32_t)(C + R + ni.phase) : dummy + 1u;
+    const uint32_t brow = bs ? (uint32_t)ni.beta_slot : db;
+    const uint32_t prow = (ph && !bs) ? (uint32_t)(C + ni.phase) : dp;
     s_ninfo[i] = brow | (prow << 8) | ((ni.flags & 3u) << 30);
     if (ph && bs) s_pbs[ni.phase] = ni.beta_slot;
   }
   __syncthreads();  // the only CTA barriers: warps are independent from here on
   const uint32_t SN = 33;
-  u64* acc = reinterpret_cast<u64*>(s_dyn) + (u64)warp * NR * SN;
+  u64* acc_c = reinterpret_cast<u64*>(s_dyn) + (u64)warp * NR * SN;  // collective rows [R + 1][SN]
+  unsigned char* acc_b = reinterpret_cast<unsigned char*>(acc_c + (u64)(R + 1) * SN);  // class rows
+  // one cycle's events in order, branch-free (cycles.cpp:157-166, 205-229,
+  // 256-281; rca.cpp:87-129): every event adds its clipped duration to the
+  // lane's rows named by its name, or to a dummy row when none applies.  The
+  // three rows one event touches are distinct (class rows / dummy, component
+  // rows / dummy, collective rows / dummy), so their read-modify-writes
+  // overlap; consecutive events may share rows and stay in order.
+  auto walk = [&](auto tag, u64 first, u64 last, i64 ce, uint32_t& fm, uint32_t& kw, int32_t& wl) {
+    using T = decltype(tag);
+    T* rb_ = reinterpret_cast<T*>(acc_b) + lane;
+    u64* rc_ = acc_c + lane;
+    bool wl_found = false;
+    auto step = [&](u64 j0, bool guard) {
+      Ev8 e[kSegWalkUnroll];
+#pragma unroll
+      for (int q = 0; q < kSegWalkUnroll; ++q) {
+        if (!guard || j0 + q < last) e[q] = ldg256(b.ev + j0 + q);
+        else {
+          e[q].a = 0;
+          e[q].b = 0;
+          e[q].c = (u64)CS_FLOW << 32;
+          e[q].d = 0;
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < kSegWalkUnroll; ++q) {
+        const uint32_t name = (uint32_t)e[q].c;
+        const uint32_t kc = (uint32_t)(e[q].c >> 32);
+        const uint32_t flags = kc >> 16;
+        const bool span = (kc & 0xffu) == CS_SPAN;
+        const uint32_t info = span ? s_ninfo[name] : (db | (dp << 8));
+        kw |= info >> 30;
+        // clipped = max(0, min(st + d, ce) - st) = min(d, ce - st) when d > 0
+        const i64 d = (i64)e[q].b;
+        T c;
+        if constexpr (sizeof(T) == 4) {
+          // ce - st in (0, dur], dur < 2^32: 32-bit arithmetic is exact
+          const uint32_t rem = (uint32_t)ce - (uint32_t)e[q].a;
+          const int32_t hi = (int32_t)(d >> 32);
+          uint32_t v = min((uint32_t)d, rem);
+          v = hi > 0 ? rem : v;
+          c = hi < 0 ? 0u : v;
+        } else {
+          const i64 rem = ce - (i64)e[q].a;
+          c = d > 0 ? (u64)(d < rem ? d : rem) : 0ull;
+        }
+        const uint32_t slot = (uint32_t)(e[q].d >> 32);
+        const bool cl = span && ((kc >> 8) & 0xffu) == CS_CAT_COLLECTIVE_COMM && (flags & CS_EV_HAS_COMM) &&
+                        slot < (uint32_t)R && c != 0;
+        T* pb = rb_ + (info & 0xffu) * SN;
+        T* pp = rb_ + ((info >> 8) & 0xffu) * SN;
+        u64* pc = rc_ + (cl ? slot : (uint32_t)R) * SN;
+        const T vb = *pb, vp = *pp;
+        const u64 vc = *pc;
+        *pb = vb + c;
+        *pp = vp + c;
+        *pc = vc + (u64)c + (1ull << kCollShift);
+        fm = (fm == 0u && (flags & CS_EV_FM_MASK)) ? (4u | (flags & CS_EV_FM_MASK)) : fm;
+        const bool hb = (flags & CS_EV_HAS_BATCH) != 0;
+        wl = (!wl_found && hb) ? ((flags & CS_EV_WL_OK) ? (int32_t)(uint32_t)e[q].d : -2) : wl;
+        wl_found |= hb;
+      }
+    };
+    u64 j0 = first;
+    for (; j0 + kSegWalkUnroll <= last; j0 += kSegWalkUnroll) step(j0, false);
+    if (j0 < last) step(j0, true);
+  };
   SegWarpSmem& w = s_w[warp];
   WarpNameRow* wrows = s_rows + warp * kWarpNameRows;
   const u64 mP = P ? ((1ull << 32) + (u64)P - 1) / (u64)P : 0;
@@ -3371,6 +3392,27 @@ __global__ void __launch_bounds__(kSegThreads, 2)
     const u64 rb = sm.range_begin[r];
     const uint32_t n = (uint32_t)(sm.range_end[r] - rb);
     const uint32_t inst = sm.range_inst[r];
+#if CS_SEG_PREFETCH
+    // pull the whole range (+ a cycle past it) into L2 at once: the stream's
+    // later iterations hit L2 instead of each waiting out a DRAM latency
+    // and the range this warp will most likely claim next (tickets go round
+    // the grid's warps), one range-time ahead
+    if (lane < 2) {
+      const uint32_t ahead = sm.prefetch_ahead == 0xffffffffu ? gridDim.x * (uint32_t)kSegWarps : sm.prefetch_ahead;
+      const uint32_t pr = lane == 0 ? r : r + ahead;
+      if ((lane == 0 || ahead) && pr < sm.n_ranges) {
+        const u64 pb = sm.range_begin[pr];
+        const uint32_t pi = sm.range_inst[pr];
+        const uint32_t bytes =
+            (uint32_t)umin64(sm.range_end[pr] - pb + 64u, b.inst_off[pi + 1] - pb) * (uint32_t)sizeof(cs_event);
+        const char* p = reinterpret_cast<const char*>(b.ev + pb);
+        for (uint32_t o = 0; o < bytes; o += 32768u) {
+          const uint32_t m = min(32768u, bytes - o);
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p + o), "r"(m) : "memory");
+        }
+      }
+    }
+#endif
     const u64 ib = b.inst_off[inst];
     const uint32_t anchor = b.inst[inst].guess;
     if (inst != cur_inst) {
@@ -3388,14 +3430,14 @@ __global__ void __launch_bounds__(kSegThreads, 2)
     i64 carry_ts = rb > ib ? b.ev[rb - 1].start_ts : LLONG_MIN;
     bool unsorted = false;
     const cs_event* pl = b.ev + rb + lane;
-    for (uint32_t j0 = 0; j0 < n; j0 += 32 * kScanUnroll) {
-      Ev8 e[kScanUnroll];
-      if (j0 + 32 * kScanUnroll <= n) {
+    for (uint32_t j0 = 0; j0 < n; j0 += 32 * kSegScanUnroll) {
+      Ev8 e[kSegScanUnroll];
+      if (j0 + 32 * kSegScanUnroll <= n) {
 #pragma unroll
-        for (int q = 0; q < kScanUnroll; ++q) e[q] = ldg256(pl + j0 + q * 32);
+        for (int q = 0; q < kSegScanUnroll; ++q) e[q] = ldg256(pl + j0 + q * 32);
       } else {
 #pragma unroll
-        for (int q = 0; q < kScanUnroll; ++q) {
+        for (int q = 0; q < kSegScanUnroll; ++q) {
           if (j0 + q * 32 + lane < n) e[q] = ldg256(pl + j0 + q * 32);
           else {
             e[q].a = ~0ull >> 1;
@@ -3404,7 +3446,7 @@ __global__ void __launch_bounds__(kSegThreads, 2)
         }
       }
 #pragma unroll
-      for (int q = 0; q < kScanUnroll; ++q) {
+      for (int q = 0; q < kSegScanUnroll; ++q) {
         const uint32_t name = (uint32_t)e[q].c;
         const uint32_t kc = (uint32_t)(e[q].c >> 32);
         const bool py = (kc & 0xffffu) == (((uint32_t)CS_CAT_PYTHON_CALL << 8) | CS_SPAN);
@@ -3482,7 +3524,7 @@ __global__ void __launch_bounds__(kSegThreads, 2)
     for (uint32_t k0 = 0; k0 == 0 || k0 < A; k0 += 32) {
       const uint32_t k = k0 + lane;
       const bool live = k < A;
-      bool hole = false, tie = false, fits = true;
+      bool hole = false, tie = false, fits = true, narrow = true;
       i64 cs = 0, ce = 0;
       u64 apos = 0, last = 0;
       if (live) {
@@ -3507,6 +3549,7 @@ __global__ void __launch_bounds__(kSegThreads, 2)
         // collective rows hold count << 48 | sum: sum <= events x duration
         const u64 dur = (u64)(ce - cs), ne = last - apos;
         fits = dur < (1ull << 32) && ne < (1ull << 16) && dur * ne < (1ull << kCollShift);
+        narrow = dur * ne < (1ull << 32);
         w.dur[lane] = (i64)dur;
       }
       if (__any_sync(0xffffffffu, tie || !fits)) {
@@ -3517,9 +3560,24 @@ __global__ void __launch_bounds__(kSegThreads, 2)
       }
       uint32_t fm = 0, kw = 0;
       int32_t wl = -1;
-      for (uint32_t q = 0; q < NR; ++q) acc[q * SN + lane] = 0;
-      if (live) seg_walk(b.ev, apos, last, ce, s_ninfo, acc + lane, dummy, (uint32_t)C, (uint32_t)R, fm, kw, wl);
-      auto row = [&](uint32_t q, uint32_t lc) -> u64 { return acc[q * SN + lc]; };
+      const bool wide = !__all_sync(0xffffffffu, narrow);
+      // zero the lane's own columns in the layout in force
+      for (int q = 0; q <= R; ++q) acc_c[q * SN + lane] = 0;
+      if (wide) {
+        for (uint32_t q = 0; q < (uint32_t)(C + P + 2); ++q) reinterpret_cast<u64*>(acc_b)[q * SN + lane] = 0;
+      } else {
+        for (uint32_t q = 0; q < (uint32_t)(C + P + 2); ++q) reinterpret_cast<uint32_t*>(acc_b)[q * SN + lane] = 0;
+      }
+      if (live) {
+        if (wide) walk(u64{}, apos, last, ce, fm, kw, wl);
+        else walk(uint32_t{}, apos, last, ce, fm, kw, wl);
+      }
+      __syncwarp();
+      auto row = [&](uint32_t q, uint32_t lc) -> u64 {  // class / component rows
+        return wide ? reinterpret_cast<const u64*>(acc_b)[q * SN + lc]
+                    : (u64)reinterpret_cast<const uint32_t*>(acc_b)[q * SN + lc];
+      };
+      auto crow = [&](uint32_t q, uint32_t lc) -> u64 { return acc_c[q * SN + lc]; };
       uint8_t stage = CS_STAGE_UNKNOWN;
       if (live) {
         const uint32_t fm_cls = fm & 3u;
@@ -3587,7 +3645,7 @@ __global__ void __launch_bounds__(kSegThreads, 2)
       for (uint32_t idx = lane; idx < nb * (uint32_t)P; idx += 32) {
         const uint32_t lc = (uint32_t)(((u64)idx * mP) >> 32), p = idx - lc * (uint32_t)P;
         const int pb = p < 16u ? s_pbs[p] : -1;
-        b.c_comp[g0 * P + idx] = (i64)row(pb >= 0 ? (uint32_t)pb : (uint32_t)(C + R) + p, lc);
+        b.c_comp[g0 * P + idx] = (i64)row(pb >= 0 ? (uint32_t)pb : (uint32_t)C + p, lc);
       }
       for (uint32_t idx = lane; idx < nb * (uint32_t)C; idx += 32) {
         const uint32_t lc = (uint32_t)(((u64)idx * mC) >> 32), c = idx - lc * (uint32_t)C;
@@ -3600,14 +3658,14 @@ __global__ void __launch_bounds__(kSegThreads, 2)
       // are re-summed in order below by the cycle's lane
       for (uint32_t idx = lane; idx < nb * (uint32_t)R; idx += 32) {
         const uint32_t lc = (uint32_t)(((u64)idx * mR) >> 32), q = idx - lc * (uint32_t)R;
-        const u64 v = row((uint32_t)C + q, lc), cn = v >> kCollShift;
+        const u64 v = crow(q, lc), cn = v >> kCollShift;
         b.c_coll[g0 * R + idx] = cn == 1u ? __ddiv_rn((double)(v & ((1ull << kCollShift) - 1)), (double)w.dur[lc]) : 0.0;
         b.c_coll_n[g0 * R + idx] = (uint8_t)(cn > 255u ? 255u : cn);
       }
       __syncwarp();
       if (live && R) {
         bool multi = false;
-        for (int q = 0; q < R; ++q) multi |= (row((uint32_t)(C + q), lane) >> kCollShift) > 1u;
+        for (int q = 0; q < R; ++q) multi |= (crow((uint32_t)q, lane) >> kCollShift) > 1u;
         if (multi) {
           const i64 dur = ce - cs;
           double* out = b.c_coll + (base + k) * R;
@@ -3617,7 +3675,7 @@ __global__ void __launch_bounds__(kSegThreads, 2)
                 ev.duration <= 0)
               continue;
             const uint32_t slot = (uint32_t)(ev.payload >> 32);
-            if (slot >= (uint32_t)R || (row((uint32_t)C + slot, lane) >> kCollShift) < 2u) continue;
+            if (slot >= (uint32_t)R || (crow(slot, lane) >> kCollShift) < 2u) continue;
             const i64 end = ev.start_ts + ev.duration;
             const i64 clipped = (end < ce ? end : ce) - ev.start_ts;
             out[slot] = __dadd_rn(out[slot], __ddiv_rn((double)clipped, (double)dur));
