@@ -1706,6 +1706,11 @@ static int cs_run_impl(cs_ctx* ctx, uint32_t mask) {
   hp.mark("all_issued");
   CS_CUDA(cudaStreamSynchronize(s));
   hp.mark("final_sync");
+  if (std::getenv("CS_STAGE_ITERS") && ctx->d_stage_ctl.p) {  // profiling: Jacobi iterations of the stage heuristic
+    unsigned int it = 0;
+    cudaMemcpy(&it, static_cast<unsigned int*>(ctx->d_stage_ctl.p) + 5, 4, cudaMemcpyDeviceToHost);
+    std::fprintf(stderr, "stage heuristic iterations: %u\n", it);
+  }
   CS_CUDA(cudaGetLastError());
   if (predicted) {
     for (uint32_t i = 0; i < n_inst; ++i) {

@@ -214,7 +214,9 @@ int segment_range_smem(const DevConfig& cfg, int do_beta, uint32_t n_names);
 // K4' (k_stage_jacobi): the stage heuristic over chunks of cycle slots with
 // Jacobi refinement; st[0] = c_stage (holding the local stages), st[1] a
 // scratch copy; *final_parity = index of the array with the result
-// (0xffffffff: no fixed point within max_iter).
+// (0xffffffff: no fixed point within max_iter); final_parity[1] iterations
+// run, [2] = 1 when K4b (k_stage_blocks) reached the fixed point, [3] K4b's
+// out-of-range flag.
 struct StageMeta {
   uint8_t* st[2];
   uint32_t n_chunks;
@@ -227,6 +229,8 @@ struct StageMeta {
   int max_iter;
 };
 constexpr uint32_t kStageChunkCycles = 256;
+// K4b (k_stage_blocks, windows <= 32, not streaming) runs first; K4' only
+// when K4b could not (final_parity[2] == 0)
 int launch_stage_heuristic(const DevBuffers& b, const DevConfig& cfg, const StageMeta& m, cudaStream_t s,
                            uint64_t* launches);
 void launch_records(const DevBuffers& b, const DevConfig& cfg, uint64_t n_blocks_cap,

@@ -1,3 +1,4 @@
+#include <type_traits>
 // cs_kernels.cu — hand-written sm_100a kernels of the trace-analysis hot path.
 //
 // Data flow (one cs_run over a batch of instances):
@@ -2868,6 +2869,55 @@ __device__ __forceinline__ double win_median(const Win& w) {
   return __dmul_rn(0.5, __dadd_rn(w.sorted[n / 2 - 1], w.sorted[n / 2]));
 }
 
+// The same trailing window held in registers when it fits a warp (W <= 32):
+// lane k holds the k-th smallest value (lanes < n) and the k-th ring slot.
+// Insert / remove are one ballot and one shuffle; no shared memory, no
+// warp barriers.
+struct RegWin {
+  double v, ring;
+  uint32_t n, head, cap;
+};
+
+__device__ __forceinline__ void win_insert(RegWin& w, double x) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t p = __popc(__ballot_sync(0xffffffffu, lane < w.n && w.v <= x));
+  const double pv = __shfl_up_sync(0xffffffffu, w.v, 1);
+  if (lane > p && lane <= w.n) w.v = pv;
+  if (lane == p) w.v = x;
+  ++w.n;
+}
+
+__device__ __forceinline__ void win_remove(RegWin& w, double y) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t m = __ballot_sync(0xffffffffu, lane < w.n && w.v == y);
+  const uint32_t p = (uint32_t)__ffs(m) - 1u;
+  const double nx = __shfl_down_sync(0xffffffffu, w.v, 1);
+  if (lane >= p && lane + 1 < w.n) w.v = nx;
+  --w.n;
+}
+
+__device__ __forceinline__ void win_push(RegWin& w, double x) {
+  const uint32_t lane = threadIdx.x & 31;
+  if (w.n == w.cap) {
+    const double oldest = __shfl_sync(0xffffffffu, w.ring, w.head);
+    win_remove(w, oldest);
+    if (lane == w.head) w.ring = x;
+    w.head = w.head + 1 == w.cap ? 0 : w.head + 1;
+  } else {
+    uint32_t tail = w.head + w.n;
+    if (tail >= w.cap) tail -= w.cap;
+    if (lane == tail) w.ring = x;
+  }
+  win_insert(w, x);
+}
+
+__device__ __forceinline__ double win_median(const RegWin& w) {
+  const uint32_t n = w.n;
+  if (n % 2 == 1) return __shfl_sync(0xffffffffu, w.v, n / 2);
+  const double a = __shfl_sync(0xffffffffu, w.v, n / 2 - 1), c = __shfl_sync(0xffffffffu, w.v, n / 2);
+  return __dmul_rn(0.5, __dadd_rn(a, c));
+}
+
 __device__ __forceinline__ void grid_barrier(unsigned int* count, unsigned int* gen) {
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -2886,8 +2936,10 @@ __device__ __forceinline__ void grid_barrier(unsigned int* count, unsigned int* 
   __syncthreads();
 }
 
+template <bool kReg>
 __global__ void __launch_bounds__(kStageWarps * 32)
     k_stage_jacobi(DevBuffers b, DevConfig cfg, StageMeta m) {
+  using WinT = typename std::conditional<kReg, RegWin, Win>::type;
   extern __shared__ __align__(16) double s_win[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint32_t W = (uint32_t)cfg.cyc.stage_window;
@@ -2896,7 +2948,7 @@ __global__ void __launch_bounds__(kStageWarps * 32)
   const uint32_t gw = blockIdx.x * kStageWarps + warp, nw = gridDim.x * kStageWarps;
   // no Unknown cycle anywhere (the common forward_mode case): nothing to do;
   // every CTA reads the same flag, so none waits at a barrier
-  if (__ldcg(b.any_unknown) == 0u) {
+  if (__ldcg(b.any_unknown) == 0u || __ldcg(m.final_parity + 2) != 0u) {  // nothing Unknown / k_stage_blocks converged
     if (blockIdx.x == 0 && threadIdx.x == 0) *m.final_parity = 0;
     return;
   }
@@ -2923,85 +2975,124 @@ __global__ void __launch_bounds__(kStageWarps * 32)
       }
       bool changed = false;
       uint32_t cur_inst = 0xffffffffu;
-      Win dw{mine, mine + W, 0, 0, W}, gwin{mine + 2 * W, mine + 3 * W, 0, 0, W};
+      WinT dw, gwin;
+      if constexpr (kReg) {
+        dw = RegWin{0.0, 0.0, 0, 0, W};
+        gwin = RegWin{0.0, 0.0, 0, 0, W};
+      } else {
+        dw = Win{mine, mine + W, 0, 0, W};
+        gwin = Win{mine + 2 * W, mine + 3 * W, 0, 0, W};
+      }
+      // staging for the window rebuild: most recent first
+      double* stage_d = mine;
+      double* stage_g = mine + 2 * W;
       u64 c0 = 0;
       const StreamCarry* sc = nullptr;
       u64 lb_lo = lo;
-      for (u64 u = lo; u < hi; ++u) {
-        const uint8_t local = b.c_local[u];
-        if (local == 3) {  // hole slot of the single-read pass: not a cycle
-          if (lane == 0) out[u] = local;
-          continue;
+      // per 32-cycle block: the cycles' inputs loaded once, coalesced, one
+      // cycle per lane; the sequential walk takes them by shuffle
+      for (u64 u0 = lo; u0 < hi; u0 += 32) {
+        const u64 ul = u0 + lane;
+        const bool lv = ul < hi;
+        uint32_t x_local = 3, x_inst = 0xffffffffu, x_in = 0;
+        double x_dur = 0.0, x_gap = -1.0;
+        if (lv) {
+          x_local = b.c_local[ul];
+          x_inst = b.c_inst[ul];
+          x_in = __ldcg(&in[ul]);
+          if (x_local != 3) {
+            const u64 c0l = b.cyc_off[x_inst];
+            const StreamCarry* scl = b.stream ? b.stream + x_inst : nullptr;
+            x_dur = (double)(b.c_end[ul] - b.c_start[ul]);
+            x_gap = ul > c0l ? (double)(b.c_start[ul] - b.c_aend[ul - 1])
+                    : (scl && scl->has_prev) ? (double)(b.c_start[ul] - scl->last_aend) : -1.0;
+          }
         }
-        const uint32_t inst = b.c_inst[u];
-        if (inst != cur_inst) {
-          // (re)build the windows from the cycles before u in its instance
-          cur_inst = inst;
-          c0 = b.cyc_off[inst];
-          sc = b.stream ? b.stream + inst : nullptr;
-          dw.n = dw.head = gwin.n = gwin.head = 0;
-          // collect most recent first in the rings' upper halves, then insert oldest first
-          uint32_t nd = 0, ng = 0;
-          i64 top = (i64)u - 1;
-          for (; top >= (i64)c0 && (nd < W || ng < W); top -= 32) {
-            const i64 j = top - lane;
-            const bool inr = j >= (i64)c0;
-            bool nonp = false, gok = false;
-            double jd = 0.0, jg = -1.0;
-            if (inr && b.c_local[j] != 3) {
-              nonp = __ldcg(&in[j]) != CS_STAGE_PREFILL;
-              jd = (double)(b.c_end[j] - b.c_start[j]);
-              jg = j > (i64)c0 ? (double)(b.c_start[j] - b.c_aend[j - 1])
-                   : (sc && sc->has_prev) ? (double)(b.c_start[j] - sc->last_aend) : -1.0;
-              gok = nonp && jg >= 0.0;
+        uint32_t x_out = x_local;
+        const uint32_t nl = (uint32_t)min((u64)32, hi - u0);
+        for (uint32_t l = 0; l < nl; ++l) {
+          const u64 u = u0 + l;
+          const uint8_t local = (uint8_t)__shfl_sync(0xffffffffu, x_local, l);
+          if (local == 3) continue;  // hole slot of the single-read pass: not a cycle
+          const uint32_t inst = __shfl_sync(0xffffffffu, x_inst, l);
+          if (inst != cur_inst) {
+            // (re)build the windows from the cycles before u in its instance
+            cur_inst = inst;
+            c0 = b.cyc_off[inst];
+            sc = b.stream ? b.stream + inst : nullptr;
+            dw.n = dw.head = gwin.n = gwin.head = 0;
+            // collect most recent first in the rings' upper halves, then insert oldest first
+            uint32_t nd = 0, ng = 0;
+            i64 top = (i64)u - 1;
+            for (; top >= (i64)c0 && (nd < W || ng < W); top -= 32) {
+              const i64 j = top - lane;
+              const bool inr = j >= (i64)c0;
+              bool nonp = false, gok = false;
+              double jd = 0.0, jg = -1.0;
+              if (inr && b.c_local[j] != 3) {
+                nonp = __ldcg(&in[j]) != CS_STAGE_PREFILL;
+                jd = (double)(b.c_end[j] - b.c_start[j]);
+                jg = j > (i64)c0 ? (double)(b.c_start[j] - b.c_aend[j - 1])
+                     : (sc && sc->has_prev) ? (double)(b.c_start[j] - sc->last_aend) : -1.0;
+                gok = nonp && jg >= 0.0;
+              }
+              const uint32_t md = __ballot_sync(0xffffffffu, inr && nonp);
+              const uint32_t mg = __ballot_sync(0xffffffffu, inr && gok);
+              const uint32_t kd = nd + __popc(md & lanemask_lt());
+              const uint32_t kg = ng + __popc(mg & lanemask_lt());
+              if (inr && nonp && kd < W) stage_d[kd] = jd;  // staging: most recent first
+              if (inr && gok && kg < W) stage_g[kg] = jg;
+              nd = min(W, nd + __popc(md));
+              ng = min(W, ng + __popc(mg));
+              if (u == lo) lb_lo = (u64)max((i64)c0, top - 31);
             }
-            const uint32_t md = __ballot_sync(0xffffffffu, inr && nonp);
-            const uint32_t mg = __ballot_sync(0xffffffffu, inr && gok);
-            const uint32_t kd = nd + __popc(md & lanemask_lt());
-            const uint32_t kg = ng + __popc(mg & lanemask_lt());
-            if (inr && nonp && kd < W) dw.sorted[kd] = jd;  // staging: most recent first
-            if (inr && gok && kg < W) gwin.sorted[kg] = jg;
-            nd = min(W, nd + __popc(md));
-            ng = min(W, ng + __popc(mg));
-            if (u == lo) lb_lo = (u64)max((i64)c0, top - 31);
+            if (u == lo && top < (i64)c0) lb_lo = c0;
+            __syncwarp();
+            // earlier micro-batches (streaming carry), most recent first
+            if (sc) {
+              for (uint32_t k = lane; k < sc->n_dur && nd + k < W; k += 32) stage_d[nd + k] = sc->dur_hist[k];
+              for (uint32_t k = lane; k < sc->n_gap && ng + k < W; k += 32) stage_g[ng + k] = sc->gap_hist[k];
+              nd = min(W, nd + sc->n_dur);
+              ng = min(W, ng + sc->n_gap);
+            }
+            __syncwarp();
+            // oldest first into the rings, then sort
+            if constexpr (kReg) {
+              dw.ring = (uint32_t)lane < nd ? stage_d[nd - 1 - lane] : 0.0;
+              gwin.ring = (uint32_t)lane < ng ? stage_g[ng - 1 - lane] : 0.0;
+              __syncwarp();
+              for (uint32_t k = 0; k < nd; ++k) win_insert(dw, __shfl_sync(0xffffffffu, dw.ring, k));
+              for (uint32_t k = 0; k < ng; ++k) win_insert(gwin, __shfl_sync(0xffffffffu, gwin.ring, k));
+            } else {
+              for (uint32_t k = lane; k < nd; k += 32) dw.ring[k] = dw.sorted[nd - 1 - k];
+              for (uint32_t k = lane; k < ng; k += 32) gwin.ring[k] = gwin.sorted[ng - 1 - k];
+              __syncwarp();
+              for (uint32_t k = 0; k < nd; ++k) win_insert(dw, dw.ring[k]);
+              for (uint32_t k = 0; k < ng; ++k) win_insert(gwin, gwin.ring[k]);
+            }
+            dw.head = 0;
+            gwin.head = 0;
           }
-          if (u == lo && top < (i64)c0) lb_lo = c0;
-          __syncwarp();
-          // earlier micro-batches (streaming carry), most recent first
-          if (sc) {
-            for (uint32_t k = lane; k < sc->n_dur && nd + k < W; k += 32) dw.sorted[nd + k] = sc->dur_hist[k];
-            for (uint32_t k = lane; k < sc->n_gap && ng + k < W; k += 32) gwin.sorted[ng + k] = sc->gap_hist[k];
-            nd = min(W, nd + sc->n_dur);
-            ng = min(W, ng + sc->n_gap);
+          const double gap = __shfl_sync(0xffffffffu, x_gap, l);
+          const double cdur = __shfl_sync(0xffffffffu, x_dur, l);
+          uint8_t stage = local;
+          if (stage == CS_STAGE_UNKNOWN && (u64)dw.n >= min_hist && gap >= 0.0) {
+            const double med_dur = win_median(dw);
+            double med_gap = gwin.n ? win_median(gwin) : 0.0;
+            med_gap = 1.0 < med_gap ? med_gap : 1.0;
+            const bool long_cycle = cdur > __dmul_rn(cfg.cyc.prefill_duration_factor, med_dur);
+            const bool long_gap = gap > __dmul_rn(cfg.cyc.prefill_gap_factor, med_gap);
+            stage = (long_cycle && long_gap) ? CS_STAGE_PREFILL : CS_STAGE_DECODE;
           }
-          __syncwarp();
-          // oldest first into the rings, then sort
-          for (uint32_t k = lane; k < nd; k += 32) dw.ring[k] = dw.sorted[nd - 1 - k];
-          for (uint32_t k = lane; k < ng; k += 32) gwin.ring[k] = gwin.sorted[ng - 1 - k];
-          __syncwarp();
-          for (uint32_t k = 0; k < nd; ++k) win_insert(dw, dw.ring[k]);
-          for (uint32_t k = 0; k < ng; ++k) win_insert(gwin, gwin.ring[k]);
-          dw.head = 0;
-          gwin.head = 0;
+          const uint32_t pin = __shfl_sync(0xffffffffu, x_in, l);
+          changed |= (stage == CS_STAGE_PREFILL) != (pin == CS_STAGE_PREFILL);
+          if ((uint32_t)lane == l) x_out = stage;
+          if (stage != CS_STAGE_PREFILL) {
+            win_push(dw, cdur);
+            if (gap >= 0.0) win_push(gwin, gap);
+          }
         }
-        const double gap = u > c0 ? (double)(b.c_start[u] - b.c_aend[u - 1])
-                           : (sc && sc->has_prev) ? (double)(b.c_start[u] - sc->last_aend) : -1.0;
-        uint8_t stage = local;
-        if (stage == CS_STAGE_UNKNOWN && (u64)dw.n >= min_hist && gap >= 0.0) {
-          const double med_dur = win_median(dw);
-          double med_gap = gwin.n ? win_median(gwin) : 0.0;
-          med_gap = 1.0 < med_gap ? med_gap : 1.0;
-          const double cdur = (double)(b.c_end[u] - b.c_start[u]);
-          const bool long_cycle = cdur > __dmul_rn(cfg.cyc.prefill_duration_factor, med_dur);
-          const bool long_gap = gap > __dmul_rn(cfg.cyc.prefill_gap_factor, med_gap);
-          stage = (long_cycle && long_gap) ? CS_STAGE_PREFILL : CS_STAGE_DECODE;
-        }
-        changed |= (stage == CS_STAGE_PREFILL) != (__ldcg(&in[u]) == CS_STAGE_PREFILL);
-        if (lane == 0) out[u] = stage;
-        if (stage != CS_STAGE_PREFILL) {
-          win_push(dw, (double)(b.c_end[u] - b.c_start[u]));
-          if (gap >= 0.0) win_push(gwin, gap);
-        }
+        if (lv) out[ul] = (uint8_t)x_out;
       }
       if (lane == 0) {
         m.lookback_lo[c] = lb_lo;
@@ -3019,11 +3110,357 @@ __global__ void __launch_bounds__(kStageWarps * 32)
       if ((it + 1) & 1)  // the result is in the scratch array: back into c_stage
         for (u64 u = (u64)blockIdx.x * blockDim.x + threadIdx.x; u < b.n_cycles; u += (u64)gridDim.x * blockDim.x)
           m.st[0][u] = __ldcg(&m.st[1][u]);
-      if (blockIdx.x == 0 && threadIdx.x == 0) *m.final_parity = 0;
+      if (blockIdx.x == 0 && threadIdx.x == 0) {
+        *m.final_parity = 0;
+        m.final_parity[1] = (unsigned int)(it + 1);  // iterations run (profiling)
+      }
       return;
     }
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) *m.final_parity = 0xffffffffu;  // did not converge
+}
+
+// ------------------------------------------ K4b helpers (k_stage_blocks)
+
+__device__ __forceinline__ int kth_bit32(uint32_t m, int k) {  // position of the k-th (0-based) set bit
+  int pos = 0;
+#pragma unroll
+  for (int w = 16; w >= 1; w >>= 1) {
+    const uint32_t low = m & ((1u << w) - 1u);
+    const int c = __popc(low);
+    if (k >= c) {
+      k -= c;
+      m >>= w;
+      pos += w;
+    } else {
+      m = low;
+    }
+  }
+  return pos;
+}
+__device__ __forceinline__ int kth_bit64(u64 m, int k) {
+  const uint32_t lo = (uint32_t)m;
+  const int c = __popc(lo);
+  return k < c ? kth_bit32(lo, k) : 32 + kth_bit32((uint32_t)(m >> 32), k - c);
+}
+
+// median of each lane's window [P - n, P) of a shared-memory list of
+// integer-valued doubles (len <= 64), exact (sorted keys value << 6 | offset)
+__device__ __forceinline__ double warp_list_median(const double* __restrict__ list, uint32_t len, uint32_t P,
+                                                   uint32_t n, bool need, u64* s_key, u64* s_cm, bool& bad) {
+  const uint32_t lane = threadIdx.x & 31;
+  u64 key[2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const uint32_t e = (uint32_t)h * 32u + lane;
+    key[h] = ~0ull;
+    if (e < len && e < 63u) {
+      const double v = list[e];
+      bad |= !(v >= 0.0 && v < 144115188075855872.0);  // < 2^57
+      key[h] = ((u64)(int64_t)v << 6) | e;
+    }
+  }
+#pragma unroll
+  for (uint32_t k = 2; k <= 64; k <<= 1) {
+#pragma unroll
+    for (uint32_t j = k >> 1; j >= 1; j >>= 1) {
+      u64 o0, o1;
+      if (j == 32) {
+        o0 = key[1];
+        o1 = key[0];
+      } else {
+        o0 = __shfl_xor_sync(0xffffffffu, key[0], j);
+        o1 = __shfl_xor_sync(0xffffffffu, key[1], j);
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const uint32_t i = (uint32_t)h * 32u + lane;
+        const u64 a = key[h], o = h ? o1 : o0;
+        const bool asc = (i & k) == 0, lower = (i & j) == 0;
+        key[h] = (lower == asc) ? (a < o ? a : o) : (a < o ? o : a);
+      }
+    }
+  }
+  s_key[lane] = key[0];
+  s_key[32 + lane] = key[1];
+  u64* s_bp = s_cm + 65;
+  s_bp[lane] = 0;
+  s_bp[32 + lane] = 0;
+  __syncwarp();
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const uint32_t t = (uint32_t)h * 32u + lane;
+    if (key[h] != ~0ull) s_bp[(uint32_t)(key[h] & 63u)] = 1ull << t;
+  }
+  __syncwarp();
+  const u64 b0 = s_bp[2 * lane], b1 = s_bp[2 * lane + 1];
+  u64 inc = b0 | b1;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const u64 y = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= (uint32_t)o) inc |= y;
+  }
+  u64 exc = __shfl_up_sync(0xffffffffu, inc, 1);
+  if (lane == 0) exc = 0;
+  s_cm[2 * lane] = exc;
+  s_cm[2 * lane + 1] = exc | b0;
+  if (lane == 31) s_cm[64] = inc;
+  __syncwarp();
+  double med = 0.0;
+  if (need && n > 0) {
+    const u64 m = s_cm[P] & ~s_cm[P - n];
+    const int t1 = kth_bit64(m, ((int)n - 1) / 2), t2 = kth_bit64(m, (int)n / 2);
+    const double v1 = (double)(int64_t)(s_key[t1] >> 6), v2 = (double)(int64_t)(s_key[t2] >> 6);
+    med = (n & 1) ? v1 : __dmul_rn(0.5, __dadd_rn(v1, v2));
+  }
+  __syncwarp();
+  return med;
+}
+
+// K4b: the chunked Jacobi of k_stage_jacobi with each chunk walked in blocks
+// of 32 cycles instead of one cycle at a time (windows <= 32, no streaming
+// carry).  Within a block, lane l's windows are the last W values of
+// (history ++ the block's non-Prefill cycles before l): the duration and
+// gap histories (oldest first, <= W each) and the block's values form one
+// list of <= 64 in shared memory.  A cycle needs only the side of each
+// median: with t(v) = fl(f * v) monotone in v, "x > fl(f * median)" holds
+// iff at least n/2 + 1 window values have t(v) < x (odd n); for even n
+// (median = (a + b) / 2 of the n/2-th and n/2+1-th) it holds iff that count
+// is >= n/2 + 1 and fails iff it is <= n/2 - 1; a count of exactly n/2
+// takes the exact median (sorted keys).  The block's own Prefill-ness is
+// speculated from the previous iterate and re-evaluated until it reproduces
+// itself (a local fixed point: cycles depend only on earlier ones).  Blocks
+// spanning an instance boundary are split into per-instance segments.
+// cycles.cpp:181-186 (median), 204-250 (decision, window updates).
+__global__ void __launch_bounds__(kStageWarps * 32)
+    k_stage_blocks(DevBuffers b, DevConfig cfg, StageMeta m) {
+  __shared__ double s_hd[kStageWarps][32], s_hg[kStageWarps][32];
+  __shared__ double s_cd[kStageWarps][64], s_cg[kStageWarps][64], s_t[kStageWarps][64];
+  __shared__ double s_stg[kStageWarps][64];  // rebuild staging (most recent first)
+  __shared__ u64 s_sort[kStageWarps][64 + 65 + 64];
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t W = (uint32_t)cfg.cyc.stage_window;
+  const uint32_t min_hist = (uint32_t)min((u64)cfg.cyc.stage_min_history, (u64)0xffffffffu);
+  const double fd = cfg.cyc.prefill_duration_factor, fg = cfg.cyc.prefill_gap_factor;
+  const bool sane = fd > 0.0 && fg > 0.0;
+  double* hd = s_hd[warp];
+  double* hg = s_hg[warp];
+  double* cd = s_cd[warp];
+  double* cg = s_cg[warp];
+  double* tt = s_t[warp];
+  double* stg = s_stg[warp];
+  u64* s_key = s_sort[warp];
+  u64* s_cm = s_sort[warp] + 64;
+  const uint32_t gw = blockIdx.x * kStageWarps + warp, nw = gridDim.x * kStageWarps;
+  if (__ldcg(b.any_unknown) == 0u) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      *m.final_parity = 0;
+      m.final_parity[2] = 1u;
+    }
+    return;
+  }
+  bool bad = false;
+  // side of "x > fl(f * median(list[P - n, P)))" (gap: f * max(1, median)):
+  // 1 / -1 decided by a count, 0 open
+  auto side = [&](const double* list, uint32_t len, uint32_t P, uint32_t n, double x, double f, bool is_gap,
+                  bool need) -> int {
+    for (uint32_t e = lane; e < len; e += 32) {
+      const double v = list[e];
+      tt[e] = __dmul_rn(f, is_gap ? (1.0 < v ? v : 1.0) : v);
+    }
+    __syncwarp();
+    int r = 0;
+    if (need && sane) {
+      uint32_t c = 0;
+      for (uint32_t j = P - n; j < P; ++j) c += tt[j] < x ? 1u : 0u;
+      const uint32_t n2 = n / 2u;
+      if (n & 1u) r = c >= n2 + 1u ? 1 : -1;
+      else r = c >= n2 + 1u ? 1 : (c + 1u <= n2 ? -1 : 0);
+    }
+    __syncwarp();
+    return r;
+  };
+  for (int it = 0; it < m.max_iter; ++it) {
+    const uint8_t* in = m.st[it & 1];
+    uint8_t* out = m.st[(it + 1) & 1];
+    for (uint32_t c = gw; c < m.n_chunks; c += nw) {
+      const u64 lo = (u64)c * kStageChunk;
+      const u64 hi = min(lo + (u64)kStageChunk, (u64)b.n_cycles);
+      bool any_unknown = false;
+      for (uint32_t i = b.c_inst[lo]; i <= b.c_inst[hi - 1] && !any_unknown; ++i)
+        any_unknown = b.inst[i].n_unknown != 0;
+      bool dirty = it == 0 && any_unknown;
+      if (!dirty && it > 0 && any_unknown) {
+        const u64 lb = __ldcg(&m.lookback_lo[c]);
+        for (u64 cc = lb / kStageChunk; cc < c && !dirty; ++cc)
+          dirty = __ldcg(&m.changed_iter[cc]) == it - 1;
+      }
+      if (!dirty) {
+        for (u64 u = lo + lane; u < hi; u += 32) out[u] = __ldcg(&in[u]);
+        continue;
+      }
+      bool changed = false;
+      uint32_t cur_inst = 0xffffffffu, nhd = 0, nhg = 0;
+      u64 lb_lo = lo;
+      for (u64 u0 = lo; u0 < hi; u0 += 32) {
+        const u64 u = u0 + lane;
+        const bool lv = u < hi;
+        uint8_t local = 3, pin = 0;
+        uint32_t inst = 0xffffffffu;
+        double dur = 0.0;
+        int64_t gap = -1;
+        if (lv) {
+          local = b.c_local[u];
+          pin = __ldcg(&in[u]);
+          inst = b.c_inst[u];
+          if (local != 3) {
+            const u64 c0 = b.cyc_off[inst];
+            dur = (double)(b.c_end[u] - b.c_start[u]);
+            gap = u > c0 ? b.c_start[u] - b.c_aend[u - 1] : -1;
+          }
+        }
+        uint8_t st = local;
+        const uint32_t nl = (uint32_t)min((u64)32, hi - u0);
+        uint32_t s0 = 0;
+        while (s0 < nl) {
+          const uint32_t inst_s = __shfl_sync(0xffffffffu, inst, s0);
+          const uint32_t diff = __ballot_sync(0xffffffffu, lane >= s0 && lane < nl && inst != inst_s);
+          const uint32_t s1 = diff ? (uint32_t)__ffs(diff) - 1u : nl;
+          const bool inseg = lane >= s0 && lane < s1 && local != 3;
+          if (inst_s != cur_inst) {
+            // history from the cycles before the segment in its instance
+            // (previous iterate), most recent first into staging
+            cur_inst = inst_s;
+            const u64 us = u0 + s0;
+            const u64 ci0 = b.cyc_off[inst_s];
+            uint32_t nd = 0, ng = 0;
+            i64 top = (i64)us - 1;
+            for (; top >= (i64)ci0 && (nd < W || ng < W); top -= 32) {
+              const i64 j = top - (i64)lane;
+              const bool inr = j >= (i64)ci0;
+              bool nonp = false, gok = false;
+              double jd = 0.0, jg = -1.0;
+              if (inr && b.c_local[j] != 3) {
+                nonp = __ldcg(&in[j]) != CS_STAGE_PREFILL;
+                jd = (double)(b.c_end[j] - b.c_start[j]);
+                jg = j > (i64)ci0 ? (double)(b.c_start[j] - b.c_aend[j - 1]) : -1.0;
+                gok = nonp && jg >= 0.0;
+              }
+              const uint32_t md = __ballot_sync(0xffffffffu, inr && nonp);
+              const uint32_t mg = __ballot_sync(0xffffffffu, inr && gok);
+              const uint32_t kd = nd + __popc(md & lanemask_lt());
+              const uint32_t kg = ng + __popc(mg & lanemask_lt());
+              if (inr && nonp && kd < W) stg[kd] = jd;
+              if (inr && gok && kg < W) stg[32 + kg] = jg;
+              nd = min(W, nd + __popc(md));
+              ng = min(W, ng + __popc(mg));
+              if (us == lo) lb_lo = (u64)max((i64)ci0, top - 31);
+            }
+            if (us == lo && top < (i64)ci0) lb_lo = ci0;
+            __syncwarp();
+            if (lane < nd) hd[lane] = stg[nd - 1 - lane];  // oldest first
+            if (lane < ng) hg[lane] = stg[32 + ng - 1 - lane];
+            nhd = nd;
+            nhg = ng;
+            __syncwarp();
+          }
+          // local fixed point of the segment's Prefill-ness
+          bool spec = local == CS_STAGE_PREFILL || (local == CS_STAGE_UNKNOWN && pin == CS_STAGE_PREFILL);
+          const uint32_t segm = __ballot_sync(0xffffffffu, inseg);
+          uint32_t td = 0, tg = 0;
+          for (int round = 0; round < 34; ++round) {
+            const bool npl = inseg && !spec, gkl = npl && gap >= 0;
+            const uint32_t bd = __ballot_sync(0xffffffffu, npl) & segm, bg = __ballot_sync(0xffffffffu, gkl) & segm;
+            const uint32_t rd = __popc(bd & lanemask_lt()), rg = __popc(bg & lanemask_lt());
+            td = __popc(bd);
+            tg = __popc(bg);
+            if (npl) cd[nhd + rd] = dur;
+            if (gkl) cg[nhg + rg] = (double)gap;
+            if (lane < nhd) cd[lane] = hd[lane];
+            if (lane < nhg) cg[lane] = hg[lane];
+            __syncwarp();
+            const uint32_t Pd = nhd + rd, Pg = nhg + rg;
+            const uint32_t n_d = min(W, Pd), n_g = min(W, Pg);
+            const bool want = inseg && local == CS_STAGE_UNKNOWN && n_d >= min_hist && gap >= 0;
+            uint8_t ns = local;
+            if (__any_sync(0xffffffffu, want)) {
+              const int sd = side(cd, nhd + td, Pd, n_d, dur, fd, false, want);
+              const int sg = side(cg, nhg + tg, Pg, n_g, (double)gap, fg, true, want && n_g > 0);
+              const bool open_d = want && sd == 0, open_g = want && n_g > 0 && sg == 0;
+              double med_dur = 0.0, mg = 0.0;
+              if (__any_sync(0xffffffffu, open_d))
+                med_dur = warp_list_median(cd, nhd + td, Pd, n_d, open_d, s_key, s_cm, bad);
+              if (__any_sync(0xffffffffu, open_g))
+                mg = warp_list_median(cg, nhg + tg, Pg, n_g, open_g, s_key, s_cm, bad);
+              if (want) {
+                const bool long_cycle = open_d ? dur > __dmul_rn(fd, med_dur) : sd > 0;
+                bool long_gap;
+                if (n_g == 0) long_gap = (double)gap > __dmul_rn(fg, 1.0);
+                else if (open_g) long_gap = (double)gap > __dmul_rn(fg, 1.0 < mg ? mg : 1.0);
+                else long_gap = sg > 0;
+                ns = (long_cycle && long_gap) ? CS_STAGE_PREFILL : CS_STAGE_DECODE;
+              }
+            }
+            const bool nspec = ns == CS_STAGE_PREFILL;
+            const bool moved = __any_sync(0xffffffffu, inseg && nspec != spec);
+            if (inseg) st = ns;
+            __syncwarp();
+            if (!moved) break;
+            if (inseg) spec = nspec;
+          }
+          // histories after the segment: last W of (history ++ segment
+          // values); the final round's lists are exactly that
+          const uint32_t ld = nhd + td, lg = nhg + tg;
+          const uint32_t kd = min(W, ld), kg = min(W, lg);
+          double vd = 0.0, vg = 0.0;
+          if (lane < kd) vd = cd[ld - kd + lane];
+          if (lane < kg) vg = cg[lg - kg + lane];
+          __syncwarp();
+          if (lane < kd) hd[lane] = vd;
+          if (lane < kg) hg[lane] = vg;
+          nhd = kd;
+          nhg = kg;
+          __syncwarp();
+          s0 = s1;
+        }
+        if (lv) {
+          out[u] = st;
+          changed |= local != 3 && (st == CS_STAGE_PREFILL) != (pin == CS_STAGE_PREFILL);
+        }
+      }
+      changed = __any_sync(0xffffffffu, changed);
+      if (lane == 0) {
+        m.lookback_lo[c] = lb_lo;
+        if (changed) {
+          m.changed_iter[c] = it;
+          atomicOr(m.any_changed + (it & 1), 1u);
+        }
+      }
+    }
+    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(m.final_parity + 3, 1u);
+    grid_barrier(m.bar_count, m.bar_gen);
+    const bool more = __ldcg(m.any_changed + (it & 1)) != 0;
+    const bool invalid = __ldcg(m.final_parity + 3) != 0;
+    grid_barrier(m.bar_count, m.bar_gen);
+    if (blockIdx.x == 0 && threadIdx.x == 0) m.any_changed[it & 1] = 0;
+    if (!more || invalid) {
+      if (invalid) {  // values beyond the exact key range: the sequential-window kernel redoes it
+        for (u64 u = (u64)blockIdx.x * blockDim.x + threadIdx.x; u < b.n_cycles; u += (u64)gridDim.x * blockDim.x)
+          m.st[0][u] = b.c_local[u];
+      } else if ((it + 1) & 1) {
+        for (u64 u = (u64)blockIdx.x * blockDim.x + threadIdx.x; u < b.n_cycles; u += (u64)gridDim.x * blockDim.x)
+          m.st[0][u] = __ldcg(&m.st[1][u]);
+      }
+      if (blockIdx.x == 0 && threadIdx.x == 0) {
+        *m.final_parity = 0;
+        m.final_parity[1] = (unsigned int)(it + 1);
+        m.final_parity[2] = invalid ? 0u : 1u;
+        m.final_parity[3] = 0u;
+      }
+      return;
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) *m.final_parity = 0xffffffffu;
 }
 
 int launch_stage_heuristic(const DevBuffers& b, const DevConfig& cfg, const StageMeta& m, cudaStream_t s,
@@ -3031,16 +3468,35 @@ int launch_stage_heuristic(const DevBuffers& b, const DevConfig& cfg, const Stag
   if (!b.n_cycles || m.n_chunks == 0) return 0;
   const size_t smem = (size_t)kStageWarps * 4 * cfg.cyc.stage_window * sizeof(double);
   if (smem > 200 * 1024) return -1;
-  cudaFuncSetAttribute(k_stage_jacobi, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int dev0 = 0, n_sm0 = 148;
+  cudaGetDevice(&dev0);
+  cudaDeviceGetAttribute(&n_sm0, cudaDevAttrMultiProcessorCount, dev0);
+  if (!b.stream && cfg.cyc.stage_window <= 32 && cfg.cyc.stage_window >= 1) {
+    // block-parallel chunks first; the sequential-window kernel below only
+    // runs when it could not (values beyond its exact key range)
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_stage_blocks, kStageWarps * 32, 0);
+    if (per_sm < 1) per_sm = 1;
+    uint64_t grid = (uint64_t)n_sm0 * per_sm;
+    const uint64_t need = (m.n_chunks + kStageWarps - 1) / kStageWarps;
+    if (grid > need) grid = need;
+    k_stage_blocks<<<(unsigned)grid, kStageWarps * 32, 0, s>>>(b, cfg, m);
+    ++*launches;
+  }
+  // windows of <= 32 values live in registers (one value per lane)
+  const bool reg = cfg.cyc.stage_window <= 32;
+  const void* fn = reg ? (const void*)k_stage_jacobi<true> : (const void*)k_stage_jacobi<false>;
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int dev = 0, n_sm = 148, per_sm = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_stage_jacobi, kStageWarps * 32, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kStageWarps * 32, smem);
   if (per_sm < 1) per_sm = 1;
   uint64_t grid = (uint64_t)n_sm * per_sm;  // persistent: every CTA resident (grid barrier)
   const uint64_t need = (m.n_chunks + kStageWarps - 1) / kStageWarps;
   if (grid > need) grid = need;
-  k_stage_jacobi<<<(unsigned)grid, kStageWarps * 32, smem, s>>>(b, cfg, m);
+  if (reg) k_stage_jacobi<true><<<(unsigned)grid, kStageWarps * 32, smem, s>>>(b, cfg, m);
+  else k_stage_jacobi<false><<<(unsigned)grid, kStageWarps * 32, smem, s>>>(b, cfg, m);
   ++*launches;
   return 0;
 }
