@@ -404,30 +404,52 @@ __device__ __forceinline__ void cache_add(SNameCache& c, NameStat* g, uint32_t n
   c.lo[k] = nl;
 }
 
-__device__ void cache_flush_warp(SNameCache& c, NameStat* g, WarpNameRow* wrows) {
+// flush one warp's per-lane caches name by name: the smallest unflushed name
+// of the warp, every lane's entry for it summed by butterflies (exact u128),
+// one set of global atomics per name (a handful of names per instance)
+__device__ void cache_flush_warp(SNameCache& c, NameStat* g, WarpNameRow*) {
   const int lane = c.lane;
-  if (lane < kWarpNameRows) {
-    wrows[lane].name = 0xffffffffu;
-    wrows[lane].cnt = 0;
-    wrows[lane].sum = wrows[lane].sq_lo = wrows[lane].sq_hi = 0;
-  }
   __syncwarp();
-  for (int i = 0; i < kNameCache; ++i) {
-    const int k = i * 32 + lane;
-    const uint32_t n = c.name[k], cn = c.cnt[k];
-    rows_merge(wrows, g, n != 0xffffffffu && cn > 0, n, cn, c.sum[k], c.lo[k], c.hi[k]);
-  }
-  __syncwarp();
-  if (lane < kWarpNameRows) {
-    const WarpNameRow r = wrows[lane];
-    if (r.name != 0xffffffffu && r.cnt) {
-      atomicAdd(&g[r.name].count, (u64)r.cnt);
-      atomicAdd(&g[r.name].sum, r.sum);
-      atomic_add_u128(&g[r.name].sumsq_lo, &g[r.name].sumsq_hi, r.sq_lo, r.sq_hi);
+  for (;;) {
+    uint32_t mine = 0xffffffffu;
+#pragma unroll
+    for (int i = 0; i < kNameCache; ++i) {
+      const int k = i * 32 + lane;
+      if (c.cnt[k] && c.name[k] < mine) mine = c.name[k];
+    }
+    const uint32_t nm = __reduce_min_sync(0xffffffffu, mine);
+    if (nm == 0xffffffffu) break;
+    uint32_t cnt = 0;
+    u64 sum = 0, lo = 0, hi = 0;
+#pragma unroll
+    for (int i = 0; i < kNameCache; ++i) {
+      const int k = i * 32 + lane;
+      if (c.cnt[k] && c.name[k] == nm) {
+        cnt = c.cnt[k];
+        sum = c.sum[k];
+        lo = c.lo[k];
+        hi = c.hi[k];
+        c.cnt[k] = 0;
+      }
+    }
+    cnt = __reduce_add_sync(0xffffffffu, cnt);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      sum += __shfl_xor_sync(0xffffffffu, sum, o);
+      const u64 ol = __shfl_xor_sync(0xffffffffu, lo, o), oh = __shfl_xor_sync(0xffffffffu, hi, o);
+      const u64 nl = lo + ol;
+      hi += oh + (nl < lo ? 1ull : 0ull);
+      lo = nl;
+    }
+    if (lane == 0) {
+      atomicAdd(&g[nm].count, (u64)cnt);
+      atomicAdd(&g[nm].sum, sum);
+      atomic_add_u128(&g[nm].sumsq_lo, &g[nm].sumsq_hi, lo, hi);
     }
   }
   __syncwarp();
   cache_clear(c);
+  __syncwarp();
 }
 
 // --------------------------------------- K1 / K12 event scan (warp streaming)
@@ -3690,6 +3712,7 @@ constexpr int kSegWalkUnroll = CS_SEG_WALK_UNROLL;  // phase B: events in flight
 constexpr int kSegThreads = 256;
 constexpr int kSegWarps = kSegThreads / 32;
 constexpr int kSegList = 128;      // anchors of one range listed in shared memory
+constexpr uint32_t kSegClaim = 1;  // consecutive ranges per ticket (more serialises the look-back chain)
 constexpr int kSegNames = 1024;    // name table staged in shared memory
 constexpr uint32_t kSegTie = 0x80000000u;  // apos flag: equal start_ts before the anchor
 
@@ -3840,14 +3863,23 @@ __global__ void __launch_bounds__(kSegThreads, 2)
     npend = rest;
     __syncwarp();
   };
+  // tickets hand out kSegClaim consecutive ranges at a time (a range's
+  // look-back needs its predecessor's count, published only when its owner
+  // reaches it, so claims larger than one range serialise the grid)
+  uint32_t r = 0, r_end = 0;
   for (;;) {
-    uint32_t r = 0;
-    if (lane == 0) r = atomicAdd(sm.ticket, 1u);
-    r = __shfl_sync(0xffffffffu, r, 0);
+    if (r == r_end) {
+      uint32_t t = 0;
+      if (lane == 0) t = atomicAdd(sm.ticket, 1u);
+      t = __shfl_sync(0xffffffffu, t, 0);
+      r = t * kSegClaim;
+      r_end = min(r + kSegClaim, sm.n_ranges);
+    }
     if (r >= sm.n_ranges) break;
-    const u64 rb = sm.range_begin[r];
-    const uint32_t n = (uint32_t)(sm.range_end[r] - rb);
-    const uint32_t inst = sm.range_inst[r];
+    const uint32_t rc = r++;
+    const u64 rb = sm.range_begin[rc];
+    const uint32_t n = (uint32_t)(sm.range_end[rc] - rb);
+    const uint32_t inst = sm.range_inst[rc];
 #if CS_SEG_PREFETCH
     // pull the whole range (+ a cycle past it) into L2 at once: the stream's
     // later iterations hit L2 instead of each waiting out a DRAM latency
@@ -3855,7 +3887,7 @@ __global__ void __launch_bounds__(kSegThreads, 2)
     // the grid's warps), one range-time ahead
     if (lane < 2) {
       const uint32_t ahead = sm.prefetch_ahead == 0xffffffffu ? gridDim.x * (uint32_t)kSegWarps : sm.prefetch_ahead;
-      const uint32_t pr = lane == 0 ? r : r + ahead;
+      const uint32_t pr = lane == 0 ? rc : rc + ahead;
       if ((lane == 0 || ahead) && pr < sm.n_ranges) {
         const u64 pb = sm.range_begin[pr];
         const uint32_t pi = sm.range_inst[pr];
@@ -3936,11 +3968,11 @@ __global__ void __launch_bounds__(kSegThreads, 2)
     if (__any_sync(0xffffffffu, unsorted) && lane == 0) atomicOr(&b.inst[inst].unsorted, 1u);
     const uint32_t A = cnt;
     if (lane == 0) {
-      if (r == 0) {
+      if (rc == 0) {
         st_relaxed(&sm.lb_state[0], kFlagPrefix | (u64)A);
         sm.range_prefix[0] = 0;
       } else {
-        st_relaxed(&sm.lb_state[r], kFlagAgg | (u64)A);
+        st_relaxed(&sm.lb_state[rc], kFlagAgg | (u64)A);
       }
     }
     if (A > (uint32_t)kSegList) {  // too dense for the list: the host re-runs two-pass
@@ -3976,7 +4008,7 @@ __global__ void __launch_bounds__(kSegThreads, 2)
     }
     // ---------------- B + C: 32 cycles per batch, lane owns cycle k0 + lane
     u64 base = 0;
-    bool have_base = r == 0;
+    bool have_base = rc == 0;
     for (uint32_t k0 = 0; k0 == 0 || k0 < A; k0 += 32) {
       const uint32_t k = k0 + lane;
       const bool live = k < A;
@@ -4045,18 +4077,25 @@ __global__ void __launch_bounds__(kSegThreads, 2)
       // slot base: decoupled look-back over the preceding ranges (they
       // published their counts long ago, when their scans finished)
       if (!have_base) {
+        // lane k looks at range r-1-k; only the ranges up to the nearest
+        // published prefix matter, so only those are waited for
         u64 excl = 0;
-        long long j = (long long)r - 1;
+        long long j = (long long)rc - 1;
         for (;;) {
           const long long idx = j - lane;
           u64 v = idx >= 0 ? ld_relaxed(&sm.lb_state[idx]) : kFlagPrefix;
-          while (__any_sync(0xffffffffu, (v & (kFlagAgg | kFlagPrefix)) == 0)) {
-            if ((v & (kFlagAgg | kFlagPrefix)) == 0) v = ld_relaxed(&sm.lb_state[idx]);
+          uint32_t pm;
+          int L;
+          for (;;) {
+            const uint32_t has = __ballot_sync(0xffffffffu, (v & (kFlagAgg | kFlagPrefix)) != 0);
+            pm = __ballot_sync(0xffffffffu, (v & kFlagPrefix) != 0);
+            L = pm ? __ffs(pm) - 1 : 31;
+            const uint32_t need = L == 31 ? 0xffffffffu : ((1u << (L + 1)) - 1u);
+            if ((has & need) == need) break;
+            if ((uint32_t)lane <= (uint32_t)L && (v & (kFlagAgg | kFlagPrefix)) == 0) v = ld_relaxed(&sm.lb_state[idx]);
           }
-          const uint32_t pm = __ballot_sync(0xffffffffu, (v & kFlagPrefix) != 0);
           const u64 val = v & kValMask;
           if (pm) {
-            const int L = __ffs(pm) - 1;
             excl += warp_sum_u64(lane <= L ? val : 0ull);
             break;
           }
@@ -4066,8 +4105,8 @@ __global__ void __launch_bounds__(kSegThreads, 2)
         base = excl;
         have_base = true;
         if (lane == 0) {
-          sm.range_prefix[r] = excl;
-          st_relaxed(&sm.lb_state[r], kFlagPrefix | (excl + A));
+          sm.range_prefix[rc] = excl;
+          st_relaxed(&sm.lb_state[rc], kFlagPrefix | (excl + A));
         }
       }
       const uint32_t um = __ballot_sync(0xffffffffu, live && !hole && stage == CS_STAGE_UNKNOWN);
