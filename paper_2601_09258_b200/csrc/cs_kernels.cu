@@ -1078,17 +1078,24 @@ __global__ void __launch_bounds__(kRecThreads) k_records_scatter(DevBuffers b, D
   }
   __syncthreads();
   // per-instance record offsets: the rank of each instance's first cycle that
-  // falls in this block (empty instances share it)
+  // falls in this block (empty instances share it); the instances of a block
+  // split across its threads (a fleet batch has hundreds per block)
+  __shared__ uint32_t s_lo;
+  const u64 ge = gb + kRecBlock < b.n_cycles ? gb + kRecBlock : b.n_cycles;
   if (threadIdx.x == 0) {
-    const u64 ge = gb + kRecBlock < b.n_cycles ? gb + kRecBlock : b.n_cycles;
     uint32_t lo = 0, hi = b.n_inst + 1;  // first i with cyc_off[i] >= gb
     while (lo < hi) {
       const uint32_t mid = (lo + hi) >> 1;
       if (b.cyc_off[mid] < gb) lo = mid + 1;
       else hi = mid;
     }
-    for (uint32_t i = lo; i < b.n_inst && b.cyc_off[i] < ge; ++i)
-      b.rec_off[i] = base + s_rank[b.cyc_off[i] - gb];
+    s_lo = lo;
+  }
+  __syncthreads();
+  for (uint32_t i = s_lo + threadIdx.x; i < b.n_inst; i += kRecThreads) {
+    const u64 c0 = b.cyc_off[i];
+    if (c0 >= ge) break;  // cyc_off is nondecreasing
+    b.rec_off[i] = base + s_rank[c0 - gb];
   }
 }
 
@@ -2960,7 +2967,7 @@ __device__ __forceinline__ void grid_barrier(unsigned int* count, unsigned int* 
 
 template <bool kReg>
 __global__ void __launch_bounds__(kStageWarps * 32)
-    k_stage_jacobi(DevBuffers b, DevConfig cfg, StageMeta m) {
+    k_stage_jacobi(DevBuffers b, DevConfig cfg, StageMeta m, int after_blocks) {
   using WinT = typename std::conditional<kReg, RegWin, Win>::type;
   extern __shared__ __align__(16) double s_win[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -2970,7 +2977,7 @@ __global__ void __launch_bounds__(kStageWarps * 32)
   const uint32_t gw = blockIdx.x * kStageWarps + warp, nw = gridDim.x * kStageWarps;
   // no Unknown cycle anywhere (the common forward_mode case): nothing to do;
   // every CTA reads the same flag, so none waits at a barrier
-  if (__ldcg(b.any_unknown) == 0u || __ldcg(m.final_parity + 2) != 0u) {  // nothing Unknown / k_stage_blocks converged
+  if (__ldcg(b.any_unknown) == 0u || (after_blocks && __ldcg(m.final_parity + 2) != 0u)) {  // nothing Unknown / k_stage_blocks converged
     if (blockIdx.x == 0 && threadIdx.x == 0) *m.final_parity = 0;
     return;
   }
@@ -3482,7 +3489,10 @@ __global__ void __launch_bounds__(kStageWarps * 32)
       return;
     }
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) *m.final_parity = 0xffffffffu;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    *m.final_parity = 0xffffffffu;
+    m.final_parity[2] = 0u;  // no fixed point: the sequential-window kernel continues from the iterate
+  }
 }
 
 int launch_stage_heuristic(const DevBuffers& b, const DevConfig& cfg, const StageMeta& m, cudaStream_t s,
@@ -3493,7 +3503,8 @@ int launch_stage_heuristic(const DevBuffers& b, const DevConfig& cfg, const Stag
   int dev0 = 0, n_sm0 = 148;
   cudaGetDevice(&dev0);
   cudaDeviceGetAttribute(&n_sm0, cudaDevAttrMultiProcessorCount, dev0);
-  if (!b.stream && cfg.cyc.stage_window <= 32 && cfg.cyc.stage_window >= 1) {
+  const bool blocks = !b.stream && cfg.cyc.stage_window <= 32 && cfg.cyc.stage_window >= 1;
+  if (blocks) {
     // block-parallel chunks first; the sequential-window kernel below only
     // runs when it could not (values beyond its exact key range)
     int per_sm = 0;
@@ -3517,8 +3528,8 @@ int launch_stage_heuristic(const DevBuffers& b, const DevConfig& cfg, const Stag
   uint64_t grid = (uint64_t)n_sm * per_sm;  // persistent: every CTA resident (grid barrier)
   const uint64_t need = (m.n_chunks + kStageWarps - 1) / kStageWarps;
   if (grid > need) grid = need;
-  if (reg) k_stage_jacobi<true><<<(unsigned)grid, kStageWarps * 32, smem, s>>>(b, cfg, m);
-  else k_stage_jacobi<false><<<(unsigned)grid, kStageWarps * 32, smem, s>>>(b, cfg, m);
+  if (reg) k_stage_jacobi<true><<<(unsigned)grid, kStageWarps * 32, smem, s>>>(b, cfg, m, blocks ? 1 : 0);
+  else k_stage_jacobi<false><<<(unsigned)grid, kStageWarps * 32, smem, s>>>(b, cfg, m, blocks ? 1 : 0);
   ++*launches;
   return 0;
 }
