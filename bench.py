@@ -519,7 +519,7 @@ def run_ours(args, rank, world, local_rank):
     n_records = sum(s.n_records for s in summ)
     P, Cs, R = an.cycle.n_phases, an.cycle.n_beta_slots, an.cycle.n_comm_slots
     # algorithmic bytes per launch
-    cyc_out = n_cycles * (48 + 4 + 2 + 4 + 8 * P + 16 * Cs + 9 * R)  # per-cycle outputs
+    cyc_out = n_cycles * (48 + 4 + 2 + 4 + 8 * P + 8 * Cs + 9 * R)  # per-cycle outputs (beta quotients formed on read)
     scan_t = sum(scan_ms) / len(scan_ms)
     red_t = sum(reduce_ms) / len(reduce_ms)
     if red_t == 0.0:  # single-read segmentation: events read once, cycle outputs written once
@@ -531,14 +531,17 @@ def run_ours(args, rank, world, local_rank):
                else ("scan_events", scan_bytes, scan_t))
     achieved = dom[1] / (dom[2] * 1e-3) / 1e9
     # dram bytes of the dominant kernel from the committed ncu --set full
-    # capture of this same command (profiles/r1_ncu_traffic.json); only for
+    # capture of this same command (profiles/r2_ncu_traffic.json, else r1); only for
     # the default workload it was taken on
     traffic = None
     kname = {"cycle_reduce": "k_cycle_reduce_v2", "scan_events": "k_scan_warp",
              "segment_range": "k_segment_range"}[dom[0]]
     step_dram = None  # ncu DRAM bytes of the step's captured kernels (the full capture)
+    tpath = os.path.join(ROOT, "profiles", "r2_ncu_traffic.json")
     try:
-        with open(os.path.join(ROOT, "profiles", "r1_ncu_traffic.json")) as f:
+        if not os.path.exists(tpath):
+            tpath = os.path.join(ROOT, "profiles", "r1_ncu_traffic.json")
+        with open(tpath) as f:
             allk = json.load(f)
         tr = allk.get(kname)
         if tr and args.workload == "c2":
@@ -569,12 +572,12 @@ def run_ours(args, rank, world, local_rank):
         "roofline": {"bound": "hbm", "kernel": dom[0], "achieved": achieved, "peak": peak,
                      "peak_source": peak_src, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "algorithmic_bytes": dom[1],
-                     "traffic_source": "profiles/r1_ncu_traffic.json (ncu --set full, dram read+write)",
+                     "traffic_source": os.path.relpath(tpath, ROOT) + " (ncu --set full, dram read+write)",
                      "kernel_ms": dom[2], "event_pass_ms": scan_t, "cycle_reduce_ms": red_t,
                      "path_frac_44p5B_per_event": path_bytes / (dev_ms * 1e-3) / 1e9 / peak,
                      "step_dram_frac_ncu": (step_dram / (dev_ms * 1e-3) / 1e9 / peak) if step_dram else None,
                      "step_dram_note": "ncu DRAM read+write of one launch of each captured kernel "
-                                       "(scan, bounds, reduce, score, detect) over the measured step time"},
+                                       "(segmentation, records, score, detect, stage) over the measured step time"},
         "e2e": {"value": world * n_events / (e2e * 1e-3), "unit": UNIT,
                 "h2d_bytes_per_step": ev_bytes + wl_bytes, "d2h_bytes_per_step": d2h,
                 "ms_per_step": e2e,
