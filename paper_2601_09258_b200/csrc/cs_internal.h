@@ -228,7 +228,10 @@ struct StageMeta {
   unsigned int* final_parity;
   int max_iter;
 };
-constexpr uint32_t kStageChunkCycles = 256;
+#ifndef CS_STAGE_CHUNK
+#define CS_STAGE_CHUNK 256
+#endif
+constexpr uint32_t kStageChunkCycles = CS_STAGE_CHUNK;  // stage heuristic chunk (cycle slots)
 // K4b (k_stage_blocks, windows <= 32, not streaming) runs first; K4' only
 // when K4b could not (final_parity[2] == 0)
 int launch_stage_heuristic(const DevBuffers& b, const DevConfig& cfg, const StageMeta& m, cudaStream_t s,

@@ -2829,7 +2829,7 @@ void launch_bounds(const DevBuffers& b, cudaStream_t s, uint64_t* launches) {
 // Stages depend only on earlier cycles, so iteration k makes at least the
 // first k chunks exact and the fixed point is the sequential result.  One
 // persistent grid, a grid barrier between iterations.
-constexpr int kStageChunk = 256;
+constexpr int kStageChunk = (int)kStageChunkCycles;
 constexpr int kStageWarps = 4;
 
 struct Win {  // one trailing window in the warp's shared memory
@@ -3149,103 +3149,6 @@ __global__ void __launch_bounds__(kStageWarps * 32)
   if (blockIdx.x == 0 && threadIdx.x == 0) *m.final_parity = 0xffffffffu;  // did not converge
 }
 
-// ------------------------------------------ K4b helpers (k_stage_blocks)
-
-__device__ __forceinline__ int kth_bit32(uint32_t m, int k) {  // position of the k-th (0-based) set bit
-  int pos = 0;
-#pragma unroll
-  for (int w = 16; w >= 1; w >>= 1) {
-    const uint32_t low = m & ((1u << w) - 1u);
-    const int c = __popc(low);
-    if (k >= c) {
-      k -= c;
-      m >>= w;
-      pos += w;
-    } else {
-      m = low;
-    }
-  }
-  return pos;
-}
-__device__ __forceinline__ int kth_bit64(u64 m, int k) {
-  const uint32_t lo = (uint32_t)m;
-  const int c = __popc(lo);
-  return k < c ? kth_bit32(lo, k) : 32 + kth_bit32((uint32_t)(m >> 32), k - c);
-}
-
-// median of each lane's window [P - n, P) of a shared-memory list of
-// integer-valued doubles (len <= 64), exact (sorted keys value << 6 | offset)
-__device__ __forceinline__ double warp_list_median(const double* __restrict__ list, uint32_t len, uint32_t P,
-                                                   uint32_t n, bool need, u64* s_key, u64* s_cm, bool& bad) {
-  const uint32_t lane = threadIdx.x & 31;
-  u64 key[2];
-#pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    const uint32_t e = (uint32_t)h * 32u + lane;
-    key[h] = ~0ull;
-    if (e < len && e < 63u) {
-      const double v = list[e];
-      bad |= !(v >= 0.0 && v < 144115188075855872.0);  // < 2^57
-      key[h] = ((u64)(int64_t)v << 6) | e;
-    }
-  }
-#pragma unroll
-  for (uint32_t k = 2; k <= 64; k <<= 1) {
-#pragma unroll
-    for (uint32_t j = k >> 1; j >= 1; j >>= 1) {
-      u64 o0, o1;
-      if (j == 32) {
-        o0 = key[1];
-        o1 = key[0];
-      } else {
-        o0 = __shfl_xor_sync(0xffffffffu, key[0], j);
-        o1 = __shfl_xor_sync(0xffffffffu, key[1], j);
-      }
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const uint32_t i = (uint32_t)h * 32u + lane;
-        const u64 a = key[h], o = h ? o1 : o0;
-        const bool asc = (i & k) == 0, lower = (i & j) == 0;
-        key[h] = (lower == asc) ? (a < o ? a : o) : (a < o ? o : a);
-      }
-    }
-  }
-  s_key[lane] = key[0];
-  s_key[32 + lane] = key[1];
-  u64* s_bp = s_cm + 65;
-  s_bp[lane] = 0;
-  s_bp[32 + lane] = 0;
-  __syncwarp();
-#pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    const uint32_t t = (uint32_t)h * 32u + lane;
-    if (key[h] != ~0ull) s_bp[(uint32_t)(key[h] & 63u)] = 1ull << t;
-  }
-  __syncwarp();
-  const u64 b0 = s_bp[2 * lane], b1 = s_bp[2 * lane + 1];
-  u64 inc = b0 | b1;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const u64 y = __shfl_up_sync(0xffffffffu, inc, o);
-    if (lane >= (uint32_t)o) inc |= y;
-  }
-  u64 exc = __shfl_up_sync(0xffffffffu, inc, 1);
-  if (lane == 0) exc = 0;
-  s_cm[2 * lane] = exc;
-  s_cm[2 * lane + 1] = exc | b0;
-  if (lane == 31) s_cm[64] = inc;
-  __syncwarp();
-  double med = 0.0;
-  if (need && n > 0) {
-    const u64 m = s_cm[P] & ~s_cm[P - n];
-    const int t1 = kth_bit64(m, ((int)n - 1) / 2), t2 = kth_bit64(m, (int)n / 2);
-    const double v1 = (double)(int64_t)(s_key[t1] >> 6), v2 = (double)(int64_t)(s_key[t2] >> 6);
-    med = (n & 1) ? v1 : __dmul_rn(0.5, __dadd_rn(v1, v2));
-  }
-  __syncwarp();
-  return med;
-}
-
 // K4b: the chunked Jacobi of k_stage_jacobi with each chunk walked in blocks
 // of 32 cycles instead of one cycle at a time (windows <= 32, no streaming
 // carry).  Within a block, lane l's windows are the last W values of
@@ -3255,8 +3158,9 @@ __device__ __forceinline__ double warp_list_median(const double* __restrict__ li
 // median: with t(v) = fl(f * v) monotone in v, "x > fl(f * median)" holds
 // iff at least n/2 + 1 window values have t(v) < x (odd n); for even n
 // (median = (a + b) / 2 of the n/2-th and n/2+1-th) it holds iff that count
-// is >= n/2 + 1 and fails iff it is <= n/2 - 1; a count of exactly n/2
-// takes the exact median (sorted keys).  The block's own Prefill-ness is
+// is >= n/2 + 1 and fails iff it is <= n/2 - 1; with a count of exactly n/2
+// the two middle values are the largest value below the threshold and the
+// smallest one at or above it.  The block's own Prefill-ness is
 // speculated from the previous iterate and re-evaluated until it reproduces
 // itself (a local fixed point: cycles depend only on earlier ones).  Blocks
 // spanning an instance boundary are split into per-instance segments.
@@ -3266,7 +3170,6 @@ __global__ void __launch_bounds__(kStageWarps * 32)
   __shared__ double s_hd[kStageWarps][32], s_hg[kStageWarps][32];
   __shared__ double s_cd[kStageWarps][64], s_cg[kStageWarps][64], s_t[kStageWarps][64];
   __shared__ double s_stg[kStageWarps][64];  // rebuild staging (most recent first)
-  __shared__ u64 s_sort[kStageWarps][64 + 65 + 64];
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint32_t W = (uint32_t)cfg.cyc.stage_window;
   const uint32_t min_hist = (uint32_t)min((u64)cfg.cyc.stage_min_history, (u64)0xffffffffu);
@@ -3278,8 +3181,6 @@ __global__ void __launch_bounds__(kStageWarps * 32)
   double* cg = s_cg[warp];
   double* tt = s_t[warp];
   double* stg = s_stg[warp];
-  u64* s_key = s_sort[warp];
-  u64* s_cm = s_sort[warp] + 64;
   const uint32_t gw = blockIdx.x * kStageWarps + warp, nw = gridDim.x * kStageWarps;
   if (__ldcg(b.any_unknown) == 0u) {
     if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -3288,23 +3189,37 @@ __global__ void __launch_bounds__(kStageWarps * 32)
     }
     return;
   }
-  bool bad = false;
-  // side of "x > fl(f * median(list[P - n, P)))" (gap: f * max(1, median)):
-  // 1 / -1 decided by a count, 0 open
+  // the count argument needs t(v) = fl(f * v) nondecreasing: f > 0; other
+  // factors go to the sequential-window kernel
+  bool bad = !sane;
+  // "x > fl(f * median(list[P - n, P)))" (gap: f * max(1, median)), from a
+  // count; a count of exactly n/2 (even n) fixes the two middle values as the
+  // largest value below the threshold and the smallest one at or above it,
+  // found by the lane alone (no warp-wide sort)
   auto side = [&](const double* list, uint32_t len, uint32_t P, uint32_t n, double x, double f, bool is_gap,
-                  bool need) -> int {
+                  bool need) -> bool {
     for (uint32_t e = lane; e < len; e += 32) {
       const double v = list[e];
       tt[e] = __dmul_rn(f, is_gap ? (1.0 < v ? v : 1.0) : v);
     }
     __syncwarp();
-    int r = 0;
-    if (need && sane) {
+    bool r = false;
+    if (need) {
       uint32_t c = 0;
       for (uint32_t j = P - n; j < P; ++j) c += tt[j] < x ? 1u : 0u;
       const uint32_t n2 = n / 2u;
-      if (n & 1u) r = c >= n2 + 1u ? 1 : -1;
-      else r = c >= n2 + 1u ? 1 : (c + 1u <= n2 ? -1 : 0);
+      if ((n & 1u) || c != n2) {
+        r = c >= n2 + 1u;
+      } else {
+        double a = -1.0, bv = 1.0 / 0.0;
+        for (uint32_t j = P - n; j < P; ++j) {
+          const double v = list[j];
+          if (tt[j] < x) a = a < v ? v : a;
+          else bv = bv < v ? bv : v;
+        }
+        const double med = __dmul_rn(0.5, __dadd_rn(a, bv));
+        r = x > __dmul_rn(f, is_gap ? (1.0 < med ? med : 1.0) : med);
+      }
     }
     __syncwarp();
     return r;
@@ -3413,20 +3328,10 @@ __global__ void __launch_bounds__(kStageWarps * 32)
             const bool want = inseg && local == CS_STAGE_UNKNOWN && n_d >= min_hist && gap >= 0;
             uint8_t ns = local;
             if (__any_sync(0xffffffffu, want)) {
-              const int sd = side(cd, nhd + td, Pd, n_d, dur, fd, false, want);
-              const int sg = side(cg, nhg + tg, Pg, n_g, (double)gap, fg, true, want && n_g > 0);
-              const bool open_d = want && sd == 0, open_g = want && n_g > 0 && sg == 0;
-              double med_dur = 0.0, mg = 0.0;
-              if (__any_sync(0xffffffffu, open_d))
-                med_dur = warp_list_median(cd, nhd + td, Pd, n_d, open_d, s_key, s_cm, bad);
-              if (__any_sync(0xffffffffu, open_g))
-                mg = warp_list_median(cg, nhg + tg, Pg, n_g, open_g, s_key, s_cm, bad);
+              const bool long_cycle = side(cd, nhd + td, Pd, n_d, dur, fd, false, want);
+              const bool lg = side(cg, nhg + tg, Pg, n_g, (double)gap, fg, true, want && n_g > 0);
               if (want) {
-                const bool long_cycle = open_d ? dur > __dmul_rn(fd, med_dur) : sd > 0;
-                bool long_gap;
-                if (n_g == 0) long_gap = (double)gap > __dmul_rn(fg, 1.0);
-                else if (open_g) long_gap = (double)gap > __dmul_rn(fg, 1.0 < mg ? mg : 1.0);
-                else long_gap = sg > 0;
+                const bool long_gap = n_g == 0 ? (double)gap > __dmul_rn(fg, 1.0) : lg;
                 ns = (long_cycle && long_gap) ? CS_STAGE_PREFILL : CS_STAGE_DECODE;
               }
             }
@@ -3473,7 +3378,7 @@ __global__ void __launch_bounds__(kStageWarps * 32)
     grid_barrier(m.bar_count, m.bar_gen);
     if (blockIdx.x == 0 && threadIdx.x == 0) m.any_changed[it & 1] = 0;
     if (!more || invalid) {
-      if (invalid) {  // values beyond the exact key range: the sequential-window kernel redoes it
+      if (invalid) {  // factors the count argument does not cover: the sequential-window kernel redoes it
         for (u64 u = (u64)blockIdx.x * blockDim.x + threadIdx.x; u < b.n_cycles; u += (u64)gridDim.x * blockDim.x)
           m.st[0][u] = b.c_local[u];
       } else if ((it + 1) & 1) {
@@ -3506,7 +3411,7 @@ int launch_stage_heuristic(const DevBuffers& b, const DevConfig& cfg, const Stag
   const bool blocks = !b.stream && cfg.cyc.stage_window <= 32 && cfg.cyc.stage_window >= 1;
   if (blocks) {
     // block-parallel chunks first; the sequential-window kernel below only
-    // runs when it could not (values beyond its exact key range)
+    // runs when it could not (stage factors <= 0) or did not converge
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_stage_blocks, kStageWarps * 32, 0);
     if (per_sm < 1) per_sm = 1;
