@@ -3648,6 +3648,7 @@ __host__ __device__ constexpr uint32_t seg_words(int P, int C, int R) {
 struct SegWarpSmem {  // fixed-size per-warp state (static shared memory)
   i64 ats[kSegList];        // range anchors: start_ts
   uint32_t apos[kSegList];  // range anchors: offset in the range | kSegTie
+  uint32_t adur[kSegList];  // range anchors: duration (0xffffffff: >= 2^32 - 1, reload)
   uint32_t pn[64];          // PythonCall compaction (name, duration)
   i64 pd[64];
   i64 dur[32];              // batch cycles: duration
@@ -3833,6 +3834,7 @@ __global__ void __launch_bounds__(kSegThreads, 2)
     // equal-timestamp test of an anchor at the range start
     i64 carry_ts = rb > ib ? b.ev[rb - 1].start_ts : LLONG_MIN;
     bool unsorted = false;
+    i64 real_last = LLONG_MIN;  // the lane's last in-range start_ts
     const cs_event* pl = b.ev + rb + lane;
     for (uint32_t j0 = 0; j0 < n; j0 += 32 * kSegScanUnroll) {
       Ev8 e[kSegScanUnroll];
@@ -3871,11 +3873,13 @@ __global__ void __launch_bounds__(kSegThreads, 2)
         const i64 before = lane == 0 ? carry_ts : prev;
         unsorted |= before > ts;
         carry_ts = __shfl_sync(0xffffffffu, ts, 31);
+        if (j0 + q * 32 + lane < n) real_last = ts;
         if (is_anchor) {
           const uint32_t ai = cnt + __popc(mk & lanemask_lt());
           if (ai < (uint32_t)kSegList) {
             w.apos[ai] = (j0 + q * 32 + lane) | (before == ts ? kSegTie : 0u);
             w.ats[ai] = ts;
+            w.adur[ai] = e[q].b < 0xffffffffull ? (uint32_t)e[q].b : 0xffffffffu;
           }
         }
         cnt += __popc(mk);
@@ -3902,25 +3906,30 @@ __global__ void __launch_bounds__(kSegThreads, 2)
     u64 npos = 0;
     if (A > 0) {
       const u64 ie = b.inst_off[inst + 1];
+      // start_ts of the event before the chunk: first the range's last event
+      i64 last_ts = __shfl_sync(0xffffffffu, real_last, (n - 1) & 31u);
       for (u64 p0 = rb + n; p0 < ie; p0 += 32) {
         const u64 p = p0 + lane;
         bool m = false;
-        i64 st = 0;
+        i64 st = LLONG_MAX;
         if (p < ie) {
           const Ev8 e = ldg256(b.ev + p);
           m = ((uint32_t)(e.c >> 32) & 0xffu) == CS_SPAN && (uint32_t)e.c == anchor;
           st = (i64)e.a;
         }
         const uint32_t bm = __ballot_sync(0xffffffffu, m);
+        const i64 prev = __shfl_up_sync(0xffffffffu, st, 1);
         if (bm) {
           const int L = __ffs(bm) - 1;
           next_start = __shfl_sync(0xffffffffu, st, L);
+          const i64 before = L == 0 ? last_ts : __shfl_sync(0xffffffffu, prev, L);
           npos = p0 + L;
           next_found = true;
+          next_tie = before == next_start;
           break;
         }
+        last_ts = __shfl_sync(0xffffffffu, st, 31);
       }
-      if (next_found) next_tie = b.ev[npos - 1].start_ts == next_start;
     }
     // ---------------- B + C: 32 cycles per batch, lane owns cycle k0 + lane
     u64 base = 0;
@@ -4039,7 +4048,8 @@ __global__ void __launch_bounds__(kSegThreads, 2)
         b.c_start[g] = cs;
         b.c_end[g] = ce;
         b.c_apos[g] = apos;
-        b.c_aend[g] = cs + b.ev[apos].duration;
+        const uint32_t ad = w.adur[k];
+        b.c_aend[g] = cs + (ad != 0xffffffffu ? (i64)ad : b.ev[apos].duration);
         b.c_first[g] = apos;
         b.c_last[g] = last;
         b.c_inst[g] = inst;
