@@ -2881,6 +2881,7 @@ __device__ __forceinline__ void win_push(Win& w, double x) {
   const int lane = threadIdx.x & 31;
   if (w.n == w.cap) {
     const double oldest = w.ring[w.head];
+    __syncwarp();  // every lane has read the slot lane 0 overwrites below
     win_remove(w, oldest);
     w.head = w.head + 1 == w.cap ? 0 : w.head + 1;
   }

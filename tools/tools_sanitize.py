@@ -66,5 +66,24 @@ an.upload_wire(rt.wire_pack(ev, off, wl))
 an.run(abi.RUN_ALL | abi.RUN_MU)
 n_cyc = sum(an.summary(i).n_cycles for i in range(len(evs)))
 an.close()
+# heuristic stages (forward_mode stripped, keywords off): the block-parallel
+# kernel (window 32) and the sequential-window kernel (window 40); and the
+# two-pass segmentation path
+evh = tr.events.copy()
+evh["flags"] &= np.uint16(0xFFFC)
+for win in (32, 40):
+    cfg = {"cycle": {"prefill_keywords": ["zz_none"], "decode_keywords": ["zz_none"], "stage_window": win}}
+    an = rt.Analyzer(0)
+    an.configure(tr.names, rt.span_names_mask(evh, len(tr.names)), n_comm_slots=tr.n_comm, run_config=cfg)
+    an.upload(evh, [0, len(evh)], tr.workloads)
+    an.run(abi.RUN_SEGMENT)
+    an.close()
+an = rt.Analyzer(0)
+an.configure(tr.names, rt.span_names_mask(tr.events, len(tr.names)), n_comm_slots=tr.n_comm)
+an.set_fused(False)
+an.upload(tr.events, [0, len(tr.events)], tr.workloads)
+an.load_model(models[0])
+an.run(abi.RUN_ALL)
+an.close()
 print("sanitize workload ok:", len(tr.events), "events,", len(res.cycles), "cycles,", len(res.alerts),
       "alerts; multi-instance batch", len(ev), "events,", n_cyc, "cycles")
