@@ -1,3 +1,4 @@
+#include <unordered_map>
 #include <type_traits>
 // cs_kernels.cu — hand-written sm_100a kernels of the trace-analysis hot path.
 //
@@ -35,6 +36,50 @@
 #include "cs_internal.h"
 
 namespace csb {
+
+// ------------------------------------------------ host launch helpers
+// Device properties, occupancy and dynamic-shared-memory attributes are
+// queried once per (host thread, device, kernel): a micro-batch run issues
+// ~25 launches and each runtime query costs microseconds of host time.
+namespace {
+struct LaunchCache {
+  int dev = -1, sms = 148, max_optin = 0;
+  std::unordered_map<const void*, int> smem_set;                 // kernel -> dynamic smem attribute set
+  std::unordered_map<unsigned long long, int> occ;               // (kernel, threads, smem) -> blocks per SM
+};
+LaunchCache& launch_cache() {
+  thread_local std::unordered_map<int, LaunchCache> per_dev;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  LaunchCache& c = per_dev[dev];
+  if (c.dev != dev) {
+    c.dev = dev;
+    cudaDeviceGetAttribute(&c.sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaDeviceGetAttribute(&c.max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  }
+  return c;
+}
+int sm_count() { return launch_cache().sms; }
+int smem_optin() { return launch_cache().max_optin; }
+void ensure_smem(const void* fn, int bytes) {
+  LaunchCache& c = launch_cache();
+  auto it = c.smem_set.find(fn);
+  if (it != c.smem_set.end() && it->second >= bytes) return;
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  c.smem_set[fn] = bytes;
+}
+int blocks_per_sm(const void* fn, int threads, size_t smem) {
+  LaunchCache& c = launch_cache();
+  const unsigned long long key = (reinterpret_cast<unsigned long long>(fn) * 1000003ull) ^
+                                 ((unsigned long long)threads << 40) ^ (unsigned long long)smem;
+  auto it = c.occ.find(key);
+  if (it != c.occ.end()) return it->second;
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, smem);
+  c.occ[key] = per_sm;
+  return per_sm;
+}
+}  // namespace
 
 using u64 = unsigned long long;
 using i64 = long long;
@@ -2712,7 +2757,7 @@ void launch_cycle_mu(const DevBuffers& b, const DevConfig& cfg, cudaStream_t s, 
   const int C = cfg.cyc.n_beta_slots > 0 ? cfg.cyc.n_beta_slots : 1;
   while (nt > 32 && nt * C * 8 > 96 * 1024) nt >>= 1;
   const int smem = (nt + 1) * C * 8 + nt * 8;  // padded [class][thread] rows + has masks
-  cudaFuncSetAttribute(k_cycle_mu, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  ensure_smem((const void*)k_cycle_mu, smem);
   k_cycle_mu<<<(unsigned)((b.n_cycles + nt - 1) / nt), nt, smem, s>>>(b, cfg);
   ++*launches;
 }
@@ -2740,10 +2785,8 @@ void launch_scan_events(const DevBuffers& b, const DevConfig&, int mode, bool sa
                         uint64_t* launches) {
   if (n_list == 0) return;
   if (sample) n_list *= kSampleSplit;
-  int dev = 0, sms = 148, per_sm = 1;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_scan_warp, kScanWarpThreads, 0);
+  const int sms = sm_count();
+  int per_sm = blocks_per_sm((const void*)k_scan_warp, kScanWarpThreads, 0);
   if (per_sm < 1) per_sm = 1;
   const uint32_t warps = kScanWarpThreads / 32;
   uint32_t grid = (uint32_t)sms * (uint32_t)per_sm;
@@ -2782,7 +2825,7 @@ void launch_cycle_reduce_tpc(const DevBuffers& b, const DevConfig& cfg, int do_b
     }
     return;
   }
-  cudaFuncSetAttribute(k_cycle_reduce_v2, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  ensure_smem((const void*)k_cycle_reduce_v2, smem);
   const unsigned grid = (unsigned)((b.n_cycles + nt - 1) / nt);
   k_cycle_reduce_v2<<<grid, nt, smem, s>>>(b, cfg, do_beta);
   ++*launches;
@@ -3406,15 +3449,12 @@ int launch_stage_heuristic(const DevBuffers& b, const DevConfig& cfg, const Stag
   if (!b.n_cycles || m.n_chunks == 0) return 0;
   const size_t smem = (size_t)kStageWarps * 4 * cfg.cyc.stage_window * sizeof(double);
   if (smem > 200 * 1024) return -1;
-  int dev0 = 0, n_sm0 = 148;
-  cudaGetDevice(&dev0);
-  cudaDeviceGetAttribute(&n_sm0, cudaDevAttrMultiProcessorCount, dev0);
+  const int n_sm0 = sm_count();
   const bool blocks = !b.stream && cfg.cyc.stage_window <= 32 && cfg.cyc.stage_window >= 1;
   if (blocks) {
     // block-parallel chunks first; the sequential-window kernel below only
     // runs when it could not (stage factors <= 0) or did not converge
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_stage_blocks, kStageWarps * 32, 0);
+    int per_sm = blocks_per_sm((const void*)k_stage_blocks, kStageWarps * 32, 0);
     if (per_sm < 1) per_sm = 1;
     uint64_t grid = (uint64_t)n_sm0 * per_sm;
     const uint64_t need = (m.n_chunks + kStageWarps - 1) / kStageWarps;
@@ -3425,11 +3465,9 @@ int launch_stage_heuristic(const DevBuffers& b, const DevConfig& cfg, const Stag
   // windows of <= 32 values live in registers (one value per lane)
   const bool reg = cfg.cyc.stage_window <= 32;
   const void* fn = reg ? (const void*)k_stage_jacobi<true> : (const void*)k_stage_jacobi<false>;
-  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  int dev = 0, n_sm = 148, per_sm = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kStageWarps * 32, smem);
+  ensure_smem(fn, (int)smem);
+  const int n_sm = n_sm0;
+  int per_sm = blocks_per_sm(fn, kStageWarps * 32, smem);
   if (per_sm < 1) per_sm = 1;
   uint64_t grid = (uint64_t)n_sm * per_sm;  // persistent: every CTA resident (grid barrier)
   const uint64_t need = (m.n_chunks + kStageWarps - 1) / kStageWarps;
@@ -3462,9 +3500,7 @@ void launch_score(const DevBuffers& b, const DevConfig& cfg, uint64_t n_records,
                   const uint64_t*, const int*, const DevModel* h_models, cudaStream_t s,
                   uint64_t* launches) {
   if (!n_records) return;
-  int dev = 0, max_optin = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  const int max_optin = smem_optin();
   bool all_lut = true;
   uint64_t need_lut = 0, need = 0;
   for (uint32_t i = 0; i < b.n_inst; ++i) {
@@ -3482,7 +3518,7 @@ void launch_score(const DevBuffers& b, const DevConfig& cfg, uint64_t n_records,
   if (all_lut) {
     uint64_t cap = (uint64_t)max_optin - 1024;
     if (need_lut < cap) cap = need_lut;
-    cudaFuncSetAttribute(k_score_lut, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cap);
+    ensure_smem((const void*)k_score_lut, (int)cap);
     const unsigned grid = (unsigned)((n_records + kLutTile - 1) / kLutTile);
     k_score_lut<<<grid, kLutThreads, cap, s>>>(b, cfg, n_records, cap);
     ++*launches;
@@ -3498,8 +3534,7 @@ void launch_score(const DevBuffers& b, const DevConfig& cfg, uint64_t n_records,
   const unsigned grid = (unsigned)((n_records + kScoreTile - 1) / kScoreTile);
 #define CS_SCORE_CASE(NF)                                                                 \
   case NF:                                                                                \
-    cudaFuncSetAttribute(k_score<NF>, cudaFuncAttributeMaxDynamicSharedMemorySize,        \
-                         (int)cap);                                                       \
+    ensure_smem((const void*)k_score<NF>, (int)cap);                                    \
     k_score<NF><<<grid, kScoreThreads, cap, s>>>(b, cfg, n_records, cap);                 \
     break;
   switch (nf) {
@@ -4141,11 +4176,9 @@ void launch_segment_range(const DevBuffers& b, const DevConfig& cfg, const SegMe
                           cudaStream_t s, uint64_t* launches) {
   const int smem = segment_range_smem(cfg, do_beta, b.n_names);
   if (smem < 0 || sm.n_ranges == 0) return;
-  cudaFuncSetAttribute(k_segment_range, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  int dev = 0, n_sm = 148, per_sm = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_segment_range, kSegThreads, smem);
+  ensure_smem((const void*)k_segment_range, smem);
+  const int n_sm = sm_count();
+  int per_sm = blocks_per_sm((const void*)k_segment_range, kSegThreads, smem);
   if (per_sm < 1) per_sm = 1;
   // persistent: every CTA resident (the look-back waits on earlier tickets)
   unsigned grid = (unsigned)(n_sm * per_sm);
