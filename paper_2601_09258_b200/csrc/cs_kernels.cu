@@ -1564,12 +1564,11 @@ __device__ __forceinline__ double window_stat_stream(const double* e, u64 t, u64
   return __ddiv_rn(sum, (double)(T - begin + 1));
 }
 
-__global__ void k_detect_flags(DevBuffers b, DevConfig cfg, uint64_t n_records) {
-  __shared__ uint32_t s_w[32];
-  n_records = records_on_device(b, n_records);
-  const u64 k = (u64)blockIdx.x * kDetBlock + threadIdx.x;
+// one record of the control chart (detector.cpp:91-130), warp-collective
+// (the previous record's statistic comes from the neighbouring lane); writes
+// rec_stat / rec_flags and counts the instance's alerts; returns alert
+__device__ __forceinline__ bool detect_record(const DevBuffers& b, const DevConfig& cfg, u64 k, bool valid) {
   const int lane = threadIdx.x & 31;
-  const bool valid = k < n_records;
   bool alert = false;
   uint32_t inst = 0xffffffffu;
   u64 t = 0, rb = 0;
@@ -1609,6 +1608,14 @@ __global__ void k_detect_flags(DevBuffers b, DevConfig cfg, uint64_t n_records) 
     b.rec_flags[k] = (armed ? 1 : 0) | (flagged ? 2 : 0) | (alert ? 4 : 0);
     if (alert) atomicAdd(&b.inst[inst].n_alerts, 1ull);
   }
+  return alert;
+}
+
+__global__ void k_detect_flags(DevBuffers b, DevConfig cfg, uint64_t n_records) {
+  __shared__ uint32_t s_w[32];
+  n_records = records_on_device(b, n_records);
+  const u64 k = (u64)blockIdx.x * kDetBlock + threadIdx.x;
+  const bool alert = detect_record(b, cfg, k, k < n_records);
   const uint32_t m = __ballot_sync(0xffffffffu, alert);
   if ((threadIdx.x & 31) == 0) s_w[threadIdx.x >> 5] = __popc(m);
   __syncthreads();
@@ -1616,6 +1623,56 @@ __global__ void k_detect_flags(DevBuffers b, DevConfig cfg, uint64_t n_records) 
     u64 v = threadIdx.x < kDetBlock / 32 ? s_w[threadIdx.x] : 0u;
     v = warp_sum_u64(v);
     if (threadIdx.x == 0) b.block_tmp[blockIdx.x] = v;
+  }
+}
+
+// Small batches (a streaming micro-batch): flags, alert list and per-instance
+// alert offsets in one CTA instead of flags + scan + offsets + scatter
+__global__ void __launch_bounds__(1024) k_detect_small(DevBuffers b, DevConfig cfg, uint64_t n_records) {
+  __shared__ uint32_t s_w[32];
+  __shared__ u64 s_base;
+  n_records = records_on_device(b, n_records);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) s_base = 0;
+  __syncthreads();
+  for (u64 k0 = 0; k0 < n_records; k0 += 1024) {
+    const u64 k = k0 + threadIdx.x;
+    const bool alert = detect_record(b, cfg, k, k < n_records);
+    const uint32_t m = __ballot_sync(0xffffffffu, alert);
+    if (lane == 0) s_w[warp] = __popc(m);
+    __syncthreads();
+    if (warp == 0) {
+      uint32_t c = s_w[lane];
+      const uint32_t x = c;
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, c, o);
+        if (lane >= o) c += y;
+      }
+      s_w[lane] = c - x;
+    }
+    __syncthreads();
+    const u64 base = s_base;
+    if (alert) b.alert_rec[base + s_w[warp] + __popc(m & lanemask_lt())] = k;
+    __syncthreads();
+    if (threadIdx.x == 1023) s_base = base + s_w[31] + __popc(m);  // last warp's prefix + its own count
+    __syncthreads();
+  }
+  // alerts are in record order: instance i's first alert is the first whose
+  // record index is >= rec_off[i]
+  const u64 total = s_base;
+  for (uint32_t i = threadIdx.x; i <= b.n_inst; i += blockDim.x) {
+    if (i == b.n_inst) {
+      b.alert_off[i] = total;
+      continue;
+    }
+    const u64 r = b.rec_off[i];
+    u64 lo = 0, hi = total;
+    while (lo < hi) {
+      const u64 mid = (lo + hi) >> 1;
+      if (b.alert_rec[mid] < r) lo = mid + 1;
+      else hi = mid;
+    }
+    b.alert_off[i] = lo;
   }
 }
 
@@ -3478,8 +3535,63 @@ int launch_stage_heuristic(const DevBuffers& b, const DevConfig& cfg, const Stag
   return 0;
 }
 
+// Small batches: record compaction and per-instance record offsets in one
+// CTA (count + scan + scatter + tail fused)
+__global__ void __launch_bounds__(1024) k_records_small(DevBuffers b, DevConfig cfg) {
+  __shared__ uint32_t s_w[32];
+  __shared__ u64 s_base;
+  const bool need_index = cfg.cyc.monitor_from_cycle > 0 || b.stream;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) s_base = 0;
+  __syncthreads();
+  for (u64 g0 = 0; g0 < b.n_cycles; g0 += 1024) {
+    const u64 g = g0 + threadIdx.x;
+    const bool ok = g < b.n_cycles && rec_ok(b, cfg, g, need_index);
+    const uint32_t m = __ballot_sync(0xffffffffu, ok);
+    if (lane == 0) s_w[warp] = __popc(m);
+    __syncthreads();
+    uint32_t tot = 0;
+    if (warp == 0) {
+      uint32_t c = s_w[lane];
+      const uint32_t x = c;
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, c, o);
+        if (lane >= o) c += y;
+      }
+      tot = __shfl_sync(0xffffffffu, c, 31);
+      s_w[lane] = c - x;
+    }
+    __syncthreads();
+    const u64 base = s_base;
+    if (ok) b.rec_cycle[base + s_w[warp] + __popc(m & lanemask_lt())] = g;
+    __syncthreads();
+    if (threadIdx.x == 0) s_base = base + tot;
+    __syncthreads();
+  }
+  // records are in cycle order: instance i's first record is the first whose
+  // cycle is >= cyc_off[i]
+  const u64 total = s_base;
+  for (uint32_t i = threadIdx.x; i <= b.n_inst; i += blockDim.x) {
+    const u64 c0 = b.cyc_off[i];
+    u64 lo = 0, hi = total;
+    while (lo < hi) {
+      const u64 mid = (lo + hi) >> 1;
+      if (b.rec_cycle[mid] < c0) lo = mid + 1;
+      else hi = mid;
+    }
+    b.rec_off[i] = i == b.n_inst ? total : lo;
+  }
+}
+
+constexpr u64 kSmallBatch = 32768;  // cycles / records handled by one CTA
+
 void launch_records(const DevBuffers& b, const DevConfig& cfg, uint64_t, cudaStream_t s,
                     uint64_t* launches) {
+  if (b.n_cycles <= kSmallBatch) {
+    k_records_small<<<1, 1024, 0, s>>>(b, cfg);
+    ++*launches;
+    return;
+  }
   const u64 nb = (b.n_cycles + kRecBlock - 1) / kRecBlock;
   if (nb) {
     k_records_count<<<(unsigned)nb, kRecThreads, 0, s>>>(b, cfg);
@@ -3555,6 +3667,11 @@ void launch_score(const DevBuffers& b, const DevConfig& cfg, uint64_t n_records,
 
 void launch_detect(const DevBuffers& b, const DevConfig& cfg, uint64_t n_records, cudaStream_t s,
                    uint64_t* launches) {
+  if (n_records <= kSmallBatch) {  // n_records: the record capacity (cycle count)
+    k_detect_small<<<1, 1024, 0, s>>>(b, cfg, n_records);
+    ++*launches;
+    return;
+  }
   const u64 nb = (n_records + kDetBlock - 1) / kDetBlock;
   if (nb) {
     const int W = cfg.ctl.strategy == CS_FIXED_POINT ? 0 : (int)cfg.ctl.window;
