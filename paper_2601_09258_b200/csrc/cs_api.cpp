@@ -203,6 +203,17 @@ struct cs_ctx {
   int reduce_variant = 0;  // profiling hook (single variant today)
   bool allow_fused = true;   // CS_OPT_FUSED (default on; 0 selects the two-pass path)
   bool used_fused = false;   // the last run segmented with k_segment_range
+  // slot-count speculation of the single-read pass: a run over the same
+  // upload and configuration as the last verified one takes its per-instance
+  // slot counts as the sizing, skips the mid-run synchronisation and checks
+  // them (with every other fallback condition) at the final one; a mismatch
+  // re-runs without speculation
+  uint64_t seg_gen = 1;               // bumped by uploads and configuration changes
+  bool no_speculate = false;          // the re-run after a failed speculation
+  uint64_t pred_gen = 0;              // seg_gen of the verified counts below
+  uint32_t pred_beta = 0;             // CS_RUN_BETA of that run
+  std::vector<uint64_t> pred_cyc_off;
+  unsigned int* pin_ctl = nullptr;    // pinned: the pass's control words at the final sync
   // cs_set_cycles: caller-given cycles of instance 0 (CS_RUN_GIVEN)
   std::vector<cs_cycle> given;
   std::vector<int64_t> given_comp;   // n x n_phases, empty = recompute
@@ -489,6 +500,7 @@ void cs_ctx_destroy(cs_ctx* ctx) {
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
   if (ctx->pin_models) cudaFreeHost(ctx->pin_models);
+  if (ctx->pin_ctl) cudaFreeHost(ctx->pin_ctl);
   delete ctx;
 }
 
@@ -506,6 +518,7 @@ int cs_set_config(cs_ctx* ctx, const cs_cycle_config* cycle, const cs_control_co
     if (cycle->frequency_bin_ns <= 0)
       return fail(ctx, CS_E_INVALID_ARGUMENT, "frequency_bin_ns must be positive");
     ctx->cyc = *cycle;
+    ++ctx->seg_gen;
   }
   if (control) {
     if (control->strategy < 0 || control->strategy > 2)
@@ -518,6 +531,7 @@ int cs_set_config(cs_ctx* ctx, const cs_cycle_config* cycle, const cs_control_co
 }
 
 static int cs_set_name_table_impl(cs_ctx* ctx, uint32_t n_names, const cs_name_info* names) {
+  if (ctx) ++ctx->seg_gen;
   if (!ctx || (n_names && !names)) return CS_E_INVALID_ARGUMENT;
   cudaSetDevice(ctx->device);
   ctx->names.assign(names, names + n_names);
@@ -623,6 +637,7 @@ int upload_layout(cs_ctx* ctx, uint32_t n_inst, const uint64_t* inst_offsets, bo
   CS_CUDA(cudaMemcpyAsync(dft, ctx->inst_first_tile.data(), n_inst * 4, cudaMemcpyHostToDevice,
                           ctx->stream));
   ctx->ranges_built_for = 0;  // k_segment_range ranges are rebuilt by the next fused run
+  ++ctx->seg_gen;
   if (!ctx->extra_keys.empty()) ctx->mt_valid = false;  // extras resolve per upload
   ctx->extra_keys.clear();
   ctx->n_extra_refs = 0;
@@ -1215,6 +1230,7 @@ static int cs_run_impl(cs_ctx* ctx, uint32_t mask) {
            dev<uint64_t>(ctx->block_tmp, nc1 / 256 + 16);
   };
   ctx->n_cyc.assign(n_inst, 0);
+  bool speculated = false;
   int e1 = -1, e2 = -1, e4 = -1, e5 = -1;
   ctx->used_fused = false;
   ctx->given_run = false;
@@ -1324,6 +1340,27 @@ static int cs_run_impl(cs_ctx* ctx, uint32_t mask) {
       ctx->timed.push_back({"segment_range", {e1, e2}});
       ctx->timed.push_back({"sample_and_setup", {e0, e1}});
       ctx->timed.push_back({"prefix_rank", {e2, e9}});
+      const uint32_t beta_bit = (mask & CS_RUN_BETA) ? 1u : 0u;
+      if (attempt == 0 && ctx->pred_gen == ctx->seg_gen && ctx->pred_beta == beta_bit &&
+          ctx->pred_cyc_off.size() == n_inst + 1 && ctx->pred_cyc_off[n_inst] <= cap && !ctx->no_speculate) {
+        // sized from the last verified run on this upload; verified at the final sync
+        if (!ctx->pin_ctl && cudaHostAlloc(reinterpret_cast<void**>(&ctx->pin_ctl), 8, cudaHostAllocDefault) != cudaSuccess)
+          return fail(ctx, CS_E_CUDA, "cudaHostAlloc(ctl)");
+        CS_CUDA(cudaMemcpyAsync(ctx->pin_ctl, ctx->d_seg_ctl.p, 8, cudaMemcpyDeviceToHost, s));
+        ctx->cyc_off.assign(ctx->pred_cyc_off.begin(), ctx->pred_cyc_off.end());
+        for (uint32_t i = 0; i < n_inst; ++i) {
+          const uint64_t na = ctx->cyc_off[i + 1] - ctx->cyc_off[i];
+          ctx->n_cyc[i] = na >= 2 ? na - 1 : 0;
+        }
+        ctx->n_cycles = ctx->cyc_off[n_inst];
+        ctx->inst_status.assign(n_inst, CS_OK);
+        ctx->used_fallback.assign(n_inst, 0);
+        ctx->fallback_cycles.assign(n_inst, 0);
+        ctx->folded.assign(n_inst, {});
+        ctx->used_fused = true;
+        speculated = true;
+        break;
+      }
       unsigned int ctl[2] = {0, 0};
       CS_CUDA(cudaMemcpyAsync(ctx->h_inst.data(), d_inst, n_inst * sizeof(InstState),
                               cudaMemcpyDeviceToHost, s));
@@ -1364,6 +1401,9 @@ static int cs_run_impl(cs_ctx* ctx, uint32_t mask) {
       ctx->fallback_cycles.assign(n_inst, 0);
       ctx->folded.assign(n_inst, {});
       ctx->used_fused = true;
+      ctx->pred_cyc_off.assign(ctx->cyc_off.begin(), ctx->cyc_off.end());  // verified counts for the next run on this upload
+      ctx->pred_gen = ctx->seg_gen;
+      ctx->pred_beta = beta_bit;
     }
     if (!ctx->used_fused) {
       // rare: redo on the two-pass path from a fresh anchor guess
@@ -1709,6 +1749,21 @@ static int cs_run_impl(cs_ctx* ctx, uint32_t mask) {
   hp.mark("all_issued");
   CS_CUDA(cudaStreamSynchronize(s));
   hp.mark("final_sync");
+  if (speculated) {
+    bool ok = ctx->pin_ctl[1] == 0u;
+    for (uint32_t i = 0; i < n_inst && ok; ++i) {
+      const auto& st = ctx->h_inst[i];
+      ok = !st.unsorted && !st.ambiguous && !st.redo && !st.no_anchor &&
+           st.n_anchors == ctx->pred_cyc_off[i + 1] - ctx->pred_cyc_off[i];
+    }
+    if (!ok) {  // counts or a fallback condition changed: run again, sized from the device
+      ctx->pred_gen = 0;
+      ctx->no_speculate = true;
+      const int rc = cs_run_impl(ctx, mask);
+      ctx->no_speculate = false;
+      return rc;
+    }
+  }
   if (std::getenv("CS_STAGE_ITERS") && ctx->d_stage_ctl.p) {  // profiling: Jacobi iterations of the stage heuristic
     unsigned int it = 0;
     cudaMemcpy(&it, static_cast<unsigned int*>(ctx->d_stage_ctl.p) + 5, 4, cudaMemcpyDeviceToHost);
@@ -2623,6 +2678,10 @@ int cs_set_option(cs_ctx* ctx, int option, int64_t value) {
   }
   if (option == 98) {  // profiling: multi-kernel reduce variant
     ctx->reduce_variant = static_cast<int>(value);
+    return CS_OK;
+  }
+  if (option == 99) {  // testing: skew the speculated slot counts by `value` (the next run must notice)
+    if (ctx->pred_cyc_off.size() >= 2) ctx->pred_cyc_off.back() += static_cast<uint64_t>(value);
     return CS_OK;
   }
   return fail(ctx, CS_E_INVALID_ARGUMENT, "unknown option");
