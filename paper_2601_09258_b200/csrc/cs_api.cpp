@@ -213,6 +213,11 @@ struct cs_ctx {
   uint64_t pred_gen = 0;              // seg_gen of the verified counts below
   uint32_t pred_beta = 0;             // CS_RUN_BETA of that run
   std::vector<uint64_t> pred_cyc_off;
+  // the anchors the last completed run over this upload and configuration
+  // verified: the next run speculates on them instead of sampling (the full
+  // moments still rank every candidate and check the guess)
+  uint64_t anchor_gen = 0;
+  std::vector<uint32_t> pred_anchor;
   unsigned int* pin_ctl = nullptr;    // pinned: the pass's control words at the final sync
   // cs_set_cycles: caller-given cycles of instance 0 (CS_RUN_GIVEN)
   std::vector<cs_cycle> given;
@@ -1187,6 +1192,15 @@ static int cs_run_impl(cs_ctx* ctx, uint32_t mask) {
     st.first_bad_record = UINT64_MAX;
     st.first_missing_record = UINT64_MAX;
   }
+  // speculative anchors from the last verified run on this upload
+  bool guessed = false;
+  if (hint == -1 && !ctx->streaming && !(mask & CS_RUN_GIVEN) && ctx->anchor_gen == ctx->seg_gen &&
+      ctx->pred_anchor.size() == n_inst) {
+    guessed = true;
+    for (uint32_t i = 0; i < n_inst; ++i) guessed &= ctx->pred_anchor[i] != UINT32_MAX;
+    if (guessed)
+      for (uint32_t i = 0; i < n_inst; ++i) ctx->h_inst[i].guess = ctx->pred_anchor[i];
+  }
   auto* d_inst = dev<InstState>(ctx->d_inst, n_inst);
   auto* d_stats = dev<NameStat>(ctx->d_stats, static_cast<size_t>(n_inst) * std::max(1u, n_names));
   const size_t cap_ev = std::max<uint64_t>(1, ctx->n_ev);
@@ -1204,7 +1218,7 @@ static int cs_run_impl(cs_ctx* ctx, uint32_t mask) {
   DevBuffers b = make_buffers(ctx);
 
   const int e0 = record_event(ctx, 0);
-  if (hint == -1 && !all_fixed && !(mask & CS_RUN_GIVEN)) {
+  if (hint == -1 && !all_fixed && !guessed && !(mask & CS_RUN_GIVEN)) {
     // speculative anchor from a sample of every instance
     if (stats_bytes) CS_CUDA(cudaMemsetAsync(d_stats, 0, stats_bytes, s));
     launch_scan_events(b, cfg, 1, true, static_cast<const uint32_t*>(ctx->d_sample_tiles.p),
@@ -1807,6 +1821,12 @@ static int cs_run_impl(cs_ctx* ctx, uint32_t mask) {
       if (ctx->stream_anchor[i] == UINT32_MAX && !ctx->h_inst[i].no_anchor &&
           ctx->h_inst[i].anchor != UINT32_MAX)
         ctx->stream_anchor[i] = ctx->h_inst[i].anchor;
+  if (!ctx->streaming && hint == -1 && !(mask & CS_RUN_GIVEN)) {
+    ctx->pred_anchor.assign(n_inst, UINT32_MAX);
+    for (uint32_t i = 0; i < n_inst; ++i)
+      if (!ctx->h_inst[i].no_anchor && !ctx->used_fallback[i]) ctx->pred_anchor[i] = ctx->h_inst[i].anchor;
+    ctx->anchor_gen = ctx->seg_gen;
+  }
   ctx->ran = true;
   ctx->last_mask = mask;
   hp.mark("done");
