@@ -3518,6 +3518,9 @@ int launch_stage_heuristic(const DevBuffers& b, const DevConfig& cfg, const Stag
     if (grid > need) grid = need;
     k_stage_blocks<<<(unsigned)grid, kStageWarps * 32, 0, s>>>(b, cfg, m);
     ++*launches;
+    // with positive factors it always reaches the fixed point (max_iter is
+    // the chunk count + 2, and each iteration settles at least one more chunk)
+    if (cfg.cyc.prefill_duration_factor > 0.0 && cfg.cyc.prefill_gap_factor > 0.0) return 0;
   }
   // windows of <= 32 values live in registers (one value per lane)
   const bool reg = cfg.cyc.stage_window <= 32;
