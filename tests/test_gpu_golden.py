@@ -135,3 +135,37 @@ def test_mu_known_answer(analyzer):
 def rt_span(b):
     from paper_2601_09258_b200 import runtime as rt
     return rt.span_names_mask(b.events, len(b.names))
+
+
+@pytest.mark.parametrize("scale", [1 << 28, 1 << 41], ids=["u64-rows", "two-pass-fallback"])
+def test_gpu_long_cycles_match_c_oracle(analyzer, scale):
+    """Long cycles and spans: at 2^28 ns cycles the single-read pass needs its
+    u64 rows (duration x events >= 2^32); at 2^41 ns it hands the run to the
+    two-pass path (duration >= 2^32, a packed collective row could
+    overflow).  Both equal the C oracle."""
+    rng = np.random.default_rng(5)
+    spec, t = [], 0
+    for i in range(60):
+        spec.append(traces.ev("run_batch", t, int(rng.integers(1, scale)), batch=int(rng.integers(1, 64)),
+                              input_len=int(rng.integers(0, 500)), output_len=int(rng.integers(0, 50)),
+                              fm="decode"))
+        for k in range(int(rng.integers(1, 120))):
+            nm = ["oncpu", "gemm_kernel", "reduce", "process_batch_result"][int(rng.integers(0, 4))]
+            cat = {"oncpu": "os_sched", "gemm_kernel": "gpu_kernel", "reduce": "collective_comm"}.get(nm, "python_call")
+            spec.append(traces.ev(nm, t + int(rng.integers(0, scale)), int(rng.integers(-5, 2 * scale)),
+                                  cat=cat, comm="c0" if nm == "reduce" else None,
+                                  rank=int(rng.integers(0, 4)) if nm == "reduce" else None))
+        t += int(rng.integers(scale // 2, 2 * scale))
+    b = traces.build(spec)
+    cfg = {"detector": {"warmup": 5, "window": 4}}
+    model = json.dumps(traces.TINY_MODEL)
+    o = csoracle.analyze(b.events, b.names, b.workloads, b.n_comm, cfg, model)
+    got, an = run_product(b.events, b.names, b.workloads, n_comm=b.n_comm, run_config=cfg,
+                          model_json=model, analyzer=analyzer, fused=True)
+    assert np.array_equal(got.cycles, o["cycles"])
+    assert np.array_equal(got.components, o["components"])
+    assert np.array_equal(got.beta_totals, o["beta_totals"])
+    assert np.array_equal(got.coll_beta.view(np.uint64), o["coll_beta"].view(np.uint64))
+    if o["status"] == 0:
+        assert np.array_equal(got.records, o["records"])
+        assert np.array_equal(got.alerts, o["alerts"])
