@@ -130,7 +130,7 @@ typedef struct cs_cycle_config { /* CycleConfig + PipelineOptions */
   int32_t latency_phase;          /* PipelineOptions::latency_component as
                                      phase index; -1 = full cycle span      */
   int32_t include_prefill;        /* PipelineOptions::include_prefill       */
-  int32_t n_beta_slots;           /* number of dense class slots (<= 64)    */
+  int32_t n_beta_slots;           /* number of dense class slots            */
   int32_t n_comm_slots;           /* collective (name,comm,rank) slots      */
   int32_t monitor_from_cycle;     /* records (and the detector stream) start
                                      at this cycle index: evaluate_trial's
@@ -668,7 +668,8 @@ int cs_alerts_to_ndjson(const cs_alert* alerts, uint64_t n_alerts, uint64_t pre_
  * cs_run continues one logical trace per instance:
  *  - the anchor chosen by the first batch (or the hint) is kept;
  *  - the detector window, warm-up count, flagged state and episode count
- *    carry over (windows <= 64), as does the stage heuristic's history;
+ *    carry over (any window; the windows in force at the stream's first
+ *    batch bound later ones), as does the stage heuristic's history;
  *  - cycle indices and episode ids continue across batches.
  * The caller resubmits each instance's trailing partial cycle with the next
  * batch: events [keep_from, n) of the last upload, where cs_stream_tail gives

@@ -281,6 +281,8 @@ struct cs_ctx {
   bool streaming = false, stream_fresh = false, stream_pending = false;
   int stream_cur = 0;
   DevBuf d_stream[2];
+  DevBuf d_shist[2], d_sdur[2], d_sgap[2];  // carried histories, window-sized rows per instance
+  uint32_t s_hw = 1, s_sw = 1;              // row lengths fixed at stream start
   pinned_vector<StreamCarry> h_stream;   // carry in force for the last batch
   pinned_vector<uint64_t> h_cyc_stage;   // pinned staging of cycle-table reads
   std::vector<uint32_t> stream_anchor;   // per instance, fixed after first batch
@@ -390,6 +392,11 @@ DevBuffers make_buffers(cs_ctx* ctx) {
   b.c_mu = static_cast<double*>(ctx->d_mu.p);
   b.c_mu_has = static_cast<uint8_t*>(ctx->d_mu_has.p);
   b.stream = ctx->streaming ? static_cast<StreamCarry*>(ctx->d_stream[ctx->stream_cur].p) : nullptr;
+  b.s_hist = ctx->streaming ? static_cast<const double*>(ctx->d_shist[ctx->stream_cur].p) : nullptr;
+  b.s_dur = ctx->streaming ? static_cast<const double*>(ctx->d_sdur[ctx->stream_cur].p) : nullptr;
+  b.s_gap = ctx->streaming ? static_cast<const double*>(ctx->d_sgap[ctx->stream_cur].p) : nullptr;
+  b.s_hw = ctx->s_hw;
+  b.s_sw = ctx->s_sw;
   b.any_unknown = static_cast<unsigned int*>(ctx->d_any_unknown.p);
   b.extra_refs = static_cast<const cs_extra_ref*>(ctx->d_extra_refs.p);
   b.n_extra_refs = ctx->n_extra_refs;
@@ -1152,14 +1159,21 @@ static int cs_run_impl(cs_ctx* ctx, uint32_t mask) {
   // streaming: advance to the carry the previous micro-batch produced
   bool all_fixed = false;
   if (ctx->streaming) {
-    if (ctx->ctl.strategy != CS_FIXED_POINT && ctx->ctl.window > kMaxStreamWindow)
-      return fail(ctx, CS_E_UNSUPPORTED, "streaming supports detector windows <= 64");
-    if (ctx->cyc.stage_window > 32)
-      return fail(ctx, CS_E_UNSUPPORTED, "streaming supports stage windows <= 32");
+    const uint32_t hw = std::max<uint32_t>(1, ctx->ctl.strategy == CS_FIXED_POINT ? 1 : ctx->ctl.window - 1);
+    const uint32_t sw = std::max<uint32_t>(1, ctx->cyc.stage_window);
+    if (!ctx->stream_fresh && (hw > ctx->s_hw || sw > ctx->s_sw))
+      return fail(ctx, CS_E_INVALID_ARGUMENT, "detector or stage window larger than at the stream's start");
     if (ctx->stream_fresh || ctx->h_stream.size() != n_inst) {
       if (!ctx->stream_fresh) return fail(ctx, CS_E_INVALID_ARGUMENT, "instance count changed mid-stream");
+      ctx->s_hw = hw;
+      ctx->s_sw = sw;
       for (auto& d : ctx->d_stream)
         if (!dev<StreamCarry>(d, n_inst)) return fail(ctx, CS_E_CUDA, "cudaMalloc(stream)");
+      for (int k = 0; k < 2; ++k)
+        if (!dev<double>(ctx->d_shist[k], static_cast<size_t>(n_inst) * hw) ||
+            !dev<double>(ctx->d_sdur[k], static_cast<size_t>(n_inst) * sw) ||
+            !dev<double>(ctx->d_sgap[k], static_cast<size_t>(n_inst) * sw))
+          return fail(ctx, CS_E_CUDA, "cudaMalloc(stream histories)");
       CS_CUDA(cudaMemsetAsync(ctx->d_stream[0].p, 0, n_inst * sizeof(StreamCarry), s));
       ctx->stream_cur = 0;
       ctx->h_stream.assign(n_inst, StreamCarry{});
@@ -1745,6 +1759,9 @@ static int cs_run_impl(cs_ctx* ctx, uint32_t mask) {
   }
   if (ctx->streaming) {
     launch_stream_update(b, cfg, static_cast<StreamCarry*>(ctx->d_stream[ctx->stream_cur ^ 1].p),
+                         static_cast<double*>(ctx->d_shist[ctx->stream_cur ^ 1].p),
+                         static_cast<double*>(ctx->d_sdur[ctx->stream_cur ^ 1].p),
+                         static_cast<double*>(ctx->d_sgap[ctx->stream_cur ^ 1].p),
                          (mask & CS_RUN_DETECT) ? 1 : 0, s);
     ++ctx->launches;
     ctx->stream_pending = true;

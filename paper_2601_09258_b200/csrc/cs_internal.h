@@ -74,17 +74,17 @@ struct DevModel {
 // Streaming (micro-batch) state carried per instance across cs_run calls:
 // the detector's last W-1 residuals, samples seen, flagged state, episode
 // count and the number of cycles already emitted.
-constexpr int kMaxStreamWindow = 64;
+// Per-instance state carried across micro-batches.  The histories live in
+// window-sized per-instance rows beside it (DevBuffers::s_hist / s_dur /
+// s_gap): any detector window and any stage window.
 struct StreamCarry {
   unsigned long long seen;
   unsigned long long episodes;
   unsigned long long cycle_off;
-  uint32_t n_hist;
+  uint32_t n_hist;     // residuals carried for the detector window (oldest first)
   uint32_t prev_flag;
-  double hist[kMaxStreamWindow - 1];
-  // stage heuristic (cycles.cpp:204-250): most recent first, <= 32 each
-  double dur_hist[32];
-  double gap_hist[32];
+  // stage heuristic (cycles.cpp:204-250): counts of the carried durations /
+  // gaps, most recent first
   uint32_t n_dur, n_gap;
   long long last_aend;
   uint32_t has_prev, pad;
@@ -157,6 +157,10 @@ struct DevBuffers {
   double* c_mu;                 // n_cycles x n_beta
   uint8_t* c_mu_has;
   StreamCarry* stream;          // per instance, null when not streaming
+  const double* s_hist;         // [n_inst][s_hw]: carried residuals (oldest first)
+  const double* s_dur;          // [n_inst][s_sw]: carried non-Prefill durations (most recent first)
+  const double* s_gap;          // [n_inst][s_sw]: carried gaps
+  uint32_t s_hw, s_sw;
   unsigned int* any_unknown;    // set by the reduces when any cycle's local stage is Unknown
   // record extras (cs_upload_extras): side table sorted by event, and the
   // per-record values / presence (n_records x n_extra_keys)
@@ -302,7 +306,8 @@ constexpr uint64_t kSortTile = 4096;
 void launch_eval_strategy(const DevBuffers& b, uint32_t inst, const uint8_t* labels,
                           uint64_t n_labels, uint64_t warmup, unsigned long long* out,
                           cudaStream_t s);
-void launch_stream_update(const DevBuffers& b, const DevConfig& cfg, StreamCarry* out, int detected,
+void launch_stream_update(const DevBuffers& b, const DevConfig& cfg, StreamCarry* out, double* out_hist,
+                          double* out_dur, double* out_gap, int detected,
                           cudaStream_t s);
 void launch_gather_records(const DevBuffers& b, const DevConfig& cfg, uint32_t inst, uint64_t r0,
                            uint64_t nr, int scored, int det, cs_record* out, cudaStream_t s);

@@ -1554,13 +1554,13 @@ __device__ __forceinline__ double window_stat(const double* e, u64 t, u64 W, int
 // Same statistic for stream position T = seen + t: residuals of earlier
 // micro-batches come from the carried history (oldest first).
 __device__ __forceinline__ double window_stat_stream(const double* e, u64 t, u64 W, int strategy,
-                                                     const StreamCarry& c) {
+                                                     const StreamCarry& c, const double* hist) {
   const u64 T = c.seen + t;
   if (strategy == CS_FIXED_POINT) return e[t];
   const u64 begin = T + 1 >= W ? T + 1 - W : 0;
   const u64 h0 = c.seen - c.n_hist;  // stream index of hist[0]
   double sum = 0.0;
-  for (u64 u = begin; u <= T; ++u) sum = __dadd_rn(sum, u < c.seen ? c.hist[u - h0] : e[u - c.seen]);
+  for (u64 u = begin; u <= T; ++u) sum = __dadd_rn(sum, u < c.seen ? hist[u - h0] : e[u - c.seen]);
   return __ddiv_rn(sum, (double)(T - begin + 1));
 }
 
@@ -1578,7 +1578,8 @@ __device__ __forceinline__ bool detect_record(const DevBuffers& b, const DevConf
     inst = upper_bound_u64(b.rec_off, b.n_inst + 1, k) - 1;
     rb = b.rec_off[inst];
     t = k - rb;
-    stat = b.stream ? window_stat_stream(b.rec_resid + rb, t, W, cfg.ctl.strategy, b.stream[inst])
+    stat = b.stream ? window_stat_stream(b.rec_resid + rb, t, W, cfg.ctl.strategy, b.stream[inst],
+                                         b.s_hist + (u64)inst * b.s_hw)
                     : window_stat(b.rec_resid + rb, t, W, cfg.ctl.strategy);
   }
   // statistic of record k-1: the neighbouring lane's, unless it is in another
@@ -1596,7 +1597,8 @@ __device__ __forceinline__ bool detect_record(const DevBuffers& b, const DevConf
       armed = T >= warm;
       if (t == 0) prev = c.prev_flag != 0;
       else if (T - 1 >= warm)
-        prev = (have_up ? up_stat : window_stat_stream(e, t - 1, W, cfg.ctl.strategy, c)) > limit;
+        prev = (have_up ? up_stat
+                        : window_stat_stream(e, t - 1, W, cfg.ctl.strategy, c, b.s_hist + (u64)inst * b.s_hw)) > limit;
     } else {
       armed = t >= warm;
       if (t >= 1 && t - 1 >= warm)
@@ -1768,12 +1770,15 @@ __global__ void __launch_bounds__(kDetThreads) k_detect_win(DevBuffers b, DevCon
 // take the batch's cycles 32 at a time (ballot compaction keeps the
 // reference's newest-first order).
 __global__ void __launch_bounds__(128) k_stream_update(DevBuffers b, DevConfig cfg, StreamCarry* out,
+                                                       double* out_hist, double* out_dur, double* out_gap,
                                                        int detected) {
   const uint32_t inst = blockIdx.x * 4 + (threadIdx.x >> 5);
   const uint32_t lane = threadIdx.x & 31;
   if (inst >= b.n_inst) return;
   const StreamCarry& c = b.stream[inst];
   StreamCarry& o = out[inst];
+  const double* chist = b.s_hist + (u64)inst * b.s_hw;
+  double* ohist = out_hist + (u64)inst * b.s_hw;
   // detector window
   if (detected) {
     const u64 r0 = b.rec_off[inst], n = b.rec_off[inst + 1] - r0;
@@ -1783,7 +1788,7 @@ __global__ void __launch_bounds__(128) k_stream_update(DevBuffers b, DevConfig c
     const u64 h0 = c.seen - c.n_hist;
     for (u64 i = lane; i < nh; i += 32) {
       const u64 u = total - nh + i;  // stream index
-      o.hist[i] = u < c.seen ? c.hist[u - h0] : b.rec_resid[r0 + (u - c.seen)];
+      ohist[i] = u < c.seen ? chist[u - h0] : b.rec_resid[r0 + (u - c.seen)];
     }
     if (lane == 0) {
       o.n_hist = (uint32_t)nh;
@@ -1792,7 +1797,7 @@ __global__ void __launch_bounds__(128) k_stream_update(DevBuffers b, DevConfig c
       o.episodes = c.episodes + b.inst[inst].n_alerts;
     }
   } else {
-    for (uint32_t i = lane; i < c.n_hist; i += 32) o.hist[i] = c.hist[i];
+    for (uint32_t i = lane; i < c.n_hist; i += 32) ohist[i] = chist[i];
     if (lane == 0) {
       o.n_hist = c.n_hist;
       o.prev_flag = c.prev_flag;
@@ -1802,7 +1807,11 @@ __global__ void __launch_bounds__(128) k_stream_update(DevBuffers b, DevConfig c
   }
   // stage-heuristic history: newest cycles of this batch first, then the carry
   const u64 c0 = b.cyc_off[inst], c1 = b.cyc_off[inst + 1];
-  const uint32_t W = (uint32_t)(cfg.cyc.stage_window < 32 ? cfg.cyc.stage_window : 32);
+  const uint32_t W = b.s_sw;
+  const double* cdur = b.s_dur + (u64)inst * b.s_sw;
+  const double* cgap = b.s_gap + (u64)inst * b.s_sw;
+  double* odur = out_dur + (u64)inst * b.s_sw;
+  double* ogap = out_gap + (u64)inst * b.s_sw;
   uint32_t nd = 0, ng = 0;
   const uint32_t lt = (1u << lane) - 1u;
   for (u64 top = c1; top > c0 && (nd < W || ng < W); top = top > c0 + 32 ? top - 32 : c0) {
@@ -1822,13 +1831,13 @@ __global__ void __launch_bounds__(128) k_stream_update(DevBuffers b, DevConfig c
     const uint32_t dm = __ballot_sync(0xffffffffu, np);
     const uint32_t gm = __ballot_sync(0xffffffffu, gv);
     const uint32_t di = nd + __popc(dm & lt), gi = ng + __popc(gm & lt);
-    if (np && di < W) o.dur_hist[di] = dur;
-    if (gv && gi < W) o.gap_hist[gi] = g;
+    if (np && di < W) odur[di] = dur;
+    if (gv && gi < W) ogap[gi] = g;
     nd = min(W, nd + __popc(dm));
     ng = min(W, ng + __popc(gm));
   }
-  for (uint32_t i = lane; i < c.n_dur && nd + i < W; i += 32) o.dur_hist[nd + i] = c.dur_hist[i];
-  for (uint32_t i = lane; i < c.n_gap && ng + i < W; i += 32) o.gap_hist[ng + i] = c.gap_hist[i];
+  for (uint32_t i = lane; i < c.n_dur && nd + i < W; i += 32) odur[nd + i] = cdur[i];
+  for (uint32_t i = lane; i < c.n_gap && ng + i < W; i += 32) ogap[ng + i] = cgap[i];
   if (lane == 0) {
     o.n_dur = min(W, nd + c.n_dur);
     o.n_gap = min(W, ng + c.n_gap);
@@ -1838,9 +1847,9 @@ __global__ void __launch_bounds__(128) k_stream_update(DevBuffers b, DevConfig c
   }
 }
 
-void launch_stream_update(const DevBuffers& b, const DevConfig& cfg, StreamCarry* out, int detected,
-                          cudaStream_t s) {
-  k_stream_update<<<(b.n_inst + 3) / 4, 128, 0, s>>>(b, cfg, out, detected);
+void launch_stream_update(const DevBuffers& b, const DevConfig& cfg, StreamCarry* out, double* out_hist,
+                          double* out_dur, double* out_gap, int detected, cudaStream_t s) {
+  k_stream_update<<<(b.n_inst + 3) / 4, 128, 0, s>>>(b, cfg, out, out_hist, out_dur, out_gap, detected);
 }
 
 // exclusive scan over instances of n_alerts: one CTA, kScanItems per thread per round
@@ -3180,8 +3189,10 @@ __global__ void __launch_bounds__(kStageWarps * 32)
             __syncwarp();
             // earlier micro-batches (streaming carry), most recent first
             if (sc) {
-              for (uint32_t k = lane; k < sc->n_dur && nd + k < W; k += 32) stage_d[nd + k] = sc->dur_hist[k];
-              for (uint32_t k = lane; k < sc->n_gap && ng + k < W; k += 32) stage_g[ng + k] = sc->gap_hist[k];
+              const double* scd = b.s_dur + (u64)inst * b.s_sw;
+              const double* scg = b.s_gap + (u64)inst * b.s_sw;
+              for (uint32_t k = lane; k < sc->n_dur && nd + k < W; k += 32) stage_d[nd + k] = scd[k];
+              for (uint32_t k = lane; k < sc->n_gap && ng + k < W; k += 32) stage_g[ng + k] = scg[k];
               nd = min(W, nd + sc->n_dur);
               ng = min(W, ng + sc->n_gap);
             }

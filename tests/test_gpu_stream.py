@@ -40,6 +40,9 @@ def _merge(traces):
     return evs, np.concatenate(wls), offs
 
 
+_WINDOWS = {"detector": None, "stage": None}  # set by a test: larger windows everywhere
+
+
 def _setup(rt, an, traces):
     names = traces[0].names
     evs, wl, offs = _merge(traces)
@@ -47,6 +50,12 @@ def _setup(rt, an, traces):
     an.set_fused(False)
     an.configure(names, rt.span_names_mask(allev, len(names)),
                  n_comm_slots=max(t.n_comm for t in traces))
+    if _WINDOWS["detector"] or _WINDOWS["stage"]:
+        if _WINDOWS["detector"]:
+            an.control.window = _WINDOWS["detector"]
+        if _WINDOWS["stage"]:
+            an.cycle.stage_window = _WINDOWS["stage"]
+        an.set_config(an.cycle, an.control)
     return evs, wl, offs, allev
 
 
@@ -103,11 +112,20 @@ def _whole_trace_reference(rt, traces, anchors):
     return ref, models
 
 
-@pytest.mark.parametrize("n_inst,strip_fm,slice_ms,hint", [(1, False, 37.0, True),
-                                                            (3, False, 113.0, False),
-                                                            (2, True, 61.0, False),
-                                                            (1, False, 10.0, True)])
-def test_stream_equals_whole_trace(rt, n_inst, strip_fm, slice_ms, hint):
+@pytest.mark.parametrize("n_inst,strip_fm,slice_ms,hint,windows", [(1, False, 37.0, True, None),
+                                                                    (3, False, 113.0, False, None),
+                                                                    (2, True, 61.0, False, None),
+                                                                    (1, False, 10.0, True, None),
+                                                                    (2, True, 41.0, False, (100, 48))])
+def test_stream_equals_whole_trace(rt, n_inst, strip_fm, slice_ms, hint, windows):
+    _WINDOWS["detector"], _WINDOWS["stage"] = windows or (None, None)
+    try:
+        _stream_equals_whole_trace(rt, n_inst, strip_fm, slice_ms, hint)
+    finally:
+        _WINDOWS["detector"] = _WINDOWS["stage"] = None
+
+
+def _stream_equals_whole_trace(rt, n_inst, strip_fm, slice_ms, hint):
     """hint=True: the anchor is given (anchor_hint); False: the first
     micro-batch (a calibration window of 20% of the trace) discovers it and
     the stream keeps it, so the whole-trace reference runs with that anchor
