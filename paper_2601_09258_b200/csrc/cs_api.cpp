@@ -300,6 +300,7 @@ struct cs_ctx {
   pinned_vector<uint64_t> h_keep;        // tail starts + tail anchor counts (stream_commit)
   pinned_vector<cs_alert> h_alerts_all;  // a push's alerts (stream_commit)
   std::vector<uint64_t> pred_anchors;    // for the run in flight (empty: no prediction)
+  bool pred_pending = false;             // pred_anchors = tail_anchors + h_new_anchors once ev_counted completes
 
   ~cs_ctx() {
     for (auto* m : model_store) delete m;
@@ -1192,7 +1193,10 @@ static int cs_run_impl(cs_ctx* ctx, uint32_t mask) {
   // a host prediction of the anchor counts applies to this run only
   std::vector<uint64_t> pred;
   pred.swap(ctx->pred_anchors);
-  const bool predicted = ctx->streaming && all_fixed && pred.size() == n_inst && !(mask & CS_RUN_GIVEN);
+  const bool pred_deferred = ctx->pred_pending;
+  ctx->pred_pending = false;
+  const bool predicted = ctx->streaming && all_fixed && (pred.size() == n_inst || pred_deferred) &&
+                         !(mask & CS_RUN_GIVEN);
   // per-instance state
   ctx->h_inst.assign(n_inst, InstState{});
   for (uint32_t i = 0; i < n_inst; ++i) {
@@ -1467,6 +1471,11 @@ static int cs_run_impl(cs_ctx* ctx, uint32_t mask) {
   // occurrence counts, so the ranking cannot be ambiguous or redone and the
   // sizing needs nothing from the device (checked after the final sync)
   if (predicted) {
+    if (pred_deferred) {
+      CS_CUDA(cudaEventSynchronize(ctx->ev_counted));
+      pred.assign(ctx->tail_anchors.begin(), ctx->tail_anchors.end());
+      for (uint32_t i = 0; i < n_inst; ++i) pred[i] += ctx->h_new_anchors[i];
+    }
     for (uint32_t i = 0; i < n_inst; ++i) {
       auto& st = ctx->h_inst[i];
       st.n_anchors = pred[i];
@@ -2031,11 +2040,9 @@ static int cs_stream_push_impl(cs_ctx* ctx, uint32_t n_inst, const uint64_t* off
                          ctx->stage_off[n_inst], static_cast<cs_event*>(ctx->d_ev.p), ctx->stream);
   if (cudaGetLastError() != cudaSuccess) return broken(fail(ctx, CS_E_CUDA, "stream assemble"));
   ctx->pred_anchors.clear();
-  if (predict) {
-    CS_CUDA(cudaEventSynchronize(ctx->ev_counted));
-    ctx->pred_anchors.assign(ctx->tail_anchors.begin(), ctx->tail_anchors.end());
-    for (uint32_t i = 0; i < n_inst; ++i) ctx->pred_anchors[i] += ctx->h_new_anchors[i];
-  }
+  // the run waits for the counts only where it sizes, after issuing its
+  // first kernels (the count's round trip overlaps them)
+  ctx->pred_pending = predict;
   hp.mark("assemble_count");
   rc = cs_run(ctx, mask);
   if (rc != CS_OK) return broken(rc);
