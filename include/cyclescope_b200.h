@@ -700,6 +700,12 @@ int cs_stream_push(cs_ctx* ctx, uint32_t n_inst, const uint64_t* offsets, const 
  * (k_score) even where a compiled cell table exists (k_score_lut); both are
  * bit-identical to GbdtModel::predict, the tests run both. */
 #define CS_OPT_TRAVERSAL 2
+/* CS_OPT_PHASE_TIMINGS (default -1): which device phases cs_get_timings
+ * reports.  -1: every phase for cs_run, only "total" for cs_stream_push (an
+ * event between a micro-batch's small kernels costs device time: it ends
+ * the overlap of one kernel's launch with its predecessor); 1: every phase
+ * always; 0: "total" only. */
+#define CS_OPT_PHASE_TIMINGS 3
 int cs_set_option(cs_ctx* ctx, int option, int64_t value);
 
 /* Pinned host memory helpers (cudaHostAlloc) for the e2e path. */

@@ -202,6 +202,7 @@ struct cs_ctx {
   uint64_t n_cycles = 0;           // cycle slots
   int reduce_variant = 0;  // profiling hook (single variant today)
   bool allow_fused = true;   // CS_OPT_FUSED (default on; 0 selects the two-pass path)
+  int phase_timings = -1;    // CS_OPT_PHASE_TIMINGS (-1: per phase except streaming pushes)
   bool used_fused = false;   // the last run segmented with k_segment_range
   // slot-count speculation of the single-read pass: a run over the same
   // upload and configuration as the last verified one takes its per-instance
@@ -1031,7 +1032,15 @@ namespace {
 const char* const kPhaseAfterEvent[16] = {"sample_and_setup", "scan_events", "prefix_rank", "bounds",
                                           "cycle_reduce", "stage_records", "score", "detect",
                                           "finish", "host_sizing", nullptr};
+// CS_OPT_PHASE_TIMINGS: an event between two small kernels costs the device
+// a few microseconds (it ends programmatic dependent launch overlap), so a
+// streaming push records only the run's first and last unless asked
+static bool phase_events(const cs_ctx* ctx) {
+  return ctx->phase_timings > 0 || (ctx->phase_timings < 0 && !ctx->streaming);
+}
+
 int record_event(cs_ctx* ctx, int idx) {
+  if (!phase_events(ctx) && idx != 0) return idx;
   cudaEventRecord(ctx->ev[idx], ctx->stream);
   if (ctx->nvtx_phase_open) nvtxRangePop();
   ctx->nvtx_phase_open = kPhaseAfterEvent[idx] != nullptr;
@@ -1776,6 +1785,10 @@ static int cs_run_impl(cs_ctx* ctx, uint32_t mask) {
     ctx->stream_pending = true;
     CS_CUDA(cudaMemcpyAsync(ctx->h_stream.data(), ctx->d_stream[ctx->stream_cur].p,
                             n_inst * sizeof(StreamCarry), cudaMemcpyDeviceToHost, s));
+  }
+  if (!phase_events(ctx)) {
+    ctx->timed.clear();
+    if (last != e0) cudaEventRecord(ctx->ev[last], ctx->stream);
   }
   ctx->timed.push_back({"total", {e0, last}});
   CS_CUDA(cudaMemcpyAsync(ctx->h_inst.data(), d_inst, n_inst * sizeof(InstState),
@@ -2710,6 +2723,10 @@ int cs_set_option(cs_ctx* ctx, int option, int64_t value) {
   if (option == CS_OPT_TRAVERSAL) {
     ctx->no_lut = value != 0;
     ctx->mt_valid = false;  // the per-instance model table carries the choice
+    return CS_OK;
+  }
+  if (option == CS_OPT_PHASE_TIMINGS) {
+    ctx->phase_timings = value < 0 ? -1 : value ? 1 : 0;
     return CS_OK;
   }
   if (option == 96) {  // tuning: events per single-read segmentation range (0 = auto)

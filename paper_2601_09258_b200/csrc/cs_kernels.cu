@@ -32,6 +32,8 @@
 
 #include <climits>
 #include <cstdint>
+#include <cstdlib>
+#include <utility>
 
 #include "cs_internal.h"
 
@@ -79,6 +81,33 @@ int blocks_per_sm(const void* fn, int threads, size_t smem) {
   c.occ[key] = per_sm;
   return per_sm;
 }
+
+// Programmatic dependent launch for the chains of small kernels a
+// micro-batch issues: the next kernel is scheduled while its predecessor
+// runs and waits at its top (pdl_enter) for the predecessor's completion
+// and memory, so the launch gap leaves the critical path.  CS_PDL=0 turns
+// it off (plain stream order).
+bool pdl_allowed() {
+  static const bool on = [] {
+    const char* e = getenv("CS_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+template <typename... K, typename... A>
+void launch_pdl(void (*kernel)(K...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, A&&... args) {
+  cudaLaunchConfig_t c = {};
+  c.gridDim = grid;
+  c.blockDim = block;
+  c.dynamicSmemBytes = smem;
+  c.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_allowed() ? 1 : 0;
+  c.attrs = attr;
+  c.numAttrs = 1;
+  cudaLaunchKernelEx(&c, kernel, std::forward<A>(args)...);
+}
 }  // namespace
 
 using u64 = unsigned long long;
@@ -90,6 +119,15 @@ constexpr u64 kValMask = (1ull << 62) - 1;
 constexpr u64 kNone = ~0ull;
 
 // ------------------------------------------------------------ primitives
+// Top of every kernel launched by launch_pdl: release the next kernel in the
+// stream (it may be scheduled now), then wait until this kernel's
+// predecessor has completed and its writes are visible.  A no-op for plain
+// launches.
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
 __device__ __forceinline__ u64 ld_acquire(const u64* p) {
   u64 v;
   asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
@@ -525,6 +563,7 @@ __device__ __forceinline__ Ev8 ldg256(const cs_event* p) {
 __global__ void __launch_bounds__(kScanWarpThreads, 3)
     k_scan_warp(DevBuffers b, int mode, const uint32_t* __restrict__ list, uint32_t n_list,
                 int sample) {
+  pdl_enter();
   constexpr int kW = kScanWarpThreads / 32;
   __shared__ WarpNameRow s_rows[kW * kWarpNameRows];
   // PythonCall spans are ~1 event in 9: they are compacted per warp and
@@ -672,6 +711,7 @@ __global__ void __launch_bounds__(kScanWarpThreads, 3)
 
 // per-instance anchor counts from the tile prefix
 __global__ void k_inst_anchor_counts(DevBuffers b) {
+  pdl_enter();
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= b.n_inst) return;
   const uint32_t t0 = b.inst_first_tile[i];
@@ -707,6 +747,7 @@ __device__ void score_from_moments(u64 count, i64 sum, double sumsq, double& mea
 }
 
 __global__ void k_rank(DevBuffers b, DevConfig cfg, int final_pass) {
+  pdl_enter();
   const int lane = threadIdx.x & 31;
   const uint32_t inst = blockIdx.x;
   if (inst >= b.n_inst) return;
@@ -924,6 +965,7 @@ __device__ __forceinline__ u64 anchor_slot(const DevBuffers& b, uint32_t inst, u
 // one; first/last events by lower_bound over equal start_ts
 // (cycles.cpp:135-156).  Replaces a binary search per cycle.
 __global__ void __launch_bounds__(256) k_bounds_tile(DevBuffers b) {
+  pdl_enter();
   const int lane = threadIdx.x & 31;
   const u64 t = (u64)blockIdx.x * 8 + (threadIdx.x >> 5);
   if (t >= b.n_tiles) return;
@@ -1001,6 +1043,7 @@ __global__ void __launch_bounds__(kRecThreads) k_records_count(DevBuffers b, Dev
 // round: thread t owns the contiguous chunk [t*c, (t+1)*c), c = ceil(n/threads)
 // (independent loads, no per-round barriers).
 __global__ void __launch_bounds__(1024, 1) k_scan_exclusive(uint64_t* v, uint64_t n, uint64_t* total) {
+  pdl_enter();
   __shared__ u64 s_part[32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const u64 c = (n + blockDim.x - 1) / blockDim.x;
@@ -1077,13 +1120,13 @@ __global__ void __launch_bounds__(kScanBlk) k_scan_apply(uint64_t* v, uint64_t n
 void launch_exclusive_scan(uint64_t* v, uint64_t n, uint64_t* total, uint64_t* tmp, cudaStream_t s,
                            uint64_t* launches) {
   if (n <= 16 * kScanBlk || !tmp) {
-    k_scan_exclusive<<<1, 1024, 0, s>>>(v, n, total);
+    launch_pdl(k_scan_exclusive, 1, 1024, 0, s, v, n, total);
     ++*launches;
     return;
   }
   const u64 nb = (n + kScanBlk - 1) / kScanBlk;
   k_scan_totals<<<(unsigned)nb, kScanBlk, 0, s>>>(v, n, tmp);
-  k_scan_exclusive<<<1, 1024, 0, s>>>(tmp, nb, total);
+  launch_pdl(k_scan_exclusive, 1, 1024, 0, s, tmp, nb, total);
   k_scan_apply<<<(unsigned)nb, kScanBlk, 0, s>>>(v, n, tmp);
   *launches += 3;
 }
@@ -1527,6 +1570,7 @@ __global__ void __launch_bounds__(kLutThreads)
 // binary search (independent across threads), thresholds read through L1.
 __global__ void __launch_bounds__(kLutThreads)
     k_score_lut_flat(DevBuffers b, DevConfig cfg, uint64_t n_records) {
+  pdl_enter();
   n_records = records_on_device(b, n_records);
   const u64 k = (u64)blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= n_records) return;
@@ -1631,6 +1675,7 @@ __global__ void k_detect_flags(DevBuffers b, DevConfig cfg, uint64_t n_records) 
 // Small batches (a streaming micro-batch): flags, alert list and per-instance
 // alert offsets in one CTA instead of flags + scan + offsets + scatter
 __global__ void __launch_bounds__(1024) k_detect_small(DevBuffers b, DevConfig cfg, uint64_t n_records) {
+  pdl_enter();
   __shared__ uint32_t s_w[32];
   __shared__ u64 s_base;
   n_records = records_on_device(b, n_records);
@@ -1772,6 +1817,7 @@ __global__ void __launch_bounds__(kDetThreads) k_detect_win(DevBuffers b, DevCon
 __global__ void __launch_bounds__(128) k_stream_update(DevBuffers b, DevConfig cfg, StreamCarry* out,
                                                        double* out_hist, double* out_dur, double* out_gap,
                                                        int detected) {
+  pdl_enter();
   const uint32_t inst = blockIdx.x * 4 + (threadIdx.x >> 5);
   const uint32_t lane = threadIdx.x & 31;
   if (inst >= b.n_inst) return;
@@ -1849,7 +1895,7 @@ __global__ void __launch_bounds__(128) k_stream_update(DevBuffers b, DevConfig c
 
 void launch_stream_update(const DevBuffers& b, const DevConfig& cfg, StreamCarry* out, double* out_hist,
                           double* out_dur, double* out_gap, int detected, cudaStream_t s) {
-  k_stream_update<<<(b.n_inst + 3) / 4, 128, 0, s>>>(b, cfg, out, out_hist, out_dur, out_gap, detected);
+  launch_pdl(k_stream_update, (b.n_inst + 3) / 4, 128, 0, s, b, cfg, out, out_hist, out_dur, out_gap, detected);
 }
 
 // exclusive scan over instances of n_alerts: one CTA, kScanItems per thread per round
@@ -2007,6 +2053,7 @@ __global__ void k_gather_alerts(DevBuffers b, DevConfig cfg, uint32_t inst, uint
 // every instance's alerts in one launch (alert_off on the device gives each
 // alert its instance); out[a] for a in [0, n_all)
 __global__ void k_gather_alerts_all(DevBuffers b, DevConfig cfg, uint64_t n_all, cs_alert* out) {
+  pdl_enter();
   const u64 a = (u64)blockIdx.x * blockDim.x + threadIdx.x;
   if (a >= n_all) return;
   uint32_t lo = 0, hi = b.n_inst;  // last instance with alert_off[inst] <= a
@@ -2021,7 +2068,7 @@ __global__ void k_gather_alerts_all(DevBuffers b, DevConfig cfg, uint64_t n_all,
 void launch_gather_alerts_all(const DevBuffers& b, const DevConfig& cfg, uint64_t n_all, cs_alert* out,
                               cudaStream_t s) {
   if (!n_all) return;
-  k_gather_alerts_all<<<(unsigned)((n_all + 255) / 256), 256, 0, s>>>(b, cfg, n_all, out);
+  launch_pdl(k_gather_alerts_all, (unsigned)((n_all + 255) / 256), 256, 0, s, b, cfg, n_all, out);
 }
 
 void launch_gather_records(const DevBuffers& b, const DevConfig& cfg, uint32_t inst, uint64_t r0,
@@ -2140,6 +2187,7 @@ constexpr int kFNamesSmem = 256;  // name infos staged in shared memory by the r
 // the instructions: consecutive records of mixed kinds diverge) were all slower.
 constexpr int kRedUnroll = 4;
 __global__ void __launch_bounds__(256, 3) k_cycle_reduce_v2(DevBuffers b, DevConfig cfg, int do_beta) {
+  pdl_enter();
   extern __shared__ __align__(16) unsigned char s_red[];
   __shared__ uint32_t s_ninfo[kFNamesSmem];
   const int P = cfg.cyc.n_phases;
@@ -2539,6 +2587,7 @@ void launch_wire_expand(const WireDev& w, const uint64_t* tile_begin, const uint
 // cycles.cpp:147) and, in keep[n_inst + i], the anchor occurrences in that
 // tail (the next micro-batch's host-side sizing starts from them)
 __global__ void __launch_bounds__(128) k_stream_keep(DevBuffers b, uint64_t* keep) {
+  pdl_enter();
   const uint32_t i = blockIdx.x * 4 + (threadIdx.x >> 5);
   const uint32_t lane = threadIdx.x & 31;
   if (i >= b.n_inst) return;
@@ -2562,6 +2611,7 @@ __global__ void __launch_bounds__(128) k_stream_assemble(const cs_event* __restr
                                                          const cs_event* __restrict__ fresh,
                                                          const uint64_t* __restrict__ meta, uint64_t total,
                                                          uint32_t n_inst, cs_event* __restrict__ out) {
+  pdl_enter();
   const uint32_t i = blockIdx.x;
   const u64 dst = meta[4 * i], ts = meta[4 * i + 1], tl = meta[4 * i + 2], ns = meta[4 * i + 3];
   const u64 end = i + 1 < n_inst ? meta[4 * (i + 1)] : total;
@@ -2574,7 +2624,7 @@ __global__ void __launch_bounds__(128) k_stream_assemble(const cs_event* __restr
 
 void launch_stream_assemble(const cs_event* prev, const cs_event* fresh, const uint64_t* meta,
                             uint32_t n_inst, uint64_t total, cs_event* out, cudaStream_t s) {
-  if (n_inst) k_stream_assemble<<<n_inst, 128, 0, s>>>(prev, fresh, meta, total, n_inst, out);
+  if (n_inst) launch_pdl(k_stream_assemble, n_inst, 128, 0, s, prev, fresh, meta, total, n_inst, out);
 }
 
 // anchor occurrences among each instance's NEW events of a micro-batch (warp
@@ -2583,6 +2633,7 @@ __global__ void __launch_bounds__(128) k_stream_count(const cs_event* __restrict
                                                       const uint64_t* __restrict__ meta,
                                                       const uint32_t* __restrict__ anchor, uint32_t n_inst,
                                                       uint64_t n_new, uint64_t* out) {
+  pdl_enter();
   const uint32_t i = blockIdx.x * 4 + (threadIdx.x >> 5);
   const uint32_t lane = threadIdx.x & 31;
   if (i >= n_inst) return;
@@ -2596,11 +2647,11 @@ __global__ void __launch_bounds__(128) k_stream_count(const cs_event* __restrict
 
 void launch_stream_count(const cs_event* fresh, const uint64_t* meta, const uint32_t* anchor, uint32_t n_inst,
                          uint64_t n_new, uint64_t* out, cudaStream_t s) {
-  if (n_inst) k_stream_count<<<(n_inst + 3) / 4, 128, 0, s>>>(fresh, meta, anchor, n_inst, n_new, out);
+  if (n_inst) launch_pdl(k_stream_count, (n_inst + 3) / 4, 128, 0, s, fresh, meta, anchor, n_inst, n_new, out);
 }
 
 void launch_stream_keep(const DevBuffers& b, uint64_t* keep, cudaStream_t s) {
-  if (b.n_inst) k_stream_keep<<<(b.n_inst + 3) / 4, 128, 0, s>>>(b, keep);
+  if (b.n_inst) launch_pdl(k_stream_keep, (b.n_inst + 3) / 4, 128, 0, s, b, keep);
 }
 
 // ------------------------------------------- counter-weighted mu (§8f #1)
@@ -2832,6 +2883,7 @@ void launch_cycle_mu(const DevBuffers& b, const DevConfig& cfg, cudaStream_t s, 
 // tile boundaries of the K0 check: a tile's first start_ts is not below the
 // previous tile's last within the same instance
 __global__ void k_tile_order(DevBuffers b) {
+  pdl_enter();
   const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t == 0 || t >= b.n_tiles) return;
   const uint32_t inst = b.tile_inst[t];
@@ -2842,7 +2894,7 @@ __global__ void k_tile_order(DevBuffers b) {
 
 void launch_tile_order(const DevBuffers& b, cudaStream_t s, uint64_t* launches) {
   if (b.n_tiles < 2) return;
-  k_tile_order<<<(b.n_tiles + 255) / 256, 256, 0, s>>>(b);
+  launch_pdl(k_tile_order, (b.n_tiles + 255) / 256, 256, 0, s, b);
   ++*launches;
 }
 
@@ -2858,7 +2910,7 @@ void launch_scan_events(const DevBuffers& b, const DevConfig&, int mode, bool sa
   uint32_t grid = (uint32_t)sms * (uint32_t)per_sm;
   const uint32_t need = (n_list + warps - 1) / warps;
   if (need < grid) grid = need;
-  k_scan_warp<<<grid, kScanWarpThreads, 0, s>>>(b, mode, list, n_list, sample ? 1 : 0);
+  launch_pdl(k_scan_warp, grid, kScanWarpThreads, 0, s, b, mode, list, n_list, sample ? 1 : 0);
   ++*launches;
 }
 
@@ -2893,7 +2945,7 @@ void launch_cycle_reduce_tpc(const DevBuffers& b, const DevConfig& cfg, int do_b
   }
   ensure_smem((const void*)k_cycle_reduce_v2, smem);
   const unsigned grid = (unsigned)((b.n_cycles + nt - 1) / nt);
-  k_cycle_reduce_v2<<<grid, nt, smem, s>>>(b, cfg, do_beta);
+  launch_pdl(k_cycle_reduce_v2, grid, nt, smem, s, b, cfg, do_beta);
   ++*launches;
 }
 
@@ -2901,14 +2953,14 @@ void launch_tile_prefix(const DevBuffers& b, cudaStream_t s, uint64_t* launches)
   cudaMemcpyAsync(b.tile_pref, b.tile_cnt, (size_t)b.n_tiles * sizeof(uint64_t),
                   cudaMemcpyDeviceToDevice, s);
   launch_exclusive_scan(b.tile_pref, b.n_tiles, b.tile_pref + b.n_tiles, b.scan_tmp, s, launches);
-  k_inst_anchor_counts<<<(b.n_inst + 255) / 256, 256, 0, s>>>(b);
+  launch_pdl(k_inst_anchor_counts, (b.n_inst + 255) / 256, 256, 0, s, b);
   *launches += 1;
 }
 
 void launch_rank(const DevBuffers& b, const DevConfig& cfg, int final_pass, cudaStream_t s,
                  uint64_t* launches) {
   if (b.n_inst == 0) return;
-  k_rank<<<b.n_inst, 32, 0, s>>>(b, cfg, final_pass);
+  launch_pdl(k_rank, b.n_inst, 32, 0, s, b, cfg, final_pass);
   ++*launches;
 }
 
@@ -2922,7 +2974,7 @@ void launch_fold(const DevBuffers& b, const DevConfig&, const uint32_t* pi, cons
 void launch_bounds(const DevBuffers& b, cudaStream_t s, uint64_t* launches) {
   if (!b.n_cycles) return;
   if (!b.n_tiles) return;
-  k_bounds_tile<<<(unsigned)((b.n_tiles + 7) / 8), 256, 0, s>>>(b);
+  launch_pdl(k_bounds_tile, (unsigned)((b.n_tiles + 7) / 8), 256, 0, s, b);
   ++*launches;
 }
 
@@ -3078,6 +3130,7 @@ __device__ __forceinline__ void grid_barrier(unsigned int* count, unsigned int* 
 template <bool kReg>
 __global__ void __launch_bounds__(kStageWarps * 32)
     k_stage_jacobi(DevBuffers b, DevConfig cfg, StageMeta m, int after_blocks) {
+  pdl_enter();
   using WinT = typename std::conditional<kReg, RegWin, Win>::type;
   extern __shared__ __align__(16) double s_win[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -3543,8 +3596,8 @@ int launch_stage_heuristic(const DevBuffers& b, const DevConfig& cfg, const Stag
   uint64_t grid = (uint64_t)n_sm * per_sm;  // persistent: every CTA resident (grid barrier)
   const uint64_t need = (m.n_chunks + kStageWarps - 1) / kStageWarps;
   if (grid > need) grid = need;
-  if (reg) k_stage_jacobi<true><<<(unsigned)grid, kStageWarps * 32, smem, s>>>(b, cfg, m, blocks ? 1 : 0);
-  else k_stage_jacobi<false><<<(unsigned)grid, kStageWarps * 32, smem, s>>>(b, cfg, m, blocks ? 1 : 0);
+  if (reg) launch_pdl(k_stage_jacobi<true>, (unsigned)grid, kStageWarps * 32, smem, s, b, cfg, m, blocks ? 1 : 0);
+  else launch_pdl(k_stage_jacobi<false>, (unsigned)grid, kStageWarps * 32, smem, s, b, cfg, m, blocks ? 1 : 0);
   ++*launches;
   return 0;
 }
@@ -3552,6 +3605,7 @@ int launch_stage_heuristic(const DevBuffers& b, const DevConfig& cfg, const Stag
 // Small batches: record compaction and per-instance record offsets in one
 // CTA (count + scan + scatter + tail fused)
 __global__ void __launch_bounds__(1024) k_records_small(DevBuffers b, DevConfig cfg) {
+  pdl_enter();
   __shared__ uint32_t s_w[32];
   __shared__ u64 s_base;
   const bool need_index = cfg.cyc.monitor_from_cycle > 0 || b.stream;
@@ -3602,7 +3656,7 @@ constexpr u64 kSmallBatch = 32768;  // cycles / records handled by one CTA
 void launch_records(const DevBuffers& b, const DevConfig& cfg, uint64_t, cudaStream_t s,
                     uint64_t* launches) {
   if (b.n_cycles <= kSmallBatch) {
-    k_records_small<<<1, 1024, 0, s>>>(b, cfg);
+    launch_pdl(k_records_small, 1, 1024, 0, s, b, cfg);
     ++*launches;
     return;
   }
@@ -3612,7 +3666,7 @@ void launch_records(const DevBuffers& b, const DevConfig& cfg, uint64_t, cudaStr
     ++*launches;
   }
   // block_tmp[nb] receives the total
-  k_scan_exclusive<<<1, 1024, 0, s>>>(b.block_tmp, nb, b.block_tmp + nb);
+  launch_pdl(k_scan_exclusive, 1, 1024, 0, s, b.block_tmp, nb, b.block_tmp + nb);
   ++*launches;
   if (nb) {
     k_records_scatter<<<(unsigned)nb, kRecThreads, 0, s>>>(b, cfg);
@@ -3636,8 +3690,8 @@ void launch_score(const DevBuffers& b, const DevConfig& cfg, uint64_t n_records,
     if (h_models[i].smem_bytes > need) need = h_models[i].smem_bytes;
   }
   if (all_lut && n_records < (u64)b.n_inst * 512) {  // short instance segments
-    k_score_lut_flat<<<(unsigned)((n_records + kLutThreads - 1) / kLutThreads), kLutThreads, 0, s>>>(
-        b, cfg, n_records);
+    launch_pdl(k_score_lut_flat, (unsigned)((n_records + kLutThreads - 1) / kLutThreads), kLutThreads, 0, s,
+               b, cfg, n_records);
     ++*launches;
     return;
   }
@@ -3682,7 +3736,7 @@ void launch_score(const DevBuffers& b, const DevConfig& cfg, uint64_t n_records,
 void launch_detect(const DevBuffers& b, const DevConfig& cfg, uint64_t n_records, cudaStream_t s,
                    uint64_t* launches) {
   if (n_records <= kSmallBatch) {  // n_records: the record capacity (cycle count)
-    k_detect_small<<<1, 1024, 0, s>>>(b, cfg, n_records);
+    launch_pdl(k_detect_small, 1, 1024, 0, s, b, cfg, n_records);
     ++*launches;
     return;
   }
@@ -3703,7 +3757,7 @@ void launch_detect(const DevBuffers& b, const DevConfig& cfg, uint64_t n_records
     }
     ++*launches;
   }
-  k_scan_exclusive<<<1, 1024, 0, s>>>(b.block_tmp, nb, b.block_tmp + nb);
+  launch_pdl(k_scan_exclusive, 1, 1024, 0, s, b.block_tmp, nb, b.block_tmp + nb);
   ++*launches;
   k_alert_off<<<1, 1024, 0, s>>>(b);
   ++*launches;

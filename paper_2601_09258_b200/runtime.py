@@ -788,6 +788,11 @@ class Analyzer:
         model has a compiled cell table."""
         self._ck(self.L.cs_set_option(self.h, 2, int(bool(enabled))))
 
+    def set_phase_timings(self, mode: int):
+        """CS_OPT_PHASE_TIMINGS: -1 per phase except streaming pushes
+        (default), 1 per phase always, 0 the run total only."""
+        self._ck(self.L.cs_set_option(self.h, 3, int(mode)))
+
     def run(self, mask: int = abi.RUN_ALL):
         self._ck(self.L.cs_run(self.h, mask))
 

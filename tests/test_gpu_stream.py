@@ -200,7 +200,8 @@ def _stream_equals_whole_trace(rt, n_inst, strip_fm, slice_ms, hint):
 def test_native_push_equals_python_push(rt):
     """cs_stream_push (tails, upload, run and alert gather in the library)
     gives the alerts of the Python-driven micro-batch loop, and the union of
-    its alerts equals the whole-trace run's."""
+    its alerts equals the whole-trace run's (with and without per-phase
+    device events)."""
     traces = _traces(rt, 3, False)
     evs = [t.events for t in traces]
     t_end = max(int(e["start_ts"].max()) for e in evs) + 1
@@ -225,6 +226,13 @@ def test_native_push_equals_python_push(rt):
                 batch.append(e[a:b])
             if native:
                 alerts.append(st.push_native(batch, wl2 if k == 0 else None))
+                # CS_OPT_PHASE_TIMINGS: a push records its total only unless
+                # asked (the option moves no data: alerts stay equal)
+                if k == 1:
+                    assert list(an.timings()) == ["total"]
+                    an.set_phase_timings(1)
+                elif k == 2:
+                    assert "total" in an.timings() and len(an.timings()) > 1
             else:
                 res = st.push(batch, wl2)
                 alerts += [r.alerts for r in res if r.summary.status == 0]
