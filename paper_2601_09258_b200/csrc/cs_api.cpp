@@ -39,15 +39,19 @@ struct NvtxScope {
 };
 #define CS_NVTX_SCOPE(name) NvtxScope nvtx_scope_(name)
 
-// CS_HOST_PROFILE=1: host-side phase times of each push on stderr (tools) and of each cs_run
+// CS_HOST_PROFILE=1: host-side phase times of each push on stderr (tools) and
+// of each cs_run; =2 also records an event on `stream` at every mark and
+// prints the device timeline (the events themselves cost device time)
 struct HostPhases {
   const char* label;
-  bool on = false;
+  int on = 0;
+  cudaStream_t stream = nullptr;
   std::chrono::steady_clock::time_point t0;
   std::string line;
+  std::vector<std::pair<const char*, cudaEvent_t>> gpu;
   explicit HostPhases(const char* l) : label(l) {
     const char* e = std::getenv("CS_HOST_PROFILE");
-    on = e && *e == '1';
+    on = e && (*e == '1' || *e == '2') ? *e - '0' : 0;
     if (on) t0 = std::chrono::steady_clock::now();
   }
   void mark(const char* name) {
@@ -55,9 +59,26 @@ struct HostPhases {
     const auto t = std::chrono::steady_clock::now();
     line += std::string(name) + "=" +
             std::to_string(std::chrono::duration<double, std::micro>(t - t0).count()) + " ";
+    if (on == 2 && stream) {
+      cudaEvent_t ev;
+      cudaEventCreate(&ev);
+      cudaEventRecord(ev, stream);
+      gpu.push_back({name, ev});
+    }
   }
   ~HostPhases() {
-    if (on) std::fprintf(stderr, "%s_us %s\n", label, line.c_str());
+    if (!on) return;
+    std::fprintf(stderr, "%s_us %s\n", label, line.c_str());
+    if (gpu.empty()) return;
+    cudaEventSynchronize(gpu.back().second);
+    std::string g;
+    for (auto& [n, ev] : gpu) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, gpu.front().second, ev);
+      g += std::string(n) + "=" + std::to_string(ms * 1e3) + " ";
+    }
+    for (auto& [n, ev] : gpu) cudaEventDestroy(ev);
+    std::fprintf(stderr, "%s_gpu_us %s\n", label, g.c_str());
   }
 };
 
@@ -1148,6 +1169,7 @@ extern "C" {
 
 static int cs_run_impl(cs_ctx* ctx, uint32_t mask) {
   HostPhases hp("cs_run");
+  if (ctx) hp.stream = ctx->stream;
   if (!ctx) return CS_E_INVALID_ARGUMENT;
   NvtxRun nvtx_run(ctx);
   if (mask & CS_RUN_MU) mask |= CS_RUN_BETA;  // mu divides by the class totals
@@ -1968,6 +1990,7 @@ static int cs_stream_push_impl(cs_ctx* ctx, uint32_t n_inst, const uint64_t* off
                    uint64_t n_workloads, const cs_workload* wl, uint32_t mask, cs_alert* alerts,
                    size_t cap, size_t* n_alerts) {
   HostPhases hp("cs_stream_push");
+  if (ctx) hp.stream = ctx->stream;
   if (!ctx || !offsets || n_inst == 0) return CS_E_INVALID_ARGUMENT;
   if (!ctx->streaming) return fail(ctx, CS_E_INVALID_ARGUMENT, "not streaming (cs_stream_begin)");
   if (ctx->stream_broken)

@@ -1020,6 +1020,7 @@ constexpr int kRecThreads = 256;
 constexpr int kRecPer = kRecBlock / kRecThreads;
 
 __global__ void __launch_bounds__(kRecThreads) k_records_count(DevBuffers b, DevConfig cfg) {
+  pdl_enter();
   __shared__ uint32_t s_w[kRecThreads / 32];
   const bool need_index = cfg.cyc.monitor_from_cycle > 0 || b.stream;
   const u64 g0 = (u64)blockIdx.x * kRecBlock + threadIdx.x;
@@ -1103,6 +1104,7 @@ __device__ __forceinline__ u64 block_incl_scan(u64 x, u64* s_w, u64* total) {
   return incl + (warp ? s_w[warp - 1] : 0);
 }
 __global__ void __launch_bounds__(kScanBlk) k_scan_totals(const uint64_t* v, uint64_t n, uint64_t* part) {
+  pdl_enter();
   __shared__ u64 s_w[32];
   const u64 i = (u64)blockIdx.x * kScanBlk + threadIdx.x;
   u64 t;
@@ -1110,6 +1112,7 @@ __global__ void __launch_bounds__(kScanBlk) k_scan_totals(const uint64_t* v, uin
   if (threadIdx.x == 0) part[blockIdx.x] = t;
 }
 __global__ void __launch_bounds__(kScanBlk) k_scan_apply(uint64_t* v, uint64_t n, const uint64_t* part) {
+  pdl_enter();
   __shared__ u64 s_w[32];
   const u64 i = (u64)blockIdx.x * kScanBlk + threadIdx.x;
   const u64 x = i < n ? v[i] : 0;
@@ -1125,13 +1128,14 @@ void launch_exclusive_scan(uint64_t* v, uint64_t n, uint64_t* total, uint64_t* t
     return;
   }
   const u64 nb = (n + kScanBlk - 1) / kScanBlk;
-  k_scan_totals<<<(unsigned)nb, kScanBlk, 0, s>>>(v, n, tmp);
+  launch_pdl(k_scan_totals, (unsigned)nb, kScanBlk, 0, s, v, n, tmp);
   launch_pdl(k_scan_exclusive, 1, 1024, 0, s, tmp, nb, total);
-  k_scan_apply<<<(unsigned)nb, kScanBlk, 0, s>>>(v, n, tmp);
+  launch_pdl(k_scan_apply, (unsigned)nb, kScanBlk, 0, s, v, n, tmp);
   *launches += 3;
 }
 
 __global__ void __launch_bounds__(kRecThreads) k_records_scatter(DevBuffers b, DevConfig cfg) {
+  pdl_enter();
   __shared__ uint32_t s_w[kRecPer][kRecThreads / 32];
   __shared__ uint32_t s_rank[kRecBlock];  // exclusive record rank of each cycle in the block
   const bool need_index = cfg.cyc.monitor_from_cycle > 0 || b.stream;
@@ -1188,6 +1192,7 @@ __global__ void __launch_bounds__(kRecThreads) k_records_scatter(DevBuffers b, D
 }
 
 __global__ void k_rec_off_tail(DevBuffers b, uint64_t* total) {
+  pdl_enter();
   // instances whose cycles start at n_cycles (trailing empty ones) and the end
   for (i64 i = b.n_inst; i >= 0 && b.cyc_off[i] == b.n_cycles; --i) b.rec_off[i] = *total;
 }
@@ -1271,6 +1276,7 @@ void launch_record_extras(const DevBuffers& b, uint64_t n_records_cap, cudaStrea
 template <int NF>
 __global__ void __launch_bounds__(kScoreThreads)
     k_score(DevBuffers b, DevConfig cfg, uint64_t n_records, uint64_t smem_cap) {
+  pdl_enter();
   extern __shared__ __align__(16) unsigned char s_model[];
   __shared__ uint32_t s_inst;
   n_records = records_on_device(b, n_records);
@@ -1526,6 +1532,7 @@ constexpr int kLutTile = 2048;  // records per CTA (>= 10 CTAs per SM at configs
 
 __global__ void __launch_bounds__(kLutThreads)
     k_score_lut(DevBuffers b, DevConfig cfg, uint64_t n_records, uint64_t smem_cap) {
+  pdl_enter();
   extern __shared__ __align__(16) unsigned char s_thr[];
   __shared__ uint32_t s_inst;
   n_records = records_on_device(b, n_records);
@@ -1658,6 +1665,7 @@ __device__ __forceinline__ bool detect_record(const DevBuffers& b, const DevConf
 }
 
 __global__ void k_detect_flags(DevBuffers b, DevConfig cfg, uint64_t n_records) {
+  pdl_enter();
   __shared__ uint32_t s_w[32];
   n_records = records_on_device(b, n_records);
   const u64 k = (u64)blockIdx.x * kDetBlock + threadIdx.x;
@@ -1735,6 +1743,7 @@ constexpr int kDetMaxW = 16;
 constexpr int kDetThreads = 256;
 template <int W>
 __global__ void __launch_bounds__(kDetThreads) k_detect_win(DevBuffers b, DevConfig cfg, uint64_t n_records) {
+  pdl_enter();
   __shared__ double s_e[kDetBlock + kDetMaxW];
   __shared__ double s_st[kDetBlock + 1];
   __shared__ uint32_t s_w[kDetThreads / 32];
@@ -1900,6 +1909,7 @@ void launch_stream_update(const DevBuffers& b, const DevConfig& cfg, StreamCarry
 
 // exclusive scan over instances of n_alerts: one CTA, kScanItems per thread per round
 __global__ void __launch_bounds__(1024) k_alert_off(DevBuffers b) {
+  pdl_enter();
   __shared__ u64 s_w[32];
   __shared__ u64 s_carry;
   if (threadIdx.x == 0) s_carry = 0;
@@ -1917,6 +1927,7 @@ __global__ void __launch_bounds__(1024) k_alert_off(DevBuffers b) {
 }
 
 __global__ void k_detect_scatter(DevBuffers b, uint64_t n_records) {
+  pdl_enter();
   __shared__ uint32_t s_w[32];
   n_records = records_on_device(b, n_records);
   const u64 k = (u64)blockIdx.x * kDetBlock + threadIdx.x;
@@ -2045,6 +2056,7 @@ __device__ __forceinline__ cs_alert make_alert(const DevBuffers& b, const DevCon
 
 __global__ void k_gather_alerts(DevBuffers b, DevConfig cfg, uint32_t inst, uint64_t a0,
                                 uint64_t na, cs_alert* out) {
+  pdl_enter();
   const u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= na) return;
   out[i] = make_alert(b, cfg, inst, i, b.alert_rec[a0 + i]);
@@ -2081,7 +2093,7 @@ void launch_gather_records(const DevBuffers& b, const DevConfig& cfg, uint32_t i
 void launch_gather_alerts(const DevBuffers& b, const DevConfig& cfg, uint32_t inst, uint64_t a0,
                           uint64_t na, cs_alert* out, cudaStream_t s) {
   if (!na) return;
-  k_gather_alerts<<<(unsigned)((na + 255) / 256), 256, 0, s>>>(b, cfg, inst, a0, na, out);
+  launch_pdl(k_gather_alerts, (unsigned)((na + 255) / 256), 256, 0, s, b, cfg, inst, a0, na, out);
 }
 
 // --------------------------------------------------- frequency fallback
@@ -3332,6 +3344,7 @@ __global__ void __launch_bounds__(kStageWarps * 32)
 // cycles.cpp:181-186 (median), 204-250 (decision, window updates).
 __global__ void __launch_bounds__(kStageWarps * 32)
     k_stage_blocks(DevBuffers b, DevConfig cfg, StageMeta m) {
+  pdl_enter();
   __shared__ double s_hd[kStageWarps][32], s_hg[kStageWarps][32];
   __shared__ double s_cd[kStageWarps][64], s_cg[kStageWarps][64], s_t[kStageWarps][64];
   __shared__ double s_stg[kStageWarps][64];  // rebuild staging (most recent first)
@@ -3580,7 +3593,7 @@ int launch_stage_heuristic(const DevBuffers& b, const DevConfig& cfg, const Stag
     uint64_t grid = (uint64_t)n_sm0 * per_sm;
     const uint64_t need = (m.n_chunks + kStageWarps - 1) / kStageWarps;
     if (grid > need) grid = need;
-    k_stage_blocks<<<(unsigned)grid, kStageWarps * 32, 0, s>>>(b, cfg, m);
+    launch_pdl(k_stage_blocks, (unsigned)grid, kStageWarps * 32, 0, s, b, cfg, m);
     ++*launches;
     // with positive factors it always reaches the fixed point (max_iter is
     // the chunk count + 2, and each iteration settles at least one more chunk)
@@ -3662,17 +3675,17 @@ void launch_records(const DevBuffers& b, const DevConfig& cfg, uint64_t, cudaStr
   }
   const u64 nb = (b.n_cycles + kRecBlock - 1) / kRecBlock;
   if (nb) {
-    k_records_count<<<(unsigned)nb, kRecThreads, 0, s>>>(b, cfg);
+    launch_pdl(k_records_count, (unsigned)nb, kRecThreads, 0, s, b, cfg);
     ++*launches;
   }
   // block_tmp[nb] receives the total
   launch_pdl(k_scan_exclusive, 1, 1024, 0, s, b.block_tmp, nb, b.block_tmp + nb);
   ++*launches;
   if (nb) {
-    k_records_scatter<<<(unsigned)nb, kRecThreads, 0, s>>>(b, cfg);
+    launch_pdl(k_records_scatter, (unsigned)nb, kRecThreads, 0, s, b, cfg);
     ++*launches;
   }
-  k_rec_off_tail<<<1, 1, 0, s>>>(b, b.block_tmp + nb);
+  launch_pdl(k_rec_off_tail, 1, 1, 0, s, b, b.block_tmp + nb);
   ++*launches;
 }
 
@@ -3700,7 +3713,7 @@ void launch_score(const DevBuffers& b, const DevConfig& cfg, uint64_t n_records,
     if (need_lut < cap) cap = need_lut;
     ensure_smem((const void*)k_score_lut, (int)cap);
     const unsigned grid = (unsigned)((n_records + kLutTile - 1) / kLutTile);
-    k_score_lut<<<grid, kLutThreads, cap, s>>>(b, cfg, n_records, cap);
+    launch_pdl(k_score_lut, grid, kLutThreads, cap, s, b, cfg, n_records, cap);
     ++*launches;
     return;
   }
@@ -3715,7 +3728,7 @@ void launch_score(const DevBuffers& b, const DevConfig& cfg, uint64_t n_records,
 #define CS_SCORE_CASE(NF)                                                                 \
   case NF:                                                                                \
     ensure_smem((const void*)k_score<NF>, (int)cap);                                    \
-    k_score<NF><<<grid, kScoreThreads, cap, s>>>(b, cfg, n_records, cap);                 \
+    launch_pdl(k_score<NF>, grid, kScoreThreads, cap, s, b, cfg, n_records, cap);                 \
     break;
   switch (nf) {
     CS_SCORE_CASE(0)
@@ -3744,7 +3757,7 @@ void launch_detect(const DevBuffers& b, const DevConfig& cfg, uint64_t n_records
   if (nb) {
     const int W = cfg.ctl.strategy == CS_FIXED_POINT ? 0 : (int)cfg.ctl.window;
     if (!b.stream && W <= kDetMaxW) {
-#define CS_DET_CASE(N)   case N:                  k_detect_win<N><<<(unsigned)nb, kDetThreads, 0, s>>>(b, cfg, n_records);     break;
+#define CS_DET_CASE(N)   case N:                  launch_pdl(k_detect_win<N>, (unsigned)nb, kDetThreads, 0, s, b, cfg, n_records);     break;
       switch (W) {
         CS_DET_CASE(0) CS_DET_CASE(1) CS_DET_CASE(2) CS_DET_CASE(3) CS_DET_CASE(4) CS_DET_CASE(5)
         CS_DET_CASE(6) CS_DET_CASE(7) CS_DET_CASE(8) CS_DET_CASE(9) CS_DET_CASE(10) CS_DET_CASE(11)
@@ -3753,16 +3766,16 @@ void launch_detect(const DevBuffers& b, const DevConfig& cfg, uint64_t n_records
       }
 #undef CS_DET_CASE
     } else {
-      k_detect_flags<<<(unsigned)nb, kDetBlock, 0, s>>>(b, cfg, n_records);
+      launch_pdl(k_detect_flags, (unsigned)nb, kDetBlock, 0, s, b, cfg, n_records);
     }
     ++*launches;
   }
   launch_pdl(k_scan_exclusive, 1, 1024, 0, s, b.block_tmp, nb, b.block_tmp + nb);
   ++*launches;
-  k_alert_off<<<1, 1024, 0, s>>>(b);
+  launch_pdl(k_alert_off, 1, 1024, 0, s, b);
   ++*launches;
   if (nb) {
-    k_detect_scatter<<<(unsigned)nb, kDetBlock, 0, s>>>(b, n_records);
+    launch_pdl(k_detect_scatter, (unsigned)nb, kDetBlock, 0, s, b, n_records);
     ++*launches;
   }
 }
@@ -3877,6 +3890,7 @@ struct SegWarpSmem {  // fixed-size per-warp state (static shared memory)
 
 __global__ void __launch_bounds__(kSegThreads, 2)
     k_segment_range(DevBuffers b, DevConfig cfg, SegMeta sm, int do_beta) {
+  pdl_enter();
   extern __shared__ __align__(16) unsigned char s_dyn[];
   __shared__ uint32_t s_ninfo[kSegNames];
   __shared__ int32_t s_pbs[16];  // phase -> class row of its name (-1: own component row)
@@ -4336,6 +4350,7 @@ __global__ void __launch_bounds__(kSegThreads, 2)
 // per instance: slot offset (global rank of its first anchor) and anchor count
 __global__ void k_range_inst(DevBuffers b, SegMeta sm, const uint32_t* inst_first_range,
                              uint64_t* slot_off) {
+  pdl_enter();
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i > b.n_inst) return;
   const u64 total = sm.n_ranges ? (sm.lb_state[sm.n_ranges - 1] & kValMask) : 0ull;
@@ -4368,13 +4383,13 @@ void launch_segment_range(const DevBuffers& b, const DevConfig& cfg, const SegMe
   // persistent: every CTA resident (the look-back waits on earlier tickets)
   unsigned grid = (unsigned)(n_sm * per_sm);
   if (grid > sm.n_ranges) grid = sm.n_ranges;
-  k_segment_range<<<grid, kSegThreads, smem, s>>>(b, cfg, sm, do_beta);
+  launch_pdl(k_segment_range, grid, kSegThreads, smem, s, b, cfg, sm, do_beta);
   ++*launches;
 }
 
 void launch_range_inst(const DevBuffers& b, const SegMeta& sm, const uint32_t* inst_first_range,
                        uint64_t* slot_off, cudaStream_t s, uint64_t* launches) {
-  k_range_inst<<<(b.n_inst + 1 + 255) / 256, 256, 0, s>>>(b, sm, inst_first_range, slot_off);
+  launch_pdl(k_range_inst, (b.n_inst + 1 + 255) / 256, 256, 0, s, b, sm, inst_first_range, slot_off);
   ++*launches;
 }
 
