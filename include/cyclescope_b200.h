@@ -704,7 +704,9 @@ int cs_stream_push(cs_ctx* ctx, uint32_t n_inst, const uint64_t* offsets, const 
  * reports.  -1: every phase for cs_run, only "total" for cs_stream_push (an
  * event between a micro-batch's small kernels costs device time: it ends
  * the overlap of one kernel's launch with its predecessor); 1: every phase
- * always; 0: "total" only. */
+ * always; 0: "total" only; 2: "total" and the segmentation pass
+ * ("segment_range", or "scan_events" and "cycle_reduce" on the two-pass
+ * path). */
 #define CS_OPT_PHASE_TIMINGS 3
 int cs_set_option(cs_ctx* ctx, int option, int64_t value);
 

@@ -1055,13 +1055,18 @@ const char* const kPhaseAfterEvent[16] = {"sample_and_setup", "scan_events", "pr
                                           "finish", "host_sizing", nullptr};
 // CS_OPT_PHASE_TIMINGS: an event between two small kernels costs the device
 // a few microseconds (it ends programmatic dependent launch overlap), so a
-// streaming push records only the run's first and last unless asked
+// streaming push records only the run's first and last unless asked; mode 2
+// keeps the events around the segmentation pass (slots 1, 2 and 4, 5)
 static bool phase_events(const cs_ctx* ctx) {
-  return ctx->phase_timings > 0 || (ctx->phase_timings < 0 && !ctx->streaming);
+  return ctx->phase_timings == 1 || (ctx->phase_timings < 0 && !ctx->streaming);
+}
+static bool phase_event_on(const cs_ctx* ctx, int idx) {
+  if (idx == 0 || phase_events(ctx)) return true;
+  return ctx->phase_timings == 2 && (idx == 1 || idx == 2 || idx == 4 || idx == 5);
 }
 
 int record_event(cs_ctx* ctx, int idx) {
-  if (!phase_events(ctx) && idx != 0) return idx;
+  if (!phase_event_on(ctx, idx)) return idx;
   cudaEventRecord(ctx->ev[idx], ctx->stream);
   if (ctx->nvtx_phase_open) nvtxRangePop();
   ctx->nvtx_phase_open = kPhaseAfterEvent[idx] != nullptr;
@@ -1808,9 +1813,12 @@ static int cs_run_impl(cs_ctx* ctx, uint32_t mask) {
     CS_CUDA(cudaMemcpyAsync(ctx->h_stream.data(), ctx->d_stream[ctx->stream_cur].p,
                             n_inst * sizeof(StreamCarry), cudaMemcpyDeviceToHost, s));
   }
-  if (!phase_events(ctx)) {
-    ctx->timed.clear();
-    if (last != e0) cudaEventRecord(ctx->ev[last], ctx->stream);
+  if (!phase_events(ctx)) {  // keep the phases whose events were recorded
+    std::vector<std::pair<std::string, std::pair<int, int>>> kept;
+    for (auto& t : ctx->timed)
+      if (phase_event_on(ctx, t.second.first) && phase_event_on(ctx, t.second.second)) kept.push_back(t);
+    ctx->timed.swap(kept);
+    if (!phase_event_on(ctx, last)) cudaEventRecord(ctx->ev[last], ctx->stream);
   }
   ctx->timed.push_back({"total", {e0, last}});
   CS_CUDA(cudaMemcpyAsync(ctx->h_inst.data(), d_inst, n_inst * sizeof(InstState),
@@ -2749,7 +2757,8 @@ int cs_set_option(cs_ctx* ctx, int option, int64_t value) {
     return CS_OK;
   }
   if (option == CS_OPT_PHASE_TIMINGS) {
-    ctx->phase_timings = value < 0 ? -1 : value ? 1 : 0;
+    if (value < -1 || value > 2) return fail(ctx, CS_E_INVALID_ARGUMENT, "phase timings: -1, 0, 1 or 2");
+    ctx->phase_timings = static_cast<int>(value);
     return CS_OK;
   }
   if (option == 96) {  // tuning: events per single-read segmentation range (0 = auto)

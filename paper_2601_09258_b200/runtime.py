@@ -790,7 +790,8 @@ class Analyzer:
 
     def set_phase_timings(self, mode: int):
         """CS_OPT_PHASE_TIMINGS: -1 per phase except streaming pushes
-        (default), 1 per phase always, 0 the run total only."""
+        (default), 1 per phase always, 0 the run total only, 2 the total and
+        the segmentation pass."""
         self._ck(self.L.cs_set_option(self.h, 3, int(mode)))
 
     def run(self, mask: int = abi.RUN_ALL):
