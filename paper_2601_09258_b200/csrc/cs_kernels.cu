@@ -1007,11 +1007,14 @@ constexpr int kRecBlock = 1024;
 // cycle g yields a record (cycles.cpp:372-383); the instance-relative index
 // test (monitor_from_cycle, streaming offsets) only loads the instance when
 // it can matter
+// the cycle's loads are issued together (no short-circuit between them)
 __device__ __forceinline__ bool rec_ok(const DevBuffers& b, const DevConfig& cfg, u64 g, bool need_index) {
-  if (!(b.c_wl[g] >= 0 && (cfg.cyc.include_prefill || b.c_stage[g] != CS_STAGE_PREFILL))) return false;
-  if (!need_index) return true;
-  const uint32_t inst = b.c_inst[g];
-  return g - b.cyc_off[inst] + (b.stream ? b.stream[inst].cycle_off : 0) >= (u64)cfg.cyc.monitor_from_cycle;
+  const int32_t wl = b.c_wl[g];
+  const uint8_t stage = b.c_stage[g];
+  const uint32_t inst = need_index ? b.c_inst[g] : 0u;
+  const bool ok = wl >= 0 && (cfg.cyc.include_prefill || stage != CS_STAGE_PREFILL);
+  if (!need_index) return ok;
+  return ok && g - b.cyc_off[inst] + (b.stream ? b.stream[inst].cycle_off : 0) >= (u64)cfg.cyc.monitor_from_cycle;
 }
 
 // kRecBlock cycles per CTA of kRecThreads, kRecBlock / kRecThreads per thread
@@ -1926,27 +1929,28 @@ __global__ void __launch_bounds__(1024) k_alert_off(DevBuffers b) {
   }
 }
 
-__global__ void k_detect_scatter(DevBuffers b, uint64_t n_records) {
+// alert list in record order: a warp per detect block, and only blocks with
+// alerts (block_tmp holds the exclusive prefix of their counts, the total at
+// [nb]) are read again -- alerts are rare, so this touches a few blocks
+constexpr int kDetScatterThreads = 256;
+__global__ void __launch_bounds__(kDetScatterThreads) k_detect_scatter(DevBuffers b, uint64_t n_records, uint64_t nb) {
   pdl_enter();
-  __shared__ uint32_t s_w[32];
   n_records = records_on_device(b, n_records);
-  const u64 k = (u64)blockIdx.x * kDetBlock + threadIdx.x;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const bool alert = k < n_records && (b.rec_flags[k] & 4);
-  const uint32_t m = __ballot_sync(0xffffffffu, alert);
-  if (lane == 0) s_w[warp] = __popc(m);
-  __syncthreads();
-  if (warp == 0) {
-    uint32_t c = lane < kDetBlock / 32 ? s_w[lane] : 0;
-    const uint32_t x = c;
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(0xffffffffu, c, o);
-      if (lane >= o) c += y;
+  const int lane = threadIdx.x & 31;
+  const u64 nw = ((u64)gridDim.x * blockDim.x) >> 5;
+  for (u64 bi = ((u64)blockIdx.x * blockDim.x + threadIdx.x) >> 5; bi < nb; bi += nw) {
+    u64 out = b.block_tmp[bi];
+    if (out == b.block_tmp[bi + 1]) continue;
+    const u64 k0 = bi * kDetBlock;
+    const u64 k1 = min(k0 + (u64)kDetBlock, (u64)n_records);
+    for (u64 kb = k0; kb < k1; kb += 32) {
+      const u64 k = kb + lane;
+      const bool alert = k < k1 && (b.rec_flags[k] & 4);
+      const uint32_t m = __ballot_sync(0xffffffffu, alert);
+      if (alert) b.alert_rec[out + __popc(m & lanemask_lt())] = k;
+      out += __popc(m);
     }
-    s_w[lane] = c - x;
   }
-  __syncthreads();
-  if (alert) b.alert_rec[b.block_tmp[blockIdx.x] + s_w[warp] + __popc(m & lanemask_lt())] = k;
 }
 
 // ------------------------------------------------- evaluate_strategy
@@ -3775,7 +3779,9 @@ void launch_detect(const DevBuffers& b, const DevConfig& cfg, uint64_t n_records
   launch_pdl(k_alert_off, 1, 1024, 0, s, b);
   ++*launches;
   if (nb) {
-    launch_pdl(k_detect_scatter, (unsigned)nb, kDetBlock, 0, s, b, n_records);
+    const u64 warps = (u64)sm_count() * 2 * (kDetScatterThreads / 32);
+    const u64 grid = (min(nb, warps) * 32 + kDetScatterThreads - 1) / kDetScatterThreads;
+    launch_pdl(k_detect_scatter, (unsigned)grid, kDetScatterThreads, 0, s, b, n_records, (uint64_t)nb);
     ++*launches;
   }
 }
@@ -3890,7 +3896,7 @@ struct SegWarpSmem {  // fixed-size per-warp state (static shared memory)
 
 __global__ void __launch_bounds__(kSegThreads, 2)
     k_segment_range(DevBuffers b, DevConfig cfg, SegMeta sm, int do_beta) {
-  pdl_enter();
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   extern __shared__ __align__(16) unsigned char s_dyn[];
   __shared__ uint32_t s_ninfo[kSegNames];
   __shared__ int32_t s_pbs[16];  // phase -> class row of its name (-1: own component row)
@@ -3916,6 +3922,9 @@ __global__ void __launch_bounds__(kSegThreads, 2)
     s_ninfo[i] = brow | (prow << 8) | ((ni.flags & 3u) << 30);
     if (ph && bs) s_pbs[ni.phase] = ni.beta_slot;
   }
+  // the name table is configuration (no earlier kernel writes it): staged
+  // while the predecessor drains, then wait for its results
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   __syncthreads();  // the only CTA barriers: warps are independent from here on
   const uint32_t SN = 33;
   u64* acc_c = reinterpret_cast<u64*>(s_dyn) + (u64)warp * NR * SN;  // collective rows [R + 1][SN]
