@@ -21,7 +21,7 @@
 //   K4   k_stage_heuristic       trailing-median heuristic for Unknown cycles
 //                                only (cycles.cpp:230-250), warp selection
 //   K5   k_records_*             record compaction (cycles.cpp:366-409)
-//   K6   k_score_lut / k_score   GBDT (compiled cell table or traversal) + PPE
+//   K6   k_score_lut_flat / k_score   GBDT (compiled cell table or traversal) + PPE
 //                                (gbdt.cpp:22-30, 173-184; detector.cpp:14-19)
 //   K7   k_detect_*              control chart, episode ids, alert compaction
 //                                (detector.cpp:91-130)
@@ -1531,53 +1531,10 @@ __device__ __forceinline__ void score_one_lut(const DevBuffers& b, const DevConf
 }
 
 constexpr int kLutThreads = 256;
-constexpr int kLutTile = 2048;  // records per CTA (>= 10 CTAs per SM at configs[1])
-
-__global__ void __launch_bounds__(kLutThreads)
-    k_score_lut(DevBuffers b, DevConfig cfg, uint64_t n_records, uint64_t smem_cap) {
-  pdl_enter();
-  extern __shared__ __align__(16) unsigned char s_thr[];
-  __shared__ uint32_t s_inst;
-  n_records = records_on_device(b, n_records);
-  const u64 r0 = (u64)blockIdx.x * kLutTile;
-  const u64 r1 = min(r0 + (u64)kLutTile, (u64)n_records);
-  const double eps = cfg.ctl.epsilon;
-  const int lat = cfg.cyc.latency_phase;
-  const int P = cfg.cyc.n_phases;
-  const void* staged = nullptr;
-  u64 r = r0;
-  while (r < r1) {
-    if (threadIdx.x == 0) s_inst = upper_bound_u64(b.rec_off, b.n_inst + 1, r) - 1;
-    __syncthreads();
-    const uint32_t inst = s_inst;
-    const u64 seg_end = min(r1, (u64)b.rec_off[inst + 1]);
-    const DevModel& m = b.models[inst];
-    const uint32_t n0 = m.lut_n[0], n1 = m.lut_n[1];
-    const double* t0 = m.lut_thr[0];
-    const double* t1 = m.lut_thr[1];
-    if ((u64)(n0 + n1) * 8 <= smem_cap) {
-      double* s0 = reinterpret_cast<double*>(s_thr);
-      if (m.lut_thr[0] != staged) {  // instances sharing a model reuse the staged copy
-        for (uint32_t i = threadIdx.x; i < n0; i += blockDim.x) s0[i] = t0[i];
-        for (uint32_t i = threadIdx.x; i < n1; i += blockDim.x) s0[n0 + i] = t1[i];
-        staged = m.lut_thr[0];
-      }
-      t0 = s0;
-      t1 = s0 + n0;
-    }
-    __syncthreads();
-    const u64 rb = b.rec_off[inst];
-    const int f0 = m.feature_ids[0], f1 = m.n_features > 1 ? m.feature_ids[1] : -1;
-    for (u64 k = r + threadIdx.x; k < seg_end; k += blockDim.x)
-      score_one_lut(b, cfg, m, inst, rb, k, t0, t1);
-    __syncthreads();
-    r = seg_end;
-  }
-}
-
-
-// Fleets with few records per instance: thread per record, its instance by
-// binary search (independent across threads), thresholds read through L1.
+// Thread per record, its instance by binary search (independent across
+// threads), thresholds read through L1.  A grid of one thread per record
+// keeps more gathers in flight than a tiled kernel with the thresholds staged
+// in shared memory (configs[1]: 83 vs 100 us), so every batch uses it.
 __global__ void __launch_bounds__(kLutThreads)
     k_score_lut_flat(DevBuffers b, DevConfig cfg, uint64_t n_records) {
   pdl_enter();
@@ -3699,25 +3656,14 @@ void launch_score(const DevBuffers& b, const DevConfig& cfg, uint64_t n_records,
   if (!n_records) return;
   const int max_optin = smem_optin();
   bool all_lut = true;
-  uint64_t need_lut = 0, need = 0;
+  uint64_t need = 0;
   for (uint32_t i = 0; i < b.n_inst; ++i) {
     all_lut &= h_models[i].lut != nullptr;
-    const uint64_t nl = (uint64_t)(h_models[i].lut_n[0] + h_models[i].lut_n[1]) * 8;
-    if (nl > need_lut) need_lut = nl;
     if (h_models[i].smem_bytes > need) need = h_models[i].smem_bytes;
   }
-  if (all_lut && n_records < (u64)b.n_inst * 512) {  // short instance segments
+  if (all_lut) {
     launch_pdl(k_score_lut_flat, (unsigned)((n_records + kLutThreads - 1) / kLutThreads), kLutThreads, 0, s,
                b, cfg, n_records);
-    ++*launches;
-    return;
-  }
-  if (all_lut) {
-    uint64_t cap = (uint64_t)max_optin - 1024;
-    if (need_lut < cap) cap = need_lut;
-    ensure_smem((const void*)k_score_lut, (int)cap);
-    const unsigned grid = (unsigned)((n_records + kLutTile - 1) / kLutTile);
-    launch_pdl(k_score_lut, grid, kLutThreads, cap, s, b, cfg, n_records, cap);
     ++*launches;
     return;
   }

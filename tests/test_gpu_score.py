@@ -4,7 +4,7 @@ detector.cpp:14-19).
 - k_score<NF> (complete-tree traversal): Extended (5-feature) models trained by
   the reference, and 2-feature Physical models with the cell table disabled
   (CS_OPT_TRAVERSAL), i.e. the path 2-feature models take past the table cap;
-- k_score_lut (cell table): the default for <= 2 features;
+- k_score_lut_flat (cell table): the default for <= 2 features;
 - a batch whose instances use models with different feature counts.
 Residuals, predictions and alerts are compared bitwise.
 """
