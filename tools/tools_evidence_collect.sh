@@ -9,7 +9,7 @@ for f in bench:bench_c2 bench_ref:bench_ref bench_twopass:bench_c2_twopass bench
          bench_c1:bench_c1 bench_c1_ref:bench_c1_ref bench_c2_halo:bench_c2_halo_n1 heuristic:heuristic_bench; do
   [ -f gpurun_out/${T}_${f%%:*}.log ] && tail -1 gpurun_out/${T}_${f%%:*}.log > profiles/${T}_${f##*:}.json
 done
-grep -h "cs_run_us\|cs_stream_push_us" gpurun_out/${T}_bench_c5.log | tail -6 > profiles/${T}_c5_host_phases.txt || true
+grep -h "cs_run_us\|cs_stream_push_us" gpurun_out/${T}_c5_host.log | tail -6 > profiles/${T}_c5_host_phases.txt || true
 [ -f gpurun_out/suite_bench.json ] && cp gpurun_out/suite_bench.json profiles/${T}_suite_bench.json
 cp gpurun_out/${T}_launches.csv profiles/${T}_launches.csv
 python tools/tools_launches.py gpurun_out/${T}_launches.csv > profiles/${T}_launches_summary.txt

@@ -10,7 +10,8 @@ timeout 900 python bench.py > gpurun_out/r2_bench.log 2>&1; echo bench=$?
 timeout 900 python bench.py --impl reference > gpurun_out/r2_bench_ref.log 2>&1; echo ref=$?
 CS_BENCH_FUSED=0 timeout 900 python bench.py --no-cpu-baseline --no-parity > gpurun_out/r2_bench_twopass.log 2>&1; echo twopass=$?
 timeout 900 python bench.py --workload c3 --no-cpu-baseline > gpurun_out/r2_bench_c3.log 2>&1; echo c3=$?
-CS_HOST_PROFILE=1 timeout 600 python bench.py --workload c5 --no-cpu-baseline > gpurun_out/r2_bench_c5.log 2>&1; echo c5=$?
+timeout 600 python bench.py --workload c5 --no-cpu-baseline > gpurun_out/r2_bench_c5.log 2>&1; echo c5=$?
+CS_HOST_PROFILE=1 timeout 600 python bench.py --workload c5 --no-cpu-baseline --steps 6 > gpurun_out/r2_c5_host.log 2>&1; echo c5host=$?
 timeout 600 python bench.py --workload c1 > gpurun_out/r2_bench_c1.log 2>&1; echo c1=$?
 timeout 600 python bench.py --workload c1 --impl reference > gpurun_out/r2_bench_c1_ref.log 2>&1; echo c1ref=$?
 timeout 600 python bench.py --c2-split halo --steps 5 > gpurun_out/r2_bench_c2_halo.log 2>&1; echo halo=$?
