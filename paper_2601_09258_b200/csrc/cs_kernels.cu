@@ -1890,6 +1890,7 @@ __global__ void __launch_bounds__(1024) k_alert_off(DevBuffers b) {
 // alerts (block_tmp holds the exclusive prefix of their counts, the total at
 // [nb]) are read again -- alerts are rare, so this touches a few blocks
 constexpr int kDetScatterThreads = 256;
+static_assert(kDetBlock == 32 * 32, "k_detect_scatter: 32 records per lane");
 __global__ void __launch_bounds__(kDetScatterThreads) k_detect_scatter(DevBuffers b, uint64_t n_records, uint64_t nb) {
   pdl_enter();
   n_records = records_on_device(b, n_records);
@@ -1898,14 +1899,33 @@ __global__ void __launch_bounds__(kDetScatterThreads) k_detect_scatter(DevBuffer
   for (u64 bi = ((u64)blockIdx.x * blockDim.x + threadIdx.x) >> 5; bi < nb; bi += nw) {
     u64 out = b.block_tmp[bi];
     if (out == b.block_tmp[bi + 1]) continue;
+    // lane l takes records [k0 + 32 l, k0 + 32 l + 32): one load round trip
+    // for the block, then the lanes' alerts in lane (= record) order
     const u64 k0 = bi * kDetBlock;
     const u64 k1 = min(k0 + (u64)kDetBlock, (u64)n_records);
-    for (u64 kb = k0; kb < k1; kb += 32) {
-      const u64 k = kb + lane;
-      const bool alert = k < k1 && (b.rec_flags[k] & 4);
-      const uint32_t m = __ballot_sync(0xffffffffu, alert);
-      if (alert) b.alert_rec[out + __popc(m & lanemask_lt())] = k;
-      out += __popc(m);
+    const u64 kb = k0 + 32u * (u64)lane;
+    uint32_t bits = 0;
+    if (kb + 32 <= k1) {
+      const uint4* p = reinterpret_cast<const uint4*>(b.rec_flags + kb);  // kb % 32 == 0
+      const uint4 v0 = p[0], v1 = p[1];
+      const uint32_t w[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) bits |= ((w[q] >> (8 * j + 2)) & 1u) << (4 * q + j);
+    } else {
+      for (u64 k = kb; k < k1; ++k) bits |= ((b.rec_flags[k] >> 2) & 1u) << (uint32_t)(k - kb);
+    }
+    const uint32_t cnt = __popc(bits);
+    uint32_t incl = cnt;
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    u64 pos = out + incl - cnt;
+    while (bits) {
+      b.alert_rec[pos++] = kb + (u64)(__ffs(bits) - 1);
+      bits &= bits - 1;
     }
   }
 }
