@@ -1144,6 +1144,19 @@ __global__ void __launch_bounds__(kRecThreads) k_records_scatter(DevBuffers b, D
   const bool need_index = cfg.cyc.monitor_from_cycle > 0 || b.stream;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const u64 gb = (u64)blockIdx.x * kRecBlock;
+  // the block's record base and first instance load while the cycles do
+  __shared__ u64 s_base;
+  __shared__ uint32_t s_lo;
+  if (threadIdx.x == 32) s_base = b.block_tmp[blockIdx.x];
+  if (threadIdx.x == 64) {
+    uint32_t lo = 0, hi = b.n_inst + 1;  // first i with cyc_off[i] >= gb
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (b.cyc_off[mid] < gb) lo = mid + 1;
+      else hi = mid;
+    }
+    s_lo = lo;
+  }
   bool ok[kRecPer];
   uint32_t m[kRecPer];
 #pragma unroll
@@ -1154,17 +1167,19 @@ __global__ void __launch_bounds__(kRecThreads) k_records_scatter(DevBuffers b, D
     if (lane == 0) s_w[r][warp] = __popc(m[r]);
   }
   __syncthreads();
-  if (threadIdx.x == 0) {  // exclusive prefix over (row, warp) in cycle order
-    uint32_t c = 0;
-    for (int r = 0; r < kRecPer; ++r)
-      for (int w = 0; w < kRecThreads / 32; ++w) {
-        const uint32_t x = s_w[r][w];
-        s_w[r][w] = c;
-        c += x;
-      }
+  static_assert(kRecPer * (kRecThreads / 32) == 32, "one warp scans the (row, warp) counts");
+  if (warp == 0) {  // exclusive prefix over (row, warp) in cycle order
+    uint32_t* sw = &s_w[0][0];
+    const uint32_t x = sw[lane];
+    uint32_t incl = x;
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    sw[lane] = incl - x;
   }
   __syncthreads();
-  const u64 base = b.block_tmp[blockIdx.x];
+  const u64 base = s_base;
 #pragma unroll
   for (int r = 0; r < kRecPer; ++r) {
     const uint32_t local = s_w[r][warp] + __popc(m[r] & lanemask_lt());
@@ -1175,18 +1190,7 @@ __global__ void __launch_bounds__(kRecThreads) k_records_scatter(DevBuffers b, D
   // per-instance record offsets: the rank of each instance's first cycle that
   // falls in this block (empty instances share it); the instances of a block
   // split across its threads (a fleet batch has hundreds per block)
-  __shared__ uint32_t s_lo;
   const u64 ge = gb + kRecBlock < b.n_cycles ? gb + kRecBlock : b.n_cycles;
-  if (threadIdx.x == 0) {
-    uint32_t lo = 0, hi = b.n_inst + 1;  // first i with cyc_off[i] >= gb
-    while (lo < hi) {
-      const uint32_t mid = (lo + hi) >> 1;
-      if (b.cyc_off[mid] < gb) lo = mid + 1;
-      else hi = mid;
-    }
-    s_lo = lo;
-  }
-  __syncthreads();
   for (uint32_t i = s_lo + threadIdx.x; i < b.n_inst; i += kRecThreads) {
     const u64 c0 = b.cyc_off[i];
     if (c0 >= ge) break;  // cyc_off is nondecreasing
@@ -1720,8 +1724,10 @@ __global__ void __launch_bounds__(kDetThreads) k_detect_win(DevBuffers b, DevCon
   for (u64 i = threadIdx.x; i < need; i += kDetThreads) s_e[i] = b.rec_resid[base + i];
   __syncthreads();
   const u64 warm = cfg.ctl.warmup;
-  // instance of the block's first record (one search per thread, cached)
-  uint32_t inst0 = upper_bound_u64(b.rec_off, b.n_inst + 1, k0) - 1;
+  // instance of the record before the block (or of the first), one search
+  // per thread; the loops walk forward from it
+  const u64 kfirst = k0 > 0 ? k0 - 1 : 0;
+  uint32_t inst0 = upper_bound_u64(b.rec_off, b.n_inst + 1, kfirst) - 1;
   auto stat_at = [&](u64 k, u64 rb) -> double {
     if (W == 0) return s_e[k - base];
     const u64 lo = k + 1 >= rb + W ? k + 1 - W : rb;
@@ -1735,16 +1741,12 @@ __global__ void __launch_bounds__(kDetThreads) k_detect_win(DevBuffers b, DevCon
     }
     return __ddiv_rn(sum, (double)(k + 1 - lo));
   };
-  // statistics of the block's records (and of the record before the block)
-  for (u64 k = k0 + threadIdx.x; k < kend; k += kDetThreads) {
+  // statistics of the block's records and of the record before the block
+  // (s_st[0]), spread over the threads alike
+  for (u64 k = kfirst + threadIdx.x; k < kend; k += kDetThreads) {
     uint32_t inst = inst0;
     while (b.rec_off[inst + 1] <= k) ++inst;
-    s_st[1 + (k - k0)] = stat_at(k, b.rec_off[inst]);
-  }
-  if (threadIdx.x == 0 && k0 > 0) {
-    const u64 k = k0 - 1;
-    const uint32_t inst = upper_bound_u64(b.rec_off, b.n_inst + 1, k) - 1;
-    s_st[0] = stat_at(k, b.rec_off[inst]);
+    s_st[1 + k - k0] = stat_at(k, b.rec_off[inst]);
   }
   __syncthreads();
   uint32_t n_alert = 0;
