@@ -3829,7 +3829,7 @@ void launch_freq_cycles(const cs_event* ev, uint64_t begin, uint64_t end, int64_
 #define CS_SEG_PREFETCH 1
 #endif
 #ifndef CS_SEG_WALK_UNROLL
-#define CS_SEG_WALK_UNROLL 4
+#define CS_SEG_WALK_UNROLL 3
 #endif
 constexpr int kSegScanUnroll = CS_SEG_SCAN_UNROLL;  // phase A: 256-bit loads in flight per lane
 constexpr int kSegWalkUnroll = CS_SEG_WALK_UNROLL;  // phase B: events in flight per lane
