@@ -191,7 +191,7 @@ struct SegMeta {
   uint32_t prefetch_ahead;       // also prefetch range r + this into L2 (0xffffffff: the grid's warps)
 };
 constexpr int32_t kHoleWl = -3;
-constexpr uint64_t kSegCycles = 30;  // target cycles per range (one warp, one cycle per lane)
+constexpr uint64_t kSegCycles = 31;  // target cycles per range (one warp, one cycle per lane; swept 28-33 on configs[1])
 
 // launchers (cs_kernels.cu); all asynchronous on `s`
 void launch_scan_events(const DevBuffers& b, const DevConfig& cfg, int mode, bool sample,
