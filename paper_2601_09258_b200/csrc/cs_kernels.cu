@@ -1534,7 +1534,10 @@ __device__ __forceinline__ void score_one_lut(const DevBuffers& b, const DevConf
   b.rec_resid[k] = res;
 }
 
-constexpr int kLutThreads = 256;
+#ifndef CS_LUT_THREADS
+#define CS_LUT_THREADS 256
+#endif
+constexpr int kLutThreads = CS_LUT_THREADS;
 // Thread per record, its instance by binary search (independent across
 // threads), thresholds read through L1.  A grid of one thread per record
 // keeps more gathers in flight than a tiled kernel with the thresholds staged
@@ -1704,7 +1707,10 @@ __global__ void __launch_bounds__(1024) k_detect_small(DevBuffers b, DevConfig c
 // (in_episode = armed && flagged at t-1, detector.cpp:107-128) comes from the
 // CTA's statistics in shared memory.  Stores are coalesced (thread stride).
 constexpr int kDetMaxW = 16;
-constexpr int kDetThreads = 256;
+#ifndef CS_DET_THREADS
+#define CS_DET_THREADS 256
+#endif
+constexpr int kDetThreads = CS_DET_THREADS;
 template <int W>
 __global__ void __launch_bounds__(kDetThreads) k_detect_win(DevBuffers b, DevConfig cfg, uint64_t n_records) {
   pdl_enter();
