@@ -177,13 +177,24 @@ struct cs_ctx {
   uint32_t n_inst = 0;
   uint64_t n_ev = 0, n_wl = 0;
   pinned_vector<uint64_t> inst_off;
-  DevBuf d_ev, d_wl, d_names, d_inst_off;
+  DevBuf d_ev, d_wl, d_names;
   DevBuf d_wire;  // cs_upload_wire staging (all columns in one allocation)
   // tiles
   // pinned: the layout's host->device copies are asynchronous (streaming pushes)
   pinned_vector<uint32_t> tile_inst, inst_first_tile;
   pinned_vector<uint64_t> tile_begin, tile_end;
-  DevBuf d_tile_inst, d_tile_begin, d_tile_end, d_inst_first_tile, d_tile_cnt, d_tile_pref;
+  // the layout (instance offsets, tiles, sample tiles) goes up as ONE copy
+  // from a pinned staging block; the p_* pointers are its device segments
+  pinned_vector<unsigned char> h_layout;
+  DevBuf d_layout;
+  cudaEvent_t ev_layout = nullptr;  // the staging block's last copy (reuse waits for it)
+  uint64_t* p_inst_off = nullptr;
+  uint64_t* p_tile_begin = nullptr;
+  uint64_t* p_tile_end = nullptr;
+  uint32_t* p_tile_inst = nullptr;
+  uint32_t* p_inst_first_tile = nullptr;
+  uint32_t* p_sample_tiles = nullptr;
+  DevBuf d_tile_cnt, d_tile_pref;
   DevBuf d_scan_tmp;
   // record extras (cs_upload_extras)
   std::vector<std::string> extra_keys;
@@ -213,7 +224,7 @@ struct cs_ctx {
   cudaEvent_t ev_counted = nullptr;  // the new events' anchor counts are on the host
   DevBuf d_keep;
   pinned_vector<uint32_t> sample_tiles;
-  DevBuf d_sample_tiles, d_redo_tiles;
+  DevBuf d_redo_tiles;
   // state
   DevBuf d_stats, d_inst, d_a_pos, d_a_start, d_a_end;
   pinned_vector<InstState> h_inst;
@@ -329,6 +340,7 @@ struct cs_ctx {
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
     if (ev_copied) cudaEventDestroy(ev_copied);
+    if (ev_layout) cudaEventDestroy(ev_layout);
     if (ev_counted) cudaEventDestroy(ev_counted);
     if (stream) cudaStreamDestroy(stream);
   }
@@ -366,11 +378,11 @@ DevBuffers make_buffers(cs_ctx* ctx) {
   b.names = static_cast<const cs_name_info*>(ctx->d_names.p);
   b.n_names = static_cast<uint32_t>(ctx->names.size());
   b.n_inst = ctx->n_inst;
-  b.inst_off = static_cast<const uint64_t*>(ctx->d_inst_off.p);
-  b.tile_inst = static_cast<const uint32_t*>(ctx->d_tile_inst.p);
-  b.tile_begin = static_cast<const uint64_t*>(ctx->d_tile_begin.p);
-  b.tile_end = static_cast<const uint64_t*>(ctx->d_tile_end.p);
-  b.inst_first_tile = static_cast<const uint32_t*>(ctx->d_inst_first_tile.p);
+  b.inst_off = ctx->p_inst_off;
+  b.tile_inst = ctx->p_tile_inst;
+  b.tile_begin = ctx->p_tile_begin;
+  b.tile_end = ctx->p_tile_end;
+  b.inst_first_tile = ctx->p_inst_first_tile;
   b.n_tiles = static_cast<uint32_t>(ctx->tile_inst.size());
   b.stats = static_cast<NameStat*>(ctx->d_stats.p);
   b.inst = static_cast<InstState*>(ctx->d_inst.p);
@@ -627,13 +639,10 @@ int upload_layout(cs_ctx* ctx, uint32_t n_inst, const uint64_t* inst_offsets, bo
   ctx->inst_off.assign(inst_offsets, inst_offsets + n_inst + 1);
   void* de = ctx->d_ev.get(std::max<uint64_t>(1, n_ev) * sizeof(cs_event));
   void* dw = ctx->d_wl.get(std::max<uint64_t>(1, n_workloads) * sizeof(cs_workload));
-  void* doff = ctx->d_inst_off.get((n_inst + 1) * sizeof(uint64_t));
-  if (!de || !dw || !doff) return fail(ctx, CS_E_CUDA, "cudaMalloc(events)");
+  if (!de || !dw) return fail(ctx, CS_E_CUDA, "cudaMalloc(events)");
   if (n_workloads)
     CS_CUDA(cudaMemcpyAsync(dw, wl, n_workloads * sizeof(cs_workload), cudaMemcpyHostToDevice,
                             ctx->stream));
-  CS_CUDA(cudaMemcpyAsync(doff, ctx->inst_off.data(), (n_inst + 1) * sizeof(uint64_t),
-                          cudaMemcpyHostToDevice, ctx->stream));
   // instance-aligned tiles
   ctx->tile_inst.clear();
   ctx->tile_begin.clear();
@@ -649,28 +658,41 @@ int upload_layout(cs_ctx* ctx, uint32_t n_inst, const uint64_t* inst_offsets, bo
   }
   const size_t nt = ctx->tile_inst.size();
   if (nt > 0xffffffffull) return fail(ctx, CS_E_UNSUPPORTED, "too many tiles");
-  auto* dti = dev<uint32_t>(ctx->d_tile_inst, nt);
-  auto* dtb = dev<uint64_t>(ctx->d_tile_begin, nt);
-  auto* dte = dev<uint64_t>(ctx->d_tile_end, nt);
-  auto* dft = dev<uint32_t>(ctx->d_inst_first_tile, n_inst);
   ctx->sample_tiles.clear();
   for (size_t t = 0; t < nt; ++t)
     if (ctx->tile_begin[t] < inst_offsets[ctx->tile_inst[t]] + kSampleEvents)
       ctx->sample_tiles.push_back(static_cast<uint32_t>(t));
-  auto* dst = dev<uint32_t>(ctx->d_sample_tiles, ctx->sample_tiles.size());
-  if (!dti || !dtb || !dte || !dft || !dst || !dev<uint64_t>(ctx->d_tile_cnt, nt) ||
-      !dev<uint64_t>(ctx->d_tile_pref, nt + 1) || !dev<uint64_t>(ctx->d_scan_tmp, nt / 1024 + 2))
-    return fail(ctx, CS_E_CUDA, "cudaMalloc(tiles)");
-  if (!ctx->sample_tiles.empty())
-    CS_CUDA(cudaMemcpyAsync(dst, ctx->sample_tiles.data(), ctx->sample_tiles.size() * 4,
-                            cudaMemcpyHostToDevice, ctx->stream));
+  // one staging block, one copy: [inst_off | tile_begin | tile_end | tile_inst |
+  // inst_first_tile | sample_tiles], each segment 16-byte aligned
+  const size_t ns = ctx->sample_tiles.size();
+  if (ctx->ev_layout) CS_CUDA(cudaEventSynchronize(ctx->ev_layout));  // staging block free again
+  else if (cudaEventCreateWithFlags(&ctx->ev_layout, cudaEventDisableTiming) != cudaSuccess)
+    return fail(ctx, CS_E_CUDA, "cudaEventCreate");
+  auto al = [](size_t x) { return (x + 15) & ~static_cast<size_t>(15); };
+  const size_t o_off = 0, o_tb = al((n_inst + 1) * 8), o_te = o_tb + al(nt * 8), o_ti = o_te + al(nt * 8),
+               o_ft = o_ti + al(nt * 4), o_st = o_ft + al(n_inst * 4u), total = o_st + al(std::max<size_t>(1, ns) * 4);
+  ctx->h_layout.resize(total);
+  unsigned char* hl = ctx->h_layout.data();
+  std::memcpy(hl + o_off, ctx->inst_off.data(), (n_inst + 1) * 8);
   if (nt) {
-    CS_CUDA(cudaMemcpyAsync(dti, ctx->tile_inst.data(), nt * 4, cudaMemcpyHostToDevice, ctx->stream));
-    CS_CUDA(cudaMemcpyAsync(dtb, ctx->tile_begin.data(), nt * 8, cudaMemcpyHostToDevice, ctx->stream));
-    CS_CUDA(cudaMemcpyAsync(dte, ctx->tile_end.data(), nt * 8, cudaMemcpyHostToDevice, ctx->stream));
+    std::memcpy(hl + o_tb, ctx->tile_begin.data(), nt * 8);
+    std::memcpy(hl + o_te, ctx->tile_end.data(), nt * 8);
+    std::memcpy(hl + o_ti, ctx->tile_inst.data(), nt * 4);
   }
-  CS_CUDA(cudaMemcpyAsync(dft, ctx->inst_first_tile.data(), n_inst * 4, cudaMemcpyHostToDevice,
-                          ctx->stream));
+  std::memcpy(hl + o_ft, ctx->inst_first_tile.data(), n_inst * 4u);
+  if (ns) std::memcpy(hl + o_st, ctx->sample_tiles.data(), ns * 4);
+  auto* dl = static_cast<unsigned char*>(ctx->d_layout.get(total));
+  if (!dl || !dev<uint64_t>(ctx->d_tile_cnt, nt) || !dev<uint64_t>(ctx->d_tile_pref, nt + 1) ||
+      !dev<uint64_t>(ctx->d_scan_tmp, nt / 1024 + 2))
+    return fail(ctx, CS_E_CUDA, "cudaMalloc(tiles)");
+  CS_CUDA(cudaMemcpyAsync(dl, hl, total, cudaMemcpyHostToDevice, ctx->stream));
+  CS_CUDA(cudaEventRecord(ctx->ev_layout, ctx->stream));
+  ctx->p_inst_off = reinterpret_cast<uint64_t*>(dl + o_off);
+  ctx->p_tile_begin = reinterpret_cast<uint64_t*>(dl + o_tb);
+  ctx->p_tile_end = reinterpret_cast<uint64_t*>(dl + o_te);
+  ctx->p_tile_inst = reinterpret_cast<uint32_t*>(dl + o_ti);
+  ctx->p_inst_first_tile = reinterpret_cast<uint32_t*>(dl + o_ft);
+  ctx->p_sample_tiles = reinterpret_cast<uint32_t*>(dl + o_st);
   ctx->ranges_built_for = 0;  // k_segment_range ranges are rebuilt by the next fused run
   ++ctx->seg_gen;
   if (!ctx->extra_keys.empty()) ctx->mt_valid = false;  // extras resolve per upload
@@ -723,7 +745,7 @@ static int cs_upload_unsorted_impl(cs_ctx* ctx, uint32_t n_inst, const uint64_t*
   }
   if (wait_copied(ctx) != CS_OK) return CS_E_CUDA;
   uint64_t launches = 0;
-  if (sort_events_device(din, dids, static_cast<const uint64_t*>(ctx->d_inst_off.p), n_inst, n,
+  if (sort_events_device(din, dids, ctx->p_inst_off, n_inst, n,
                          static_cast<cs_event*>(ctx->d_ev.p), dord, dsc, dh, dht, dex, ctx->stream,
                          &launches) != 0)
     return fail(ctx, CS_E_CUDA, std::string("device sort: ") + cudaGetErrorString(cudaGetLastError()));
@@ -887,8 +909,7 @@ static int cs_upload_wire_impl(cs_ctx* ctx, uint32_t n_inst, const uint64_t* ins
     ctx->n_wl = n_wl32;
     launch_wl32_expand(dwl32, n_wl32, static_cast<cs_workload*>(dw), ctx->stream);
   }
-  launch_wire_expand(dv, static_cast<const uint64_t*>(ctx->d_tile_begin.p),
-                     static_cast<const uint64_t*>(ctx->d_tile_end.p), static_cast<uint32_t>(nt),
+  launch_wire_expand(dv, ctx->p_tile_begin, ctx->p_tile_end, static_cast<uint32_t>(nt),
                      static_cast<cs_event*>(ctx->d_ev.p), ctx->stream);
   CS_CUDA(cudaGetLastError());
   CS_CUDA(cudaEventSynchronize(ctx->ev_copied));  // the expand keeps running
@@ -1275,7 +1296,7 @@ static int cs_run_impl(cs_ctx* ctx, uint32_t mask) {
   if (hint == -1 && !all_fixed && !guessed && !(mask & CS_RUN_GIVEN)) {
     // speculative anchor from a sample of every instance
     if (stats_bytes) CS_CUDA(cudaMemsetAsync(d_stats, 0, stats_bytes, s));
-    launch_scan_events(b, cfg, 1, true, static_cast<const uint32_t*>(ctx->d_sample_tiles.p),
+    launch_scan_events(b, cfg, 1, true, ctx->p_sample_tiles,
                        static_cast<uint32_t>(ctx->sample_tiles.size()), s, &ctx->launches);
     launch_rank(b, cfg, 0, s, &ctx->launches);
   }
@@ -1482,7 +1503,7 @@ static int cs_run_impl(cs_ctx* ctx, uint32_t mask) {
       b = make_buffers(ctx);
       if (hint == -1) {
         if (stats_bytes) CS_CUDA(cudaMemsetAsync(d_stats, 0, stats_bytes, s));
-        launch_scan_events(b, cfg, 1, true, static_cast<const uint32_t*>(ctx->d_sample_tiles.p),
+        launch_scan_events(b, cfg, 1, true, ctx->p_sample_tiles,
                            static_cast<uint32_t>(ctx->sample_tiles.size()), s, &ctx->launches);
         launch_rank(b, cfg, 0, s, &ctx->launches);
       }
