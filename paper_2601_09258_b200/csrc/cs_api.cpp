@@ -219,8 +219,7 @@ struct cs_ctx {
   size_t pin_models_cap = 0;
   std::vector<uint64_t> stage_off;
   pinned_vector<uint64_t> assemble_host, h_new_anchors;
-  pinned_vector<uint32_t> h_anchor_ids;
-  DevBuf d_anchor_ids, d_new_anchors;
+  DevBuf d_new_anchors;
   cudaEvent_t ev_counted = nullptr;  // the new events' anchor counts are on the host
   DevBuf d_keep;
   pinned_vector<uint32_t> sample_tiles;
@@ -2065,34 +2064,38 @@ static int cs_stream_push_impl(cs_ctx* ctx, uint32_t n_inst, const uint64_t* off
   // the new events go up first; in steady state (every anchor fixed) a tiny
   // kernel counts their anchor occurrences while the host prepares the batch
   // layout, so the run can size its cycle tables without a mid-run sync
+  // meta: 4 words per instance, then the fixed anchor ids (u32) when the
+  // counts are predicted -- one copy
+  bool predict = ctx->tail_anchors.size() == n_inst && ctx->stream_anchor.size() == n_inst && !ctx->stream_fresh;
+  for (uint32_t i = 0; i < n_inst && predict; ++i) predict = ctx->stream_anchor[i] != UINT32_MAX;
+  const size_t meta_words = 4ull * n_inst + (predict ? (n_inst + 1ull) / 2 : 0);
   auto* d_new = dev<cs_event>(ctx->d_new_ev, std::max<uint64_t>(1, n_new));
-  auto* d_meta = dev<uint64_t>(ctx->d_assemble, 4ull * n_inst);
+  auto* d_meta = dev<uint64_t>(ctx->d_assemble, meta_words);
   if (!d_new || !d_meta) return broken(fail(ctx, CS_E_CUDA, "cudaMalloc(stream)"));
   if (n_new && cudaMemcpyAsync(d_new, ev, n_new * sizeof(cs_event), cudaMemcpyHostToDevice,
                                ctx->stream) != cudaSuccess)
     return broken(fail(ctx, CS_E_CUDA, "cudaMemcpyAsync(stream events)"));
   auto& meta = ctx->assemble_host;
-  meta.resize(4ull * n_inst);
+  meta.resize(meta_words);
   for (uint32_t i = 0; i < n_inst; ++i) {
     meta[4 * i + 0] = ctx->stage_off[i];
     meta[4 * i + 1] = ctx->tail_start[i];
     meta[4 * i + 2] = ctx->tail_len[i];
     meta[4 * i + 3] = offsets[i];
   }
+  if (predict)
+    std::memcpy(reinterpret_cast<uint32_t*>(meta.data() + 4ull * n_inst), ctx->stream_anchor.data(),
+                n_inst * sizeof(uint32_t));
   if (cudaMemcpyAsync(d_meta, meta.data(), meta.size() * 8, cudaMemcpyHostToDevice, ctx->stream) !=
       cudaSuccess)
     return broken(fail(ctx, CS_E_CUDA, "cudaMemcpyAsync(stream meta)"));
-  bool predict = ctx->tail_anchors.size() == n_inst && ctx->stream_anchor.size() == n_inst && !ctx->stream_fresh;
-  for (uint32_t i = 0; i < n_inst && predict; ++i) predict = ctx->stream_anchor[i] != UINT32_MAX;
   if (predict) {
-    ctx->h_anchor_ids.assign(ctx->stream_anchor.begin(), ctx->stream_anchor.end());
     ctx->h_new_anchors.resize(n_inst);
-    auto* da = dev<uint32_t>(ctx->d_anchor_ids, n_inst);
+    const uint32_t* da = reinterpret_cast<const uint32_t*>(d_meta + 4ull * n_inst);
     auto* dc = dev<uint64_t>(ctx->d_new_anchors, n_inst);
-    if (!da || !dc) return broken(fail(ctx, CS_E_CUDA, "cudaMalloc(stream count)"));
+    if (!dc) return broken(fail(ctx, CS_E_CUDA, "cudaMalloc(stream count)"));
     if (!ctx->ev_counted && cudaEventCreateWithFlags(&ctx->ev_counted, cudaEventDisableTiming) != cudaSuccess)
       return broken(fail(ctx, CS_E_CUDA, "cudaEventCreate"));
-    CS_CUDA(cudaMemcpyAsync(da, ctx->h_anchor_ids.data(), n_inst * 4ull, cudaMemcpyHostToDevice, ctx->stream));
     launch_stream_count(d_new, d_meta, da, n_inst, n_new, dc, ctx->stream);
     CS_CUDA(cudaMemcpyAsync(ctx->h_new_anchors.data(), dc, n_inst * 8ull, cudaMemcpyDeviceToHost, ctx->stream));
     CS_CUDA(cudaEventRecord(ctx->ev_counted, ctx->stream));
