@@ -233,6 +233,7 @@ struct cs_ctx {
   uint64_t n_cycles = 0;           // cycle slots
   int reduce_variant = 0;  // profiling hook (single variant today)
   bool allow_fused = true;   // CS_OPT_FUSED (default on; 0 selects the two-pass path)
+  bool no_fused_score = false;  // option 95 (testing): score in its own kernel after compaction
   int phase_timings = -1;    // CS_OPT_PHASE_TIMINGS (-1: per phase except streaming pushes)
   bool used_fused = false;   // the last run segmented with k_segment_range
   // slot-count speculation of the single-read pass: a run over the same
@@ -1695,47 +1696,8 @@ static int cs_run_impl(cs_ctx* ctx, uint32_t mask) {
       return fail(ctx, CS_E_UNSUPPORTED, "stage_window too large for the device heuristic (<= 1600)");
   }
   hp.mark("stage");
-  launch_records(b, cfg, 0, s, &ctx->launches);
-  hp.mark("records");
-  if (!ctx->extra_keys.empty() && ctx->n_cycles) {
-    const uint64_t K = ctx->extra_keys.size();
-    if (!dev<double>(ctx->d_rec_extra, ctx->n_cycles * K) || !dev<uint8_t>(ctx->d_rec_extra_has, ctx->n_cycles * K))
-      return fail(ctx, CS_E_CUDA, "cudaMalloc(record extras)");
-    b = make_buffers(ctx);
-    launch_record_extras(b, ctx->n_cycles, s, &ctx->launches);
-  }
-  const int e6m = record_event(ctx, 6);
-  ctx->timed.push_back({"stage_records", {e5, e6m}});
-  int e6 = e6m;
-  // ---- counter-weighted mu (cycle_stats with a CounterTable, rca.cpp:97-126)
-  if ((mask & CS_RUN_MU) && ctx->n_metrics && nt) {
-    const uint64_t nm = static_cast<uint64_t>(ctx->n_metrics) * nt;
-    if (!dev<uint64_t>(ctx->d_m_off, nm + 1) || !dev<uint64_t>(ctx->d_scan_tmp, nm / 1024 + 2))
-      return fail(ctx, CS_E_CUDA, "cudaMalloc(counter series)");
-    b = make_buffers(ctx);
-    launch_counter_series(b, s, &ctx->launches);
-    uint64_t n_samples = 0;
-    CS_CUDA(cudaMemcpyAsync(&n_samples, static_cast<uint64_t*>(ctx->d_m_off.p) + nm, 8,
-                            cudaMemcpyDeviceToHost, s));
-    CS_CUDA(cudaStreamSynchronize(s));
-    const size_t C = std::max<int32_t>(1, ctx->cyc.n_beta_slots);
-    if (!dev<int64_t>(ctx->d_s_ts, std::max<uint64_t>(1, n_samples)) ||
-        !dev<double>(ctx->d_s_val, std::max<uint64_t>(1, n_samples)) ||
-        !dev<double>(ctx->d_mu, std::max<uint64_t>(1, ctx->n_cycles) * C) ||
-        !dev<uint8_t>(ctx->d_mu_has, std::max<uint64_t>(1, ctx->n_cycles) * C))
-      return fail(ctx, CS_E_CUDA, "cudaMalloc(mu)");
-    b = make_buffers(ctx);
-    launch_counter_scatter(b, s, &ctx->launches);
-    launch_cycle_mu(b, cfg, s, &ctx->launches);
-    e6 = record_event(ctx, 10);
-    ctx->timed.push_back({"mu", {e6m, e6}});
-  }
-  // record counts stay on the device: scoring and detection launch over the
-  // cycle count as capacity and clamp to rec_off[n_inst] (no host round trip)
-  const uint64_t rec_cap = ctx->n_cycles;
-  ctx->rec_off.assign(n_inst + 1, 0);
-  int last = e6;
-  // ---- score + detect
+  // the per-instance model table first: record compaction can score the
+  // records it writes (cell-table models without record extras)
   if (mask & (CS_RUN_SCORE | CS_RUN_DETECT)) {
     bool reuse = ctx->mt_valid && ctx->mt_gen == ctx->model_gen && ctx->mt_n_inst == n_inst &&
                  ctx->h_models.size() == n_inst &&
@@ -1804,12 +1766,61 @@ static int cs_run_impl(cs_ctx* ctx, uint32_t mask) {
     ctx->mt_valid = true;
     }  // rebuild
     b = make_buffers(ctx);
+  }
+  bool fuse_score = (mask & (CS_RUN_SCORE | CS_RUN_DETECT)) && ctx->extra_keys.empty() && !ctx->no_fused_score;
+  for (uint32_t i = 0; i < n_inst && fuse_score; ++i) fuse_score = ctx->h_models[i].lut != nullptr;
+  // scores written by compaction carry absolute record indices in
+  // first_bad_record / first_missing_record (converted after the final sync)
+  const bool score_abs = launch_records(b, cfg, fuse_score ? 1 : 0, s, &ctx->launches);
+  hp.mark("records");
+  if (!ctx->extra_keys.empty() && ctx->n_cycles) {
+    const uint64_t K = ctx->extra_keys.size();
+    if (!dev<double>(ctx->d_rec_extra, ctx->n_cycles * K) || !dev<uint8_t>(ctx->d_rec_extra_has, ctx->n_cycles * K))
+      return fail(ctx, CS_E_CUDA, "cudaMalloc(record extras)");
+    b = make_buffers(ctx);
+    launch_record_extras(b, ctx->n_cycles, s, &ctx->launches);
+  }
+  const int e6m = record_event(ctx, 6);
+  ctx->timed.push_back({"stage_records", {e5, e6m}});
+  int e6 = e6m;
+  // ---- counter-weighted mu (cycle_stats with a CounterTable, rca.cpp:97-126)
+  if ((mask & CS_RUN_MU) && ctx->n_metrics && nt) {
+    const uint64_t nm = static_cast<uint64_t>(ctx->n_metrics) * nt;
+    if (!dev<uint64_t>(ctx->d_m_off, nm + 1) || !dev<uint64_t>(ctx->d_scan_tmp, nm / 1024 + 2))
+      return fail(ctx, CS_E_CUDA, "cudaMalloc(counter series)");
+    b = make_buffers(ctx);
+    launch_counter_series(b, s, &ctx->launches);
+    uint64_t n_samples = 0;
+    CS_CUDA(cudaMemcpyAsync(&n_samples, static_cast<uint64_t*>(ctx->d_m_off.p) + nm, 8,
+                            cudaMemcpyDeviceToHost, s));
+    CS_CUDA(cudaStreamSynchronize(s));
+    const size_t C = std::max<int32_t>(1, ctx->cyc.n_beta_slots);
+    if (!dev<int64_t>(ctx->d_s_ts, std::max<uint64_t>(1, n_samples)) ||
+        !dev<double>(ctx->d_s_val, std::max<uint64_t>(1, n_samples)) ||
+        !dev<double>(ctx->d_mu, std::max<uint64_t>(1, ctx->n_cycles) * C) ||
+        !dev<uint8_t>(ctx->d_mu_has, std::max<uint64_t>(1, ctx->n_cycles) * C))
+      return fail(ctx, CS_E_CUDA, "cudaMalloc(mu)");
+    b = make_buffers(ctx);
+    launch_counter_scatter(b, s, &ctx->launches);
+    launch_cycle_mu(b, cfg, s, &ctx->launches);
+    e6 = record_event(ctx, 10);
+    ctx->timed.push_back({"mu", {e6m, e6}});
+  }
+  // record counts stay on the device: scoring and detection launch over the
+  // cycle count as capacity and clamp to rec_off[n_inst] (no host round trip)
+  const uint64_t rec_cap = ctx->n_cycles;
+  ctx->rec_off.assign(n_inst + 1, 0);
+  int last = e6;
+  // ---- score + detect
+  if (mask & (CS_RUN_SCORE | CS_RUN_DETECT)) {
+    b = make_buffers(ctx);
     if (!dev<uint64_t>(ctx->block_tmp, rec_cap / 256 + 16))
       return fail(ctx, CS_E_CUDA, "cudaMalloc(block_tmp)");
     b = make_buffers(ctx);
     hp.mark("models");
-    launch_score(b, cfg, rec_cap, ctx->rec_off.data(), ctx->model_of_inst.data(),
-                 ctx->h_models.data(), s, &ctx->launches);
+    if (!score_abs)
+      launch_score(b, cfg, rec_cap, ctx->rec_off.data(), ctx->model_of_inst.data(),
+                   ctx->h_models.data(), s, &ctx->launches);
     hp.mark("score");
     const int e7 = record_event(ctx, 7);
     ctx->timed.push_back({"score", {e6, e7}});
@@ -1889,6 +1900,10 @@ static int cs_run_impl(cs_ctx* ctx, uint32_t mask) {
     // (FeatureMismatch, checked before ppe) or whose latency is <= 0
     InstState& st = ctx->h_inst[i];
     if (!(mask & (CS_RUN_SCORE | CS_RUN_DETECT))) continue;
+    if (score_abs) {
+      if (st.first_bad_record != UINT64_MAX) st.first_bad_record -= ctx->rec_off[i];
+      if (st.first_missing_record != UINT64_MAX) st.first_missing_record -= ctx->rec_off[i];
+    }
     const bool miss = st.first_missing_record != UINT64_MAX && st.first_missing_record <= st.first_bad_record;
     if (miss) st.first_bad_record = st.first_missing_record;
     if (ctx->inst_status[i] == CS_OK && st.first_bad_record != UINT64_MAX)
@@ -2783,6 +2798,10 @@ int cs_set_option(cs_ctx* ctx, int option, int64_t value) {
   if (option == CS_OPT_PHASE_TIMINGS) {
     if (value < -1 || value > 2) return fail(ctx, CS_E_INVALID_ARGUMENT, "phase timings: -1, 0, 1 or 2");
     ctx->phase_timings = static_cast<int>(value);
+    return CS_OK;
+  }
+  if (option == 95) {  // testing: 1 scores in k_score_lut_flat instead of during record compaction
+    ctx->no_fused_score = value != 0;
     return CS_OK;
   }
   if (option == 96) {  // tuning: events per single-read segmentation range (0 = auto)

@@ -240,8 +240,11 @@ constexpr uint32_t kStageChunkCycles = CS_STAGE_CHUNK;  // stage heuristic chunk
 // when K4b could not (final_parity[2] == 0)
 int launch_stage_heuristic(const DevBuffers& b, const DevConfig& cfg, const StageMeta& m, cudaStream_t s,
                            uint64_t* launches);
-void launch_records(const DevBuffers& b, const DevConfig& cfg, uint64_t n_blocks_cap,
-                    cudaStream_t s, uint64_t* launches);
+// record compaction; fuse_score != 0 also scores every record it writes
+// (cell-table models, no record extras; first_bad / first_missing record are
+// then absolute record indices).  Returns whether it scored.
+bool launch_records(const DevBuffers& b, const DevConfig& cfg, int fuse_score, cudaStream_t s,
+                    uint64_t* launches);
 // per record: the extras of its cycle (last event carrying each key wins)
 void launch_record_extras(const DevBuffers& b, uint64_t n_records_cap, cudaStream_t s, uint64_t* launches);
 void launch_score(const DevBuffers& b, const DevConfig& cfg, uint64_t n_records_total,

@@ -1019,7 +1019,10 @@ __device__ __forceinline__ bool rec_ok(const DevBuffers& b, const DevConfig& cfg
 
 // kRecBlock cycles per CTA of kRecThreads, kRecBlock / kRecThreads per thread
 // (thread stride: coalesced), independent loads in flight
-constexpr int kRecThreads = 256;
+#ifndef CS_REC_THREADS
+#define CS_REC_THREADS 256
+#endif
+constexpr int kRecThreads = CS_REC_THREADS;
 constexpr int kRecPer = kRecBlock / kRecThreads;
 
 __global__ void __launch_bounds__(kRecThreads) k_records_count(DevBuffers b, DevConfig cfg) {
@@ -1137,7 +1140,11 @@ void launch_exclusive_scan(uint64_t* v, uint64_t n, uint64_t* total, uint64_t* t
   *launches += 3;
 }
 
-__global__ void __launch_bounds__(kRecThreads) k_records_scatter(DevBuffers b, DevConfig cfg) {
+__device__ __forceinline__ void score_one_lut(const DevBuffers& b, const DevConfig& cfg,
+                                              const DevModel& m, uint32_t inst, u64 rb, u64 k, u64 g,
+                                              const double* t0, const double* t1);
+
+__global__ void __launch_bounds__(kRecThreads) k_records_scatter(DevBuffers b, DevConfig cfg, int fuse_score) {
   pdl_enter();
   __shared__ uint32_t s_w[kRecPer][kRecThreads / 32];
   __shared__ uint32_t s_rank[kRecBlock];  // exclusive record rank of each cycle in the block
@@ -1185,6 +1192,17 @@ __global__ void __launch_bounds__(kRecThreads) k_records_scatter(DevBuffers b, D
     const uint32_t local = s_w[r][warp] + __popc(m[r] & lanemask_lt());
     s_rank[threadIdx.x + r * kRecThreads] = local;
     if (ok[r]) b.rec_cycle[base + local] = gb + threadIdx.x + (u64)r * kRecThreads;
+  }
+  if (fuse_score) {  // score the block's records here (the cycle rows are at hand)
+#pragma unroll
+    for (int r = 0; r < kRecPer; ++r) {
+      if (!ok[r]) continue;
+      const u64 g = gb + threadIdx.x + (u64)r * kRecThreads;
+      const uint32_t inst = b.n_inst == 1 ? 0u : b.c_inst[g];
+      const DevModel& md = b.models[inst];
+      score_one_lut(b, cfg, md, inst, 0, base + s_rank[threadIdx.x + r * kRecThreads], g, md.lut_thr[0],
+                    md.lut_thr[1]);
+    }
   }
   __syncthreads();
   // per-instance record offsets: the rank of each instance's first cycle that
@@ -1485,15 +1503,15 @@ __device__ __forceinline__ uint32_t count_less(const double* __restrict__ t, uin
 // One record through the compiled cell table: latency target (cycles.cpp:
 // 384-390), features (baseline.cpp:61-62), prediction (gbdt.cpp:173-184),
 // ppe (detector.cpp:14-19).
+// record k of cycle g; the atomics store k - rb (rb = 0: absolute indices)
 __device__ __forceinline__ void score_one_lut(const DevBuffers& b, const DevConfig& cfg,
-                                              const DevModel& m, uint32_t inst, u64 rb, u64 k,
+                                              const DevModel& m, uint32_t inst, u64 rb, u64 k, u64 g,
                                               const double* t0, const double* t1) {
   const double eps = cfg.ctl.epsilon;
   const int lat = cfg.cyc.latency_phase;
   const int P = cfg.cyc.n_phases;
   const uint32_t n0 = m.lut_n[0], n1 = m.lut_n[1];
   const int f0 = m.feature_ids[0], f1 = m.n_features > 1 ? m.feature_ids[1] : -1;
-  const u64 g = b.rec_cycle[k];
   const cs_workload w = b.wl[b.c_wl[g]];
   i64 target = b.c_end[g] - b.c_start[g];
   if (lat >= 0) {
@@ -1550,7 +1568,7 @@ __global__ void __launch_bounds__(kLutThreads)
   if (k >= n_records) return;
   const uint32_t inst = upper_bound_u64(b.rec_off, b.n_inst + 1, k) - 1;
   const DevModel& m = b.models[inst];
-  score_one_lut(b, cfg, m, inst, b.rec_off[inst], k, m.lut_thr[0], m.lut_thr[1]);
+  score_one_lut(b, cfg, m, inst, b.rec_off[inst], k, b.rec_cycle[k], m.lut_thr[0], m.lut_thr[1]);
 }
 
 // ------------------------------------------------------------ K7 detect
@@ -3655,12 +3673,12 @@ __global__ void __launch_bounds__(1024) k_records_small(DevBuffers b, DevConfig 
 
 constexpr u64 kSmallBatch = 32768;  // cycles / records handled by one CTA
 
-void launch_records(const DevBuffers& b, const DevConfig& cfg, uint64_t, cudaStream_t s,
+bool launch_records(const DevBuffers& b, const DevConfig& cfg, int fuse_score, cudaStream_t s,
                     uint64_t* launches) {
   if (b.n_cycles <= kSmallBatch) {
     launch_pdl(k_records_small, 1, 1024, 0, s, b, cfg);
     ++*launches;
-    return;
+    return false;
   }
   const u64 nb = (b.n_cycles + kRecBlock - 1) / kRecBlock;
   if (nb) {
@@ -3671,11 +3689,12 @@ void launch_records(const DevBuffers& b, const DevConfig& cfg, uint64_t, cudaStr
   launch_pdl(k_scan_exclusive, 1, 1024, 0, s, b.block_tmp, nb, b.block_tmp + nb);
   ++*launches;
   if (nb) {
-    launch_pdl(k_records_scatter, (unsigned)nb, kRecThreads, 0, s, b, cfg);
+    launch_pdl(k_records_scatter, (unsigned)nb, kRecThreads, 0, s, b, cfg, fuse_score);
     ++*launches;
   }
   launch_pdl(k_rec_off_tail, 1, 1, 0, s, b, b.block_tmp + nb);
   ++*launches;
+  return fuse_score != 0 && nb != 0;
 }
 
 void launch_score(const DevBuffers& b, const DevConfig& cfg, uint64_t n_records,
