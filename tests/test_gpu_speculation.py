@@ -58,3 +58,31 @@ def test_speculated_runs_equal_fresh_runs(rt):
         an.run(abi.RUN_SEGMENT | abi.RUN_BETA)
         _same(an, ref2)
     an.close()
+
+
+def test_phase_timing_modes_move_no_data(rt):
+    """CS_OPT_PHASE_TIMINGS only chooses which device events a run records:
+    -1 / 1 every phase, 2 the segmentation pass and the total, 0 the total.
+    Tables are identical in every mode; an out-of-range mode is rejected."""
+    tr = rt.synth_trace(4000, 31, 32, n_ranks=4, fault="nvlink_saturation", onset=3000, duration=150,
+                        compact_names=False)
+    an = rt.Analyzer(0)
+    an.configure(tr.names, rt.span_names_mask(tr.events, len(tr.names)), n_comm_slots=tr.n_comm)
+    an.upload(tr.events, [0, len(tr.events)], tr.workloads)
+    an.run(abi.RUN_SEGMENT | abi.RUN_BETA)
+    ref = _tables(an)
+    full = set(an.timings())
+    assert "total" in full and len(full) > 3
+    for mode, expect in ((2, None), (0, {"total"}), (1, full), (-1, full)):
+        an.set_phase_timings(mode)
+        an.run(abi.RUN_SEGMENT | abi.RUN_BETA)
+        _same(an, ref)
+        got = set(an.timings())
+        if expect is None:
+            assert "total" in got and got & {"segment_range", "scan_events"} and got < full, got
+        else:
+            assert got == expect, (mode, got)
+        assert all(v >= 0.0 for v in an.timings().values())
+    with pytest.raises(Exception):
+        an.set_phase_timings(3)
+    an.close()
